@@ -1,0 +1,312 @@
+/*
+ * cg_oracle.c -- plain, slow, sequential CPU oracle for the batched Cudagrind
+ * transfer checker.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * It shares no code, header, table or constant generator with the CUDA path
+ * (paper_1310_0901_b200/csrc) and never includes it; every constant below is
+ * restated from the paper / SURVEY.md, not imported.
+ *
+ * What it computes (§3):
+ * events are replayed one at a time, in trace order, exactly as a wrapper
+ * around each driver call would see them:
+ *   O1 host_mark        -- S:45-62
+ *   O2 host_set_vbits   -- S:79
+ *   O3 register         -- Fig. 2 caption P:88
+ *   O4 free             -- S:148-156
+ *   O5 copy check+apply -- P:80-82, S:157-165, S:192, S:63-80, S:222-248,
+ *                          S:278-281; readings R-1..R-16
+ *   O6 leak report      -- P:12 (abstract)
+ *
+ * State (SURVEY §8(c) "State"):
+ *   host window [h0, h0+s);  A: one addressability bit per host byte, bit
+ *   (x-h0)&7 of byte (x-h0)>>3, 1 = addressable (R-2);  V: one byte of
+ *   validity bits per host byte, bit set = bit undefined (R-1);  fresh state
+ *   A=0 (unaddressable), V=0xFF.  The device allocation list is an
+ *   unsorted array searched linearly -- the paper's Fig. 2 "list".
+ *
+ * Parity pins: see tests/test_oracle_*.py (paper worked example P:137-146 ->
+ * P:234-235, SPEC examples, closed forms, invariants, numpy brute force).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OR_NONE UINT64_MAX
+
+/* event ops (tracegen/__init__.py) */
+enum { OR_MARK = 1, OR_SETV = 2, OR_REG = 3, OR_FREE = 4, OR_COPY = 5 };
+/* copy kinds: host->device, device->host, device->device */
+enum { OR_HTOD = 1, OR_DTOH = 2, OR_DTOD = 3 };
+/* host mark states (host_alloc / host_write / host_free) */
+enum { OR_NOACCESS = 0, OR_UNDEFINED = 1, OR_DEFINED = 2 };
+
+/* diagnostic flags in SPEC's emission order (reading R-14) */
+#define F_DST_NOT_ALLOCATED   (1u << 0)
+#define F_DST_TOO_SMALL       (1u << 1)
+#define F_SRC_NOT_ALLOCATED   (1u << 2)
+#define F_SRC_TOO_SMALL       (1u << 3)   /* P:82, Listing 5 */
+#define F_HOST_UNADDRESSABLE  (1u << 4)   /* P:80 (host side, via Memcheck A-bits) */
+#define F_HOST_UNDEFINED      (1u << 5)   /* P:81 (Warning, footnote) */
+#define F_BAD_PITCH           (1u << 6)   /* R-12 */
+#define F_INVALID_RANGE       (1u << 7)
+#define F_BAD_KIND            (1u << 8)   /* R-16 */
+
+typedef struct {
+    uint32_t op, kind;
+    uint64_t seq, width, height;
+    uint64_t dst, dst_x, dst_y, dst_pitch;
+    uint64_t src, src_x, src_y, src_pitch;
+} or_event;                                    /* 96 bytes */
+
+typedef struct {
+    uint64_t first_unaddr, first_undef, undef_count;
+    uint64_t dst_expected, dst_found, src_expected, src_found;
+    uint32_t flags, status;
+} or_verdict;                                  /* 64 bytes */
+
+typedef struct { uint64_t base, size, seq; } or_alloc;
+
+typedef struct {
+    uint64_t h0, s;
+    uint8_t *A;            /* s/8 bytes */
+    uint8_t *V;            /* s bytes   */
+    or_alloc *live;        /* unsorted list of live allocations (Fig. 2) */
+    uint64_t n_live, cap_live;
+    uint64_t last_reg_seq;
+    int undef_is_error;    /* CLI flag promotes HostUndefined */
+} or_state;
+
+/* ---------------------------------------------------------------- state */
+or_state *or_create(uint64_t h0, uint64_t s, int undef_is_error) {
+    or_state *st = (or_state *)calloc(1, sizeof(or_state));
+    if (!st) return NULL;
+    st->h0 = h0; st->s = s; st->undef_is_error = undef_is_error;
+    st->A = (uint8_t *)calloc(s / 8 + 1, 1);          /* A = 0: unaddressable */
+    st->V = (uint8_t *)malloc(s ? s : 1);
+    if (!st->A || !st->V) { free(st->A); free(st->V); free(st); return NULL; }
+    memset(st->V, 0xFF, s);                            /* V = all undefined  */
+    st->cap_live = 16;
+    st->live = (or_alloc *)malloc(st->cap_live * sizeof(or_alloc));
+    return st;
+}
+
+void or_destroy(or_state *st) {
+    if (!st) return;
+    free(st->A); free(st->V); free(st->live); free(st);
+}
+
+uint8_t *or_A(or_state *st) { return st->A; }
+uint8_t *or_V(or_state *st) { return st->V; }
+
+static int in_window(const or_state *st, uint64_t x) {
+    return x >= st->h0 && x - st->h0 < st->s;
+}
+
+static int a_get(const or_state *st, uint64_t x) {        /* x inside window */
+    uint64_t i = x - st->h0;
+    return (st->A[i >> 3] >> (i & 7)) & 1;
+}
+
+static void a_put(or_state *st, uint64_t x, int bit) {
+    uint64_t i = x - st->h0;
+    if (bit) st->A[i >> 3] |= (uint8_t)(1u << (i & 7));
+    else     st->A[i >> 3] &= (uint8_t)~(1u << (i & 7));
+}
+
+/* addr(x) of SURVEY §8(a)-a4: inside the window and A-bit set (R-15) */
+static int addressable(const or_state *st, uint64_t x) {
+    return in_window(st, x) && a_get(st, x);
+}
+
+/* ------------------------------------------------------- O1 host_mark */
+/* returns 0 on success, 1 (INVALID_VALUE) if the range leaves the window */
+int or_mark(or_state *st, uint64_t addr, uint64_t len, uint32_t state) {
+    if (state > OR_DEFINED) return 1;
+    if (len == 0) return 0;
+    if (addr < st->h0 || len > st->s || addr - st->h0 > st->s - len) return 1;
+    for (uint64_t k = 0; k < len; k++) {
+        uint64_t x = addr + k;
+        a_put(st, x, state != OR_NOACCESS);
+        st->V[x - st->h0] = (state == OR_DEFINED) ? 0x00 : 0xFF;
+    }
+    return 0;
+}
+
+/* --------------------------------------------------- O2 host_set_vbits */
+int or_set_vbits(or_state *st, uint64_t addr, uint64_t len, const uint8_t *vb) {
+    if (len == 0) return 0;
+    if (addr < st->h0 || len > st->s || addr - st->h0 > st->s - len) return 1;
+    for (uint64_t k = 0; k < len; k++)                 /* defined => addressable */
+        if (!a_get(st, addr + k)) return 1;
+    for (uint64_t k = 0; k < len; k++) st->V[addr + k - st->h0] = vb[k];
+    return 0;
+}
+
+/* -------------------------------------------------------- O3 register */
+int or_register(or_state *st, uint64_t base, uint64_t size, uint64_t seq) {
+    if (seq <= st->last_reg_seq) return 1;               /* seq strictly increasing */
+    if (size == 0 || base == 0) return 1;
+    if (size > UINT64_MAX - base) return 1;               /* end must fit in 64 bits */
+    for (uint64_t i = 0; i < st->n_live; i++) {            /* S:143 OverlapWithLive */
+        const or_alloc *e = &st->live[i];
+        if (base < e->base + e->size && e->base < base + size) return 1;
+    }
+    if (st->n_live == st->cap_live) {
+        st->cap_live *= 2;
+        st->live = (or_alloc *)realloc(st->live, st->cap_live * sizeof(or_alloc));
+    }
+    st->live[st->n_live].base = base;
+    st->live[st->n_live].size = size;
+    st->live[st->n_live].seq = seq;
+    st->n_live++;
+    st->last_reg_seq = seq;
+    return 0;
+}
+
+/* ------------------------------------------------------------ O4 free */
+int or_free(or_state *st, uint64_t ptr, uint64_t seq) {
+    if (seq <= st->last_reg_seq) return 1;
+    for (uint64_t i = 0; i < st->n_live; i++) {
+        if (st->live[i].base == ptr) {                    /* S:150 base match only */
+            st->live[i] = st->live[st->n_live - 1];
+            st->n_live--;
+            st->last_reg_seq = seq;
+            return 0;
+        }
+    }
+    return 1;                                             /* InvalidFree, no mutation */
+}
+
+/* ----------------------------------------------------------- O5 copy */
+/* start = base + Y*pitch + X  (CUDA_MEMCPY2D start address, R-11);
+ * span  = 0 if W==0 or H==0, else (H-1)*pitch + W;
+ * the side is a valid range iff start+span fits in 64 bits (R-10). */
+static int side_range(uint64_t base, uint64_t x, uint64_t y, uint64_t pitch,
+                      uint64_t w, uint64_t h, uint64_t *start, uint64_t *span) {
+    unsigned __int128 st = (unsigned __int128)base + (unsigned __int128)y * pitch + x;
+    unsigned __int128 sp = (w == 0 || h == 0) ? 0
+                         : (unsigned __int128)(h - 1) * pitch + w;
+    if (st + sp > (unsigned __int128)UINT64_MAX) return 0;
+    *start = (uint64_t)st;
+    *span = (uint64_t)sp;
+    return 1;
+}
+
+/* coverage anchored on the allocation containing start */
+static void device_side(const or_state *st, uint64_t start, uint64_t span,
+                        uint32_t f_na, uint32_t f_small, uint32_t *flags,
+                        uint64_t *expected, uint64_t *found) {
+    for (uint64_t i = 0; i < st->n_live; i++) {
+        const or_alloc *e = &st->live[i];
+        if (e->base <= start && start < e->base + e->size) {
+            uint64_t avail = e->base + e->size - start;
+            if (avail < span) { *flags |= f_small; *expected = span; *found = avail; }
+            return;
+        }
+    }
+    *flags |= f_na;
+}
+
+void or_check_copy(or_state *st, const or_event *ev, or_verdict *v) {
+    v->first_unaddr = OR_NONE; v->first_undef = OR_NONE; v->undef_count = 0;
+    v->dst_expected = v->dst_found = v->src_expected = v->src_found = 0;
+    v->flags = 0; v->status = 0;
+    uint32_t kind = ev->kind;
+    uint64_t W = ev->width, H = ev->height;
+    if (kind < OR_HTOD || kind > OR_DTOD) {
+        v->flags = F_BAD_KIND; v->status = 1; return;
+    }
+    /* (i) validation: pitch rule (pitch >= WidthInBytes + XInBytes) and ranges */
+    if ((unsigned __int128)ev->dst_pitch < (unsigned __int128)W + ev->dst_x ||
+        (unsigned __int128)ev->src_pitch < (unsigned __int128)W + ev->src_x)
+        v->flags |= F_BAD_PITCH;
+    uint64_t ds = 0, dspan = 0, ss = 0, sspan = 0;
+    int dok = side_range(ev->dst, ev->dst_x, ev->dst_y, ev->dst_pitch, W, H, &ds, &dspan);
+    int sok = side_range(ev->src, ev->src_x, ev->src_y, ev->src_pitch, W, H, &ss, &sspan);
+    int nbytes_ok = ((unsigned __int128)W * H <= (unsigned __int128)UINT64_MAX);
+    if (!dok || !sok || !nbytes_ok) v->flags |= F_INVALID_RANGE;
+
+    /* (ii) device endpoints, dst then src */
+    if (kind == OR_HTOD || kind == OR_DTOD)
+        if (dok) device_side(st, ds, dspan, F_DST_NOT_ALLOCATED, F_DST_TOO_SMALL,
+                             &v->flags, &v->dst_expected, &v->dst_found);
+    if (kind == OR_DTOH || kind == OR_DTOD)
+        if (sok) device_side(st, ss, sspan, F_SRC_NOT_ALLOCATED, F_SRC_TOO_SMALL,
+                             &v->flags, &v->src_expected, &v->src_found);
+
+    /* (iii) host side: HtoD reads src, DtoH writes dst.  Row-major logical
+     * offsets o = r*W + c at address x = start + r*pitch + c (R-11). */
+    if ((kind == OR_HTOD && sok && nbytes_ok) || (kind == OR_DTOH && dok && nbytes_ok)) {
+        uint64_t hstart = (kind == OR_HTOD) ? ss : ds;
+        uint64_t hpitch = (kind == OR_HTOD) ? ev->src_pitch : ev->dst_pitch;
+        for (uint64_t r = 0; r < H && W; r++) {
+            for (uint64_t c = 0; c < W; c++) {
+                uint64_t x = hstart + r * hpitch + c;
+                uint64_t o = r * W + c;
+                int ad = addressable(st, x);
+                if (!ad) {
+                    if (v->first_unaddr == OR_NONE) v->first_unaddr = o;
+                } else if (kind == OR_HTOD && st->V[x - st->h0] != 0) {   /* R-1, R-3 */
+                    if (v->first_undef == OR_NONE) v->first_undef = o;
+                    v->undef_count++;
+                }
+            }
+        }
+    }
+    /* (iv) flags and status (R-4, R-8) */
+    if (v->first_unaddr != OR_NONE) v->flags |= F_HOST_UNADDRESSABLE;
+    if (v->undef_count > 0 && v->first_unaddr == OR_NONE) v->flags |= F_HOST_UNDEFINED;
+    uint32_t errors = v->flags & ~(st->undef_is_error ? 0u : F_HOST_UNDEFINED);
+    v->status = errors ? 1u : 0u;
+
+    /* (v) DtoH with no Error: the written host bytes become defined (R-5, R-7) */
+    if (kind == OR_DTOH && v->status == 0) {
+        for (uint64_t r = 0; r < H && W; r++)
+            for (uint64_t c = 0; c < W; c++)
+                st->V[ds + r * ev->dst_pitch + c - st->h0] = 0x00;
+    }
+}
+
+/* ------------------------------------------------------ O6 leak report */
+static int cmp_base(const void *a, const void *b) {
+    uint64_t x = ((const or_alloc *)a)->base, y = ((const or_alloc *)b)->base;
+    return x < y ? -1 : x > y;
+}
+
+uint64_t or_leaks(or_state *st, or_alloc *out, uint64_t cap) {
+    or_alloc *tmp = (or_alloc *)malloc((st->n_live + 1) * sizeof(or_alloc));
+    memcpy(tmp, st->live, st->n_live * sizeof(or_alloc));
+    qsort(tmp, st->n_live, sizeof(or_alloc), cmp_base);
+    for (uint64_t i = 0; i < st->n_live && i < cap; i++) out[i] = tmp[i];
+    free(tmp);
+    return st->n_live;
+}
+
+/* --------------------------------------------------------------- replay */
+/* Replays n events in order.  out_v receives one verdict per COPY event (in
+ * order); out_status receives one status per event (call status for
+ * MARK/SETV/REG/FREE, verdict status for COPY). Returns the number of copies. */
+uint64_t or_replay(or_state *st, const or_event *ev, uint64_t n, const uint8_t *blob,
+                   or_verdict *out_v, uint32_t *out_status) {
+    uint64_t nc = 0;
+    for (uint64_t i = 0; i < n; i++) {
+        const or_event *e = &ev[i];
+        uint32_t s = 0;
+        switch (e->op) {
+        case OR_MARK: s = (uint32_t)or_mark(st, e->dst, e->width, e->kind); break;
+        case OR_SETV: s = (uint32_t)or_set_vbits(st, e->dst, e->width, blob + e->src); break;
+        case OR_REG:  s = (uint32_t)or_register(st, e->dst, e->width, e->seq); break;
+        case OR_FREE: s = (uint32_t)or_free(st, e->dst, e->seq); break;
+        case OR_COPY:
+            or_check_copy(st, e, &out_v[nc]);
+            s = out_v[nc].status;
+            nc++;
+            break;
+        default: s = 1; break;
+        }
+        if (out_status) out_status[i] = s;
+    }
+    return nc;
+}

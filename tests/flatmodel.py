@@ -1,0 +1,179 @@
+"""An independent brute-force flat model ("an independent
+brute-force checker using dense per-byte A-bit and per-bit V-bit arrays").
+
+Used ONLY to pin the C oracle on tiny inputs.  It shares nothing with the
+oracle (different language, different algorithms): the allocation list is a
+``bisect``-searched sorted list, the host side is evaluated with numpy index
+arithmetic (``np.add.outer`` over rows x columns), first offsets come from
+``np.flatnonzero`` and counts from ``np.count_nonzero``.  Memory: dense
+unpacked arrays, so keep windows small (<= a few MiB).
+"""
+from __future__ import annotations
+
+import bisect
+
+import numpy as np
+
+NONE = (1 << 64) - 1
+U64 = (1 << 64) - 1
+FLAG = dict(DST_NA=1, DST_SMALL=2, SRC_NA=4, SRC_SMALL=8, HOST_UNADDR=16,
+            HOST_UNDEF=32, BAD_PITCH=64, INVALID_RANGE=128, BAD_KIND=256)
+
+
+class FlatModel:
+    def __init__(self, h0: int, s: int, undef_is_error: bool = False):
+        self.h0, self.s = h0, s
+        self.a = np.zeros(s, bool)               # unpacked A
+        self.v = np.full(s, 0xFF, np.uint8)
+        self.bases: list = []                     # sorted live bases
+        self.info: dict = {}                      # base -> (size, seq)
+        self.last = 0
+        self.uie = undef_is_error
+
+    # packed A in the on-device format (R-2) for state comparison
+    def packed_a(self) -> np.ndarray:
+        return np.packbits(self.a, bitorder="little")
+
+    def _win(self, addr, n):
+        return addr >= self.h0 and addr + n <= self.h0 + self.s
+
+    def mark(self, addr, n, state):
+        if state > 2:
+            return 1
+        if n == 0:
+            return 0
+        if not self._win(addr, n):
+            return 1
+        i = addr - self.h0
+        self.a[i:i + n] = state != 0
+        self.v[i:i + n] = 0 if state == 2 else 0xFF
+        return 0
+
+    def setv(self, addr, data):
+        n = len(data)
+        if n == 0:
+            return 0
+        if not self._win(addr, n):
+            return 1
+        i = addr - self.h0
+        if not self.a[i:i + n].all():
+            return 1
+        self.v[i:i + n] = np.frombuffer(bytes(data), np.uint8)
+        return 0
+
+    def _containing(self, x):
+        k = bisect.bisect_right(self.bases, x) - 1
+        if k >= 0:
+            b = self.bases[k]
+            if x < b + self.info[b][0]:
+                return b
+        return None
+
+    def register(self, base, size, seq):
+        if seq <= self.last or size == 0 or base == 0 or base + size > U64:
+            return 1
+        k = bisect.bisect_left(self.bases, base)
+        if k < len(self.bases) and self.bases[k] < base + size:
+            return 1
+        if k > 0 and self.bases[k - 1] + self.info[self.bases[k - 1]][0] > base:
+            return 1
+        self.bases.insert(k, base)
+        self.info[base] = (size, seq)
+        self.last = seq
+        return 0
+
+    def free(self, ptr, seq):
+        if seq <= self.last or ptr not in self.info:
+            return 1
+        self.bases.remove(ptr)
+        del self.info[ptr]
+        self.last = seq
+        return 0
+
+    def leaks(self):
+        return [(b, self.info[b][0], self.info[b][1]) for b in self.bases]
+
+    def _host_index(self, start, pitch, w, h):
+        """addresses of the logical bytes o = r*w + c, in o order"""
+        r = np.arange(h, dtype=object) if h else np.zeros(0, dtype=object)
+        c = np.arange(w, dtype=object) if w else np.zeros(0, dtype=object)
+        return np.add.outer(np.asarray(r) * pitch + start, np.asarray(c)).ravel()
+
+    def copy(self, e):
+        kind, w, h = int(e["kind"]), int(e["width"]), int(e["height"])
+        out = dict(first_unaddr=NONE, first_undef=NONE, undef_count=0, dst_expected=0,
+                   dst_found=0, src_expected=0, src_found=0, flags=0, status=0)
+        if kind not in (1, 2, 3):
+            out["flags"] = FLAG["BAD_KIND"]; out["status"] = 1
+            return out
+        sides = {}
+        for p in ("dst", "src"):
+            base, x, y, pitch = (int(e[p]), int(e[p + "_x"]), int(e[p + "_y"]), int(e[p + "_pitch"]))
+            if pitch < w + x:
+                out["flags"] |= FLAG["BAD_PITCH"]
+            start = base + y * pitch + x
+            span = 0 if (w == 0 or h == 0) else (h - 1) * pitch + w
+            sides[p] = (start, span, pitch, start + span <= U64)
+        bytes_ok = w * h <= U64
+        if not (sides["dst"][3] and sides["src"][3] and bytes_ok):
+            out["flags"] |= FLAG["INVALID_RANGE"]
+        dev = {1: ["dst"], 2: ["src"], 3: ["dst", "src"]}[kind]
+        for p in dev:
+            start, span, _, ok = sides[p]
+            if not ok:
+                continue
+            b = self._containing(start)
+            P = p.upper()
+            if b is None:
+                out["flags"] |= FLAG[P + "_NA"]
+            else:
+                avail = b + self.info[b][0] - start
+                if avail < span:
+                    out["flags"] |= FLAG[P + "_SMALL"]
+                    out[p + "_expected"], out[p + "_found"] = span, avail
+        hp = {1: "src", 2: "dst", 3: None}[kind]
+        if hp is not None and sides[hp][3] and bytes_ok and w and h:
+            start, _, pitch, _ = sides[hp]
+            xs = self._host_index(start, pitch, w, h)
+            inwin = np.array([(self.h0 <= x < self.h0 + self.s) for x in xs], bool)
+            idx = np.array([x - self.h0 if iw else 0 for x, iw in zip(xs, inwin)], np.int64)
+            addr = inwin & self.a[idx]
+            bad = np.flatnonzero(~addr)
+            if len(bad):
+                out["first_unaddr"] = int(bad[0])
+            if kind == 1:
+                und = addr & (self.v[idx] != 0)
+                u = np.flatnonzero(und)
+                out["undef_count"] = int(np.count_nonzero(und))
+                if len(u):
+                    out["first_undef"] = int(u[0])
+        if out["first_unaddr"] != NONE:
+            out["flags"] |= FLAG["HOST_UNADDR"]
+        if out["undef_count"] and out["first_unaddr"] == NONE:
+            out["flags"] |= FLAG["HOST_UNDEF"]
+        err = out["flags"] & ~(0 if self.uie else FLAG["HOST_UNDEF"])
+        out["status"] = 1 if err else 0
+        if kind == 2 and out["status"] == 0 and w and h:
+            start, _, pitch, _ = sides["dst"]
+            xs = self._host_index(start, pitch, w, h)
+            self.v[np.array([x - self.h0 for x in xs], np.int64)] = 0
+        return out
+
+    def replay(self, events, blob):
+        verdicts, status = [], []
+        for e in events:
+            op = int(e["op"])
+            if op == 1:
+                status.append(self.mark(int(e["dst"]), int(e["width"]), int(e["kind"])))
+            elif op == 2:
+                off, n = int(e["src"]), int(e["width"])
+                status.append(self.setv(int(e["dst"]), bytes(blob[off:off + n])))
+            elif op == 3:
+                status.append(self.register(int(e["dst"]), int(e["width"]), int(e["seq"])))
+            elif op == 4:
+                status.append(self.free(int(e["dst"]), int(e["seq"])))
+            elif op == 5:
+                v = self.copy(e)
+                verdicts.append(v)
+                status.append(v["status"])
+        return verdicts, status

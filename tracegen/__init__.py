@@ -1,0 +1,550 @@
+"""Seeded synthetic trace generators (input data only).
+
+This module is shared by the tests, ``bench.py`` and the oracle wrapper as the
+single source of *inputs*.  It deliberately contains none of the checking
+arithmetic of the method (no start-address folding, no span, no coverage, no
+shadow scan, no verdict logic): it only records what a program did -- host
+buffer allocations/writes, device allocations/frees and copy calls -- the way
+the paper's wrappers observe them (§3: "Anytime a program
+handles memory on the device or transfers data between the device and/or the
+host the respective Cudagrind wrapper will be called").
+
+Event stream format (one numpy structured record per call, ``EVENT_DTYPE``):
+
+=========  ==========================================================
+op         meaning of the fields
+=========  ==========================================================
+MARK       host shadow update: ``dst`` = addr,
+           ``width`` = len, ``kind`` = state (NOACCESS/UNDEFINED/DEFINED)
+SETV       exact V-bytes: ``dst`` = addr, ``width`` = len,
+           ``src`` = offset of the bytes in the trace's ``blob``
+REG        device allocation (Fig. 2 caption P:88): ``dst`` = base,
+           ``width`` = size
+FREE       device free: ``dst`` = ptr
+COPY       one cuMemcpy{HtoD,DtoH,DtoD,2D} call: ``kind``,
+           ``width`` (WidthInBytes), ``height`` (1 for 1D), and per side the
+           raw CUDA_MEMCPY2D fields base / X / Y / pitch
+=========  ==========================================================
+
+``seq`` is one global, strictly increasing event counter (SPEC's
+``SimState.seq``).
+
+Device addresses come from SPEC's deterministic bump allocator (S:370:
+"Device addresses come from a deterministic bump allocator starting at
+0x0100_0000"), with a 256-byte alignment (an invented detail, R-17).
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+from typing import Dict, List, Optional
+
+import numpy as np
+
+OP_MARK, OP_SETV, OP_REG, OP_FREE, OP_COPY = 1, 2, 3, 4, 5
+HTOD, DTOH, DTOD = 1, 2, 3
+NOACCESS, UNDEFINED, DEFINED = 0, 1, 2
+
+EVENT_DTYPE = np.dtype([
+    ("op", "<u4"), ("kind", "<u4"), ("seq", "<u8"),
+    ("width", "<u8"), ("height", "<u8"),
+    ("dst", "<u8"), ("dst_x", "<u8"), ("dst_y", "<u8"), ("dst_pitch", "<u8"),
+    ("src", "<u8"), ("src_x", "<u8"), ("src_y", "<u8"), ("src_pitch", "<u8"),
+])
+assert EVENT_DTYPE.itemsize == 96
+
+DEVICE_HEAP_BASE = 0x0100_0000
+DEVICE_ALIGN = 256               # invented (R-17)
+KiB, MiB, GiB = 1 << 10, 1 << 20, 1 << 30
+
+
+@dataclasses.dataclass
+class Trace:
+    """A recorded call stream plus the host shadow window it lives in."""
+    name: str
+    events: np.ndarray            # EVENT_DTYPE[n]
+    blob: np.ndarray              # uint8 bytes referenced by SETV events
+    host_base: int                # H0 (4096-aligned)
+    host_size: int                # S  (multiple of 4096)
+    meta: Dict = dataclasses.field(default_factory=dict)
+
+    @property
+    def copy_index(self) -> np.ndarray:
+        return np.flatnonzero(self.events["op"] == OP_COPY)
+
+    @property
+    def n_copies(self) -> int:
+        return int(np.count_nonzero(self.events["op"] == OP_COPY))
+
+
+class TraceBuilder:
+    """Append-only recorder. Columns are kept as Python lists of tuples for
+    small traces and as bulk numpy blocks for the large configurations."""
+
+    def __init__(self, name: str, host_base: int, host_size: int):
+        assert host_base % 4096 == 0 and host_size % 4096 == 0
+        self.name = name
+        self.host_base = host_base
+        self.host_size = host_size
+        self._blocks: List[np.ndarray] = []
+        self._rows: List[tuple] = []
+        self._blob = bytearray()
+        self._seq = 0
+        self.heap_cursor = DEVICE_HEAP_BASE
+        self.meta: Dict = {}
+
+    # -- raw appends ---------------------------------------------------------
+    def _flush_rows(self):
+        if self._rows:
+            arr = np.zeros(len(self._rows), EVENT_DTYPE)
+            for i, r in enumerate(self._rows):
+                arr[i] = r
+            self._blocks.append(arr)
+            self._rows = []
+
+    def _next_seq(self) -> int:
+        self._seq += 1
+        return self._seq
+
+    def _row(self, op, kind=0, width=0, height=0, dst=0, dst_x=0, dst_y=0,
+             dst_pitch=0, src=0, src_x=0, src_y=0, src_pitch=0) -> int:
+        seq = self._next_seq()
+        self._rows.append((op, kind, seq, width, height, dst, dst_x, dst_y,
+                           dst_pitch, src, src_x, src_y, src_pitch))
+        return seq
+
+    def block(self, arr: np.ndarray) -> np.ndarray:
+        """Append a pre-built EVENT_DTYPE block; assigns its seq numbers."""
+        self._flush_rows()
+        arr = arr.copy()
+        arr["seq"] = np.arange(self._seq + 1, self._seq + 1 + len(arr), dtype=np.uint64)
+        self._seq += len(arr)
+        self._blocks.append(arr)
+        return arr
+
+    # -- calls ---------------------------------------------------------------
+    def mark(self, addr: int, length: int, state: int) -> int:
+        return self._row(OP_MARK, kind=state, dst=addr, width=length)
+
+    def setv(self, addr: int, vbytes: bytes) -> int:
+        off = len(self._blob)
+        self._blob += bytes(vbytes)
+        return self._row(OP_SETV, dst=addr, width=len(vbytes), src=off)
+
+    def register(self, base: int, size: int) -> int:
+        return self._row(OP_REG, dst=base, width=size)
+
+    def free(self, ptr: int) -> int:
+        return self._row(OP_FREE, dst=ptr)
+
+    def malloc(self, size: int) -> int:
+        """Play the driver: bump allocate, then record REG."""
+        base = self.heap_cursor
+        self.heap_cursor = (base + size + DEVICE_ALIGN - 1) // DEVICE_ALIGN * DEVICE_ALIGN
+        self.register(base, size)
+        return base
+
+    def copy1d(self, kind: int, dst: int, src: int, nbytes: int) -> int:
+        """cuMemcpyHtoD/DtoH/DtoD: a 2D copy of one row, pitch = width."""
+        return self._row(OP_COPY, kind=kind, width=nbytes, height=1,
+                         dst=dst, dst_pitch=nbytes, src=src, src_pitch=nbytes)
+
+    def copy2d(self, kind: int, width: int, height: int,
+               dst: int, dst_x: int, dst_y: int, dst_pitch: int,
+               src: int, src_x: int, src_y: int, src_pitch: int) -> int:
+        """cuMemcpy2D with raw CUDA_MEMCPY2D fields."""
+        return self._row(OP_COPY, kind=kind, width=width, height=height,
+                         dst=dst, dst_x=dst_x, dst_y=dst_y, dst_pitch=dst_pitch,
+                         src=src, src_x=src_x, src_y=src_y, src_pitch=src_pitch)
+
+    def build(self) -> Trace:
+        self._flush_rows()
+        ev = np.concatenate(self._blocks) if self._blocks else np.zeros(0, EVENT_DTYPE)
+        return Trace(self.name, ev, np.frombuffer(bytes(self._blob), np.uint8).copy(),
+                     self.host_base, self.host_size, self.meta)
+
+
+def _log_uniform(rng: np.random.Generator, a: float, b: float, n: int) -> np.ndarray:
+    """exp(U[ln a, ln b]) rounded down (SURVEY §8(d) recipe)."""
+    return np.floor(np.exp(rng.uniform(math.log(a), math.log(b), n))).astype(np.uint64)
+
+
+# ---------------------------------------------------------------------------
+# Config 1: the toy trace (BASELINE.json configs[0])
+# ---------------------------------------------------------------------------
+def toy() -> Trace:
+    H0 = 0x10000
+    tb = TraceBuilder("toy", H0, 64 * KiB)
+    h0, h1, h2, h3 = H0 + 0x0000, H0 + 0x0200, H0 + 0x0800, H0 + 0x2000
+    # host buffers (host_alloc = UNDEFINED, host_write = DEFINED)
+    tb.mark(h0, 256, UNDEFINED); tb.mark(h0, 256, DEFINED)
+    tb.mark(h1, 1024, UNDEFINED); tb.mark(h1, 100, DEFINED); tb.mark(h1 + 132, 1024 - 132, DEFINED)
+    tb.setv(h1 + 500, b"\x0f")
+    tb.mark(h2, 4096, UNDEFINED); tb.mark(h2, 4096, DEFINED)
+    tb.mark(h3, 4096, UNDEFINED)
+    d0 = tb.malloc(256); d1 = tb.malloc(1024); d2 = tb.malloc(4096)
+    c = {}
+    c["C1"] = tb.copy1d(HTOD, d0, h0, 256)
+    c["C2"] = tb.copy1d(HTOD, d1, h1, 1024)
+    c["C3"] = tb.copy1d(HTOD, d2, h2, 4096)
+    c["C4"] = tb.copy1d(DTOH, h3, d2, 4096)
+    c["C5"] = tb.copy1d(HTOD, d2, h3, 4096)
+    c["C6"] = tb.copy1d(HTOD, d0, h2, 272)
+    c["C7"] = tb.copy1d(DTOH, h1, d1, 1024)
+    c["C8"] = tb.copy1d(HTOD, d0, h1, 256)
+    tb.free(d1)
+    c["C9"] = tb.copy1d(HTOD, d1, h1, 1024)
+    c["C10"] = tb.copy1d(DTOH, h0, d0, 256)
+    tb.free(d0)
+    tb.meta.update(dict(d=[d0, d1, d2], h=[h0, h1, h2, h3], copies=c))
+    return tb.build()
+
+
+# ---------------------------------------------------------------------------
+# The paper's worked example: Listing 2 -> Listing 5
+# ---------------------------------------------------------------------------
+def listing2() -> Trace:
+    size = 1000000
+    H0 = 1 << 20
+    tb = TraceBuilder("listing2", H0, 32 * MiB)
+    c = tb.malloc(size * 4)                          # P:139 sizeof(float)
+    a = tb.malloc(size * 8)
+    b = tb.malloc(size * 8)
+    a_h, b_h, c_host = H0, H0 + 8 * MiB + 4096, H0 + 16 * MiB + 8192
+    tb.mark(a_h, size * 8, DEFINED)
+    tb.mark(b_h, size * 8, DEFINED)
+    tb.mark(c_host, size * 8, UNDEFINED)
+    tb.copy1d(HTOD, a, a_h, size * 8)
+    tb.copy1d(HTOD, b, b_h, size * 8)
+    s = tb.copy1d(DTOH, c_host, c, size * 8)
+    tb.meta.update(dict(c=c, a=a, b=b, c_host=c_host, faulty_seq=s))
+    return tb.build()
+
+
+# ---------------------------------------------------------------------------
+# Random tiny traces (<=200 events in a 64 KiB window)
+# ---------------------------------------------------------------------------
+def random_tiny(seed: int, n_events: int = 200, window: int = 64 * KiB,
+                host_base: int = 0x40000) -> Trace:
+    """Unaligned, overlapping, out-of-window, 2D, reuse-after-free: everything
+    the method must handle, at sizes a brute-force checker finishes quickly."""
+    rng = np.random.default_rng(seed)
+    tb = TraceBuilder(f"tiny{seed}", host_base, window)
+    live: List[tuple] = []
+    freed: List[tuple] = []
+    cursor = DEVICE_HEAP_BASE
+
+    def rand_host(maxlen=4096):
+        # mostly inside the window, sometimes straddling either edge
+        u = rng.random()
+        if u < 0.05:
+            start = host_base - int(rng.integers(1, 64))
+        elif u < 0.10:
+            start = host_base + window - int(rng.integers(1, 64))
+        else:
+            start = host_base + int(rng.integers(0, window))
+        return start, int(rng.integers(0, maxlen))
+
+    def rand_dev():
+        u = rng.random()
+        if live and u < 0.75:
+            b, s = live[int(rng.integers(len(live)))]
+            return b + int(rng.integers(0, s + 2))       # sometimes one past end
+        if freed and u < 0.85:
+            b, s = freed[int(rng.integers(len(freed)))]
+            return b + int(rng.integers(0, s))
+        return DEVICE_HEAP_BASE + int(rng.integers(0, 1 << 16))
+
+    # a few large host buffers first, so that many copies see addressable bytes
+    for _ in range(4):
+        a = host_base + int(rng.integers(0, window // 2))
+        l = int(rng.integers(window // 8, window // 2))
+        tb.mark(a, min(l, host_base + window - a), int(rng.choice([UNDEFINED, DEFINED], p=[0.3, 0.7])))
+    for _ in range(n_events - 4):
+        u = rng.random()
+        if u < 0.18:
+            a, l = rand_host(6000)
+            st = int(rng.integers(0, 3))
+            a = max(a, host_base); l = min(l, host_base + window - a)
+            tb.mark(a, l, st)
+        elif u < 0.24:
+            a, l = rand_host(64)
+            a = max(a, host_base); l = min(l, host_base + window - a)
+            tb.setv(a, rng.integers(0, 256, l, dtype=np.uint8).tobytes())
+        elif u < 0.34:
+            size = int(rng.integers(0, 3000))
+            if freed and rng.random() < 0.3:             # address reuse
+                b, s = freed[int(rng.integers(len(freed)))]
+                base = b + int(rng.integers(0, 64))
+            elif rng.random() < 0.05:
+                base = int(rng.choice([0, cursor]))        # base 0 / duplicate
+            else:
+                base = cursor
+                cursor = (cursor + max(size, 1) + int(rng.integers(0, 3)) * 128 + 255) // 256 * 256
+            tb.register(base, size)
+            # our own bookkeeping only to aim later calls; no checking here
+            if size and base and not any(b < base + size and base < b + s for b, s in live):
+                live.append((base, size))
+        elif u < 0.42:
+            if live and rng.random() < 0.8:
+                i = int(rng.integers(len(live)))
+                b, s = live[i]
+                ptr = b if rng.random() < 0.85 else b + int(rng.integers(0, 16))
+                tb.free(ptr)
+                if ptr == b:
+                    freed.append(live.pop(i))
+            else:
+                tb.free(int(rng.choice([0, DEVICE_HEAP_BASE + 8])))
+        else:
+            kind = int(rng.choice([HTOD, DTOH, DTOD], p=[0.45, 0.4, 0.15]))
+            two_d = rng.random() < 0.35
+            if kind == HTOD:
+                dst = rand_dev(); src, ln = rand_host()
+            elif kind == DTOH:
+                dst, ln = rand_host(); src = rand_dev()
+            else:
+                dst = rand_dev(); src = rand_dev(); ln = int(rng.integers(0, 4096))
+            if not two_d:
+                if rng.random() < 0.05:
+                    ln = 0
+                tb.copy1d(kind, dst, src, ln)
+            else:
+                w = int(rng.integers(0, 200)); h = int(rng.integers(0, 24))
+                def side():
+                    x = int(rng.integers(0, 64)); y = int(rng.integers(0, 4))
+                    pitch = w + x + int(rng.integers(0, 64))
+                    if rng.random() < 0.1:
+                        pitch = int(rng.integers(0, max(w + x, 1)))   # BAD_PITCH
+                    return x, y, pitch
+                dx, dy, dp = side(); sx, sy, sp = side()
+                if rng.random() < 0.02:
+                    dy = 1 << 62                                     # overflow
+                tb.copy2d(kind, w, h, dst, dx, dy, dp, src, sx, sy, sp)
+    return tb.build()
+
+
+# ---------------------------------------------------------------------------
+# Config 2: 1M small copies vs a 100k-entry table, 1% injected (configs[1])
+# ---------------------------------------------------------------------------
+INJ_NONE, INJ_DST_NA, INJ_SRC_NA, INJ_TOO_SMALL, INJ_HOST_UNADDR, INJ_HOST_UNDEF, INJ_DTOD_BAD_SRC = range(7)
+
+
+def c2_small(seed: int = 13100902, n_copies: int = 1_000_000, n_allocs: int = 100_000,
+             inject_frac: float = 0.01, redzone: int = 16) -> Trace:
+    """SURVEY §8(d) C2.  Every copy gets a private host buffer (malloc-like:
+    16-byte aligned, >= ``redzone`` NOACCESS bytes on both sides), so the trace
+    is a single hazard-free batch and the dirty set is exactly the injected
+    set.  HtoD sources are written (DEFINED); DtoH destinations are allocated
+    but not written (UNDEFINED), like ``c_host`` in Listing 2."""
+    assert redzone >= 16 and redzone % 16 == 0
+    rng = np.random.default_rng(seed)
+    H0 = 1 << 32
+    # ---- device allocations (bump allocator)
+    sizes = _log_uniform(rng, 64, 64 * KiB, n_allocs)
+    aligned = (sizes + DEVICE_ALIGN - 1) // DEVICE_ALIGN * DEVICE_ALIGN
+    bases = (DEVICE_HEAP_BASE + np.concatenate([[0], np.cumsum(aligned)[:-1]])).astype(np.uint64)
+    heap_end = int(bases[-1] + aligned[-1])
+    n_freed = max(1, n_allocs // 100)
+    freed_ids = rng.choice(n_allocs, n_freed, replace=False)
+    usable = np.ones(n_allocs, bool); usable[freed_ids] = False
+    use_ids = np.flatnonzero(usable)
+    order = use_ids[np.argsort(sizes[use_ids], kind="stable")]
+    sorted_sizes = sizes[order]
+
+    def pick_alloc(lens):
+        """an allocation at least as large as the copy, uniformly among those"""
+        lo = np.searchsorted(sorted_sizes, lens, side="left")
+        lo = np.minimum(lo, len(order) - 1)
+        p = lo + np.floor(rng.random(len(lens)) * (len(order) - lo)).astype(np.int64)
+        return order[np.minimum(p, len(order) - 1)]
+
+    # ---- copies: kind mix 50/40/10, length log-uniform 64 B-64 KiB
+    kinds = rng.choice(np.array([HTOD, DTOH, DTOD], np.uint32), n_copies, p=[0.5, 0.4, 0.1])
+    lens = _log_uniform(rng, 64, 64 * KiB, n_copies)
+    aid = pick_alloc(lens)
+    lens = np.minimum(lens, sizes[aid])
+    dev = bases[aid] + np.floor(rng.random(n_copies) * (sizes[aid] - lens + 1)).astype(np.uint64)
+    aid2 = pick_alloc(lens)
+    dev2 = bases[aid2] + np.floor(rng.random(n_copies) * (sizes[aid2] - lens + 1)).astype(np.uint64)
+
+    # ---- injection classes (1 %), kinds made consistent with the class
+    inj = np.zeros(n_copies, np.uint8)
+    n_inj = int(round(n_copies * inject_frac))
+    inj_idx = rng.choice(n_copies, n_inj, replace=False)
+    inj[inj_idx] = np.arange(n_inj) % 6 + 1
+    kinds[(inj == INJ_DST_NA) & (kinds == DTOH)] = HTOD
+    kinds[(inj == INJ_SRC_NA) & (kinds == HTOD)] = DTOH
+    kinds[(inj == INJ_HOST_UNADDR) & (kinds == DTOD)] = HTOD
+    kinds[inj == INJ_HOST_UNDEF] = HTOD
+    kinds[inj == INJ_DTOD_BAD_SRC] = DTOD
+
+    # device pointers per side: HtoD dst=dev; DtoH src=dev; DtoD dst=dev, src=dev2
+    dptr_dst = np.where(kinds == DTOH, 0, dev).astype(np.uint64)
+    dptr_src = np.where(kinds == DTOH, dev, np.where(kinds == DTOD, dev2, 0)).astype(np.uint64)
+    freed_bases = bases[freed_ids]
+
+    def bad_ptr(mask):
+        """alternately inside a freed allocation (use after free) or past the heap"""
+        k = int(np.count_nonzero(mask))
+        fb = freed_bases[rng.integers(0, len(freed_bases), k)]
+        beyond = heap_end + rng.integers(0, 1 << 20, k).astype(np.uint64)
+        return np.where(np.arange(k) % 2 == 0, fb, beyond).astype(np.uint64)
+    m = inj == INJ_DST_NA; dptr_dst[m] = bad_ptr(m)
+    m = inj == INJ_SRC_NA; dptr_src[m] = bad_ptr(m)
+    m = inj == INJ_DTOD_BAD_SRC; dptr_src[m] = bad_ptr(m)
+    # TooSmall: the device range starts max(len-over,1) bytes before its
+    # allocation's end, over = 1..64 (the copy runs past the end)
+    m = np.flatnonzero(inj == INJ_TOO_SMALL)
+    over = rng.integers(1, 65, len(m)).astype(np.uint64)
+    room = np.maximum(lens[m].astype(np.int64) - over.astype(np.int64), 1).astype(np.uint64)
+    a_end = bases[aid[m]] + sizes[aid[m]]
+    on_src = kinds[m] == DTOH
+    dptr_src[m[on_src]] = (a_end - room)[on_src]
+    dptr_dst[m[~on_src]] = (a_end - room)[~on_src]
+
+    # ---- host buffers: private, 16-aligned, redzoned
+    has_host = kinds != DTOD
+    buf_len = np.where(has_host, lens, 0).astype(np.uint64)
+    copy_len = lens.copy()
+    m = inj == INJ_HOST_UNADDR       # +1..redzone bytes past the buffer end
+    copy_len[m] += rng.integers(1, redzone + 1, int(np.count_nonzero(m))).astype(np.uint64)
+    slot = np.where(has_host, (buf_len + 2 * redzone + 15) // 16 * 16, 0).astype(np.uint64)
+    host_start = (H0 + 4096 + redzone + np.concatenate([[0], np.cumsum(slot)[:-1]])).astype(np.uint64)
+    end = int(host_start[-1]) - redzone + int(slot[-1]) + 4096
+    S = (end - H0 + MiB - 1) // MiB * MiB
+
+    tb = TraceBuilder("c2_small", H0, S)
+    hidx = np.flatnonzero(has_host)
+    marks = np.zeros(len(hidx), EVENT_DTYPE)
+    marks["op"] = OP_MARK
+    marks["dst"] = host_start[hidx]
+    marks["width"] = buf_len[hidx]
+    marks["kind"] = np.where(kinds[hidx] == HTOD, DEFINED, UNDEFINED)
+    tb.block(marks)
+    # HostUndefined: 1..16 random bytes of the source get a random non-zero V-byte
+    for i in np.flatnonzero(inj == INJ_HOST_UNDEF):
+        k = min(int(rng.integers(1, 17)), int(buf_len[i]))
+        for p in np.sort(rng.choice(int(buf_len[i]), k, replace=False)):
+            tb.setv(int(host_start[i]) + int(p), bytes([int(rng.integers(1, 256))]))
+    regs = np.zeros(n_allocs, EVENT_DTYPE)
+    regs["op"] = OP_REG; regs["dst"] = bases; regs["width"] = sizes
+    tb.block(regs)
+    frees = np.zeros(n_freed, EVENT_DTYPE)
+    frees["op"] = OP_FREE; frees["dst"] = np.sort(freed_bases)
+    tb.block(frees)
+    cp = np.zeros(n_copies, EVENT_DTYPE)
+    cp["op"] = OP_COPY; cp["kind"] = kinds; cp["width"] = copy_len; cp["height"] = 1
+    cp["dst_pitch"] = copy_len; cp["src_pitch"] = copy_len
+    cp["dst"] = np.where(kinds == DTOH, host_start, dptr_dst)
+    cp["src"] = np.where(kinds == HTOD, host_start, dptr_src)
+    tb.block(cp)
+    tb.meta.update(dict(inject=inj, kinds=kinds, n_freed=n_freed, n_allocs=n_allocs, seed=seed))
+    return tb.build()
+
+
+# ---------------------------------------------------------------------------
+# Config 3: one 8 GiB HtoD buffer, one undefined byte per MiB (configs[2])
+# ---------------------------------------------------------------------------
+def c3_single(seed: int = 13100903, size: int = 8 * GiB, dtoh: bool = False,
+              stride: int = MiB) -> Trace:
+    rng = np.random.default_rng(seed)
+    H0 = 1 << 36
+    S = size + 8 * KiB
+    tb = TraceBuilder("c3_single" + ("_dtoh" if dtoh else ""), H0, S)
+    hbuf = H0 + 4096
+    tb.mark(hbuf, size, DEFINED if not dtoh else UNDEFINED)
+    n_holes = size // stride
+    offs = np.arange(n_holes, dtype=np.uint64) * stride + rng.integers(0, stride, n_holes).astype(np.uint64)
+    vals = rng.integers(1, 256, n_holes).astype(np.uint8)
+    if not dtoh:
+        rows = np.zeros(n_holes, EVENT_DTYPE)
+        rows["op"] = OP_SETV; rows["dst"] = hbuf + offs; rows["width"] = 1
+        rows["src"] = np.arange(n_holes, dtype=np.uint64)
+        tb._blob += vals.tobytes()
+        tb.block(rows)
+    d = tb.malloc(size)
+    if dtoh:
+        tb.copy1d(DTOH, hbuf, d, size)
+    else:
+        tb.copy1d(HTOD, d, hbuf, size)
+    tb.meta.update(dict(hole_offsets=offs, hole_values=vals, size=size, dtoh=dtoh))
+    return tb.build()
+
+
+# ---------------------------------------------------------------------------
+# Config 4: 100k cuMemcpy2D pitched copies (configs[3])
+# ---------------------------------------------------------------------------
+def c4_pitched(seed: int = 13100904, n_copies: int = 100_000, n_bufs: int = 32,
+               rows: int = 4096, width: int = 16 * KiB, pitch: int = 16896,
+               inject_frac: float = 0.01) -> Trace:
+    """W log-uniform [1 KiB, 16 KiB], H log-uniform [1, 4096] (SURVEY's
+    reading of "width 1-16 KB, height 1-4096"); host 2D buffers whose pitch
+    padding is NOACCESS; injected column overruns into the padding, BAD_PITCH
+    and device height overruns."""
+    rng = np.random.default_rng(seed)
+    H0 = 1 << 40
+    guard = MiB
+    buf_bytes = rows * pitch
+    n_host = 2 * n_bufs
+    S = (n_host * (buf_bytes + guard) + guard + (1 << 20) - 1) // (1 << 20) * (1 << 20)
+    tb = TraceBuilder("c4_pitched", H0, S)
+    hbase = H0 + guard + np.arange(n_host, dtype=np.uint64) * (buf_bytes + guard)
+    # valid width of every row addressable; padding stays NOACCESS
+    r = np.arange(rows, dtype=np.uint64)
+    marks = np.zeros(n_host * rows, EVENT_DTYPE)
+    marks["op"] = OP_MARK
+    marks["dst"] = (hbase[:, None] + r[None, :] * pitch).ravel()
+    marks["width"] = width
+    marks["kind"] = np.repeat(np.where(np.arange(n_host) < n_bufs, DEFINED, UNDEFINED), rows)
+    tb.block(marks)
+    dbases = np.array([tb.malloc(buf_bytes) for _ in range(n_host)], dtype=np.uint64)
+
+    kinds = np.where(rng.random(n_copies) < 0.5, HTOD, DTOH).astype(np.uint32)
+    W = _log_uniform(rng, KiB, width + 1, n_copies)
+    W = np.minimum(W, width)
+    H = _log_uniform(rng, 1, rows + 1, n_copies)
+    H = np.minimum(H, rows)
+    hb = rng.integers(0, n_bufs, n_copies)
+    hb = np.where(kinds == HTOD, hb, hb + n_bufs)
+    db = rng.integers(0, n_host, n_copies)
+    hx = np.floor(rng.random(n_copies) * (width - W + 1)).astype(np.uint64)
+    hy = np.floor(rng.random(n_copies) * (rows - H + 1)).astype(np.uint64)
+    dx = np.floor(rng.random(n_copies) * (width - W + 1)).astype(np.uint64)
+    dy = np.floor(rng.random(n_copies) * (rows - H + 1)).astype(np.uint64)
+    hpitch = np.full(n_copies, pitch, np.uint64)
+    dpitch = np.full(n_copies, pitch, np.uint64)
+
+    inj = np.zeros(n_copies, np.uint8)
+    n_inj = int(round(n_copies * inject_frac))
+    inj_idx = rng.choice(n_copies, n_inj, replace=False)
+    cls = np.arange(n_inj) % 3 + 1           # 1 column overrun, 2 BAD_PITCH, 3 height overrun
+    inj[inj_idx] = cls
+    m = np.flatnonzero(inj == 1)             # X+W in (16 KiB, pitch]
+    hx[m] = width - W[m] + rng.integers(1, pitch - width + 1, len(m)).astype(np.uint64)
+    m = np.flatnonzero(inj == 2)             # X+W > pitch
+    hx[m] = pitch - W[m] + rng.integers(1, 64, len(m)).astype(np.uint64)
+    m = np.flatnonzero(inj == 3)             # device rows past the allocation (Y stays inside)
+    H[m] = np.maximum(H[m], 9)
+    hy[m] = np.minimum(hy[m], rows - H[m])
+    dy[m] = rows - H[m] + rng.integers(1, 9, len(m)).astype(np.uint64)
+
+    cp = np.zeros(n_copies, EVENT_DTYPE)
+    cp["op"] = OP_COPY; cp["kind"] = kinds; cp["width"] = W; cp["height"] = H
+    is_h2d = kinds == HTOD
+    cp["src"] = np.where(is_h2d, hbase[hb], dbases[db])
+    cp["src_x"] = np.where(is_h2d, hx, dx); cp["src_y"] = np.where(is_h2d, hy, dy)
+    cp["src_pitch"] = np.where(is_h2d, hpitch, dpitch)
+    cp["dst"] = np.where(is_h2d, dbases[db], hbase[hb])
+    cp["dst_x"] = np.where(is_h2d, dx, hx); cp["dst_y"] = np.where(is_h2d, dy, hy)
+    cp["dst_pitch"] = np.where(is_h2d, dpitch, hpitch)
+    tb.block(cp)
+    tb.meta.update(dict(inject=inj, kinds=kinds, W=W, H=H, seed=seed))
+    return tb.build()
+
+
+CONFIGS = {
+    "toy": toy,
+    "c2_small": c2_small,
+    "c3_single": c3_single,
+    "c4_pitched": c4_pitched,
+}
