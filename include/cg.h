@@ -1,0 +1,267 @@
+/*
+ * cg.h -- C ABI of the B200-native batched Cudagrind transfer checker.
+ *
+ * Cudagrind (Baumann & Gracia, arXiv 1310.0901) wraps "all CUDA Driver API
+ * functions related to allocation, deallocation and transfer of memory" and
+ * cross-checks their parameters "against this list [of device allocations]
+ * as well as the knowledge of Valgrind about the ... host memory" (PAPER.md
+ * §2.2, §3).  This library is the data-parallel core of those
+ * checks: it receives what the wrappers observe -- device allocations/frees
+ * and batches of copy descriptors -- and answers, on a B200, the paper's error
+ * classes plus the DtoH definedness update and the leak
+ * sweep (abstract).
+ *
+ * Conventions
+ *  - Every function returns a cg_status (int).  Per-descriptor problems never
+ *    fail a call: they are reported in the cg_verdict array ("report and
+ *    continue").  Call-level problems (bad arguments, CUDA errors)
+ *    return a nonzero status and set cg_last_error(ctx).
+ *  - "d_" pointers are device pointers on the context's device; "h_" pointers
+ *    are host pointers.  The library never frees caller memory.
+ *  - "stream" is a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)
+ *    or NULL for the legacy default stream.  Asynchronous calls only enqueue
+ *    work; the caller synchronises.
+ *  - A context is single-writer: calls on one context must
+ *    not overlap from several host threads.
+ *  - Arithmetic is unsigned 64-bit; there is no floating point anywhere.
+ *
+ * Host shadow format (readings R-1, R-2):
+ *  - the host window is [host_base, host_base + host_size), host_base and
+ *    host_size multiples of 4096;
+ *  - V: one byte per host byte, bit k set = bit k of that byte undefined
+ *    (Memcheck's V polarity); a byte is undefined iff its V-byte != 0;
+ *  - A: one bit per host byte, bit (x-host_base)&7 of byte (x-host_base)>>3,
+ *    1 = addressable;
+ *  - host bytes outside the window are unaddressable (R-15); fresh state is
+ *    A = 0, V = 0xFF.
+ */
+#ifndef CG_H_
+#define CG_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (SPEC S:303-306 DriverStatus; CG_ERR_INVALID_VALUE mirrors
+ *      CUDA_ERROR_INVALID_VALUE = 1, the "invalid argument" of P:188) ---- */
+typedef int cg_status;
+enum {
+  CG_OK = 0,
+  CG_ERR_INVALID_VALUE = 1,
+  CG_ERR_INVALID_CONTEXT = 2,
+  CG_ERR_OUT_OF_MEMORY = 3,
+  CG_ERR_NOT_INITIALIZED = 4,
+  CG_ERR_CUDA = 5,
+  CG_ERR_NCCL = 6
+};
+
+/* ---- copy kinds: host/device, device/host, device/device ---- */
+enum { CG_HTOD = 1, CG_DTOH = 2, CG_DTOD = 3 };
+
+/* ---- host mark states (SPEC S:355-358 host_alloc / host_write / host_free) ---- */
+enum { CG_NOACCESS = 0, CG_UNDEFINED = 1, CG_DEFINED = 2 };
+
+#define CG_NONE UINT64_MAX
+
+/* ---- verdict flags, in SPEC's diagnostic order (R-14) ---- */
+enum {
+  CG_F_DST_NOT_ALLOCATED = 1u << 0,  /* P:80 copy into unallocated memory            */
+  CG_F_DST_TOO_SMALL = 1u << 1,      /* P:82 copying more than was allocated          */
+  CG_F_SRC_NOT_ALLOCATED = 1u << 2,  /* P:80 copy from unallocated memory             */
+  CG_F_SRC_TOO_SMALL = 1u << 3,      /* P:82, Listing 5                         */
+  CG_F_HOST_UNADDRESSABLE = 1u << 4, /* P:77/P:80 host range not addressable (A-bits) */
+  CG_F_HOST_UNDEFINED = 1u << 5,     /* P:81 undefined host data sent (Warning)      */
+  CG_F_BAD_PITCH = 1u << 6,          /* R-12: pitch < WidthInBytes + XInBytes         */
+  CG_F_INVALID_RANGE = 1u << 7,      /* an address range overflows 64 bits      */
+  CG_F_BAD_KIND = 1u << 8            /* R-16: kind not in {HTOD, DTOH, DTOD}          */
+};
+
+/* One cuMemcpy{HtoD,DtoH,DtoD,2D} call, with the raw CUDA_MEMCPY2D fields
+ * (P:62).  96 bytes, 8-byte aligned, array-of-structs.
+ *  - 1D copies are 2D copies with height = 1, x = y = 0, pitch = width.
+ *  - per side: start = base + y*pitch + x; span = (width==0 || height==0) ? 0
+ *    : (height-1)*pitch + width; row r covers [start + r*pitch, +width).
+ *  - seq: position of the call in the program's single global event order
+ *    (SPEC SimState.seq); the allocation table is evaluated "as of" seq
+ *    (an allocation e is visible iff e.alloc_seq < seq < e.free_seq). */
+typedef struct {
+  uint32_t kind;       /* CG_HTOD / CG_DTOH / CG_DTOD                  */
+  uint32_t reserved;   /* must be 0                                    */
+  uint64_t seq;
+  uint64_t width;      /* WidthInBytes                                 */
+  uint64_t height;     /* Height (1 for 1D)                            */
+  uint64_t dst, dst_x, dst_y, dst_pitch;
+  uint64_t src, src_x, src_y, src_pitch;
+} cg_copy_desc;
+
+/* Result for one descriptor.  64 bytes.  Clean = {NONE, NONE, 0, 0,0,0,0, 0, 0}.
+ *  - first_unaddr: lowest logical offset o = r*width + c of a host byte that is
+ *    not addressable (SPEC check_addressable S:63-71), else CG_NONE;
+ *  - first_undef / undef_count: HtoD only -- lowest offset / number of
+ *    addressable host bytes with a nonzero V-byte (R-3, R-6);
+ *  - *_expected / *_found: for *_TOO_SMALL only, the device span and the bytes
+ *    from start to the end of the allocation containing start (Listing 5
+ *    "Expected 8000000 allocated bytes but only found 4000000"; S:160,
+ *    S:192); 0 otherwise (R-19);
+ *  - status: CG_ERR_INVALID_VALUE iff an Error flag is set;
+ *    every flag except HOST_UNDEFINED is an Error unless undef_is_error. */
+typedef struct {
+  uint64_t first_unaddr, first_undef, undef_count;
+  uint64_t dst_expected, dst_found, src_expected, src_found;
+  uint32_t flags, status;
+} cg_verdict;
+
+/* One live allocation in a leak report, ascending base. */
+typedef struct {
+  uint64_t base, size, alloc_seq;
+} cg_alloc_record;
+
+/* One host shadow update for cg_host_mark_batch.  24 bytes. */
+typedef struct {
+  uint64_t addr, len;
+  uint32_t state;      /* CG_NOACCESS / CG_UNDEFINED / CG_DEFINED */
+  uint32_t reserved;
+} cg_mark;
+
+/* Context configuration.  All device buffers are caller-owned (e.g. torch
+ * tensors) and must stay alive until cg_ctx_destroy.
+ *  - host_base/host_size: the global host window (multiples of 4096).
+ *  - shard_base/shard_size: the part of the window whose shadow this context
+ *    stores (host-address-range sharding across GPUs); 0/0 = the whole window.
+ *    Multiples of 4096, inside the window.
+ *  - v_buf: shard_size bytes; a_buf: shard_size/8 bytes; both 16-byte aligned.
+ *  - workspace: >= cg_workspace_size(cfg) bytes, 256-byte aligned.
+ *  - max_descs: largest n accepted by one check/apply/mark-batch call.
+ *  - max_allocs: allocation-table capacity (live entries plus tombstones).
+ *  - host_staging: nonzero reserves device staging in the workspace for
+ *    cg_check_copies_host (descriptors + verdicts of max_descs). */
+typedef struct {
+  uint64_t host_base, host_size;
+  uint64_t shard_base, shard_size;
+  uint64_t max_descs, max_allocs;
+  uint32_t undef_is_error;  /* S:284 promotes HOST_UNDEFINED to an Error */
+  uint32_t host_staging;
+  int32_t device;           /* CUDA device ordinal                       */
+  int32_t reserved;
+  void *v_buf, *a_buf, *workspace;
+  uint64_t workspace_size;
+} cg_config;
+
+typedef struct cg_ctx cg_ctx;
+
+/* Bytes of device workspace a context with this configuration needs (0 if the
+ * configuration is invalid). */
+uint64_t cg_workspace_size(const cg_config *cfg);
+
+/* Creates a context: validates cfg, carves the workspace, resets the shard's
+ * shadow to the fresh state (A = 0, V = 0xFF) on the device.  Synchronous.
+ * Errors: CG_ERR_INVALID_VALUE (null, misaligned or inconsistent window /
+ * shard / buffers, workspace too small), CG_ERR_CUDA. */
+cg_status cg_ctx_create(const cg_config *cfg, cg_ctx **out);
+
+/* Frees the context (not the caller's buffers).  Does not run the leak sweep:
+ * call cg_leak_report first (SPEC S:317 runs it at destroy; here it is explicit).
+ * Errors: CG_ERR_INVALID_CONTEXT on NULL. */
+cg_status cg_ctx_destroy(cg_ctx *ctx);
+
+/* Message for the last call-level error on ctx ("" if none); owned by ctx. */
+const char *cg_last_error(const cg_ctx *ctx);
+
+/* Host shadow update (SPEC mark_addressable / mark_unaddressable S:45-62;
+ * host_alloc / host_write / host_free S:355-363): every byte of
+ * [addr, addr+len) gets NOACCESS (A=0, V=0xFF), UNDEFINED (A=1, V=0xFF) or
+ * DEFINED (A=1, V=0x00).  Stream-ordered.  Only the part inside this context's
+ * shard is stored.  Errors: CG_ERR_INVALID_VALUE if the range leaves the
+ * window or state is unknown (nothing is changed). */
+cg_status cg_host_mark(cg_ctx *ctx, uint64_t addr, uint64_t len, uint32_t state, void *stream);
+
+/* n marks applied as if by n cg_host_mark calls in order.  h_marks is a host
+ * array, copied before return.  An invalid mark (range leaving the window,
+ * unknown state) is skipped and only it: its status (CG_ERR_INVALID_VALUE) is
+ * written to h_status[i] when h_status is not NULL (CG_OK for applied marks).
+ * Returns CG_OK if every mark was applied, else CG_ERR_INVALID_VALUE (also for
+ * n > max_descs or NULL h_marks, when nothing is applied). */
+cg_status cg_host_mark_batch(cg_ctx *ctx, const cg_mark *h_marks, uint64_t n, uint32_t *h_status,
+                             void *stream);
+
+/* Sets exact V-bytes (partial-bit definedness) of
+ * [addr, addr+len) from the host array h_vbytes (copied before return).
+ * Synchronous on stream.  Errors: CG_ERR_INVALID_VALUE if any byte of the
+ * range is unaddressable or outside the window (defined => addressable);
+ * nothing is changed then. */
+cg_status cg_host_set_vbits(cg_ctx *ctx, uint64_t addr, uint64_t len, const uint8_t *h_vbytes,
+                            void *stream);
+
+/* Registers a device allocation (Fig. 2 caption P:88: "Each allocation
+ * generates a new entry into the list"; SPEC register_linear S:139-147).
+ * seq must exceed the seq of every earlier successful cg_register_alloc /
+ * cg_free.  Errors (no mutation): CG_ERR_INVALID_VALUE for size 0, base 0,
+ * base+size > 2^64-1, overlap with a live allocation, non-increasing
+ * seq; CG_ERR_OUT_OF_MEMORY when the table (live + tombstones) is full. */
+cg_status cg_register_alloc(cg_ctx *ctx, uint64_t base, uint64_t size, uint64_t seq);
+
+/* Frees the live allocation whose base is ptr (SPEC unregister_linear
+ * S:148-156, mem_free S:332-340).  The entry stays in the table as a
+ * tombstone with free_seq = seq so that descriptors with smaller seq still see
+ * it.  Errors (no mutation): CG_ERR_INVALID_VALUE = InvalidFree (ptr is not a
+ * live base: offset pointer, double free, 0) or non-increasing seq. */
+cg_status cg_free(cg_ctx *ctx, uint64_t ptr, uint64_t seq);
+
+/* Drops tombstones with free_seq <= before_seq (no later descriptor may have
+ * seq < before_seq).  Synchronous host operation. */
+cg_status cg_registry_compact(cg_ctx *ctx, uint64_t before_seq);
+
+/* The check for a batch of n descriptors:
+ * validation, batched interval search in the allocation table as of each
+ * desc.seq, host A/V shadow scan, verdicts.
+ * Contract: every registry event with seq < max(desc.seq) has been submitted;
+ * the host shadow is read as of the call (snapshot), so the batch must be
+ * hazard-free (no HtoD may overlap an earlier DtoH of the same batch; see
+ * cg_plan_batches).  d_descs: device array of n cg_copy_desc; d_out: device
+ * array of n cg_verdict (fully overwritten).  Asynchronous on stream.
+ * Errors: CG_ERR_INVALID_VALUE (null, n > max_descs), CG_ERR_CUDA. */
+cg_status cg_check_copies(cg_ctx *ctx, const cg_copy_desc *d_descs, uint64_t n, cg_verdict *d_out,
+                          void *stream);
+
+/* The DtoH shadow update (BASELINE north_star (3)):
+ * for every descriptor with kind == CG_DTOH and verdict status == CG_OK, every
+ * written host byte becomes defined (V := 0x00); other descriptors are ignored
+ * (no mutation on error).  Asynchronous on stream.
+ * Errors: as cg_check_copies. */
+cg_status cg_apply_dtoh(cg_ctx *ctx, const cg_copy_desc *d_descs, const cg_verdict *d_verdicts,
+                        uint64_t n, void *stream);
+
+/* End-to-end entry point with HOST buffers: copies h_descs to the device,
+ * runs cg_check_copies (and cg_apply_dtoh if apply != 0) and copies the
+ * verdicts back to h_out.  Synchronous.  Requires cfg.host_staging.  Errors: as
+ * cg_check_copies; CG_ERR_NOT_INITIALIZED without host staging. */
+cg_status cg_check_copies_host(cg_ctx *ctx, const cg_copy_desc *h_descs, uint64_t n, cg_verdict *h_out,
+                               int apply, void *stream);
+
+/* Leak sweep on the device: writes the live allocations
+ * (ascending base) to d_out (at most cap records) and their total number to
+ * *d_count (a device u64).  Asynchronous on stream. */
+cg_status cg_leak_sweep(cg_ctx *ctx, cg_alloc_record *d_out, uint64_t cap, uint64_t *d_count, void *stream);
+
+/* Synchronous leak report (abstract P:12): runs the device sweep
+ * and copies min(cap, k) records to h_out; *n_out = k.  Errors:
+ * CG_ERR_INVALID_VALUE if n_out is NULL (h_out may be NULL when cap == 0). */
+cg_status cg_leak_report(cg_ctx *ctx, cg_alloc_record *h_out, uint64_t cap, uint64_t *n_out);
+
+/* Epoch planner (host): splits n descriptors (host array, in call order) into
+ * consecutive batches such that no HtoD's host range overlaps the host range
+ * of an earlier DtoH in the same batch (the batch contract above; reading
+ * R-20, conservative on 2D bounding intervals).  Writes the end index of every
+ * batch to h_cuts (at most n entries; the last is n) and their number to
+ * *n_cuts.  Errors: CG_ERR_INVALID_VALUE on NULL. */
+cg_status cg_plan_batches(const cg_copy_desc *h_descs, uint64_t n, uint64_t *h_cuts, uint64_t *n_cuts);
+
+/* Number of kernels this context has launched so far (for bench accounting). */
+uint64_t cg_kernel_launches(const cg_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CG_H_ */

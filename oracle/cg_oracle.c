@@ -225,7 +225,9 @@ void or_check_copy(or_state *st, const or_event *ev, or_verdict *v) {
     uint64_t ds = 0, dspan = 0, ss = 0, sspan = 0;
     int dok = side_range(ev->dst, ev->dst_x, ev->dst_y, ev->dst_pitch, W, H, &ds, &dspan);
     int sok = side_range(ev->src, ev->src_x, ev->src_y, ev->src_pitch, W, H, &ss, &sspan);
-    int nbytes_ok = ((unsigned __int128)W * H <= (unsigned __int128)UINT64_MAX);
+    /* R-10: a copy moving more than 2^38 bytes (256 GiB, more than any B200 or
+     * host window here holds) is an invalid range as well */
+    int nbytes_ok = ((unsigned __int128)W * H <= ((unsigned __int128)1 << 38));
     if (!dok || !sok || !nbytes_ok) v->flags |= F_INVALID_RANGE;
 
     /* (ii) device endpoints, dst then src */

@@ -1,0 +1,282 @@
+"""B200-native batched Cudagrind transfer checker (arXiv 1310.0901).
+
+Thin Python binding over the C-ABI library ``libcgcheck.so`` (include/cg.h).
+Functions keep the C names (``cg_check_copies`` ...) and only marshal
+arguments; every step of the check runs in the library's sm_100a kernels.
+PyTorch provides device memory (the shadow store and workspace are torch
+tensors) and streams.
+
+There is no CPU fallback: importing this package without the built library
+raises.  Build it with ``python -m paper_1310_0901_b200.build`` (or
+``__graft_entry__.build()``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcgcheck.so")
+
+# ---- ABI constants (include/cg.h) -----------------------------------------
+CG_OK, CG_ERR_INVALID_VALUE, CG_ERR_INVALID_CONTEXT, CG_ERR_OUT_OF_MEMORY = 0, 1, 2, 3
+CG_ERR_NOT_INITIALIZED, CG_ERR_CUDA, CG_ERR_NCCL = 4, 5, 6
+CG_HTOD, CG_DTOH, CG_DTOD = 1, 2, 3
+CG_NOACCESS, CG_UNDEFINED, CG_DEFINED = 0, 1, 2
+CG_NONE = (1 << 64) - 1
+CG_F_DST_NOT_ALLOCATED = 1 << 0
+CG_F_DST_TOO_SMALL = 1 << 1
+CG_F_SRC_NOT_ALLOCATED = 1 << 2
+CG_F_SRC_TOO_SMALL = 1 << 3
+CG_F_HOST_UNADDRESSABLE = 1 << 4
+CG_F_HOST_UNDEFINED = 1 << 5
+CG_F_BAD_PITCH = 1 << 6
+CG_F_INVALID_RANGE = 1 << 7
+CG_F_BAD_KIND = 1 << 8
+
+DESC_DTYPE = np.dtype([
+    ("kind", "<u4"), ("reserved", "<u4"), ("seq", "<u8"), ("width", "<u8"), ("height", "<u8"),
+    ("dst", "<u8"), ("dst_x", "<u8"), ("dst_y", "<u8"), ("dst_pitch", "<u8"),
+    ("src", "<u8"), ("src_x", "<u8"), ("src_y", "<u8"), ("src_pitch", "<u8"),
+])
+VERDICT_DTYPE = np.dtype([
+    ("first_unaddr", "<u8"), ("first_undef", "<u8"), ("undef_count", "<u8"),
+    ("dst_expected", "<u8"), ("dst_found", "<u8"), ("src_expected", "<u8"), ("src_found", "<u8"),
+    ("flags", "<u4"), ("status", "<u4"),
+])
+ALLOC_RECORD_DTYPE = np.dtype([("base", "<u8"), ("size", "<u8"), ("alloc_seq", "<u8")])
+MARK_DTYPE = np.dtype([("addr", "<u8"), ("len", "<u8"), ("state", "<u4"), ("reserved", "<u4")])
+assert DESC_DTYPE.itemsize == 96 and VERDICT_DTYPE.itemsize == 64
+assert ALLOC_RECORD_DTYPE.itemsize == 24 and MARK_DTYPE.itemsize == 24
+
+
+class cg_config(ctypes.Structure):
+    _fields_ = [
+        ("host_base", ctypes.c_uint64), ("host_size", ctypes.c_uint64),
+        ("shard_base", ctypes.c_uint64), ("shard_size", ctypes.c_uint64),
+        ("max_descs", ctypes.c_uint64), ("max_allocs", ctypes.c_uint64),
+        ("undef_is_error", ctypes.c_uint32), ("host_staging", ctypes.c_uint32),
+        ("device", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("v_buf", ctypes.c_void_p), ("a_buf", ctypes.c_void_p), ("workspace", ctypes.c_void_p),
+        ("workspace_size", ctypes.c_uint64),
+    ]
+
+
+class CgError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"cg status {status}: {msg}")
+        self.status = status
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1310_0901_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, U64, U32, I = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int
+    sig = {
+        "cg_workspace_size": (U64, [P]),
+        "cg_ctx_create": (I, [P, P]),
+        "cg_ctx_destroy": (I, [P]),
+        "cg_last_error": (ctypes.c_char_p, [P]),
+        "cg_host_mark": (I, [P, U64, U64, U32, P]),
+        "cg_host_mark_batch": (I, [P, P, U64, P, P]),
+        "cg_host_set_vbits": (I, [P, U64, U64, P, P]),
+        "cg_register_alloc": (I, [P, U64, U64, U64]),
+        "cg_free": (I, [P, U64, U64]),
+        "cg_registry_compact": (I, [P, U64]),
+        "cg_check_copies": (I, [P, P, U64, P, P]),
+        "cg_apply_dtoh": (I, [P, P, P, U64, P]),
+        "cg_check_copies_host": (I, [P, P, U64, P, I, P]),
+        "cg_leak_sweep": (I, [P, P, U64, P, P]),
+        "cg_leak_report": (I, [P, P, U64, P]),
+        "cg_plan_batches": (I, [P, U64, P, P]),
+        "cg_kernel_launches": (U64, [P]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+_lib = _load()
+EXPORTED = ("cg_workspace_size", "cg_ctx_create", "cg_ctx_destroy", "cg_last_error", "cg_host_mark",
+            "cg_host_mark_batch", "cg_host_set_vbits", "cg_register_alloc", "cg_free", "cg_registry_compact",
+            "cg_check_copies", "cg_apply_dtoh", "cg_check_copies_host", "cg_leak_sweep", "cg_leak_report",
+            "cg_plan_batches", "cg_kernel_launches")
+
+# ---- same-name thin wrappers (status codes returned unchanged) -------------
+cg_workspace_size = _lib.cg_workspace_size
+cg_ctx_create = _lib.cg_ctx_create
+cg_ctx_destroy = _lib.cg_ctx_destroy
+cg_last_error = _lib.cg_last_error
+cg_host_mark = _lib.cg_host_mark
+cg_host_mark_batch = _lib.cg_host_mark_batch
+cg_host_set_vbits = _lib.cg_host_set_vbits
+cg_register_alloc = _lib.cg_register_alloc
+cg_free = _lib.cg_free
+cg_registry_compact = _lib.cg_registry_compact
+cg_check_copies = _lib.cg_check_copies
+cg_apply_dtoh = _lib.cg_apply_dtoh
+cg_check_copies_host = _lib.cg_check_copies_host
+cg_leak_sweep = _lib.cg_leak_sweep
+cg_leak_report = _lib.cg_leak_report
+cg_plan_batches = _lib.cg_plan_batches
+cg_kernel_launches = _lib.cg_kernel_launches
+
+
+def plan_batches(descs: np.ndarray) -> np.ndarray:
+    """Batch end indices (cg_plan_batches) for a host DESC_DTYPE array."""
+    d = np.ascontiguousarray(descs, dtype=DESC_DTYPE)
+    cuts = np.zeros(max(len(d), 1), np.uint64)
+    nc = ctypes.c_uint64(0)
+    st = _lib.cg_plan_batches(d.ctypes.data if len(d) else None, len(d), cuts.ctypes.data, ctypes.byref(nc))
+    if st:
+        raise CgError(st, "cg_plan_batches")
+    return cuts[: nc.value]
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+class Checker:
+    """One context (one GPU, one shard of the host window).
+
+    Device memory -- the V/A shadow store and the workspace -- are torch
+    tensors owned by this object; the library only borrows them.
+    """
+
+    def __init__(self, host_base: int, host_size: int, *, max_descs: int = 1 << 20,
+                 max_allocs: int = 1 << 18, undef_is_error: bool = False, device: int = 0,
+                 shard_base: int = 0, shard_size: int = 0, host_staging: bool = False):
+        import torch
+        self.torch = torch
+        self.device = device
+        dev = torch.device("cuda", device)
+        ss = shard_size or host_size
+        self.cfg = cg_config(host_base=host_base, host_size=host_size, shard_base=shard_base,
+                             shard_size=shard_size, max_descs=max_descs, max_allocs=max_allocs,
+                             undef_is_error=int(undef_is_error), host_staging=int(host_staging),
+                             device=device)
+        ws = _lib.cg_workspace_size(ctypes.byref(self.cfg))
+        if ws == 0:
+            raise CgError(CG_ERR_INVALID_VALUE, "invalid configuration")
+        self.V = torch.empty(ss, dtype=torch.uint8, device=dev)
+        self.A = torch.empty(ss // 8, dtype=torch.uint8, device=dev)
+        self.workspace = torch.empty(ws, dtype=torch.uint8, device=dev)
+        self.cfg.v_buf = self.V.data_ptr()
+        self.cfg.a_buf = self.A.data_ptr()
+        self.cfg.workspace = self.workspace.data_ptr()
+        self.cfg.workspace_size = ws
+        ctx = ctypes.c_void_p()
+        st = _lib.cg_ctx_create(ctypes.byref(self.cfg), ctypes.byref(ctx))
+        if st:
+            raise CgError(st, "cg_ctx_create failed")
+        self.ctx = ctx
+        self.max_descs = max_descs
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            _lib.cg_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _ok(self, st: int, what: str):
+        if st:
+            raise CgError(st, f"{what}: {_lib.cg_last_error(self.ctx).decode()}")
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(_lib.cg_kernel_launches(self.ctx))
+
+    # ---- host shadow plumbing ---------------------------------------------
+    def host_mark(self, addr: int, length: int, state: int, stream=None) -> int:
+        return _lib.cg_host_mark(self.ctx, addr, length, state, _stream_ptr(stream))
+
+    def host_mark_batch(self, marks: np.ndarray, status_out: Optional[np.ndarray] = None, stream=None) -> int:
+        m = np.ascontiguousarray(marks, dtype=MARK_DTYPE)
+        if status_out is not None:
+            assert status_out.dtype == np.uint32 and status_out.flags.c_contiguous and len(status_out) >= len(m)
+        return _lib.cg_host_mark_batch(self.ctx, m.ctypes.data if len(m) else None, len(m),
+                                       status_out.ctypes.data if status_out is not None else None,
+                                       _stream_ptr(stream))
+
+    def host_set_vbits(self, addr: int, vbytes: bytes, stream=None) -> int:
+        b = np.ascontiguousarray(np.frombuffer(bytes(vbytes), np.uint8))
+        return _lib.cg_host_set_vbits(self.ctx, addr, len(b), b.ctypes.data if len(b) else None,
+                                      _stream_ptr(stream))
+
+    # ---- registry ------------------------------------------------------------
+    def register_alloc(self, base: int, size: int, seq: int) -> int:
+        return _lib.cg_register_alloc(self.ctx, base, size, seq)
+
+    def free(self, ptr: int, seq: int) -> int:
+        return _lib.cg_free(self.ctx, ptr, seq)
+
+    # ---- the hot path --------------------------------------------------------
+    def check_copies(self, d_descs, d_out=None, stream=None):
+        """d_descs: a CUDA uint8 tensor holding n DESC_DTYPE records."""
+        torch = self.torch
+        n = d_descs.numel() // DESC_DTYPE.itemsize
+        if d_out is None:
+            d_out = torch.empty(n * VERDICT_DTYPE.itemsize, dtype=torch.uint8, device=d_descs.device)
+        self._ok(_lib.cg_check_copies(self.ctx, d_descs.data_ptr(), n, d_out.data_ptr(), _stream_ptr(stream)),
+                 "cg_check_copies")
+        return d_out
+
+    def apply_dtoh(self, d_descs, d_verdicts, stream=None):
+        n = d_descs.numel() // DESC_DTYPE.itemsize
+        self._ok(_lib.cg_apply_dtoh(self.ctx, d_descs.data_ptr(), d_verdicts.data_ptr(), n, _stream_ptr(stream)),
+                 "cg_apply_dtoh")
+
+    def check_copies_host(self, descs: np.ndarray, out: Optional[np.ndarray] = None, apply: bool = True,
+                          stream=None) -> np.ndarray:
+        d = np.ascontiguousarray(descs, dtype=DESC_DTYPE)
+        if out is None:
+            out = np.empty(len(d), VERDICT_DTYPE)
+        self._ok(_lib.cg_check_copies_host(self.ctx, d.ctypes.data, len(d), out.ctypes.data, int(apply),
+                                           _stream_ptr(stream)), "cg_check_copies_host")
+        return out
+
+    def leak_sweep(self, d_out, cap: int, d_count, stream=None):
+        self._ok(_lib.cg_leak_sweep(self.ctx, d_out.data_ptr(), cap, d_count.data_ptr(), _stream_ptr(stream)),
+                 "cg_leak_sweep")
+
+    def leak_report(self) -> np.ndarray:
+        n = ctypes.c_uint64(0)
+        self._ok(_lib.cg_leak_report(self.ctx, None, 0, ctypes.byref(n)), "cg_leak_report")
+        out = np.zeros(n.value, ALLOC_RECORD_DTYPE)
+        if n.value:
+            self._ok(_lib.cg_leak_report(self.ctx, out.ctypes.data, n.value, ctypes.byref(n)), "cg_leak_report")
+        return out
+
+    # ---- state download (tests) ---------------------------------------------
+    def shadow(self):
+        self.torch.cuda.synchronize(self.device)
+        return self.A.cpu().numpy(), self.V.cpu().numpy()
+
+
+def to_device_descs(descs: np.ndarray, device: int = 0):
+    import torch
+    d = np.ascontiguousarray(descs, dtype=DESC_DTYPE)
+    return torch.from_numpy(d.view(np.uint8).copy()).to(torch.device("cuda", device))
+
+
+def verdicts_to_numpy(d_verdicts) -> np.ndarray:
+    return d_verdicts.cpu().numpy().view(VERDICT_DTYPE)
+
+
+from .replay import replay_events  # noqa: E402,F401

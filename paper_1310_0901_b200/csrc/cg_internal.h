@@ -1,0 +1,73 @@
+// Internal interface between the C-ABI runtime (cg_runtime.cu) and the
+// sm_100a kernels (cg_kernels.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "cg.h"
+
+namespace cgk {
+
+constexpr uint64_t kNone = UINT64_MAX;
+constexpr uint64_t kInf = UINT64_MAX;          // free_seq of a live allocation
+constexpr uint64_t kMaxCopyBytes = 1ull << 38;  // R-10: larger copies are INVALID_RANGE
+constexpr uint64_t kMaxDescs = 1ull << 24;      // per call (keeps sum of weights < 2^63)
+
+// Host window [wb, we) and the shard [sb, se) whose shadow this GPU stores.
+struct ShadowView {
+  uint64_t wb, we, sb, se;
+  uint8_t* V;   // se - sb bytes
+  uint8_t* A;   // (se - sb) / 8 bytes
+};
+
+// Allocation table: structure of arrays sorted by (base, alloc_seq), with the
+// running maximum of end addresses.
+struct Table {
+  const uint64_t* base;
+  const uint64_t* end;
+  const uint64_t* aseq;
+  const uint64_t* fseq;
+  const uint64_t* pmax;
+  uint64_t n;
+  uint32_t stride;   // splitter stride (every stride-th base is staged in smem)
+  uint32_t nsplit;
+};
+
+// A planned pass over n weighted items: P = exclusive prefix sum of weights
+// (P[n] = total), cut into chunks of T >= t_min weight units (T grows so that
+// the number of chunks never exceeds max_chunks); chunk_first[c] = the item
+// whose weight interval contains c*T.
+struct Plan {
+  uint64_t* weight;       // [n]
+  uint64_t* P;            // [n + 1]
+  uint64_t* bsum;         // [nblocks + 1]
+  uint32_t* chunk_first;  // [max_chunks]
+  uint64_t max_chunks;
+  uint64_t t_min;
+};
+
+struct Launch {
+  int num_sms;
+  int persist_blocks;     // persistent grid for the chunked kernels
+  uint64_t* counter;      // host counter of kernel launches
+};
+
+constexpr int kScanTile = 2048;   // items per block of the prefix scan
+
+uint64_t scan_blocks(uint64_t n);
+
+cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out,
+                         const Table& t, const ShadowView& sv, const Plan& p, uint32_t err_mask,
+                         cudaStream_t s);
+cudaError_t apply_dtoh(const Launch& L, const cg_copy_desc* d, const cg_verdict* v, uint64_t n,
+                       const ShadowView& sv, const Plan& p, cudaStream_t s);
+cudaError_t mark_batch(const Launch& L, const cg_mark* d_marks, uint64_t n, const ShadowView& sv,
+                       const Plan& p, cudaStream_t s);
+cudaError_t fresh_shadow(const Launch& L, const ShadowView& sv, cudaStream_t s);
+cudaError_t setv_check(const Launch& L, uint64_t addr, uint64_t len, const ShadowView& sv,
+                       uint32_t* d_flag, cudaStream_t s);
+cudaError_t leak_sweep(const Launch& L, const Table& t, const Plan& p, cg_alloc_record* out,
+                       uint64_t cap, uint64_t* d_count, cudaStream_t s);
+
+}  // namespace cgk

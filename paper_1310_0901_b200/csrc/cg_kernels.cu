@@ -1,0 +1,850 @@
+// sm_100a kernels of the batched Cudagrind transfer checker.
+//
+// Hot path of one check + apply:
+//   a1+a3  k_check_prep     one thread per descriptor: CUDA_MEMCPY2D start /
+//                           span / pitch / overflow validation, then a batched
+//                           interval search of every device endpoint in the
+//                           lifetime-stamped, base-sorted allocation table
+//                           (splitters staged in shared memory; PAPER.md P:77,
+//                           P:80).  Writes
+//                           the device half of the verdict and the item weight.
+//   a2     k_scan_* + k_plan   exclusive prefix sum of weights and the chunk ->
+//                           first item map: equal-weight chunks, so a 64-byte
+//                           copy and an 8 GiB copy are load-balanced alike.
+//   a4     k_check_scan     persistent grid; a warp per chunk; 128-bit
+//                           coalesced non-allocating loads of V (16 B/lane) and
+//                           A (2 B/lane), a warp-uniform clean test and, only
+//                           for dirty 16-byte groups, per-byte masks with
+//                           __ffs (first violation) and __popc (count); warp
+//                           shuffles reduce min/min/sum ("bitwise
+//                           precision").
+//   a5     inline in k_check_scan for descriptors that fit one chunk,
+//          k_finalize_split for the ones split across chunks (u64 atomics only
+//          for non-identity partials): flags + status.
+//   a6     k_apply_prep + plan + k_apply   V := 0 over DtoH ranges with
+//                           status OK (BASELINE north_star (3)).
+//   a8     k_live + scan + k_leak_scatter (abstract P:12).
+// Plumbing (setup, untimed): k_fill (fresh shadow), k_mark (S:45-62,
+// S:355-363), k_setv_check.
+//
+// Layout: V is one byte per host byte, A one bit per host byte (LSB first),
+// both indexed by (x - shard_base); H0 % 4096 == 0 so a 16-byte V group maps to
+// one aligned 16-bit A half-word and a 128-byte V range to one 16-byte A vector.
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "cg_internal.h"
+
+namespace cgk {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kUnroll = 4;
+
+// ---------------------------------------------------------------------------
+// small device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint32_t ldg_u16(const uint16_t* p) {
+  unsigned short r;
+  asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void stg_zero16(uint4* p) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%1,%1,%1};" ::"l"(p), "r"(0u));
+}
+__device__ __forceinline__ void stg_val16(uint4* p, uint32_t v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%1,%1,%1};" ::"l"(p), "r"(v));
+}
+
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
+
+// one bit per byte of w: bit j set iff byte j of w is nonzero
+__device__ __forceinline__ uint32_t nz4(uint32_t w) {
+  uint32_t t = (((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w) & 0x80808080u;
+  return ((t >> 7) * 0x01020408u) >> 24;
+}
+__device__ __forceinline__ uint32_t nz16(uint4 v) {
+  return nz4(v.x) | (nz4(v.y) << 4) | (nz4(v.z) << 8) | (nz4(v.w) << 12);
+}
+
+// mask of the bits [lo, hi) of a `width`-bit group starting at gb, with lo/hi
+// absolute positions; lo <= gb + width, hi >= gb (caller guarantees overlap)
+__device__ __forceinline__ uint32_t range_mask(uint64_t gb, int width, uint64_t lo, uint64_t hi) {
+  uint32_t full = (width == 32) ? 0xffffffffu : ((1u << width) - 1u);
+  uint32_t m = full;
+  if (gb < lo) {
+    uint64_t sh = lo - gb;
+    m = sh >= (uint64_t)width ? 0u : (m << sh) & full;
+  }
+  if (gb + width > hi) {
+    uint64_t sh = gb + width - hi;
+    m = sh >= (uint64_t)width ? 0u : m & (full >> sh);
+  }
+  return m;
+}
+
+__device__ __forceinline__ uint64_t warp_min(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = umin64(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_sum(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// a1: descriptor normalisation (CUDA_MEMCPY2D start-address rule, pitch rule,
+// 64-bit overflow) -- DESIGN.md readings R-10, R-11, R-12, R-16
+// ---------------------------------------------------------------------------
+// start = base + y*pitch + x; span = (w==0||h==0) ? 0 : (h-1)*pitch + w;
+// valid iff start + span <= 2^64 - 1 (every partial sum is then exact).
+__device__ __forceinline__ bool fold_side(uint64_t base, uint64_t x, uint64_t y, uint64_t pitch,
+                                          uint64_t w, uint64_t h, uint64_t& start, uint64_t& span) {
+  if (__umul64hi(y, pitch) != 0) return false;
+  uint64_t s = y * pitch;
+  uint64_t t = s + x;
+  if (t < s) return false;
+  uint64_t st = t + base;
+  if (st < t) return false;
+  uint64_t sp = 0;
+  if (w != 0 && h != 0) {
+    if (__umul64hi(h - 1, pitch) != 0) return false;
+    uint64_t q = (h - 1) * pitch;
+    sp = q + w;
+    if (sp < q) return false;
+  }
+  uint64_t e = st + sp;
+  if (e < st) return false;
+  start = st;
+  span = sp;
+  return true;
+}
+
+struct Norm {
+  uint32_t kind, flags;
+  bool dok, sok;
+  uint64_t ds, dspan, ss, sspan;
+  bool host;           // has a host side that is scanned
+  uint64_t hstart, hpitch, W, nbytes;
+};
+
+__device__ __forceinline__ Norm normalize(const cg_copy_desc& d) {
+  Norm n;
+  n.kind = d.kind;
+  n.flags = 0;
+  n.dok = n.sok = false;
+  n.ds = n.dspan = n.ss = n.sspan = 0;
+  n.host = false;
+  n.hstart = n.hpitch = n.nbytes = 0;
+  n.W = d.width;
+  if (d.kind < CG_HTOD || d.kind > CG_DTOD) {
+    n.flags = CG_F_BAD_KIND;
+    return n;
+  }
+  const uint64_t W = d.width, H = d.height;
+  // pitch rule: pitch >= WidthInBytes + XInBytes (evaluated without overflow)
+  if (W + d.dst_x < W || d.dst_pitch < W + d.dst_x) n.flags |= CG_F_BAD_PITCH;
+  if (W + d.src_x < W || d.src_pitch < W + d.src_x) n.flags |= CG_F_BAD_PITCH;
+  n.dok = fold_side(d.dst, d.dst_x, d.dst_y, d.dst_pitch, W, H, n.ds, n.dspan);
+  n.sok = fold_side(d.src, d.src_x, d.src_y, d.src_pitch, W, H, n.ss, n.sspan);
+  const bool bytes_ok = __umul64hi(W, H) == 0 && W * H <= kMaxCopyBytes;
+  if (!n.dok || !n.sok || !bytes_ok) n.flags |= CG_F_INVALID_RANGE;
+  if (d.kind == CG_HTOD && n.sok && bytes_ok) {
+    n.host = true;
+    n.hstart = n.ss;
+    n.hpitch = d.src_pitch;
+    n.nbytes = W * H;
+  } else if (d.kind == CG_DTOH && n.dok && bytes_ok) {
+    n.host = true;
+    n.hstart = n.ds;
+    n.hpitch = d.dst_pitch;
+    n.nbytes = W * H;
+  }
+  return n;
+}
+
+// ---------------------------------------------------------------------------
+// a3: batched interval search (lifetime-stamped, base-sorted table)
+// ---------------------------------------------------------------------------
+// Returns true and the containing allocation's end if some entry e has
+// base_e <= start < end_e and aseq_e < seq < fseq_e.  At most one entry can
+// match (live allocations never overlap).  Probe i = last base <= start
+// (smem splitters, then a short global binary search), then walk left while
+// the prefix max of ends exceeds start (one step without address reuse).
+__device__ __forceinline__ bool table_lookup(const Table& t, const uint64_t* s_split, uint64_t start,
+                                             uint64_t seq, uint64_t& end_out) {
+  if (t.nsplit == 0 || s_split[0] > start) return false;
+  uint32_t lo = 0, hi = t.nsplit;
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (s_split[mid] <= start) lo = mid; else hi = mid;
+  }
+  uint64_t a = (uint64_t)lo * t.stride;
+  uint64_t b = umin64(a + t.stride, t.n);
+  while (b - a > 1) {
+    uint64_t mid = (a + b) >> 1;
+    if (__ldg(t.base + mid) <= start) a = mid; else b = mid;
+  }
+  for (int64_t j = (int64_t)a; j >= 0; --j) {
+    if (__ldg(t.pmax + j) <= start) break;
+    const uint64_t e = __ldg(t.end + j);
+    if (e > start && __ldg(t.aseq + j) < seq && seq < __ldg(t.fseq + j)) {
+      end_out = e;
+      return true;
+    }
+  }
+  return false;
+}
+
+__device__ __forceinline__ void load_splitters(const Table& t, uint64_t* s_split) {
+  for (uint32_t k = threadIdx.x; k < t.nsplit; k += blockDim.x)
+    s_split[k] = t.base[(uint64_t)k * t.stride];
+  __syncthreads();
+}
+
+// Check weights (units): HtoD 1 per host byte (V-byte + 1/8 A-byte), DtoH 1 per
+// 8 host bytes (A only), plus kItemCost per descriptor (its fixed work).
+constexpr uint64_t kItemCost = 256;
+
+__device__ __forceinline__ uint64_t check_host_units(const Norm& nm) {
+  if (!nm.host) return 0;
+  return nm.kind == CG_HTOD ? nm.nbytes : (nm.nbytes + 7) >> 3;
+}
+
+__global__ void __launch_bounds__(kThreads) k_check_prep(const cg_copy_desc* __restrict__ descs,
+                                                         uint64_t n, Table t, cg_verdict* __restrict__ out,
+                                                         uint64_t* __restrict__ weight) {
+  extern __shared__ uint64_t s_split[];
+  load_splitters(t, s_split);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const cg_copy_desc d = descs[i];
+    const Norm nm = normalize(d);
+    uint32_t flags = nm.flags;
+    uint64_t de = 0, df = 0, se = 0, sf = 0;
+    if (!(flags & CG_F_BAD_KIND)) {
+      uint64_t end;
+      if ((nm.kind == CG_HTOD || nm.kind == CG_DTOD) && nm.dok) {      // dst side first
+        if (!table_lookup(t, s_split, nm.ds, d.seq, end)) {
+          flags |= CG_F_DST_NOT_ALLOCATED;
+        } else if (end - nm.ds < nm.dspan) {
+          flags |= CG_F_DST_TOO_SMALL;
+          de = nm.dspan;
+          df = end - nm.ds;
+        }
+      }
+      if ((nm.kind == CG_DTOH || nm.kind == CG_DTOD) && nm.sok) {
+        if (!table_lookup(t, s_split, nm.ss, d.seq, end)) {
+          flags |= CG_F_SRC_NOT_ALLOCATED;
+        } else if (end - nm.ss < nm.sspan) {
+          flags |= CG_F_SRC_TOO_SMALL;
+          se = nm.sspan;
+          sf = end - nm.ss;
+        }
+      }
+    }
+    cg_verdict v;
+    v.first_unaddr = kNone;
+    v.first_undef = kNone;
+    v.undef_count = 0;
+    v.dst_expected = de;
+    v.dst_found = df;
+    v.src_expected = se;
+    v.src_found = sf;
+    v.flags = flags;
+    v.status = 0;
+    out[i] = v;
+    weight[i] = kItemCost + check_host_units(nm);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a2: exclusive prefix sum (3 kernels) and the chunk plan
+// ---------------------------------------------------------------------------
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = kScanTile / kScanThreads;   // 8
+
+__device__ __forceinline__ uint64_t block_exclusive_scan(uint64_t x, uint64_t* s_warp, uint64_t& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint64_t inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint64_t y = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_warp[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    uint64_t w = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
+    uint64_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint64_t y = __shfl_up_sync(kFull, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < (int)(blockDim.x >> 5)) s_warp[lane] = wi - w;
+    if (lane == 31) s_warp[32] = wi;
+  }
+  __syncthreads();
+  total = s_warp[32];
+  uint64_t r = inc - x + s_warp[wid];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint64_t* __restrict__ in, uint64_t n,
+                                                              uint64_t* __restrict__ bsum) {
+  __shared__ uint64_t s_warp[33];
+  const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+  uint64_t acc = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    uint64_t i = base + (uint64_t)j * kScanThreads + threadIdx.x;
+    if (i < n) acc += in[i];
+  }
+  uint64_t total;
+  block_exclusive_scan(acc, s_warp, total);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = total;
+}
+
+// single block: exclusive scan of bsum[0..nb) in place, bsum[nb] = total
+__global__ void __launch_bounds__(1024) k_scan_top(uint64_t* __restrict__ bsum, uint64_t nb) {
+  __shared__ uint64_t s_warp[33];
+  uint64_t carry = 0;
+  for (uint64_t base = 0; base < nb; base += blockDim.x) {
+    uint64_t i = base + threadIdx.x;
+    uint64_t x = i < nb ? bsum[i] : 0;
+    uint64_t total;
+    uint64_t ex = block_exclusive_scan(x, s_warp, total);
+    if (i < nb) bsum[i] = carry + ex;
+    carry += total;
+  }
+  if (threadIdx.x == 0) bsum[nb] = carry;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint64_t* __restrict__ in, uint64_t n,
+                                                            const uint64_t* __restrict__ bsum,
+                                                            uint64_t* __restrict__ out, uint64_t nb) {
+  __shared__ uint64_t s_items[kScanTile];
+  __shared__ uint64_t s_warp[33];
+  const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    uint64_t i = base + (uint64_t)j * kScanThreads + threadIdx.x;
+    s_items[j * kScanThreads + threadIdx.x] = i < n ? in[i] : 0;
+  }
+  __syncthreads();
+  uint64_t loc[kScanItems];
+  uint64_t acc = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    loc[j] = acc;
+    acc += s_items[threadIdx.x * kScanItems + j];
+  }
+  uint64_t total;
+  uint64_t ex = block_exclusive_scan(acc, s_warp, total) + bsum[blockIdx.x];
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) s_items[threadIdx.x * kScanItems + j] = ex + loc[j];
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    uint64_t i = base + (uint64_t)j * kScanThreads + threadIdx.x;
+    if (i < n) out[i] = s_items[j * kScanThreads + threadIdx.x];
+  }
+  if (blockIdx.x == nb - 1 && threadIdx.x == 0) out[n] = bsum[nb];
+}
+
+struct ChunkGeom {
+  uint64_t total, T, nchunks;
+};
+
+__device__ __forceinline__ ChunkGeom chunk_geom(const uint64_t* P, uint64_t n, uint64_t t_min,
+                                                uint64_t max_chunks) {
+  ChunkGeom g;
+  g.total = P[n];
+  uint64_t T = (g.total + max_chunks - 1) / max_chunks;
+  g.T = umax64(T, t_min);
+  g.nchunks = (g.total + g.T - 1) / g.T;
+  return g;
+}
+
+// chunk_first[c] = the item whose weight interval [P[d], P[d+1]) contains c*T
+__global__ void __launch_bounds__(kThreads) k_plan(const uint64_t* __restrict__ P, uint64_t n, uint64_t t_min,
+                                                   uint64_t max_chunks, uint32_t* __restrict__ chunk_first) {
+  const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
+  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < g.nchunks;
+       c += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t target = c * g.T;
+    uint64_t lo = 0, hi = n;   // P[lo] <= target < P[hi]
+    while (hi - lo > 1) {
+      uint64_t mid = (lo + hi) >> 1;
+      if (__ldg(P + mid) <= target) lo = mid; else hi = mid;
+    }
+    chunk_first[c] = (uint32_t)lo;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a4: the host shadow scan
+// ---------------------------------------------------------------------------
+struct Partial {
+  uint64_t fu, fd, cnt;   // first unaddressable, first undefined, undefined count
+};
+
+// HtoD: V and A over shard-relative bytes [q0, q1); logical offset of q0 is ob.
+__device__ __forceinline__ void scan_vbits(const ShadowView& sv, uint64_t q0, uint64_t q1, uint64_t ob,
+                                           Partial& p) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t k0 = q0 >> 4, k1 = (q1 + 15) >> 4;
+  const uint4* V4 = reinterpret_cast<const uint4*>(sv.V);
+  const uint16_t* A2 = reinterpret_cast<const uint16_t*>(sv.A);
+  for (uint64_t kb = k0; kb < k1; kb += 32 * kUnroll) {
+    uint4 v[kUnroll];
+    uint32_t a[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint64_t k = kb + (uint64_t)u * 32 + lane;
+      if (k < k1) {
+        v[u] = ldg_stream(V4 + k);
+        a[u] = ldg_u16(A2 + k);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint64_t k = kb + (uint64_t)u * 32 + lane;
+      if (k < k1) {
+        const uint64_t qb = k << 4;
+        const bool whole = qb >= q0 && qb + 16 <= q1;
+        if (!whole || (v[u].x | v[u].y | v[u].z | v[u].w) != 0 || a[u] != 0xFFFFu) {
+          const uint32_t m = range_mask(qb, 16, q0, q1);
+          const uint32_t bad = ~a[u] & m;
+          const uint32_t und = nz16(v[u]) & a[u] & m;
+          if (bad) p.fu = umin64(p.fu, ob + (qb + (__ffs(bad) - 1) - q0));
+          if (und) {
+            p.fd = umin64(p.fd, ob + (qb + (__ffs(und) - 1) - q0));
+            p.cnt += __popc(und);
+          }
+        }
+      }
+    }
+  }
+}
+
+// DtoH: A only, 128 host bytes (one 16-byte A vector) per lane and step.
+__device__ __forceinline__ void scan_abits(const ShadowView& sv, uint64_t q0, uint64_t q1, uint64_t ob,
+                                           Partial& p) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t k0 = q0 >> 7, k1 = (q1 + 127) >> 7;
+  const uint4* A16 = reinterpret_cast<const uint4*>(sv.A);
+  for (uint64_t kb = k0; kb < k1; kb += 32 * kUnroll) {
+    uint4 a[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint64_t k = kb + (uint64_t)u * 32 + lane;
+      if (k < k1) a[u] = ldg_stream(A16 + k);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint64_t k = kb + (uint64_t)u * 32 + lane;
+      if (k < k1) {
+        const uint64_t qb = k << 7;
+        const bool whole = qb >= q0 && qb + 128 <= q1;
+        if (!whole || (a[u].x & a[u].y & a[u].z & a[u].w) != 0xffffffffu) {
+          const uint32_t w[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint64_t gb = qb + 32 * j;
+            if (gb + 32 <= q0 || gb >= q1) continue;
+            const uint32_t bad = ~w[j] & range_mask(gb, 32, q0, q1);
+            if (bad) {
+              p.fu = umin64(p.fu, ob + (gb + (__ffs(bad) - 1) - q0));
+              break;
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+// One contiguous physical segment [x, x+len) whose first byte has logical
+// offset o.  Bytes outside the global window are unaddressable (R-15); only the
+// shard's bytes are read.
+__device__ __forceinline__ void scan_segment(const ShadowView& sv, bool htod, uint64_t x, uint64_t len,
+                                             uint64_t o, Partial& p) {
+  const uint64_t end = x + len;
+  if (x < sv.wb) p.fu = umin64(p.fu, o);
+  if (end > sv.we) p.fu = umin64(p.fu, o + (umax64(x, sv.we) - x));
+  const uint64_t y0 = umax64(x, sv.sb), y1 = umin64(end, sv.se);
+  if (y0 < y1) {
+    if (htod) scan_vbits(sv, y0 - sv.sb, y1 - sv.sb, o + (y0 - x), p);
+    else scan_abits(sv, y0 - sv.sb, y1 - sv.sb, o + (y0 - x), p);
+  }
+}
+
+// Logical host bytes [lo, hi) of a descriptor, row by row (R-11).
+template <typename SegFn>
+__device__ __forceinline__ void for_rows(const Norm& nm, uint64_t lo, uint64_t hi, SegFn fn) {
+  const uint64_t W = nm.W;
+  uint64_t r = lo / W;
+  uint64_t c = lo - r * W;
+  uint64_t o = lo;
+  while (o < hi) {
+    const uint64_t seg = umin64(W - c, hi - o);
+    fn(nm.hstart + r * nm.hpitch + c, seg, o);
+    o += seg;
+    ++r;
+    c = 0;
+  }
+}
+
+__device__ __forceinline__ void finalize_fields(uint32_t& flags, uint32_t& status, uint64_t fu, uint64_t cnt,
+                                                uint32_t err_mask) {
+  if (fu != kNone) flags |= CG_F_HOST_UNADDRESSABLE;
+  if (cnt != 0 && fu == kNone) flags |= CG_F_HOST_UNDEFINED;
+  status = (flags & err_mask) ? (uint32_t)CG_ERR_INVALID_VALUE : (uint32_t)CG_OK;
+}
+
+__global__ void __launch_bounds__(kThreads) k_check_scan(const cg_copy_desc* __restrict__ descs, uint64_t n,
+                                                         const uint64_t* __restrict__ P,
+                                                         const uint32_t* __restrict__ chunk_first,
+                                                         uint64_t t_min, uint64_t max_chunks, ShadowView sv,
+                                                         cg_verdict* __restrict__ out, uint32_t err_mask) {
+  const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t c = gw; c < g.nchunks; c += nw) {
+    const uint64_t w0 = c * g.T, w1 = umin64(w0 + g.T, g.total);
+    for (uint64_t d = chunk_first[c]; d < n; ++d) {
+      const uint64_t pd = P[d];
+      if (pd >= w1) break;
+      const uint64_t pd1 = P[d + 1];
+      const cg_copy_desc dd = descs[d];
+      const Norm nm = normalize(dd);
+      Partial p{kNone, kNone, 0};
+      if (nm.host && nm.nbytes) {
+        // this chunk's share of the descriptor's weight interval, minus the
+        // kItemCost prefix, mapped to logical host bytes
+        uint64_t a = umax64(w0, pd) - pd, b = umin64(w1, pd1) - pd;
+        a = a > kItemCost ? a - kItemCost : 0;
+        b = b > kItemCost ? b - kItemCost : 0;
+        uint64_t lo = a, hi = b;
+        if (nm.kind == CG_DTOH) {
+          lo = a << 3;
+          hi = umin64(b << 3, nm.nbytes);
+        }
+        const bool htod = nm.kind == CG_HTOD;
+        if (lo < hi)
+          for_rows(nm, lo, hi, [&](uint64_t x, uint64_t len, uint64_t o) { scan_segment(sv, htod, x, len, o, p); });
+      }
+      if (__any_sync(kFull, p.fu != kNone || p.fd != kNone || p.cnt != 0)) {
+        p.fu = warp_min(p.fu);
+        p.fd = warp_min(p.fd);
+        p.cnt = warp_sum(p.cnt);
+      }
+      if (lane == 0) {
+        cg_verdict* v = out + d;
+        if (pd >= w0 && pd1 <= w1) {          // the whole descriptor is in this chunk
+          uint32_t flags = v->flags, status;
+          finalize_fields(flags, status, p.fu, p.cnt, err_mask);
+          v->first_unaddr = p.fu;
+          v->first_undef = p.fd;
+          v->undef_count = p.cnt;
+          v->flags = flags;
+          v->status = status;
+        } else {                              // split: merge, finalize later
+          if (p.fu != kNone) atomicMin(reinterpret_cast<unsigned long long*>(&v->first_unaddr), p.fu);
+          if (p.fd != kNone) atomicMin(reinterpret_cast<unsigned long long*>(&v->first_undef), p.fd);
+          if (p.cnt) atomicAdd(reinterpret_cast<unsigned long long*>(&v->undef_count), p.cnt);
+        }
+      }
+    }
+  }
+}
+
+// a5 for descriptors split across chunks
+__global__ void __launch_bounds__(kThreads) k_finalize_split(uint64_t n, const uint64_t* __restrict__ P,
+                                                             uint64_t t_min, uint64_t max_chunks,
+                                                             cg_verdict* __restrict__ out, uint32_t err_mask) {
+  const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
+  for (uint64_t d = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; d < n;
+       d += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t pd = P[d], pd1 = P[d + 1];
+    if (pd1 == pd || pd / g.T == (pd1 - 1) / g.T) continue;
+    cg_verdict* v = out + d;
+    uint32_t flags = v->flags, status;
+    finalize_fields(flags, status, v->first_unaddr, v->undef_count, err_mask);
+    v->flags = flags;
+    v->status = status;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a6: DtoH apply
+// ---------------------------------------------------------------------------
+constexpr uint64_t kApplyItemCost = 64;
+
+__global__ void __launch_bounds__(kThreads) k_apply_prep(const cg_copy_desc* __restrict__ descs,
+                                                         const cg_verdict* __restrict__ verd, uint64_t n,
+                                                         uint64_t* __restrict__ weight) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t w = 0;
+    if (descs[i].kind == CG_DTOH && verd[i].status == CG_OK) {
+      const Norm nm = normalize(descs[i]);
+      if (nm.host && nm.nbytes) w = kApplyItemCost + nm.nbytes;
+    }
+    weight[i] = w;
+  }
+}
+
+// fill shard-relative V bytes [q0, q1) with the byte value `val` (0x00/0xFF)
+__device__ __forceinline__ void fill_v(const ShadowView& sv, uint64_t q0, uint64_t q1, uint32_t val) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t k0 = q0 >> 4, k1 = (q1 + 15) >> 4;
+  uint4* V4 = reinterpret_cast<uint4*>(sv.V);
+  const uint32_t word = val * 0x01010101u;
+  for (uint64_t k = k0 + lane; k < k1; k += 32) {
+    const uint64_t qb = k << 4;
+    if (qb >= q0 && qb + 16 <= q1) {
+      stg_val16(V4 + k, word);
+    } else {
+      for (uint64_t q = umax64(qb, q0); q < umin64(qb + 16, q1); ++q) sv.V[q] = (uint8_t)val;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_apply(const cg_copy_desc* __restrict__ descs, uint64_t n,
+                                                    const uint64_t* __restrict__ P,
+                                                    const uint32_t* __restrict__ chunk_first, uint64_t t_min,
+                                                    uint64_t max_chunks, ShadowView sv) {
+  const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t c = gw; c < g.nchunks; c += nw) {
+    const uint64_t w0 = c * g.T, w1 = umin64(w0 + g.T, g.total);
+    for (uint64_t d = chunk_first[c]; d < n; ++d) {
+      const uint64_t pd = P[d];
+      if (pd >= w1) break;
+      const uint64_t pd1 = P[d + 1];
+      if (pd1 == pd) continue;
+      const Norm nm = normalize(descs[d]);
+      uint64_t a = umax64(w0, pd) - pd, b = umin64(w1, pd1) - pd;
+      a = a > kApplyItemCost ? a - kApplyItemCost : 0;
+      b = b > kApplyItemCost ? b - kApplyItemCost : 0;
+      if (a < b)
+        for_rows(nm, a, b, [&](uint64_t x, uint64_t len, uint64_t) {
+          const uint64_t y0 = umax64(x, sv.sb), y1 = umin64(x + len, sv.se);
+          if (y0 < y1) fill_v(sv, y0 - sv.sb, y1 - sv.sb, 0u);
+        });
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// plumbing: fresh shadow, marks, set_vbits check
+// ---------------------------------------------------------------------------
+__global__ void k_fill(uint4* __restrict__ p, uint64_t n16, uint32_t word) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    stg_val16(p + i, word);
+}
+
+__global__ void __launch_bounds__(kThreads) k_mark_prep(const cg_mark* __restrict__ marks, uint64_t n,
+                                                        uint64_t* __restrict__ weight) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    weight[i] = marks[i].len ? marks[i].len + kApplyItemCost : 0;
+}
+
+// A bits [q0, q1) := bit (set or clear); partial words with atomics because a
+// neighbouring mark of the same batch may own the other bits of the word
+__device__ __forceinline__ void put_abits(const ShadowView& sv, uint64_t q0, uint64_t q1, bool set) {
+  const int lane = threadIdx.x & 31;
+  uint32_t* A4 = reinterpret_cast<uint32_t*>(sv.A);
+  const uint64_t k0 = q0 >> 5, k1 = (q1 + 31) >> 5;
+  for (uint64_t k = k0 + lane; k < k1; k += 32) {
+    const uint32_t m = range_mask(k << 5, 32, q0, q1);
+    if (m == 0xffffffffu) A4[k] = set ? 0xffffffffu : 0u;
+    else if (set) atomicOr(A4 + k, m);
+    else atomicAnd(A4 + k, ~m);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_mark(const cg_mark* __restrict__ marks, uint64_t n,
+                                                   const uint64_t* __restrict__ P,
+                                                   const uint32_t* __restrict__ chunk_first, uint64_t t_min,
+                                                   uint64_t max_chunks, ShadowView sv) {
+  const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t c = gw; c < g.nchunks; c += nw) {
+    const uint64_t w0 = c * g.T, w1 = umin64(w0 + g.T, g.total);
+    for (uint64_t d = chunk_first[c]; d < n; ++d) {
+      const uint64_t pd = P[d];
+      if (pd >= w1) break;
+      const uint64_t pd1 = P[d + 1];
+      if (pd1 == pd) continue;
+      uint64_t a = umax64(w0, pd) - pd, b = umin64(w1, pd1) - pd;
+      a = a > kApplyItemCost ? a - kApplyItemCost : 0;
+      b = b > kApplyItemCost ? b - kApplyItemCost : 0;
+      if (a >= b) continue;
+      const cg_mark mk = marks[d];
+      const uint64_t x = mk.addr + a, end = mk.addr + b;
+      const uint64_t y0 = umax64(x, sv.sb), y1 = umin64(end, sv.se);
+      if (y0 >= y1) continue;
+      fill_v(sv, y0 - sv.sb, y1 - sv.sb, mk.state == CG_DEFINED ? 0x00u : 0xFFu);
+      put_abits(sv, y0 - sv.sb, y1 - sv.sb, mk.state != CG_NOACCESS);
+    }
+  }
+}
+
+__global__ void k_setv_check(ShadowView sv, uint64_t addr, uint64_t len, uint32_t* __restrict__ flag) {
+  const uint64_t y0 = umax64(addr, sv.sb), y1 = umin64(addr + len, sv.se);
+  for (uint64_t q = y0 - sv.sb + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < y1 - sv.sb;
+       q += (uint64_t)gridDim.x * blockDim.x)
+    if (!((sv.A[q >> 3] >> (q & 7)) & 1)) atomicOr(flag, 1u);
+}
+
+// ---------------------------------------------------------------------------
+// a8: leak sweep
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_live(Table t, uint64_t* __restrict__ weight) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < t.n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    weight[i] = t.fseq[i] == kInf ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(kThreads) k_leak_scatter(Table t, const uint64_t* __restrict__ P,
+                                                           cg_alloc_record* __restrict__ out, uint64_t cap,
+                                                           uint64_t* __restrict__ count) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < t.n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (t.fseq[i] == kInf && P[i] < cap) {
+      cg_alloc_record r;
+      r.base = t.base[i];
+      r.size = t.end[i] - t.base[i];
+      r.alloc_seq = t.aseq[i];
+      out[P[i]] = r;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *count = P[t.n];
+}
+
+inline int blocks_for(uint64_t n, int threads, int cap) {
+  uint64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  return (int)(b < (uint64_t)cap ? b : (uint64_t)cap);
+}
+
+}  // namespace
+
+uint64_t scan_blocks(uint64_t n) { return (n + kScanTile - 1) / kScanTile; }
+
+// prefix sum of p.weight[0..n) into p.P[0..n], then the chunk plan
+static cudaError_t plan(const Launch& L, uint64_t n, const Plan& p, cudaStream_t s) {
+  const uint64_t nb = scan_blocks(n);
+  if (nb > 0) {
+    k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, n, p.bsum);
+    k_scan_top<<<1, 1024, 0, s>>>(p.bsum, nb);
+    k_scan_down<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, n, p.bsum, p.P, nb);
+    *L.counter += 3;
+  } else {
+    cudaMemsetAsync(p.P, 0, sizeof(uint64_t), s);
+  }
+  k_plan<<<L.num_sms * 4, kThreads, 0, s>>>(p.P, n, p.t_min, p.max_chunks, p.chunk_first);
+  *L.counter += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out, const Table& t,
+                         const ShadowView& sv, const Plan& p, uint32_t err_mask, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const size_t smem = (size_t)t.nsplit * sizeof(uint64_t);
+  k_check_prep<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, smem, s>>>(d, n, t, out, p.weight);
+  *L.counter += 1;
+  cudaError_t e = plan(L, n, p, s);
+  if (e != cudaSuccess) return e;
+  k_check_scan<<<L.persist_blocks, kThreads, 0, s>>>(d, n, p.P, p.chunk_first, p.t_min, p.max_chunks, sv, out,
+                                                     err_mask);
+  k_finalize_split<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(n, p.P, p.t_min, p.max_chunks,
+                                                                               out, err_mask);
+  *L.counter += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t apply_dtoh(const Launch& L, const cg_copy_desc* d, const cg_verdict* v, uint64_t n,
+                       const ShadowView& sv, const Plan& p, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  k_apply_prep<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(d, v, n, p.weight);
+  *L.counter += 1;
+  cudaError_t e = plan(L, n, p, s);
+  if (e != cudaSuccess) return e;
+  k_apply<<<L.persist_blocks, kThreads, 0, s>>>(d, n, p.P, p.chunk_first, p.t_min, p.max_chunks, sv);
+  *L.counter += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t mark_batch(const Launch& L, const cg_mark* d_marks, uint64_t n, const ShadowView& sv, const Plan& p,
+                       cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  k_mark_prep<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(d_marks, n, p.weight);
+  *L.counter += 1;
+  cudaError_t e = plan(L, n, p, s);
+  if (e != cudaSuccess) return e;
+  k_mark<<<L.persist_blocks, kThreads, 0, s>>>(d_marks, n, p.P, p.chunk_first, p.t_min, p.max_chunks, sv);
+  *L.counter += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t fresh_shadow(const Launch& L, const ShadowView& sv, cudaStream_t s) {
+  const uint64_t nv = (sv.se - sv.sb) / 16, na = (sv.se - sv.sb) / 128;
+  k_fill<<<L.num_sms * 8, kThreads, 0, s>>>(reinterpret_cast<uint4*>(sv.V), nv, 0xffffffffu);
+  if (na) k_fill<<<L.num_sms * 8, kThreads, 0, s>>>(reinterpret_cast<uint4*>(sv.A), na, 0u);
+  *L.counter += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t setv_check(const Launch& L, uint64_t addr, uint64_t len, const ShadowView& sv, uint32_t* d_flag,
+                       cudaStream_t s) {
+  cudaMemsetAsync(d_flag, 0, sizeof(uint32_t), s);
+  k_setv_check<<<blocks_for(len, kThreads, L.num_sms * 4), kThreads, 0, s>>>(sv, addr, len, d_flag);
+  *L.counter += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t leak_sweep(const Launch& L, const Table& t, const Plan& p, cg_alloc_record* out, uint64_t cap,
+                       uint64_t* d_count, cudaStream_t s) {
+  if (t.n == 0) return cudaMemsetAsync(d_count, 0, sizeof(uint64_t), s);
+  k_live<<<blocks_for(t.n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(t, p.weight);
+  const uint64_t nb = scan_blocks(t.n);
+  k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, t.n, p.bsum);
+  k_scan_top<<<1, 1024, 0, s>>>(p.bsum, nb);
+  k_scan_down<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, t.n, p.bsum, p.P, nb);
+  k_leak_scatter<<<blocks_for(t.n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(t, p.P, out, cap, d_count);
+  *L.counter += 5;
+  return cudaGetLastError();
+}
+
+int persistent_blocks_check() {
+  int b = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_check_scan, kThreads, 0);
+  return b;
+}
+
+}  // namespace cgk

@@ -1,0 +1,519 @@
+// C-ABI runtime of the batched Cudagrind transfer checker (include/cg.h).
+//
+// Owns: the context (window, shard, caller buffers carved into device tables
+// and plan scratch), the registry host mirror (sorted,
+// lifetime-stamped entries; live set for overlap / free validation), its
+// upload to the device table, pinned staging, and the host epoch planner.
+// Every step of the check itself runs in the kernels of cg_kernels.cu.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "cg.h"
+#include "cg_internal.h"
+
+namespace cgk {
+int persistent_blocks_check();
+}
+
+namespace {
+
+constexpr uint64_t kAlign = 256;
+constexpr uint64_t kChunkMin = 16 * 1024;        // t_min of the chunk plans (weight units)
+constexpr uint64_t kMarkRun = 1u << 20;          // marks uploaded per run
+
+uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+struct Entry {
+  uint64_t base, end, aseq, fseq;
+};
+
+struct Layout {
+  uint64_t table, weight, P, bsum, chunk, marks, flags, leaks, desc_stage, verdict_stage, total;
+  uint64_t max_items, max_chunks;
+};
+
+bool valid_config(const cg_config* c) {
+  if (!c) return false;
+  if (c->host_size == 0 || c->host_base % 4096 || c->host_size % 4096) return false;
+  if (c->host_base + c->host_size < c->host_base) return false;
+  uint64_t sb = c->shard_size ? c->shard_base : c->host_base;
+  uint64_t ss = c->shard_size ? c->shard_size : c->host_size;
+  if (sb % 4096 || ss % 4096 || ss == 0) return false;
+  if (sb < c->host_base || sb + ss > c->host_base + c->host_size) return false;
+  if (c->max_descs == 0 || c->max_descs > cgk::kMaxDescs) return false;
+  if (c->max_allocs == 0 || c->max_allocs > (1ull << 32)) return false;
+  return true;
+}
+
+Layout layout_of(const cg_config* c) {
+  Layout L{};
+  L.max_items = std::max(c->max_descs, c->max_allocs);
+  L.max_chunks = std::max<uint64_t>(1u << 20, 2 * c->max_descs);
+  uint64_t off = 0;
+  auto take = [&](uint64_t bytes) {
+    uint64_t o = off;
+    off = align_up(off + bytes, kAlign);
+    return o;
+  };
+  L.table = take(5 * c->max_allocs * 8);
+  L.weight = take(L.max_items * 8);
+  L.P = take((L.max_items + 1) * 8);
+  L.bsum = take((cgk::scan_blocks(L.max_items) + 1) * 8);
+  L.chunk = take(L.max_chunks * 4);
+  L.marks = take(std::min<uint64_t>(c->max_descs, kMarkRun) * sizeof(cg_mark));
+  L.flags = take(256);
+  L.leaks = take(c->max_allocs * sizeof(cg_alloc_record));
+  L.desc_stage = c->host_staging ? take(c->max_descs * sizeof(cg_copy_desc)) : 0;
+  L.verdict_stage = c->host_staging ? take(c->max_descs * sizeof(cg_verdict)) : 0;
+  L.total = off;
+  return L;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+struct cg_ctx {
+  cg_config cfg;
+  Layout lay;
+  cgk::ShadowView sv;
+  cgk::Launch launch;
+  uint64_t launches = 0;
+  uint8_t* ws = nullptr;
+  // registry host mirror
+  std::vector<Entry> table;                 // sorted by (base, aseq)
+  std::map<uint64_t, uint64_t> live;        // base -> end of live allocations
+  uint64_t last_seq = 0;
+  bool dirty = true;
+  // pinned staging
+  uint64_t* h_table = nullptr;              // 5 * max_allocs
+  cg_mark* h_marks = nullptr;               // kMarkRun
+  cudaEvent_t staged = nullptr;
+  std::string err;
+
+  uint64_t* d(uint64_t off) { return reinterpret_cast<uint64_t*>(ws + off); }
+
+  cg_status fail(cg_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    err = buf;
+    return s;
+  }
+  cg_status cuda(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return CG_OK;
+    return fail(CG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  }
+
+  cgk::Plan plan() {
+    cgk::Plan p;
+    p.weight = d(lay.weight);
+    p.P = d(lay.P);
+    p.bsum = d(lay.bsum);
+    p.chunk_first = reinterpret_cast<uint32_t*>(ws + lay.chunk);
+    p.max_chunks = lay.max_chunks;
+    p.t_min = kChunkMin;
+    return p;
+  }
+
+  cgk::Table dev_table() {
+    cgk::Table t;
+    const uint64_t cap = cfg.max_allocs;
+    uint64_t* b = d(lay.table);
+    t.base = b;
+    t.end = b + cap;
+    t.aseq = b + 2 * cap;
+    t.fseq = b + 3 * cap;
+    t.pmax = b + 4 * cap;
+    t.n = table.size();
+    uint64_t stride = std::max<uint64_t>(32, (t.n + 4095) / 4096);
+    t.stride = (uint32_t)stride;
+    t.nsplit = (uint32_t)((t.n + stride - 1) / stride);
+    return t;
+  }
+
+  // upload the registry mirror (SoA + prefix max of ends) if it changed
+  cg_status sync_table(cudaStream_t s) {
+    if (!dirty) return CG_OK;
+    const uint64_t n = table.size(), cap = cfg.max_allocs;
+    if (n) {
+      cudaError_t e = cudaEventSynchronize(staged);   // previous upload finished reading h_table
+      if (e != cudaSuccess) return cuda(e, "cudaEventSynchronize");
+      uint64_t pm = 0;
+      for (uint64_t i = 0; i < n; ++i) {
+        const Entry& x = table[i];
+        h_table[i] = x.base;
+        h_table[cap + i] = x.end;
+        h_table[2 * cap + i] = x.aseq;
+        h_table[3 * cap + i] = x.fseq;
+        pm = std::max(pm, x.end);
+        h_table[4 * cap + i] = pm;
+      }
+      uint64_t* dt = d(lay.table);
+      for (int k = 0; k < 5; ++k) {
+        e = cudaMemcpyAsync(dt + k * cap, h_table + k * cap, n * 8, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return cuda(e, "table upload");
+      }
+      cudaEventRecord(staged, s);
+    }
+    dirty = false;
+    return CG_OK;
+  }
+
+  uint32_t err_mask() const {
+    return cfg.undef_is_error ? 0xffffffffu : ~(uint32_t)CG_F_HOST_UNDEFINED;
+  }
+};
+
+extern "C" {
+
+uint64_t cg_workspace_size(const cg_config* cfg) {
+  if (!valid_config(cfg)) return 0;
+  return layout_of(cfg).total;
+}
+
+cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
+  if (!out) return CG_ERR_INVALID_VALUE;
+  *out = nullptr;
+  if (!valid_config(cfg)) return CG_ERR_INVALID_VALUE;
+  const Layout lay = layout_of(cfg);
+  if (!cfg->v_buf || !cfg->a_buf || !cfg->workspace) return CG_ERR_INVALID_VALUE;
+  if (cfg->workspace_size < lay.total) return CG_ERR_INVALID_VALUE;
+  if ((uintptr_t)cfg->v_buf % 16 || (uintptr_t)cfg->a_buf % 16 || (uintptr_t)cfg->workspace % kAlign)
+    return CG_ERR_INVALID_VALUE;
+  DeviceGuard g(cfg->device);
+  cg_ctx* c = new cg_ctx();
+  c->cfg = *cfg;
+  c->lay = lay;
+  c->ws = static_cast<uint8_t*>(cfg->workspace);
+  c->sv.wb = cfg->host_base;
+  c->sv.we = cfg->host_base + cfg->host_size;
+  c->sv.sb = cfg->shard_size ? cfg->shard_base : cfg->host_base;
+  c->sv.se = c->sv.sb + (cfg->shard_size ? cfg->shard_size : cfg->host_size);
+  c->sv.V = static_cast<uint8_t*>(cfg->v_buf);
+  c->sv.A = static_cast<uint8_t*>(cfg->a_buf);
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, cfg->device);
+  if (e != cudaSuccess) {
+    delete c;
+    return CG_ERR_CUDA;
+  }
+  c->launch.num_sms = prop.multiProcessorCount;
+  int per_sm = cgk::persistent_blocks_check();
+  c->launch.persist_blocks = prop.multiProcessorCount * std::max(per_sm, 1);
+  c->launch.counter = &c->launches;
+  if (cudaMallocHost(&c->h_table, 5 * cfg->max_allocs * 8) != cudaSuccess ||
+      cudaMallocHost(&c->h_marks, std::min<uint64_t>(cfg->max_descs, kMarkRun) * sizeof(cg_mark)) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->staged, cudaEventDisableTiming) != cudaSuccess) {
+    cg_ctx_destroy(c);
+    return CG_ERR_OUT_OF_MEMORY;
+  }
+  cudaEventRecord(c->staged, 0);
+  e = cgk::fresh_shadow(c->launch, c->sv, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    cg_ctx_destroy(c);
+    return CG_ERR_CUDA;
+  }
+  *out = c;
+  return CG_OK;
+}
+
+cg_status cg_ctx_destroy(cg_ctx* c) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  DeviceGuard g(c->cfg.device);
+  if (c->staged) {
+    cudaEventSynchronize(c->staged);
+    cudaEventDestroy(c->staged);
+  }
+  if (c->h_table) cudaFreeHost(c->h_table);
+  if (c->h_marks) cudaFreeHost(c->h_marks);
+  delete c;
+  return CG_OK;
+}
+
+const char* cg_last_error(const cg_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+uint64_t cg_kernel_launches(const cg_ctx* c) { return c ? c->launches : 0; }
+
+static bool in_window(const cg_ctx* c, uint64_t addr, uint64_t len) {
+  return addr >= c->sv.wb && len <= c->sv.we - c->sv.wb && addr - c->sv.wb <= (c->sv.we - c->sv.wb) - len;
+}
+
+cg_status cg_host_mark_batch(cg_ctx* c, const cg_mark* h_marks, uint64_t n, uint32_t* h_status, void* stream) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (n == 0) return CG_OK;
+  if (!h_marks) return c->fail(CG_ERR_INVALID_VALUE, "null marks");
+  if (n > c->cfg.max_descs) return c->fail(CG_ERR_INVALID_VALUE, "n > max_descs");
+  DeviceGuard g(c->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint64_t cap = std::min<uint64_t>(c->cfg.max_descs, kMarkRun);
+  cg_mark* dm = reinterpret_cast<cg_mark*>(c->ws + c->lay.marks);
+  cg_status ret = CG_OK;
+  // runs of pairwise-disjoint valid marks are applied in parallel, runs in order
+  uint64_t i = 0;
+  while (i < n) {
+    std::map<uint64_t, uint64_t> run;   // start -> end of the marks of this run
+    uint64_t j = i, k = 0;
+    cudaError_t e = cudaEventSynchronize(c->staged);   // the previous run's upload has been read
+    if (e != cudaSuccess) return c->cuda(e, "cudaEventSynchronize");
+    while (j < n && k < cap) {
+      const cg_mark& m = h_marks[j];
+      const bool valid = m.state <= CG_DEFINED && (m.len == 0 || in_window(c, m.addr, m.len));
+      if (h_status) h_status[j] = valid ? CG_OK : CG_ERR_INVALID_VALUE;
+      if (!valid) {
+        ret = c->fail(CG_ERR_INVALID_VALUE, "mark %llu invalid (state or range)", (unsigned long long)j);
+        ++j;
+        continue;
+      }
+      if (m.len) {
+        const uint64_t a = m.addr, b = m.addr + m.len;
+        auto it = run.upper_bound(a);
+        bool overlap = (it != run.end() && it->first < b);
+        if (!overlap && it != run.begin()) overlap = std::prev(it)->second > a;
+        if (overlap) break;
+        run.emplace(a, b);
+        c->h_marks[k++] = m;
+      }
+      ++j;
+    }
+    if (k) {
+      e = cudaMemcpyAsync(dm, c->h_marks, k * sizeof(cg_mark), cudaMemcpyHostToDevice, s);
+      if (e != cudaSuccess) return c->cuda(e, "marks upload");
+      e = cgk::mark_batch(c->launch, dm, k, c->sv, c->plan(), s);
+      if (e != cudaSuccess) return c->cuda(e, "mark kernels");
+      cudaEventRecord(c->staged, s);
+    }
+    i = j;
+  }
+  return ret;
+}
+
+cg_status cg_host_mark(cg_ctx* c, uint64_t addr, uint64_t len, uint32_t state, void* stream) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  cg_mark m{addr, len, state, 0};
+  return cg_host_mark_batch(c, &m, 1, nullptr, stream);
+}
+
+cg_status cg_host_set_vbits(cg_ctx* c, uint64_t addr, uint64_t len, const uint8_t* h_vbytes, void* stream) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (len == 0) return CG_OK;
+  if (!h_vbytes) return c->fail(CG_ERR_INVALID_VALUE, "null vbytes");
+  if (!in_window(c, addr, len)) return c->fail(CG_ERR_INVALID_VALUE, "set_vbits range outside the host window");
+  DeviceGuard g(c->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint64_t y0 = std::max(addr, c->sv.sb), y1 = std::min(addr + len, c->sv.se);
+  if (y0 >= y1) return CG_OK;   // nothing of it in this shard
+  uint32_t* flag = reinterpret_cast<uint32_t*>(c->ws + c->lay.flags);
+  cudaError_t e = cgk::setv_check(c->launch, addr, len, c->sv, flag, s);
+  uint32_t h_flag = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h_flag, flag, sizeof h_flag, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return c->cuda(e, "set_vbits check");
+  if (h_flag) return c->fail(CG_ERR_INVALID_VALUE, "set_vbits on unaddressable bytes");
+  e = cudaMemcpyAsync(c->sv.V + (y0 - c->sv.sb), h_vbytes + (y0 - addr), y1 - y0, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return c->cuda(e, "set_vbits copy");
+}
+
+cg_status cg_register_alloc(cg_ctx* c, uint64_t base, uint64_t size, uint64_t seq) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (size == 0 || base == 0) return c->fail(CG_ERR_INVALID_VALUE, "register: size 0 or base 0");
+  if (size > UINT64_MAX - base) return c->fail(CG_ERR_INVALID_VALUE, "register: range overflows");
+  if (seq <= c->last_seq) return c->fail(CG_ERR_INVALID_VALUE, "register: seq not increasing");
+  const uint64_t end = base + size;
+  auto it = c->live.lower_bound(base);
+  if (it != c->live.end() && it->first < end)
+    return c->fail(CG_ERR_INVALID_VALUE, "register: overlaps a live allocation");
+  if (it != c->live.begin() && std::prev(it)->second > base)
+    return c->fail(CG_ERR_INVALID_VALUE, "register: overlaps a live allocation");
+  if (c->table.size() >= c->cfg.max_allocs) return c->fail(CG_ERR_OUT_OF_MEMORY, "allocation table full");
+  Entry x{base, end, seq, cgk::kInf};
+  auto pos = std::upper_bound(c->table.begin(), c->table.end(), base,
+                              [](uint64_t b, const Entry& e) { return b < e.base; });
+  c->table.insert(pos, x);
+  c->live.emplace(base, end);
+  c->last_seq = seq;
+  c->dirty = true;
+  return CG_OK;
+}
+
+cg_status cg_free(cg_ctx* c, uint64_t ptr, uint64_t seq) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (seq <= c->last_seq) return c->fail(CG_ERR_INVALID_VALUE, "free: seq not increasing");
+  auto it = c->live.find(ptr);
+  if (it == c->live.end()) return c->fail(CG_ERR_INVALID_VALUE, "InvalidFree: not a live base");
+  auto pos = std::lower_bound(c->table.begin(), c->table.end(), ptr,
+                              [](const Entry& e, uint64_t b) { return e.base < b; });
+  for (; pos != c->table.end() && pos->base == ptr; ++pos) {
+    if (pos->fseq == cgk::kInf) {
+      pos->fseq = seq;
+      break;
+    }
+  }
+  c->live.erase(it);
+  c->last_seq = seq;
+  c->dirty = true;
+  return CG_OK;
+}
+
+cg_status cg_registry_compact(cg_ctx* c, uint64_t before_seq) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  auto it = std::remove_if(c->table.begin(), c->table.end(),
+                           [&](const Entry& e) { return e.fseq != cgk::kInf && e.fseq <= before_seq; });
+  if (it != c->table.end()) {
+    c->table.erase(it, c->table.end());
+    c->dirty = true;
+  }
+  return CG_OK;
+}
+
+cg_status cg_check_copies(cg_ctx* c, const cg_copy_desc* d_descs, uint64_t n, cg_verdict* d_out, void* stream) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (n == 0) return CG_OK;
+  if (!d_descs || !d_out) return c->fail(CG_ERR_INVALID_VALUE, "null descriptor or verdict array");
+  if (n > c->cfg.max_descs) return c->fail(CG_ERR_INVALID_VALUE, "n > max_descs");
+  DeviceGuard g(c->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cg_status st = c->sync_table(s);
+  if (st != CG_OK) return st;
+  cudaError_t e = cgk::check_copies(c->launch, d_descs, n, d_out, c->dev_table(), c->sv, c->plan(), c->err_mask(), s);
+  return c->cuda(e, "check kernels");
+}
+
+cg_status cg_apply_dtoh(cg_ctx* c, const cg_copy_desc* d_descs, const cg_verdict* d_verdicts, uint64_t n,
+                        void* stream) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (n == 0) return CG_OK;
+  if (!d_descs || !d_verdicts) return c->fail(CG_ERR_INVALID_VALUE, "null descriptor or verdict array");
+  if (n > c->cfg.max_descs) return c->fail(CG_ERR_INVALID_VALUE, "n > max_descs");
+  DeviceGuard g(c->cfg.device);
+  cudaError_t e = cgk::apply_dtoh(c->launch, d_descs, d_verdicts, n, c->sv, c->plan(), static_cast<cudaStream_t>(stream));
+  return c->cuda(e, "apply kernels");
+}
+
+cg_status cg_check_copies_host(cg_ctx* c, const cg_copy_desc* h_descs, uint64_t n, cg_verdict* h_out, int apply,
+                               void* stream) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (!c->cfg.host_staging) return c->fail(CG_ERR_NOT_INITIALIZED, "context created without host staging");
+  if (n == 0) return CG_OK;
+  if (!h_descs || !h_out) return c->fail(CG_ERR_INVALID_VALUE, "null host arrays");
+  if (n > c->cfg.max_descs) return c->fail(CG_ERR_INVALID_VALUE, "n > max_descs");
+  DeviceGuard g(c->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cg_copy_desc* dd = reinterpret_cast<cg_copy_desc*>(c->ws + c->lay.desc_stage);
+  cg_verdict* dv = reinterpret_cast<cg_verdict*>(c->ws + c->lay.verdict_stage);
+  cudaError_t e = cudaMemcpyAsync(dd, h_descs, n * sizeof(cg_copy_desc), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return c->cuda(e, "descriptor upload");
+  cg_status st = cg_check_copies(c, dd, n, dv, stream);
+  if (st != CG_OK) return st;
+  if (apply) {
+    st = cg_apply_dtoh(c, dd, dv, n, stream);
+    if (st != CG_OK) return st;
+  }
+  e = cudaMemcpyAsync(h_out, dv, n * sizeof(cg_verdict), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return c->cuda(e, "verdict download");
+}
+
+cg_status cg_leak_sweep(cg_ctx* c, cg_alloc_record* d_out, uint64_t cap, uint64_t* d_count, void* stream) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (!d_count || (cap && !d_out)) return c->fail(CG_ERR_INVALID_VALUE, "null output");
+  DeviceGuard g(c->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cg_status st = c->sync_table(s);
+  if (st != CG_OK) return st;
+  cudaError_t e = cgk::leak_sweep(c->launch, c->dev_table(), c->plan(), d_out, cap, d_count, s);
+  return c->cuda(e, "leak sweep");
+}
+
+cg_status cg_leak_report(cg_ctx* c, cg_alloc_record* h_out, uint64_t cap, uint64_t* n_out) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (!n_out || (cap && !h_out)) return c->fail(CG_ERR_INVALID_VALUE, "null output");
+  DeviceGuard g(c->cfg.device);
+  cg_alloc_record* d_rec = reinterpret_cast<cg_alloc_record*>(c->ws + c->lay.leaks);
+  uint64_t* d_cnt = reinterpret_cast<uint64_t*>(c->ws + c->lay.flags + 64);
+  cg_status st = cg_leak_sweep(c, d_rec, c->cfg.max_allocs, d_cnt, 0);
+  uint64_t k = 0;
+  if (st == CG_OK) {
+    cudaError_t e = cudaMemcpy(&k, d_cnt, sizeof k, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && cap && k)
+      e = cudaMemcpy(h_out, d_rec, std::min(cap, k) * sizeof(cg_alloc_record), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) st = c->cuda(e, "leak report download");
+  }
+  *n_out = k;
+  return st;
+}
+
+static bool host_range(const cg_copy_desc& d, uint64_t& lo, uint64_t& hi) {
+  const bool htod = d.kind == CG_HTOD;
+  if (!htod && d.kind != CG_DTOH) return false;
+  const uint64_t base = htod ? d.src : d.dst, x = htod ? d.src_x : d.dst_x;
+  const uint64_t y = htod ? d.src_y : d.dst_y, pitch = htod ? d.src_pitch : d.dst_pitch;
+  if (d.width == 0 || d.height == 0) return false;
+  unsigned __int128 st = (unsigned __int128)base + (unsigned __int128)y * pitch + x;
+  unsigned __int128 sp = (unsigned __int128)(d.height - 1) * pitch + d.width;
+  if (st + sp > (unsigned __int128)UINT64_MAX) return false;
+  lo = (uint64_t)st;
+  hi = (uint64_t)(st + sp);
+  return true;
+}
+
+cg_status cg_plan_batches(const cg_copy_desc* h_descs, uint64_t n, uint64_t* h_cuts, uint64_t* n_cuts) {
+  if (!n_cuts || (n && (!h_descs || !h_cuts))) return CG_ERR_INVALID_VALUE;
+  std::map<uint64_t, uint64_t> dtoh;   // merged DtoH host intervals of the open batch
+  uint64_t k = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t lo, hi;
+    if (!host_range(h_descs[i], lo, hi)) continue;
+    if (h_descs[i].kind == CG_HTOD) {
+      auto it = dtoh.upper_bound(lo);
+      bool overlap = it != dtoh.end() && it->first < hi;
+      if (!overlap && it != dtoh.begin()) overlap = std::prev(it)->second > lo;
+      if (overlap) {
+        h_cuts[k++] = i;
+        dtoh.clear();
+      }
+    } else {
+      // insert [lo, hi) merging neighbours
+      auto it = dtoh.upper_bound(lo);
+      if (it != dtoh.begin() && std::prev(it)->second >= lo) {
+        --it;
+        lo = it->first;
+        hi = std::max(hi, it->second);
+        it = dtoh.erase(it);
+      }
+      while (it != dtoh.end() && it->first <= hi) {
+        hi = std::max(hi, it->second);
+        it = dtoh.erase(it);
+      }
+      dtoh.emplace(lo, hi);
+    }
+  }
+  if (n) h_cuts[k++] = n;
+  *n_cuts = k;
+  return CG_OK;
+}
+
+}  // extern "C"

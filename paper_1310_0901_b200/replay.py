@@ -1,0 +1,85 @@
+"""Replay a recorded call stream through the C ABI (the way the paper's
+wrappers see a program: "Anytime a program handles memory on the device
+or transfers data ... the respective Cudagrind wrapper will be called").
+
+``events`` is any numpy structured array with the fields
+``op, kind, seq, width, height, dst, dst_x, dst_y, dst_pitch, src, src_x,
+src_y, src_pitch`` (op: 1 host mark, 2 set V-bytes, 3 register, 4 free,
+5 copy).  Host shadow updates are applied in order; between two of them, all
+registry events are submitted first (the table is lifetime-stamped, so a copy
+sees exactly the allocations live at its seq) and the copies are checked in the
+hazard-free batches cg_plan_batches cuts (check, then DtoH apply, per batch).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+OP_MARK, OP_SETV, OP_REG, OP_FREE, OP_COPY = 1, 2, 3, 4, 5
+_DESC_FIELDS = ("kind", "seq", "width", "height", "dst", "dst_x", "dst_y", "dst_pitch",
+                "src", "src_x", "src_y", "src_pitch")
+
+
+def events_to_descs(ev: np.ndarray) -> np.ndarray:
+    from . import DESC_DTYPE
+    d = np.zeros(len(ev), DESC_DTYPE)
+    for f in _DESC_FIELDS:
+        d[f] = ev[f]
+    return d
+
+
+def replay_events(chk, events: np.ndarray, blob=None, stream=None):
+    """Returns (verdicts of the COPY events in order, status per event)."""
+    import torch
+    from . import MARK_DTYPE, VERDICT_DTYPE, to_device_descs, verdicts_to_numpy
+
+    ops = np.asarray(events["op"])
+    n = len(events)
+    status = np.zeros(n, np.uint32)
+    is_copy = ops == OP_COPY
+    copy_rank = np.cumsum(is_copy) - 1
+    verdicts = np.zeros(int(is_copy.sum()), VERDICT_DTYPE)
+    i = 0
+    while i < n:
+        op = ops[i]
+        if op == OP_MARK:
+            j = i
+            while j < n and ops[j] == OP_MARK:
+                j += 1
+            m = np.zeros(j - i, MARK_DTYPE)
+            m["addr"] = events["dst"][i:j]
+            m["len"] = events["width"][i:j]
+            m["state"] = events["kind"][i:j]
+            st = np.zeros(j - i, np.uint32)
+            chk.host_mark_batch(m, status_out=st, stream=stream)
+            status[i:j] = st
+            i = j
+        elif op == OP_SETV:
+            off, ln = int(events["src"][i]), int(events["width"][i])
+            status[i] = chk.host_set_vbits(int(events["dst"][i]), bytes(blob[off:off + ln]), stream=stream)
+            i += 1
+        else:
+            j = i
+            while j < n and ops[j] in (OP_REG, OP_FREE, OP_COPY):
+                j += 1
+            for k in range(i, j):
+                if ops[k] == OP_REG:
+                    status[k] = chk.register_alloc(int(events["dst"][k]), int(events["width"][k]),
+                                                   int(events["seq"][k]))
+                elif ops[k] == OP_FREE:
+                    status[k] = chk.free(int(events["dst"][k]), int(events["seq"][k]))
+            idx = np.flatnonzero(is_copy[i:j]) + i
+            if len(idx):
+                descs = events_to_descs(events[idx])
+                cuts = [0] + [int(c) for c in __import__(__package__).plan_batches(descs)]
+                for a, b in zip(cuts[:-1], cuts[1:]):
+                    for s0 in range(a, b, chk.max_descs):
+                        s1 = min(b, s0 + chk.max_descs)
+                        dd = to_device_descs(descs[s0:s1], chk.device)
+                        dv = chk.check_copies(dd, stream=stream)
+                        chk.apply_dtoh(dd, dv, stream=stream)
+                        v = verdicts_to_numpy(dv)
+                        verdicts[copy_rank[idx[s0:s1]]] = v
+                        status[idx[s0:s1]] = v["status"]
+            i = j
+    torch.cuda.synchronize(chk.device)
+    return verdicts, status

@@ -114,7 +114,7 @@ class FlatModel:
             start = base + y * pitch + x
             span = 0 if (w == 0 or h == 0) else (h - 1) * pitch + w
             sides[p] = (start, span, pitch, start + span <= U64)
-        bytes_ok = w * h <= U64
+        bytes_ok = w * h <= (1 << 38)          # R-10
         if not (sides["dst"][3] and sides["src"][3] and bytes_ok):
             out["flags"] |= FLAG["INVALID_RANGE"]
         dev = {1: ["dst"], 2: ["src"], 3: ["dst", "src"]}[kind]

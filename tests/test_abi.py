@@ -1,0 +1,106 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol
+include/cg.h declares, the ctypes/numpy layouts match the header, and the
+host-side epoch planner (cg_plan_batches) cuts exactly at DtoH->HtoD hazards."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import tracegen as tg
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "cg.h")
+
+
+@pytest.fixture(scope="module")
+def cg():
+    from paper_1310_0901_b200 import build
+    build.build()
+    import paper_1310_0901_b200 as m
+    return m
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(cg_[a-z_]+)\s*\(", src)))
+
+
+def test_every_declared_symbol_is_exported(cg):
+    names = declared_functions()
+    assert len(names) >= 17
+    lib = ctypes.CDLL(cg.LIB_PATH)
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(cg.EXPORTED)
+
+
+def test_struct_sizes_match_header(cg):
+    assert ctypes.sizeof(cg.cg_config) == 96
+    assert cg.DESC_DTYPE.itemsize == 96 and cg.VERDICT_DTYPE.itemsize == 64
+    # the header states the same sizes in its comments
+    src = open(HEADER).read()
+    assert "96 bytes" in src and "64 bytes" in src and "24 bytes" in src
+
+
+def test_workspace_size_validation(cg):
+    c = cg.cg_config(host_base=1 << 20, host_size=1 << 20, max_descs=1000, max_allocs=100)
+    assert cg.cg_workspace_size(ctypes.byref(c)) > 0
+    bad = cg.cg_config(host_base=(1 << 20) + 1, host_size=1 << 20, max_descs=1000, max_allocs=100)
+    assert cg.cg_workspace_size(ctypes.byref(bad)) == 0
+    bad = cg.cg_config(host_base=1 << 20, host_size=1 << 20, shard_base=1 << 21, shard_size=4096,
+                       max_descs=1000, max_allocs=100)
+    assert cg.cg_workspace_size(ctypes.byref(bad)) == 0
+
+
+def _hazard_free(descs, a, b):
+    """brute force: no HtoD in [a,b) overlaps the host bytes of an earlier DtoH in [a,b)"""
+    def host(d):
+        if d["kind"] not in (1, 2) or d["width"] == 0 or d["height"] == 0:
+            return None
+        p = "src" if d["kind"] == 1 else "dst"
+        s = int(d[p]) + int(d[p + "_y"]) * int(d[p + "_pitch"]) + int(d[p + "_x"])
+        e = s + (int(d["height"]) - 1) * int(d[p + "_pitch"]) + int(d["width"])
+        return None if e > (1 << 64) - 1 else (s, e)
+    seen = []
+    for i in range(a, b):
+        r = host(descs[i])
+        if r is None:
+            continue
+        if descs[i]["kind"] == 2:
+            seen.append(r)
+        elif any(r[0] < e and s < r[1] for s, e in seen):
+            return False
+    return True
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_plan_batches_cuts_only_at_hazards(cg, seed):
+    from paper_1310_0901_b200.replay import events_to_descs
+    tr = tg.random_tiny(seed)
+    ev = tr.events[tr.events["op"] == tg.OP_COPY]
+    descs = events_to_descs(ev)
+    cuts = [0] + [int(c) for c in cg.plan_batches(descs)]
+    assert cuts[-1] == len(descs)
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        assert b > a
+        assert _hazard_free(descs, a, b)           # every batch is hazard-free
+        if b < len(descs):                          # and each cut is necessary (greedy)
+            assert not _hazard_free(descs, a, b + 1)
+
+
+def test_plan_batches_toy(cg):
+    """Appendix A.1: the toy trace's copies form the epochs {C1-C4}, {C5-C7}, {C8-C10}."""
+    from paper_1310_0901_b200.replay import events_to_descs
+    tr = tg.toy()
+    descs = events_to_descs(tr.events[tr.events["op"] == tg.OP_COPY])
+    assert [int(c) for c in cg.plan_batches(descs)] == [4, 7, 10]
+
+
+def test_plan_batches_c2_single_epoch(cg):
+    from paper_1310_0901_b200.replay import events_to_descs
+    tr = tg.c2_small(n_copies=20000, n_allocs=2000)
+    descs = events_to_descs(tr.events[tr.events["op"] == tg.OP_COPY])
+    assert [int(c) for c in cg.plan_batches(descs)] == [len(descs)]
