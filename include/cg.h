@@ -261,6 +261,25 @@ cg_status cg_plan_batches(const cg_copy_desc *h_descs, uint64_t n, uint64_t *h_c
 /* Number of kernels this context has launched so far (for bench accounting). */
 uint64_t cg_kernel_launches(const cg_ctx *ctx);
 
+/* Per-stage device timing (bench instrumentation).  After cg_profile_begin,
+ * every asynchronous call brackets each of its stages with CUDA events on the
+ * call's stream.  cg_profile_end synchronises, writes the accumulated
+ * milliseconds and launch counts of the stages to ms[CG_STAGE_COUNT] and
+ * launches[CG_STAGE_COUNT] (either may be NULL) and stops recording. */
+enum {
+  CG_STAGE_CHECK_PREP = 0,   /* a1+a3: k_check_prep                      */
+  CG_STAGE_CHECK_PLAN = 1,   /* a2: prefix sum + chunk plan              */
+  CG_STAGE_CHECK_SCAN = 2,   /* a4+a5: k_check_scan (the shadow scan)    */
+  CG_STAGE_CHECK_FINAL = 3,  /* a5: k_finalize_split                     */
+  CG_STAGE_APPLY_PREP = 4,   /* a6: k_apply_prep                         */
+  CG_STAGE_APPLY_PLAN = 5,   /* a6: prefix sum + chunk plan              */
+  CG_STAGE_APPLY = 6,        /* a6: k_apply (the DtoH shadow update)     */
+  CG_STAGE_LEAK = 7,         /* a8: leak sweep                           */
+  CG_STAGE_COUNT = 8
+};
+cg_status cg_profile_begin(cg_ctx *ctx);
+cg_status cg_profile_end(cg_ctx *ctx, double *ms, uint64_t *launches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -95,6 +95,8 @@ def _load() -> ctypes.CDLL:
         "cg_leak_report": (I, [P, P, U64, P]),
         "cg_plan_batches": (I, [P, U64, P, P]),
         "cg_kernel_launches": (U64, [P]),
+        "cg_profile_begin": (I, [P]),
+        "cg_profile_end": (I, [P, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -107,7 +109,7 @@ _lib = _load()
 EXPORTED = ("cg_workspace_size", "cg_ctx_create", "cg_ctx_destroy", "cg_last_error", "cg_host_mark",
             "cg_host_mark_batch", "cg_host_set_vbits", "cg_register_alloc", "cg_free", "cg_registry_compact",
             "cg_check_copies", "cg_apply_dtoh", "cg_check_copies_host", "cg_leak_sweep", "cg_leak_report",
-            "cg_plan_batches", "cg_kernel_launches")
+            "cg_plan_batches", "cg_kernel_launches", "cg_profile_begin", "cg_profile_end")
 
 # ---- same-name thin wrappers (status codes returned unchanged) -------------
 cg_workspace_size = _lib.cg_workspace_size
@@ -127,6 +129,10 @@ cg_leak_sweep = _lib.cg_leak_sweep
 cg_leak_report = _lib.cg_leak_report
 cg_plan_batches = _lib.cg_plan_batches
 cg_kernel_launches = _lib.cg_kernel_launches
+cg_profile_begin = _lib.cg_profile_begin
+cg_profile_end = _lib.cg_profile_end
+STAGES = ("check_prep", "check_plan", "check_scan", "check_finalize", "apply_prep", "apply_plan", "apply",
+          "leak_sweep")
 
 
 def plan_batches(descs: np.ndarray) -> np.ndarray:
@@ -262,6 +268,16 @@ class Checker:
         if n.value:
             self._ok(_lib.cg_leak_report(self.ctx, out.ctypes.data, n.value, ctypes.byref(n)), "cg_leak_report")
         return out
+
+    # ---- instrumentation -----------------------------------------------------
+    def profile_begin(self):
+        self._ok(_lib.cg_profile_begin(self.ctx), "cg_profile_begin")
+
+    def profile_end(self) -> dict:
+        ms = np.zeros(len(STAGES), np.float64)
+        n = np.zeros(len(STAGES), np.uint64)
+        self._ok(_lib.cg_profile_end(self.ctx, ms.ctypes.data, n.ctypes.data), "cg_profile_end")
+        return {s: (float(ms[i]), int(n[i])) for i, s in enumerate(STAGES)}
 
     # ---- state download (tests) ---------------------------------------------
     def shadow(self):

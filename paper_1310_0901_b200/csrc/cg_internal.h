@@ -47,10 +47,21 @@ struct Plan {
   uint64_t t_min;
 };
 
+// Optional per-stage event recording (cg_profile_begin / cg_profile_end).
+struct Profiler {
+  bool on = false;
+  void (*mark)(void* self, int stage, bool begin, cudaStream_t s) = nullptr;
+  void* self = nullptr;
+};
+
 struct Launch {
   int num_sms;
   int persist_blocks;     // persistent grid for the chunked kernels
   uint64_t* counter;      // host counter of kernel launches
+  Profiler* prof;
+  void stage(int st, bool begin, cudaStream_t s) const {
+    if (prof && prof->on) prof->mark(prof->self, st, begin, s);
+  }
 };
 
 constexpr int kScanTile = 2048;   // items per block of the prefix scan

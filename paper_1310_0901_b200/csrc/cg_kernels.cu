@@ -776,14 +776,22 @@ cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_
                          const ShadowView& sv, const Plan& p, uint32_t err_mask, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   const size_t smem = (size_t)t.nsplit * sizeof(uint64_t);
+  L.stage(CG_STAGE_CHECK_PREP, true, s);
   k_check_prep<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, smem, s>>>(d, n, t, out, p.weight);
   *L.counter += 1;
+  L.stage(CG_STAGE_CHECK_PREP, false, s);
+  L.stage(CG_STAGE_CHECK_PLAN, true, s);
   cudaError_t e = plan(L, n, p, s);
   if (e != cudaSuccess) return e;
+  L.stage(CG_STAGE_CHECK_PLAN, false, s);
+  L.stage(CG_STAGE_CHECK_SCAN, true, s);
   k_check_scan<<<L.persist_blocks, kThreads, 0, s>>>(d, n, p.P, p.chunk_first, p.t_min, p.max_chunks, sv, out,
                                                      err_mask);
+  L.stage(CG_STAGE_CHECK_SCAN, false, s);
+  L.stage(CG_STAGE_CHECK_FINAL, true, s);
   k_finalize_split<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(n, p.P, p.t_min, p.max_chunks,
                                                                                out, err_mask);
+  L.stage(CG_STAGE_CHECK_FINAL, false, s);
   *L.counter += 2;
   return cudaGetLastError();
 }
@@ -791,11 +799,17 @@ cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_
 cudaError_t apply_dtoh(const Launch& L, const cg_copy_desc* d, const cg_verdict* v, uint64_t n,
                        const ShadowView& sv, const Plan& p, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
+  L.stage(CG_STAGE_APPLY_PREP, true, s);
   k_apply_prep<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(d, v, n, p.weight);
   *L.counter += 1;
+  L.stage(CG_STAGE_APPLY_PREP, false, s);
+  L.stage(CG_STAGE_APPLY_PLAN, true, s);
   cudaError_t e = plan(L, n, p, s);
   if (e != cudaSuccess) return e;
+  L.stage(CG_STAGE_APPLY_PLAN, false, s);
+  L.stage(CG_STAGE_APPLY, true, s);
   k_apply<<<L.persist_blocks, kThreads, 0, s>>>(d, n, p.P, p.chunk_first, p.t_min, p.max_chunks, sv);
+  L.stage(CG_STAGE_APPLY, false, s);
   *L.counter += 1;
   return cudaGetLastError();
 }
@@ -831,12 +845,14 @@ cudaError_t setv_check(const Launch& L, uint64_t addr, uint64_t len, const Shado
 cudaError_t leak_sweep(const Launch& L, const Table& t, const Plan& p, cg_alloc_record* out, uint64_t cap,
                        uint64_t* d_count, cudaStream_t s) {
   if (t.n == 0) return cudaMemsetAsync(d_count, 0, sizeof(uint64_t), s);
+  L.stage(CG_STAGE_LEAK, true, s);
   k_live<<<blocks_for(t.n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(t, p.weight);
   const uint64_t nb = scan_blocks(t.n);
   k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, t.n, p.bsum);
   k_scan_top<<<1, 1024, 0, s>>>(p.bsum, nb);
   k_scan_down<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, t.n, p.bsum, p.P, nb);
   k_leak_scatter<<<blocks_for(t.n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(t, p.P, out, cap, d_count);
+  L.stage(CG_STAGE_LEAK, false, s);
   *L.counter += 5;
   return cudaGetLastError();
 }

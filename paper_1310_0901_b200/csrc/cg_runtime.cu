@@ -109,6 +109,26 @@ struct cg_ctx {
   cg_mark* h_marks = nullptr;               // kMarkRun
   cudaEvent_t staged = nullptr;
   std::string err;
+  // profiling (cg_profile_begin / end)
+  cgk::Profiler prof;
+  struct Rec { int stage; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t open_ev[CG_STAGE_COUNT] = {};
+
+  cudaEvent_t get_event() {
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  static void mark_cb(void* self, int stage, bool begin, cudaStream_t s) {
+    cg_ctx* c = static_cast<cg_ctx*>(self);
+    cudaEvent_t e = c->get_event();
+    cudaEventRecord(e, s);
+    if (begin) c->open_ev[stage] = e;
+    else c->recs.push_back({stage, c->open_ev[stage], e});
+  }
 
   uint64_t* d(uint64_t off) { return reinterpret_cast<uint64_t*>(ws + off); }
 
@@ -223,6 +243,9 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
   int per_sm = cgk::persistent_blocks_check();
   c->launch.persist_blocks = prop.multiProcessorCount * std::max(per_sm, 1);
   c->launch.counter = &c->launches;
+  c->prof.mark = &cg_ctx::mark_cb;
+  c->prof.self = c;
+  c->launch.prof = &c->prof;
   if (cudaMallocHost(&c->h_table, 5 * cfg->max_allocs * 8) != cudaSuccess ||
       cudaMallocHost(&c->h_marks, std::min<uint64_t>(cfg->max_descs, kMarkRun) * sizeof(cg_mark)) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->staged, cudaEventDisableTiming) != cudaSuccess) {
@@ -247,6 +270,8 @@ cg_status cg_ctx_destroy(cg_ctx* c) {
     cudaEventSynchronize(c->staged);
     cudaEventDestroy(c->staged);
   }
+  for (auto& r : c->recs) { c->pool.push_back(r.a); c->pool.push_back(r.b); }
+  for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
   if (c->h_table) cudaFreeHost(c->h_table);
   if (c->h_marks) cudaFreeHost(c->h_marks);
   delete c;
@@ -256,6 +281,37 @@ cg_status cg_ctx_destroy(cg_ctx* c) {
 const char* cg_last_error(const cg_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 uint64_t cg_kernel_launches(const cg_ctx* c) { return c ? c->launches : 0; }
+
+cg_status cg_profile_begin(cg_ctx* c) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  c->prof.on = true;
+  return CG_OK;
+}
+
+cg_status cg_profile_end(cg_ctx* c, double* ms, uint64_t* launches) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  DeviceGuard g(c->cfg.device);
+  c->prof.on = false;
+  double acc[CG_STAGE_COUNT] = {};
+  uint64_t cnt[CG_STAGE_COUNT] = {};
+  cg_status st = CG_OK;
+  for (auto& r : c->recs) {
+    cudaError_t e = cudaEventSynchronize(r.b);
+    float t = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.a, r.b);
+    if (e != cudaSuccess) st = c->cuda(e, "profile events");
+    acc[r.stage] += t;
+    cnt[r.stage] += 1;
+    c->pool.push_back(r.a);
+    c->pool.push_back(r.b);
+  }
+  c->recs.clear();
+  for (int k = 0; k < CG_STAGE_COUNT; ++k) {
+    if (ms) ms[k] = acc[k];
+    if (launches) launches[k] = cnt[k];
+  }
+  return st;
+}
 
 static bool in_window(const cg_ctx* c, uint64_t addr, uint64_t len) {
   return addr >= c->sv.wb && len <= c->sv.we - c->sv.wb && addr - c->sv.wb <= (c->sv.we - c->sv.wb) - len;
