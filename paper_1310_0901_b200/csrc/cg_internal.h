@@ -43,6 +43,8 @@ struct Plan {
   uint64_t* P;            // [n + 1]
   uint64_t* bsum;         // [nblocks + 1]
   uint32_t* chunk_first;  // [max_chunks]
+  void* meta;             // [n] ScanMeta (check plans only)
+  uint32_t* counter;      // dynamic group counter of the scan
   uint64_t max_chunks;
   uint64_t t_min;
 };
@@ -57,6 +59,7 @@ struct Profiler {
 struct Launch {
   int num_sms;
   int persist_blocks;     // persistent grid for the chunked kernels
+  int scan_blocks;        // persistent grid of the TMA-ring scan
   uint64_t* counter;      // host counter of kernel launches
   Profiler* prof;
   void stage(int st, bool begin, cudaStream_t s) const {
@@ -67,6 +70,8 @@ struct Launch {
 constexpr int kScanTile = 2048;   // items per block of the prefix scan
 
 uint64_t scan_blocks(uint64_t n);
+int persistent_blocks(int which);   // 0: k_check_scan, 1: k_apply (per SM)
+size_t scan_meta_bytes();
 
 cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out,
                          const Table& t, const ShadowView& sv, const Plan& p, uint32_t err_mask,

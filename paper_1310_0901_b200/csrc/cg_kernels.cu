@@ -177,6 +177,11 @@ __device__ __forceinline__ Norm normalize(const cg_copy_desc& d) {
   return n;
 }
 
+// packed per-descriptor metadata written by k_check_prep for the scan
+struct __align__(16) ScanMeta {
+  uint64_t hstart, hpitch, W, info;   // info: nbytes | kind << 40 | host << 42 | flags << 48
+};
+
 // ---------------------------------------------------------------------------
 // a3: batched interval search (lifetime-stamped, base-sorted table)
 // ---------------------------------------------------------------------------
@@ -227,7 +232,8 @@ __device__ __forceinline__ uint64_t check_host_units(const Norm& nm) {
 
 __global__ void __launch_bounds__(kThreads) k_check_prep(const cg_copy_desc* __restrict__ descs,
                                                          uint64_t n, Table t, cg_verdict* __restrict__ out,
-                                                         uint64_t* __restrict__ weight) {
+                                                         uint64_t* __restrict__ weight,
+                                                         ScanMeta* __restrict__ meta) {
   extern __shared__ uint64_t s_split[];
   load_splitters(t, s_split);
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -269,6 +275,12 @@ __global__ void __launch_bounds__(kThreads) k_check_prep(const cg_copy_desc* __r
     v.status = 0;
     out[i] = v;
     weight[i] = kItemCost + check_host_units(nm);
+    ScanMeta m;
+    m.hstart = nm.hstart;
+    m.hpitch = nm.hpitch;
+    m.W = nm.W;
+    m.info = nm.nbytes | ((uint64_t)(nm.kind & 3u) << 40) | ((uint64_t)nm.host << 42) | ((uint64_t)flags << 48);
+    meta[i] = m;
   }
 }
 
@@ -399,100 +411,430 @@ __global__ void __launch_bounds__(kThreads) k_plan(const uint64_t* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------
-// a4: the host shadow scan
+// a4: the host shadow scan -- one TMA bulk-copy ring per warp
 // ---------------------------------------------------------------------------
+// Work: equal-weight groups of the prefix-summed descriptor weights, handed
+// out dynamically (one atomic per group).  Inside a group a warp walks its
+// descriptors in order; a warp-uniform generator cuts every descriptor's host
+// range into row segments (R-11), clips them to the window (bytes outside are
+// unaddressable, R-15) and to this GPU's shard, and cuts the shard part into
+// tiles that never cross a 4 KiB (HtoD: V bytes) or 32 KiB (DtoH: host bytes
+// whose A bits fill 4 KiB) boundary.  Lane 0 stages each tile with
+// cp.async.bulk (V and/or A, 128-byte aligned supersets) into the next ring
+// slot and arms the slot's mbarrier with the byte count; the warp consumes the
+// slots in order from shared memory while kStages-1 later tiles are in flight.
+// The descriptor metadata the generator needs comes from a 32-descriptor
+// register window (one coalesced load per 32 descriptors).
+constexpr int kRingWarps = 4;
+constexpr int kStages = 4;
+constexpr uint32_t kTileV = 4096;      // HtoD: V bytes per tile
+constexpr uint32_t kTileA = kTileV / 8;
+constexpr uint32_t kDtohBlock = 32768; // DtoH: host bytes per tile (4 KiB of A)
+constexpr uint32_t kTileData = 1, kTileHtod = 2, kTileEnd = 4, kTileWhole = 8;
+
+struct __align__(16) TileInfo {
+  uint64_t ob;        // logical offset of staged host byte 0
+  uint64_t pend_fu;   // END tiles: first unaddressable offset found analytically
+  uint32_t d;         // descriptor
+  uint32_t flags;
+  uint32_t q0, q1;    // valid host bytes [q0, q1) relative to the staged base
+};
+
+struct WarpRing {
+  uint8_t data[kStages][kTileV + kTileA];
+  TileInfo info[kStages];
+  uint64_t bar[kStages];
+};
+constexpr size_t kScanSmem = sizeof(WarpRing) * kRingWarps;
+
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 struct Partial {
   uint64_t fu, fd, cnt;   // first unaddressable, first undefined, undefined count
 };
 
-// HtoD: V and A over shard-relative bytes [q0, q1); logical offset of q0 is ob.
-__device__ __forceinline__ void scan_vbits(const ShadowView& sv, uint64_t q0, uint64_t q1, uint64_t ob,
-                                           Partial& p) {
+__device__ __forceinline__ void finalize_fields(uint32_t& flags, uint32_t& status, uint64_t fu, uint64_t cnt,
+                                                uint32_t err_mask) {
+  if (fu != kNone) flags |= CG_F_HOST_UNADDRESSABLE;
+  if (cnt != 0 && fu == kNone) flags |= CG_F_HOST_UNDEFINED;
+  status = (flags & err_mask) ? (uint32_t)CG_ERR_INVALID_VALUE : (uint32_t)CG_OK;
+}
+
+// HtoD tile: V bytes and their A bits, host bytes [q0, q1) of the staged tile
+__device__ __forceinline__ void consume_htod(const uint8_t* st, uint32_t q0, uint32_t q1, uint64_t ob,
+                                             Partial& p) {
   const int lane = threadIdx.x & 31;
-  const uint64_t k0 = q0 >> 4, k1 = (q1 + 15) >> 4;
-  const uint4* V4 = reinterpret_cast<const uint4*>(sv.V);
-  const uint16_t* A2 = reinterpret_cast<const uint16_t*>(sv.A);
-  for (uint64_t kb = k0; kb < k1; kb += 32 * kUnroll) {
-    uint4 v[kUnroll];
-    uint32_t a[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const uint64_t k = kb + (uint64_t)u * 32 + lane;
-      if (k < k1) {
-        v[u] = ldg_stream(V4 + k);
-        a[u] = ldg_u16(A2 + k);
+  const uint4* V4 = reinterpret_cast<const uint4*>(st);
+  const uint16_t* A2 = reinterpret_cast<const uint16_t*>(st + kTileV);
+  const uint32_t g1 = (q1 + 15) >> 4;
+#pragma unroll 4
+  for (uint32_t g = (q0 >> 4) + lane; g < g1; g += 32) {
+    const uint4 v = V4[g];
+    const uint32_t a = A2[g];
+    const uint32_t qb = g << 4;
+    const bool whole = qb >= q0 && qb + 16 <= q1;
+    if (!whole || (v.x | v.y | v.z | v.w) != 0 || a != 0xFFFFu) {
+      const uint32_t m = range_mask(qb, 16, q0, q1);
+      const uint32_t bad = ~a & m;
+      const uint32_t und = nz16(v) & a & m;
+      if (bad) p.fu = umin64(p.fu, ob + qb + (__ffs(bad) - 1));
+      if (und) {
+        p.fd = umin64(p.fd, ob + qb + (__ffs(und) - 1));
+        p.cnt += __popc(und);
       }
     }
+  }
+}
+
+// DtoH tile: A bits only (one 16-byte A vector = 128 host bytes per lane step)
+__device__ __forceinline__ void consume_dtoh(const uint8_t* st, uint32_t q0, uint32_t q1, uint64_t ob,
+                                             Partial& p) {
+  const int lane = threadIdx.x & 31;
+  const uint4* A16 = reinterpret_cast<const uint4*>(st);
+  const uint32_t g1 = (q1 + 127) >> 7;
+#pragma unroll 2
+  for (uint32_t g = (q0 >> 7) + lane; g < g1; g += 32) {
+    const uint4 a = A16[g];
+    const uint32_t qb = g << 7;
+    const bool whole = qb >= q0 && qb + 128 <= q1;
+    if (!whole || (a.x & a.y & a.z & a.w) != 0xffffffffu) {
+      const uint32_t w[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const uint64_t k = kb + (uint64_t)u * 32 + lane;
-      if (k < k1) {
-        const uint64_t qb = k << 4;
-        const bool whole = qb >= q0 && qb + 16 <= q1;
-        if (!whole || (v[u].x | v[u].y | v[u].z | v[u].w) != 0 || a[u] != 0xFFFFu) {
-          const uint32_t m = range_mask(qb, 16, q0, q1);
-          const uint32_t bad = ~a[u] & m;
-          const uint32_t und = nz16(v[u]) & a[u] & m;
-          if (bad) p.fu = umin64(p.fu, ob + (qb + (__ffs(bad) - 1) - q0));
-          if (und) {
-            p.fd = umin64(p.fd, ob + (qb + (__ffs(und) - 1) - q0));
-            p.cnt += __popc(und);
-          }
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t gb = qb + 32 * j;
+        if (gb + 32 <= q0 || gb >= q1) continue;
+        const uint32_t bad = ~w[j] & range_mask(gb, 32, q0, q1);
+        if (bad) {
+          p.fu = umin64(p.fu, ob + gb + (__ffs(bad) - 1));
+          break;
         }
       }
     }
   }
 }
 
-// DtoH: A only, 128 host bytes (one 16-byte A vector) per lane and step.
-__device__ __forceinline__ void scan_abits(const ShadowView& sv, uint64_t q0, uint64_t q1, uint64_t ob,
-                                           Partial& p) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t k0 = q0 >> 7, k1 = (q1 + 127) >> 7;
-  const uint4* A16 = reinterpret_cast<const uint4*>(sv.A);
-  for (uint64_t kb = k0; kb < k1; kb += 32 * kUnroll) {
-    uint4 a[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const uint64_t k = kb + (uint64_t)u * 32 + lane;
-      if (k < k1) a[u] = ldg_stream(A16 + k);
+// Warp-uniform tile generator (every lane runs it identically).
+struct TileGen {
+  // inputs
+  const ScanMeta* meta;
+  const uint64_t* P;
+  const uint32_t* chunk_first;
+  uint32_t* counter;
+  uint64_t n, T, nchunks, total;
+  uint64_t wb, we, sb, se;
+  // group state
+  uint64_t w0, w1, g_pending;   // g_pending valid in lane 0
+  bool in_group;
+  // descriptor window (lane i holds descriptor wbase + i)
+  uint64_t wbase;
+  uint64_t m_hstart, m_hpitch, m_W, m_info, m_ps, m_pe;
+  // current descriptor / piece
+  uint64_t d, hstart, hpitch, W, info;
+  bool have_piece, whole, htod;
+  uint64_t o, hi, r, col, pend_fu;
+  // current segment (shard part)
+  bool seg_active;
+  uint64_t cur, seg_end, seg_ob;
+
+  __device__ __forceinline__ void load_window(uint64_t base) {
+    const int lane = threadIdx.x & 31;
+    wbase = base;
+    const uint64_t i = base + lane;
+    if (i < n) {
+      const ScanMeta m = meta[i];
+      m_hstart = m.hstart;
+      m_hpitch = m.hpitch;
+      m_W = m.W;
+      m_info = m.info;
+      m_ps = P[i];
+      m_pe = P[i + 1];
+    } else {
+      m_ps = m_pe = ~0ull;
     }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const uint64_t k = kb + (uint64_t)u * 32 + lane;
-      if (k < k1) {
-        const uint64_t qb = k << 7;
-        const bool whole = qb >= q0 && qb + 128 <= q1;
-        if (!whole || (a[u].x & a[u].y & a[u].z & a[u].w) != 0xffffffffu) {
-          const uint32_t w[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint64_t gb = qb + 32 * j;
-            if (gb + 32 <= q0 || gb >= q1) continue;
-            const uint32_t bad = ~w[j] & range_mask(gb, 32, q0, q1);
-            if (bad) {
-              p.fu = umin64(p.fu, ob + (gb + (__ffs(bad) - 1) - q0));
-              break;
-            }
-          }
+  }
+
+  // next group from the dynamic counter; false when the work is exhausted
+  __device__ __forceinline__ bool next_group() {
+    const int lane = threadIdx.x & 31;
+    const uint64_t g = __shfl_sync(kFull, g_pending, 0);
+    if (g >= nchunks) return false;
+    if (lane == 0) g_pending = atomicAdd(counter, 1u);
+    w0 = g * T;
+    w1 = umin64(w0 + T, total);
+    d = chunk_first[g];
+    if (d < wbase || d >= wbase + 32) load_window(d);
+    in_group = true;
+    return true;
+  }
+
+  // start the piece of descriptor d in the current group; false if d is past it
+  __device__ __forceinline__ bool start_piece() {
+    if (d >= n) return false;
+    if (d >= wbase + 32) load_window(d);
+    const int src = (int)(d - wbase);
+    const uint64_t pd = __shfl_sync(kFull, m_ps, src);
+    if (pd >= w1) return false;
+    const uint64_t pd1 = __shfl_sync(kFull, m_pe, src);
+    hstart = __shfl_sync(kFull, m_hstart, src);
+    hpitch = __shfl_sync(kFull, m_hpitch, src);
+    W = __shfl_sync(kFull, m_W, src);
+    info = __shfl_sync(kFull, m_info, src);
+    const uint64_t nbytes = info & ((1ull << 40) - 1);
+    const uint32_t kind = (uint32_t)(info >> 40) & 3u;
+    const bool host = (info >> 42) & 1u;
+    htod = kind == CG_HTOD;
+    whole = pd >= w0 && pd1 <= w1;
+    uint64_t a = umax64(w0, pd) - pd, b = umin64(w1, pd1) - pd;
+    a = a > kItemCost ? a - kItemCost : 0;
+    b = b > kItemCost ? b - kItemCost : 0;
+    uint64_t lo = a;
+    hi = b;
+    if (!htod) {
+      lo = a << 3;
+      hi = umin64(b << 3, nbytes);
+    }
+    if (!host || lo >= hi) {
+      o = hi = 0;
+    } else {
+      o = lo;
+      r = lo / W;
+      col = lo - r * W;
+    }
+    pend_fu = kNone;
+    seg_active = false;
+    have_piece = true;
+    return true;
+  }
+
+  // Fills t (and the staged global offset qa) with the next tile; false when
+  // the warp has no more work.
+  __device__ __forceinline__ bool next(TileInfo& t, uint64_t& qa) {
+    while (true) {
+      if (!have_piece) {
+        if (!in_group) {
+          if (!next_group()) return false;
+        }
+        if (!start_piece()) {
+          in_group = false;
+          continue;
         }
       }
+      if (!seg_active) {
+        if (o >= hi) {   // piece without (further) shard bytes: a data-less END tile
+          t.ob = 0;
+          t.pend_fu = pend_fu;
+          t.d = (uint32_t)d;
+          t.flags = kTileEnd | (whole ? kTileWhole : 0u) | (htod ? kTileHtod : 0u);
+          t.q0 = t.q1 = 0;
+          qa = 0;
+          have_piece = false;
+          ++d;
+          return true;
+        }
+        const uint64_t len = umin64(W - col, hi - o);
+        const uint64_t x = hstart + r * hpitch + col;
+        const uint64_t so = o;
+        o += len;
+        col += len;
+        if (col == W) {
+          ++r;
+          col = 0;
+        }
+        if (x < wb) pend_fu = umin64(pend_fu, so);
+        if (x + len > we) pend_fu = umin64(pend_fu, so + (umax64(x, we) - x));
+        const uint64_t y0 = umax64(x, sb), y1 = umin64(x + len, se);
+        if (y0 >= y1) continue;
+        cur = y0 - sb;
+        seg_end = y1 - sb;
+        seg_ob = so - x + sb;   // logical offset of shard byte q is seg_ob + q (mod 2^64)
+        seg_active = true;
+      }
+      const uint64_t blk = htod ? kTileV : kDtohBlock;
+      const uint64_t tq0 = cur, tq1 = umin64(seg_end, (cur & ~(blk - 1)) + blk);
+      qa = tq0 & ~127ull;
+      t.ob = seg_ob + qa;
+      t.d = (uint32_t)d;
+      t.flags = kTileData | (htod ? kTileHtod : 0u);
+      t.q0 = (uint32_t)(tq0 - qa);
+      t.q1 = (uint32_t)(tq1 - qa);
+      cur = tq1;
+      if (cur >= seg_end) {
+        seg_active = false;
+        if (o >= hi) {   // last segment of the piece: this tile ends it
+          t.flags |= kTileEnd | (whole ? kTileWhole : 0u);
+          have_piece = false;
+          ++d;
+        }
+      }
+      t.pend_fu = pend_fu;
+      return true;
+    }
+  }
+};
+
+__device__ __forceinline__ void issue_tile(WarpRing& ring, int s, const TileInfo& t, uint64_t qa,
+                                           const ShadowView& sv, uint64_t policy) {
+  if ((threadIdx.x & 31) == 0) {
+    ring.info[s] = t;
+    if (t.flags & kTileData) {
+      const uint32_t span = (t.q1 + 127u) & ~127u;   // staged host bytes (multiple of 128)
+      if (t.flags & kTileHtod) {
+        mbar_arrive_tx(&ring.bar[s], span + span / 8);
+        bulk_g2s(ring.data[s], sv.V + qa, span, &ring.bar[s], policy);
+        bulk_g2s(ring.data[s] + kTileV, sv.A + qa / 8, span / 8, &ring.bar[s], policy);
+      } else {
+        mbar_arrive_tx(&ring.bar[s], span / 8);
+        bulk_g2s(ring.data[s], sv.A + qa / 8, span / 8, &ring.bar[s], policy);
+      }
+    } else {
+      mbar_arrive(&ring.bar[s]);
     }
   }
 }
 
-// One contiguous physical segment [x, x+len) whose first byte has logical
-// offset o.  Bytes outside the global window are unaddressable (R-15); only the
-// shard's bytes are read.
-__device__ __forceinline__ void scan_segment(const ShadowView& sv, bool htod, uint64_t x, uint64_t len,
-                                             uint64_t o, Partial& p) {
-  const uint64_t end = x + len;
-  if (x < sv.wb) p.fu = umin64(p.fu, o);
-  if (end > sv.we) p.fu = umin64(p.fu, o + (umax64(x, sv.we) - x));
-  const uint64_t y0 = umax64(x, sv.sb), y1 = umin64(end, sv.se);
-  if (y0 < y1) {
-    if (htod) scan_vbits(sv, y0 - sv.sb, y1 - sv.sb, o + (y0 - x), p);
-    else scan_abits(sv, y0 - sv.sb, y1 - sv.sb, o + (y0 - x), p);
+__global__ void __launch_bounds__(kRingWarps * 32) k_check_scan(
+    const ScanMeta* __restrict__ meta, uint64_t n, const uint64_t* __restrict__ P,
+    const uint32_t* __restrict__ chunk_first, uint32_t* counter, uint64_t t_min, uint64_t max_chunks,
+    ShadowView sv, cg_verdict* __restrict__ out, uint32_t err_mask) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  WarpRing& ring = reinterpret_cast<WarpRing*>(smem)[wid];
+  const ChunkGeom geo = chunk_geom(P, n, t_min, max_chunks);
+  if (lane == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&ring.bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const uint64_t policy = evict_first_policy();
+
+  TileGen gen;
+  gen.meta = meta;
+  gen.P = P;
+  gen.chunk_first = chunk_first;
+  gen.counter = counter;
+  gen.n = n;
+  gen.T = geo.T;
+  gen.nchunks = geo.nchunks;
+  gen.total = geo.total;
+  gen.wb = sv.wb;
+  gen.we = sv.we;
+  gen.sb = sv.sb;
+  gen.se = sv.se;
+  gen.g_pending = lane == 0 ? atomicAdd(counter, 1u) : 0;
+  gen.in_group = false;
+  gen.have_piece = false;
+  gen.seg_active = false;
+  gen.wbase = ~0ull >> 1;   // empty window
+  gen.d = 0;
+
+  // prologue: fill the ring
+  int filled = 0;
+  for (; filled < kStages; ++filled) {
+    TileInfo t;
+    uint64_t qa;
+    if (!gen.next(t, qa)) break;
+    issue_tile(ring, filled, t, qa, sv, policy);
+  }
+  uint32_t phase = 0;   // bit s = parity to wait for on slot s
+  Partial p{kNone, kNone, 0};
+  for (int s = 0, left = filled; left > 0; s = (s + 1 == kStages) ? 0 : s + 1) {
+    mbar_wait(&ring.bar[s], (phase >> s) & 1u);
+    phase ^= 1u << s;
+    const TileInfo t = ring.info[s];
+    if (t.flags & kTileData) {
+      if (t.flags & kTileHtod) consume_htod(ring.data[s], t.q0, t.q1, t.ob, p);
+      else consume_dtoh(ring.data[s], t.q0, t.q1, t.ob, p);
+    }
+    if (t.flags & kTileEnd) {
+      p.fu = umin64(p.fu, t.pend_fu);
+      if (__any_sync(kFull, p.fu != kNone || p.fd != kNone || p.cnt != 0)) {
+        p.fu = warp_min(p.fu);
+        p.fd = warp_min(p.fd);
+        p.cnt = warp_sum(p.cnt);
+      }
+      if (lane == 0) {
+        cg_verdict* v = out + t.d;
+        if (t.flags & kTileWhole) {
+          const uint32_t pflags = (uint32_t)(__ldg(&meta[t.d].info) >> 48);
+          uint32_t flags = pflags, status;
+          finalize_fields(flags, status, p.fu, p.cnt, err_mask);
+          v->first_unaddr = p.fu;
+          v->first_undef = p.fd;
+          v->undef_count = p.cnt;
+          v->flags = flags;
+          v->status = status;
+        } else {
+          if (p.fu != kNone) atomicMin(reinterpret_cast<unsigned long long*>(&v->first_unaddr), p.fu);
+          if (p.fd != kNone) atomicMin(reinterpret_cast<unsigned long long*>(&v->first_undef), p.fd);
+          if (p.cnt) atomicAdd(reinterpret_cast<unsigned long long*>(&v->undef_count), p.cnt);
+        }
+      }
+      p = Partial{kNone, kNone, 0};
+    }
+    __syncwarp();
+    // refill this slot: generic-proxy reads of the slot are ordered before the
+    // async-proxy writes of the next bulk copy
+    TileInfo nt;
+    uint64_t qa;
+    if (gen.next(nt, qa)) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue_tile(ring, s, nt, qa, sv, policy);
+    } else {
+      --left;
+    }
+  }
+}
+
+// a5 for descriptors split across groups
+__global__ void __launch_bounds__(kThreads) k_finalize_split(uint64_t n, const uint64_t* __restrict__ P,
+                                                             uint64_t t_min, uint64_t max_chunks,
+                                                             cg_verdict* __restrict__ out, uint32_t err_mask) {
+  const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
+  for (uint64_t d = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; d < n;
+       d += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t pd = P[d], pd1 = P[d + 1];
+    if (pd1 == pd || pd / g.T == (pd1 - 1) / g.T) continue;
+    cg_verdict* v = out + d;
+    uint32_t flags = v->flags, status;
+    finalize_fields(flags, status, v->first_unaddr, v->undef_count, err_mask);
+    v->flags = flags;
+    v->status = status;
   }
 }
 
@@ -512,87 +854,6 @@ __device__ __forceinline__ void for_rows(const Norm& nm, uint64_t lo, uint64_t h
   }
 }
 
-__device__ __forceinline__ void finalize_fields(uint32_t& flags, uint32_t& status, uint64_t fu, uint64_t cnt,
-                                                uint32_t err_mask) {
-  if (fu != kNone) flags |= CG_F_HOST_UNADDRESSABLE;
-  if (cnt != 0 && fu == kNone) flags |= CG_F_HOST_UNDEFINED;
-  status = (flags & err_mask) ? (uint32_t)CG_ERR_INVALID_VALUE : (uint32_t)CG_OK;
-}
-
-__global__ void __launch_bounds__(kThreads) k_check_scan(const cg_copy_desc* __restrict__ descs, uint64_t n,
-                                                         const uint64_t* __restrict__ P,
-                                                         const uint32_t* __restrict__ chunk_first,
-                                                         uint64_t t_min, uint64_t max_chunks, ShadowView sv,
-                                                         cg_verdict* __restrict__ out, uint32_t err_mask) {
-  const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
-  const int lane = threadIdx.x & 31;
-  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t c = gw; c < g.nchunks; c += nw) {
-    const uint64_t w0 = c * g.T, w1 = umin64(w0 + g.T, g.total);
-    for (uint64_t d = chunk_first[c]; d < n; ++d) {
-      const uint64_t pd = P[d];
-      if (pd >= w1) break;
-      const uint64_t pd1 = P[d + 1];
-      const cg_copy_desc dd = descs[d];
-      const Norm nm = normalize(dd);
-      Partial p{kNone, kNone, 0};
-      if (nm.host && nm.nbytes) {
-        // this chunk's share of the descriptor's weight interval, minus the
-        // kItemCost prefix, mapped to logical host bytes
-        uint64_t a = umax64(w0, pd) - pd, b = umin64(w1, pd1) - pd;
-        a = a > kItemCost ? a - kItemCost : 0;
-        b = b > kItemCost ? b - kItemCost : 0;
-        uint64_t lo = a, hi = b;
-        if (nm.kind == CG_DTOH) {
-          lo = a << 3;
-          hi = umin64(b << 3, nm.nbytes);
-        }
-        const bool htod = nm.kind == CG_HTOD;
-        if (lo < hi)
-          for_rows(nm, lo, hi, [&](uint64_t x, uint64_t len, uint64_t o) { scan_segment(sv, htod, x, len, o, p); });
-      }
-      if (__any_sync(kFull, p.fu != kNone || p.fd != kNone || p.cnt != 0)) {
-        p.fu = warp_min(p.fu);
-        p.fd = warp_min(p.fd);
-        p.cnt = warp_sum(p.cnt);
-      }
-      if (lane == 0) {
-        cg_verdict* v = out + d;
-        if (pd >= w0 && pd1 <= w1) {          // the whole descriptor is in this chunk
-          uint32_t flags = v->flags, status;
-          finalize_fields(flags, status, p.fu, p.cnt, err_mask);
-          v->first_unaddr = p.fu;
-          v->first_undef = p.fd;
-          v->undef_count = p.cnt;
-          v->flags = flags;
-          v->status = status;
-        } else {                              // split: merge, finalize later
-          if (p.fu != kNone) atomicMin(reinterpret_cast<unsigned long long*>(&v->first_unaddr), p.fu);
-          if (p.fd != kNone) atomicMin(reinterpret_cast<unsigned long long*>(&v->first_undef), p.fd);
-          if (p.cnt) atomicAdd(reinterpret_cast<unsigned long long*>(&v->undef_count), p.cnt);
-        }
-      }
-    }
-  }
-}
-
-// a5 for descriptors split across chunks
-__global__ void __launch_bounds__(kThreads) k_finalize_split(uint64_t n, const uint64_t* __restrict__ P,
-                                                             uint64_t t_min, uint64_t max_chunks,
-                                                             cg_verdict* __restrict__ out, uint32_t err_mask) {
-  const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
-  for (uint64_t d = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; d < n;
-       d += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t pd = P[d], pd1 = P[d + 1];
-    if (pd1 == pd || pd / g.T == (pd1 - 1) / g.T) continue;
-    cg_verdict* v = out + d;
-    uint32_t flags = v->flags, status;
-    finalize_fields(flags, status, v->first_unaddr, v->undef_count, err_mask);
-    v->flags = flags;
-    v->status = status;
-  }
-}
 
 // ---------------------------------------------------------------------------
 // a6: DtoH apply
@@ -776,17 +1037,19 @@ cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_
                          const ShadowView& sv, const Plan& p, uint32_t err_mask, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   const size_t smem = (size_t)t.nsplit * sizeof(uint64_t);
+  ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
   L.stage(CG_STAGE_CHECK_PREP, true, s);
-  k_check_prep<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, smem, s>>>(d, n, t, out, p.weight);
+  k_check_prep<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, smem, s>>>(d, n, t, out, p.weight, meta);
   *L.counter += 1;
   L.stage(CG_STAGE_CHECK_PREP, false, s);
   L.stage(CG_STAGE_CHECK_PLAN, true, s);
   cudaError_t e = plan(L, n, p, s);
   if (e != cudaSuccess) return e;
   L.stage(CG_STAGE_CHECK_PLAN, false, s);
+  cudaMemsetAsync(p.counter, 0, sizeof(uint32_t), s);
   L.stage(CG_STAGE_CHECK_SCAN, true, s);
-  k_check_scan<<<L.persist_blocks, kThreads, 0, s>>>(d, n, p.P, p.chunk_first, p.t_min, p.max_chunks, sv, out,
-                                                     err_mask);
+  k_check_scan<<<L.scan_blocks, kRingWarps * 32, kScanSmem, s>>>(meta, n, p.P, p.chunk_first, p.counter,
+                                                                 p.t_min, p.max_chunks, sv, out, err_mask);
   L.stage(CG_STAGE_CHECK_SCAN, false, s);
   L.stage(CG_STAGE_CHECK_FINAL, true, s);
   k_finalize_split<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(n, p.P, p.t_min, p.max_chunks,
@@ -857,10 +1120,17 @@ cudaError_t leak_sweep(const Launch& L, const Table& t, const Plan& p, cg_alloc_
   return cudaGetLastError();
 }
 
-int persistent_blocks_check() {
+int persistent_blocks(int which) {
   int b = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_check_scan, kThreads, 0);
+  if (which == 0) {
+    cudaFuncSetAttribute(k_check_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_check_scan, kRingWarps * 32, kScanSmem);
+  } else {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_apply, kThreads, 0);
+  }
   return b;
 }
+
+size_t scan_meta_bytes() { return sizeof(ScanMeta); }
 
 }  // namespace cgk

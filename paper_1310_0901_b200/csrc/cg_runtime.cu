@@ -19,14 +19,11 @@
 #include "cg.h"
 #include "cg_internal.h"
 
-namespace cgk {
-int persistent_blocks_check();
-}
 
 namespace {
 
 constexpr uint64_t kAlign = 256;
-constexpr uint64_t kChunkMin = 16 * 1024;        // t_min of the chunk plans (weight units)
+constexpr uint64_t kChunkMin = 128 * 1024;       // t_min of the chunk plans (weight units)
 constexpr uint64_t kMarkRun = 1u << 20;          // marks uploaded per run
 
 uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
@@ -36,7 +33,7 @@ struct Entry {
 };
 
 struct Layout {
-  uint64_t table, weight, P, bsum, chunk, marks, flags, leaks, desc_stage, verdict_stage, total;
+  uint64_t table, weight, P, bsum, chunk, meta, marks, flags, leaks, desc_stage, verdict_stage, total;
   uint64_t max_items, max_chunks;
 };
 
@@ -68,6 +65,7 @@ Layout layout_of(const cg_config* c) {
   L.P = take((L.max_items + 1) * 8);
   L.bsum = take((cgk::scan_blocks(L.max_items) + 1) * 8);
   L.chunk = take(L.max_chunks * 4);
+  L.meta = take(c->max_descs * cgk::scan_meta_bytes());
   L.marks = take(std::min<uint64_t>(c->max_descs, kMarkRun) * sizeof(cg_mark));
   L.flags = take(256);
   L.leaks = take(c->max_allocs * sizeof(cg_alloc_record));
@@ -152,6 +150,8 @@ struct cg_ctx {
     p.P = d(lay.P);
     p.bsum = d(lay.bsum);
     p.chunk_first = reinterpret_cast<uint32_t*>(ws + lay.chunk);
+    p.meta = ws + lay.meta;
+    p.counter = reinterpret_cast<uint32_t*>(ws + lay.flags + 128);
     p.max_chunks = lay.max_chunks;
     p.t_min = kChunkMin;
     return p;
@@ -240,8 +240,8 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
     return CG_ERR_CUDA;
   }
   c->launch.num_sms = prop.multiProcessorCount;
-  int per_sm = cgk::persistent_blocks_check();
-  c->launch.persist_blocks = prop.multiProcessorCount * std::max(per_sm, 1);
+  c->launch.persist_blocks = prop.multiProcessorCount * std::max(cgk::persistent_blocks(1), 1);
+  c->launch.scan_blocks = prop.multiProcessorCount * std::max(cgk::persistent_blocks(0), 1);
   c->launch.counter = &c->launches;
   c->prof.mark = &cg_ctx::mark_cb;
   c->prof.self = c;
