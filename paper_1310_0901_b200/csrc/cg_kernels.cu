@@ -279,7 +279,9 @@ __global__ void __launch_bounds__(kThreads) k_check_prep(const cg_copy_desc* __r
     m.hstart = nm.hstart;
     m.hpitch = nm.hpitch;
     m.W = nm.W;
-    m.info = nm.nbytes | ((uint64_t)(nm.kind & 3u) << 40) | ((uint64_t)nm.host << 42) | ((uint64_t)flags << 48);
+    const bool contig = d.height == 1 || d.width == nm.hpitch;
+    m.info = nm.nbytes | ((uint64_t)(nm.kind & 3u) << 40) | ((uint64_t)nm.host << 42) | ((uint64_t)contig << 43) |
+             ((uint64_t)flags << 48);
     meta[i] = m;
   }
 }
@@ -549,28 +551,43 @@ __device__ __forceinline__ void consume_dtoh(const uint8_t* st, uint32_t q0, uin
   }
 }
 
-// Warp-uniform tile generator (every lane runs it identically).
+// Tile generator.  Descriptor bookkeeping is lane-parallel: lane i of the warp
+// owns descriptor wbase+i of a 32-descriptor window and, whenever the window or
+// the group changes, computes that descriptor's piece (its share of the
+// group's weight interval) -- for contiguous host ranges directly as a shard
+// byte range [qs, qe) plus the analytic out-of-window offset -- and finalises
+// pieces without shard bytes itself (DtoD, invalid or empty host sides,
+// ranges outside the shard).  The warp-uniform part only walks the remaining
+// descriptors (ballot/ffs over the window) and cuts their shard ranges into
+// block-aligned tiles; non-contiguous 2D pieces go row by row.
+constexpr uint32_t kPieceIn = 1, kPieceWhole = 2, kPieceHtod = 4, kPiece2D = 8, kPieceEmpty = 16;
+
 struct TileGen {
   // inputs
   const ScanMeta* meta;
   const uint64_t* P;
   const uint32_t* chunk_first;
   uint32_t* counter;
+  cg_verdict* out;
+  uint32_t err_mask;
   uint64_t n, T, nchunks, total;
   uint64_t wb, we, sb, se;
   // group state
   uint64_t w0, w1, g_pending;   // g_pending valid in lane 0
   bool in_group;
-  // descriptor window (lane i holds descriptor wbase + i)
+  // window: lane i <-> descriptor wbase + i
   uint64_t wbase;
-  uint64_t m_hstart, m_hpitch, m_W, m_info, m_ps, m_pe;
-  // current descriptor / piece
-  uint64_t d, hstart, hpitch, W, info;
-  bool have_piece, whole, htod;
-  uint64_t o, hi, r, col, pend_fu;
-  // current segment (shard part)
+  uint64_t m_x0, m_pitch, m_W, m_info, m_ps, m_pe;
+  uint64_t p_qs, p_qe, p_ob, p_fu, p_lo, p_hi;   // lane's piece in the current group
+  uint32_t p_fl;
+  // warp-uniform walk
+  uint64_t d;                   // next descriptor to look at
+  bool have_piece;              // a piece is being cut into tiles
+  uint32_t fl;
+  uint64_t cur, qend, ob, pend_fu, cd;
+  // 2D rows
   bool seg_active;
-  uint64_t cur, seg_end, seg_ob;
+  uint64_t o, hi, r, col, x0, pitch, W;
 
   __device__ __forceinline__ void load_window(uint64_t base) {
     const int lane = threadIdx.x & 31;
@@ -578,18 +595,74 @@ struct TileGen {
     const uint64_t i = base + lane;
     if (i < n) {
       const ScanMeta m = meta[i];
-      m_hstart = m.hstart;
-      m_hpitch = m.hpitch;
+      m_x0 = m.hstart;
+      m_pitch = m.hpitch;
       m_W = m.W;
       m_info = m.info;
       m_ps = P[i];
       m_pe = P[i + 1];
     } else {
+      m_info = 0;
       m_ps = m_pe = ~0ull;
     }
   }
 
-  // next group from the dynamic counter; false when the work is exhausted
+  // lane-parallel: this lane's piece in group [w0, w1); pieces without shard
+  // bytes are finalised (whole) or merged (split) right here
+  __device__ __forceinline__ void compute_pieces() {
+    const int lane = threadIdx.x & 31;
+    p_fl = 0;
+    if (!(m_ps < w1 && m_pe > w0)) return;
+    const uint64_t nbytes = m_info & ((1ull << 40) - 1);
+    const uint32_t kind = (uint32_t)(m_info >> 40) & 3u;
+    const bool host = (m_info >> 42) & 1u, contig = (m_info >> 43) & 1u;
+    const bool htod = kind == CG_HTOD;
+    uint32_t f = kPieceIn | (htod ? kPieceHtod : 0u);
+    if (m_ps >= w0 && m_pe <= w1) f |= kPieceWhole;
+    uint64_t a = umax64(w0, m_ps) - m_ps, b = umin64(w1, m_pe) - m_ps;
+    a = a > kItemCost ? a - kItemCost : 0;
+    b = b > kItemCost ? b - kItemCost : 0;
+    uint64_t lo = a, hi = b;
+    if (!htod) {
+      lo = a << 3;
+      hi = umin64(b << 3, nbytes);
+    }
+    p_fu = kNone;
+    p_qs = p_qe = 0;
+    if (!host || lo >= hi) {
+      f |= kPieceEmpty;
+    } else if (!contig) {
+      f |= kPiece2D;
+      p_lo = lo;
+      p_hi = hi;
+    } else {
+      const uint64_t x = m_x0 + lo, len = hi - lo;
+      if (x < wb) p_fu = lo;
+      else if (x + len > we) p_fu = lo + (umax64(x, we) - x);
+      const uint64_t y0 = umax64(x, sb), y1 = umin64(x + len, se);
+      if (y0 < y1) {
+        p_qs = y0 - sb;
+        p_qe = y1 - sb;
+        p_ob = lo - x + sb;   // logical offset of shard byte q is p_ob + q (mod 2^64)
+      } else {
+        f |= kPieceEmpty;
+      }
+    }
+    p_fl = f;
+    if (f & kPieceEmpty) {
+      cg_verdict* v = out + (wbase + lane);
+      if (f & kPieceWhole) {
+        uint32_t flags = (uint32_t)(m_info >> 48), status;
+        finalize_fields(flags, status, p_fu, 0, err_mask);
+        v->first_unaddr = p_fu;
+        v->flags = flags;
+        v->status = status;
+      } else if (p_fu != kNone) {
+        atomicMin(reinterpret_cast<unsigned long long*>(&v->first_unaddr), p_fu);
+      }
+    }
+  }
+
   __device__ __forceinline__ bool next_group() {
     const int lane = threadIdx.x & 31;
     const uint64_t g = __shfl_sync(kFull, g_pending, 0);
@@ -599,47 +672,64 @@ struct TileGen {
     w1 = umin64(w0 + T, total);
     d = chunk_first[g];
     if (d < wbase || d >= wbase + 32) load_window(d);
+    compute_pieces();
     in_group = true;
     return true;
   }
 
-  // start the piece of descriptor d in the current group; false if d is past it
-  __device__ __forceinline__ bool start_piece() {
-    if (d >= n) return false;
-    if (d >= wbase + 32) load_window(d);
-    const int src = (int)(d - wbase);
-    const uint64_t pd = __shfl_sync(kFull, m_ps, src);
-    if (pd >= w1) return false;
-    const uint64_t pd1 = __shfl_sync(kFull, m_pe, src);
-    hstart = __shfl_sync(kFull, m_hstart, src);
-    hpitch = __shfl_sync(kFull, m_hpitch, src);
-    W = __shfl_sync(kFull, m_W, src);
-    info = __shfl_sync(kFull, m_info, src);
-    const uint64_t nbytes = info & ((1ull << 40) - 1);
-    const uint32_t kind = (uint32_t)(info >> 40) & 3u;
-    const bool host = (info >> 42) & 1u;
-    htod = kind == CG_HTOD;
-    whole = pd >= w0 && pd1 <= w1;
-    uint64_t a = umax64(w0, pd) - pd, b = umin64(w1, pd1) - pd;
-    a = a > kItemCost ? a - kItemCost : 0;
-    b = b > kItemCost ? b - kItemCost : 0;
-    uint64_t lo = a;
-    hi = b;
-    if (!htod) {
-      lo = a << 3;
-      hi = umin64(b << 3, nbytes);
+  // advance d to the next descriptor of the group with shard work; false when
+  // the group is exhausted
+  __device__ __forceinline__ bool next_piece() {
+    const int lane = threadIdx.x & 31;
+    while (true) {
+      const uint32_t rel = (uint32_t)(d - wbase);
+      const bool live = (p_fl & kPieceIn) && !(p_fl & kPieceEmpty) && (uint32_t)lane >= rel;
+      const uint32_t m = __ballot_sync(kFull, live);
+      if (m) {
+        const int src = __ffs(m) - 1;
+        d = wbase + src;
+        fl = __shfl_sync(kFull, p_fl, src);
+        cd = d;
+        if (fl & kPiece2D) {
+          x0 = __shfl_sync(kFull, m_x0, src);
+          pitch = __shfl_sync(kFull, m_pitch, src);
+          W = __shfl_sync(kFull, m_W, src);
+          o = __shfl_sync(kFull, p_lo, src);
+          hi = __shfl_sync(kFull, p_hi, src);
+          r = o / W;
+          col = o - r * W;
+          pend_fu = kNone;
+          seg_active = false;
+        } else {
+          cur = __shfl_sync(kFull, p_qs, src);
+          qend = __shfl_sync(kFull, p_qe, src);
+          ob = __shfl_sync(kFull, p_ob, src);
+          pend_fu = __shfl_sync(kFull, p_fu, src);
+        }
+        ++d;
+        have_piece = true;
+        return true;
+      }
+      // nothing left in this window: continue in the next window if the group does
+      const bool last_in = __shfl_sync(kFull, p_fl, 31) & kPieceIn;
+      if (!last_in || wbase + 32 >= n) return false;
+      load_window(wbase + 32);
+      d = wbase;
+      compute_pieces();
     }
-    if (!host || lo >= hi) {
-      o = hi = 0;
-    } else {
-      o = lo;
-      r = lo / W;
-      col = lo - r * W;
-    }
-    pend_fu = kNone;
-    seg_active = false;
-    have_piece = true;
-    return true;
+  }
+
+  __device__ __forceinline__ void emit(TileInfo& t, uint64_t& qa) {
+    const bool htod = fl & kPieceHtod;
+    const uint64_t blk = htod ? kTileV : kDtohBlock;
+    const uint64_t tq0 = cur, tq1 = umin64(qend, (cur & ~(blk - 1)) + blk);
+    qa = tq0 & ~127ull;
+    t.ob = ob + qa;
+    t.d = (uint32_t)cd;
+    t.flags = kTileData | (htod ? kTileHtod : 0u);
+    t.q0 = (uint32_t)(tq0 - qa);
+    t.q1 = (uint32_t)(tq1 - qa);
+    cur = tq1;
   }
 
   // Fills t (and the staged global offset qa) with the next tile; false when
@@ -647,28 +737,35 @@ struct TileGen {
   __device__ __forceinline__ bool next(TileInfo& t, uint64_t& qa) {
     while (true) {
       if (!have_piece) {
-        if (!in_group) {
-          if (!next_group()) return false;
-        }
-        if (!start_piece()) {
+        if (!in_group && !next_group()) return false;
+        if (!next_piece()) {
           in_group = false;
           continue;
         }
       }
+      if (!(fl & kPiece2D)) {                       // contiguous: one shard range
+        emit(t, qa);
+        if (cur >= qend) {
+          t.flags |= kTileEnd | ((fl & kPieceWhole) ? kTileWhole : 0u);
+          have_piece = false;
+        }
+        t.pend_fu = pend_fu;
+        return true;
+      }
+      // 2D: row segments (R-11)
       if (!seg_active) {
-        if (o >= hi) {   // piece without (further) shard bytes: a data-less END tile
+        if (o >= hi) {   // no further rows: a data-less END tile
           t.ob = 0;
           t.pend_fu = pend_fu;
-          t.d = (uint32_t)d;
-          t.flags = kTileEnd | (whole ? kTileWhole : 0u) | (htod ? kTileHtod : 0u);
+          t.d = (uint32_t)cd;
+          t.flags = kTileEnd | ((fl & kPieceWhole) ? kTileWhole : 0u) | ((fl & kPieceHtod) ? kTileHtod : 0u);
           t.q0 = t.q1 = 0;
           qa = 0;
           have_piece = false;
-          ++d;
           return true;
         }
         const uint64_t len = umin64(W - col, hi - o);
-        const uint64_t x = hstart + r * hpitch + col;
+        const uint64_t x = x0 + r * pitch + col;
         const uint64_t so = o;
         o += len;
         col += len;
@@ -681,25 +778,16 @@ struct TileGen {
         const uint64_t y0 = umax64(x, sb), y1 = umin64(x + len, se);
         if (y0 >= y1) continue;
         cur = y0 - sb;
-        seg_end = y1 - sb;
-        seg_ob = so - x + sb;   // logical offset of shard byte q is seg_ob + q (mod 2^64)
+        qend = y1 - sb;
+        ob = so - x + sb;
         seg_active = true;
       }
-      const uint64_t blk = htod ? kTileV : kDtohBlock;
-      const uint64_t tq0 = cur, tq1 = umin64(seg_end, (cur & ~(blk - 1)) + blk);
-      qa = tq0 & ~127ull;
-      t.ob = seg_ob + qa;
-      t.d = (uint32_t)d;
-      t.flags = kTileData | (htod ? kTileHtod : 0u);
-      t.q0 = (uint32_t)(tq0 - qa);
-      t.q1 = (uint32_t)(tq1 - qa);
-      cur = tq1;
-      if (cur >= seg_end) {
+      emit(t, qa);
+      if (cur >= qend) {
         seg_active = false;
-        if (o >= hi) {   // last segment of the piece: this tile ends it
-          t.flags |= kTileEnd | (whole ? kTileWhole : 0u);
+        if (o >= hi) {
+          t.flags |= kTileEnd | ((fl & kPieceWhole) ? kTileWhole : 0u);
           have_piece = false;
-          ++d;
         }
       }
       t.pend_fu = pend_fu;
@@ -707,6 +795,7 @@ struct TileGen {
     }
   }
 };
+
 
 __device__ __forceinline__ void issue_tile(WarpRing& ring, int s, const TileInfo& t, uint64_t qa,
                                            const ShadowView& sv, uint64_t policy) {
@@ -745,6 +834,8 @@ __global__ void __launch_bounds__(kRingWarps * 32) k_check_scan(
 
   TileGen gen;
   gen.meta = meta;
+  gen.out = out;
+  gen.err_mask = err_mask;
   gen.P = P;
   gen.chunk_first = chunk_first;
   gen.counter = counter;
@@ -762,6 +853,7 @@ __global__ void __launch_bounds__(kRingWarps * 32) k_check_scan(
   gen.seg_active = false;
   gen.wbase = ~0ull >> 1;   // empty window
   gen.d = 0;
+  gen.p_fl = 0;
 
   // prologue: fill the ring
   int filled = 0;
