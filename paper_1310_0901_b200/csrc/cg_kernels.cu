@@ -950,20 +950,154 @@ __device__ __forceinline__ void for_rows(const Norm& nm, uint64_t lo, uint64_t h
 // ---------------------------------------------------------------------------
 // a6: DtoH apply
 // ---------------------------------------------------------------------------
+// The written host bytes of every DtoH descriptor with status OK become
+// defined: V := 0x00.  Same equal-weight dynamic groups and lane-parallel
+// descriptor window as the scan; the zeros are written by bulk asynchronous
+// copies (cp.async.bulk shared -> global, <= 4 KiB each) from a zero page in
+// shared memory, so one lane instruction writes 4 KiB; only the unaligned
+// head/tail bytes (< 16 per segment) use byte stores.
 constexpr uint64_t kApplyItemCost = 64;
+constexpr uint32_t kZeroPage = 4096;
 
 __global__ void __launch_bounds__(kThreads) k_apply_prep(const cg_copy_desc* __restrict__ descs,
                                                          const cg_verdict* __restrict__ verd, uint64_t n,
-                                                         uint64_t* __restrict__ weight) {
+                                                         uint64_t* __restrict__ weight, ScanMeta* __restrict__ meta) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t w = 0;
-    if (descs[i].kind == CG_DTOH && verd[i].status == CG_OK) {
-      const Norm nm = normalize(descs[i]);
-      if (nm.host && nm.nbytes) w = kApplyItemCost + nm.nbytes;
+    const cg_copy_desc d = descs[i];
+    if (d.kind == CG_DTOH && verd[i].status == CG_OK) {
+      const Norm nm = normalize(d);
+      if (nm.host && nm.nbytes) {
+        w = kApplyItemCost + nm.nbytes;
+        ScanMeta m;
+        m.hstart = nm.hstart;
+        m.hpitch = nm.hpitch;
+        m.W = nm.W;
+        const bool contig = d.height == 1 || d.width == nm.hpitch;
+        m.info = nm.nbytes | ((uint64_t)contig << 43);
+        meta[i] = m;
+      }
     }
     weight[i] = w;
   }
+}
+
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+
+// zero shard bytes [q0, q1) from one lane: byte stores for the unaligned
+// edges, bulk stores of the zero page for the 16-byte aligned middle
+__device__ __forceinline__ void lane_zero(uint8_t* V, uint64_t q0, uint64_t q1, const uint8_t* zeros) {
+  const uint64_t a0 = (q0 + 15) & ~15ull, a1 = q1 & ~15ull;
+  if (a0 >= a1) {
+    for (uint64_t q = q0; q < q1; ++q) V[q] = 0;
+    return;
+  }
+  for (uint64_t q = q0; q < a0; ++q) V[q] = 0;
+  for (uint64_t q = a1; q < q1; ++q) V[q] = 0;
+  for (uint64_t p = a0; p < a1; p += kZeroPage) bulk_s2g(V + p, zeros, (uint32_t)umin64(kZeroPage, a1 - p));
+}
+
+// zero [q0, q1) with the whole warp: lane j takes the 4 KiB pages j, j+32, ...
+__device__ __forceinline__ void warp_zero(uint8_t* V, uint64_t q0, uint64_t q1, const uint8_t* zeros) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t a0 = (q0 + 15) & ~15ull, a1 = q1 & ~15ull;
+  if (a0 >= a1) {
+    if (lane == 0)
+      for (uint64_t q = q0; q < q1; ++q) V[q] = 0;
+    return;
+  }
+  if (lane == 0)
+    for (uint64_t q = q0; q < a0; ++q) V[q] = 0;
+  if (lane == 1)
+    for (uint64_t q = a1; q < q1; ++q) V[q] = 0;
+  for (uint64_t p = a0 + (uint64_t)lane * kZeroPage; p < a1; p += 32ull * kZeroPage)
+    bulk_s2g(V + p, zeros, (uint32_t)umin64(kZeroPage, a1 - p));
+}
+
+__global__ void __launch_bounds__(kThreads) k_apply(const ScanMeta* __restrict__ meta, uint64_t n,
+                                                    const uint64_t* __restrict__ P,
+                                                    const uint32_t* __restrict__ chunk_first, uint32_t* counter,
+                                                    uint64_t t_min, uint64_t max_chunks, ShadowView sv) {
+  __shared__ __align__(128) uint8_t zeros[kZeroPage];
+  for (uint32_t i = threadIdx.x; i < kZeroPage / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(zeros)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  const ChunkGeom geo = chunk_geom(P, n, t_min, max_chunks);
+  const int lane = threadIdx.x & 31;
+  uint32_t gnext = lane == 0 ? atomicAdd(counter, 1u) : 0;
+  while (true) {
+    const uint64_t g = __shfl_sync(kFull, gnext, 0);
+    if (g >= geo.nchunks) break;
+    if (lane == 0) gnext = atomicAdd(counter, 1u);
+    const uint64_t w0 = g * geo.T, w1 = umin64(w0 + geo.T, geo.total);
+    for (uint64_t base = chunk_first[g];; base += 32) {
+      // lane-parallel: this lane's descriptor piece in the group
+      const uint64_t i = base + lane;
+      uint64_t ps = ~0ull, pe = ~0ull;
+      if (i < n) {
+        ps = P[i];
+        pe = P[i + 1];
+      }
+      const bool in = ps < w1 && pe > w0 && pe > ps;
+      bool small = false, big = false;
+      uint64_t qs = 0, qe = 0, lo = 0, hi = 0;
+      ScanMeta m{0, 0, 0, 0};
+      if (in) {
+        m = meta[i];
+        uint64_t a = umax64(w0, ps) - ps, b = umin64(w1, pe) - ps;
+        lo = a > kApplyItemCost ? a - kApplyItemCost : 0;
+        hi = b > kApplyItemCost ? b - kApplyItemCost : 0;
+        if (lo < hi) {
+          if ((m.info >> 43) & 1u) {
+            const uint64_t x = m.hstart + lo, y0 = umax64(x, sv.sb), y1 = umin64(x + (hi - lo), sv.se);
+            if (y0 < y1) {
+              qs = y0 - sv.sb;
+              qe = y1 - sv.sb;
+              small = qe - qs <= 2 * kZeroPage;
+              big = !small;
+            }
+          } else {
+            big = true;   // 2D: rows, whole warp
+          }
+        }
+      }
+      if (small) lane_zero(sv.V, qs, qe, zeros);
+      uint32_t todo = __ballot_sync(kFull, big);
+      while (todo) {
+        const int src = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const uint64_t s_info = __shfl_sync(kFull, m.info, src);
+        if ((s_info >> 43) & 1u) {
+          warp_zero(sv.V, __shfl_sync(kFull, qs, src), __shfl_sync(kFull, qe, src), zeros);
+        } else {
+          const uint64_t x0 = __shfl_sync(kFull, m.hstart, src), pitch = __shfl_sync(kFull, m.hpitch, src);
+          const uint64_t W = __shfl_sync(kFull, m.W, src);
+          uint64_t o = __shfl_sync(kFull, lo, src);
+          const uint64_t h = __shfl_sync(kFull, hi, src);
+          uint64_t r = o / W, c = o - r * W;
+          while (o < h) {
+            const uint64_t len = umin64(W - c, h - o);
+            const uint64_t x = x0 + r * pitch + c;
+            const uint64_t y0 = umax64(x, sv.sb), y1 = umin64(x + len, sv.se);
+            if (y0 < y1) warp_zero(sv.V, y0 - sv.sb, y1 - sv.sb, zeros);
+            o += len;
+            ++r;
+            c = 0;
+          }
+        }
+      }
+      // continue with the next 32 descriptors while the group does
+      if (!(__shfl_sync(kFull, (uint32_t)(ps < w1), 31) && base + 32 < n)) break;
+    }
+  }
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // fill shard-relative V bytes [q0, q1) with the byte value `val` (0x00/0xFF)
@@ -978,33 +1112,6 @@ __device__ __forceinline__ void fill_v(const ShadowView& sv, uint64_t q0, uint64
       stg_val16(V4 + k, word);
     } else {
       for (uint64_t q = umax64(qb, q0); q < umin64(qb + 16, q1); ++q) sv.V[q] = (uint8_t)val;
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kThreads) k_apply(const cg_copy_desc* __restrict__ descs, uint64_t n,
-                                                    const uint64_t* __restrict__ P,
-                                                    const uint32_t* __restrict__ chunk_first, uint64_t t_min,
-                                                    uint64_t max_chunks, ShadowView sv) {
-  const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
-  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t c = gw; c < g.nchunks; c += nw) {
-    const uint64_t w0 = c * g.T, w1 = umin64(w0 + g.T, g.total);
-    for (uint64_t d = chunk_first[c]; d < n; ++d) {
-      const uint64_t pd = P[d];
-      if (pd >= w1) break;
-      const uint64_t pd1 = P[d + 1];
-      if (pd1 == pd) continue;
-      const Norm nm = normalize(descs[d]);
-      uint64_t a = umax64(w0, pd) - pd, b = umin64(w1, pd1) - pd;
-      a = a > kApplyItemCost ? a - kApplyItemCost : 0;
-      b = b > kApplyItemCost ? b - kApplyItemCost : 0;
-      if (a < b)
-        for_rows(nm, a, b, [&](uint64_t x, uint64_t len, uint64_t) {
-          const uint64_t y0 = umax64(x, sv.sb), y1 = umin64(x + len, sv.se);
-          if (y0 < y1) fill_v(sv, y0 - sv.sb, y1 - sv.sb, 0u);
-        });
     }
   }
 }
@@ -1154,8 +1261,9 @@ cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_
 cudaError_t apply_dtoh(const Launch& L, const cg_copy_desc* d, const cg_verdict* v, uint64_t n,
                        const ShadowView& sv, const Plan& p, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
+  ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
   L.stage(CG_STAGE_APPLY_PREP, true, s);
-  k_apply_prep<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(d, v, n, p.weight);
+  k_apply_prep<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(d, v, n, p.weight, meta);
   *L.counter += 1;
   L.stage(CG_STAGE_APPLY_PREP, false, s);
   L.stage(CG_STAGE_APPLY_PLAN, true, s);
@@ -1163,7 +1271,8 @@ cudaError_t apply_dtoh(const Launch& L, const cg_copy_desc* d, const cg_verdict*
   if (e != cudaSuccess) return e;
   L.stage(CG_STAGE_APPLY_PLAN, false, s);
   L.stage(CG_STAGE_APPLY, true, s);
-  k_apply<<<L.persist_blocks, kThreads, 0, s>>>(d, n, p.P, p.chunk_first, p.t_min, p.max_chunks, sv);
+  cudaMemsetAsync(p.counter, 0, sizeof(uint32_t), s);
+  k_apply<<<L.persist_blocks, kThreads, 0, s>>>(meta, n, p.P, p.chunk_first, p.counter, p.t_min, p.max_chunks, sv);
   L.stage(CG_STAGE_APPLY, false, s);
   *L.counter += 1;
   return cudaGetLastError();
