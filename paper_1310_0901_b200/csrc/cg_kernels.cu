@@ -551,16 +551,35 @@ __device__ __forceinline__ void consume_dtoh(const uint8_t* st, uint32_t q0, uin
   }
 }
 
-// Tile generator.  Descriptor bookkeeping is lane-parallel: lane i of the warp
-// owns descriptor wbase+i of a 32-descriptor window and, whenever the window or
-// the group changes, computes that descriptor's piece (its share of the
-// group's weight interval) -- for contiguous host ranges directly as a shard
-// byte range [qs, qe) plus the analytic out-of-window offset -- and finalises
-// pieces without shard bytes itself (DtoD, invalid or empty host sides,
-// ranges outside the shard).  The warp-uniform part only walks the remaining
-// descriptors (ballot/ffs over the window) and cuts their shard ranges into
-// block-aligned tiles; non-contiguous 2D pieces go row by row.
+// Tile generator.  All bookkeeping is lane-parallel:
+//  * descriptor window: lane i owns descriptor wbase+i and, whenever the window
+//    or the group changes, computes its piece (its share of the group's weight
+//    interval) -- for contiguous host ranges directly as a shard byte range
+//    plus the analytic first out-of-window offset -- and finalises pieces
+//    without shard bytes itself (DtoD, invalid or empty host sides, ranges
+//    outside the shard);
+//  * segment window: lane j owns one contiguous shard range (a contiguous
+//    piece, or one row of a 2D piece, R-11) and its number of block-aligned
+//    tiles; a warp prefix sum numbers all tiles of the window, and every tile
+//    is issued by the lane that owns it (tile parameters never leave that
+//    lane's registers).
+// The warp-uniform part is a cursor over tile numbers plus a small phase
+// machine (group -> window -> contiguous pieces -> 2D pieces row by row).
 constexpr uint32_t kPieceIn = 1, kPieceWhole = 2, kPieceHtod = 4, kPiece2D = 8, kPieceEmpty = 16;
+constexpr uint32_t kSegEndLast = 1u << 8;   // the segment's last tile ends its piece
+constexpr int kPhaseGroup = 0, kPhaseContig = 1, kPhase2D = 2, kPhaseWindow = 3;
+
+__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t x, uint32_t& total) {
+  const int lane = threadIdx.x & 31;
+  uint32_t inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o) inc += y;
+  }
+  total = __shfl_sync(kFull, inc, 31);
+  return inc - x;
+}
 
 struct TileGen {
   // inputs
@@ -572,22 +591,24 @@ struct TileGen {
   uint32_t err_mask;
   uint64_t n, T, nchunks, total;
   uint64_t wb, we, sb, se;
-  // group state
-  uint64_t w0, w1, g_pending;   // g_pending valid in lane 0
-  bool in_group;
-  // window: lane i <-> descriptor wbase + i
+  // group
+  uint64_t w0, w1;
+  uint32_t g_pending;   // lane 0
+  int phase;
+  // descriptor window (lane i <-> wbase + i)
   uint64_t wbase;
   uint64_t m_x0, m_pitch, m_W, m_info, m_ps, m_pe;
-  uint64_t p_qs, p_qe, p_ob, p_fu, p_lo, p_hi;   // lane's piece in the current group
   uint32_t p_fl;
-  // warp-uniform walk
-  uint64_t d;                   // next descriptor to look at
-  bool have_piece;              // a piece is being cut into tiles
-  uint32_t fl;
-  uint64_t cur, qend, ob, pend_fu, cd;
-  // 2D rows
-  bool seg_active;
-  uint64_t o, hi, r, col, x0, pitch, W;
+  uint64_t p_lo, p_hi, p_qs, p_qe, p_ob, p_fu;
+  uint32_t twod;        // remaining 2D pieces of the window (lane mask)
+  // segment window (lane j)
+  uint64_t s_q0, s_q1, s_ob, s_pfu;
+  uint32_t s_d, s_fl, s_k, s_excl;
+  uint32_t K, t;
+  // current 2D piece
+  bool in2d;
+  uint64_t x0, pitch, W, lo2, hi2, r2, fu2;
+  uint32_t d2, fl2;
 
   __device__ __forceinline__ void load_window(uint64_t base) {
     const int lane = threadIdx.x & 31;
@@ -607,203 +628,200 @@ struct TileGen {
     }
   }
 
-  // lane-parallel: this lane's piece in group [w0, w1); pieces without shard
-  // bytes are finalised (whole) or merged (split) right here
   __device__ __forceinline__ void compute_pieces() {
     const int lane = threadIdx.x & 31;
     p_fl = 0;
-    if (!(m_ps < w1 && m_pe > w0)) return;
-    const uint64_t nbytes = m_info & ((1ull << 40) - 1);
-    const uint32_t kind = (uint32_t)(m_info >> 40) & 3u;
-    const bool host = (m_info >> 42) & 1u, contig = (m_info >> 43) & 1u;
-    const bool htod = kind == CG_HTOD;
-    uint32_t f = kPieceIn | (htod ? kPieceHtod : 0u);
-    if (m_ps >= w0 && m_pe <= w1) f |= kPieceWhole;
-    uint64_t a = umax64(w0, m_ps) - m_ps, b = umin64(w1, m_pe) - m_ps;
-    a = a > kItemCost ? a - kItemCost : 0;
-    b = b > kItemCost ? b - kItemCost : 0;
-    uint64_t lo = a, hi = b;
-    if (!htod) {
-      lo = a << 3;
-      hi = umin64(b << 3, nbytes);
-    }
-    p_fu = kNone;
-    p_qs = p_qe = 0;
-    if (!host || lo >= hi) {
-      f |= kPieceEmpty;
-    } else if (!contig) {
-      f |= kPiece2D;
-      p_lo = lo;
-      p_hi = hi;
-    } else {
-      const uint64_t x = m_x0 + lo, len = hi - lo;
-      if (x < wb) p_fu = lo;
-      else if (x + len > we) p_fu = lo + (umax64(x, we) - x);
-      const uint64_t y0 = umax64(x, sb), y1 = umin64(x + len, se);
-      if (y0 < y1) {
-        p_qs = y0 - sb;
-        p_qe = y1 - sb;
-        p_ob = lo - x + sb;   // logical offset of shard byte q is p_ob + q (mod 2^64)
-      } else {
+    if (m_ps < w1 && m_pe > w0) {
+      const uint64_t nbytes = m_info & ((1ull << 40) - 1);
+      const uint32_t kind = (uint32_t)(m_info >> 40) & 3u;
+      const bool host = (m_info >> 42) & 1u, contig = (m_info >> 43) & 1u;
+      const bool htod = kind == CG_HTOD;
+      uint32_t f = kPieceIn | (htod ? kPieceHtod : 0u);
+      if (m_ps >= w0 && m_pe <= w1) f |= kPieceWhole;
+      uint64_t a = umax64(w0, m_ps) - m_ps, b = umin64(w1, m_pe) - m_ps;
+      a = a > kItemCost ? a - kItemCost : 0;
+      b = b > kItemCost ? b - kItemCost : 0;
+      uint64_t lo = a, hi = b;
+      if (!htod) {
+        lo = a << 3;
+        hi = umin64(b << 3, nbytes);
+      }
+      p_fu = kNone;
+      if (!host || lo >= hi) {
         f |= kPieceEmpty;
+      } else if (!contig) {
+        f |= kPiece2D;
+        p_lo = lo;
+        p_hi = hi;
+      } else {
+        const uint64_t x = m_x0 + lo, len = hi - lo;
+        if (x < wb) p_fu = lo;
+        else if (x + len > we) p_fu = lo + (umax64(x, we) - x);
+        const uint64_t y0 = umax64(x, sb), y1 = umin64(x + len, se);
+        if (y0 < y1) {
+          p_qs = y0 - sb;
+          p_qe = y1 - sb;
+          p_ob = lo - x + sb;   // logical offset of shard byte q is p_ob + q (mod 2^64)
+        } else {
+          f |= kPieceEmpty;
+        }
+      }
+      p_fl = f;
+      if (f & kPieceEmpty) {
+        cg_verdict* v = out + (wbase + lane);
+        if (f & kPieceWhole) {
+          uint32_t flags = (uint32_t)(m_info >> 48), status;
+          finalize_fields(flags, status, p_fu, 0, err_mask);
+          v->first_unaddr = p_fu;
+          v->flags = flags;
+          v->status = status;
+        } else if (p_fu != kNone) {
+          atomicMin(reinterpret_cast<unsigned long long*>(&v->first_unaddr), p_fu);
+        }
       }
     }
-    p_fl = f;
-    if (f & kPieceEmpty) {
-      cg_verdict* v = out + (wbase + lane);
-      if (f & kPieceWhole) {
-        uint32_t flags = (uint32_t)(m_info >> 48), status;
-        finalize_fields(flags, status, p_fu, 0, err_mask);
-        v->first_unaddr = p_fu;
-        v->flags = flags;
-        v->status = status;
-      } else if (p_fu != kNone) {
-        atomicMin(reinterpret_cast<unsigned long long*>(&v->first_unaddr), p_fu);
-      }
+    const uint32_t live2d = __ballot_sync(kFull, (p_fl & (kPiece2D | kPieceEmpty)) == kPiece2D);
+    twod = live2d;
+    // the contiguous pieces form the first segment window
+    const bool live = (p_fl & (kPieceIn | kPiece2D | kPieceEmpty)) == kPieceIn;
+    set_segment(live, p_qs, p_qe, p_ob, p_fu, (uint32_t)(wbase + lane),
+                (p_fl & kPieceHtod ? kTileHtod : 0u) | (p_fl & kPieceWhole ? kTileWhole : 0u) | kSegEndLast |
+                    ((uint32_t)(m_info >> 48) << 16));
+    phase = kPhaseContig;
+  }
+
+  __device__ __forceinline__ void set_segment(bool live, uint64_t q0, uint64_t q1, uint64_t ob, uint64_t pfu,
+                                              uint32_t d, uint32_t fl) {
+    s_q0 = q0;
+    s_q1 = q1;
+    s_ob = ob;
+    s_pfu = pfu;
+    s_d = d;
+    s_fl = fl;
+    uint32_t k = 0;
+    if (live) {
+      const uint64_t sh = (fl & kTileHtod) ? 12 : 15;   // log2 of the tile block
+      k = (uint32_t)(((q1 - 1) >> sh) - (q0 >> sh) + 1);
     }
+    s_k = k;
+    s_excl = warp_excl_scan(k, K);
+    t = 0;
   }
 
   __device__ __forceinline__ bool next_group() {
     const int lane = threadIdx.x & 31;
-    const uint64_t g = __shfl_sync(kFull, g_pending, 0);
+    const uint32_t g = __shfl_sync(kFull, g_pending, 0);
     if (g >= nchunks) return false;
     if (lane == 0) g_pending = atomicAdd(counter, 1u);
-    w0 = g * T;
+    w0 = (uint64_t)g * T;
     w1 = umin64(w0 + T, total);
-    d = chunk_first[g];
+    const uint64_t d = chunk_first[g];
     if (d < wbase || d >= wbase + 32) load_window(d);
     compute_pieces();
-    in_group = true;
     return true;
   }
 
-  // advance d to the next descriptor of the group with shard work; false when
-  // the group is exhausted
-  __device__ __forceinline__ bool next_piece() {
+  // rows [r2, r2 + 32) of the current 2D piece as a segment window
+  __device__ __forceinline__ void row_window() {
     const int lane = threadIdx.x & 31;
-    while (true) {
-      const uint32_t rel = (uint32_t)(d - wbase);
-      const bool live = (p_fl & kPieceIn) && !(p_fl & kPieceEmpty) && (uint32_t)lane >= rel;
-      const uint32_t m = __ballot_sync(kFull, live);
-      if (m) {
-        const int src = __ffs(m) - 1;
-        d = wbase + src;
-        fl = __shfl_sync(kFull, p_fl, src);
-        cd = d;
-        if (fl & kPiece2D) {
+    const uint64_t r = r2 + lane;
+    const uint64_t rs = r * W;                       // logical offset of the row start
+    bool live = false;
+    uint64_t q0 = 0, q1 = 0, ob = 0, cand = kNone;
+    if (rs < hi2) {
+      const uint64_t L0 = umax64(lo2, rs), L1 = umin64(hi2, rs + W);
+      const uint64_t x = x0 + r * pitch + (L0 - rs), len = L1 - L0;
+      if (x < wb) cand = L0;
+      else if (x + len > we) cand = L0 + (umax64(x, we) - x);
+      const uint64_t y0 = umax64(x, sb), y1 = umin64(x + len, se);
+      if (y0 < y1) {
+        live = true;
+        q0 = y0 - sb;
+        q1 = y1 - sb;
+        ob = L0 - x + sb;
+      }
+    }
+    fu2 = umin64(fu2, warp_min(cand));
+    set_segment(live, q0, q1, ob, kNone, d2, fl2 & kTileHtod);
+    r2 += 32;
+  }
+
+  // issues the next tile into ring slot s; false when the warp has no more work
+  __device__ __forceinline__ bool next(WarpRing& ring, int s, const ShadowView& sv, uint64_t policy) {
+    const int lane = threadIdx.x & 31;
+    while (t >= K) {
+      if (phase == kPhaseGroup) {
+        if (!next_group()) return false;
+      } else if (phase == kPhaseContig || phase == kPhase2D) {
+        phase = kPhase2D;
+        if (in2d) {
+          if (r2 * W < hi2) {
+            row_window();
+          } else {   // all rows done: a data-less END tile carrying the analytic offset
+            in2d = false;
+            if (lane == 0) {
+              TileInfo ti;
+              ti.ob = 0;
+              ti.pend_fu = fu2;
+              ti.d = d2;
+              ti.flags = kTileEnd | (fl2 & ~kSegEndLast);
+              ti.q0 = ti.q1 = 0;
+              ring.info[s] = ti;
+              mbar_arrive(&ring.bar[s]);
+            }
+            return true;
+          }
+        } else if (twod) {
+          const int src = __ffs(twod) - 1;
+          twod &= twod - 1;
           x0 = __shfl_sync(kFull, m_x0, src);
           pitch = __shfl_sync(kFull, m_pitch, src);
           W = __shfl_sync(kFull, m_W, src);
-          o = __shfl_sync(kFull, p_lo, src);
-          hi = __shfl_sync(kFull, p_hi, src);
-          r = o / W;
-          col = o - r * W;
-          pend_fu = kNone;
-          seg_active = false;
+          lo2 = __shfl_sync(kFull, p_lo, src);
+          hi2 = __shfl_sync(kFull, p_hi, src);
+          const uint32_t pf = __shfl_sync(kFull, p_fl, src);
+          const uint32_t prep = (uint32_t)(__shfl_sync(kFull, m_info, src) >> 48);
+          d2 = (uint32_t)(wbase + src);
+          fl2 = (pf & kPieceHtod ? kTileHtod : 0u) | (pf & kPieceWhole ? kTileWhole : 0u) | (prep << 16);
+          r2 = lo2 / W;
+          fu2 = kNone;
+          in2d = true;
         } else {
-          cur = __shfl_sync(kFull, p_qs, src);
-          qend = __shfl_sync(kFull, p_qe, src);
-          ob = __shfl_sync(kFull, p_ob, src);
-          pend_fu = __shfl_sync(kFull, p_fu, src);
+          phase = kPhaseWindow;
         }
-        ++d;
-        have_piece = true;
-        return true;
+      } else {   // kPhaseWindow: the group may continue past this window
+        const bool more = (__shfl_sync(kFull, p_fl, 31) & kPieceIn) && wbase + 32 < n;
+        if (more) {
+          load_window(wbase + 32);
+          compute_pieces();
+        } else {
+          phase = kPhaseGroup;
+        }
       }
-      // nothing left in this window: continue in the next window if the group does
-      const bool last_in = __shfl_sync(kFull, p_fl, 31) & kPieceIn;
-      if (!last_in || wbase + 32 >= n) return false;
-      load_window(wbase + 32);
-      d = wbase;
-      compute_pieces();
     }
-  }
-
-  __device__ __forceinline__ void emit(TileInfo& t, uint64_t& qa) {
-    const bool htod = fl & kPieceHtod;
-    const uint64_t blk = htod ? kTileV : kDtohBlock;
-    const uint64_t tq0 = cur, tq1 = umin64(qend, (cur & ~(blk - 1)) + blk);
-    qa = tq0 & ~127ull;
-    t.ob = ob + qa;
-    t.d = (uint32_t)cd;
-    t.flags = kTileData | (htod ? kTileHtod : 0u);
-    t.q0 = (uint32_t)(tq0 - qa);
-    t.q1 = (uint32_t)(tq1 - qa);
-    cur = tq1;
-  }
-
-  // Fills t (and the staged global offset qa) with the next tile; false when
-  // the warp has no more work.
-  __device__ __forceinline__ bool next(TileInfo& t, uint64_t& qa) {
-    while (true) {
-      if (!have_piece) {
-        if (!in_group && !next_group()) return false;
-        if (!next_piece()) {
-          in_group = false;
-          continue;
-        }
-      }
-      if (!(fl & kPiece2D)) {                       // contiguous: one shard range
-        emit(t, qa);
-        if (cur >= qend) {
-          t.flags |= kTileEnd | ((fl & kPieceWhole) ? kTileWhole : 0u);
-          have_piece = false;
-        }
-        t.pend_fu = pend_fu;
-        return true;
-      }
-      // 2D: row segments (R-11)
-      if (!seg_active) {
-        if (o >= hi) {   // no further rows: a data-less END tile
-          t.ob = 0;
-          t.pend_fu = pend_fu;
-          t.d = (uint32_t)cd;
-          t.flags = kTileEnd | ((fl & kPieceWhole) ? kTileWhole : 0u) | ((fl & kPieceHtod) ? kTileHtod : 0u);
-          t.q0 = t.q1 = 0;
-          qa = 0;
-          have_piece = false;
-          return true;
-        }
-        const uint64_t len = umin64(W - col, hi - o);
-        const uint64_t x = x0 + r * pitch + col;
-        const uint64_t so = o;
-        o += len;
-        col += len;
-        if (col == W) {
-          ++r;
-          col = 0;
-        }
-        if (x < wb) pend_fu = umin64(pend_fu, so);
-        if (x + len > we) pend_fu = umin64(pend_fu, so + (umax64(x, we) - x));
-        const uint64_t y0 = umax64(x, sb), y1 = umin64(x + len, se);
-        if (y0 >= y1) continue;
-        cur = y0 - sb;
-        qend = y1 - sb;
-        ob = so - x + sb;
-        seg_active = true;
-      }
-      emit(t, qa);
-      if (cur >= qend) {
-        seg_active = false;
-        if (o >= hi) {
-          t.flags |= kTileEnd | ((fl & kPieceWhole) ? kTileWhole : 0u);
-          have_piece = false;
-        }
-      }
-      t.pend_fu = pend_fu;
-      return true;
-    }
-  }
-};
-
-
-__device__ __forceinline__ void issue_tile(WarpRing& ring, int s, const TileInfo& t, uint64_t qa,
-                                           const ShadowView& sv, uint64_t policy) {
-  if ((threadIdx.x & 31) == 0) {
-    ring.info[s] = t;
-    if (t.flags & kTileData) {
-      const uint32_t span = (t.q1 + 127u) & ~127u;   // staged host bytes (multiple of 128)
-      if (t.flags & kTileHtod) {
+    // tile t belongs to the last lane whose tiles start at or before t
+    const uint32_t own = __ballot_sync(kFull, s_k != 0 && s_excl <= t);
+    const int owner = 31 - __clz(own);
+    if (lane == owner) {
+      const uint32_t j = t - s_excl;
+      const uint32_t sh = (s_fl & kTileHtod) ? 12 : 15;
+      const uint64_t base = (s_q0 >> sh) << sh;
+      const uint64_t tq0 = j ? base + ((uint64_t)j << sh) : s_q0;
+      const uint64_t tq1 = umin64(s_q1, base + ((uint64_t)(j + 1) << sh));
+      const uint64_t qa = tq0 & ~127ull;
+      TileInfo ti;
+      ti.ob = s_ob + qa;
+      ti.pend_fu = s_pfu;
+      ti.d = s_d;
+      uint32_t f = kTileData | (s_fl & ~(kSegEndLast | kTileWhole));
+      if (j + 1 == s_k && (s_fl & kSegEndLast)) f |= kTileEnd | (s_fl & kTileWhole);
+      ti.flags = f;
+      ti.q0 = (uint32_t)(tq0 - qa);
+      ti.q1 = (uint32_t)(tq1 - qa);
+      ring.info[s] = ti;
+      const uint32_t span = (ti.q1 + 127u) & ~127u;   // staged host bytes (multiple of 128)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (f & kTileHtod) {
         mbar_arrive_tx(&ring.bar[s], span + span / 8);
         bulk_g2s(ring.data[s], sv.V + qa, span, &ring.bar[s], policy);
         bulk_g2s(ring.data[s] + kTileV, sv.A + qa / 8, span / 8, &ring.bar[s], policy);
@@ -811,11 +829,11 @@ __device__ __forceinline__ void issue_tile(WarpRing& ring, int s, const TileInfo
         mbar_arrive_tx(&ring.bar[s], span / 8);
         bulk_g2s(ring.data[s], sv.A + qa / 8, span / 8, &ring.bar[s], policy);
       }
-    } else {
-      mbar_arrive(&ring.bar[s]);
     }
+    ++t;
+    return true;
   }
-}
+};
 
 __global__ void __launch_bounds__(kRingWarps * 32) k_check_scan(
     const ScanMeta* __restrict__ meta, uint64_t n, const uint64_t* __restrict__ P,
@@ -834,11 +852,11 @@ __global__ void __launch_bounds__(kRingWarps * 32) k_check_scan(
 
   TileGen gen;
   gen.meta = meta;
-  gen.out = out;
-  gen.err_mask = err_mask;
   gen.P = P;
   gen.chunk_first = chunk_first;
   gen.counter = counter;
+  gen.out = out;
+  gen.err_mask = err_mask;
   gen.n = n;
   gen.T = geo.T;
   gen.nchunks = geo.nchunks;
@@ -848,21 +866,15 @@ __global__ void __launch_bounds__(kRingWarps * 32) k_check_scan(
   gen.sb = sv.sb;
   gen.se = sv.se;
   gen.g_pending = lane == 0 ? atomicAdd(counter, 1u) : 0;
-  gen.in_group = false;
-  gen.have_piece = false;
-  gen.seg_active = false;
-  gen.wbase = ~0ull >> 1;   // empty window
-  gen.d = 0;
+  gen.phase = kPhaseGroup;
+  gen.wbase = ~0ull >> 1;   // no window yet
   gen.p_fl = 0;
+  gen.twod = 0;
+  gen.in2d = false;
+  gen.K = gen.t = 0;
 
-  // prologue: fill the ring
   int filled = 0;
-  for (; filled < kStages; ++filled) {
-    TileInfo t;
-    uint64_t qa;
-    if (!gen.next(t, qa)) break;
-    issue_tile(ring, filled, t, qa, sv, policy);
-  }
+  while (filled < kStages && gen.next(ring, filled, sv, policy)) ++filled;
   uint32_t phase = 0;   // bit s = parity to wait for on slot s
   Partial p{kNone, kNone, 0};
   for (int s = 0, left = filled; left > 0; s = (s + 1 == kStages) ? 0 : s + 1) {
@@ -883,8 +895,7 @@ __global__ void __launch_bounds__(kRingWarps * 32) k_check_scan(
       if (lane == 0) {
         cg_verdict* v = out + t.d;
         if (t.flags & kTileWhole) {
-          const uint32_t pflags = (uint32_t)(__ldg(&meta[t.d].info) >> 48);
-          uint32_t flags = pflags, status;
+          uint32_t flags = t.flags >> 16, status;
           finalize_fields(flags, status, p.fu, p.cnt, err_mask);
           v->first_unaddr = p.fu;
           v->first_undef = p.fd;
@@ -900,18 +911,10 @@ __global__ void __launch_bounds__(kRingWarps * 32) k_check_scan(
       p = Partial{kNone, kNone, 0};
     }
     __syncwarp();
-    // refill this slot: generic-proxy reads of the slot are ordered before the
-    // async-proxy writes of the next bulk copy
-    TileInfo nt;
-    uint64_t qa;
-    if (gen.next(nt, qa)) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_tile(ring, s, nt, qa, sv, policy);
-    } else {
-      --left;
-    }
+    if (!gen.next(ring, s, sv, policy)) --left;
   }
 }
+
 
 // a5 for descriptors split across groups
 __global__ void __launch_bounds__(kThreads) k_finalize_split(uint64_t n, const uint64_t* __restrict__ P,
