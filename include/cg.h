@@ -181,8 +181,9 @@ cg_status cg_host_mark(cg_ctx *ctx, uint64_t addr, uint64_t len, uint32_t state,
  * array, copied before return.  An invalid mark (range leaving the window,
  * unknown state) is skipped and only it: its status (CG_ERR_INVALID_VALUE) is
  * written to h_status[i] when h_status is not NULL (CG_OK for applied marks).
+ * Any n is accepted (uploaded in runs of at most min(max_descs, 2^20) marks).
  * Returns CG_OK if every mark was applied, else CG_ERR_INVALID_VALUE (also for
- * n > max_descs or NULL h_marks, when nothing is applied). */
+ * NULL h_marks, when nothing is applied). */
 cg_status cg_host_mark_batch(cg_ctx *ctx, const cg_mark *h_marks, uint64_t n, uint32_t *h_status,
                              void *stream);
 

@@ -498,58 +498,89 @@ __device__ __forceinline__ void finalize_fields(uint32_t& flags, uint32_t& statu
   status = (flags & err_mask) ? (uint32_t)CG_ERR_INVALID_VALUE : (uint32_t)CG_OK;
 }
 
-// HtoD tile: V bytes and their A bits, host bytes [q0, q1) of the staged tile
+// HtoD tile: V bytes and their A bits, host bytes [q0, q1) of the staged tile.
+// Fast path: every lane folds its full 32-byte groups into one OR of the V
+// words and one AND of the A words (2 LDS.128 + 1 LDS.32 + 5 logic ops per 32
+// host bytes); only a lane that saw an undefined or unaddressable byte rescans
+// its groups with per-byte masks (__ffs for the first offset, __popc for the
+// count).  The partial 32-byte groups at the tile edges always take the
+// masked path.
+__device__ __forceinline__ void htod_group(const uint8_t* st, uint32_t i, uint32_t m, uint64_t ob, Partial& p) {
+  const uint4 v0 = reinterpret_cast<const uint4*>(st)[2 * i];
+  const uint4 v1 = reinterpret_cast<const uint4*>(st)[2 * i + 1];
+  const uint32_t a = reinterpret_cast<const uint32_t*>(st + kTileV)[i];
+  const uint32_t bad = ~a & m;
+  const uint32_t und = (nz16(v0) | (nz16(v1) << 16)) & a & m;
+  const uint64_t gb = ob + 32ull * i;
+  if (bad) p.fu = umin64(p.fu, gb + (__ffs(bad) - 1));
+  if (und) {
+    p.fd = umin64(p.fd, gb + (__ffs(und) - 1));
+    p.cnt += __popc(und);
+  }
+}
+
 __device__ __forceinline__ void consume_htod(const uint8_t* st, uint32_t q0, uint32_t q1, uint64_t ob,
                                              Partial& p) {
   const int lane = threadIdx.x & 31;
+  const uint32_t i0 = (q0 + 31) >> 5, i1 = q1 >> 5;   // full 32-byte groups [i0, i1)
   const uint4* V4 = reinterpret_cast<const uint4*>(st);
-  const uint16_t* A2 = reinterpret_cast<const uint16_t*>(st + kTileV);
-  const uint32_t g1 = (q1 + 15) >> 4;
+  const uint32_t* A4 = reinterpret_cast<const uint32_t*>(st + kTileV);
+  uint32_t orv = 0, anda = 0xffffffffu;
 #pragma unroll 4
-  for (uint32_t g = (q0 >> 4) + lane; g < g1; g += 32) {
-    const uint4 v = V4[g];
-    const uint32_t a = A2[g];
-    const uint32_t qb = g << 4;
-    const bool whole = qb >= q0 && qb + 16 <= q1;
-    if (!whole || (v.x | v.y | v.z | v.w) != 0 || a != 0xFFFFu) {
-      const uint32_t m = range_mask(qb, 16, q0, q1);
-      const uint32_t bad = ~a & m;
-      const uint32_t und = nz16(v) & a & m;
-      if (bad) p.fu = umin64(p.fu, ob + qb + (__ffs(bad) - 1));
-      if (und) {
-        p.fd = umin64(p.fd, ob + qb + (__ffs(und) - 1));
-        p.cnt += __popc(und);
-      }
+  for (uint32_t i = i0 + lane; i < i1; i += 32) {
+    const uint4 v0 = V4[2 * i], v1 = V4[2 * i + 1];
+    orv |= v0.x | v0.y | v0.z | v0.w | v1.x | v1.y | v1.z | v1.w;
+    anda &= A4[i];
+  }
+  if (orv != 0 || anda != 0xffffffffu)
+    for (uint32_t i = i0 + lane; i < i1; i += 32) htod_group(st, i, 0xffffffffu, ob, p);
+  // partial edge groups
+  if (i0 > i1) {                                   // [q0, q1) inside one 32-byte group
+    if (lane == 0) htod_group(st, i1, range_mask((uint64_t)i1 << 5, 32, q0, q1), ob, p);
+  } else {
+    if (lane == 0 && (q0 & 31)) htod_group(st, i0 - 1, range_mask((uint64_t)(i0 - 1) << 5, 32, q0, q1), ob, p);
+    if (lane == 1 && (q1 & 31)) htod_group(st, i1, range_mask((uint64_t)i1 << 5, 32, q0, q1), ob, p);
+  }
+}
+
+// DtoH tile: A bits only; one 16-byte A vector covers 128 host bytes
+__device__ __forceinline__ void dtoh_group(const uint8_t* st, uint32_t i, uint32_t q0, uint32_t q1, uint64_t ob,
+                                           Partial& p) {
+  const uint4 a = reinterpret_cast<const uint4*>(st)[i];
+  const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t gb = i * 128 + 32 * j;
+    if (gb + 32 <= q0 || gb >= q1) continue;
+    const uint32_t bad = ~w[j] & range_mask(gb, 32, q0, q1);
+    if (bad) {
+      p.fu = umin64(p.fu, ob + gb + (__ffs(bad) - 1));
+      break;
     }
   }
 }
 
-// DtoH tile: A bits only (one 16-byte A vector = 128 host bytes per lane step)
 __device__ __forceinline__ void consume_dtoh(const uint8_t* st, uint32_t q0, uint32_t q1, uint64_t ob,
                                              Partial& p) {
   const int lane = threadIdx.x & 31;
+  const uint32_t i0 = (q0 + 127) >> 7, i1 = q1 >> 7;   // full 128-byte groups [i0, i1)
   const uint4* A16 = reinterpret_cast<const uint4*>(st);
-  const uint32_t g1 = (q1 + 127) >> 7;
-#pragma unroll 2
-  for (uint32_t g = (q0 >> 7) + lane; g < g1; g += 32) {
-    const uint4 a = A16[g];
-    const uint32_t qb = g << 7;
-    const bool whole = qb >= q0 && qb + 128 <= q1;
-    if (!whole || (a.x & a.y & a.z & a.w) != 0xffffffffu) {
-      const uint32_t w[4] = {a.x, a.y, a.z, a.w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t gb = qb + 32 * j;
-        if (gb + 32 <= q0 || gb >= q1) continue;
-        const uint32_t bad = ~w[j] & range_mask(gb, 32, q0, q1);
-        if (bad) {
-          p.fu = umin64(p.fu, ob + gb + (__ffs(bad) - 1));
-          break;
-        }
-      }
-    }
+  uint32_t anda = 0xffffffffu;
+#pragma unroll 4
+  for (uint32_t i = i0 + lane; i < i1; i += 32) {
+    const uint4 a = A16[i];
+    anda &= a.x & a.y & a.z & a.w;
+  }
+  if (anda != 0xffffffffu)
+    for (uint32_t i = i0 + lane; i < i1; i += 32) dtoh_group(st, i, q0, q1, ob, p);
+  if (i0 > i1) {
+    if (lane == 0) dtoh_group(st, i1, q0, q1, ob, p);
+  } else {
+    if (lane == 0 && (q0 & 127)) dtoh_group(st, i0 - 1, q0, q1, ob, p);
+    if (lane == 1 && (q1 & 127)) dtoh_group(st, i1, q0, q1, ob, p);
   }
 }
+
 
 // Tile generator.  All bookkeeping is lane-parallel:
 //  * descriptor window: lane i owns descriptor wbase+i and, whenever the window
@@ -804,10 +835,12 @@ struct TileGen {
     const int owner = 31 - __clz(own);
     if (lane == owner) {
       const uint32_t j = t - s_excl;
-      const uint32_t sh = (s_fl & kTileHtod) ? 12 : 15;
-      const uint64_t base = (s_q0 >> sh) << sh;
-      const uint64_t tq0 = j ? base + ((uint64_t)j << sh) : s_q0;
-      const uint64_t tq1 = umin64(s_q1, base + ((uint64_t)(j + 1) << sh));
+      const bool htod = s_fl & kTileHtod;
+      const uint64_t bmask = htod ? ~(uint64_t)(kTileV - 1) : ~(uint64_t)(kDtohBlock - 1);
+      const uint64_t bsz = htod ? kTileV : kDtohBlock;
+      const uint64_t base = s_q0 & bmask;
+      const uint64_t tq0 = j ? base + j * bsz : s_q0;
+      const uint64_t tq1 = umin64(s_q1, base + (j + 1) * bsz);
       const uint64_t qa = tq0 & ~127ull;
       TileInfo ti;
       ti.ob = s_ob + qa;

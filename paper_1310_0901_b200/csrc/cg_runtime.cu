@@ -321,7 +321,6 @@ cg_status cg_host_mark_batch(cg_ctx* c, const cg_mark* h_marks, uint64_t n, uint
   if (!c) return CG_ERR_INVALID_CONTEXT;
   if (n == 0) return CG_OK;
   if (!h_marks) return c->fail(CG_ERR_INVALID_VALUE, "null marks");
-  if (n > c->cfg.max_descs) return c->fail(CG_ERR_INVALID_VALUE, "n > max_descs");
   DeviceGuard g(c->cfg.device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const uint64_t cap = std::min<uint64_t>(c->cfg.max_descs, kMarkRun);

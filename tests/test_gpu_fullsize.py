@@ -1,0 +1,121 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (the whole batch in one cg_check_copies + one cg_apply_dtoh).
+
+The oracle recomputes a sample of descriptors one by one: it replays every
+setup event (host marks, V-bytes, registry) and only the sampled copies.  In
+C2 and C4 the copies are independent (private host ranges in C2; in C4 DtoH
+targets are never HtoD sources and DtoH checks read only A bits), so the
+sampled verdicts equal the full replay's.  Everything else is checked with
+properties that hold at any size: C2's dirty set equals its injected set, C3's
+count / first offset are the generator's closed form, and the final shadow
+equals the setup state with exactly the non-injected DtoH ranges defined.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import tracegen as tg
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.fixture(scope="module")
+def cg():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_1310_0901_b200 import build
+    build.build()
+    import paper_1310_0901_b200 as m
+    return m
+
+
+def gpu_batch(cg, tr):
+    """Setup events through the ABI, then the whole copy batch in one call."""
+    import torch
+    from paper_1310_0901_b200.replay import events_to_descs
+    ev = tr.events
+    copies = ev[ev["op"] == tg.OP_COPY]
+    nreg = int(np.count_nonzero(ev["op"] == tg.OP_REG))
+    chk = cg.Checker(tr.host_base, tr.host_size, max_descs=max(len(copies), 1024), max_allocs=max(nreg, 1024))
+    _, st = cg.replay_events(chk, ev[ev["op"] != tg.OP_COPY], tr.blob)
+    assert not st.any(), "every setup call of the generated trace is valid"
+    descs = events_to_descs(copies)
+    dd = cg.to_device_descs(descs)
+    dv = chk.check_copies(dd)
+    chk.apply_dtoh(dd, dv)
+    torch.cuda.synchronize()
+    return chk, descs, cg.verdicts_to_numpy(dv)
+
+
+def sampled_oracle(tr, idx):
+    """Oracle verdicts of the copies idx (indices into the copy list)."""
+    ev = tr.events
+    is_copy = ev["op"] == tg.OP_COPY
+    keep = ~is_copy
+    pos = np.flatnonzero(is_copy)[idx]
+    keep[pos] = True
+    o = oracle.Oracle(tr.host_base, tr.host_size)
+    v, _ = o.replay(ev[keep], tr.blob)
+    return o, v
+
+
+def compare(gv, ov, idx):
+    for f in ov.dtype.names:
+        a, b = gv[f][idx], ov[f]
+        bad = np.flatnonzero(a != b)
+        assert len(bad) == 0, (f, idx[bad[:5]], a[bad[:5]], b[bad[:5]])
+
+
+def test_c2_full(cg):
+    tr = tg.c2_small()
+    chk, descs, gv = gpu_batch(cg, tr)
+    rng = np.random.default_rng(1)
+    inj = tr.meta["inject"]
+    # every injected copy plus 10k random ones, plus the first and last
+    idx = np.unique(np.concatenate([np.flatnonzero(inj), rng.choice(len(descs), 10000, replace=False),
+                                    [0, len(descs) - 1]]))
+    o, ov = sampled_oracle(tr, idx)
+    compare(gv, ov, idx)
+    # property at full size: the dirty set is exactly the injected set
+    assert np.array_equal(gv["flags"] != 0, inj != 0)
+    # final shadow: setup state + the non-injected DtoH ranges defined
+    A, V = chk.shadow()
+    assert np.array_equal(A, o.A)
+    expect = o.V.copy()
+    for i in np.flatnonzero((descs["kind"] == tg.DTOH) & (inj == 0)):
+        a = int(descs["dst"][i]) - tr.host_base
+        expect[a:a + int(descs["width"][i])] = 0
+    assert np.array_equal(V, expect)
+    chk.close()
+
+
+@pytest.mark.parametrize("dtoh", [False, True])
+def test_c3_full(cg, dtoh):
+    tr = tg.c3_single(dtoh=dtoh)
+    chk, descs, gv = gpu_batch(cg, tr)
+    o, ov = sampled_oracle(tr, np.array([0]))
+    compare(gv, ov, np.array([0]))
+    if not dtoh:
+        offs = tr.meta["hole_offsets"]
+        assert gv[0]["undef_count"] == len(offs) == 8192            # closed form
+        assert gv[0]["first_undef"] == offs[0]
+    else:
+        A, V = chk.shadow()
+        assert not V[4096:4096 + tr.meta["size"]].any()
+        assert np.array_equal(V, o.V)
+    chk.close()
+
+
+def test_c4_full_sampled(cg):
+    tr = tg.c4_pitched()
+    chk, descs, gv = gpu_batch(cg, tr)
+    rng = np.random.default_rng(2)
+    inj = tr.meta["inject"]
+    idx = np.unique(np.concatenate([rng.choice(np.flatnonzero(inj), 200, replace=False),
+                                    rng.choice(len(descs), 800, replace=False)]))
+    o, ov = sampled_oracle(tr, idx)
+    compare(gv, ov, idx)
+    assert np.all(gv["flags"][inj == 0] == 0)
+    A, _ = chk.shadow()
+    assert np.array_equal(A, o.A)
+    chk.close()

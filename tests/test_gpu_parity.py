@@ -110,6 +110,12 @@ def test_c4_scaled(cg):
     run_parity(cg, tr)
 
 
+def test_mark_batch_larger_than_max_descs(cg):
+    """2048 consecutive host marks through a context with max_descs = 1000"""
+    tr = tg.c4_pitched(n_copies=900, n_bufs=4, rows=256, inject_frac=0.03)
+    run_parity(cg, tr, max_descs=1000)
+
+
 # ---------------------------------------------------------------------------
 # edge cases of the ABI
 # ---------------------------------------------------------------------------
