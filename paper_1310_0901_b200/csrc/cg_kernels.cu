@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(kThreads) k_plan(const uint64_t* __restrict__ 
 // The descriptor metadata the generator needs comes from a 32-descriptor
 // register window (one coalesced load per 32 descriptors).
 constexpr int kRingWarps = 4;
-constexpr int kStages = 4;
+constexpr int kStages = 3;
 constexpr uint32_t kTileV = 4096;      // HtoD: V bytes per tile
 constexpr uint32_t kTileA = kTileV / 8;
 constexpr uint32_t kDtohBlock = 32768; // DtoH: host bytes per tile (4 KiB of A)
@@ -868,7 +868,7 @@ struct TileGen {
   }
 };
 
-__global__ void __launch_bounds__(kRingWarps * 32) k_check_scan(
+__global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
     const ScanMeta* __restrict__ meta, uint64_t n, const uint64_t* __restrict__ P,
     const uint32_t* __restrict__ chunk_first, uint32_t* counter, uint64_t t_min, uint64_t max_chunks,
     ShadowView sv, cg_verdict* __restrict__ out, uint32_t err_mask) {
