@@ -234,8 +234,23 @@ cg_status cg_check_copies(cg_ctx *ctx, const cg_copy_desc *d_descs, uint64_t n, 
 cg_status cg_apply_dtoh(cg_ctx *ctx, const cg_copy_desc *d_descs, const cg_verdict *d_verdicts,
                         uint64_t n, void *stream);
 
+/* cg_check_copies followed by cg_apply_dtoh, fused: the shadow scan applies
+ * every DtoH descriptor that fits one of its work groups as soon as its verdict
+ * is final, and a residual apply pass handles the rest.  Same results as the
+ * two calls PROVIDED that no HtoD host range of the batch overlaps any DtoH
+ * host range of the batch (check with cg_batch_disjoint); otherwise call the
+ * two functions.  Asynchronous on stream.  Errors: as cg_check_copies. */
+cg_status cg_check_apply(cg_ctx *ctx, const cg_copy_desc *d_descs, uint64_t n, cg_verdict *d_out,
+                         void *stream);
+
+/* Host helper: *disjoint = 1 iff no HtoD host range of the n descriptors
+ * overlaps any DtoH host range of them (the precondition of cg_check_apply).
+ * Errors: CG_ERR_INVALID_VALUE on NULL. */
+cg_status cg_batch_disjoint(const cg_copy_desc *h_descs, uint64_t n, int *disjoint);
+
 /* End-to-end entry point with HOST buffers: copies h_descs to the device,
- * runs cg_check_copies (and cg_apply_dtoh if apply != 0) and copies the
+ * runs cg_check_copies (apply = 0), cg_check_copies + cg_apply_dtoh
+ * (apply = 1) or cg_check_apply (apply = 2, same precondition) and copies the
  * verdicts back to h_out.  Synchronous.  Requires cfg.host_staging.  Errors: as
  * cg_check_copies; CG_ERR_NOT_INITIALIZED without host staging. */
 cg_status cg_check_copies_host(cg_ctx *ctx, const cg_copy_desc *h_descs, uint64_t n, cg_verdict *h_out,

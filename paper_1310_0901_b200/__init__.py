@@ -91,6 +91,8 @@ def _load() -> ctypes.CDLL:
         "cg_check_copies": (I, [P, P, U64, P, P]),
         "cg_apply_dtoh": (I, [P, P, P, U64, P]),
         "cg_check_copies_host": (I, [P, P, U64, P, I, P]),
+        "cg_check_apply": (I, [P, P, U64, P, P]),
+        "cg_batch_disjoint": (I, [P, U64, P]),
         "cg_leak_sweep": (I, [P, P, U64, P, P]),
         "cg_leak_report": (I, [P, P, U64, P]),
         "cg_plan_batches": (I, [P, U64, P, P]),
@@ -109,7 +111,8 @@ _lib = _load()
 EXPORTED = ("cg_workspace_size", "cg_ctx_create", "cg_ctx_destroy", "cg_last_error", "cg_host_mark",
             "cg_host_mark_batch", "cg_host_set_vbits", "cg_register_alloc", "cg_free", "cg_registry_compact",
             "cg_check_copies", "cg_apply_dtoh", "cg_check_copies_host", "cg_leak_sweep", "cg_leak_report",
-            "cg_plan_batches", "cg_kernel_launches", "cg_profile_begin", "cg_profile_end")
+            "cg_plan_batches", "cg_kernel_launches", "cg_profile_begin", "cg_profile_end", "cg_check_apply",
+            "cg_batch_disjoint")
 
 # ---- same-name thin wrappers (status codes returned unchanged) -------------
 cg_workspace_size = _lib.cg_workspace_size
@@ -125,6 +128,8 @@ cg_registry_compact = _lib.cg_registry_compact
 cg_check_copies = _lib.cg_check_copies
 cg_apply_dtoh = _lib.cg_apply_dtoh
 cg_check_copies_host = _lib.cg_check_copies_host
+cg_check_apply = _lib.cg_check_apply
+cg_batch_disjoint = _lib.cg_batch_disjoint
 cg_leak_sweep = _lib.cg_leak_sweep
 cg_leak_report = _lib.cg_leak_report
 cg_plan_batches = _lib.cg_plan_batches
@@ -144,6 +149,16 @@ def plan_batches(descs: np.ndarray) -> np.ndarray:
     if st:
         raise CgError(st, "cg_plan_batches")
     return cuts[: nc.value]
+
+
+def batch_disjoint(descs: np.ndarray) -> bool:
+    """cg_batch_disjoint: no HtoD host range overlaps any DtoH host range."""
+    d = np.ascontiguousarray(descs, dtype=DESC_DTYPE)
+    out = ctypes.c_int(0)
+    st = _lib.cg_batch_disjoint(d.ctypes.data if len(d) else None, len(d), ctypes.byref(out))
+    if st:
+        raise CgError(st, "cg_batch_disjoint")
+    return bool(out.value)
 
 
 def _stream_ptr(stream) -> Optional[int]:
@@ -243,13 +258,24 @@ class Checker:
                  "cg_check_copies")
         return d_out
 
+    def check_apply(self, d_descs, d_out=None, stream=None):
+        """cg_check_apply (fused check + DtoH apply; needs a disjoint batch)."""
+        torch = self.torch
+        n = d_descs.numel() // DESC_DTYPE.itemsize
+        if d_out is None:
+            d_out = torch.empty(n * VERDICT_DTYPE.itemsize, dtype=torch.uint8, device=d_descs.device)
+        self._ok(_lib.cg_check_apply(self.ctx, d_descs.data_ptr(), n, d_out.data_ptr(), _stream_ptr(stream)),
+                 "cg_check_apply")
+        return d_out
+
     def apply_dtoh(self, d_descs, d_verdicts, stream=None):
         n = d_descs.numel() // DESC_DTYPE.itemsize
         self._ok(_lib.cg_apply_dtoh(self.ctx, d_descs.data_ptr(), d_verdicts.data_ptr(), n, _stream_ptr(stream)),
                  "cg_apply_dtoh")
 
-    def check_copies_host(self, descs: np.ndarray, out: Optional[np.ndarray] = None, apply: bool = True,
+    def check_copies_host(self, descs: np.ndarray, out: Optional[np.ndarray] = None, apply: int = 1,
                           stream=None) -> np.ndarray:
+        """apply: 0 check only, 1 check + apply, 2 fused cg_check_apply."""
         d = np.ascontiguousarray(descs, dtype=DESC_DTYPE)
         if out is None:
             out = np.empty(len(d), VERDICT_DTYPE)

@@ -74,10 +74,10 @@ int persistent_blocks(int which);   // 0: k_check_scan, 1: k_apply (per SM)
 size_t scan_meta_bytes();
 
 cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out,
-                         const Table& t, const ShadowView& sv, const Plan& p, uint32_t err_mask,
+                         const Table& t, const ShadowView& sv, const Plan& p, uint32_t err_mask, bool fuse,
                          cudaStream_t s);
 cudaError_t apply_dtoh(const Launch& L, const cg_copy_desc* d, const cg_verdict* v, uint64_t n,
-                       const ShadowView& sv, const Plan& p, cudaStream_t s);
+                       const ShadowView& sv, const Plan& p, bool after_fused, cudaStream_t s);
 cudaError_t mark_batch(const Launch& L, const cg_mark* d_marks, uint64_t n, const ShadowView& sv,
                        const Plan& p, cudaStream_t s);
 cudaError_t fresh_shadow(const Launch& L, const ShadowView& sv, cudaStream_t s);

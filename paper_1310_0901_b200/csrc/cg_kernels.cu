@@ -432,7 +432,7 @@ constexpr int kStages = 3;
 constexpr uint32_t kTileV = 4096;      // HtoD: V bytes per tile
 constexpr uint32_t kTileA = kTileV / 8;
 constexpr uint32_t kDtohBlock = 32768; // DtoH: host bytes per tile (4 KiB of A)
-constexpr uint32_t kTileData = 1, kTileHtod = 2, kTileEnd = 4, kTileWhole = 8;
+constexpr uint32_t kTileData = 1, kTileHtod = 2, kTileEnd = 4, kTileWhole = 8, kTileFuse = 16;
 
 struct __align__(16) TileInfo {
   uint64_t ob;        // logical offset of staged host byte 0
@@ -440,6 +440,7 @@ struct __align__(16) TileInfo {
   uint32_t d;         // descriptor
   uint32_t flags;
   uint32_t q0, q1;    // valid host bytes [q0, q1) relative to the staged base
+  uint64_t qs, qe;    // kTileFuse END tiles: the piece's shard range (fused DtoH apply)
 };
 
 struct WarpRing {
@@ -582,6 +583,21 @@ __device__ __forceinline__ void consume_dtoh(const uint8_t* st, uint32_t q0, uin
 }
 
 
+// V := 0 over shard bytes [q0, q1) with the whole warp (16-byte stores, byte
+// stores at the unaligned edges)
+__device__ __forceinline__ void warp_store_zero(uint8_t* V, uint64_t q0, uint64_t q1) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t a0 = (q0 + 15) & ~15ull, a1 = q1 & ~15ull;
+  if (a0 >= a1) {
+    if (lane < (int)(q1 - q0)) V[q0 + lane] = 0;
+    return;
+  }
+  if (lane < (int)(a0 - q0)) V[q0 + lane] = 0;
+  if (lane < (int)(q1 - a1)) V[a1 + lane] = 0;
+  uint4* V4 = reinterpret_cast<uint4*>(V);
+  for (uint64_t k = (a0 >> 4) + lane; k < (a1 >> 4); k += 32) stg_val16(V4 + k, 0u);
+}
+
 // Tile generator.  All bookkeeping is lane-parallel:
 //  * descriptor window: lane i owns descriptor wbase+i and, whenever the window
 //    or the group changes, computes its piece (its share of the group's weight
@@ -622,6 +638,7 @@ struct TileGen {
   uint32_t err_mask;
   uint64_t n, T, nchunks, total;
   uint64_t wb, we, sb, se;
+  bool fuse;            // check + apply in one pass (cg_check_apply)
   // group
   uint64_t w0, w1;
   uint32_t g_pending;   // lane 0
@@ -847,7 +864,14 @@ struct TileGen {
       ti.pend_fu = s_pfu;
       ti.d = s_d;
       uint32_t f = kTileData | (s_fl & ~(kSegEndLast | kTileWhole));
-      if (j + 1 == s_k && (s_fl & kSegEndLast)) f |= kTileEnd | (s_fl & kTileWhole);
+      if (j + 1 == s_k && (s_fl & kSegEndLast)) {
+        f |= kTileEnd | (s_fl & kTileWhole);
+        if (fuse && !htod) {   // a contiguous DtoH piece: the consumer may apply it
+          f |= kTileFuse;
+          ti.qs = s_q0;
+          ti.qe = s_q1;
+        }
+      }
       ti.flags = f;
       ti.q0 = (uint32_t)(tq0 - qa);
       ti.q1 = (uint32_t)(tq1 - qa);
@@ -871,7 +895,7 @@ struct TileGen {
 __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
     const ScanMeta* __restrict__ meta, uint64_t n, const uint64_t* __restrict__ P,
     const uint32_t* __restrict__ chunk_first, uint32_t* counter, uint64_t t_min, uint64_t max_chunks,
-    ShadowView sv, cg_verdict* __restrict__ out, uint32_t err_mask) {
+    ShadowView sv, cg_verdict* __restrict__ out, uint32_t err_mask, int fuse) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpRing& ring = reinterpret_cast<WarpRing*>(smem)[wid];
@@ -898,6 +922,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
   gen.we = sv.we;
   gen.sb = sv.sb;
   gen.se = sv.se;
+  gen.fuse = fuse != 0;
   gen.g_pending = lane == 0 ? atomicAdd(counter, 1u) : 0;
   gen.phase = kPhaseGroup;
   gen.wbase = ~0ull >> 1;   // no window yet
@@ -925,6 +950,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
         p.fd = warp_min(p.fd);
         p.cnt = warp_sum(p.cnt);
       }
+      bool apply = false;
       if (lane == 0) {
         cg_verdict* v = out + t.d;
         if (t.flags & kTileWhole) {
@@ -935,6 +961,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
           v->undef_count = p.cnt;
           v->flags = flags;
           v->status = status;
+          apply = (t.flags & kTileFuse) && status == CG_OK;
         } else {
           if (p.fu != kNone) atomicMin(reinterpret_cast<unsigned long long*>(&v->first_unaddr), p.fu);
           if (p.fd != kNone) atomicMin(reinterpret_cast<unsigned long long*>(&v->first_undef), p.fd);
@@ -942,6 +969,8 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
         }
       }
       p = Partial{kNone, kNone, 0};
+      // fused a6: a whole contiguous DtoH piece with status OK becomes defined
+      if (__shfl_sync(kFull, apply, 0)) warp_store_zero(sv.V, t.qs, t.qe);
     }
     __syncwarp();
     if (!gen.next(ring, s, sv, policy)) --left;
@@ -995,22 +1024,34 @@ __device__ __forceinline__ void for_rows(const Norm& nm, uint64_t lo, uint64_t h
 constexpr uint64_t kApplyItemCost = 64;
 constexpr uint32_t kZeroPage = 4096;
 
+// fusedP != nullptr: the check that just ran (cg_check_apply) already applied
+// every whole contiguous DtoH piece of its plan (fusedP, its chunk geometry);
+// only the remaining ones get weight here.
 __global__ void __launch_bounds__(kThreads) k_apply_prep(const cg_copy_desc* __restrict__ descs,
                                                          const cg_verdict* __restrict__ verd, uint64_t n,
-                                                         uint64_t* __restrict__ weight, ScanMeta* __restrict__ meta) {
+                                                         uint64_t* __restrict__ weight, ScanMeta* __restrict__ meta,
+                                                         const uint64_t* __restrict__ fusedP, uint64_t t_min,
+                                                         uint64_t max_chunks) {
+  uint64_t fT = 1;
+  if (fusedP) fT = chunk_geom(fusedP, n, t_min, max_chunks).T;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t w = 0;
     const cg_copy_desc d = descs[i];
     if (d.kind == CG_DTOH && verd[i].status == CG_OK) {
       const Norm nm = normalize(d);
-      if (nm.host && nm.nbytes) {
+      const bool contig = d.height == 1 || d.width == nm.hpitch;
+      bool done = false;
+      if (fusedP && contig) {
+        const uint64_t pd = fusedP[i], pd1 = fusedP[i + 1];
+        done = pd / fT == (pd1 - 1) / fT;
+      }
+      if (nm.host && nm.nbytes && !done) {
         w = kApplyItemCost + nm.nbytes;
         ScanMeta m;
         m.hstart = nm.hstart;
         m.hpitch = nm.hpitch;
         m.W = nm.W;
-        const bool contig = d.height == 1 || d.width == nm.hpitch;
         m.info = nm.nbytes | ((uint64_t)contig << 43);
         meta[i] = m;
       }
@@ -1269,7 +1310,7 @@ static cudaError_t plan(const Launch& L, uint64_t n, const Plan& p, cudaStream_t
 }
 
 cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out, const Table& t,
-                         const ShadowView& sv, const Plan& p, uint32_t err_mask, cudaStream_t s) {
+                         const ShadowView& sv, const Plan& p, uint32_t err_mask, bool fuse, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   const size_t smem = (size_t)t.nsplit * sizeof(uint64_t);
   ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
@@ -1284,7 +1325,8 @@ cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_
   cudaMemsetAsync(p.counter, 0, sizeof(uint32_t), s);
   L.stage(CG_STAGE_CHECK_SCAN, true, s);
   k_check_scan<<<L.scan_blocks, kRingWarps * 32, kScanSmem, s>>>(meta, n, p.P, p.chunk_first, p.counter,
-                                                                 p.t_min, p.max_chunks, sv, out, err_mask);
+                                                                 p.t_min, p.max_chunks, sv, out, err_mask,
+                                                                 fuse ? 1 : 0);
   L.stage(CG_STAGE_CHECK_SCAN, false, s);
   L.stage(CG_STAGE_CHECK_FINAL, true, s);
   k_finalize_split<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(n, p.P, p.t_min, p.max_chunks,
@@ -1295,11 +1337,12 @@ cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_
 }
 
 cudaError_t apply_dtoh(const Launch& L, const cg_copy_desc* d, const cg_verdict* v, uint64_t n,
-                       const ShadowView& sv, const Plan& p, cudaStream_t s) {
+                       const ShadowView& sv, const Plan& p, bool after_fused, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
   L.stage(CG_STAGE_APPLY_PREP, true, s);
-  k_apply_prep<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(d, v, n, p.weight, meta);
+  k_apply_prep<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(
+      d, v, n, p.weight, meta, after_fused ? p.P : nullptr, p.t_min, p.max_chunks);
   *L.counter += 1;
   L.stage(CG_STAGE_APPLY_PREP, false, s);
   L.stage(CG_STAGE_APPLY_PLAN, true, s);

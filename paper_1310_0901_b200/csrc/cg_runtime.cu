@@ -453,7 +453,8 @@ cg_status cg_check_copies(cg_ctx* c, const cg_copy_desc* d_descs, uint64_t n, cg
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cg_status st = c->sync_table(s);
   if (st != CG_OK) return st;
-  cudaError_t e = cgk::check_copies(c->launch, d_descs, n, d_out, c->dev_table(), c->sv, c->plan(), c->err_mask(), s);
+  cudaError_t e =
+      cgk::check_copies(c->launch, d_descs, n, d_out, c->dev_table(), c->sv, c->plan(), c->err_mask(), false, s);
   return c->cuda(e, "check kernels");
 }
 
@@ -464,8 +465,24 @@ cg_status cg_apply_dtoh(cg_ctx* c, const cg_copy_desc* d_descs, const cg_verdict
   if (!d_descs || !d_verdicts) return c->fail(CG_ERR_INVALID_VALUE, "null descriptor or verdict array");
   if (n > c->cfg.max_descs) return c->fail(CG_ERR_INVALID_VALUE, "n > max_descs");
   DeviceGuard g(c->cfg.device);
-  cudaError_t e = cgk::apply_dtoh(c->launch, d_descs, d_verdicts, n, c->sv, c->plan(), static_cast<cudaStream_t>(stream));
+  cudaError_t e =
+      cgk::apply_dtoh(c->launch, d_descs, d_verdicts, n, c->sv, c->plan(), false, static_cast<cudaStream_t>(stream));
   return c->cuda(e, "apply kernels");
+}
+
+cg_status cg_check_apply(cg_ctx* c, const cg_copy_desc* d_descs, uint64_t n, cg_verdict* d_out, void* stream) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (n == 0) return CG_OK;
+  if (!d_descs || !d_out) return c->fail(CG_ERR_INVALID_VALUE, "null descriptor or verdict array");
+  if (n > c->cfg.max_descs) return c->fail(CG_ERR_INVALID_VALUE, "n > max_descs");
+  DeviceGuard g(c->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cg_status st = c->sync_table(s);
+  if (st != CG_OK) return st;
+  cudaError_t e =
+      cgk::check_copies(c->launch, d_descs, n, d_out, c->dev_table(), c->sv, c->plan(), c->err_mask(), true, s);
+  if (e == cudaSuccess) e = cgk::apply_dtoh(c->launch, d_descs, d_out, n, c->sv, c->plan(), true, s);
+  return c->cuda(e, "check+apply kernels");
 }
 
 cg_status cg_check_copies_host(cg_ctx* c, const cg_copy_desc* h_descs, uint64_t n, cg_verdict* h_out, int apply,
@@ -481,9 +498,9 @@ cg_status cg_check_copies_host(cg_ctx* c, const cg_copy_desc* h_descs, uint64_t 
   cg_verdict* dv = reinterpret_cast<cg_verdict*>(c->ws + c->lay.verdict_stage);
   cudaError_t e = cudaMemcpyAsync(dd, h_descs, n * sizeof(cg_copy_desc), cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return c->cuda(e, "descriptor upload");
-  cg_status st = cg_check_copies(c, dd, n, dv, stream);
+  cg_status st = apply == 2 ? cg_check_apply(c, dd, n, dv, stream) : cg_check_copies(c, dd, n, dv, stream);
   if (st != CG_OK) return st;
-  if (apply) {
+  if (apply == 1) {
     st = cg_apply_dtoh(c, dd, dv, n, stream);
     if (st != CG_OK) return st;
   }
@@ -533,6 +550,36 @@ static bool host_range(const cg_copy_desc& d, uint64_t& lo, uint64_t& hi) {
   lo = (uint64_t)st;
   hi = (uint64_t)(st + sp);
   return true;
+}
+
+cg_status cg_batch_disjoint(const cg_copy_desc* h_descs, uint64_t n, int* disjoint) {
+  if (!disjoint || (n && !h_descs)) return CG_ERR_INVALID_VALUE;
+  struct Iv {
+    uint64_t lo, hi;
+    bool htod;
+  };
+  std::vector<Iv> v;
+  v.reserve(n);
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t lo, hi;
+    if (host_range(h_descs[i], lo, hi)) v.push_back({lo, hi, h_descs[i].kind == CG_HTOD});
+  }
+  std::sort(v.begin(), v.end(), [](const Iv& a, const Iv& b) { return a.lo < b.lo; });
+  uint64_t end_h = 0, end_d = 0;   // furthest end of HtoD / DtoH ranges starting earlier
+  bool seen_h = false, seen_d = false;
+  *disjoint = 1;
+  for (const Iv& x : v) {
+    if (x.htod) {
+      if (seen_d && x.lo < end_d) { *disjoint = 0; break; }
+      end_h = seen_h ? std::max(end_h, x.hi) : x.hi;
+      seen_h = true;
+    } else {
+      if (seen_h && x.lo < end_h) { *disjoint = 0; break; }
+      end_d = seen_d ? std::max(end_d, x.hi) : x.hi;
+      seen_d = true;
+    }
+  }
+  return CG_OK;
 }
 
 cg_status cg_plan_batches(const cg_copy_desc* h_descs, uint64_t n, uint64_t* h_cuts, uint64_t* n_cuts) {

@@ -27,8 +27,9 @@ def events_to_descs(ev: np.ndarray) -> np.ndarray:
     return d
 
 
-def replay_events(chk, events: np.ndarray, blob=None, stream=None):
-    """Returns (verdicts of the COPY events in order, status per event)."""
+def replay_events(chk, events: np.ndarray, blob=None, stream=None, fuse: bool = True):
+    """Returns (verdicts of the COPY events in order, status per event).
+    With fuse, batches that cg_batch_disjoint accepts use cg_check_apply."""
     import torch
     from . import MARK_DTYPE, VERDICT_DTYPE, to_device_descs, verdicts_to_numpy
 
@@ -71,12 +72,16 @@ def replay_events(chk, events: np.ndarray, blob=None, stream=None):
             if len(idx):
                 descs = events_to_descs(events[idx])
                 cuts = [0] + [int(c) for c in __import__(__package__).plan_batches(descs)]
+                pkg = __import__(__package__)
                 for a, b in zip(cuts[:-1], cuts[1:]):
                     for s0 in range(a, b, chk.max_descs):
                         s1 = min(b, s0 + chk.max_descs)
                         dd = to_device_descs(descs[s0:s1], chk.device)
-                        dv = chk.check_copies(dd, stream=stream)
-                        chk.apply_dtoh(dd, dv, stream=stream)
+                        if fuse and pkg.batch_disjoint(descs[s0:s1]):
+                            dv = chk.check_apply(dd, stream=stream)
+                        else:
+                            dv = chk.check_copies(dd, stream=stream)
+                            chk.apply_dtoh(dd, dv, stream=stream)
                         v = verdicts_to_numpy(dv)
                         verdicts[copy_rank[idx[s0:s1]]] = v
                         status[idx[s0:s1]] = v["status"]

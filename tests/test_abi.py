@@ -104,3 +104,37 @@ def test_plan_batches_c2_single_epoch(cg):
     tr = tg.c2_small(n_copies=20000, n_allocs=2000)
     descs = events_to_descs(tr.events[tr.events["op"] == tg.OP_COPY])
     assert [int(c) for c in cg.plan_batches(descs)] == [len(descs)]
+
+
+def _disjoint_brute(descs):
+    def host(d):
+        if d["kind"] not in (1, 2) or d["width"] == 0 or d["height"] == 0:
+            return None
+        p = "src" if d["kind"] == 1 else "dst"
+        s = int(d[p]) + int(d[p + "_y"]) * int(d[p + "_pitch"]) + int(d[p + "_x"])
+        e = s + (int(d["height"]) - 1) * int(d[p + "_pitch"]) + int(d["width"])
+        return None if e > (1 << 64) - 1 else (s, e, int(d["kind"]))
+    r = [h for h in map(host, descs) if h]
+    for a in r:
+        for b in r:
+            if a[2] == 1 and b[2] == 2 and a[0] < b[1] and b[0] < a[1]:
+                return False
+    return True
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_batch_disjoint_matches_brute_force(cg, seed):
+    from paper_1310_0901_b200.replay import events_to_descs
+    tr = tg.random_tiny(seed)
+    descs = events_to_descs(tr.events[tr.events["op"] == tg.OP_COPY])
+    rng = np.random.default_rng(seed)
+    for _ in range(10):
+        a = int(rng.integers(0, len(descs)))
+        b = int(rng.integers(a, len(descs) + 1))
+        assert cg.batch_disjoint(descs[a:b]) == _disjoint_brute(descs[a:b])
+
+
+def test_batch_disjoint_configs(cg):
+    from paper_1310_0901_b200.replay import events_to_descs
+    for tr in (tg.c2_small(n_copies=20000, n_allocs=2000), tg.c4_pitched(n_copies=2000, n_bufs=2, rows=64)):
+        assert cg.batch_disjoint(events_to_descs(tr.events[tr.events["op"] == tg.OP_COPY]))

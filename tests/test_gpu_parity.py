@@ -41,10 +41,10 @@ def assert_verdicts_equal(gv, ov, where=""):
         assert len(bad) == 0, f"{where} field {f}: {len(bad)} mismatches, first at {bad[:5]}: gpu {a[bad[:5]]} oracle {b[bad[:5]]}"
 
 
-def run_parity(cg, tr, undef_is_error=False, **kw):
+def run_parity(cg, tr, undef_is_error=False, fuse=True, **kw):
     o, ov, os_, oleaks = oracle.replay_trace(tr, undef_is_error=undef_is_error)
     chk = new_checker(cg, tr, undef_is_error=undef_is_error, **kw)
-    gv, gs = cg.replay_events(chk, tr.events, tr.blob)
+    gv, gs = cg.replay_events(chk, tr.events, tr.blob, fuse=fuse)
     assert_verdicts_equal(gv, ov, tr.name)
     assert np.array_equal(gs, os_), np.flatnonzero(gs != os_)[:10]
     gl = chk.leak_report()
@@ -72,6 +72,12 @@ def test_random_tiny_traces(cg, seed):
     run_parity(cg, tg.random_tiny(seed))
 
 
+@pytest.mark.parametrize("seed", range(40))
+def test_random_tiny_unfused(cg, seed):
+    """check and apply as two calls (cg_check_copies + cg_apply_dtoh)"""
+    run_parity(cg, tg.random_tiny(seed + 3000), fuse=False)
+
+
 @pytest.mark.parametrize("seed", range(8))
 def test_random_tiny_undef_is_error(cg, seed):
     run_parity(cg, tg.random_tiny(seed + 7000), undef_is_error=True)
@@ -88,9 +94,10 @@ def test_small_max_descs_splits_batches(cg):
     run_parity(cg, tg.random_tiny(4242, n_events=300), max_descs=7)
 
 
-def test_c2_scaled(cg):
+@pytest.mark.parametrize("fuse", [True, False])
+def test_c2_scaled(cg, fuse):
     tr = tg.c2_small(n_copies=60000, n_allocs=6000)
-    v = run_parity(cg, tr)
+    v = run_parity(cg, tr, fuse=fuse)
     assert np.array_equal(v["flags"] != 0, tr.meta["inject"] != 0)
 
 
@@ -101,8 +108,9 @@ def test_c3_scaled(cg):
     assert v[0]["first_undef"] == tr.meta["hole_offsets"][0]
 
 
-def test_c3_dtoh_scaled(cg):
-    run_parity(cg, tg.c3_single(size=128 << 20, dtoh=True))
+@pytest.mark.parametrize("fuse", [True, False])
+def test_c3_dtoh_scaled(cg, fuse):
+    run_parity(cg, tg.c3_single(size=128 << 20, dtoh=True), fuse=fuse)
 
 
 def test_c4_scaled(cg):
