@@ -1024,21 +1024,29 @@ __device__ __forceinline__ void for_rows(const Norm& nm, uint64_t lo, uint64_t h
 constexpr uint64_t kApplyItemCost = 64;
 constexpr uint32_t kZeroPage = 4096;
 
+// The applicable descriptors (DtoH, status OK, host bytes) are compacted to
+// the front of weight[] / meta[] (order is irrelevant: the apply is idempotent
+// and commutative), so the apply walk never crosses runs of inapplicable
+// descriptors; weight[] must be zero on entry.
 // fusedP != nullptr: the check that just ran (cg_check_apply) already applied
 // every whole contiguous DtoH piece of its plan (fusedP, its chunk geometry);
-// only the remaining ones get weight here.
+// only the remaining ones are compacted here.
 __global__ void __launch_bounds__(kThreads) k_apply_prep(const cg_copy_desc* __restrict__ descs,
                                                          const cg_verdict* __restrict__ verd, uint64_t n,
                                                          uint64_t* __restrict__ weight, ScanMeta* __restrict__ meta,
+                                                         uint32_t* __restrict__ count,
                                                          const uint64_t* __restrict__ fusedP, uint64_t t_min,
                                                          uint64_t max_chunks) {
   uint64_t fT = 1;
   if (fusedP) fT = chunk_geom(fusedP, n, t_min, max_chunks).T;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (uint64_t b0 = (uint64_t)blockIdx.x * blockDim.x; b0 < n; b0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = b0 + threadIdx.x;
+    bool ok = false;
+    ScanMeta m;
     uint64_t w = 0;
-    const cg_copy_desc d = descs[i];
-    if (d.kind == CG_DTOH && verd[i].status == CG_OK) {
+    if (i < n && descs[i].kind == CG_DTOH && verd[i].status == CG_OK) {
+      const cg_copy_desc d = descs[i];
       const Norm nm = normalize(d);
       const bool contig = d.height == 1 || d.width == nm.hpitch;
       bool done = false;
@@ -1047,16 +1055,26 @@ __global__ void __launch_bounds__(kThreads) k_apply_prep(const cg_copy_desc* __r
         done = pd / fT == (pd1 - 1) / fT;
       }
       if (nm.host && nm.nbytes && !done) {
+        ok = true;
         w = kApplyItemCost + nm.nbytes;
-        ScanMeta m;
         m.hstart = nm.hstart;
         m.hpitch = nm.hpitch;
         m.W = nm.W;
         m.info = nm.nbytes | ((uint64_t)contig << 43);
-        meta[i] = m;
       }
     }
-    weight[i] = w;
+    const uint32_t mask = __ballot_sync(kFull, ok);
+    if (mask) {
+      const int leader = __ffs(mask) - 1;
+      uint32_t base = 0;
+      if (lane == leader) base = atomicAdd(count, (uint32_t)__popc(mask));
+      base = __shfl_sync(kFull, base, leader);
+      if (ok) {
+        const uint32_t k = base + __popc(mask & ((1u << lane) - 1u));
+        weight[k] = w;
+        meta[k] = m;
+      }
+    }
   }
 }
 
@@ -1341,8 +1359,10 @@ cudaError_t apply_dtoh(const Launch& L, const cg_copy_desc* d, const cg_verdict*
   if (n == 0) return cudaSuccess;
   ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
   L.stage(CG_STAGE_APPLY_PREP, true, s);
+  cudaMemsetAsync(p.weight, 0, n * sizeof(uint64_t), s);
+  cudaMemsetAsync(p.counter + 1, 0, sizeof(uint32_t), s);
   k_apply_prep<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(
-      d, v, n, p.weight, meta, after_fused ? p.P : nullptr, p.t_min, p.max_chunks);
+      d, v, n, p.weight, meta, p.counter + 1, after_fused ? p.P : nullptr, p.t_min, p.max_chunks);
   *L.counter += 1;
   L.stage(CG_STAGE_APPLY_PREP, false, s);
   L.stage(CG_STAGE_APPLY_PLAN, true, s);
