@@ -221,8 +221,9 @@ cg_status cg_registry_compact(cg_ctx *ctx, uint64_t before_seq);
  * the host shadow is read as of the call (snapshot), so the batch must be
  * hazard-free (no HtoD may overlap an earlier DtoH of the same batch; see
  * cg_plan_batches).  d_descs: device array of n cg_copy_desc; d_out: device
- * array of n cg_verdict (fully overwritten).  Asynchronous on stream.
- * Errors: CG_ERR_INVALID_VALUE (null, n > max_descs), CG_ERR_CUDA. */
+ * array of n cg_verdict (fully overwritten); both 16-byte aligned.
+ * Asynchronous on stream.
+ * Errors: CG_ERR_INVALID_VALUE (null, misaligned, n > max_descs), CG_ERR_CUDA. */
 cg_status cg_check_copies(cg_ctx *ctx, const cg_copy_desc *d_descs, uint64_t n, cg_verdict *d_out,
                           void *stream);
 

@@ -448,6 +448,7 @@ cg_status cg_check_copies(cg_ctx* c, const cg_copy_desc* d_descs, uint64_t n, cg
   if (!c) return CG_ERR_INVALID_CONTEXT;
   if (n == 0) return CG_OK;
   if (!d_descs || !d_out) return c->fail(CG_ERR_INVALID_VALUE, "null descriptor or verdict array");
+  if ((uintptr_t)d_descs % 16 || (uintptr_t)d_out % 16) return c->fail(CG_ERR_INVALID_VALUE, "arrays not 16-byte aligned");
   if (n > c->cfg.max_descs) return c->fail(CG_ERR_INVALID_VALUE, "n > max_descs");
   DeviceGuard g(c->cfg.device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -474,6 +475,7 @@ cg_status cg_check_apply(cg_ctx* c, const cg_copy_desc* d_descs, uint64_t n, cg_
   if (!c) return CG_ERR_INVALID_CONTEXT;
   if (n == 0) return CG_OK;
   if (!d_descs || !d_out) return c->fail(CG_ERR_INVALID_VALUE, "null descriptor or verdict array");
+  if ((uintptr_t)d_descs % 16 || (uintptr_t)d_out % 16) return c->fail(CG_ERR_INVALID_VALUE, "arrays not 16-byte aligned");
   if (n > c->cfg.max_descs) return c->fail(CG_ERR_INVALID_VALUE, "n > max_descs");
   DeviceGuard g(c->cfg.device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
