@@ -86,9 +86,18 @@ enum {
  *  - seq: position of the call in the program's single global event order
  *    (SPEC SimState.seq); the allocation table is evaluated "as of" seq
  *    (an allocation e is visible iff e.alloc_seq < seq < e.free_seq). */
+/* Shard mode bits of cg_copy_desc.reserved (host-address-range sharding
+ * across GPUs; 0 on a single GPU):
+ *  - CG_SHARD_NOT_OWNER: another shard owns the device side (no lookups here);
+ *  - CG_SHARD_RAW: the descriptor's host range spans several shards; this
+ *    shard writes only its raw partial (first_unaddr, first_undef, undef_count,
+ *    device fields, flags without HOST_*; status 0) for cg_straddler_pack /
+ *    cg_straddler_finalize after the collective merge. */
+enum { CG_SHARD_NOT_OWNER = 1u << 0, CG_SHARD_RAW = 1u << 1 };
+
 typedef struct {
   uint32_t kind;       /* CG_HTOD / CG_DTOH / CG_DTOD                  */
-  uint32_t reserved;   /* must be 0                                    */
+  uint32_t reserved;   /* shard mode bits (CG_SHARD_*), 0 on one GPU   */
   uint64_t seq;
   uint64_t width;      /* WidthInBytes                                 */
   uint64_t height;     /* Height (1 for 1D)                            */
@@ -195,6 +204,13 @@ cg_status cg_host_mark_batch(cg_ctx *ctx, const cg_mark *h_marks, uint64_t n, ui
 cg_status cg_host_set_vbits(cg_ctx *ctx, uint64_t addr, uint64_t len, const uint8_t *h_vbytes,
                             void *stream);
 
+/* Synchronous query: *all_addressable = 1 iff every byte of [addr, addr+len)
+ * that this context's shard stores is addressable and the range lies in the
+ * window (a sharded cg_host_set_vbits asks every shard first).  Errors:
+ * CG_ERR_INVALID_VALUE on NULL. */
+cg_status cg_host_query_addressable(cg_ctx *ctx, uint64_t addr, uint64_t len, uint32_t *all_addressable,
+                                    void *stream);
+
 /* Registers a device allocation (Fig. 2 caption P:88: "Each allocation
  * generates a new entry into the list"; SPEC register_linear S:139-147).
  * seq must exceed the seq of every earlier successful cg_register_alloc /
@@ -256,6 +272,37 @@ cg_status cg_batch_disjoint(const cg_copy_desc *h_descs, uint64_t n, int *disjoi
  * cg_check_copies; CG_ERR_NOT_INITIALIZED without host staging. */
 cg_status cg_check_copies_host(cg_ctx *ctx, const cg_copy_desc *h_descs, uint64_t n, cg_verdict *h_out,
                                int apply, void *stream);
+
+/* Straddler exchange, step 1 (device, asynchronous): the m raw partial
+ * verdicts d_raw (CG_SHARD_RAW descriptors, in the same order on every shard)
+ * become three arrays for collectives: d_mins[2m] (reduce with MIN, u64),
+ * d_sums[5m] (SUM, u64), d_maxs[m] (MAX, u32).  Errors: CG_ERR_INVALID_VALUE
+ * on NULL. */
+cg_status cg_straddler_pack(cg_ctx *ctx, const cg_verdict *d_raw, uint64_t m, uint64_t *d_mins,
+                            uint64_t *d_sums, uint32_t *d_maxs, void *stream);
+
+/* Straddler exchange, step 2: after the three all-reduces over all shards,
+ * writes the m final verdicts (flags and status derived exactly as for an
+ * unsharded descriptor) to d_out.  Errors: CG_ERR_INVALID_VALUE on NULL. */
+cg_status cg_straddler_finalize(cg_ctx *ctx, const uint64_t *d_mins, const uint64_t *d_sums,
+                                const uint32_t *d_maxs, uint64_t m, cg_verdict *d_out, void *stream);
+
+/* Verdicts with any flag set -> d_idx[k] (position in d_verdicts) and
+ * d_dirty[k], k < *d_count (a device u32; order not specified).  Clean
+ * verdicts are canonical ({NONE, NONE, 0, 0, 0, 0, 0, 0, 0}), so (count, idx,
+ * dirty) reconstruct the array -- the payload of the verdict gather to the
+ * root.  d_idx / d_dirty need room for n entries.  Asynchronous. */
+cg_status cg_compact_dirty(cg_ctx *ctx, const cg_verdict *d_verdicts, uint64_t n, uint64_t *d_idx,
+                           cg_verdict *d_dirty, uint32_t *d_count, void *stream);
+
+/* Host helper for host-address-range sharding over `world` equal shards of
+ * the window [host_base, host_base + host_size): per descriptor, the owner
+ * shard (the one holding the host start, clamped into the window; index mod
+ * world without a host side) and the first/last shard holding shadow bytes of
+ * its host range (first < last: a straddler).  Errors: CG_ERR_INVALID_VALUE if
+ * the shards are not multiples of 4096 or on NULL. */
+cg_status cg_shard_plan(const cg_copy_desc *h_descs, uint64_t n, uint64_t host_base, uint64_t host_size,
+                        uint32_t world, uint32_t *h_owner, uint32_t *h_first, uint32_t *h_last);
 
 /* Leak sweep on the device: writes the live allocations
  * (ascending base) to d_out (at most cap records) and their total number to

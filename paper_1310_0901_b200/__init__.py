@@ -92,6 +92,11 @@ def _load() -> ctypes.CDLL:
         "cg_apply_dtoh": (I, [P, P, P, U64, P]),
         "cg_check_copies_host": (I, [P, P, U64, P, I, P]),
         "cg_check_apply": (I, [P, P, U64, P, P]),
+        "cg_straddler_pack": (I, [P, P, U64, P, P, P, P]),
+        "cg_straddler_finalize": (I, [P, P, P, P, U64, P, P]),
+        "cg_compact_dirty": (I, [P, P, U64, P, P, P, P]),
+        "cg_host_query_addressable": (I, [P, U64, U64, P, P]),
+        "cg_shard_plan": (I, [P, U64, U64, U64, U32, P, P, P]),
         "cg_batch_disjoint": (I, [P, U64, P]),
         "cg_leak_sweep": (I, [P, P, U64, P, P]),
         "cg_leak_report": (I, [P, P, U64, P]),
@@ -112,7 +117,8 @@ EXPORTED = ("cg_workspace_size", "cg_ctx_create", "cg_ctx_destroy", "cg_last_err
             "cg_host_mark_batch", "cg_host_set_vbits", "cg_register_alloc", "cg_free", "cg_registry_compact",
             "cg_check_copies", "cg_apply_dtoh", "cg_check_copies_host", "cg_leak_sweep", "cg_leak_report",
             "cg_plan_batches", "cg_kernel_launches", "cg_profile_begin", "cg_profile_end", "cg_check_apply",
-            "cg_batch_disjoint")
+            "cg_batch_disjoint", "cg_straddler_pack", "cg_straddler_finalize", "cg_compact_dirty", "cg_shard_plan",
+            "cg_host_query_addressable")
 
 # ---- same-name thin wrappers (status codes returned unchanged) -------------
 cg_workspace_size = _lib.cg_workspace_size
@@ -129,6 +135,12 @@ cg_check_copies = _lib.cg_check_copies
 cg_apply_dtoh = _lib.cg_apply_dtoh
 cg_check_copies_host = _lib.cg_check_copies_host
 cg_check_apply = _lib.cg_check_apply
+cg_straddler_pack = _lib.cg_straddler_pack
+cg_straddler_finalize = _lib.cg_straddler_finalize
+cg_compact_dirty = _lib.cg_compact_dirty
+cg_host_query_addressable = _lib.cg_host_query_addressable
+cg_shard_plan = _lib.cg_shard_plan
+CG_SHARD_NOT_OWNER, CG_SHARD_RAW = 1, 2
 cg_batch_disjoint = _lib.cg_batch_disjoint
 cg_leak_sweep = _lib.cg_leak_sweep
 cg_leak_report = _lib.cg_leak_report
@@ -159,6 +171,17 @@ def batch_disjoint(descs: np.ndarray) -> bool:
     if st:
         raise CgError(st, "cg_batch_disjoint")
     return bool(out.value)
+
+
+def shard_plan(descs: np.ndarray, host_base: int, host_size: int, world: int):
+    """cg_shard_plan: (owner, first shard, last shard) per descriptor."""
+    d = np.ascontiguousarray(descs, dtype=DESC_DTYPE)
+    owner, first, last = (np.zeros(len(d), np.uint32) for _ in range(3))
+    st = _lib.cg_shard_plan(d.ctypes.data if len(d) else None, len(d), host_base, host_size, world,
+                            owner.ctypes.data, first.ctypes.data, last.ctypes.data)
+    if st:
+        raise CgError(st, "cg_shard_plan")
+    return owner, first, last
 
 
 def _stream_ptr(stream) -> Optional[int]:
@@ -239,6 +262,12 @@ class Checker:
         b = np.ascontiguousarray(np.frombuffer(bytes(vbytes), np.uint8))
         return _lib.cg_host_set_vbits(self.ctx, addr, len(b), b.ctypes.data if len(b) else None,
                                       _stream_ptr(stream))
+
+    def host_query_addressable(self, addr: int, length: int, stream=None) -> bool:
+        out = ctypes.c_uint32(0)
+        self._ok(_lib.cg_host_query_addressable(self.ctx, addr, length, ctypes.byref(out), _stream_ptr(stream)),
+                 "cg_host_query_addressable")
+        return bool(out.value)
 
     # ---- registry ------------------------------------------------------------
     def register_alloc(self, base: int, size: int, seq: int) -> int:

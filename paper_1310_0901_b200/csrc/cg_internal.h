@@ -78,6 +78,12 @@ cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_
                          cudaStream_t s);
 cudaError_t apply_dtoh(const Launch& L, const cg_copy_desc* d, const cg_verdict* v, uint64_t n,
                        const ShadowView& sv, const Plan& p, bool after_fused, cudaStream_t s);
+cudaError_t straddler_pack(const Launch& L, const cg_verdict* v, uint64_t m, uint64_t* mins, uint64_t* sums,
+                           uint32_t* maxs, cudaStream_t s);
+cudaError_t straddler_finalize(const Launch& L, const uint64_t* mins, const uint64_t* sums, const uint32_t* maxs,
+                               uint64_t m, cg_verdict* v, uint32_t err_mask, cudaStream_t s);
+cudaError_t compact_dirty(const Launch& L, const cg_verdict* v, uint64_t n, uint64_t* idx, cg_verdict* dirty,
+                          uint32_t* count, cudaStream_t s);
 cudaError_t mark_batch(const Launch& L, const cg_mark* d_marks, uint64_t n, const ShadowView& sv,
                        const Plan& p, cudaStream_t s);
 cudaError_t fresh_shadow(const Launch& L, const ShadowView& sv, cudaStream_t s);

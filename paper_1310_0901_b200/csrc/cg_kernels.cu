@@ -242,7 +242,8 @@ __global__ void __launch_bounds__(kThreads) k_check_prep(const cg_copy_desc* __r
     const Norm nm = normalize(d);
     uint32_t flags = nm.flags;
     uint64_t de = 0, df = 0, se = 0, sf = 0;
-    if (!(flags & CG_F_BAD_KIND)) {
+    const bool owner = !(d.reserved & CG_SHARD_NOT_OWNER);   // only the owner shard looks up the device side
+    if (!(flags & CG_F_BAD_KIND) && owner) {
       uint64_t end;
       if ((nm.kind == CG_HTOD || nm.kind == CG_DTOD) && nm.dok) {      // dst side first
         if (!table_lookup(t, s_split, nm.ds, d.seq, end)) {
@@ -280,8 +281,9 @@ __global__ void __launch_bounds__(kThreads) k_check_prep(const cg_copy_desc* __r
     m.hpitch = nm.hpitch;
     m.W = nm.W;
     const bool contig = d.height == 1 || d.width == nm.hpitch;
+    const bool raw = d.reserved & CG_SHARD_RAW;   // partial of a straddler: no finalisation here
     m.info = nm.nbytes | ((uint64_t)(nm.kind & 3u) << 40) | ((uint64_t)nm.host << 42) | ((uint64_t)contig << 43) |
-             ((uint64_t)flags << 48);
+             ((uint64_t)raw << 44) | ((uint64_t)flags << 48);
     meta[i] = m;
   }
 }
@@ -432,7 +434,7 @@ constexpr int kStages = 3;
 constexpr uint32_t kTileV = 4096;      // HtoD: V bytes per tile
 constexpr uint32_t kTileA = kTileV / 8;
 constexpr uint32_t kDtohBlock = 32768; // DtoH: host bytes per tile (4 KiB of A)
-constexpr uint32_t kTileData = 1, kTileHtod = 2, kTileEnd = 4, kTileWhole = 8, kTileFuse = 16;
+constexpr uint32_t kTileData = 1, kTileHtod = 2, kTileEnd = 4, kTileWhole = 8, kTileFuse = 16, kTileRaw = 32;
 
 struct __align__(16) TileInfo {
   uint64_t ob;        // logical offset of staged host byte 0
@@ -717,7 +719,9 @@ struct TileGen {
       p_fl = f;
       if (f & kPieceEmpty) {
         cg_verdict* v = out + (wbase + lane);
-        if (f & kPieceWhole) {
+        if ((f & kPieceWhole) && ((m_info >> 44) & 1u)) {
+          v->first_unaddr = p_fu;   // raw partial (straddler): finalised after the merge
+        } else if (f & kPieceWhole) {
           uint32_t flags = (uint32_t)(m_info >> 48), status;
           finalize_fields(flags, status, p_fu, 0, err_mask);
           v->first_unaddr = p_fu;
@@ -734,7 +738,7 @@ struct TileGen {
     const bool live = (p_fl & (kPieceIn | kPiece2D | kPieceEmpty)) == kPieceIn;
     set_segment(live, p_qs, p_qe, p_ob, p_fu, (uint32_t)(wbase + lane),
                 (p_fl & kPieceHtod ? kTileHtod : 0u) | (p_fl & kPieceWhole ? kTileWhole : 0u) | kSegEndLast |
-                    ((uint32_t)(m_info >> 48) << 16));
+                    (((m_info >> 44) & 1u) ? kTileRaw : 0u) | ((uint32_t)(m_info >> 48) << 16));
     phase = kPhaseContig;
   }
 
@@ -828,9 +832,10 @@ struct TileGen {
           lo2 = __shfl_sync(kFull, p_lo, src);
           hi2 = __shfl_sync(kFull, p_hi, src);
           const uint32_t pf = __shfl_sync(kFull, p_fl, src);
-          const uint32_t prep = (uint32_t)(__shfl_sync(kFull, m_info, src) >> 48);
+          const uint64_t info = __shfl_sync(kFull, m_info, src);
           d2 = (uint32_t)(wbase + src);
-          fl2 = (pf & kPieceHtod ? kTileHtod : 0u) | (pf & kPieceWhole ? kTileWhole : 0u) | (prep << 16);
+          fl2 = (pf & kPieceHtod ? kTileHtod : 0u) | (pf & kPieceWhole ? kTileWhole : 0u) |
+                (((info >> 44) & 1u) ? kTileRaw : 0u) | ((uint32_t)(info >> 48) << 16);
           r2 = lo2 / W;
           fu2 = kNone;
           in2d = true;
@@ -866,7 +871,7 @@ struct TileGen {
       uint32_t f = kTileData | (s_fl & ~(kSegEndLast | kTileWhole));
       if (j + 1 == s_k && (s_fl & kSegEndLast)) {
         f |= kTileEnd | (s_fl & kTileWhole);
-        if (fuse && !htod) {   // a contiguous DtoH piece: the consumer may apply it
+        if (fuse && !htod && !(s_fl & kTileRaw)) {   // a contiguous DtoH piece: the consumer may apply it
           f |= kTileFuse;
           ti.qs = s_q0;
           ti.qe = s_q1;
@@ -953,7 +958,11 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
       bool apply = false;
       if (lane == 0) {
         cg_verdict* v = out + t.d;
-        if (t.flags & kTileWhole) {
+        if ((t.flags & (kTileWhole | kTileRaw)) == (kTileWhole | kTileRaw)) {
+          v->first_unaddr = p.fu;   // raw partial (straddler): finalised after the merge
+          v->first_undef = p.fd;
+          v->undef_count = p.cnt;
+        } else if (t.flags & kTileWhole) {
           uint32_t flags = t.flags >> 16, status;
           finalize_fields(flags, status, p.fu, p.cnt, err_mask);
           v->first_unaddr = p.fu;
@@ -981,12 +990,14 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
 // a5 for descriptors split across groups
 __global__ void __launch_bounds__(kThreads) k_finalize_split(uint64_t n, const uint64_t* __restrict__ P,
                                                              uint64_t t_min, uint64_t max_chunks,
-                                                             cg_verdict* __restrict__ out, uint32_t err_mask) {
+                                                             cg_verdict* __restrict__ out, uint32_t err_mask,
+                                                             const ScanMeta* __restrict__ meta) {
   const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
   for (uint64_t d = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; d < n;
        d += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t pd = P[d], pd1 = P[d + 1];
     if (pd1 == pd || pd / g.T == (pd1 - 1) / g.T) continue;
+    if ((meta[d].info >> 44) & 1u) continue;   // raw partial of a straddler
     cg_verdict* v = out + d;
     uint32_t flags = v->flags, status;
     finalize_fields(flags, status, v->first_unaddr, v->undef_count, err_mask);
@@ -1045,7 +1056,9 @@ __global__ void __launch_bounds__(kThreads) k_apply_prep(const cg_copy_desc* __r
     bool ok = false;
     ScanMeta m;
     uint64_t w = 0;
-    if (i < n && descs[i].kind == CG_DTOH && verd[i].status == CG_OK) {
+    // after a fused check, straddler partials (CG_SHARD_RAW) are not final yet
+    if (i < n && descs[i].kind == CG_DTOH && verd[i].status == CG_OK &&
+        !(fusedP && (descs[i].reserved & CG_SHARD_RAW))) {
       const cg_copy_desc d = descs[i];
       const Norm nm = normalize(d);
       const bool contig = d.height == 1 || d.width == nm.hpitch;
@@ -1277,6 +1290,73 @@ __global__ void k_setv_check(ShadowView sv, uint64_t addr, uint64_t len, uint32_
 }
 
 // ---------------------------------------------------------------------------
+// e: straddler exchange (descriptors whose host range spans several shards)
+// ---------------------------------------------------------------------------
+// Raw partials of m straddlers -> structure of arrays for three collectives:
+// mins[2m] = {first_unaddr, first_undef}, sums[5m] = {undef_count, dst_expected,
+// dst_found, src_expected, src_found} (only the owner shard has nonzero device
+// fields), maxs[m] = flags (validation flags are identical on every shard and
+// only the owner adds device flags, so MAX = OR here).
+__global__ void k_straddler_pack(const cg_verdict* __restrict__ v, uint64_t m, uint64_t* __restrict__ mins,
+                                 uint64_t* __restrict__ sums, uint32_t* __restrict__ maxs) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const cg_verdict x = v[i];
+    mins[i] = x.first_unaddr;
+    mins[m + i] = x.first_undef;
+    sums[i] = x.undef_count;
+    sums[m + i] = x.dst_expected;
+    sums[2 * m + i] = x.dst_found;
+    sums[3 * m + i] = x.src_expected;
+    sums[4 * m + i] = x.src_found;
+    maxs[i] = x.flags;
+  }
+}
+
+// merged fields -> final verdicts (a5 after the exchange)
+__global__ void k_straddler_finalize(const uint64_t* __restrict__ mins, const uint64_t* __restrict__ sums,
+                                     const uint32_t* __restrict__ maxs, uint64_t m, cg_verdict* __restrict__ v,
+                                     uint32_t err_mask) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    cg_verdict x;
+    x.first_unaddr = mins[i];
+    x.first_undef = mins[m + i];
+    x.undef_count = sums[i];
+    x.dst_expected = sums[m + i];
+    x.dst_found = sums[2 * m + i];
+    x.src_expected = sums[3 * m + i];
+    x.src_found = sums[4 * m + i];
+    x.flags = maxs[i];
+    finalize_fields(x.flags, x.status, x.first_unaddr, x.undef_count, err_mask);
+    v[i] = x;
+  }
+}
+
+// verdicts with any flag (order not kept) -> (index, verdict) lists for the
+// gather to the root; clean verdicts are canonical and are not sent
+__global__ void k_compact_dirty(const cg_verdict* __restrict__ v, uint64_t n, uint64_t* __restrict__ idx,
+                                cg_verdict* __restrict__ dirty, uint32_t* __restrict__ count) {
+  const int lane = threadIdx.x & 31;
+  for (uint64_t b0 = (uint64_t)blockIdx.x * blockDim.x; b0 < n; b0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = b0 + threadIdx.x;
+    const bool d = i < n && v[i].flags != 0;
+    const uint32_t mask = __ballot_sync(kFull, d);
+    if (mask) {
+      const int leader = __ffs(mask) - 1;
+      uint32_t base = 0;
+      if (lane == leader) base = atomicAdd(count, (uint32_t)__popc(mask));
+      base = __shfl_sync(kFull, base, leader);
+      if (d) {
+        const uint32_t k = base + __popc(mask & ((1u << lane) - 1u));
+        idx[k] = i;
+        dirty[k] = v[i];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // a8: leak sweep
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) k_live(Table t, uint64_t* __restrict__ weight) {
@@ -1348,7 +1428,7 @@ cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_
   L.stage(CG_STAGE_CHECK_SCAN, false, s);
   L.stage(CG_STAGE_CHECK_FINAL, true, s);
   k_finalize_split<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(n, p.P, p.t_min, p.max_chunks,
-                                                                               out, err_mask);
+                                                                               out, err_mask, meta);
   L.stage(CG_STAGE_CHECK_FINAL, false, s);
   *L.counter += 2;
   return cudaGetLastError();
@@ -1417,6 +1497,32 @@ cudaError_t leak_sweep(const Launch& L, const Table& t, const Plan& p, cg_alloc_
   k_leak_scatter<<<blocks_for(t.n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(t, p.P, out, cap, d_count);
   L.stage(CG_STAGE_LEAK, false, s);
   *L.counter += 5;
+  return cudaGetLastError();
+}
+
+cudaError_t straddler_pack(const Launch& L, const cg_verdict* v, uint64_t m, uint64_t* mins, uint64_t* sums,
+                           uint32_t* maxs, cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  k_straddler_pack<<<blocks_for(m, kThreads, L.num_sms * 8), kThreads, 0, s>>>(v, m, mins, sums, maxs);
+  *L.counter += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t straddler_finalize(const Launch& L, const uint64_t* mins, const uint64_t* sums, const uint32_t* maxs,
+                               uint64_t m, cg_verdict* v, uint32_t err_mask, cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  k_straddler_finalize<<<blocks_for(m, kThreads, L.num_sms * 8), kThreads, 0, s>>>(mins, sums, maxs, m, v,
+                                                                                    err_mask);
+  *L.counter += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t compact_dirty(const Launch& L, const cg_verdict* v, uint64_t n, uint64_t* idx, cg_verdict* dirty,
+                          uint32_t* count, cudaStream_t s) {
+  cudaMemsetAsync(count, 0, sizeof(uint32_t), s);
+  if (n == 0) return cudaGetLastError();
+  k_compact_dirty<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(v, n, idx, dirty, count);
+  *L.counter += 1;
   return cudaGetLastError();
 }
 

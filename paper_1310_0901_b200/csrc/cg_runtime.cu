@@ -392,6 +392,29 @@ cg_status cg_host_set_vbits(cg_ctx* c, uint64_t addr, uint64_t len, const uint8_
   return c->cuda(e, "set_vbits copy");
 }
 
+cg_status cg_host_query_addressable(cg_ctx* c, uint64_t addr, uint64_t len, uint32_t* all_addressable, void* stream) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (!all_addressable) return c->fail(CG_ERR_INVALID_VALUE, "null output");
+  *all_addressable = 1;
+  if (len == 0) return CG_OK;
+  if (!in_window(c, addr, len)) {
+    *all_addressable = 0;
+    return CG_OK;
+  }
+  const uint64_t y0 = std::max(addr, c->sv.sb), y1 = std::min(addr + len, c->sv.se);
+  if (y0 >= y1) return CG_OK;
+  DeviceGuard g(c->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint32_t* flag = reinterpret_cast<uint32_t*>(c->ws + c->lay.flags);
+  cudaError_t e = cgk::setv_check(c->launch, addr, len, c->sv, flag, s);
+  uint32_t h_flag = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h_flag, flag, sizeof h_flag, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return c->cuda(e, "addressability query");
+  *all_addressable = h_flag ? 0 : 1;
+  return CG_OK;
+}
+
 cg_status cg_register_alloc(cg_ctx* c, uint64_t base, uint64_t size, uint64_t seq) {
   if (!c) return CG_ERR_INVALID_CONTEXT;
   if (size == 0 || base == 0) return c->fail(CG_ERR_INVALID_VALUE, "register: size 0 or base 0");
@@ -511,6 +534,36 @@ cg_status cg_check_copies_host(cg_ctx* c, const cg_copy_desc* h_descs, uint64_t 
   return c->cuda(e, "verdict download");
 }
 
+cg_status cg_straddler_pack(cg_ctx* c, const cg_verdict* d_raw, uint64_t m, uint64_t* d_mins, uint64_t* d_sums,
+                            uint32_t* d_maxs, void* stream) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (m == 0) return CG_OK;
+  if (!d_raw || !d_mins || !d_sums || !d_maxs) return c->fail(CG_ERR_INVALID_VALUE, "null straddler arrays");
+  DeviceGuard g(c->cfg.device);
+  return c->cuda(cgk::straddler_pack(c->launch, d_raw, m, d_mins, d_sums, d_maxs, static_cast<cudaStream_t>(stream)),
+                 "straddler pack");
+}
+
+cg_status cg_straddler_finalize(cg_ctx* c, const uint64_t* d_mins, const uint64_t* d_sums, const uint32_t* d_maxs,
+                                uint64_t m, cg_verdict* d_out, void* stream) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (m == 0) return CG_OK;
+  if (!d_out || !d_mins || !d_sums || !d_maxs) return c->fail(CG_ERR_INVALID_VALUE, "null straddler arrays");
+  DeviceGuard g(c->cfg.device);
+  return c->cuda(cgk::straddler_finalize(c->launch, d_mins, d_sums, d_maxs, m, d_out, c->err_mask(),
+                                         static_cast<cudaStream_t>(stream)),
+                 "straddler finalize");
+}
+
+cg_status cg_compact_dirty(cg_ctx* c, const cg_verdict* d_verdicts, uint64_t n, uint64_t* d_idx,
+                           cg_verdict* d_dirty, uint32_t* d_count, void* stream) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (!d_count || (n && (!d_verdicts || !d_idx || !d_dirty))) return c->fail(CG_ERR_INVALID_VALUE, "null arrays");
+  DeviceGuard g(c->cfg.device);
+  return c->cuda(cgk::compact_dirty(c->launch, d_verdicts, n, d_idx, d_dirty, d_count, static_cast<cudaStream_t>(stream)),
+                 "compact dirty");
+}
+
 cg_status cg_leak_sweep(cg_ctx* c, cg_alloc_record* d_out, uint64_t cap, uint64_t* d_count, void* stream) {
   if (!c) return CG_ERR_INVALID_CONTEXT;
   if (!d_count || (cap && !d_out)) return c->fail(CG_ERR_INVALID_VALUE, "null output");
@@ -580,6 +633,35 @@ cg_status cg_batch_disjoint(const cg_copy_desc* h_descs, uint64_t n, int* disjoi
       end_d = seen_d ? std::max(end_d, x.hi) : x.hi;
       seen_d = true;
     }
+  }
+  return CG_OK;
+}
+
+cg_status cg_shard_plan(const cg_copy_desc* h_descs, uint64_t n, uint64_t host_base, uint64_t host_size,
+                        uint32_t world, uint32_t* h_owner, uint32_t* h_first, uint32_t* h_last) {
+  if (world == 0 || host_size == 0 || host_size % world || (host_size / world) % 4096) return CG_ERR_INVALID_VALUE;
+  if (n && (!h_descs || !h_owner || !h_first || !h_last)) return CG_ERR_INVALID_VALUE;
+  const uint64_t shard = host_size / world, we = host_base + host_size;
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t lo, hi;
+    uint32_t owner = (uint32_t)(i % world), first = owner, last = owner;
+    if (host_range(h_descs[i], lo, hi)) {
+      // owner: the shard holding the host start (clamped into the window)
+      const uint64_t s0 = lo < host_base ? 0 : lo >= we ? host_size - 1 : lo - host_base;
+      owner = (uint32_t)(s0 / shard);
+      const uint64_t a = std::max(lo, host_base), b = std::min(hi, we);
+      if (a < b) {   // shards holding shadow bytes of the range
+        first = (uint32_t)((a - host_base) / shard);
+        last = (uint32_t)((b - 1 - host_base) / shard);
+        if (owner < first) first = owner;
+        if (owner > last) last = owner;
+      } else {
+        first = last = owner;
+      }
+    }
+    h_owner[i] = owner;
+    h_first[i] = first;
+    h_last[i] = last;
   }
   return CG_OK;
 }

@@ -1,0 +1,311 @@
+"""Host-address-range sharding across GPUs (BASELINE north_star:
+"The shadow address space and copy batch are partitioned across the 8 B200s
+by host-address range, with an NCCL gather over NVLink only for the
+per-descriptor verdicts").
+
+Rank r stores the shadow of shard r = [H0 + r*S/G, H0 + (r+1)*S/G) of the
+global window (its context's shard) and replays every setup event (only its
+shard part is stored; the allocation table is replicated).  A batch is split
+with cg_shard_plan:
+
+* a descriptor whose host range lies in one shard goes to that shard's rank
+  only (the owner), which finalises it locally;
+* a straddler (host range over several shards) goes to every rank, flagged
+  CG_SHARD_RAW (and CG_SHARD_NOT_OWNER except on its owner): each rank writes
+  its raw partial, the partials are merged with three all-reduces (MIN of the
+  first offsets, SUM of the count and of the owner-only device fields, MAX of
+  the flags -- validation flags are identical everywhere, device flags come
+  from the owner only, so MAX = OR), and cg_straddler_finalize derives flags
+  and status on every rank; each rank then applies its shard part of the
+  straddling DtoH copies whose merged verdict is OK;
+* the root gathers every rank's dirty verdicts (cg_compact_dirty: clean
+  verdicts are canonical and are not sent) plus their counts and assembles the
+  dense verdict array.
+
+Two communicators implement the same three collectives: TorchComm
+(torch.distributed -- NCCL over NVLink on GPUs) and LoopbackGroup (G shards in
+one process on one GPU, reductions across the G tensors) for single-GPU
+testing.  The descriptors' reserved field carries the shard mode bits.
+"""
+from __future__ import annotations
+
+from typing import List, Optional
+
+import numpy as np
+
+from . import (CG_NONE, CG_SHARD_NOT_OWNER, CG_SHARD_RAW, DESC_DTYPE, VERDICT_DTYPE, Checker, CgError, _lib,
+               _stream_ptr, shard_plan, batch_disjoint, to_device_descs)
+
+
+class BatchPlan:
+    """Per-rank descriptor lists of one batch (identical on every rank)."""
+
+    def __init__(self, descs: np.ndarray, host_base: int, host_size: int, world: int):
+        self.n = len(descs)
+        self.world = world
+        owner, first, last = shard_plan(descs, host_base, host_size, world)
+        self.owner = owner
+        self.straddler = first < last
+        self.strad_idx = np.flatnonzero(self.straddler)
+        self.mine_idx = [np.flatnonzero((owner == r) & ~self.straddler) for r in range(world)]
+        self.descs = descs
+
+    def local(self, rank: int):
+        """(local descriptors with mode bits, global indices, n_mine, m)."""
+        mine, strad = self.mine_idx[rank], self.strad_idx
+        idx = np.concatenate([mine, strad])
+        d = np.ascontiguousarray(self.descs[idx]).copy()
+        d["reserved"] = 0
+        if len(strad):
+            bits = np.full(len(strad), CG_SHARD_RAW, np.uint32)
+            bits[self.owner[strad] != rank] |= CG_SHARD_NOT_OWNER
+            d["reserved"][len(mine):] = bits
+        return d, idx, len(mine), len(strad)
+
+
+class ShardedChecker:
+    """One rank: a Checker over its shard of the global window."""
+
+    def __init__(self, host_base: int, host_size: int, rank: int, world: int, device: int = 0, **kw):
+        if host_size % world or (host_size // world) % 4096:
+            raise CgError(1, "shards must be multiples of 4096 bytes")
+        self.host_base, self.host_size, self.rank, self.world = host_base, host_size, rank, world
+        shard = host_size // world
+        self.chk = Checker(host_base, host_size, shard_base=host_base + rank * shard, shard_size=shard,
+                           device=device, **kw)
+        self.device = device
+        self.torch = self.chk.torch
+
+    def close(self):
+        self.chk.close()
+
+    # ---- per-rank steps (all in the library's kernels) ---------------------
+    def check(self, plan: BatchPlan, fuse: bool):
+        d, idx, n_mine, m = plan.local(self.rank)
+        dd = to_device_descs(d, self.device)
+        # fused only when the rank's whole batch is apply-disjoint
+        fused = fuse and batch_disjoint(d)
+        dv = self.chk.check_apply(dd) if fused else self.chk.check_copies(dd)
+        return dict(dd=dd, dv=dv, idx=idx, n_mine=n_mine, m=m, fused=fused)
+
+    def pack(self, st):
+        torch, m = self.torch, st["m"]
+        mins = torch.empty(2 * m, dtype=torch.int64, device=self.device)
+        sums = torch.empty(5 * m, dtype=torch.int64, device=self.device)
+        maxs = torch.empty(m, dtype=torch.int32, device=self.device)
+        if m:
+            raw = st["dv"].data_ptr() + st["n_mine"] * VERDICT_DTYPE.itemsize
+            self.chk._ok(_lib.cg_straddler_pack(self.chk.ctx, raw, m, mins.data_ptr(), sums.data_ptr(),
+                                                maxs.data_ptr(), _stream_ptr(None)), "cg_straddler_pack")
+        return mins, sums, maxs
+
+    def finalize(self, st, mins, sums, maxs):
+        m = st["m"]
+        if m:
+            out = st["dv"].data_ptr() + st["n_mine"] * VERDICT_DTYPE.itemsize
+            self.chk._ok(_lib.cg_straddler_finalize(self.chk.ctx, mins.data_ptr(), sums.data_ptr(), maxs.data_ptr(),
+                                                    m, out, _stream_ptr(None)), "cg_straddler_finalize")
+
+    def apply(self, st):
+        """DtoH apply after the merge: the straddlers (each rank its shard
+        part), plus everything if the check was not fused."""
+        W = VERDICT_DTYPE.itemsize
+        if not st["fused"]:
+            self.chk.apply_dtoh(st["dd"], st["dv"])
+        elif st["m"]:
+            n0 = st["n_mine"] * DESC_DTYPE.itemsize
+            self.chk.apply_dtoh(st["dd"][n0:], st["dv"][st["n_mine"] * W:])
+
+    def compact(self, st):
+        torch, n = self.torch, st["n_mine"]
+        idx = torch.empty(max(n, 1), dtype=torch.int64, device=self.device)
+        dirty = torch.empty(max(n, 1) * VERDICT_DTYPE.itemsize, dtype=torch.uint8, device=self.device)
+        cnt = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.chk._ok(_lib.cg_compact_dirty(self.chk.ctx, st["dv"].data_ptr(), n, idx.data_ptr(), dirty.data_ptr(),
+                                           cnt.data_ptr(), _stream_ptr(None)), "cg_compact_dirty")
+        return cnt, idx, dirty
+
+
+def _clean(n: int) -> np.ndarray:
+    v = np.zeros(n, VERDICT_DTYPE)
+    v["first_unaddr"] = CG_NONE
+    v["first_undef"] = CG_NONE
+    return v
+
+
+def _assemble(plan: BatchPlan, per_rank, strad_dv) -> np.ndarray:
+    """Dense verdicts from every rank's (count, local idx, dirty) + the merged
+    straddlers (root side)."""
+    out = _clean(plan.n)
+    for r, (cnt, idx, dirty) in enumerate(per_rank):
+        c = int(cnt)
+        if c:
+            gidx = plan.mine_idx[r][idx[:c]]
+            out[gidx] = dirty[:c]
+    if len(plan.strad_idx):
+        out[plan.strad_idx] = strad_dv
+    return out
+
+
+class TorchComm:
+    """Collectives over torch.distributed (NCCL on GPUs)."""
+
+    def __init__(self):
+        import torch.distributed as dist
+        self.dist = dist
+
+    def allreduce3(self, mins, sums, maxs):
+        d = self.dist
+        if mins.numel():
+            d.all_reduce(mins, op=d.ReduceOp.MIN)   # u64 order mapped onto i64 by the caller
+            d.all_reduce(sums, op=d.ReduceOp.SUM)
+            d.all_reduce(maxs, op=d.ReduceOp.MAX)
+
+    def gather_dirty(self, cnt, idx, dirty, root: int = 0):
+        """all ranks' (count, idx, dirty) -> list on every rank (padded all_gather)."""
+        import torch
+        d = self.dist
+        world = d.get_world_size()
+        counts = [torch.zeros(1, dtype=torch.int32, device=cnt.device) for _ in range(world)]
+        d.all_gather(counts, cnt)
+        mx = max(1, max(int(c.item()) for c in counts))
+        W = VERDICT_DTYPE.itemsize
+        pi = torch.zeros(mx, dtype=torch.int64, device=cnt.device)
+        pd = torch.zeros(mx * W, dtype=torch.uint8, device=cnt.device)
+        c0 = int(cnt.item())
+        pi[:c0] = idx[:c0]
+        pd[:c0 * W] = dirty[:c0 * W]
+        gi = [torch.empty_like(pi) for _ in range(world)]
+        gd = [torch.empty_like(pd) for _ in range(world)]
+        d.all_gather(gi, pi)
+        d.all_gather(gd, pd)
+        return [(int(counts[r].item()), gi[r].cpu().numpy(), gd[r].cpu().numpy().view(VERDICT_DTYPE))
+                for r in range(world)]
+
+
+def _u64_min_fix(t):
+    """MIN over u64 fields held in int64 tensors: map u64 order onto i64 order
+    (flip the sign bit) before and after the reduction."""
+    return t ^ (-(1 << 63))
+
+
+def run_distributed(sc: ShardedChecker, plan: BatchPlan, comm: Optional[TorchComm] = None, fuse: bool = True,
+                    root: int = 0) -> Optional[np.ndarray]:
+    """One rank's part of a sharded batch; returns the dense verdicts on root."""
+    comm = comm or TorchComm()
+    st = sc.check(plan, fuse)
+    mins, sums, maxs = sc.pack(st)
+    if st["m"]:
+        mins = _u64_min_fix(mins)
+        comm.allreduce3(mins, sums, maxs)
+        mins = _u64_min_fix(mins)
+    sc.finalize(st, mins, sums, maxs)
+    sc.apply(st)
+    cnt, idx, dirty = sc.compact(st)
+    gathered = comm.gather_dirty(cnt, idx, dirty, root)
+    if sc.rank != root:
+        return None
+    W = VERDICT_DTYPE.itemsize
+    strad = st["dv"][st["n_mine"] * W:].cpu().numpy().view(VERDICT_DTYPE)
+    return _assemble(plan, gathered, strad)
+
+
+class LoopbackGroup:
+    """G shards in one process on one GPU: the same per-rank kernels, with the
+    three all-reduces and the gather done across the G device tensors."""
+
+    def __init__(self, host_base: int, host_size: int, world: int, device: int = 0, **kw):
+        self.ranks = [ShardedChecker(host_base, host_size, r, world, device, **kw) for r in range(world)]
+        self.host_base, self.host_size, self.world = host_base, host_size, world
+
+    def close(self):
+        for r in self.ranks:
+            r.close()
+
+    def run(self, plan: BatchPlan, fuse: bool = True) -> np.ndarray:
+        import torch
+        sts = [sc.check(plan, fuse) for sc in self.ranks]
+        packed = [sc.pack(st) for sc, st in zip(self.ranks, sts)]
+        if plan.strad_idx.size:
+            mins = _u64_min_fix(torch.stack([_u64_min_fix(p[0]) for p in packed]).min(0).values)
+            sums = torch.stack([p[1] for p in packed]).sum(0)
+            maxs = torch.stack([p[2] for p in packed]).max(0).values
+        for sc, st, p in zip(self.ranks, sts, packed):
+            if st["m"]:
+                sc.finalize(st, mins.clone(), sums.clone(), maxs.clone())
+            sc.apply(st)
+        per_rank = []
+        for sc, st in zip(self.ranks, sts):
+            cnt, idx, dirty = sc.compact(st)
+            c = int(cnt.item())
+            per_rank.append((c, idx[:max(c, 1)].cpu().numpy(),
+                             dirty[:max(c, 1) * VERDICT_DTYPE.itemsize].cpu().numpy().view(VERDICT_DTYPE)))
+        W = VERDICT_DTYPE.itemsize
+        st0 = sts[0]
+        strad = st0["dv"][st0["n_mine"] * W:].cpu().numpy().view(VERDICT_DTYPE)
+        return _assemble(plan, per_rank, strad)
+
+
+def replay_sharded(group: LoopbackGroup, events: np.ndarray, blob=None, fuse: bool = True):
+    """Replay a call stream over the G shards of a LoopbackGroup: setup calls go
+    to every shard, copies are checked in hazard-free batches sharded by host
+    range.  Returns (verdicts of the copies, status per event)."""
+    from .replay import OP_COPY, OP_FREE, OP_MARK, OP_REG, OP_SETV, events_to_descs
+    from . import MARK_DTYPE, plan_batches
+    ops = np.asarray(events["op"])
+    n = len(events)
+    status = np.zeros(n, np.uint32)
+    is_copy = ops == OP_COPY
+    copy_rank = np.cumsum(is_copy) - 1
+    verdicts = np.zeros(int(is_copy.sum()), VERDICT_DTYPE)
+    i = 0
+    while i < n:
+        op = ops[i]
+        if op == OP_MARK:
+            j = i
+            while j < n and ops[j] == OP_MARK:
+                j += 1
+            m = np.zeros(j - i, MARK_DTYPE)
+            m["addr"], m["len"], m["state"] = events["dst"][i:j], events["width"][i:j], events["kind"][i:j]
+            sts = []
+            for sc in group.ranks:
+                s_ = np.zeros(j - i, np.uint32)
+                sc.chk.host_mark_batch(m, status_out=s_)
+                sts.append(s_)
+            status[i:j] = sts[0]
+            i = j
+        elif op == OP_SETV:
+            off, ln = int(events["src"][i]), int(events["width"][i])
+            addr = int(events["dst"][i])
+            # all-or-nothing across shards: every shard must hold only addressable bytes of it
+            if all(sc.chk.host_query_addressable(addr, ln) for sc in group.ranks):
+                rs = [sc.chk.host_set_vbits(addr, bytes(blob[off:off + ln])) for sc in group.ranks]
+                status[i] = max(rs)
+            else:
+                status[i] = 1
+            i += 1
+        else:
+            j = i
+            while j < n and ops[j] in (OP_REG, OP_FREE, OP_COPY):
+                j += 1
+            for k in range(i, j):
+                if ops[k] == OP_REG:
+                    rs = [sc.chk.register_alloc(int(events["dst"][k]), int(events["width"][k]),
+                                                int(events["seq"][k])) for sc in group.ranks]
+                    status[k] = rs[0]
+                elif ops[k] == OP_FREE:
+                    rs = [sc.chk.free(int(events["dst"][k]), int(events["seq"][k])) for sc in group.ranks]
+                    status[k] = rs[0]
+            idx = np.flatnonzero(is_copy[i:j]) + i
+            if len(idx):
+                descs = events_to_descs(events[idx])
+                cuts = [0] + [int(c) for c in plan_batches(descs)]
+                for a, b in zip(cuts[:-1], cuts[1:]):
+                    plan = BatchPlan(descs[a:b], group.host_base, group.host_size, group.world)
+                    v = group.run(plan, fuse=fuse)
+                    verdicts[copy_rank[idx[a:b]]] = v
+                    status[idx[a:b]] = v["status"]
+            i = j
+    import torch
+    torch.cuda.synchronize()
+    return verdicts, status

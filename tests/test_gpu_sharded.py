@@ -1,0 +1,71 @@
+"""Sharded checking on one GPU (loopback): G contexts, each holding one shard
+of the host window, run the per-rank kernels; the straddler all-reduces and
+the verdict gather are done across the G device tensors.  Results must equal
+the unsharded sequential oracle bit for bit (verdicts, statuses, leaks, and
+the concatenated shard shadows), for G = 2, 4, 8 -- shard invariance."""
+import numpy as np
+import pytest
+
+import oracle
+import tracegen as tg
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cg():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_1310_0901_b200 import build
+    build.build()
+    import paper_1310_0901_b200 as m
+    return m
+
+
+def run_sharded(cg, tr, world, fuse=True):
+    from paper_1310_0901_b200.sharded import LoopbackGroup, replay_sharded
+    o, ov, os_, oleaks = oracle.replay_trace(tr)
+    nreg = max(int(np.count_nonzero(tr.events["op"] == tg.OP_REG)), 1024)
+    grp = LoopbackGroup(tr.host_base, tr.host_size, world, max_descs=max(tr.n_copies, 1024), max_allocs=nreg)
+    gv, gs = replay_sharded(grp, tr.events, tr.blob, fuse=fuse)
+    for f in ov.dtype.names:
+        bad = np.flatnonzero(gv[f] != ov[f])
+        assert len(bad) == 0, (world, f, bad[:5], gv[f][bad[:5]], ov[f][bad[:5]])
+    assert np.array_equal(gs, os_), np.flatnonzero(gs != os_)[:10]
+    for sc in grp.ranks:
+        l = sc.chk.leak_report()
+        assert np.array_equal(l["base"], oleaks["base"]) and np.array_equal(l["size"], oleaks["size"])
+    shards = [sc.chk.shadow() for sc in grp.ranks]
+    A = np.concatenate([s[0] for s in shards])
+    V = np.concatenate([s[1] for s in shards])
+    assert np.array_equal(A, o.A) and np.array_equal(V, o.V)
+    grp.close()
+    return gv
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("seed", range(12))
+def test_random_tiny_sharded(cg, world, seed):
+    run_sharded(cg, tg.random_tiny(seed + 11000), world, fuse=bool(seed % 2))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_c2_sharded(cg, world):
+    tr = tg.c2_small(n_copies=30000, n_allocs=3000)
+    run_sharded(cg, tr, world)
+
+
+def test_c3_single_descriptor_straddles_all_shards(cg):
+    tr = tg.c3_single(size=64 << 20, stride=1 << 16)
+    v = run_sharded(cg, tr, 4)
+    assert v[0]["undef_count"] == len(tr.meta["hole_offsets"])
+
+
+@pytest.mark.parametrize("dtoh", [False, True])
+def test_c3_dtoh_straddler_apply(cg, dtoh):
+    run_sharded(cg, tg.c3_single(size=32 << 20, dtoh=dtoh), 4)
+
+
+def test_c4_sharded(cg):
+    tr = tg.c4_pitched(n_copies=1500, n_bufs=4, rows=128, inject_frac=0.05)
+    run_sharded(cg, tr, 2)

@@ -449,7 +449,7 @@ def c3_single(seed: int = 13100903, size: int = 8 * GiB, dtoh: bool = False,
               stride: int = MiB) -> Trace:
     rng = np.random.default_rng(seed)
     H0 = 1 << 36
-    S = size + 8 * KiB
+    S = size + 32 * KiB          # divisible into 4096-multiple shards for G <= 8
     tb = TraceBuilder("c3_single" + ("_dtoh" if dtoh else ""), H0, S)
     hbuf = H0 + 4096
     tb.mark(hbuf, size, DEFINED if not dtoh else UNDEFINED)
