@@ -113,27 +113,44 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+C2_SHARD = 8 << 30        # per-rank window of the weak-scaling C2 workload (7.94 GiB used)
+
+
 def make_workload(name: str, rank: int = 0, scale: float = 1.0):
+    """Rank r's workload.  Weak scaling: rank r's host buffers live in shard r
+    of a global window [2^32, 2^32 + world * 8 GiB); its copies, allocations and
+    verdicts are its own."""
     import tracegen as tg
     if name == "c2_small":
         n = max(1000, int(1_000_000 * scale))
-        return tg.c2_small(seed=13100902 + rank, n_copies=n, n_allocs=max(1000, int(100_000 * min(scale, 1.0))))
+        shard = C2_SHARD if scale >= 1.0 else None
+        return tg.c2_small(seed=13100902 + rank, n_copies=n, n_allocs=max(1000, int(100_000 * min(scale, 1.0))),
+                           host_base=(1 << 32) + rank * C2_SHARD, host_size=shard)
     if name == "c3_single":
         return tg.c3_single(seed=13100903 + rank, size=int((8 << 30) * scale) // (1 << 20) * (1 << 20))
     if name == "c4_pitched":
         return tg.c4_pitched(seed=13100904 + rank, n_copies=max(1000, int(100_000 * scale)))
+    if name == "c5_sharded":
+        return tg.c5_sharded(seed=13100905 + rank, scale=scale)
     raise SystemExit(f"unknown config {name}")
 
 
-def setup_checker(cg, tr, device: int, host_staging: bool):
+def setup_checker(cg, tr, device: int, host_staging: bool, rank: int = 0, world: int = 1):
     """Replays the non-copy events (host marks, V-bytes, registry) and returns
-    the checker and the copy descriptors (host array)."""
+    the checker and the copy descriptors (host array).  With world > 1 the
+    context holds shard `rank` of the global window."""
     from paper_1310_0901_b200.replay import events_to_descs
     ev = tr.events
     copies = ev[ev["op"] == 5]
     nreg = int(np.count_nonzero(ev["op"] == 3))
-    chk = cg.Checker(tr.host_base, tr.host_size, max_descs=max(len(copies), 1024),
-                     max_allocs=max(nreg, 1024), device=device, host_staging=host_staging)
+    if world > 1:
+        gbase = tr.host_base - rank * tr.host_size
+        chk = cg.Checker(gbase, world * tr.host_size, shard_base=tr.host_base, shard_size=tr.host_size,
+                         max_descs=max(len(copies), 1024), max_allocs=max(nreg, 1024), device=device,
+                         host_staging=host_staging)
+    else:
+        chk = cg.Checker(tr.host_base, tr.host_size, max_descs=max(len(copies), 1024),
+                         max_allocs=max(nreg, 1024), device=device, host_staging=host_staging)
     setup = ev[ev["op"] != 5]
     t0 = time.perf_counter()
     cg.replay_events(chk, setup, tr.blob)
@@ -164,7 +181,7 @@ def run_ours(args, rank, world, device):
 
     torch.cuda.set_device(device)
     tr = make_workload(args.config, rank, args.scale)
-    chk, descs, t_setup, nreg = setup_checker(cg, tr, device, host_staging=not args.no_e2e)
+    chk, descs, t_setup, nreg = setup_checker(cg, tr, device, host_staging=not args.no_e2e, rank=rank, world=world)
     n = len(descs)
     stream = torch.cuda.current_stream()
     d_descs = cg.to_device_descs(descs, device)
@@ -177,6 +194,14 @@ def run_ours(args, rank, world, device):
     # and the apply run fused (cg_check_apply), else as two calls
     fused = cg.batch_disjoint(descs) and not args.unfused
 
+    comm = None
+    if world > 1:
+        from paper_1310_0901_b200.sharded import TorchComm
+        comm = TorchComm()
+        g_idx = torch.empty(n, dtype=torch.int64, device=device)
+        g_dirty = torch.empty(n * 64, dtype=torch.uint8, device=device)
+        g_cnt = torch.zeros(1, dtype=torch.int32, device=device)
+
     def step():
         if fused:
             chk.check_apply(d_descs, d_out, stream=stream)
@@ -184,6 +209,11 @@ def run_ours(args, rank, world, device):
             chk.check_copies(d_descs, d_out, stream=stream)
             chk.apply_dtoh(d_descs, d_out, stream=stream)
         chk.leak_sweep(d_leaks, nalloc, d_cnt, stream=stream)
+        if comm is not None:
+            # the exchange: compacted dirty verdicts of every rank to the root (NCCL)
+            cg.cg_compact_dirty(chk.ctx, d_out.data_ptr(), n, g_idx.data_ptr(), g_dirty.data_ptr(),
+                                g_cnt.data_ptr(), stream.cuda_stream)
+            comm.gather_dirty(g_cnt, g_idx, g_dirty)
 
     for _ in range(args.warmup):
         step()

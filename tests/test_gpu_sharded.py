@@ -69,3 +69,11 @@ def test_c3_dtoh_straddler_apply(cg, dtoh):
 def test_c4_sharded(cg):
     tr = tg.c4_pitched(n_copies=1500, n_bufs=4, rows=128, inject_frac=0.05)
     run_sharded(cg, tr, 2)
+
+
+@pytest.mark.parametrize("world", [1, 8])
+def test_c5_scaled_sharded(cg, world):
+    """C5 at 1% scale: 100k copies, interleaved alloc/free bursts, ping-pong
+    epochs, large copies straddling shard boundaries, final leak report."""
+    tr = tg.c5_sharded(scale=0.01)
+    run_sharded(cg, tr, world, fuse=True)

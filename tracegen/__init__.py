@@ -330,7 +330,8 @@ INJ_NONE, INJ_DST_NA, INJ_SRC_NA, INJ_TOO_SMALL, INJ_HOST_UNADDR, INJ_HOST_UNDEF
 
 
 def c2_small(seed: int = 13100902, n_copies: int = 1_000_000, n_allocs: int = 100_000,
-             inject_frac: float = 0.01, redzone: int = 16) -> Trace:
+             inject_frac: float = 0.01, redzone: int = 16, host_base: int = 1 << 32,
+             host_size: Optional[int] = None) -> Trace:
     """SURVEY §8(d) C2.  Every copy gets a private host buffer (malloc-like:
     16-byte aligned, >= ``redzone`` NOACCESS bytes on both sides), so the trace
     is a single hazard-free batch and the dirty set is exactly the injected
@@ -338,7 +339,7 @@ def c2_small(seed: int = 13100902, n_copies: int = 1_000_000, n_allocs: int = 10
     but not written (UNDEFINED), like ``c_host`` in Listing 2."""
     assert redzone >= 16 and redzone % 16 == 0
     rng = np.random.default_rng(seed)
-    H0 = 1 << 32
+    H0 = host_base
     # ---- device allocations (bump allocator, S:370)
     sizes = _log_uniform(rng, 64, 64 * KiB, n_allocs)
     aligned = (sizes + DEVICE_ALIGN - 1) // DEVICE_ALIGN * DEVICE_ALIGN
@@ -412,6 +413,9 @@ def c2_small(seed: int = 13100902, n_copies: int = 1_000_000, n_allocs: int = 10
     host_start = (H0 + 4096 + redzone + np.concatenate([[0], np.cumsum(slot)[:-1]])).astype(np.uint64)
     end = int(host_start[-1]) - redzone + int(slot[-1]) + 4096
     S = (end - H0 + MiB - 1) // MiB * MiB
+    if host_size is not None:           # a fixed window (e.g. one shard of a sharded bench)
+        assert host_size >= S, (host_size, S)
+        S = host_size
 
     tb = TraceBuilder("c2_small", H0, S)
     hidx = np.flatnonzero(has_host)
@@ -548,3 +552,196 @@ CONFIGS = {
     "c3_single": c3_single,
     "c4_pitched": c4_pitched,
 }
+
+
+# ---------------------------------------------------------------------------
+# Config 5: 64 GB host shadow, 10M mixed descriptors, interleaved alloc/free,
+# final leak report (configs[4]); scale < 1 shrinks every count and the window
+# ---------------------------------------------------------------------------
+def c5_sharded(seed: int = 13100905, scale: float = 1.0, shards: int = 8, inject_frac: float = 0.01,
+               redzone: int = 16) -> Trace:
+    """SURVEY §8(d) C5.  Window 64 GiB (x scale) cut into 64 KiB slots, one host
+    buffer per slot (even slots: written HtoD sources; odd slots: allocated DtoH
+    targets), except 128 MiB (x scale) bands centred on the `shards`-1 shard
+    boundaries, which hold 100 large (1-64 MiB) straddling HtoD/DtoH buffers
+    (HtoD and DtoH on disjoint halves).  Registry: 100k initial allocations;
+    after every 10k descriptors 50 random live ones are freed and 50 new ones
+    allocated (bump, no reuse); at the end all but a seeded 1 % are freed.
+    10M copies HtoD 45 % / DtoH 45 % / DtoD 10 %, 1 % injected (incl. use after
+    free), plus 10 deliberate DtoH -> HtoD ping-pongs on odd slots (the only
+    batch hazards: ~11 epochs)."""
+    rng = np.random.default_rng(seed)
+    H0 = 1 << 44
+    S = int(round((64 << 30) * scale)) // (shards * 65536) * (shards * 65536)
+    slot = 65536
+    n_slots = S // slot
+    band = max(2 * slot, int((128 << 20) * scale) // slot * slot)
+    bounds = [H0 + k * (S // shards) for k in range(1, shards)]
+    slot_start = H0 + np.arange(n_slots, dtype=np.uint64) * slot
+    in_band = np.zeros(n_slots, bool)
+    for b in bounds:
+        lo, hi = (b - band // 2 - H0) // slot, (b + band // 2 - H0) // slot
+        in_band[lo:hi] = True
+    free_slots = np.flatnonzero(~in_band)
+    buf_len = np.minimum(_log_uniform(rng, 64, slot, n_slots), slot - 2 * redzone - 64).astype(np.uint64)
+    buf_start = slot_start + redzone
+    is_src = (np.arange(n_slots) % 2 == 0)
+
+    tb = TraceBuilder("c5_sharded", H0, S)
+    marks = np.zeros(len(free_slots), EVENT_DTYPE)
+    marks["op"] = OP_MARK
+    marks["dst"] = buf_start[free_slots]
+    marks["width"] = buf_len[free_slots]
+    marks["kind"] = np.where(is_src[free_slots], DEFINED, UNDEFINED)
+    tb.block(marks)
+    # straddling band buffers: each band = [HtoD half | DtoH half] around the boundary
+    big = []      # (host start, length, kind) of a region straddling boundary b
+    for k, b in enumerate(bounds):
+        half = band // 2
+        if k % 2 == 0:      # HtoD sources across even boundaries
+            tb.mark(b - half + 4096, band - 8192, DEFINED)
+            big.append((b - half + 4096, band - 8192, HTOD))
+        else:               # DtoH targets across odd boundaries
+            tb.mark(b - half + 4096, band - 8192, UNDEFINED)
+            big.append((b - half + 4096, band - 8192, DTOH))
+    # one 64 MiB device buffer per band for the large copies
+    big_dev = [tb.malloc(64 << 20) for _ in bounds]
+
+    n_copies = max(1000, int(10_000_000 * scale))
+    n_init = max(1000, int(100_000 * scale))
+    burst_every, burst = 10_000, 50
+    sizes0 = _log_uniform(rng, 64, 64 * KiB, n_init)
+    live_base: List[int] = []
+    live_size: List[int] = []
+    freed: List[tuple] = []
+    rows = []
+    for sz in sizes0:
+        base = tb.heap_cursor
+        tb.heap_cursor = (base + int(sz) + DEVICE_ALIGN - 1) // DEVICE_ALIGN * DEVICE_ALIGN
+        live_base.append(base)
+        live_size.append(int(sz))
+    regs = np.zeros(n_init, EVENT_DTYPE)
+    regs["op"] = OP_REG
+    regs["dst"] = np.array(live_base, np.uint64)
+    regs["width"] = sizes0
+    tb.block(regs)
+    # HostUndefined injections are prepared on even slots up front (S:79)
+    inj_classes = 7
+    n_inj = int(round(n_copies * inject_frac))
+    kinds_all = rng.choice(np.array([HTOD, DTOH, DTOD], np.uint32), n_copies, p=[0.45, 0.45, 0.10])
+    inj = np.zeros(n_copies, np.uint8)
+    inj_idx = rng.choice(n_copies, n_inj, replace=False)
+    inj[inj_idx] = np.arange(n_inj) % 6 + 1
+    kinds_all[(inj == INJ_HOST_UNDEF) | (inj == INJ_DST_NA)] = HTOD
+    kinds_all[inj == INJ_SRC_NA] = DTOH
+    kinds_all[inj == INJ_DTOD_BAD_SRC] = DTOD
+    kinds_all[(inj == INJ_HOST_UNADDR) & (kinds_all == DTOD)] = HTOD
+    src_slots = free_slots[is_src[free_slots]]
+    dst_slots = free_slots[~is_src[free_slots]]
+    slot_pick = np.where(kinds_all == HTOD, rng.choice(src_slots, n_copies), rng.choice(dst_slots, n_copies))
+    undef_slots = np.unique(slot_pick[inj == INJ_HOST_UNDEF])
+    for sl in undef_slots:
+        k = int(rng.integers(1, 17))
+        for p in np.sort(rng.choice(int(buf_len[sl]), min(k, int(buf_len[sl])), replace=False)):
+            tb.setv(int(buf_start[sl]) + int(p), bytes([int(rng.integers(1, 256))]))
+    lens = np.minimum(_log_uniform(rng, 64, 64 * KiB, n_copies), buf_len[slot_pick]).astype(np.uint64)
+    pingpong = set(int(x) for x in rng.choice(np.flatnonzero(inj == 0), 10, replace=False))
+    big_at = set(int(x) for x in rng.choice(n_copies, 100, replace=False))
+    heap_end_probe = 1 << 50
+
+    chunk_rows = []
+    for c0 in range(0, n_copies, burst_every):
+        c1 = min(n_copies, c0 + burst_every)
+        if c0:
+            # registry burst: free 50 random live, allocate 50 new (bump, no reuse)
+            fr = rng.choice(len(live_base), burst, replace=False)
+            for j in sorted(fr, reverse=True):
+                tb.free(live_base[j])
+                freed.append((live_base[j], live_size[j]))
+                live_base.pop(j)
+                live_size.pop(j)
+            for sz in _log_uniform(rng, 64, 64 * KiB, burst):
+                live_base.append(tb.malloc(int(sz)))
+                live_size.append(int(sz))
+        lb = np.array(live_base, np.uint64)
+        ls = np.array(live_size, np.uint64)
+        m = c1 - c0
+        kinds = kinds_all[c0:c1]
+        ln = lens[c0:c1].copy()
+        a1 = rng.integers(0, len(lb), m)
+        a2 = rng.integers(0, len(lb), m)
+        ln = np.where(kinds == DTOD, np.minimum(ln, np.minimum(ls[a1], ls[a2])), np.minimum(ln, ls[a1]))
+        ln = np.maximum(ln, 1)
+        off1 = np.floor(rng.random(m) * (ls[a1] - ln + 1)).astype(np.uint64)
+        off2 = np.floor(rng.random(m) * (ls[a2] - np.minimum(ln, ls[a2]) + 1)).astype(np.uint64)
+        dev1, dev2 = lb[a1] + off1, lb[a2] + off2
+        host = buf_start[slot_pick[c0:c1]]
+        cls = inj[c0:c1]
+        cp = np.zeros(m, EVENT_DTYPE)
+        cp["op"] = OP_COPY
+        cp["kind"] = kinds
+        cp["height"] = 1
+        dst = np.where(kinds == DTOH, host, dev1)
+        src = np.where(kinds == HTOD, host, np.where(kinds == DTOH, dev1, dev2))
+        width = ln.copy()
+        # injections
+        bad = lambda k: (np.array([f[0] for f in freed], np.uint64)[rng.integers(0, len(freed), k)]
+                         if freed and rng.random() < 0.5 else heap_end_probe + rng.integers(0, 1 << 20, k).astype(np.uint64))
+        mk = cls == INJ_DST_NA
+        if mk.any():
+            dst[mk] = bad(int(mk.sum()))
+        mk = (cls == INJ_SRC_NA) | (cls == INJ_DTOD_BAD_SRC)
+        if mk.any():
+            src[mk] = bad(int(mk.sum()))
+        mk = np.flatnonzero(cls == INJ_TOO_SMALL)
+        for i in mk:
+            over = int(rng.integers(1, 65))
+            end = int(lb[a1[i]] + ls[a1[i]])
+            room = max(int(ln[i]) - over, 1)
+            if kinds[i] == DTOH:
+                src[i] = end - room
+            else:
+                dst[i] = end - room
+        mk = cls == INJ_HOST_UNADDR
+        width[mk] = buf_len[slot_pick[c0:c1][mk]] + rng.integers(1, redzone + 1, int(mk.sum())).astype(np.uint64)
+        cp["dst"], cp["src"], cp["width"] = dst, src, width
+        cp["dst_pitch"] = width
+        cp["src_pitch"] = width
+        # large straddlers inside the boundary bands
+        for i in range(c0, c1):
+            if i in big_at and big and cls[i - c0] == 0:
+                j = int(rng.integers(len(big)))
+                hs, hl, kd = big[j]
+                L = int(min(_log_uniform(rng, 1 << 20, 64 << 20, 1)[0], hl))
+                start = hs + (hl - L) // 2          # centred on the shard boundary
+                k = i - c0
+                cp[k]["kind"] = kd
+                if kd == DTOH:
+                    cp[k]["dst"], cp[k]["src"] = start, big_dev[j]
+                else:
+                    cp[k]["src"], cp[k]["dst"] = start, big_dev[j]
+                cp[k]["width"] = L
+                cp[k]["dst_pitch"] = L
+                cp[k]["src_pitch"] = L
+        tb.block(cp)
+        # deliberate ping-pongs: a DtoH into an odd slot, then an HtoD reading it back
+        for i in range(c0, c1):
+            if i in pingpong:
+                sl = int(rng.choice(dst_slots))
+                ln2 = int(buf_len[sl])
+                d = tb.malloc(ln2)
+                live_base.append(d)
+                live_size.append(ln2)
+                tb.copy1d(DTOH, int(buf_start[sl]), d, ln2)
+                tb.copy1d(HTOD, d, int(buf_start[sl]), ln2)
+    # final frees: all but 1 % leak
+    keep = set(int(x) for x in rng.choice(len(live_base), max(1, len(live_base) // 100), replace=False))
+    fr = np.zeros(len(live_base) - len(keep), EVENT_DTYPE)
+    fr["op"] = OP_FREE
+    fr["dst"] = [b for j, b in enumerate(live_base) if j not in keep]
+    tb.block(fr)
+    tb.meta.update(dict(inject=inj, shards=shards, bounds=bounds, n_leaks=len(keep), scale=scale))
+    return tb.build()
+
+
+CONFIGS["c5_sharded"] = c5_sharded
