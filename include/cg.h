@@ -105,6 +105,17 @@ typedef struct {
   uint64_t src, src_x, src_y, src_pitch;
 } cg_copy_desc;
 
+/* Compact form of a 1D copy (cuMemcpyHtoD / DtoH / DtoD): 40 bytes; equal to
+ * the cg_copy_desc {kind, seq, width = bytes, height = 1, dst, src,
+ * pitches = bytes, x = y = 0}. */
+typedef struct {
+  uint32_t kind, reserved;
+  uint64_t seq, dst, src, bytes;
+} cg_copy1d;
+
+/* descriptor formats accepted by cg_check_host */
+enum { CG_FMT_2D = 0, CG_FMT_1D = 1 };
+
 /* Result for one descriptor.  64 bytes.  Clean = {NONE, NONE, 0, 0,0,0,0, 0, 0}.
  *  - first_unaddr: lowest logical offset o = r*width + c of a host byte that is
  *    not addressable (SPEC check_addressable S:63-71), else CG_NONE;
@@ -272,6 +283,25 @@ cg_status cg_batch_disjoint(const cg_copy_desc *h_descs, uint64_t n, int *disjoi
  * cg_check_copies; CG_ERR_NOT_INITIALIZED without host staging. */
 cg_status cg_check_copies_host(cg_ctx *ctx, const cg_copy_desc *h_descs, uint64_t n, cg_verdict *h_out,
                                int apply, void *stream);
+
+/* Expands n compact 1D descriptors (device array d_in) into cg_copy_desc
+ * records (device array d_out); asynchronous.  Errors: CG_ERR_INVALID_VALUE on
+ * NULL. */
+cg_status cg_expand_copy1d(cg_ctx *ctx, const cg_copy1d *d_in, uint64_t n, cg_copy_desc *d_out, void *stream);
+
+/* End-to-end entry point with HOST buffers and a compact result: uploads the
+ * n host descriptors (format CG_FMT_2D: cg_copy_desc, CG_FMT_1D: cg_copy1d),
+ * checks them -- apply = 0: cg_check_copies, 1: + cg_apply_dtoh, 2:
+ * cg_check_apply (needs an apply-disjoint batch) -- and downloads only the
+ * dirty verdicts: h_idx[k] (descriptor index) and h_dirty[k] for
+ * k < min(*n_dirty, cap), in unspecified order; every other descriptor's
+ * verdict is the clean one.  The batch is processed in up to 4 chunks whose
+ * host->device copies run on a second stream under the previous chunk's
+ * kernels (pinned host memory makes them asynchronous).  Synchronous.
+ * Requires cfg.host_staging.  Errors: as cg_check_copies; CG_ERR_NOT_INITIALIZED
+ * without host staging. */
+cg_status cg_check_host(cg_ctx *ctx, const void *h_descs, uint32_t format, uint64_t n, int apply, uint64_t *h_idx,
+                        cg_verdict *h_dirty, uint64_t cap, uint64_t *n_dirty, void *stream);
 
 /* Straddler exchange, step 1 (device, asynchronous): the m raw partial
  * verdicts d_raw (CG_SHARD_RAW descriptors, in the same order on every shard)

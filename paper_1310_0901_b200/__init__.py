@@ -96,6 +96,8 @@ def _load() -> ctypes.CDLL:
         "cg_straddler_finalize": (I, [P, P, P, P, U64, P, P]),
         "cg_compact_dirty": (I, [P, P, U64, P, P, P, P]),
         "cg_host_query_addressable": (I, [P, U64, U64, P, P]),
+        "cg_expand_copy1d": (I, [P, P, U64, P, P]),
+        "cg_check_host": (I, [P, P, U32, U64, I, P, P, U64, P, P]),
         "cg_shard_plan": (I, [P, U64, U64, U64, U32, P, P, P]),
         "cg_batch_disjoint": (I, [P, U64, P]),
         "cg_leak_sweep": (I, [P, P, U64, P, P]),
@@ -118,7 +120,7 @@ EXPORTED = ("cg_workspace_size", "cg_ctx_create", "cg_ctx_destroy", "cg_last_err
             "cg_check_copies", "cg_apply_dtoh", "cg_check_copies_host", "cg_leak_sweep", "cg_leak_report",
             "cg_plan_batches", "cg_kernel_launches", "cg_profile_begin", "cg_profile_end", "cg_check_apply",
             "cg_batch_disjoint", "cg_straddler_pack", "cg_straddler_finalize", "cg_compact_dirty", "cg_shard_plan",
-            "cg_host_query_addressable")
+            "cg_host_query_addressable", "cg_expand_copy1d", "cg_check_host")
 
 # ---- same-name thin wrappers (status codes returned unchanged) -------------
 cg_workspace_size = _lib.cg_workspace_size
@@ -139,6 +141,11 @@ cg_straddler_pack = _lib.cg_straddler_pack
 cg_straddler_finalize = _lib.cg_straddler_finalize
 cg_compact_dirty = _lib.cg_compact_dirty
 cg_host_query_addressable = _lib.cg_host_query_addressable
+cg_expand_copy1d = _lib.cg_expand_copy1d
+cg_check_host = _lib.cg_check_host
+CG_FMT_2D, CG_FMT_1D = 0, 1
+COPY1D_DTYPE = np.dtype([("kind", "<u4"), ("reserved", "<u4"), ("seq", "<u8"), ("dst", "<u8"), ("src", "<u8"),
+                         ("bytes", "<u8")])
 cg_shard_plan = _lib.cg_shard_plan
 CG_SHARD_NOT_OWNER, CG_SHARD_RAW = 1, 2
 cg_batch_disjoint = _lib.cg_batch_disjoint
@@ -311,6 +318,20 @@ class Checker:
         self._ok(_lib.cg_check_copies_host(self.ctx, d.ctypes.data, len(d), out.ctypes.data, int(apply),
                                            _stream_ptr(stream)), "cg_check_copies_host")
         return out
+
+    def check_host(self, descs: np.ndarray, apply: int = 1, cap: Optional[int] = None, stream=None):
+        """cg_check_host: host descriptors (DESC_DTYPE or COPY1D_DTYPE) in,
+        dirty verdicts out.  Returns (n_dirty, idx, dirty verdicts)."""
+        fmt = CG_FMT_1D if descs.dtype == COPY1D_DTYPE else CG_FMT_2D
+        n = len(descs)
+        cap = n if cap is None else cap
+        idx = np.empty(max(cap, 1), np.uint64)
+        dirty = np.empty(max(cap, 1), VERDICT_DTYPE)
+        nd = ctypes.c_uint64(0)
+        self._ok(_lib.cg_check_host(self.ctx, descs.ctypes.data, fmt, n, int(apply), idx.ctypes.data,
+                                    dirty.ctypes.data, cap, ctypes.byref(nd), _stream_ptr(stream)), "cg_check_host")
+        m = min(nd.value, cap)
+        return nd.value, idx[:m], dirty[:m]
 
     def leak_sweep(self, d_out, cap: int, d_count, stream=None):
         self._ok(_lib.cg_leak_sweep(self.ctx, d_out.data_ptr(), cap, d_count.data_ptr(), _stream_ptr(stream)),

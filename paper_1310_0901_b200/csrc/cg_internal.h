@@ -29,6 +29,7 @@ struct Table {
   const uint64_t* aseq;
   const uint64_t* fseq;
   const uint64_t* pmax;
+  const uint64_t* split;   // base[k * stride], k < nsplit (16-byte aligned, padded to even)
   uint64_t n;
   uint32_t stride;   // splitter stride (every stride-th base is staged in smem)
   uint32_t nsplit;
@@ -83,7 +84,8 @@ cudaError_t straddler_pack(const Launch& L, const cg_verdict* v, uint64_t m, uin
 cudaError_t straddler_finalize(const Launch& L, const uint64_t* mins, const uint64_t* sums, const uint32_t* maxs,
                                uint64_t m, cg_verdict* v, uint32_t err_mask, cudaStream_t s);
 cudaError_t compact_dirty(const Launch& L, const cg_verdict* v, uint64_t n, uint64_t* idx, cg_verdict* dirty,
-                          uint32_t* count, cudaStream_t s);
+                          uint32_t* count, uint64_t idx_base, bool reset, cudaStream_t s);
+cudaError_t expand_1d(const Launch& L, const cg_copy1d* in, uint64_t n, cg_copy_desc* out, cudaStream_t s);
 cudaError_t mark_batch(const Launch& L, const cg_mark* d_marks, uint64_t n, const ShadowView& sv,
                        const Plan& p, cudaStream_t s);
 cudaError_t fresh_shadow(const Launch& L, const ShadowView& sv, cudaStream_t s);

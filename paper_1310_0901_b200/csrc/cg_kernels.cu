@@ -201,13 +201,13 @@ __device__ __forceinline__ bool table_lookup(const Table& t, const uint64_t* s_s
   uint64_t a = (uint64_t)lo * t.stride;
   uint64_t b = umin64(a + t.stride, t.n);
   while (b - a > 1) {
-    uint64_t mid = (a + b) >> 1;
+    const uint64_t mid = (a + b) >> 1;
     if (__ldg(t.base + mid) <= start) a = mid; else b = mid;
   }
   for (int64_t j = (int64_t)a; j >= 0; --j) {
-    if (__ldg(t.pmax + j) <= start) break;
-    const uint64_t e = __ldg(t.end + j);
-    if (e > start && __ldg(t.aseq + j) < seq && seq < __ldg(t.fseq + j)) {
+    const uint64_t pm = __ldg(t.pmax + j), e = __ldg(t.end + j), as = __ldg(t.aseq + j), fs = __ldg(t.fseq + j);
+    if (pm <= start) break;
+    if (e > start && as < seq && seq < fs) {
       end_out = e;
       return true;
     }
@@ -215,9 +215,12 @@ __device__ __forceinline__ bool table_lookup(const Table& t, const uint64_t* s_s
   return false;
 }
 
+// the splitters (every stride-th base) are a contiguous array uploaded with the
+// table: coalesced 16-byte loads into shared memory
 __device__ __forceinline__ void load_splitters(const Table& t, uint64_t* s_split) {
-  for (uint32_t k = threadIdx.x; k < t.nsplit; k += blockDim.x)
-    s_split[k] = t.base[(uint64_t)k * t.stride];
+  const uint4* src = reinterpret_cast<const uint4*>(t.split);
+  uint4* dst = reinterpret_cast<uint4*>(s_split);
+  for (uint32_t k = threadIdx.x; k < (t.nsplit + 1) / 2; k += blockDim.x) dst[k] = __ldg(src + k);
   __syncthreads();
 }
 
@@ -1333,10 +1336,30 @@ __global__ void k_straddler_finalize(const uint64_t* __restrict__ mins, const ui
   }
 }
 
+__global__ void k_expand_1d(const cg_copy1d* __restrict__ in, uint64_t n, cg_copy_desc* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const cg_copy1d a = in[i];
+    cg_copy_desc d;
+    d.kind = a.kind;
+    d.reserved = a.reserved;
+    d.seq = a.seq;
+    d.width = a.bytes;
+    d.height = 1;
+    d.dst = a.dst;
+    d.dst_x = d.dst_y = 0;
+    d.dst_pitch = a.bytes;
+    d.src = a.src;
+    d.src_x = d.src_y = 0;
+    d.src_pitch = a.bytes;
+    out[i] = d;
+  }
+}
+
 // verdicts with any flag (order not kept) -> (index, verdict) lists for the
 // gather to the root; clean verdicts are canonical and are not sent
 __global__ void k_compact_dirty(const cg_verdict* __restrict__ v, uint64_t n, uint64_t* __restrict__ idx,
-                                cg_verdict* __restrict__ dirty, uint32_t* __restrict__ count) {
+                                cg_verdict* __restrict__ dirty, uint32_t* __restrict__ count, uint64_t idx_base) {
   const int lane = threadIdx.x & 31;
   for (uint64_t b0 = (uint64_t)blockIdx.x * blockDim.x; b0 < n; b0 += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t i = b0 + threadIdx.x;
@@ -1349,7 +1372,7 @@ __global__ void k_compact_dirty(const cg_verdict* __restrict__ v, uint64_t n, ui
       base = __shfl_sync(kFull, base, leader);
       if (d) {
         const uint32_t k = base + __popc(mask & ((1u << lane) - 1u));
-        idx[k] = i;
+        idx[k] = idx_base + i;
         dirty[k] = v[i];
       }
     }
@@ -1410,10 +1433,10 @@ static cudaError_t plan(const Launch& L, uint64_t n, const Plan& p, cudaStream_t
 cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out, const Table& t,
                          const ShadowView& sv, const Plan& p, uint32_t err_mask, bool fuse, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  const size_t smem = (size_t)t.nsplit * sizeof(uint64_t);
+  const size_t smem = ((size_t)t.nsplit + 1) * sizeof(uint64_t);
   ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
   L.stage(CG_STAGE_CHECK_PREP, true, s);
-  k_check_prep<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, smem, s>>>(d, n, t, out, p.weight, meta);
+  k_check_prep<<<blocks_for(n, kThreads, L.num_sms * 4), kThreads, smem, s>>>(d, n, t, out, p.weight, meta);
   *L.counter += 1;
   L.stage(CG_STAGE_CHECK_PREP, false, s);
   L.stage(CG_STAGE_CHECK_PLAN, true, s);
@@ -1518,10 +1541,17 @@ cudaError_t straddler_finalize(const Launch& L, const uint64_t* mins, const uint
 }
 
 cudaError_t compact_dirty(const Launch& L, const cg_verdict* v, uint64_t n, uint64_t* idx, cg_verdict* dirty,
-                          uint32_t* count, cudaStream_t s) {
-  cudaMemsetAsync(count, 0, sizeof(uint32_t), s);
+                          uint32_t* count, uint64_t idx_base, bool reset, cudaStream_t s) {
+  if (reset) cudaMemsetAsync(count, 0, sizeof(uint32_t), s);
   if (n == 0) return cudaGetLastError();
-  k_compact_dirty<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(v, n, idx, dirty, count);
+  k_compact_dirty<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(v, n, idx, dirty, count, idx_base);
+  *L.counter += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t expand_1d(const Launch& L, const cg_copy1d* in, uint64_t n, cg_copy_desc* out, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  k_expand_1d<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(in, n, out);
   *L.counter += 1;
   return cudaGetLastError();
 }

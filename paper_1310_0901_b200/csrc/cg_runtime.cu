@@ -33,7 +33,8 @@ struct Entry {
 };
 
 struct Layout {
-  uint64_t table, weight, P, bsum, chunk, meta, marks, flags, leaks, desc_stage, verdict_stage, total;
+  uint64_t table, weight, P, bsum, chunk, meta, marks, flags, leaks, desc_stage, verdict_stage, raw_stage,
+      idx_stage, dirty_stage, total;
   uint64_t max_items, max_chunks;
 };
 
@@ -60,7 +61,7 @@ Layout layout_of(const cg_config* c) {
     off = align_up(off + bytes, kAlign);
     return o;
   };
-  L.table = take(5 * c->max_allocs * 8);
+  L.table = take(5 * c->max_allocs * 8 + (4096 + 3) * 8);   // SoA + splitters
   L.weight = take(L.max_items * 8);
   L.P = take((L.max_items + 1) * 8);
   L.bsum = take((cgk::scan_blocks(L.max_items) + 1) * 8);
@@ -71,6 +72,9 @@ Layout layout_of(const cg_config* c) {
   L.leaks = take(c->max_allocs * sizeof(cg_alloc_record));
   L.desc_stage = c->host_staging ? take(c->max_descs * sizeof(cg_copy_desc)) : 0;
   L.verdict_stage = c->host_staging ? take(c->max_descs * sizeof(cg_verdict)) : 0;
+  L.raw_stage = c->host_staging ? take(c->max_descs * sizeof(cg_copy1d)) : 0;
+  L.idx_stage = c->host_staging ? take(c->max_descs * sizeof(uint64_t)) : 0;
+  L.dirty_stage = c->host_staging ? take(c->max_descs * sizeof(cg_verdict)) : 0;
   L.total = off;
   return L;
 }
@@ -106,6 +110,8 @@ struct cg_ctx {
   uint64_t* h_table = nullptr;              // 5 * max_allocs
   cg_mark* h_marks = nullptr;               // kMarkRun
   cudaEvent_t staged = nullptr;
+  cudaStream_t copy_stream = nullptr;        // host -> device uploads of cg_check_host
+  cudaEvent_t chunk_ev[4] = {};
   std::string err;
   // profiling (cg_profile_begin / end)
   cgk::Profiler prof;
@@ -166,8 +172,9 @@ struct cg_ctx {
     t.aseq = b + 2 * cap;
     t.fseq = b + 3 * cap;
     t.pmax = b + 4 * cap;
+    t.split = b + ((5 * cap + 1) & ~1ull);   // 16-byte aligned
     t.n = table.size();
-    uint64_t stride = std::max<uint64_t>(32, (t.n + 4095) / 4096);
+    const uint64_t stride = split_stride(t.n);
     t.stride = (uint32_t)stride;
     t.nsplit = (uint32_t)((t.n + stride - 1) / stride);
     return t;
@@ -190,15 +197,26 @@ struct cg_ctx {
         pm = std::max(pm, x.end);
         h_table[4 * cap + i] = pm;
       }
+      const uint64_t stride = split_stride(n), nsplit = (n + stride - 1) / stride;
+      const uint64_t so = (5 * cap + 1) & ~1ull;
+      for (uint64_t k = 0; k < nsplit; ++k) h_table[so + k] = table[k * stride].base;
+      h_table[so + nsplit] = UINT64_MAX;   // padding for the 16-byte loads
       uint64_t* dt = d(lay.table);
       for (int k = 0; k < 5; ++k) {
         e = cudaMemcpyAsync(dt + k * cap, h_table + k * cap, n * 8, cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) return cuda(e, "table upload");
       }
+      e = cudaMemcpyAsync(dt + so, h_table + so, (nsplit + 1) * 8, cudaMemcpyHostToDevice, s);
+      if (e != cudaSuccess) return cuda(e, "splitter upload");
       cudaEventRecord(staged, s);
     }
     dirty = false;
     return CG_OK;
+  }
+
+  static uint64_t split_stride(uint64_t n) {
+    const uint64_t stride = std::max<uint64_t>(32, (n + 4095) / 4096);
+    return (stride + 31) / 32 * 32;   // whole 256-byte blocks of bases per bucket
   }
 
   uint32_t err_mask() const {
@@ -246,13 +264,20 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
   c->prof.mark = &cg_ctx::mark_cb;
   c->prof.self = c;
   c->launch.prof = &c->prof;
-  if (cudaMallocHost(&c->h_table, 5 * cfg->max_allocs * 8) != cudaSuccess ||
+  if (cudaMallocHost(&c->h_table, 5 * cfg->max_allocs * 8 + (4096 + 3) * 8) != cudaSuccess ||
       cudaMallocHost(&c->h_marks, std::min<uint64_t>(cfg->max_descs, kMarkRun) * sizeof(cg_mark)) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->staged, cudaEventDisableTiming) != cudaSuccess) {
     cg_ctx_destroy(c);
     return CG_ERR_OUT_OF_MEMORY;
   }
   cudaEventRecord(c->staged, 0);
+  if (cfg->host_staging) {
+    if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+      cg_ctx_destroy(c);
+      return CG_ERR_CUDA;
+    }
+    for (auto& ev : c->chunk_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  }
   e = cgk::fresh_shadow(c->launch, c->sv, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
@@ -270,6 +295,9 @@ cg_status cg_ctx_destroy(cg_ctx* c) {
     cudaEventSynchronize(c->staged);
     cudaEventDestroy(c->staged);
   }
+  for (auto& ev : c->chunk_ev)
+    if (ev) cudaEventDestroy(ev);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   for (auto& r : c->recs) { c->pool.push_back(r.a); c->pool.push_back(r.b); }
   for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
   if (c->h_table) cudaFreeHost(c->h_table);
@@ -534,6 +562,75 @@ cg_status cg_check_copies_host(cg_ctx* c, const cg_copy_desc* h_descs, uint64_t 
   return c->cuda(e, "verdict download");
 }
 
+cg_status cg_expand_copy1d(cg_ctx* c, const cg_copy1d* d_in, uint64_t n, cg_copy_desc* d_out, void* stream) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (n && (!d_in || !d_out)) return c->fail(CG_ERR_INVALID_VALUE, "null arrays");
+  DeviceGuard g(c->cfg.device);
+  return c->cuda(cgk::expand_1d(c->launch, d_in, n, d_out, static_cast<cudaStream_t>(stream)), "expand 1d");
+}
+
+cg_status cg_check_host(cg_ctx* c, const void* h_descs, uint32_t format, uint64_t n, int apply, uint64_t* h_idx,
+                        cg_verdict* h_dirty, uint64_t cap, uint64_t* n_dirty, void* stream) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (!c->cfg.host_staging) return c->fail(CG_ERR_NOT_INITIALIZED, "context created without host staging");
+  if (!n_dirty || (cap && (!h_idx || !h_dirty))) return c->fail(CG_ERR_INVALID_VALUE, "null outputs");
+  *n_dirty = 0;
+  if (n == 0) return CG_OK;
+  if (!h_descs || format > CG_FMT_1D || apply < 0 || apply > 2) return c->fail(CG_ERR_INVALID_VALUE, "bad arguments");
+  if (n > c->cfg.max_descs) return c->fail(CG_ERR_INVALID_VALUE, "n > max_descs");
+  DeviceGuard g(c->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cg_copy_desc* dd = reinterpret_cast<cg_copy_desc*>(c->ws + c->lay.desc_stage);
+  cg_verdict* dv = reinterpret_cast<cg_verdict*>(c->ws + c->lay.verdict_stage);
+  cg_copy1d* draw = reinterpret_cast<cg_copy1d*>(c->ws + c->lay.raw_stage);
+  uint64_t* didx = reinterpret_cast<uint64_t*>(c->ws + c->lay.idx_stage);
+  cg_verdict* ddirty = reinterpret_cast<cg_verdict*>(c->ws + c->lay.dirty_stage);
+  uint32_t* dcount = reinterpret_cast<uint32_t*>(c->ws + c->lay.flags + 192);
+  const size_t esz = format == CG_FMT_1D ? sizeof(cg_copy1d) : sizeof(cg_copy_desc);
+  uint8_t* dst = format == CG_FMT_1D ? reinterpret_cast<uint8_t*>(draw) : reinterpret_cast<uint8_t*>(dd);
+  const uint64_t nchunks = n >= (1u << 19) ? 4 : 1;
+  const uint64_t per = (n + nchunks - 1) / nchunks;
+  // uploads: all chunks on the copy stream (it waits for earlier work on s first)
+  cudaError_t e = cudaEventRecord(c->chunk_ev[0], s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(c->copy_stream, c->chunk_ev[0], 0);
+  for (uint64_t k = 0; k < nchunks && e == cudaSuccess; ++k) {
+    const uint64_t a = k * per, b = std::min(n, a + per);
+    if (a >= b) break;
+    e = cudaMemcpyAsync(dst + a * esz, static_cast<const uint8_t*>(h_descs) + a * esz, (b - a) * esz,
+                        cudaMemcpyHostToDevice, c->copy_stream);
+    if (e == cudaSuccess) e = cudaEventRecord(c->chunk_ev[k], c->copy_stream);
+  }
+  if (e != cudaSuccess) return c->cuda(e, "descriptor upload");
+  e = cudaMemsetAsync(dcount, 0, sizeof(uint32_t), s);
+  if (e != cudaSuccess) return c->cuda(e, "memset");
+  for (uint64_t k = 0; k < nchunks; ++k) {
+    const uint64_t a = k * per, b = std::min(n, a + per);
+    if (a >= b) break;
+    e = cudaStreamWaitEvent(s, c->chunk_ev[k], 0);
+    if (e == cudaSuccess && format == CG_FMT_1D) e = cgk::expand_1d(c->launch, draw + a, b - a, dd + a, s);
+    if (e != cudaSuccess) return c->cuda(e, "chunk wait / expand");
+    cg_status st = apply == 2 ? cg_check_apply(c, dd + a, b - a, dv + a, stream)
+                              : cg_check_copies(c, dd + a, b - a, dv + a, stream);
+    if (st == CG_OK && apply == 1) st = cg_apply_dtoh(c, dd + a, dv + a, b - a, stream);
+    if (st != CG_OK) return st;
+    e = cgk::compact_dirty(c->launch, dv + a, b - a, didx, ddirty, dcount, a, false, s);
+    if (e != cudaSuccess) return c->cuda(e, "compact");
+  }
+  uint32_t cnt = 0;
+  e = cudaMemcpyAsync(&cnt, dcount, sizeof cnt, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return c->cuda(e, "count download");
+  *n_dirty = cnt;
+  const uint64_t m = std::min<uint64_t>(cnt, cap);
+  if (m) {
+    e = cudaMemcpyAsync(h_idx, didx, m * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_dirty, ddirty, m * sizeof(cg_verdict), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return c->cuda(e, "dirty download");
+  }
+  return CG_OK;
+}
+
 cg_status cg_straddler_pack(cg_ctx* c, const cg_verdict* d_raw, uint64_t m, uint64_t* d_mins, uint64_t* d_sums,
                             uint32_t* d_maxs, void* stream) {
   if (!c) return CG_ERR_INVALID_CONTEXT;
@@ -560,8 +657,9 @@ cg_status cg_compact_dirty(cg_ctx* c, const cg_verdict* d_verdicts, uint64_t n, 
   if (!c) return CG_ERR_INVALID_CONTEXT;
   if (!d_count || (n && (!d_verdicts || !d_idx || !d_dirty))) return c->fail(CG_ERR_INVALID_VALUE, "null arrays");
   DeviceGuard g(c->cfg.device);
-  return c->cuda(cgk::compact_dirty(c->launch, d_verdicts, n, d_idx, d_dirty, d_count, static_cast<cudaStream_t>(stream)),
-                 "compact dirty");
+  return c->cuda(
+      cgk::compact_dirty(c->launch, d_verdicts, n, d_idx, d_dirty, d_count, 0, true, static_cast<cudaStream_t>(stream)),
+      "compact dirty");
 }
 
 cg_status cg_leak_sweep(cg_ctx* c, cg_alloc_record* d_out, uint64_t cap, uint64_t* d_count, void* stream) {

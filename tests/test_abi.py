@@ -25,7 +25,7 @@ def cg():
 def declared_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(cg_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(cg_[a-z_0-9]+)\s*\(", src)))
 
 
 def test_every_declared_symbol_is_exported(cg):

@@ -219,3 +219,34 @@ def test_leak_sweep_device(cg):
     assert int(cnt.item()) == len(oleaks)
     assert np.array_equal(rec["base"], oleaks["base"]) and np.array_equal(rec["alloc_seq"], oleaks["seq"])
     chk.close()
+
+
+@pytest.mark.parametrize("fmt", ["1d", "2d"])
+def test_check_host_compact_chunked(cg, fmt):
+    """cg_check_host: 600k host descriptors (4 pipelined chunks), dirty-only
+    result; the dense verdicts it implies equal the oracle's."""
+    from paper_1310_0901_b200.replay import events_to_descs
+    tr = tg.c2_small(n_copies=600000, n_allocs=2000)
+    o, ov, _, _ = oracle.replay_trace(tr)
+    chk = new_checker(cg, tr, host_staging=True)
+    ev = tr.events
+    _, st = cg.replay_events(chk, ev[ev["op"] != tg.OP_COPY], tr.blob)
+    assert not st.any()
+    descs = events_to_descs(ev[ev["op"] == tg.OP_COPY])
+    if fmt == "1d":
+        d1 = np.zeros(len(descs), cg.COPY1D_DTYPE)
+        for f in ("kind", "seq", "dst", "src"):
+            d1[f] = descs[f]
+        d1["bytes"] = descs["width"]
+        nd, idx, dirty = chk.check_host(d1, apply=2)
+    else:
+        nd, idx, dirty = chk.check_host(descs, apply=2)
+    dense = np.zeros(len(descs), cg.VERDICT_DTYPE)
+    dense["first_unaddr"] = cg.CG_NONE
+    dense["first_undef"] = cg.CG_NONE
+    dense[idx.astype(np.int64)] = dirty
+    assert nd == int(np.count_nonzero(ov["flags"]))
+    assert_verdicts_equal(dense, ov, "check_host")
+    A, V = chk.shadow()
+    assert np.array_equal(V, o.V) and np.array_equal(A, o.A)
+    chk.close()
