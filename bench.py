@@ -53,6 +53,25 @@ def algorithmic_bytes(descs: np.ndarray, verdicts: np.ndarray | None):
     return check, apply
 
 
+def fused_apply_bytes(descs: np.ndarray, verdicts: np.ndarray, max_descs: int) -> float:
+    """Bytes the fused scan writes itself in cg_check_apply: DtoH descriptors
+    with status OK, contiguous, whose check weight interval lies inside one
+    scan group (the rest go to the residual apply pass).  Replicates the
+    library's plan (weight = 256 + host units; group T = max(128 KiB,
+    ceil(total / max(2^20, 2 max_descs)))) for accounting only."""
+    nb = descs["width"].astype(np.uint64) * descs["height"].astype(np.uint64)
+    units = np.where(descs["kind"] == 1, nb, np.where(descs["kind"] == 2, (nb + np.uint64(7)) // np.uint64(8), 0))
+    w = np.uint64(256) + units.astype(np.uint64)
+    P = np.concatenate([[0], np.cumsum(w, dtype=np.uint64)])
+    total = int(P[-1])
+    chunks = max(1 << 20, 2 * max_descs)
+    T = max(128 * 1024, -(-total // chunks))
+    whole = (P[:-1] // T) == ((P[1:] - 1) // T)
+    contig = (descs["height"] == 1) | (descs["width"] == descs["dst_pitch"])
+    ok = (descs["kind"] == 2) & (verdicts["status"] == 0) & contig & whole
+    return float(nb[ok].astype(np.float64).sum())
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -305,12 +324,15 @@ def run_ours(args, rank, world, device):
     scan_ms, scan_n = stages["check_scan"]
     apply_ms, apply_n = stages["apply"]
     scan_avg = scan_ms / max(scan_n, 1)
-    achieved = check_b / (scan_avg * 1e-3) / 1e9
+    scan_bytes = check_b + (fused_apply_bytes(descs, verd, max(n, 1024)) if fused else 0.0)
+    achieved = scan_bytes / (scan_avg * 1e-3) / 1e9
     traffic = None
     prof_json = os.path.join(ROOT, "profiles", f"ncu_{args.config}_check_scan.json")
     if os.path.exists(prof_json):
         with open(prof_json) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            pj = json.load(f)
+        if pj.get("fused") == fused:
+            traffic = pj.get("dram_bytes_per_launch")
     value = world * bytes_per_step / (ms_step * 1e-3) / 1e9
     res = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -327,12 +349,13 @@ def run_ours(args, rank, world, device):
         "frac_of_hbm": value / (world * peak),
         "roofline": {"bound": "hbm", "kernel": "k_check_scan", "achieved": achieved, "peak": peak,
                      "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "algorithmic_bytes_per_launch": check_b,
+                     "traffic": traffic, "algorithmic_bytes_per_launch": scan_bytes,
                      "avg_launch_ms": scan_avg,
                      "share_of_step": scan_ms / ms if ms > 0 else None},
         "stages_ms_per_step": {k: v[0] / max(args.steps, 1) for k, v in stages.items()},
-        "apply_roofline": {"achieved": apply_b / (apply_ms / max(apply_n, 1) * 1e-3) / 1e9 if apply_ms else None,
-                           "unit": "GB/s", "peak": peak},
+        "apply_roofline": {"achieved": (apply_b - (scan_bytes - check_b)) / (apply_ms / max(apply_n, 1) * 1e-3) / 1e9
+                           if apply_ms else None, "unit": "GB/s", "peak": peak,
+                           "note": "k_apply alone (the residual pass when fused)"},
         "gpu_launches": int(launches),
         "gpu_launches_per_step": launches / args.steps,
         "clocks": clocks.summary(),
