@@ -55,8 +55,8 @@ def algorithmic_bytes(descs: np.ndarray, verdicts: np.ndarray | None):
 
 def fused_apply_bytes(descs: np.ndarray, verdicts: np.ndarray, max_descs: int) -> float:
     """Bytes the fused scan writes itself in cg_check_apply: DtoH descriptors
-    with status OK, contiguous, whose check weight interval lies inside one
-    scan group (the rest go to the residual apply pass).  Replicates the
+    with status OK, contiguous and not split by the scan's grouping (weight at
+    most one group, or inside one group); the rest go to the residual pass.  Replicates the
     library's plan (weight = 256 + host units; group T = max(128 KiB,
     ceil(total / max(2^20, 2 max_descs)))) for accounting only."""
     nb = descs["width"].astype(np.uint64) * descs["height"].astype(np.uint64)
@@ -66,7 +66,7 @@ def fused_apply_bytes(descs: np.ndarray, verdicts: np.ndarray, max_descs: int) -
     total = int(P[-1])
     chunks = max(1 << 20, 2 * max_descs)
     T = max(128 * 1024, -(-total // chunks))
-    whole = (P[:-1] // T) == ((P[1:] - 1) // T)
+    whole = ((P[1:] - P[:-1]) <= T) | ((P[:-1] // T) == ((P[1:] - 1) // T))
     contig = (descs["height"] == 1) | (descs["width"] == descs["dst_pitch"])
     ok = (descs["kind"] == 2) & (verdicts["status"] == 0) & contig & whole
     return float(nb[ok].astype(np.float64).sum())

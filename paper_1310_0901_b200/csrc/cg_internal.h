@@ -45,7 +45,8 @@ struct Plan {
   uint64_t* bsum;         // [nblocks + 1]
   uint32_t* chunk_first;  // [max_chunks]
   void* meta;             // [n] ScanMeta (check plans only)
-  uint32_t* counter;      // dynamic group counter of the scan
+  uint32_t* counter;      // [0] group counter, [1] apply compaction count, [2] residual-list count
+  uint32_t* resid;        // [n] fused check: DtoH descriptors left to the residual apply
   uint64_t max_chunks;
   uint64_t t_min;
 };

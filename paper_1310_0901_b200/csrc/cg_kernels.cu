@@ -325,10 +325,18 @@ __device__ __forceinline__ uint64_t block_exclusive_scan(uint64_t x, uint64_t* s
   return r;
 }
 
+// n_dev != nullptr: the item count is min(n, *n_dev), known only on the device
+__device__ __forceinline__ uint64_t eff_n(uint64_t n, const uint32_t* n_dev) {
+  return n_dev ? umin64(n, *n_dev) : n;
+}
+
 __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint64_t* __restrict__ in, uint64_t n,
-                                                              uint64_t* __restrict__ bsum) {
+                                                              uint64_t* __restrict__ bsum,
+                                                              const uint32_t* __restrict__ n_dev) {
   __shared__ uint64_t s_warp[33];
+  n = eff_n(n, n_dev);
   const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+  if (base >= n && base > 0) return;
   uint64_t acc = 0;
 #pragma unroll
   for (int j = 0; j < kScanItems; ++j) {
@@ -340,9 +348,12 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint64_t* __
   if (threadIdx.x == 0) bsum[blockIdx.x] = total;
 }
 
-// single block: exclusive scan of bsum[0..nb) in place, bsum[nb] = total
-__global__ void __launch_bounds__(1024) k_scan_top(uint64_t* __restrict__ bsum, uint64_t nb) {
+// single block: exclusive scan of bsum[0..nb) in place; bsum[nb] = out[n] = total
+__global__ void __launch_bounds__(1024) k_scan_top(uint64_t* __restrict__ bsum, uint64_t n,
+                                                   uint64_t* __restrict__ out, const uint32_t* __restrict__ n_dev) {
   __shared__ uint64_t s_warp[33];
+  n = eff_n(n, n_dev);
+  const uint64_t nb = (n + kScanTile - 1) / kScanTile;
   uint64_t carry = 0;
   for (uint64_t base = 0; base < nb; base += blockDim.x) {
     uint64_t i = base + threadIdx.x;
@@ -352,15 +363,21 @@ __global__ void __launch_bounds__(1024) k_scan_top(uint64_t* __restrict__ bsum, 
     if (i < nb) bsum[i] = carry + ex;
     carry += total;
   }
-  if (threadIdx.x == 0) bsum[nb] = carry;
+  if (threadIdx.x == 0) {
+    bsum[nb] = carry;
+    out[n] = carry;
+  }
 }
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint64_t* __restrict__ in, uint64_t n,
                                                             const uint64_t* __restrict__ bsum,
-                                                            uint64_t* __restrict__ out, uint64_t nb) {
+                                                            uint64_t* __restrict__ out,
+                                                            const uint32_t* __restrict__ n_dev) {
   __shared__ uint64_t s_items[kScanTile];
   __shared__ uint64_t s_warp[33];
+  n = eff_n(n, n_dev);
   const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+  if (base >= n) return;
 #pragma unroll
   for (int j = 0; j < kScanItems; ++j) {
     uint64_t i = base + (uint64_t)j * kScanThreads + threadIdx.x;
@@ -384,7 +401,6 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint64_t* __re
     uint64_t i = base + (uint64_t)j * kScanThreads + threadIdx.x;
     if (i < n) out[i] = s_items[j * kScanThreads + threadIdx.x];
   }
-  if (blockIdx.x == nb - 1 && threadIdx.x == 0) out[n] = bsum[nb];
 }
 
 struct ChunkGeom {
@@ -403,7 +419,9 @@ __device__ __forceinline__ ChunkGeom chunk_geom(const uint64_t* P, uint64_t n, u
 
 // chunk_first[c] = the item whose weight interval [P[d], P[d+1]) contains c*T
 __global__ void __launch_bounds__(kThreads) k_plan(const uint64_t* __restrict__ P, uint64_t n, uint64_t t_min,
-                                                   uint64_t max_chunks, uint32_t* __restrict__ chunk_first) {
+                                                   uint64_t max_chunks, uint32_t* __restrict__ chunk_first,
+                                                   const uint32_t* __restrict__ n_dev) {
+  n = eff_n(n, n_dev);
   const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
   for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < g.nchunks;
        c += (uint64_t)gridDim.x * blockDim.x) {
@@ -684,14 +702,17 @@ struct TileGen {
   __device__ __forceinline__ void compute_pieces() {
     const int lane = threadIdx.x & 31;
     p_fl = 0;
-    if (m_ps < w1 && m_pe > w0) {
+    // a descriptor of at most one group's weight is never split: it belongs
+    // to the group its weight interval starts in
+    const bool small = m_pe - m_ps <= T;
+    if (small ? (m_ps >= w0 && m_ps < w1) : (m_ps < w1 && m_pe > w0)) {
       const uint64_t nbytes = m_info & ((1ull << 40) - 1);
       const uint32_t kind = (uint32_t)(m_info >> 40) & 3u;
       const bool host = (m_info >> 42) & 1u, contig = (m_info >> 43) & 1u;
       const bool htod = kind == CG_HTOD;
       uint32_t f = kPieceIn | (htod ? kPieceHtod : 0u);
-      if (m_ps >= w0 && m_pe <= w1) f |= kPieceWhole;
-      uint64_t a = umax64(w0, m_ps) - m_ps, b = umin64(w1, m_pe) - m_ps;
+      if (small || (m_ps >= w0 && m_pe <= w1)) f |= kPieceWhole;
+      uint64_t a = small ? 0 : umax64(w0, m_ps) - m_ps, b = small ? m_pe - m_ps : umin64(w1, m_pe) - m_ps;
       a = a > kItemCost ? a - kItemCost : 0;
       b = b > kItemCost ? b - kItemCost : 0;
       uint64_t lo = a, hi = b;
@@ -846,7 +867,7 @@ struct TileGen {
           phase = kPhaseWindow;
         }
       } else {   // kPhaseWindow: the group may continue past this window
-        const bool more = (__shfl_sync(kFull, p_fl, 31) & kPieceIn) && wbase + 32 < n;
+        const bool more = __shfl_sync(kFull, m_ps, 31) < w1 && wbase + 32 < n;
         if (more) {
           load_window(wbase + 32);
           compute_pieces();
@@ -903,7 +924,8 @@ struct TileGen {
 __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
     const ScanMeta* __restrict__ meta, uint64_t n, const uint64_t* __restrict__ P,
     const uint32_t* __restrict__ chunk_first, uint32_t* counter, uint64_t t_min, uint64_t max_chunks,
-    ShadowView sv, cg_verdict* __restrict__ out, uint32_t err_mask, int fuse) {
+    ShadowView sv, cg_verdict* __restrict__ out, uint32_t err_mask, int fuse, uint32_t* __restrict__ resid,
+    uint32_t* __restrict__ resid_n) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpRing& ring = reinterpret_cast<WarpRing*>(smem)[wid];
@@ -974,6 +996,8 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
           v->flags = flags;
           v->status = status;
           apply = (t.flags & kTileFuse) && status == CG_OK;
+          // a whole 2D DtoH piece with status OK: the residual pass applies it
+          if (fuse && !(t.flags & (kTileFuse | kTileHtod)) && status == CG_OK) resid[atomicAdd(resid_n, 1u)] = t.d;
         } else {
           if (p.fu != kNone) atomicMin(reinterpret_cast<unsigned long long*>(&v->first_unaddr), p.fu);
           if (p.fd != kNone) atomicMin(reinterpret_cast<unsigned long long*>(&v->first_undef), p.fd);
@@ -994,18 +1018,24 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
 __global__ void __launch_bounds__(kThreads) k_finalize_split(uint64_t n, const uint64_t* __restrict__ P,
                                                              uint64_t t_min, uint64_t max_chunks,
                                                              cg_verdict* __restrict__ out, uint32_t err_mask,
-                                                             const ScanMeta* __restrict__ meta) {
+                                                             const ScanMeta* __restrict__ meta, int fuse,
+                                                             uint32_t* __restrict__ resid,
+                                                             uint32_t* __restrict__ resid_n) {
   const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
   for (uint64_t d = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; d < n;
        d += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t pd = P[d], pd1 = P[d + 1];
-    if (pd1 == pd || pd / g.T == (pd1 - 1) / g.T) continue;
-    if ((meta[d].info >> 44) & 1u) continue;   // raw partial of a straddler
+    if (pd1 - pd <= g.T || pd / g.T == (pd1 - 1) / g.T) continue;   // not split (see compute_pieces)
+    const uint64_t info = meta[d].info;
+    if ((info >> 44) & 1u) continue;   // raw partial of a straddler
     cg_verdict* v = out + d;
     uint32_t flags = v->flags, status;
     finalize_fields(flags, status, v->first_unaddr, v->undef_count, err_mask);
     v->flags = flags;
     v->status = status;
+    // fused check: a split DtoH piece is applied by the residual pass
+    if (fuse && status == CG_OK && ((info >> 40) & 3u) == CG_DTOH && ((info >> 42) & 1u))
+      resid[atomicAdd(resid_n, 1u)] = (uint32_t)d;
   }
 }
 
@@ -1042,41 +1072,26 @@ constexpr uint32_t kZeroPage = 4096;
 // the front of weight[] / meta[] (order is irrelevant: the apply is idempotent
 // and commutative), so the apply walk never crosses runs of inapplicable
 // descriptors; weight[] must be zero on entry.
-// fusedP != nullptr: the check that just ran (cg_check_apply) already applied
-// every whole contiguous DtoH piece of its plan (fusedP, its chunk geometry);
-// only the remaining ones are compacted here.
 __global__ void __launch_bounds__(kThreads) k_apply_prep(const cg_copy_desc* __restrict__ descs,
                                                          const cg_verdict* __restrict__ verd, uint64_t n,
                                                          uint64_t* __restrict__ weight, ScanMeta* __restrict__ meta,
-                                                         uint32_t* __restrict__ count,
-                                                         const uint64_t* __restrict__ fusedP, uint64_t t_min,
-                                                         uint64_t max_chunks) {
-  uint64_t fT = 1;
-  if (fusedP) fT = chunk_geom(fusedP, n, t_min, max_chunks).T;
+                                                         uint32_t* __restrict__ count) {
   const int lane = threadIdx.x & 31;
   for (uint64_t b0 = (uint64_t)blockIdx.x * blockDim.x; b0 < n; b0 += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t i = b0 + threadIdx.x;
     bool ok = false;
     ScanMeta m;
     uint64_t w = 0;
-    // after a fused check, straddler partials (CG_SHARD_RAW) are not final yet
-    if (i < n && descs[i].kind == CG_DTOH && verd[i].status == CG_OK &&
-        !(fusedP && (descs[i].reserved & CG_SHARD_RAW))) {
+    if (i < n && descs[i].kind == CG_DTOH && verd[i].status == CG_OK) {
       const cg_copy_desc d = descs[i];
       const Norm nm = normalize(d);
-      const bool contig = d.height == 1 || d.width == nm.hpitch;
-      bool done = false;
-      if (fusedP && contig) {
-        const uint64_t pd = fusedP[i], pd1 = fusedP[i + 1];
-        done = pd / fT == (pd1 - 1) / fT;
-      }
-      if (nm.host && nm.nbytes && !done) {
+      if (nm.host && nm.nbytes) {
         ok = true;
         w = kApplyItemCost + nm.nbytes;
         m.hstart = nm.hstart;
         m.hpitch = nm.hpitch;
         m.W = nm.W;
-        m.info = nm.nbytes | ((uint64_t)contig << 43);
+        m.info = nm.nbytes | ((uint64_t)(d.height == 1 || d.width == nm.hpitch) << 43);
       }
     }
     const uint32_t mask = __ballot_sync(kFull, ok);
@@ -1091,6 +1106,28 @@ __global__ void __launch_bounds__(kThreads) k_apply_prep(const cg_copy_desc* __r
         meta[k] = m;
       }
     }
+  }
+}
+
+// after cg_check_apply: the DtoH descriptors the fused scan did not apply
+// itself (split across groups, or 2D) and whose verdict is OK were listed by
+// the scan / k_finalize_split; compact weights and metadata for them
+__global__ void __launch_bounds__(kThreads) k_apply_list_prep(const cg_copy_desc* __restrict__ descs,
+                                                              const uint32_t* __restrict__ list,
+                                                              const uint32_t* __restrict__ count,
+                                                              uint64_t* __restrict__ weight,
+                                                              ScanMeta* __restrict__ meta) {
+  const uint64_t m = *count;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += (uint64_t)gridDim.x * blockDim.x) {
+    const cg_copy_desc d = descs[list[k]];
+    const Norm nm = normalize(d);
+    ScanMeta mm;
+    mm.hstart = nm.hstart;
+    mm.hpitch = nm.hpitch;
+    mm.W = nm.W;
+    mm.info = nm.nbytes | ((uint64_t)(d.height == 1 || d.width == nm.hpitch) << 43);
+    meta[k] = mm;
+    weight[k] = kApplyItemCost + nm.nbytes;
   }
 }
 
@@ -1133,7 +1170,9 @@ __device__ __forceinline__ void warp_zero(uint8_t* V, uint64_t q0, uint64_t q1, 
 __global__ void __launch_bounds__(kThreads) k_apply(const ScanMeta* __restrict__ meta, uint64_t n,
                                                     const uint64_t* __restrict__ P,
                                                     const uint32_t* __restrict__ chunk_first, uint32_t* counter,
-                                                    uint64_t t_min, uint64_t max_chunks, ShadowView sv) {
+                                                    uint64_t t_min, uint64_t max_chunks, ShadowView sv,
+                                                    const uint32_t* __restrict__ n_dev) {
+  n = eff_n(n, n_dev);
   __shared__ __align__(128) uint8_t zeros[kZeroPage];
   for (uint32_t i = threadIdx.x; i < kZeroPage / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(zeros)[i] = make_uint4(0, 0, 0, 0);
@@ -1415,18 +1454,14 @@ inline int blocks_for(uint64_t n, int threads, int cap) {
 uint64_t scan_blocks(uint64_t n) { return (n + kScanTile - 1) / kScanTile; }
 
 // prefix sum of p.weight[0..n) into p.P[0..n], then the chunk plan
-static cudaError_t plan(const Launch& L, uint64_t n, const Plan& p, cudaStream_t s) {
-  const uint64_t nb = scan_blocks(n);
-  if (nb > 0) {
-    k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, n, p.bsum);
-    k_scan_top<<<1, 1024, 0, s>>>(p.bsum, nb);
-    k_scan_down<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, n, p.bsum, p.P, nb);
-    *L.counter += 3;
-  } else {
-    cudaMemsetAsync(p.P, 0, sizeof(uint64_t), s);
-  }
-  k_plan<<<L.num_sms * 4, kThreads, 0, s>>>(p.P, n, p.t_min, p.max_chunks, p.chunk_first);
-  *L.counter += 1;
+static cudaError_t plan(const Launch& L, uint64_t n, const Plan& p, cudaStream_t s,
+                        const uint32_t* n_dev = nullptr) {
+  const uint64_t nb = std::max<uint64_t>(scan_blocks(n), 1);
+  k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, n, p.bsum, n_dev);
+  k_scan_top<<<1, 1024, 0, s>>>(p.bsum, n, p.P, n_dev);
+  k_scan_down<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, n, p.bsum, p.P, n_dev);
+  k_plan<<<L.num_sms * 4, kThreads, 0, s>>>(p.P, n, p.t_min, p.max_chunks, p.chunk_first, n_dev);
+  *L.counter += 4;
   return cudaGetLastError();
 }
 
@@ -1443,15 +1478,15 @@ cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_
   cudaError_t e = plan(L, n, p, s);
   if (e != cudaSuccess) return e;
   L.stage(CG_STAGE_CHECK_PLAN, false, s);
-  cudaMemsetAsync(p.counter, 0, sizeof(uint32_t), s);
+  cudaMemsetAsync(p.counter, 0, 3 * sizeof(uint32_t), s);   // group counter, (apply), residual count
   L.stage(CG_STAGE_CHECK_SCAN, true, s);
   k_check_scan<<<L.scan_blocks, kRingWarps * 32, kScanSmem, s>>>(meta, n, p.P, p.chunk_first, p.counter,
                                                                  p.t_min, p.max_chunks, sv, out, err_mask,
-                                                                 fuse ? 1 : 0);
+                                                                 fuse ? 1 : 0, p.resid, p.counter + 2);
   L.stage(CG_STAGE_CHECK_SCAN, false, s);
   L.stage(CG_STAGE_CHECK_FINAL, true, s);
-  k_finalize_split<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(n, p.P, p.t_min, p.max_chunks,
-                                                                               out, err_mask, meta);
+  k_finalize_split<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(
+      n, p.P, p.t_min, p.max_chunks, out, err_mask, meta, fuse ? 1 : 0, p.resid, p.counter + 2);
   L.stage(CG_STAGE_CHECK_FINAL, false, s);
   *L.counter += 2;
   return cudaGetLastError();
@@ -1461,20 +1496,26 @@ cudaError_t apply_dtoh(const Launch& L, const cg_copy_desc* d, const cg_verdict*
                        const ShadowView& sv, const Plan& p, bool after_fused, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
+  const uint32_t* n_dev = after_fused ? p.counter + 2 : nullptr;   // residual list count
   L.stage(CG_STAGE_APPLY_PREP, true, s);
-  cudaMemsetAsync(p.weight, 0, n * sizeof(uint64_t), s);
-  cudaMemsetAsync(p.counter + 1, 0, sizeof(uint32_t), s);
-  k_apply_prep<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(
-      d, v, n, p.weight, meta, p.counter + 1, after_fused ? p.P : nullptr, p.t_min, p.max_chunks);
+  if (after_fused) {
+    k_apply_list_prep<<<L.num_sms * 2, kThreads, 0, s>>>(d, p.resid, n_dev, p.weight, meta);
+  } else {
+    cudaMemsetAsync(p.weight, 0, n * sizeof(uint64_t), s);
+    cudaMemsetAsync(p.counter + 1, 0, sizeof(uint32_t), s);
+    k_apply_prep<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(d, v, n, p.weight, meta,
+                                                                             p.counter + 1);
+  }
   *L.counter += 1;
   L.stage(CG_STAGE_APPLY_PREP, false, s);
   L.stage(CG_STAGE_APPLY_PLAN, true, s);
-  cudaError_t e = plan(L, n, p, s);
+  cudaError_t e = plan(L, n, p, s, n_dev);
   if (e != cudaSuccess) return e;
   L.stage(CG_STAGE_APPLY_PLAN, false, s);
   L.stage(CG_STAGE_APPLY, true, s);
   cudaMemsetAsync(p.counter, 0, sizeof(uint32_t), s);
-  k_apply<<<L.persist_blocks, kThreads, 0, s>>>(meta, n, p.P, p.chunk_first, p.counter, p.t_min, p.max_chunks, sv);
+  k_apply<<<L.persist_blocks, kThreads, 0, s>>>(meta, n, p.P, p.chunk_first, p.counter, p.t_min, p.max_chunks, sv,
+                                                n_dev);
   L.stage(CG_STAGE_APPLY, false, s);
   *L.counter += 1;
   return cudaGetLastError();
@@ -1514,9 +1555,9 @@ cudaError_t leak_sweep(const Launch& L, const Table& t, const Plan& p, cg_alloc_
   L.stage(CG_STAGE_LEAK, true, s);
   k_live<<<blocks_for(t.n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(t, p.weight);
   const uint64_t nb = scan_blocks(t.n);
-  k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, t.n, p.bsum);
-  k_scan_top<<<1, 1024, 0, s>>>(p.bsum, nb);
-  k_scan_down<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, t.n, p.bsum, p.P, nb);
+  k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, t.n, p.bsum, nullptr);
+  k_scan_top<<<1, 1024, 0, s>>>(p.bsum, t.n, p.P, nullptr);
+  k_scan_down<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, t.n, p.bsum, p.P, nullptr);
   k_leak_scatter<<<blocks_for(t.n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(t, p.P, out, cap, d_count);
   L.stage(CG_STAGE_LEAK, false, s);
   *L.counter += 5;

@@ -33,7 +33,7 @@ struct Entry {
 };
 
 struct Layout {
-  uint64_t table, weight, P, bsum, chunk, meta, marks, flags, leaks, desc_stage, verdict_stage, raw_stage,
+  uint64_t table, weight, P, bsum, chunk, meta, resid, marks, flags, leaks, desc_stage, verdict_stage, raw_stage,
       idx_stage, dirty_stage, total;
   uint64_t max_items, max_chunks;
 };
@@ -67,6 +67,7 @@ Layout layout_of(const cg_config* c) {
   L.bsum = take((cgk::scan_blocks(L.max_items) + 1) * 8);
   L.chunk = take(L.max_chunks * 4);
   L.meta = take(c->max_descs * cgk::scan_meta_bytes());
+  L.resid = take(c->max_descs * sizeof(uint32_t));
   L.marks = take(std::min<uint64_t>(c->max_descs, kMarkRun) * sizeof(cg_mark));
   L.flags = take(256);
   L.leaks = take(c->max_allocs * sizeof(cg_alloc_record));
@@ -158,6 +159,7 @@ struct cg_ctx {
     p.chunk_first = reinterpret_cast<uint32_t*>(ws + lay.chunk);
     p.meta = ws + lay.meta;
     p.counter = reinterpret_cast<uint32_t*>(ws + lay.flags + 128);
+    p.resid = reinterpret_cast<uint32_t*>(ws + lay.resid);
     p.max_chunks = lay.max_chunks;
     p.t_min = kChunkMin;
     return p;
