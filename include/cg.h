@@ -352,6 +352,19 @@ cg_status cg_leak_report(cg_ctx *ctx, cg_alloc_record *h_out, uint64_t cap, uint
  * *n_cuts.  Errors: CG_ERR_INVALID_VALUE on NULL. */
 cg_status cg_plan_batches(const cg_copy_desc *h_descs, uint64_t n, uint64_t *h_cuts, uint64_t *n_cuts);
 
+/* Diagnostic text (SPEC format_text S:454-462): renders
+ * one line pair per set flag of *v, in flag order, for a copy of the given
+ * kind, into buf (NUL-terminated, truncated to cap).  The TooSmall text is the
+ * paper's Listing 5 verbatim: "Error: Allocated device memory too
+ * small for device->host copy.\nExpected 8000000 allocated bytes but only
+ * found 4000000."; the other messages follow SPEC's "Error: <message>." /
+ * "Warning: <message>." template.  Returns the number of characters needed
+ * (excluding the NUL), like snprintf. */
+uint64_t cg_format_verdict(const cg_verdict *v, uint32_t kind, char *buf, uint64_t cap);
+
+/* "Warning: Device memory leak of <size> bytes."; as above. */
+uint64_t cg_format_leak(const cg_alloc_record *r, char *buf, uint64_t cap);
+
 /* Number of kernels this context has launched so far (for bench accounting). */
 uint64_t cg_kernel_launches(const cg_ctx *ctx);
 

@@ -98,6 +98,8 @@ def _load() -> ctypes.CDLL:
         "cg_host_query_addressable": (I, [P, U64, U64, P, P]),
         "cg_expand_copy1d": (I, [P, P, U64, P, P]),
         "cg_check_host": (I, [P, P, U32, U64, I, P, P, U64, P, P]),
+        "cg_format_verdict": (U64, [P, U32, P, U64]),
+        "cg_format_leak": (U64, [P, P, U64]),
         "cg_shard_plan": (I, [P, U64, U64, U64, U32, P, P, P]),
         "cg_batch_disjoint": (I, [P, U64, P]),
         "cg_leak_sweep": (I, [P, P, U64, P, P]),
@@ -120,7 +122,8 @@ EXPORTED = ("cg_workspace_size", "cg_ctx_create", "cg_ctx_destroy", "cg_last_err
             "cg_check_copies", "cg_apply_dtoh", "cg_check_copies_host", "cg_leak_sweep", "cg_leak_report",
             "cg_plan_batches", "cg_kernel_launches", "cg_profile_begin", "cg_profile_end", "cg_check_apply",
             "cg_batch_disjoint", "cg_straddler_pack", "cg_straddler_finalize", "cg_compact_dirty", "cg_shard_plan",
-            "cg_host_query_addressable", "cg_expand_copy1d", "cg_check_host")
+            "cg_host_query_addressable", "cg_expand_copy1d", "cg_check_host", "cg_format_verdict",
+            "cg_format_leak")
 
 # ---- same-name thin wrappers (status codes returned unchanged) -------------
 cg_workspace_size = _lib.cg_workspace_size
@@ -143,6 +146,24 @@ cg_compact_dirty = _lib.cg_compact_dirty
 cg_host_query_addressable = _lib.cg_host_query_addressable
 cg_expand_copy1d = _lib.cg_expand_copy1d
 cg_check_host = _lib.cg_check_host
+cg_format_verdict = _lib.cg_format_verdict
+cg_format_leak = _lib.cg_format_leak
+
+
+def format_verdict(v, kind: int) -> str:
+    """Diagnostic text of one verdict (cg_format_verdict; Listing 5 style)."""
+    a = np.ascontiguousarray(np.asarray(v, dtype=VERDICT_DTYPE).reshape(1))
+    need = _lib.cg_format_verdict(a.ctypes.data, int(kind), None, 0)
+    buf = ctypes.create_string_buffer(need + 1)
+    _lib.cg_format_verdict(a.ctypes.data, int(kind), buf, need + 1)
+    return buf.value.decode()
+
+
+def format_leak(rec) -> str:
+    a = np.ascontiguousarray(np.asarray(rec, dtype=ALLOC_RECORD_DTYPE).reshape(1))
+    buf = ctypes.create_string_buffer(128)
+    _lib.cg_format_leak(a.ctypes.data, buf, 128)
+    return buf.value.decode()
 CG_FMT_2D, CG_FMT_1D = 0, 1
 COPY1D_DTYPE = np.dtype([("kind", "<u4"), ("reserved", "<u4"), ("seq", "<u8"), ("dst", "<u8"), ("src", "<u8"),
                          ("bytes", "<u8")])

@@ -312,6 +312,58 @@ const char* cg_last_error(const cg_ctx* c) { return c ? c->err.c_str() : "null c
 
 uint64_t cg_kernel_launches(const cg_ctx* c) { return c ? c->launches : 0; }
 
+static const char* direction(uint32_t kind) {
+  return kind == CG_HTOD ? "host->device" : kind == CG_DTOH ? "device->host" : "device->device";
+}
+
+uint64_t cg_format_verdict(const cg_verdict* v, uint32_t kind, char* buf, uint64_t cap) {
+  std::string t;
+  char line[256];
+  auto add = [&](const char* fmt, auto... args) {
+    snprintf(line, sizeof line, fmt, args...);
+    t += line;
+  };
+  if (!v) return 0;
+  const char* dir = direction(kind);
+  const unsigned long long de = v->dst_expected, df = v->dst_found, se = v->src_expected, sf = v->src_found;
+  const unsigned long long fu = v->first_unaddr, fd = v->first_undef, uc = v->undef_count;
+  if (v->flags & CG_F_DST_NOT_ALLOCATED) add("Error: Destination device memory of %s copy is not allocated.\n", dir);
+  if (v->flags & CG_F_DST_TOO_SMALL)
+    add("Error: Allocated device memory too small for %s copy.\nExpected %llu allocated bytes but only found %llu.\n",
+        dir, de, df);
+  if (v->flags & CG_F_SRC_NOT_ALLOCATED) add("Error: Source device memory of %s copy is not allocated.\n", dir);
+  if (v->flags & CG_F_SRC_TOO_SMALL)
+    add("Error: Allocated device memory too small for %s copy.\nExpected %llu allocated bytes but only found %llu.\n",
+        dir, se, sf);
+  if (v->flags & CG_F_HOST_UNADDRESSABLE)
+    add("Error: Host memory of %s copy is not addressable (first unaddressable byte at offset %llu).\n", dir, fu);
+  if (v->flags & CG_F_HOST_UNDEFINED)
+    add("Warning: Undefined host data copied to the device (%llu undefined bytes, first at offset %llu).\n", uc, fd);
+  if (v->flags & CG_F_BAD_PITCH) add("Error: Pitch of %s copy smaller than width plus X offset.\n", dir);
+  if (v->flags & CG_F_INVALID_RANGE) add("Error: Address range of %s copy overflows.\n", dir);
+  if (v->flags & CG_F_BAD_KIND) add("Error: Unknown copy kind %u.\n", kind);
+  if (cap) {
+    const uint64_t m = std::min<uint64_t>(t.size(), cap - 1);
+    if (buf) {
+      std::memcpy(buf, t.data(), m);
+      buf[m] = 0;
+    }
+  }
+  return t.size();
+}
+
+uint64_t cg_format_leak(const cg_alloc_record* r, char* buf, uint64_t cap) {
+  if (!r) return 0;
+  char line[128];
+  const int k = snprintf(line, sizeof line, "Warning: Device memory leak of %llu bytes.\n", (unsigned long long)r->size);
+  if (cap && buf) {
+    const uint64_t m = std::min<uint64_t>((uint64_t)k, cap - 1);
+    std::memcpy(buf, line, m);
+    buf[m] = 0;
+  }
+  return (uint64_t)k;
+}
+
 cg_status cg_profile_begin(cg_ctx* c) {
   if (!c) return CG_ERR_INVALID_CONTEXT;
   c->prof.on = true;

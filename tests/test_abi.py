@@ -138,3 +138,41 @@ def test_batch_disjoint_configs(cg):
     from paper_1310_0901_b200.replay import events_to_descs
     for tr in (tg.c2_small(n_copies=20000, n_allocs=2000), tg.c4_pitched(n_copies=2000, n_bufs=2, rows=64)):
         assert cg.batch_disjoint(events_to_descs(tr.events[tr.events["op"] == tg.OP_COPY]))
+
+
+def test_listing5_text_from_verdict(cg):
+    """NEXT-4: the TooSmall verdict of the paper's worked example renders the
+    first two lines of Listing 5 byte for byte (tests/golden)."""
+    lines = [l for l in open(os.path.join(ROOT, "tests", "golden", "listing5.txt")) if not l.startswith("#")]
+    v = np.zeros(1, cg.VERDICT_DTYPE)[0]
+    v["first_unaddr"] = v["first_undef"] = cg.CG_NONE
+    v["src_expected"], v["src_found"], v["flags"], v["status"] = 8000000, 4000000, cg.CG_F_SRC_TOO_SMALL, 1
+    assert cg.format_verdict(v, cg.CG_DTOH) == "".join(lines)
+    assert cg.format_verdict(np.zeros(1, cg.VERDICT_DTYPE)[0], cg.CG_HTOD) == ""
+    rec = np.zeros(1, cg.ALLOC_RECORD_DTYPE)[0]
+    rec["size"] = 4096
+    assert cg.format_leak(rec) == "Warning: Device memory leak of 4096 bytes.\n"   # S:461
+
+
+def test_format_is_injective_on_fuzzed_verdicts(cg):
+    """formatting is injective over (flags, expected, found, offsets)."""
+    rng = np.random.default_rng(0)
+    seen = {}
+    for _ in range(3000):
+        v = np.zeros(1, cg.VERDICT_DTYPE)[0]
+        v["flags"] = int(rng.integers(1, 1 << 9))
+        for f in ("first_unaddr", "first_undef", "undef_count", "dst_expected", "dst_found", "src_expected", "src_found"):
+            v[f] = int(rng.integers(0, 1 << 40))
+        k = int(rng.integers(1, 4))
+        key = cg.format_verdict(v, k)
+        rel = tuple(int(v[f]) for f in v.dtype.names if f != "status") + (k,)
+        # only fields a set flag reports are part of the identity
+        fl = int(v["flags"])
+        ident = (k, fl,
+                 int(v["dst_expected"]) if fl & 2 else None, int(v["dst_found"]) if fl & 2 else None,
+                 int(v["src_expected"]) if fl & 8 else None, int(v["src_found"]) if fl & 8 else None,
+                 int(v["first_unaddr"]) if fl & 16 else None,
+                 (int(v["undef_count"]), int(v["first_undef"])) if fl & 32 else None)
+        if key in seen:
+            assert seen[key] == ident
+        seen[key] = ident
