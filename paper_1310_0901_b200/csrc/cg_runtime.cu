@@ -338,7 +338,7 @@ uint64_t cg_format_verdict(const cg_verdict* v, uint32_t kind, char* buf, uint64
   if (v->flags & CG_F_HOST_UNADDRESSABLE)
     add("Error: Host memory of %s copy is not addressable (first unaddressable byte at offset %llu).\n", dir, fu);
   if (v->flags & CG_F_HOST_UNDEFINED)
-    add("Warning: Undefined host data copied to the device (%llu undefined bytes, first at offset %llu).\n", uc, fd);
+    add("Warning: Undefined host data in %s copy (%llu undefined bytes, first at offset %llu).\n", dir, uc, fd);
   if (v->flags & CG_F_BAD_PITCH) add("Error: Pitch of %s copy smaller than width plus X offset.\n", dir);
   if (v->flags & CG_F_INVALID_RANGE) add("Error: Address range of %s copy overflows.\n", dir);
   if (v->flags & CG_F_BAD_KIND) add("Error: Unknown copy kind %u.\n", kind);
