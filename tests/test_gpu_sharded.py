@@ -77,3 +77,29 @@ def test_c5_scaled_sharded(cg, world):
     epochs, large copies straddling shard boundaries, final leak report."""
     tr = tg.c5_sharded(scale=0.01)
     run_sharded(cg, tr, world, fuse=True)
+
+
+def test_nccl_path_single_rank(cg):
+    """The torch.distributed (NCCL) driver end to end on a 1-rank process
+    group: check, (empty) straddler exchange, dirty-verdict gather, assembly."""
+    import os
+    import torch
+    import torch.distributed as dist
+    from paper_1310_0901_b200.replay import events_to_descs
+    from paper_1310_0901_b200.sharded import BatchPlan, ShardedChecker, run_distributed
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        tr = tg.c2_small(n_copies=20000, n_allocs=2000)
+        o, ov, _, _ = oracle.replay_trace(tr)
+        sc = ShardedChecker(tr.host_base, tr.host_size, 0, 1, max_descs=20000, max_allocs=4096)
+        ev = tr.events
+        cg.replay_events(sc.chk, ev[ev["op"] != tg.OP_COPY], tr.blob)
+        descs = events_to_descs(ev[ev["op"] == tg.OP_COPY])
+        v = run_distributed(sc, BatchPlan(descs, tr.host_base, tr.host_size, 1))
+        for f in ov.dtype.names:
+            assert np.array_equal(v[f], ov[f]), f
+        sc.close()
+    finally:
+        dist.destroy_process_group()
