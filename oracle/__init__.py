@@ -71,6 +71,8 @@ def _load():
         lib.or_check_copy.argtypes = [P, P, P]
         lib.or_leaks.restype = U64; lib.or_leaks.argtypes = [P, P, U64]
         lib.or_replay.restype = U64; lib.or_replay.argtypes = [P, P, U64, P, P, P]
+        lib.or_track_device.argtypes = [P, I]
+        lib.or_device_vbits.restype = I; lib.or_device_vbits.argtypes = [P, U64, U64, P]
         _lib = lib
     return _lib
 
@@ -78,12 +80,14 @@ def _load():
 class Oracle:
     """Sequential replay state: host window shadow + device allocation list."""
 
-    def __init__(self, host_base: int, host_size: int, undef_is_error: bool = False):
+    def __init__(self, host_base: int, host_size: int, undef_is_error: bool = False, track_device: bool = False):
         self.lib = _load()
         self.h0, self.s = host_base, host_size
         self.st = self.lib.or_create(host_base, host_size, int(undef_is_error))
         if not self.st:
             raise MemoryError("oracle state allocation failed")
+        if track_device:
+            self.lib.or_track_device(self.st, 1)
 
     def close(self):
         if self.st:
@@ -127,6 +131,12 @@ class Oracle:
         self.lib.or_check_copy(self.st, ev.ctypes.data, out.ctypes.data)
         return out[0]
 
+    def device_vbits(self, addr: int, length: int) -> Optional[np.ndarray]:
+        out = np.zeros(max(length, 1), np.uint8)
+        if self.lib.or_device_vbits(self.st, addr, length, out.ctypes.data):
+            return None
+        return out[:length]
+
     def leaks(self) -> np.ndarray:
         n = self.lib.or_leaks(self.st, None, 0)
         out = np.zeros(n, ALLOC_DTYPE)
@@ -146,9 +156,9 @@ class Oracle:
         return out_v[:ncopy], out_s[:n]
 
 
-def replay_trace(trace, undef_is_error: bool = False):
+def replay_trace(trace, undef_is_error: bool = False, track_device: bool = False):
     """Convenience: fresh oracle, replay the whole trace, return
     (oracle, verdicts, statuses, leaks)."""
-    o = Oracle(trace.host_base, trace.host_size, undef_is_error)
+    o = Oracle(trace.host_base, trace.host_size, undef_is_error, track_device)
     v, s = o.replay(trace.events, trace.blob)
     return o, v, s, o.leaks()

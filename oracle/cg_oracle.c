@@ -73,7 +73,9 @@ typedef struct {
     uint8_t *A;            /* s/8 bytes */
     uint8_t *V;            /* s bytes   */
     or_alloc *live;        /* unsorted list of live allocations (Fig. 2) */
+    uint8_t **dv;          /* NEXT-1: device V-bytes of live[i] (track mode), else NULL */
     uint64_t n_live, cap_live;
+    int track;             /* NEXT-1: propagate V-bits through copies (SPEC copy_vbits) */
     uint64_t last_reg_seq;
     int undef_is_error;    /* CLI flag promotes HostUndefined */
 } or_state;
@@ -89,12 +91,21 @@ or_state *or_create(uint64_t h0, uint64_t s, int undef_is_error) {
     memset(st->V, 0xFF, s);                            /* V = all undefined  */
     st->cap_live = 16;
     st->live = (or_alloc *)malloc(st->cap_live * sizeof(or_alloc));
+    st->dv = (uint8_t **)calloc(st->cap_live, sizeof(uint8_t *));
     return st;
 }
 
+/* NEXT-1: device
+ * allocations carry V-bits too (fresh: undefined); an error-free HtoD copies
+ * host V-bits to the device, DtoD device to device (as if staged through a
+ * scratch buffer), DtoH device to host -- instead of R-5's "DtoH marks
+ * the host range defined".  Must be set before the first registration. */
+void or_track_device(or_state *st, int on) { st->track = on; }
+
 void or_destroy(or_state *st) {
     if (!st) return;
-    free(st->A); free(st->V); free(st->live); free(st);
+    for (uint64_t i = 0; i < st->n_live; i++) free(st->dv[i]);
+    free(st->A); free(st->V); free(st->live); free(st->dv); free(st);
 }
 
 uint8_t *or_A(or_state *st) { return st->A; }
@@ -156,10 +167,16 @@ int or_register(or_state *st, uint64_t base, uint64_t size, uint64_t seq) {
     if (st->n_live == st->cap_live) {
         st->cap_live *= 2;
         st->live = (or_alloc *)realloc(st->live, st->cap_live * sizeof(or_alloc));
+        st->dv = (uint8_t **)realloc(st->dv, st->cap_live * sizeof(uint8_t *));
     }
     st->live[st->n_live].base = base;
     st->live[st->n_live].size = size;
     st->live[st->n_live].seq = seq;
+    st->dv[st->n_live] = NULL;
+    if (st->track) {                                      /* fresh device memory is undefined */
+        st->dv[st->n_live] = (uint8_t *)malloc(size);
+        memset(st->dv[st->n_live], 0xFF, size);
+    }
     st->n_live++;
     st->last_reg_seq = seq;
     return 0;
@@ -170,7 +187,9 @@ int or_free(or_state *st, uint64_t ptr, uint64_t seq) {
     if (seq <= st->last_reg_seq) return 1;
     for (uint64_t i = 0; i < st->n_live; i++) {
         if (st->live[i].base == ptr) {                    /* S:150 base match only */
+            free(st->dv[i]);
             st->live[i] = st->live[st->n_live - 1];
+            st->dv[i] = st->dv[st->n_live - 1];
             st->n_live--;
             st->last_reg_seq = seq;
             return 0;
@@ -207,6 +226,28 @@ static void device_side(const or_state *st, uint64_t start, uint64_t span,
         }
     }
     *flags |= f_na;
+}
+
+/* device V-bytes at device address x (inside a live allocation) */
+static uint8_t *device_vbits(const or_state *st, uint64_t x) {
+    for (uint64_t i = 0; i < st->n_live; i++) {
+        const or_alloc *e = &st->live[i];
+        if (e->base <= x && x < e->base + e->size) return st->dv[i] + (x - e->base);
+    }
+    return NULL;
+}
+
+/* device V-bytes of [x, x+len) into out (test view; 1 if not inside one live allocation) */
+int or_device_vbits(const or_state *st, uint64_t x, uint64_t len, uint8_t *out) {
+    for (uint64_t i = 0; i < st->n_live; i++) {
+        const or_alloc *e = &st->live[i];
+        if (e->base <= x && x < e->base + e->size) {
+            if (len > e->base + e->size - x || !st->dv[i]) return 1;
+            memcpy(out, st->dv[i] + (x - e->base), len);
+            return 0;
+        }
+    }
+    return 1;
 }
 
 void or_check_copy(or_state *st, const or_event *ev, or_verdict *v) {
@@ -264,10 +305,27 @@ void or_check_copy(or_state *st, const or_event *ev, or_verdict *v) {
     v->status = errors ? 1u : 0u;
 
     /* (v) DtoH with no Error: the written host bytes become defined (R-5, R-7) */
-    if (kind == OR_DTOH && v->status == 0) {
+    if (kind == OR_DTOH && v->status == 0 && !st->track) {
         for (uint64_t r = 0; r < H && W; r++)
             for (uint64_t c = 0; c < W; c++)
                 st->V[ds + r * ev->dst_pitch + c - st->h0] = 0x00;
+    }
+    /* (v') NEXT-1: with device V-bits, an error-free copy moves V-bits */
+    if (st->track && v->status == 0 && W && H) {
+        uint8_t *dd = NULL, *sd = NULL;   /* device V of dst / src at their start */
+        if (kind == OR_HTOD || kind == OR_DTOD) dd = device_vbits(st, ds);
+        if (kind == OR_DTOH || kind == OR_DTOD) sd = device_vbits(st, ss);
+        uint8_t *tmp = (uint8_t *)malloc(W * H);           /* logical order, staged */
+        for (uint64_t r = 0; r < H; r++)
+            for (uint64_t c = 0; c < W; c++)
+                tmp[r * W + c] = (kind == OR_HTOD) ? st->V[ss + r * ev->src_pitch + c - st->h0]
+                                                   : sd[r * ev->src_pitch + c];
+        for (uint64_t r = 0; r < H; r++)
+            for (uint64_t c = 0; c < W; c++) {
+                if (kind == OR_DTOH) st->V[ds + r * ev->dst_pitch + c - st->h0] = tmp[r * W + c];
+                else dd[r * ev->dst_pitch + c] = tmp[r * W + c];
+            }
+        free(tmp);
     }
 }
 

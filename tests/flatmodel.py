@@ -21,8 +21,10 @@ FLAG = dict(DST_NA=1, DST_SMALL=2, SRC_NA=4, SRC_SMALL=8, HOST_UNADDR=16,
 
 
 class FlatModel:
-    def __init__(self, h0: int, s: int, undef_is_error: bool = False):
+    def __init__(self, h0: int, s: int, undef_is_error: bool = False, track: bool = False):
         self.h0, self.s = h0, s
+        self.track = track
+        self.dv: dict = {}                        # base -> numpy V-bytes of the allocation (NEXT-1)
         self.a = np.zeros(s, bool)               # unpacked A
         self.v = np.full(s, 0xFF, np.uint8)
         self.bases: list = []                     # sorted live bases
@@ -79,6 +81,8 @@ class FlatModel:
             return 1
         self.bases.insert(k, base)
         self.info[base] = (size, seq)
+        if self.track:
+            self.dv[base] = np.full(size, 0xFF, np.uint8)
         self.last = seq
         return 0
 
@@ -87,6 +91,7 @@ class FlatModel:
             return 1
         self.bases.remove(ptr)
         del self.info[ptr]
+        self.dv.pop(ptr, None)
         self.last = seq
         return 0
 
@@ -153,10 +158,28 @@ class FlatModel:
             out["flags"] |= FLAG["HOST_UNDEF"]
         err = out["flags"] & ~(0 if self.uie else FLAG["HOST_UNDEF"])
         out["status"] = 1 if err else 0
-        if kind == 2 and out["status"] == 0 and w and h:
+        if kind == 2 and out["status"] == 0 and w and h and not self.track:
             start, _, pitch, _ = sides["dst"]
             xs = self._host_index(start, pitch, w, h)
             self.v[np.array([x - self.h0 for x in xs], np.int64)] = 0
+        if self.track and out["status"] == 0 and w and h:
+            def read(p):
+                start, _, pitch, _ = sides[p]
+                xs = self._host_index(start, pitch, w, h)
+                if p == {1: "src", 2: "dst", 3: None}[kind]:
+                    return self.v[np.array([x - self.h0 for x in xs], np.int64)].copy()
+                b = self._containing(start)
+                return self.dv[b][np.array([x - b for x in xs], np.int64)].copy()
+
+            def write(p, vals):
+                start, _, pitch, _ = sides[p]
+                xs = self._host_index(start, pitch, w, h)
+                if kind == 2:
+                    self.v[np.array([x - self.h0 for x in xs], np.int64)] = vals
+                else:
+                    b = self._containing(start)
+                    self.dv[b][np.array([x - b for x in xs], np.int64)] = vals
+            write("dst", read("src"))    # read everything first: memmove semantics
         return out
 
     def replay(self, events, blob):
