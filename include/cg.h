@@ -156,7 +156,14 @@ typedef struct {
  *  - max_descs: largest n accepted by one check/apply/mark-batch call.
  *  - max_allocs: allocation-table capacity (live entries plus tombstones).
  *  - host_staging: nonzero reserves device staging in the workspace for
- *    cg_check_copies_host (descriptors + verdicts of max_descs). */
+ *    cg_check_copies_host (descriptors + verdicts of max_descs).
+ *  - dev_vbuf / dev_vsize (NEXT-1; SPEC copy_vbits S:81-89):
+ *    non-NULL enables device V-bit tracking.  Every registered allocation gets
+ *    `size` bytes of device V-bits in this caller-owned pool (bump allocated,
+ *    never reused; fresh = undefined) and cg_apply_copies moves V-bits
+ *    through error-free copies (HtoD host->device, DtoD device->device with
+ *    memmove semantics, DtoH device->host) instead of R-5's "DtoH marks the
+ *    host range defined".  Requires an unsharded context. */
 typedef struct {
   uint64_t host_base, host_size;
   uint64_t shard_base, shard_size;
@@ -167,6 +174,8 @@ typedef struct {
   int32_t reserved;
   void *v_buf, *a_buf, *workspace;
   uint64_t workspace_size;
+  void *dev_vbuf;           /* NEXT-1 device V-bit pool (or NULL)        */
+  uint64_t dev_vsize;
 } cg_config;
 
 typedef struct cg_ctx cg_ctx;
@@ -254,13 +263,33 @@ cg_status cg_registry_compact(cg_ctx *ctx, uint64_t before_seq);
 cg_status cg_check_copies(cg_ctx *ctx, const cg_copy_desc *d_descs, uint64_t n, cg_verdict *d_out,
                           void *stream);
 
-/* The DtoH shadow update (BASELINE north_star (3)):
+/* The DtoH shadow update (BASELINE north_star (3));
+ * with device V-bit tracking (cfg.dev_vbuf) this is cg_apply_copies:
  * for every descriptor with kind == CG_DTOH and verdict status == CG_OK, every
  * written host byte becomes defined (V := 0x00); other descriptors are ignored
  * (no mutation on error).  Asynchronous on stream.
  * Errors: as cg_check_copies. */
 cg_status cg_apply_dtoh(cg_ctx *ctx, const cg_copy_desc *d_descs, const cg_verdict *d_verdicts,
                         uint64_t n, void *stream);
+
+/* The a6 step generalised (NEXT-1): without device V-bit tracking identical
+ * to cg_apply_dtoh; with it, every descriptor whose verdict is OK moves its
+ * V-bits (HtoD: host -> device pool, DtoD: pool -> pool as if staged through a
+ * scratch buffer, DtoH: pool -> host).  Must follow the cg_check_copies call of
+ * the same descriptor array (it uses the device V offsets that check found);
+ * the batch must be hazard-free for propagation (cg_plan_batches with
+ * CG_PLAN_PROPAGATE).  With tracking it synchronises on stream at the end.
+ * Errors: as cg_apply_dtoh; CG_ERR_INVALID_VALUE if the preceding check was of
+ * other descriptors, or a self-overlapping 2D DtoD with unequal pitches moves
+ * more bytes than the 8 MiB staging area (its V-bits are then not moved). */
+cg_status cg_apply_copies(cg_ctx *ctx, const cg_copy_desc *d_descs, const cg_verdict *d_verdicts, uint64_t n,
+                          void *stream);
+
+/* Downloads the device V-bits of [addr, addr+len) (inside one allocation live
+ * now) to h_out (NEXT-1 state inspection).  Synchronous.  Errors:
+ * CG_ERR_NOT_INITIALIZED without tracking; CG_ERR_INVALID_VALUE if the range
+ * is not inside one live allocation. */
+cg_status cg_device_vbits(cg_ctx *ctx, uint64_t addr, uint64_t len, uint8_t *h_out);
 
 /* cg_check_copies followed by cg_apply_dtoh, fused: the shadow scan applies
  * every DtoH descriptor that fits one of its work groups as soon as its verdict
@@ -351,6 +380,14 @@ cg_status cg_leak_report(cg_ctx *ctx, cg_alloc_record *h_out, uint64_t cap, uint
  * batch to h_cuts (at most n entries; the last is n) and their number to
  * *n_cuts.  Errors: CG_ERR_INVALID_VALUE on NULL. */
 cg_status cg_plan_batches(const cg_copy_desc *h_descs, uint64_t n, uint64_t *h_cuts, uint64_t *n_cuts);
+
+/* As cg_plan_batches, for device V-bit tracking (NEXT-1): a batch is cut
+ * before any copy whose reads (HtoD host source, DtoD/DtoH device source)
+ * overlap an earlier write of the batch (DtoH host target, HtoD/DtoD device
+ * target) or whose writes overlap an earlier read or write -- so every copy's
+ * propagation in a batch can run in parallel (a DtoD overlapping itself is
+ * fine).  Conservative on 2D bounding intervals. */
+cg_status cg_plan_batches_propagate(const cg_copy_desc *h_descs, uint64_t n, uint64_t *h_cuts, uint64_t *n_cuts);
 
 /* Diagnostic text (SPEC format_text S:454-462): renders
  * one line pair per set flag of *v, in flag order, for a copy of the given

@@ -62,6 +62,7 @@ class cg_config(ctypes.Structure):
         ("device", ctypes.c_int32), ("reserved", ctypes.c_int32),
         ("v_buf", ctypes.c_void_p), ("a_buf", ctypes.c_void_p), ("workspace", ctypes.c_void_p),
         ("workspace_size", ctypes.c_uint64),
+        ("dev_vbuf", ctypes.c_void_p), ("dev_vsize", ctypes.c_uint64),
     ]
 
 
@@ -99,6 +100,9 @@ def _load() -> ctypes.CDLL:
         "cg_expand_copy1d": (I, [P, P, U64, P, P]),
         "cg_check_host": (I, [P, P, U32, U64, I, P, P, U64, P, P]),
         "cg_format_verdict": (U64, [P, U32, P, U64]),
+        "cg_apply_copies": (I, [P, P, P, U64, P]),
+        "cg_device_vbits": (I, [P, U64, U64, P]),
+        "cg_plan_batches_propagate": (I, [P, U64, P, P]),
         "cg_format_leak": (U64, [P, P, U64]),
         "cg_shard_plan": (I, [P, U64, U64, U64, U32, P, P, P]),
         "cg_batch_disjoint": (I, [P, U64, P]),
@@ -123,7 +127,7 @@ EXPORTED = ("cg_workspace_size", "cg_ctx_create", "cg_ctx_destroy", "cg_last_err
             "cg_plan_batches", "cg_kernel_launches", "cg_profile_begin", "cg_profile_end", "cg_check_apply",
             "cg_batch_disjoint", "cg_straddler_pack", "cg_straddler_finalize", "cg_compact_dirty", "cg_shard_plan",
             "cg_host_query_addressable", "cg_expand_copy1d", "cg_check_host", "cg_format_verdict",
-            "cg_format_leak")
+            "cg_format_leak", "cg_apply_copies", "cg_device_vbits", "cg_plan_batches_propagate")
 
 # ---- same-name thin wrappers (status codes returned unchanged) -------------
 cg_workspace_size = _lib.cg_workspace_size
@@ -148,6 +152,9 @@ cg_expand_copy1d = _lib.cg_expand_copy1d
 cg_check_host = _lib.cg_check_host
 cg_format_verdict = _lib.cg_format_verdict
 cg_format_leak = _lib.cg_format_leak
+cg_apply_copies = _lib.cg_apply_copies
+cg_device_vbits = _lib.cg_device_vbits
+cg_plan_batches_propagate = _lib.cg_plan_batches_propagate
 
 
 def format_verdict(v, kind: int) -> str:
@@ -180,12 +187,14 @@ STAGES = ("check_prep", "check_plan", "check_scan", "check_finalize", "apply_pre
           "leak_sweep")
 
 
-def plan_batches(descs: np.ndarray) -> np.ndarray:
-    """Batch end indices (cg_plan_batches) for a host DESC_DTYPE array."""
+def plan_batches(descs: np.ndarray, propagate: bool = False) -> np.ndarray:
+    """Batch end indices (cg_plan_batches, or cg_plan_batches_propagate for
+    device V-bit tracking) for a host DESC_DTYPE array."""
     d = np.ascontiguousarray(descs, dtype=DESC_DTYPE)
     cuts = np.zeros(max(len(d), 1), np.uint64)
     nc = ctypes.c_uint64(0)
-    st = _lib.cg_plan_batches(d.ctypes.data if len(d) else None, len(d), cuts.ctypes.data, ctypes.byref(nc))
+    fn = _lib.cg_plan_batches_propagate if propagate else _lib.cg_plan_batches
+    st = fn(d.ctypes.data if len(d) else None, len(d), cuts.ctypes.data, ctypes.byref(nc))
     if st:
         raise CgError(st, "cg_plan_batches")
     return cuts[: nc.value]
@@ -228,7 +237,7 @@ class Checker:
 
     def __init__(self, host_base: int, host_size: int, *, max_descs: int = 1 << 20,
                  max_allocs: int = 1 << 18, undef_is_error: bool = False, device: int = 0,
-                 shard_base: int = 0, shard_size: int = 0, host_staging: bool = False):
+                 shard_base: int = 0, shard_size: int = 0, host_staging: bool = False, dev_vsize: int = 0):
         import torch
         self.torch = torch
         self.device = device
@@ -238,6 +247,11 @@ class Checker:
                              shard_size=shard_size, max_descs=max_descs, max_allocs=max_allocs,
                              undef_is_error=int(undef_is_error), host_staging=int(host_staging),
                              device=device)
+        self.tracking = dev_vsize > 0
+        if self.tracking:   # NEXT-1 device V-bit pool
+            self.dev_v = torch.empty(dev_vsize, dtype=torch.uint8, device=dev)
+            self.cfg.dev_vbuf = self.dev_v.data_ptr()
+            self.cfg.dev_vsize = dev_vsize
         ws = _lib.cg_workspace_size(ctypes.byref(self.cfg))
         if ws == 0:
             raise CgError(CG_ERR_INVALID_VALUE, "invalid configuration")
@@ -314,6 +328,18 @@ class Checker:
         self._ok(_lib.cg_check_copies(self.ctx, d_descs.data_ptr(), n, d_out.data_ptr(), _stream_ptr(stream)),
                  "cg_check_copies")
         return d_out
+
+    def apply_copies(self, d_descs, d_verdicts, stream=None):
+        """cg_apply_copies: the a6 step (V-bit propagation with tracking)."""
+        n = d_descs.numel() // DESC_DTYPE.itemsize
+        self._ok(_lib.cg_apply_copies(self.ctx, d_descs.data_ptr(), d_verdicts.data_ptr(), n, _stream_ptr(stream)),
+                 "cg_apply_copies")
+
+    def device_vbits(self, addr: int, length: int) -> np.ndarray:
+        out = np.zeros(max(length, 1), np.uint8)
+        self.torch.cuda.synchronize(self.device)
+        self._ok(_lib.cg_device_vbits(self.ctx, addr, length, out.ctypes.data), "cg_device_vbits")
+        return out[:length]
 
     def check_apply(self, d_descs, d_out=None, stream=None):
         """cg_check_apply (fused check + DtoH apply; needs a disjoint batch)."""

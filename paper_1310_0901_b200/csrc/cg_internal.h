@@ -30,6 +30,7 @@ struct Table {
   const uint64_t* fseq;
   const uint64_t* pmax;
   const uint64_t* split;   // base[k * stride], k < nsplit (16-byte aligned, padded to even)
+  const uint64_t* pool;    // NEXT-1: device V-pool offset of each entry (nullptr without tracking)
   uint64_t n;
   uint32_t stride;   // splitter stride (every stride-th base is staged in smem)
   uint32_t nsplit;
@@ -47,6 +48,7 @@ struct Plan {
   void* meta;             // [n] ScanMeta (check plans only)
   uint32_t* counter;      // [0] group counter, [1] apply compaction count, [2] residual-list count
   uint32_t* resid;        // [n] fused check: DtoH descriptors left to the residual apply
+  uint64_t* dvoff;        // [2n] NEXT-1: device V offsets (dst, src) found by the last check
   uint64_t max_chunks;
   uint64_t t_min;
 };
@@ -73,6 +75,10 @@ constexpr int kScanTile = 2048;   // items per block of the prefix scan
 
 uint64_t scan_blocks(uint64_t n);
 int persistent_blocks(int which);   // 0: k_check_scan, 1: k_apply (per SM)
+size_t prop_meta_bytes();
+uint64_t stage_bytes();
+cudaError_t propagate(const Launch& L, const cg_copy_desc* d, const cg_verdict* v, uint64_t n, const ShadowView& sv,
+                      uint8_t* pool, const Plan& p, uint8_t* scratch, uint32_t* overflow, cudaStream_t s);
 size_t scan_meta_bytes();
 
 cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out,

@@ -191,7 +191,7 @@ struct __align__(16) ScanMeta {
 // (smem splitters, then a short global binary search), then walk left while
 // the prefix max of ends exceeds start (one step without address reuse).
 __device__ __forceinline__ bool table_lookup(const Table& t, const uint64_t* s_split, uint64_t start,
-                                             uint64_t seq, uint64_t& end_out) {
+                                             uint64_t seq, uint64_t& end_out, uint64_t& idx_out) {
   if (t.nsplit == 0 || s_split[0] > start) return false;
   uint32_t lo = 0, hi = t.nsplit;
   while (hi - lo > 1) {
@@ -209,6 +209,7 @@ __device__ __forceinline__ bool table_lookup(const Table& t, const uint64_t* s_s
     if (pm <= start) break;
     if (e > start && as < seq && seq < fs) {
       end_out = e;
+      idx_out = (uint64_t)j;
       return true;
     }
   }
@@ -236,7 +237,8 @@ __device__ __forceinline__ uint64_t check_host_units(const Norm& nm) {
 __global__ void __launch_bounds__(kThreads) k_check_prep(const cg_copy_desc* __restrict__ descs,
                                                          uint64_t n, Table t, cg_verdict* __restrict__ out,
                                                          uint64_t* __restrict__ weight,
-                                                         ScanMeta* __restrict__ meta) {
+                                                         ScanMeta* __restrict__ meta,
+                                                         uint64_t* __restrict__ dvoff) {
   extern __shared__ uint64_t s_split[];
   load_splitters(t, s_split);
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -246,26 +248,37 @@ __global__ void __launch_bounds__(kThreads) k_check_prep(const cg_copy_desc* __r
     uint32_t flags = nm.flags;
     uint64_t de = 0, df = 0, se = 0, sf = 0;
     const bool owner = !(d.reserved & CG_SHARD_NOT_OWNER);   // only the owner shard looks up the device side
+    uint64_t dv_dst = 0, dv_src = 0;   // NEXT-1: device V-bit offsets in the pool
     if (!(flags & CG_F_BAD_KIND) && owner) {
-      uint64_t end;
+      uint64_t end, j;
       if ((nm.kind == CG_HTOD || nm.kind == CG_DTOD) && nm.dok) {      // dst side first
-        if (!table_lookup(t, s_split, nm.ds, d.seq, end)) {
+        if (!table_lookup(t, s_split, nm.ds, d.seq, end, j)) {
           flags |= CG_F_DST_NOT_ALLOCATED;
-        } else if (end - nm.ds < nm.dspan) {
-          flags |= CG_F_DST_TOO_SMALL;
-          de = nm.dspan;
-          df = end - nm.ds;
+        } else {
+          if (end - nm.ds < nm.dspan) {
+            flags |= CG_F_DST_TOO_SMALL;
+            de = nm.dspan;
+            df = end - nm.ds;
+          }
+          if (t.pool) dv_dst = __ldg(t.pool + j) + (nm.ds - __ldg(t.base + j));
         }
       }
       if ((nm.kind == CG_DTOH || nm.kind == CG_DTOD) && nm.sok) {
-        if (!table_lookup(t, s_split, nm.ss, d.seq, end)) {
+        if (!table_lookup(t, s_split, nm.ss, d.seq, end, j)) {
           flags |= CG_F_SRC_NOT_ALLOCATED;
-        } else if (end - nm.ss < nm.sspan) {
-          flags |= CG_F_SRC_TOO_SMALL;
-          se = nm.sspan;
-          sf = end - nm.ss;
+        } else {
+          if (end - nm.ss < nm.sspan) {
+            flags |= CG_F_SRC_TOO_SMALL;
+            se = nm.sspan;
+            sf = end - nm.ss;
+          }
+          if (t.pool) dv_src = __ldg(t.pool + j) + (nm.ss - __ldg(t.base + j));
         }
       }
+    }
+    if (t.pool) {
+      dvoff[2 * i] = dv_dst;
+      dvoff[2 * i + 1] = dv_src;
     }
     cg_verdict v;
     v.first_unaddr = kNone;
@@ -1267,6 +1280,173 @@ __device__ __forceinline__ void fill_v(const ShadowView& sv, uint64_t q0, uint64
 }
 
 // ---------------------------------------------------------------------------
+// NEXT-1: V-bit propagation (SPEC copy_vbits S:81-89) through error-free copies
+// ---------------------------------------------------------------------------
+struct __align__(16) PropMeta {
+  uint64_t src, dst;        // offsets: host V (x - shard_base) or device V pool
+  uint64_t spitch, dpitch;
+  uint64_t W, info;         // info: nbytes | src in pool << 41 | dst in pool << 42
+};
+constexpr uint64_t kPropItemCost = 64;
+constexpr uint64_t kStageBytes = 8ull << 20;   // staging of self-overlapping 2D DtoD
+
+// Every descriptor with status OK and bytes to move gets a compacted PropMeta
+// and weight; a DtoD whose pool source and target ranges overlap goes to the
+// memmove list instead (processed by k_memmove, one CTA each).
+__global__ void __launch_bounds__(kThreads) k_prop_prep(const cg_copy_desc* __restrict__ descs,
+                                                        const cg_verdict* __restrict__ verd, uint64_t n,
+                                                        const uint64_t* __restrict__ dvoff, uint64_t sb,
+                                                        uint64_t* __restrict__ weight, PropMeta* __restrict__ pm,
+                                                        uint32_t* __restrict__ count, uint32_t* __restrict__ mm,
+                                                        uint32_t* __restrict__ mm_count) {
+  const int lane = threadIdx.x & 31;
+  for (uint64_t b0 = (uint64_t)blockIdx.x * blockDim.x; b0 < n; b0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = b0 + threadIdx.x;
+    bool ok = false;
+    PropMeta m;
+    uint64_t w = 0;
+    if (i < n && verd[i].status == CG_OK) {
+      const cg_copy_desc d = descs[i];
+      const Norm nm = normalize(d);
+      const uint64_t nb = d.width * d.height;   // status OK: no INVALID_RANGE, so no overflow
+      if (nb) {
+        m.W = d.width;
+        m.spitch = d.src_pitch;
+        m.dpitch = d.dst_pitch;
+        if (d.kind == CG_HTOD) {
+          m.src = nm.ss - sb;
+          m.dst = dvoff[2 * i];
+          m.info = nb | (1ull << 42);
+        } else if (d.kind == CG_DTOH) {
+          m.src = dvoff[2 * i + 1];
+          m.dst = nm.ds - sb;
+          m.info = nb | (1ull << 41);
+        } else {
+          m.src = dvoff[2 * i + 1];
+          m.dst = dvoff[2 * i];
+          m.info = nb | (3ull << 41);
+        }
+        ok = true;
+        if (d.kind == CG_DTOD && m.src < m.dst + nm.dspan && m.dst < m.src + nm.sspan) {
+          ok = false;   // overlaps itself: memmove list
+          mm[atomicAdd(mm_count, 1u)] = (uint32_t)i;
+        }
+        w = kPropItemCost + nb;
+      }
+    }
+    const uint32_t mask = __ballot_sync(kFull, ok);
+    if (mask) {
+      const int leader = __ffs(mask) - 1;
+      uint32_t base = 0;
+      if (lane == leader) base = atomicAdd(count, (uint32_t)__popc(mask));
+      base = __shfl_sync(kFull, base, leader);
+      if (ok) {
+        const uint32_t k = base + __popc(mask & ((1u << lane) - 1u));
+        weight[k] = w;
+        pm[k] = m;
+      }
+    }
+  }
+}
+
+// copy len bytes src -> dst with the whole warp (16-byte vectors when the two
+// are equally aligned, else bytes)
+__device__ __forceinline__ void warp_copy(uint8_t* dst, const uint8_t* src, uint64_t len) {
+  const int lane = threadIdx.x & 31;
+  if ((((uintptr_t)dst ^ (uintptr_t)src) & 15) == 0 && len >= 64) {
+    const uint64_t head = (16 - ((uintptr_t)dst & 15)) & 15;
+    const uint64_t body = (len - head) & ~15ull;
+    if ((uint64_t)lane < head) dst[lane] = src[lane];
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
+    uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+    for (uint64_t k = lane; k < body / 16; k += 32) d4[k] = s4[k];
+    for (uint64_t k = head + body + lane; k < len; k += 32) dst[k] = src[k];
+  } else {
+    for (uint64_t k = lane; k < len; k += 32) dst[k] = src[k];
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_propagate(const PropMeta* __restrict__ pm, uint64_t n,
+                                                        const uint64_t* __restrict__ P,
+                                                        const uint32_t* __restrict__ chunk_first, uint32_t* counter,
+                                                        uint64_t t_min, uint64_t max_chunks, uint8_t* V,
+                                                        uint8_t* pool, const uint32_t* __restrict__ n_dev) {
+  n = eff_n(n, n_dev);
+  const ChunkGeom geo = chunk_geom(P, n, t_min, max_chunks);
+  const int lane = threadIdx.x & 31;
+  uint32_t gnext = lane == 0 ? atomicAdd(counter, 1u) : 0;
+  while (true) {
+    const uint64_t g = __shfl_sync(kFull, gnext, 0);
+    if (g >= geo.nchunks) break;
+    if (lane == 0) gnext = atomicAdd(counter, 1u);
+    const uint64_t w0 = g * geo.T, w1 = umin64(w0 + geo.T, geo.total);
+    for (uint64_t d = chunk_first[g]; d < n; ++d) {
+      const uint64_t pd = P[d];
+      if (pd >= w1) break;
+      const uint64_t pd1 = P[d + 1];
+      uint64_t a = umax64(w0, pd) - pd, b = umin64(w1, pd1) - pd;
+      a = a > kPropItemCost ? a - kPropItemCost : 0;
+      b = b > kPropItemCost ? b - kPropItemCost : 0;
+      if (a >= b) continue;
+      const PropMeta m = pm[d];
+      uint8_t* sbase = ((m.info >> 41) & 1u) ? pool : V;
+      uint8_t* dbase = ((m.info >> 42) & 1u) ? pool : V;
+      uint64_t r = a / m.W, c = a - r * m.W, o = a;
+      while (o < b) {   // row segments (R-11); both sides advance by their own pitch
+        const uint64_t len = umin64(m.W - c, b - o);
+        warp_copy(dbase + m.dst + r * m.dpitch + c, sbase + m.src + r * m.spitch + c, len);
+        o += len;
+        ++r;
+        c = 0;
+      }
+    }
+  }
+}
+
+// self-overlapping DtoD, one CTA each: equal pitches shift every byte by the
+// same delta, so a directional block copy is exact memmove; unequal pitches
+// stage all logical bytes first (scratch of kStageBytes), else set *overflow
+__global__ void __launch_bounds__(kThreads) k_memmove(const cg_copy_desc* __restrict__ descs,
+                                                      const uint64_t* __restrict__ dvoff,
+                                                      const uint32_t* __restrict__ mm,
+                                                      const uint32_t* __restrict__ mm_count, uint8_t* pool,
+                                                      uint8_t* scratch, uint32_t* overflow) {
+  const uint32_t cnt = *mm_count;
+  for (uint32_t k = 0; k < cnt; ++k) {
+    const uint32_t i = mm[k];
+    const cg_copy_desc d = descs[i];
+    const uint64_t W = d.width, H = d.height, so = dvoff[2 * i + 1], dso = dvoff[2 * i];
+    // equal pitches: entry k on block k mod grid; unequal: block 0 (the scratch is shared)
+    if (d.src_pitch == d.dst_pitch ? k % gridDim.x != blockIdx.x : blockIdx.x != 0) continue;
+    if (d.src_pitch == d.dst_pitch) {
+      const bool fwd = dso < so;   // moving down: ascending addresses; up: descending
+      for (uint64_t rr = 0; rr < H; ++rr) {
+        const uint64_t r = fwd ? rr : H - 1 - rr;
+        for (uint64_t c0 = 0; c0 < W; c0 += blockDim.x) {
+          const uint64_t cb = fwd ? c0 : (W > c0 + blockDim.x ? W - c0 - blockDim.x : 0);
+          const uint64_t ce = fwd ? umin64(W, c0 + blockDim.x) : W - c0;
+          const uint64_t c = cb + threadIdx.x;
+          uint8_t x = 0;
+          if (c < ce) x = pool[so + r * d.src_pitch + c];
+          __syncthreads();
+          if (c < ce) pool[dso + r * d.dst_pitch + c] = x;
+          __syncthreads();
+        }
+      }
+    } else if (W * H <= kStageBytes) {
+      for (uint64_t o = threadIdx.x; o < W * H; o += blockDim.x)
+        scratch[o] = pool[so + (o / W) * d.src_pitch + o % W];
+      __syncthreads();
+      for (uint64_t o = threadIdx.x; o < W * H; o += blockDim.x)
+        pool[dso + (o / W) * d.dst_pitch + o % W] = scratch[o];
+      __syncthreads();
+    } else if (threadIdx.x == 0) {
+      atomicOr(overflow, 1u);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // plumbing: fresh shadow, marks, set_vbits check
 // ---------------------------------------------------------------------------
 __global__ void k_fill(uint4* __restrict__ p, uint64_t n16, uint32_t word) {
@@ -1471,7 +1651,8 @@ cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_
   const size_t smem = ((size_t)t.nsplit + 1) * sizeof(uint64_t);
   ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
   L.stage(CG_STAGE_CHECK_PREP, true, s);
-  k_check_prep<<<blocks_for(n, kThreads, L.num_sms * 4), kThreads, smem, s>>>(d, n, t, out, p.weight, meta);
+  k_check_prep<<<blocks_for(n, kThreads, L.num_sms * 4), kThreads, smem, s>>>(d, n, t, out, p.weight, meta,
+                                                                              p.dvoff);
   *L.counter += 1;
   L.stage(CG_STAGE_CHECK_PREP, false, s);
   L.stage(CG_STAGE_CHECK_PLAN, true, s);
@@ -1596,6 +1777,36 @@ cudaError_t expand_1d(const Launch& L, const cg_copy1d* in, uint64_t n, cg_copy_
   *L.counter += 1;
   return cudaGetLastError();
 }
+
+cudaError_t propagate(const Launch& L, const cg_copy_desc* d, const cg_verdict* v, uint64_t n, const ShadowView& sv,
+                      uint8_t* pool, const Plan& p, uint8_t* scratch, uint32_t* overflow, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  PropMeta* pm = reinterpret_cast<PropMeta*>(p.meta);   // 48 B per item: the meta area holds max_descs of them
+  uint32_t* cnt = p.counter + 1;
+  uint32_t* mm_count = p.counter + 3;
+  cudaMemsetAsync(p.weight, 0, n * sizeof(uint64_t), s);
+  cudaMemsetAsync(p.counter, 0, 4 * sizeof(uint32_t), s);
+  cudaMemsetAsync(overflow, 0, sizeof(uint32_t), s);
+  L.stage(CG_STAGE_APPLY_PREP, true, s);
+  k_prop_prep<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(d, v, n, p.dvoff, sv.sb, p.weight, pm,
+                                                                          cnt, p.resid, mm_count);
+  L.stage(CG_STAGE_APPLY_PREP, false, s);
+  L.stage(CG_STAGE_APPLY_PLAN, true, s);
+  cudaError_t e = plan(L, n, p, s, cnt);
+  if (e != cudaSuccess) return e;
+  L.stage(CG_STAGE_APPLY_PLAN, false, s);
+  L.stage(CG_STAGE_APPLY, true, s);
+  cudaMemsetAsync(p.counter, 0, sizeof(uint32_t), s);
+  k_propagate<<<L.persist_blocks, kThreads, 0, s>>>(pm, n, p.P, p.chunk_first, p.counter, p.t_min, p.max_chunks,
+                                                    sv.V, pool, cnt);
+  k_memmove<<<64, kThreads, 0, s>>>(d, p.dvoff, p.resid, mm_count, pool, scratch, overflow);
+  L.stage(CG_STAGE_APPLY, false, s);
+  *L.counter += 3;
+  return cudaGetLastError();
+}
+
+size_t prop_meta_bytes() { return sizeof(PropMeta); }
+uint64_t stage_bytes() { return kStageBytes; }
 
 int persistent_blocks(int which) {
   int b = 0;

@@ -29,11 +29,12 @@ constexpr uint64_t kMarkRun = 1u << 20;          // marks uploaded per run
 uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 struct Entry {
-  uint64_t base, end, aseq, fseq;
+  uint64_t base, end, aseq, fseq, pool;   // pool: NEXT-1 device V offset of the allocation
 };
 
 struct Layout {
-  uint64_t table, weight, P, bsum, chunk, meta, resid, marks, flags, leaks, desc_stage, verdict_stage, raw_stage,
+  uint64_t table, weight, P, bsum, chunk, meta, resid, dvoff, scratch, marks, flags, leaks, desc_stage,
+      verdict_stage, raw_stage,
       idx_stage, dirty_stage, total;
   uint64_t max_items, max_chunks;
 };
@@ -48,6 +49,9 @@ bool valid_config(const cg_config* c) {
   if (sb < c->host_base || sb + ss > c->host_base + c->host_size) return false;
   if (c->max_descs == 0 || c->max_descs > cgk::kMaxDescs) return false;
   if (c->max_allocs == 0 || c->max_allocs > (1ull << 32)) return false;
+  if (c->dev_vbuf && (c->dev_vsize == 0 || (c->shard_size && (c->shard_base != c->host_base ||
+                                                              c->shard_size != c->host_size))))
+    return false;   // NEXT-1 tracking needs a pool and an unsharded context
   return true;
 }
 
@@ -61,13 +65,15 @@ Layout layout_of(const cg_config* c) {
     off = align_up(off + bytes, kAlign);
     return o;
   };
-  L.table = take(5 * c->max_allocs * 8 + (4096 + 3) * 8);   // SoA + splitters
+  L.table = take(6 * c->max_allocs * 8 + (4096 + 3) * 8);   // SoA (+ pool offsets) + splitters
   L.weight = take(L.max_items * 8);
   L.P = take((L.max_items + 1) * 8);
   L.bsum = take((cgk::scan_blocks(L.max_items) + 1) * 8);
   L.chunk = take(L.max_chunks * 4);
-  L.meta = take(c->max_descs * cgk::scan_meta_bytes());
+  L.meta = take(c->max_descs * std::max(cgk::scan_meta_bytes(), cgk::prop_meta_bytes()));
   L.resid = take(c->max_descs * sizeof(uint32_t));
+  L.dvoff = c->dev_vbuf ? take(c->max_descs * 16) : 0;
+  L.scratch = c->dev_vbuf ? take(cgk::stage_bytes()) : 0;
   L.marks = take(std::min<uint64_t>(c->max_descs, kMarkRun) * sizeof(cg_mark));
   L.flags = take(256);
   L.leaks = take(c->max_allocs * sizeof(cg_alloc_record));
@@ -107,6 +113,9 @@ struct cg_ctx {
   std::map<uint64_t, uint64_t> live;        // base -> end of live allocations
   uint64_t last_seq = 0;
   bool dirty = true;
+  uint64_t pool_cursor = 0;                 // NEXT-1 bump allocator in dev_vbuf
+  const void* last_check = nullptr;         // descriptors of the last check (for cg_apply_copies)
+  uint64_t last_check_n = 0;
   // pinned staging
   uint64_t* h_table = nullptr;              // 5 * max_allocs
   cg_mark* h_marks = nullptr;               // kMarkRun
@@ -160,6 +169,7 @@ struct cg_ctx {
     p.meta = ws + lay.meta;
     p.counter = reinterpret_cast<uint32_t*>(ws + lay.flags + 128);
     p.resid = reinterpret_cast<uint32_t*>(ws + lay.resid);
+    p.dvoff = cfg.dev_vbuf ? reinterpret_cast<uint64_t*>(ws + lay.dvoff) : nullptr;
     p.max_chunks = lay.max_chunks;
     p.t_min = kChunkMin;
     return p;
@@ -174,7 +184,8 @@ struct cg_ctx {
     t.aseq = b + 2 * cap;
     t.fseq = b + 3 * cap;
     t.pmax = b + 4 * cap;
-    t.split = b + ((5 * cap + 1) & ~1ull);   // 16-byte aligned
+    t.pool = cfg.dev_vbuf ? b + 5 * cap : nullptr;
+    t.split = b + ((6 * cap + 1) & ~1ull);   // 16-byte aligned
     t.n = table.size();
     const uint64_t stride = split_stride(t.n);
     t.stride = (uint32_t)stride;
@@ -198,13 +209,14 @@ struct cg_ctx {
         h_table[3 * cap + i] = x.fseq;
         pm = std::max(pm, x.end);
         h_table[4 * cap + i] = pm;
+        h_table[5 * cap + i] = x.pool;
       }
       const uint64_t stride = split_stride(n), nsplit = (n + stride - 1) / stride;
-      const uint64_t so = (5 * cap + 1) & ~1ull;
+      const uint64_t so = (6 * cap + 1) & ~1ull;
       for (uint64_t k = 0; k < nsplit; ++k) h_table[so + k] = table[k * stride].base;
       h_table[so + nsplit] = UINT64_MAX;   // padding for the 16-byte loads
       uint64_t* dt = d(lay.table);
-      for (int k = 0; k < 5; ++k) {
+      for (int k = 0; k < 6; ++k) {
         e = cudaMemcpyAsync(dt + k * cap, h_table + k * cap, n * 8, cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) return cuda(e, "table upload");
       }
@@ -227,6 +239,9 @@ struct cg_ctx {
 };
 
 extern "C" {
+
+cg_status cg_apply_copies(cg_ctx* c, const cg_copy_desc* d_descs, const cg_verdict* d_verdicts, uint64_t n,
+                          void* stream);
 
 uint64_t cg_workspace_size(const cg_config* cfg) {
   if (!valid_config(cfg)) return 0;
@@ -266,7 +281,7 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
   c->prof.mark = &cg_ctx::mark_cb;
   c->prof.self = c;
   c->launch.prof = &c->prof;
-  if (cudaMallocHost(&c->h_table, 5 * cfg->max_allocs * 8 + (4096 + 3) * 8) != cudaSuccess ||
+  if (cudaMallocHost(&c->h_table, 6 * cfg->max_allocs * 8 + (4096 + 3) * 8) != cudaSuccess ||
       cudaMallocHost(&c->h_marks, std::min<uint64_t>(cfg->max_descs, kMarkRun) * sizeof(cg_mark)) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->staged, cudaEventDisableTiming) != cudaSuccess) {
     cg_ctx_destroy(c);
@@ -281,6 +296,7 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
     for (auto& ev : c->chunk_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   }
   e = cgk::fresh_shadow(c->launch, c->sv, 0);
+  if (e == cudaSuccess && cfg->dev_vbuf) e = cudaMemset(cfg->dev_vbuf, 0xFF, cfg->dev_vsize);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     cg_ctx_destroy(c);
@@ -509,7 +525,14 @@ cg_status cg_register_alloc(cg_ctx* c, uint64_t base, uint64_t size, uint64_t se
   if (it != c->live.begin() && std::prev(it)->second > base)
     return c->fail(CG_ERR_INVALID_VALUE, "register: overlaps a live allocation");
   if (c->table.size() >= c->cfg.max_allocs) return c->fail(CG_ERR_OUT_OF_MEMORY, "allocation table full");
-  Entry x{base, end, seq, cgk::kInf};
+  uint64_t pool = 0;
+  if (c->cfg.dev_vbuf) {   // NEXT-1: V-bits of the allocation, same alignment mod 256 as its base
+    pool = (c->pool_cursor + 255) / 256 * 256 + (base & 255);
+    if (pool + size > c->cfg.dev_vsize || pool + size < pool)
+      return c->fail(CG_ERR_OUT_OF_MEMORY, "device V-bit pool full");
+  }
+  Entry x{base, end, seq, cgk::kInf, pool};
+  if (c->cfg.dev_vbuf) c->pool_cursor = pool + size;
   auto pos = std::upper_bound(c->table.begin(), c->table.end(), base,
                               [](uint64_t b, const Entry& e) { return b < e.base; });
   c->table.insert(pos, x);
@@ -561,12 +584,15 @@ cg_status cg_check_copies(cg_ctx* c, const cg_copy_desc* d_descs, uint64_t n, cg
   if (st != CG_OK) return st;
   cudaError_t e =
       cgk::check_copies(c->launch, d_descs, n, d_out, c->dev_table(), c->sv, c->plan(), c->err_mask(), false, s);
+  c->last_check = d_descs;
+  c->last_check_n = n;
   return c->cuda(e, "check kernels");
 }
 
 cg_status cg_apply_dtoh(cg_ctx* c, const cg_copy_desc* d_descs, const cg_verdict* d_verdicts, uint64_t n,
                         void* stream) {
   if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (c->cfg.dev_vbuf) return cg_apply_copies(c, d_descs, d_verdicts, n, stream);   // NEXT-1: a6 moves V-bits
   if (n == 0) return CG_OK;
   if (!d_descs || !d_verdicts) return c->fail(CG_ERR_INVALID_VALUE, "null descriptor or verdict array");
   if (n > c->cfg.max_descs) return c->fail(CG_ERR_INVALID_VALUE, "n > max_descs");
@@ -574,6 +600,45 @@ cg_status cg_apply_dtoh(cg_ctx* c, const cg_copy_desc* d_descs, const cg_verdict
   cudaError_t e =
       cgk::apply_dtoh(c->launch, d_descs, d_verdicts, n, c->sv, c->plan(), false, static_cast<cudaStream_t>(stream));
   return c->cuda(e, "apply kernels");
+}
+
+cg_status cg_apply_copies(cg_ctx* c, const cg_copy_desc* d_descs, const cg_verdict* d_verdicts, uint64_t n,
+                          void* stream) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (!c->cfg.dev_vbuf) return cg_apply_dtoh(c, d_descs, d_verdicts, n, stream);
+  if (n == 0) return CG_OK;
+  if (!d_descs || !d_verdicts) return c->fail(CG_ERR_INVALID_VALUE, "null descriptor or verdict array");
+  if (d_descs != c->last_check || n != c->last_check_n)
+    return c->fail(CG_ERR_INVALID_VALUE, "cg_apply_copies must follow the check of the same descriptors");
+  DeviceGuard g(c->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint32_t* overflow = reinterpret_cast<uint32_t*>(c->ws + c->lay.flags + 224);
+  cudaError_t e = cgk::propagate(c->launch, d_descs, d_verdicts, n, c->sv, static_cast<uint8_t*>(c->cfg.dev_vbuf),
+                                 c->plan(), c->ws + c->lay.scratch, overflow, s);
+  uint32_t h_over = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h_over, overflow, sizeof h_over, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return c->cuda(e, "propagate");
+  if (h_over) return c->fail(CG_ERR_INVALID_VALUE, "self-overlapping 2D DtoD larger than the staging area");
+  return CG_OK;
+}
+
+cg_status cg_device_vbits(cg_ctx* c, uint64_t addr, uint64_t len, uint8_t* h_out) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (!c->cfg.dev_vbuf) return c->fail(CG_ERR_NOT_INITIALIZED, "no device V-bit tracking");
+  if (len && !h_out) return c->fail(CG_ERR_INVALID_VALUE, "null output");
+  auto it = c->live.upper_bound(addr);
+  if (it == c->live.begin()) return c->fail(CG_ERR_INVALID_VALUE, "not inside a live allocation");
+  --it;
+  if (addr >= it->second || len > it->second - addr) return c->fail(CG_ERR_INVALID_VALUE, "not inside a live allocation");
+  auto pos = std::lower_bound(c->table.begin(), c->table.end(), it->first,
+                              [](const Entry& e, uint64_t b) { return e.base < b; });
+  for (; pos != c->table.end() && pos->base == it->first && pos->fseq != cgk::kInf; ++pos) {
+  }
+  DeviceGuard g(c->cfg.device);
+  cudaError_t e = cudaMemcpy(h_out, static_cast<uint8_t*>(c->cfg.dev_vbuf) + pos->pool + (addr - pos->base), len,
+                             cudaMemcpyDeviceToHost);
+  return c->cuda(e, "device V download");
 }
 
 cg_status cg_check_apply(cg_ctx* c, const cg_copy_desc* d_descs, uint64_t n, cg_verdict* d_out, void* stream) {
@@ -586,9 +651,14 @@ cg_status cg_check_apply(cg_ctx* c, const cg_copy_desc* d_descs, uint64_t n, cg_
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cg_status st = c->sync_table(s);
   if (st != CG_OK) return st;
+  if (c->cfg.dev_vbuf) {   // NEXT-1 tracking: check, then propagate (not fused)
+    st = cg_check_copies(c, d_descs, n, d_out, stream);
+    return st != CG_OK ? st : cg_apply_copies(c, d_descs, d_out, n, stream);
+  }
   cudaError_t e =
       cgk::check_copies(c->launch, d_descs, n, d_out, c->dev_table(), c->sv, c->plan(), c->err_mask(), true, s);
   if (e == cudaSuccess) e = cgk::apply_dtoh(c->launch, d_descs, d_out, n, c->sv, c->plan(), true, s);
+  c->last_check = nullptr;
   return c->cuda(e, "check+apply kernels");
 }
 
@@ -815,6 +885,73 @@ cg_status cg_shard_plan(const cg_copy_desc* h_descs, uint64_t n, uint64_t host_b
     h_first[i] = first;
     h_last[i] = last;
   }
+  return CG_OK;
+}
+
+// folded [lo, hi) of one side (false on overflow or no bytes)
+static bool side_range(const cg_copy_desc& d, bool dst, uint64_t& lo, uint64_t& hi) {
+  const uint64_t base = dst ? d.dst : d.src, x = dst ? d.dst_x : d.src_x;
+  const uint64_t y = dst ? d.dst_y : d.src_y, pitch = dst ? d.dst_pitch : d.src_pitch;
+  if (d.width == 0 || d.height == 0) return false;
+  unsigned __int128 st = (unsigned __int128)base + (unsigned __int128)y * pitch + x;
+  unsigned __int128 sp = (unsigned __int128)(d.height - 1) * pitch + d.width;
+  if (st + sp > (unsigned __int128)UINT64_MAX) return false;
+  lo = (uint64_t)st;
+  hi = (uint64_t)(st + sp);
+  return true;
+}
+
+namespace {
+struct IvSet {   // disjoint merged intervals
+  std::map<uint64_t, uint64_t> m;
+  bool overlaps(uint64_t lo, uint64_t hi) const {
+    auto it = m.upper_bound(lo);
+    if (it != m.end() && it->first < hi) return true;
+    return it != m.begin() && std::prev(it)->second > lo;
+  }
+  void add(uint64_t lo, uint64_t hi) {
+    auto it = m.upper_bound(lo);
+    if (it != m.begin() && std::prev(it)->second >= lo) {
+      --it;
+      lo = it->first;
+      hi = std::max(hi, it->second);
+      it = m.erase(it);
+    }
+    while (it != m.end() && it->first <= hi) {
+      hi = std::max(hi, it->second);
+      it = m.erase(it);
+    }
+    m.emplace(lo, hi);
+  }
+};
+}  // namespace
+
+cg_status cg_plan_batches_propagate(const cg_copy_desc* h_descs, uint64_t n, uint64_t* h_cuts, uint64_t* n_cuts) {
+  if (!n_cuts || (n && (!h_descs || !h_cuts))) return CG_ERR_INVALID_VALUE;
+  IvSet hr, hw, dr, dw;   // host / device reads and writes of the open batch
+  uint64_t k = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const cg_copy_desc& d = h_descs[i];
+    if (d.kind < CG_HTOD || d.kind > CG_DTOD) continue;
+    uint64_t rlo, rhi, wlo, whi;
+    const bool r_ok = side_range(d, false, rlo, rhi), w_ok = side_range(d, true, wlo, whi);
+    IvSet& R = d.kind == CG_HTOD ? hr : dr;   // the source's address space
+    IvSet& W = d.kind == CG_DTOH ? hw : dw;   // the destination's
+    IvSet& Rw = d.kind == CG_HTOD ? hw : dw;  // writes in the source's space
+    IvSet& Wr = d.kind == CG_DTOH ? hr : dr;  // reads in the destination's space
+    const bool conflict = (r_ok && Rw.overlaps(rlo, rhi)) || (w_ok && (Wr.overlaps(wlo, whi) || W.overlaps(wlo, whi)));
+    if (conflict) {
+      h_cuts[k++] = i;
+      hr.m.clear();
+      hw.m.clear();
+      dr.m.clear();
+      dw.m.clear();
+    }
+    if (r_ok) R.add(rlo, rhi);
+    if (w_ok) W.add(wlo, whi);
+  }
+  if (n) h_cuts[k++] = n;
+  *n_cuts = k;
   return CG_OK;
 }
 

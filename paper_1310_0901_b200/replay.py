@@ -71,13 +71,17 @@ def replay_events(chk, events: np.ndarray, blob=None, stream=None, fuse: bool = 
             idx = np.flatnonzero(is_copy[i:j]) + i
             if len(idx):
                 descs = events_to_descs(events[idx])
-                cuts = [0] + [int(c) for c in __import__(__package__).plan_batches(descs)]
                 pkg = __import__(__package__)
+                tracking = getattr(chk, "tracking", False)
+                cuts = [0] + [int(c) for c in pkg.plan_batches(descs, propagate=tracking)]
                 for a, b in zip(cuts[:-1], cuts[1:]):
                     for s0 in range(a, b, chk.max_descs):
                         s1 = min(b, s0 + chk.max_descs)
                         dd = to_device_descs(descs[s0:s1], chk.device)
-                        if fuse and pkg.batch_disjoint(descs[s0:s1]):
+                        if tracking:    # NEXT-1: check, then move V-bits
+                            dv = chk.check_copies(dd, stream=stream)
+                            chk.apply_copies(dd, dv, stream=stream)
+                        elif fuse and pkg.batch_disjoint(descs[s0:s1]):
                             dv = chk.check_apply(dd, stream=stream)
                         else:
                             dv = chk.check_copies(dd, stream=stream)

@@ -38,7 +38,7 @@ def test_every_declared_symbol_is_exported(cg):
 
 
 def test_struct_sizes_match_header(cg):
-    assert ctypes.sizeof(cg.cg_config) == 96
+    assert ctypes.sizeof(cg.cg_config) == 112
     assert cg.DESC_DTYPE.itemsize == 96 and cg.VERDICT_DTYPE.itemsize == 64
     # the header states the same sizes in its comments
     src = open(HEADER).read()
@@ -176,3 +176,48 @@ def test_format_is_injective_on_fuzzed_verdicts(cg):
         if key in seen:
             assert seen[key] == ident
         seen[key] = ident
+
+
+def _sets(d):
+    """(space, lo, hi) reads and writes of one descriptor for propagation"""
+    def rng(p):
+        if d["width"] == 0 or d["height"] == 0:
+            return None
+        s = int(d[p]) + int(d[p + "_y"]) * int(d[p + "_pitch"]) + int(d[p + "_x"])
+        e = s + (int(d["height"]) - 1) * int(d[p + "_pitch"]) + int(d["width"])
+        return None if e > (1 << 64) - 1 else (s, e)
+    k = int(d["kind"])
+    if k not in (1, 2, 3):
+        return [], []
+    r, w = rng("src"), rng("dst")
+    rs = "h" if k == 1 else "d"
+    ws = "h" if k == 2 else "d"
+    return ([(rs,) + r] if r else []), ([(ws,) + w] if w else [])
+
+
+def _prop_ok(descs, a, b):
+    R, W = [], []
+    for i in range(a, b):
+        r, w = _sets(descs[i])
+        for x in r:
+            if any(x[0] == y[0] and x[1] < y[2] and y[1] < x[2] for y in W):
+                return False
+        for x in w:
+            if any(x[0] == y[0] and x[1] < y[2] and y[1] < x[2] for y in R + W):
+                return False
+        R += r
+        W += w
+    return True
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_plan_batches_propagate(cg, seed):
+    from paper_1310_0901_b200.replay import events_to_descs
+    tr = tg.random_tiny(seed + 20000)
+    descs = events_to_descs(tr.events[tr.events["op"] == tg.OP_COPY])
+    cuts = [0] + [int(c) for c in cg.plan_batches(descs, propagate=True)]
+    assert cuts[-1] == len(descs)
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        assert _prop_ok(descs, a, b)
+        if b < len(descs):
+            assert not _prop_ok(descs, a, b + 1)

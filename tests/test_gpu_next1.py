@@ -1,0 +1,102 @@
+"""NEXT-1 on the GPU: device V-bit tracking (SPEC copy_vbits) bit-exact against
+the oracle's tracking mode -- verdicts, statuses, leaks, host A/V and the
+device V-bits of every allocation live at the end."""
+import numpy as np
+import pytest
+
+import oracle
+import tracegen as tg
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cg():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_1310_0901_b200 import build
+    build.build()
+    import paper_1310_0901_b200 as m
+    return m
+
+
+def run_tracking(cg, tr, **kw):
+    o, ov, os_, oleaks = oracle.replay_trace(tr, track_device=True)
+    ev = tr.events
+    regs = ev[ev["op"] == tg.OP_REG]
+    pool = int(sum(int(x) + 256 for x in regs["width"])) + (1 << 20)
+    chk = cg.Checker(tr.host_base, tr.host_size, max_descs=max(tr.n_copies, 1024),
+                     max_allocs=max(len(regs), 1024), dev_vsize=pool, **kw)
+    gv, gs = cg.replay_events(chk, ev, tr.blob)
+    for f in ov.dtype.names:
+        bad = np.flatnonzero(gv[f] != ov[f])
+        assert len(bad) == 0, (f, bad[:5], gv[f][bad[:5]], ov[f][bad[:5]])
+    assert np.array_equal(gs, os_)
+    gl = chk.leak_report()
+    assert np.array_equal(gl["base"], oleaks["base"]) and np.array_equal(gl["size"], oleaks["size"])
+    A, V = chk.shadow()
+    assert np.array_equal(A, o.A) and np.array_equal(V, o.V)
+    for r in oleaks:
+        b, n = int(r["base"]), int(r["size"])
+        assert np.array_equal(chk.device_vbits(b, n), o.device_vbits(b, n)), hex(b)
+    chk.close()
+    return gv
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_random_tiny_tracking(cg, seed):
+    run_tracking(cg, tg.random_tiny(seed + 20000))
+
+
+def test_c2_scaled_tracking(cg):
+    run_tracking(cg, tg.c2_small(n_copies=20000, n_allocs=2000))
+
+
+def test_c4_scaled_tracking(cg):
+    run_tracking(cg, tg.c4_pitched(n_copies=600, n_bufs=2, rows=64, inject_frac=0.05))
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_round_trip(cg, seed):
+    """any host pattern, HtoD -> DtoD -> DtoH into a fresh range, comes back bit-exact."""
+    rng = np.random.default_rng(seed)
+    H0 = 1 << 20
+    tb = tg.TraceBuilder("rt", H0, 1 << 20)
+    n = int(rng.integers(1, 60000))
+    d0, d1 = tb.malloc(n + 200), tb.malloc(n + 200)
+    pat = rng.integers(0, 256, n, dtype=np.uint8)
+    pat[rng.random(n) < 0.6] = 0
+    tb.mark(H0, n, tg.DEFINED)
+    tb.setv(H0, pat.tobytes())
+    tb.mark(H0 + (1 << 19), n, tg.UNDEFINED)
+    a, b = int(rng.integers(0, 100)), int(rng.integers(0, 100))
+    tb.copy1d(tg.HTOD, d0 + a, H0, n)
+    tb.copy1d(tg.DTOD, d1 + b, d0 + a, n)
+    tb.copy1d(tg.DTOH, H0 + (1 << 19), d1 + b, n)
+    tr = tb.build()
+    run_tracking(cg, tr)
+    o = oracle.replay_trace(tr, track_device=True)[0]
+    assert np.array_equal(o.V[1 << 19:(1 << 19) + n], pat)
+
+
+@pytest.mark.parametrize("shape", ["1d", "2d_equal", "2d_unequal"])
+@pytest.mark.parametrize("shift", [-4100, -33, 7, 5000])
+def test_self_overlapping_dtod(cg, shape, shift):
+    """memmove semantics for a DtoD overlapping itself"""
+    rng = np.random.default_rng(abs(shift))
+    H0 = 1 << 20
+    tb = tg.TraceBuilder("mm", H0, 1 << 18)
+    d = tb.malloc(1 << 17)
+    pat = rng.integers(0, 256, 1 << 16, dtype=np.uint8)
+    tb.mark(H0, 1 << 16, tg.DEFINED)
+    tb.setv(H0, pat.tobytes())
+    tb.copy1d(tg.HTOD, d + 20000, H0, 1 << 16)
+    s0 = 30000
+    if shape == "1d":
+        tb.copy1d(tg.DTOD, d + s0 + shift, d + s0, 20000)
+    elif shape == "2d_equal":
+        tb.copy2d(tg.DTOD, 300, 40, d, 0, 0, 700, d, 0, 0, 700) if False else \
+            tb.copy2d(tg.DTOD, 300, 40, d + s0 + shift, 0, 0, 700, d + s0, 0, 0, 700)
+    else:
+        tb.copy2d(tg.DTOD, 300, 40, d + s0 + shift, 0, 0, 650, d + s0, 0, 0, 700)
+    run_tracking(cg, tb.build())
