@@ -40,16 +40,20 @@ METRIC = "shadow GB/s and copy-descriptors/s validated (1/2/4/8 B200, % of HBM p
 UNIT = "GB/s"
 
 
-def algorithmic_bytes(descs: np.ndarray, verdicts: np.ndarray | None):
+def algorithmic_bytes(descs: np.ndarray, verdicts: np.ndarray | None, track: bool = False):
     """Shadow bytes the method must move: HtoD 1 V-byte + 1/8
     A-byte per host byte; DtoH 1/8 A-byte per host byte for the check and 1
-    V-byte written per host byte by the apply when the verdict has no Error."""
+    V-byte written per host byte by the apply when the verdict has no Error.
+    With device V-bit tracking (NEXT-1) the apply instead reads and writes one
+    V-byte per byte of every error-free copy (HtoD, DtoD, DtoH)."""
     nb = descs["width"].astype(np.float64) * descs["height"].astype(np.float64)
     htod = descs["kind"] == 1
     dtoh = descs["kind"] == 2
     check = float(nb[htod].sum()) * 1.125 + float(nb[dtoh].sum()) * 0.125
-    ok = dtoh if verdicts is None else dtoh & (verdicts["status"] == 0)
-    apply = float(nb[ok].sum())
+    okv = np.ones(len(descs), bool) if verdicts is None else verdicts["status"] == 0
+    if track:
+        return check, 2.0 * float(nb[okv & (descs["kind"] >= 1) & (descs["kind"] <= 3)].sum())
+    apply = float(nb[dtoh & okv].sum())
     return check, apply
 
 
@@ -155,7 +159,7 @@ def make_workload(name: str, rank: int = 0, scale: float = 1.0):
     raise SystemExit(f"unknown config {name}")
 
 
-def setup_checker(cg, tr, device: int, host_staging: bool, rank: int = 0, world: int = 1):
+def setup_checker(cg, tr, device: int, host_staging: bool, rank: int = 0, world: int = 1, track: bool = False):
     """Replays the non-copy events (host marks, V-bytes, registry) and returns
     the checker and the copy descriptors (host array).  With world > 1 the
     context holds shard `rank` of the global window."""
@@ -169,8 +173,10 @@ def setup_checker(cg, tr, device: int, host_staging: bool, rank: int = 0, world:
                          max_descs=max(len(copies), 1024), max_allocs=max(nreg, 1024), device=device,
                          host_staging=host_staging)
     else:
+        regs = ev[ev["op"] == 3]
+        pool = int(regs["width"].astype(np.int64).sum()) + 256 * len(regs) + (1 << 20) if track else 0
         chk = cg.Checker(tr.host_base, tr.host_size, max_descs=max(len(copies), 1024),
-                         max_allocs=max(nreg, 1024), device=device, host_staging=host_staging)
+                         max_allocs=max(nreg, 1024), device=device, host_staging=host_staging, dev_vsize=pool)
     setup = ev[ev["op"] != 5]
     t0 = time.perf_counter()
     cg.replay_events(chk, setup, tr.blob)
@@ -201,7 +207,8 @@ def run_ours(args, rank, world, device):
 
     torch.cuda.set_device(device)
     tr = make_workload(args.config, rank, args.scale)
-    chk, descs, t_setup, nreg = setup_checker(cg, tr, device, host_staging=not args.no_e2e, rank=rank, world=world)
+    chk, descs, t_setup, nreg = setup_checker(cg, tr, device, host_staging=not args.no_e2e, rank=rank, world=world,
+                                              track=args.track)
     n = len(descs)
     stream = torch.cuda.current_stream()
     d_descs = cg.to_device_descs(descs, device)
@@ -212,7 +219,7 @@ def run_ours(args, rank, world, device):
 
     # the batch is one epoch; if no HtoD range overlaps a DtoH range the check
     # and the apply run fused (cg_check_apply), else as two calls
-    fused = cg.batch_disjoint(descs) and not args.unfused
+    fused = cg.batch_disjoint(descs) and not args.unfused and not args.track
 
     comm = None
     if world > 1:
@@ -223,7 +230,10 @@ def run_ours(args, rank, world, device):
         g_cnt = torch.zeros(1, dtype=torch.int32, device=device)
 
     def step():
-        if fused:
+        if args.track:      # NEXT-1: check, then V-bit propagation
+            chk.check_copies(d_descs, d_out, stream=stream)
+            chk.apply_copies(d_descs, d_out, stream=stream)
+        elif fused:
             chk.check_apply(d_descs, d_out, stream=stream)
         else:
             chk.check_copies(d_descs, d_out, stream=stream)
@@ -239,7 +249,7 @@ def run_ours(args, rank, world, device):
         step()
     torch.cuda.synchronize()
     verd = cg.verdicts_to_numpy(d_out)
-    check_b, apply_b = algorithmic_bytes(descs, verd)
+    check_b, apply_b = algorithmic_bytes(descs, verd, track=args.track)
     bytes_per_step = check_b + apply_b
 
     if world > 1:
@@ -344,7 +354,8 @@ def run_ours(args, rank, world, device):
                    "shadow_bytes_per_step": bytes_per_step, "check_bytes": check_b, "apply_bytes": apply_b,
                    "l2": "no flush: >= 8.5 GB of shadow streamed per step vs 126 MB L2",
                    "parallelism": f"host-range shards x{world}",
-                   "entry": "cg_check_apply (fused)" if fused else "cg_check_copies + cg_apply_dtoh"},
+                   "entry": ("cg_check_copies + cg_apply_copies (NEXT-1 V-bit propagation)" if args.track else
+                             "cg_check_apply (fused)" if fused else "cg_check_copies + cg_apply_dtoh")},
         "descriptors_per_s": world * n / (ms_step * 1e-3),
         "frac_of_hbm": value / (world * peak),
         "roofline": {"bound": "hbm", "kernel": "k_check_scan", "achieved": achieved, "peak": peak,
@@ -431,6 +442,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-registry-rate", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="check and apply as two calls")
+    ap.add_argument("--track", action="store_true", help="NEXT-1 device V-bit tracking (apply = propagation)")
     args = ap.parse_args()
     assert args.warmup >= 1
 

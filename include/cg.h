@@ -163,7 +163,8 @@ typedef struct {
  *    never reused; fresh = undefined) and cg_apply_copies moves V-bits
  *    through error-free copies (HtoD host->device, DtoD device->device with
  *    memmove semantics, DtoH device->host) instead of R-5's "DtoH marks the
- *    host range defined".  Requires an unsharded context. */
+ *    host range defined".  dev_vsize must be a multiple of 16.  Requires an
+ *    unsharded context. */
 typedef struct {
   uint64_t host_base, host_size;
   uint64_t shard_base, shard_size;

@@ -249,6 +249,7 @@ class Checker:
                              device=device)
         self.tracking = dev_vsize > 0
         if self.tracking:   # NEXT-1 device V-bit pool
+            dev_vsize = (dev_vsize + 15) // 16 * 16
             self.dev_v = torch.empty(dev_vsize, dtype=torch.uint8, device=dev)
             self.cfg.dev_vbuf = self.dev_v.data_ptr()
             self.cfg.dev_vsize = dev_vsize

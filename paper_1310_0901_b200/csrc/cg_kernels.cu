@@ -1349,21 +1349,45 @@ __global__ void __launch_bounds__(kThreads) k_prop_prep(const cg_copy_desc* __re
   }
 }
 
-// copy len bytes src -> dst with the whole warp (16-byte vectors when the two
-// are equally aligned, else bytes)
+// 16 bytes from an arbitrary address: the two aligned 16-byte vectors around
+// it, realigned with funnel shifts (both vectors start inside the source
+// range, and V / pool sizes are multiples of 16, so no read leaves its buffer)
+__device__ __forceinline__ uint4 load_unaligned16(const uint8_t* p) {
+  const uintptr_t a = (uintptr_t)p & ~(uintptr_t)15;
+  const uint32_t m = (uint32_t)((uintptr_t)p & 15);
+  const uint4 lo = *reinterpret_cast<const uint4*>(a);
+  if (m == 0) return lo;
+  const uint4 hi = *reinterpret_cast<const uint4*>(a + 16);
+  const uint32_t q = m >> 2, r = (m & 3) * 8;
+  const uint32_t w0 = q == 0 ? lo.x : q == 1 ? lo.y : q == 2 ? lo.z : lo.w;
+  const uint32_t w1 = q == 0 ? lo.y : q == 1 ? lo.z : q == 2 ? lo.w : hi.x;
+  const uint32_t w2 = q == 0 ? lo.z : q == 1 ? lo.w : q == 2 ? hi.x : hi.y;
+  const uint32_t w3 = q == 0 ? lo.w : q == 1 ? hi.x : q == 2 ? hi.y : hi.z;
+  const uint32_t w4 = q == 0 ? hi.x : q == 1 ? hi.y : q == 2 ? hi.z : hi.w;
+  return make_uint4(__funnelshift_r(w0, w1, r), __funnelshift_r(w1, w2, r), __funnelshift_r(w2, w3, r),
+                    __funnelshift_r(w3, w4, r));
+}
+
+// copy len bytes src -> dst with the whole warp: 16-byte stores to the aligned
+// body of dst (sources realigned when the two are not equally aligned), byte
+// copies for the unaligned head / tail
 __device__ __forceinline__ void warp_copy(uint8_t* dst, const uint8_t* src, uint64_t len) {
   const int lane = threadIdx.x & 31;
-  if ((((uintptr_t)dst ^ (uintptr_t)src) & 15) == 0 && len >= 64) {
-    const uint64_t head = (16 - ((uintptr_t)dst & 15)) & 15;
-    const uint64_t body = (len - head) & ~15ull;
-    if ((uint64_t)lane < head) dst[lane] = src[lane];
-    const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
-    uint4* d4 = reinterpret_cast<uint4*>(dst + head);
-    for (uint64_t k = lane; k < body / 16; k += 32) d4[k] = s4[k];
-    for (uint64_t k = head + body + lane; k < len; k += 32) dst[k] = src[k];
-  } else {
+  if (len < 64) {
     for (uint64_t k = lane; k < len; k += 32) dst[k] = src[k];
+    return;
   }
+  const uint64_t head = (16 - ((uintptr_t)dst & 15)) & 15;
+  const uint64_t body = (len - head) & ~15ull;
+  if ((uint64_t)lane < head) dst[lane] = src[lane];
+  uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+  if ((((uintptr_t)dst ^ (uintptr_t)src) & 15) == 0) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
+    for (uint64_t k = lane; k < body / 16; k += 32) d4[k] = s4[k];
+  } else {
+    for (uint64_t k = lane; k < body / 16; k += 32) d4[k] = load_unaligned16(src + head + 16 * k);
+  }
+  for (uint64_t k = head + body + lane; k < len; k += 32) dst[k] = src[k];
 }
 
 __global__ void __launch_bounds__(kThreads) k_propagate(const PropMeta* __restrict__ pm, uint64_t n,

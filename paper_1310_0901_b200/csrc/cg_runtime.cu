@@ -49,7 +49,7 @@ bool valid_config(const cg_config* c) {
   if (sb < c->host_base || sb + ss > c->host_base + c->host_size) return false;
   if (c->max_descs == 0 || c->max_descs > cgk::kMaxDescs) return false;
   if (c->max_allocs == 0 || c->max_allocs > (1ull << 32)) return false;
-  if (c->dev_vbuf && (c->dev_vsize == 0 || (c->shard_size && (c->shard_base != c->host_base ||
+  if (c->dev_vbuf && (c->dev_vsize == 0 || c->dev_vsize % 16 || (c->shard_size && (c->shard_base != c->host_base ||
                                                               c->shard_size != c->host_size))))
     return false;   // NEXT-1 tracking needs a pool and an unsharded context
   return true;
