@@ -72,6 +72,10 @@ def _load():
         lib.or_leaks.restype = U64; lib.or_leaks.argtypes = [P, P, U64]
         lib.or_replay.restype = U64; lib.or_replay.argtypes = [P, P, U64, P, P, P]
         lib.or_track_device.argtypes = [P, I]
+        lib.or_array_bytes.restype = U64; lib.or_array_bytes.argtypes = [U64, U64, U64, U64, U64]
+        lib.or_register_array.restype = I; lib.or_register_array.argtypes = [P, U64, U64, U64]
+        lib.or_free_array.restype = I; lib.or_free_array.argtypes = [P, U64, U64]
+        lib.or_array_leaks.restype = U64; lib.or_array_leaks.argtypes = [P, P, U64]
         lib.or_device_vbits.restype = I; lib.or_device_vbits.argtypes = [P, U64, U64, P]
         _lib = lib
     return _lib
@@ -136,6 +140,22 @@ class Oracle:
         if self.lib.or_device_vbits(self.st, addr, length, out.ctypes.data):
             return None
         return out[:length]
+
+    def array_bytes(self, width, height, depth, fmt, channels) -> int:
+        return self.lib.or_array_bytes(width, height, depth, fmt, channels)
+
+    def register_array(self, handle, total, seq) -> int:
+        return self.lib.or_register_array(self.st, handle, total, seq)
+
+    def free_array(self, handle, seq) -> int:
+        return self.lib.or_free_array(self.st, handle, seq)
+
+    def array_leaks(self) -> np.ndarray:
+        n = self.lib.or_array_leaks(self.st, None, 0)
+        out = np.zeros(n, ALLOC_DTYPE)
+        if n:
+            self.lib.or_array_leaks(self.st, out.ctypes.data, n)
+        return np.sort(out, order="base")
 
     def leaks(self) -> np.ndarray:
         n = self.lib.or_leaks(self.st, None, 0)

@@ -36,9 +36,10 @@
 #define OR_NONE UINT64_MAX
 
 /* event ops (tracegen/__init__.py) */
-enum { OR_MARK = 1, OR_SETV = 2, OR_REG = 3, OR_FREE = 4, OR_COPY = 5 };
-/* copy kinds: host->device, device->host, device->device */
-enum { OR_HTOD = 1, OR_DTOH = 2, OR_DTOD = 3 };
+enum { OR_MARK = 1, OR_SETV = 2, OR_REG = 3, OR_FREE = 4, OR_COPY = 5, OR_REGA = 6, OR_FREEA = 7 };
+/* copy kinds: host->device, device->host, device->device, and the
+ * device-array transfers HtoA / AtoH (NEXT-3: Fig. 2 caption P:88) */
+enum { OR_HTOD = 1, OR_DTOH = 2, OR_DTOD = 3, OR_HTOA = 4, OR_ATOH = 5 };
 /* host mark states (host_alloc / host_write / host_free) */
 enum { OR_NOACCESS = 0, OR_UNDEFINED = 1, OR_DEFINED = 2 };
 
@@ -76,6 +77,8 @@ typedef struct {
     uint8_t **dv;          /* NEXT-1: device V-bytes of live[i] (track mode), else NULL */
     uint64_t n_live, cap_live;
     int track;             /* NEXT-1: propagate V-bits through copies (SPEC copy_vbits) */
+    or_alloc *arr;         /* NEXT-3: unsorted list of live device arrays {handle, total_bytes, seq} */
+    uint64_t n_arr, cap_arr;
     uint64_t last_reg_seq;
     int undef_is_error;    /* CLI flag promotes HostUndefined */
 } or_state;
@@ -105,7 +108,7 @@ void or_track_device(or_state *st, int on) { st->track = on; }
 void or_destroy(or_state *st) {
     if (!st) return;
     for (uint64_t i = 0; i < st->n_live; i++) free(st->dv[i]);
-    free(st->A); free(st->V); free(st->live); free(st->dv); free(st);
+    free(st->A); free(st->V); free(st->live); free(st->dv); free(st->arr); free(st);
 }
 
 uint8_t *or_A(or_state *st) { return st->A; }
@@ -182,6 +185,57 @@ int or_register(or_state *st, uint64_t base, uint64_t size, uint64_t seq) {
     return 0;
 }
 
+/* ---------------------------------------------- NEXT-3 device arrays */
+/* SPEC ArrayDescriptor: total_bytes = width * max(height,1) *
+ * max(depth,1) * format_bytes * channels; formats u8,u16,u32,s8,s16,s32,f16,
+ * f32 (codes 0..7) are 1,2,4,1,2,4,2,4 bytes; channels in {1,2,4}; width >= 1.
+ * Returns 0 for an invalid descriptor. */
+uint64_t or_array_bytes(uint64_t width, uint64_t height, uint64_t depth, uint64_t format, uint64_t channels) {
+    static const uint64_t fb[8] = {1, 2, 4, 1, 2, 4, 2, 4};
+    if (width == 0 || format > 7 || (channels != 1 && channels != 2 && channels != 4)) return 0;
+    unsigned __int128 t = (unsigned __int128)width * (height ? height : 1);
+    t *= (depth ? depth : 1);
+    t *= fb[format] * channels;
+    return t > (unsigned __int128)UINT64_MAX ? 0 : (uint64_t)t;
+}
+
+/* register_array: DuplicateHandle (a live array has this handle),
+ * zero-extent descriptor or non-increasing seq -> 1, no mutation */
+int or_register_array(or_state *st, uint64_t handle, uint64_t total, uint64_t seq) {
+    if (seq <= st->last_reg_seq || total == 0) return 1;
+    for (uint64_t i = 0; i < st->n_arr; i++)
+        if (st->arr[i].base == handle) return 1;
+    if (st->n_arr == st->cap_arr) {
+        st->cap_arr = st->cap_arr ? 2 * st->cap_arr : 16;
+        st->arr = (or_alloc *)realloc(st->arr, st->cap_arr * sizeof(or_alloc));
+    }
+    st->arr[st->n_arr].base = handle;
+    st->arr[st->n_arr].size = total;
+    st->arr[st->n_arr].seq = seq;
+    st->n_arr++;
+    st->last_reg_seq = seq;
+    return 0;
+}
+
+/* unregister_array: UnknownHandle -> 1, no mutation */
+int or_free_array(or_state *st, uint64_t handle, uint64_t seq) {
+    if (seq <= st->last_reg_seq) return 1;
+    for (uint64_t i = 0; i < st->n_arr; i++) {
+        if (st->arr[i].base == handle) {
+            st->arr[i] = st->arr[st->n_arr - 1];
+            st->n_arr--;
+            st->last_reg_seq = seq;
+            return 0;
+        }
+    }
+    return 1;
+}
+
+uint64_t or_array_leaks(or_state *st, or_alloc *out, uint64_t cap) {
+    for (uint64_t i = 0; i < st->n_arr && i < cap; i++) out[i] = st->arr[i];
+    return st->n_arr;
+}
+
 /* ------------------------------------------------------------ O4 free */
 int or_free(or_state *st, uint64_t ptr, uint64_t seq) {
     if (seq <= st->last_reg_seq) return 1;
@@ -250,15 +304,72 @@ int or_device_vbits(const or_state *st, uint64_t x, uint64_t len, uint8_t *out) 
     return 1;
 }
 
+/* NEXT-3 check_array_transfer: the array side is (handle, byte
+ * offset) = (dst, dst_x) for HtoA and (src, src_x) for AtoH; the array holds
+ * the W*H logical bytes contiguously from the offset.  Unknown handle ->
+ * *_NOT_ALLOCATED; offset + W*H > total_bytes -> *_TOO_SMALL with expected =
+ * W*H and found = total_bytes - offset (0 past the end).  The host side is
+ * checked as for HtoD / DtoH (pitch rule on the host side only). */
+static void check_array_copy(or_state *st, const or_event *ev, or_verdict *v) {
+    const int htoa = ev->kind == OR_HTOA;
+    const uint64_t W = ev->width, H = ev->height;
+    const uint64_t handle = htoa ? ev->dst : ev->src, off = htoa ? ev->dst_x : ev->src_x;
+    const uint64_t hb = htoa ? ev->src : ev->dst, hx = htoa ? ev->src_x : ev->dst_x;
+    const uint64_t hy = htoa ? ev->src_y : ev->dst_y, hp = htoa ? ev->src_pitch : ev->dst_pitch;
+    if ((unsigned __int128)hp < (unsigned __int128)W + hx) v->flags |= F_BAD_PITCH;
+    uint64_t hs = 0, hspan = 0;
+    const int hok = side_range(hb, hx, hy, hp, W, H, &hs, &hspan);
+    const unsigned __int128 nb = (unsigned __int128)W * H;
+    const int nbytes_ok = nb <= ((unsigned __int128)1 << 38);
+    const int aok = (unsigned __int128)off + nb <= (unsigned __int128)UINT64_MAX;
+    if (!hok || !nbytes_ok || !aok) v->flags |= F_INVALID_RANGE;
+    if (aok && nbytes_ok) {
+        int found = 0;
+        for (uint64_t i = 0; i < st->n_arr; i++) {
+            if (st->arr[i].base != handle) continue;
+            found = 1;
+            const uint64_t total = st->arr[i].size;
+            if (off + (uint64_t)nb > total) {
+                v->flags |= htoa ? F_DST_TOO_SMALL : F_SRC_TOO_SMALL;
+                if (htoa) { v->dst_expected = (uint64_t)nb; v->dst_found = off < total ? total - off : 0; }
+                else      { v->src_expected = (uint64_t)nb; v->src_found = off < total ? total - off : 0; }
+            }
+        }
+        if (!found) v->flags |= htoa ? F_DST_NOT_ALLOCATED : F_SRC_NOT_ALLOCATED;
+    }
+    if (hok && nbytes_ok) {
+        for (uint64_t r = 0; r < H && W; r++)
+            for (uint64_t c = 0; c < W; c++) {
+                const uint64_t x = hs + r * hp + c, o = r * W + c;
+                if (!addressable(st, x)) {
+                    if (v->first_unaddr == OR_NONE) v->first_unaddr = o;
+                } else if (htoa && st->V[x - st->h0] != 0) {
+                    if (v->first_undef == OR_NONE) v->first_undef = o;
+                    v->undef_count++;
+                }
+            }
+    }
+    if (v->first_unaddr != OR_NONE) v->flags |= F_HOST_UNADDRESSABLE;
+    if (v->undef_count > 0 && v->first_unaddr == OR_NONE) v->flags |= F_HOST_UNDEFINED;
+    const uint32_t errors = v->flags & ~(st->undef_is_error ? 0u : F_HOST_UNDEFINED);
+    v->status = errors ? 1u : 0u;
+    /* AtoH with no Error: the host bytes become defined (R-5, also in NEXT-1
+     * mode: array V-bits are not tracked, R-30) */
+    if (!htoa && v->status == 0)
+        for (uint64_t r = 0; r < H && W; r++)
+            for (uint64_t c = 0; c < W; c++) st->V[hs + r * hp + c - st->h0] = 0x00;
+}
+
 void or_check_copy(or_state *st, const or_event *ev, or_verdict *v) {
     v->first_unaddr = OR_NONE; v->first_undef = OR_NONE; v->undef_count = 0;
     v->dst_expected = v->dst_found = v->src_expected = v->src_found = 0;
     v->flags = 0; v->status = 0;
     uint32_t kind = ev->kind;
     uint64_t W = ev->width, H = ev->height;
-    if (kind < OR_HTOD || kind > OR_DTOD) {
+    if (kind < OR_HTOD || kind > OR_ATOH) {
         v->flags = F_BAD_KIND; v->status = 1; return;
     }
+    if (kind == OR_HTOA || kind == OR_ATOH) { check_array_copy(st, ev, v); return; }
     /* (i) validation: pitch rule (pitch >= WidthInBytes + XInBytes) and ranges */
     if ((unsigned __int128)ev->dst_pitch < (unsigned __int128)W + ev->dst_x ||
         (unsigned __int128)ev->src_pitch < (unsigned __int128)W + ev->src_x)
@@ -359,6 +470,11 @@ uint64_t or_replay(or_state *st, const or_event *ev, uint64_t n, const uint8_t *
         case OR_SETV: s = (uint32_t)or_set_vbits(st, e->dst, e->width, blob + e->src); break;
         case OR_REG:  s = (uint32_t)or_register(st, e->dst, e->width, e->seq); break;
         case OR_FREE: s = (uint32_t)or_free(st, e->dst, e->seq); break;
+        case OR_REGA:
+            s = (uint32_t)or_register_array(st, e->dst, or_array_bytes(e->width, e->height, e->dst_x, e->dst_y,
+                                                                     e->dst_pitch), e->seq);
+            break;
+        case OR_FREEA: s = (uint32_t)or_free_array(st, e->dst, e->seq); break;
         case OR_COPY:
             or_check_copy(st, e, &out_v[nc]);
             s = out_v[nc].status;

@@ -25,6 +25,7 @@ class FlatModel:
         self.h0, self.s = h0, s
         self.track = track
         self.dv: dict = {}                        # base -> numpy V-bytes of the allocation (NEXT-1)
+        self.arrays: dict = {}                    # handle -> total bytes (NEXT-3)
         self.a = np.zeros(s, bool)               # unpacked A
         self.v = np.full(s, 0xFF, np.uint8)
         self.bases: list = []                     # sorted live bases
@@ -95,6 +96,77 @@ class FlatModel:
         self.last = seq
         return 0
 
+    @staticmethod
+    def array_bytes(w, h, d, fmt, ch):
+        if w == 0 or fmt > 7 or ch not in (1, 2, 4):
+            return 0
+        t = w * max(h, 1) * max(d, 1) * [1, 2, 4, 1, 2, 4, 2, 4][fmt] * ch
+        return t if t <= U64 else 0
+
+    def register_array(self, handle, total, seq):
+        if seq <= self.last or total == 0 or handle in self.arrays:
+            return 1
+        self.arrays[handle] = total
+        self.last = seq
+        return 0
+
+    def free_array(self, handle, seq):
+        if seq <= self.last or handle not in self.arrays:
+            return 1
+        del self.arrays[handle]
+        self.last = seq
+        return 0
+
+    def array_copy(self, e):
+        kind, w, h = int(e["kind"]), int(e["width"]), int(e["height"])
+        htoa = kind == 4
+        out = dict(first_unaddr=NONE, first_undef=NONE, undef_count=0, dst_expected=0,
+                   dst_found=0, src_expected=0, src_found=0, flags=0, status=0)
+        hs = "src" if htoa else "dst"
+        aside = "dst" if htoa else "src"
+        handle, off = int(e[aside]), int(e[aside + "_x"])
+        base, x, y, pitch = int(e[hs]), int(e[hs + "_x"]), int(e[hs + "_y"]), int(e[hs + "_pitch"])
+        if pitch < w + x:
+            out["flags"] |= FLAG["BAD_PITCH"]
+        start = base + y * pitch + x
+        span = 0 if (w == 0 or h == 0) else (h - 1) * pitch + w
+        nb = w * h
+        hok, nbok, aok = start + span <= U64, nb <= (1 << 38), off + nb <= U64
+        if not (hok and nbok and aok):
+            out["flags"] |= FLAG["INVALID_RANGE"]
+        P = "DST" if htoa else "SRC"
+        if aok and nbok:
+            if handle not in self.arrays:
+                out["flags"] |= FLAG[P + "_NA"]
+            elif off + nb > self.arrays[handle]:
+                out["flags"] |= FLAG[P + "_SMALL"]
+                tot = self.arrays[handle]
+                out[aside + "_expected"], out[aside + "_found"] = nb, (tot - off if off < tot else 0)
+        if hok and nbok and w and h:
+            xs = self._host_index(start, pitch, w, h)
+            inwin = np.array([(self.h0 <= xx < self.h0 + self.s) for xx in xs], bool)
+            idx = np.array([xx - self.h0 if iw else 0 for xx, iw in zip(xs, inwin)], np.int64)
+            addr = inwin & self.a[idx]
+            bad = np.flatnonzero(~addr)
+            if len(bad):
+                out["first_unaddr"] = int(bad[0])
+            if htoa:
+                und = addr & (self.v[idx] != 0)
+                u = np.flatnonzero(und)
+                out["undef_count"] = int(np.count_nonzero(und))
+                if len(u):
+                    out["first_undef"] = int(u[0])
+        if out["first_unaddr"] != NONE:
+            out["flags"] |= FLAG["HOST_UNADDR"]
+        if out["undef_count"] and out["first_unaddr"] == NONE:
+            out["flags"] |= FLAG["HOST_UNDEF"]
+        err = out["flags"] & ~(0 if self.uie else FLAG["HOST_UNDEF"])
+        out["status"] = 1 if err else 0
+        if not htoa and out["status"] == 0 and w and h:
+            xs = self._host_index(start, pitch, w, h)
+            self.v[np.array([xx - self.h0 for xx in xs], np.int64)] = 0
+        return out
+
     def leaks(self):
         return [(b, self.info[b][0], self.info[b][1]) for b in self.bases]
 
@@ -108,6 +180,8 @@ class FlatModel:
         kind, w, h = int(e["kind"]), int(e["width"]), int(e["height"])
         out = dict(first_unaddr=NONE, first_undef=NONE, undef_count=0, dst_expected=0,
                    dst_found=0, src_expected=0, src_found=0, flags=0, status=0)
+        if kind in (4, 5):
+            return self.array_copy(e)
         if kind not in (1, 2, 3):
             out["flags"] = FLAG["BAD_KIND"]; out["status"] = 1
             return out
@@ -199,4 +273,10 @@ class FlatModel:
                 v = self.copy(e)
                 verdicts.append(v)
                 status.append(v["status"])
+            elif op == 6:
+                tot = self.array_bytes(int(e["width"]), int(e["height"]), int(e["dst_x"]), int(e["dst_y"]),
+                                       int(e["dst_pitch"]))
+                status.append(self.register_array(int(e["dst"]), tot, int(e["seq"])))
+            elif op == 7:
+                status.append(self.free_array(int(e["dst"]), int(e["seq"])))
         return verdicts, status

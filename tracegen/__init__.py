@@ -41,8 +41,8 @@ from typing import Dict, List, Optional
 
 import numpy as np
 
-OP_MARK, OP_SETV, OP_REG, OP_FREE, OP_COPY = 1, 2, 3, 4, 5
-HTOD, DTOH, DTOD = 1, 2, 3
+OP_MARK, OP_SETV, OP_REG, OP_FREE, OP_COPY, OP_REGA, OP_FREEA = 1, 2, 3, 4, 5, 6, 7
+HTOD, DTOH, DTOD, HTOA, ATOH = 1, 2, 3, 4, 5
 NOACCESS, UNDEFINED, DEFINED = 0, 1, 2
 
 EVENT_DTYPE = np.dtype([
@@ -137,6 +137,25 @@ class TraceBuilder:
     def free(self, ptr: int) -> int:
         return self._row(OP_FREE, dst=ptr)
 
+    def register_array(self, handle: int, width: int, height: int = 0, depth: int = 0, fmt: int = 0,
+                       channels: int = 1) -> int:
+        """cuArrayCreate (Fig. 2 caption P:88; SPEC ArrayDescriptor S:125-128):
+        REGA with dst = handle, width/height, dst_x = depth, dst_y = format code,
+        dst_pitch = channels."""
+        return self._row(OP_REGA, dst=handle, width=width, height=height, dst_x=depth, dst_y=fmt,
+                         dst_pitch=channels)
+
+    def free_array(self, handle: int) -> int:
+        return self._row(OP_FREEA, dst=handle)
+
+    def copy_htoa(self, handle: int, offset: int, src: int, nbytes: int) -> int:
+        return self._row(OP_COPY, kind=HTOA, width=nbytes, height=1, dst=handle, dst_x=offset,
+                         src=src, src_pitch=nbytes)
+
+    def copy_atoh(self, dst: int, handle: int, offset: int, nbytes: int) -> int:
+        return self._row(OP_COPY, kind=ATOH, width=nbytes, height=1, dst=dst, dst_pitch=nbytes,
+                         src=handle, src_x=offset)
+
     def malloc(self, size: int) -> int:
         """Play the driver: bump allocate, then record REG."""
         base = self.heap_cursor
@@ -225,7 +244,7 @@ def listing2() -> Trace:
 # Random tiny traces (<=200 events in a 64 KiB window)
 # ---------------------------------------------------------------------------
 def random_tiny(seed: int, n_events: int = 200, window: int = 64 * KiB,
-                host_base: int = 0x40000) -> Trace:
+                host_base: int = 0x40000, arrays: bool = False) -> Trace:
     """Unaligned, overlapping, out-of-window, 2D, reuse-after-free: everything
     the method must handle, at sizes a brute-force checker finishes quickly."""
     rng = np.random.default_rng(seed)
@@ -260,8 +279,27 @@ def random_tiny(seed: int, n_events: int = 200, window: int = 64 * KiB,
         a = host_base + int(rng.integers(0, window // 2))
         l = int(rng.integers(window // 8, window // 2))
         tb.mark(a, min(l, host_base + window - a), int(rng.choice([UNDEFINED, DEFINED], p=[0.3, 0.7])))
+    handles: List[tuple] = []      # (handle, nominal bytes) of created arrays
     for _ in range(n_events - 4):
         u = rng.random()
+        if arrays and u < 0.22:         # NEXT-3: device arrays and their transfers
+            v = rng.random()
+            if v < 0.25 or not handles:
+                h = int(rng.choice([0x1000 + len(handles), int(rng.integers(1, 8))]))
+                w = int(rng.integers(0, 400)); fmt = int(rng.integers(0, 9)); ch = int(rng.choice([1, 2, 3, 4]))
+                tb.register_array(h, w, int(rng.integers(0, 3)), int(rng.integers(0, 2)), fmt, ch)
+                handles.append((h, max(w, 1) * 8))
+            elif v < 0.35:
+                tb.free_array(int(rng.choice([hh for hh, _ in handles] + [99])))
+            else:
+                h, cap = handles[int(rng.integers(len(handles)))]
+                off = int(rng.integers(0, cap + 16))
+                a, l = rand_host(cap + 64)
+                if rng.random() < 0.5:
+                    tb.copy_htoa(h, off, a, l)
+                else:
+                    tb.copy_atoh(a, h, off, l)
+            continue
         if u < 0.18:
             a, l = rand_host(6000)
             st = int(rng.integers(0, 3))
