@@ -57,8 +57,18 @@ enum {
   CG_ERR_NCCL = 6
 };
 
-/* ---- copy kinds: host/device, device/host, device/device ---- */
-enum { CG_HTOD = 1, CG_DTOH = 2, CG_DTOD = 3 };
+/* ---- copy kinds: host/device, device/host, device/device ----
+ * NEXT-3 ("CUDA arrays"): transfers
+ * between host memory and a registered device array.  The array side is
+ * (handle, byte offset): HTOA uses dst = handle, dst_x = offset; ATOH uses
+ * src = handle, src_x = offset; its y / pitch are ignored.  The host side is a
+ * pitched range like HTOD's source / DTOH's destination (pitch rule on the host
+ * side only).  The array must be live at desc.seq (else *_NOT_ALLOCATED) and
+ * offset + width*height <= its total bytes (else *_TOO_SMALL with expected =
+ * width*height, found = total - offset or 0; R-29).  Array contents
+ * carry no V-bits (R-30): an error-free ATOH makes its host range defined, an
+ * HTOA only reads the host shadow. */
+enum { CG_HTOD = 1, CG_DTOH = 2, CG_DTOD = 3, CG_HTOA = 4, CG_ATOH = 5 };
 
 /* ---- host mark states (SPEC S:355-358 host_alloc / host_write / host_free) ---- */
 enum { CG_NOACCESS = 0, CG_UNDEFINED = 1, CG_DEFINED = 2 };
@@ -75,7 +85,7 @@ enum {
   CG_F_HOST_UNDEFINED = 1u << 5,     /* P:81 undefined host data sent (Warning)      */
   CG_F_BAD_PITCH = 1u << 6,          /* R-12: pitch < WidthInBytes + XInBytes         */
   CG_F_INVALID_RANGE = 1u << 7,      /* an address range overflows 64 bits      */
-  CG_F_BAD_KIND = 1u << 8            /* R-16: kind not in {HTOD, DTOH, DTOD}          */
+  CG_F_BAD_KIND = 1u << 8            /* R-16: kind not in {HTOD, DTOH, DTOD, HTOA, ATOH} */
 };
 
 /* One cuMemcpy{HtoD,DtoH,DtoD,2D} call, with the raw CUDA_MEMCPY2D fields
@@ -96,7 +106,7 @@ enum {
 enum { CG_SHARD_NOT_OWNER = 1u << 0, CG_SHARD_RAW = 1u << 1 };
 
 typedef struct {
-  uint32_t kind;       /* CG_HTOD / CG_DTOH / CG_DTOD                  */
+  uint32_t kind;       /* CG_HTOD / CG_DTOH / CG_DTOD / CG_HTOA / CG_ATOH */
   uint32_t reserved;   /* shard mode bits (CG_SHARD_*), 0 on one GPU   */
   uint64_t seq;
   uint64_t width;      /* WidthInBytes                                 */
@@ -251,6 +261,33 @@ cg_status cg_free(cg_ctx *ctx, uint64_t ptr, uint64_t seq);
  * seq < before_seq).  Synchronous host operation. */
 cg_status cg_registry_compact(cg_ctx *ctx, uint64_t before_seq);
 
+/* NEXT-3: bytes of a CUDA array (SPEC register_array S:166-168):
+ * width * max(height,1) * max(depth,1) * format_bytes * channels, with
+ * format_bytes = {1,2,4,1,2,4,2,4}[format] (u8,u16,u32,i8,i16,i32,f16,f32) and
+ * channels in {1,2,4}.  0 for width 0, an unknown format / channel count or a
+ * product above 2^64-1. */
+uint64_t cg_array_bytes(uint64_t width, uint64_t height, uint64_t depth, uint32_t format, uint32_t channels);
+
+/* NEXT-3: registers a device array under its handle (cuArrayCreate /
+ * cuArray3DCreate).  Shares the seq order of cg_register_alloc /
+ * cg_free.  Errors (no mutation): CG_ERR_INVALID_VALUE for a zero extent
+ * (cg_array_bytes == 0), a handle that is already live
+ * (DuplicateHandle) or a non-increasing seq; CG_ERR_OUT_OF_MEMORY when the
+ * array table (live + tombstones, capacity max_allocs) is full. */
+cg_status cg_register_array(cg_ctx *ctx, uint64_t handle, uint64_t width, uint64_t height, uint64_t depth,
+                            uint32_t format, uint32_t channels, uint64_t seq);
+
+/* NEXT-3: frees the live array with this handle (cuArrayDestroy); it stays a
+ * tombstone with free_seq = seq (dropped by cg_registry_compact).  Errors (no
+ * mutation): CG_ERR_INVALID_VALUE = UnknownHandle or non-increasing seq. */
+cg_status cg_free_array(cg_ctx *ctx, uint64_t handle, uint64_t seq);
+
+/* NEXT-3: live arrays at the end of the program (the array half of the leak
+ * report): records {handle, total bytes, alloc_seq} in ascending
+ * handle order into the host array h_out (at most cap), *n_out = how many are
+ * live.  Synchronous host operation. */
+cg_status cg_array_report(cg_ctx *ctx, cg_alloc_record *h_out, uint64_t cap, uint64_t *n_out);
+
 /* The check for a batch of n descriptors:
  * validation, batched interval search in the allocation table as of each
  * desc.seq, host A/V shadow scan, verdicts.
@@ -266,8 +303,8 @@ cg_status cg_check_copies(cg_ctx *ctx, const cg_copy_desc *d_descs, uint64_t n, 
 
 /* The DtoH shadow update (BASELINE north_star (3));
  * with device V-bit tracking (cfg.dev_vbuf) this is cg_apply_copies:
- * for every descriptor with kind == CG_DTOH and verdict status == CG_OK, every
- * written host byte becomes defined (V := 0x00); other descriptors are ignored
+ * for every descriptor with kind == CG_DTOH or CG_ATOH and verdict status ==
+ * CG_OK, every written host byte becomes defined (V := 0x00); other descriptors are ignored
  * (no mutation on error).  Asynchronous on stream.
  * Errors: as cg_check_copies. */
 cg_status cg_apply_dtoh(cg_ctx *ctx, const cg_copy_desc *d_descs, const cg_verdict *d_verdicts,
@@ -276,7 +313,7 @@ cg_status cg_apply_dtoh(cg_ctx *ctx, const cg_copy_desc *d_descs, const cg_verdi
 /* The a6 step generalised (NEXT-1): without device V-bit tracking identical
  * to cg_apply_dtoh; with it, every descriptor whose verdict is OK moves its
  * V-bits (HtoD: host -> device pool, DtoD: pool -> pool as if staged through a
- * scratch buffer, DtoH: pool -> host).  Must follow the cg_check_copies call of
+ * scratch buffer, DtoH: pool -> host; AtoH: host defined, HtoA: nothing, R-30).  Must follow the cg_check_copies call of
  * the same descriptor array (it uses the device V offsets that check found);
  * the batch must be hazard-free for propagation (cg_plan_batches with
  * CG_PLAN_PROPAGATE).  With tracking it synchronises on stream at the end.

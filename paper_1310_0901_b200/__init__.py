@@ -24,7 +24,7 @@ LIB_PATH = os.path.join(_HERE, "libcgcheck.so")
 # ---- ABI constants (include/cg.h) -----------------------------------------
 CG_OK, CG_ERR_INVALID_VALUE, CG_ERR_INVALID_CONTEXT, CG_ERR_OUT_OF_MEMORY = 0, 1, 2, 3
 CG_ERR_NOT_INITIALIZED, CG_ERR_CUDA, CG_ERR_NCCL = 4, 5, 6
-CG_HTOD, CG_DTOH, CG_DTOD = 1, 2, 3
+CG_HTOD, CG_DTOH, CG_DTOD, CG_HTOA, CG_ATOH = 1, 2, 3, 4, 5
 CG_NOACCESS, CG_UNDEFINED, CG_DEFINED = 0, 1, 2
 CG_NONE = (1 << 64) - 1
 CG_F_DST_NOT_ALLOCATED = 1 << 0
@@ -112,6 +112,10 @@ def _load() -> ctypes.CDLL:
         "cg_kernel_launches": (U64, [P]),
         "cg_profile_begin": (I, [P]),
         "cg_profile_end": (I, [P, P, P]),
+        "cg_array_bytes": (U64, [U64, U64, U64, U32, U32]),
+        "cg_register_array": (I, [P, U64, U64, U64, U64, U32, U32, U64]),
+        "cg_free_array": (I, [P, U64, U64]),
+        "cg_array_report": (I, [P, P, U64, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -127,7 +131,8 @@ EXPORTED = ("cg_workspace_size", "cg_ctx_create", "cg_ctx_destroy", "cg_last_err
             "cg_plan_batches", "cg_kernel_launches", "cg_profile_begin", "cg_profile_end", "cg_check_apply",
             "cg_batch_disjoint", "cg_straddler_pack", "cg_straddler_finalize", "cg_compact_dirty", "cg_shard_plan",
             "cg_host_query_addressable", "cg_expand_copy1d", "cg_check_host", "cg_format_verdict",
-            "cg_format_leak", "cg_apply_copies", "cg_device_vbits", "cg_plan_batches_propagate")
+            "cg_format_leak", "cg_apply_copies", "cg_device_vbits", "cg_plan_batches_propagate",
+            "cg_array_bytes", "cg_register_array", "cg_free_array", "cg_array_report")
 
 # ---- same-name thin wrappers (status codes returned unchanged) -------------
 cg_workspace_size = _lib.cg_workspace_size
@@ -155,6 +160,10 @@ cg_format_leak = _lib.cg_format_leak
 cg_apply_copies = _lib.cg_apply_copies
 cg_device_vbits = _lib.cg_device_vbits
 cg_plan_batches_propagate = _lib.cg_plan_batches_propagate
+cg_array_bytes = _lib.cg_array_bytes
+cg_register_array = _lib.cg_register_array
+cg_free_array = _lib.cg_free_array
+cg_array_report = _lib.cg_array_report
 
 
 def format_verdict(v, kind: int) -> str:
@@ -318,6 +327,23 @@ class Checker:
 
     def free(self, ptr: int, seq: int) -> int:
         return _lib.cg_free(self.ctx, ptr, seq)
+
+    def register_array(self, handle: int, width: int, height: int, depth: int, fmt: int, channels: int,
+                       seq: int) -> int:
+        """NEXT-3 cg_register_array (cuArrayCreate / cuArray3DCreate)."""
+        return _lib.cg_register_array(self.ctx, handle, width, height, depth, fmt, channels, seq)
+
+    def free_array(self, handle: int, seq: int) -> int:
+        return _lib.cg_free_array(self.ctx, handle, seq)
+
+    def array_report(self) -> np.ndarray:
+        """live arrays {handle, total bytes, alloc_seq}, ascending handle"""
+        n = ctypes.c_uint64(0)
+        self._ok(_lib.cg_array_report(self.ctx, None, 0, ctypes.byref(n)), "cg_array_report")
+        out = np.zeros(n.value, ALLOC_RECORD_DTYPE)
+        if n.value:
+            self._ok(_lib.cg_array_report(self.ctx, out.ctypes.data, n.value, ctypes.byref(n)), "cg_array_report")
+        return out
 
     # ---- the hot path --------------------------------------------------------
     def check_copies(self, d_descs, d_out=None, stream=None):

@@ -32,6 +32,12 @@ struct Table {
   const uint64_t* split;   // base[k * stride], k < nsplit (16-byte aligned, padded to even)
   const uint64_t* pool;    // NEXT-1: device V-pool offset of each entry (nullptr without tracking)
   uint64_t n;
+  // NEXT-3 device arrays: sorted by (handle, alloc_seq)
+  const uint64_t* ahandle;
+  const uint64_t* atotal;
+  const uint64_t* aaseq;
+  const uint64_t* afseq;
+  uint64_t na;
   uint32_t stride;   // splitter stride (every stride-th base is staged in smem)
   uint32_t nsplit;
 };

@@ -136,33 +136,61 @@ __device__ __forceinline__ bool fold_side(uint64_t base, uint64_t x, uint64_t y,
 
 struct Norm {
   uint32_t kind, flags;
+  uint32_t skind;      // scan kind: CG_HTOD-like (V + A), CG_DTOH-like (A), CG_DTOD (no host side)
   bool dok, sok;
   uint64_t ds, dspan, ss, sspan;
   bool host;           // has a host side that is scanned
   uint64_t hstart, hpitch, W, nbytes;
+  bool aok;            // NEXT-3: the array side (handle, byte offset) of HtoA / AtoH
+  uint64_t ahandle, aoff;
 };
 
 __device__ __forceinline__ Norm normalize(const cg_copy_desc& d) {
   Norm n;
   n.kind = d.kind;
   n.flags = 0;
-  n.dok = n.sok = false;
+  n.skind = CG_DTOD;
+  n.dok = n.sok = n.aok = false;
   n.ds = n.dspan = n.ss = n.sspan = 0;
   n.host = false;
   n.hstart = n.hpitch = n.nbytes = 0;
+  n.ahandle = n.aoff = 0;
   n.W = d.width;
-  if (d.kind < CG_HTOD || d.kind > CG_DTOD) {
+  if (d.kind < CG_HTOD || d.kind > CG_ATOH) {
     n.flags = CG_F_BAD_KIND;
     return n;
   }
   const uint64_t W = d.width, H = d.height;
+  const bool bytes_ok = __umul64hi(W, H) == 0 && W * H <= kMaxCopyBytes;
+  if (d.kind >= CG_HTOA) {   // NEXT-3 array transfer: pitch rule and fold on the host side only
+    const bool htoa = d.kind == CG_HTOA;
+    const uint64_t hx = htoa ? d.src_x : d.dst_x, hp = htoa ? d.src_pitch : d.dst_pitch;
+    if (W + hx < W || hp < W + hx) n.flags |= CG_F_BAD_PITCH;
+    uint64_t hs = 0, hspan = 0;
+    const bool hok = htoa ? fold_side(d.src, d.src_x, d.src_y, d.src_pitch, W, H, hs, hspan)
+                          : fold_side(d.dst, d.dst_x, d.dst_y, d.dst_pitch, W, H, hs, hspan);
+    n.ahandle = htoa ? d.dst : d.src;
+    n.aoff = htoa ? d.dst_x : d.src_x;
+    n.aok = bytes_ok && n.aoff + W * H >= n.aoff;
+    if (!hok || !n.aok) n.flags |= CG_F_INVALID_RANGE;
+    n.skind = htoa ? CG_HTOD : CG_DTOH;
+    if (htoa) { n.sok = hok; n.ss = hs; n.sspan = hspan; }
+    else      { n.dok = hok; n.ds = hs; n.dspan = hspan; }
+    if (hok && bytes_ok) {
+      n.host = true;
+      n.hstart = hs;
+      n.hpitch = hp;
+      n.nbytes = W * H;
+    }
+    return n;
+  }
   // pitch rule: pitch >= WidthInBytes + XInBytes (evaluated without overflow)
   if (W + d.dst_x < W || d.dst_pitch < W + d.dst_x) n.flags |= CG_F_BAD_PITCH;
   if (W + d.src_x < W || d.src_pitch < W + d.src_x) n.flags |= CG_F_BAD_PITCH;
   n.dok = fold_side(d.dst, d.dst_x, d.dst_y, d.dst_pitch, W, H, n.ds, n.dspan);
   n.sok = fold_side(d.src, d.src_x, d.src_y, d.src_pitch, W, H, n.ss, n.sspan);
-  const bool bytes_ok = __umul64hi(W, H) == 0 && W * H <= kMaxCopyBytes;
   if (!n.dok || !n.sok || !bytes_ok) n.flags |= CG_F_INVALID_RANGE;
+  n.skind = d.kind;
   if (d.kind == CG_HTOD && n.sok && bytes_ok) {
     n.host = true;
     n.hstart = n.ss;
@@ -216,6 +244,22 @@ __device__ __forceinline__ bool table_lookup(const Table& t, const uint64_t* s_s
   return false;
 }
 
+// NEXT-3: the array with this handle alive at seq -> its total bytes
+__device__ __forceinline__ bool array_lookup(const Table& t, uint64_t handle, uint64_t seq, uint64_t& total) {
+  uint64_t lo = 0, hi = t.na;   // first entry with handle >= handle
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (__ldg(t.ahandle + mid) < handle) lo = mid + 1; else hi = mid;
+  }
+  for (uint64_t j = lo; j < t.na && __ldg(t.ahandle + j) == handle; ++j) {
+    if (__ldg(t.aaseq + j) < seq && seq < __ldg(t.afseq + j)) {
+      total = __ldg(t.atotal + j);
+      return true;
+    }
+  }
+  return false;
+}
+
 // the splitters (every stride-th base) are a contiguous array uploaded with the
 // table: coalesced 16-byte loads into shared memory
 __device__ __forceinline__ void load_splitters(const Table& t, uint64_t* s_split) {
@@ -231,7 +275,7 @@ constexpr uint64_t kItemCost = 256;
 
 __device__ __forceinline__ uint64_t check_host_units(const Norm& nm) {
   if (!nm.host) return 0;
-  return nm.kind == CG_HTOD ? nm.nbytes : (nm.nbytes + 7) >> 3;
+  return nm.skind == CG_HTOD ? nm.nbytes : (nm.nbytes + 7) >> 3;
 }
 
 __global__ void __launch_bounds__(kThreads) k_check_prep(const cg_copy_desc* __restrict__ descs,
@@ -249,7 +293,19 @@ __global__ void __launch_bounds__(kThreads) k_check_prep(const cg_copy_desc* __r
     uint64_t de = 0, df = 0, se = 0, sf = 0;
     const bool owner = !(d.reserved & CG_SHARD_NOT_OWNER);   // only the owner shard looks up the device side
     uint64_t dv_dst = 0, dv_src = 0;   // NEXT-1: device V-bit offsets in the pool
-    if (!(flags & CG_F_BAD_KIND) && owner) {
+    if (nm.kind >= CG_HTOA && owner) {  // NEXT-3: array side
+      const bool htoa = nm.kind == CG_HTOA;
+      uint64_t total;
+      if (nm.aok) {
+        if (!array_lookup(t, nm.ahandle, d.seq, total)) {
+          flags |= htoa ? CG_F_DST_NOT_ALLOCATED : CG_F_SRC_NOT_ALLOCATED;
+        } else if (nm.aoff + d.width * d.height > total) {
+          flags |= htoa ? CG_F_DST_TOO_SMALL : CG_F_SRC_TOO_SMALL;
+          const uint64_t ex = d.width * d.height, fd = nm.aoff < total ? total - nm.aoff : 0;
+          if (htoa) { de = ex; df = fd; } else { se = ex; sf = fd; }
+        }
+      }
+    } else if (!(flags & CG_F_BAD_KIND) && owner) {
       uint64_t end, j;
       if ((nm.kind == CG_HTOD || nm.kind == CG_DTOD) && nm.dok) {      // dst side first
         if (!table_lookup(t, s_split, nm.ds, d.seq, end, j)) {
@@ -298,7 +354,7 @@ __global__ void __launch_bounds__(kThreads) k_check_prep(const cg_copy_desc* __r
     m.W = nm.W;
     const bool contig = d.height == 1 || d.width == nm.hpitch;
     const bool raw = d.reserved & CG_SHARD_RAW;   // partial of a straddler: no finalisation here
-    m.info = nm.nbytes | ((uint64_t)(nm.kind & 3u) << 40) | ((uint64_t)nm.host << 42) | ((uint64_t)contig << 43) |
+    m.info = nm.nbytes | ((uint64_t)(nm.skind & 3u) << 40) | ((uint64_t)nm.host << 42) | ((uint64_t)contig << 43) |
              ((uint64_t)raw << 44) | ((uint64_t)flags << 48);
     meta[i] = m;
   }
@@ -1095,7 +1151,7 @@ __global__ void __launch_bounds__(kThreads) k_apply_prep(const cg_copy_desc* __r
     bool ok = false;
     ScanMeta m;
     uint64_t w = 0;
-    if (i < n && descs[i].kind == CG_DTOH && verd[i].status == CG_OK) {
+    if (i < n && (descs[i].kind == CG_DTOH || descs[i].kind == CG_ATOH) && verd[i].status == CG_OK) {
       const cg_copy_desc d = descs[i];
       const Norm nm = normalize(d);
       if (nm.host && nm.nbytes) {
@@ -1309,11 +1365,15 @@ __global__ void __launch_bounds__(kThreads) k_prop_prep(const cg_copy_desc* __re
       const cg_copy_desc d = descs[i];
       const Norm nm = normalize(d);
       const uint64_t nb = d.width * d.height;   // status OK: no INVALID_RANGE, so no overflow
-      if (nb) {
+      if (nb && d.kind != CG_HTOA) {   // array V-bits are not tracked (R-30): HtoA moves nothing
         m.W = d.width;
         m.spitch = d.src_pitch;
         m.dpitch = d.dst_pitch;
-        if (d.kind == CG_HTOD) {
+        if (d.kind == CG_ATOH) {       // ... and AtoH makes the host bytes defined (R-5)
+          m.src = 0;
+          m.dst = nm.ds - sb;
+          m.info = nb | (1ull << 43);
+        } else if (d.kind == CG_HTOD) {
           m.src = nm.ss - sb;
           m.dst = dvoff[2 * i];
           m.info = nb | (1ull << 42);
@@ -1415,10 +1475,13 @@ __global__ void __launch_bounds__(kThreads) k_propagate(const PropMeta* __restri
       const PropMeta m = pm[d];
       uint8_t* sbase = ((m.info >> 41) & 1u) ? pool : V;
       uint8_t* dbase = ((m.info >> 42) & 1u) ? pool : V;
+      const bool zero = (m.info >> 43) & 1u;
       uint64_t r = a / m.W, c = a - r * m.W, o = a;
       while (o < b) {   // row segments (R-11); both sides advance by their own pitch
         const uint64_t len = umin64(m.W - c, b - o);
-        warp_copy(dbase + m.dst + r * m.dpitch + c, sbase + m.src + r * m.spitch + c, len);
+        const uint64_t q = m.dst + r * m.dpitch + c;
+        if (zero) warp_store_zero(dbase, q, q + len);
+        else warp_copy(dbase + q, sbase + m.src + r * m.spitch + c, len);
         o += len;
         ++r;
         c = 0;

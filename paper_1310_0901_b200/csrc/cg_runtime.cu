@@ -32,8 +32,12 @@ struct Entry {
   uint64_t base, end, aseq, fseq, pool;   // pool: NEXT-1 device V offset of the allocation
 };
 
+struct ArrayEntry {   // NEXT-3 device array (SPEC register_array S:166-168)
+  uint64_t handle, total, aseq, fseq;
+};
+
 struct Layout {
-  uint64_t table, weight, P, bsum, chunk, meta, resid, dvoff, scratch, marks, flags, leaks, desc_stage,
+  uint64_t table, arrays, weight, P, bsum, chunk, meta, resid, dvoff, scratch, marks, flags, leaks, desc_stage,
       verdict_stage, raw_stage,
       idx_stage, dirty_stage, total;
   uint64_t max_items, max_chunks;
@@ -66,6 +70,7 @@ Layout layout_of(const cg_config* c) {
     return o;
   };
   L.table = take(6 * c->max_allocs * 8 + (4096 + 3) * 8);   // SoA (+ pool offsets) + splitters
+  L.arrays = take(4 * c->max_allocs * 8);                    // NEXT-3 array table (SoA)
   L.weight = take(L.max_items * 8);
   L.P = take((L.max_items + 1) * 8);
   L.bsum = take((cgk::scan_blocks(L.max_items) + 1) * 8);
@@ -111,13 +116,15 @@ struct cg_ctx {
   // registry host mirror
   std::vector<Entry> table;                 // sorted by (base, aseq)
   std::map<uint64_t, uint64_t> live;        // base -> end of live allocations
+  std::vector<ArrayEntry> arrays;           // NEXT-3: sorted by (handle, aseq)
+  std::map<uint64_t, uint64_t> live_arrays; // handle -> total bytes
   uint64_t last_seq = 0;
   bool dirty = true;
   uint64_t pool_cursor = 0;                 // NEXT-1 bump allocator in dev_vbuf
   const void* last_check = nullptr;         // descriptors of the last check (for cg_apply_copies)
   uint64_t last_check_n = 0;
   // pinned staging
-  uint64_t* h_table = nullptr;              // 5 * max_allocs
+  uint64_t* h_table = nullptr;              // 10 * max_allocs + splitters
   cg_mark* h_marks = nullptr;               // kMarkRun
   cudaEvent_t staged = nullptr;
   cudaStream_t copy_stream = nullptr;        // host -> device uploads of cg_check_host
@@ -187,6 +194,12 @@ struct cg_ctx {
     t.pool = cfg.dev_vbuf ? b + 5 * cap : nullptr;
     t.split = b + ((6 * cap + 1) & ~1ull);   // 16-byte aligned
     t.n = table.size();
+    uint64_t* a = d(lay.arrays);
+    t.ahandle = a;
+    t.atotal = a + cap;
+    t.aaseq = a + 2 * cap;
+    t.afseq = a + 3 * cap;
+    t.na = arrays.size();
     const uint64_t stride = split_stride(t.n);
     t.stride = (uint32_t)stride;
     t.nsplit = (uint32_t)((t.n + stride - 1) / stride);
@@ -222,8 +235,26 @@ struct cg_ctx {
       }
       e = cudaMemcpyAsync(dt + so, h_table + so, (nsplit + 1) * 8, cudaMemcpyHostToDevice, s);
       if (e != cudaSuccess) return cuda(e, "splitter upload");
-      cudaEventRecord(staged, s);
     }
+    if (const uint64_t na = arrays.size()) {
+      uint64_t* ha = h_table + ((6 * cap + 1) & ~1ull) + 4096 + 3;
+      if (!n) {
+        cudaError_t e = cudaEventSynchronize(staged);
+        if (e != cudaSuccess) return cuda(e, "cudaEventSynchronize");
+      }
+      for (uint64_t i = 0; i < na; ++i) {
+        ha[i] = arrays[i].handle;
+        ha[cap + i] = arrays[i].total;
+        ha[2 * cap + i] = arrays[i].aseq;
+        ha[3 * cap + i] = arrays[i].fseq;
+      }
+      uint64_t* da = d(lay.arrays);
+      for (int k = 0; k < 4; ++k) {
+        cudaError_t e = cudaMemcpyAsync(da + k * cap, ha + k * cap, na * 8, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return cuda(e, "array table upload");
+      }
+    }
+    if (n || !arrays.empty()) cudaEventRecord(staged, s);
     dirty = false;
     return CG_OK;
   }
@@ -281,7 +312,7 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
   c->prof.mark = &cg_ctx::mark_cb;
   c->prof.self = c;
   c->launch.prof = &c->prof;
-  if (cudaMallocHost(&c->h_table, 6 * cfg->max_allocs * 8 + (4096 + 3) * 8) != cudaSuccess ||
+  if (cudaMallocHost(&c->h_table, 10 * cfg->max_allocs * 8 + (4096 + 5) * 8) != cudaSuccess ||
       cudaMallocHost(&c->h_marks, std::min<uint64_t>(cfg->max_descs, kMarkRun) * sizeof(cg_mark)) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->staged, cudaEventDisableTiming) != cudaSuccess) {
     cg_ctx_destroy(c);
@@ -329,7 +360,8 @@ const char* cg_last_error(const cg_ctx* c) { return c ? c->err.c_str() : "null c
 uint64_t cg_kernel_launches(const cg_ctx* c) { return c ? c->launches : 0; }
 
 static const char* direction(uint32_t kind) {
-  return kind == CG_HTOD ? "host->device" : kind == CG_DTOH ? "device->host" : "device->device";
+  return kind == CG_HTOD ? "host->device" : kind == CG_DTOH ? "device->host" : kind == CG_HTOA ? "host->array"
+         : kind == CG_ATOH ? "array->host" : "device->device";
 }
 
 uint64_t cg_format_verdict(const cg_verdict* v, uint32_t kind, char* buf, uint64_t cap) {
@@ -341,16 +373,17 @@ uint64_t cg_format_verdict(const cg_verdict* v, uint32_t kind, char* buf, uint64
   };
   if (!v) return 0;
   const char* dir = direction(kind);
+  const char* mem = kind == CG_HTOA || kind == CG_ATOH ? "device array" : "device memory";
   const unsigned long long de = v->dst_expected, df = v->dst_found, se = v->src_expected, sf = v->src_found;
   const unsigned long long fu = v->first_unaddr, fd = v->first_undef, uc = v->undef_count;
-  if (v->flags & CG_F_DST_NOT_ALLOCATED) add("Error: Destination device memory of %s copy is not allocated.\n", dir);
+  if (v->flags & CG_F_DST_NOT_ALLOCATED) add("Error: Destination %s of %s copy is not allocated.\n", mem, dir);
   if (v->flags & CG_F_DST_TOO_SMALL)
-    add("Error: Allocated device memory too small for %s copy.\nExpected %llu allocated bytes but only found %llu.\n",
-        dir, de, df);
-  if (v->flags & CG_F_SRC_NOT_ALLOCATED) add("Error: Source device memory of %s copy is not allocated.\n", dir);
+    add("Error: Allocated %s too small for %s copy.\nExpected %llu allocated bytes but only found %llu.\n",
+        mem, dir, de, df);
+  if (v->flags & CG_F_SRC_NOT_ALLOCATED) add("Error: Source %s of %s copy is not allocated.\n", mem, dir);
   if (v->flags & CG_F_SRC_TOO_SMALL)
-    add("Error: Allocated device memory too small for %s copy.\nExpected %llu allocated bytes but only found %llu.\n",
-        dir, se, sf);
+    add("Error: Allocated %s too small for %s copy.\nExpected %llu allocated bytes but only found %llu.\n",
+        mem, dir, se, sf);
   if (v->flags & CG_F_HOST_UNADDRESSABLE)
     add("Error: Host memory of %s copy is not addressable (first unaddressable byte at offset %llu).\n", dir, fu);
   if (v->flags & CG_F_HOST_UNDEFINED)
@@ -569,6 +602,69 @@ cg_status cg_registry_compact(cg_ctx* c, uint64_t before_seq) {
     c->table.erase(it, c->table.end());
     c->dirty = true;
   }
+  auto ia = std::remove_if(c->arrays.begin(), c->arrays.end(),
+                           [&](const ArrayEntry& e) { return e.fseq != cgk::kInf && e.fseq <= before_seq; });
+  if (ia != c->arrays.end()) {
+    c->arrays.erase(ia, c->arrays.end());
+    c->dirty = true;
+  }
+  return CG_OK;
+}
+
+uint64_t cg_array_bytes(uint64_t width, uint64_t height, uint64_t depth, uint32_t format, uint32_t channels) {
+  static const uint64_t fb[8] = {1, 2, 4, 1, 2, 4, 2, 4};
+  if (width == 0 || format > 7 || (channels != 1 && channels != 2 && channels != 4)) return 0;
+  unsigned __int128 t = (unsigned __int128)width * (height ? height : 1) * (depth ? depth : 1);
+  t *= fb[format] * channels;
+  return t > (unsigned __int128)UINT64_MAX ? 0 : (uint64_t)t;
+}
+
+cg_status cg_register_array(cg_ctx* c, uint64_t handle, uint64_t width, uint64_t height, uint64_t depth,
+                            uint32_t format, uint32_t channels, uint64_t seq) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  const uint64_t total = cg_array_bytes(width, height, depth, format, channels);
+  if (total == 0) return c->fail(CG_ERR_INVALID_VALUE, "register_array: zero extent or bad descriptor");
+  if (seq <= c->last_seq) return c->fail(CG_ERR_INVALID_VALUE, "register_array: seq not increasing");
+  if (c->live_arrays.count(handle)) return c->fail(CG_ERR_INVALID_VALUE, "register_array: DuplicateHandle");
+  if (c->arrays.size() >= c->cfg.max_allocs) return c->fail(CG_ERR_OUT_OF_MEMORY, "array table full");
+  auto pos = std::upper_bound(c->arrays.begin(), c->arrays.end(), handle,
+                              [](uint64_t h, const ArrayEntry& e) { return h < e.handle; });
+  c->arrays.insert(pos, ArrayEntry{handle, total, seq, cgk::kInf});
+  c->live_arrays.emplace(handle, total);
+  c->last_seq = seq;
+  c->dirty = true;
+  return CG_OK;
+}
+
+cg_status cg_free_array(cg_ctx* c, uint64_t handle, uint64_t seq) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (seq <= c->last_seq) return c->fail(CG_ERR_INVALID_VALUE, "free_array: seq not increasing");
+  auto it = c->live_arrays.find(handle);
+  if (it == c->live_arrays.end()) return c->fail(CG_ERR_INVALID_VALUE, "free_array: UnknownHandle");
+  auto pos = std::lower_bound(c->arrays.begin(), c->arrays.end(), handle,
+                              [](const ArrayEntry& e, uint64_t h) { return e.handle < h; });
+  for (; pos != c->arrays.end() && pos->handle == handle; ++pos) {
+    if (pos->fseq == cgk::kInf) {
+      pos->fseq = seq;
+      break;
+    }
+  }
+  c->live_arrays.erase(it);
+  c->last_seq = seq;
+  c->dirty = true;
+  return CG_OK;
+}
+
+cg_status cg_array_report(cg_ctx* c, cg_alloc_record* h_out, uint64_t cap, uint64_t* n_out) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (!n_out || (cap && !h_out)) return c->fail(CG_ERR_INVALID_VALUE, "null output");
+  uint64_t k = 0;
+  for (const ArrayEntry& e : c->arrays) {
+    if (e.fseq != cgk::kInf) continue;
+    if (k < cap) h_out[k] = cg_alloc_record{e.handle, e.total, e.aseq};
+    ++k;
+  }
+  *n_out = k;
   return CG_OK;
 }
 
@@ -815,9 +911,13 @@ cg_status cg_leak_report(cg_ctx* c, cg_alloc_record* h_out, uint64_t cap, uint64
   return st;
 }
 
+// host -> device direction (HtoD, HtoA: the host side is read) vs device -> host
+static bool reads_host(uint32_t kind) { return kind == CG_HTOD || kind == CG_HTOA; }
+static bool writes_host(uint32_t kind) { return kind == CG_DTOH || kind == CG_ATOH; }
+
 static bool host_range(const cg_copy_desc& d, uint64_t& lo, uint64_t& hi) {
-  const bool htod = d.kind == CG_HTOD;
-  if (!htod && d.kind != CG_DTOH) return false;
+  const bool htod = reads_host(d.kind);
+  if (!htod && !writes_host(d.kind)) return false;
   const uint64_t base = htod ? d.src : d.dst, x = htod ? d.src_x : d.dst_x;
   const uint64_t y = htod ? d.src_y : d.dst_y, pitch = htod ? d.src_pitch : d.dst_pitch;
   if (d.width == 0 || d.height == 0) return false;
@@ -839,7 +939,7 @@ cg_status cg_batch_disjoint(const cg_copy_desc* h_descs, uint64_t n, int* disjoi
   v.reserve(n);
   for (uint64_t i = 0; i < n; ++i) {
     uint64_t lo, hi;
-    if (host_range(h_descs[i], lo, hi)) v.push_back({lo, hi, h_descs[i].kind == CG_HTOD});
+    if (host_range(h_descs[i], lo, hi)) v.push_back({lo, hi, reads_host(h_descs[i].kind)});
   }
   std::sort(v.begin(), v.end(), [](const Iv& a, const Iv& b) { return a.lo < b.lo; });
   uint64_t end_h = 0, end_d = 0;   // furthest end of HtoD / DtoH ranges starting earlier
@@ -932,13 +1032,15 @@ cg_status cg_plan_batches_propagate(const cg_copy_desc* h_descs, uint64_t n, uin
   uint64_t k = 0;
   for (uint64_t i = 0; i < n; ++i) {
     const cg_copy_desc& d = h_descs[i];
-    if (d.kind < CG_HTOD || d.kind > CG_DTOD) continue;
+    if (d.kind < CG_HTOD || d.kind > CG_ATOH) continue;
     uint64_t rlo, rhi, wlo, whi;
-    const bool r_ok = side_range(d, false, rlo, rhi), w_ok = side_range(d, true, wlo, whi);
-    IvSet& R = d.kind == CG_HTOD ? hr : dr;   // the source's address space
-    IvSet& W = d.kind == CG_DTOH ? hw : dw;   // the destination's
-    IvSet& Rw = d.kind == CG_HTOD ? hw : dw;  // writes in the source's space
-    IvSet& Wr = d.kind == CG_DTOH ? hr : dr;  // reads in the destination's space
+    // array sides carry no tracked V-bits (R-30): HtoA only reads the host, AtoH only writes it
+    const bool r_ok = d.kind != CG_ATOH && side_range(d, false, rlo, rhi);
+    const bool w_ok = d.kind != CG_HTOA && side_range(d, true, wlo, whi);
+    IvSet& R = reads_host(d.kind) ? hr : dr;   // the source's address space
+    IvSet& W = writes_host(d.kind) ? hw : dw;  // the destination's
+    IvSet& Rw = reads_host(d.kind) ? hw : dw;  // writes in the source's space
+    IvSet& Wr = writes_host(d.kind) ? hr : dr; // reads in the destination's space
     const bool conflict = (r_ok && Rw.overlaps(rlo, rhi)) || (w_ok && (Wr.overlaps(wlo, whi) || W.overlaps(wlo, whi)));
     if (conflict) {
       h_cuts[k++] = i;
@@ -962,7 +1064,7 @@ cg_status cg_plan_batches(const cg_copy_desc* h_descs, uint64_t n, uint64_t* h_c
   for (uint64_t i = 0; i < n; ++i) {
     uint64_t lo, hi;
     if (!host_range(h_descs[i], lo, hi)) continue;
-    if (h_descs[i].kind == CG_HTOD) {
+    if (reads_host(h_descs[i].kind)) {
       auto it = dtoh.upper_bound(lo);
       bool overlap = it != dtoh.end() && it->first < hi;
       if (!overlap && it != dtoh.begin()) overlap = std::prev(it)->second > lo;

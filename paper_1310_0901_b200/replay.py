@@ -5,7 +5,8 @@ or transfers data ... the respective Cudagrind wrapper will be called").
 ``events`` is any numpy structured array with the fields
 ``op, kind, seq, width, height, dst, dst_x, dst_y, dst_pitch, src, src_x,
 src_y, src_pitch`` (op: 1 host mark, 2 set V-bytes, 3 register, 4 free,
-5 copy).  Host shadow updates are applied in order; between two of them, all
+5 copy, 6 register array [dst = handle, width, height, dst_x = depth,
+dst_y = format, dst_pitch = channels], 7 free array [dst = handle]).  Host shadow updates are applied in order; between two of them, all
 registry events are submitted first (the table is lifetime-stamped, so a copy
 sees exactly the allocations live at its seq) and the copies are checked in the
 hazard-free batches cg_plan_batches cuts (check, then DtoH apply, per batch).
@@ -14,7 +15,8 @@ from __future__ import annotations
 
 import numpy as np
 
-OP_MARK, OP_SETV, OP_REG, OP_FREE, OP_COPY = 1, 2, 3, 4, 5
+OP_MARK, OP_SETV, OP_REG, OP_FREE, OP_COPY, OP_REGA, OP_FREEA = 1, 2, 3, 4, 5, 6, 7
+_REGISTRY = (OP_REG, OP_FREE, OP_COPY, OP_REGA, OP_FREEA)
 _DESC_FIELDS = ("kind", "seq", "width", "height", "dst", "dst_x", "dst_y", "dst_pitch",
                 "src", "src_x", "src_y", "src_pitch")
 
@@ -60,7 +62,7 @@ def replay_events(chk, events: np.ndarray, blob=None, stream=None, fuse: bool = 
             i += 1
         else:
             j = i
-            while j < n and ops[j] in (OP_REG, OP_FREE, OP_COPY):
+            while j < n and ops[j] in _REGISTRY:
                 j += 1
             for k in range(i, j):
                 if ops[k] == OP_REG:
@@ -68,6 +70,12 @@ def replay_events(chk, events: np.ndarray, blob=None, stream=None, fuse: bool = 
                                                    int(events["seq"][k]))
                 elif ops[k] == OP_FREE:
                     status[k] = chk.free(int(events["dst"][k]), int(events["seq"][k]))
+                elif ops[k] == OP_REGA:
+                    e = events[k]
+                    status[k] = chk.register_array(int(e["dst"]), int(e["width"]), int(e["height"]), int(e["dst_x"]),
+                                                   int(e["dst_y"]), int(e["dst_pitch"]), int(e["seq"]))
+                elif ops[k] == OP_FREEA:
+                    status[k] = chk.free_array(int(events["dst"][k]), int(events["seq"][k]))
             idx = np.flatnonzero(is_copy[i:j]) + i
             if len(idx):
                 descs = events_to_descs(events[idx])

@@ -55,12 +55,15 @@ def test_workspace_size_validation(cg):
     assert cg.cg_workspace_size(ctypes.byref(bad)) == 0
 
 
+READS_HOST, WRITES_HOST = (1, 4), (2, 5)   # HtoD / HtoA read the host, DtoH / AtoH write it
+
+
 def _hazard_free(descs, a, b):
-    """brute force: no HtoD in [a,b) overlaps the host bytes of an earlier DtoH in [a,b)"""
+    """brute force: no host read in [a,b) overlaps the host bytes of an earlier host write in [a,b)"""
     def host(d):
-        if d["kind"] not in (1, 2) or d["width"] == 0 or d["height"] == 0:
+        if d["kind"] not in (1, 2, 4, 5) or d["width"] == 0 or d["height"] == 0:
             return None
-        p = "src" if d["kind"] == 1 else "dst"
+        p = "src" if d["kind"] in READS_HOST else "dst"
         s = int(d[p]) + int(d[p + "_y"]) * int(d[p + "_pitch"]) + int(d[p + "_x"])
         e = s + (int(d["height"]) - 1) * int(d[p + "_pitch"]) + int(d["width"])
         return None if e > (1 << 64) - 1 else (s, e)
@@ -69,17 +72,18 @@ def _hazard_free(descs, a, b):
         r = host(descs[i])
         if r is None:
             continue
-        if descs[i]["kind"] == 2:
+        if descs[i]["kind"] in WRITES_HOST:
             seen.append(r)
         elif any(r[0] < e and s < r[1] for s, e in seen):
             return False
     return True
 
 
+@pytest.mark.parametrize("arrays", [False, True])
 @pytest.mark.parametrize("seed", range(30))
-def test_plan_batches_cuts_only_at_hazards(cg, seed):
+def test_plan_batches_cuts_only_at_hazards(cg, seed, arrays):
     from paper_1310_0901_b200.replay import events_to_descs
-    tr = tg.random_tiny(seed)
+    tr = tg.random_tiny(seed, arrays=arrays)
     ev = tr.events[tr.events["op"] == tg.OP_COPY]
     descs = events_to_descs(ev)
     cuts = [0] + [int(c) for c in cg.plan_batches(descs)]
@@ -108,24 +112,25 @@ def test_plan_batches_c2_single_epoch(cg):
 
 def _disjoint_brute(descs):
     def host(d):
-        if d["kind"] not in (1, 2) or d["width"] == 0 or d["height"] == 0:
+        if d["kind"] not in (1, 2, 4, 5) or d["width"] == 0 or d["height"] == 0:
             return None
-        p = "src" if d["kind"] == 1 else "dst"
+        p = "src" if d["kind"] in READS_HOST else "dst"
         s = int(d[p]) + int(d[p + "_y"]) * int(d[p + "_pitch"]) + int(d[p + "_x"])
         e = s + (int(d["height"]) - 1) * int(d[p + "_pitch"]) + int(d["width"])
-        return None if e > (1 << 64) - 1 else (s, e, int(d["kind"]))
+        return None if e > (1 << 64) - 1 else (s, e, int(d["kind"]) in READS_HOST)
     r = [h for h in map(host, descs) if h]
     for a in r:
         for b in r:
-            if a[2] == 1 and b[2] == 2 and a[0] < b[1] and b[0] < a[1]:
+            if a[2] and not b[2] and a[0] < b[1] and b[0] < a[1]:
                 return False
     return True
 
 
+@pytest.mark.parametrize("arrays", [False, True])
 @pytest.mark.parametrize("seed", range(40))
-def test_batch_disjoint_matches_brute_force(cg, seed):
+def test_batch_disjoint_matches_brute_force(cg, seed, arrays):
     from paper_1310_0901_b200.replay import events_to_descs
-    tr = tg.random_tiny(seed)
+    tr = tg.random_tiny(seed, arrays=arrays)
     descs = events_to_descs(tr.events[tr.events["op"] == tg.OP_COPY])
     rng = np.random.default_rng(seed)
     for _ in range(10):
@@ -187,11 +192,13 @@ def _sets(d):
         e = s + (int(d["height"]) - 1) * int(d[p + "_pitch"]) + int(d["width"])
         return None if e > (1 << 64) - 1 else (s, e)
     k = int(d["kind"])
-    if k not in (1, 2, 3):
+    if k not in (1, 2, 3, 4, 5):
         return [], []
-    r, w = rng("src"), rng("dst")
-    rs = "h" if k == 1 else "d"
-    ws = "h" if k == 2 else "d"
+    # array sides carry no tracked V-bits (R-30): HtoA reads the host only, AtoH writes it only
+    r = rng("src") if k != 5 else None
+    w = rng("dst") if k != 4 else None
+    rs = "h" if k in READS_HOST else "d"
+    ws = "h" if k in WRITES_HOST else "d"
     return ([(rs,) + r] if r else []), ([(ws,) + w] if w else [])
 
 
@@ -210,10 +217,11 @@ def _prop_ok(descs, a, b):
     return True
 
 
+@pytest.mark.parametrize("arrays", [False, True])
 @pytest.mark.parametrize("seed", range(30))
-def test_plan_batches_propagate(cg, seed):
+def test_plan_batches_propagate(cg, seed, arrays):
     from paper_1310_0901_b200.replay import events_to_descs
-    tr = tg.random_tiny(seed + 20000)
+    tr = tg.random_tiny(seed + 20000, arrays=arrays)
     descs = events_to_descs(tr.events[tr.events["op"] == tg.OP_COPY])
     cuts = [0] + [int(c) for c in cg.plan_batches(descs, propagate=True)]
     assert cuts[-1] == len(descs)
@@ -221,3 +229,29 @@ def test_plan_batches_propagate(cg, seed):
         assert _prop_ok(descs, a, b)
         if b < len(descs):
             assert not _prop_ok(descs, a, b + 1)
+
+
+def test_array_bytes_matches_oracle(cg):
+    """NEXT-3: cg_array_bytes against the oracle's or_array_bytes
+    over random descriptors, including zero extents, bad formats / channel
+    counts and products that overflow 64 bits."""
+    import oracle
+    rng = np.random.default_rng(3)
+    o = oracle.Oracle(1 << 20, 1 << 12)
+    for _ in range(5000):
+        big = rng.random() < 0.1
+        w, h, d = (int(rng.integers(0, 1 << 40 if big else 300)) for _ in range(3))
+        f, c = int(rng.integers(0, 10)), int(rng.integers(0, 6))
+        assert cg.cg_array_bytes(w, h, d, f, c) == o.array_bytes(w, h, d, f, c), (w, h, d, f, c)
+    assert cg.cg_array_bytes(64, 8, 0, 3, 2) == 1024
+
+
+def test_array_format_text(cg):
+    """NEXT-4 wording for array transfers: the noun and direction change, the Listing-5 shape stays."""
+    v = np.zeros(1, cg.VERDICT_DTYPE)[0]
+    v["first_unaddr"] = v["first_undef"] = cg.CG_NONE
+    v["dst_expected"], v["dst_found"], v["flags"], v["status"] = 100, 24, cg.CG_F_DST_TOO_SMALL, 1
+    assert cg.format_verdict(v, cg.CG_HTOA) == ("Error: Allocated device array too small for host->array copy.\n"
+                                                "Expected 100 allocated bytes but only found 24.\n")
+    v["flags"] = cg.CG_F_SRC_NOT_ALLOCATED
+    assert cg.format_verdict(v, cg.CG_ATOH) == "Error: Source device array of array->host copy is not allocated.\n"
