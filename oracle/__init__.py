@@ -43,6 +43,7 @@ F_HOST_UNDEFINED = 1 << 5
 F_BAD_PITCH = 1 << 6
 F_INVALID_RANGE = 1 << 7
 F_BAD_KIND = 1 << 8
+F_CONCURRENT = 1 << 9
 
 
 def build(force: bool = False) -> str:
@@ -77,6 +78,10 @@ def _load():
         lib.or_free_array.restype = I; lib.or_free_array.argtypes = [P, U64, U64]
         lib.or_array_leaks.restype = U64; lib.or_array_leaks.argtypes = [P, P, U64]
         lib.or_device_vbits.restype = I; lib.or_device_vbits.argtypes = [P, U64, U64, P]
+        lib.or_track_concurrency.argtypes = [P, I]
+        lib.or_sync.argtypes = [P, U32, U64]
+        lib.or_check_copy_mt.argtypes = [P, P, U32, P]
+        lib.or_replay_mt.restype = U64; lib.or_replay_mt.argtypes = [P, P, U64, P, P, P, P]
         _lib = lib
     return _lib
 
@@ -84,7 +89,8 @@ def _load():
 class Oracle:
     """Sequential replay state: host window shadow + device allocation list."""
 
-    def __init__(self, host_base: int, host_size: int, undef_is_error: bool = False, track_device: bool = False):
+    def __init__(self, host_base: int, host_size: int, undef_is_error: bool = False, track_device: bool = False,
+                 concurrency: bool = False):
         self.lib = _load()
         self.h0, self.s = host_base, host_size
         self.st = self.lib.or_create(host_base, host_size, int(undef_is_error))
@@ -92,6 +98,8 @@ class Oracle:
             raise MemoryError("oracle state allocation failed")
         if track_device:
             self.lib.or_track_device(self.st, 1)
+        if concurrency:
+            self.lib.or_track_concurrency(self.st, 1)
 
     def close(self):
         if self.st:
@@ -129,11 +137,15 @@ class Oracle:
     def free(self, ptr, seq) -> int:
         return self.lib.or_free(self.st, ptr, seq)
 
-    def check_copy(self, event: np.ndarray) -> np.ndarray:
+    def check_copy(self, event: np.ndarray, thread: int = 0) -> np.ndarray:
         ev = np.ascontiguousarray(np.asarray(event).reshape(1))
         out = np.zeros(1, VERDICT_DTYPE)
-        self.lib.or_check_copy(self.st, ev.ctypes.data, out.ctypes.data)
+        self.lib.or_check_copy_mt(self.st, ev.ctypes.data, thread, out.ctypes.data)
         return out[0]
+
+    def sync(self, thread: int, seq: int):
+        """NEXT-2 ctx_synchronize of a thread"""
+        self.lib.or_sync(self.st, thread, seq)
 
     def device_vbits(self, addr: int, length: int) -> Optional[np.ndarray]:
         out = np.zeros(max(length, 1), np.uint8)
@@ -164,21 +176,26 @@ class Oracle:
         return out
 
     # -- whole traces --------------------------------------------------------
-    def replay(self, events: np.ndarray, blob: Optional[np.ndarray] = None):
-        """Returns (verdicts per COPY event, status per event)."""
+    def replay(self, events: np.ndarray, blob: Optional[np.ndarray] = None, threads: Optional[np.ndarray] = None):
+        """Returns (verdicts per COPY event, status per event); threads[i] is
+        the thread of event i (NEXT-2; None = all thread 0)."""
         ev = np.ascontiguousarray(events)
         n = len(ev)
         ncopy = int(np.count_nonzero(ev["op"] == 5))
         out_v = np.zeros(max(ncopy, 1), VERDICT_DTYPE)
         out_s = np.zeros(max(n, 1), np.uint32)
         b = np.ascontiguousarray(blob if blob is not None and len(blob) else np.zeros(1, np.uint8))
-        self.lib.or_replay(self.st, ev.ctypes.data, n, b.ctypes.data, out_v.ctypes.data, out_s.ctypes.data)
+        t = None if threads is None else np.ascontiguousarray(threads, dtype=np.uint32)
+        assert t is None or len(t) == n
+        self.lib.or_replay_mt(self.st, ev.ctypes.data, n, b.ctypes.data, t.ctypes.data if t is not None else None,
+                              out_v.ctypes.data, out_s.ctypes.data)
         return out_v[:ncopy], out_s[:n]
 
 
-def replay_trace(trace, undef_is_error: bool = False, track_device: bool = False):
+def replay_trace(trace, undef_is_error: bool = False, track_device: bool = False, concurrency: bool = False):
     """Convenience: fresh oracle, replay the whole trace, return
-    (oracle, verdicts, statuses, leaks)."""
-    o = Oracle(trace.host_base, trace.host_size, undef_is_error, track_device)
-    v, s = o.replay(trace.events, trace.blob)
+    (oracle, verdicts, statuses, leaks).  With concurrency, the trace's
+    per-event threads (NEXT-2) are used."""
+    o = Oracle(trace.host_base, trace.host_size, undef_is_error, track_device, concurrency)
+    v, s = o.replay(trace.events, trace.blob, getattr(trace, "threads", None) if concurrency else None)
     return o, v, s, o.leaks()

@@ -18,6 +18,8 @@
  *   O5 copy check+apply -- P:80-82, S:157-165, S:192, S:63-80, S:222-248,
  *                          S:278-281; readings R-1..R-16
  *   O6 leak report      -- P:12 (abstract)
+ *   O7 concurrency      -- NEXT-2: P:83, S:216-219, S:258-266, S:285;
+ *                          DESIGN.md readings R-31..R-35
  *
  * State (SURVEY §8(c) "State"):
  *   host window [h0, h0+s);  A: one addressability bit per host byte, bit
@@ -36,7 +38,7 @@
 #define OR_NONE UINT64_MAX
 
 /* event ops (tracegen/__init__.py) */
-enum { OR_MARK = 1, OR_SETV = 2, OR_REG = 3, OR_FREE = 4, OR_COPY = 5, OR_REGA = 6, OR_FREEA = 7 };
+enum { OR_MARK = 1, OR_SETV = 2, OR_REG = 3, OR_FREE = 4, OR_COPY = 5, OR_REGA = 6, OR_FREEA = 7, OR_SYNC = 8 };
 /* copy kinds: host->device, device->host, device->device, and the
  * device-array transfers HtoA / AtoH (NEXT-3: Fig. 2 caption P:88) */
 enum { OR_HTOD = 1, OR_DTOH = 2, OR_DTOD = 3, OR_HTOA = 4, OR_ATOH = 5 };
@@ -53,6 +55,7 @@ enum { OR_NOACCESS = 0, OR_UNDEFINED = 1, OR_DEFINED = 2 };
 #define F_BAD_PITCH           (1u << 6)   /* R-12 */
 #define F_INVALID_RANGE       (1u << 7)
 #define F_BAD_KIND            (1u << 8)   /* R-16 */
+#define F_CONCURRENT          (1u << 9)   /* P:83, S:260 ConcurrentHazard (Warning) */
 
 typedef struct {
     uint32_t op, kind;
@@ -69,6 +72,11 @@ typedef struct {
 
 typedef struct { uint64_t base, size, seq; } or_alloc;
 
+/* NEXT-2 AccessStamp of one recorded access: the byte range it
+ * touched in one address space, its thread, seq and direction */
+typedef struct { uint64_t lo, hi, seq; uint32_t thread, is_write; } or_stamp;
+typedef struct { uint64_t seq; uint32_t thread; } or_sync_ev;
+
 typedef struct {
     uint64_t h0, s;
     uint8_t *A;            /* s/8 bytes */
@@ -81,6 +89,11 @@ typedef struct {
     uint64_t n_arr, cap_arr;
     uint64_t last_reg_seq;
     int undef_is_error;    /* CLI flag promotes HostUndefined */
+    int conc;              /* NEXT-2: run check_concurrent on every copy */
+    or_stamp *stamps[2];   /* NEXT-2: every recorded access, in order; [0] host, [1] device space */
+    uint64_t n_stamps[2], cap_stamps[2];
+    or_sync_ev *syncs;     /* NEXT-2: ctx_synchronize events */
+    uint64_t n_syncs, cap_syncs;
 } or_state;
 
 /* ---------------------------------------------------------------- state */
@@ -108,7 +121,8 @@ void or_track_device(or_state *st, int on) { st->track = on; }
 void or_destroy(or_state *st) {
     if (!st) return;
     for (uint64_t i = 0; i < st->n_live; i++) free(st->dv[i]);
-    free(st->A); free(st->V); free(st->live); free(st->dv); free(st->arr); free(st);
+    free(st->A); free(st->V); free(st->live); free(st->dv); free(st->arr);
+    free(st->stamps[0]); free(st->stamps[1]); free(st->syncs); free(st);
 }
 
 uint8_t *or_A(or_state *st) { return st->A; }
@@ -440,6 +454,105 @@ void or_check_copy(or_state *st, const or_event *ev, or_verdict *v) {
     }
 }
 
+/* ------------------------------------------------------ O7 concurrency */
+/* NEXT-2 ("certain concurrent accesses when several
+ * threads are used"; SPEC check_concurrent S:258-266 with the rule of S:285):
+ * a copy's access is a ConcurrentHazard (Warning) iff the most recent earlier
+ * recorded access overlapping it was made by a different thread, that thread
+ * has not synchronised since (ctx_synchronize), and one of the two
+ * writes.  Readings: R-31 one context per thread, so a sync by
+ * thread t marks exactly t's stamps; R-32 every side of a copy is an access
+ * (host read of HtoD/HtoA, device write of HtoD, device read of DtoH/DtoD,
+ * host write of DtoH/AtoH, device write of DtoD) -- array sides are not
+ * stamped; R-33 the access range is the side's folded [start, start+span)
+ * (2D: the bounding range), empty or overflowing sides make no access;
+ * R-34 every copy with a valid kind is checked, only copies without an Error
+ * (the ones the driver performs) record stamps, after their check; two
+ * stamps of the same copy count as one access that writes if either writes. */
+void or_track_concurrency(or_state *st, int on) { st->conc = on; }
+
+void or_sync(or_state *st, uint32_t thread, uint64_t seq) {
+    if (st->n_syncs == st->cap_syncs) {
+        st->cap_syncs = st->cap_syncs ? 2 * st->cap_syncs : 16;
+        st->syncs = (or_sync_ev *)realloc(st->syncs, st->cap_syncs * sizeof(or_sync_ev));
+    }
+    st->syncs[st->n_syncs].seq = seq;
+    st->syncs[st->n_syncs].thread = thread;
+    st->n_syncs++;
+}
+
+/* synced_after -- thread t synchronised after its stamp at seq a and before seq b */
+static int synced_between(const or_state *st, uint32_t t, uint64_t a, uint64_t b) {
+    for (uint64_t i = 0; i < st->n_syncs; i++)
+        if (st->syncs[i].thread == t && st->syncs[i].seq > a && st->syncs[i].seq < b) return 1;
+    return 0;
+}
+
+/* S:260 for one new access against every stamp recorded so far */
+static int conc_hazard(const or_state *st, int space, uint64_t lo, uint64_t hi, int is_write,
+                       uint32_t thread, uint64_t seq) {
+    int found = 0, prev_write = 0;
+    uint64_t best = 0;
+    uint32_t prev_thread = 0;
+    for (uint64_t i = 0; i < st->n_stamps[space]; i++) {
+        const or_stamp *p = &st->stamps[space][i];
+        if (p->lo >= hi || lo >= p->hi || p->seq >= seq) continue;   /* no overlap / not earlier */
+        if (!found || p->seq > best) {
+            found = 1; best = p->seq; prev_thread = p->thread; prev_write = (int)p->is_write;
+        } else if (p->seq == best) {
+            prev_write |= (int)p->is_write;                          /* R-34 */
+        }
+    }
+    if (!found) return 0;
+    return prev_thread != thread && !synced_between(st, prev_thread, best, seq) && (prev_write || is_write);
+}
+
+static void add_stamp(or_state *st, int space, uint64_t lo, uint64_t hi, int is_write, uint32_t thread,
+                      uint64_t seq) {
+    if (st->n_stamps[space] == st->cap_stamps[space]) {
+        st->cap_stamps[space] = st->cap_stamps[space] ? 2 * st->cap_stamps[space] : 64;
+        st->stamps[space] = (or_stamp *)realloc(st->stamps[space], st->cap_stamps[space] * sizeof(or_stamp));
+    }
+    or_stamp *p = &st->stamps[space][st->n_stamps[space]++];
+    p->lo = lo; p->hi = hi; p->seq = seq; p->thread = thread; p->is_write = (uint32_t)is_write;
+}
+
+/* R-32: the accesses of one copy: (space, side is dst, is_write) */
+static int copy_accesses(uint32_t kind, int space[2], int dst[2], int wr[2]) {
+    switch (kind) {
+    case OR_HTOD: space[0] = 0; dst[0] = 0; wr[0] = 0; space[1] = 1; dst[1] = 1; wr[1] = 1; return 2;
+    case OR_DTOH: space[0] = 1; dst[0] = 0; wr[0] = 0; space[1] = 0; dst[1] = 1; wr[1] = 1; return 2;
+    case OR_DTOD: space[0] = 1; dst[0] = 0; wr[0] = 0; space[1] = 1; dst[1] = 1; wr[1] = 1; return 2;
+    case OR_HTOA: space[0] = 0; dst[0] = 0; wr[0] = 0; return 1;
+    case OR_ATOH: space[0] = 0; dst[0] = 1; wr[0] = 1; return 1;
+    default: return 0;
+    }
+}
+
+static void check_concurrent(or_state *st, const or_event *e, uint32_t thread, or_verdict *v) {
+    int space[2], dst[2], wr[2];
+    uint64_t lo[2], hi[2];
+    int ok[2] = {0, 0};
+    const int na = copy_accesses(e->kind, space, dst, wr);
+    for (int k = 0; k < na; k++) {
+        uint64_t start, span;
+        const int fits = dst[k] ? side_range(e->dst, e->dst_x, e->dst_y, e->dst_pitch, e->width, e->height, &start, &span)
+                                : side_range(e->src, e->src_x, e->src_y, e->src_pitch, e->width, e->height, &start, &span);
+        if (!fits || span == 0) continue;                                /* R-33 */
+        ok[k] = 1; lo[k] = start; hi[k] = start + span;
+        if (conc_hazard(st, space[k], lo[k], hi[k], wr[k], thread, e->seq)) v->flags |= F_CONCURRENT;
+    }
+    if (v->status == 0)                                                 /* R-34 */
+        for (int k = 0; k < na; k++)
+            if (ok[k]) add_stamp(st, space[k], lo[k], hi[k], wr[k], thread, e->seq);
+}
+
+/* one copy by a given thread: O5 then, in concurrency mode, O7 */
+void or_check_copy_mt(or_state *st, const or_event *ev, uint32_t thread, or_verdict *v) {
+    or_check_copy(st, ev, v);
+    if (st->conc) check_concurrent(st, ev, thread, v);
+}
+
 /* ------------------------------------------------------ O6 leak report */
 static int cmp_base(const void *a, const void *b) {
     uint64_t x = ((const or_alloc *)a)->base, y = ((const or_alloc *)b)->base;
@@ -459,8 +572,18 @@ uint64_t or_leaks(or_state *st, or_alloc *out, uint64_t cap) {
 /* Replays n events in order.  out_v receives one verdict per COPY event (in
  * order); out_status receives one status per event (call status for
  * MARK/SETV/REG/FREE, verdict status for COPY). Returns the number of copies. */
+uint64_t or_replay_mt(or_state *st, const or_event *ev, uint64_t n, const uint8_t *blob, const uint32_t *threads,
+                      or_verdict *out_v, uint32_t *out_status);
+
 uint64_t or_replay(or_state *st, const or_event *ev, uint64_t n, const uint8_t *blob,
                    or_verdict *out_v, uint32_t *out_status) {
+    return or_replay_mt(st, ev, n, blob, NULL, out_v, out_status);
+}
+
+/* as or_replay; threads[i] is the thread of event i (NULL: all thread 0);
+ * SYNC events are ctx_synchronize of their thread */
+uint64_t or_replay_mt(or_state *st, const or_event *ev, uint64_t n, const uint8_t *blob, const uint32_t *threads,
+                      or_verdict *out_v, uint32_t *out_status) {
     uint64_t nc = 0;
     for (uint64_t i = 0; i < n; i++) {
         const or_event *e = &ev[i];
@@ -475,8 +598,10 @@ uint64_t or_replay(or_state *st, const or_event *ev, uint64_t n, const uint8_t *
                                                                      e->dst_pitch), e->seq);
             break;
         case OR_FREEA: s = (uint32_t)or_free_array(st, e->dst, e->seq); break;
+        case OR_SYNC: or_sync(st, threads ? threads[i] : 0, e->seq); break;
         case OR_COPY:
             or_check_copy(st, e, &out_v[nc]);
+            if (st->conc) check_concurrent(st, e, threads ? threads[i] : 0, &out_v[nc]);
             s = out_v[nc].status;
             nc++;
             break;

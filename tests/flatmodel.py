@@ -17,12 +17,45 @@ import numpy as np
 NONE = (1 << 64) - 1
 U64 = (1 << 64) - 1
 FLAG = dict(DST_NA=1, DST_SMALL=2, SRC_NA=4, SRC_SMALL=8, HOST_UNADDR=16,
-            HOST_UNDEF=32, BAD_PITCH=64, INVALID_RANGE=128, BAD_KIND=256)
+            HOST_UNDEF=32, BAD_PITCH=64, INVALID_RANGE=128, BAD_KIND=256, CONCURRENT=512)
+
+
+class _PagedLast:
+    """NEXT-2: per-byte "id of the last recorded access" over a sparse 64-bit
+    address space (dense 4 KiB numpy pages, -1 = never accessed)."""
+    PAGE = 4096
+
+    def __init__(self):
+        self.pages: dict = {}
+
+    def _chunks(self, lo, hi):
+        while lo < hi:
+            pg, off = divmod(lo, self.PAGE)
+            n = min(hi - lo, self.PAGE - off)
+            yield pg, off, n
+            lo += n
+
+    def max_id(self, lo, hi) -> int:
+        m = -1
+        for pg, off, n in self._chunks(lo, hi):
+            a = self.pages.get(pg)
+            if a is not None:
+                m = max(m, int(a[off:off + n].max()))
+        return m
+
+    def paint(self, lo, hi, ident):
+        for pg, off, n in self._chunks(lo, hi):
+            a = self.pages.setdefault(pg, np.full(self.PAGE, -1, np.int64))
+            a[off:off + n] = ident
 
 
 class FlatModel:
-    def __init__(self, h0: int, s: int, undef_is_error: bool = False, track: bool = False):
+    def __init__(self, h0: int, s: int, undef_is_error: bool = False, track: bool = False, conc: bool = False):
         self.h0, self.s = h0, s
+        self.conc = conc                          # NEXT-2 per-byte last-access model
+        self.last_acc = (_PagedLast(), _PagedLast())   # host space, device space
+        self.stamps: list = []                    # id -> (thread, seq, is_write)
+        self.syncs: dict = {}                     # thread -> sorted sync seqs
         self.track = track
         self.dv: dict = {}                        # base -> numpy V-bytes of the allocation (NEXT-1)
         self.arrays: dict = {}                    # handle -> total bytes (NEXT-3)
@@ -256,10 +289,46 @@ class FlatModel:
             write("dst", read("src"))    # read everything first: memmove semantics
         return out
 
-    def replay(self, events, blob):
+    def sync(self, thread, seq):
+        bisect.insort(self.syncs.setdefault(thread, []), seq)
+
+    def concurrency(self, e, thread, out):
+        """NEXT-2 per byte: the last recorded access of every byte of the new
+        access's range; the newest of them decides (R-31..R-34)."""
+        kind, w, h = int(e["kind"]), int(e["width"]), int(e["height"])
+        acc = {1: [(0, "src", 0), (1, "dst", 1)], 2: [(1, "src", 0), (0, "dst", 1)],
+               3: [(1, "src", 0), (1, "dst", 1)], 4: [(0, "src", 0)], 5: [(0, "dst", 1)]}.get(kind, [])
+        rng = []
+        for space, p, wr in acc:
+            start = int(e[p]) + int(e[p + "_y"]) * int(e[p + "_pitch"]) + int(e[p + "_x"])
+            span = 0 if (w == 0 or h == 0) else (h - 1) * int(e[p + "_pitch"]) + w
+            if span == 0 or start + span > U64:
+                continue
+            rng.append((space, start, start + span, wr))
+        seq = int(e["seq"])
+        for space, lo, hi, wr in rng:
+            m = self.last_acc[space].max_id(lo, hi)
+            if m < 0:
+                continue
+            pt, ps, pw = self.stamps[m]
+            s_list = self.syncs.get(pt, [])
+            synced = bisect.bisect_right(s_list, ps) < bisect.bisect_left(s_list, seq)
+            if pt != thread and not synced and (pw or wr):
+                out["flags"] |= FLAG["CONCURRENT"]
+        if out["status"] == 0:
+            for space, lo, hi, wr in sorted(rng, key=lambda r: r[3]):   # reads first: a write wins a tie
+                self.stamps.append((thread, seq, wr))
+                self.last_acc[space].paint(lo, hi, len(self.stamps) - 1)
+
+    def replay(self, events, blob, threads=None):
         verdicts, status = [], []
-        for e in events:
+        for i, e in enumerate(events):
             op = int(e["op"])
+            th = int(threads[i]) if threads is not None else 0
+            if op == 8:
+                self.sync(th, int(e["seq"]))
+                status.append(0)
+                continue
             if op == 1:
                 status.append(self.mark(int(e["dst"]), int(e["width"]), int(e["kind"])))
             elif op == 2:
@@ -271,6 +340,8 @@ class FlatModel:
                 status.append(self.free(int(e["dst"]), int(e["seq"])))
             elif op == 5:
                 v = self.copy(e)
+                if self.conc:
+                    self.concurrency(e, th, v)
                 verdicts.append(v)
                 status.append(v["status"])
             elif op == 6:

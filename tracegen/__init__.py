@@ -24,10 +24,12 @@ FREE       device free: ``dst`` = ptr
 COPY       one cuMemcpy{HtoD,DtoH,DtoD,2D} call: ``kind``,
            ``width`` (WidthInBytes), ``height`` (1 for 1D), and per side the
            raw CUDA_MEMCPY2D fields base / X / Y / pitch
+SYNC       NEXT-2 ctx_synchronize of the event's thread
 =========  ==========================================================
 
 ``seq`` is one global, strictly increasing event counter (SPEC's
-``SimState.seq``, S:308).
+``SimState.seq``).  ``Trace.threads[i]`` is the thread that issued
+event i (NEXT-2; all 0 for single-threaded traces).
 
 Device addresses come from SPEC's deterministic bump allocator (S:370:
 "Device addresses come from a deterministic bump allocator starting at
@@ -41,7 +43,7 @@ from typing import Dict, List, Optional
 
 import numpy as np
 
-OP_MARK, OP_SETV, OP_REG, OP_FREE, OP_COPY, OP_REGA, OP_FREEA = 1, 2, 3, 4, 5, 6, 7
+OP_MARK, OP_SETV, OP_REG, OP_FREE, OP_COPY, OP_REGA, OP_FREEA, OP_SYNC = 1, 2, 3, 4, 5, 6, 7, 8
 HTOD, DTOH, DTOD, HTOA, ATOH = 1, 2, 3, 4, 5
 NOACCESS, UNDEFINED, DEFINED = 0, 1, 2
 
@@ -67,6 +69,7 @@ class Trace:
     host_base: int                # H0 (4096-aligned)
     host_size: int                # S  (multiple of 4096)
     meta: Dict = dataclasses.field(default_factory=dict)
+    threads: Optional[np.ndarray] = None   # uint32[n]: issuing thread per event (NEXT-2)
 
     @property
     def copy_index(self) -> np.ndarray:
@@ -87,7 +90,10 @@ class TraceBuilder:
         self.host_base = host_base
         self.host_size = host_size
         self._blocks: List[np.ndarray] = []
+        self._tblocks: List[np.ndarray] = []
         self._rows: List[tuple] = []
+        self._row_threads: List[int] = []
+        self.thread = 0                    # NEXT-2: thread of the next recorded events
         self._blob = bytearray()
         self._seq = 0
         self.heap_cursor = DEVICE_HEAP_BASE
@@ -100,7 +106,9 @@ class TraceBuilder:
             for i, r in enumerate(self._rows):
                 arr[i] = r
             self._blocks.append(arr)
+            self._tblocks.append(np.array(self._row_threads, np.uint32))
             self._rows = []
+            self._row_threads = []
 
     def _next_seq(self) -> int:
         self._seq += 1
@@ -111,6 +119,7 @@ class TraceBuilder:
         seq = self._next_seq()
         self._rows.append((op, kind, seq, width, height, dst, dst_x, dst_y,
                            dst_pitch, src, src_x, src_y, src_pitch))
+        self._row_threads.append(self.thread)
         return seq
 
     def block(self, arr: np.ndarray) -> np.ndarray:
@@ -120,6 +129,7 @@ class TraceBuilder:
         arr["seq"] = np.arange(self._seq + 1, self._seq + 1 + len(arr), dtype=np.uint64)
         self._seq += len(arr)
         self._blocks.append(arr)
+        self._tblocks.append(np.full(len(arr), self.thread, np.uint32))
         return arr
 
     # -- calls ---------------------------------------------------------------
@@ -136,6 +146,10 @@ class TraceBuilder:
 
     def free(self, ptr: int) -> int:
         return self._row(OP_FREE, dst=ptr)
+
+    def sync(self) -> int:
+        """NEXT-2: ctx_synchronize by the current thread."""
+        return self._row(OP_SYNC)
 
     def register_array(self, handle: int, width: int, height: int = 0, depth: int = 0, fmt: int = 0,
                        channels: int = 1) -> int:
@@ -179,8 +193,9 @@ class TraceBuilder:
     def build(self) -> Trace:
         self._flush_rows()
         ev = np.concatenate(self._blocks) if self._blocks else np.zeros(0, EVENT_DTYPE)
+        th = np.concatenate(self._tblocks) if self._tblocks else np.zeros(0, np.uint32)
         return Trace(self.name, ev, np.frombuffer(bytes(self._blob), np.uint8).copy(),
-                     self.host_base, self.host_size, self.meta)
+                     self.host_base, self.host_size, self.meta, th)
 
 
 def _log_uniform(rng: np.random.Generator, a: float, b: float, n: int) -> np.ndarray:
@@ -244,10 +259,14 @@ def listing2() -> Trace:
 # Random tiny traces (<=200 events in a 64 KiB window)
 # ---------------------------------------------------------------------------
 def random_tiny(seed: int, n_events: int = 200, window: int = 64 * KiB,
-                host_base: int = 0x40000, arrays: bool = False) -> Trace:
+                host_base: int = 0x40000, arrays: bool = False, threads: int = 0) -> Trace:
     """Unaligned, overlapping, out-of-window, 2D, reuse-after-free: everything
-    the method must handle, at sizes a brute-force checker finishes quickly."""
+    the method must handle, at sizes a brute-force checker finishes quickly.
+    threads > 0 (NEXT-2): every event is issued by a random one of `threads`
+    threads and SYNC events are interleaved (drawn from a second generator,
+    so the call stream itself is the same as with threads = 0)."""
     rng = np.random.default_rng(seed)
+    rng_t = np.random.default_rng(seed + 0x5EED) if threads else None
     tb = TraceBuilder(f"tiny{seed}", host_base, window)
     live: List[tuple] = []
     freed: List[tuple] = []
@@ -281,6 +300,10 @@ def random_tiny(seed: int, n_events: int = 200, window: int = 64 * KiB,
         tb.mark(a, min(l, host_base + window - a), int(rng.choice([UNDEFINED, DEFINED], p=[0.3, 0.7])))
     handles: List[tuple] = []      # (handle, nominal bytes) of created arrays
     for _ in range(n_events - 4):
+        if rng_t is not None:
+            tb.thread = int(rng_t.integers(threads))
+            if rng_t.random() < 0.08:
+                tb.sync()
         u = rng.random()
         if arrays and u < 0.22:         # NEXT-3: device arrays and their transfers
             v = rng.random()
