@@ -375,8 +375,47 @@ def run_ours(args, rank, world, device):
     }
     if rank == 0 and not args.no_registry_rate:
         res["registry_events_per_s"] = registry_rate(cg, tr, device)
+    if args.conc:
+        res["next2"] = conc_rate(cg, descs, d_out, args, device, stream)
     chk.close()
     return res
+
+
+def conc_rate(cg, descs, d_out, args, device, stream):
+    """NEXT-2: cg_conc_check on the same batch and verdicts, issued by
+    args.conc random threads; every call gets the batch with its seqs shifted
+    past the previous call's (the contract), so the last-access map is carried
+    from call to call as in a long program."""
+    import torch
+    n = len(descs)
+    rng = np.random.default_rng(0x2C)
+    th = torch.from_numpy(rng.integers(0, args.conc, n).astype(np.int32)).to(device)
+    span = int(descs["seq"].max()) + 1
+    k, w = max(3, args.steps // 4), max(3, args.warmup)
+    arrs = []
+    for i in range(k + w):
+        d = descs.copy()
+        d["seq"] += np.uint64(i * span)
+        arrs.append(cg.to_device_descs(d, device))
+    conc = cg.ConcChecker(n, 4 * n, device)
+    for i in range(w):
+        conc.check(arrs[i], th, d_out, stream=stream)
+    torch.cuda.synchronize()
+    l0 = conc.kernel_launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(w, w + k):
+        conc.check(arrs[i], th, d_out, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / k
+    v = cg.verdicts_to_numpy(d_out)
+    out = {"threads": args.conc, "ms_per_call": ms, "copies_per_s": n / (ms * 1e-3),
+           "hazard_copies": int(np.count_nonzero(v["flags"] & cg.CG_F_CONCURRENT)),
+           "map_ranges": conc.stamps(), "gpu_launches_per_call": (conc.kernel_launches - l0) / k,
+           "entry": "cg_conc_check (synchronous: 3 host reads of counts per address space)"}
+    conc.close()
+    return out
 
 
 class OracleArm:
@@ -443,6 +482,7 @@ def main():
     ap.add_argument("--no-registry-rate", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="check and apply as two calls")
     ap.add_argument("--track", action="store_true", help="NEXT-1 device V-bit tracking (apply = propagation)")
+    ap.add_argument("--conc", type=int, default=0, help="NEXT-2: also time cg_conc_check with this many threads")
     args = ap.parse_args()
     assert args.warmup >= 1
 

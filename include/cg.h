@@ -85,7 +85,8 @@ enum {
   CG_F_HOST_UNDEFINED = 1u << 5,     /* P:81 undefined host data sent (Warning)      */
   CG_F_BAD_PITCH = 1u << 6,          /* R-12: pitch < WidthInBytes + XInBytes         */
   CG_F_INVALID_RANGE = 1u << 7,      /* an address range overflows 64 bits      */
-  CG_F_BAD_KIND = 1u << 8            /* R-16: kind not in {HTOD, DTOH, DTOD, HTOA, ATOH} */
+  CG_F_BAD_KIND = 1u << 8,           /* R-16: kind not in {HTOD, DTOH, DTOD, HTOA, ATOH} */
+  CG_F_CONCURRENT = 1u << 9          /* NEXT-2: ConcurrentHazard, a Warning (cg_conc_check) */
 };
 
 /* One cuMemcpy{HtoD,DtoH,DtoD,2D} call, with the raw CUDA_MEMCPY2D fields
@@ -287,6 +288,48 @@ cg_status cg_free_array(cg_ctx *ctx, uint64_t handle, uint64_t seq);
  * handle order into the host array h_out (at most cap), *n_out = how many are
  * live.  Synchronous host operation. */
 cg_status cg_array_report(cg_ctx *ctx, cg_alloc_record *h_out, uint64_t cap, uint64_t *n_out);
+
+/* ---- NEXT-2: concurrency hazards ("certain concurrent
+ * accesses when several threads are used"; SPEC check_concurrent S:258-266,
+ * rule S:285; R-31..R-35) ----
+ * A separate checker object that owns its device memory.  Every side of a
+ * copy is an access of its address space (host / device; R-32) over its
+ * folded [start, start+span) (R-33).  An access is a ConcurrentHazard iff the
+ * newest earlier recorded access overlapping it was made by another thread
+ * that has not called cg_conc_sync since, and one of the two writes.  Only
+ * copies whose verdict status is CG_OK are recorded (R-34).  The state between
+ * calls is, per address space, the last-access map: disjoint ranges tagged
+ * with the stamp that touched them last. */
+typedef struct cg_conc cg_conc;
+
+/* max_n: largest batch of cg_conc_check; max_stamps: capacity of each address
+ * space's last-access map (ranges).  2*max_n + max_stamps < 2^30.  Allocates
+ * on `device` with cudaMalloc (freed by cg_conc_destroy).  Errors:
+ * CG_ERR_INVALID_VALUE, CG_ERR_CUDA, CG_ERR_OUT_OF_MEMORY. */
+cg_status cg_conc_create(int device, uint64_t max_n, uint64_t max_stamps, cg_conc **out);
+cg_status cg_conc_destroy(cg_conc *c);
+const char *cg_conc_last_error(const cg_conc *c);
+
+/* ctx_synchronize by `thread` at `seq` (R-31: marks that thread's
+ * earlier stamps synced for every later access).  Must be submitted before the
+ * cg_conc_check of any copy with a larger seq.  Host-only. */
+cg_status cg_conc_sync(cg_conc *c, uint32_t thread, uint64_t seq);
+
+/* check_concurrent for a batch: d_descs (n cg_copy_desc, in seq order, every
+ * seq larger than those of earlier batches) with their issuing threads
+ * d_threads (n uint32) and the verdicts the transfer check wrote for them
+ * (d_verdicts; status decides R-34's recording).  Sets CG_F_CONCURRENT in the
+ * verdict flags of every hazardous copy (status unchanged, R-35), then updates
+ * the last-access maps.  Overlaps inside the batch are resolved exactly (no
+ * planner cut is needed).  Synchronous on stream.  Errors: CG_ERR_INVALID_VALUE
+ * (null, n > max_n), CG_ERR_OUT_OF_MEMORY (a map would exceed max_stamps: the
+ * flags are written, the maps are left as before), CG_ERR_CUDA. */
+cg_status cg_conc_check(cg_conc *c, const cg_copy_desc *d_descs, const uint32_t *d_threads, uint64_t n,
+                        cg_verdict *d_verdicts, void *stream);
+
+/* Ranges in the host / device last-access maps (inspection). */
+cg_status cg_conc_stamps(const cg_conc *c, uint64_t *n_host, uint64_t *n_device);
+uint64_t cg_conc_kernel_launches(const cg_conc *c);
 
 /* The check for a batch of n descriptors:
  * validation, batched interval search in the allocation table as of each

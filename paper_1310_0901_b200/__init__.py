@@ -36,6 +36,7 @@ CG_F_HOST_UNDEFINED = 1 << 5
 CG_F_BAD_PITCH = 1 << 6
 CG_F_INVALID_RANGE = 1 << 7
 CG_F_BAD_KIND = 1 << 8
+CG_F_CONCURRENT = 1 << 9
 
 DESC_DTYPE = np.dtype([
     ("kind", "<u4"), ("reserved", "<u4"), ("seq", "<u8"), ("width", "<u8"), ("height", "<u8"),
@@ -116,6 +117,13 @@ def _load() -> ctypes.CDLL:
         "cg_register_array": (I, [P, U64, U64, U64, U64, U32, U32, U64]),
         "cg_free_array": (I, [P, U64, U64]),
         "cg_array_report": (I, [P, P, U64, P]),
+        "cg_conc_create": (I, [I, U64, U64, P]),
+        "cg_conc_destroy": (I, [P]),
+        "cg_conc_last_error": (ctypes.c_char_p, [P]),
+        "cg_conc_sync": (I, [P, U32, U64]),
+        "cg_conc_check": (I, [P, P, P, U64, P, P]),
+        "cg_conc_stamps": (I, [P, P, P]),
+        "cg_conc_kernel_launches": (U64, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -132,7 +140,9 @@ EXPORTED = ("cg_workspace_size", "cg_ctx_create", "cg_ctx_destroy", "cg_last_err
             "cg_batch_disjoint", "cg_straddler_pack", "cg_straddler_finalize", "cg_compact_dirty", "cg_shard_plan",
             "cg_host_query_addressable", "cg_expand_copy1d", "cg_check_host", "cg_format_verdict",
             "cg_format_leak", "cg_apply_copies", "cg_device_vbits", "cg_plan_batches_propagate",
-            "cg_array_bytes", "cg_register_array", "cg_free_array", "cg_array_report")
+            "cg_array_bytes", "cg_register_array", "cg_free_array", "cg_array_report", "cg_conc_create",
+            "cg_conc_destroy", "cg_conc_last_error", "cg_conc_sync", "cg_conc_check", "cg_conc_stamps",
+            "cg_conc_kernel_launches")
 
 # ---- same-name thin wrappers (status codes returned unchanged) -------------
 cg_workspace_size = _lib.cg_workspace_size
@@ -164,6 +174,13 @@ cg_array_bytes = _lib.cg_array_bytes
 cg_register_array = _lib.cg_register_array
 cg_free_array = _lib.cg_free_array
 cg_array_report = _lib.cg_array_report
+cg_conc_create = _lib.cg_conc_create
+cg_conc_destroy = _lib.cg_conc_destroy
+cg_conc_last_error = _lib.cg_conc_last_error
+cg_conc_sync = _lib.cg_conc_sync
+cg_conc_check = _lib.cg_conc_check
+cg_conc_stamps = _lib.cg_conc_stamps
+cg_conc_kernel_launches = _lib.cg_conc_kernel_launches
 
 
 def format_verdict(v, kind: int) -> str:
@@ -433,6 +450,55 @@ class Checker:
     def shadow(self):
         self.torch.cuda.synchronize(self.device)
         return self.A.cpu().numpy(), self.V.cpu().numpy()
+
+
+class ConcChecker:
+    """NEXT-2 concurrency checker (cg_conc_*): owns its device memory."""
+
+    def __init__(self, max_n: int, max_stamps: int, device: int = 0):
+        import torch
+        self.torch = torch
+        self.device = device
+        self.max_n = max_n
+        h = ctypes.c_void_p()
+        st = _lib.cg_conc_create(device, max_n, max_stamps, ctypes.byref(h))
+        if st:
+            raise CgError(st, "cg_conc_create")
+        self.h = h
+
+    def close(self):
+        if self.h:
+            _lib.cg_conc_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _ok(self, st: int, what: str):
+        if st:
+            raise CgError(st, f"{what}: {_lib.cg_conc_last_error(self.h).decode()}")
+
+    def sync(self, thread: int, seq: int):
+        self._ok(_lib.cg_conc_sync(self.h, thread, seq), "cg_conc_sync")
+
+    def check(self, d_descs, d_threads, d_verdicts, stream=None):
+        """d_descs: CUDA uint8 tensor of DESC_DTYPE records; d_threads: CUDA int32/uint32 tensor (one per copy)."""
+        n = d_descs.numel() // DESC_DTYPE.itemsize
+        assert d_threads.numel() == n
+        self._ok(_lib.cg_conc_check(self.h, d_descs.data_ptr(), d_threads.data_ptr(), n, d_verdicts.data_ptr(),
+                                    _stream_ptr(stream)), "cg_conc_check")
+
+    def stamps(self):
+        a, b = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        self._ok(_lib.cg_conc_stamps(self.h, ctypes.byref(a), ctypes.byref(b)), "cg_conc_stamps")
+        return a.value, b.value
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(_lib.cg_conc_kernel_launches(self.h))
 
 
 def to_device_descs(descs: np.ndarray, device: int = 0):

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcgcheck.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("cg_kernels.cu", "cg_runtime.cu")]
+SOURCES = [os.path.join(CSRC, f) for f in ("cg_kernels.cu", "cg_runtime.cu", "cg_conc.cu")]
 HEADERS = [os.path.join(ROOT, "include", "cg.h"), os.path.join(CSRC, "cg_internal.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

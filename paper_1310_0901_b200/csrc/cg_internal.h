@@ -14,6 +14,30 @@ constexpr uint64_t kInf = UINT64_MAX;          // free_seq of a live allocation
 constexpr uint64_t kMaxCopyBytes = 1ull << 38;  // R-10: larger copies are INVALID_RANGE
 constexpr uint64_t kMaxDescs = 1ull << 24;      // per call (keeps sum of weights < 2^63)
 
+// start = base + y*pitch + x; span = (w==0||h==0) ? 0 : (h-1)*pitch + w;
+// valid iff start + span <= 2^64 - 1 (every partial sum is then exact).
+__device__ __forceinline__ bool fold_side(uint64_t base, uint64_t x, uint64_t y, uint64_t pitch,
+                                          uint64_t w, uint64_t h, uint64_t& start, uint64_t& span) {
+  if (__umul64hi(y, pitch) != 0) return false;
+  uint64_t s = y * pitch;
+  uint64_t t = s + x;
+  if (t < s) return false;
+  uint64_t st = t + base;
+  if (st < t) return false;
+  uint64_t sp = 0;
+  if (w != 0 && h != 0) {
+    if (__umul64hi(h - 1, pitch) != 0) return false;
+    uint64_t q = (h - 1) * pitch;
+    sp = q + w;
+    if (sp < q) return false;
+  }
+  uint64_t e = st + sp;
+  if (e < st) return false;
+  start = st;
+  span = sp;
+  return true;
+}
+
 // Host window [wb, we) and the shard [sb, se) whose shadow this GPU stores.
 struct ShadowView {
   uint64_t wb, we, sb, se;

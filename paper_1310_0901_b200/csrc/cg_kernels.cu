@@ -110,29 +110,7 @@ __device__ __forceinline__ uint64_t warp_sum(uint64_t v) {
 // a1: descriptor normalisation (CUDA_MEMCPY2D start-address rule, pitch rule,
 // 64-bit overflow) -- DESIGN.md readings R-10, R-11, R-12, R-16
 // ---------------------------------------------------------------------------
-// start = base + y*pitch + x; span = (w==0||h==0) ? 0 : (h-1)*pitch + w;
-// valid iff start + span <= 2^64 - 1 (every partial sum is then exact).
-__device__ __forceinline__ bool fold_side(uint64_t base, uint64_t x, uint64_t y, uint64_t pitch,
-                                          uint64_t w, uint64_t h, uint64_t& start, uint64_t& span) {
-  if (__umul64hi(y, pitch) != 0) return false;
-  uint64_t s = y * pitch;
-  uint64_t t = s + x;
-  if (t < s) return false;
-  uint64_t st = t + base;
-  if (st < t) return false;
-  uint64_t sp = 0;
-  if (w != 0 && h != 0) {
-    if (__umul64hi(h - 1, pitch) != 0) return false;
-    uint64_t q = (h - 1) * pitch;
-    sp = q + w;
-    if (sp < q) return false;
-  }
-  uint64_t e = st + sp;
-  if (e < st) return false;
-  start = st;
-  span = sp;
-  return true;
-}
+// fold_side (cg_internal.h): CUDA_MEMCPY2D start / span of one side
 
 struct Norm {
   uint32_t kind, flags;

@@ -15,8 +15,8 @@ from __future__ import annotations
 
 import numpy as np
 
-OP_MARK, OP_SETV, OP_REG, OP_FREE, OP_COPY, OP_REGA, OP_FREEA = 1, 2, 3, 4, 5, 6, 7
-_REGISTRY = (OP_REG, OP_FREE, OP_COPY, OP_REGA, OP_FREEA)
+OP_MARK, OP_SETV, OP_REG, OP_FREE, OP_COPY, OP_REGA, OP_FREEA, OP_SYNC = 1, 2, 3, 4, 5, 6, 7, 8
+_REGISTRY = (OP_REG, OP_FREE, OP_COPY, OP_REGA, OP_FREEA, OP_SYNC)
 _DESC_FIELDS = ("kind", "seq", "width", "height", "dst", "dst_x", "dst_y", "dst_pitch",
                 "src", "src_x", "src_y", "src_pitch")
 
@@ -29,9 +29,12 @@ def events_to_descs(ev: np.ndarray) -> np.ndarray:
     return d
 
 
-def replay_events(chk, events: np.ndarray, blob=None, stream=None, fuse: bool = True):
+def replay_events(chk, events: np.ndarray, blob=None, stream=None, fuse: bool = True, conc=None, threads=None):
     """Returns (verdicts of the COPY events in order, status per event).
-    With fuse, batches that cg_batch_disjoint accepts use cg_check_apply."""
+    With fuse, batches that cg_batch_disjoint accepts use cg_check_apply.
+    conc (a ConcChecker) adds NEXT-2: SYNC events go to cg_conc_sync and every
+    checked batch to cg_conc_check with the copies' threads (threads[i] = the
+    issuing thread of event i, default all 0)."""
     import torch
     from . import MARK_DTYPE, VERDICT_DTYPE, to_device_descs, verdicts_to_numpy
 
@@ -76,6 +79,8 @@ def replay_events(chk, events: np.ndarray, blob=None, stream=None, fuse: bool = 
                                                    int(e["dst_y"]), int(e["dst_pitch"]), int(e["seq"]))
                 elif ops[k] == OP_FREEA:
                     status[k] = chk.free_array(int(events["dst"][k]), int(events["seq"][k]))
+                elif ops[k] == OP_SYNC and conc is not None:
+                    conc.sync(int(threads[k]) if threads is not None else 0, int(events["seq"][k]))
             idx = np.flatnonzero(is_copy[i:j]) + i
             if len(idx):
                 descs = events_to_descs(events[idx])
@@ -94,6 +99,10 @@ def replay_events(chk, events: np.ndarray, blob=None, stream=None, fuse: bool = 
                         else:
                             dv = chk.check_copies(dd, stream=stream)
                             chk.apply_dtoh(dd, dv, stream=stream)
+                        if conc is not None:
+                            th = np.zeros(s1 - s0, np.int32) if threads is None else \
+                                np.asarray(threads[idx[s0:s1]]).astype(np.int32)
+                            conc.check(dd, torch.from_numpy(th).to(dd.device), dv, stream=stream)
                         v = verdicts_to_numpy(dv)
                         verdicts[copy_rank[idx[s0:s1]]] = v
                         status[idx[s0:s1]] = v["status"]

@@ -806,3 +806,23 @@ def c5_sharded(seed: int = 13100905, scale: float = 1.0, shards: int = 8, inject
 
 
 CONFIGS["c5_sharded"] = c5_sharded
+
+
+# ---------------------------------------------------------------------------
+# NEXT-2: multi-threaded variants of any trace
+# ---------------------------------------------------------------------------
+def with_threads(tr: Trace, n_threads: int, sync_frac: float = 0.01, seed: int = 0x7C) -> Trace:
+    """Every event of `tr` is issued by a uniformly random one of n_threads
+    threads, and SYNC events (each by a random thread) are inserted at a
+    `sync_frac` fraction of the positions; seqs are renumbered 1..n (the call
+    order is unchanged, so every non-SYNC event keeps its meaning)."""
+    rng = np.random.default_rng(seed)
+    n = len(tr.events)
+    ns = int(round(n * sync_frac))
+    at = np.sort(rng.integers(0, n + 1, ns))
+    syncs = np.zeros(ns, EVENT_DTYPE)
+    syncs["op"] = OP_SYNC
+    ev = np.insert(tr.events, at, syncs)
+    ev["seq"] = np.arange(1, len(ev) + 1, dtype=np.uint64)
+    th = rng.integers(0, n_threads, len(ev)).astype(np.uint32)
+    return Trace(f"{tr.name}_t{n_threads}", ev, tr.blob, tr.host_base, tr.host_size, dict(tr.meta), th)
