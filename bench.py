@@ -40,31 +40,38 @@ METRIC = "shadow GB/s and copy-descriptors/s validated (1/2/4/8 B200, % of HBM p
 UNIT = "GB/s"
 
 
-def algorithmic_bytes(descs: np.ndarray, verdicts: np.ndarray | None, track: bool = False):
+def algorithmic_bytes(descs: np.ndarray, verdicts: np.ndarray | None, track: bool = False, two_bit: bool = False):
     """Shadow bytes the method must move: HtoD 1 V-byte + 1/8
     A-byte per host byte; DtoH 1/8 A-byte per host byte for the check and 1
     V-byte written per host byte by the apply when the verdict has no Error.
     With device V-bit tracking (NEXT-1) the apply instead reads and writes one
-    V-byte per byte of every error-free copy (HtoD, DtoD, DtoH)."""
+    V-byte per byte of every error-free copy (HtoD, DtoD, DtoH).  With the
+    NEXT-4 2-bit shadow both checks read 0.25 B per host byte and the apply
+    writes 0.25 B."""
     nb = descs["width"].astype(np.float64) * descs["height"].astype(np.float64)
     htod = descs["kind"] == 1
     dtoh = descs["kind"] == 2
-    check = float(nb[htod].sum()) * 1.125 + float(nb[dtoh].sum()) * 0.125
     okv = np.ones(len(descs), bool) if verdicts is None else verdicts["status"] == 0
+    if two_bit:
+        return 0.25 * float(nb[htod | dtoh].sum()), 0.25 * float(nb[dtoh & okv].sum())
+    check = float(nb[htod].sum()) * 1.125 + float(nb[dtoh].sum()) * 0.125
     if track:
         return check, 2.0 * float(nb[okv & (descs["kind"] >= 1) & (descs["kind"] <= 3)].sum())
     apply = float(nb[dtoh & okv].sum())
     return check, apply
 
 
-def fused_apply_bytes(descs: np.ndarray, verdicts: np.ndarray, max_descs: int) -> float:
+def fused_apply_bytes(descs: np.ndarray, verdicts: np.ndarray, max_descs: int, two_bit: bool = False) -> float:
     """Bytes the fused scan writes itself in cg_check_apply: DtoH descriptors
     with status OK, contiguous and not split by the scan's grouping (weight at
     most one group, or inside one group); the rest go to the residual pass.  Replicates the
     library's plan (weight = 256 + host units; group T = max(128 KiB,
     ceil(total / max(2^20, 2 max_descs)))) for accounting only."""
     nb = descs["width"].astype(np.uint64) * descs["height"].astype(np.uint64)
-    units = np.where(descs["kind"] == 1, nb, np.where(descs["kind"] == 2, (nb + np.uint64(7)) // np.uint64(8), 0))
+    if two_bit:
+        units = np.where((descs["kind"] == 1) | (descs["kind"] == 2), (nb + np.uint64(3)) // np.uint64(4), 0)
+    else:
+        units = np.where(descs["kind"] == 1, nb, np.where(descs["kind"] == 2, (nb + np.uint64(7)) // np.uint64(8), 0))
     w = np.uint64(256) + units.astype(np.uint64)
     P = np.concatenate([[0], np.cumsum(w, dtype=np.uint64)])
     total = int(P[-1])
@@ -73,7 +80,7 @@ def fused_apply_bytes(descs: np.ndarray, verdicts: np.ndarray, max_descs: int) -
     whole = ((P[1:] - P[:-1]) <= T) | ((P[:-1] // T) == ((P[1:] - 1) // T))
     contig = (descs["height"] == 1) | (descs["width"] == descs["dst_pitch"])
     ok = (descs["kind"] == 2) & (verdicts["status"] == 0) & contig & whole
-    return float(nb[ok].astype(np.float64).sum())
+    return float(nb[ok].astype(np.float64).sum()) * (0.25 if two_bit else 1.0)
 
 
 def load_peaks():
@@ -159,7 +166,8 @@ def make_workload(name: str, rank: int = 0, scale: float = 1.0):
     raise SystemExit(f"unknown config {name}")
 
 
-def setup_checker(cg, tr, device: int, host_staging: bool, rank: int = 0, world: int = 1, track: bool = False):
+def setup_checker(cg, tr, device: int, host_staging: bool, rank: int = 0, world: int = 1, track: bool = False,
+                  shadow_format: int = 0):
     """Replays the non-copy events (host marks, V-bytes, registry) and returns
     the checker and the copy descriptors (host array).  With world > 1 the
     context holds shard `rank` of the global window."""
@@ -171,12 +179,13 @@ def setup_checker(cg, tr, device: int, host_staging: bool, rank: int = 0, world:
         gbase = tr.host_base - rank * tr.host_size
         chk = cg.Checker(gbase, world * tr.host_size, shard_base=tr.host_base, shard_size=tr.host_size,
                          max_descs=max(len(copies), 1024), max_allocs=max(nreg, 1024), device=device,
-                         host_staging=host_staging)
+                         host_staging=host_staging, shadow_format=shadow_format)
     else:
         regs = ev[ev["op"] == 3]
         pool = int(regs["width"].astype(np.int64).sum()) + 256 * len(regs) + (1 << 20) if track else 0
         chk = cg.Checker(tr.host_base, tr.host_size, max_descs=max(len(copies), 1024),
-                         max_allocs=max(nreg, 1024), device=device, host_staging=host_staging, dev_vsize=pool)
+                         max_allocs=max(nreg, 1024), device=device, host_staging=host_staging, dev_vsize=pool,
+                         shadow_format=shadow_format)
     setup = ev[ev["op"] != 5]
     t0 = time.perf_counter()
     cg.replay_events(chk, setup, tr.blob)
@@ -207,8 +216,9 @@ def run_ours(args, rank, world, device):
 
     torch.cuda.set_device(device)
     tr = make_workload(args.config, rank, args.scale)
+    two_bit = args.shadow == "2bit"
     chk, descs, t_setup, nreg = setup_checker(cg, tr, device, host_staging=not args.no_e2e, rank=rank, world=world,
-                                              track=args.track)
+                                              track=args.track, shadow_format=1 if two_bit else 0)
     n = len(descs)
     stream = torch.cuda.current_stream()
     d_descs = cg.to_device_descs(descs, device)
@@ -249,7 +259,7 @@ def run_ours(args, rank, world, device):
         step()
     torch.cuda.synchronize()
     verd = cg.verdicts_to_numpy(d_out)
-    check_b, apply_b = algorithmic_bytes(descs, verd, track=args.track)
+    check_b, apply_b = algorithmic_bytes(descs, verd, track=args.track, two_bit=two_bit)
     bytes_per_step = check_b + apply_b
 
     if world > 1:
@@ -334,10 +344,10 @@ def run_ours(args, rank, world, device):
     scan_ms, scan_n = stages["check_scan"]
     apply_ms, apply_n = stages["apply"]
     scan_avg = scan_ms / max(scan_n, 1)
-    scan_bytes = check_b + (fused_apply_bytes(descs, verd, max(n, 1024)) if fused else 0.0)
+    scan_bytes = check_b + (fused_apply_bytes(descs, verd, max(n, 1024), two_bit) if fused else 0.0)
     achieved = scan_bytes / (scan_avg * 1e-3) / 1e9
     traffic = None
-    prof_json = os.path.join(ROOT, "profiles", f"ncu_{args.config}_check_scan.json")
+    prof_json = os.path.join(ROOT, "profiles", f"ncu_{args.config}{'_2bit' if two_bit else ''}_check_scan.json")
     if os.path.exists(prof_json):
         with open(prof_json) as f:
             pj = json.load(f)
@@ -354,6 +364,7 @@ def run_ours(args, rank, world, device):
                    "shadow_bytes_per_step": bytes_per_step, "check_bytes": check_b, "apply_bytes": apply_b,
                    "l2": "no flush: >= 8.5 GB of shadow streamed per step vs 126 MB L2",
                    "parallelism": f"host-range shards x{world}",
+                   "shadow_format": "2-bit states (NEXT-4)" if two_bit else "V bytes + A bits",
                    "entry": ("cg_check_copies + cg_apply_copies (NEXT-1 V-bit propagation)" if args.track else
                              "cg_check_apply (fused)" if fused else "cg_check_copies + cg_apply_dtoh")},
         "descriptors_per_s": world * n / (ms_step * 1e-3),
@@ -483,6 +494,8 @@ def main():
     ap.add_argument("--unfused", action="store_true", help="check and apply as two calls")
     ap.add_argument("--track", action="store_true", help="NEXT-1 device V-bit tracking (apply = propagation)")
     ap.add_argument("--conc", type=int, default=0, help="NEXT-2: also time cg_conc_check with this many threads")
+    ap.add_argument("--shadow", default="bytes", choices=["bytes", "2bit"],
+                    help="host shadow format: V bytes + A bits, or NEXT-4 2-bit states")
     args = ap.parse_args()
     assert args.warmup >= 1
 

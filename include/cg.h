@@ -175,7 +175,19 @@ typedef struct {
  *    through error-free copies (HtoD host->device, DtoD device->device with
  *    memmove semantics, DtoH device->host) instead of R-5's "DtoH marks the
  *    host range defined".  dev_vsize must be a multiple of 16.  Requires an
- *    unsharded context. */
+ *    unsharded context.
+ *  - shadow_format (NEXT-4): CG_SHADOW_BYTES (0) = one V byte per
+ *    host byte + one A bit per host byte (v_buf / a_buf as above);
+ *    CG_SHADOW_2BIT (1) = Memcheck-style compressed states, 2 bits per host
+ *    byte {NOACCESS, PARTIAL, DEFINED, UNDEFINED} in v_buf (shard_size/4
+ *    bytes, 16-byte aligned; a_buf unused, may be NULL).  Exact partial
+ *    V-bytes (cg_host_set_vbits values other than 0x00 / 0xFF) are kept in a
+ *    host-side table for cg_host_shadow_read; the checks only need "some bit
+ *    undefined", which the state holds (R-36).  The scan then reads
+ *    0.25 B per host byte for both kinds and the DtoH apply writes 0.25 B.
+ *    Not combinable with dev_vbuf. */
+enum { CG_SHADOW_BYTES = 0, CG_SHADOW_2BIT = 1 };
+
 typedef struct {
   uint64_t host_base, host_size;
   uint64_t shard_base, shard_size;
@@ -183,7 +195,7 @@ typedef struct {
   uint32_t undef_is_error;  /* S:284 promotes HOST_UNDEFINED to an Error */
   uint32_t host_staging;
   int32_t device;           /* CUDA device ordinal                       */
-  int32_t reserved;
+  int32_t shadow_format;    /* CG_SHADOW_BYTES / CG_SHADOW_2BIT (NEXT-4) */
   void *v_buf, *a_buf, *workspace;
   uint64_t workspace_size;
   void *dev_vbuf;           /* NEXT-1 device V-bit pool (or NULL)        */
@@ -235,6 +247,13 @@ cg_status cg_host_mark_batch(cg_ctx *ctx, const cg_mark *h_marks, uint64_t n, ui
  * nothing is changed then. */
 cg_status cg_host_set_vbits(cg_ctx *ctx, uint64_t addr, uint64_t len, const uint8_t *h_vbytes,
                             void *stream);
+
+/* Synchronous read of the host shadow of [addr, addr+len), which must lie in
+ * this context's shard, in the plain form of either format: h_a[i] = 1 if
+ * byte addr+i is addressable else 0, h_v[i] = its V-byte (0xFF for
+ * unaddressable bytes); either output may be NULL.  Inspection / tests.
+ * Errors: CG_ERR_INVALID_VALUE (range outside the shard), CG_ERR_CUDA. */
+cg_status cg_host_shadow_read(cg_ctx *ctx, uint64_t addr, uint64_t len, uint8_t *h_a, uint8_t *h_v, void *stream);
 
 /* Synchronous query: *all_addressable = 1 iff every byte of [addr, addr+len)
  * that this context's shard stores is addressable and the range lies in the

@@ -60,7 +60,7 @@ class cg_config(ctypes.Structure):
         ("shard_base", ctypes.c_uint64), ("shard_size", ctypes.c_uint64),
         ("max_descs", ctypes.c_uint64), ("max_allocs", ctypes.c_uint64),
         ("undef_is_error", ctypes.c_uint32), ("host_staging", ctypes.c_uint32),
-        ("device", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("device", ctypes.c_int32), ("shadow_format", ctypes.c_int32),
         ("v_buf", ctypes.c_void_p), ("a_buf", ctypes.c_void_p), ("workspace", ctypes.c_void_p),
         ("workspace_size", ctypes.c_uint64),
         ("dev_vbuf", ctypes.c_void_p), ("dev_vsize", ctypes.c_uint64),
@@ -117,6 +117,7 @@ def _load() -> ctypes.CDLL:
         "cg_register_array": (I, [P, U64, U64, U64, U64, U32, U32, U64]),
         "cg_free_array": (I, [P, U64, U64]),
         "cg_array_report": (I, [P, P, U64, P]),
+        "cg_host_shadow_read": (I, [P, U64, U64, P, P, P]),
         "cg_conc_create": (I, [I, U64, U64, P]),
         "cg_conc_destroy": (I, [P]),
         "cg_conc_last_error": (ctypes.c_char_p, [P]),
@@ -140,7 +141,7 @@ EXPORTED = ("cg_workspace_size", "cg_ctx_create", "cg_ctx_destroy", "cg_last_err
             "cg_batch_disjoint", "cg_straddler_pack", "cg_straddler_finalize", "cg_compact_dirty", "cg_shard_plan",
             "cg_host_query_addressable", "cg_expand_copy1d", "cg_check_host", "cg_format_verdict",
             "cg_format_leak", "cg_apply_copies", "cg_device_vbits", "cg_plan_batches_propagate",
-            "cg_array_bytes", "cg_register_array", "cg_free_array", "cg_array_report", "cg_conc_create",
+            "cg_host_shadow_read", "cg_array_bytes", "cg_register_array", "cg_free_array", "cg_array_report", "cg_conc_create",
             "cg_conc_destroy", "cg_conc_last_error", "cg_conc_sync", "cg_conc_check", "cg_conc_stamps",
             "cg_conc_kernel_launches")
 
@@ -171,6 +172,8 @@ cg_apply_copies = _lib.cg_apply_copies
 cg_device_vbits = _lib.cg_device_vbits
 cg_plan_batches_propagate = _lib.cg_plan_batches_propagate
 cg_array_bytes = _lib.cg_array_bytes
+cg_host_shadow_read = _lib.cg_host_shadow_read
+CG_SHADOW_BYTES, CG_SHADOW_2BIT = 0, 1
 cg_register_array = _lib.cg_register_array
 cg_free_array = _lib.cg_free_array
 cg_array_report = _lib.cg_array_report
@@ -263,7 +266,8 @@ class Checker:
 
     def __init__(self, host_base: int, host_size: int, *, max_descs: int = 1 << 20,
                  max_allocs: int = 1 << 18, undef_is_error: bool = False, device: int = 0,
-                 shard_base: int = 0, shard_size: int = 0, host_staging: bool = False, dev_vsize: int = 0):
+                 shard_base: int = 0, shard_size: int = 0, host_staging: bool = False, dev_vsize: int = 0,
+                 shadow_format: int = 0):
         import torch
         self.torch = torch
         self.device = device
@@ -272,7 +276,10 @@ class Checker:
         self.cfg = cg_config(host_base=host_base, host_size=host_size, shard_base=shard_base,
                              shard_size=shard_size, max_descs=max_descs, max_allocs=max_allocs,
                              undef_is_error=int(undef_is_error), host_staging=int(host_staging),
-                             device=device)
+                             device=device, shadow_format=shadow_format)
+        self.two_bit = shadow_format == CG_SHADOW_2BIT
+        self.shard_base = shard_base if shard_size else host_base
+        self.shard_size = ss
         self.tracking = dev_vsize > 0
         if self.tracking:   # NEXT-1 device V-bit pool
             dev_vsize = (dev_vsize + 15) // 16 * 16
@@ -282,11 +289,15 @@ class Checker:
         ws = _lib.cg_workspace_size(ctypes.byref(self.cfg))
         if ws == 0:
             raise CgError(CG_ERR_INVALID_VALUE, "invalid configuration")
-        self.V = torch.empty(ss, dtype=torch.uint8, device=dev)
-        self.A = torch.empty(ss // 8, dtype=torch.uint8, device=dev)
+        if self.two_bit:   # NEXT-4: 2-bit states, shard/4 bytes; no A bitmap
+            self.V = torch.empty(ss // 4, dtype=torch.uint8, device=dev)
+            self.A = None
+        else:
+            self.V = torch.empty(ss, dtype=torch.uint8, device=dev)
+            self.A = torch.empty(ss // 8, dtype=torch.uint8, device=dev)
         self.workspace = torch.empty(ws, dtype=torch.uint8, device=dev)
         self.cfg.v_buf = self.V.data_ptr()
-        self.cfg.a_buf = self.A.data_ptr()
+        self.cfg.a_buf = self.A.data_ptr() if self.A is not None else None
         self.cfg.workspace = self.workspace.data_ptr()
         self.cfg.workspace_size = ws
         ctx = ctypes.c_void_p()
@@ -448,8 +459,20 @@ class Checker:
 
     # ---- state download (tests) ---------------------------------------------
     def shadow(self):
+        """(packed A bits, V bytes) of the whole shard in the bytes-format layout"""
         self.torch.cuda.synchronize(self.device)
-        return self.A.cpu().numpy(), self.V.cpu().numpy()
+        if not self.two_bit:
+            return self.A.cpu().numpy(), self.V.cpu().numpy()
+        a, v = self.shadow_read(self.shard_base, self.shard_size)
+        return np.packbits(a, bitorder="little"), v
+
+    def shadow_read(self, addr: int, length: int, stream=None):
+        """cg_host_shadow_read: (addressable 0/1 per byte, V byte per byte)"""
+        a = np.zeros(max(length, 1), np.uint8)
+        v = np.zeros(max(length, 1), np.uint8)
+        self._ok(_lib.cg_host_shadow_read(self.ctx, addr, length, a.ctypes.data, v.ctypes.data, _stream_ptr(stream)),
+                 "cg_host_shadow_read")
+        return a[:length], v[:length]
 
 
 class ConcChecker:

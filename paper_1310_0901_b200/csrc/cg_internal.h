@@ -41,9 +41,15 @@ __device__ __forceinline__ bool fold_side(uint64_t base, uint64_t x, uint64_t y,
 // Host window [wb, we) and the shard [sb, se) whose shadow this GPU stores.
 struct ShadowView {
   uint64_t wb, we, sb, se;
-  uint8_t* V;   // se - sb bytes
-  uint8_t* A;   // (se - sb) / 8 bytes
+  uint8_t* V;   // bytes format: se - sb V bytes; 2-bit format: (se - sb) / 4 state bytes
+  uint8_t* A;   // bytes format: (se - sb) / 8 bytes (unused in the 2-bit format)
+  uint32_t two_bit;   // NEXT-4 compressed shadow (CG_SHADOW_2BIT)
 };
+
+// NEXT-4 2-bit host states (R-36): host byte q <-> bits 2(q&15),
+// 2(q&15)+1 of 32-bit word q>>4.  bit 0 set = some V bit undefined, state 0 =
+// unaddressable (A = 0, V = 0xFF implied).
+constexpr uint32_t kSt2NoAccess = 0u, kSt2Partial = 1u, kSt2Defined = 2u, kSt2Undefined = 3u;
 
 // Allocation table: structure of arrays sorted by (base, alloc_seq), with the
 // running maximum of end addresses.

@@ -251,8 +251,9 @@ __device__ __forceinline__ void load_splitters(const Table& t, uint64_t* s_split
 // 8 host bytes (A only), plus kItemCost per descriptor (its fixed work).
 constexpr uint64_t kItemCost = 256;
 
-__device__ __forceinline__ uint64_t check_host_units(const Norm& nm) {
+__device__ __forceinline__ uint64_t check_host_units(const Norm& nm, bool two_bit) {
   if (!nm.host) return 0;
+  if (two_bit) return (nm.nbytes + 3) >> 2;   // NEXT-4: one state byte per 4 host bytes, both kinds
   return nm.skind == CG_HTOD ? nm.nbytes : (nm.nbytes + 7) >> 3;
 }
 
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(kThreads) k_check_prep(const cg_copy_desc* __r
                                                          uint64_t n, Table t, cg_verdict* __restrict__ out,
                                                          uint64_t* __restrict__ weight,
                                                          ScanMeta* __restrict__ meta,
-                                                         uint64_t* __restrict__ dvoff) {
+                                                         uint64_t* __restrict__ dvoff, int two_bit) {
   extern __shared__ uint64_t s_split[];
   load_splitters(t, s_split);
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -325,7 +326,7 @@ __global__ void __launch_bounds__(kThreads) k_check_prep(const cg_copy_desc* __r
     v.flags = flags;
     v.status = 0;
     out[i] = v;
-    weight[i] = kItemCost + check_host_units(nm);
+    weight[i] = kItemCost + check_host_units(nm, two_bit != 0);
     ScanMeta m;
     m.hstart = nm.hstart;
     m.hpitch = nm.hpitch;
@@ -502,6 +503,7 @@ constexpr int kStages = 3;
 constexpr uint32_t kTileV = 4096;      // HtoD: V bytes per tile
 constexpr uint32_t kTileA = kTileV / 8;
 constexpr uint32_t kDtohBlock = 32768; // DtoH: host bytes per tile (4 KiB of A)
+constexpr uint32_t k2bitBlock = 16384; // NEXT-4 2-bit states: host bytes per tile (4 KiB of states)
 constexpr uint32_t kTileData = 1, kTileHtod = 2, kTileEnd = 4, kTileWhole = 8, kTileFuse = 16, kTileRaw = 32;
 
 struct __align__(16) TileInfo {
@@ -653,6 +655,102 @@ __device__ __forceinline__ void consume_dtoh(const uint8_t* st, uint32_t q0, uin
 }
 
 
+// ---- NEXT-4 2-bit shadow (R-36): 16 host bytes per 32-bit state word ----
+// pair mask of host bytes [lo, hi) in the word whose first host byte is gb
+__device__ __forceinline__ uint32_t pair_mask(uint64_t gb, uint64_t lo, uint64_t hi) {
+  const uint64_t b0 = lo > gb ? umin64(lo - gb, 16) : 0;
+  const uint64_t b1 = hi > gb ? umin64(hi - gb, 16) : 0;
+  if (b1 <= b0) return 0u;
+  const uint32_t him = b1 >= 16 ? 0xffffffffu : ((1u << (2 * b1)) - 1u);
+  return him & ~((1u << (2 * b0)) - 1u);
+}
+
+// one state word: unaddressable = state 0, undefined = bit 0 (PARTIAL / UNDEFINED, always addressable)
+template <bool kHtod>
+__device__ __forceinline__ void word2(uint32_t w, uint32_t m, uint64_t gb, Partial& p) {
+  const uint32_t u = ~(w | (w >> 1)) & 0x55555555u & m;
+  if (u) p.fu = umin64(p.fu, gb + ((__ffs(u) - 1) >> 1));
+  if (kHtod) {
+    const uint32_t und = w & 0x55555555u & m;
+    if (und) {
+      p.fd = umin64(p.fd, gb + ((__ffs(und) - 1) >> 1));
+      p.cnt += __popc(und);
+    }
+  }
+}
+
+// a staged state tile, host bytes [q0, q1): fast fold per 64 host bytes (one
+// LDS.128), per-word masks only for dirty groups and the edge words
+template <bool kHtod>
+__device__ __forceinline__ void consume_2bit(const uint8_t* st, uint32_t q0, uint32_t q1, uint64_t ob, Partial& p) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t* W = reinterpret_cast<const uint32_t*>(st);
+  const uint4* W4 = reinterpret_cast<const uint4*>(st);
+  const uint32_t g0 = (q0 + 63) >> 6, g1 = q1 >> 6;   // full 64-byte groups [g0, g1)
+  const uint32_t e0 = q0 >> 4, e1 = (q1 + 15) >> 4;   // all words touched
+  if (g0 < g1) {
+    uint32_t acc = 0;
+#pragma unroll 4
+    for (uint32_t i = g0 + lane; i < g1; i += 32) {
+      const uint4 v = W4[i];
+      if (kHtod) {
+        acc |= (v.x ^ 0xAAAAAAAAu) | (v.y ^ 0xAAAAAAAAu) | (v.z ^ 0xAAAAAAAAu) | (v.w ^ 0xAAAAAAAAu);
+      } else {
+        acc |= ~((v.x | (v.x >> 1)) & (v.y | (v.y >> 1)) & (v.z | (v.z >> 1)) & (v.w | (v.w >> 1))) & 0x55555555u;
+      }
+    }
+    if (acc)
+      for (uint32_t i = g0 + lane; i < g1; i += 32)
+#pragma unroll
+        for (uint32_t j = 0; j < 4; ++j) word2<kHtod>(W[4 * i + j], 0xffffffffu, ob + 64ull * i + 16 * j, p);
+    if (lane < 4) {
+      const uint32_t k = e0 + lane;
+      if (k < 4 * g0) word2<kHtod>(W[k], pair_mask(16ull * k, q0, q1), ob + 16ull * k, p);
+    } else if (lane < 8) {
+      const uint32_t k = 4 * g1 + (lane - 4);
+      if (k < e1) word2<kHtod>(W[k], pair_mask(16ull * k, q0, q1), ob + 16ull * k, p);
+    }
+  } else {
+    for (uint32_t k = e0 + lane; k < e1; k += 32) word2<kHtod>(W[k], pair_mask(16ull * k, q0, q1), ob + 16ull * k, p);
+  }
+}
+
+// states of host bytes [q0, q1) := pat (0x00000000 NOACCESS, 0xAAAAAAAA DEFINED,
+// 0xFFFFFFFF UNDEFINED); partial words with atomics because a neighbouring
+// range of the same batch may own the other bytes of the word
+__device__ __forceinline__ void fill2_word(uint32_t* S, uint64_t k, uint32_t m, uint32_t pat) {
+  if (m == 0xffffffffu) {
+    S[k] = pat;
+  } else if (m) {
+    if (m & ~pat) atomicAnd(S + k, ~(m & ~pat));
+    if (m & pat) atomicOr(S + k, m & pat);
+  }
+}
+
+__device__ __forceinline__ void warp_fill2(uint8_t* states, uint64_t q0, uint64_t q1, uint32_t pat) {
+  const int lane = threadIdx.x & 31;
+  uint32_t* S = reinterpret_cast<uint32_t*>(states);
+  const uint64_t g0 = (q0 + 63) >> 6, g1 = q1 >> 6, e0 = q0 >> 4, e1 = (q1 + 15) >> 4;
+  if (g0 < g1) {
+    uint4* S4 = reinterpret_cast<uint4*>(states);
+    for (uint64_t i = g0 + lane; i < g1; i += 32) stg_val16(S4 + i, pat);
+    if (lane < 4) {
+      const uint64_t k = e0 + lane;
+      if (k < 4 * g0) fill2_word(S, k, pair_mask(16ull * k, q0, q1), pat);
+    } else if (lane < 8) {
+      const uint64_t k = 4 * g1 + (lane - 4);
+      if (k < e1) fill2_word(S, k, pair_mask(16ull * k, q0, q1), pat);
+    }
+  } else {
+    for (uint64_t k = e0 + lane; k < e1; k += 32) fill2_word(S, k, pair_mask(16ull * k, q0, q1), pat);
+  }
+}
+
+__device__ __forceinline__ void lane_fill2(uint8_t* states, uint64_t q0, uint64_t q1, uint32_t pat) {
+  uint32_t* S = reinterpret_cast<uint32_t*>(states);
+  for (uint64_t k = q0 >> 4; k < (q1 + 15) >> 4; ++k) fill2_word(S, k, pair_mask(16ull * k, q0, q1), pat);
+}
+
 // V := 0 over shard bytes [q0, q1) with the whole warp (16-byte stores, byte
 // stores at the unaligned edges)
 __device__ __forceinline__ void warp_store_zero(uint8_t* V, uint64_t q0, uint64_t q1) {
@@ -709,6 +807,7 @@ struct TileGen {
   uint64_t n, T, nchunks, total;
   uint64_t wb, we, sb, se;
   bool fuse;            // check + apply in one pass (cg_check_apply)
+  bool two_bit;         // NEXT-4 2-bit states: 16 KiB host bytes per tile for both kinds
   // group
   uint64_t w0, w1;
   uint32_t g_pending;   // lane 0
@@ -763,7 +862,10 @@ struct TileGen {
       a = a > kItemCost ? a - kItemCost : 0;
       b = b > kItemCost ? b - kItemCost : 0;
       uint64_t lo = a, hi = b;
-      if (!htod) {
+      if (two_bit) {
+        lo = a << 2;
+        hi = umin64(b << 2, nbytes);
+      } else if (!htod) {
         lo = a << 3;
         hi = umin64(b << 3, nbytes);
       }
@@ -823,7 +925,7 @@ struct TileGen {
     s_fl = fl;
     uint32_t k = 0;
     if (live) {
-      const uint64_t sh = (fl & kTileHtod) ? 12 : 15;   // log2 of the tile block
+      const uint64_t sh = two_bit ? 14 : (fl & kTileHtod) ? 12 : 15;   // log2 of the tile block
       k = (uint32_t)(((q1 - 1) >> sh) - (q0 >> sh) + 1);
     }
     s_k = k;
@@ -929,12 +1031,11 @@ struct TileGen {
     if (lane == owner) {
       const uint32_t j = t - s_excl;
       const bool htod = s_fl & kTileHtod;
-      const uint64_t bmask = htod ? ~(uint64_t)(kTileV - 1) : ~(uint64_t)(kDtohBlock - 1);
-      const uint64_t bsz = htod ? kTileV : kDtohBlock;
-      const uint64_t base = s_q0 & bmask;
+      const uint64_t bsz = two_bit ? k2bitBlock : htod ? kTileV : kDtohBlock;
+      const uint64_t base = s_q0 & ~(bsz - 1);
       const uint64_t tq0 = j ? base + j * bsz : s_q0;
       const uint64_t tq1 = umin64(s_q1, base + (j + 1) * bsz);
-      const uint64_t qa = tq0 & ~127ull;
+      const uint64_t qa = tq0 & (two_bit ? ~63ull : ~127ull);
       TileInfo ti;
       ti.ob = s_ob + qa;
       ti.pend_fu = s_pfu;
@@ -952,8 +1053,15 @@ struct TileGen {
       ti.q0 = (uint32_t)(tq0 - qa);
       ti.q1 = (uint32_t)(tq1 - qa);
       ring.info[s] = ti;
-      const uint32_t span = (ti.q1 + 127u) & ~127u;   // staged host bytes (multiple of 128)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (two_bit) {   // host bytes [qa, qa + span) <-> 16-byte aligned state bytes [qa/4, (qa + span)/4)
+        const uint32_t span = (ti.q1 + 63u) & ~63u;
+        mbar_arrive_tx(&ring.bar[s], span / 4);
+        bulk_g2s(ring.data[s], sv.V + qa / 4, span / 4, &ring.bar[s], policy);
+        ++t;
+        return true;
+      }
+      const uint32_t span = (ti.q1 + 127u) & ~127u;   // staged host bytes (multiple of 128)
       if (f & kTileHtod) {
         mbar_arrive_tx(&ring.bar[s], span + span / 8);
         bulk_g2s(ring.data[s], sv.V + qa, span, &ring.bar[s], policy);
@@ -1000,6 +1108,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
   gen.sb = sv.sb;
   gen.se = sv.se;
   gen.fuse = fuse != 0;
+  gen.two_bit = sv.two_bit != 0;
   gen.g_pending = lane == 0 ? atomicAdd(counter, 1u) : 0;
   gen.phase = kPhaseGroup;
   gen.wbase = ~0ull >> 1;   // no window yet
@@ -1017,8 +1126,14 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
     phase ^= 1u << s;
     const TileInfo t = ring.info[s];
     if (t.flags & kTileData) {
-      if (t.flags & kTileHtod) consume_htod(ring.data[s], t.q0, t.q1, t.ob, p);
-      else consume_dtoh(ring.data[s], t.q0, t.q1, t.ob, p);
+      if (gen.two_bit) {
+        if (t.flags & kTileHtod) consume_2bit<true>(ring.data[s], t.q0, t.q1, t.ob, p);
+        else consume_2bit<false>(ring.data[s], t.q0, t.q1, t.ob, p);
+      } else if (t.flags & kTileHtod) {
+        consume_htod(ring.data[s], t.q0, t.q1, t.ob, p);
+      } else {
+        consume_dtoh(ring.data[s], t.q0, t.q1, t.ob, p);
+      }
     }
     if (t.flags & kTileEnd) {
       p.fu = umin64(p.fu, t.pend_fu);
@@ -1053,7 +1168,10 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
       }
       p = Partial{kNone, kNone, 0};
       // fused a6: a whole contiguous DtoH piece with status OK becomes defined
-      if (__shfl_sync(kFull, apply, 0)) warp_store_zero(sv.V, t.qs, t.qe);
+      if (__shfl_sync(kFull, apply, 0)) {
+        if (gen.two_bit) warp_fill2(sv.V, t.qs, t.qe, 0xAAAAAAAAu);
+        else warp_store_zero(sv.V, t.qs, t.qe);
+      }
     }
     __syncwarp();
     if (!gen.next(ring, s, sv, policy)) --left;
@@ -1256,7 +1374,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(const ScanMeta* __restrict__
             if (y0 < y1) {
               qs = y0 - sv.sb;
               qe = y1 - sv.sb;
-              small = qe - qs <= 2 * kZeroPage;
+              small = qe - qs <= (sv.two_bit ? 256u : 2 * kZeroPage);
               big = !small;
             }
           } else {
@@ -1264,14 +1382,19 @@ __global__ void __launch_bounds__(kThreads) k_apply(const ScanMeta* __restrict__
           }
         }
       }
-      if (small) lane_zero(sv.V, qs, qe, zeros);
+      if (small) {
+        if (sv.two_bit) lane_fill2(sv.V, qs, qe, 0xAAAAAAAAu);
+        else lane_zero(sv.V, qs, qe, zeros);
+      }
       uint32_t todo = __ballot_sync(kFull, big);
       while (todo) {
         const int src = __ffs(todo) - 1;
         todo &= todo - 1;
         const uint64_t s_info = __shfl_sync(kFull, m.info, src);
         if ((s_info >> 43) & 1u) {
-          warp_zero(sv.V, __shfl_sync(kFull, qs, src), __shfl_sync(kFull, qe, src), zeros);
+          const uint64_t a = __shfl_sync(kFull, qs, src), b = __shfl_sync(kFull, qe, src);
+          if (sv.two_bit) warp_fill2(sv.V, a, b, 0xAAAAAAAAu);
+          else warp_zero(sv.V, a, b, zeros);
         } else {
           const uint64_t x0 = __shfl_sync(kFull, m.hstart, src), pitch = __shfl_sync(kFull, m.hpitch, src);
           const uint64_t W = __shfl_sync(kFull, m.W, src);
@@ -1282,7 +1405,10 @@ __global__ void __launch_bounds__(kThreads) k_apply(const ScanMeta* __restrict__
             const uint64_t len = umin64(W - c, h - o);
             const uint64_t x = x0 + r * pitch + c;
             const uint64_t y0 = umax64(x, sv.sb), y1 = umin64(x + len, sv.se);
-            if (y0 < y1) warp_zero(sv.V, y0 - sv.sb, y1 - sv.sb, zeros);
+            if (y0 < y1) {
+              if (sv.two_bit) warp_fill2(sv.V, y0 - sv.sb, y1 - sv.sb, 0xAAAAAAAAu);
+              else warp_zero(sv.V, y0 - sv.sb, y1 - sv.sb, zeros);
+            }
             o += len;
             ++r;
             c = 0;
@@ -1563,8 +1689,13 @@ __global__ void __launch_bounds__(kThreads) k_mark(const cg_mark* __restrict__ m
       const uint64_t x = mk.addr + a, end = mk.addr + b;
       const uint64_t y0 = umax64(x, sv.sb), y1 = umin64(end, sv.se);
       if (y0 >= y1) continue;
-      fill_v(sv, y0 - sv.sb, y1 - sv.sb, mk.state == CG_DEFINED ? 0x00u : 0xFFu);
-      put_abits(sv, y0 - sv.sb, y1 - sv.sb, mk.state != CG_NOACCESS);
+      if (sv.two_bit) {
+        warp_fill2(sv.V, y0 - sv.sb, y1 - sv.sb,
+                   mk.state == CG_DEFINED ? 0xAAAAAAAAu : mk.state == CG_UNDEFINED ? 0xFFFFFFFFu : 0u);
+      } else {
+        fill_v(sv, y0 - sv.sb, y1 - sv.sb, mk.state == CG_DEFINED ? 0x00u : 0xFFu);
+        put_abits(sv, y0 - sv.sb, y1 - sv.sb, mk.state != CG_NOACCESS);
+      }
     }
   }
 }
@@ -1573,7 +1704,9 @@ __global__ void k_setv_check(ShadowView sv, uint64_t addr, uint64_t len, uint32_
   const uint64_t y0 = umax64(addr, sv.sb), y1 = umin64(addr + len, sv.se);
   for (uint64_t q = y0 - sv.sb + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < y1 - sv.sb;
        q += (uint64_t)gridDim.x * blockDim.x)
-    if (!((sv.A[q >> 3] >> (q & 7)) & 1)) atomicOr(flag, 1u);
+    if (sv.two_bit ? ((reinterpret_cast<const uint32_t*>(sv.V)[q >> 4] >> (2 * (q & 15))) & 3u) == kSt2NoAccess
+                   : !((sv.A[q >> 3] >> (q & 7)) & 1))
+      atomicOr(flag, 1u);
 }
 
 // ---------------------------------------------------------------------------
@@ -1717,7 +1850,7 @@ cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_
   ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
   L.stage(CG_STAGE_CHECK_PREP, true, s);
   k_check_prep<<<blocks_for(n, kThreads, L.num_sms * 4), kThreads, smem, s>>>(d, n, t, out, p.weight, meta,
-                                                                              p.dvoff);
+                                                                              p.dvoff, (int)sv.two_bit);
   *L.counter += 1;
   L.stage(CG_STAGE_CHECK_PREP, false, s);
   L.stage(CG_STAGE_CHECK_PLAN, true, s);
@@ -1780,6 +1913,11 @@ cudaError_t mark_batch(const Launch& L, const cg_mark* d_marks, uint64_t n, cons
 }
 
 cudaError_t fresh_shadow(const Launch& L, const ShadowView& sv, cudaStream_t s) {
+  if (sv.two_bit) {   // every state NOACCESS
+    k_fill<<<L.num_sms * 8, kThreads, 0, s>>>(reinterpret_cast<uint4*>(sv.V), (sv.se - sv.sb) / 64, 0u);
+    *L.counter += 1;
+    return cudaGetLastError();
+  }
   const uint64_t nv = (sv.se - sv.sb) / 16, na = (sv.se - sv.sb) / 128;
   k_fill<<<L.num_sms * 8, kThreads, 0, s>>>(reinterpret_cast<uint4*>(sv.V), nv, 0xffffffffu);
   if (na) k_fill<<<L.num_sms * 8, kThreads, 0, s>>>(reinterpret_cast<uint4*>(sv.A), na, 0u);

@@ -53,6 +53,8 @@ bool valid_config(const cg_config* c) {
   if (sb < c->host_base || sb + ss > c->host_base + c->host_size) return false;
   if (c->max_descs == 0 || c->max_descs > cgk::kMaxDescs) return false;
   if (c->max_allocs == 0 || c->max_allocs > (1ull << 32)) return false;
+  if (c->shadow_format != CG_SHADOW_BYTES && c->shadow_format != CG_SHADOW_2BIT) return false;
+  if (c->shadow_format == CG_SHADOW_2BIT && c->dev_vbuf) return false;   // NEXT-1 needs exact host V-bytes
   if (c->dev_vbuf && (c->dev_vsize == 0 || c->dev_vsize % 16 || (c->shard_size && (c->shard_base != c->host_base ||
                                                               c->shard_size != c->host_size))))
     return false;   // NEXT-1 tracking needs a pool and an unsharded context
@@ -117,6 +119,7 @@ struct cg_ctx {
   std::vector<Entry> table;                 // sorted by (base, aseq)
   std::map<uint64_t, uint64_t> live;        // base -> end of live allocations
   std::vector<ArrayEntry> arrays;           // NEXT-3: sorted by (handle, aseq)
+  std::map<uint64_t, uint8_t> partial;      // NEXT-4 2-bit format: exact V-bytes of PARTIAL host bytes
   std::map<uint64_t, uint64_t> live_arrays; // handle -> total bytes
   uint64_t last_seq = 0;
   bool dirty = true;
@@ -284,9 +287,10 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
   *out = nullptr;
   if (!valid_config(cfg)) return CG_ERR_INVALID_VALUE;
   const Layout lay = layout_of(cfg);
-  if (!cfg->v_buf || !cfg->a_buf || !cfg->workspace) return CG_ERR_INVALID_VALUE;
+  const bool two_bit = cfg->shadow_format == CG_SHADOW_2BIT;
+  if (!cfg->v_buf || (!two_bit && !cfg->a_buf) || !cfg->workspace) return CG_ERR_INVALID_VALUE;
   if (cfg->workspace_size < lay.total) return CG_ERR_INVALID_VALUE;
-  if ((uintptr_t)cfg->v_buf % 16 || (uintptr_t)cfg->a_buf % 16 || (uintptr_t)cfg->workspace % kAlign)
+  if ((uintptr_t)cfg->v_buf % 16 || (!two_bit && (uintptr_t)cfg->a_buf % 16) || (uintptr_t)cfg->workspace % kAlign)
     return CG_ERR_INVALID_VALUE;
   DeviceGuard g(cfg->device);
   cg_ctx* c = new cg_ctx();
@@ -298,7 +302,8 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
   c->sv.sb = cfg->shard_size ? cfg->shard_base : cfg->host_base;
   c->sv.se = c->sv.sb + (cfg->shard_size ? cfg->shard_size : cfg->host_size);
   c->sv.V = static_cast<uint8_t*>(cfg->v_buf);
-  c->sv.A = static_cast<uint8_t*>(cfg->a_buf);
+  c->sv.A = two_bit ? nullptr : static_cast<uint8_t*>(cfg->a_buf);
+  c->sv.two_bit = two_bit ? 1u : 0u;
   cudaDeviceProp prop;
   cudaError_t e = cudaGetDeviceProperties(&prop, cfg->device);
   if (e != cudaSuccess) {
@@ -518,9 +523,71 @@ cg_status cg_host_set_vbits(cg_ctx* c, uint64_t addr, uint64_t len, const uint8_
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return c->cuda(e, "set_vbits check");
   if (h_flag) return c->fail(CG_ERR_INVALID_VALUE, "set_vbits on unaddressable bytes");
+  if (c->sv.two_bit) {   // NEXT-4: read-modify-write the state words; exact partial V-bytes go to the host table
+    const uint64_t q0 = y0 - c->sv.sb, q1 = y1 - c->sv.sb, k0 = q0 >> 4, k1 = (q1 + 15) >> 4;
+    std::vector<uint32_t> w(k1 - k0);
+    uint32_t* S = reinterpret_cast<uint32_t*>(c->sv.V);
+    e = cudaMemcpyAsync(w.data(), S + k0, w.size() * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return c->cuda(e, "set_vbits read");
+    for (uint64_t q = q0; q < q1; ++q) {
+      const uint8_t v = h_vbytes[q - q0 + (y0 - addr)];
+      const uint32_t st = v == 0x00 ? cgk::kSt2Defined : v == 0xFF ? cgk::kSt2Undefined : cgk::kSt2Partial;
+      uint32_t& x = w[(q >> 4) - k0];
+      const int sh = 2 * (int)(q & 15);
+      x = (x & ~(3u << sh)) | (st << sh);
+      if (st == cgk::kSt2Partial) c->partial[q + c->sv.sb] = v;
+      else c->partial.erase(q + c->sv.sb);
+    }
+    e = cudaMemcpyAsync(S + k0, w.data(), w.size() * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    return c->cuda(e, "set_vbits write");
+  }
   e = cudaMemcpyAsync(c->sv.V + (y0 - c->sv.sb), h_vbytes + (y0 - addr), y1 - y0, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   return c->cuda(e, "set_vbits copy");
+}
+
+cg_status cg_host_shadow_read(cg_ctx* c, uint64_t addr, uint64_t len, uint8_t* h_a, uint8_t* h_v, void* stream) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (len == 0) return CG_OK;
+  if (addr < c->sv.sb || addr > c->sv.se || len > c->sv.se - addr)
+    return c->fail(CG_ERR_INVALID_VALUE, "shadow read outside this context's shard");
+  DeviceGuard g(c->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint64_t q0 = addr - c->sv.sb, q1 = q0 + len;
+  cudaError_t e = cudaSuccess;
+  if (c->sv.two_bit) {
+    const uint64_t k0 = q0 >> 4, k1 = (q1 + 15) >> 4;
+    std::vector<uint32_t> w(k1 - k0);
+    e = cudaMemcpyAsync(w.data(), reinterpret_cast<uint32_t*>(c->sv.V) + k0, w.size() * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return c->cuda(e, "shadow read");
+    for (uint64_t q = q0; q < q1; ++q) {
+      const uint32_t st = (w[(q >> 4) - k0] >> (2 * (q & 15))) & 3u;
+      if (h_a) h_a[q - q0] = st != cgk::kSt2NoAccess;
+      if (h_v) {
+        uint8_t v = st == cgk::kSt2Defined ? 0x00 : 0xFF;
+        if (st == cgk::kSt2Partial) {
+          auto it = c->partial.find(q + c->sv.sb);
+          v = it != c->partial.end() ? it->second : 0xFF;
+        }
+        h_v[q - q0] = v;
+      }
+    }
+    return CG_OK;
+  }
+  if (h_v) e = cudaMemcpyAsync(h_v, c->sv.V + q0, len, cudaMemcpyDeviceToHost, s);
+  std::vector<uint8_t> a;
+  if (e == cudaSuccess && h_a) {
+    a.resize((q1 + 7) / 8 - q0 / 8);
+    e = cudaMemcpyAsync(a.data(), c->sv.A + q0 / 8, a.size(), cudaMemcpyDeviceToHost, s);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return c->cuda(e, "shadow read");
+  if (h_a)
+    for (uint64_t q = q0; q < q1; ++q) h_a[q - q0] = (a[q / 8 - q0 / 8] >> (q & 7)) & 1u;
+  return CG_OK;
 }
 
 cg_status cg_host_query_addressable(cg_ctx* c, uint64_t addr, uint64_t len, uint32_t* all_addressable, void* stream) {

@@ -22,11 +22,11 @@ def cg():
     return m
 
 
-def run_sharded(cg, tr, world, fuse=True):
+def run_sharded(cg, tr, world, fuse=True, **kw):
     from paper_1310_0901_b200.sharded import LoopbackGroup, replay_sharded
     o, ov, os_, oleaks = oracle.replay_trace(tr)
     nreg = max(int(np.count_nonzero(tr.events["op"] == tg.OP_REG)), 1024)
-    grp = LoopbackGroup(tr.host_base, tr.host_size, world, max_descs=max(tr.n_copies, 1024), max_allocs=nreg)
+    grp = LoopbackGroup(tr.host_base, tr.host_size, world, max_descs=max(tr.n_copies, 1024), max_allocs=nreg, **kw)
     gv, gs = replay_sharded(grp, tr.events, tr.blob, fuse=fuse)
     for f in ov.dtype.names:
         bad = np.flatnonzero(gv[f] != ov[f])
