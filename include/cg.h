@@ -502,6 +502,20 @@ uint64_t cg_format_verdict(const cg_verdict *v, uint32_t kind, char *buf, uint64
 /* "Warning: Device memory leak of <size> bytes."; as above. */
 uint64_t cg_format_leak(const cg_alloc_record *r, char *buf, uint64_t cap);
 
+/* NEXT-4 ERROR SUMMARY (Listing 4 P:219 for the shape):
+ * counts the diagnostics of n verdicts on the device -- one per set flag;
+ * HOST_UNDEFINED (unless undef_is_error) and CONCURRENT are Warnings,
+ * every other flag an Error.  d_counts: device array of 2 uint64
+ * {errors, warnings}, overwritten.  Stateless, asynchronous on stream.
+ * Registry errors (InvalidFree) and leaks are counted by the caller from the
+ * call statuses and cg_leak_report.  Errors: CG_ERR_INVALID_VALUE, CG_ERR_CUDA. */
+cg_status cg_summarize(const cg_verdict *d_verdicts, uint64_t n, uint32_t undef_is_error, uint64_t *d_counts,
+                       void *stream);
+
+/* "ERROR SUMMARY: <e> errors, <w> warnings (<s> suppressed)\n";
+ * returns the length, writes at most cap-1 bytes + NUL. */
+uint64_t cg_format_summary(uint64_t errors, uint64_t warnings, uint64_t suppressed, char *buf, uint64_t cap);
+
 /* Number of kernels this context has launched so far (for bench accounting). */
 uint64_t cg_kernel_launches(const cg_ctx *ctx);
 

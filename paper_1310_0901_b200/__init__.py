@@ -118,6 +118,8 @@ def _load() -> ctypes.CDLL:
         "cg_free_array": (I, [P, U64, U64]),
         "cg_array_report": (I, [P, P, U64, P]),
         "cg_host_shadow_read": (I, [P, U64, U64, P, P, P]),
+        "cg_summarize": (I, [P, U64, U32, P, P]),
+        "cg_format_summary": (U64, [U64, U64, U64, P, U64]),
         "cg_conc_create": (I, [I, U64, U64, P]),
         "cg_conc_destroy": (I, [P]),
         "cg_conc_last_error": (ctypes.c_char_p, [P]),
@@ -141,7 +143,7 @@ EXPORTED = ("cg_workspace_size", "cg_ctx_create", "cg_ctx_destroy", "cg_last_err
             "cg_batch_disjoint", "cg_straddler_pack", "cg_straddler_finalize", "cg_compact_dirty", "cg_shard_plan",
             "cg_host_query_addressable", "cg_expand_copy1d", "cg_check_host", "cg_format_verdict",
             "cg_format_leak", "cg_apply_copies", "cg_device_vbits", "cg_plan_batches_propagate",
-            "cg_host_shadow_read", "cg_array_bytes", "cg_register_array", "cg_free_array", "cg_array_report", "cg_conc_create",
+            "cg_host_shadow_read", "cg_summarize", "cg_format_summary", "cg_array_bytes", "cg_register_array", "cg_free_array", "cg_array_report", "cg_conc_create",
             "cg_conc_destroy", "cg_conc_last_error", "cg_conc_sync", "cg_conc_check", "cg_conc_stamps",
             "cg_conc_kernel_launches")
 
@@ -173,6 +175,27 @@ cg_device_vbits = _lib.cg_device_vbits
 cg_plan_batches_propagate = _lib.cg_plan_batches_propagate
 cg_array_bytes = _lib.cg_array_bytes
 cg_host_shadow_read = _lib.cg_host_shadow_read
+cg_summarize = _lib.cg_summarize
+cg_format_summary = _lib.cg_format_summary
+
+
+def summarize(d_verdicts, undef_is_error: bool = False, stream=None):
+    """NEXT-4: (errors, warnings) of the verdicts in a CUDA uint8 tensor"""
+    import torch
+    n = d_verdicts.numel() // VERDICT_DTYPE.itemsize
+    out = torch.zeros(2, dtype=torch.int64, device=d_verdicts.device)
+    st = _lib.cg_summarize(d_verdicts.data_ptr(), n, int(undef_is_error), out.data_ptr(), _stream_ptr(stream))
+    if st:
+        raise CgError(st, "cg_summarize")
+    e, w = out.cpu().tolist()
+    return int(e), int(w)
+
+
+def format_summary(errors: int, warnings: int, suppressed: int = 0) -> str:
+    k = _lib.cg_format_summary(errors, warnings, suppressed, None, 0)
+    buf = ctypes.create_string_buffer(k + 1)
+    _lib.cg_format_summary(errors, warnings, suppressed, buf, k + 1)
+    return buf.value.decode()
 CG_SHADOW_BYTES, CG_SHADOW_2BIT = 0, 1
 cg_register_array = _lib.cg_register_array
 cg_free_array = _lib.cg_free_array

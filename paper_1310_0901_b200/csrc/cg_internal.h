@@ -132,6 +132,8 @@ cudaError_t expand_1d(const Launch& L, const cg_copy1d* in, uint64_t n, cg_copy_
 cudaError_t mark_batch(const Launch& L, const cg_mark* d_marks, uint64_t n, const ShadowView& sv,
                        const Plan& p, cudaStream_t s);
 cudaError_t fresh_shadow(const Launch& L, const ShadowView& sv, cudaStream_t s);
+cudaError_t summarize(const cg_verdict* v, uint64_t n, uint32_t warn_mask, unsigned long long* d_counts,
+                      cudaStream_t s);
 cudaError_t setv_check(const Launch& L, uint64_t addr, uint64_t len, const ShadowView& sv,
                        uint32_t* d_flag, cudaStream_t s);
 cudaError_t leak_sweep(const Launch& L, const Table& t, const Plan& p, cg_alloc_record* out,

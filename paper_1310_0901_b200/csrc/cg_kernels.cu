@@ -1710,6 +1710,25 @@ __global__ void k_setv_check(ShadowView sv, uint64_t addr, uint64_t len, uint32_
 }
 
 // ---------------------------------------------------------------------------
+// NEXT-4: ERROR SUMMARY counts: one diagnostic per set flag
+// ---------------------------------------------------------------------------
+__global__ void k_summary(const cg_verdict* __restrict__ v, uint64_t n, uint32_t warn_mask,
+                          unsigned long long* __restrict__ counts) {
+  uint64_t e = 0, w = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t f = v[i].flags;
+    e += __popc(f & ~warn_mask);
+    w += __popc(f & warn_mask);
+  }
+  e = warp_sum(e);
+  w = warp_sum(w);
+  if ((threadIdx.x & 31) == 0 && (e | w)) {
+    atomicAdd(counts, (unsigned long long)e);
+    atomicAdd(counts + 1, (unsigned long long)w);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // e: straddler exchange (descriptors whose host range spans several shards)
 // ---------------------------------------------------------------------------
 // Raw partials of m straddlers -> structure of arrays for three collectives:
@@ -1909,6 +1928,15 @@ cudaError_t mark_batch(const Launch& L, const cg_mark* d_marks, uint64_t n, cons
   if (e != cudaSuccess) return e;
   k_mark<<<L.persist_blocks, kThreads, 0, s>>>(d_marks, n, p.P, p.chunk_first, p.t_min, p.max_chunks, sv);
   *L.counter += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t summarize(const cg_verdict* v, uint64_t n, uint32_t warn_mask, unsigned long long* d_counts,
+                      cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(d_counts, 0, 2 * sizeof(unsigned long long), s);
+  if (e != cudaSuccess || n == 0) return e;
+  k_summary<<<(unsigned)std::min<uint64_t>((n + kThreads - 1) / kThreads, 148 * 8), kThreads, 0, s>>>(v, n, warn_mask,
+                                                                                               d_counts);
   return cudaGetLastError();
 }
 

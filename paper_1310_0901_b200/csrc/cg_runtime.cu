@@ -406,6 +406,27 @@ uint64_t cg_format_verdict(const cg_verdict* v, uint32_t kind, char* buf, uint64
   return t.size();
 }
 
+cg_status cg_summarize(const cg_verdict* d_verdicts, uint64_t n, uint32_t undef_is_error, uint64_t* d_counts,
+                       void* stream) {
+  if (!d_counts || (n && !d_verdicts)) return CG_ERR_INVALID_VALUE;
+  const uint32_t warn = CG_F_CONCURRENT | (undef_is_error ? 0u : (uint32_t)CG_F_HOST_UNDEFINED);
+  cudaError_t e = cgk::summarize(d_verdicts, n, warn, reinterpret_cast<unsigned long long*>(d_counts),
+                                 static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? CG_OK : CG_ERR_CUDA;
+}
+
+uint64_t cg_format_summary(uint64_t errors, uint64_t warnings, uint64_t suppressed, char* buf, uint64_t cap) {
+  char line[160];
+  const int k = snprintf(line, sizeof line, "ERROR SUMMARY: %llu errors, %llu warnings (%llu suppressed)\n",
+                         (unsigned long long)errors, (unsigned long long)warnings, (unsigned long long)suppressed);
+  if (cap && buf) {
+    const uint64_t m = std::min<uint64_t>((uint64_t)k, cap - 1);
+    std::memcpy(buf, line, m);
+    buf[m] = 0;
+  }
+  return (uint64_t)k;
+}
+
 uint64_t cg_format_leak(const cg_alloc_record* r, char* buf, uint64_t cap) {
   if (!r) return 0;
   char line[128];

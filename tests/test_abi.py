@@ -255,3 +255,9 @@ def test_array_format_text(cg):
                                                 "Expected 100 allocated bytes but only found 24.\n")
     v["flags"] = cg.CG_F_SRC_NOT_ALLOCATED
     assert cg.format_verdict(v, cg.CG_ATOH) == "Error: Source device array of array->host copy is not allocated.\n"
+
+
+def test_error_summary_line(cg):
+    """1 error, 0 suppressions -> "ERROR SUMMARY: 1 errors, 0 warnings (0 suppressed)" """
+    assert cg.format_summary(1, 0, 0) == "ERROR SUMMARY: 1 errors, 0 warnings (0 suppressed)\n"
+    assert cg.format_summary(12, 345, 6) == "ERROR SUMMARY: 12 errors, 345 warnings (6 suppressed)\n"

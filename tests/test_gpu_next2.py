@@ -106,3 +106,19 @@ def test_map_capacity_error(cg):
     assert e.value.status == cg.CG_ERR_OUT_OF_MEMORY
     conc.close()
     chk.close()
+
+
+@pytest.mark.parametrize("uie", [False, True])
+def test_error_summary_counts(cg, uie):
+    """NEXT-4 cg_summarize: one diagnostic per set flag; HOST_UNDEFINED (unless
+    undef_is_error) and CONCURRENT are the Warnings"""
+    import torch
+    tr = tg.with_threads(tg.c2_small(n_copies=20000, n_allocs=2000), 4)
+    o, ov, _, _ = oracle.replay_trace(tr, undef_is_error=uie, concurrency=True)
+    d = torch.from_numpy(ov.view(np.uint8).copy()).cuda()
+    e, w = cg.summarize(d, undef_is_error=uie)
+    f = ov["flags"].astype(np.uint64)
+    bits = np.array([[(int(x) >> b) & 1 for b in range(10)] for x in f])
+    warn = [5, 9] if not uie else [9]
+    assert w == int(bits[:, warn].sum()) and e == int(bits.sum()) - w
+    assert w > 0 and e > 0
