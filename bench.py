@@ -216,9 +216,10 @@ def run_ours(args, rank, world, device):
 
     torch.cuda.set_device(device)
     tr = make_workload(args.config, rank, args.scale)
-    two_bit = args.shadow == "2bit"
+    two_bit = args.shadow in ("2bit", "sparse")
     chk, descs, t_setup, nreg = setup_checker(cg, tr, device, host_staging=not args.no_e2e, rank=rank, world=world,
-                                              track=args.track, shadow_format=1 if two_bit else 0)
+                                              track=args.track,
+                                              shadow_format={"bytes": 0, "2bit": 1, "sparse": 2}[args.shadow])
     n = len(descs)
     stream = torch.cuda.current_stream()
     d_descs = cg.to_device_descs(descs, device)
@@ -347,7 +348,8 @@ def run_ours(args, rank, world, device):
     scan_bytes = check_b + (fused_apply_bytes(descs, verd, max(n, 1024), two_bit) if fused else 0.0)
     achieved = scan_bytes / (scan_avg * 1e-3) / 1e9
     traffic = None
-    prof_json = os.path.join(ROOT, "profiles", f"ncu_{args.config}{'_2bit' if two_bit else ''}_check_scan.json")
+    suffix = "" if args.shadow == "bytes" else "_" + args.shadow
+    prof_json = os.path.join(ROOT, "profiles", f"ncu_{args.config}{suffix}_check_scan.json")
     if os.path.exists(prof_json):
         with open(prof_json) as f:
             pj = json.load(f)
@@ -364,7 +366,8 @@ def run_ours(args, rank, world, device):
                    "shadow_bytes_per_step": bytes_per_step, "check_bytes": check_b, "apply_bytes": apply_b,
                    "l2": "no flush: >= 8.5 GB of shadow streamed per step vs 126 MB L2",
                    "parallelism": f"host-range shards x{world}",
-                   "shadow_format": "2-bit states (NEXT-4)" if two_bit else "V bytes + A bits",
+                   "shadow_format": {"bytes": "V bytes + A bits", "2bit": "2-bit states (NEXT-4)",
+                                     "sparse": "2-bit states in the two-level sparse map (NEXT-4)"}[args.shadow],
                    "entry": ("cg_check_copies + cg_apply_copies (NEXT-1 V-bit propagation)" if args.track else
                              "cg_check_apply (fused)" if fused else "cg_check_copies + cg_apply_dtoh")},
         "descriptors_per_s": world * n / (ms_step * 1e-3),
@@ -494,7 +497,7 @@ def main():
     ap.add_argument("--unfused", action="store_true", help="check and apply as two calls")
     ap.add_argument("--track", action="store_true", help="NEXT-1 device V-bit tracking (apply = propagation)")
     ap.add_argument("--conc", type=int, default=0, help="NEXT-2: also time cg_conc_check with this many threads")
-    ap.add_argument("--shadow", default="bytes", choices=["bytes", "2bit"],
+    ap.add_argument("--shadow", default="bytes", choices=["bytes", "2bit", "sparse"],
                     help="host shadow format: V bytes + A bits, or NEXT-4 2-bit states")
     args = ap.parse_args()
     assert args.warmup >= 1

@@ -185,8 +185,16 @@ typedef struct {
  *    host-side table for cg_host_shadow_read; the checks only need "some bit
  *    undefined", which the state holds (R-36).  The scan then reads
  *    0.25 B per host byte for both kinds and the DtoH apply writes 0.25 B.
- *    Not combinable with dev_vbuf. */
-enum { CG_SHADOW_BYTES = 0, CG_SHADOW_2BIT = 1 };
+ *    Not combinable with dev_vbuf.
+ *    CG_SHADOW_SPARSE (2) = the same states in a Memcheck-style two-level map
+ *    over the whole 64-bit host address space: 64 KiB host chunks, each with
+ *    a 16 KiB secondary of states allocated on first mark (a chunk without one
+ *    is NOACCESS).  host_base must be 0 and host_size is the capacity in host
+ *    bytes (a multiple of 65536): v_buf holds host_size/65536 + 1 secondaries
+ *    (the first is the distinguished NOACCESS one).  Every host address is
+ *    then "in the window"; marks that need more secondaries than the capacity
+ *    fail with CG_ERR_OUT_OF_MEMORY.  Unsharded, no dev_vbuf. */
+enum { CG_SHADOW_BYTES = 0, CG_SHADOW_2BIT = 1, CG_SHADOW_SPARSE = 2 };
 
 typedef struct {
   uint64_t host_base, host_size;

@@ -196,7 +196,7 @@ def format_summary(errors: int, warnings: int, suppressed: int = 0) -> str:
     buf = ctypes.create_string_buffer(k + 1)
     _lib.cg_format_summary(errors, warnings, suppressed, buf, k + 1)
     return buf.value.decode()
-CG_SHADOW_BYTES, CG_SHADOW_2BIT = 0, 1
+CG_SHADOW_BYTES, CG_SHADOW_2BIT, CG_SHADOW_SPARSE = 0, 1, 2
 cg_register_array = _lib.cg_register_array
 cg_free_array = _lib.cg_free_array
 cg_array_report = _lib.cg_array_report
@@ -290,19 +290,31 @@ class Checker:
     def __init__(self, host_base: int, host_size: int, *, max_descs: int = 1 << 20,
                  max_allocs: int = 1 << 18, undef_is_error: bool = False, device: int = 0,
                  shard_base: int = 0, shard_size: int = 0, host_staging: bool = False, dev_vsize: int = 0,
-                 shadow_format: int = 0):
+                 shadow_format: int = 0, sparse_capacity: int = 0):
+        """shadow_format CG_SHADOW_SPARSE: the library map covers the whole
+        64-bit host space with room for sparse_capacity host bytes (default:
+        host_size + 128 KiB, rounded to 64 KiB); host_base / host_size then
+        only name the window shadow() reads back."""
         import torch
         self.torch = torch
         self.device = device
         dev = torch.device("cuda", device)
         ss = shard_size or host_size
+        self.sparse = shadow_format == CG_SHADOW_SPARSE
+        self.view = (host_base, host_size)
+        if self.sparse:
+            cap = sparse_capacity or host_size + (128 << 10)
+            cap = (cap + 65535) // 65536 * 65536
+            host_base, host_size, shard_base, shard_size = 0, cap, 0, 0
         self.cfg = cg_config(host_base=host_base, host_size=host_size, shard_base=shard_base,
                              shard_size=shard_size, max_descs=max_descs, max_allocs=max_allocs,
                              undef_is_error=int(undef_is_error), host_staging=int(host_staging),
                              device=device, shadow_format=shadow_format)
-        self.two_bit = shadow_format == CG_SHADOW_2BIT
+        self.two_bit = shadow_format in (CG_SHADOW_2BIT, CG_SHADOW_SPARSE)
         self.shard_base = shard_base if shard_size else host_base
         self.shard_size = ss
+        if self.sparse:
+            self.shard_base, self.shard_size = self.view
         self.tracking = dev_vsize > 0
         if self.tracking:   # NEXT-1 device V-bit pool
             dev_vsize = (dev_vsize + 15) // 16 * 16
@@ -312,7 +324,10 @@ class Checker:
         ws = _lib.cg_workspace_size(ctypes.byref(self.cfg))
         if ws == 0:
             raise CgError(CG_ERR_INVALID_VALUE, "invalid configuration")
-        if self.two_bit:   # NEXT-4: 2-bit states, shard/4 bytes; no A bitmap
+        if self.sparse:    # NEXT-4: secondaries of 16 KiB states, the first one distinguished
+            self.V = torch.empty((host_size // 65536 + 1) * 16384, dtype=torch.uint8, device=dev)
+            self.A = None
+        elif self.two_bit:   # NEXT-4: 2-bit states, shard/4 bytes; no A bitmap
             self.V = torch.empty(ss // 4, dtype=torch.uint8, device=dev)
             self.A = None
         else:

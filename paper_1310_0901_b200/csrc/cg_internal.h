@@ -43,8 +43,23 @@ struct ShadowView {
   uint64_t wb, we, sb, se;
   uint8_t* V;   // bytes format: se - sb V bytes; 2-bit format: (se - sb) / 4 state bytes
   uint8_t* A;   // bytes format: (se - sb) / 8 bytes (unused in the 2-bit format)
-  uint32_t two_bit;   // NEXT-4 compressed shadow (CG_SHADOW_2BIT)
+  uint32_t two_bit;   // NEXT-4 compressed shadow (CG_SHADOW_2BIT, CG_SHADOW_SPARSE)
+  // NEXT-4 sparse two-level map (CG_SHADOW_SPARSE): host byte q lives in the
+  // 64 KiB chunk q >> 16, whose 16 KiB of states is secondary dir(chunk) of V
+  // (secondary 0 = the distinguished all-NOACCESS one, never written); the
+  // directory is an open-addressing table, Fibonacci-hashed, linear probing
+  uint32_t sparse;
+  uint32_t dir_bits;        // log2 of the slot count
+  const uint64_t* dir_key;  // chunk + 1, 0 = empty slot
+  const uint32_t* dir_val;  // secondary index
+  uint64_t v_bytes;         // size of V (fresh-shadow fill)
 };
+
+constexpr uint64_t kChunkShift = 16;               // 64 KiB host bytes per chunk
+constexpr uint64_t kSecondaryBytes = 1ull << 14;   // their 2-bit states
+__host__ __device__ __forceinline__ uint64_t dir_hash(uint64_t chunk, uint32_t bits) {
+  return (chunk * 0x9E3779B97F4A7C15ull) >> (64 - bits);
+}
 
 // NEXT-4 2-bit host states (R-36): host byte q <-> bits 2(q&15),
 // 2(q&15)+1 of 32-bit word q>>4.  bit 0 set = some V bit undefined, state 0 =

@@ -751,6 +751,43 @@ __device__ __forceinline__ void lane_fill2(uint8_t* states, uint64_t q0, uint64_
   for (uint64_t k = q0 >> 4; k < (q1 + 15) >> 4; ++k) fill2_word(S, k, pair_mask(16ull * k, q0, q1), pat);
 }
 
+// NEXT-4 sparse map: the secondary holding `chunk` (0 = distinguished NOACCESS)
+__device__ __forceinline__ uint32_t sparse_secondary(const ShadowView& sv, uint64_t chunk) {
+  const uint64_t mask = (1ull << sv.dir_bits) - 1;
+  for (uint64_t h = dir_hash(chunk, sv.dir_bits);; h = (h + 1) & mask) {
+    const uint64_t k = __ldg(sv.dir_key + h);
+    if (k == chunk + 1) return __ldg(sv.dir_val + h);
+    if (k == 0) return 0u;
+  }
+}
+
+// a states base for `chunk`: base + (q >> 2) is the state byte of host byte q of the chunk
+__device__ __forceinline__ uint8_t* chunk_base(const ShadowView& sv, uint64_t chunk, uint32_t sec) {
+  return reinterpret_cast<uint8_t*>(reinterpret_cast<uintptr_t>(sv.V) + (uint64_t)sec * kSecondaryBytes -
+                                    ((chunk << kChunkShift) >> 2));
+}
+
+// states of shard bytes [q0, q1) := pat in either 2-bit layout (sparse: chunk
+// by chunk; chunks without a secondary are NOACCESS and left alone)
+template <bool kWarp>
+__device__ __forceinline__ void fill2_any(const ShadowView& sv, uint64_t q0, uint64_t q1, uint32_t pat) {
+  if (!sv.sparse) {
+    if (kWarp) warp_fill2(sv.V, q0, q1, pat);
+    else lane_fill2(sv.V, q0, q1, pat);
+    return;
+  }
+  for (uint64_t q = q0; q < q1;) {
+    const uint64_t c = q >> kChunkShift;
+    const uint64_t n = umin64(q1 - q, (1ull << kChunkShift) - (q & ((1ull << kChunkShift) - 1)));
+    const uint32_t sec = sparse_secondary(sv, c);
+    if (sec) {
+      if (kWarp) warp_fill2(chunk_base(sv, c, sec), q, q + n, pat);
+      else lane_fill2(chunk_base(sv, c, sec), q, q + n, pat);
+    }
+    q += n;
+  }
+}
+
 // V := 0 over shard bytes [q0, q1) with the whole warp (16-byte stores, byte
 // stores at the unaligned edges)
 __device__ __forceinline__ void warp_store_zero(uint8_t* V, uint64_t q0, uint64_t q1) {
@@ -1056,8 +1093,13 @@ struct TileGen {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       if (two_bit) {   // host bytes [qa, qa + span) <-> 16-byte aligned state bytes [qa/4, (qa + span)/4)
         const uint32_t span = (ti.q1 + 63u) & ~63u;
+        const uint8_t* base = sv.V;
+        if (sv.sparse) {   // a tile never leaves its 16 KiB block, so never its chunk
+          const uint64_t c = qa >> kChunkShift;
+          base = chunk_base(sv, c, sparse_secondary(sv, c));
+        }
         mbar_arrive_tx(&ring.bar[s], span / 4);
-        bulk_g2s(ring.data[s], sv.V + qa / 4, span / 4, &ring.bar[s], policy);
+        bulk_g2s(ring.data[s], base + qa / 4, span / 4, &ring.bar[s], policy);
         ++t;
         return true;
       }
@@ -1169,7 +1211,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
       p = Partial{kNone, kNone, 0};
       // fused a6: a whole contiguous DtoH piece with status OK becomes defined
       if (__shfl_sync(kFull, apply, 0)) {
-        if (gen.two_bit) warp_fill2(sv.V, t.qs, t.qe, 0xAAAAAAAAu);
+        if (gen.two_bit) fill2_any<true>(sv, t.qs, t.qe, 0xAAAAAAAAu);
         else warp_store_zero(sv.V, t.qs, t.qe);
       }
     }
@@ -1383,7 +1425,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(const ScanMeta* __restrict__
         }
       }
       if (small) {
-        if (sv.two_bit) lane_fill2(sv.V, qs, qe, 0xAAAAAAAAu);
+        if (sv.two_bit) fill2_any<false>(sv, qs, qe, 0xAAAAAAAAu);
         else lane_zero(sv.V, qs, qe, zeros);
       }
       uint32_t todo = __ballot_sync(kFull, big);
@@ -1393,7 +1435,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(const ScanMeta* __restrict__
         const uint64_t s_info = __shfl_sync(kFull, m.info, src);
         if ((s_info >> 43) & 1u) {
           const uint64_t a = __shfl_sync(kFull, qs, src), b = __shfl_sync(kFull, qe, src);
-          if (sv.two_bit) warp_fill2(sv.V, a, b, 0xAAAAAAAAu);
+          if (sv.two_bit) fill2_any<true>(sv, a, b, 0xAAAAAAAAu);
           else warp_zero(sv.V, a, b, zeros);
         } else {
           const uint64_t x0 = __shfl_sync(kFull, m.hstart, src), pitch = __shfl_sync(kFull, m.hpitch, src);
@@ -1406,7 +1448,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(const ScanMeta* __restrict__
             const uint64_t x = x0 + r * pitch + c;
             const uint64_t y0 = umax64(x, sv.sb), y1 = umin64(x + len, sv.se);
             if (y0 < y1) {
-              if (sv.two_bit) warp_fill2(sv.V, y0 - sv.sb, y1 - sv.sb, 0xAAAAAAAAu);
+              if (sv.two_bit) fill2_any<true>(sv, y0 - sv.sb, y1 - sv.sb, 0xAAAAAAAAu);
               else warp_zero(sv.V, y0 - sv.sb, y1 - sv.sb, zeros);
             }
             o += len;
@@ -1690,8 +1732,8 @@ __global__ void __launch_bounds__(kThreads) k_mark(const cg_mark* __restrict__ m
       const uint64_t y0 = umax64(x, sv.sb), y1 = umin64(end, sv.se);
       if (y0 >= y1) continue;
       if (sv.two_bit) {
-        warp_fill2(sv.V, y0 - sv.sb, y1 - sv.sb,
-                   mk.state == CG_DEFINED ? 0xAAAAAAAAu : mk.state == CG_UNDEFINED ? 0xFFFFFFFFu : 0u);
+        fill2_any<true>(sv, y0 - sv.sb, y1 - sv.sb,
+                        mk.state == CG_DEFINED ? 0xAAAAAAAAu : mk.state == CG_UNDEFINED ? 0xFFFFFFFFu : 0u);
       } else {
         fill_v(sv, y0 - sv.sb, y1 - sv.sb, mk.state == CG_DEFINED ? 0x00u : 0xFFu);
         put_abits(sv, y0 - sv.sb, y1 - sv.sb, mk.state != CG_NOACCESS);
@@ -1703,10 +1745,20 @@ __global__ void __launch_bounds__(kThreads) k_mark(const cg_mark* __restrict__ m
 __global__ void k_setv_check(ShadowView sv, uint64_t addr, uint64_t len, uint32_t* __restrict__ flag) {
   const uint64_t y0 = umax64(addr, sv.sb), y1 = umin64(addr + len, sv.se);
   for (uint64_t q = y0 - sv.sb + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < y1 - sv.sb;
-       q += (uint64_t)gridDim.x * blockDim.x)
-    if (sv.two_bit ? ((reinterpret_cast<const uint32_t*>(sv.V)[q >> 4] >> (2 * (q & 15))) & 3u) == kSt2NoAccess
-                   : !((sv.A[q >> 3] >> (q & 7)) & 1))
-      atomicOr(flag, 1u);
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    bool bad;
+    if (sv.sparse) {
+      const uint64_t c = q >> kChunkShift;
+      const uint32_t sec = sparse_secondary(sv, c);
+      bad = sec == 0 || ((reinterpret_cast<const uint32_t*>(chunk_base(sv, c, sec))[q >> 4] >> (2 * (q & 15))) & 3u) ==
+                            kSt2NoAccess;
+    } else if (sv.two_bit) {
+      bad = ((reinterpret_cast<const uint32_t*>(sv.V)[q >> 4] >> (2 * (q & 15))) & 3u) == kSt2NoAccess;
+    } else {
+      bad = !((sv.A[q >> 3] >> (q & 7)) & 1);
+    }
+    if (bad) atomicOr(flag, 1u);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1942,7 +1994,7 @@ cudaError_t summarize(const cg_verdict* v, uint64_t n, uint32_t warn_mask, unsig
 
 cudaError_t fresh_shadow(const Launch& L, const ShadowView& sv, cudaStream_t s) {
   if (sv.two_bit) {   // every state NOACCESS
-    k_fill<<<L.num_sms * 8, kThreads, 0, s>>>(reinterpret_cast<uint4*>(sv.V), (sv.se - sv.sb) / 64, 0u);
+    k_fill<<<L.num_sms * 8, kThreads, 0, s>>>(reinterpret_cast<uint4*>(sv.V), sv.v_bytes / 16, 0u);
     *L.counter += 1;
     return cudaGetLastError();
   }

@@ -39,12 +39,18 @@ struct ArrayEntry {   // NEXT-3 device array (SPEC register_array S:166-168)
 struct Layout {
   uint64_t table, arrays, weight, P, bsum, chunk, meta, resid, dvoff, scratch, marks, flags, leaks, desc_stage,
       verdict_stage, raw_stage,
-      idx_stage, dirty_stage, total;
+      idx_stage, dirty_stage, dir, total;
+  uint32_t dir_bits;
   uint64_t max_items, max_chunks;
 };
 
 bool valid_config(const cg_config* c) {
   if (!c) return false;
+  if (c->shadow_format == CG_SHADOW_SPARSE) {   // NEXT-4 two-level map: capacity only, unsharded
+    if (c->host_base != 0 || c->host_size == 0 || c->host_size % 65536 || c->shard_size || c->dev_vbuf) return false;
+    if (c->max_descs == 0 || c->max_descs > cgk::kMaxDescs) return false;
+    return c->max_allocs != 0 && c->max_allocs <= (1ull << 32);
+  }
   if (c->host_size == 0 || c->host_base % 4096 || c->host_size % 4096) return false;
   if (c->host_base + c->host_size < c->host_base) return false;
   uint64_t sb = c->shard_size ? c->shard_base : c->host_base;
@@ -89,6 +95,13 @@ Layout layout_of(const cg_config* c) {
   L.raw_stage = c->host_staging ? take(c->max_descs * sizeof(cg_copy1d)) : 0;
   L.idx_stage = c->host_staging ? take(c->max_descs * sizeof(uint64_t)) : 0;
   L.dirty_stage = c->host_staging ? take(c->max_descs * sizeof(cg_verdict)) : 0;
+  L.dir_bits = 0;
+  L.dir = 0;
+  if (c->shadow_format == CG_SHADOW_SPARSE) {   // directory: >= 2x the secondaries, power of two
+    const uint64_t nsec = c->host_size / 65536 + 1;
+    while ((1ull << L.dir_bits) < 2 * nsec) ++L.dir_bits;
+    L.dir = take((1ull << L.dir_bits) * 12);
+  }
   L.total = off;
   return L;
 }
@@ -120,6 +133,48 @@ struct cg_ctx {
   std::map<uint64_t, uint64_t> live;        // base -> end of live allocations
   std::vector<ArrayEntry> arrays;           // NEXT-3: sorted by (handle, aseq)
   std::map<uint64_t, uint8_t> partial;      // NEXT-4 2-bit format: exact V-bytes of PARTIAL host bytes
+  std::map<uint64_t, uint32_t> chunks;      // NEXT-4 sparse map: chunk -> secondary (1-based)
+  std::vector<uint32_t> dir_host;           // directory image: 2^bits u64 keys then 2^bits u32 values
+  bool dir_dirty = false;
+
+  // sparse map: make sure every chunk of [a, b) has a secondary; false if the pool is full
+  bool ensure_chunks(uint64_t a, uint64_t b) {
+    const uint64_t cap = cfg.host_size / 65536;
+    for (uint64_t c = a >> cgk::kChunkShift; c <= (b - 1) >> cgk::kChunkShift; ++c) {
+      if (chunks.count(c)) continue;
+      if (chunks.size() >= cap) return false;
+      const uint32_t sec = (uint32_t)chunks.size() + 1;
+      chunks.emplace(c, sec);
+      const uint64_t slots = 1ull << lay.dir_bits;
+      uint64_t* keys = reinterpret_cast<uint64_t*>(dir_host.data());
+      uint32_t* vals = dir_host.data() + 2 * slots;
+      for (uint64_t h = cgk::dir_hash(c, lay.dir_bits);; h = (h + 1) & (slots - 1)) {
+        if (keys[h] == 0) {
+          keys[h] = c + 1;
+          vals[h] = sec;
+          break;
+        }
+      }
+      dir_dirty = true;
+    }
+    return true;
+  }
+  cg_status upload_dir(cudaStream_t s) {
+    if (!dir_dirty) return CG_OK;
+    cudaError_t e = cudaMemcpyAsync(ws + lay.dir, dir_host.data(), dir_host.size() * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);   // the host image may change right after
+    if (e != cudaSuccess) return cuda(e, "directory upload");
+    dir_dirty = false;
+    return CG_OK;
+  }
+  // device pointer of the state word holding host byte q (sparse: nullptr if its chunk has no secondary)
+  uint32_t* state_word(uint64_t q) {
+    if (!sv.sparse) return reinterpret_cast<uint32_t*>(sv.V) + (q >> 4);
+    auto it = chunks.find(q >> cgk::kChunkShift);
+    if (it == chunks.end()) return nullptr;
+    return reinterpret_cast<uint32_t*>(sv.V + (uint64_t)it->second * cgk::kSecondaryBytes) +
+           ((q & ((1ull << cgk::kChunkShift) - 1)) >> 4);
+  }
   std::map<uint64_t, uint64_t> live_arrays; // handle -> total bytes
   uint64_t last_seq = 0;
   bool dirty = true;
@@ -287,7 +342,8 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
   *out = nullptr;
   if (!valid_config(cfg)) return CG_ERR_INVALID_VALUE;
   const Layout lay = layout_of(cfg);
-  const bool two_bit = cfg->shadow_format == CG_SHADOW_2BIT;
+  const bool sparse = cfg->shadow_format == CG_SHADOW_SPARSE;
+  const bool two_bit = cfg->shadow_format == CG_SHADOW_2BIT || sparse;
   if (!cfg->v_buf || (!two_bit && !cfg->a_buf) || !cfg->workspace) return CG_ERR_INVALID_VALUE;
   if (cfg->workspace_size < lay.total) return CG_ERR_INVALID_VALUE;
   if ((uintptr_t)cfg->v_buf % 16 || (!two_bit && (uintptr_t)cfg->a_buf % 16) || (uintptr_t)cfg->workspace % kAlign)
@@ -304,6 +360,18 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
   c->sv.V = static_cast<uint8_t*>(cfg->v_buf);
   c->sv.A = two_bit ? nullptr : static_cast<uint8_t*>(cfg->a_buf);
   c->sv.two_bit = two_bit ? 1u : 0u;
+  c->sv.sparse = sparse ? 1u : 0u;
+  c->sv.v_bytes = sparse ? (cfg->host_size / 65536 + 1) * cgk::kSecondaryBytes : two_bit ? cfg->host_size / 4
+                                                                                          : cfg->host_size;
+  if (cfg->shard_size && !sparse) c->sv.v_bytes = two_bit ? cfg->shard_size / 4 : cfg->shard_size;
+  if (sparse) {   // the whole 64-bit space; the directory lives in the workspace
+    c->sv.wb = c->sv.sb = 0;
+    c->sv.we = c->sv.se = UINT64_MAX;
+    c->sv.dir_bits = lay.dir_bits;
+    c->sv.dir_key = reinterpret_cast<const uint64_t*>(c->ws + lay.dir);
+    c->sv.dir_val = reinterpret_cast<const uint32_t*>(c->ws + lay.dir + (8ull << lay.dir_bits));
+    c->dir_host.assign((1ull << lay.dir_bits) * 3, 0u);   // keys (2 words each) + values
+  }
   cudaDeviceProp prop;
   cudaError_t e = cudaGetDeviceProperties(&prop, cfg->device);
   if (e != cudaSuccess) {
@@ -471,6 +539,7 @@ cg_status cg_profile_end(cg_ctx* c, double* ms, uint64_t* launches) {
 }
 
 static bool in_window(const cg_ctx* c, uint64_t addr, uint64_t len) {
+  if (c->sv.sparse) return len <= UINT64_MAX - addr;
   return addr >= c->sv.wb && len <= c->sv.we - c->sv.wb && addr - c->sv.wb <= (c->sv.we - c->sv.wb) - len;
 }
 
@@ -505,12 +574,20 @@ cg_status cg_host_mark_batch(cg_ctx* c, const cg_mark* h_marks, uint64_t n, uint
         bool overlap = (it != run.end() && it->first < b);
         if (!overlap && it != run.begin()) overlap = std::prev(it)->second > a;
         if (overlap) break;
+        if (c->sv.sparse && m.state != CG_NOACCESS && !c->ensure_chunks(a, b)) {   // NEXT-4: pool full
+          if (h_status) h_status[j] = CG_ERR_OUT_OF_MEMORY;
+          ret = c->fail(CG_ERR_OUT_OF_MEMORY, "sparse host map: no secondary left for mark %llu",
+                        (unsigned long long)j);
+          ++j;
+          continue;
+        }
         run.emplace(a, b);
         c->h_marks[k++] = m;
       }
       ++j;
     }
     if (k) {
+      if (c->upload_dir(s) != CG_OK) return CG_ERR_CUDA;
       e = cudaMemcpyAsync(dm, c->h_marks, k * sizeof(cg_mark), cudaMemcpyHostToDevice, s);
       if (e != cudaSuccess) return c->cuda(e, "marks upload");
       e = cgk::mark_batch(c->launch, dm, k, c->sv, c->plan(), s);
@@ -545,24 +622,31 @@ cg_status cg_host_set_vbits(cg_ctx* c, uint64_t addr, uint64_t len, const uint8_
   if (e != cudaSuccess) return c->cuda(e, "set_vbits check");
   if (h_flag) return c->fail(CG_ERR_INVALID_VALUE, "set_vbits on unaddressable bytes");
   if (c->sv.two_bit) {   // NEXT-4: read-modify-write the state words; exact partial V-bytes go to the host table
-    const uint64_t q0 = y0 - c->sv.sb, q1 = y1 - c->sv.sb, k0 = q0 >> 4, k1 = (q1 + 15) >> 4;
-    std::vector<uint32_t> w(k1 - k0);
-    uint32_t* S = reinterpret_cast<uint32_t*>(c->sv.V);
-    e = cudaMemcpyAsync(w.data(), S + k0, w.size() * 4, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return c->cuda(e, "set_vbits read");
-    for (uint64_t q = q0; q < q1; ++q) {
-      const uint8_t v = h_vbytes[q - q0 + (y0 - addr)];
-      const uint32_t st = v == 0x00 ? cgk::kSt2Defined : v == 0xFF ? cgk::kSt2Undefined : cgk::kSt2Partial;
-      uint32_t& x = w[(q >> 4) - k0];
-      const int sh = 2 * (int)(q & 15);
-      x = (x & ~(3u << sh)) | (st << sh);
-      if (st == cgk::kSt2Partial) c->partial[q + c->sv.sb] = v;
-      else c->partial.erase(q + c->sv.sb);
+    const uint64_t q0 = y0 - c->sv.sb, q1 = y1 - c->sv.sb;
+    for (uint64_t a = q0; a < q1;) {   // pieces that stay inside one chunk of the sparse map
+      const uint64_t rem = c->sv.sparse ? (1ull << cgk::kChunkShift) - (a & ((1ull << cgk::kChunkShift) - 1)) : q1 - a;
+      const uint64_t b = q1 - a <= rem ? q1 : a + rem;
+      const uint64_t k0 = a >> 4, k1 = (b + 15) >> 4;
+      uint32_t* S = c->state_word(a);   // addressable, so its chunk has a secondary
+      std::vector<uint32_t> w(k1 - k0);
+      e = cudaMemcpyAsync(w.data(), S, w.size() * 4, cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) return c->cuda(e, "set_vbits read");
+      for (uint64_t q = a; q < b; ++q) {
+        const uint8_t v = h_vbytes[q - q0 + (y0 - addr)];
+        const uint32_t st = v == 0x00 ? cgk::kSt2Defined : v == 0xFF ? cgk::kSt2Undefined : cgk::kSt2Partial;
+        uint32_t& x = w[(q >> 4) - k0];
+        const int sh = 2 * (int)(q & 15);
+        x = (x & ~(3u << sh)) | (st << sh);
+        if (st == cgk::kSt2Partial) c->partial[q + c->sv.sb] = v;
+        else c->partial.erase(q + c->sv.sb);
+      }
+      e = cudaMemcpyAsync(S, w.data(), w.size() * 4, cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) return c->cuda(e, "set_vbits write");
+      a = b;
     }
-    e = cudaMemcpyAsync(S + k0, w.data(), w.size() * 4, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    return c->cuda(e, "set_vbits write");
+    return CG_OK;
   }
   e = cudaMemcpyAsync(c->sv.V + (y0 - c->sv.sb), h_vbytes + (y0 - addr), y1 - y0, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -574,18 +658,25 @@ cg_status cg_host_shadow_read(cg_ctx* c, uint64_t addr, uint64_t len, uint8_t* h
   if (len == 0) return CG_OK;
   if (addr < c->sv.sb || addr > c->sv.se || len > c->sv.se - addr)
     return c->fail(CG_ERR_INVALID_VALUE, "shadow read outside this context's shard");
+  if (c->sv.sparse && len > (1ull << 32)) return c->fail(CG_ERR_INVALID_VALUE, "sparse shadow read above 4 GiB");
   DeviceGuard g(c->cfg.device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const uint64_t q0 = addr - c->sv.sb, q1 = q0 + len;
   cudaError_t e = cudaSuccess;
   if (c->sv.two_bit) {
-    const uint64_t k0 = q0 >> 4, k1 = (q1 + 15) >> 4;
-    std::vector<uint32_t> w(k1 - k0);
-    e = cudaMemcpyAsync(w.data(), reinterpret_cast<uint32_t*>(c->sv.V) + k0, w.size() * 4, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return c->cuda(e, "shadow read");
-    for (uint64_t q = q0; q < q1; ++q) {
-      const uint32_t st = (w[(q >> 4) - k0] >> (2 * (q & 15))) & 3u;
+    for (uint64_t a = q0; a < q1;) {   // pieces that stay inside one chunk of the sparse map
+      const uint64_t rem = c->sv.sparse ? (1ull << cgk::kChunkShift) - (a & ((1ull << cgk::kChunkShift) - 1)) : q1 - a;
+      const uint64_t b = q1 - a <= rem ? q1 : a + rem;
+      const uint64_t k0 = a >> 4, k1 = (b + 15) >> 4;
+      std::vector<uint32_t> w(k1 - k0, 0u);   // a chunk without a secondary reads as NOACCESS
+      if (uint32_t* S = c->state_word(a)) {
+        e = cudaMemcpy(w.data(), S, w.size() * 4, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return c->cuda(e, "shadow read");
+      }
+      for (uint64_t q = a; q < b; ++q) {
+        const uint32_t st = (w[(q >> 4) - k0] >> (2 * (q & 15))) & 3u;
       if (h_a) h_a[q - q0] = st != cgk::kSt2NoAccess;
       if (h_v) {
         uint8_t v = st == cgk::kSt2Defined ? 0x00 : 0xFF;
@@ -595,6 +686,8 @@ cg_status cg_host_shadow_read(cg_ctx* c, uint64_t addr, uint64_t len, uint8_t* h
         }
         h_v[q - q0] = v;
       }
+      }
+      a = b;
     }
     return CG_OK;
   }

@@ -136,3 +136,70 @@ def test_c3_straddler_sharded(cg):
 def test_c5_scaled_sharded(cg):
     from test_gpu_sharded import run_sharded
     run_sharded(cg, tg.c5_sharded(scale=0.01), 8, **TWO)
+
+
+# ---------------------------------------------------------------------------
+# the sparse two-level map (CG_SHADOW_SPARSE): the whole 64-bit host space
+# ---------------------------------------------------------------------------
+SPARSE = dict(shadow_format=2)
+
+
+def test_sparse_toy_and_listing2(cg):
+    run_parity(cg, tg.toy(), **SPARSE)
+    v = run_parity(cg, tg.listing2(), **SPARSE)
+    assert (v[2]["src_expected"], v[2]["src_found"]) == (8000000, 4000000)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_sparse_random_tiny(cg, seed):
+    run_parity(cg, tg.random_tiny(seed + 500, arrays=seed % 3 == 0), fuse=bool(seed % 2), **SPARSE)
+
+
+@pytest.mark.parametrize("fuse", [True, False])
+def test_sparse_c2_scaled(cg, fuse):
+    tr = tg.c2_small(n_copies=30000, n_allocs=3000)
+    v = run_parity(cg, tr, fuse=fuse, **SPARSE)
+    assert np.array_equal(v["flags"] != 0, tr.meta["inject"] != 0)
+
+
+def test_sparse_c4_scaled(cg):
+    run_parity(cg, tg.c4_pitched(n_copies=2000, n_bufs=4, rows=128, inject_frac=0.03), **SPARSE)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_sparse_relocated_regions(cg, seed):
+    """relocation invariance: host regions scattered over the 64-bit space
+    (the GPU's sparse map) give the verdicts the oracle computes with the
+    regions packed into one dense window; each region's final shadow matches"""
+    dense, sparse, bases, R = tg.sparse_regions(seed)
+    o, ov, os_, _ = oracle.replay_trace(dense)
+    chk = cg.Checker(sparse.host_base, R, max_descs=max(sparse.n_copies, 64), max_allocs=4096,
+                     sparse_capacity=len(bases) * (R + 65536), **SPARSE)
+    gv, gs = cg.replay_events(chk, sparse.events, sparse.blob, fuse=bool(seed % 2))
+    for f in ov.dtype.names:
+        bad = np.flatnonzero(gv[f] != ov[f])
+        assert len(bad) == 0, (f, bad[:5], gv[f][bad[:5]], ov[f][bad[:5]])
+    assert np.array_equal(gs, os_)
+    for k, b in enumerate(bases):
+        a, v = chk.shadow_read(b, R)
+        lo = k * R
+        assert np.array_equal(v, o.V[lo:lo + R]), k
+        A = np.unpackbits(o.A, bitorder="little")[lo:lo + R]
+        assert np.array_equal(a, A), k
+    a, v = chk.shadow_read(1 << 40, 4096)                          # never marked: NOACCESS
+    assert not a.any() and (v == 0xFF).all()
+    chk.close()
+
+
+def test_sparse_capacity(cg):
+    chk = cg.Checker(0, 1 << 16, max_descs=64, max_allocs=64, sparse_capacity=2 * 65536, **SPARSE)
+    assert chk.host_mark(0x7F00_0000_0000, 65536 + 10, cg.CG_DEFINED) == 0       # two chunks
+    st = np.zeros(1, np.uint32)
+    m = np.zeros(1, cg.MARK_DTYPE)
+    m[0] = (0x5500_0000_0000, 16, cg.CG_UNDEFINED, 0)
+    assert chk.host_mark_batch(m, status_out=st) == cg.CG_ERR_OUT_OF_MEMORY
+    assert st[0] == cg.CG_ERR_OUT_OF_MEMORY
+    assert chk.host_mark(0x5500_0000_0000, 16, cg.CG_NOACCESS) == 0              # needs no secondary
+    assert chk.host_query_addressable(0x7F00_0000_0000, 65536 + 10)
+    assert not chk.host_query_addressable(0x7F00_0000_0000, 65536 + 11)
+    chk.close()

@@ -826,3 +826,76 @@ def with_threads(tr: Trace, n_threads: int, sync_frac: float = 0.01, seed: int =
     ev["seq"] = np.arange(1, len(ev) + 1, dtype=np.uint64)
     th = rng.integers(0, n_threads, len(ev)).astype(np.uint32)
     return Trace(f"{tr.name}_t{n_threads}", ev, tr.blob, tr.host_base, tr.host_size, dict(tr.meta), th)
+
+
+# ---------------------------------------------------------------------------
+# NEXT-4: host regions scattered over the 64-bit space (sparse host map)
+# ---------------------------------------------------------------------------
+def sparse_regions(seed: int = 0, n_regions: int = 6, region: int = 256 * KiB, n_copies: int = 400):
+    """The same program twice: `dense` keeps its n_regions host regions packed
+    in one window [H0, H0 + n_regions*region) (what the dense oracle can
+    represent), `sparse` places region k at bases[k], scattered over the
+    64-bit address space (64 KiB aligned).  Every host range of every event
+    stays inside one region, so the two programs have the same meaning: the
+    verdicts (logical offsets, counts, flags) must be identical.
+    Returns (dense, sparse, bases, region)."""
+    rng = np.random.default_rng(seed + 0x5AA5)
+    H0 = 1 << 20
+    tb = TraceBuilder(f"regions{seed}", H0, n_regions * region)
+    allocs = [tb.malloc(int(rng.integers(256, 64 * KiB))) for _ in range(24)]
+    sizes = {}
+    for k in range(n_regions):   # fragmented regions: DEFINED / UNDEFINED runs with NOACCESS gaps
+        o = 0
+        while o < region:
+            n = int(rng.integers(64, 24 * KiB))
+            n = min(n, region - o)
+            st = int(rng.choice([DEFINED, UNDEFINED, NOACCESS], p=[0.6, 0.25, 0.15]))
+            tb.mark(H0 + k * region + o, n, st)
+            o += n
+        for _ in range(4):
+            a = int(rng.integers(0, region - 64))
+            tb.setv(H0 + k * region + a, rng.integers(0, 256, int(rng.integers(1, 64)), dtype=np.uint8).tobytes())
+    for b in allocs:
+        sizes[b] = None
+    for _ in range(n_copies):
+        k = int(rng.integers(n_regions))
+        d = allocs[int(rng.integers(len(allocs)))]
+        kind = int(rng.choice([HTOD, DTOH], p=[0.55, 0.45]))
+        if rng.random() < 0.3:   # 2D, host side pitched inside the region
+            w = int(rng.integers(1, 512)); h = int(rng.integers(1, 32)); pitch = w + int(rng.integers(0, 256))
+            span = (h - 1) * pitch + w
+            a = H0 + k * region + int(rng.integers(0, region - span))
+            if kind == HTOD:
+                tb.copy2d(HTOD, w, h, d, 0, 0, w, a, 0, 0, pitch)
+            else:
+                tb.copy2d(DTOH, w, h, a, 0, 0, pitch, d, 0, 0, w)
+        else:
+            n = int(rng.integers(1, 32 * KiB))
+            a = H0 + k * region + int(rng.integers(0, region - n))
+            if kind == HTOD:
+                tb.copy1d(HTOD, d, a, n)
+            else:
+                tb.copy1d(DTOH, a, d, n)
+        if rng.random() < 0.1:
+            tb.mark(H0 + k * region + int(rng.integers(0, region - 4096)), 4096,
+                    int(rng.choice([DEFINED, UNDEFINED, NOACCESS])))
+    dense = tb.build()
+    # scattered bases: distinct 64 KiB-aligned slots far apart
+    slots = rng.choice(1 << 30, n_regions, replace=False)          # 8 MiB slots over 2^53 bytes
+    bases = [((1 << 32) + int(s) * (1 << 23) + int(rng.integers(0, 1 << 22))) & ~0xFFFF for s in slots]
+
+    def move(x):
+        k = (int(x) - H0) // region
+        return bases[k] + (int(x) - H0 - k * region)
+
+    ev = dense.events.copy()
+    for i, e in enumerate(ev):
+        op = int(e["op"])
+        if op in (OP_MARK, OP_SETV):
+            ev[i]["dst"] = move(e["dst"])
+        elif op == OP_COPY:
+            p = "src" if int(e["kind"]) == HTOD else "dst"
+            ev[i][p] = move(e[p])
+    sparse = Trace(dense.name + "_sparse", ev, dense.blob, bases[0] & ~0xFFFF, region, dict(dense.meta),
+                   dense.threads)
+    return dense, sparse, bases, region
