@@ -65,8 +65,8 @@ def fused_apply_bytes(descs: np.ndarray, verdicts: np.ndarray, max_descs: int, t
     """Bytes the fused scan writes itself in cg_check_apply: DtoH descriptors
     with status OK, contiguous and not split by the scan's grouping (weight at
     most one group, or inside one group); the rest go to the residual pass.  Replicates the
-    library's plan (weight = 256 + host units; group T = max(128 KiB,
-    ceil(total / max(2^20, 2 max_descs)))) for accounting only."""
+    library's plan (weight = 256 + host units; never split below Trule =
+    max(128 KiB, T), T = max(32 KiB, ceil(total / max(2^20, 2 max_descs)))) for accounting only."""
     nb = descs["width"].astype(np.uint64) * descs["height"].astype(np.uint64)
     if two_bit:
         units = np.where((descs["kind"] == 1) | (descs["kind"] == 2), (nb + np.uint64(3)) // np.uint64(4), 0)
@@ -76,8 +76,8 @@ def fused_apply_bytes(descs: np.ndarray, verdicts: np.ndarray, max_descs: int, t
     P = np.concatenate([[0], np.cumsum(w, dtype=np.uint64)])
     total = int(P[-1])
     chunks = max(1 << 20, 2 * max_descs)
-    T = max(128 * 1024, -(-total // chunks))
-    whole = ((P[1:] - P[:-1]) <= T) | ((P[:-1] // T) == ((P[1:] - 1) // T))
+    T = max(32 * 1024, -(-total // chunks))
+    whole = (P[1:] - P[:-1]) <= max(T, 128 * 1024)   # descriptors of at most Trule weight are never split
     contig = (descs["height"] == 1) | (descs["width"] == descs["dst_pitch"])
     ok = (descs["kind"] == 2) & (verdicts["status"] == 0) & contig & whole
     return float(nb[ok].astype(np.float64).sum()) * (0.25 if two_bit else 1.0)

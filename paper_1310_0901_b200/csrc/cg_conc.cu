@@ -105,34 +105,56 @@ __global__ void k_hist_to_r(Space S0, Space S1, uint64_t nh0, uint64_t nh1) {
   if (i < nh1) { S1.rs[i] = S1.hs[i]; S1.re[i] = S1.he[i]; S1.rkey[i] = 2u * (uint32_t)i + S1.hw[i]; }
 }
 
+// warp-aggregated slot allocation: one atomic per warp and counter
+__device__ __forceinline__ unsigned long long warp_slot(bool want, unsigned long long* counter) {
+  const uint32_t m = __ballot_sync(0xffffffffu, want);
+  if (!m) return 0;
+  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  return base + __popc(m & ((1u << lane) - 1u));
+}
+
 // one thread per copy: its accesses become queries; performed copies' accesses
 // are appended to R (R-33, R-34).  counts: [qn0, qn1, rn0, rn1]
 __global__ void k_access(const cg_copy_desc* __restrict__ d, const cg_verdict* __restrict__ v, uint64_t n,
                          Space S0, Space S1, uint64_t nh0, uint64_t nh1, unsigned long long* counts) {
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const cg_copy_desc c = d[i];
-  int sp[2], dst[2], wr[2];
-  const int na = copy_accesses(c.kind, sp, dst, wr);
-  const bool performed = v[i].status == CG_OK;
-  for (int k = 0; k < na; ++k) {
-    uint64_t start, span;
-    const bool ok = dst[k] ? cgk::fold_side(c.dst, c.dst_x, c.dst_y, c.dst_pitch, c.width, c.height, start, span)
-                           : cgk::fold_side(c.src, c.src_x, c.src_y, c.src_pitch, c.width, c.height, start, span);
-    if (!ok || span == 0) continue;
-    Space& S = sp[k] ? S1 : S0;
-    const uint64_t nh = sp[k] ? nh1 : nh0;
-    const uint32_t key = 2u * (uint32_t)(nh + i) + (uint32_t)wr[k];
-    const unsigned long long q = atomicAdd(counts + sp[k], 1ull);
-    S.qs[q] = start;
-    S.qe[q] = start + span;
-    S.qkey[q] = key;
-    S.qcopy[q] = (uint32_t)i;
-    if (performed) {
-      const unsigned long long r = nh + atomicAdd(counts + 2 + sp[k], 1ull);
-      S.rs[r] = start;
-      S.re[r] = start + span;
-      S.rkey[r] = key;
+  int sp[2] = {0, 0}, dst[2] = {0, 0}, wr[2] = {0, 0};
+  int na = 0;
+  bool performed = false;
+  cg_copy_desc c;
+  if (i < n) {
+    c = d[i];
+    na = copy_accesses(c.kind, sp, dst, wr);
+    performed = v[i].status == CG_OK;
+  }
+  for (int k = 0; k < 2; ++k) {   // warp-uniform loop: every lane takes part in the ballots
+    uint64_t start = 0, span = 0;
+    bool ok = false;
+    if (k < na) {
+      ok = dst[k] ? cgk::fold_side(c.dst, c.dst_x, c.dst_y, c.dst_pitch, c.width, c.height, start, span)
+                  : cgk::fold_side(c.src, c.src_x, c.src_y, c.src_pitch, c.width, c.height, start, span);
+      ok = ok && span != 0;
+    }
+    for (int space = 0; space < 2; ++space) {
+      const bool mine = ok && sp[k] == space;
+      const unsigned long long q = warp_slot(mine, counts + space);
+      const unsigned long long r = warp_slot(mine && performed, counts + 2 + space);
+      if (!mine) continue;
+      Space& S = space ? S1 : S0;
+      const uint64_t nh = space ? nh1 : nh0;
+      const uint32_t key = 2u * (uint32_t)(nh + i) + (uint32_t)wr[k];
+      S.qs[q] = start;
+      S.qe[q] = start + span;
+      S.qkey[q] = key;
+      S.qcopy[q] = (uint32_t)i;
+      if (performed) {
+        S.rs[nh + r] = start;
+        S.re[nh + r] = start + span;
+        S.rkey[nh + r] = key;
+      }
     }
   }
 }
@@ -157,6 +179,40 @@ __global__ void k_merge_level(const uint32_t* __restrict__ in, uint32_t* __restr
     c = lo - s0;
   }
   out[(((b < sib) ? b : sib) << (L - 1)) + r + c] = key;
+}
+
+// levels 1..kSmemLevels of the merge-sort tree for one 2^kSmemLevels tile in shared memory
+constexpr int kSmemLevels = 8;
+__global__ void __launch_bounds__(1 << kSmemLevels) k_merge_tile(uint32_t* __restrict__ mst, uint64_t n, uint64_t cap,
+                                                                 int levels) {
+  __shared__ uint32_t buf[2][1 << kSmemLevels];
+  const uint32_t t = threadIdx.x;
+  const uint64_t base = (uint64_t)blockIdx.x << kSmemLevels;
+  const uint32_t m = (uint32_t)min((uint64_t)1 << kSmemLevels, n - base);   // valid keys of this tile
+  if (t < m) buf[0][t] = mst[base + t];
+  __syncthreads();
+  int cur = 0;
+  for (int L = 1; L <= levels; ++L) {
+    if (t < m) {
+      const uint32_t half = 1u << (L - 1);
+      const uint32_t b = t >> (L - 1), sib = b ^ 1u, r = t - (b << (L - 1)), s0 = sib << (L - 1);
+      const uint32_t key = buf[cur][t];
+      uint32_t c = 0;
+      if (s0 < m) {
+        uint32_t lo = s0, hi = min(s0 + half, m);
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (buf[cur][mid] < key) lo = mid + 1; else hi = mid;
+        }
+        c = lo - s0;
+      }
+      const uint32_t o = (min(b, sib) << (L - 1)) + r + c;
+      buf[cur ^ 1][o] = key;
+      mst[(uint64_t)L * cap + base + o] = key;
+    }
+    cur ^= 1;
+    __syncthreads();
+  }
 }
 
 __global__ void k_endpoints(const uint64_t* __restrict__ rs, const uint64_t* __restrict__ re, uint64_t n,
@@ -494,7 +550,13 @@ cg_status cg_conc::run_space(int sp, const cg_copy_desc* d, const uint32_t* thre
     e = cub::DeviceRadixSort::SortPairs(temp, tb, S.rs, rs_sorted, S.rkey, mst, (int)rn, 0, 64, s);
     if (e != cudaSuccess) return cuda(e, "sort R");
     const int L = ceil_log2(rn);
-    for (int l = 1; l <= L; ++l) {
+    const int Ls = std::min(L, kSmemLevels);   // levels inside 256-key tiles: one pass in shared memory
+    if (Ls) {
+      k_merge_tile<<<(unsigned)((rn + (1u << kSmemLevels) - 1) >> kSmemLevels), 1 << kSmemLevels, 0, s>>>(mst, rn, cap,
+                                                                                                         Ls);
+      ++launches;
+    }
+    for (int l = Ls + 1; l <= L; ++l) {
       k_merge_level<<<grid_for(rn), kT, 0, s>>>(mst + (uint64_t)(l - 1) * cap, mst + (uint64_t)l * cap, rn, l);
       ++launches;
     }

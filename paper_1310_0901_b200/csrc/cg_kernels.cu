@@ -451,8 +451,12 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint64_t* __re
   }
 }
 
+// T: the chunk map's granularity (weight units); Trule >= T: descriptors of
+// at most Trule weight are never split (owned by the group their weight
+// interval starts in), heavier ones always go through the split path
+constexpr uint64_t kSmallT = 128 * 1024;
 struct ChunkGeom {
-  uint64_t total, T, nchunks;
+  uint64_t total, T, nchunks, Trule;
 };
 
 __device__ __forceinline__ ChunkGeom chunk_geom(const uint64_t* P, uint64_t n, uint64_t t_min,
@@ -462,6 +466,7 @@ __device__ __forceinline__ ChunkGeom chunk_geom(const uint64_t* P, uint64_t n, u
   uint64_t T = (g.total + max_chunks - 1) / max_chunks;
   g.T = umax64(T, t_min);
   g.nchunks = (g.total + g.T - 1) / g.T;
+  g.Trule = umax64(g.T, kSmallT);
   return g;
 }
 
@@ -504,6 +509,7 @@ constexpr uint32_t kTileV = 4096;      // HtoD: V bytes per tile
 constexpr uint32_t kTileA = kTileV / 8;
 constexpr uint32_t kDtohBlock = 32768; // DtoH: host bytes per tile (4 KiB of A)
 constexpr uint32_t k2bitBlock = 16384; // NEXT-4 2-bit states: host bytes per tile (4 KiB of states)
+constexpr uint32_t kGrab = 4;          // chunks per group while the plan is far from its end
 constexpr uint32_t kTileData = 1, kTileHtod = 2, kTileEnd = 4, kTileWhole = 8, kTileFuse = 16, kTileRaw = 32;
 
 struct __align__(16) TileInfo {
@@ -841,13 +847,15 @@ struct TileGen {
   uint32_t* counter;
   cg_verdict* out;
   uint32_t err_mask;
-  uint64_t n, T, nchunks, total;
+  uint64_t n, T, nchunks, total, Trule;
+  uint32_t nwarps;      // warps of the grid (group grab size policy)
   uint64_t wb, we, sb, se;
   bool fuse;            // check + apply in one pass (cg_check_apply)
   bool two_bit;         // NEXT-4 2-bit states: 16 KiB host bytes per tile for both kinds
   // group
   uint64_t w0, w1;
-  uint32_t g_pending;   // lane 0
+  uint32_t g_pending;   // lane 0: first chunk of the next group
+  uint32_t k_pending;   // lane 0: its chunk count
   int phase;
   // descriptor window (lane i <-> wbase + i)
   uint64_t wbase;
@@ -887,14 +895,14 @@ struct TileGen {
     p_fl = 0;
     // a descriptor of at most one group's weight is never split: it belongs
     // to the group its weight interval starts in
-    const bool small = m_pe - m_ps <= T;
+    const bool small = m_pe - m_ps <= Trule;
     if (small ? (m_ps >= w0 && m_ps < w1) : (m_ps < w1 && m_pe > w0)) {
       const uint64_t nbytes = m_info & ((1ull << 40) - 1);
       const uint32_t kind = (uint32_t)(m_info >> 40) & 3u;
       const bool host = (m_info >> 42) & 1u, contig = (m_info >> 43) & 1u;
       const bool htod = kind == CG_HTOD;
       uint32_t f = kPieceIn | (htod ? kPieceHtod : 0u);
-      if (small || (m_ps >= w0 && m_pe <= w1)) f |= kPieceWhole;
+      if (small) f |= kPieceWhole;
       uint64_t a = small ? 0 : umax64(w0, m_ps) - m_ps, b = small ? m_pe - m_ps : umin64(w1, m_pe) - m_ps;
       a = a > kItemCost ? a - kItemCost : 0;
       b = b > kItemCost ? b - kItemCost : 0;
@@ -973,10 +981,14 @@ struct TileGen {
   __device__ __forceinline__ bool next_group() {
     const int lane = threadIdx.x & 31;
     const uint32_t g = __shfl_sync(kFull, g_pending, 0);
+    const uint32_t k = __shfl_sync(kFull, k_pending, 0);
     if (g >= nchunks) return false;
-    if (lane == 0) g_pending = atomicAdd(counter, 1u);
+    if (lane == 0) {   // kGrab chunks at a time while plenty are left, single chunks for the tail
+      k_pending = (uint64_t)g + 16ull * kGrab * nwarps < nchunks ? kGrab : 1u;
+      g_pending = atomicAdd(counter, k_pending);
+    }
     w0 = (uint64_t)g * T;
-    w1 = umin64(w0 + T, total);
+    w1 = umin64((uint64_t)(g + k) * T, total);
     const uint64_t d = chunk_first[g];
     if (d < wbase || d >= wbase + 32) load_window(d);
     compute_pieces();
@@ -1145,13 +1157,16 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
   gen.T = geo.T;
   gen.nchunks = geo.nchunks;
   gen.total = geo.total;
+  gen.Trule = geo.Trule;
+  gen.nwarps = gridDim.x * kRingWarps;
   gen.wb = sv.wb;
   gen.we = sv.we;
   gen.sb = sv.sb;
   gen.se = sv.se;
   gen.fuse = fuse != 0;
   gen.two_bit = sv.two_bit != 0;
-  gen.g_pending = lane == 0 ? atomicAdd(counter, 1u) : 0;
+  gen.k_pending = kGrab;
+  gen.g_pending = lane == 0 ? atomicAdd(counter, kGrab) : 0;
   gen.phase = kPhaseGroup;
   gen.wbase = ~0ull >> 1;   // no window yet
   gen.p_fl = 0;
@@ -1232,7 +1247,7 @@ __global__ void __launch_bounds__(kThreads) k_finalize_split(uint64_t n, const u
   for (uint64_t d = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; d < n;
        d += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t pd = P[d], pd1 = P[d + 1];
-    if (pd1 - pd <= g.T || pd / g.T == (pd1 - 1) / g.T) continue;   // not split (see compute_pieces)
+    if (pd1 - pd <= g.Trule) continue;   // never split (see compute_pieces)
     const uint64_t info = meta[d].info;
     if ((info >> 44) & 1u) continue;   // raw partial of a straddler
     cg_verdict* v = out + d;

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -23,8 +24,9 @@
 namespace {
 
 constexpr uint64_t kAlign = 256;
-constexpr uint64_t kChunkMin = 128 * 1024;       // t_min of the chunk plans (weight units)
+constexpr uint64_t kChunkMin = 32 * 1024;        // t_min of the chunk plans (weight units)
 constexpr uint64_t kMarkRun = 1u << 20;          // marks uploaded per run
+constexpr uint64_t kHostChunks = 5;              // cg_check_host upload / check pipeline depth
 
 uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
@@ -186,7 +188,9 @@ struct cg_ctx {
   cg_mark* h_marks = nullptr;               // kMarkRun
   cudaEvent_t staged = nullptr;
   cudaStream_t copy_stream = nullptr;        // host -> device uploads of cg_check_host
-  cudaEvent_t chunk_ev[4] = {};
+  cudaEvent_t chunk_ev[kHostChunks] = {};
+  uint64_t host_chunks = 2;                   // cg_check_host pipeline (env CG_HOST_CHUNKS / CG_HOST_GEOMETRIC)
+  bool host_geometric = true;
   std::string err;
   // profiling (cg_profile_begin / end)
   cgk::Profiler prof;
@@ -392,6 +396,8 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
     return CG_ERR_OUT_OF_MEMORY;
   }
   cudaEventRecord(c->staged, 0);
+  if (const char* hc = getenv("CG_HOST_CHUNKS")) c->host_chunks = std::min<uint64_t>(std::max(atoi(hc), 1), kHostChunks);
+  if (const char* hg = getenv("CG_HOST_GEOMETRIC")) c->host_geometric = atoi(hg) != 0;
   if (cfg->host_staging) {
     if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
       cg_ctx_destroy(c);
@@ -989,14 +995,21 @@ cg_status cg_check_host(cg_ctx* c, const void* h_descs, uint32_t format, uint64_
   uint32_t* dcount = reinterpret_cast<uint32_t*>(c->ws + c->lay.flags + 192);
   const size_t esz = format == CG_FMT_1D ? sizeof(cg_copy1d) : sizeof(cg_copy_desc);
   uint8_t* dst = format == CG_FMT_1D ? reinterpret_cast<uint8_t*>(draw) : reinterpret_cast<uint8_t*>(dd);
-  const uint64_t nchunks = n >= (1u << 19) ? 4 : 1;
-  const uint64_t per = (n + nchunks - 1) / nchunks;
+  // geometric chunks (sizes 1 : 2 : 4 : ...): the first upload is short, and
+  // every later chunk's upload (PCIe, ~50 GB/s) finishes while the previous
+  // chunk is being checked (the check is slower per descriptor than the upload)
+  const uint64_t nchunks = n >= (1u << 19) ? c->host_chunks : 1;
+  uint64_t bound[kHostChunks + 1];
+  bound[0] = 0;
+  for (uint64_t k = 1; k <= nchunks; ++k)
+    bound[k] = k == nchunks ? n
+               : c->host_geometric ? n * ((1ull << k) - 1) / ((1ull << nchunks) - 1) : n * k / nchunks;
   // uploads: all chunks on the copy stream (it waits for earlier work on s first)
   cudaError_t e = cudaEventRecord(c->chunk_ev[0], s);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(c->copy_stream, c->chunk_ev[0], 0);
   for (uint64_t k = 0; k < nchunks && e == cudaSuccess; ++k) {
-    const uint64_t a = k * per, b = std::min(n, a + per);
-    if (a >= b) break;
+    const uint64_t a = bound[k], b = bound[k + 1];
+    if (a >= b) continue;
     e = cudaMemcpyAsync(dst + a * esz, static_cast<const uint8_t*>(h_descs) + a * esz, (b - a) * esz,
                         cudaMemcpyHostToDevice, c->copy_stream);
     if (e == cudaSuccess) e = cudaEventRecord(c->chunk_ev[k], c->copy_stream);
@@ -1005,8 +1018,8 @@ cg_status cg_check_host(cg_ctx* c, const void* h_descs, uint32_t format, uint64_
   e = cudaMemsetAsync(dcount, 0, sizeof(uint32_t), s);
   if (e != cudaSuccess) return c->cuda(e, "memset");
   for (uint64_t k = 0; k < nchunks; ++k) {
-    const uint64_t a = k * per, b = std::min(n, a + per);
-    if (a >= b) break;
+    const uint64_t a = bound[k], b = bound[k + 1];
+    if (a >= b) continue;
     e = cudaStreamWaitEvent(s, c->chunk_ev[k], 0);
     if (e == cudaSuccess && format == CG_FMT_1D) e = cgk::expand_1d(c->launch, draw + a, b - a, dd + a, s);
     if (e != cudaSuccess) return c->cuda(e, "chunk wait / expand");
