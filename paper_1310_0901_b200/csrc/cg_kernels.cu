@@ -671,6 +671,14 @@ __device__ __forceinline__ uint32_t pair_mask(uint64_t gb, uint64_t lo, uint64_t
   return him & ~((1u << (2 * b0)) - 1u);
 }
 
+// the same for a touched word k of a staged tile (k >= q0 >> 4, 16 k < q1; 32-bit arithmetic)
+__device__ __forceinline__ uint32_t pair_mask32(uint32_t k, uint32_t q0, uint32_t q1) {
+  const int base = (int)(k << 4);
+  const int b0 = max((int)q0 - base, 0), b1 = min((int)q1 - base, 16);
+  const uint32_t him = b1 >= 16 ? 0xffffffffu : ((1u << (2 * b1)) - 1u);
+  return him & ~((1u << (2 * b0)) - 1u);
+}
+
 // one state word: unaddressable = state 0, undefined = bit 0 (PARTIAL / UNDEFINED, always addressable)
 template <bool kHtod>
 __device__ __forceinline__ void word2(uint32_t w, uint32_t m, uint64_t gb, Partial& p) {
@@ -711,13 +719,13 @@ __device__ __forceinline__ void consume_2bit(const uint8_t* st, uint32_t q0, uin
         for (uint32_t j = 0; j < 4; ++j) word2<kHtod>(W[4 * i + j], 0xffffffffu, ob + 64ull * i + 16 * j, p);
     if (lane < 4) {
       const uint32_t k = e0 + lane;
-      if (k < 4 * g0) word2<kHtod>(W[k], pair_mask(16ull * k, q0, q1), ob + 16ull * k, p);
+      if (k < 4 * g0) word2<kHtod>(W[k], pair_mask32(k, q0, q1), ob + 16ull * k, p);
     } else if (lane < 8) {
       const uint32_t k = 4 * g1 + (lane - 4);
-      if (k < e1) word2<kHtod>(W[k], pair_mask(16ull * k, q0, q1), ob + 16ull * k, p);
+      if (k < e1) word2<kHtod>(W[k], pair_mask32(k, q0, q1), ob + 16ull * k, p);
     }
   } else {
-    for (uint32_t k = e0 + lane; k < e1; k += 32) word2<kHtod>(W[k], pair_mask(16ull * k, q0, q1), ob + 16ull * k, p);
+    for (uint32_t k = e0 + lane; k < e1; k += 32) word2<kHtod>(W[k], pair_mask32(k, q0, q1), ob + 16ull * k, p);
   }
 }
 
