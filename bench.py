@@ -147,6 +147,14 @@ class ClockSampler:
 C2_SHARD = 8 << 30        # per-rank window of the weak-scaling C2 workload (7.94 GiB used)
 
 
+def workload_name(config: str) -> str:
+    """config.workload of both arms"""
+    if config == "c2_small":
+        return ("c2_small (BASELINE.json configs[1]: 1M small copies 64 B-64 KiB log-uniform "
+                "vs a 100k-entry allocation table, 1% injected violations)")
+    return config
+
+
 def make_workload(name: str, rank: int = 0, scale: float = 1.0):
     """Rank r's workload.  Weak scaling: rank r's host buffers live in shard r
     of a global window [2^32, 2^32 + world * 8 GiB); its copies, allocations and
@@ -234,11 +242,24 @@ def run_ours(args, rank, world, device):
 
     comm = None
     if world > 1:
-        from paper_1310_0901_b200.sharded import TorchComm
-        comm = TorchComm()
+        import torch.distributed as dist
+        comm = dist
         g_idx = torch.empty(n, dtype=torch.int64, device=device)
         g_dirty = torch.empty(n * 64, dtype=torch.uint8, device=device)
         g_cnt = torch.zeros(1, dtype=torch.int32, device=device)
+        # one untimed probe fixes the padded gather size (the batch is the same every step)
+        if fused:
+            chk.check_apply(d_descs, d_out, stream=stream)
+        else:
+            chk.check_copies(d_descs, d_out, stream=stream)
+        cg.cg_compact_dirty(chk.ctx, d_out.data_ptr(), n, g_idx.data_ptr(), g_dirty.data_ptr(),
+                            g_cnt.data_ptr(), stream.cuda_stream)
+        mx_t = g_cnt.to(torch.int64)
+        dist.all_reduce(mx_t, op=dist.ReduceOp.MAX)
+        mx = max(1, int(mx_t.item()))
+        all_cnt = torch.zeros(world, dtype=torch.int32, device=device)
+        all_idx = torch.empty(world * mx, dtype=torch.int64, device=device)
+        all_dirty = torch.empty(world * mx * 64, dtype=torch.uint8, device=device)
 
     def step():
         if args.track:      # NEXT-1: check, then V-bit propagation
@@ -251,10 +272,13 @@ def run_ours(args, rank, world, device):
             chk.apply_dtoh(d_descs, d_out, stream=stream)
         chk.leak_sweep(d_leaks, nalloc, d_cnt, stream=stream)
         if comm is not None:
-            # the exchange: compacted dirty verdicts of every rank to the root (NCCL)
+            # the exchange: every rank's compacted dirty verdicts (count, index,
+            # 64-byte verdict) gathered over NCCL, device to device, no host sync
             cg.cg_compact_dirty(chk.ctx, d_out.data_ptr(), n, g_idx.data_ptr(), g_dirty.data_ptr(),
                                 g_cnt.data_ptr(), stream.cuda_stream)
-            comm.gather_dirty(g_cnt, g_idx, g_dirty)
+            comm.all_gather_into_tensor(all_cnt, g_cnt)
+            comm.all_gather_into_tensor(all_idx, g_idx[:mx])
+            comm.all_gather_into_tensor(all_dirty, g_dirty[:mx * 64])
 
     for _ in range(args.warmup):
         step()
@@ -278,6 +302,9 @@ def run_ours(args, rank, world, device):
     stages = chk.profile_end()
     if world > 1:
         torch.distributed.barrier()
+        tot = g_cnt.to(torch.int64)
+        torch.distributed.all_reduce(tot)
+        assert int(all_cnt.to(torch.int64).sum().item()) == int(tot.item()), "dirty-verdict gather lost records"
     launches = chk.kernel_launches - launches0
     ms = ev0.elapsed_time(ev1)
     if world > 1:
@@ -360,8 +387,7 @@ def run_ours(args, rank, world, device):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": f"{args.config} (BASELINE.json configs[1]: 1M small copies 64 B-64 KiB log-uniform "
-                               f"vs a 100k-entry allocation table, 1% injected violations)" if args.config == "c2_small" else args.config,
+        "config": {"workload": workload_name(args.config),
                    "descriptors_per_step": n, "allocations": nreg, "host_window_bytes": tr.host_size,
                    "shadow_bytes_per_step": bytes_per_step, "check_bytes": check_b, "apply_bytes": apply_b,
                    "l2": "no flush: >= 8.5 GB of shadow streamed per step vs 126 MB L2",
@@ -521,7 +547,7 @@ def main():
         out = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_t / args.steps * 1e3,
                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-               "data": "synthetic", "config": {"workload": args.config},
+               "data": "synthetic", "config": {"workload": workload_name(args.config)},
                "cpu_baseline": arm.describe(val, tot_t, args.steps),
                "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(out))

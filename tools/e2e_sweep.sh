@@ -1,7 +1,7 @@
 #!/bin/bash
 # e2e (cg_check_host) pipeline sweep: chunk count x geometric sizes
 mkdir -p gpurun_out
-for g in 0 1; do for c in 1 2 3 4 5; do
+for g in 1; do for c in 2 3 4 5; do
   CG_HOST_CHUNKS=$c CG_HOST_GEOMETRIC=$g timeout 300 python bench.py --steps 12 --warmup 3 --no-cpu-baseline --no-registry-rate \
     > gpurun_out/e2e_c${c}_g${g}.json 2>/dev/null
   python -c "import json; d=json.load(open('gpurun_out/e2e_c${c}_g${g}.json')); print('chunks $c geo $g', round(d['ms_per_step'],3), round(d['e2e']['ms_per_step'],3))" >> gpurun_out/e2e_sweep.txt
