@@ -238,7 +238,25 @@ def run_ours(args, rank, world, device):
 
     # the batch is one epoch; if no HtoD range overlaps a DtoH range the check
     # and the apply run fused (cg_check_apply), else as two calls
-    fused = cg.batch_disjoint(descs) and not args.unfused and not args.track
+    # the batch contract (R-20): the copies are checked in the epochs
+    # cg_plan_batches cuts (one epoch for C2-C4; C5's ping-pongs make ~11); an
+    # epoch whose HtoD and DtoH host ranges are disjoint runs fused
+    cuts = [0] + [int(c) for c in cg.plan_batches(descs, propagate=args.track)]
+    epochs = [(a, b) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
+    efused = [cg.batch_disjoint(descs[a:b]) and not args.unfused and not args.track for a, b in epochs]
+    fused = all(efused)
+
+    def check_epochs():
+        for (a, b), fu in zip(epochs, efused):
+            dd, dv = d_descs[a * 96:b * 96], d_out[a * 64:b * 64]
+            if args.track:      # NEXT-1: check, then V-bit propagation
+                chk.check_copies(dd, dv, stream=stream)
+                chk.apply_copies(dd, dv, stream=stream)
+            elif fu:
+                chk.check_apply(dd, dv, stream=stream)
+            else:
+                chk.check_copies(dd, dv, stream=stream)
+                chk.apply_dtoh(dd, dv, stream=stream)
 
     comm = None
     if world > 1:
@@ -248,10 +266,7 @@ def run_ours(args, rank, world, device):
         g_dirty = torch.empty(n * 64, dtype=torch.uint8, device=device)
         g_cnt = torch.zeros(1, dtype=torch.int32, device=device)
         # one untimed probe fixes the padded gather size (the batch is the same every step)
-        if fused:
-            chk.check_apply(d_descs, d_out, stream=stream)
-        else:
-            chk.check_copies(d_descs, d_out, stream=stream)
+        check_epochs()
         cg.cg_compact_dirty(chk.ctx, d_out.data_ptr(), n, g_idx.data_ptr(), g_dirty.data_ptr(),
                             g_cnt.data_ptr(), stream.cuda_stream)
         mx_t = g_cnt.to(torch.int64)
@@ -262,14 +277,7 @@ def run_ours(args, rank, world, device):
         all_dirty = torch.empty(world * mx * 64, dtype=torch.uint8, device=device)
 
     def step():
-        if args.track:      # NEXT-1: check, then V-bit propagation
-            chk.check_copies(d_descs, d_out, stream=stream)
-            chk.apply_copies(d_descs, d_out, stream=stream)
-        elif fused:
-            chk.check_apply(d_descs, d_out, stream=stream)
-        else:
-            chk.check_copies(d_descs, d_out, stream=stream)
-            chk.apply_dtoh(d_descs, d_out, stream=stream)
+        check_epochs()
         chk.leak_sweep(d_leaks, nalloc, d_cnt, stream=stream)
         if comm is not None:
             # the exchange: every rank's compacted dirty verdicts (count, index,
@@ -337,11 +345,20 @@ def run_ours(args, rank, world, device):
         h_dirty = torch.empty(cap * 64, dtype=torch.uint8).pin_memory()
         nd_box = ctypes.c_uint64(0)
 
+        e_base = []   # per epoch: first dirty slot in the host result buffers
+
         def e2e_step():
-            st = cg.cg_check_host(chk.ctx, hd.ctypes.data, cg.CG_FMT_1D if is1d else cg.CG_FMT_2D, n,
-                                  2 if fused else 1, h_idx.data_ptr(), h_dirty.data_ptr(), cap, ctypes.byref(nd_box),
-                                  stream.cuda_stream)
-            assert st == 0
+            e_base.clear()
+            got = 0
+            for (a, b), fu in zip(epochs, efused):
+                st = cg.cg_check_host(chk.ctx, hd.ctypes.data + a * hd.dtype.itemsize,
+                                      cg.CG_FMT_1D if is1d else cg.CG_FMT_2D, b - a, 2 if fu else 1,
+                                      h_idx.data_ptr() + got * 8, h_dirty.data_ptr() + got * 64, cap - got,
+                                      ctypes.byref(nd_box), stream.cuda_stream)
+                assert st == 0
+                e_base.append(got)
+                got += nd_box.value
+            nd_box.value = got
             chk.leak_sweep(d_leaks, nalloc, d_cnt, stream=stream)
         for _ in range(max(1, args.warmup // 2)):
             e2e_step()
@@ -361,7 +378,10 @@ def run_ours(args, rank, world, device):
         assert nd_box.value == n_dirty_ref
         dense = verd.copy()
         dense["flags"] = 0
-        dense[h_idx.numpy()[:n_dirty_ref]] = h_dirty.numpy()[:n_dirty_ref * 64].view(cg.VERDICT_DTYPE)
+        gidx = h_idx.numpy()[:n_dirty_ref].copy()
+        for (a, _), g0, g1 in zip(epochs, e_base, e_base[1:] + [n_dirty_ref]):
+            gidx[g0:g1] += a   # epoch-relative indices -> batch indices
+        dense[gidx] = h_dirty.numpy()[:n_dirty_ref * 64].view(cg.VERDICT_DTYPE)
         assert np.array_equal(dense["flags"], verd["flags"])
         e2e = {"value": world * bytes_per_step / (e_ms * 1e-3) / 1e9, "unit": UNIT,
                "ms_per_step": e_ms, "entry": "cg_check_host (%s descriptors, dirty-only result)" % ("1D" if is1d else "2D"),
@@ -372,8 +392,10 @@ def run_ours(args, rank, world, device):
     scan_ms, scan_n = stages["check_scan"]
     apply_ms, apply_n = stages["apply"]
     scan_avg = scan_ms / max(scan_n, 1)
-    scan_bytes = check_b + (fused_apply_bytes(descs, verd, max(n, 1024), two_bit) if fused else 0.0)
-    achieved = scan_bytes / (scan_avg * 1e-3) / 1e9
+    scan_bytes = check_b + sum(fused_apply_bytes(descs[a:b], verd[a:b], max(n, 1024), two_bit)
+                               for (a, b), fu in zip(epochs, efused) if fu)
+    launches_scan = max(scan_n / max(args.steps, 1), 1.0)   # one per epoch
+    achieved = scan_bytes / (scan_avg * launches_scan * 1e-3) / 1e9
     traffic = None
     suffix = "" if args.shadow == "bytes" else "_" + args.shadow
     prof_json = os.path.join(ROOT, "profiles", f"ncu_{args.config}{suffix}_check_scan.json")
@@ -395,16 +417,18 @@ def run_ours(args, rank, world, device):
                    "shadow_format": {"bytes": "V bytes + A bits", "2bit": "2-bit states (NEXT-4)",
                                      "sparse": "2-bit states in the two-level sparse map (NEXT-4)"}[args.shadow],
                    "entry": ("cg_check_copies + cg_apply_copies (NEXT-1 V-bit propagation)" if args.track else
-                             "cg_check_apply (fused)" if fused else "cg_check_copies + cg_apply_dtoh")},
+                             "cg_check_apply (fused)" if fused else "cg_check_copies + cg_apply_dtoh"
+                             if not any(efused) else "cg_check_apply / cg_check_copies + cg_apply_dtoh per epoch"),
+                   "epochs": len(epochs)},
         "descriptors_per_s": world * n / (ms_step * 1e-3),
         "frac_of_hbm": value / (world * peak),
         "roofline": {"bound": "hbm", "kernel": "k_check_scan", "achieved": achieved, "peak": peak,
                      "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "algorithmic_bytes_per_launch": scan_bytes,
+                     "traffic": traffic, "algorithmic_bytes_per_launch": scan_bytes / launches_scan,
                      "avg_launch_ms": scan_avg,
                      "share_of_step": scan_ms / ms if ms > 0 else None},
         "stages_ms_per_step": {k: v[0] / max(args.steps, 1) for k, v in stages.items()},
-        "apply_roofline": {"achieved": (apply_b - (scan_bytes - check_b)) / (apply_ms / max(apply_n, 1) * 1e-3) / 1e9
+        "apply_roofline": {"achieved": (apply_b - (scan_bytes - check_b)) / (apply_ms / max(args.steps, 1) * 1e-3) / 1e9
                            if apply_ms else None, "unit": "GB/s", "peak": peak,
                            "note": "k_apply alone (the residual pass when fused)"},
         "gpu_launches": int(launches),
