@@ -60,15 +60,33 @@ __device__ __forceinline__ uint32_t pred32(const uint32_t* a, uint64_t n, uint32
   return lo ? a[lo - 1] : kNoKey;
 }
 
-// the same over the low halves of (node << 32 | key) pairs of one node list
-__device__ __forceinline__ uint32_t pred_pairs(const uint64_t* a, uint64_t b, uint64_t e, uint32_t lim) {
+// the same over the keys of (node << kb | key) pairs of one node list
+__device__ __forceinline__ uint32_t pred_pairs(const uint64_t* a, uint64_t b, uint64_t e, uint32_t lim, uint64_t kmask) {
   uint64_t lo = b, hi = e;
   while (lo < hi) {
     const uint64_t mid = (lo + hi) >> 1;
-    if ((uint32_t)a[mid] < lim) lo = mid + 1; else hi = mid;
+    if ((uint32_t)(a[mid] & kmask) < lim) lo = mid + 1; else hi = mid;
   }
-  return lo > b ? (uint32_t)a[lo - 1] : kNoKey;
+  return lo > b ? (uint32_t)(a[lo - 1] & kmask) : kNoKey;
 }
+
+__device__ __forceinline__ uint64_t warp_min64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_max64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
 
 __device__ __forceinline__ uint32_t kmax(uint32_t a, uint32_t b) {
   return a == kNoKey ? b : b == kNoKey ? a : (a > b ? a : b);
@@ -99,62 +117,110 @@ __device__ __forceinline__ int copy_accesses(uint32_t kind, int sp[2], int dst[2
   }
 }
 
-__global__ void k_hist_to_r(Space S0, Space S1, uint64_t nh0, uint64_t nh1) {
-  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (i < nh0) { S0.rs[i] = S0.hs[i]; S0.re[i] = S0.he[i]; S0.rkey[i] = 2u * (uint32_t)i + S0.hw[i]; }
-  if (i < nh1) { S1.rs[i] = S1.hs[i]; S1.re[i] = S1.he[i]; S1.rkey[i] = 2u * (uint32_t)i + S1.hw[i]; }
+
+
+// block-level aggregation of the per-space key ranges: one atomic per block and value
+__device__ __forceinline__ void block_range(unsigned long long* counts, const uint64_t mn[2], const uint64_t mx[2]) {
+  __shared__ uint64_t red[kT / 32][4];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint64_t v[4] = {warp_min64(mn[0]), warp_max64(mx[0]), warp_min64(mn[1]), warp_max64(mx[1])};
+  if (lane == 0)
+    for (int k = 0; k < 4; ++k) red[w][k] = v[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int j = 1; j < (int)(blockDim.x >> 5); ++j) {
+      v[0] = min(v[0], red[j][0]);
+      v[1] = max(v[1], red[j][1]);
+      v[2] = min(v[2], red[j][2]);
+      v[3] = max(v[3], red[j][3]);
+    }
+    for (int sp = 0; sp < 2; ++sp)
+      if (v[2 * sp] <= v[2 * sp + 1]) {
+        atomicMin(counts + 8 + 2 * sp, (unsigned long long)v[2 * sp]);
+        atomicMax(counts + 9 + 2 * sp, (unsigned long long)v[2 * sp + 1]);
+      }
+  }
 }
 
-// warp-aggregated slot allocation: one atomic per warp and counter
-__device__ __forceinline__ unsigned long long warp_slot(bool want, unsigned long long* counter) {
-  const uint32_t m = __ballot_sync(0xffffffffu, want);
-  if (!m) return 0;
-  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
-  unsigned long long base = 0;
-  if (lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(m));
-  base = __shfl_sync(0xffffffffu, base, leader);
-  return base + __popc(m & ((1u << lane) - 1u));
+__global__ void __launch_bounds__(kT) k_hist_to_r(Space S0, Space S1, uint64_t nh0, uint64_t nh1,
+                                                  unsigned long long* counts) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t mn[2] = {~0ull, ~0ull}, mx[2] = {0, 0};
+  if (i < nh0) {
+    S0.rs[i] = mn[0] = S0.hs[i];
+    S0.re[i] = mx[0] = S0.he[i];
+    S0.rkey[i] = 2u * (uint32_t)i + S0.hw[i];
+  }
+  if (i < nh1) {
+    S1.rs[i] = mn[1] = S1.hs[i];
+    S1.re[i] = mx[1] = S1.he[i];
+    S1.rkey[i] = 2u * (uint32_t)i + S1.hw[i];
+  }
+  block_range(counts, mn, mx);
 }
 
 // one thread per copy: its accesses become queries; performed copies' accesses
-// are appended to R (R-33, R-34).  counts: [qn0, qn1, rn0, rn1]
-__global__ void k_access(const cg_copy_desc* __restrict__ d, const cg_verdict* __restrict__ v, uint64_t n,
-                         Space S0, Space S1, uint64_t nh0, uint64_t nh1, unsigned long long* counts) {
+// are appended to R (R-33, R-34).  Slots come from one block-wide exclusive
+// scan of the four packed counters and one atomic per block and counter.
+// counts: [qn0, qn1, rn0, rn1, ...]
+__global__ void __launch_bounds__(kT) k_access(const cg_copy_desc* __restrict__ d, const cg_verdict* __restrict__ v,
+                                               uint64_t n, Space S0, Space S1, uint64_t nh0, uint64_t nh1,
+                                               unsigned long long* counts) {
+  using Scan = cub::BlockScan<unsigned long long, kT>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ unsigned long long s_base[4];
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   int sp[2] = {0, 0}, dst[2] = {0, 0}, wr[2] = {0, 0};
-  int na = 0;
-  bool performed = false;
-  cg_copy_desc c;
+  bool ok[2] = {false, false}, performed = false;
+  uint64_t st[2] = {0, 0}, sn[2] = {0, 0};
   if (i < n) {
-    c = d[i];
-    na = copy_accesses(c.kind, sp, dst, wr);
+    const cg_copy_desc c = d[i];
+    const int na = copy_accesses(c.kind, sp, dst, wr);
     performed = v[i].status == CG_OK;
-  }
-  for (int k = 0; k < 2; ++k) {   // warp-uniform loop: every lane takes part in the ballots
-    uint64_t start = 0, span = 0;
-    bool ok = false;
-    if (k < na) {
-      ok = dst[k] ? cgk::fold_side(c.dst, c.dst_x, c.dst_y, c.dst_pitch, c.width, c.height, start, span)
-                  : cgk::fold_side(c.src, c.src_x, c.src_y, c.src_pitch, c.width, c.height, start, span);
-      ok = ok && span != 0;
+    for (int k = 0; k < na; ++k) {
+      ok[k] = dst[k] ? cgk::fold_side(c.dst, c.dst_x, c.dst_y, c.dst_pitch, c.width, c.height, st[k], sn[k])
+                     : cgk::fold_side(c.src, c.src_x, c.src_y, c.src_pitch, c.width, c.height, st[k], sn[k]);
+      ok[k] = ok[k] && sn[k] != 0;
     }
-    for (int space = 0; space < 2; ++space) {
-      const bool mine = ok && sp[k] == space;
-      const unsigned long long q = warp_slot(mine, counts + space);
-      const unsigned long long r = warp_slot(mine && performed, counts + 2 + space);
-      if (!mine) continue;
-      Space& S = space ? S1 : S0;
-      const uint64_t nh = space ? nh1 : nh0;
-      const uint32_t key = 2u * (uint32_t)(nh + i) + (uint32_t)wr[k];
-      S.qs[q] = start;
-      S.qe[q] = start + span;
-      S.qkey[q] = key;
-      S.qcopy[q] = (uint32_t)i;
-      if (performed) {
-        S.rs[nh + r] = start;
-        S.re[nh + r] = start + span;
-        S.rkey[nh + r] = key;
-      }
+  }
+  // packed 16-bit counters: queries of space 0 / 1, recorded of space 0 / 1 (<= 2 each per thread)
+  unsigned long long mine = 0;
+  uint64_t mn[2] = {~0ull, ~0ull}, mx[2] = {0, 0};
+  for (int k = 0; k < 2; ++k) {
+    if (!ok[k]) continue;
+    mine += 1ull << (16 * sp[k]);
+    if (performed) {
+      mine += 1ull << (16 * (2 + sp[k]));
+      mn[sp[k]] = min(mn[sp[k]], st[k]);
+      mx[sp[k]] = max(mx[sp[k]], st[k] + sn[k]);
+    }
+  }
+  unsigned long long pre, tot;
+  Scan(scan_tmp).ExclusiveSum(mine, pre, tot);
+  if (threadIdx.x == 0)
+    for (int c = 0; c < 4; ++c) {
+      const unsigned long long t = (tot >> (16 * c)) & 0xffffull;
+      s_base[c] = t ? atomicAdd(counts + c, t) : 0ull;
+    }
+  block_range(counts, mn, mx);   // contains the __syncthreads that publishes s_base
+  unsigned long long q[2] = {s_base[0] + (pre & 0xffffull), s_base[1] + ((pre >> 16) & 0xffffull)};
+  unsigned long long r[2] = {s_base[2] + ((pre >> 32) & 0xffffull), s_base[3] + ((pre >> 48) & 0xffffull)};
+  for (int k = 0; k < 2; ++k) {
+    if (!ok[k]) continue;
+    const int space = sp[k];
+    Space& S = space ? S1 : S0;
+    const uint64_t nh = space ? nh1 : nh0;
+    const uint32_t key = 2u * (uint32_t)(nh + i) + (uint32_t)wr[k];
+    const unsigned long long qq = q[space]++;
+    S.qs[qq] = st[k];
+    S.qe[qq] = st[k] + sn[k];
+    S.qkey[qq] = key;
+    S.qcopy[qq] = (uint32_t)i;
+    if (performed) {
+      const unsigned long long rr = nh + r[space]++;
+      S.rs[rr] = st[k];
+      S.re[rr] = st[k] + sn[k];
+      S.rkey[rr] = key;
     }
   }
 }
@@ -245,7 +311,7 @@ __global__ void k_cover_count(const uint64_t* __restrict__ rs, const uint64_t* _
 __global__ void k_cover_emit(const uint64_t* __restrict__ rs, const uint64_t* __restrict__ re,
                              const uint32_t* __restrict__ rkey, uint64_t n, const uint64_t* __restrict__ coords,
                              const unsigned long long* __restrict__ m_dev, uint64_t M,
-                             const uint32_t* __restrict__ off, uint64_t* __restrict__ pairs) {
+                             const uint32_t* __restrict__ off, uint64_t* __restrict__ pairs, int kb) {
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   uint64_t l, r;
@@ -253,16 +319,28 @@ __global__ void k_cover_emit(const uint64_t* __restrict__ rs, const uint64_t* __
   uint64_t o = off[i];
   const uint64_t key = rkey[i];
   for (l += M, r += M; l < r; l >>= 1, r >>= 1) {
-    if (l & 1) pairs[o++] = (l++ << 32) | key;
-    if (r & 1) pairs[o++] = (--r << 32) | key;
+    if (l & 1) pairs[o++] = (l++ << kb) | key;
+    if (r & 1) pairs[o++] = (--r << kb) | key;
   }
 }
 
-__global__ void k_node_offsets(const uint64_t* __restrict__ pairs, uint64_t P, uint64_t nodes,
-                               uint32_t* __restrict__ noff) {
-  const uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (v <= nodes) noff[v] = (uint32_t)lower_bound64(pairs, P, v << 32);
+// node list offsets: off(v) = first pair with node >= v.  The first pair of
+// every node list is scattered to rev[nodes - node] (rev pre-filled with P),
+// then an inclusive min-scan over rev fills the empty nodes: off(v) = scanned[nodes - v]
+__global__ void k_fill_u32(uint32_t* __restrict__ a, uint64_t n, uint32_t val) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < n) a[i] = val;
 }
+__global__ void k_node_starts(const uint64_t* __restrict__ pairs, uint64_t P, int kb, uint64_t nodes,
+                              uint32_t* __restrict__ rev) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const uint64_t node = pairs[i] >> kb;
+  if (i == 0 || (pairs[i - 1] >> kb) != node) rev[nodes - node] = (uint32_t)i;
+}
+struct MinU32 {
+  __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a < b ? a : b; }
+};
 
 struct Syncs {
   const uint32_t* thr;   // sorted by (thread, seq)
@@ -288,9 +366,11 @@ struct Tree {
   int levels;
   const uint64_t* coords;
   const unsigned long long* m_dev;
-  const uint32_t* noff;
+  const uint32_t* noff;   // reversed: the offset of node v is noff[nodes - v]
+  uint64_t nodes;
   const uint64_t* pairs;
   uint64_t M;
+  uint64_t kmask;   // key bits of a pair (node << kb | key)
 };
 
 __device__ uint32_t newest_overlap(const Tree& T, uint64_t s, uint64_t e, uint32_t lim) {
@@ -315,7 +395,7 @@ __device__ uint32_t newest_overlap(const Tree& T, uint64_t s, uint64_t e, uint32
   const uint64_t k1 = lower_bound64(T.coords, m, s + 1);   // coords[k] <= s < coords[k+1]
   if (k1 > 0 && k1 < m) {
     for (uint64_t v = T.M + (k1 - 1); v >= 1; v >>= 1)
-      best = kmax(best, pred_pairs(T.pairs, T.noff[v], T.noff[v + 1], lim));
+      best = kmax(best, pred_pairs(T.pairs, T.noff[T.nodes - v], T.noff[T.nodes - v - 1], lim, T.kmask));
   }
   return best;
 }
@@ -355,8 +435,8 @@ __global__ void k_winners(Tree T, uint32_t* __restrict__ win) {
   if (k + 1 >= m) return;
   uint32_t best = kNoKey;
   for (uint64_t v = T.M + k; v >= 1; v >>= 1) {
-    const uint32_t b = T.noff[v], e = T.noff[v + 1];
-    if (e > b) best = kmax(best, (uint32_t)T.pairs[e - 1]);
+    const uint32_t b = T.noff[T.nodes - v], e = T.noff[T.nodes - v - 1];
+    if (e > b) best = kmax(best, (uint32_t)(T.pairs[e - 1] & T.kmask));
   }
   win[k] = best;
 }
@@ -420,7 +500,7 @@ struct cg_conc {
   uint64_t *qs[2], *qe[2];
   uint32_t *qkey[2], *qcopy[2];
   uint64_t *rs, *re, *rs_sorted, *ep, *ep_sorted, *coords;
-  uint32_t *rkey, *mst, *cnt, *off, *noff, *win, *flag, *pos, *tkey, *tidx, *tkey2, *tidx2;
+  uint32_t *rkey, *mst, *cnt, *off, *noff, *noff2, *win, *flag, *pos, *tkey, *tidx, *tkey2, *tidx2;
   uint64_t *ts, *te;
   uint64_t* pairs = nullptr;
   uint64_t* pairs2 = nullptr;
@@ -514,7 +594,7 @@ struct cg_conc {
     if (h_counts) cudaFreeHost(h_counts);
   }
   cg_status run_space(int sp, const cg_copy_desc* d, const uint32_t* threads, uint64_t n, cg_verdict* v,
-                      uint64_t qn, uint64_t rn, cudaStream_t s);
+                      uint64_t qn, uint64_t rn, int addr_bits, cudaStream_t s);
 };
 
 namespace {
@@ -531,7 +611,7 @@ int ceil_log2(uint64_t x) {
 }  // namespace
 
 cg_status cg_conc::run_space(int sp, const cg_copy_desc* d, const uint32_t* threads, uint64_t n, cg_verdict* v,
-                             uint64_t qn, uint64_t rn, cudaStream_t s) {
+                             uint64_t qn, uint64_t rn, int addr_bits, cudaStream_t s) {
   const uint64_t nh0 = nh[sp];
   if (qn == 0) return CG_OK;   // no access of this space in the batch: nothing recorded either
   Space S = space(sp);
@@ -545,9 +625,10 @@ cg_status cg_conc::run_space(int sp, const cg_copy_desc* d, const uint32_t* thre
   const uint64_t M = next_pow2(std::max<uint64_t>(2 * rn, 2));
   if (rn) {
     // (A) merge-sort tree over R sorted by start
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, S.rs, rs_sorted, S.rkey, mst, (int)rn, 0, 64, s);
+    // R's addresses share every bit above addr_bits: sort only the bits that differ
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, S.rs, rs_sorted, S.rkey, mst, (int)rn, 0, addr_bits, s);
     if (ensure_temp(tb) != CG_OK) return CG_ERR_OUT_OF_MEMORY;
-    e = cub::DeviceRadixSort::SortPairs(temp, tb, S.rs, rs_sorted, S.rkey, mst, (int)rn, 0, 64, s);
+    e = cub::DeviceRadixSort::SortPairs(temp, tb, S.rs, rs_sorted, S.rkey, mst, (int)rn, 0, addr_bits, s);
     if (e != cudaSuccess) return cuda(e, "sort R");
     const int L = ceil_log2(rn);
     const int Ls = std::min(L, kSmemLevels);   // levels inside 256-key tiles: one pass in shared memory
@@ -567,9 +648,9 @@ cg_status cg_conc::run_space(int sp, const cg_copy_desc* d, const uint32_t* thre
     k_endpoints<<<grid_for(rn), kT, 0, s>>>(S.rs, S.re, rn, ep);
     ++launches;
     tb = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, tb, ep, ep_sorted, (int)(2 * rn), 0, 64, s);
+    cub::DeviceRadixSort::SortKeys(nullptr, tb, ep, ep_sorted, (int)(2 * rn), 0, addr_bits, s);
     if (ensure_temp(tb) != CG_OK) return CG_ERR_OUT_OF_MEMORY;
-    e = cub::DeviceRadixSort::SortKeys(temp, tb, ep, ep_sorted, (int)(2 * rn), 0, 64, s);
+    e = cub::DeviceRadixSort::SortKeys(temp, tb, ep, ep_sorted, (int)(2 * rn), 0, addr_bits, s);
     if (e != cudaSuccess) return cuda(e, "sort endpoints");
     tb = 0;
     cub::DeviceSelect::Unique(nullptr, tb, ep_sorted, coords, counts + 4, (int)(2 * rn), s);
@@ -590,21 +671,30 @@ cg_status cg_conc::run_space(int sp, const cg_copy_desc* d, const uint32_t* thre
     if (e != cudaSuccess) return cuda(e, "cover total");
     const uint64_t P = (uint64_t)tail[0] + tail[1];
     if (ensure_pairs(P) != CG_OK) return CG_ERR_OUT_OF_MEMORY;
-    k_cover_emit<<<grid_for(rn), kT, 0, s>>>(S.rs, S.re, S.rkey, rn, coords, counts + 4, M, off, pairs2);
+    const int kb = std::max(ceil_log2(2 * (nh0 + n) + 2), 1);   // bits of a key (2 ord + is_write)
+    k_cover_emit<<<grid_for(rn), kT, 0, s>>>(S.rs, S.re, S.rkey, rn, coords, counts + 4, M, off, pairs2, kb);
     ++launches;
-    const int end_bit = 32 + ceil_log2(2 * M) + 1;
+    const int end_bit = kb + ceil_log2(2 * M) + 1;
     tb = 0;
     cub::DeviceRadixSort::SortKeys(nullptr, tb, pairs2, pairs, (int)P, 0, end_bit, s);
     if (ensure_temp(tb) != CG_OK) return CG_ERR_OUT_OF_MEMORY;
     e = cub::DeviceRadixSort::SortKeys(temp, tb, pairs2, pairs, (int)P, 0, end_bit, s);
     if (e != cudaSuccess) return cuda(e, "sort cover pairs");
-    k_node_offsets<<<grid_for(2 * M + 1), kT, 0, s>>>(pairs, P, 2 * M, noff);
-    ++launches;
+    k_fill_u32<<<grid_for(2 * M + 1), kT, 0, s>>>(noff2, 2 * M + 1, (uint32_t)P);
+    k_node_starts<<<grid_for(P), kT, 0, s>>>(pairs, P, kb, 2 * M, noff2);
+    launches += 2;
+    tb = 0;
+    cub::DeviceScan::InclusiveScan(nullptr, tb, noff2, noff, MinU32(), (int)(2 * M + 1), s);
+    if (ensure_temp(tb) != CG_OK) return CG_ERR_OUT_OF_MEMORY;
+    e = cub::DeviceScan::InclusiveScan(temp, tb, noff2, noff, MinU32(), (int)(2 * M + 1), s);
+    if (e != cudaSuccess) return cuda(e, "node offsets");
     T.coords = coords;
     T.m_dev = counts + 4;
     T.noff = noff;
+    T.nodes = 2 * M;
     T.pairs = pairs;
     T.M = M;
+    T.kmask = (1ull << kb) - 1;
     k_query<<<grid_for(qn), kT, 0, s>>>(S, qn, T, st, sy, v);
     ++launches;
     e = cudaGetLastError();
@@ -676,11 +766,11 @@ cg_status cg_conc_create(int device, uint64_t max_n, uint64_t max_stamps, cg_con
   ok = ok && c->alloc(c->rs, 2 * cap) && c->alloc(c->re, 2 * cap) && c->alloc(c->rkey, 2 * cap) &&
        c->alloc(c->rs_sorted, cap) && c->alloc(c->ep, ncap) && c->alloc(c->ep_sorted, ncap) &&
        c->alloc(c->coords, ncap) && c->alloc(c->mst, (uint64_t)c->levels * cap) && c->alloc(c->cnt, cap) &&
-       c->alloc(c->off, cap) && c->alloc(c->noff, 2 * next_pow2(ncap) + 2) && c->alloc(c->win, ncap) &&
+       c->alloc(c->off, cap) && c->alloc(c->noff, 2 * next_pow2(ncap) + 2) && c->alloc(c->noff2, 2 * next_pow2(ncap) + 2) && c->alloc(c->win, ncap) &&
        c->alloc(c->flag, ncap) && c->alloc(c->pos, ncap) && c->alloc(c->tkey, ncap) && c->alloc(c->tidx, ncap) &&
        c->alloc(c->tkey2, ncap) && c->alloc(c->tidx2, ncap) && c->alloc(c->ts, ncap) && c->alloc(c->te, ncap) &&
-       c->alloc(c->counts, 8);
-  ok = ok && cudaMallocHost(&c->h_counts, 8 * sizeof(unsigned long long)) == cudaSuccess;
+       c->alloc(c->counts, 16);
+  ok = ok && cudaMallocHost(&c->h_counts, 16 * sizeof(unsigned long long)) == cudaSuccess;
   if (prev >= 0) cudaSetDevice(prev);
   if (!ok) {
     delete c;
@@ -725,24 +815,28 @@ cg_status cg_conc_check(cg_conc* c, const cg_copy_desc* d_descs, const uint32_t*
   cudaError_t e = cudaSuccess;
   if (st == CG_OK) {
     // counts: queries per space, recorded batch accesses per space (R holds the map first)
-    e = cudaMemsetAsync(c->counts, 0, 8 * sizeof(unsigned long long), s);
+    e = cudaMemsetAsync(c->counts, 0, 16 * sizeof(unsigned long long), s);
+    for (int sp = 0; sp < 2 && e == cudaSuccess; ++sp)   // min start of R per space
+      e = cudaMemsetAsync(c->counts + 8 + 2 * sp, 0xFF, sizeof(unsigned long long), s);
     Space S0 = c->space(0), S1 = c->space(1);
     const uint64_t mh = std::max(c->nh[0], c->nh[1]);
     if (e == cudaSuccess && mh) {
-      k_hist_to_r<<<grid_for(mh), kT, 0, s>>>(S0, S1, c->nh[0], c->nh[1]);
+      k_hist_to_r<<<grid_for(mh), kT, 0, s>>>(S0, S1, c->nh[0], c->nh[1], c->counts);
       ++c->launches;
     }
     if (e == cudaSuccess) {
       k_access<<<grid_for(n), kT, 0, s>>>(d_descs, d_verdicts, n, S0, S1, c->nh[0], c->nh[1], c->counts);
       ++c->launches;
-      e = cudaMemcpyAsync(c->h_counts, c->counts, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+      e = cudaMemcpyAsync(c->h_counts, c->counts, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) st = c->cuda(e, "access kernels");
   }
   for (int sp = 0; sp < 2 && st == CG_OK; ++sp) {
     const uint64_t qn = c->h_counts[sp], rn = c->nh[sp] + c->h_counts[2 + sp];
-    st = c->run_space(sp, d_descs, d_threads, n, d_verdicts, qn, rn, s);
+    const uint64_t lo = c->h_counts[8 + 2 * sp], hi = c->h_counts[9 + 2 * sp];
+    const int bits = lo < hi ? 64 - __builtin_clzll(lo ^ hi) : 1;   // the address bits R's keys differ in
+    st = c->run_space(sp, d_descs, d_threads, n, d_verdicts, qn, rn, std::max(bits, 1), s);
   }
   if (prev >= 0) cudaSetDevice(prev);
   return st;
