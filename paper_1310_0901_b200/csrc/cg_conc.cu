@@ -247,6 +247,34 @@ __global__ void k_merge_level(const uint32_t* __restrict__ in, uint32_t* __restr
   out[(((b < sib) ? b : sib) << (L - 1)) + r + c] = key;
 }
 
+// keys of the sorted run [s0, min(s0 + h, n)) below key (0 if the run is empty)
+__device__ __forceinline__ uint64_t count_below(const uint32_t* __restrict__ in, uint64_t s0, uint64_t h, uint64_t n,
+                                                uint32_t key) {
+  if (s0 >= n) return 0;
+  uint64_t lo = s0, hi = s0 + h < n ? s0 + h : n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (in[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo - s0;
+}
+
+// levels L and L+1 at once from level L-1 (runs of h = 2^(L-1)): an element's
+// place among its 2 and its 4 runs
+__global__ void k_merge_2levels(const uint32_t* __restrict__ in, uint32_t* __restrict__ outL,
+                                uint32_t* __restrict__ outL1, uint64_t n, int L) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int sh = L - 1;
+  const uint64_t h = 1ull << sh, b = i >> sh, r = i - (b << sh), key_b = b;
+  const uint32_t key = in[i];
+  const uint64_t sib = key_b ^ 1ull, q0 = key_b & ~3ull, other = (key_b & 2ull) ? q0 : q0 + 2;
+  const uint64_t c1 = count_below(in, sib << sh, h, n, key);
+  const uint64_t c2 = count_below(in, other << sh, h, n, key) + count_below(in, (other + 1) << sh, h, n, key);
+  outL[((b & ~1ull) << sh) + r + c1] = key;
+  outL1[(q0 << sh) + r + c1 + c2] = key;
+}
+
 // levels 1..kSmemLevels of the merge-sort tree for one 2^kSmemLevels tile in shared memory
 constexpr int kSmemLevels = 8;
 __global__ void __launch_bounds__(1 << kSmemLevels) k_merge_tile(uint32_t* __restrict__ mst, uint64_t n, uint64_t cap,
@@ -295,11 +323,12 @@ __device__ __forceinline__ void leaf_range(const uint64_t* coords, uint64_t m, u
 
 __global__ void k_cover_count(const uint64_t* __restrict__ rs, const uint64_t* __restrict__ re, uint64_t n,
                               const uint64_t* __restrict__ coords, const unsigned long long* __restrict__ m_dev,
-                              uint64_t M, uint32_t* __restrict__ cnt) {
+                              uint64_t M, uint32_t* __restrict__ cnt, uint64_t* __restrict__ lr) {
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   uint64_t l, r;
   leaf_range(coords, *m_dev, rs[i], re[i], l, r);
+  lr[i] = (l << 32) | r;   // reused by k_cover_emit
   uint32_t k = 0;
   for (l += M, r += M; l < r; l >>= 1, r >>= 1) {
     if (l & 1) { ++k; ++l; }
@@ -308,14 +337,11 @@ __global__ void k_cover_count(const uint64_t* __restrict__ rs, const uint64_t* _
   cnt[i] = k;
 }
 
-__global__ void k_cover_emit(const uint64_t* __restrict__ rs, const uint64_t* __restrict__ re,
-                             const uint32_t* __restrict__ rkey, uint64_t n, const uint64_t* __restrict__ coords,
-                             const unsigned long long* __restrict__ m_dev, uint64_t M,
-                             const uint32_t* __restrict__ off, uint64_t* __restrict__ pairs, int kb) {
+__global__ void k_cover_emit(const uint64_t* __restrict__ lr, const uint32_t* __restrict__ rkey, uint64_t n,
+                             uint64_t M, const uint32_t* __restrict__ off, uint64_t* __restrict__ pairs, int kb) {
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  uint64_t l, r;
-  leaf_range(coords, *m_dev, rs[i], re[i], l, r);
+  uint64_t l = lr[i] >> 32, r = lr[i] & 0xffffffffull;
   uint64_t o = off[i];
   const uint64_t key = rkey[i];
   for (l += M, r += M; l < r; l >>= 1, r >>= 1) {
@@ -637,8 +663,15 @@ cg_status cg_conc::run_space(int sp, const cg_copy_desc* d, const uint32_t* thre
                                                                                                          Ls);
       ++launches;
     }
-    for (int l = Ls + 1; l <= L; ++l) {
-      k_merge_level<<<grid_for(rn), kT, 0, s>>>(mst + (uint64_t)(l - 1) * cap, mst + (uint64_t)l * cap, rn, l);
+    for (int l = Ls + 1; l <= L;) {
+      if (l + 1 <= L) {
+        k_merge_2levels<<<grid_for(rn), kT, 0, s>>>(mst + (uint64_t)(l - 1) * cap, mst + (uint64_t)l * cap,
+                                                    mst + (uint64_t)(l + 1) * cap, rn, l);
+        l += 2;
+      } else {
+        k_merge_level<<<grid_for(rn), kT, 0, s>>>(mst + (uint64_t)(l - 1) * cap, mst + (uint64_t)l * cap, rn, l);
+        ++l;
+      }
       ++launches;
     }
     T.rs_sorted = rs_sorted;
@@ -657,7 +690,7 @@ cg_status cg_conc::run_space(int sp, const cg_copy_desc* d, const uint32_t* thre
     if (ensure_temp(tb) != CG_OK) return CG_ERR_OUT_OF_MEMORY;
     e = cub::DeviceSelect::Unique(temp, tb, ep_sorted, coords, counts + 4, (int)(2 * rn), s);
     if (e != cudaSuccess) return cuda(e, "unique endpoints");
-    k_cover_count<<<grid_for(rn), kT, 0, s>>>(S.rs, S.re, rn, coords, counts + 4, M, cnt);
+    k_cover_count<<<grid_for(rn), kT, 0, s>>>(S.rs, S.re, rn, coords, counts + 4, M, cnt, ts);
     ++launches;
     tb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, (int)rn, s);
@@ -672,7 +705,7 @@ cg_status cg_conc::run_space(int sp, const cg_copy_desc* d, const uint32_t* thre
     const uint64_t P = (uint64_t)tail[0] + tail[1];
     if (ensure_pairs(P) != CG_OK) return CG_ERR_OUT_OF_MEMORY;
     const int kb = std::max(ceil_log2(2 * (nh0 + n) + 2), 1);   // bits of a key (2 ord + is_write)
-    k_cover_emit<<<grid_for(rn), kT, 0, s>>>(S.rs, S.re, S.rkey, rn, coords, counts + 4, M, off, pairs2, kb);
+    k_cover_emit<<<grid_for(rn), kT, 0, s>>>(ts, S.rkey, rn, M, off, pairs2, kb);
     ++launches;
     const int end_bit = kb + ceil_log2(2 * M) + 1;
     tb = 0;
