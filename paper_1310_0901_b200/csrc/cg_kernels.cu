@@ -598,6 +598,25 @@ __device__ __forceinline__ void htod_group(const uint8_t* st, uint32_t i, uint32
   }
 }
 
+// a partial 32-byte HtoD group g with the whole warp: lane j looks at host byte 32 g + j
+__device__ __forceinline__ void htod_edge(const uint8_t* st, uint32_t g, uint32_t q0, uint32_t q1, uint64_t ob,
+                                          Partial& p) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t x = (g << 5) + lane;
+  const bool in = x >= q0 && x < q1;
+  const uint32_t a = (st[kTileV + (x >> 3)] >> (x & 7)) & 1u;
+  const uint32_t bad = __ballot_sync(kFull, in && !a);
+  const uint32_t und = __ballot_sync(kFull, in && a && st[x] != 0);
+  if (lane == 0) {
+    const uint64_t gb = ob + ((uint64_t)g << 5);
+    if (bad) p.fu = umin64(p.fu, gb + (__ffs(bad) - 1));
+    if (und) {
+      p.fd = umin64(p.fd, gb + (__ffs(und) - 1));
+      p.cnt += __popc(und);
+    }
+  }
+}
+
 __device__ __forceinline__ void consume_htod(const uint8_t* st, uint32_t q0, uint32_t q1, uint64_t ob,
                                              Partial& p) {
   const int lane = threadIdx.x & 31;
@@ -613,12 +632,12 @@ __device__ __forceinline__ void consume_htod(const uint8_t* st, uint32_t q0, uin
   }
   if (orv != 0 || anda != 0xffffffffu)
     for (uint32_t i = i0 + lane; i < i1; i += 32) htod_group(st, i, 0xffffffffu, ob, p);
-  // partial edge groups
+  // partial edge groups, warp-parallel
   if (i0 > i1) {                                   // [q0, q1) inside one 32-byte group
-    if (lane == 0) htod_group(st, i1, range_mask((uint64_t)i1 << 5, 32, q0, q1), ob, p);
+    htod_edge(st, i1, q0, q1, ob, p);
   } else {
-    if (lane == 0 && (q0 & 31)) htod_group(st, i0 - 1, range_mask((uint64_t)(i0 - 1) << 5, 32, q0, q1), ob, p);
-    if (lane == 1 && (q1 & 31)) htod_group(st, i1, range_mask((uint64_t)i1 << 5, 32, q0, q1), ob, p);
+    if (q0 & 31) htod_edge(st, i0 - 1, q0, q1, ob, p);
+    if (q1 & 31) htod_edge(st, i1, q0, q1, ob, p);
   }
 }
 
@@ -639,6 +658,28 @@ __device__ __forceinline__ void dtoh_group(const uint8_t* st, uint32_t i, uint32
   }
 }
 
+// a partial 128-byte DtoH group g: lanes 0-3 take its four A words
+__device__ __forceinline__ void dtoh_edge(const uint8_t* st, uint32_t g, uint32_t q0, uint32_t q1, uint64_t ob,
+                                          Partial& p) {
+  const int lane = threadIdx.x & 31;
+  uint32_t bad = 0;
+  if (lane < 4) {
+    const uint32_t k = g * 4 + lane;
+    const int base = (int)(k << 5);
+    const int lo = max((int)q0 - base, 0), hi = min((int)q1 - base, 32);
+    if (hi > lo) {
+      const uint32_t m = (hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
+      bad = ~reinterpret_cast<const uint32_t*>(st)[k] & m;
+    }
+  }
+  const uint32_t any = __ballot_sync(kFull, bad != 0);
+  if (any) {
+    const int fl = __ffs(any) - 1;
+    const uint32_t b = __shfl_sync(kFull, bad, fl);
+    if (lane == 0) p.fu = umin64(p.fu, ob + ((uint64_t)(g * 4 + fl) << 5) + (__ffs(b) - 1));
+  }
+}
+
 __device__ __forceinline__ void consume_dtoh(const uint8_t* st, uint32_t q0, uint32_t q1, uint64_t ob,
                                              Partial& p) {
   const int lane = threadIdx.x & 31;
@@ -653,10 +694,10 @@ __device__ __forceinline__ void consume_dtoh(const uint8_t* st, uint32_t q0, uin
   if (anda != 0xffffffffu)
     for (uint32_t i = i0 + lane; i < i1; i += 32) dtoh_group(st, i, q0, q1, ob, p);
   if (i0 > i1) {
-    if (lane == 0) dtoh_group(st, i1, q0, q1, ob, p);
+    dtoh_edge(st, i1, q0, q1, ob, p);
   } else {
-    if (lane == 0 && (q0 & 127)) dtoh_group(st, i0 - 1, q0, q1, ob, p);
-    if (lane == 1 && (q1 & 127)) dtoh_group(st, i1, q0, q1, ob, p);
+    if (q0 & 127) dtoh_edge(st, i0 - 1, q0, q1, ob, p);
+    if (q1 & 127) dtoh_edge(st, i1, q0, q1, ob, p);
   }
 }
 
