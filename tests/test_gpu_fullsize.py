@@ -29,20 +29,24 @@ def cg():
     return m
 
 
-def gpu_batch(cg, tr):
-    """Setup events through the ABI, then the whole copy batch in one call."""
+def gpu_batch(cg, tr, fused=False, **kw):
+    """Setup events through the ABI, then the whole copy batch in one call
+    (cg_check_copies + cg_apply_dtoh, or the bench's fused cg_check_apply)."""
     import torch
     from paper_1310_0901_b200.replay import events_to_descs
     ev = tr.events
     copies = ev[ev["op"] == tg.OP_COPY]
     nreg = int(np.count_nonzero(ev["op"] == tg.OP_REG))
-    chk = cg.Checker(tr.host_base, tr.host_size, max_descs=max(len(copies), 1024), max_allocs=max(nreg, 1024))
+    chk = cg.Checker(tr.host_base, tr.host_size, max_descs=max(len(copies), 1024), max_allocs=max(nreg, 1024), **kw)
     _, st = cg.replay_events(chk, ev[ev["op"] != tg.OP_COPY], tr.blob)
     assert not st.any(), "every setup call of the generated trace is valid"
     descs = events_to_descs(copies)
     dd = cg.to_device_descs(descs)
-    dv = chk.check_copies(dd)
-    chk.apply_dtoh(dd, dv)
+    if fused:
+        dv = chk.check_apply(dd)
+    else:
+        dv = chk.check_copies(dd)
+        chk.apply_dtoh(dd, dv)
     torch.cuda.synchronize()
     return chk, descs, cg.verdicts_to_numpy(dv)
 
@@ -119,3 +123,22 @@ def test_c4_full_sampled(cg):
     A, _ = chk.shadow()
     assert np.array_equal(A, o.A)
     chk.close()
+
+
+@pytest.mark.parametrize("fmt", [0, 1, 2])
+def test_c2_full_fused_formats(cg, fmt):
+    """the bench's launch configuration (one fused cg_check_apply over the 1M
+    batch) in every host shadow format (NEXT-4: 2-bit, sparse map)"""
+    tr = tg.c2_small()
+    chk, descs, gv = gpu_batch(cg, tr, fused=True, shadow_format=fmt)
+    rng = np.random.default_rng(2 + fmt)
+    inj = tr.meta["inject"]
+    idx = np.unique(np.concatenate([np.flatnonzero(inj), rng.choice(len(descs), 5000, replace=False)]))
+    o, ov = sampled_oracle(tr, idx)
+    compare(gv, ov, idx)
+    assert np.array_equal(gv["flags"] != 0, inj != 0)
+    # the fused apply defined exactly the non-injected DtoH ranges: sample some
+    dtoh = np.flatnonzero((descs["kind"] == 2) & (inj == 0))
+    for i in rng.choice(dtoh, 50, replace=False):
+        a, v = chk.shadow_read(int(descs["dst"][i]), int(descs["width"][i]))
+        assert a.all() and not v.any(), i
