@@ -349,7 +349,8 @@ cg_status cg_conc_sync(cg_conc *c, uint32_t thread, uint64_t seq);
  * verdict flags of every hazardous copy (status unchanged, R-35), then updates
  * the last-access maps.  Overlaps inside the batch are resolved exactly (no
  * planner cut is needed).  Synchronous on stream.  Errors: CG_ERR_INVALID_VALUE
- * (null, n > max_n), CG_ERR_OUT_OF_MEMORY (a map would exceed max_stamps: the
+ * (null, n > max_n, seqs not strictly increasing or not above every seq of
+ * the earlier batches -- nothing is flagged or recorded then), CG_ERR_OUT_OF_MEMORY (a map would exceed max_stamps: the
  * flags are written, the maps are left as before), CG_ERR_CUDA. */
 cg_status cg_conc_check(cg_conc *c, const cg_copy_desc *d_descs, const uint32_t *d_threads, uint64_t n,
                         cg_verdict *d_verdicts, void *stream);

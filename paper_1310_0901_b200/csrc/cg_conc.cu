@@ -177,6 +177,10 @@ __global__ void __launch_bounds__(kT) k_access(const cg_copy_desc* __restrict__ 
     const cg_copy_desc c = d[i];
     const int na = copy_accesses(c.kind, sp, dst, wr);
     performed = v[i].status == CG_OK;
+    // the contract: seqs strictly increase inside the batch (counts[12] flags a violation)
+    if (i > 0 && d[i - 1].seq >= c.seq) atomicOr(counts + 12, 1ull);
+    if (i == 0) counts[13] = c.seq;       // the batch's first seq, checked against the previous batch
+    if (i + 1 == n) counts[14] = c.seq;   // and its last
     for (int k = 0; k < na; ++k) {
       ok[k] = dst[k] ? cgk::fold_side(c.dst, c.dst_x, c.dst_y, c.dst_pitch, c.width, c.height, st[k], sn[k])
                      : cgk::fold_side(c.src, c.src_x, c.src_y, c.src_pitch, c.width, c.height, st[k], sn[k]);
@@ -512,6 +516,7 @@ struct cg_conc {
   uint64_t max_n = 0, max_stamps = 0, cap = 0, qcap = 0;
   int levels = 1;
   uint64_t nh[2] = {0, 0};
+  uint64_t last_seq = 0;   // largest seq of the batches checked so far
   uint64_t launches = 0;
   std::string err;
   std::vector<std::pair<uint32_t, uint64_t>> syncs;
@@ -866,11 +871,16 @@ cg_status cg_conc_check(cg_conc* c, const cg_copy_desc* d_descs, const uint32_t*
     if (e != cudaSuccess) st = c->cuda(e, "access kernels");
   }
   for (int sp = 0; sp < 2 && st == CG_OK; ++sp) {
+    if (sp == 0 && (c->h_counts[12] || c->h_counts[13] <= c->last_seq)) {
+      st = c->fail(CG_ERR_INVALID_VALUE, "batch seqs must increase, and exceed those of earlier batches");
+      break;
+    }
     const uint64_t qn = c->h_counts[sp], rn = c->nh[sp] + c->h_counts[2 + sp];
     const uint64_t lo = c->h_counts[8 + 2 * sp], hi = c->h_counts[9 + 2 * sp];
     const int bits = lo < hi ? 64 - __builtin_clzll(lo ^ hi) : 1;   // the address bits R's keys differ in
     st = c->run_space(sp, d_descs, d_threads, n, d_verdicts, qn, rn, std::max(bits, 1), s);
   }
+  if (st == CG_OK) c->last_seq = c->h_counts[14];
   if (prev >= 0) cudaSetDevice(prev);
   return st;
 }

@@ -67,6 +67,10 @@ def replay_events(chk, events: np.ndarray, blob=None, stream=None, fuse: bool = 
             j = i
             while j < n and ops[j] in _REGISTRY:
                 j += 1
+            if j == i:   # an unknown op: invalid call, like the oracle's replay
+                status[i] = 1
+                i += 1
+                continue
             for k in range(i, j):
                 if ops[k] == OP_REG:
                     status[k] = chk.register_alloc(int(events["dst"][k]), int(events["width"][k]),

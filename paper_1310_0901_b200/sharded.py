@@ -250,7 +250,7 @@ def replay_sharded(group: LoopbackGroup, events: np.ndarray, blob=None, fuse: bo
     """Replay a call stream over the G shards of a LoopbackGroup: setup calls go
     to every shard, copies are checked in hazard-free batches sharded by host
     range.  Returns (verdicts of the copies, status per event)."""
-    from .replay import OP_COPY, OP_FREE, OP_MARK, OP_REG, OP_SETV, events_to_descs
+    from .replay import OP_COPY, OP_FREE, OP_FREEA, OP_MARK, OP_REG, OP_REGA, OP_SETV, OP_SYNC, events_to_descs
     from . import MARK_DTYPE, plan_batches
     ops = np.asarray(events["op"])
     n = len(events)
@@ -286,8 +286,12 @@ def replay_sharded(group: LoopbackGroup, events: np.ndarray, blob=None, fuse: bo
             i += 1
         else:
             j = i
-            while j < n and ops[j] in (OP_REG, OP_FREE, OP_COPY):
+            while j < n and ops[j] in (OP_REG, OP_FREE, OP_COPY, OP_REGA, OP_FREEA, OP_SYNC):   # SYNC: NEXT-2 only
                 j += 1
+            if j == i:   # an unknown op: invalid call, like the oracle's replay
+                status[i] = 1
+                i += 1
+                continue
             for k in range(i, j):
                 if ops[k] == OP_REG:
                     rs = [sc.chk.register_alloc(int(events["dst"][k]), int(events["width"][k]),
@@ -295,6 +299,15 @@ def replay_sharded(group: LoopbackGroup, events: np.ndarray, blob=None, fuse: bo
                     status[k] = rs[0]
                 elif ops[k] == OP_FREE:
                     rs = [sc.chk.free(int(events["dst"][k]), int(events["seq"][k])) for sc in group.ranks]
+                    status[k] = rs[0]
+                elif ops[k] == OP_REGA:   # NEXT-3 arrays are replicated like allocations
+                    e = events[k]
+                    rs = [sc.chk.register_array(int(e["dst"]), int(e["width"]), int(e["height"]), int(e["dst_x"]),
+                                                int(e["dst_y"]), int(e["dst_pitch"]), int(e["seq"]))
+                          for sc in group.ranks]
+                    status[k] = rs[0]
+                elif ops[k] == OP_FREEA:
+                    rs = [sc.chk.free_array(int(events["dst"][k]), int(events["seq"][k])) for sc in group.ranks]
                     status[k] = rs[0]
             idx = np.flatnonzero(is_copy[i:j]) + i
             if len(idx):

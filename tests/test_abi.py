@@ -261,3 +261,15 @@ def test_error_summary_line(cg):
     """1 error, 0 suppressions -> "ERROR SUMMARY: 1 errors, 0 warnings (0 suppressed)" """
     assert cg.format_summary(1, 0, 0) == "ERROR SUMMARY: 1 errors, 0 warnings (0 suppressed)\n"
     assert cg.format_summary(12, 345, 6) == "ERROR SUMMARY: 12 errors, 345 warnings (6 suppressed)\n"
+
+
+def test_replay_unknown_op_is_an_invalid_call():
+    """an event with an unknown op is an invalid call (status 1) in the oracle;
+    the GPU replays must agree without a GPU call (checked on the host path)"""
+    import oracle
+    tr = tg.random_tiny(5)
+    ev = tr.events.copy()
+    ev[3]["op"] = 42
+    o = oracle.Oracle(tr.host_base, tr.host_size)
+    _, st = o.replay(ev, tr.blob)
+    assert st[3] == 1

@@ -122,3 +122,32 @@ def test_error_summary_counts(cg, uie):
     warn = [5, 9] if not uie else [9]
     assert w == int(bits[:, warn].sum()) and e == int(bits.sum()) - w
     assert w > 0 and e > 0
+
+
+def test_batch_order_contract(cg):
+    """cg_conc_check rejects a batch whose seqs do not increase, or that does
+    not come after the previous batch, and then changes nothing"""
+    import torch
+    from paper_1310_0901_b200.replay import events_to_descs
+    tr = tg.with_threads(tg.c2_small(n_copies=2000, n_allocs=500), 2)
+    ev = tr.events
+    chk = cg.Checker(tr.host_base, tr.host_size, max_descs=4096, max_allocs=4096)
+    cg.replay_events(chk, ev[ev["op"] != tg.OP_COPY], tr.blob)
+    copies = ev[ev["op"] == tg.OP_COPY]
+    descs = events_to_descs(copies)
+    th = torch.from_numpy(tr.threads[ev["op"] == tg.OP_COPY].astype(np.int32)).cuda()
+    conc = cg.ConcChecker(4096, 1 << 16)
+    dd = cg.to_device_descs(descs[:1000])
+    dv = chk.check_copies(dd)
+    conc.check(dd, th[:1000], dv)
+    before = conc.stamps()
+    for bad in (descs[:1000], descs[1000:2000][::-1].copy()):   # repeated / descending seqs
+        d2 = cg.to_device_descs(bad)
+        v2 = chk.check_copies(d2)
+        with pytest.raises(cg.CgError):
+            conc.check(d2, th[:1000], v2)
+        assert conc.stamps() == before
+    d3 = cg.to_device_descs(descs[1000:2000])
+    conc.check(d3, th[1000:2000], chk.check_copies(d3))       # the next batch in order is fine
+    conc.close()
+    chk.close()

@@ -109,3 +109,12 @@ def test_array_registry_errors(cg):
     rep = chk.array_report()
     assert [int(x) for x in rep["base"]] == [100, 101, 102, 200]
     chk.close()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("seed", range(6))
+def test_random_tiny_arrays_sharded(cg, world, seed):
+    """array transfers through host-range shards (their host side is sharded
+    like HtoD / DtoH; the array side is looked up by the owner shard only)"""
+    from test_gpu_sharded import run_sharded
+    run_sharded(cg, tg.random_tiny(seed + 31000, arrays=True), world, fuse=bool(seed % 2))

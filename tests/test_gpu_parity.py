@@ -250,3 +250,12 @@ def test_check_host_compact_chunked(cg, fmt):
     A, V = chk.shadow()
     assert np.array_equal(V, o.V) and np.array_equal(A, o.A)
     chk.close()
+
+
+def test_unknown_op_status(cg):
+    """an unknown event op is an invalid call on both sides (oracle status 1)"""
+    tr = tg.random_tiny(5)
+    ev = tr.events.copy()
+    ev[3]["op"] = 42
+    tr2 = tg.Trace(tr.name, ev, tr.blob, tr.host_base, tr.host_size, tr.meta)
+    run_parity(cg, tr2)
