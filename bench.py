@@ -271,10 +271,8 @@ def run_ours(args, rank, world, device):
                             g_cnt.data_ptr(), stream.cuda_stream)
         mx_t = g_cnt.to(torch.int64)
         dist.all_reduce(mx_t, op=dist.ReduceOp.MAX)
-        mx = max(1, int(mx_t.item()))
-        all_cnt = torch.zeros(world, dtype=torch.int32, device=device)
-        all_idx = torch.empty(world * mx, dtype=torch.int64, device=device)
-        all_dirty = torch.empty(world * mx * 64, dtype=torch.uint8, device=device)
+        from paper_1310_0901_b200.sharded import PackedDirtyGather
+        pg = PackedDirtyGather(dist, max(1, int(mx_t.item())), torch.device("cuda", device))
 
     def step():
         check_epochs()
@@ -282,11 +280,9 @@ def run_ours(args, rank, world, device):
         if comm is not None:
             # the exchange: every rank's compacted dirty verdicts (count, index,
             # 64-byte verdict) gathered over NCCL, device to device, no host sync
-            cg.cg_compact_dirty(chk.ctx, d_out.data_ptr(), n, g_idx.data_ptr(), g_dirty.data_ptr(),
-                                g_cnt.data_ptr(), stream.cuda_stream)
-            comm.all_gather_into_tensor(all_cnt, g_cnt)
-            comm.all_gather_into_tensor(all_idx, g_idx[:mx])
-            comm.all_gather_into_tensor(all_dirty, g_dirty[:mx * 64])
+            cg.cg_compact_dirty(chk.ctx, d_out.data_ptr(), n, pg.idx_ptr(), pg.dirty_ptr(), pg.count_ptr(),
+                                stream.cuda_stream)
+            pg.gather()   # one NCCL all_gather of the packed (count, index, verdict) buffers
 
     for _ in range(args.warmup):
         step()
@@ -310,9 +306,12 @@ def run_ours(args, rank, world, device):
     stages = chk.profile_end()
     if world > 1:
         torch.distributed.barrier()
-        tot = g_cnt.to(torch.int64)
+        got = pg.unpack()
+        mine = got[rank]
+        tot = torch.tensor([mine[0]], dtype=torch.int64, device=device)
         torch.distributed.all_reduce(tot)
-        assert int(all_cnt.to(torch.int64).sum().item()) == int(tot.item()), "dirty-verdict gather lost records"
+        assert sum(c for c, _, _ in got) == int(tot.item()), "dirty-verdict gather lost records"
+        assert np.array_equal(mine[2]["flags"], verd["flags"][mine[1]]), "gathered verdicts differ"
     launches = chk.kernel_launches - launches0
     ms = ev0.elapsed_time(ev1)
     if world > 1:

@@ -183,6 +183,50 @@ class TorchComm:
                 for r in range(world)]
 
 
+class PackedDirtyGather:
+    """The N>1 bench exchange in ONE collective: each rank packs (count,
+    index[mx], verdict[mx]) into a fixed buffer of 16 + 72 mx bytes that
+    cg_compact_dirty writes straight into (count at byte 0, indices at 16,
+    verdicts after them), and one all_gather_into_tensor moves every rank's
+    buffer to every rank, device to device, with no host synchronisation.
+    mx must bound every rank's dirty count (the bench fixes it from an
+    untimed probe of the same batch)."""
+
+    def __init__(self, dist, mx: int, device):
+        import torch
+        self.dist = dist
+        self.world = dist.get_world_size()
+        self.mx = mx + (mx & 1)   # keeps the verdicts 16-byte aligned
+        self.nbytes = 16 + 72 * self.mx
+        self.send = torch.zeros(self.nbytes, dtype=torch.uint8, device=device)
+        self.recv = torch.empty(self.world * self.nbytes, dtype=torch.uint8, device=device)
+
+    # device pointers for cg_compact_dirty
+    def count_ptr(self) -> int:
+        return self.send.data_ptr()
+
+    def idx_ptr(self) -> int:
+        return self.send.data_ptr() + 16
+
+    def dirty_ptr(self) -> int:
+        return self.send.data_ptr() + 16 + 8 * self.mx
+
+    def gather(self):
+        self.dist.all_gather_into_tensor(self.recv, self.send)
+
+    def unpack(self):
+        """host view of the last gather: [(count, idx, verdicts)] per rank"""
+        buf = self.recv.cpu().numpy()
+        out = []
+        for r in range(self.world):
+            b = buf[r * self.nbytes:(r + 1) * self.nbytes]
+            c = int(b[:4].view(np.int32)[0])
+            idx = b[16:16 + 8 * self.mx].view(np.int64)[:c]
+            dv = b[16 + 8 * self.mx:].view(VERDICT_DTYPE)[:c]
+            out.append((c, idx, dv))
+        return out
+
+
 def _u64_min_fix(t):
     """MIN over u64 fields held in int64 tensors: map u64 order onto i64 order
     (flip the sign bit) before and after the reduction."""

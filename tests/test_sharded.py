@@ -147,3 +147,48 @@ def test_gloo_world2_exchange():
         assert [g[0] for g in gathered] == [1, 2]
         assert gathered[1][1] == [1, 3] and gathered[1][3] == [2, 2]
     assert res[0][2] == res[1][2]
+
+
+def _packed_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import sys
+    sys.path.insert(0, ROOT)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1310_0901_b200 import VERDICT_DTYPE
+        from paper_1310_0901_b200.sharded import PackedDirtyGather
+        g = PackedDirtyGather(dist, 5, torch.device("cpu"))
+        c = 2 + rank
+        # what cg_compact_dirty would write into the send buffer
+        g.send[:4] = torch.from_numpy(np.array([c], np.int32).view(np.uint8))
+        idx = np.arange(c, dtype=np.int64) * 3 + rank
+        g.send[16:16 + 8 * c] = torch.from_numpy(idx.view(np.uint8))
+        dv = np.zeros(c, VERDICT_DTYPE)
+        dv["flags"] = 100 + rank
+        dv["first_unaddr"] = idx * 7
+        off = 16 + 8 * g.mx
+        g.send[off:off + 64 * c] = torch.from_numpy(dv.view(np.uint8))
+        g.gather()
+        q.put((rank, [(cc, i.tolist(), d["flags"].tolist(), d["first_unaddr"].tolist()) for cc, i, d in g.unpack()]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_packed_gather():
+    """the bench's one-collective exchange of compacted verdicts on world_size 2"""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_packed_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=180) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        for src in range(world):
+            c, idx, flags, fu = res[r][src]
+            assert c == 2 + src
+            assert idx == [3 * k + src for k in range(c)]
+            assert flags == [100 + src] * c and fu == [7 * x for x in idx]
