@@ -1129,10 +1129,10 @@ struct TileGen {
     if (lane == owner) {
       const uint32_t j = t - s_excl;
       const bool htod = s_fl & kTileHtod;
-      const uint64_t bsz = two_bit ? k2bitBlock : htod ? kTileV : kDtohBlock;
-      const uint64_t base = s_q0 & ~(bsz - 1);
-      const uint64_t tq0 = j ? base + j * bsz : s_q0;
-      const uint64_t tq1 = umin64(s_q1, base + (j + 1) * bsz);
+      const uint32_t bsh = two_bit ? 14u : htod ? 12u : 15u;   // log2 of the tile block
+      const uint64_t base = (s_q0 >> bsh) << bsh;
+      const uint64_t tq0 = j ? base + ((uint64_t)j << bsh) : s_q0;
+      const uint64_t tq1 = umin64(s_q1, base + ((uint64_t)(j + 1) << bsh));
       const uint64_t qa = tq0 & (two_bit ? ~63ull : ~127ull);
       TileInfo ti;
       ti.ob = s_ob + qa;
