@@ -273,3 +273,16 @@ def test_replay_unknown_op_is_an_invalid_call():
     o = oracle.Oracle(tr.host_base, tr.host_size)
     _, st = o.replay(ev, tr.blob)
     assert st[3] == 1
+
+
+def test_header_is_plain_c(tmp_path):
+    """include/cg.h is a C header: a C11 translation unit that includes it and
+    takes the address of every declared function compiles with gcc"""
+    import subprocess
+    names = declared_functions()
+    src = tmp_path / "use.c"
+    src.write_text('#include "cg.h"\n#include <stddef.h>\ntypedef void (*fn)(void);\nfn table[] = {\n' +
+                   ",\n".join(f"  (fn)&{n}" for n in names) + "\n};\nint main(void) { return table[0] == NULL; }\n")
+    r = subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-pedantic", "-fsyntax-only",
+                        "-I", os.path.join(ROOT, "include"), str(src)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
