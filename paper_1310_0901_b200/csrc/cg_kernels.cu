@@ -41,28 +41,11 @@ namespace cgk {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kUnroll = 4;
 
 // ---------------------------------------------------------------------------
 // small device helpers
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-__device__ __forceinline__ uint32_t ldg_u16(const uint16_t* p) {
-  unsigned short r;
-  asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(r) : "l"(p));
-  return r;
-}
-__device__ __forceinline__ void stg_zero16(uint4* p) {
-  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%1,%1,%1};" ::"l"(p), "r"(0u));
-}
 __device__ __forceinline__ void stg_val16(uint4* p, uint32_t v) {
   asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%1,%1,%1};" ::"l"(p), "r"(v));
 }
@@ -507,8 +490,9 @@ constexpr int kRingWarps = 4;
 constexpr int kStages = 3;
 constexpr uint32_t kTileV = 4096;      // HtoD: V bytes per tile
 constexpr uint32_t kTileA = kTileV / 8;
-constexpr uint32_t kDtohBlock = 32768; // DtoH: host bytes per tile (4 KiB of A)
-constexpr uint32_t k2bitBlock = 16384; // NEXT-4 2-bit states: host bytes per tile (4 KiB of states)
+// tile blocks (log2 of host bytes): HtoD 4 KiB (= kTileV V bytes), DtoH 32 KiB
+// (4 KiB of A), NEXT-4 2-bit states 16 KiB for both kinds (4 KiB of states)
+constexpr uint32_t kHtodShift = 12, kDtohShift = 15, k2bitShift = 14;
 constexpr uint32_t kGrab = 4;          // chunks per group while the plan is far from its end
 constexpr uint32_t kTileData = 1, kTileHtod = 2, kTileEnd = 4, kTileWhole = 8, kTileFuse = 16, kTileRaw = 32;
 
@@ -1019,7 +1003,7 @@ struct TileGen {
     s_fl = fl;
     uint32_t k = 0;
     if (live) {
-      const uint64_t sh = two_bit ? 14 : (fl & kTileHtod) ? 12 : 15;   // log2 of the tile block
+      const uint64_t sh = two_bit ? k2bitShift : (fl & kTileHtod) ? kHtodShift : kDtohShift;   // log2 of the tile block
       k = (uint32_t)(((q1 - 1) >> sh) - (q0 >> sh) + 1);
     }
     s_k = k;
@@ -1129,7 +1113,7 @@ struct TileGen {
     if (lane == owner) {
       const uint32_t j = t - s_excl;
       const bool htod = s_fl & kTileHtod;
-      const uint32_t bsh = two_bit ? 14u : htod ? 12u : 15u;   // log2 of the tile block
+      const uint32_t bsh = two_bit ? k2bitShift : htod ? kHtodShift : kDtohShift;   // log2 of the tile block
       const uint64_t base = (s_q0 >> bsh) << bsh;
       const uint64_t tq0 = j ? base + ((uint64_t)j << bsh) : s_q0;
       const uint64_t tq1 = umin64(s_q1, base + ((uint64_t)(j + 1) << bsh));
