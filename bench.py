@@ -241,17 +241,24 @@ def run_ours(args, rank, world, device):
     # the batch contract (R-20): the copies are checked in the epochs
     # cg_plan_batches cuts (one epoch for C2-C4; C5's ping-pongs make ~11); an
     # epoch whose HtoD and DtoH host ranges are disjoint runs fused
-    cuts = [0] + [int(c) for c in cg.plan_batches(descs, propagate=args.track)]
+    cuts = [0] + [int(c) for c in cg.plan_batches(descs)]
     epochs = [(a, b) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
     efused = [cg.batch_disjoint(descs[a:b]) and not args.unfused and not args.track for a, b in epochs]
     fused = all(efused)
+    waves = []   # NEXT-1: per epoch, the device index lists of its propagation waves (cg_plan_waves)
+    t_waves = 0.0
+    if args.track:
+        t0 = time.perf_counter()
+        for a, b in epochs:
+            waves.append(cg.Waves(descs[a:b], device))
+        t_waves = time.perf_counter() - t0
 
     def check_epochs():
-        for (a, b), fu in zip(epochs, efused):
+        for k, ((a, b), fu) in enumerate(zip(epochs, efused)):
             dd, dv = d_descs[a * 96:b * 96], d_out[a * 64:b * 64]
-            if args.track:      # NEXT-1: check, then V-bit propagation
+            if args.track:      # NEXT-1: check, then V-bit propagation wave by wave
                 chk.check_copies(dd, dv, stream=stream)
-                chk.apply_copies(dd, dv, stream=stream)
+                chk.apply_waves(dd, dv, waves[k], stream=stream)
             elif fu:
                 chk.check_apply(dd, dv, stream=stream)
             else:
@@ -418,7 +425,9 @@ def run_ours(args, rank, world, device):
                    "entry": ("cg_check_copies + cg_apply_copies (NEXT-1 V-bit propagation)" if args.track else
                              "cg_check_apply (fused)" if fused else "cg_check_copies + cg_apply_dtoh"
                              if not any(efused) else "cg_check_apply / cg_check_copies + cg_apply_dtoh per epoch"),
-                   "epochs": len(epochs)},
+                   "epochs": len(epochs),
+                   "propagation_waves": sum(w.n_waves for w in waves) if args.track else None,
+                   "wave_planning_s": t_waves if args.track else None},
         "descriptors_per_s": world * n / (ms_step * 1e-3),
         "frac_of_hbm": value / (world * peak),
         "roofline": {"bound": "hbm", "kernel": "k_check_scan", "achieved": achieved, "peak": peak,

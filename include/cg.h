@@ -394,6 +394,41 @@ cg_status cg_apply_dtoh(cg_ctx *ctx, const cg_copy_desc *d_descs, const cg_verdi
 cg_status cg_apply_copies(cg_ctx *ctx, const cg_copy_desc *d_descs, const cg_verdict *d_verdicts, uint64_t n,
                           void *stream);
 
+/* NEXT-1 propagation of a subset: the m descriptors d_index[0..m) (device
+ * uint32 indices into the n descriptors of the preceding cg_check_copies, each
+ * at most once) move their V-bits as in cg_apply_copies.  With the waves of
+ * cg_plan_waves this propagates a batch whose copies read or write each
+ * other's bytes: wave by wave, in level order.  max_bytes: the largest
+ * width*height among the m copies if the caller knows it (waves of copies up
+ * to 1 MiB then run one warp per copy without a plan), else 0.
+ * Asynchronous on stream: a
+ * self-overlapping 2D DtoD that does not fit the staging area is reported by
+ * the next cg_apply_flush.  Errors: CG_ERR_INVALID_VALUE (null, m > n, not
+ * the checked descriptors), CG_ERR_NOT_INITIALIZED without tracking, CG_ERR_CUDA. */
+cg_status cg_apply_copies_subset(cg_ctx *ctx, const cg_copy_desc *d_descs, const cg_verdict *d_verdicts, uint64_t n,
+                                 const uint32_t *d_index, uint64_t m, uint64_t max_bytes, void *stream);
+
+/* Synchronises stream and reports (then clears) a staging overflow of the
+ * cg_apply_copies_subset calls since the last flush (CG_ERR_INVALID_VALUE). */
+cg_status cg_apply_flush(cg_ctx *ctx, void *stream);
+
+/* All waves of a batch in one call: wave w is d_index[h_wave_start[w] ..
+ * h_wave_start[w+1]) with largest copy h_max_bytes[w] (host arrays of
+ * n_waves + 1 and n_waves entries), propagated in order by
+ * cg_apply_copies_subset, then cg_apply_flush.  Synchronous. */
+cg_status cg_apply_copies_waves(cg_ctx *ctx, const cg_copy_desc *d_descs, const cg_verdict *d_verdicts, uint64_t n,
+                                const uint32_t *d_index, const uint64_t *h_wave_start, const uint64_t *h_max_bytes,
+                                uint32_t n_waves, void *stream);
+
+/* NEXT-1 wave planner (host): h_level[i] = 1 + the highest level of an
+ * earlier descriptor of the batch whose V-bit reads / writes conflict with
+ * descriptor i's (read-after-write, write-after-read, write-after-write on
+ * host or device bytes, the sets of cg_plan_batches_propagate; R-28), 0 if
+ * none; *n_levels = number of levels.  Propagating level 0, then 1, ... with
+ * cg_apply_copies_subset equals propagating the copies one by one in order.
+ * Errors: CG_ERR_INVALID_VALUE on NULL. */
+cg_status cg_plan_waves(const cg_copy_desc *h_descs, uint64_t n, uint32_t *h_level, uint32_t *n_levels);
+
 /* Downloads the device V-bits of [addr, addr+len) (inside one allocation live
  * now) to h_out (NEXT-1 state inspection).  Synchronous.  Errors:
  * CG_ERR_NOT_INITIALIZED without tracking; CG_ERR_INVALID_VALUE if the range

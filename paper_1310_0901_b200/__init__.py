@@ -118,6 +118,10 @@ def _load() -> ctypes.CDLL:
         "cg_free_array": (I, [P, U64, U64]),
         "cg_array_report": (I, [P, P, U64, P]),
         "cg_host_shadow_read": (I, [P, U64, U64, P, P, P]),
+        "cg_apply_copies_subset": (I, [P, P, P, U64, P, U64, U64, P]),
+        "cg_plan_waves": (I, [P, U64, P, P]),
+        "cg_apply_flush": (I, [P, P]),
+        "cg_apply_copies_waves": (I, [P, P, P, U64, P, P, P, U32, P]),
         "cg_summarize": (I, [P, U64, U32, P, P]),
         "cg_format_summary": (U64, [U64, U64, U64, P, U64]),
         "cg_conc_create": (I, [I, U64, U64, P]),
@@ -143,7 +147,7 @@ EXPORTED = ("cg_workspace_size", "cg_ctx_create", "cg_ctx_destroy", "cg_last_err
             "cg_batch_disjoint", "cg_straddler_pack", "cg_straddler_finalize", "cg_compact_dirty", "cg_shard_plan",
             "cg_host_query_addressable", "cg_expand_copy1d", "cg_check_host", "cg_format_verdict",
             "cg_format_leak", "cg_apply_copies", "cg_device_vbits", "cg_plan_batches_propagate",
-            "cg_host_shadow_read", "cg_summarize", "cg_format_summary", "cg_array_bytes", "cg_register_array", "cg_free_array", "cg_array_report", "cg_conc_create",
+            "cg_host_shadow_read", "cg_apply_copies_subset", "cg_plan_waves", "cg_apply_flush", "cg_apply_copies_waves", "cg_summarize", "cg_format_summary", "cg_array_bytes", "cg_register_array", "cg_free_array", "cg_array_report", "cg_conc_create",
             "cg_conc_destroy", "cg_conc_last_error", "cg_conc_sync", "cg_conc_check", "cg_conc_stamps",
             "cg_conc_kernel_launches")
 
@@ -175,6 +179,27 @@ cg_device_vbits = _lib.cg_device_vbits
 cg_plan_batches_propagate = _lib.cg_plan_batches_propagate
 cg_array_bytes = _lib.cg_array_bytes
 cg_host_shadow_read = _lib.cg_host_shadow_read
+cg_apply_copies_subset = _lib.cg_apply_copies_subset
+cg_plan_waves = _lib.cg_plan_waves
+cg_apply_flush = _lib.cg_apply_flush
+cg_apply_copies_waves = _lib.cg_apply_copies_waves
+
+
+class Waves:
+    """NEXT-1 propagation waves of one checked batch, uploaded once: the
+    concatenated device index lists plus host offsets / largest copy per wave
+    (for cg_apply_copies_waves)."""
+
+    def __init__(self, descs: np.ndarray, device: int = 0):
+        import torch
+        lev, nl = plan_waves(descs)
+        order = np.argsort(lev, kind="stable").astype(np.uint32)
+        self.start = np.searchsorted(lev[order], np.arange(nl + 1)).astype(np.uint64)
+        nb = descs["width"].astype(np.uint64) * descs["height"].astype(np.uint64)
+        self.max_bytes = np.array([int(nb[order[self.start[w]:self.start[w + 1]]].max())
+                                   if self.start[w + 1] > self.start[w] else 0 for w in range(nl)], np.uint64)
+        self.index = torch.from_numpy(order.astype(np.int32)).to(torch.device("cuda", device))
+        self.n_waves = nl
 cg_summarize = _lib.cg_summarize
 cg_format_summary = _lib.cg_format_summary
 
@@ -250,6 +275,30 @@ def plan_batches(descs: np.ndarray, propagate: bool = False) -> np.ndarray:
     if st:
         raise CgError(st, "cg_plan_batches")
     return cuts[: nc.value]
+
+
+def plan_waves(descs: np.ndarray):
+    """cg_plan_waves: (level per descriptor, number of levels) for NEXT-1
+    propagation of a batch whose copies touch each other's bytes."""
+    d = np.ascontiguousarray(descs, dtype=DESC_DTYPE)
+    lev = np.zeros(max(len(d), 1), np.uint32)
+    nl = ctypes.c_uint32(0)
+    st = _lib.cg_plan_waves(d.ctypes.data if len(d) else None, len(d), lev.ctypes.data, ctypes.byref(nl))
+    if st:
+        raise CgError(st, "cg_plan_waves")
+    return lev[:len(d)], int(nl.value)
+
+
+def wave_indices(levels: np.ndarray, n_levels: int, descs: Optional[np.ndarray] = None):
+    """per level, the (uint32) indices of its descriptors in batch order; with
+    descs, (indices, largest width*height) pairs for cg_apply_copies_subset"""
+    order = np.argsort(levels, kind="stable").astype(np.uint32)
+    bounds = np.searchsorted(levels[order], np.arange(n_levels + 1))
+    waves = [order[bounds[w]:bounds[w + 1]] for w in range(n_levels)]
+    if descs is None:
+        return waves
+    nb = descs["width"].astype(np.uint64) * descs["height"].astype(np.uint64)
+    return [(w, int(nb[w].max()) if len(w) else 0) for w in waves]
 
 
 def batch_disjoint(descs: np.ndarray) -> bool:
@@ -422,11 +471,30 @@ class Checker:
                  "cg_check_copies")
         return d_out
 
-    def apply_copies(self, d_descs, d_verdicts, stream=None):
-        """cg_apply_copies: the a6 step (V-bit propagation with tracking)."""
+    def apply_copies(self, d_descs, d_verdicts, index=None, max_bytes: int = 0, stream=None):
+        """cg_apply_copies: the a6 step (V-bit propagation with tracking);
+        with index (a CUDA uint32/int32 tensor of descriptor indices) only that
+        subset (cg_apply_copies_subset, one wave of cg_plan_waves)."""
         n = d_descs.numel() // DESC_DTYPE.itemsize
-        self._ok(_lib.cg_apply_copies(self.ctx, d_descs.data_ptr(), d_verdicts.data_ptr(), n, _stream_ptr(stream)),
-                 "cg_apply_copies")
+        if index is None:
+            self._ok(_lib.cg_apply_copies(self.ctx, d_descs.data_ptr(), d_verdicts.data_ptr(), n,
+                                          _stream_ptr(stream)), "cg_apply_copies")
+        else:
+            self._ok(_lib.cg_apply_copies_subset(self.ctx, d_descs.data_ptr(), d_verdicts.data_ptr(), n,
+                                                 index.data_ptr(), index.numel(), max_bytes, _stream_ptr(stream)),
+                     "cg_apply_copies_subset")
+
+    def apply_waves(self, d_descs, d_verdicts, waves: "Waves", stream=None):
+        """cg_apply_copies_waves: every wave of the batch, in order, one call"""
+        n = d_descs.numel() // DESC_DTYPE.itemsize
+        self._ok(_lib.cg_apply_copies_waves(self.ctx, d_descs.data_ptr(), d_verdicts.data_ptr(), n,
+                                            waves.index.data_ptr(), waves.start.ctypes.data,
+                                            waves.max_bytes.ctypes.data, waves.n_waves, _stream_ptr(stream)),
+                 "cg_apply_copies_waves")
+
+    def apply_flush(self, stream=None):
+        """cg_apply_flush: sync, report a staging overflow of the subset calls"""
+        self._ok(_lib.cg_apply_flush(self.ctx, _stream_ptr(stream)), "cg_apply_flush")
 
     def device_vbits(self, addr: int, length: int) -> np.ndarray:
         out = np.zeros(max(length, 1), np.uint8)

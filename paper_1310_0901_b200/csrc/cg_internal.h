@@ -128,8 +128,12 @@ uint64_t scan_blocks(uint64_t n);
 int persistent_blocks(int which);   // 0: k_check_scan, 1: k_apply (per SM)
 size_t prop_meta_bytes();
 uint64_t stage_bytes();
-cudaError_t propagate(const Launch& L, const cg_copy_desc* d, const cg_verdict* v, uint64_t n, const ShadowView& sv,
-                      uint8_t* pool, const Plan& p, uint8_t* scratch, uint32_t* overflow, cudaStream_t s);
+cudaError_t propagate(const Launch& L, const cg_copy_desc* d, const cg_verdict* v, const uint32_t* index, uint64_t n,
+                      const ShadowView& sv, uint8_t* pool, const Plan& p, uint8_t* scratch, uint32_t* overflow,
+                      cudaStream_t s, bool reset_overflow);
+cudaError_t propagate_direct(const Launch& L, const cg_copy_desc* d, const cg_verdict* v, const uint32_t* index,
+                             uint64_t m, uint64_t max_bytes, const ShadowView& sv, uint8_t* pool, const Plan& p,
+                             uint8_t* scratch, uint32_t* overflow, cudaStream_t s);
 size_t scan_meta_bytes();
 
 cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out,

@@ -1544,18 +1544,20 @@ constexpr uint64_t kStageBytes = 8ull << 20;   // staging of self-overlapping 2D
 // and weight; a DtoD whose pool source and target ranges overlap goes to the
 // memmove list instead (processed by k_memmove, one CTA each).
 __global__ void __launch_bounds__(kThreads) k_prop_prep(const cg_copy_desc* __restrict__ descs,
-                                                        const cg_verdict* __restrict__ verd, uint64_t n,
+                                                        const cg_verdict* __restrict__ verd,
+                                                        const uint32_t* __restrict__ index, uint64_t n,
                                                         const uint64_t* __restrict__ dvoff, uint64_t sb,
                                                         uint64_t* __restrict__ weight, PropMeta* __restrict__ pm,
                                                         uint32_t* __restrict__ count, uint32_t* __restrict__ mm,
                                                         uint32_t* __restrict__ mm_count) {
   const int lane = threadIdx.x & 31;
   for (uint64_t b0 = (uint64_t)blockIdx.x * blockDim.x; b0 < n; b0 += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i = b0 + threadIdx.x;
+    const uint64_t k = b0 + threadIdx.x;
+    const uint64_t i = k < n ? (index ? (uint64_t)index[k] : k) : ~0ull;   // a wave's subset, or all
     bool ok = false;
     PropMeta m;
     uint64_t w = 0;
-    if (i < n && verd[i].status == CG_OK) {
+    if (k < n && verd[i].status == CG_OK) {
       const cg_copy_desc d = descs[i];
       const Norm nm = normalize(d);
       const uint64_t nb = d.width * d.height;   // status OK: no INVALID_RANGE, so no overflow
@@ -1635,12 +1637,20 @@ __device__ __forceinline__ void warp_copy(uint8_t* dst, const uint8_t* src, uint
   const uint64_t body = (len - head) & ~15ull;
   if ((uint64_t)lane < head) dst[lane] = src[lane];
   uint4* d4 = reinterpret_cast<uint4*>(dst + head);
-  if ((((uintptr_t)dst ^ (uintptr_t)src) & 15) == 0) {
-    const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
-    for (uint64_t k = lane; k < body / 16; k += 32) d4[k] = s4[k];
-  } else {
-    for (uint64_t k = lane; k < body / 16; k += 32) d4[k] = load_unaligned16(src + head + 16 * k);
+  const uint64_t nv = body / 16;
+  const bool same = (((uintptr_t)dst ^ (uintptr_t)src) & 15) == 0;
+  // four vectors per lane in flight: all loads before the stores (src and dst may alias)
+  uint64_t k = lane;
+  for (; k + 96 < nv; k += 128) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      v[u] = same ? reinterpret_cast<const uint4*>(src + head)[k + 32 * u] : load_unaligned16(src + head + 16 * (k + 32 * u));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) d4[k + 32 * u] = v[u];
   }
+  for (; k < nv; k += 32)
+    d4[k] = same ? reinterpret_cast<const uint4*>(src + head)[k] : load_unaligned16(src + head + 16 * k);
   for (uint64_t k = head + body + lane; k < len; k += 32) dst[k] = src[k];
 }
 
@@ -1681,6 +1691,123 @@ __global__ void __launch_bounds__(kThreads) k_propagate(const PropMeta* __restri
         c = 0;
       }
     }
+  }
+}
+
+// copy len bytes with the whole CTA (the block-wide analogue of warp_copy)
+__device__ __forceinline__ void block_copy(uint8_t* dst, const uint8_t* src, uint64_t len) {
+  const uint32_t t = threadIdx.x, nt = blockDim.x;
+  if (len < 64) {
+    for (uint64_t k = t; k < len; k += nt) dst[k] = src[k];
+    return;
+  }
+  const uint64_t head = (16 - ((uintptr_t)dst & 15)) & 15;
+  const uint64_t body = (len - head) & ~15ull;
+  if (t < head) dst[t] = src[t];
+  uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+  const bool same = (((uintptr_t)dst ^ (uintptr_t)src) & 15) == 0;
+  for (uint64_t k = t; k < body / 16; k += nt)
+    d4[k] = same ? reinterpret_cast<const uint4*>(src + head)[k] : load_unaligned16(src + head + 16 * k);
+  for (uint64_t k = head + body + t; k < len; k += nt) dst[k] = src[k];
+}
+
+__device__ __forceinline__ void block_zero(uint8_t* dst, uint64_t len) {
+  for (uint64_t k = threadIdx.x; k < len; k += blockDim.x) dst[k] = 0;
+}
+
+// one wave copy's V-bit move: bases, offsets (false: nothing to move, or a
+// self-overlapping DtoD, which the caller hands to the memmove list)
+struct WaveCopy {
+  uint8_t *sbase, *dbase;
+  uint64_t src, dst, W, nb;
+  bool zero, self_overlap;
+};
+__device__ __forceinline__ bool wave_copy(const cg_copy_desc& d, uint32_t i, const uint64_t* dvoff, uint64_t sb,
+                                          uint8_t* V, uint8_t* pool, WaveCopy& w) {
+  w.W = d.width;
+  w.nb = d.width * d.height;
+  w.zero = w.self_overlap = false;
+  if (w.nb == 0 || d.kind == CG_HTOA || d.kind < CG_HTOD || d.kind > CG_ATOH) return false;
+  const Norm nm = normalize(d);
+  w.sbase = w.dbase = V;
+  w.src = w.dst = 0;
+  if (d.kind == CG_ATOH) {   // R-30: the host range becomes defined
+    w.dst = nm.ds - sb;
+    w.zero = true;
+  } else if (d.kind == CG_HTOD) {
+    w.src = nm.ss - sb;
+    w.dst = dvoff[2 * i];
+    w.dbase = pool;
+  } else if (d.kind == CG_DTOH) {
+    w.src = dvoff[2 * i + 1];
+    w.dst = nm.ds - sb;
+    w.sbase = pool;
+  } else {
+    w.src = dvoff[2 * i + 1];
+    w.dst = dvoff[2 * i];
+    w.sbase = w.dbase = pool;
+    w.self_overlap = w.src < w.dst + nm.dspan && w.dst < w.src + nm.sspan;
+    if (w.self_overlap) return false;
+  }
+  return true;
+}
+
+// one propagation wave (NEXT-1, cg_plan_waves) without a plan, three launches
+// per wave.  Many copies: a warp per copy; few: CTA (x, y) moves the y-th
+// 16 KiB slice of copy x.  A self-overlapping DtoD goes to the memmove list.
+constexpr uint64_t kDirectSlice = 16384;
+__global__ void __launch_bounds__(kThreads) k_prop_direct_warp(const cg_copy_desc* __restrict__ descs,
+                                                               const cg_verdict* __restrict__ verd,
+                                                               const uint32_t* __restrict__ index, uint64_t m,
+                                                               const uint64_t* __restrict__ dvoff, uint64_t sb,
+                                                               uint8_t* V, uint8_t* pool, uint32_t* __restrict__ mm,
+                                                               uint32_t* __restrict__ mm_count) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t k = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < m; k += nw) {
+    const uint32_t i = index[k];
+    if (verd[i].status != CG_OK) continue;
+    const cg_copy_desc d = descs[i];
+    WaveCopy w;
+    if (!wave_copy(d, i, dvoff, sb, V, pool, w)) {
+      if (w.self_overlap && lane == 0) mm[atomicAdd(mm_count, 1u)] = i;
+      continue;
+    }
+    for (uint64_t r = 0; r < d.height; ++r) {
+      if (w.zero) warp_store_zero(w.dbase, w.dst + r * d.dst_pitch, w.dst + r * d.dst_pitch + w.W);
+      else warp_copy(w.dbase + w.dst + r * d.dst_pitch, w.sbase + w.src + r * d.src_pitch, w.W);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_prop_direct(const cg_copy_desc* __restrict__ descs,
+                                                          const cg_verdict* __restrict__ verd,
+                                                          const uint32_t* __restrict__ index, uint64_t m,
+                                                          const uint64_t* __restrict__ dvoff, uint64_t sb, uint8_t* V,
+                                                          uint8_t* pool, uint32_t* __restrict__ mm,
+                                                          uint32_t* __restrict__ mm_count) {
+  const uint64_t k = blockIdx.x;
+  if (k >= m) return;
+  const uint32_t i = index[k];
+  if (verd[i].status != CG_OK) return;
+  const cg_copy_desc d = descs[i];
+  const uint64_t lo = (uint64_t)blockIdx.y * kDirectSlice;
+  if (lo >= d.width * d.height) return;
+  WaveCopy w;
+  if (!wave_copy(d, i, dvoff, sb, V, pool, w)) {
+    if (w.self_overlap && blockIdx.y == 0 && threadIdx.x == 0) mm[atomicAdd(mm_count, 1u)] = i;   // once
+    return;
+  }
+  const uint64_t W = w.W, hi = umin64(w.nb, lo + kDirectSlice), src = w.src, dst = w.dst;
+  uint8_t *sbase = w.sbase, *dbase = w.dbase;
+  uint64_t r = lo / W, c = lo - r * W, o = lo;
+  while (o < hi) {   // row segments (R-11); both sides advance by their own pitch
+    const uint64_t len = umin64(W - c, hi - o);
+    if (w.zero) block_zero(dbase + dst + r * d.dst_pitch + c, len);
+    else block_copy(dbase + dst + r * d.dst_pitch + c, sbase + src + r * d.src_pitch + c, len);
+    o += len;
+    ++r;
+    c = 0;
   }
 }
 
@@ -2109,17 +2236,18 @@ cudaError_t expand_1d(const Launch& L, const cg_copy1d* in, uint64_t n, cg_copy_
   return cudaGetLastError();
 }
 
-cudaError_t propagate(const Launch& L, const cg_copy_desc* d, const cg_verdict* v, uint64_t n, const ShadowView& sv,
-                      uint8_t* pool, const Plan& p, uint8_t* scratch, uint32_t* overflow, cudaStream_t s) {
+cudaError_t propagate(const Launch& L, const cg_copy_desc* d, const cg_verdict* v, const uint32_t* index, uint64_t n,
+                      const ShadowView& sv, uint8_t* pool, const Plan& p, uint8_t* scratch, uint32_t* overflow,
+                      cudaStream_t s, bool reset_overflow) {
   if (n == 0) return cudaSuccess;
   PropMeta* pm = reinterpret_cast<PropMeta*>(p.meta);   // 48 B per item: the meta area holds max_descs of them
   uint32_t* cnt = p.counter + 1;
   uint32_t* mm_count = p.counter + 3;
   cudaMemsetAsync(p.weight, 0, n * sizeof(uint64_t), s);
   cudaMemsetAsync(p.counter, 0, 4 * sizeof(uint32_t), s);
-  cudaMemsetAsync(overflow, 0, sizeof(uint32_t), s);
+  if (reset_overflow) cudaMemsetAsync(overflow, 0, sizeof(uint32_t), s);
   L.stage(CG_STAGE_APPLY_PREP, true, s);
-  k_prop_prep<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(d, v, n, p.dvoff, sv.sb, p.weight, pm,
+  k_prop_prep<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(d, v, index, n, p.dvoff, sv.sb, p.weight, pm,
                                                                           cnt, p.resid, mm_count);
   L.stage(CG_STAGE_APPLY_PREP, false, s);
   L.stage(CG_STAGE_APPLY_PLAN, true, s);
@@ -2133,6 +2261,27 @@ cudaError_t propagate(const Launch& L, const cg_copy_desc* d, const cg_verdict* 
   k_memmove<<<64, kThreads, 0, s>>>(d, p.dvoff, p.resid, mm_count, pool, scratch, overflow);
   L.stage(CG_STAGE_APPLY, false, s);
   *L.counter += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t propagate_direct(const Launch& L, const cg_copy_desc* d, const cg_verdict* v, const uint32_t* index,
+                             uint64_t m, uint64_t max_bytes, const ShadowView& sv, uint8_t* pool, const Plan& p,
+                             uint8_t* scratch, uint32_t* overflow, cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  uint32_t* mm_count = p.counter + 3;
+  cudaMemsetAsync(mm_count, 0, sizeof(uint32_t), s);
+  L.stage(CG_STAGE_APPLY, true, s);
+  const uint64_t slices = std::max<uint64_t>(1, (max_bytes + kDirectSlice - 1) / kDirectSlice);
+  if (m * slices > (uint64_t)L.num_sms * 512) {   // very many copies: a warp each
+    k_prop_direct_warp<<<blocks_for(m * 32, kThreads, 1 << 20), kThreads, 0, s>>>(d, v, index, m, p.dvoff, sv.sb,
+                                                                                   sv.V, pool, p.resid, mm_count);
+  } else {   // CTA slices keep the larger copies of the later waves streaming
+    k_prop_direct<<<dim3((unsigned)m, (unsigned)slices), kThreads, 0, s>>>(d, v, index, m, p.dvoff, sv.sb, sv.V, pool,
+                                                                          p.resid, mm_count);
+  }
+  k_memmove<<<64, kThreads, 0, s>>>(d, p.dvoff, p.resid, mm_count, pool, scratch, overflow);
+  L.stage(CG_STAGE_APPLY, false, s);
+  *L.counter += 2;
   return cudaGetLastError();
 }
 

@@ -335,6 +335,7 @@ extern "C" {
 
 cg_status cg_apply_copies(cg_ctx* c, const cg_copy_desc* d_descs, const cg_verdict* d_verdicts, uint64_t n,
                           void* stream);
+cg_status cg_apply_flush(cg_ctx* c, void* stream);
 
 uint64_t cg_workspace_size(const cg_config* cfg) {
   if (!valid_config(cfg)) return 0;
@@ -405,7 +406,8 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
     }
     for (auto& ev : c->chunk_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   }
-  e = cgk::fresh_shadow(c->launch, c->sv, 0);
+  e = cudaMemset(c->ws + lay.flags, 0, 256);   // counters, overflow flag
+  if (e == cudaSuccess) e = cgk::fresh_shadow(c->launch, c->sv, 0);
   if (e == cudaSuccess && cfg->dev_vbuf) e = cudaMemset(cfg->dev_vbuf, 0xFF, cfg->dev_vsize);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
@@ -885,6 +887,60 @@ cg_status cg_apply_dtoh(cg_ctx* c, const cg_copy_desc* d_descs, const cg_verdict
   return c->cuda(e, "apply kernels");
 }
 
+cg_status cg_apply_copies_subset(cg_ctx* c, const cg_copy_desc* d_descs, const cg_verdict* d_verdicts, uint64_t n,
+                                 const uint32_t* d_index, uint64_t m, uint64_t max_bytes, void* stream) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (!c->cfg.dev_vbuf) return c->fail(CG_ERR_NOT_INITIALIZED, "no device V-bit tracking");
+  if (n == 0 || m == 0) return CG_OK;
+  if (!d_descs || !d_verdicts || !d_index) return c->fail(CG_ERR_INVALID_VALUE, "null descriptor, verdict or index array");
+  if (m > n) return c->fail(CG_ERR_INVALID_VALUE, "m > n");
+  if (d_descs != c->last_check || n != c->last_check_n)
+    return c->fail(CG_ERR_INVALID_VALUE, "cg_apply_copies must follow the check of the same descriptors");
+  DeviceGuard g(c->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint32_t* overflow = reinterpret_cast<uint32_t*>(c->ws + c->lay.flags + 224);
+  // asynchronous: a staging overflow stays flagged until cg_apply_flush.  Waves
+  // of copies up to kDirectMax bytes take the plan-free warp-per-copy kernel.
+  constexpr uint64_t kDirectMax = 1ull << 20;
+  uint8_t* pool = static_cast<uint8_t*>(c->cfg.dev_vbuf);
+  cudaError_t e = max_bytes && max_bytes <= kDirectMax
+                      ? cgk::propagate_direct(c->launch, d_descs, d_verdicts, d_index, m, max_bytes, c->sv, pool,
+                                              c->plan(), c->ws + c->lay.scratch, overflow, s)
+                      : cgk::propagate(c->launch, d_descs, d_verdicts, d_index, m, c->sv, pool, c->plan(),
+                                       c->ws + c->lay.scratch, overflow, s, false);
+  return c->cuda(e, "propagate");
+}
+
+cg_status cg_apply_copies_waves(cg_ctx* c, const cg_copy_desc* d_descs, const cg_verdict* d_verdicts, uint64_t n,
+                                const uint32_t* d_index, const uint64_t* h_wave_start, const uint64_t* h_max_bytes,
+                                uint32_t n_waves, void* stream) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (n_waves && (!h_wave_start || !h_max_bytes)) return c->fail(CG_ERR_INVALID_VALUE, "null wave arrays");
+  for (uint32_t w = 0; w < n_waves; ++w) {   // in level order, all launches from this loop
+    if (h_wave_start[w + 1] < h_wave_start[w] || h_wave_start[w + 1] > n)
+      return c->fail(CG_ERR_INVALID_VALUE, "wave offsets not increasing or beyond n");
+    const cg_status st = cg_apply_copies_subset(c, d_descs, d_verdicts, n, d_index + h_wave_start[w],
+                                                h_wave_start[w + 1] - h_wave_start[w], h_max_bytes[w], stream);
+    if (st != CG_OK) return st;
+  }
+  return cg_apply_flush(c, stream);
+}
+
+cg_status cg_apply_flush(cg_ctx* c, void* stream) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (!c->cfg.dev_vbuf) return CG_OK;
+  DeviceGuard g(c->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint32_t* overflow = reinterpret_cast<uint32_t*>(c->ws + c->lay.flags + 224);
+  uint32_t h_over = 0;
+  cudaError_t e = cudaMemcpyAsync(&h_over, overflow, sizeof h_over, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(overflow, 0, sizeof(uint32_t), s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return c->cuda(e, "propagate");
+  if (h_over) return c->fail(CG_ERR_INVALID_VALUE, "self-overlapping 2D DtoD larger than the staging area");
+  return CG_OK;
+}
+
 cg_status cg_apply_copies(cg_ctx* c, const cg_copy_desc* d_descs, const cg_verdict* d_verdicts, uint64_t n,
                           void* stream) {
   if (!c) return CG_ERR_INVALID_CONTEXT;
@@ -896,8 +952,9 @@ cg_status cg_apply_copies(cg_ctx* c, const cg_copy_desc* d_descs, const cg_verdi
   DeviceGuard g(c->cfg.device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   uint32_t* overflow = reinterpret_cast<uint32_t*>(c->ws + c->lay.flags + 224);
-  cudaError_t e = cgk::propagate(c->launch, d_descs, d_verdicts, n, c->sv, static_cast<uint8_t*>(c->cfg.dev_vbuf),
-                                 c->plan(), c->ws + c->lay.scratch, overflow, s);
+  cudaError_t e = cgk::propagate(c->launch, d_descs, d_verdicts, nullptr, n, c->sv,
+                                 static_cast<uint8_t*>(c->cfg.dev_vbuf), c->plan(), c->ws + c->lay.scratch, overflow, s,
+                                 true);
   uint32_t h_over = 0;
   if (e == cudaSuccess) e = cudaMemcpyAsync(&h_over, overflow, sizeof h_over, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -1219,6 +1276,83 @@ struct IvSet {   // disjoint merged intervals
   }
 };
 }  // namespace
+
+namespace {
+// disjoint intervals of host or device addresses, each with the highest wave
+// level (+1) that read (or wrote) it so far
+struct LevelMap {
+  std::map<uint64_t, std::pair<uint64_t, uint32_t>> m;   // start -> (end, level + 1)
+  uint32_t max_over(uint64_t lo, uint64_t hi) const {
+    uint32_t r = 0;
+    auto it = m.upper_bound(lo);
+    if (it != m.begin()) --it;
+    for (; it != m.end() && it->first < hi; ++it)
+      if (it->second.first > lo) r = std::max(r, it->second.second);
+    return r;
+  }
+  void split(uint64_t x) {   // make x an interval boundary
+    auto it = m.upper_bound(x);
+    if (it == m.begin()) return;
+    --it;
+    if (it->first < x && it->second.first > x) {
+      m.emplace(x, it->second);
+      it->second.first = x;
+    }
+  }
+  void erase(uint64_t lo, uint64_t hi) {
+    split(lo);
+    split(hi);
+    m.erase(m.lower_bound(lo), m.lower_bound(hi));
+  }
+  void assign(uint64_t lo, uint64_t hi, uint32_t v) {
+    erase(lo, hi);
+    m.emplace(lo, std::make_pair(hi, v));
+  }
+  void paint_max(uint64_t lo, uint64_t hi, uint32_t v) {
+    split(lo);
+    split(hi);
+    uint64_t cur = lo;
+    for (auto it = m.lower_bound(lo); it != m.end() && it->first < hi; ++it) {
+      if (it->first > cur) it = m.emplace_hint(it, cur, std::make_pair(it->first, v));   // the gap before it
+      else it->second.second = std::max(it->second.second, v);
+      cur = it->second.first;
+    }
+    if (cur < hi) m.emplace(cur, std::make_pair(hi, v));
+  }
+};
+}  // namespace
+
+cg_status cg_plan_waves(const cg_copy_desc* h_descs, uint64_t n, uint32_t* h_level, uint32_t* n_levels) {
+  if (!n_levels || (n && (!h_descs || !h_level))) return CG_ERR_INVALID_VALUE;
+  // per address space ([0] host, [1] device): the levels of earlier readers and
+  // writers.  A write at level l dominates every earlier access of its range
+  // (it conflicted with all of them), so it replaces the writer entries and
+  // clears the reader entries there; reads merge by max.
+  LevelMap rd[2], wr[2];
+  uint32_t top = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const cg_copy_desc& d = h_descs[i];
+    h_level[i] = 0;
+    if (d.kind < CG_HTOD || d.kind > CG_ATOH) continue;
+    uint64_t rlo, rhi, wlo, whi;
+    // the same read / write sets as cg_plan_batches_propagate (R-28, R-30)
+    const bool r_ok = d.kind != CG_ATOH && side_range(d, false, rlo, rhi);
+    const bool w_ok = d.kind != CG_HTOA && side_range(d, true, wlo, whi);
+    const int rs = reads_host(d.kind) ? 0 : 1, ws = writes_host(d.kind) ? 0 : 1;
+    uint32_t lv = 0;   // = 1 + the highest conflicting earlier level (maps hold level + 1), 0 if none
+    if (r_ok) lv = std::max(lv, wr[rs].max_over(rlo, rhi));                                        // RAW
+    if (w_ok) lv = std::max(lv, std::max(rd[ws].max_over(wlo, whi), wr[ws].max_over(wlo, whi)));   // WAR, WAW
+    h_level[i] = lv;
+    if (r_ok) rd[rs].paint_max(rlo, rhi, lv + 1);
+    if (w_ok) {
+      rd[ws].erase(wlo, whi);
+      wr[ws].assign(wlo, whi, lv + 1);
+    }
+    top = std::max(top, lv + 1);
+  }
+  *n_levels = n ? std::max(top, 1u) : 0;
+  return CG_OK;
+}
 
 cg_status cg_plan_batches_propagate(const cg_copy_desc* h_descs, uint64_t n, uint64_t* h_cuts, uint64_t* n_cuts) {
   if (!n_cuts || (n && (!h_descs || !h_cuts))) return CG_ERR_INVALID_VALUE;

@@ -90,14 +90,20 @@ def replay_events(chk, events: np.ndarray, blob=None, stream=None, fuse: bool = 
                 descs = events_to_descs(events[idx])
                 pkg = __import__(__package__)
                 tracking = getattr(chk, "tracking", False)
-                cuts = [0] + [int(c) for c in pkg.plan_batches(descs, propagate=tracking)]
+                # R-20 epochs for the check; with tracking, each epoch's V-bit
+                # propagation runs in the waves of cg_plan_waves (R-28)
+                cuts = [0] + [int(c) for c in pkg.plan_batches(descs)]
                 for a, b in zip(cuts[:-1], cuts[1:]):
                     for s0 in range(a, b, chk.max_descs):
                         s1 = min(b, s0 + chk.max_descs)
                         dd = to_device_descs(descs[s0:s1], chk.device)
-                        if tracking:    # NEXT-1: check, then move V-bits
+                        if tracking:    # NEXT-1: check, then move V-bits wave by wave
                             dv = chk.check_copies(dd, stream=stream)
-                            chk.apply_copies(dd, dv, stream=stream)
+                            waves = pkg.Waves(descs[s0:s1], chk.device)
+                            if waves.n_waves <= 1:
+                                chk.apply_copies(dd, dv, stream=stream)
+                            else:
+                                chk.apply_waves(dd, dv, waves, stream=stream)
                         elif fuse and pkg.batch_disjoint(descs[s0:s1]):
                             dv = chk.check_apply(dd, stream=stream)
                         else:

@@ -286,3 +286,29 @@ def test_header_is_plain_c(tmp_path):
     r = subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-pedantic", "-fsyntax-only",
                         "-I", os.path.join(ROOT, "include"), str(src)], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.parametrize("arrays", [False, True])
+@pytest.mark.parametrize("seed", range(30))
+def test_plan_waves_brute_force(cg, seed, arrays):
+    """cg_plan_waves: level(i) = 1 + the highest level of an earlier copy whose
+    V-bit reads / writes conflict with copy i's (RAW, WAR, WAW), 0 if none --
+    recomputed here by brute force over all earlier pairs"""
+    from paper_1310_0901_b200.replay import events_to_descs
+    tr = tg.random_tiny(seed + 50000, arrays=arrays)
+    descs = events_to_descs(tr.events[tr.events["op"] == tg.OP_COPY])
+    lev, nl = cg.plan_waves(descs)
+    sets = [_sets(d) for d in descs]
+
+    def ov(x, y):
+        return x[0] == y[0] and x[1] < y[2] and y[1] < x[2]
+    want = []
+    for i, (ri, wi) in enumerate(sets):
+        lv = 0
+        for j in range(i):
+            rj, wj = sets[j]
+            if any(ov(a, b) for a in ri for b in wj) or any(ov(a, b) for a in wi for b in rj + wj):
+                lv = max(lv, want[j] + 1)
+        want.append(lv)
+    assert list(lev) == want
+    assert nl == (max(want) + 1 if want else 0)

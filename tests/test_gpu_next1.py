@@ -100,3 +100,26 @@ def test_self_overlapping_dtod(cg, shape, shift):
     else:
         tb.copy2d(tg.DTOD, 300, 40, d + s0 + shift, 0, 0, 650, d + s0, 0, 0, 700)
     run_tracking(cg, tb.build())
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_round_trip_large_waves(cg, seed):
+    """HtoD -> DtoD -> DtoH chains of 2-3 MiB copies: three waves whose copies
+    exceed the warp-per-copy limit, so each wave takes the planned path"""
+    rng = np.random.default_rng(seed + 100)
+    H0 = 1 << 24
+    tb = tg.TraceBuilder("rtl", H0, 16 << 20)
+    n = int(rng.integers(2 << 20, 3 << 20))
+    d0, d1 = tb.malloc(n + 256), tb.malloc(n + 256)
+    pat = rng.integers(0, 256, n, dtype=np.uint8)
+    pat[rng.random(n) < 0.7] = 0
+    tb.mark(H0, n, tg.DEFINED)
+    tb.setv(H0, pat.tobytes())
+    tb.mark(H0 + (8 << 20), n, tg.UNDEFINED)
+    tb.copy1d(tg.HTOD, d0, H0, n)
+    tb.copy1d(tg.DTOD, d1 + 16, d0, n)
+    tb.copy1d(tg.DTOH, H0 + (8 << 20), d1 + 16, n)
+    tr = tb.build()
+    run_tracking(cg, tr)
+    o = oracle.replay_trace(tr, track_device=True)[0]
+    assert np.array_equal(o.V[8 << 20:(8 << 20) + n], pat)
