@@ -411,6 +411,22 @@ def run_ours(args, rank, world, device):
         if pj.get("fused") == fused:
             traffic = pj.get("dram_bytes_per_launch")
     value = world * bytes_per_step / (ms_step * 1e-3) / 1e9
+    roof = {"bound": "hbm", "kernel": "k_check_scan", "achieved": achieved, "peak": peak,
+            "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "algorithmic_bytes_per_launch": scan_bytes / launches_scan,
+            "avg_launch_ms": scan_avg,
+            "share_of_step": scan_ms / ms if ms > 0 else None}
+    check_roof = None
+    if args.track and apply_ms:
+        # NEXT-1: the propagation (k_prop_waves, one cooperative launch per
+        # epoch with waves) dominates the step: 1 B read + 1 B written per byte
+        # of every error-free copy
+        check_roof, launches_apply = roof, max(apply_n / max(args.steps, 1), 1.0)
+        ach = apply_b / (apply_ms / max(args.steps, 1) * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": "k_prop_waves", "achieved": ach, "peak": peak,
+                "peak_source": peak_kind, "unit": "GB/s", "frac": ach / peak, "traffic": None,
+                "algorithmic_bytes_per_launch": apply_b / launches_apply,
+                "avg_launch_ms": apply_ms / max(apply_n, 1), "share_of_step": apply_ms / ms if ms > 0 else None}
     res = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -430,11 +446,8 @@ def run_ours(args, rank, world, device):
                    "wave_planning_s": t_waves if args.track else None},
         "descriptors_per_s": world * n / (ms_step * 1e-3),
         "frac_of_hbm": value / (world * peak),
-        "roofline": {"bound": "hbm", "kernel": "k_check_scan", "achieved": achieved, "peak": peak,
-                     "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "algorithmic_bytes_per_launch": scan_bytes / launches_scan,
-                     "avg_launch_ms": scan_avg,
-                     "share_of_step": scan_ms / ms if ms > 0 else None},
+        "roofline": roof,
+        "check_roofline": check_roof,
         "stages_ms_per_step": {k: v[0] / max(args.steps, 1) for k, v in stages.items()},
         "apply_roofline": {"achieved": (apply_b - (scan_bytes - check_b)) / (apply_ms / max(args.steps, 1) * 1e-3) / 1e9
                            if apply_ms else None, "unit": "GB/s", "peak": peak,

@@ -174,7 +174,9 @@ typedef struct {
  *    never reused; fresh = undefined) and cg_apply_copies moves V-bits
  *    through error-free copies (HtoD host->device, DtoD device->device with
  *    memmove semantics, DtoH device->host) instead of R-5's "DtoH marks the
- *    host range defined".  dev_vsize must be a multiple of 16.  Requires an
+ *    host range defined".  dev_vbuf must be 16-byte aligned and dev_vsize a
+ *    multiple of 16 (the propagation stages 16-byte-aligned supersets of
+ *    its ranges with bulk copies).  Requires an
  *    unsharded context.
  *  - shadow_format (NEXT-4): CG_SHADOW_BYTES (0) = one V byte per
  *    host byte + one A bit per host byte (v_buf / a_buf as above);

@@ -115,6 +115,7 @@ struct Launch {
   int num_sms;
   int persist_blocks;     // persistent grid for the chunked kernels
   int scan_blocks;        // persistent grid of the TMA-ring scan
+  int wave_blocks;        // cooperative grid of k_prop_waves (all co-resident)
   uint64_t* counter;      // host counter of kernel launches
   Profiler* prof;
   void stage(int st, bool begin, cudaStream_t s) const {
@@ -125,7 +126,7 @@ struct Launch {
 constexpr int kScanTile = 2048;   // items per block of the prefix scan
 
 uint64_t scan_blocks(uint64_t n);
-int persistent_blocks(int which);   // 0: k_check_scan, 1: k_apply (per SM)
+int persistent_blocks(int which);   // 0: k_check_scan, 1: k_apply, 2: k_prop_waves (per SM)
 size_t prop_meta_bytes();
 uint64_t stage_bytes();
 cudaError_t propagate(const Launch& L, const cg_copy_desc* d, const cg_verdict* v, const uint32_t* index, uint64_t n,
@@ -134,6 +135,9 @@ cudaError_t propagate(const Launch& L, const cg_copy_desc* d, const cg_verdict* 
 cudaError_t propagate_direct(const Launch& L, const cg_copy_desc* d, const cg_verdict* v, const uint32_t* index,
                              uint64_t m, uint64_t max_bytes, const ShadowView& sv, uint8_t* pool, const Plan& p,
                              uint8_t* scratch, uint32_t* overflow, cudaStream_t s);
+cudaError_t propagate_waves(const Launch& L, const cg_copy_desc* d, const cg_verdict* v, const uint32_t* index,
+                            uint64_t m, const uint32_t* d_wstart, uint32_t n_waves, const ShadowView& sv,
+                            uint8_t* pool, const Plan& p, uint8_t* scratch, uint32_t* overflow, cudaStream_t s);
 size_t scan_meta_bytes();
 
 cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out,

@@ -31,6 +31,7 @@
 // both indexed by (x - shard_base); H0 % 4096 == 0 so a 16-byte V group maps to
 // one aligned 16-bit A half-word and a 128-byte V range to one 16-byte A vector.
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -1811,9 +1812,63 @@ __global__ void __launch_bounds__(kThreads) k_prop_direct(const cg_copy_desc* __
   }
 }
 
-// self-overlapping DtoD, one CTA each: equal pitches shift every byte by the
-// same delta, so a directional block copy is exact memmove; unequal pitches
-// stage all logical bytes first (scratch of kStageBytes), else set *overflow
+// one self-overlapping DtoD with the whole CTA: equal pitches shift every byte
+// by the same delta, so a directional block copy is exact memmove; unequal
+// pitches stage all logical bytes first (scratch of kStageBytes), else set
+// *overflow
+__device__ __forceinline__ void block_memmove(const cg_copy_desc& d, uint64_t so, uint64_t dso, uint8_t* pool,
+                                              uint8_t* scratch, uint32_t* overflow) {
+  const uint64_t W = d.width, H = d.height;
+  if (d.src_pitch == d.dst_pitch || H == 1) {
+    // chunks of 16 bytes per thread, each read completely before it is
+    // written; moving down the chunks go in ascending order, up descending, so
+    // a chunk's stores only reach source bytes already read
+    const bool fwd = dso < so;
+    const uint64_t CH = 16ull * blockDim.x;
+    const bool vec = ((so ^ dso) & 15) == 0 && d.src_pitch % 16 == 0;   // 16-byte vectors line up
+    for (uint64_t rr = 0; rr < H; ++rr) {
+      const uint64_t r = fwd ? rr : H - 1 - rr;
+      const uint8_t* rs = pool + so + r * d.src_pitch;
+      uint8_t* rd = pool + dso + r * d.dst_pitch;
+      for (uint64_t c0 = 0; c0 < W; c0 += CH) {
+        const uint64_t cb = fwd ? c0 : (W > c0 + CH ? W - c0 - CH : 0);
+        const uint64_t ce = fwd ? umin64(W, c0 + CH) : W - c0;
+        const uint64_t c = cb + 16ull * threadIdx.x;
+        const bool full = vec && c + 16 <= ce && ((uintptr_t)(rs + c) & 15) == 0;
+        uint4 x = make_uint4(0, 0, 0, 0);
+        uint8_t* xb = reinterpret_cast<uint8_t*>(&x);
+        if (full) {
+          x = __ldcg(reinterpret_cast<const uint4*>(rs + c));
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (c + q < ce) xb[q] = __ldcg(rs + c + q);
+        }
+        __syncthreads();
+        if (full) {
+          *reinterpret_cast<uint4*>(rd + c) = x;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (c + q < ce) rd[c + q] = xb[q];
+        }
+        __syncthreads();
+      }
+    }
+  } else if (W * H <= kStageBytes) {
+    for (uint64_t o = threadIdx.x; o < W * H; o += blockDim.x)
+      scratch[o] = __ldcg(pool + so + (o / W) * d.src_pitch + o % W);
+    __syncthreads();
+    for (uint64_t o = threadIdx.x; o < W * H; o += blockDim.x)
+      pool[dso + (o / W) * d.dst_pitch + o % W] = __ldcg(scratch + o);
+    __syncthreads();
+  } else if (threadIdx.x == 0) {
+    atomicOr(overflow, 1u);
+  }
+}
+
+// the memmove list of one wave, one CTA per entry (equal pitches: entry k on
+// block k mod grid; unequal: block 0, the scratch is shared)
 __global__ void __launch_bounds__(kThreads) k_memmove(const cg_copy_desc* __restrict__ descs,
                                                       const uint64_t* __restrict__ dvoff,
                                                       const uint32_t* __restrict__ mm,
@@ -1823,33 +1878,354 @@ __global__ void __launch_bounds__(kThreads) k_memmove(const cg_copy_desc* __rest
   for (uint32_t k = 0; k < cnt; ++k) {
     const uint32_t i = mm[k];
     const cg_copy_desc d = descs[i];
-    const uint64_t W = d.width, H = d.height, so = dvoff[2 * i + 1], dso = dvoff[2 * i];
-    // equal pitches: entry k on block k mod grid; unequal: block 0 (the scratch is shared)
-    if (d.src_pitch == d.dst_pitch ? k % gridDim.x != blockIdx.x : blockIdx.x != 0) continue;
-    if (d.src_pitch == d.dst_pitch) {
-      const bool fwd = dso < so;   // moving down: ascending addresses; up: descending
-      for (uint64_t rr = 0; rr < H; ++rr) {
-        const uint64_t r = fwd ? rr : H - 1 - rr;
-        for (uint64_t c0 = 0; c0 < W; c0 += blockDim.x) {
-          const uint64_t cb = fwd ? c0 : (W > c0 + blockDim.x ? W - c0 - blockDim.x : 0);
-          const uint64_t ce = fwd ? umin64(W, c0 + blockDim.x) : W - c0;
-          const uint64_t c = cb + threadIdx.x;
-          uint8_t x = 0;
-          if (c < ce) x = pool[so + r * d.src_pitch + c];
-          __syncthreads();
-          if (c < ce) pool[dso + r * d.dst_pitch + c] = x;
-          __syncthreads();
+    const bool shared = d.src_pitch != d.dst_pitch && d.height > 1;
+    if (shared ? blockIdx.x != 0 : k % gridDim.x != blockIdx.x) continue;
+    block_memmove(d, dvoff[2 * i + 1], dvoff[2 * i], pool, scratch, overflow);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// NEXT-1: all waves of a batch in one persistent cooperative launch
+// ---------------------------------------------------------------------------
+// cg_plan_waves orders the batch's copies into dependency waves (R-28); wave w
+// is positions [wstart[w], wstart[w+1]) of the wave-ordered index.  k_wave_prep
+// writes one PropMeta and weight per position (no compaction, so the wave
+// bounds stay valid); one prefix sum over all positions; k_prop_waves then
+// runs wave after wave with a grid barrier in between: the weight range of a
+// wave is cut into equal pieces, one per warp, so a wave of 170k small copies
+// and a wave of five 64 KiB copies both keep every warp streaming.  A copy
+// whose weight range spans several pieces is moved by all of them, each its
+// own bytes.  Self-overlapping DtoDs (memmove) go to a list worked off at the
+// end of their wave, between two barriers, one CTA per entry.
+constexpr uint64_t kWaveItemCost = 1024;     // per-copy latency, in bytes of bandwidth
+constexpr uint64_t kWaveMinPiece = 16384;    // smallest per-warp share of a wave
+constexpr uint64_t kPropMemmove = 1ull << 44;
+
+__global__ void __launch_bounds__(kThreads) k_wave_prep(const cg_copy_desc* __restrict__ descs,
+                                                        const cg_verdict* __restrict__ verd,
+                                                        const uint32_t* __restrict__ index, uint64_t m,
+                                                        const uint64_t* __restrict__ dvoff, uint64_t sb,
+                                                        uint64_t* __restrict__ weight, PropMeta* __restrict__ pm,
+                                                        uint32_t* __restrict__ mm, uint32_t* __restrict__ mm_count) {
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = index[k];
+    uint64_t w = 0;
+    PropMeta pmk;
+    pmk.info = 0;
+    if (verd[i].status == CG_OK) {
+      const cg_copy_desc d = descs[i];
+      const uint64_t nb = d.width * d.height;   // status OK: no INVALID_RANGE, so no overflow
+      if (nb && d.kind != CG_HTOA) {   // array V-bits are not tracked (R-30): HtoA moves nothing
+        const Norm nm = normalize(d);
+        pmk.W = d.width;
+        pmk.spitch = d.src_pitch;
+        pmk.dpitch = d.dst_pitch;
+        if (d.kind == CG_ATOH) {       // ... and AtoH makes the host bytes defined (R-5)
+          pmk.src = 0;
+          pmk.dst = nm.ds - sb;
+          pmk.info = nb | (1ull << 43);
+        } else if (d.kind == CG_HTOD) {
+          pmk.src = nm.ss - sb;
+          pmk.dst = dvoff[2 * i];
+          pmk.info = nb | (1ull << 42);
+        } else if (d.kind == CG_DTOH) {
+          pmk.src = dvoff[2 * i + 1];
+          pmk.dst = nm.ds - sb;
+          pmk.info = nb | (1ull << 41);
+        } else {
+          pmk.src = dvoff[2 * i + 1];
+          pmk.dst = dvoff[2 * i];
+          pmk.info = nb | (3ull << 41);
+        }
+        w = kWaveItemCost + nb;
+        if (d.kind == CG_DTOD && pmk.src < pmk.dst + nm.dspan && pmk.dst < pmk.src + nm.sspan) {
+          w = 0;   // overlaps itself: the wave's memmove list
+          pmk.info |= kPropMemmove;
+          mm[atomicAdd(mm_count, 1u)] = (uint32_t)k;
         }
       }
-    } else if (W * H <= kStageBytes) {
-      for (uint64_t o = threadIdx.x; o < W * H; o += blockDim.x)
-        scratch[o] = pool[so + (o / W) * d.src_pitch + o % W];
-      __syncthreads();
-      for (uint64_t o = threadIdx.x; o < W * H; o += blockDim.x)
-        pool[dso + (o / W) * d.dst_pitch + o % W] = scratch[o];
-      __syncthreads();
-    } else if (threadIdx.x == 0) {
-      atomicOr(overflow, 1u);
+    }
+    weight[k] = w;
+    pm[k] = pmk;
+  }
+}
+
+// Per warp, a ring of kWStages tiles of up to kWTile source bytes: lane 0
+// stages the 16-byte-aligned superset of a tile's source bytes with one
+// cp.async.bulk (mbarrier transaction count), the warp then writes the tile's
+// destination from shared memory with 16-byte stores to its aligned body
+// (realigned with funnel shifts when source and destination differ mod 16) and
+// byte stores for the head (lanes 0-15) and tail (lanes 16-31).  Loads are the
+// latency-bound side, stores are posted: the ring keeps kWStages - 1 tiles of
+// loads in flight per warp while one is written.
+constexpr int kWRing = 4;                  // warps per CTA
+constexpr int kWStages = 6;
+constexpr uint32_t kWTile = 2048;          // source bytes per tile
+constexpr uint32_t kWBuf = kWTile + 128;   // staged span <= kWTile + 15, rounded up to 16
+
+struct __align__(16) WTile {
+  uint64_t D;     // destination of the tile's first byte (generic address)
+  uint32_t L;     // bytes
+  uint32_t so;    // offset of the first source byte in the staged buffer; bit 31: zero tile (no staging)
+};
+struct WaveRing {
+  uint8_t data[kWStages][kWBuf];
+  WTile info[kWStages];
+  uint64_t bar[kWStages];
+};
+constexpr size_t kWaveSmem = sizeof(WaveRing) * kWRing;
+
+__device__ __forceinline__ void bulk_g2s_nohint(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// the tile generator of one warp (warp-uniform state; the 32-copy metadata
+// window is lane-distributed): wave -> this warp's pieces of the wave's weight
+// range -> copies -> row segments (R-11) -> tiles of <= kWTile bytes
+struct WaveGen {
+  const PropMeta* pm;
+  const uint64_t* P;
+  uint8_t *V, *pool;
+  uint64_t gw, nw;
+  // wave and piece
+  uint64_t a, b, w0, w1, piece, np, pc, s, e;
+  bool have_piece;
+  // window: lane i <-> position k0 + i
+  uint64_t k0, pk, pk1;
+  PropMeta m;
+  uint32_t j;
+  // current copy
+  bool in_copy;
+  uint64_t o, y, r, c, W, src, dst, sp, dp;
+  uint8_t *sb, *db;
+  bool zero;
+
+  __device__ __forceinline__ void begin_wave(const uint32_t* wstart, uint32_t w) {
+    a = __ldg(wstart + w);
+    b = __ldg(wstart + w + 1);
+    w0 = __ldg(P + a);
+    w1 = __ldg(P + b);
+    piece = umax64((w1 - w0 + nw - 1) / nw, kWaveMinPiece);
+    np = w1 > w0 ? (w1 - w0 + piece - 1) / piece : 0;
+    pc = gw;
+    have_piece = in_copy = false;
+  }
+
+  __device__ __forceinline__ void load_window() {
+    const uint64_t kk = k0 + (threadIdx.x & 31);
+    pk = pk1 = ~0ull;
+    m.info = 0;
+    if (kk < b) {
+      pk = __ldg(P + kk);
+      pk1 = __ldg(P + kk + 1);
+      m = pm[kk];
+    }
+  }
+
+  // the warp's next piece of the wave: 32-ary search for the last position
+  // k in [a, b) with P[k] <= s (its weight range holds s)
+  __device__ __forceinline__ bool begin_piece() {
+    if (pc >= np) return false;
+    s = w0 + pc * piece;
+    e = umin64(s + piece, w1);
+    pc += nw;
+    const uint32_t lane = threadIdx.x & 31;
+    uint64_t lo = a, hi = b;
+    while (hi - lo > 1) {
+      const uint64_t step = (hi - lo + 31) >> 5, x = lo + lane * step;
+      const uint32_t le = __ballot_sync(kFull, x < hi && __ldg(P + x) <= s);
+      lo += (uint64_t)(__popc(le) - 1) * step;
+      hi = umin64(lo + step, hi);
+    }
+    k0 = lo;
+    j = ~0u;   // next_copy starts at window lane 0
+    load_window();
+    have_piece = true;
+    return true;
+  }
+
+  // the next copy with bytes in the current piece (or the next piece)
+  __device__ __forceinline__ bool next_copy() {
+    in_copy = false;
+    while (true) {
+      if (!have_piece && !begin_piece()) return false;
+      if (++j == 32) {
+        k0 += 32;
+        j = 0;
+        load_window();
+      }
+      if (k0 + j >= b) {
+        have_piece = false;
+        continue;
+      }
+      const uint64_t pd = __shfl_sync(kFull, pk, j);
+      if (pd >= e) {
+        have_piece = false;
+        continue;
+      }
+      const uint64_t pd1 = __shfl_sync(kFull, pk1, j);
+      uint64_t x = umax64(s, pd) - pd, yy = umin64(e, pd1) - pd;
+      x = x > kWaveItemCost ? x - kWaveItemCost : 0;
+      yy = yy > kWaveItemCost ? yy - kWaveItemCost : 0;
+      if (x >= yy) continue;   // nothing to move here (or a memmove entry, weight 0)
+      const uint64_t info = __shfl_sync(kFull, m.info, j);
+      W = __shfl_sync(kFull, m.W, j);
+      src = __shfl_sync(kFull, m.src, j);
+      dst = __shfl_sync(kFull, m.dst, j);
+      sp = __shfl_sync(kFull, m.spitch, j);
+      dp = __shfl_sync(kFull, m.dpitch, j);
+      sb = ((info >> 41) & 1u) ? pool : V;
+      db = ((info >> 42) & 1u) ? pool : V;
+      zero = (info >> 43) & 1u;
+      r = x < W ? 0 : x / W;
+      c = x - r * W;
+      o = x;
+      y = yy;
+      in_copy = true;
+      return true;
+    }
+  }
+
+  // issues the next tile into ring slot `slot`; false when the wave holds no more for this warp
+  __device__ __forceinline__ bool next(WaveRing& ring, int slot) {
+    if (!in_copy || o >= y)
+      if (!next_copy()) return false;
+    const uint64_t len = umin64(umin64(W - c, y - o), kWTile);
+    const uint8_t* S = sb + src + r * sp + c;
+    uint8_t* D = db + dst + r * dp + c;
+    o += len;
+    c += len;
+    if (c == W) {
+      ++r;
+      c = 0;
+    }
+    if ((threadIdx.x & 31) == 0) {
+      WTile t;
+      t.D = (uint64_t)D;
+      t.L = (uint32_t)len;
+      if (zero) {
+        t.so = 1u << 31;
+        ring.info[slot] = t;
+        mbar_arrive(&ring.bar[slot]);
+      } else {
+        const uint32_t so = (uint32_t)((uintptr_t)S & 15);
+        const uint32_t span = (so + (uint32_t)len + 15u) & ~15u;
+        t.so = so;
+        ring.info[slot] = t;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_tx(&ring.bar[slot], span);
+        bulk_g2s_nohint(ring.data[slot], S - so, span, &ring.bar[slot]);
+      }
+    }
+    return true;
+  }
+};
+
+__device__ __forceinline__ uint4 funnel16(uint4 lo, uint4 hi, uint32_t m) {
+  const uint32_t q = m >> 2, r = (m & 3) * 8;
+  const uint32_t w0 = q == 0 ? lo.x : q == 1 ? lo.y : q == 2 ? lo.z : lo.w;
+  const uint32_t w1 = q == 0 ? lo.y : q == 1 ? lo.z : q == 2 ? lo.w : hi.x;
+  const uint32_t w2 = q == 0 ? lo.z : q == 1 ? lo.w : q == 2 ? hi.x : hi.y;
+  const uint32_t w3 = q == 0 ? lo.w : q == 1 ? hi.x : q == 2 ? hi.y : hi.z;
+  const uint32_t w4 = q == 0 ? hi.x : q == 1 ? hi.y : q == 2 ? hi.z : hi.w;
+  return make_uint4(__funnelshift_r(w0, w1, r), __funnelshift_r(w1, w2, r), __funnelshift_r(w2, w3, r),
+                    __funnelshift_r(w3, w4, r));
+}
+
+// writes one staged tile to its destination
+__device__ __forceinline__ void wave_consume(const WTile& t, const uint8_t* buf) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint8_t* D = reinterpret_cast<uint8_t*>(t.D);
+  const uint32_t L = t.L;
+  const bool zero = t.so >> 31;
+  const uint32_t so = t.so & 31u;
+  const uint32_t hd = min(L, (uint32_t)((16 - ((uintptr_t)D & 15)) & 15));
+  const uint32_t nv = (L - hd) >> 4, tl = L - hd - 16 * nv;
+  if (lane < hd) D[lane] = zero ? 0 : buf[so + lane];
+  else if (lane >= 16 && lane - 16 < tl) D[hd + 16 * nv + lane - 16] = zero ? 0 : buf[so + hd + 16 * nv + lane - 16];
+  uint4* d4 = reinterpret_cast<uint4*>(D + hd);
+  const uint32_t base = so + hd, sh = base & 15;
+  if (zero) {
+    for (uint32_t v = lane; v < nv; v += 32) d4[v] = make_uint4(0, 0, 0, 0);
+  } else if (sh == 0) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(buf + base);
+    for (uint32_t v = lane; v < nv; v += 32) d4[v] = s4[v];
+  } else {
+    const uint4* s4 = reinterpret_cast<const uint4*>(buf + (base & ~15u));
+    for (uint32_t v = lane; v < nv; v += 32) d4[v] = funnel16(s4[v], s4[v + 1], sh);
+  }
+}
+
+__global__ void __launch_bounds__(kWRing * 32) k_prop_waves(const cg_copy_desc* __restrict__ descs,
+                                                            const uint32_t* __restrict__ index,
+                                                            const PropMeta* __restrict__ pm,
+                                                            const uint64_t* __restrict__ P,
+                                                            const uint32_t* __restrict__ wstart, uint32_t n_waves,
+                                                            uint8_t* V, uint8_t* pool,
+                                                            const uint64_t* __restrict__ dvoff,
+                                                            const uint32_t* __restrict__ mm,
+                                                            const uint32_t* __restrict__ mm_count, uint8_t* scratch,
+                                                            uint32_t* overflow) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  WaveRing& ring = reinterpret_cast<WaveRing*>(smem)[wid];
+  if (lane == 0) {
+    for (int s = 0; s < kWStages; ++s) mbar_init(&ring.bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  WaveGen gen;
+  gen.pm = pm;
+  gen.P = P;
+  gen.V = V;
+  gen.pool = pool;
+  gen.gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  gen.nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t nmm = *mm_count;
+  uint32_t phase = 0;   // bit s = parity to wait for on slot s
+  gen.begin_wave(wstart, 0);
+  gen.begin_piece();
+  for (uint32_t w = 0; w < n_waves; ++w) {
+    int filled = 0;
+    while (filled < kWStages && gen.next(ring, filled)) ++filled;
+    for (int s = 0, left = filled; left > 0; s = (s + 1 == kWStages) ? 0 : s + 1) {
+      mbar_wait(&ring.bar[s], (phase >> s) & 1u);
+      phase ^= 1u << s;
+      const WTile t = ring.info[s];
+      wave_consume(t, ring.data[s]);
+      __syncwarp();
+      if (!gen.next(ring, s)) --left;
+    }
+    const uint64_t a = gen.a, b = gen.b;
+    if (w + 1 < n_waves) {   // the next wave's first piece: search + metadata (static) before the barrier
+      gen.begin_wave(wstart, w + 1);
+      gen.begin_piece();
+    }
+    bool has_mm = nmm > 64;   // a short list is searched for this wave's entries first
+    for (uint32_t k = 0; k < nmm && !has_mm; ++k) {
+      const uint32_t pos = __ldcg(mm + k);
+      has_mm = pos >= a && pos < b;
+    }
+    if (has_mm) {   // this wave's self-overlapping DtoDs, after its other copies
+      grid.sync();
+      for (uint32_t k = 0; k < nmm; ++k) {   // entry k on CTA k mod grid; unequal pitches: CTA 0 (shared scratch)
+        const uint32_t pos = __ldcg(mm + k);
+        if (pos < a || pos >= b) continue;
+        const uint32_t i = __ldg(index + pos);
+        const cg_copy_desc d = descs[i];
+        const bool shared = d.src_pitch != d.dst_pitch && d.height > 1;
+        if (shared ? blockIdx.x != 0 : k % gridDim.x != blockIdx.x) continue;
+        block_memmove(d, __ldg(dvoff + 2 * i + 1), __ldg(dvoff + 2 * i), pool, scratch, overflow);
+      }
+    }
+    if (w + 1 < n_waves) {
+      grid.sync();
+      // the next wave's bulk copies (async proxy) read bytes this wave stored (generic proxy)
+      asm volatile("fence.proxy.async.global;" ::: "memory");
     }
   }
 }
@@ -2285,6 +2661,39 @@ cudaError_t propagate_direct(const Launch& L, const cg_copy_desc* d, const cg_ve
   return cudaGetLastError();
 }
 
+cudaError_t propagate_waves(const Launch& L, const cg_copy_desc* d, const cg_verdict* v, const uint32_t* index,
+                            uint64_t m, const uint32_t* d_wstart, uint32_t n_waves, const ShadowView& sv,
+                            uint8_t* pool, const Plan& p, uint8_t* scratch, uint32_t* overflow, cudaStream_t s) {
+  if (m == 0 || n_waves == 0) return cudaSuccess;
+  PropMeta* pm = reinterpret_cast<PropMeta*>(p.meta);
+  uint32_t* mm_count = p.counter + 3;
+  cudaMemsetAsync(mm_count, 0, sizeof(uint32_t), s);
+  L.stage(CG_STAGE_APPLY_PREP, true, s);
+  k_wave_prep<<<blocks_for(m, kThreads, L.num_sms * 8), kThreads, 0, s>>>(d, v, index, m, p.dvoff, sv.sb, p.weight,
+                                                                          pm, p.resid, mm_count);
+  L.stage(CG_STAGE_APPLY_PREP, false, s);
+  L.stage(CG_STAGE_APPLY_PLAN, true, s);
+  const uint64_t nb = std::max<uint64_t>(scan_blocks(m), 1);
+  k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, m, p.bsum, nullptr);
+  k_scan_top<<<1, 1024, 0, s>>>(p.bsum, m, p.P, nullptr);
+  k_scan_down<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, m, p.bsum, p.P, nullptr);
+  L.stage(CG_STAGE_APPLY_PLAN, false, s);
+  L.stage(CG_STAGE_APPLY, true, s);
+  uint8_t* V = sv.V;
+  const uint64_t* P = p.P;
+  const uint64_t* dvoff = p.dvoff;
+  const uint32_t* mm = p.resid;
+  const uint32_t* mmc = mm_count;
+  void* args[] = {(void*)&d, (void*)&index, (void*)&pm, (void*)&P, (void*)&d_wstart, (void*)&n_waves, (void*)&V,
+                  (void*)&pool, (void*)&dvoff, (void*)&mm, (void*)&mmc, (void*)&scratch, (void*)&overflow};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_prop_waves, dim3((unsigned)L.wave_blocks),
+                                              dim3(kWRing * 32), args, kWaveSmem, s);
+  L.stage(CG_STAGE_APPLY, false, s);
+  *L.counter += 5;
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 size_t prop_meta_bytes() { return sizeof(PropMeta); }
 uint64_t stage_bytes() { return kStageBytes; }
 
@@ -2293,8 +2702,11 @@ int persistent_blocks(int which) {
   if (which == 0) {
     cudaFuncSetAttribute(k_check_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_check_scan, kRingWarps * 32, kScanSmem);
-  } else {
+  } else if (which == 1) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_apply, kThreads, 0);
+  } else {
+    cudaFuncSetAttribute(k_prop_waves, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWaveSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_prop_waves, kWRing * 32, kWaveSmem);
   }
   return b;
 }

@@ -39,7 +39,7 @@ struct ArrayEntry {   // NEXT-3 device array (SPEC register_array S:166-168)
 };
 
 struct Layout {
-  uint64_t table, arrays, weight, P, bsum, chunk, meta, resid, dvoff, scratch, marks, flags, leaks, desc_stage,
+  uint64_t table, arrays, weight, P, bsum, chunk, meta, resid, dvoff, scratch, waves, marks, flags, leaks, desc_stage,
       verdict_stage, raw_stage,
       idx_stage, dirty_stage, dir, total;
   uint32_t dir_bits;
@@ -63,7 +63,7 @@ bool valid_config(const cg_config* c) {
   if (c->max_allocs == 0 || c->max_allocs > (1ull << 32)) return false;
   if (c->shadow_format != CG_SHADOW_BYTES && c->shadow_format != CG_SHADOW_2BIT) return false;
   if (c->shadow_format == CG_SHADOW_2BIT && c->dev_vbuf) return false;   // NEXT-1 needs exact host V-bytes
-  if (c->dev_vbuf && (c->dev_vsize == 0 || c->dev_vsize % 16 || (c->shard_size && (c->shard_base != c->host_base ||
+  if (c->dev_vbuf && (c->dev_vsize == 0 || c->dev_vsize % 16 || (uintptr_t)c->dev_vbuf % 16 || (c->shard_size && (c->shard_base != c->host_base ||
                                                               c->shard_size != c->host_size))))
     return false;   // NEXT-1 tracking needs a pool and an unsharded context
   return true;
@@ -89,6 +89,7 @@ Layout layout_of(const cg_config* c) {
   L.resid = take(c->max_descs * sizeof(uint32_t));
   L.dvoff = c->dev_vbuf ? take(c->max_descs * 16) : 0;
   L.scratch = c->dev_vbuf ? take(cgk::stage_bytes()) : 0;
+  L.waves = c->dev_vbuf ? take((c->max_descs + 1) * sizeof(uint32_t)) : 0;   // NEXT-1 wave offsets
   L.marks = take(std::min<uint64_t>(c->max_descs, kMarkRun) * sizeof(cg_mark));
   L.flags = take(256);
   L.leaks = take(c->max_allocs * sizeof(cg_alloc_record));
@@ -189,6 +190,8 @@ struct cg_ctx {
   cudaEvent_t staged = nullptr;
   cudaStream_t copy_stream = nullptr;        // host -> device uploads of cg_check_host
   cudaEvent_t chunk_ev[kHostChunks] = {};
+  bool wave_kernel = true;                   // cg_apply_copies_waves: one cooperative launch (env CG_WAVE_KERNEL=0: per wave)
+  std::vector<uint32_t> h_wstart;            // its wave offsets, rebased, before upload
   uint64_t host_chunks = 2;                   // cg_check_host pipeline (env CG_HOST_CHUNKS / CG_HOST_GEOMETRIC)
   bool host_geometric = true;
   std::string err;
@@ -386,6 +389,7 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
   c->launch.num_sms = prop.multiProcessorCount;
   c->launch.persist_blocks = prop.multiProcessorCount * std::max(cgk::persistent_blocks(1), 1);
   c->launch.scan_blocks = prop.multiProcessorCount * std::max(cgk::persistent_blocks(0), 1);
+  c->launch.wave_blocks = prop.multiProcessorCount * std::max(cgk::persistent_blocks(2), 1);
   c->launch.counter = &c->launches;
   c->prof.mark = &cg_ctx::mark_cb;
   c->prof.self = c;
@@ -399,6 +403,7 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
   cudaEventRecord(c->staged, 0);
   if (const char* hc = getenv("CG_HOST_CHUNKS")) c->host_chunks = std::min<uint64_t>(std::max(atoi(hc), 1), kHostChunks);
   if (const char* hg = getenv("CG_HOST_GEOMETRIC")) c->host_geometric = atoi(hg) != 0;
+  if (const char* wk = getenv("CG_WAVE_KERNEL")) c->wave_kernel = atoi(wk) != 0;
   if (cfg->host_staging) {
     if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
       cg_ctx_destroy(c);
@@ -916,9 +921,31 @@ cg_status cg_apply_copies_waves(cg_ctx* c, const cg_copy_desc* d_descs, const cg
                                 uint32_t n_waves, void* stream) {
   if (!c) return CG_ERR_INVALID_CONTEXT;
   if (n_waves && (!h_wave_start || !h_max_bytes)) return c->fail(CG_ERR_INVALID_VALUE, "null wave arrays");
-  for (uint32_t w = 0; w < n_waves; ++w) {   // in level order, all launches from this loop
+  for (uint32_t w = 0; w < n_waves; ++w)
     if (h_wave_start[w + 1] < h_wave_start[w] || h_wave_start[w + 1] > n)
       return c->fail(CG_ERR_INVALID_VALUE, "wave offsets not increasing or beyond n");
+  if (c->wave_kernel && n_waves && c->cfg.dev_vbuf) {   // every wave in one cooperative launch
+    if (!d_descs || !d_verdicts || !d_index) return c->fail(CG_ERR_INVALID_VALUE, "null descriptor, verdict or index array");
+    if (d_descs != c->last_check || n != c->last_check_n)
+      return c->fail(CG_ERR_INVALID_VALUE, "cg_apply_copies must follow the check of the same descriptors");
+    const uint64_t a = h_wave_start[0], m = h_wave_start[n_waves] - a;
+    if (m) {
+      DeviceGuard g(c->cfg.device);
+      cudaStream_t s = static_cast<cudaStream_t>(stream);
+      c->h_wstart.resize(n_waves + 1);
+      for (uint32_t w = 0; w <= n_waves; ++w) c->h_wstart[w] = (uint32_t)(h_wave_start[w] - a);
+      uint32_t* dw = reinterpret_cast<uint32_t*>(c->ws + c->lay.waves);
+      cudaError_t e = cudaMemcpyAsync(dw, c->h_wstart.data(), (n_waves + 1) * sizeof(uint32_t),
+                                      cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess)
+        e = cgk::propagate_waves(c->launch, d_descs, d_verdicts, d_index + a, m, dw, n_waves, c->sv,
+                                 static_cast<uint8_t*>(c->cfg.dev_vbuf), c->plan(), c->ws + c->lay.scratch,
+                                 reinterpret_cast<uint32_t*>(c->ws + c->lay.flags + 224), s);
+      if (e != cudaSuccess) return c->cuda(e, "propagate waves");
+    }
+    return cg_apply_flush(c, stream);
+  }
+  for (uint32_t w = 0; w < n_waves; ++w) {   // in level order, all launches from this loop
     const cg_status st = cg_apply_copies_subset(c, d_descs, d_verdicts, n, d_index + h_wave_start[w],
                                                 h_wave_start[w + 1] - h_wave_start[w], h_max_bytes[w], stream);
     if (st != CG_OK) return st;

@@ -123,3 +123,39 @@ def test_round_trip_large_waves(cg, seed):
     run_tracking(cg, tr)
     o = oracle.replay_trace(tr, track_device=True)[0]
     assert np.array_equal(o.V[8 << 20:(8 << 20) + n], pat)
+
+
+@pytest.mark.parametrize("wave_kernel", ["0", "1"])
+def test_c2_scaled_tracking_both_wave_paths(cg, monkeypatch, wave_kernel):
+    """cg_apply_copies_waves in one cooperative launch (default) and wave by
+    wave (CG_WAVE_KERNEL=0) give the same, oracle-exact device V-bits"""
+    monkeypatch.setenv("CG_WAVE_KERNEL", wave_kernel)
+    run_tracking(cg, tg.c2_small(n_copies=30000, n_allocs=1500))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_deep_chains_tracking(cg, seed):
+    """many dependency waves: copies ping-pong over few host buffers and
+    allocations, so most copies conflict with an earlier one (R-28)"""
+    rng = np.random.default_rng(seed + 500)
+    H0 = 1 << 20
+    tb = tg.TraceBuilder("chain", H0, 1 << 20)
+    devs = [tb.malloc(1 << 14) for _ in range(4)]
+    tb.mark(H0, 1 << 16, tg.DEFINED)
+    pat = rng.integers(0, 256, 1 << 16, dtype=np.uint8)
+    pat[rng.random(1 << 16) < 0.5] = 0
+    tb.setv(H0, pat.tobytes())
+    tb.mark(H0 + (1 << 17), 1 << 16, tg.UNDEFINED)
+    for _ in range(400):
+        n = int(rng.integers(1, 9000))
+        k = int(rng.integers(0, 3))
+        if k == 0:
+            tb.copy1d(tg.HTOD, devs[rng.integers(4)] + int(rng.integers(0, (1 << 14) - n)),
+                      H0 + int(rng.integers(0, (1 << 16) - n)), n)
+        elif k == 1:
+            tb.copy1d(tg.DTOD, devs[rng.integers(4)] + int(rng.integers(0, (1 << 14) - n)),
+                      devs[rng.integers(4)] + int(rng.integers(0, (1 << 14) - n)), n)
+        else:
+            tb.copy1d(tg.DTOH, H0 + (1 << 17) + int(rng.integers(0, (1 << 16) - n)),
+                      devs[rng.integers(4)] + int(rng.integers(0, (1 << 14) - n)), n)
+    run_tracking(cg, tb.build())
