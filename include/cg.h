@@ -167,7 +167,8 @@ typedef struct {
  *  - max_descs: largest n accepted by one check/apply/mark-batch call.
  *  - max_allocs: allocation-table capacity (live entries plus tombstones).
  *  - host_staging: nonzero reserves device staging in the workspace for
- *    cg_check_copies_host (descriptors + verdicts of max_descs).
+ *    cg_check_copies_host / cg_check_host[_submit] (two slots of descriptors,
+ *    verdicts and dirty lists of max_descs each).
  *  - dev_vbuf / dev_vsize (NEXT-1; SPEC copy_vbits S:81-89):
  *    non-NULL enables device V-bit tracking.  Every registered allocation gets
  *    `size` bytes of device V-bits in this caller-owned pool (bump allocated,
@@ -454,7 +455,8 @@ cg_status cg_batch_disjoint(const cg_copy_desc *h_descs, uint64_t n, int *disjoi
 /* End-to-end entry point with HOST buffers: copies h_descs to the device,
  * runs cg_check_copies (apply = 0), cg_check_copies + cg_apply_dtoh
  * (apply = 1) or cg_check_apply (apply = 2, same precondition) and copies the
- * verdicts back to h_out.  Synchronous.  Requires cfg.host_staging.  Errors: as
+ * verdicts back to h_out.  Synchronous.  Requires cfg.host_staging and staging
+ * slot 0 free (no batch submitted to it and not waited for).  Errors: as
  * cg_check_copies; CG_ERR_NOT_INITIALIZED without host staging. */
 cg_status cg_check_copies_host(cg_ctx *ctx, const cg_copy_desc *h_descs, uint64_t n, cg_verdict *h_out,
                                int apply, void *stream);
@@ -477,6 +479,24 @@ cg_status cg_expand_copy1d(cg_ctx *ctx, const cg_copy1d *d_in, uint64_t n, cg_co
  * without host staging. */
 cg_status cg_check_host(cg_ctx *ctx, const void *h_descs, uint32_t format, uint64_t n, int apply, uint64_t *h_idx,
                         cg_verdict *h_dirty, uint64_t cap, uint64_t *n_dirty, void *stream);
+
+/* The same in two halves, for a stream of batches (double buffering): the
+ * context has two staging slots.  cg_check_host_submit enqueues batch n's
+ * upload (copy stream, waiting only until the slot's previous batch stopped
+ * reading its staging), check (stream) and dirty-verdict compaction into
+ * staging slot `slot` (0 or 1) and returns without waiting, so the next
+ * batch's upload overlaps this batch's kernels.  cg_check_host_wait(slot)
+ * waits for that batch and downloads its dirty verdicts (on a third stream:
+ * kernels of a batch submitted later keep running).  Batches are checked in
+ * submission order on the stream, exactly as consecutive cg_check_host calls.
+ * h_descs (pinned for the upload to be asynchronous) must stay unchanged until
+ * the wait returns.  A slot takes one batch at a time.  Errors: as
+ * cg_check_host; CG_ERR_INVALID_VALUE for a slot > 1, a submit to a slot whose
+ * batch was not waited for, or a wait on a slot with no batch. */
+cg_status cg_check_host_submit(cg_ctx *ctx, const void *h_descs, uint32_t format, uint64_t n, int apply,
+                               uint32_t slot, void *stream);
+cg_status cg_check_host_wait(cg_ctx *ctx, uint32_t slot, uint64_t *h_idx, cg_verdict *h_dirty, uint64_t cap,
+                             uint64_t *n_dirty);
 
 /* Straddler exchange, step 1 (device, asynchronous): the m raw partial
  * verdicts d_raw (CG_SHARD_RAW descriptors, in the same order on every shard)

@@ -100,6 +100,8 @@ def _load() -> ctypes.CDLL:
         "cg_host_query_addressable": (I, [P, U64, U64, P, P]),
         "cg_expand_copy1d": (I, [P, P, U64, P, P]),
         "cg_check_host": (I, [P, P, U32, U64, I, P, P, U64, P, P]),
+        "cg_check_host_submit": (I, [P, P, U32, U64, I, U32, P]),
+        "cg_check_host_wait": (I, [P, U32, P, P, U64, P]),
         "cg_format_verdict": (U64, [P, U32, P, U64]),
         "cg_apply_copies": (I, [P, P, P, U64, P]),
         "cg_device_vbits": (I, [P, U64, U64, P]),
@@ -145,7 +147,7 @@ EXPORTED = ("cg_workspace_size", "cg_ctx_create", "cg_ctx_destroy", "cg_last_err
             "cg_check_copies", "cg_apply_dtoh", "cg_check_copies_host", "cg_leak_sweep", "cg_leak_report",
             "cg_plan_batches", "cg_kernel_launches", "cg_profile_begin", "cg_profile_end", "cg_check_apply",
             "cg_batch_disjoint", "cg_straddler_pack", "cg_straddler_finalize", "cg_compact_dirty", "cg_shard_plan",
-            "cg_host_query_addressable", "cg_expand_copy1d", "cg_check_host", "cg_format_verdict",
+            "cg_host_query_addressable", "cg_expand_copy1d", "cg_check_host", "cg_check_host_submit", "cg_check_host_wait", "cg_format_verdict",
             "cg_format_leak", "cg_apply_copies", "cg_device_vbits", "cg_plan_batches_propagate",
             "cg_host_shadow_read", "cg_apply_copies_subset", "cg_plan_waves", "cg_apply_flush", "cg_apply_copies_waves", "cg_summarize", "cg_format_summary", "cg_array_bytes", "cg_register_array", "cg_free_array", "cg_array_report", "cg_conc_create",
             "cg_conc_destroy", "cg_conc_last_error", "cg_conc_sync", "cg_conc_check", "cg_conc_stamps",
@@ -172,6 +174,8 @@ cg_compact_dirty = _lib.cg_compact_dirty
 cg_host_query_addressable = _lib.cg_host_query_addressable
 cg_expand_copy1d = _lib.cg_expand_copy1d
 cg_check_host = _lib.cg_check_host
+cg_check_host_submit = _lib.cg_check_host_submit
+cg_check_host_wait = _lib.cg_check_host_wait
 cg_format_verdict = _lib.cg_format_verdict
 cg_format_leak = _lib.cg_format_leak
 cg_apply_copies = _lib.cg_apply_copies
@@ -538,6 +542,23 @@ class Checker:
         nd = ctypes.c_uint64(0)
         self._ok(_lib.cg_check_host(self.ctx, descs.ctypes.data, fmt, n, int(apply), idx.ctypes.data,
                                     dirty.ctypes.data, cap, ctypes.byref(nd), _stream_ptr(stream)), "cg_check_host")
+        m = min(nd.value, cap)
+        return nd.value, idx[:m], dirty[:m]
+
+    def check_host_submit(self, descs: np.ndarray, slot: int, apply: int = 1, stream=None):
+        """cg_check_host_submit: enqueue a host batch into staging slot 0/1
+        (descs must stay alive and unchanged until check_host_wait(slot))"""
+        fmt = CG_FMT_1D if descs.dtype == COPY1D_DTYPE else CG_FMT_2D
+        self._ok(_lib.cg_check_host_submit(self.ctx, descs.ctypes.data, fmt, len(descs), int(apply), int(slot),
+                                           _stream_ptr(stream)), "cg_check_host_submit")
+
+    def check_host_wait(self, slot: int, cap: int):
+        """cg_check_host_wait: (n_dirty, idx, dirty verdicts) of the slot's batch"""
+        idx = np.empty(max(cap, 1), np.uint64)
+        dirty = np.empty(max(cap, 1), VERDICT_DTYPE)
+        nd = ctypes.c_uint64(0)
+        self._ok(_lib.cg_check_host_wait(self.ctx, int(slot), idx.ctypes.data, dirty.ctypes.data, cap,
+                                         ctypes.byref(nd)), "cg_check_host_wait")
         m = min(nd.value, cap)
         return nd.value, idx[:m], dirty[:m]
 

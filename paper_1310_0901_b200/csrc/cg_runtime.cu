@@ -27,6 +27,7 @@ constexpr uint64_t kAlign = 256;
 constexpr uint64_t kChunkMin = 32 * 1024;        // t_min of the chunk plans (weight units)
 constexpr uint64_t kMarkRun = 1u << 20;          // marks uploaded per run
 constexpr uint64_t kHostChunks = 5;              // cg_check_host upload / check pipeline depth
+constexpr uint32_t kHostSlots = 2;               // cg_check_host_submit staging slots (double buffering)
 
 uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
@@ -93,11 +94,12 @@ Layout layout_of(const cg_config* c) {
   L.marks = take(std::min<uint64_t>(c->max_descs, kMarkRun) * sizeof(cg_mark));
   L.flags = take(256);
   L.leaks = take(c->max_allocs * sizeof(cg_alloc_record));
-  L.desc_stage = c->host_staging ? take(c->max_descs * sizeof(cg_copy_desc)) : 0;
-  L.verdict_stage = c->host_staging ? take(c->max_descs * sizeof(cg_verdict)) : 0;
-  L.raw_stage = c->host_staging ? take(c->max_descs * sizeof(cg_copy1d)) : 0;
-  L.idx_stage = c->host_staging ? take(c->max_descs * sizeof(uint64_t)) : 0;
-  L.dirty_stage = c->host_staging ? take(c->max_descs * sizeof(cg_verdict)) : 0;
+  // host staging: kHostSlots slots (cg_check_host_submit double-buffers batches)
+  L.desc_stage = c->host_staging ? take(kHostSlots * c->max_descs * sizeof(cg_copy_desc)) : 0;
+  L.verdict_stage = c->host_staging ? take(kHostSlots * c->max_descs * sizeof(cg_verdict)) : 0;
+  L.raw_stage = c->host_staging ? take(kHostSlots * c->max_descs * sizeof(cg_copy1d)) : 0;
+  L.idx_stage = c->host_staging ? take(kHostSlots * c->max_descs * sizeof(uint64_t)) : 0;
+  L.dirty_stage = c->host_staging ? take(kHostSlots * c->max_descs * sizeof(cg_verdict)) : 0;
   L.dir_bits = 0;
   L.dir = 0;
   if (c->shadow_format == CG_SHADOW_SPARSE) {   // directory: >= 2x the secondaries, power of two
@@ -189,7 +191,12 @@ struct cg_ctx {
   cg_mark* h_marks = nullptr;               // kMarkRun
   cudaEvent_t staged = nullptr;
   cudaStream_t copy_stream = nullptr;        // host -> device uploads of cg_check_host
-  cudaEvent_t chunk_ev[kHostChunks] = {};
+  cudaStream_t out_stream = nullptr;         // device -> host dirty-verdict downloads (cg_check_host_wait)
+  cudaEvent_t chunk_ev[kHostSlots][kHostChunks] = {};
+  cudaEvent_t slot_free[kHostSlots] = {};    // the slot's last batch stopped reading its staging
+  cudaEvent_t slot_done[kHostSlots] = {};    // ... and its dirty count is on the host
+  bool slot_busy[kHostSlots] = {};
+  uint32_t* h_count = nullptr;               // pinned, one dirty count per slot
   bool wave_kernel = true;                   // cg_apply_copies_waves: one cooperative launch (env CG_WAVE_KERNEL=0: per wave)
   std::vector<uint32_t> h_wstart;            // its wave offsets, rebased, before upload
   uint64_t host_chunks = 2;                   // cg_check_host pipeline (env CG_HOST_CHUNKS / CG_HOST_GEOMETRIC)
@@ -405,11 +412,19 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
   if (const char* hg = getenv("CG_HOST_GEOMETRIC")) c->host_geometric = atoi(hg) != 0;
   if (const char* wk = getenv("CG_WAVE_KERNEL")) c->wave_kernel = atoi(wk) != 0;
   if (cfg->host_staging) {
-    if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->out_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMallocHost(&c->h_count, kHostSlots * sizeof(uint32_t)) != cudaSuccess) {
       cg_ctx_destroy(c);
       return CG_ERR_CUDA;
     }
-    for (auto& ev : c->chunk_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    for (auto& slot : c->chunk_ev)
+      for (auto& ev : slot) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    for (uint32_t k = 0; k < kHostSlots; ++k) {
+      cudaEventCreateWithFlags(&c->slot_free[k], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&c->slot_done[k], cudaEventDisableTiming);
+      cudaEventRecord(c->slot_free[k], 0);
+    }
   }
   e = cudaMemset(c->ws + lay.flags, 0, 256);   // counters, overflow flag
   if (e == cudaSuccess) e = cgk::fresh_shadow(c->launch, c->sv, 0);
@@ -430,9 +445,18 @@ cg_status cg_ctx_destroy(cg_ctx* c) {
     cudaEventSynchronize(c->staged);
     cudaEventDestroy(c->staged);
   }
-  for (auto& ev : c->chunk_ev)
-    if (ev) cudaEventDestroy(ev);
+  if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+  if (c->out_stream) cudaStreamSynchronize(c->out_stream);
+  for (auto& slot : c->chunk_ev)
+    for (auto& ev : slot)
+      if (ev) cudaEventDestroy(ev);
+  for (uint32_t k = 0; k < kHostSlots; ++k) {
+    if (c->slot_free[k]) cudaEventDestroy(c->slot_free[k]);
+    if (c->slot_done[k]) cudaEventSynchronize(c->slot_done[k]), cudaEventDestroy(c->slot_done[k]);
+  }
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->out_stream) cudaStreamDestroy(c->out_stream);
+  if (c->h_count) cudaFreeHost(c->h_count);
   for (auto& r : c->recs) { c->pool.push_back(r.a); c->pool.push_back(r.b); }
   for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
   if (c->h_table) cudaFreeHost(c->h_table);
@@ -1038,9 +1062,11 @@ cg_status cg_check_copies_host(cg_ctx* c, const cg_copy_desc* h_descs, uint64_t 
   if (n > c->cfg.max_descs) return c->fail(CG_ERR_INVALID_VALUE, "n > max_descs");
   DeviceGuard g(c->cfg.device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c->slot_busy[0]) return c->fail(CG_ERR_INVALID_VALUE, "staging slot 0 holds a submitted batch");
   cg_copy_desc* dd = reinterpret_cast<cg_copy_desc*>(c->ws + c->lay.desc_stage);
   cg_verdict* dv = reinterpret_cast<cg_verdict*>(c->ws + c->lay.verdict_stage);
-  cudaError_t e = cudaMemcpyAsync(dd, h_descs, n * sizeof(cg_copy_desc), cudaMemcpyHostToDevice, s);
+  cudaError_t e = cudaStreamWaitEvent(s, c->slot_free[0], 0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dd, h_descs, n * sizeof(cg_copy_desc), cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return c->cuda(e, "descriptor upload");
   cg_status st = apply == 2 ? cg_check_apply(c, dd, n, dv, stream) : cg_check_copies(c, dd, n, dv, stream);
   if (st != CG_OK) return st;
@@ -1060,43 +1086,55 @@ cg_status cg_expand_copy1d(cg_ctx* c, const cg_copy1d* d_in, uint64_t n, cg_copy
   return c->cuda(cgk::expand_1d(c->launch, d_in, n, d_out, static_cast<cudaStream_t>(stream)), "expand 1d");
 }
 
-cg_status cg_check_host(cg_ctx* c, const void* h_descs, uint32_t format, uint64_t n, int apply, uint64_t* h_idx,
-                        cg_verdict* h_dirty, uint64_t cap, uint64_t* n_dirty, void* stream) {
+static cg_status check_host_submit(cg_ctx* c, const void* h_descs, uint32_t format, uint64_t n, int apply,
+                                   uint32_t slot, void* stream, bool chunked);
+
+cg_status cg_check_host_submit(cg_ctx* c, const void* h_descs, uint32_t format, uint64_t n, int apply, uint32_t slot,
+                               void* stream) {
+  // one chunk: with batches in flight on both slots the whole upload already
+  // runs under the previous batch's kernels
+  return check_host_submit(c, h_descs, format, n, apply, slot, stream, false);
+}
+
+static cg_status check_host_submit(cg_ctx* c, const void* h_descs, uint32_t format, uint64_t n, int apply,
+                                   uint32_t slot, void* stream, bool chunked) {
   if (!c) return CG_ERR_INVALID_CONTEXT;
   if (!c->cfg.host_staging) return c->fail(CG_ERR_NOT_INITIALIZED, "context created without host staging");
-  if (!n_dirty || (cap && (!h_idx || !h_dirty))) return c->fail(CG_ERR_INVALID_VALUE, "null outputs");
-  *n_dirty = 0;
-  if (n == 0) return CG_OK;
-  if (!h_descs || format > CG_FMT_1D || apply < 0 || apply > 2) return c->fail(CG_ERR_INVALID_VALUE, "bad arguments");
+  if (slot >= kHostSlots) return c->fail(CG_ERR_INVALID_VALUE, "slot out of range");
+  if (c->slot_busy[slot]) return c->fail(CG_ERR_INVALID_VALUE, "slot holds a batch not yet waited for");
+  if (n && (!h_descs || format > CG_FMT_1D || apply < 0 || apply > 2))
+    return c->fail(CG_ERR_INVALID_VALUE, "bad arguments");
   if (n > c->cfg.max_descs) return c->fail(CG_ERR_INVALID_VALUE, "n > max_descs");
   DeviceGuard g(c->cfg.device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cg_copy_desc* dd = reinterpret_cast<cg_copy_desc*>(c->ws + c->lay.desc_stage);
-  cg_verdict* dv = reinterpret_cast<cg_verdict*>(c->ws + c->lay.verdict_stage);
-  cg_copy1d* draw = reinterpret_cast<cg_copy1d*>(c->ws + c->lay.raw_stage);
-  uint64_t* didx = reinterpret_cast<uint64_t*>(c->ws + c->lay.idx_stage);
-  cg_verdict* ddirty = reinterpret_cast<cg_verdict*>(c->ws + c->lay.dirty_stage);
-  uint32_t* dcount = reinterpret_cast<uint32_t*>(c->ws + c->lay.flags + 192);
+  const uint64_t md = c->cfg.max_descs;
+  cg_copy_desc* dd = reinterpret_cast<cg_copy_desc*>(c->ws + c->lay.desc_stage) + slot * md;
+  cg_verdict* dv = reinterpret_cast<cg_verdict*>(c->ws + c->lay.verdict_stage) + slot * md;
+  cg_copy1d* draw = reinterpret_cast<cg_copy1d*>(c->ws + c->lay.raw_stage) + slot * md;
+  uint64_t* didx = reinterpret_cast<uint64_t*>(c->ws + c->lay.idx_stage) + slot * md;
+  cg_verdict* ddirty = reinterpret_cast<cg_verdict*>(c->ws + c->lay.dirty_stage) + slot * md;
+  uint32_t* dcount = reinterpret_cast<uint32_t*>(c->ws + c->lay.flags + 192) + slot;
   const size_t esz = format == CG_FMT_1D ? sizeof(cg_copy1d) : sizeof(cg_copy_desc);
   uint8_t* dst = format == CG_FMT_1D ? reinterpret_cast<uint8_t*>(draw) : reinterpret_cast<uint8_t*>(dd);
   // geometric chunks (sizes 1 : 2 : 4 : ...): the first upload is short, and
   // every later chunk's upload (PCIe, ~50 GB/s) finishes while the previous
   // chunk is being checked (the check is slower per descriptor than the upload)
-  const uint64_t nchunks = n >= (1u << 19) ? c->host_chunks : 1;
+  const uint64_t nchunks = chunked && n >= (1u << 19) ? c->host_chunks : 1;
   uint64_t bound[kHostChunks + 1];
   bound[0] = 0;
   for (uint64_t k = 1; k <= nchunks; ++k)
     bound[k] = k == nchunks ? n
                : c->host_geometric ? n * ((1ull << k) - 1) / ((1ull << nchunks) - 1) : n * k / nchunks;
-  // uploads: all chunks on the copy stream (it waits for earlier work on s first)
-  cudaError_t e = cudaEventRecord(c->chunk_ev[0], s);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(c->copy_stream, c->chunk_ev[0], 0);
+  // uploads on the copy stream, after the slot's previous batch stopped reading
+  // its staging (not after all work on s: the previous batch of the other slot
+  // is still being checked while this one uploads)
+  cudaError_t e = cudaStreamWaitEvent(c->copy_stream, c->slot_free[slot], 0);
   for (uint64_t k = 0; k < nchunks && e == cudaSuccess; ++k) {
     const uint64_t a = bound[k], b = bound[k + 1];
     if (a >= b) continue;
     e = cudaMemcpyAsync(dst + a * esz, static_cast<const uint8_t*>(h_descs) + a * esz, (b - a) * esz,
                         cudaMemcpyHostToDevice, c->copy_stream);
-    if (e == cudaSuccess) e = cudaEventRecord(c->chunk_ev[k], c->copy_stream);
+    if (e == cudaSuccess) e = cudaEventRecord(c->chunk_ev[slot][k], c->copy_stream);
   }
   if (e != cudaSuccess) return c->cuda(e, "descriptor upload");
   e = cudaMemsetAsync(dcount, 0, sizeof(uint32_t), s);
@@ -1104,7 +1142,7 @@ cg_status cg_check_host(cg_ctx* c, const void* h_descs, uint32_t format, uint64_
   for (uint64_t k = 0; k < nchunks; ++k) {
     const uint64_t a = bound[k], b = bound[k + 1];
     if (a >= b) continue;
-    e = cudaStreamWaitEvent(s, c->chunk_ev[k], 0);
+    e = cudaStreamWaitEvent(s, c->chunk_ev[slot][k], 0);
     if (e == cudaSuccess && format == CG_FMT_1D) e = cgk::expand_1d(c->launch, draw + a, b - a, dd + a, s);
     if (e != cudaSuccess) return c->cuda(e, "chunk wait / expand");
     cg_status st = apply == 2 ? cg_check_apply(c, dd + a, b - a, dv + a, stream)
@@ -1114,19 +1152,50 @@ cg_status cg_check_host(cg_ctx* c, const void* h_descs, uint32_t format, uint64_
     e = cgk::compact_dirty(c->launch, dv + a, b - a, didx, ddirty, dcount, a, false, s);
     if (e != cudaSuccess) return c->cuda(e, "compact");
   }
-  uint32_t cnt = 0;
-  e = cudaMemcpyAsync(&cnt, dcount, sizeof cnt, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  e = cudaEventRecord(c->slot_free[slot], s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(c->h_count + slot, dcount, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaEventRecord(c->slot_done[slot], s);
   if (e != cudaSuccess) return c->cuda(e, "count download");
+  c->slot_busy[slot] = true;
+  return CG_OK;
+}
+
+cg_status cg_check_host_wait(cg_ctx* c, uint32_t slot, uint64_t* h_idx, cg_verdict* h_dirty, uint64_t cap,
+                             uint64_t* n_dirty) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (slot >= kHostSlots || !c->slot_busy[slot]) return c->fail(CG_ERR_INVALID_VALUE, "no batch submitted to slot");
+  if (!n_dirty || (cap && (!h_idx || !h_dirty))) return c->fail(CG_ERR_INVALID_VALUE, "null outputs");
+  DeviceGuard g(c->cfg.device);
+  c->slot_busy[slot] = false;
+  cudaError_t e = cudaEventSynchronize(c->slot_done[slot]);
+  if (e != cudaSuccess) return c->cuda(e, "batch wait");
+  const uint64_t cnt = c->h_count[slot];
   *n_dirty = cnt;
-  const uint64_t m = std::min<uint64_t>(cnt, cap);
-  if (m) {
-    e = cudaMemcpyAsync(h_idx, didx, m * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(h_dirty, ddirty, m * sizeof(cg_verdict), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  const uint64_t m = std::min<uint64_t>(cnt, cap), md = c->cfg.max_descs;
+  if (m) {   // on the result stream: the next batch's kernels on the check stream keep running
+    const uint64_t* didx = reinterpret_cast<const uint64_t*>(c->ws + c->lay.idx_stage) + slot * md;
+    const cg_verdict* ddirty = reinterpret_cast<const cg_verdict*>(c->ws + c->lay.dirty_stage) + slot * md;
+    e = cudaMemcpyAsync(h_idx, didx, m * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->out_stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(h_dirty, ddirty, m * sizeof(cg_verdict), cudaMemcpyDeviceToHost, c->out_stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->out_stream);
     if (e != cudaSuccess) return c->cuda(e, "dirty download");
   }
   return CG_OK;
+}
+
+cg_status cg_check_host(cg_ctx* c, const void* h_descs, uint32_t format, uint64_t n, int apply, uint64_t* h_idx,
+                        cg_verdict* h_dirty, uint64_t cap, uint64_t* n_dirty, void* stream) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (!c->cfg.host_staging) return c->fail(CG_ERR_NOT_INITIALIZED, "context created without host staging");
+  if (!n_dirty || (cap && (!h_idx || !h_dirty))) return c->fail(CG_ERR_INVALID_VALUE, "null outputs");
+  *n_dirty = 0;
+  if (n == 0) return CG_OK;
+  if (!h_descs || format > CG_FMT_1D || apply < 0 || apply > 2) return c->fail(CG_ERR_INVALID_VALUE, "bad arguments");
+  const uint32_t slot = c->slot_busy[0] ? 1u : 0u;
+  cg_status st = check_host_submit(c, h_descs, format, n, apply, slot, stream, true);
+  if (st != CG_OK) return st;
+  return cg_check_host_wait(c, slot, h_idx, h_dirty, cap, n_dirty);
 }
 
 cg_status cg_straddler_pack(cg_ctx* c, const cg_verdict* d_raw, uint64_t m, uint64_t* d_mins, uint64_t* d_sums,

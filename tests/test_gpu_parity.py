@@ -252,6 +252,50 @@ def test_check_host_compact_chunked(cg, fmt):
     chk.close()
 
 
+@pytest.mark.parametrize("parts", [2, 5])
+def test_check_host_submit_pipelined(cg, parts):
+    """cg_check_host_submit / _wait: the batch cut into consecutive parts,
+    part k+1 submitted to the other staging slot before part k is waited
+    for; the dense verdicts and the final shadow equal the oracle's
+    sequential replay.  Misuse of a slot is an invalid call."""
+    from paper_1310_0901_b200.replay import events_to_descs
+    tr = tg.c2_small(n_copies=300000, n_allocs=2000)
+    o, ov, _, _ = oracle.replay_trace(tr)
+    chk = new_checker(cg, tr, host_staging=True)
+    ev = tr.events
+    _, st = cg.replay_events(chk, ev[ev["op"] != tg.OP_COPY], tr.blob)
+    assert not st.any()
+    descs = events_to_descs(ev[ev["op"] == tg.OP_COPY])
+    d1 = np.zeros(len(descs), cg.COPY1D_DTYPE)
+    for f in ("kind", "seq", "dst", "src"):
+        d1[f] = descs[f]
+    d1["bytes"] = descs["width"]
+    cuts = np.linspace(0, len(d1), parts + 1).astype(np.int64)
+    pieces = [d1[a:b] for a, b in zip(cuts[:-1], cuts[1:])]
+    dense = np.zeros(len(descs), cg.VERDICT_DTYPE)
+    dense["first_unaddr"] = cg.CG_NONE
+    dense["first_undef"] = cg.CG_NONE
+    total = 0
+    chk.check_host_submit(pieces[0], 0, apply=2)
+    with pytest.raises(cg.CgError):
+        chk.check_host_submit(pieces[0], 0, apply=2)   # slot 0 is busy
+    with pytest.raises(cg.CgError):
+        chk.check_host_wait(1, 16)                     # nothing submitted to slot 1
+    for k in range(parts):
+        if k + 1 < parts:
+            chk.check_host_submit(pieces[k + 1], (k + 1) % 2, apply=2)
+        nd, idx, dirty = chk.check_host_wait(k % 2, len(pieces[k]))
+        dense[idx.astype(np.int64) + cuts[k]] = dirty
+        total += nd
+    with pytest.raises(cg.CgError):
+        chk.check_host_submit(pieces[0], 2, apply=2)   # no slot 2
+    assert total == int(np.count_nonzero(ov["flags"]))
+    assert_verdicts_equal(dense, ov, "check_host_submit")
+    A, V = chk.shadow()
+    assert np.array_equal(V, o.V) and np.array_equal(A, o.A)
+    chk.close()
+
+
 def test_unknown_op_status(cg):
     """an unknown event op is an invalid call on both sides (oracle status 1)"""
     tr = tg.random_tiny(5)
