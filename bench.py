@@ -442,8 +442,10 @@ def run_ours(args, rank, world, device):
         # of every error-free copy
         check_roof, launches_apply = roof, max(apply_n / max(args.steps, 1), 1.0)
         ach = apply_b / (apply_ms / max(args.steps, 1) * 1e-3) / 1e9
+        wj = os.path.join(ROOT, "profiles", f"ncu_{args.config}_track_prop_waves.json")
+        wtraffic = json.load(open(wj)).get("dram_bytes_per_launch") if os.path.exists(wj) else None
         roof = {"bound": "hbm", "kernel": "k_prop_waves", "achieved": ach, "peak": peak,
-                "peak_source": peak_kind, "unit": "GB/s", "frac": ach / peak, "traffic": None,
+                "peak_source": peak_kind, "unit": "GB/s", "frac": ach / peak, "traffic": wtraffic,
                 "algorithmic_bytes_per_launch": apply_b / launches_apply,
                 "avg_launch_ms": apply_ms / max(apply_n, 1), "share_of_step": apply_ms / ms if ms > 0 else None}
     res = {
