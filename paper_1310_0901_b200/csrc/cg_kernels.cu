@@ -44,6 +44,16 @@ namespace {
 constexpr int kThreads = 256;
 constexpr unsigned kFull = 0xffffffffu;
 
+// Programmatic dependent launch: every kernel waits for its stream
+// predecessor's completion (griddepcontrol.wait: all its writes visible) and
+// then lets its own successor launch, so launch latency and block scheduling
+// of back-to-back kernels overlap the previous kernel's tail.  A no-op for
+// kernels launched without the PDL attribute.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---------------------------------------------------------------------------
 // small device helpers
 // ---------------------------------------------------------------------------
@@ -190,9 +200,33 @@ __device__ __forceinline__ bool table_lookup(const Table& t, const uint64_t* s_s
   }
   uint64_t a = (uint64_t)lo * t.stride;
   uint64_t b = umin64(a + t.stride, t.n);
-  while (b - a > 1) {
-    const uint64_t mid = (a + b) >> 1;
-    if (__ldg(t.base + mid) <= start) a = mid; else b = mid;
+  if (t.stride == 32) {
+    // two independent-load rounds instead of five dependent ones: the bucket's
+    // 8 every-4th bases (64 B), then the 4 bases of the chosen quarter (32 B);
+    // each picks the last entry <= start (the first always is)
+    const uint4* q = reinterpret_cast<const uint4*>(t.l2 + a / 4);
+    uint32_t c2 = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint4 v = __ldg(q + k);
+      c2 += (a + 8 * k < b && (((uint64_t)v.y << 32) | v.x) <= start) +
+            (a + 8 * k + 4 < b && (((uint64_t)v.w << 32) | v.z) <= start);
+    }
+    const uint64_t a1 = a + 4 * (c2 - 1);
+    const uint4* r = reinterpret_cast<const uint4*>(t.base + a1);
+    uint32_t c1 = 0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const uint4 v = __ldg(r + k);
+      c1 += (a1 + 2 * k < b && (((uint64_t)v.y << 32) | v.x) <= start) +
+            (a1 + 2 * k + 1 < b && (((uint64_t)v.w << 32) | v.z) <= start);
+    }
+    a = a1 + c1 - 1;
+  } else {
+    while (b - a > 1) {
+      const uint64_t mid = (a + b) >> 1;
+      if (__ldg(t.base + mid) <= start) a = mid; else b = mid;
+    }
   }
   for (int64_t j = (int64_t)a; j >= 0; --j) {
     const uint64_t pm = __ldg(t.pmax + j), e = __ldg(t.end + j), as = __ldg(t.aseq + j), fs = __ldg(t.fseq + j);
@@ -245,7 +279,12 @@ __global__ void __launch_bounds__(kThreads) k_check_prep(const cg_copy_desc* __r
                                                          uint64_t n, Table t, cg_verdict* __restrict__ out,
                                                          uint64_t* __restrict__ weight,
                                                          ScanMeta* __restrict__ meta,
-                                                         uint64_t* __restrict__ dvoff, int two_bit) {
+                                                         uint64_t* __restrict__ dvoff, int two_bit,
+                                                         uint32_t* __restrict__ counter) {
+  pdl_entry();
+  // the scan's group counter, (apply count), residual count: reset here
+  // instead of by a memset node, which would break the PDL chain
+  if (blockIdx.x == 0 && threadIdx.x < 3) counter[threadIdx.x] = 0;
   extern __shared__ uint64_t s_split[];
   load_splitters(t, s_split);
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -365,6 +404,7 @@ __device__ __forceinline__ uint64_t eff_n(uint64_t n, const uint32_t* n_dev) {
 __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint64_t* __restrict__ in, uint64_t n,
                                                               uint64_t* __restrict__ bsum,
                                                               const uint32_t* __restrict__ n_dev) {
+  pdl_entry();
   __shared__ uint64_t s_warp[33];
   n = eff_n(n, n_dev);
   const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
@@ -383,6 +423,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint64_t* __
 // single block: exclusive scan of bsum[0..nb) in place; bsum[nb] = out[n] = total
 __global__ void __launch_bounds__(1024) k_scan_top(uint64_t* __restrict__ bsum, uint64_t n,
                                                    uint64_t* __restrict__ out, const uint32_t* __restrict__ n_dev) {
+  pdl_entry();
   __shared__ uint64_t s_warp[33];
   n = eff_n(n, n_dev);
   const uint64_t nb = (n + kScanTile - 1) / kScanTile;
@@ -405,6 +446,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint64_t* __re
                                                             const uint64_t* __restrict__ bsum,
                                                             uint64_t* __restrict__ out,
                                                             const uint32_t* __restrict__ n_dev) {
+  pdl_entry();
   __shared__ uint64_t s_items[kScanTile];
   __shared__ uint64_t s_warp[33];
   n = eff_n(n, n_dev);
@@ -458,6 +500,7 @@ __device__ __forceinline__ ChunkGeom chunk_geom(const uint64_t* P, uint64_t n, u
 __global__ void __launch_bounds__(kThreads) k_plan(const uint64_t* __restrict__ P, uint64_t n, uint64_t t_min,
                                                    uint64_t max_chunks, uint32_t* __restrict__ chunk_first,
                                                    const uint32_t* __restrict__ n_dev) {
+  pdl_entry();
   n = eff_n(n, n_dev);
   const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
   for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < g.nchunks;
@@ -1169,6 +1212,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
     const uint32_t* __restrict__ chunk_first, uint32_t* counter, uint64_t t_min, uint64_t max_chunks,
     ShadowView sv, cg_verdict* __restrict__ out, uint32_t err_mask, int fuse, uint32_t* __restrict__ resid,
     uint32_t* __restrict__ resid_n) {
+  pdl_entry();
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpRing& ring = reinterpret_cast<WarpRing*>(smem)[wid];
@@ -1277,6 +1321,7 @@ __global__ void __launch_bounds__(kThreads) k_finalize_split(uint64_t n, const u
                                                              const ScanMeta* __restrict__ meta, int fuse,
                                                              uint32_t* __restrict__ resid,
                                                              uint32_t* __restrict__ resid_n) {
+  pdl_entry();
   const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
   for (uint64_t d = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; d < n;
        d += (uint64_t)gridDim.x * blockDim.x) {
@@ -1332,6 +1377,7 @@ __global__ void __launch_bounds__(kThreads) k_apply_prep(const cg_copy_desc* __r
                                                          const cg_verdict* __restrict__ verd, uint64_t n,
                                                          uint64_t* __restrict__ weight, ScanMeta* __restrict__ meta,
                                                          uint32_t* __restrict__ count) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   for (uint64_t b0 = (uint64_t)blockIdx.x * blockDim.x; b0 < n; b0 += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t i = b0 + threadIdx.x;
@@ -1372,7 +1418,10 @@ __global__ void __launch_bounds__(kThreads) k_apply_list_prep(const cg_copy_desc
                                                               const uint32_t* __restrict__ list,
                                                               const uint32_t* __restrict__ count,
                                                               uint64_t* __restrict__ weight,
-                                                              ScanMeta* __restrict__ meta) {
+                                                              ScanMeta* __restrict__ meta,
+                                                              uint32_t* __restrict__ group_counter) {
+  pdl_entry();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *group_counter = 0;   // k_apply's (no memset node)
   const uint64_t m = *count;
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += (uint64_t)gridDim.x * blockDim.x) {
     const cg_copy_desc d = descs[list[k]];
@@ -1428,6 +1477,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(const ScanMeta* __restrict__
                                                     const uint32_t* __restrict__ chunk_first, uint32_t* counter,
                                                     uint64_t t_min, uint64_t max_chunks, ShadowView sv,
                                                     const uint32_t* __restrict__ n_dev) {
+  pdl_entry();
   n = eff_n(n, n_dev);
   __shared__ __align__(128) uint8_t zeros[kZeroPage];
   for (uint32_t i = threadIdx.x; i < kZeroPage / 16; i += blockDim.x)
@@ -1489,18 +1539,17 @@ __global__ void __launch_bounds__(kThreads) k_apply(const ScanMeta* __restrict__
         } else {
           const uint64_t x0 = __shfl_sync(kFull, m.hstart, src), pitch = __shfl_sync(kFull, m.hpitch, src);
           const uint64_t W = __shfl_sync(kFull, m.W, src);
-          uint64_t o = __shfl_sync(kFull, lo, src);
-          const uint64_t h = __shfl_sync(kFull, hi, src);
-          uint64_t r = o / W, c = o - r * W;
-          while (o < h) {
-            const uint64_t len = umin64(W - c, h - o);
+          const uint64_t o = __shfl_sync(kFull, lo, src), h = __shfl_sync(kFull, hi, src);
+          uint64_t oo = o, r = o / W, c = o - r * W;
+          while (oo < h) {   // row segments (R-11), each with the whole warp
+            const uint64_t len = umin64(W - c, h - oo);
             const uint64_t x = x0 + r * pitch + c;
             const uint64_t y0 = umax64(x, sv.sb), y1 = umin64(x + len, sv.se);
             if (y0 < y1) {
               if (sv.two_bit) fill2_any<true>(sv, y0 - sv.sb, y1 - sv.sb, 0xAAAAAAAAu);
               else warp_zero(sv.V, y0 - sv.sb, y1 - sv.sb, zeros);
             }
-            o += len;
+            oo += len;
             ++r;
             c = 0;
           }
@@ -1551,6 +1600,7 @@ __global__ void __launch_bounds__(kThreads) k_prop_prep(const cg_copy_desc* __re
                                                         uint64_t* __restrict__ weight, PropMeta* __restrict__ pm,
                                                         uint32_t* __restrict__ count, uint32_t* __restrict__ mm,
                                                         uint32_t* __restrict__ mm_count) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   for (uint64_t b0 = (uint64_t)blockIdx.x * blockDim.x; b0 < n; b0 += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t k = b0 + threadIdx.x;
@@ -1660,6 +1710,7 @@ __global__ void __launch_bounds__(kThreads) k_propagate(const PropMeta* __restri
                                                         const uint32_t* __restrict__ chunk_first, uint32_t* counter,
                                                         uint64_t t_min, uint64_t max_chunks, uint8_t* V,
                                                         uint8_t* pool, const uint32_t* __restrict__ n_dev) {
+  pdl_entry();
   n = eff_n(n, n_dev);
   const ChunkGeom geo = chunk_geom(P, n, t_min, max_chunks);
   const int lane = threadIdx.x & 31;
@@ -1763,6 +1814,7 @@ __global__ void __launch_bounds__(kThreads) k_prop_direct_warp(const cg_copy_des
                                                                const uint64_t* __restrict__ dvoff, uint64_t sb,
                                                                uint8_t* V, uint8_t* pool, uint32_t* __restrict__ mm,
                                                                uint32_t* __restrict__ mm_count) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t k = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < m; k += nw) {
@@ -1787,6 +1839,7 @@ __global__ void __launch_bounds__(kThreads) k_prop_direct(const cg_copy_desc* __
                                                           const uint64_t* __restrict__ dvoff, uint64_t sb, uint8_t* V,
                                                           uint8_t* pool, uint32_t* __restrict__ mm,
                                                           uint32_t* __restrict__ mm_count) {
+  pdl_entry();
   const uint64_t k = blockIdx.x;
   if (k >= m) return;
   const uint32_t i = index[k];
@@ -1874,6 +1927,7 @@ __global__ void __launch_bounds__(kThreads) k_memmove(const cg_copy_desc* __rest
                                                       const uint32_t* __restrict__ mm,
                                                       const uint32_t* __restrict__ mm_count, uint8_t* pool,
                                                       uint8_t* scratch, uint32_t* overflow) {
+  pdl_entry();
   const uint32_t cnt = *mm_count;
   for (uint32_t k = 0; k < cnt; ++k) {
     const uint32_t i = mm[k];
@@ -1907,6 +1961,7 @@ __global__ void __launch_bounds__(kThreads) k_wave_prep(const cg_copy_desc* __re
                                                         const uint64_t* __restrict__ dvoff, uint64_t sb,
                                                         uint64_t* __restrict__ weight, PropMeta* __restrict__ pm,
                                                         uint32_t* __restrict__ mm, uint32_t* __restrict__ mm_count) {
+  pdl_entry();
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t i = index[k];
     uint64_t w = 0;
@@ -2169,6 +2224,7 @@ __global__ void __launch_bounds__(kWRing * 32) k_prop_waves(const cg_copy_desc* 
                                                             const uint32_t* __restrict__ mm,
                                                             const uint32_t* __restrict__ mm_count, uint8_t* scratch,
                                                             uint32_t* overflow) {
+  pdl_entry();
   extern __shared__ __align__(128) uint8_t smem[];
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -2234,6 +2290,7 @@ __global__ void __launch_bounds__(kWRing * 32) k_prop_waves(const cg_copy_desc* 
 // plumbing: fresh shadow, marks, set_vbits check
 // ---------------------------------------------------------------------------
 __global__ void k_fill(uint4* __restrict__ p, uint64_t n16, uint32_t word) {
+  pdl_entry();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16;
        i += (uint64_t)gridDim.x * blockDim.x)
     stg_val16(p + i, word);
@@ -2241,6 +2298,7 @@ __global__ void k_fill(uint4* __restrict__ p, uint64_t n16, uint32_t word) {
 
 __global__ void __launch_bounds__(kThreads) k_mark_prep(const cg_mark* __restrict__ marks, uint64_t n,
                                                         uint64_t* __restrict__ weight) {
+  pdl_entry();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
     weight[i] = marks[i].len ? marks[i].len + kApplyItemCost : 0;
@@ -2264,6 +2322,7 @@ __global__ void __launch_bounds__(kThreads) k_mark(const cg_mark* __restrict__ m
                                                    const uint64_t* __restrict__ P,
                                                    const uint32_t* __restrict__ chunk_first, uint64_t t_min,
                                                    uint64_t max_chunks, ShadowView sv) {
+  pdl_entry();
   const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -2294,6 +2353,7 @@ __global__ void __launch_bounds__(kThreads) k_mark(const cg_mark* __restrict__ m
 }
 
 __global__ void k_setv_check(ShadowView sv, uint64_t addr, uint64_t len, uint32_t* __restrict__ flag) {
+  pdl_entry();
   const uint64_t y0 = umax64(addr, sv.sb), y1 = umin64(addr + len, sv.se);
   for (uint64_t q = y0 - sv.sb + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < y1 - sv.sb;
        q += (uint64_t)gridDim.x * blockDim.x) {
@@ -2317,6 +2377,7 @@ __global__ void k_setv_check(ShadowView sv, uint64_t addr, uint64_t len, uint32_
 // ---------------------------------------------------------------------------
 __global__ void k_summary(const cg_verdict* __restrict__ v, uint64_t n, uint32_t warn_mask,
                           unsigned long long* __restrict__ counts) {
+  pdl_entry();
   uint64_t e = 0, w = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t f = v[i].flags;
@@ -2341,6 +2402,7 @@ __global__ void k_summary(const cg_verdict* __restrict__ v, uint64_t n, uint32_t
 // only the owner adds device flags, so MAX = OR here).
 __global__ void k_straddler_pack(const cg_verdict* __restrict__ v, uint64_t m, uint64_t* __restrict__ mins,
                                  uint64_t* __restrict__ sums, uint32_t* __restrict__ maxs) {
+  pdl_entry();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const cg_verdict x = v[i];
@@ -2359,6 +2421,7 @@ __global__ void k_straddler_pack(const cg_verdict* __restrict__ v, uint64_t m, u
 __global__ void k_straddler_finalize(const uint64_t* __restrict__ mins, const uint64_t* __restrict__ sums,
                                      const uint32_t* __restrict__ maxs, uint64_t m, cg_verdict* __restrict__ v,
                                      uint32_t err_mask) {
+  pdl_entry();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
        i += (uint64_t)gridDim.x * blockDim.x) {
     cg_verdict x;
@@ -2376,6 +2439,7 @@ __global__ void k_straddler_finalize(const uint64_t* __restrict__ mins, const ui
 }
 
 __global__ void k_expand_1d(const cg_copy1d* __restrict__ in, uint64_t n, cg_copy_desc* __restrict__ out) {
+  pdl_entry();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const cg_copy1d a = in[i];
@@ -2399,6 +2463,7 @@ __global__ void k_expand_1d(const cg_copy1d* __restrict__ in, uint64_t n, cg_cop
 // gather to the root; clean verdicts are canonical and are not sent
 __global__ void k_compact_dirty(const cg_verdict* __restrict__ v, uint64_t n, uint64_t* __restrict__ idx,
                                 cg_verdict* __restrict__ dirty, uint32_t* __restrict__ count, uint64_t idx_base) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   for (uint64_t b0 = (uint64_t)blockIdx.x * blockDim.x; b0 < n; b0 += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t i = b0 + threadIdx.x;
@@ -2422,6 +2487,7 @@ __global__ void k_compact_dirty(const cg_verdict* __restrict__ v, uint64_t n, ui
 // a8: leak sweep
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) k_live(Table t, uint64_t* __restrict__ weight) {
+  pdl_entry();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < t.n;
        i += (uint64_t)gridDim.x * blockDim.x)
     weight[i] = t.fseq[i] == kInf ? 1 : 0;
@@ -2430,6 +2496,7 @@ __global__ void __launch_bounds__(kThreads) k_live(Table t, uint64_t* __restrict
 __global__ void __launch_bounds__(kThreads) k_leak_scatter(Table t, const uint64_t* __restrict__ P,
                                                            cg_alloc_record* __restrict__ out, uint64_t cap,
                                                            uint64_t* __restrict__ count) {
+  pdl_entry();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < t.n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     if (t.fseq[i] == kInf && P[i] < cap) {
@@ -2451,16 +2518,32 @@ inline int blocks_for(uint64_t n, int threads, int cap) {
 
 }  // namespace
 
+// kernel launch with the programmatic-stream-serialization attribute (PDL)
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 uint64_t scan_blocks(uint64_t n) { return (n + kScanTile - 1) / kScanTile; }
 
 // prefix sum of p.weight[0..n) into p.P[0..n], then the chunk plan
 static cudaError_t plan(const Launch& L, uint64_t n, const Plan& p, cudaStream_t s,
                         const uint32_t* n_dev = nullptr) {
   const uint64_t nb = std::max<uint64_t>(scan_blocks(n), 1);
-  k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, n, p.bsum, n_dev);
-  k_scan_top<<<1, 1024, 0, s>>>(p.bsum, n, p.P, n_dev);
-  k_scan_down<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, n, p.bsum, p.P, n_dev);
-  k_plan<<<L.num_sms * 4, kThreads, 0, s>>>(p.P, n, p.t_min, p.max_chunks, p.chunk_first, n_dev);
+  launch_pdl(k_scan_reduce, (unsigned)nb, kScanThreads, 0, s, p.weight, n, p.bsum, n_dev);
+  launch_pdl(k_scan_top, 1, 1024, 0, s, p.bsum, n, p.P, n_dev);
+  launch_pdl(k_scan_down, (unsigned)nb, kScanThreads, 0, s, p.weight, n, p.bsum, p.P, n_dev);
+  launch_pdl(k_plan, L.num_sms * 4, kThreads, 0, s, p.P, n, p.t_min, p.max_chunks, p.chunk_first, n_dev);
   *L.counter += 4;
   return cudaGetLastError();
 }
@@ -2471,22 +2554,21 @@ cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_
   const size_t smem = ((size_t)t.nsplit + 1) * sizeof(uint64_t);
   ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
   L.stage(CG_STAGE_CHECK_PREP, true, s);
-  k_check_prep<<<blocks_for(n, kThreads, L.num_sms * 4), kThreads, smem, s>>>(d, n, t, out, p.weight, meta,
-                                                                              p.dvoff, (int)sv.two_bit);
+  launch_pdl(k_check_prep, blocks_for(n, kThreads, L.num_sms * 4), kThreads, smem, s, d, n, t, out, p.weight, meta,
+                                                                              p.dvoff, (int)sv.two_bit, p.counter);
   *L.counter += 1;
   L.stage(CG_STAGE_CHECK_PREP, false, s);
   L.stage(CG_STAGE_CHECK_PLAN, true, s);
   cudaError_t e = plan(L, n, p, s);
   if (e != cudaSuccess) return e;
   L.stage(CG_STAGE_CHECK_PLAN, false, s);
-  cudaMemsetAsync(p.counter, 0, 3 * sizeof(uint32_t), s);   // group counter, (apply), residual count
   L.stage(CG_STAGE_CHECK_SCAN, true, s);
-  k_check_scan<<<L.scan_blocks, kRingWarps * 32, kScanSmem, s>>>(meta, n, p.P, p.chunk_first, p.counter,
+  launch_pdl(k_check_scan, L.scan_blocks, kRingWarps * 32, kScanSmem, s, meta, n, p.P, p.chunk_first, p.counter,
                                                                  p.t_min, p.max_chunks, sv, out, err_mask,
                                                                  fuse ? 1 : 0, p.resid, p.counter + 2);
   L.stage(CG_STAGE_CHECK_SCAN, false, s);
   L.stage(CG_STAGE_CHECK_FINAL, true, s);
-  k_finalize_split<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(
+  launch_pdl(k_finalize_split, blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s, 
       n, p.P, p.t_min, p.max_chunks, out, err_mask, meta, fuse ? 1 : 0, p.resid, p.counter + 2);
   L.stage(CG_STAGE_CHECK_FINAL, false, s);
   *L.counter += 2;
@@ -2500,11 +2582,11 @@ cudaError_t apply_dtoh(const Launch& L, const cg_copy_desc* d, const cg_verdict*
   const uint32_t* n_dev = after_fused ? p.counter + 2 : nullptr;   // residual list count
   L.stage(CG_STAGE_APPLY_PREP, true, s);
   if (after_fused) {
-    k_apply_list_prep<<<L.num_sms * 2, kThreads, 0, s>>>(d, p.resid, n_dev, p.weight, meta);
+    launch_pdl(k_apply_list_prep, L.num_sms * 2, kThreads, 0, s, d, p.resid, n_dev, p.weight, meta, p.counter);
   } else {
     cudaMemsetAsync(p.weight, 0, n * sizeof(uint64_t), s);
     cudaMemsetAsync(p.counter + 1, 0, sizeof(uint32_t), s);
-    k_apply_prep<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(d, v, n, p.weight, meta,
+    launch_pdl(k_apply_prep, blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s, d, v, n, p.weight, meta,
                                                                              p.counter + 1);
   }
   *L.counter += 1;
@@ -2514,8 +2596,8 @@ cudaError_t apply_dtoh(const Launch& L, const cg_copy_desc* d, const cg_verdict*
   if (e != cudaSuccess) return e;
   L.stage(CG_STAGE_APPLY_PLAN, false, s);
   L.stage(CG_STAGE_APPLY, true, s);
-  cudaMemsetAsync(p.counter, 0, sizeof(uint32_t), s);
-  k_apply<<<L.persist_blocks, kThreads, 0, s>>>(meta, n, p.P, p.chunk_first, p.counter, p.t_min, p.max_chunks, sv,
+  if (!after_fused) cudaMemsetAsync(p.counter, 0, sizeof(uint32_t), s);
+  launch_pdl(k_apply, L.persist_blocks, kThreads, 0, s, meta, n, p.P, p.chunk_first, p.counter, p.t_min, p.max_chunks, sv,
                                                 n_dev);
   L.stage(CG_STAGE_APPLY, false, s);
   *L.counter += 1;
@@ -2525,11 +2607,11 @@ cudaError_t apply_dtoh(const Launch& L, const cg_copy_desc* d, const cg_verdict*
 cudaError_t mark_batch(const Launch& L, const cg_mark* d_marks, uint64_t n, const ShadowView& sv, const Plan& p,
                        cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  k_mark_prep<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(d_marks, n, p.weight);
+  launch_pdl(k_mark_prep, blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s, d_marks, n, p.weight);
   *L.counter += 1;
   cudaError_t e = plan(L, n, p, s);
   if (e != cudaSuccess) return e;
-  k_mark<<<L.persist_blocks, kThreads, 0, s>>>(d_marks, n, p.P, p.chunk_first, p.t_min, p.max_chunks, sv);
+  launch_pdl(k_mark, L.persist_blocks, kThreads, 0, s, d_marks, n, p.P, p.chunk_first, p.t_min, p.max_chunks, sv);
   *L.counter += 1;
   return cudaGetLastError();
 }
@@ -2538,20 +2620,20 @@ cudaError_t summarize(const cg_verdict* v, uint64_t n, uint32_t warn_mask, unsig
                       cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(d_counts, 0, 2 * sizeof(unsigned long long), s);
   if (e != cudaSuccess || n == 0) return e;
-  k_summary<<<(unsigned)std::min<uint64_t>((n + kThreads - 1) / kThreads, 148 * 8), kThreads, 0, s>>>(v, n, warn_mask,
+  launch_pdl(k_summary, (unsigned)std::min<uint64_t>((n + kThreads - 1) / kThreads, 148 * 8), kThreads, 0, s, v, n, warn_mask,
                                                                                                d_counts);
   return cudaGetLastError();
 }
 
 cudaError_t fresh_shadow(const Launch& L, const ShadowView& sv, cudaStream_t s) {
   if (sv.two_bit) {   // every state NOACCESS
-    k_fill<<<L.num_sms * 8, kThreads, 0, s>>>(reinterpret_cast<uint4*>(sv.V), sv.v_bytes / 16, 0u);
+    launch_pdl(k_fill, L.num_sms * 8, kThreads, 0, s, reinterpret_cast<uint4*>(sv.V), sv.v_bytes / 16, 0u);
     *L.counter += 1;
     return cudaGetLastError();
   }
   const uint64_t nv = (sv.se - sv.sb) / 16, na = (sv.se - sv.sb) / 128;
-  k_fill<<<L.num_sms * 8, kThreads, 0, s>>>(reinterpret_cast<uint4*>(sv.V), nv, 0xffffffffu);
-  if (na) k_fill<<<L.num_sms * 8, kThreads, 0, s>>>(reinterpret_cast<uint4*>(sv.A), na, 0u);
+  launch_pdl(k_fill, L.num_sms * 8, kThreads, 0, s, reinterpret_cast<uint4*>(sv.V), nv, 0xffffffffu);
+  if (na) launch_pdl(k_fill, L.num_sms * 8, kThreads, 0, s, reinterpret_cast<uint4*>(sv.A), na, 0u);
   *L.counter += 2;
   return cudaGetLastError();
 }
@@ -2559,7 +2641,7 @@ cudaError_t fresh_shadow(const Launch& L, const ShadowView& sv, cudaStream_t s) 
 cudaError_t setv_check(const Launch& L, uint64_t addr, uint64_t len, const ShadowView& sv, uint32_t* d_flag,
                        cudaStream_t s) {
   cudaMemsetAsync(d_flag, 0, sizeof(uint32_t), s);
-  k_setv_check<<<blocks_for(len, kThreads, L.num_sms * 4), kThreads, 0, s>>>(sv, addr, len, d_flag);
+  launch_pdl(k_setv_check, blocks_for(len, kThreads, L.num_sms * 4), kThreads, 0, s, sv, addr, len, d_flag);
   *L.counter += 1;
   return cudaGetLastError();
 }
@@ -2568,12 +2650,12 @@ cudaError_t leak_sweep(const Launch& L, const Table& t, const Plan& p, cg_alloc_
                        uint64_t* d_count, cudaStream_t s) {
   if (t.n == 0) return cudaMemsetAsync(d_count, 0, sizeof(uint64_t), s);
   L.stage(CG_STAGE_LEAK, true, s);
-  k_live<<<blocks_for(t.n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(t, p.weight);
+  launch_pdl(k_live, blocks_for(t.n, kThreads, L.num_sms * 8), kThreads, 0, s, t, p.weight);
   const uint64_t nb = scan_blocks(t.n);
-  k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, t.n, p.bsum, nullptr);
-  k_scan_top<<<1, 1024, 0, s>>>(p.bsum, t.n, p.P, nullptr);
-  k_scan_down<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, t.n, p.bsum, p.P, nullptr);
-  k_leak_scatter<<<blocks_for(t.n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(t, p.P, out, cap, d_count);
+  launch_pdl(k_scan_reduce, (unsigned)nb, kScanThreads, 0, s, p.weight, t.n, p.bsum, nullptr);
+  launch_pdl(k_scan_top, 1, 1024, 0, s, p.bsum, t.n, p.P, nullptr);
+  launch_pdl(k_scan_down, (unsigned)nb, kScanThreads, 0, s, p.weight, t.n, p.bsum, p.P, nullptr);
+  launch_pdl(k_leak_scatter, blocks_for(t.n, kThreads, L.num_sms * 8), kThreads, 0, s, t, p.P, out, cap, d_count);
   L.stage(CG_STAGE_LEAK, false, s);
   *L.counter += 5;
   return cudaGetLastError();
@@ -2582,7 +2664,7 @@ cudaError_t leak_sweep(const Launch& L, const Table& t, const Plan& p, cg_alloc_
 cudaError_t straddler_pack(const Launch& L, const cg_verdict* v, uint64_t m, uint64_t* mins, uint64_t* sums,
                            uint32_t* maxs, cudaStream_t s) {
   if (m == 0) return cudaSuccess;
-  k_straddler_pack<<<blocks_for(m, kThreads, L.num_sms * 8), kThreads, 0, s>>>(v, m, mins, sums, maxs);
+  launch_pdl(k_straddler_pack, blocks_for(m, kThreads, L.num_sms * 8), kThreads, 0, s, v, m, mins, sums, maxs);
   *L.counter += 1;
   return cudaGetLastError();
 }
@@ -2590,7 +2672,7 @@ cudaError_t straddler_pack(const Launch& L, const cg_verdict* v, uint64_t m, uin
 cudaError_t straddler_finalize(const Launch& L, const uint64_t* mins, const uint64_t* sums, const uint32_t* maxs,
                                uint64_t m, cg_verdict* v, uint32_t err_mask, cudaStream_t s) {
   if (m == 0) return cudaSuccess;
-  k_straddler_finalize<<<blocks_for(m, kThreads, L.num_sms * 8), kThreads, 0, s>>>(mins, sums, maxs, m, v,
+  launch_pdl(k_straddler_finalize, blocks_for(m, kThreads, L.num_sms * 8), kThreads, 0, s, mins, sums, maxs, m, v,
                                                                                     err_mask);
   *L.counter += 1;
   return cudaGetLastError();
@@ -2600,14 +2682,14 @@ cudaError_t compact_dirty(const Launch& L, const cg_verdict* v, uint64_t n, uint
                           uint32_t* count, uint64_t idx_base, bool reset, cudaStream_t s) {
   if (reset) cudaMemsetAsync(count, 0, sizeof(uint32_t), s);
   if (n == 0) return cudaGetLastError();
-  k_compact_dirty<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(v, n, idx, dirty, count, idx_base);
+  launch_pdl(k_compact_dirty, blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s, v, n, idx, dirty, count, idx_base);
   *L.counter += 1;
   return cudaGetLastError();
 }
 
 cudaError_t expand_1d(const Launch& L, const cg_copy1d* in, uint64_t n, cg_copy_desc* out, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  k_expand_1d<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(in, n, out);
+  launch_pdl(k_expand_1d, blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s, in, n, out);
   *L.counter += 1;
   return cudaGetLastError();
 }
@@ -2623,7 +2705,7 @@ cudaError_t propagate(const Launch& L, const cg_copy_desc* d, const cg_verdict* 
   cudaMemsetAsync(p.counter, 0, 4 * sizeof(uint32_t), s);
   if (reset_overflow) cudaMemsetAsync(overflow, 0, sizeof(uint32_t), s);
   L.stage(CG_STAGE_APPLY_PREP, true, s);
-  k_prop_prep<<<blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s>>>(d, v, index, n, p.dvoff, sv.sb, p.weight, pm,
+  launch_pdl(k_prop_prep, blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s, d, v, index, n, p.dvoff, sv.sb, p.weight, pm,
                                                                           cnt, p.resid, mm_count);
   L.stage(CG_STAGE_APPLY_PREP, false, s);
   L.stage(CG_STAGE_APPLY_PLAN, true, s);
@@ -2632,9 +2714,9 @@ cudaError_t propagate(const Launch& L, const cg_copy_desc* d, const cg_verdict* 
   L.stage(CG_STAGE_APPLY_PLAN, false, s);
   L.stage(CG_STAGE_APPLY, true, s);
   cudaMemsetAsync(p.counter, 0, sizeof(uint32_t), s);
-  k_propagate<<<L.persist_blocks, kThreads, 0, s>>>(pm, n, p.P, p.chunk_first, p.counter, p.t_min, p.max_chunks,
+  launch_pdl(k_propagate, L.persist_blocks, kThreads, 0, s, pm, n, p.P, p.chunk_first, p.counter, p.t_min, p.max_chunks,
                                                     sv.V, pool, cnt);
-  k_memmove<<<64, kThreads, 0, s>>>(d, p.dvoff, p.resid, mm_count, pool, scratch, overflow);
+  launch_pdl(k_memmove, 64, kThreads, 0, s, d, p.dvoff, p.resid, mm_count, pool, scratch, overflow);
   L.stage(CG_STAGE_APPLY, false, s);
   *L.counter += 3;
   return cudaGetLastError();
@@ -2649,13 +2731,13 @@ cudaError_t propagate_direct(const Launch& L, const cg_copy_desc* d, const cg_ve
   L.stage(CG_STAGE_APPLY, true, s);
   const uint64_t slices = std::max<uint64_t>(1, (max_bytes + kDirectSlice - 1) / kDirectSlice);
   if (m * slices > (uint64_t)L.num_sms * 512) {   // very many copies: a warp each
-    k_prop_direct_warp<<<blocks_for(m * 32, kThreads, 1 << 20), kThreads, 0, s>>>(d, v, index, m, p.dvoff, sv.sb,
+    launch_pdl(k_prop_direct_warp, blocks_for(m * 32, kThreads, 1 << 20), kThreads, 0, s, d, v, index, m, p.dvoff, sv.sb,
                                                                                    sv.V, pool, p.resid, mm_count);
   } else {   // CTA slices keep the larger copies of the later waves streaming
-    k_prop_direct<<<dim3((unsigned)m, (unsigned)slices), kThreads, 0, s>>>(d, v, index, m, p.dvoff, sv.sb, sv.V, pool,
+    launch_pdl(k_prop_direct, dim3((unsigned)m, (unsigned)slices), kThreads, 0, s, d, v, index, m, p.dvoff, sv.sb, sv.V, pool,
                                                                           p.resid, mm_count);
   }
-  k_memmove<<<64, kThreads, 0, s>>>(d, p.dvoff, p.resid, mm_count, pool, scratch, overflow);
+  launch_pdl(k_memmove, 64, kThreads, 0, s, d, p.dvoff, p.resid, mm_count, pool, scratch, overflow);
   L.stage(CG_STAGE_APPLY, false, s);
   *L.counter += 2;
   return cudaGetLastError();
@@ -2669,14 +2751,14 @@ cudaError_t propagate_waves(const Launch& L, const cg_copy_desc* d, const cg_ver
   uint32_t* mm_count = p.counter + 3;
   cudaMemsetAsync(mm_count, 0, sizeof(uint32_t), s);
   L.stage(CG_STAGE_APPLY_PREP, true, s);
-  k_wave_prep<<<blocks_for(m, kThreads, L.num_sms * 8), kThreads, 0, s>>>(d, v, index, m, p.dvoff, sv.sb, p.weight,
+  launch_pdl(k_wave_prep, blocks_for(m, kThreads, L.num_sms * 8), kThreads, 0, s, d, v, index, m, p.dvoff, sv.sb, p.weight,
                                                                           pm, p.resid, mm_count);
   L.stage(CG_STAGE_APPLY_PREP, false, s);
   L.stage(CG_STAGE_APPLY_PLAN, true, s);
   const uint64_t nb = std::max<uint64_t>(scan_blocks(m), 1);
-  k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, m, p.bsum, nullptr);
-  k_scan_top<<<1, 1024, 0, s>>>(p.bsum, m, p.P, nullptr);
-  k_scan_down<<<(unsigned)nb, kScanThreads, 0, s>>>(p.weight, m, p.bsum, p.P, nullptr);
+  launch_pdl(k_scan_reduce, (unsigned)nb, kScanThreads, 0, s, p.weight, m, p.bsum, nullptr);
+  launch_pdl(k_scan_top, 1, 1024, 0, s, p.bsum, m, p.P, nullptr);
+  launch_pdl(k_scan_down, (unsigned)nb, kScanThreads, 0, s, p.weight, m, p.bsum, p.P, nullptr);
   L.stage(CG_STAGE_APPLY_PLAN, false, s);
   L.stage(CG_STAGE_APPLY, true, s);
   uint8_t* V = sv.V;

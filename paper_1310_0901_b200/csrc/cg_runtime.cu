@@ -80,7 +80,7 @@ Layout layout_of(const cg_config* c) {
     off = align_up(off + bytes, kAlign);
     return o;
   };
-  L.table = take(6 * c->max_allocs * 8 + (4096 + 3) * 8);   // SoA (+ pool offsets) + splitters
+  L.table = take(6 * c->max_allocs * 8 + (4096 + 3) * 8 + (c->max_allocs / 4 + 16) * 8);   // SoA (+ pool offsets) + splitters + every 4th base
   L.arrays = take(4 * c->max_allocs * 8);                    // NEXT-3 array table (SoA)
   L.weight = take(L.max_items * 8);
   L.P = take((L.max_items + 1) * 8);
@@ -265,6 +265,7 @@ struct cg_ctx {
     t.pmax = b + 4 * cap;
     t.pool = cfg.dev_vbuf ? b + 5 * cap : nullptr;
     t.split = b + ((6 * cap + 1) & ~1ull);   // 16-byte aligned
+    t.l2 = b + l2_offset(cap);
     t.n = table.size();
     uint64_t* a = d(lay.arrays);
     t.ahandle = a;
@@ -300,12 +301,16 @@ struct cg_ctx {
       const uint64_t so = (6 * cap + 1) & ~1ull;
       for (uint64_t k = 0; k < nsplit; ++k) h_table[so + k] = table[k * stride].base;
       h_table[so + nsplit] = UINT64_MAX;   // padding for the 16-byte loads
+      const uint64_t hl2 = so + 4099 + 4 * cap, nl2 = (n + 3) / 4;   // host staging of every 4th base
+      for (uint64_t k = 0; k < nl2; ++k) h_table[hl2 + k] = table[4 * k].base;
       uint64_t* dt = d(lay.table);
       for (int k = 0; k < 6; ++k) {
         e = cudaMemcpyAsync(dt + k * cap, h_table + k * cap, n * 8, cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) return cuda(e, "table upload");
       }
       e = cudaMemcpyAsync(dt + so, h_table + so, (nsplit + 1) * 8, cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(dt + l2_offset(cap), h_table + hl2, nl2 * 8, cudaMemcpyHostToDevice, s);
       if (e != cudaSuccess) return cuda(e, "splitter upload");
     }
     if (const uint64_t na = arrays.size()) {
@@ -330,6 +335,9 @@ struct cg_ctx {
     dirty = false;
     return CG_OK;
   }
+
+  // word offset of the every-4th-base array in the device table (64-byte aligned)
+  static uint64_t l2_offset(uint64_t cap) { return ((((6 * cap + 1) & ~1ull) + 4099) + 7) & ~7ull; }
 
   static uint64_t split_stride(uint64_t n) {
     const uint64_t stride = std::max<uint64_t>(32, (n + 4095) / 4096);
@@ -401,7 +409,7 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
   c->prof.mark = &cg_ctx::mark_cb;
   c->prof.self = c;
   c->launch.prof = &c->prof;
-  if (cudaMallocHost(&c->h_table, 10 * cfg->max_allocs * 8 + (4096 + 5) * 8) != cudaSuccess ||
+  if (cudaMallocHost(&c->h_table, 10 * cfg->max_allocs * 8 + (4096 + 5) * 8 + (cfg->max_allocs / 4 + 16) * 8) != cudaSuccess ||
       cudaMallocHost(&c->h_marks, std::min<uint64_t>(cfg->max_descs, kMarkRun) * sizeof(cg_mark)) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->staged, cudaEventDisableTiming) != cudaSuccess) {
     cg_ctx_destroy(c);
