@@ -1952,8 +1952,8 @@ __global__ void __launch_bounds__(kThreads) k_memmove(const cg_copy_desc* __rest
 // whose weight range spans several pieces is moved by all of them, each its
 // own bytes.  Self-overlapping DtoDs (memmove) go to a list worked off at the
 // end of their wave, between two barriers, one CTA per entry.
-constexpr uint64_t kWaveItemCost = 1024;     // per-copy latency, in bytes of bandwidth
-constexpr uint64_t kWaveMinPiece = 16384;    // smallest per-warp share of a wave
+constexpr uint64_t kWaveItemCost = 2048;     // per-copy latency, in bytes of bandwidth (env CG_WAVE_COST)
+constexpr uint64_t kWaveMinPiece = 2048;     // smallest per-warp share of a wave (env CG_WAVE_PIECE)
 constexpr uint64_t kPropMemmove = 1ull << 44;
 
 __global__ void __launch_bounds__(kThreads) k_wave_prep(const cg_copy_desc* __restrict__ descs,
@@ -1961,7 +1961,8 @@ __global__ void __launch_bounds__(kThreads) k_wave_prep(const cg_copy_desc* __re
                                                         const uint32_t* __restrict__ index, uint64_t m,
                                                         const uint64_t* __restrict__ dvoff, uint64_t sb,
                                                         uint64_t* __restrict__ weight, PropMeta* __restrict__ pm,
-                                                        uint32_t* __restrict__ mm, uint32_t* __restrict__ mm_count) {
+                                                        uint32_t* __restrict__ mm, uint32_t* __restrict__ mm_count,
+                                                        uint64_t item_cost) {
   pdl_entry();
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t i = index[k];
@@ -1993,7 +1994,7 @@ __global__ void __launch_bounds__(kThreads) k_wave_prep(const cg_copy_desc* __re
           pmk.dst = dvoff[2 * i];
           pmk.info = nb | (3ull << 41);
         }
-        w = kWaveItemCost + nb;
+        w = item_cost + nb;
         if (d.kind == CG_DTOD && pmk.src < pmk.dst + nm.dspan && pmk.dst < pmk.src + nm.sspan) {
           w = 0;   // overlaps itself: the wave's memmove list
           pmk.info |= kPropMemmove;
@@ -2046,6 +2047,7 @@ struct WaveGen {
   const uint64_t* P;
   uint8_t *V, *pool;
   uint64_t gw, nw;
+  uint64_t item_cost, min_piece;
   // wave and piece
   uint64_t a, b, w0, w1, piece, np, pc, s, e;
   bool have_piece;
@@ -2064,7 +2066,7 @@ struct WaveGen {
     b = __ldg(wstart + w + 1);
     w0 = __ldg(P + a);
     w1 = __ldg(P + b);
-    piece = umax64((w1 - w0 + nw - 1) / nw, kWaveMinPiece);
+    piece = umax64((w1 - w0 + nw - 1) / nw, min_piece);
     np = w1 > w0 ? (w1 - w0 + piece - 1) / piece : 0;
     pc = gw;
     have_piece = in_copy = false;
@@ -2124,8 +2126,8 @@ struct WaveGen {
       }
       const uint64_t pd1 = __shfl_sync(kFull, pk1, j);
       uint64_t x = umax64(s, pd) - pd, yy = umin64(e, pd1) - pd;
-      x = x > kWaveItemCost ? x - kWaveItemCost : 0;
-      yy = yy > kWaveItemCost ? yy - kWaveItemCost : 0;
+      x = x > item_cost ? x - item_cost : 0;
+      yy = yy > item_cost ? yy - item_cost : 0;
       if (x >= yy) continue;   // nothing to move here (or a memmove entry, weight 0)
       const uint64_t info = __shfl_sync(kFull, m.info, j);
       W = __shfl_sync(kFull, m.W, j);
@@ -2224,7 +2226,7 @@ __global__ void __launch_bounds__(kWRing * 32) k_prop_waves(const cg_copy_desc* 
                                                             const uint64_t* __restrict__ dvoff,
                                                             const uint32_t* __restrict__ mm,
                                                             const uint32_t* __restrict__ mm_count, uint8_t* scratch,
-                                                            uint32_t* overflow) {
+                                                            uint32_t* overflow, uint64_t item_cost, uint64_t min_piece) {
   pdl_entry();
   extern __shared__ __align__(128) uint8_t smem[];
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
@@ -2242,6 +2244,8 @@ __global__ void __launch_bounds__(kWRing * 32) k_prop_waves(const cg_copy_desc* 
   gen.pool = pool;
   gen.gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   gen.nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  gen.item_cost = item_cost;
+  gen.min_piece = min_piece;
   const uint32_t nmm = *mm_count;
   uint32_t phase = 0;   // bit s = parity to wait for on slot s
   gen.begin_wave(wstart, 0);
@@ -2756,8 +2760,16 @@ cudaError_t propagate_waves(const Launch& L, const cg_copy_desc* d, const cg_ver
   uint32_t* mm_count = p.counter + 3;
   cudaMemsetAsync(mm_count, 0, sizeof(uint32_t), s);
   L.stage(CG_STAGE_APPLY_PREP, true, s);
+  static const uint64_t item_cost = [] {
+    const char* e = getenv("CG_WAVE_COST");
+    return e ? (uint64_t)atoll(e) : kWaveItemCost;
+  }();
+  static const uint64_t min_piece = [] {
+    const char* e = getenv("CG_WAVE_PIECE");
+    return e ? std::max<uint64_t>((uint64_t)atoll(e), 1) : kWaveMinPiece;
+  }();
   launch_pdl(k_wave_prep, blocks_for(m, kThreads, L.num_sms * 8), kThreads, 0, s, d, v, index, m, p.dvoff, sv.sb, p.weight,
-                                                                          pm, p.resid, mm_count);
+                                                                          pm, p.resid, mm_count, item_cost);
   L.stage(CG_STAGE_APPLY_PREP, false, s);
   L.stage(CG_STAGE_APPLY_PLAN, true, s);
   const uint64_t nb = std::max<uint64_t>(scan_blocks(m), 1);
@@ -2771,8 +2783,10 @@ cudaError_t propagate_waves(const Launch& L, const cg_copy_desc* d, const cg_ver
   const uint64_t* dvoff = p.dvoff;
   const uint32_t* mm = p.resid;
   const uint32_t* mmc = mm_count;
+  uint64_t ic = item_cost, mp = min_piece;
   void* args[] = {(void*)&d, (void*)&index, (void*)&pm, (void*)&P, (void*)&d_wstart, (void*)&n_waves, (void*)&V,
-                  (void*)&pool, (void*)&dvoff, (void*)&mm, (void*)&mmc, (void*)&scratch, (void*)&overflow};
+                  (void*)&pool, (void*)&dvoff, (void*)&mm, (void*)&mmc, (void*)&scratch, (void*)&overflow, (void*)&ic,
+                  (void*)&mp};
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_prop_waves, dim3((unsigned)L.wave_blocks),
                                               dim3(kWRing * 32), args, kWaveSmem, s);
   L.stage(CG_STAGE_APPLY, false, s);
