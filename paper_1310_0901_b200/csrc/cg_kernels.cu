@@ -1208,6 +1208,9 @@ struct TileGen {
   }
 };
 
+// one instantiation per host shadow format (kTwoBit: NEXT-4 2-bit states):
+// the other format's paths are compiled out of each
+template <bool kTwoBit>
 __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
     const ScanMeta* __restrict__ meta, uint64_t n, const uint64_t* __restrict__ P,
     const uint32_t* __restrict__ chunk_first, uint32_t* counter, uint64_t t_min, uint64_t max_chunks,
@@ -1243,7 +1246,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
   gen.sb = sv.sb;
   gen.se = sv.se;
   gen.fuse = fuse != 0;
-  gen.two_bit = sv.two_bit != 0;
+  gen.two_bit = kTwoBit;
   gen.k_pending = kGrab;
   gen.g_pending = lane == 0 ? atomicAdd(counter, kGrab) : 0;
   gen.phase = kPhaseGroup;
@@ -2572,7 +2575,7 @@ cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_
   if (e != cudaSuccess) return e;
   L.stage(CG_STAGE_CHECK_PLAN, false, s);
   L.stage(CG_STAGE_CHECK_SCAN, true, s);
-  launch_pdl(k_check_scan, L.scan_blocks, kRingWarps * 32, kScanSmem, s, meta, n, p.P, p.chunk_first, p.counter,
+  launch_pdl(sv.two_bit ? k_check_scan<true> : k_check_scan<false>, L.scan_blocks, kRingWarps * 32, kScanSmem, s, meta, n, p.P, p.chunk_first, p.counter,
                                                                  p.t_min, p.max_chunks, sv, out, err_mask,
                                                                  fuse ? 1 : 0, p.resid, p.counter + 2);
   L.stage(CG_STAGE_CHECK_SCAN, false, s);
@@ -2801,8 +2804,12 @@ uint64_t stage_bytes() { return kStageBytes; }
 int persistent_blocks(int which) {
   int b = 0;
   if (which == 0) {
-    cudaFuncSetAttribute(k_check_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_check_scan, kRingWarps * 32, kScanSmem);
+    int b2 = 0;
+    cudaFuncSetAttribute(k_check_scan<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem);
+    cudaFuncSetAttribute(k_check_scan<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_check_scan<false>, kRingWarps * 32, kScanSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_check_scan<true>, kRingWarps * 32, kScanSmem);
+    b = std::min(b, b2);
   } else if (which == 1) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_apply, kThreads, 0);
   } else {
