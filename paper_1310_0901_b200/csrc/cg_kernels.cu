@@ -1208,9 +1208,10 @@ struct TileGen {
   }
 };
 
-// one instantiation per host shadow format (kTwoBit: NEXT-4 2-bit states):
-// the other format's paths are compiled out of each
-template <bool kTwoBit>
+// one instantiation per host shadow format (kTwoBit: NEXT-4 2-bit states)
+// and apply mode (kFuse: cg_check_apply): the other paths are compiled out of
+// each, which relieves instruction-cache stalls
+template <bool kTwoBit, bool kFuse>
 __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
     const ScanMeta* __restrict__ meta, uint64_t n, const uint64_t* __restrict__ P,
     const uint32_t* __restrict__ chunk_first, uint32_t* counter, uint64_t t_min, uint64_t max_chunks,
@@ -1245,7 +1246,8 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
   gen.we = sv.we;
   gen.sb = sv.sb;
   gen.se = sv.se;
-  gen.fuse = fuse != 0;
+  gen.fuse = kFuse;
+  (void)fuse;
   gen.two_bit = kTwoBit;
   gen.k_pending = kGrab;
   gen.g_pending = lane == 0 ? atomicAdd(counter, kGrab) : 0;
@@ -1298,7 +1300,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
           v->status = status;
           apply = (t.flags & kTileFuse) && status == CG_OK;
           // a whole 2D DtoH piece with status OK: the residual pass applies it
-          if (fuse && !(t.flags & (kTileFuse | kTileHtod)) && status == CG_OK) resid[atomicAdd(resid_n, 1u)] = t.d;
+          if (kFuse && !(t.flags & (kTileFuse | kTileHtod)) && status == CG_OK) resid[atomicAdd(resid_n, 1u)] = t.d;
         } else {
           if (p.fu != kNone) atomicMin(reinterpret_cast<unsigned long long*>(&v->first_unaddr), p.fu);
           if (p.fd != kNone) atomicMin(reinterpret_cast<unsigned long long*>(&v->first_undef), p.fd);
@@ -1476,6 +1478,7 @@ __device__ __forceinline__ void warp_zero(uint8_t* V, uint64_t q0, uint64_t q1, 
     bulk_s2g(V + p, zeros, (uint32_t)umin64(kZeroPage, a1 - p));
 }
 
+template <bool kTwoBit>
 __global__ void __launch_bounds__(kThreads) k_apply(const ScanMeta* __restrict__ meta, uint64_t n,
                                                     const uint64_t* __restrict__ P,
                                                     const uint32_t* __restrict__ chunk_first, uint32_t* counter,
@@ -1519,7 +1522,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(const ScanMeta* __restrict__
             if (y0 < y1) {
               qs = y0 - sv.sb;
               qe = y1 - sv.sb;
-              small = qe - qs <= (sv.two_bit ? 256u : 2 * kZeroPage);
+              small = qe - qs <= (kTwoBit ? 256u : 2 * kZeroPage);
               big = !small;
             }
           } else {
@@ -1528,7 +1531,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(const ScanMeta* __restrict__
         }
       }
       if (small) {
-        if (sv.two_bit) fill2_any<false>(sv, qs, qe, 0xAAAAAAAAu);
+        if (kTwoBit) fill2_any<false>(sv, qs, qe, 0xAAAAAAAAu);
         else lane_zero(sv.V, qs, qe, zeros);
       }
       uint32_t todo = __ballot_sync(kFull, big);
@@ -1538,7 +1541,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(const ScanMeta* __restrict__
         const uint64_t s_info = __shfl_sync(kFull, m.info, src);
         if ((s_info >> 43) & 1u) {
           const uint64_t a = __shfl_sync(kFull, qs, src), b = __shfl_sync(kFull, qe, src);
-          if (sv.two_bit) fill2_any<true>(sv, a, b, 0xAAAAAAAAu);
+          if (kTwoBit) fill2_any<true>(sv, a, b, 0xAAAAAAAAu);
           else warp_zero(sv.V, a, b, zeros);
         } else {
           const uint64_t x0 = __shfl_sync(kFull, m.hstart, src), pitch = __shfl_sync(kFull, m.hpitch, src);
@@ -1550,7 +1553,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(const ScanMeta* __restrict__
             const uint64_t x = x0 + r * pitch + c;
             const uint64_t y0 = umax64(x, sv.sb), y1 = umin64(x + len, sv.se);
             if (y0 < y1) {
-              if (sv.two_bit) fill2_any<true>(sv, y0 - sv.sb, y1 - sv.sb, 0xAAAAAAAAu);
+              if (kTwoBit) fill2_any<true>(sv, y0 - sv.sb, y1 - sv.sb, 0xAAAAAAAAu);
               else warp_zero(sv.V, y0 - sv.sb, y1 - sv.sb, zeros);
             }
             oo += len;
@@ -2575,7 +2578,8 @@ cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_
   if (e != cudaSuccess) return e;
   L.stage(CG_STAGE_CHECK_PLAN, false, s);
   L.stage(CG_STAGE_CHECK_SCAN, true, s);
-  launch_pdl(sv.two_bit ? k_check_scan<true> : k_check_scan<false>, L.scan_blocks, kRingWarps * 32, kScanSmem, s, meta, n, p.P, p.chunk_first, p.counter,
+  launch_pdl(sv.two_bit ? (fuse ? k_check_scan<true, true> : k_check_scan<true, false>)
+                        : (fuse ? k_check_scan<false, true> : k_check_scan<false, false>), L.scan_blocks, kRingWarps * 32, kScanSmem, s, meta, n, p.P, p.chunk_first, p.counter,
                                                                  p.t_min, p.max_chunks, sv, out, err_mask,
                                                                  fuse ? 1 : 0, p.resid, p.counter + 2);
   L.stage(CG_STAGE_CHECK_SCAN, false, s);
@@ -2609,7 +2613,7 @@ cudaError_t apply_dtoh(const Launch& L, const cg_copy_desc* d, const cg_verdict*
   L.stage(CG_STAGE_APPLY_PLAN, false, s);
   L.stage(CG_STAGE_APPLY, true, s);
   if (!after_fused) cudaMemsetAsync(p.counter, 0, sizeof(uint32_t), s);
-  launch_pdl(k_apply, L.persist_blocks, kThreads, 0, s, meta, n, p.P, p.chunk_first, p.counter, p.t_min, p.max_chunks, sv,
+  launch_pdl(sv.two_bit ? k_apply<true> : k_apply<false>, L.persist_blocks, kThreads, 0, s, meta, n, p.P, p.chunk_first, p.counter, p.t_min, p.max_chunks, sv,
                                                 n_dev);
   L.stage(CG_STAGE_APPLY, false, s);
   *L.counter += 1;
@@ -2804,14 +2808,18 @@ uint64_t stage_bytes() { return kStageBytes; }
 int persistent_blocks(int which) {
   int b = 0;
   if (which == 0) {
-    int b2 = 0;
-    cudaFuncSetAttribute(k_check_scan<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem);
-    cudaFuncSetAttribute(k_check_scan<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_check_scan<false>, kRingWarps * 32, kScanSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_check_scan<true>, kRingWarps * 32, kScanSmem);
-    b = std::min(b, b2);
+    b = 1 << 20;
+    for (auto k : {k_check_scan<false, false>, k_check_scan<false, true>, k_check_scan<true, false>,
+                   k_check_scan<true, true>}) {
+      int bk = 0;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bk, k, kRingWarps * 32, kScanSmem);
+      b = std::min(b, bk);
+    }
   } else if (which == 1) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_apply, kThreads, 0);
+    // the bytes-format instantiation sizes the persistent grid (extra CTAs of
+    // the 2-bit one just find the group counter exhausted)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_apply<false>, kThreads, 0);
   } else {
     cudaFuncSetAttribute(k_prop_waves, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWaveSmem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_prop_waves, kWRing * 32, kWaveSmem);
