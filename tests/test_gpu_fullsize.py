@@ -142,3 +142,31 @@ def test_c2_full_fused_formats(cg, fmt):
     for i in rng.choice(dtoh, 50, replace=False):
         a, v = chk.shadow_read(int(descs["dst"][i]), int(descs["width"][i]))
         assert a.all() and not v.any(), i
+
+
+def test_c2_full_tracking(cg):
+    """NEXT-1 at full C2 size, as `bench.py --track` runs it: R-20 epochs for the
+    check, each epoch's V-bit propagation in its 128 dependency waves through
+    one cooperative k_prop_waves launch (R-28).  The oracle replays the whole
+    trace sequentially in tracking mode: every verdict, the whole host shadow
+    and the device V-bits of 3000 sampled live allocations must agree."""
+    tr = tg.c2_small()
+    ev = tr.events
+    o, ov, os_, oleaks = oracle.replay_trace(tr, track_device=True)
+    regs = ev[ev["op"] == tg.OP_REG]
+    pool = int(regs["width"].astype(np.int64).sum()) + 256 * len(regs) + (1 << 20)
+    copies = ev[ev["op"] == tg.OP_COPY]
+    chk = cg.Checker(tr.host_base, tr.host_size, max_descs=len(copies), max_allocs=max(len(regs), 1024),
+                     dev_vsize=pool)
+    gv, gs = cg.replay_events(chk, ev, tr.blob)
+    for f in ov.dtype.names:
+        bad = np.flatnonzero(gv[f] != ov[f])
+        assert len(bad) == 0, (f, bad[:5])
+    assert np.array_equal(gs, os_)
+    A, V = chk.shadow()
+    assert np.array_equal(A, o.A) and np.array_equal(V, o.V)
+    rng = np.random.default_rng(7)
+    for r in oleaks[rng.choice(len(oleaks), size=min(3000, len(oleaks)), replace=False)]:
+        b, n = int(r["base"]), int(r["size"])
+        assert np.array_equal(chk.device_vbits(b, n), o.device_vbits(b, n)), hex(b)
+    chk.close()
