@@ -853,9 +853,9 @@ __device__ __forceinline__ uint8_t* chunk_base(const ShadowView& sv, uint64_t ch
 
 // states of shard bytes [q0, q1) := pat in either 2-bit layout (sparse: chunk
 // by chunk; chunks without a secondary are NOACCESS and left alone)
-template <bool kWarp>
+template <bool kWarp, bool kMaySparse = true>
 __device__ __forceinline__ void fill2_any(const ShadowView& sv, uint64_t q0, uint64_t q1, uint32_t pat) {
-  if (!sv.sparse) {
+  if (!kMaySparse || !sv.sparse) {
     if (kWarp) warp_fill2(sv.V, q0, q1, pat);
     else lane_fill2(sv.V, q0, q1, pat);
     return;
@@ -930,6 +930,7 @@ struct TileGen {
   uint64_t wb, we, sb, se;
   bool fuse;            // check + apply in one pass (cg_check_apply)
   bool two_bit;         // NEXT-4 2-bit states: 16 KiB host bytes per tile for both kinds
+  bool sparse;          // NEXT-4 two-level sparse map (2-bit states behind a chunk directory)
   // group
   uint64_t w0, w1;
   uint32_t g_pending;   // lane 0: first chunk of the next group
@@ -1184,7 +1185,7 @@ struct TileGen {
       if (two_bit) {   // host bytes [qa, qa + span) <-> 16-byte aligned state bytes [qa/4, (qa + span)/4)
         const uint32_t span = (ti.q1 + 63u) & ~63u;
         const uint8_t* base = sv.V;
-        if (sv.sparse) {   // a tile never leaves its 16 KiB block, so never its chunk
+        if (sparse) {   // a tile never leaves its 16 KiB block, so never its chunk
           const uint64_t c = qa >> kChunkShift;
           base = chunk_base(sv, c, sparse_secondary(sv, c));
         }
@@ -1211,7 +1212,7 @@ struct TileGen {
 // one instantiation per host shadow format (kTwoBit: NEXT-4 2-bit states)
 // and apply mode (kFuse: cg_check_apply): the other paths are compiled out of
 // each, which relieves instruction-cache stalls
-template <bool kTwoBit, bool kFuse>
+template <bool kTwoBit, bool kFuse, bool kSparse>
 __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
     const ScanMeta* __restrict__ meta, uint64_t n, const uint64_t* __restrict__ P,
     const uint32_t* __restrict__ chunk_first, uint32_t* counter, uint64_t t_min, uint64_t max_chunks,
@@ -1249,6 +1250,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
   gen.fuse = kFuse;
   (void)fuse;
   gen.two_bit = kTwoBit;
+  gen.sparse = kSparse;
   gen.k_pending = kGrab;
   gen.g_pending = lane == 0 ? atomicAdd(counter, kGrab) : 0;
   gen.phase = kPhaseGroup;
@@ -1310,7 +1312,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
       p = Partial{kNone, kNone, 0};
       // fused a6: a whole contiguous DtoH piece with status OK becomes defined
       if (__shfl_sync(kFull, apply, 0)) {
-        if (gen.two_bit) fill2_any<true>(sv, t.qs, t.qe, 0xAAAAAAAAu);
+        if (gen.two_bit) fill2_any<true, kSparse>(sv, t.qs, t.qe, 0xAAAAAAAAu);
         else warp_store_zero(sv.V, t.qs, t.qe);
       }
     }
@@ -2578,8 +2580,10 @@ cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_
   if (e != cudaSuccess) return e;
   L.stage(CG_STAGE_CHECK_PLAN, false, s);
   L.stage(CG_STAGE_CHECK_SCAN, true, s);
-  launch_pdl(sv.two_bit ? (fuse ? k_check_scan<true, true> : k_check_scan<true, false>)
-                        : (fuse ? k_check_scan<false, true> : k_check_scan<false, false>), L.scan_blocks, kRingWarps * 32, kScanSmem, s, meta, n, p.P, p.chunk_first, p.counter,
+  auto scan = !sv.two_bit ? (fuse ? k_check_scan<false, true, false> : k_check_scan<false, false, false>)
+              : sv.sparse ? (fuse ? k_check_scan<true, true, true> : k_check_scan<true, false, true>)
+                          : (fuse ? k_check_scan<true, true, false> : k_check_scan<true, false, false>);
+  launch_pdl(scan, L.scan_blocks, kRingWarps * 32, kScanSmem, s, meta, n, p.P, p.chunk_first, p.counter,
                                                                  p.t_min, p.max_chunks, sv, out, err_mask,
                                                                  fuse ? 1 : 0, p.resid, p.counter + 2);
   L.stage(CG_STAGE_CHECK_SCAN, false, s);
@@ -2809,8 +2813,9 @@ int persistent_blocks(int which) {
   int b = 0;
   if (which == 0) {
     b = 1 << 20;
-    for (auto k : {k_check_scan<false, false>, k_check_scan<false, true>, k_check_scan<true, false>,
-                   k_check_scan<true, true>}) {
+    for (auto k : {k_check_scan<false, false, false>, k_check_scan<false, true, false>,
+                   k_check_scan<true, false, false>, k_check_scan<true, true, false>, k_check_scan<true, false, true>,
+                   k_check_scan<true, true, true>}) {
       int bk = 0;
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bk, k, kRingWarps * 32, kScanSmem);
