@@ -96,6 +96,7 @@ struct Plan {
   uint64_t* weight;       // [n]
   uint64_t* P;            // [n + 1]
   uint64_t* bsum;         // [nblocks + 1]
+  uint64_t* fbsum;        // [kFinishMaxBlocks] k_finish's per-block sums
   uint32_t* chunk_first;  // [max_chunks]
   void* meta;             // [n] ScanMeta (check plans only)
   uint32_t* counter;      // [0] group counter, [1] apply compaction count, [2] residual-list count
@@ -117,6 +118,7 @@ struct Launch {
   int persist_blocks;     // persistent grid for the chunked kernels
   int scan_blocks;        // persistent grid of the TMA-ring scan
   int wave_blocks;        // cooperative grid of k_prop_waves (all co-resident)
+  int finish_blocks;      // cooperative grid of k_finish
   uint64_t* counter;      // host counter of kernel launches
   Profiler* prof;
   void stage(int st, bool begin, cudaStream_t s) const {
@@ -127,7 +129,8 @@ struct Launch {
 constexpr int kScanTile = 2048;   // items per block of the prefix scan
 
 uint64_t scan_blocks(uint64_t n);
-int persistent_blocks(int which);   // 0: k_check_scan, 1: k_apply, 2: k_prop_waves (per SM)
+int persistent_blocks(int which);   // 0: k_check_scan, 1: k_apply, 2: k_prop_waves, 3: k_finish (per SM)
+constexpr uint64_t kFinishMaxBlocks = 4096;
 size_t prop_meta_bytes();
 uint64_t stage_bytes();
 cudaError_t propagate(const Launch& L, const cg_copy_desc* d, const cg_verdict* v, const uint32_t* index, uint64_t n,
@@ -144,6 +147,8 @@ size_t scan_meta_bytes();
 cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out,
                          const Table& t, const ShadowView& sv, const Plan& p, uint32_t err_mask, bool fuse,
                          cudaStream_t s);
+cudaError_t check_apply(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out, const Table& t,
+                        const ShadowView& sv, const Plan& p, uint32_t err_mask, cudaStream_t s);
 cudaError_t apply_dtoh(const Launch& L, const cg_copy_desc* d, const cg_verdict* v, uint64_t n,
                        const ShadowView& sv, const Plan& p, bool after_fused, cudaStream_t s);
 cudaError_t straddler_pack(const Launch& L, const cg_verdict* v, uint64_t m, uint64_t* mins, uint64_t* sums,

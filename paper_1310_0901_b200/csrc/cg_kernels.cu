@@ -1480,19 +1480,12 @@ __device__ __forceinline__ void warp_zero(uint8_t* V, uint64_t q0, uint64_t q1, 
     bulk_s2g(V + p, zeros, (uint32_t)umin64(kZeroPage, a1 - p));
 }
 
+// the apply walk over planned groups (shared by k_apply and k_finish)
 template <bool kTwoBit>
-__global__ void __launch_bounds__(kThreads) k_apply(const ScanMeta* __restrict__ meta, uint64_t n,
-                                                    const uint64_t* __restrict__ P,
-                                                    const uint32_t* __restrict__ chunk_first, uint32_t* counter,
-                                                    uint64_t t_min, uint64_t max_chunks, ShadowView sv,
-                                                    const uint32_t* __restrict__ n_dev) {
-  pdl_entry();
-  n = eff_n(n, n_dev);
-  __shared__ __align__(128) uint8_t zeros[kZeroPage];
-  for (uint32_t i = threadIdx.x; i < kZeroPage / 16; i += blockDim.x)
-    reinterpret_cast<uint4*>(zeros)[i] = make_uint4(0, 0, 0, 0);
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  __syncthreads();
+__device__ __forceinline__ void apply_body(const ScanMeta* __restrict__ meta, uint64_t n,
+                                           const uint64_t* __restrict__ P, const uint32_t* __restrict__ chunk_first,
+                                           uint32_t* counter, uint64_t t_min, uint64_t max_chunks,
+                                           const ShadowView& sv, const uint8_t* zeros) {
   const ChunkGeom geo = chunk_geom(P, n, t_min, max_chunks);
   const int lane = threadIdx.x & 31;
   uint32_t gnext = lane == 0 ? atomicAdd(counter, 1u) : 0;
@@ -1570,6 +1563,130 @@ __global__ void __launch_bounds__(kThreads) k_apply(const ScanMeta* __restrict__
   }
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+__device__ __forceinline__ void zero_page(uint8_t* zeros) {
+  for (uint32_t i = threadIdx.x; i < kZeroPage / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(zeros)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+}
+
+template <bool kTwoBit>
+__global__ void __launch_bounds__(kThreads) k_apply(const ScanMeta* __restrict__ meta, uint64_t n,
+                                                    const uint64_t* __restrict__ P,
+                                                    const uint32_t* __restrict__ chunk_first, uint32_t* counter,
+                                                    uint64_t t_min, uint64_t max_chunks, ShadowView sv,
+                                                    const uint32_t* __restrict__ n_dev) {
+  pdl_entry();
+  n = eff_n(n, n_dev);
+  __shared__ __align__(128) uint8_t zeros[kZeroPage];
+  zero_page(zeros);
+  apply_body<kTwoBit>(meta, n, P, chunk_first, counter, t_min, max_chunks, sv, zeros);
+}
+
+// cg_check_apply's tail in one cooperative launch (after the fused scan):
+// finalise split descriptors (k_finalize_split), then -- only if the scan or
+// the finalisation left a residual DtoH list (split or 2D pieces) -- its
+// records and weights, their prefix sum, the chunk plan and the apply walk,
+// with grid barriers between the phases.  An empty list (C2: every DtoH piece
+// was applied by the scan) costs one launch and one barrier instead of six
+// launches.
+template <bool kTwoBit>
+__global__ void __launch_bounds__(kThreads) k_finish(
+    const cg_copy_desc* __restrict__ descs, uint64_t n, uint64_t* P, uint64_t t_min, uint64_t max_chunks,
+    cg_verdict* __restrict__ out, uint32_t err_mask, ScanMeta* meta, uint32_t* __restrict__ resid,
+    uint32_t* counter, uint64_t* __restrict__ weight, uint64_t* __restrict__ bsum, uint32_t* __restrict__ chunk_first,
+    ShadowView sv) {
+  pdl_entry();
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  __shared__ __align__(128) uint8_t zeros[kZeroPage];
+  __shared__ uint64_t s_warp[33];
+  uint32_t* resid_n = counter + 2;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nthr = (uint64_t)gridDim.x * blockDim.x;
+  {   // a5 for split descriptors
+    const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
+    for (uint64_t d = tid; d < n; d += nthr) {
+      const uint64_t pd = P[d], pd1 = P[d + 1];
+      if (pd1 - pd <= g.Trule) continue;   // never split (see compute_pieces)
+      const uint64_t info = meta[d].info;
+      if ((info >> 44) & 1u) continue;     // raw partial of a straddler
+      cg_verdict* v = out + d;
+      uint32_t flags = v->flags, status;
+      finalize_fields(flags, status, v->first_unaddr, v->undef_count, err_mask);
+      v->flags = flags;
+      v->status = status;
+      if (status == CG_OK && ((info >> 40) & 3u) == CG_DTOH && ((info >> 42) & 1u))
+        resid[atomicAdd(resid_n, 1u)] = (uint32_t)d;
+    }
+    if (tid == 0) counter[0] = 0;   // the apply walk's group counter
+  }
+  grid.sync();
+  const uint64_t m = __ldcg(resid_n);
+  if (m == 0) return;   // uniform: nothing left to apply
+  for (uint64_t k = tid; k < m; k += nthr) {   // residual records (k_apply_list_prep)
+    const cg_copy_desc d = descs[resid[k]];
+    const Norm nm = normalize(d);
+    ScanMeta mm;
+    mm.hstart = nm.hstart;
+    mm.hpitch = nm.hpitch;
+    mm.W = nm.W;
+    mm.info = nm.nbytes | ((uint64_t)(d.height == 1 || d.width == nm.hpitch) << 43);
+    meta[k] = mm;
+    weight[k] = kApplyItemCost + nm.nbytes;
+  }
+  grid.sync();
+  // prefix sum of weight[0..m) into P: block b owns items [b*per, (b+1)*per)
+  const uint64_t per = (m + gridDim.x - 1) / gridDim.x;
+  const uint64_t lo = umin64(m, (uint64_t)blockIdx.x * per), hi = umin64(m, lo + per);
+  {
+    uint64_t acc = 0;
+    for (uint64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) acc += __ldcg(weight + k);
+    uint64_t total;
+    block_exclusive_scan(acc, s_warp, total);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = total;
+  }
+  grid.sync();
+  if (blockIdx.x == 0) {   // exclusive scan of the block sums
+    uint64_t carry = 0;
+    for (uint64_t b0 = 0; b0 < gridDim.x; b0 += blockDim.x) {
+      const uint64_t b = b0 + threadIdx.x;
+      const uint64_t x = b < gridDim.x ? __ldcg(bsum + b) : 0;
+      uint64_t total;
+      const uint64_t ex = block_exclusive_scan(x, s_warp, total);
+      if (b < gridDim.x) bsum[b] = carry + ex;
+      carry += total;
+    }
+    if (threadIdx.x == 0) P[m] = carry;
+  }
+  grid.sync();
+  {
+    uint64_t carry = __ldcg(bsum + blockIdx.x);
+    for (uint64_t k0 = lo; k0 < hi; k0 += blockDim.x) {
+      const uint64_t k = k0 + threadIdx.x;
+      const uint64_t x = k < hi ? __ldcg(weight + k) : 0;
+      uint64_t total;
+      const uint64_t ex = block_exclusive_scan(x, s_warp, total);
+      if (k < hi) P[k] = carry + ex;
+      carry += total;
+    }
+  }
+  grid.sync();
+  {   // the chunk plan (k_plan)
+    const ChunkGeom g = chunk_geom(P, m, t_min, max_chunks);
+    for (uint64_t c = tid; c < g.nchunks; c += nthr) {
+      const uint64_t target = c * g.T;
+      uint64_t a = 0, b = m;   // P[a] <= target < P[b]
+      while (b - a > 1) {
+        const uint64_t mid = (a + b) >> 1;
+        if (__ldcg(P + mid) <= target) a = mid; else b = mid;
+      }
+      chunk_first[c] = (uint32_t)a;
+    }
+  }
+  zero_page(zeros);
+  grid.sync();
+  apply_body<kTwoBit>(meta, m, P, chunk_first, counter, t_min, max_chunks, sv, zeros);
 }
 
 // fill shard-relative V bytes [q0, q1) with the byte value `val` (0x00/0xFF)
@@ -2565,9 +2682,9 @@ static cudaError_t plan(const Launch& L, uint64_t n, const Plan& p, cudaStream_t
   return cudaGetLastError();
 }
 
-cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out, const Table& t,
-                         const ShadowView& sv, const Plan& p, uint32_t err_mask, bool fuse, cudaStream_t s) {
-  if (n == 0) return cudaSuccess;
+// a1-a4: prep, plan and the shadow scan
+static void check_front(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out, const Table& t,
+                        const ShadowView& sv, const Plan& p, uint32_t err_mask, bool fuse, cudaStream_t s) {
   const size_t smem = ((size_t)t.nsplit + 1) * sizeof(uint64_t);
   ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
   L.stage(CG_STAGE_CHECK_PREP, true, s);
@@ -2576,8 +2693,7 @@ cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_
   *L.counter += 1;
   L.stage(CG_STAGE_CHECK_PREP, false, s);
   L.stage(CG_STAGE_CHECK_PLAN, true, s);
-  cudaError_t e = plan(L, n, p, s);
-  if (e != cudaSuccess) return e;
+  plan(L, n, p, s);
   L.stage(CG_STAGE_CHECK_PLAN, false, s);
   L.stage(CG_STAGE_CHECK_SCAN, true, s);
   auto scan = !sv.two_bit ? (fuse ? k_check_scan<false, true, false> : k_check_scan<false, false, false>)
@@ -2587,11 +2703,45 @@ cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_
                                                                  p.t_min, p.max_chunks, sv, out, err_mask,
                                                                  fuse ? 1 : 0, p.resid, p.counter + 2);
   L.stage(CG_STAGE_CHECK_SCAN, false, s);
+  *L.counter += 1;
+}
+
+cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out, const Table& t,
+                         const ShadowView& sv, const Plan& p, uint32_t err_mask, bool fuse, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  check_front(L, d, n, out, t, sv, p, err_mask, fuse, s);
+  ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
   L.stage(CG_STAGE_CHECK_FINAL, true, s);
   launch_pdl(k_finalize_split, blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s, 
       n, p.P, p.t_min, p.max_chunks, out, err_mask, meta, fuse ? 1 : 0, p.resid, p.counter + 2);
   L.stage(CG_STAGE_CHECK_FINAL, false, s);
-  *L.counter += 2;
+  *L.counter += 1;
+  return cudaGetLastError();
+}
+
+// cg_check_apply: the fused scan, then k_finish (finalise + residual apply)
+cudaError_t check_apply(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out, const Table& t,
+                        const ShadowView& sv, const Plan& p, uint32_t err_mask, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  check_front(L, d, n, out, t, sv, p, err_mask, true, s);
+  L.stage(CG_STAGE_APPLY, true, s);
+  ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
+  uint64_t* P = p.P;
+  uint64_t t_min = p.t_min, max_chunks = p.max_chunks;
+  uint32_t* resid = p.resid;
+  uint32_t* counter = p.counter;
+  uint64_t* weight = p.weight;
+  uint64_t* bsum = p.fbsum;
+  uint32_t* chunk_first = p.chunk_first;
+  ShadowView svc = sv;
+  void* args[] = {(void*)&d, (void*)&n, (void*)&P, (void*)&t_min, (void*)&max_chunks, (void*)&out, (void*)&err_mask,
+                  (void*)&meta, (void*)&resid, (void*)&counter, (void*)&weight, (void*)&bsum, (void*)&chunk_first,
+                  (void*)&svc};
+  cudaError_t e = cudaLaunchCooperativeKernel(sv.two_bit ? (const void*)k_finish<true> : (const void*)k_finish<false>,
+                                              dim3((unsigned)L.finish_blocks), dim3(kThreads), args, 0, s);
+  L.stage(CG_STAGE_APPLY, false, s);
+  *L.counter += 1;
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -2821,6 +2971,11 @@ int persistent_blocks(int which) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bk, k, kRingWarps * 32, kScanSmem);
       b = std::min(b, bk);
     }
+  } else if (which == 3) {
+    int b2 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_finish<false>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_finish<true>, kThreads, 0);
+    b = std::min(b, b2);
   } else if (which == 1) {
     // the bytes-format instantiation sizes the persistent grid (extra CTAs of
     // the 2-bit one just find the group counter exhausted)

@@ -40,7 +40,7 @@ struct ArrayEntry {   // NEXT-3 device array (SPEC register_array S:166-168)
 };
 
 struct Layout {
-  uint64_t table, arrays, weight, P, bsum, chunk, meta, resid, dvoff, scratch, waves, marks, flags, leaks, desc_stage,
+  uint64_t table, arrays, weight, P, bsum, fbsum, chunk, meta, resid, dvoff, scratch, waves, marks, flags, leaks, desc_stage,
       verdict_stage, raw_stage,
       idx_stage, dirty_stage, dir, total;
   uint32_t dir_bits;
@@ -85,6 +85,7 @@ Layout layout_of(const cg_config* c) {
   L.weight = take(L.max_items * 8);
   L.P = take((L.max_items + 1) * 8);
   L.bsum = take((cgk::scan_blocks(L.max_items) + 1) * 8);
+  L.fbsum = take(cgk::kFinishMaxBlocks * 8);   // k_finish's per-block sums
   L.chunk = take(L.max_chunks * 4);
   L.meta = take(c->max_descs * std::max(cgk::scan_meta_bytes(), cgk::prop_meta_bytes()));
   L.resid = take(c->max_descs * sizeof(uint32_t));
@@ -244,6 +245,7 @@ struct cg_ctx {
     p.weight = d(lay.weight);
     p.P = d(lay.P);
     p.bsum = d(lay.bsum);
+    p.fbsum = d(lay.fbsum);
     p.chunk_first = reinterpret_cast<uint32_t*>(ws + lay.chunk);
     p.meta = ws + lay.meta;
     p.counter = reinterpret_cast<uint32_t*>(ws + lay.flags + 128);
@@ -405,6 +407,8 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
   c->launch.persist_blocks = prop.multiProcessorCount * std::max(cgk::persistent_blocks(1), 1);
   c->launch.scan_blocks = prop.multiProcessorCount * std::max(cgk::persistent_blocks(0), 1);
   c->launch.wave_blocks = prop.multiProcessorCount * std::max(cgk::persistent_blocks(2), 1);
+  c->launch.finish_blocks = std::min(prop.multiProcessorCount * std::max(cgk::persistent_blocks(3), 1),
+                                     (int)cgk::kFinishMaxBlocks);
   c->launch.counter = &c->launches;
   c->prof.mark = &cg_ctx::mark_cb;
   c->prof.self = c;
@@ -1054,9 +1058,7 @@ cg_status cg_check_apply(cg_ctx* c, const cg_copy_desc* d_descs, uint64_t n, cg_
     st = cg_check_copies(c, d_descs, n, d_out, stream);
     return st != CG_OK ? st : cg_apply_copies(c, d_descs, d_out, n, stream);
   }
-  cudaError_t e =
-      cgk::check_copies(c->launch, d_descs, n, d_out, c->dev_table(), c->sv, c->plan(), c->err_mask(), true, s);
-  if (e == cudaSuccess) e = cgk::apply_dtoh(c->launch, d_descs, d_out, n, c->sv, c->plan(), true, s);
+  cudaError_t e = cgk::check_apply(c->launch, d_descs, n, d_out, c->dev_table(), c->sv, c->plan(), c->err_mask(), s);
   c->last_check = nullptr;
   return c->cuda(e, "check+apply kernels");
 }
