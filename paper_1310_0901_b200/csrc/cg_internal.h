@@ -77,6 +77,7 @@ struct Table {
   const uint64_t* split;   // base[k * stride], k < nsplit (16-byte aligned, padded to even)
   const uint64_t* l2;      // base[4 k], k < ceil(n / 4) (64-byte aligned)
   const uint64_t* pool;    // NEXT-1: device V-pool offset of each entry (nullptr without tracking)
+  const uint4* walk;       // per entry 32 B: (prefix max of ends, end, alloc seq, free seq), the lookup walk's reads
   uint64_t n;
   // NEXT-3 device arrays: sorted by (handle, alloc_seq)
   const uint64_t* ahandle;

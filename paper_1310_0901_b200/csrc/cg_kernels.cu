@@ -230,7 +230,9 @@ __device__ __forceinline__ bool table_lookup(const Table& t, const uint64_t* s_s
     }
   }
   for (int64_t j = (int64_t)a; j >= 0; --j) {
-    const uint64_t pm = __ldg(t.pmax + j), e = __ldg(t.end + j), as = __ldg(t.aseq + j), fs = __ldg(t.fseq + j);
+    const uint4 w0 = __ldg(t.walk + 2 * j), w1 = __ldg(t.walk + 2 * j + 1);   // one 32-byte sector
+    const uint64_t pm = ((uint64_t)w0.y << 32) | w0.x, e = ((uint64_t)w0.w << 32) | w0.z;
+    const uint64_t as = ((uint64_t)w1.y << 32) | w1.x, fs = ((uint64_t)w1.w << 32) | w1.z;
     if (pm <= start) break;
     if (e > start && as < seq && seq < fs) {
       end_out = e;

@@ -40,7 +40,7 @@ struct ArrayEntry {   // NEXT-3 device array (SPEC register_array S:166-168)
 };
 
 struct Layout {
-  uint64_t table, arrays, weight, P, bsum, fbsum, chunk, meta, resid, dvoff, scratch, waves, marks, flags, leaks, desc_stage,
+  uint64_t table, walk, arrays, weight, P, bsum, fbsum, chunk, meta, resid, dvoff, scratch, waves, marks, flags, leaks, desc_stage,
       verdict_stage, raw_stage,
       idx_stage, dirty_stage, dir, total;
   uint32_t dir_bits;
@@ -81,6 +81,7 @@ Layout layout_of(const cg_config* c) {
     return o;
   };
   L.table = take(6 * c->max_allocs * 8 + (4096 + 3) * 8 + (c->max_allocs / 4 + 16) * 8);   // SoA (+ pool offsets) + splitters + every 4th base
+  L.walk = take(4 * c->max_allocs * 8);                      // (prefix max, end, alloc seq, free seq) per entry
   L.arrays = take(4 * c->max_allocs * 8);                    // NEXT-3 array table (SoA)
   L.weight = take(L.max_items * 8);
   L.P = take((L.max_items + 1) * 8);
@@ -190,6 +191,7 @@ struct cg_ctx {
   // pinned staging
   uint64_t* h_table = nullptr;              // 10 * max_allocs + splitters
   cg_mark* h_marks = nullptr;               // kMarkRun
+  uint64_t* h_walk = nullptr;               // 4 * max_allocs: the lookup walk's records before upload
   cudaEvent_t staged = nullptr;
   cudaStream_t copy_stream = nullptr;        // host -> device uploads of cg_check_host
   cudaStream_t out_stream = nullptr;         // device -> host dirty-verdict downloads (cg_check_host_wait)
@@ -266,6 +268,7 @@ struct cg_ctx {
     t.fseq = b + 3 * cap;
     t.pmax = b + 4 * cap;
     t.pool = cfg.dev_vbuf ? b + 5 * cap : nullptr;
+    t.walk = reinterpret_cast<const uint4*>(d(lay.walk));
     t.split = b + ((6 * cap + 1) & ~1ull);   // 16-byte aligned
     t.l2 = b + l2_offset(cap);
     t.n = table.size();
@@ -298,6 +301,10 @@ struct cg_ctx {
         pm = std::max(pm, x.end);
         h_table[4 * cap + i] = pm;
         h_table[5 * cap + i] = x.pool;
+        h_walk[4 * i] = pm;
+        h_walk[4 * i + 1] = x.end;
+        h_walk[4 * i + 2] = x.aseq;
+        h_walk[4 * i + 3] = x.fseq;
       }
       const uint64_t stride = split_stride(n), nsplit = (n + stride - 1) / stride;
       const uint64_t so = (6 * cap + 1) & ~1ull;
@@ -310,6 +317,8 @@ struct cg_ctx {
         e = cudaMemcpyAsync(dt + k * cap, h_table + k * cap, n * 8, cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) return cuda(e, "table upload");
       }
+      e = cudaMemcpyAsync(d(lay.walk), h_walk, n * 32, cudaMemcpyHostToDevice, s);
+      if (e != cudaSuccess) return cuda(e, "walk upload");
       e = cudaMemcpyAsync(dt + so, h_table + so, (nsplit + 1) * 8, cudaMemcpyHostToDevice, s);
       if (e == cudaSuccess)
         e = cudaMemcpyAsync(dt + l2_offset(cap), h_table + hl2, nl2 * 8, cudaMemcpyHostToDevice, s);
@@ -415,6 +424,7 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
   c->launch.prof = &c->prof;
   if (cudaMallocHost(&c->h_table, 10 * cfg->max_allocs * 8 + (4096 + 5) * 8 + (cfg->max_allocs / 4 + 16) * 8) != cudaSuccess ||
       cudaMallocHost(&c->h_marks, std::min<uint64_t>(cfg->max_descs, kMarkRun) * sizeof(cg_mark)) != cudaSuccess ||
+      cudaMallocHost(&c->h_walk, 4 * cfg->max_allocs * sizeof(uint64_t)) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->staged, cudaEventDisableTiming) != cudaSuccess) {
     cg_ctx_destroy(c);
     return CG_ERR_OUT_OF_MEMORY;
@@ -473,6 +483,7 @@ cg_status cg_ctx_destroy(cg_ctx* c) {
   for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
   if (c->h_table) cudaFreeHost(c->h_table);
   if (c->h_marks) cudaFreeHost(c->h_marks);
+  if (c->h_walk) cudaFreeHost(c->h_walk);
   delete c;
   return CG_OK;
 }
