@@ -278,17 +278,13 @@ __device__ __forceinline__ uint64_t check_host_units(const Norm& nm, bool two_bi
   return nm.skind == CG_HTOD ? nm.nbytes : (nm.nbytes + 7) >> 3;
 }
 
-__global__ void __launch_bounds__(kThreads) k_check_prep(const cg_copy_desc* __restrict__ descs,
-                                                         uint64_t n, Table t, cg_verdict* __restrict__ out,
-                                                         uint64_t* __restrict__ weight,
-                                                         ScanMeta* __restrict__ meta,
-                                                         uint64_t* __restrict__ dvoff, int two_bit,
-                                                         uint32_t* __restrict__ counter) {
-  pdl_entry();
+__device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs, uint64_t n, const Table& t,
+                                          cg_verdict* __restrict__ out, uint64_t* __restrict__ weight,
+                                          ScanMeta* __restrict__ meta, uint64_t* __restrict__ dvoff, int two_bit,
+                                          uint32_t* __restrict__ counter, uint64_t* s_split) {
   // the scan's group counter, (apply count), residual count: reset here
   // instead of by a memset node, which would break the PDL chain
   if (blockIdx.x == 0 && threadIdx.x < 3) counter[threadIdx.x] = 0;
-  extern __shared__ uint64_t s_split[];
   load_splitters(t, s_split);
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
@@ -363,6 +359,17 @@ __global__ void __launch_bounds__(kThreads) k_check_prep(const cg_copy_desc* __r
              ((uint64_t)raw << 44) | ((uint64_t)flags << 48);
     meta[i] = m;
   }
+}
+
+__global__ void __launch_bounds__(kThreads) k_check_prep(const cg_copy_desc* __restrict__ descs,
+                                                         uint64_t n, Table t, cg_verdict* __restrict__ out,
+                                                         uint64_t* __restrict__ weight,
+                                                         ScanMeta* __restrict__ meta,
+                                                         uint64_t* __restrict__ dvoff, int two_bit,
+                                                         uint32_t* __restrict__ counter) {
+  pdl_entry();
+  extern __shared__ uint64_t s_split[];
+  prep_body(descs, n, t, out, weight, meta, dvoff, two_bit, counter, s_split);
 }
 
 // ---------------------------------------------------------------------------
@@ -515,6 +522,71 @@ __global__ void __launch_bounds__(kThreads) k_plan(const uint64_t* __restrict__ 
       if (__ldg(P + mid) <= target) lo = mid; else hi = mid;
     }
     chunk_first[c] = (uint32_t)lo;
+  }
+}
+
+// a1-a3 + a2 in one cooperative launch: the prep (k_check_prep), then the
+// exclusive prefix sum of the weights and the chunk map with grid barriers
+// between the phases (k_scan_reduce / _top / _down, k_plan): one launch and
+// four barriers instead of five launches.
+__global__ void __launch_bounds__(kThreads) k_front(const cg_copy_desc* __restrict__ descs, uint64_t n, Table t,
+                                                    cg_verdict* __restrict__ out, uint64_t* __restrict__ weight,
+                                                    ScanMeta* __restrict__ meta, uint64_t* __restrict__ dvoff,
+                                                    int two_bit, uint32_t* __restrict__ counter, uint64_t* P,
+                                                    uint64_t* __restrict__ bsum, uint64_t t_min, uint64_t max_chunks,
+                                                    uint32_t* __restrict__ chunk_first) {
+  pdl_entry();
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  extern __shared__ uint64_t s_split[];
+  __shared__ uint64_t s_warp[33];
+  prep_body(descs, n, t, out, weight, meta, dvoff, two_bit, counter, s_split);
+  grid.sync();
+  // block b owns items [b*per, (b+1)*per)
+  const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const uint64_t lo = umin64(n, (uint64_t)blockIdx.x * per), hi = umin64(n, lo + per);
+  {
+    uint64_t acc = 0;
+    for (uint64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) acc += __ldcg(weight + k);
+    uint64_t total;
+    block_exclusive_scan(acc, s_warp, total);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = total;
+  }
+  grid.sync();
+  if (blockIdx.x == 0) {
+    uint64_t carry = 0;
+    for (uint64_t b0 = 0; b0 < gridDim.x; b0 += blockDim.x) {
+      const uint64_t b = b0 + threadIdx.x;
+      const uint64_t x = b < gridDim.x ? __ldcg(bsum + b) : 0;
+      uint64_t total;
+      const uint64_t ex = block_exclusive_scan(x, s_warp, total);
+      if (b < gridDim.x) bsum[b] = carry + ex;
+      carry += total;
+    }
+    if (threadIdx.x == 0) P[n] = carry;
+  }
+  grid.sync();
+  {
+    uint64_t carry = __ldcg(bsum + blockIdx.x);
+    for (uint64_t k0 = lo; k0 < hi; k0 += blockDim.x) {
+      const uint64_t k = k0 + threadIdx.x;
+      const uint64_t x = k < hi ? __ldcg(weight + k) : 0;
+      uint64_t total;
+      const uint64_t ex = block_exclusive_scan(x, s_warp, total);
+      if (k < hi) P[k] = carry + ex;
+      carry += total;
+    }
+  }
+  grid.sync();
+  const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
+  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < g.nchunks;
+       c += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t target = c * g.T;
+    uint64_t a = 0, b = n;   // P[a] <= target < P[b]
+    while (b - a > 1) {
+      const uint64_t mid = (a + b) >> 1;
+      if (__ldcg(P + mid) <= target) a = mid; else b = mid;
+    }
+    chunk_first[c] = (uint32_t)a;
   }
 }
 
@@ -2690,13 +2762,31 @@ static void check_front(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_v
   const size_t smem = ((size_t)t.nsplit + 1) * sizeof(uint64_t);
   ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
   L.stage(CG_STAGE_CHECK_PREP, true, s);
-  launch_pdl(k_check_prep, blocks_for(n, kThreads, L.num_sms * 4), kThreads, smem, s, d, n, t, out, p.weight, meta,
-                                                                              p.dvoff, (int)sv.two_bit, p.counter);
-  *L.counter += 1;
-  L.stage(CG_STAGE_CHECK_PREP, false, s);
-  L.stage(CG_STAGE_CHECK_PLAN, true, s);
-  plan(L, n, p, s);
-  L.stage(CG_STAGE_CHECK_PLAN, false, s);
+  if (L.front_blocks > 0 && smem <= kFrontSmem) {   // prep + plan in one cooperative launch
+    const Table tc = t;
+    int two_bit = (int)sv.two_bit;
+    uint64_t* weight = p.weight;
+    uint64_t* dvoff = p.dvoff;
+    uint32_t* counter = p.counter;
+    uint64_t* P = p.P;
+    uint64_t* bsum = p.fbsum;
+    uint64_t t_min = p.t_min, max_chunks = p.max_chunks;
+    uint32_t* chunk_first = p.chunk_first;
+    void* args[] = {(void*)&d, (void*)&n, (void*)&tc, (void*)&out, (void*)&weight, (void*)&meta, (void*)&dvoff,
+                    (void*)&two_bit, (void*)&counter, (void*)&P, (void*)&bsum, (void*)&t_min, (void*)&max_chunks,
+                    (void*)&chunk_first};
+    cudaLaunchCooperativeKernel((const void*)k_front, dim3((unsigned)L.front_blocks), dim3(kThreads), args, smem, s);
+    *L.counter += 1;
+    L.stage(CG_STAGE_CHECK_PREP, false, s);
+  } else {
+    launch_pdl(k_check_prep, blocks_for(n, kThreads, L.num_sms * 4), kThreads, smem, s, d, n, t, out, p.weight, meta,
+               p.dvoff, (int)sv.two_bit, p.counter);
+    *L.counter += 1;
+    L.stage(CG_STAGE_CHECK_PREP, false, s);
+    L.stage(CG_STAGE_CHECK_PLAN, true, s);
+    plan(L, n, p, s);
+    L.stage(CG_STAGE_CHECK_PLAN, false, s);
+  }
   L.stage(CG_STAGE_CHECK_SCAN, true, s);
   auto scan = !sv.two_bit ? (fuse ? k_check_scan<false, true, false> : k_check_scan<false, false, false>)
               : sv.sparse ? (fuse ? k_check_scan<true, true, true> : k_check_scan<true, false, true>)
@@ -2973,6 +3063,9 @@ int persistent_blocks(int which) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bk, k, kRingWarps * 32, kScanSmem);
       b = std::min(b, bk);
     }
+  } else if (which == 4) {   // k_front with the largest splitter array (4097 words)
+    cudaFuncSetAttribute(k_front, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFrontSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_front, kThreads, kFrontSmem);
   } else if (which == 3) {
     int b2 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_finish<false>, kThreads, 0);
