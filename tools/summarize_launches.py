@@ -5,13 +5,13 @@ import csv
 import sys
 
 
-def main(path, out=None, first="k_check_prep"):
+def main(path, out=None, first=("k_front", "k_check_prep")):
     """Only launches from the first `first` kernel on (the bench steps; the
     setup kernels before it -- fresh shadow, host marks, V-byte checks -- are
     excluded)."""
     rows = [r for r in csv.DictReader(l for l in open(path) if l.startswith('"'))
             if r.get("Metric Name") == "gpu__time_duration.sum"]
-    start = next((i for i, r in enumerate(rows) if first in r["Kernel Name"]), 0)
+    start = next((i for i, r in enumerate(rows) if any(f in r["Kernel Name"] for f in first)), 0)
     rows = rows[start:]
     agg = collections.OrderedDict()
     for r in rows:
