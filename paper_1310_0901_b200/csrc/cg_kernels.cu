@@ -23,7 +23,9 @@
 //          for non-identity partials): flags + status.
 //   a6     k_apply_prep + plan + k_apply   V := 0 over DtoH ranges with
 //                           status OK (BASELINE north_star (3)).
-//   a8     k_live + scan + k_leak_scatter (abstract P:12).
+//   a8     k_leak: one cooperative launch (per-slice live counts, grid barrier,
+//          compaction in base order); CG_LEAK_COOP=0: k_live + scan +
+//          k_leak_scatter (abstract P:12).
 // Plumbing (setup, untimed): k_fill (fresh shadow), k_mark (S:45-62,
 // S:355-363), k_setv_check.
 //
@@ -2714,6 +2716,47 @@ __global__ void __launch_bounds__(kThreads) k_leak_scatter(Table t, const uint64
   if (blockIdx.x == 0 && threadIdx.x == 0) *count = P[t.n];
 }
 
+// The whole sweep in one cooperative launch: block b counts the live entries of
+// its contiguous slice [lo, hi), one grid barrier, then b's output offset is the
+// sum of the counts of blocks < b and the slice is compacted in base order
+// (k_live + prefix sum + k_leak_scatter without the 4 intermediate launches).
+__global__ void __launch_bounds__(kThreads) k_leak(Table t, uint64_t* __restrict__ bsum,
+                                                   cg_alloc_record* __restrict__ out, uint64_t cap,
+                                                   uint64_t* __restrict__ count) {
+  pdl_entry();
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  __shared__ uint64_t s_warp[33];
+  const uint64_t n = t.n;
+  const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const uint64_t lo = umin64(n, (uint64_t)blockIdx.x * per), hi = umin64(n, lo + per);
+  uint64_t total;
+  {
+    uint64_t acc = 0;
+    for (uint64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) acc += t.fseq[k] == kInf ? 1 : 0;
+    block_exclusive_scan(acc, s_warp, total);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = total;
+  }
+  grid.sync();
+  uint64_t part = 0;
+  for (uint32_t j = threadIdx.x; j < blockIdx.x; j += blockDim.x) part += __ldcg(bsum + j);
+  block_exclusive_scan(part, s_warp, total);
+  uint64_t carry = total;
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *count = carry + __ldcg(bsum + blockIdx.x);
+  for (uint64_t k0 = lo; k0 < hi; k0 += blockDim.x) {
+    const uint64_t k = k0 + threadIdx.x;
+    const bool live = k < hi && t.fseq[k] == kInf;
+    const uint64_t ex = block_exclusive_scan(live ? 1 : 0, s_warp, total);
+    if (live && carry + ex < cap) {
+      cg_alloc_record r;
+      r.base = t.base[k];
+      r.size = t.end[k] - t.base[k];
+      r.alloc_seq = t.aseq[k];
+      out[carry + ex] = r;
+    }
+    carry += total;
+  }
+}
+
 inline int blocks_for(uint64_t n, int threads, int cap) {
   uint64_t b = (n + threads - 1) / threads;
   if (b < 1) b = 1;
@@ -2912,6 +2955,18 @@ cudaError_t leak_sweep(const Launch& L, const Table& t, const Plan& p, cg_alloc_
                        uint64_t* d_count, cudaStream_t s) {
   if (t.n == 0) return cudaMemsetAsync(d_count, 0, sizeof(uint64_t), s);
   L.stage(CG_STAGE_LEAK, true, s);
+  if (L.leak_blocks > 0) {   // one cooperative launch
+    Table tc = t;
+    uint64_t* bsum = p.fbsum;
+    void* args[] = {(void*)&tc, (void*)&bsum, (void*)&out, (void*)&cap, (void*)&d_count};
+    const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)L.leak_blocks,
+                                                                          (t.n + kThreads - 1) / kThreads));
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_leak, dim3(g), dim3(kThreads), args, 0, s);
+    L.stage(CG_STAGE_LEAK, false, s);
+    *L.counter += 1;
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+  }
   launch_pdl(k_live, blocks_for(t.n, kThreads, L.num_sms * 8), kThreads, 0, s, t, p.weight);
   const uint64_t nb = scan_blocks(t.n);
   launch_pdl(k_scan_reduce, (unsigned)nb, kScanThreads, 0, s, p.weight, t.n, p.bsum, nullptr);
@@ -3066,6 +3121,8 @@ int persistent_blocks(int which) {
   } else if (which == 4) {   // k_front with the largest splitter array (4097 words)
     cudaFuncSetAttribute(k_front, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFrontSmem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_front, kThreads, kFrontSmem);
+  } else if (which == 5) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_leak, kThreads, 0);
   } else if (which == 3) {
     int b2 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_finish<false>, kThreads, 0);

@@ -221,6 +221,32 @@ def test_leak_sweep_device(cg):
     chk.close()
 
 
+@pytest.mark.parametrize("coop", ["1", "0"])
+@pytest.mark.parametrize("cap_frac", [1.0, 0.37])
+def test_leak_sweep_device_large_capped(cg, monkeypatch, coop, cap_frac):
+    """a8 on a 100k-entry table (many grid slices), the cooperative one-launch
+    sweep (CG_LEAK_COOP=1) and the 5-launch one: the count is the full k, the
+    first min(cap, k) records in base order equal the oracle's."""
+    import torch
+    monkeypatch.setenv("CG_LEAK_COOP", coop)
+    tr = tg.c2_small(n_copies=2000, n_allocs=100000)
+    o, _, _, oleaks = oracle.replay_trace(tr)
+    chk = new_checker(cg, tr)
+    cg.replay_events(chk, tr.events, tr.blob)
+    k = len(oleaks)
+    cap = max(1, int(k * cap_frac))
+    out = torch.full((k * 24,), 0xAB, dtype=torch.uint8, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    chk.leak_sweep(out, cap, cnt)
+    torch.cuda.synchronize()
+    rec = out.cpu().numpy().view(cg.ALLOC_RECORD_DTYPE)
+    assert int(cnt.item()) == k
+    assert np.array_equal(rec["base"][:cap], oleaks["base"][:cap])
+    assert np.array_equal(rec["alloc_seq"][:cap], oleaks["seq"][:cap])
+    assert np.all(out.cpu().numpy()[cap * 24:] == 0xAB)   # nothing written past cap
+    chk.close()
+
+
 @pytest.mark.parametrize("fmt", ["1d", "2d"])
 def test_check_host_compact_chunked(cg, fmt):
     """cg_check_host: 600k host descriptors (4 pipelined chunks), dirty-only
