@@ -318,6 +318,47 @@ int or_device_vbits(const or_state *st, uint64_t x, uint64_t len, uint8_t *out) 
     return 1;
 }
 
+/* (iii) the host-side scan of one copy: every logical byte o = r*W + c
+ * (row-major, R-11) at address x = start + r*pitch + c, in increasing o.
+ * first_unaddr = the first o whose byte is not addressable (outside the window
+ * counts as unaddressable, R-15); if `defined` is asked (HtoD), first_undef /
+ * undef_count over the addressable bytes with a nonzero V-byte (R-1, R-3).
+ * The loop visits o in increasing order, so once first_unaddr is set a byte
+ * outside the window can change nothing (it is not counted as undefined and
+ * cannot lower first_unaddr): such bytes are skipped -- the rest of a row past
+ * the window end, the part of a row before the window start, whole rows before
+ * the window, and (pitch > 0, so rows only move up) every row from the first
+ * one that starts at or past the window end.  This keeps copies of any size
+ * (R-10 allows up to 2^64-1 logical bytes) bounded by the window. */
+static void host_scan(const or_state *st, uint64_t start, uint64_t pitch, uint64_t W, uint64_t H,
+                      int defined, or_verdict *v) {
+    const uint64_t wend = st->h0 + st->s;
+    for (uint64_t r = 0; r < H && W; r++) {
+        const uint64_t xr = start + r * pitch;
+        if (v->first_unaddr != OR_NONE) {
+            if (pitch > 0 && xr >= wend) break;
+            if (pitch > 0 && xr + W <= st->h0) {       /* rows r .. r+k end before the window */
+                r += (st->h0 - xr - W) / pitch;
+                continue;
+            }
+        }
+        for (uint64_t c = 0; c < W; c++) {
+            const uint64_t x = xr + c, o = r * W + c;
+            if (!in_window(st, x) && v->first_unaddr != OR_NONE) {
+                if (x >= wend) break;                   /* the rest of the row is further out */
+                c = st->h0 - xr - 1;                    /* continue at the window start */
+                continue;
+            }
+            if (!addressable(st, x)) {
+                if (v->first_unaddr == OR_NONE) v->first_unaddr = o;
+            } else if (defined && st->V[x - st->h0] != 0) {
+                if (v->first_undef == OR_NONE) v->first_undef = o;
+                v->undef_count++;
+            }
+        }
+    }
+}
+
 /* NEXT-3 check_array_transfer: the array side is (handle, byte
  * offset) = (dst, dst_x) for HtoA and (src, src_x) for AtoH; the array holds
  * the W*H logical bytes contiguously from the offset.  Unknown handle ->
@@ -334,7 +375,7 @@ static void check_array_copy(or_state *st, const or_event *ev, or_verdict *v) {
     uint64_t hs = 0, hspan = 0;
     const int hok = side_range(hb, hx, hy, hp, W, H, &hs, &hspan);
     const unsigned __int128 nb = (unsigned __int128)W * H;
-    const int nbytes_ok = nb <= ((unsigned __int128)1 << 38);
+    const int nbytes_ok = nb <= (unsigned __int128)UINT64_MAX;       /* R-10: logical bytes fit 64 bits */
     const int aok = (unsigned __int128)off + nb <= (unsigned __int128)UINT64_MAX;
     if (!hok || !nbytes_ok || !aok) v->flags |= F_INVALID_RANGE;
     if (aok && nbytes_ok) {
@@ -351,18 +392,7 @@ static void check_array_copy(or_state *st, const or_event *ev, or_verdict *v) {
         }
         if (!found) v->flags |= htoa ? F_DST_NOT_ALLOCATED : F_SRC_NOT_ALLOCATED;
     }
-    if (hok && nbytes_ok) {
-        for (uint64_t r = 0; r < H && W; r++)
-            for (uint64_t c = 0; c < W; c++) {
-                const uint64_t x = hs + r * hp + c, o = r * W + c;
-                if (!addressable(st, x)) {
-                    if (v->first_unaddr == OR_NONE) v->first_unaddr = o;
-                } else if (htoa && st->V[x - st->h0] != 0) {
-                    if (v->first_undef == OR_NONE) v->first_undef = o;
-                    v->undef_count++;
-                }
-            }
-    }
+    if (hok && nbytes_ok) host_scan(st, hs, hp, W, H, htoa, v);
     if (v->first_unaddr != OR_NONE) v->flags |= F_HOST_UNADDRESSABLE;
     if (v->undef_count > 0 && v->first_unaddr == OR_NONE) v->flags |= F_HOST_UNDEFINED;
     const uint32_t errors = v->flags & ~(st->undef_is_error ? 0u : F_HOST_UNDEFINED);
@@ -391,9 +421,10 @@ void or_check_copy(or_state *st, const or_event *ev, or_verdict *v) {
     uint64_t ds = 0, dspan = 0, ss = 0, sspan = 0;
     int dok = side_range(ev->dst, ev->dst_x, ev->dst_y, ev->dst_pitch, W, H, &ds, &dspan);
     int sok = side_range(ev->src, ev->src_x, ev->src_y, ev->src_pitch, W, H, &ss, &sspan);
-    /* R-10: a copy moving more than 2^38 bytes (256 GiB, more than any B200 or
-     * host window here holds) is an invalid range as well */
-    int nbytes_ok = ((unsigned __int128)W * H <= ((unsigned __int128)1 << 38));
+    /* R-10 ("InvalidRange on overflow"): a side whose
+     * start + span, or a copy whose logical byte count W*H (the offsets
+     * reported below), does not fit in 64 bits is an invalid range */
+    int nbytes_ok = ((unsigned __int128)W * H <= (unsigned __int128)UINT64_MAX);
     if (!dok || !sok || !nbytes_ok) v->flags |= F_INVALID_RANGE;
 
     /* (ii) device endpoints, dst then src */
@@ -409,19 +440,7 @@ void or_check_copy(or_state *st, const or_event *ev, or_verdict *v) {
     if ((kind == OR_HTOD && sok && nbytes_ok) || (kind == OR_DTOH && dok && nbytes_ok)) {
         uint64_t hstart = (kind == OR_HTOD) ? ss : ds;
         uint64_t hpitch = (kind == OR_HTOD) ? ev->src_pitch : ev->dst_pitch;
-        for (uint64_t r = 0; r < H && W; r++) {
-            for (uint64_t c = 0; c < W; c++) {
-                uint64_t x = hstart + r * hpitch + c;
-                uint64_t o = r * W + c;
-                int ad = addressable(st, x);
-                if (!ad) {
-                    if (v->first_unaddr == OR_NONE) v->first_unaddr = o;
-                } else if (kind == OR_HTOD && st->V[x - st->h0] != 0) {   /* R-1, R-3 */
-                    if (v->first_undef == OR_NONE) v->first_undef = o;
-                    v->undef_count++;
-                }
-            }
-        }
+        host_scan(st, hstart, hpitch, W, H, kind == OR_HTOD, v);
     }
     /* (iv) flags and status (R-4, R-8) */
     if (v->first_unaddr != OR_NONE) v->flags |= F_HOST_UNADDRESSABLE;

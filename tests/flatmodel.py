@@ -164,7 +164,7 @@ class FlatModel:
         start = base + y * pitch + x
         span = 0 if (w == 0 or h == 0) else (h - 1) * pitch + w
         nb = w * h
-        hok, nbok, aok = start + span <= U64, nb <= (1 << 38), off + nb <= U64
+        hok, nbok, aok = start + span <= U64, nb <= U64, off + nb <= U64   # R-10: overflow only
         if not (hok and nbok and aok):
             out["flags"] |= FLAG["INVALID_RANGE"]
         P = "DST" if htoa else "SRC"
@@ -226,7 +226,7 @@ class FlatModel:
             start = base + y * pitch + x
             span = 0 if (w == 0 or h == 0) else (h - 1) * pitch + w
             sides[p] = (start, span, pitch, start + span <= U64)
-        bytes_ok = w * h <= (1 << 38)          # R-10
+        bytes_ok = w * h <= U64               # R-10: overflow only
         if not (sides["dst"][3] and sides["src"][3] and bytes_ok):
             out["flags"] |= FLAG["INVALID_RANGE"]
         dev = {1: ["dst"], 2: ["src"], 3: ["dst", "src"]}[kind]

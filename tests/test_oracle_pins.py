@@ -296,3 +296,99 @@ def test_c4_injection_classes():
     assert np.all(f[inj == 1] == F_HOST_UNADDRESSABLE)            # column overrun into padding
     assert np.all(f[inj == 2] & F_BAD_PITCH)                      # X+W > pitch
     assert np.all((f[inj == 3] == F_DST_TOO_SMALL) | (f[inj == 3] == F_SRC_TOO_SMALL))
+
+
+# --------------------------------------------------------------------------
+# R-10: no size cap -- INVALID_RANGE only on 64-bit overflow ("arithmetic
+# overflow of start+len -> InvalidRange"); bytes outside the
+# window are unaddressable (R-15), so check_addressable's "lowest
+# offending byte offset" of a copy running past the window end is the
+# offset of the window end.  Every expected value below is derived by hand.
+# --------------------------------------------------------------------------
+def test_huge_copies_hand_derived():
+    tr = tg.huge_copies()
+    o, v, s, leaks = oracle.replay_trace(tr)
+    H0, S = tr.host_base, tr.host_size                  # 1 MiB, 4 MiB
+    start = tr.meta["start"]                            # H0 + 4096
+    to_end = H0 + S - start                             # 4 MiB - 4096 = 4190208 bytes left in the window
+    assert to_end == 4190208
+    # the five undefined bytes sit at start + d, d in HUGE_D (all < to_end)
+    assert all(d < to_end for d in tg.HUGE_D)
+    names = list(tr.meta["copies"])
+    V = {k: v[i] for i, k in enumerate(names)}
+    for k in names:                                     # no copy is an INVALID_RANGE except the overflow one
+        assert bool(V[k]["flags"] & F_INVALID_RANGE) == (k == "overflow"), k
+    # 1D, W*H = 2^38+1 and 2^40: every byte from start to the window end is
+    # addressable, the first one past it is not -> first_unaddr = to_end;
+    # the 5 undefined bytes are all before it (R-4: raw count reported, but
+    # HOST_UNDEFINED only when first_unaddr is NONE)
+    for k in ("1d_2^38+1", "1d_2^40"):
+        assert V[k]["first_unaddr"] == 4190208
+        assert (V[k]["first_undef"], V[k]["undef_count"]) == (100, 5)
+        assert V[k]["flags"] == F_HOST_UNADDRESSABLE and V[k]["status"] == 1
+    # 2D, W = 525313, H = 523265 (W*H = 2^38+1), pitch 528384: row r covers
+    # start + [528384 r, 528384 r + 525313).  Row 7 starts at 3698688 < 4190208
+    # and ends at 4224001 > 4190208, rows 0..6 end before the window end; so the
+    # first unaddressable logical offset is 7*525313 + (4190208 - 3698688) =
+    # 3677191 + 491520 = 4168711.  Undefined bytes: d=100 (row 0, o=100),
+    # d=525318 (between rows 0 and 1: pitch padding, not a logical byte),
+    # d=1056778 (row 2 col 10, o=1050636), d=2000000 (row 3 col 414848,
+    # o=1990787), d=3698788 (row 7 col 100, o=3677291) -> 4 bytes, first 100.
+    assert V["2d_2^38+1"]["first_unaddr"] == 7 * 525313 + (4190208 - 7 * 528384) == 4168711
+    assert (V["2d_2^38+1"]["first_undef"], V["2d_2^38+1"]["undef_count"]) == (100, 4)
+    # 2D, W = H = 2^20, pitch 2^20 + 2^16 = 1114112: row 3 starts at 3342336
+    # and ends at 4390912 > 4190208 (row 2 ends at 3276800), so first_unaddr =
+    # 3*2^20 + (4190208 - 3342336) = 3145728 + 847872 = 3993600.  Undefined:
+    # d=100 (row 0), d=525318 (row 0), d=1056778 (padding [1048576, 1114112)),
+    # d=2000000 (row 1), d=3698788 (row 3 col 356452, before the window end).
+    assert V["2d_2^40"]["first_unaddr"] == 3 * (1 << 20) + (4190208 - 3 * 1114112) == 3993600
+    assert (V["2d_2^40"]["first_undef"], V["2d_2^40"]["undef_count"]) == (100, 4)
+    # host start 4 KiB before the window: offset 0 is unaddressable; the raw
+    # undefined count covers the whole window: offsets shift by 8192
+    assert V["1d_before"]["first_unaddr"] == 0
+    assert (V["1d_before"]["first_undef"], V["1d_before"]["undef_count"]) == (100 + 8192, 5)
+    # DtoH: A-bits only (R-6); the error means no apply (R-7): V keeps the 5 undefined bytes
+    assert V["dtoh_1d_2^40"]["first_unaddr"] == 4190208 and V["dtoh_2d_2^40"]["first_unaddr"] == 3993600
+    for k in ("dtoh_1d_2^40", "dtoh_2d_2^40"):
+        assert V[k]["first_undef"] == NONE and V[k]["undef_count"] == 0 and V[k]["status"] == 1
+    assert int(np.count_nonzero(o.V)) == 5
+    # W*H = 2^65 does not fit 64 bits (the spans do: pitch 0) -> INVALID_RANGE,
+    # BAD_PITCH (0 < W); the host side is not scanned
+    assert V["overflow"]["flags"] == F_INVALID_RANGE | F_BAD_PITCH
+    assert V["overflow"]["first_unaddr"] == NONE and V["overflow"]["undef_count"] == 0
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_overlapping_rows_multiplicity(seed):
+    """BAD_PITCH rows that overlap (pitch < W, R-12): the oracle loops over the
+    W*H logical bytes row by row.  An independent derivation over PHYSICAL
+    bytes u = x - start: u lies in rows r_lo(u)..r_hi(u), r_lo = 0 if u < W
+    else (u - W) // pitch + 1, r_hi = min(H - 1, u // pitch); its first logical
+    offset is u + r_lo (W - pitch), which grows with u, so first_unaddr /
+    first_undef are those of the first bad physical byte and undef_count is
+    the sum of the row counts of the undefined physical bytes.  pitch 0: every
+    row is the same W bytes -> count = H * (undefined bytes of the row)."""
+    W, pitch, H = [(4096, 64, 20000), (1000, 999, 3000), (64, 1, 50000), (4096, 0, 5000)][seed]
+    tr = tg.overlap_rows(seed, W=W, pitch=pitch, H=H)
+    o, v, s, _ = oracle.replay_trace(tr)
+    start, h0 = tr.meta["start"], tr.host_base
+    span = (H - 1) * pitch + W
+    A = np.unpackbits(o.A, bitorder="little").astype(bool)
+    ok = A[start - h0:start - h0 + span]
+    und = ok & (o.V[start - h0:start - h0 + span] != 0)
+    u = np.arange(span, dtype=np.int64)
+    if pitch:
+        r_lo = np.where(u < W, 0, (u - W) // pitch + 1)
+        r_hi = np.minimum(H - 1, u // pitch)
+    else:
+        r_lo, r_hi = np.zeros(span, np.int64), np.full(span, H - 1)
+    first_o = u + r_lo * (W - pitch)
+    assert np.all(np.diff(first_o) > 0)
+    exp_cnt = int(np.sum((r_hi - r_lo + 1)[und]))
+    exp_fd = int(first_o[und][0]) if und.any() else NONE
+    exp_fu = int(first_o[~ok][0]) if (~ok).any() else NONE
+    assert (v[0]["first_unaddr"], v[0]["first_undef"], v[0]["undef_count"]) == (exp_fu, exp_fd, exp_cnt)
+    assert v[0]["flags"] & F_BAD_PITCH and v[0]["status"] == 1
+    # pitch 0: H copies of row 0 = the first W physical bytes
+    row = ok[:W] & (o.V[start - h0:start - h0 + W] != 0)
+    assert v[1]["undef_count"] == H * int(np.count_nonzero(row))

@@ -899,3 +899,67 @@ def sparse_regions(seed: int = 0, n_regions: int = 6, region: int = 256 * KiB, n
     sparse = Trace(dense.name + "_sparse", ev, dense.blob, bases[0] & ~0xFFFF, region, dict(dense.meta),
                    dense.threads)
     return dense, sparse, bases, region
+
+
+# ---------------------------------------------------------------------------
+# R-10: copies larger than any window (no size cap: INVALID_RANGE only on
+# 64-bit overflow, S:49 / S:58 / S:65)
+# ---------------------------------------------------------------------------
+HUGE_D = (100, 525318, 1056778, 2000000, 3698788)   # undefined bytes: offsets from HUGE_START
+
+
+def huge_copies() -> Trace:
+    """A 4 MiB window, fully DEFINED except five undefined bytes at
+    HUGE_START + d (d in HUGE_D), one 2 TiB device allocation, and copies of
+    2^38 + 1 and 2^40 logical bytes (1D and pitched 2D) whose host side starts
+    inside the window (or 4 KiB before it), plus one whose W*H overflows 64
+    bits.  The expected verdicts are derived by hand in
+    tests/test_oracle_pins.py::test_huge_copies_hand_derived."""
+    H0, S = 1 << 20, 4 * MiB
+    tb = TraceBuilder("huge", H0, S)
+    start = H0 + 4096
+    tb.mark(H0, S, DEFINED)
+    for k, d in enumerate(HUGE_D):
+        tb.setv(start + d, bytes([0x01 << k]))
+    dev = 1 << 44
+    tb.register(dev, 1 << 41)
+    wa, ha, pa = 525313, 523265, 528384                 # 2^38 + 1 = 525313 * 523265, pitch > W
+    wb, hb, pb = 1 << 20, 1 << 20, (1 << 20) + (1 << 16)   # 2^40
+    c = {}
+    c["1d_2^38+1"] = tb.copy1d(HTOD, dev, start, (1 << 38) + 1)
+    c["1d_2^40"] = tb.copy1d(HTOD, dev, start, 1 << 40)
+    c["2d_2^38+1"] = tb.copy2d(HTOD, wa, ha, dev, 0, 0, wa, start, 0, 0, pa)
+    c["2d_2^40"] = tb.copy2d(HTOD, wb, hb, dev, 0, 0, wb, start, 0, 0, pb)
+    c["1d_before"] = tb.copy1d(HTOD, dev, H0 - 4096, 1 << 40)
+    c["dtoh_1d_2^40"] = tb.copy1d(DTOH, start, dev, 1 << 40)
+    c["dtoh_2d_2^40"] = tb.copy2d(DTOH, wb, hb, start, 0, 0, pb, dev, 0, 0, wb)
+    c["overflow"] = tb.copy2d(HTOD, 1 << 33, 1 << 32, dev, 0, 0, 0, start, 0, 0, 0)
+    tb.meta.update(dict(start=start, dev=dev, copies=c))
+    return tb.build()
+
+
+def overlap_rows(seed: int = 0, W: int = 4096, pitch: int = 64, H: int = 20000, dtoh: bool = False) -> Trace:
+    """BAD_PITCH 2D copies whose rows overlap (pitch < W): every physical byte
+    belongs to several rows and is counted once per row (R-12).  A 4 MiB
+    window, DEFINED with scattered undefined bytes and a NOACCESS hole placed
+    by the seed; one HtoD (or DtoH) of W x H logical bytes plus one with pitch
+    0 (all rows on the same bytes)."""
+    rng = np.random.default_rng(seed + 0x0E1A)
+    H0, S = 1 << 20, 4 * MiB
+    tb = TraceBuilder(f"overlap{seed}", H0, S)
+    tb.mark(H0, S, DEFINED)
+    start = H0 + 4096 + int(rng.integers(0, 4096))
+    span = (H - 1) * pitch + W
+    for _ in range(8):
+        tb.setv(start + int(rng.integers(0, span)), bytes([int(rng.integers(1, 256))]))
+    if rng.random() < 0.5:                                    # a NOACCESS hole somewhere in the span
+        tb.mark(start + int(rng.integers(0, span)), int(rng.integers(1, 64)), NOACCESS)
+    dev = tb.malloc(1 << 30)
+    if dtoh:
+        tb.copy2d(DTOH, W, H, start, 0, 0, pitch, dev, 0, 0, W)
+        tb.copy2d(DTOH, W, H, start, 0, 0, 0, dev, 0, 0, W)
+    else:
+        tb.copy2d(HTOD, W, H, dev, 0, 0, W, start, 0, 0, pitch)
+        tb.copy2d(HTOD, W, H, dev, 0, 0, W, start, 0, 0, 0)
+    tb.meta.update(dict(start=start, dev=dev))
+    return tb.build()
