@@ -58,7 +58,7 @@ enum {
 };
 
 /* ---- copy kinds: host/device, device/host, device/device ----
- * NEXT-3 ("CUDA arrays"): transfers
+ * NEXT-3 (Fig. 2 caption P:88 "device arrays"): transfers
  * between host memory and a registered device array.  The array side is
  * (handle, byte offset): HTOA uses dst = handle, dst_x = offset; ATOH uses
  * src = handle, src_x = offset; its y / pitch are ignored.  The host side is a
@@ -289,7 +289,11 @@ cg_status cg_register_alloc(cg_ctx *ctx, uint64_t base, uint64_t size, uint64_t 
 cg_status cg_free(cg_ctx *ctx, uint64_t ptr, uint64_t seq);
 
 /* Drops tombstones with free_seq <= before_seq (no later descriptor may have
- * seq < before_seq).  Synchronous host operation. */
+ * seq < before_seq).  Synchronous host operation.  Tombstones count against
+ * max_allocs until dropped: a long-running caller compacts at its epoch
+ * boundaries (the replay driver does when half the capacity was registered
+ * since the last compaction), else cg_register_alloc eventually returns
+ * CG_ERR_OUT_OF_MEMORY. */
 cg_status cg_registry_compact(cg_ctx *ctx, uint64_t before_seq);
 
 /* NEXT-3: bytes of a CUDA array (SPEC register_array S:166-168):
@@ -300,7 +304,7 @@ cg_status cg_registry_compact(cg_ctx *ctx, uint64_t before_seq);
 uint64_t cg_array_bytes(uint64_t width, uint64_t height, uint64_t depth, uint32_t format, uint32_t channels);
 
 /* NEXT-3: registers a device array under its handle (cuArrayCreate /
- * cuArray3DCreate).  Shares the seq order of cg_register_alloc /
+ * cuArray3DCreate; the Fig. 2 caption P:88 lists arrays in the allocation list).  Shares the seq order of cg_register_alloc /
  * cg_free.  Errors (no mutation): CG_ERR_INVALID_VALUE for a zero extent
  * (cg_array_bytes == 0), a handle that is already live
  * (DuplicateHandle) or a non-increasing seq; CG_ERR_OUT_OF_MEMORY when the

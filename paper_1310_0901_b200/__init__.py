@@ -397,6 +397,7 @@ class Checker:
             raise CgError(st, "cg_ctx_create failed")
         self.ctx = ctx
         self.max_descs = max_descs
+        self.max_allocs = max_allocs
 
     def close(self):
         if getattr(self, "ctx", None):
@@ -443,6 +444,10 @@ class Checker:
     # ---- registry ------------------------------------------------------------
     def register_alloc(self, base: int, size: int, seq: int) -> int:
         return _lib.cg_register_alloc(self.ctx, base, size, seq)
+
+    def registry_compact(self, before_seq: int) -> int:
+        """cg_registry_compact: drop tombstones no descriptor with seq >= before_seq can see"""
+        return _lib.cg_registry_compact(self.ctx, before_seq)
 
     def free(self, ptr: int, seq: int) -> int:
         return _lib.cg_free(self.ctx, ptr, seq)

@@ -11,8 +11,9 @@ namespace cgk {
 
 constexpr uint64_t kNone = UINT64_MAX;
 constexpr uint64_t kInf = UINT64_MAX;          // free_seq of a live allocation
-constexpr uint64_t kMaxCopyBytes = 1ull << 38;  // R-10: larger copies are INVALID_RANGE
-constexpr uint64_t kMaxDescs = 1ull << 24;      // per call (keeps sum of weights < 2^63)
+constexpr uint64_t kMaxShardBytes = 1ull << 38;  // host bytes one context stores (config limit; scan weights < 2^40 each)
+constexpr uint64_t kDeferBytes = 1ull << 36;     // sparse map: longer host sides go to the deferred pass
+constexpr uint64_t kMaxDescs = 1ull << 24;       // per call (keeps sum of weights < 2^63)
 
 // start = base + y*pitch + x; span = (w==0||h==0) ? 0 : (h-1)*pitch + w;
 // valid iff start + span <= 2^64 - 1 (every partial sum is then exact).
@@ -53,6 +54,10 @@ struct ShadowView {
   const uint64_t* dir_key;  // chunk + 1, 0 = empty slot
   const uint32_t* dir_val;  // secondary index
   uint64_t v_bytes;         // size of V (fresh-shadow fill)
+  // sparse map: the chunks that have a secondary, ascending (the deferred
+  // pass walks them instead of the whole 64-bit range of a huge copy)
+  const uint64_t* chunk_list;
+  uint64_t n_chunks;
 };
 
 constexpr uint64_t kChunkShift = 16;               // 64 KiB host bytes per chunk
@@ -100,8 +105,10 @@ struct Plan {
   uint64_t* fbsum;        // [kFinishMaxBlocks] k_finish's per-block sums
   uint32_t* chunk_first;  // [max_chunks]
   void* meta;             // [n] ScanMeta (check plans only)
-  uint32_t* counter;      // [0] group counter, [1] apply compaction count, [2] residual-list count
+  uint32_t* counter;      // [0] group counter, [1] apply compaction count, [2] residual-list count,
+                          // [3] memmove-list count, [4] deferred-list count, [5] deferred-list cursor
   uint32_t* resid;        // [n] fused check: DtoH descriptors left to the residual apply
+  uint32_t* defer;        // [n] descriptors whose host side the deferred pass checks (R-10, R-12)
   uint64_t* dvoff;        // [2n] NEXT-1: device V offsets (dst, src) found by the last check
   uint64_t max_chunks;
   uint64_t t_min;

@@ -136,7 +136,9 @@ __device__ __forceinline__ Norm normalize(const cg_copy_desc& d) {
     return n;
   }
   const uint64_t W = d.width, H = d.height;
-  const bool bytes_ok = __umul64hi(W, H) == 0 && W * H <= kMaxCopyBytes;
+  // R-10: the logical byte count W*H -- the range of the offsets a
+  // verdict reports -- must fit in 64 bits; there is no size cap
+  const bool bytes_ok = __umul64hi(W, H) == 0;
   if (d.kind >= CG_HTOA) {   // NEXT-3 array transfer: pitch rule and fold on the host side only
     const bool htoa = d.kind == CG_HTOA;
     const uint64_t hx = htoa ? d.src_x : d.dst_x, hp = htoa ? d.src_pitch : d.dst_pitch;
@@ -180,10 +182,83 @@ __device__ __forceinline__ Norm normalize(const cg_copy_desc& d) {
   return n;
 }
 
+// ---------------------------------------------------------------------------
+// R-10 / R-15: analytic clipping of a host side.  The side's rows are
+// x_r = x0 + r*pitch (r < H), W bytes each, logical offset o = r*W + c (R-11);
+// a contiguous side (H == 1 or pitch == W) is one row of N = W*H bytes.  Host
+// bytes outside the window are unaddressable, so the scan only needs the bytes
+// inside this GPU's shard; those outside the window only contribute the lowest
+// logical offset among them (pfu), which has a closed form: o grows with the
+// address along the rows (pitch >= 0), so it is the first byte at or past the
+// window end, or offset 0 when the side starts below the window.
+// ---------------------------------------------------------------------------
+// first row r with x0 + r*pitch + W > lim (H if none); x0 + W cannot overflow
+// (start + span fits in 64 bits and span >= W)
+__device__ __forceinline__ uint64_t first_row_past(uint64_t x0, uint64_t W, uint64_t pitch, uint64_t H,
+                                                   uint64_t lim) {
+  if (x0 + W > lim) return 0;
+  if (pitch == 0) return H;
+  const uint64_t r = (lim - x0 - W) / pitch + 1;
+  return r < H ? r : H;
+}
+
+struct HostClip {
+  uint64_t olo, ohi;   // logical [olo, ohi): every shard byte of a side whose rows do not overlap (maybe empty)
+  uint64_t pfu;        // lowest logical offset of a byte outside the window (kNone if none)
+  bool overlap;        // BAD_PITCH rows that overlap (pitch < W): the deferred pass (multiplicity, R-12)
+};
+
+// nm.host must hold (a valid, bytes_ok host side)
+__device__ __forceinline__ HostClip host_clip(const Norm& nm, uint64_t H, const ShadowView& sv) {
+  HostClip c;
+  c.olo = c.ohi = 0;
+  c.pfu = kNone;
+  const bool contig = H == 1 || nm.W == nm.hpitch;
+  const uint64_t W = contig ? nm.nbytes : nm.W, Hr = contig ? 1 : H, pitch = contig ? 0 : nm.hpitch;
+  c.overlap = !contig && pitch < W;
+  if (nm.nbytes == 0) return c;
+  const uint64_t x0 = nm.hstart;
+  if (x0 < sv.wb) {
+    c.pfu = 0;
+  } else {
+    const uint64_t r = first_row_past(x0, W, pitch, Hr, sv.we);
+    if (r < Hr) {
+      const uint64_t xr = x0 + r * pitch;
+      c.pfu = r * W + (sv.we > xr ? sv.we - xr : 0);
+    }
+  }
+  if (c.overlap) return c;
+  const uint64_t rlo = first_row_past(x0, W, pitch, Hr, sv.sb);
+  if (rlo == Hr) return c;
+  const uint64_t xlo = x0 + rlo * pitch;
+  if (xlo >= sv.se) return c;
+  uint64_t rhi = Hr - 1;
+  if (pitch) rhi = umin64(rhi, (sv.se - 1 - x0) / pitch);
+  const uint64_t xhi = x0 + rhi * pitch;
+  c.olo = rlo * W + (sv.sb > xlo ? sv.sb - xlo : 0);
+  c.ohi = rhi * W + umin64(W, sv.se - xhi);
+  return c;
+}
+
+// olo of host_clip without the rest (the scan's generator, per piece): the
+// logical offset of the first shard byte; 0 unless the side starts below the shard
+__device__ __forceinline__ uint64_t clip_base(uint64_t x0, uint64_t W, uint64_t pitch, bool contig, uint64_t sb) {
+  if (x0 >= sb) return 0;
+  if (contig) return sb - x0;
+  const uint64_t r = first_row_past(x0, W, pitch, ~0ull, sb);
+  const uint64_t xr = x0 + r * pitch;
+  return r * W + (sb > xr ? sb - xr : 0);
+}
+
 // packed per-descriptor metadata written by k_check_prep for the scan
 struct __align__(16) ScanMeta {
-  uint64_t hstart, hpitch, W, info;   // info: nbytes | kind << 40 | host << 42 | flags << 48
+  uint64_t hstart, hpitch, W, info;   // info: see kInfo*
 };
+// info: scanned bytes (the shard clip, < 2^40) | scan kind << 40 | host << 42 |
+// contiguous << 43 | raw << 44 | pfu << 45 | deferred << 46 | flags << 48
+constexpr int kInfoKind = 40, kInfoHost = 42, kInfoContig = 43, kInfoRaw = 44, kInfoPfu = 45, kInfoDefer = 46,
+              kInfoFlags = 48;
+constexpr uint64_t kInfoBytes = (1ull << 40) - 1;
 
 // ---------------------------------------------------------------------------
 // a3: batched interval search (lifetime-stamped, base-sorted table)
@@ -274,19 +349,20 @@ __device__ __forceinline__ void load_splitters(const Table& t, uint64_t* s_split
 // 8 host bytes (A only), plus kItemCost per descriptor (its fixed work).
 constexpr uint64_t kItemCost = 256;
 
-__device__ __forceinline__ uint64_t check_host_units(const Norm& nm, bool two_bit) {
-  if (!nm.host) return 0;
-  if (two_bit) return (nm.nbytes + 3) >> 2;   // NEXT-4: one state byte per 4 host bytes, both kinds
-  return nm.skind == CG_HTOD ? nm.nbytes : (nm.nbytes + 7) >> 3;
+__device__ __forceinline__ uint64_t check_host_units(uint32_t skind, uint64_t nscan, bool two_bit) {
+  if (two_bit) return (nscan + 3) >> 2;   // NEXT-4: one state byte per 4 host bytes, both kinds
+  return skind == CG_HTOD ? nscan : (nscan + 7) >> 3;
 }
 
 __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs, uint64_t n, const Table& t,
                                           cg_verdict* __restrict__ out, uint64_t* __restrict__ weight,
-                                          ScanMeta* __restrict__ meta, uint64_t* __restrict__ dvoff, int two_bit,
-                                          uint32_t* __restrict__ counter, uint64_t* s_split) {
-  // the scan's group counter, (apply count), residual count: reset here
-  // instead of by a memset node, which would break the PDL chain
-  if (blockIdx.x == 0 && threadIdx.x < 3) counter[threadIdx.x] = 0;
+                                          ScanMeta* __restrict__ meta, uint64_t* __restrict__ dvoff,
+                                          const ShadowView& sv, uint32_t* __restrict__ counter,
+                                          uint32_t* __restrict__ defer, uint64_t* s_split) {
+  // the scan's group counter, (apply count), residual count, deferred list
+  // count and cursor: reset here instead of by a memset node, which would
+  // break the PDL chain
+  if (blockIdx.x == 0 && threadIdx.x < 6 && threadIdx.x != 3) counter[threadIdx.x] = 0;
   load_splitters(t, s_split);
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
@@ -339,8 +415,15 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
       dvoff[2 * i] = dv_dst;
       dvoff[2 * i + 1] = dv_src;
     }
+    // R-10 / R-15: the shard part of the host side, and the analytic first
+    // offset outside the window (initial first_unaddr: partials min into it)
+    HostClip hc{0, 0, kNone, false};
+    if (nm.host) hc = host_clip(nm, d.height, sv);
+    const bool deferred = nm.host && (hc.overlap || (sv.sparse && hc.ohi - hc.olo > kDeferBytes));
+    const uint64_t nscan = nm.host && !deferred ? hc.ohi - hc.olo : 0;
+    if (deferred) defer[atomicAdd(counter + 4, 1u)] = (uint32_t)i;
     cg_verdict v;
-    v.first_unaddr = kNone;
+    v.first_unaddr = hc.pfu;
     v.first_undef = kNone;
     v.undef_count = 0;
     v.dst_expected = de;
@@ -350,15 +433,16 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
     v.flags = flags;
     v.status = 0;
     out[i] = v;
-    weight[i] = kItemCost + check_host_units(nm, two_bit != 0);
+    weight[i] = kItemCost + check_host_units(nm.skind, nscan, sv.two_bit != 0);
     ScanMeta m;
     m.hstart = nm.hstart;
     m.hpitch = nm.hpitch;
     m.W = nm.W;
     const bool contig = d.height == 1 || d.width == nm.hpitch;
     const bool raw = d.reserved & CG_SHARD_RAW;   // partial of a straddler: no finalisation here
-    m.info = nm.nbytes | ((uint64_t)(nm.skind & 3u) << 40) | ((uint64_t)nm.host << 42) | ((uint64_t)contig << 43) |
-             ((uint64_t)raw << 44) | ((uint64_t)flags << 48);
+    m.info = nscan | ((uint64_t)(nm.skind & 3u) << kInfoKind) | ((uint64_t)(nscan != 0) << kInfoHost) |
+             ((uint64_t)contig << kInfoContig) | ((uint64_t)raw << kInfoRaw) | ((uint64_t)(hc.pfu != kNone) << kInfoPfu) |
+             ((uint64_t)deferred << kInfoDefer) | ((uint64_t)flags << kInfoFlags);
     meta[i] = m;
   }
 }
@@ -367,11 +451,12 @@ __global__ void __launch_bounds__(kThreads) k_check_prep(const cg_copy_desc* __r
                                                          uint64_t n, Table t, cg_verdict* __restrict__ out,
                                                          uint64_t* __restrict__ weight,
                                                          ScanMeta* __restrict__ meta,
-                                                         uint64_t* __restrict__ dvoff, int two_bit,
-                                                         uint32_t* __restrict__ counter) {
+                                                         uint64_t* __restrict__ dvoff, ShadowView sv,
+                                                         uint32_t* __restrict__ counter,
+                                                         uint32_t* __restrict__ defer) {
   pdl_entry();
   extern __shared__ uint64_t s_split[];
-  prep_body(descs, n, t, out, weight, meta, dvoff, two_bit, counter, s_split);
+  prep_body(descs, n, t, out, weight, meta, dvoff, sv, counter, defer, s_split);
 }
 
 // ---------------------------------------------------------------------------
@@ -534,14 +619,15 @@ __global__ void __launch_bounds__(kThreads) k_plan(const uint64_t* __restrict__ 
 __global__ void __launch_bounds__(kThreads) k_front(const cg_copy_desc* __restrict__ descs, uint64_t n, Table t,
                                                     cg_verdict* __restrict__ out, uint64_t* __restrict__ weight,
                                                     ScanMeta* __restrict__ meta, uint64_t* __restrict__ dvoff,
-                                                    int two_bit, uint32_t* __restrict__ counter, uint64_t* P,
+                                                    ShadowView sv, uint32_t* __restrict__ counter,
+                                                    uint32_t* __restrict__ defer, uint64_t* P,
                                                     uint64_t* __restrict__ bsum, uint64_t t_min, uint64_t max_chunks,
                                                     uint32_t* __restrict__ chunk_first) {
   pdl_entry();
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   extern __shared__ uint64_t s_split[];
   __shared__ uint64_t s_warp[33];
-  prep_body(descs, n, t, out, weight, meta, dvoff, two_bit, counter, s_split);
+  prep_body(descs, n, t, out, weight, meta, dvoff, sv, counter, defer, s_split);
   grid.sync();
   // block b owns items [b*per, (b+1)*per)
   const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
@@ -876,14 +962,19 @@ __device__ __forceinline__ void consume_2bit(const uint8_t* st, uint32_t q0, uin
 }
 
 // states of host bytes [q0, q1) := pat (0x00000000 NOACCESS, 0xAAAAAAAA DEFINED,
-// 0xFFFFFFFF UNDEFINED); partial words with atomics because a neighbouring
-// range of the same batch may own the other bytes of the word
+// 0xFFFFFFFF UNDEFINED); a partial word is updated in ONE atomic step (CAS
+// loop) because a neighbouring range of the same batch may own its other bytes
+// and a concurrent scan may read it: an AND-then-OR pair would expose an
+// intermediate state (PARTIAL 01 -> 00 -> DEFINED 10 passes through NOACCESS)
 __device__ __forceinline__ void fill2_word(uint32_t* S, uint64_t k, uint32_t m, uint32_t pat) {
   if (m == 0xffffffffu) {
     S[k] = pat;
   } else if (m) {
-    if (m & ~pat) atomicAnd(S + k, ~(m & ~pat));
-    if (m & pat) atomicOr(S + k, m & pat);
+    uint32_t old = *reinterpret_cast<volatile uint32_t*>(S + k), prev;
+    do {
+      prev = old;
+      old = atomicCAS(S + k, prev, (prev & ~m) | (pat & m));
+    } while (old != prev);
   }
 }
 
@@ -1051,10 +1142,11 @@ struct TileGen {
     // a descriptor of at most one group's weight is never split: it belongs
     // to the group its weight interval starts in
     const bool small = m_pe - m_ps <= Trule;
-    if (small ? (m_ps >= w0 && m_ps < w1) : (m_ps < w1 && m_pe > w0)) {
-      const uint64_t nbytes = m_info & ((1ull << 40) - 1);
-      const uint32_t kind = (uint32_t)(m_info >> 40) & 3u;
-      const bool host = (m_info >> 42) & 1u, contig = (m_info >> 43) & 1u;
+    const bool deferred = (m_info >> kInfoDefer) & 1u;   // the deferred pass checks it (k_check_scan's tail)
+    if (!deferred && (small ? (m_ps >= w0 && m_ps < w1) : (m_ps < w1 && m_pe > w0))) {
+      const uint64_t nbytes = m_info & kInfoBytes;
+      const uint32_t kind = (uint32_t)(m_info >> kInfoKind) & 3u;
+      const bool host = (m_info >> kInfoHost) & 1u, contig = (m_info >> kInfoContig) & 1u;
       const bool htod = kind == CG_HTOD;
       uint32_t f = kPieceIn | (htod ? kPieceHtod : 0u);
       if (small) f |= kPieceWhole;
@@ -1069,17 +1161,26 @@ struct TileGen {
         lo = a << 3;
         hi = umin64(b << 3, nbytes);
       }
+      // a whole piece carries the side's analytic first offset outside the
+      // window (R-15; the prep stored it as the initial first_unaddr); split
+      // pieces min into that initial value
       p_fu = kNone;
+      if (small && ((m_info >> kInfoPfu) & 1u)) p_fu = out[wbase + lane].first_unaddr;
       if (!host || lo >= hi) {
         f |= kPieceEmpty;
+      } else {
+        // [lo, hi) counts scanned bytes from the side's first shard byte (R-10 clip)
+        const uint64_t ob = clip_base(m_x0, m_W, m_pitch, contig, sb);
+        lo += ob;
+        hi += ob;
+      }
+      if (f & kPieceEmpty) {
       } else if (!contig) {
         f |= kPiece2D;
         p_lo = lo;
         p_hi = hi;
       } else {
         const uint64_t x = m_x0 + lo, len = hi - lo;
-        if (x < wb) p_fu = lo;
-        else if (x + len > we) p_fu = lo + (umax64(x, we) - x);
         const uint64_t y0 = umax64(x, sb), y1 = umin64(x + len, se);
         if (y0 < y1) {
           p_qs = y0 - sb;
@@ -1092,16 +1193,14 @@ struct TileGen {
       p_fl = f;
       if (f & kPieceEmpty) {
         cg_verdict* v = out + (wbase + lane);
-        if ((f & kPieceWhole) && ((m_info >> 44) & 1u)) {
+        if ((f & kPieceWhole) && ((m_info >> kInfoRaw) & 1u)) {
           v->first_unaddr = p_fu;   // raw partial (straddler): finalised after the merge
         } else if (f & kPieceWhole) {
-          uint32_t flags = (uint32_t)(m_info >> 48), status;
+          uint32_t flags = (uint32_t)(m_info >> kInfoFlags), status;
           finalize_fields(flags, status, p_fu, 0, err_mask);
           v->first_unaddr = p_fu;
           v->flags = flags;
           v->status = status;
-        } else if (p_fu != kNone) {
-          atomicMin(reinterpret_cast<unsigned long long*>(&v->first_unaddr), p_fu);
         }
       }
     }
@@ -1111,7 +1210,7 @@ struct TileGen {
     const bool live = (p_fl & (kPieceIn | kPiece2D | kPieceEmpty)) == kPieceIn;
     set_segment(live, p_qs, p_qe, p_ob, p_fu, (uint32_t)(wbase + lane),
                 (p_fl & kPieceHtod ? kTileHtod : 0u) | (p_fl & kPieceWhole ? kTileWhole : 0u) | kSegEndLast |
-                    (((m_info >> 44) & 1u) ? kTileRaw : 0u) | ((uint32_t)(m_info >> 48) << 16));
+                    (((m_info >> kInfoRaw) & 1u) ? kTileRaw : 0u) | ((uint32_t)(m_info >> kInfoFlags) << 16));
     phase = kPhaseContig;
   }
 
@@ -1150,18 +1249,17 @@ struct TileGen {
     return true;
   }
 
-  // rows [r2, r2 + 32) of the current 2D piece as a segment window
+  // rows [r2, r2 + 32) of the current 2D piece as a segment window (the
+  // piece lies in the shard clip, so every row segment is shard bytes)
   __device__ __forceinline__ void row_window() {
     const int lane = threadIdx.x & 31;
     const uint64_t r = r2 + lane;
     const uint64_t rs = r * W;                       // logical offset of the row start
     bool live = false;
-    uint64_t q0 = 0, q1 = 0, ob = 0, cand = kNone;
+    uint64_t q0 = 0, q1 = 0, ob = 0;
     if (rs < hi2) {
       const uint64_t L0 = umax64(lo2, rs), L1 = umin64(hi2, rs + W);
       const uint64_t x = x0 + r * pitch + (L0 - rs), len = L1 - L0;
-      if (x < wb) cand = L0;
-      else if (x + len > we) cand = L0 + (umax64(x, we) - x);
       const uint64_t y0 = umax64(x, sb), y1 = umin64(x + len, se);
       if (y0 < y1) {
         live = true;
@@ -1170,7 +1268,6 @@ struct TileGen {
         ob = L0 - x + sb;
       }
     }
-    fu2 = umin64(fu2, warp_min(cand));
     set_segment(live, q0, q1, ob, kNone, d2, fl2 & kTileHtod);
     r2 += 32;
   }
@@ -1212,9 +1309,9 @@ struct TileGen {
           const uint64_t info = __shfl_sync(kFull, m_info, src);
           d2 = (uint32_t)(wbase + src);
           fl2 = (pf & kPieceHtod ? kTileHtod : 0u) | (pf & kPieceWhole ? kTileWhole : 0u) |
-                (((info >> 44) & 1u) ? kTileRaw : 0u) | ((uint32_t)(info >> 48) << 16);
+                (((info >> kInfoRaw) & 1u) ? kTileRaw : 0u) | ((uint32_t)(info >> kInfoFlags) << 16);
           r2 = lo2 / W;
-          fu2 = kNone;
+          fu2 = __shfl_sync(kFull, p_fu, src);
           in2d = true;
         } else {
           phase = kPhaseWindow;
@@ -1285,6 +1382,196 @@ struct TileGen {
   }
 };
 
+// ---------------------------------------------------------------------------
+// The deferred pass (R-10, R-12): host sides the tile generator does not take
+// -- BAD_PITCH rows that overlap (pitch < W: a physical byte lies in several
+// rows and counts once per row) and, in the sparse map, sides longer than
+// kDeferBytes (walked over the chunks that have a secondary; the bytes between
+// them are NOACCESS).  One warp per descriptor, taken from a list by warps
+// whose ring has drained, in physical address order with plain 16-byte loads.
+// Along a side the logical offset grows with the address (rows move up by
+// pitch >= 0), so each lane's first bad / undefined byte gives its minimum.
+// Physical byte u = x - x0 of overlapping rows lies in rows r_lo..r_hi,
+// r_lo = u < W ? 0 : (u - W) / pitch + 1, r_hi = min(H - 1, u / pitch), with
+// first logical offset u + r_lo (W - pitch) (pitch 0: rows 0..H-1, offset u).
+// Pathological inputs only: not tuned.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t even_bits(uint32_t x) {   // bit 2j -> bit j
+  x &= 0x55555555u;
+  x = (x | (x >> 1)) & 0x33333333u;
+  x = (x | (x >> 2)) & 0x0F0F0F0Fu;
+  x = (x | (x >> 4)) & 0x00FF00FFu;
+  return (x | (x >> 8)) & 0x0000FFFFu;
+}
+
+// addressable / undefined masks of the 16 host bytes at shard byte q (q % 16 == 0)
+__device__ __forceinline__ void host16(const ShadowView& sv, uint64_t q, uint32_t& addr, uint32_t& und) {
+  if (!sv.two_bit) {
+    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(sv.V + q));
+    addr = __ldcg(reinterpret_cast<const unsigned short*>(sv.A + (q >> 3)));
+    und = nz16(v) & addr;
+    return;
+  }
+  uint32_t w;
+  if (sv.sparse) {
+    const uint64_t c = q >> kChunkShift;
+    w = __ldcg(reinterpret_cast<const unsigned int*>(chunk_base(sv, c, sparse_secondary(sv, c)) + (q >> 2)));
+  } else {
+    w = __ldcg(reinterpret_cast<const unsigned int*>(sv.V) + (q >> 4));
+  }
+  addr = even_bits(w | (w >> 1));   // state != 00
+  und = even_bits(w);               // PARTIAL / UNDEFINED (always addressable)
+}
+
+struct DeferSide {
+  uint64_t x0, W, pitch, H;   // rows; a contiguous side is one row of N bytes
+  bool overlap, htod;
+};
+
+__device__ __forceinline__ uint64_t ov_rlo(const DeferSide& s, uint64_t u) {
+  return (s.pitch == 0 || u < s.W) ? 0 : (u - s.W) / s.pitch + 1;
+}
+
+// physical host bytes [a, b) of the side, inside the stored shard; rowbase =
+// the logical offset of a when the segment lies in one row (non-overlapping rows)
+__device__ __noinline__ void defer_segment(const ShadowView& sv, const DeferSide& s, uint64_t a, uint64_t b,
+                                           uint64_t rowbase, Partial& p) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t g1 = b - sv.sb;
+  for (uint64_t g = ((a - sv.sb) & ~15ull) + 16ull * lane; g < g1; g += 512) {
+    const uint64_t xa = sv.sb + g;   // address of the group's byte 0
+    uint32_t m = 0xFFFFu;
+    if (xa < a) m &= 0xFFFFu << (uint32_t)(a - xa);
+    if (xa + 16 > b) m &= 0xFFFFu >> (uint32_t)(xa + 16 - b);
+    uint32_t ad, un;
+    host16(sv, g, ad, un);
+    const uint32_t bad = ~ad & m;
+    uint32_t u = s.htod ? un & m : 0u;
+    if (!(bad | u)) continue;
+    if (bad) {
+      const uint64_t x = xa + (__ffs(bad) - 1);
+      p.fu = umin64(p.fu, s.overlap ? (x - s.x0) + ov_rlo(s, x - s.x0) * (s.W - s.pitch) : rowbase + (x - a));
+    }
+    if (u) {
+      const uint64_t x = xa + (__ffs(u) - 1);
+      p.fd = umin64(p.fd, s.overlap ? (x - s.x0) + ov_rlo(s, x - s.x0) * (s.W - s.pitch) : rowbase + (x - a));
+      if (!s.overlap) {
+        p.cnt += __popc(u);
+      } else {
+        while (u) {   // each undefined byte counts once per row it lies in
+          const uint64_t uu = xa + (__ffs(u) - 1) - s.x0;
+          u &= u - 1;
+          p.cnt += s.pitch == 0 ? s.H : umin64(s.H - 1, uu / s.pitch) - ov_rlo(s, uu) + 1;
+        }
+      }
+    }
+  }
+}
+
+// the side's bytes in the physical range [a, e) (inside the stored shard)
+__device__ __forceinline__ void defer_range(const ShadowView& sv, const DeferSide& s, uint64_t a, uint64_t e,
+                                            Partial& p) {
+  if (s.overlap) {
+    defer_segment(sv, s, a, e, 0, p);
+    return;
+  }
+  for (uint64_t r = first_row_past(s.x0, s.W, s.pitch, s.H, a); r < s.H; ++r) {
+    const uint64_t xr = s.x0 + r * s.pitch;
+    if (xr >= e) break;
+    const uint64_t sa = umax64(xr, a), sb = umin64(xr + s.W, e);
+    if (sa < sb) defer_segment(sv, s, sa, sb, r * s.W + (sa - xr), p);
+    if (s.pitch == 0) break;
+  }
+}
+
+// lowest logical offset of a side byte in the NOACCESS gap [y, a) (kNone if none)
+__device__ __forceinline__ uint64_t gap_offset(const DeferSide& s, uint64_t y, uint64_t a) {
+  if (y >= a) return kNone;
+  if (s.overlap || s.pitch == 0) {   // the side's bytes are the contiguous [x0, x0 + span)
+    const uint64_t b = umax64(y, s.x0);
+    if (b >= a) return kNone;
+    return s.overlap ? (b - s.x0) + ov_rlo(s, b - s.x0) * (s.W - s.pitch) : b - s.x0;
+  }
+  const uint64_t r = first_row_past(s.x0, s.W, s.pitch, s.H, y);
+  if (r >= s.H) return kNone;
+  const uint64_t xr = s.x0 + r * s.pitch, b = umax64(xr, y);
+  return b < a ? r * s.W + (b - xr) : kNone;
+}
+
+__device__ __noinline__ void defer_one(const cg_copy_desc* __restrict__ descs, uint32_t d,
+                                       const ScanMeta* __restrict__ meta, const ShadowView& sv,
+                                       cg_verdict* __restrict__ out, uint32_t err_mask, int fuse,
+                                       uint32_t* __restrict__ resid, uint32_t* __restrict__ resid_n) {
+  const int lane = threadIdx.x & 31;
+  const cg_copy_desc dd = descs[d];
+  const Norm nm = normalize(dd);
+  const HostClip hc = host_clip(nm, dd.height, sv);
+  const bool contig = dd.height == 1 || dd.width == nm.hpitch;
+  DeferSide s;
+  s.x0 = nm.hstart;
+  s.W = contig ? nm.nbytes : nm.W;
+  s.pitch = contig ? 0 : nm.hpitch;
+  s.H = contig ? 1 : dd.height;
+  s.overlap = hc.overlap;
+  s.htod = nm.skind == CG_HTOD;
+  const uint64_t hi = s.x0 + ((s.H - 1) * s.pitch + s.W);   // end of the physical span (fits: R-10)
+  Partial p{lane == 0 ? hc.pfu : kNone, kNone, 0};
+  if (!sv.sparse) {   // dense: overlapping rows only; the shard part of the span
+    const uint64_t a = umax64(s.x0, sv.sb), b = umin64(hi, sv.se);
+    if (a < b) defer_range(sv, s, a, b, p);
+  } else {            // sparse: the chunks with a secondary, ascending
+    uint64_t k0 = 0, k1 = sv.n_chunks;
+    while (k0 < k1) {
+      const uint64_t mid = (k0 + k1) >> 1;
+      if (sv.chunk_list[mid] < (s.x0 >> kChunkShift)) k0 = mid + 1; else k1 = mid;
+    }
+    uint64_t y = s.x0;   // side bytes below y are done
+    for (uint64_t k = k0; k < sv.n_chunks; ++k) {
+      const uint64_t ca = sv.chunk_list[k] << kChunkShift, clast = ca + ((1ull << kChunkShift) - 1);
+      if (ca >= hi) break;
+      const uint64_t a = umax64(ca, s.x0), e = umin64(clast, hi - 1) + 1;
+      if (lane == 0) p.fu = umin64(p.fu, gap_offset(s, y, a));
+      defer_range(sv, s, a, e, p);
+      y = e;
+    }
+    if (lane == 0) p.fu = umin64(p.fu, gap_offset(s, y, hi));
+  }
+  p.fu = warp_min(p.fu);
+  p.fd = warp_min(p.fd);
+  p.cnt = warp_sum(p.cnt);
+  if (lane == 0) {
+    const uint64_t info = meta[d].info;
+    cg_verdict* v = out + d;
+    v->first_unaddr = p.fu;
+    v->first_undef = p.fd;
+    v->undef_count = p.cnt;
+    if (!((info >> kInfoRaw) & 1u)) {   // a raw straddler partial is finalised after the merge
+      uint32_t flags = (uint32_t)(info >> kInfoFlags), status;
+      finalize_fields(flags, status, p.fu, p.cnt, err_mask);
+      v->flags = flags;
+      v->status = status;
+      if (fuse && status == CG_OK && !s.htod) resid[atomicAdd(resid_n, 1u)] = d;   // the residual pass applies it
+    }
+  }
+  __syncwarp();
+}
+
+// a warp whose ring has drained takes deferred descriptors until the list is done
+__device__ __noinline__ void defer_tail(const cg_copy_desc* __restrict__ descs, const uint32_t* __restrict__ defer,
+                                        uint32_t* counter, const ScanMeta* __restrict__ meta, const ShadowView& sv,
+                                        cg_verdict* __restrict__ out, uint32_t err_mask, int fuse,
+                                        uint32_t* __restrict__ resid, uint32_t* __restrict__ resid_n) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t n = *reinterpret_cast<volatile uint32_t*>(counter + 4);   // final: written by the prep
+  while (true) {
+    uint32_t k = 0;
+    if (lane == 0) k = atomicAdd(counter + 5, 1u);
+    k = __shfl_sync(kFull, k, 0);
+    if (k >= n) break;
+    defer_one(descs, defer[k], meta, sv, out, err_mask, fuse, resid, resid_n);
+  }
+}
+
 // one instantiation per host shadow format (kTwoBit: NEXT-4 2-bit states)
 // and apply mode (kFuse: cg_check_apply): the other paths are compiled out of
 // each, which relieves instruction-cache stalls
@@ -1293,7 +1580,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
     const ScanMeta* __restrict__ meta, uint64_t n, const uint64_t* __restrict__ P,
     const uint32_t* __restrict__ chunk_first, uint32_t* counter, uint64_t t_min, uint64_t max_chunks,
     ShadowView sv, cg_verdict* __restrict__ out, uint32_t err_mask, int fuse, uint32_t* __restrict__ resid,
-    uint32_t* __restrict__ resid_n) {
+    uint32_t* __restrict__ resid_n, const cg_copy_desc* __restrict__ descs, const uint32_t* __restrict__ defer) {
   pdl_entry();
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1395,6 +1682,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
     __syncwarp();
     if (!gen.next(ring, s, sv, policy)) --left;
   }
+  defer_tail(descs, defer, counter, meta, sv, out, err_mask, kFuse ? 1 : 0, resid, resid_n);
 }
 
 
@@ -1412,14 +1700,14 @@ __global__ void __launch_bounds__(kThreads) k_finalize_split(uint64_t n, const u
     const uint64_t pd = P[d], pd1 = P[d + 1];
     if (pd1 - pd <= g.Trule) continue;   // never split (see compute_pieces)
     const uint64_t info = meta[d].info;
-    if ((info >> 44) & 1u) continue;   // raw partial of a straddler
+    if ((info >> kInfoRaw) & 1u) continue;   // raw partial of a straddler
     cg_verdict* v = out + d;
     uint32_t flags = v->flags, status;
     finalize_fields(flags, status, v->first_unaddr, v->undef_count, err_mask);
     v->flags = flags;
     v->status = status;
     // fused check: a split DtoH piece is applied by the residual pass
-    if (fuse && status == CG_OK && ((info >> 40) & 3u) == CG_DTOH && ((info >> 42) & 1u))
+    if (fuse && status == CG_OK && ((info >> kInfoKind) & 3u) == CG_DTOH && ((info >> kInfoHost) & 1u))
       resid[atomicAdd(resid_n, 1u)] = (uint32_t)d;
   }
 }
@@ -1451,6 +1739,7 @@ __device__ __forceinline__ void for_rows(const Norm& nm, uint64_t lo, uint64_t h
 // shared memory, so one lane instruction writes 4 KiB; only the unaligned
 // head/tail bytes (< 16 per segment) use byte stores.
 constexpr uint64_t kApplyItemCost = 64;
+constexpr int kApplyContig = 63;   // apply records: info = host bytes | contiguous << 63
 constexpr uint32_t kZeroPage = 4096;
 
 // The applicable descriptors (DtoH, status OK, host bytes) are compacted to
@@ -1477,7 +1766,7 @@ __global__ void __launch_bounds__(kThreads) k_apply_prep(const cg_copy_desc* __r
         m.hstart = nm.hstart;
         m.hpitch = nm.hpitch;
         m.W = nm.W;
-        m.info = nm.nbytes | ((uint64_t)(d.height == 1 || d.width == nm.hpitch) << 43);
+        m.info = nm.nbytes | ((uint64_t)(d.height == 1 || d.width == nm.hpitch) << kApplyContig);
       }
     }
     const uint32_t mask = __ballot_sync(kFull, ok);
@@ -1514,7 +1803,7 @@ __global__ void __launch_bounds__(kThreads) k_apply_list_prep(const cg_copy_desc
     mm.hstart = nm.hstart;
     mm.hpitch = nm.hpitch;
     mm.W = nm.W;
-    mm.info = nm.nbytes | ((uint64_t)(d.height == 1 || d.width == nm.hpitch) << 43);
+    mm.info = nm.nbytes | ((uint64_t)(d.height == 1 || d.width == nm.hpitch) << kApplyContig);
     meta[k] = mm;
     weight[k] = kApplyItemCost + nm.nbytes;
   }
@@ -1588,7 +1877,7 @@ __device__ __forceinline__ void apply_body(const ScanMeta* __restrict__ meta, ui
         lo = a > kApplyItemCost ? a - kApplyItemCost : 0;
         hi = b > kApplyItemCost ? b - kApplyItemCost : 0;
         if (lo < hi) {
-          if ((m.info >> 43) & 1u) {
+          if ((m.info >> kApplyContig) & 1u) {
             const uint64_t x = m.hstart + lo, y0 = umax64(x, sv.sb), y1 = umin64(x + (hi - lo), sv.se);
             if (y0 < y1) {
               qs = y0 - sv.sb;
@@ -1610,7 +1899,7 @@ __device__ __forceinline__ void apply_body(const ScanMeta* __restrict__ meta, ui
         const int src = __ffs(todo) - 1;
         todo &= todo - 1;
         const uint64_t s_info = __shfl_sync(kFull, m.info, src);
-        if ((s_info >> 43) & 1u) {
+        if ((s_info >> kApplyContig) & 1u) {
           const uint64_t a = __shfl_sync(kFull, qs, src), b = __shfl_sync(kFull, qe, src);
           if (kTwoBit) fill2_any<true>(sv, a, b, 0xAAAAAAAAu);
           else warp_zero(sv.V, a, b, zeros);
@@ -1686,13 +1975,13 @@ __global__ void __launch_bounds__(kThreads) k_finish(
       const uint64_t pd = P[d], pd1 = P[d + 1];
       if (pd1 - pd <= g.Trule) continue;   // never split (see compute_pieces)
       const uint64_t info = meta[d].info;
-      if ((info >> 44) & 1u) continue;     // raw partial of a straddler
+      if ((info >> kInfoRaw) & 1u) continue;     // raw partial of a straddler
       cg_verdict* v = out + d;
       uint32_t flags = v->flags, status;
       finalize_fields(flags, status, v->first_unaddr, v->undef_count, err_mask);
       v->flags = flags;
       v->status = status;
-      if (status == CG_OK && ((info >> 40) & 3u) == CG_DTOH && ((info >> 42) & 1u))
+      if (status == CG_OK && ((info >> kInfoKind) & 3u) == CG_DTOH && ((info >> kInfoHost) & 1u))
         resid[atomicAdd(resid_n, 1u)] = (uint32_t)d;
     }
     if (tid == 0) counter[0] = 0;   // the apply walk's group counter
@@ -1707,7 +1996,7 @@ __global__ void __launch_bounds__(kThreads) k_finish(
     mm.hstart = nm.hstart;
     mm.hpitch = nm.hpitch;
     mm.W = nm.W;
-    mm.info = nm.nbytes | ((uint64_t)(d.height == 1 || d.width == nm.hpitch) << 43);
+    mm.info = nm.nbytes | ((uint64_t)(d.height == 1 || d.width == nm.hpitch) << kApplyContig);
     meta[k] = mm;
     weight[k] = kApplyItemCost + nm.nbytes;
   }
@@ -2800,30 +3089,33 @@ static cudaError_t plan(const Launch& L, uint64_t n, const Plan& p, cudaStream_t
 }
 
 // a1-a4: prep, plan and the shadow scan
-static void check_front(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out, const Table& t,
+static cudaError_t check_front(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out, const Table& t,
                         const ShadowView& sv, const Plan& p, uint32_t err_mask, bool fuse, cudaStream_t s) {
   const size_t smem = ((size_t)t.nsplit + 1) * sizeof(uint64_t);
   ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
   L.stage(CG_STAGE_CHECK_PREP, true, s);
   if (L.front_blocks > 0 && smem <= kFrontSmem) {   // prep + plan in one cooperative launch
     const Table tc = t;
-    int two_bit = (int)sv.two_bit;
+    ShadowView svc = sv;
     uint64_t* weight = p.weight;
     uint64_t* dvoff = p.dvoff;
     uint32_t* counter = p.counter;
+    uint32_t* defer = p.defer;
     uint64_t* P = p.P;
     uint64_t* bsum = p.fbsum;
     uint64_t t_min = p.t_min, max_chunks = p.max_chunks;
     uint32_t* chunk_first = p.chunk_first;
     void* args[] = {(void*)&d, (void*)&n, (void*)&tc, (void*)&out, (void*)&weight, (void*)&meta, (void*)&dvoff,
-                    (void*)&two_bit, (void*)&counter, (void*)&P, (void*)&bsum, (void*)&t_min, (void*)&max_chunks,
-                    (void*)&chunk_first};
-    cudaLaunchCooperativeKernel((const void*)k_front, dim3((unsigned)L.front_blocks), dim3(kThreads), args, smem, s);
+                    (void*)&svc, (void*)&counter, (void*)&defer, (void*)&P, (void*)&bsum, (void*)&t_min,
+                    (void*)&max_chunks, (void*)&chunk_first};
+    const cudaError_t e =
+        cudaLaunchCooperativeKernel((const void*)k_front, dim3((unsigned)L.front_blocks), dim3(kThreads), args, smem, s);
     *L.counter += 1;
     L.stage(CG_STAGE_CHECK_PREP, false, s);
+    if (e != cudaSuccess) return e;   // nothing after it may consume a stale plan
   } else {
     launch_pdl(k_check_prep, blocks_for(n, kThreads, L.num_sms * 4), kThreads, smem, s, d, n, t, out, p.weight, meta,
-               p.dvoff, (int)sv.two_bit, p.counter);
+               p.dvoff, sv, p.counter, p.defer);
     *L.counter += 1;
     L.stage(CG_STAGE_CHECK_PREP, false, s);
     L.stage(CG_STAGE_CHECK_PLAN, true, s);
@@ -2836,15 +3128,17 @@ static void check_front(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_v
                           : (fuse ? k_check_scan<true, true, false> : k_check_scan<true, false, false>);
   launch_pdl(scan, L.scan_blocks, kRingWarps * 32, kScanSmem, s, meta, n, p.P, p.chunk_first, p.counter,
                                                                  p.t_min, p.max_chunks, sv, out, err_mask,
-                                                                 fuse ? 1 : 0, p.resid, p.counter + 2);
+                                                                 fuse ? 1 : 0, p.resid, p.counter + 2, d, p.defer);
   L.stage(CG_STAGE_CHECK_SCAN, false, s);
   *L.counter += 1;
+  return cudaGetLastError();
 }
 
 cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out, const Table& t,
                          const ShadowView& sv, const Plan& p, uint32_t err_mask, bool fuse, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  check_front(L, d, n, out, t, sv, p, err_mask, fuse, s);
+  cudaError_t e = check_front(L, d, n, out, t, sv, p, err_mask, fuse, s);
+  if (e != cudaSuccess) return e;
   ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
   L.stage(CG_STAGE_CHECK_FINAL, true, s);
   launch_pdl(k_finalize_split, blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s, 
@@ -2858,7 +3152,8 @@ cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_
 cudaError_t check_apply(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out, const Table& t,
                         const ShadowView& sv, const Plan& p, uint32_t err_mask, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  check_front(L, d, n, out, t, sv, p, err_mask, true, s);
+  cudaError_t e = check_front(L, d, n, out, t, sv, p, err_mask, true, s);
+  if (e != cudaSuccess) return e;
   L.stage(CG_STAGE_APPLY, true, s);
   ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
   uint64_t* P = p.P;
@@ -2872,7 +3167,7 @@ cudaError_t check_apply(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_v
   void* args[] = {(void*)&d, (void*)&n, (void*)&P, (void*)&t_min, (void*)&max_chunks, (void*)&out, (void*)&err_mask,
                   (void*)&meta, (void*)&resid, (void*)&counter, (void*)&weight, (void*)&bsum, (void*)&chunk_first,
                   (void*)&svc};
-  cudaError_t e = cudaLaunchCooperativeKernel(sv.two_bit ? (const void*)k_finish<true> : (const void*)k_finish<false>,
+  e = cudaLaunchCooperativeKernel(sv.two_bit ? (const void*)k_finish<true> : (const void*)k_finish<false>,
                                               dim3((unsigned)L.finish_blocks), dim3(kThreads), args, 0, s);
   L.stage(CG_STAGE_APPLY, false, s);
   *L.counter += 1;

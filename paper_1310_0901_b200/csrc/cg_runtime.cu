@@ -40,7 +40,8 @@ struct ArrayEntry {   // NEXT-3 device array (SPEC register_array S:166-168)
 };
 
 struct Layout {
-  uint64_t table, walk, arrays, weight, P, bsum, fbsum, chunk, meta, resid, dvoff, scratch, waves, marks, flags, leaks, desc_stage,
+  uint64_t table, walk, arrays, weight, P, bsum, fbsum, chunk, meta, resid, defer, dvoff, scratch, waves, marks, flags, leaks,
+      desc_stage, chunk_list,
       verdict_stage, raw_stage,
       idx_stage, dirty_stage, dir, total;
   uint32_t dir_bits;
@@ -59,6 +60,7 @@ bool valid_config(const cg_config* c) {
   uint64_t sb = c->shard_size ? c->shard_base : c->host_base;
   uint64_t ss = c->shard_size ? c->shard_size : c->host_size;
   if (sb % 4096 || ss % 4096 || ss == 0) return false;
+  if (ss > cgk::kMaxShardBytes) return false;   // one GPU stores at most 2^38 host bytes (no B200 holds more shadow)
   if (sb < c->host_base || sb + ss > c->host_base + c->host_size) return false;
   if (c->max_descs == 0 || c->max_descs > cgk::kMaxDescs) return false;
   if (c->max_allocs == 0 || c->max_allocs > (1ull << 32)) return false;
@@ -90,6 +92,7 @@ Layout layout_of(const cg_config* c) {
   L.chunk = take(L.max_chunks * 4);
   L.meta = take(c->max_descs * std::max(cgk::scan_meta_bytes(), cgk::prop_meta_bytes()));
   L.resid = take(c->max_descs * sizeof(uint32_t));
+  L.defer = take(c->max_descs * sizeof(uint32_t));
   L.dvoff = c->dev_vbuf ? take(c->max_descs * 16) : 0;
   L.scratch = c->dev_vbuf ? take(cgk::stage_bytes()) : 0;
   L.waves = c->dev_vbuf ? take((c->max_descs + 1) * sizeof(uint32_t)) : 0;   // NEXT-1 wave offsets
@@ -108,6 +111,7 @@ Layout layout_of(const cg_config* c) {
     const uint64_t nsec = c->host_size / 65536 + 1;
     while ((1ull << L.dir_bits) < 2 * nsec) ++L.dir_bits;
     L.dir = take((1ull << L.dir_bits) * 12);
+    L.chunk_list = take(nsec * 8);   // the chunks with a secondary, ascending (deferred pass)
   }
   L.total = off;
   return L;
@@ -166,9 +170,15 @@ struct cg_ctx {
     }
     return true;
   }
+  std::vector<uint64_t> chunk_ids;          // sorted chunk list image (sparse map)
   cg_status upload_dir(cudaStream_t s) {
     if (!dir_dirty) return CG_OK;
     cudaError_t e = cudaMemcpyAsync(ws + lay.dir, dir_host.data(), dir_host.size() * 4, cudaMemcpyHostToDevice, s);
+    chunk_ids.clear();
+    for (const auto& kv : chunks) chunk_ids.push_back(kv.first);
+    if (e == cudaSuccess && !chunk_ids.empty())
+      e = cudaMemcpyAsync(ws + lay.chunk_list, chunk_ids.data(), chunk_ids.size() * 8, cudaMemcpyHostToDevice, s);
+    sv.n_chunks = chunk_ids.size();
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);   // the host image may change right after
     if (e != cudaSuccess) return cuda(e, "directory upload");
     dir_dirty = false;
@@ -252,6 +262,7 @@ struct cg_ctx {
     p.meta = ws + lay.meta;
     p.counter = reinterpret_cast<uint32_t*>(ws + lay.flags + 128);
     p.resid = reinterpret_cast<uint32_t*>(ws + lay.resid);
+    p.defer = reinterpret_cast<uint32_t*>(ws + lay.defer);
     p.dvoff = cfg.dev_vbuf ? reinterpret_cast<uint64_t*>(ws + lay.dvoff) : nullptr;
     p.max_chunks = lay.max_chunks;
     p.t_min = kChunkMin;
@@ -404,6 +415,7 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
     c->sv.dir_bits = lay.dir_bits;
     c->sv.dir_key = reinterpret_cast<const uint64_t*>(c->ws + lay.dir);
     c->sv.dir_val = reinterpret_cast<const uint32_t*>(c->ws + lay.dir + (8ull << lay.dir_bits));
+    c->sv.chunk_list = reinterpret_cast<const uint64_t*>(c->ws + lay.chunk_list);
     c->dir_host.assign((1ull << lay.dir_bits) * 3, 0u);   // keys (2 words each) + values
   }
   cudaDeviceProp prop;

@@ -44,6 +44,7 @@ def replay_events(chk, events: np.ndarray, blob=None, stream=None, fuse: bool = 
     is_copy = ops == OP_COPY
     copy_rank = np.cumsum(is_copy) - 1
     verdicts = np.zeros(int(is_copy.sum()), VERDICT_DTYPE)
+    regs_since = 0
     i = 0
     while i < n:
         op = ops[i]
@@ -71,6 +72,14 @@ def replay_events(chk, events: np.ndarray, blob=None, stream=None, fuse: bool = 
                 status[i] = 1
                 i += 1
                 continue
+            # every later copy has seq >= this block's first seq: tombstones freed
+            # before it are invisible to them (cg_registry_compact), so drop
+            # them before the table (live + tombstones) can fill up
+            n_reg = int(np.count_nonzero((ops[i:j] == OP_REG) | (ops[i:j] == OP_REGA)))
+            regs_since += n_reg
+            if regs_since > getattr(chk, "max_allocs", 1 << 62) // 2:
+                chk.registry_compact(int(events["seq"][i]))
+                regs_since = n_reg
             for k in range(i, j):
                 if ops[k] == OP_REG:
                     status[k] = chk.register_alloc(int(events["dst"][k]), int(events["width"][k]),

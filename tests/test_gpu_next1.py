@@ -95,8 +95,7 @@ def test_self_overlapping_dtod(cg, shape, shift):
     if shape == "1d":
         tb.copy1d(tg.DTOD, d + s0 + shift, d + s0, 20000)
     elif shape == "2d_equal":
-        tb.copy2d(tg.DTOD, 300, 40, d, 0, 0, 700, d, 0, 0, 700) if False else \
-            tb.copy2d(tg.DTOD, 300, 40, d + s0 + shift, 0, 0, 700, d + s0, 0, 0, 700)
+        tb.copy2d(tg.DTOD, 300, 40, d + s0 + shift, 0, 0, 700, d + s0, 0, 0, 700)
     else:
         tb.copy2d(tg.DTOD, 300, 40, d + s0 + shift, 0, 0, 650, d + s0, 0, 0, 700)
     run_tracking(cg, tb.build())
