@@ -65,9 +65,13 @@ enum {
  * pitched range like HTOD's source / DTOH's destination (pitch rule on the host
  * side only).  The array must be live at desc.seq (else *_NOT_ALLOCATED) and
  * offset + width*height <= its total bytes (else *_TOO_SMALL with expected =
- * width*height, found = total - offset or 0; R-29).  Array contents
- * carry no V-bits (R-30): an error-free ATOH makes its host range defined, an
- * HTOA only reads the host shadow. */
+ * width*height, found = total - offset or 0; R-29).  Array V-bits
+ * (R-30, "array V-bits tracked in a per-array shadow"): without device
+ * V-bit tracking an error-free ATOH makes its host range defined and an HTOA
+ * only reads the host shadow (as DTOH / HTOD, R-5); with tracking
+ * (cfg.dev_vbuf) every array gets its own V-bits in the pool (fresh =
+ * undefined) and error-free HTOA / ATOH copy V-bits host -> array / array ->
+ * host. */
 enum { CG_HTOD = 1, CG_DTOH = 2, CG_DTOD = 3, CG_HTOA = 4, CG_ATOH = 5 };
 
 /* ---- host mark states (SPEC S:355-358 host_alloc / host_write / host_free) ---- */
@@ -391,7 +395,8 @@ cg_status cg_apply_dtoh(cg_ctx *ctx, const cg_copy_desc *d_descs, const cg_verdi
 /* The a6 step generalised (NEXT-1): without device V-bit tracking identical
  * to cg_apply_dtoh; with it, every descriptor whose verdict is OK moves its
  * V-bits (HtoD: host -> device pool, DtoD: pool -> pool as if staged through a
- * scratch buffer, DtoH: pool -> host; AtoH: host defined, HtoA: nothing, R-30).  Must follow the cg_check_copies call of
+ * scratch buffer, DtoH: pool -> host; HtoA: host -> array V-bits, AtoH: array
+ * V-bits -> host, R-30).  Must follow the cg_check_copies call of
  * the same descriptor array (it uses the device V offsets that check found);
  * the batch must be hazard-free for propagation (cg_plan_batches with
  * CG_PLAN_PROPAGATE).  With tracking it synchronises on stream at the end.
@@ -441,6 +446,12 @@ cg_status cg_plan_waves(const cg_copy_desc *h_descs, uint64_t n, uint32_t *h_lev
  * CG_ERR_NOT_INITIALIZED without tracking; CG_ERR_INVALID_VALUE if the range
  * is not inside one live allocation. */
 cg_status cg_device_vbits(cg_ctx *ctx, uint64_t addr, uint64_t len, uint8_t *h_out);
+
+/* NEXT-1 x NEXT-3: downloads the V-bits of bytes [offset, offset+len) of the
+ * live array `handle` (its per-array shadow; R-30) to h_out.
+ * Synchronous.  Errors: CG_ERR_NOT_INITIALIZED without tracking;
+ * CG_ERR_INVALID_VALUE if there is no such live array or the range leaves it. */
+cg_status cg_array_vbits(cg_ctx *ctx, uint64_t handle, uint64_t offset, uint64_t len, uint8_t *h_out);
 
 /* cg_check_copies followed by cg_apply_dtoh, fused: the shadow scan applies
  * every DtoH descriptor that fits one of its work groups as soon as its verdict

@@ -78,6 +78,7 @@ def _load():
         lib.or_free_array.restype = I; lib.or_free_array.argtypes = [P, U64, U64]
         lib.or_array_leaks.restype = U64; lib.or_array_leaks.argtypes = [P, P, U64]
         lib.or_device_vbits.restype = I; lib.or_device_vbits.argtypes = [P, U64, U64, P]
+        lib.or_array_vbits.restype = I; lib.or_array_vbits.argtypes = [P, U64, U64, U64, P]
         lib.or_track_concurrency.argtypes = [P, I]
         lib.or_sync.argtypes = [P, U32, U64]
         lib.or_check_copy_mt.argtypes = [P, P, U32, P]
@@ -150,6 +151,13 @@ class Oracle:
     def device_vbits(self, addr: int, length: int) -> Optional[np.ndarray]:
         out = np.zeros(max(length, 1), np.uint8)
         if self.lib.or_device_vbits(self.st, addr, length, out.ctypes.data):
+            return None
+        return out[:length]
+
+    def array_vbits(self, handle: int, offset: int, length: int) -> Optional[np.ndarray]:
+        """NEXT-1 x NEXT-3: V-bytes of an array's per-array shadow"""
+        out = np.zeros(max(length, 1), np.uint8)
+        if self.lib.or_array_vbits(self.st, handle, offset, length, out.ctypes.data):
             return None
         return out[:length]
 

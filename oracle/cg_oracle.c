@@ -86,6 +86,7 @@ typedef struct {
     uint64_t n_live, cap_live;
     int track;             /* NEXT-1: propagate V-bits through copies (SPEC copy_vbits) */
     or_alloc *arr;         /* NEXT-3: unsorted list of live device arrays {handle, total_bytes, seq} */
+    uint8_t **av;          /* NEXT-3 x NEXT-1: V-bytes of arr[i] (track mode), else NULL */
     uint64_t n_arr, cap_arr;
     uint64_t last_reg_seq;
     int undef_is_error;    /* CLI flag promotes HostUndefined */
@@ -121,7 +122,8 @@ void or_track_device(or_state *st, int on) { st->track = on; }
 void or_destroy(or_state *st) {
     if (!st) return;
     for (uint64_t i = 0; i < st->n_live; i++) free(st->dv[i]);
-    free(st->A); free(st->V); free(st->live); free(st->dv); free(st->arr);
+    for (uint64_t i = 0; i < st->n_arr; i++) free(st->av[i]);
+    free(st->A); free(st->V); free(st->live); free(st->dv); free(st->arr); free(st->av);
     free(st->stamps[0]); free(st->stamps[1]); free(st->syncs); free(st);
 }
 
@@ -222,10 +224,16 @@ int or_register_array(or_state *st, uint64_t handle, uint64_t total, uint64_t se
     if (st->n_arr == st->cap_arr) {
         st->cap_arr = st->cap_arr ? 2 * st->cap_arr : 16;
         st->arr = (or_alloc *)realloc(st->arr, st->cap_arr * sizeof(or_alloc));
+        st->av = (uint8_t **)realloc(st->av, st->cap_arr * sizeof(uint8_t *));
     }
     st->arr[st->n_arr].base = handle;
     st->arr[st->n_arr].size = total;
     st->arr[st->n_arr].seq = seq;
+    st->av[st->n_arr] = NULL;
+    if (st->track) {                       /* S:252 per-array shadow; fresh = undefined */
+        st->av[st->n_arr] = (uint8_t *)malloc(total);
+        memset(st->av[st->n_arr], 0xFF, total);
+    }
     st->n_arr++;
     st->last_reg_seq = seq;
     return 0;
@@ -236,7 +244,9 @@ int or_free_array(or_state *st, uint64_t handle, uint64_t seq) {
     if (seq <= st->last_reg_seq) return 1;
     for (uint64_t i = 0; i < st->n_arr; i++) {
         if (st->arr[i].base == handle) {
+            free(st->av[i]);
             st->arr[i] = st->arr[st->n_arr - 1];
+            st->av[i] = st->av[st->n_arr - 1];
             st->n_arr--;
             st->last_reg_seq = seq;
             return 0;
@@ -359,13 +369,25 @@ static void host_scan(const or_state *st, uint64_t start, uint64_t pitch, uint64
     }
 }
 
+/* array V-bytes [off, off+len) of the live array `handle` into out (test view;
+ * 1 if there is none, it has no V-bytes or the range leaves it) */
+int or_array_vbits(const or_state *st, uint64_t handle, uint64_t off, uint64_t len, uint8_t *out) {
+    for (uint64_t i = 0; i < st->n_arr; i++) {
+        if (st->arr[i].base != handle) continue;
+        if (!st->av[i] || off > st->arr[i].size || len > st->arr[i].size - off) return 1;
+        memcpy(out, st->av[i] + off, len);
+        return 0;
+    }
+    return 1;
+}
+
 /* NEXT-3 check_array_transfer: the array side is (handle, byte
  * offset) = (dst, dst_x) for HtoA and (src, src_x) for AtoH; the array holds
  * the W*H logical bytes contiguously from the offset.  Unknown handle ->
  * *_NOT_ALLOCATED; offset + W*H > total_bytes -> *_TOO_SMALL with expected =
  * W*H and found = total_bytes - offset (0 past the end).  The host side is
  * checked as for HtoD / DtoH (pitch rule on the host side only). */
-static void check_array_copy(or_state *st, const or_event *ev, or_verdict *v) {
+static void check_array_copy(const or_state *st, const or_event *ev, or_verdict *v) {
     const int htoa = ev->kind == OR_HTOA;
     const uint64_t W = ev->width, H = ev->height;
     const uint64_t handle = htoa ? ev->dst : ev->src, off = htoa ? ev->dst_x : ev->src_x;
@@ -397,14 +419,10 @@ static void check_array_copy(or_state *st, const or_event *ev, or_verdict *v) {
     if (v->undef_count > 0 && v->first_unaddr == OR_NONE) v->flags |= F_HOST_UNDEFINED;
     const uint32_t errors = v->flags & ~(st->undef_is_error ? 0u : F_HOST_UNDEFINED);
     v->status = errors ? 1u : 0u;
-    /* AtoH with no Error: the host bytes become defined (R-5, also in NEXT-1
-     * mode: array V-bits are not tracked, R-30) */
-    if (!htoa && v->status == 0)
-        for (uint64_t r = 0; r < H && W; r++)
-            for (uint64_t c = 0; c < W; c++) st->V[hs + r * hp + c - st->h0] = 0x00;
 }
 
-void or_check_copy(or_state *st, const or_event *ev, or_verdict *v) {
+/* O5 (i)-(iv): the checks of one copy; reads the state, changes nothing */
+static void check_only(const or_state *st, const or_event *ev, or_verdict *v) {
     v->first_unaddr = OR_NONE; v->first_undef = OR_NONE; v->undef_count = 0;
     v->dst_expected = v->dst_found = v->src_expected = v->src_found = 0;
     v->flags = 0; v->status = 0;
@@ -447,30 +465,66 @@ void or_check_copy(or_state *st, const or_event *ev, or_verdict *v) {
     if (v->undef_count > 0 && v->first_unaddr == OR_NONE) v->flags |= F_HOST_UNDEFINED;
     uint32_t errors = v->flags & ~(st->undef_is_error ? 0u : F_HOST_UNDEFINED);
     v->status = errors ? 1u : 0u;
+}
 
-    /* (v) DtoH with no Error: the written host bytes become defined (R-5, R-7) */
-    if (kind == OR_DTOH && v->status == 0 && !st->track) {
-        for (uint64_t r = 0; r < H && W; r++)
-            for (uint64_t c = 0; c < W; c++)
-                st->V[ds + r * ev->dst_pitch + c - st->h0] = 0x00;
+/* (v) without device V-bits: the host bytes an error-free DtoH / AtoH wrote
+ * become defined (R-5, R-7) -- those of them inside [lo, hi) (the whole
+ * window in the sequential replay; one thread's slice in the parallel one) */
+static void apply_defined(or_state *st, const or_event *ev, uint64_t lo, uint64_t hi) {
+    const uint64_t W = ev->width, H = ev->height;
+    const uint64_t hs = ev->dst + ev->dst_y * ev->dst_pitch + ev->dst_x;   /* fits: no Error */
+    for (uint64_t r = 0; r < H && W; r++) {
+        const uint64_t xr = hs + r * ev->dst_pitch;
+        for (uint64_t c = 0; c < W; c++)
+            if (xr + c >= lo && xr + c < hi) st->V[xr + c - st->h0] = 0x00;
     }
-    /* (v') NEXT-1: with device V-bits, an error-free copy moves V-bits */
-    if (st->track && v->status == 0 && W && H) {
-        uint8_t *dd = NULL, *sd = NULL;   /* device V of dst / src at their start */
-        if (kind == OR_HTOD || kind == OR_DTOD) dd = device_vbits(st, ds);
-        if (kind == OR_DTOH || kind == OR_DTOD) sd = device_vbits(st, ss);
-        uint8_t *tmp = (uint8_t *)malloc(W * H);           /* logical order, staged */
-        for (uint64_t r = 0; r < H; r++)
-            for (uint64_t c = 0; c < W; c++)
-                tmp[r * W + c] = (kind == OR_HTOD) ? st->V[ss + r * ev->src_pitch + c - st->h0]
-                                                   : sd[r * ev->src_pitch + c];
-        for (uint64_t r = 0; r < H; r++)
-            for (uint64_t c = 0; c < W; c++) {
-                if (kind == OR_DTOH) st->V[ds + r * ev->dst_pitch + c - st->h0] = tmp[r * W + c];
-                else dd[r * ev->dst_pitch + c] = tmp[r * W + c];
-            }
-        free(tmp);
-    }
+}
+
+/* NEXT-3 x NEXT-1 ("array V-bits tracked in a per-array shadow", R-30):
+ * the V-bytes of the live array with this handle, at the byte offset */
+static uint8_t *array_vbits(const or_state *st, uint64_t handle, uint64_t off) {
+    for (uint64_t i = 0; i < st->n_arr; i++)
+        if (st->arr[i].base == handle) return st->av[i] + off;
+    return NULL;
+}
+
+/* (v') NEXT-1: with device V-bits, an error-free copy moves V-bits (SPEC
+ * copy_vbits S:81-89): host -> device, device -> device (staged: memmove,
+ * S:84), device -> host, and with arrays host -> array / array -> host (R-30) */
+static void move_vbits(or_state *st, const or_event *ev) {
+    const uint32_t kind = ev->kind;
+    const uint64_t W = ev->width, H = ev->height;
+    if (!W || !H) return;
+    const uint64_t ds = ev->dst + ev->dst_y * ev->dst_pitch + ev->dst_x;
+    const uint64_t ss = ev->src + ev->src_y * ev->src_pitch + ev->src_x;
+    uint8_t *dd = NULL, *sd = NULL;   /* device / array V of dst / src at their start */
+    if (kind == OR_HTOD || kind == OR_DTOD) dd = device_vbits(st, ds);
+    if (kind == OR_DTOH || kind == OR_DTOD) sd = device_vbits(st, ss);
+    if (kind == OR_HTOA) dd = array_vbits(st, ev->dst, ev->dst_x);
+    if (kind == OR_ATOH) sd = array_vbits(st, ev->src, ev->src_x);
+    const int host_src = kind == OR_HTOD || kind == OR_HTOA, host_dst = kind == OR_DTOH || kind == OR_ATOH;
+    /* an array side is W*H contiguous bytes from its offset (R-29): pitch W, no y */
+    const uint64_t sp = kind == OR_ATOH ? W : ev->src_pitch, dp = kind == OR_HTOA ? W : ev->dst_pitch;
+    const uint64_t hs = kind == OR_HTOA ? ev->src + ev->src_y * ev->src_pitch + ev->src_x : ss;
+    const uint64_t hd = kind == OR_ATOH ? ev->dst + ev->dst_y * ev->dst_pitch + ev->dst_x : ds;
+    uint8_t *tmp = (uint8_t *)malloc(W * H);           /* logical order, staged */
+    for (uint64_t r = 0; r < H; r++)
+        for (uint64_t c = 0; c < W; c++)
+            tmp[r * W + c] = host_src ? st->V[hs + r * sp + c - st->h0] : sd[r * sp + c];
+    for (uint64_t r = 0; r < H; r++)
+        for (uint64_t c = 0; c < W; c++) {
+            if (host_dst) st->V[hd + r * dp + c - st->h0] = tmp[r * W + c];
+            else dd[r * dp + c] = tmp[r * W + c];
+        }
+    free(tmp);
+}
+
+/* O5: check one copy, then (no Error) its effect on the shadow */
+void or_check_copy(or_state *st, const or_event *ev, or_verdict *v) {
+    check_only(st, ev, v);
+    if (v->status != 0) return;                              /* R-7: the copy fails, nothing moves */
+    if (st->track) move_vbits(st, ev);
+    else if (ev->kind == OR_DTOH || ev->kind == OR_ATOH) apply_defined(st, ev, st->h0, st->h0 + st->s);
 }
 
 /* ------------------------------------------------------ O7 concurrency */

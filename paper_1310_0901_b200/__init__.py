@@ -105,6 +105,7 @@ def _load() -> ctypes.CDLL:
         "cg_format_verdict": (U64, [P, U32, P, U64]),
         "cg_apply_copies": (I, [P, P, P, U64, P]),
         "cg_device_vbits": (I, [P, U64, U64, P]),
+        "cg_array_vbits": (I, [P, U64, U64, U64, P]),
         "cg_plan_batches_propagate": (I, [P, U64, P, P]),
         "cg_format_leak": (U64, [P, P, U64]),
         "cg_shard_plan": (I, [P, U64, U64, U64, U32, P, P, P]),
@@ -148,7 +149,7 @@ EXPORTED = ("cg_workspace_size", "cg_ctx_create", "cg_ctx_destroy", "cg_last_err
             "cg_plan_batches", "cg_kernel_launches", "cg_profile_begin", "cg_profile_end", "cg_check_apply",
             "cg_batch_disjoint", "cg_straddler_pack", "cg_straddler_finalize", "cg_compact_dirty", "cg_shard_plan",
             "cg_host_query_addressable", "cg_expand_copy1d", "cg_check_host", "cg_check_host_submit", "cg_check_host_wait", "cg_format_verdict",
-            "cg_format_leak", "cg_apply_copies", "cg_device_vbits", "cg_plan_batches_propagate",
+            "cg_format_leak", "cg_apply_copies", "cg_device_vbits", "cg_array_vbits", "cg_plan_batches_propagate",
             "cg_host_shadow_read", "cg_apply_copies_subset", "cg_plan_waves", "cg_apply_flush", "cg_apply_copies_waves", "cg_summarize", "cg_format_summary", "cg_array_bytes", "cg_register_array", "cg_free_array", "cg_array_report", "cg_conc_create",
             "cg_conc_destroy", "cg_conc_last_error", "cg_conc_sync", "cg_conc_check", "cg_conc_stamps",
             "cg_conc_kernel_launches")
@@ -180,6 +181,7 @@ cg_format_verdict = _lib.cg_format_verdict
 cg_format_leak = _lib.cg_format_leak
 cg_apply_copies = _lib.cg_apply_copies
 cg_device_vbits = _lib.cg_device_vbits
+cg_array_vbits = _lib.cg_array_vbits
 cg_plan_batches_propagate = _lib.cg_plan_batches_propagate
 cg_array_bytes = _lib.cg_array_bytes
 cg_host_shadow_read = _lib.cg_host_shadow_read
@@ -509,6 +511,12 @@ class Checker:
         out = np.zeros(max(length, 1), np.uint8)
         self.torch.cuda.synchronize(self.device)
         self._ok(_lib.cg_device_vbits(self.ctx, addr, length, out.ctypes.data), "cg_device_vbits")
+        return out[:length]
+
+    def array_vbits(self, handle: int, offset: int, length: int) -> np.ndarray:
+        out = np.zeros(max(length, 1), np.uint8)
+        self.torch.cuda.synchronize(self.device)
+        self._ok(_lib.cg_array_vbits(self.ctx, handle, offset, length, out.ctypes.data), "cg_array_vbits")
         return out[:length]
 
     def check_apply(self, d_descs, d_out=None, stream=None):

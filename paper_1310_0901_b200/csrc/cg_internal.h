@@ -89,6 +89,7 @@ struct Table {
   const uint64_t* atotal;
   const uint64_t* aaseq;
   const uint64_t* afseq;
+  const uint64_t* apool;   // NEXT-1 x NEXT-3: device V-pool offset of each array's V-bits (nullptr without tracking)
   uint64_t na;
   uint32_t stride;   // splitter stride (every stride-th base is staged in smem)
   uint32_t nsplit;

@@ -321,7 +321,8 @@ __device__ __forceinline__ bool table_lookup(const Table& t, const uint64_t* s_s
 }
 
 // NEXT-3: the array with this handle alive at seq -> its total bytes
-__device__ __forceinline__ bool array_lookup(const Table& t, uint64_t handle, uint64_t seq, uint64_t& total) {
+__device__ __forceinline__ bool array_lookup(const Table& t, uint64_t handle, uint64_t seq, uint64_t& total,
+                                             uint64_t& idx) {
   uint64_t lo = 0, hi = t.na;   // first entry with handle >= handle
   while (lo < hi) {
     const uint64_t mid = (lo + hi) >> 1;
@@ -330,6 +331,7 @@ __device__ __forceinline__ bool array_lookup(const Table& t, uint64_t handle, ui
   for (uint64_t j = lo; j < t.na && __ldg(t.ahandle + j) == handle; ++j) {
     if (__ldg(t.aaseq + j) < seq && seq < __ldg(t.afseq + j)) {
       total = __ldg(t.atotal + j);
+      idx = j;
       return true;
     }
   }
@@ -359,10 +361,11 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
                                           ScanMeta* __restrict__ meta, uint64_t* __restrict__ dvoff,
                                           const ShadowView& sv, uint32_t* __restrict__ counter,
                                           uint32_t* __restrict__ defer, uint64_t* s_split) {
-  // the scan's group counter, (apply count), residual count, deferred list
-  // count and cursor: reset here instead of by a memset node, which would
-  // break the PDL chain
-  if (blockIdx.x == 0 && threadIdx.x < 6 && threadIdx.x != 3) counter[threadIdx.x] = 0;
+  // the scan's group counter, (apply count), residual count: reset here
+  // instead of by a memset node, which would break the PDL chain.  The
+  // deferred list (count, cursor: counter[4], [5]) is appended to right here,
+  // so the kernel after the scan resets it for the next check.
+  if (blockIdx.x == 0 && threadIdx.x < 3) counter[threadIdx.x] = 0;
   load_splitters(t, s_split);
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
@@ -374,14 +377,18 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
     uint64_t dv_dst = 0, dv_src = 0;   // NEXT-1: device V-bit offsets in the pool
     if (nm.kind >= CG_HTOA && owner) {  // NEXT-3: array side
       const bool htoa = nm.kind == CG_HTOA;
-      uint64_t total;
+      uint64_t total, j;
       if (nm.aok) {
-        if (!array_lookup(t, nm.ahandle, d.seq, total)) {
+        if (!array_lookup(t, nm.ahandle, d.seq, total, j)) {
           flags |= htoa ? CG_F_DST_NOT_ALLOCATED : CG_F_SRC_NOT_ALLOCATED;
-        } else if (nm.aoff + d.width * d.height > total) {
-          flags |= htoa ? CG_F_DST_TOO_SMALL : CG_F_SRC_TOO_SMALL;
-          const uint64_t ex = d.width * d.height, fd = nm.aoff < total ? total - nm.aoff : 0;
-          if (htoa) { de = ex; df = fd; } else { se = ex; sf = fd; }
+        } else {
+          if (nm.aoff + d.width * d.height > total) {
+            flags |= htoa ? CG_F_DST_TOO_SMALL : CG_F_SRC_TOO_SMALL;
+            const uint64_t ex = d.width * d.height, fd = nm.aoff < total ? total - nm.aoff : 0;
+            if (htoa) { de = ex; df = fd; } else { se = ex; sf = fd; }
+          }
+          // NEXT-1 x NEXT-3 (S:252 per-array shadow, R-30): the array side's V-bits in the pool
+          if (t.apool) (htoa ? dv_dst : dv_src) = __ldg(t.apool + j) + nm.aoff;
         }
       }
     } else if (!(flags & CG_F_BAD_KIND) && owner) {
@@ -1694,6 +1701,9 @@ __global__ void __launch_bounds__(kThreads) k_finalize_split(uint64_t n, const u
                                                              uint32_t* __restrict__ resid,
                                                              uint32_t* __restrict__ resid_n) {
   pdl_entry();
+  // the deferred list of the next check starts empty (its prep appends to it,
+  // so it cannot reset it itself); resid_n = counter + 2
+  if (blockIdx.x == 0 && threadIdx.x == 0) resid_n[2] = resid_n[3] = 0;
   const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
   for (uint64_t d = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; d < n;
        d += (uint64_t)gridDim.x * blockDim.x) {
@@ -1984,7 +1994,10 @@ __global__ void __launch_bounds__(kThreads) k_finish(
       if (status == CG_OK && ((info >> kInfoKind) & 3u) == CG_DTOH && ((info >> kInfoHost) & 1u))
         resid[atomicAdd(resid_n, 1u)] = (uint32_t)d;
     }
-    if (tid == 0) counter[0] = 0;   // the apply walk's group counter
+    if (tid == 0) {
+      counter[0] = 0;   // the apply walk's group counter
+      counter[4] = counter[5] = 0;   // the deferred list of the next check (the prep appends to it)
+    }
   }
   grid.sync();
   const uint64_t m = __ldcg(resid_n);
@@ -2103,14 +2116,20 @@ __global__ void __launch_bounds__(kThreads) k_prop_prep(const cg_copy_desc* __re
       const cg_copy_desc d = descs[i];
       const Norm nm = normalize(d);
       const uint64_t nb = d.width * d.height;   // status OK: no INVALID_RANGE, so no overflow
-      if (nb && d.kind != CG_HTOA) {   // array V-bits are not tracked (R-30): HtoA moves nothing
+      if (nb) {
         m.W = d.width;
         m.spitch = d.src_pitch;
         m.dpitch = d.dst_pitch;
-        if (d.kind == CG_ATOH) {       // ... and AtoH makes the host bytes defined (R-5)
-          m.src = 0;
+        if (d.kind == CG_HTOA) {       // S:252 / R-30: host -> the array's V-bits (W*H contiguous bytes)
+          m.src = nm.ss - sb;
+          m.dst = dvoff[2 * i];
+          m.dpitch = d.width;
+          m.info = nb | (1ull << 42);
+        } else if (d.kind == CG_ATOH) {   // the array's V-bits -> host
+          m.src = dvoff[2 * i + 1];
+          m.spitch = d.width;
           m.dst = nm.ds - sb;
-          m.info = nb | (1ull << 43);
+          m.info = nb | (1ull << 41);
         } else if (d.kind == CG_HTOD) {
           m.src = nm.ss - sb;
           m.dst = dvoff[2 * i];
@@ -2262,7 +2281,7 @@ __device__ __forceinline__ void block_zero(uint8_t* dst, uint64_t len) {
 // self-overlapping DtoD, which the caller hands to the memmove list)
 struct WaveCopy {
   uint8_t *sbase, *dbase;
-  uint64_t src, dst, W, nb;
+  uint64_t src, dst, W, nb, spitch, dpitch;
   bool zero, self_overlap;
 };
 __device__ __forceinline__ bool wave_copy(const cg_copy_desc& d, uint32_t i, const uint64_t* dvoff, uint64_t sb,
@@ -2270,13 +2289,22 @@ __device__ __forceinline__ bool wave_copy(const cg_copy_desc& d, uint32_t i, con
   w.W = d.width;
   w.nb = d.width * d.height;
   w.zero = w.self_overlap = false;
-  if (w.nb == 0 || d.kind == CG_HTOA || d.kind < CG_HTOD || d.kind > CG_ATOH) return false;
+  w.spitch = d.src_pitch;
+  w.dpitch = d.dst_pitch;
+  if (w.nb == 0 || d.kind < CG_HTOD || d.kind > CG_ATOH) return false;
   const Norm nm = normalize(d);
   w.sbase = w.dbase = V;
   w.src = w.dst = 0;
-  if (d.kind == CG_ATOH) {   // R-30: the host range becomes defined
+  if (d.kind == CG_HTOA) {   // S:252 / R-30: host -> the array's V-bits
+    w.src = nm.ss - sb;
+    w.dst = dvoff[2 * i];
+    w.dbase = pool;
+    w.dpitch = d.width;
+  } else if (d.kind == CG_ATOH) {   // the array's V-bits -> host
+    w.src = dvoff[2 * i + 1];
+    w.sbase = pool;
+    w.spitch = d.width;
     w.dst = nm.ds - sb;
-    w.zero = true;
   } else if (d.kind == CG_HTOD) {
     w.src = nm.ss - sb;
     w.dst = dvoff[2 * i];
@@ -2318,8 +2346,8 @@ __global__ void __launch_bounds__(kThreads) k_prop_direct_warp(const cg_copy_des
       continue;
     }
     for (uint64_t r = 0; r < d.height; ++r) {
-      if (w.zero) warp_store_zero(w.dbase, w.dst + r * d.dst_pitch, w.dst + r * d.dst_pitch + w.W);
-      else warp_copy(w.dbase + w.dst + r * d.dst_pitch, w.sbase + w.src + r * d.src_pitch, w.W);
+      if (w.zero) warp_store_zero(w.dbase, w.dst + r * w.dpitch, w.dst + r * w.dpitch + w.W);
+      else warp_copy(w.dbase + w.dst + r * w.dpitch, w.sbase + w.src + r * w.spitch, w.W);
     }
   }
 }
@@ -2348,8 +2376,8 @@ __global__ void __launch_bounds__(kThreads) k_prop_direct(const cg_copy_desc* __
   uint64_t r = lo / W, c = lo - r * W, o = lo;
   while (o < hi) {   // row segments (R-11); both sides advance by their own pitch
     const uint64_t len = umin64(W - c, hi - o);
-    if (w.zero) block_zero(dbase + dst + r * d.dst_pitch + c, len);
-    else block_copy(dbase + dst + r * d.dst_pitch + c, sbase + src + r * d.src_pitch + c, len);
+    if (w.zero) block_zero(dbase + dst + r * w.dpitch + c, len);
+    else block_copy(dbase + dst + r * w.dpitch + c, sbase + src + r * w.spitch + c, len);
     o += len;
     ++r;
     c = 0;
@@ -2462,15 +2490,21 @@ __global__ void __launch_bounds__(kThreads) k_wave_prep(const cg_copy_desc* __re
     if (verd[i].status == CG_OK) {
       const cg_copy_desc d = descs[i];
       const uint64_t nb = d.width * d.height;   // status OK: no INVALID_RANGE, so no overflow
-      if (nb && d.kind != CG_HTOA) {   // array V-bits are not tracked (R-30): HtoA moves nothing
+      if (nb) {
         const Norm nm = normalize(d);
         pmk.W = d.width;
         pmk.spitch = d.src_pitch;
         pmk.dpitch = d.dst_pitch;
-        if (d.kind == CG_ATOH) {       // ... and AtoH makes the host bytes defined (R-5)
-          pmk.src = 0;
+        if (d.kind == CG_HTOA) {       // S:252 / R-30: host -> the array's V-bits (W*H contiguous bytes)
+          pmk.src = nm.ss - sb;
+          pmk.dst = dvoff[2 * i];
+          pmk.dpitch = d.width;
+          pmk.info = nb | (1ull << 42);
+        } else if (d.kind == CG_ATOH) {   // the array's V-bits -> host
+          pmk.src = dvoff[2 * i + 1];
+          pmk.spitch = d.width;
           pmk.dst = nm.ds - sb;
-          pmk.info = nb | (1ull << 43);
+          pmk.info = nb | (1ull << 41);
         } else if (d.kind == CG_HTOD) {
           pmk.src = nm.ss - sb;
           pmk.dst = dvoff[2 * i];

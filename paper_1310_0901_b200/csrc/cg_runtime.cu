@@ -36,7 +36,7 @@ struct Entry {
 };
 
 struct ArrayEntry {   // NEXT-3 device array (SPEC register_array S:166-168)
-  uint64_t handle, total, aseq, fseq;
+  uint64_t handle, total, aseq, fseq, pool;   // pool: NEXT-1 offset of its V-bits (R-30)
 };
 
 struct Layout {
@@ -84,7 +84,7 @@ Layout layout_of(const cg_config* c) {
   };
   L.table = take(6 * c->max_allocs * 8 + (4096 + 3) * 8 + (c->max_allocs / 4 + 16) * 8);   // SoA (+ pool offsets) + splitters + every 4th base
   L.walk = take(4 * c->max_allocs * 8);                      // (prefix max, end, alloc seq, free seq) per entry
-  L.arrays = take(4 * c->max_allocs * 8);                    // NEXT-3 array table (SoA)
+  L.arrays = take(5 * c->max_allocs * 8);                    // NEXT-3 array table (SoA + pool offsets)
   L.weight = take(L.max_items * 8);
   L.P = take((L.max_items + 1) * 8);
   L.bsum = take((cgk::scan_blocks(L.max_items) + 1) * 8);
@@ -202,6 +202,7 @@ struct cg_ctx {
   uint64_t* h_table = nullptr;              // 10 * max_allocs + splitters
   cg_mark* h_marks = nullptr;               // kMarkRun
   uint64_t* h_walk = nullptr;               // 4 * max_allocs: the lookup walk's records before upload
+  uint64_t* h_arrays = nullptr;             // 5 * max_allocs: the array table before upload
   cudaEvent_t staged = nullptr;
   cudaStream_t copy_stream = nullptr;        // host -> device uploads of cg_check_host
   cudaStream_t out_stream = nullptr;         // device -> host dirty-verdict downloads (cg_check_host_wait)
@@ -288,6 +289,7 @@ struct cg_ctx {
     t.atotal = a + cap;
     t.aaseq = a + 2 * cap;
     t.afseq = a + 3 * cap;
+    t.apool = cfg.dev_vbuf ? a + 4 * cap : nullptr;
     t.na = arrays.size();
     const uint64_t stride = split_stride(t.n);
     t.stride = (uint32_t)stride;
@@ -336,7 +338,7 @@ struct cg_ctx {
       if (e != cudaSuccess) return cuda(e, "splitter upload");
     }
     if (const uint64_t na = arrays.size()) {
-      uint64_t* ha = h_table + ((6 * cap + 1) & ~1ull) + 4096 + 3;
+      uint64_t* ha = h_arrays;
       if (!n) {
         cudaError_t e = cudaEventSynchronize(staged);
         if (e != cudaSuccess) return cuda(e, "cudaEventSynchronize");
@@ -346,9 +348,10 @@ struct cg_ctx {
         ha[cap + i] = arrays[i].total;
         ha[2 * cap + i] = arrays[i].aseq;
         ha[3 * cap + i] = arrays[i].fseq;
+        ha[4 * cap + i] = arrays[i].pool;
       }
       uint64_t* da = d(lay.arrays);
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < 5; ++k) {
         cudaError_t e = cudaMemcpyAsync(da + k * cap, ha + k * cap, na * 8, cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) return cuda(e, "array table upload");
       }
@@ -441,6 +444,7 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
   if (cudaMallocHost(&c->h_table, 10 * cfg->max_allocs * 8 + (4096 + 5) * 8 + (cfg->max_allocs / 4 + 16) * 8) != cudaSuccess ||
       cudaMallocHost(&c->h_marks, std::min<uint64_t>(cfg->max_descs, kMarkRun) * sizeof(cg_mark)) != cudaSuccess ||
       cudaMallocHost(&c->h_walk, 4 * cfg->max_allocs * sizeof(uint64_t)) != cudaSuccess ||
+      cudaMallocHost(&c->h_arrays, 5 * cfg->max_allocs * sizeof(uint64_t)) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->staged, cudaEventDisableTiming) != cudaSuccess) {
     cg_ctx_destroy(c);
     return CG_ERR_OUT_OF_MEMORY;
@@ -500,6 +504,7 @@ cg_status cg_ctx_destroy(cg_ctx* c) {
   if (c->h_table) cudaFreeHost(c->h_table);
   if (c->h_marks) cudaFreeHost(c->h_marks);
   if (c->h_walk) cudaFreeHost(c->h_walk);
+  if (c->h_arrays) cudaFreeHost(c->h_arrays);
   delete c;
   return CG_OK;
 }
@@ -886,7 +891,14 @@ cg_status cg_register_array(cg_ctx* c, uint64_t handle, uint64_t width, uint64_t
   if (c->arrays.size() >= c->cfg.max_allocs) return c->fail(CG_ERR_OUT_OF_MEMORY, "array table full");
   auto pos = std::upper_bound(c->arrays.begin(), c->arrays.end(), handle,
                               [](uint64_t h, const ArrayEntry& e) { return h < e.handle; });
-  c->arrays.insert(pos, ArrayEntry{handle, total, seq, cgk::kInf});
+  uint64_t pool = 0;
+  if (c->cfg.dev_vbuf) {   // NEXT-1: the array's V-bits, fresh = undefined (the pool starts 0xFF, never reused)
+    pool = (c->pool_cursor + 15) / 16 * 16;
+    if (pool + total > c->cfg.dev_vsize || pool + total < pool)
+      return c->fail(CG_ERR_OUT_OF_MEMORY, "device V-bit pool full");
+    c->pool_cursor = pool + total;
+  }
+  c->arrays.insert(pos, ArrayEntry{handle, total, seq, cgk::kInf, pool});
   c->live_arrays.emplace(handle, total);
   c->last_seq = seq;
   c->dirty = true;
@@ -1069,6 +1081,23 @@ cg_status cg_device_vbits(cg_ctx* c, uint64_t addr, uint64_t len, uint8_t* h_out
   cudaError_t e = cudaMemcpy(h_out, static_cast<uint8_t*>(c->cfg.dev_vbuf) + pos->pool + (addr - pos->base), len,
                              cudaMemcpyDeviceToHost);
   return c->cuda(e, "device V download");
+}
+
+cg_status cg_array_vbits(cg_ctx* c, uint64_t handle, uint64_t offset, uint64_t len, uint8_t* h_out) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (!c->cfg.dev_vbuf) return c->fail(CG_ERR_NOT_INITIALIZED, "no device V-bit tracking");
+  if (len && !h_out) return c->fail(CG_ERR_INVALID_VALUE, "null output");
+  auto it = c->live_arrays.find(handle);
+  if (it == c->live_arrays.end() || offset > it->second || len > it->second - offset)
+    return c->fail(CG_ERR_INVALID_VALUE, "not inside a live array");
+  auto pos = std::lower_bound(c->arrays.begin(), c->arrays.end(), handle,
+                              [](const ArrayEntry& e, uint64_t h) { return e.handle < h; });
+  for (; pos != c->arrays.end() && pos->handle == handle && pos->fseq != cgk::kInf; ++pos) {
+  }
+  DeviceGuard g(c->cfg.device);
+  cudaError_t e = cudaMemcpy(h_out, static_cast<uint8_t*>(c->cfg.dev_vbuf) + pos->pool + offset, len,
+                             cudaMemcpyDeviceToHost);
+  return c->cuda(e, "array V download");
 }
 
 cg_status cg_check_apply(cg_ctx* c, const cg_copy_desc* d_descs, uint64_t n, cg_verdict* d_out, void* stream) {
@@ -1385,6 +1414,25 @@ static bool side_range(const cg_copy_desc& d, bool dst, uint64_t& lo, uint64_t& 
   return true;
 }
 
+// the V-bit bytes a copy reads / writes (NEXT-1, R-28): host and device sides
+// by address (2D: bounding range); an array side (R-29, R-30) by byte offset
+// [offset, offset + W*H) in that array's own space
+static bool array_side(const cg_copy_desc& d, bool dst, uint64_t& lo, uint64_t& hi) {
+  const uint64_t off = dst ? d.dst_x : d.src_x;
+  if (d.width == 0 || d.height == 0) return false;
+  const unsigned __int128 nb = (unsigned __int128)d.width * d.height;
+  if (off + nb > (unsigned __int128)UINT64_MAX) return false;
+  lo = off;
+  hi = (uint64_t)(off + nb);
+  return true;
+}
+static bool copy_read(const cg_copy_desc& d, uint64_t& lo, uint64_t& hi) {
+  return d.kind == CG_ATOH ? array_side(d, false, lo, hi) : side_range(d, false, lo, hi);
+}
+static bool copy_write(const cg_copy_desc& d, uint64_t& lo, uint64_t& hi) {
+  return d.kind == CG_HTOA ? array_side(d, true, lo, hi) : side_range(d, true, lo, hi);
+}
+
 namespace {
 struct IvSet {   // disjoint merged intervals
   std::map<uint64_t, uint64_t> m;
@@ -1462,24 +1510,28 @@ cg_status cg_plan_waves(const cg_copy_desc* h_descs, uint64_t n, uint32_t* h_lev
   // (it conflicted with all of them), so it replaces the writer entries and
   // clears the reader entries there; reads merge by max.
   LevelMap rd[2], wr[2];
+  std::map<uint64_t, LevelMap> ard, awr;   // per array handle (R-30): its byte offsets
   uint32_t top = 0;
   for (uint64_t i = 0; i < n; ++i) {
     const cg_copy_desc& d = h_descs[i];
     h_level[i] = 0;
     if (d.kind < CG_HTOD || d.kind > CG_ATOH) continue;
-    uint64_t rlo, rhi, wlo, whi;
+    uint64_t rlo = 0, rhi = 0, wlo = 0, whi = 0;
     // the same read / write sets as cg_plan_batches_propagate (R-28, R-30)
-    const bool r_ok = d.kind != CG_ATOH && side_range(d, false, rlo, rhi);
-    const bool w_ok = d.kind != CG_HTOA && side_range(d, true, wlo, whi);
+    const bool r_ok = copy_read(d, rlo, rhi), w_ok = copy_write(d, wlo, whi);
     const int rs = reads_host(d.kind) ? 0 : 1, ws = writes_host(d.kind) ? 0 : 1;
+    LevelMap& R = d.kind == CG_ATOH ? ard[d.src] : rd[rs];
+    LevelMap& Rw = d.kind == CG_ATOH ? awr[d.src] : wr[rs];
+    LevelMap& W = d.kind == CG_HTOA ? awr[d.dst] : wr[ws];
+    LevelMap& Wr = d.kind == CG_HTOA ? ard[d.dst] : rd[ws];
     uint32_t lv = 0;   // = 1 + the highest conflicting earlier level (maps hold level + 1), 0 if none
-    if (r_ok) lv = std::max(lv, wr[rs].max_over(rlo, rhi));                                        // RAW
-    if (w_ok) lv = std::max(lv, std::max(rd[ws].max_over(wlo, whi), wr[ws].max_over(wlo, whi)));   // WAR, WAW
+    if (r_ok) lv = std::max(lv, Rw.max_over(rlo, rhi));                                      // RAW
+    if (w_ok) lv = std::max(lv, std::max(Wr.max_over(wlo, whi), W.max_over(wlo, whi)));      // WAR, WAW
     h_level[i] = lv;
-    if (r_ok) rd[rs].paint_max(rlo, rhi, lv + 1);
+    if (r_ok) R.paint_max(rlo, rhi, lv + 1);
     if (w_ok) {
-      rd[ws].erase(wlo, whi);
-      wr[ws].assign(wlo, whi, lv + 1);
+      Wr.erase(wlo, whi);
+      W.assign(wlo, whi, lv + 1);
     }
     top = std::max(top, lv + 1);
   }
@@ -1490,26 +1542,31 @@ cg_status cg_plan_waves(const cg_copy_desc* h_descs, uint64_t n, uint32_t* h_lev
 cg_status cg_plan_batches_propagate(const cg_copy_desc* h_descs, uint64_t n, uint64_t* h_cuts, uint64_t* n_cuts) {
   if (!n_cuts || (n && (!h_descs || !h_cuts))) return CG_ERR_INVALID_VALUE;
   IvSet hr, hw, dr, dw;   // host / device reads and writes of the open batch
+  std::map<uint64_t, IvSet> ar, aw;   // per array handle: reads / writes of its V-bits (R-30)
   uint64_t k = 0;
   for (uint64_t i = 0; i < n; ++i) {
     const cg_copy_desc& d = h_descs[i];
     if (d.kind < CG_HTOD || d.kind > CG_ATOH) continue;
-    uint64_t rlo, rhi, wlo, whi;
-    // array sides carry no tracked V-bits (R-30): HtoA only reads the host, AtoH only writes it
-    const bool r_ok = d.kind != CG_ATOH && side_range(d, false, rlo, rhi);
-    const bool w_ok = d.kind != CG_HTOA && side_range(d, true, wlo, whi);
-    IvSet& R = reads_host(d.kind) ? hr : dr;   // the source's address space
-    IvSet& W = writes_host(d.kind) ? hw : dw;  // the destination's
-    IvSet& Rw = reads_host(d.kind) ? hw : dw;  // writes in the source's space
-    IvSet& Wr = writes_host(d.kind) ? hr : dr; // reads in the destination's space
-    const bool conflict = (r_ok && Rw.overlaps(rlo, rhi)) || (w_ok && (Wr.overlaps(wlo, whi) || W.overlaps(wlo, whi)));
+    uint64_t rlo = 0, rhi = 0, wlo = 0, whi = 0;
+    const bool r_ok = copy_read(d, rlo, rhi), w_ok = copy_write(d, wlo, whi);
+    bool conflict;
+    {
+      IvSet& W = d.kind == CG_HTOA ? aw[d.dst] : writes_host(d.kind) ? hw : dw;   // the destination's space
+      IvSet& Rw = d.kind == CG_ATOH ? aw[d.src] : reads_host(d.kind) ? hw : dw;   // writes in the source's space
+      IvSet& Wr = d.kind == CG_HTOA ? ar[d.dst] : writes_host(d.kind) ? hr : dr;  // reads in the destination's
+      conflict = (r_ok && Rw.overlaps(rlo, rhi)) || (w_ok && (Wr.overlaps(wlo, whi) || W.overlaps(wlo, whi)));
+    }
     if (conflict) {
       h_cuts[k++] = i;
       hr.m.clear();
       hw.m.clear();
       dr.m.clear();
       dw.m.clear();
+      ar.clear();
+      aw.clear();
     }
+    IvSet& R = d.kind == CG_ATOH ? ar[d.src] : reads_host(d.kind) ? hr : dr;    // the source's address space
+    IvSet& W = d.kind == CG_HTOA ? aw[d.dst] : writes_host(d.kind) ? hw : dw;   // the destination's
     if (r_ok) R.add(rlo, rhi);
     if (w_ok) W.add(wlo, whi);
   }

@@ -59,6 +59,7 @@ class FlatModel:
         self.track = track
         self.dv: dict = {}                        # base -> numpy V-bytes of the allocation (NEXT-1)
         self.arrays: dict = {}                    # handle -> total bytes (NEXT-3)
+        self.av: dict = {}                        # handle -> numpy V-bytes of the array (track mode)
         self.a = np.zeros(s, bool)               # unpacked A
         self.v = np.full(s, 0xFF, np.uint8)
         self.bases: list = []                     # sorted live bases
@@ -140,6 +141,8 @@ class FlatModel:
         if seq <= self.last or total == 0 or handle in self.arrays:
             return 1
         self.arrays[handle] = total
+        if self.track:                            # S:252 per-array shadow, fresh = undefined
+            self.av[handle] = np.full(total, 0xFF, np.uint8)
         self.last = seq
         return 0
 
@@ -147,6 +150,7 @@ class FlatModel:
         if seq <= self.last or handle not in self.arrays:
             return 1
         del self.arrays[handle]
+        self.av.pop(handle, None)
         self.last = seq
         return 0
 
@@ -195,9 +199,15 @@ class FlatModel:
             out["flags"] |= FLAG["HOST_UNDEF"]
         err = out["flags"] & ~(0 if self.uie else FLAG["HOST_UNDEF"])
         out["status"] = 1 if err else 0
-        if not htoa and out["status"] == 0 and w and h:
-            xs = self._host_index(start, pitch, w, h)
-            self.v[np.array([xx - self.h0 for xx in xs], np.int64)] = 0
+        if out["status"] == 0 and w and h:
+            idx = np.array([xx - self.h0 for xx in self._host_index(start, pitch, w, h)], np.int64)
+            if self.track:                        # V-bits move host <-> the array's shadow
+                if htoa:
+                    self.av[handle][off:off + nb] = self.v[idx]
+                else:
+                    self.v[idx] = self.av[handle][off:off + nb]
+            elif not htoa:
+                self.v[idx] = 0
         return out
 
     def leaks(self):

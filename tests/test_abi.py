@@ -191,14 +191,19 @@ def _sets(d):
         s = int(d[p]) + int(d[p + "_y"]) * int(d[p + "_pitch"]) + int(d[p + "_x"])
         e = s + (int(d["height"]) - 1) * int(d[p + "_pitch"]) + int(d["width"])
         return None if e > (1 << 64) - 1 else (s, e)
+    def arr(p):   # an array side (R-29): bytes [offset, offset + W*H) of that array's own space (R-30)
+        if d["width"] == 0 or d["height"] == 0:
+            return None
+        s = int(d[p + "_x"])
+        e = s + int(d["width"]) * int(d["height"])
+        return None if e > (1 << 64) - 1 else (s, e)
     k = int(d["kind"])
     if k not in (1, 2, 3, 4, 5):
         return [], []
-    # array sides carry no tracked V-bits (R-30): HtoA reads the host only, AtoH writes it only
-    r = rng("src") if k != 5 else None
-    w = rng("dst") if k != 4 else None
-    rs = "h" if k in READS_HOST else "d"
-    ws = "h" if k in WRITES_HOST else "d"
+    r = rng("src") if k != 5 else arr("src")
+    w = rng("dst") if k != 4 else arr("dst")
+    rs = ("a", int(d["src"])) if k == 5 else "h" if k in READS_HOST else "d"
+    ws = ("a", int(d["dst"])) if k == 4 else "h" if k in WRITES_HOST else "d"
     return ([(rs,) + r] if r else []), ([(ws,) + w] if w else [])
 
 

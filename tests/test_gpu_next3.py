@@ -27,7 +27,10 @@ def run(cg, tr, mode):
     regs = ev[ev["op"] == tg.OP_REG]
     kw = {}
     if track:
-        kw["dev_vsize"] = int(sum(int(x) + 256 for x in regs["width"])) + (1 << 20)
+        rega = ev[ev["op"] == tg.OP_REGA]
+        arr = sum(o.array_bytes(int(e["width"]), int(e["height"]), int(e["dst_x"]), int(e["dst_y"]),
+                                int(e["dst_pitch"])) + 16 for e in rega)
+        kw["dev_vsize"] = int(sum(int(x) + 256 for x in regs["width"])) + arr + (1 << 20)
     chk = cg.Checker(tr.host_base, tr.host_size, max_descs=max(tr.n_copies, 64),
                      max_allocs=max(len(ev), 64), **kw)
     gv, gs = cg.replay_events(chk, ev, tr.blob, fuse=(mode == "fused"))
@@ -43,6 +46,10 @@ def run(cg, tr, mode):
     assert np.array_equal(ga["alloc_seq"], oa["seq"])
     A, V = chk.shadow()
     assert np.array_equal(A, o.A) and np.array_equal(V, o.V)
+    if track:   # R-30 / S:252: every live array's own V-bits
+        for a in oa:
+            h, n = int(a["base"]), int(a["size"])
+            assert np.array_equal(chk.array_vbits(h, 0, n), o.array_vbits(h, 0, n)), h
     chk.close()
     return gv
 

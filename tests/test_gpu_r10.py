@@ -71,7 +71,7 @@ def test_overlapping_rows_2_40_closed_form(cg, fmt):
     und = [5, 777, 4095]
     for u in und:
         tb.setv(start + u, b"\x10")
-    dev = tb.malloc(1 << 20)
+    dev = tb.malloc(1 << 41)                     # the device side is contiguous: 2^40 bytes
     tb.copy2d(tg.HTOD, 4096, 1 << 28, dev, 0, 0, 4096, start, 0, 0, 0)
     tb.copy2d(tg.HTOD, 4096, 1 << 28, dev, 0, 0, 4096, start, 0, 0, 1)
     tr = tb.build()

@@ -963,3 +963,93 @@ def overlap_rows(seed: int = 0, W: int = 4096, pitch: int = 64, H: int = 20000, 
         tb.copy2d(HTOD, W, H, dev, 0, 0, W, start, 0, 0, 0)
     tb.meta.update(dict(start=start, dev=dev))
     return tb.build()
+
+
+# ---------------------------------------------------------------------------
+# Random medium traces: the scan's work-splitting boundaries (4 KiB
+# HtoD tiles, 32 KiB DtoH tiles / chunk-map units, 128 KiB split threshold)
+# ---------------------------------------------------------------------------
+SPLIT_BOUNDARIES = (4 * KiB, 32 * KiB, 128 * KiB)
+
+
+def random_medium(seed: int, n_copies: int = 120, window: int = 64 * MiB, host_base: int = 0x4000_0000) -> Trace:
+    """Copies up to 8 MiB with unaligned starts, 2D copies with hundreds of
+    rows, ranges straddling either window edge, and violations planted one
+    byte before / at / after multiples of 4 KiB, 32 KiB and 128 KiB -- both as
+    absolute shard offsets (tile and block edges) and as logical offsets from a
+    copy's start (piece and split edges).  Setup first (marks, planted bytes),
+    then the copies; DtoH applies make later epochs differ."""
+    rng = np.random.default_rng(seed + 0x3ED1)
+    host_base += int(rng.integers(0, 16)) * 4096
+    tb = TraceBuilder(f"medium{seed}", host_base, window)
+    tb.mark(host_base, window, DEFINED)
+    for _ in range(int(rng.integers(0, 6))):                       # UNDEFINED runs (malloc'ed, unwritten)
+        a = int(rng.integers(0, window - MiB))
+        tb.mark(host_base + a, int(rng.integers(1, 256 * KiB)), UNDEFINED)
+    def boundary_offset(limit):
+        b = int(rng.choice(SPLIT_BOUNDARIES))
+        k = int(rng.integers(1, max(2, limit // b)))
+        return k * b + int(rng.integers(-1, 2))
+    # planted at absolute shard offsets around tile / block edges
+    for _ in range(60):
+        q = min(max(boundary_offset(window), 0), window - 1)
+        if rng.random() < 0.7:
+            tb.setv(host_base + q, bytes([int(rng.integers(1, 256))]))
+        else:
+            tb.mark(host_base + q, int(rng.integers(1, 3)), NOACCESS)
+    allocs = [tb.malloc(32 * MiB) for _ in range(6)]
+    copies = []
+    for _ in range(n_copies):
+        kind = int(rng.choice([HTOD, DTOH], p=[0.55, 0.45]))
+        u = rng.random()
+        if u < 0.25:                                               # sizes right at the boundaries
+            n = max(boundary_offset(8 * MiB), 0)
+        else:
+            n = int(_log_uniform(rng, 1, 8 * MiB, 1)[0])
+        two_d = rng.random() < 0.3
+        if two_d:
+            w = int(_log_uniform(rng, 1, 64 * KiB, 1)[0])
+            h = int(rng.integers(2, 700))
+            while w * h > 8 * MiB and h > 2:
+                h //= 2
+            pitch = w + int(rng.choice([0, int(rng.integers(1, 4096))]))
+            x = int(rng.integers(0, 64))
+            if rng.random() < 0.06:
+                pitch = int(rng.integers(1, max(w + x, 2)))        # BAD_PITCH (may overlap rows)
+            else:
+                pitch += x
+            span = (h - 1) * pitch + w + x
+        else:
+            w, h, pitch, x, span = n, 1, n, 0, n
+        v = rng.random()
+        if v < 0.06:                                               # straddles the window end
+            start = host_base + window - int(rng.integers(1, max(2, span)))
+        elif v < 0.1:                                              # starts below the window
+            start = host_base - int(rng.integers(1, 8 * KiB))
+        else:
+            start = host_base + int(rng.integers(0, max(1, window - span)))
+        if rng.random() < 0.35 and w * h > 2:                      # planted at a logical boundary of this copy
+            o = min(max(boundary_offset(w * h), 0), w * h - 1)
+            r, c = divmod(o, w)
+            xaddr = start + x + r * pitch + c
+            if host_base <= xaddr < host_base + window:
+                if kind == HTOD and rng.random() < 0.6:
+                    tb.setv(xaddr, bytes([int(rng.integers(1, 256))]))
+                else:
+                    tb.mark(xaddr, 1, NOACCESS)
+        dev = allocs[int(rng.integers(len(allocs)))]
+        doff = int(rng.integers(0, 32 * MiB))
+        if rng.random() < 0.8:                                     # fits (else TooSmall)
+            doff = int(rng.integers(0, max(1, 32 * MiB - w * h - 1)))
+        copies.append((kind, w, h, pitch, x, start, dev + doff))
+    for kind, w, h, pitch, x, start, dptr in copies:
+        if h == 1 and x == 0 and pitch == w:
+            if kind == HTOD:
+                tb.copy1d(HTOD, dptr, start, w)
+            else:
+                tb.copy1d(DTOH, start, dptr, w)
+        elif kind == HTOD:
+            tb.copy2d(HTOD, w, h, dptr, 0, 0, w, start, x, 0, pitch)
+        else:
+            tb.copy2d(DTOH, w, h, start, x, 0, pitch, dptr, 0, 0, w)
+    return tb.build()
