@@ -218,14 +218,21 @@ def registry_rate(cg, tr, device):
     return len(regs) / dt if dt > 0 else None
 
 
-def run_ours(args, rank, world, device):
+def run_ours(args, rank, world, device, config=None, steps=None, warmup=None, e2e_on=None, extras=True):
+    """One workload: setup (untimed), warm-up, `steps` timed steps, e2e; the
+    JSON fields of the line.  config / steps / warmup / e2e_on override args
+    (the per_config runs of the default line)."""
     import torch
     import paper_1310_0901_b200 as cg
 
     torch.cuda.set_device(device)
-    tr = make_workload(args.config, rank, args.scale)
+    config = config or args.config
+    steps = steps or args.steps
+    warmup = warmup or args.warmup
+    no_e2e = args.no_e2e if e2e_on is None else not e2e_on
+    tr = make_workload(config, rank, args.scale)
     two_bit = args.shadow in ("2bit", "sparse")
-    chk, descs, t_setup, nreg = setup_checker(cg, tr, device, host_staging=not args.no_e2e, rank=rank, world=world,
+    chk, descs, t_setup, nreg = setup_checker(cg, tr, device, host_staging=not no_e2e, rank=rank, world=world,
                                               track=args.track,
                                               shadow_format={"bytes": 0, "2bit": 1, "sparse": 2}[args.shadow])
     n = len(descs)
@@ -291,12 +298,13 @@ def run_ours(args, rank, world, device):
                                 stream.cuda_stream)
             pg.gather()   # one NCCL all_gather of the packed (count, index, verdict) buffers
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize()
     verd = cg.verdicts_to_numpy(d_out)
     check_b, apply_b = algorithmic_bytes(descs, verd, track=args.track, two_bit=two_bit)
-    bytes_per_step = check_b + apply_b
+    desc_b = float(n) * (96 + 64)   # every descriptor read, every verdict written
+    bytes_per_step = check_b + apply_b + desc_b
 
     if world > 1:
         torch.distributed.barrier()
@@ -306,7 +314,7 @@ def run_ours(args, rank, world, device):
     chk.profile_begin()
     with ClockSampler(device) as clocks:
         ev0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             step()
         ev1.record(stream)
         torch.cuda.synchronize()
@@ -325,13 +333,13 @@ def run_ours(args, rank, world, device):
         t = torch.tensor([ms], dtype=torch.float64, device=device)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    ms_step = ms / args.steps
+    ms_step = ms / steps
 
     # e2e through the public host-buffer entry point cg_check_host (pinned
     # buffers; 1D copies in the compact 40-byte form when the batch allows it;
     # dirty verdicts only come back)
     e2e = None
-    if not args.no_e2e:
+    if not no_e2e:
         is1d = bool(np.all(descs["height"] == 1) and np.all(descs["dst_x"] == 0) and np.all(descs["src_x"] == 0)
                     and np.all(descs["dst_y"] == 0) and np.all(descs["src_y"] == 0)
                     and np.all(descs["dst_pitch"] == descs["width"]) and np.all(descs["src_pitch"] == descs["width"]))
@@ -385,9 +393,9 @@ def run_ours(args, rank, world, device):
                 e_base.append(got[0])
                 got[0] += nd_box.value
             nd_box.value = got[0]
-        e2e_run(max(1, args.warmup // 2))
+        e2e_run(max(1, warmup // 2))
         torch.cuda.synchronize()
-        k = max(3, args.steps // 4)
+        k = max(3, steps // 4)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         e2e_run(k)
@@ -419,11 +427,11 @@ def run_ours(args, rank, world, device):
     scan_avg = scan_ms / max(scan_n, 1)
     scan_bytes = check_b + sum(fused_apply_bytes(descs[a:b], verd[a:b], max(n, 1024), two_bit)
                                for (a, b), fu in zip(epochs, efused) if fu)
-    launches_scan = max(scan_n / max(args.steps, 1), 1.0)   # one per epoch
+    launches_scan = max(scan_n / max(steps, 1), 1.0)   # one per epoch
     achieved = scan_bytes / (scan_avg * launches_scan * 1e-3) / 1e9
     traffic = None
     suffix = "" if args.shadow == "bytes" else "_" + args.shadow
-    prof_json = os.path.join(ROOT, "profiles", f"ncu_{args.config}{suffix}_check_scan.json")
+    prof_json = os.path.join(ROOT, "profiles", f"ncu_{config}{suffix}_check_scan.json")
     if os.path.exists(prof_json):
         with open(prof_json) as f:
             pj = json.load(f)
@@ -440,21 +448,25 @@ def run_ours(args, rank, world, device):
         # NEXT-1: the propagation (k_prop_waves, one cooperative launch per
         # epoch with waves) dominates the step: 1 B read + 1 B written per byte
         # of every error-free copy
-        check_roof, launches_apply = roof, max(apply_n / max(args.steps, 1), 1.0)
-        ach = apply_b / (apply_ms / max(args.steps, 1) * 1e-3) / 1e9
-        wj = os.path.join(ROOT, "profiles", f"ncu_{args.config}_track_prop_waves.json")
+        check_roof, launches_apply = roof, max(apply_n / max(steps, 1), 1.0)
+        ach = apply_b / (apply_ms / max(steps, 1) * 1e-3) / 1e9
+        wj = os.path.join(ROOT, "profiles", f"ncu_{config}_track_prop_waves.json")
         wtraffic = json.load(open(wj)).get("dram_bytes_per_launch") if os.path.exists(wj) else None
         roof = {"bound": "hbm", "kernel": "k_prop_waves", "achieved": ach, "peak": peak,
                 "peak_source": peak_kind, "unit": "GB/s", "frac": ach / peak, "traffic": wtraffic,
                 "algorithmic_bytes_per_launch": apply_b / launches_apply,
                 "avg_launch_ms": apply_ms / max(apply_n, 1), "share_of_step": apply_ms / ms if ms > 0 else None}
     res = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+        "warmup": warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": workload_name(args.config),
+        "config": {"workload": workload_name(config),
                    "descriptors_per_step": n, "allocations": nreg, "host_window_bytes": tr.host_size,
-                   "shadow_bytes_per_step": bytes_per_step, "check_bytes": check_b, "apply_bytes": apply_b,
+                   "algorithmic_bytes_per_step": bytes_per_step, "check_bytes": check_b, "apply_bytes": apply_b,
+                   "descriptor_bytes": desc_b,
+                   "bytes_counted": "shadow: HtoD 1.125 B + DtoH 0.125 B per host byte checked, 1 B per host "
+                                    "byte a DtoH apply defines; descriptors: 96 B read + 64 B verdict written "
+                                    "(SURVEY §8(d))",
                    "l2": "no flush: >= 8.5 GB of shadow streamed per step vs 126 MB L2",
                    "parallelism": f"host-range shards x{world}",
                    "shadow_format": {"bytes": "V bytes + A bits", "2bit": "2-bit states (NEXT-4)",
@@ -466,25 +478,53 @@ def run_ours(args, rank, world, device):
                    "propagation_waves": sum(w.n_waves for w in waves) if args.track else None,
                    "wave_planning_s": t_waves if args.track else None},
         "descriptors_per_s": world * n / (ms_step * 1e-3),
+        "shadow_gbs": world * (check_b + apply_b) / (ms_step * 1e-3) / 1e9,
         "frac_of_hbm": value / (world * peak),
         "roofline": roof,
         "check_roofline": check_roof,
-        "stages_ms_per_step": {k: v[0] / max(args.steps, 1) for k, v in stages.items()},
-        "apply_roofline": {"achieved": (apply_b - (scan_bytes - check_b)) / (apply_ms / max(args.steps, 1) * 1e-3) / 1e9
+        "stages_ms_per_step": {k: v[0] / max(steps, 1) for k, v in stages.items()},
+        "apply_roofline": {"achieved": (apply_b - (scan_bytes - check_b)) / (apply_ms / max(steps, 1) * 1e-3) / 1e9
                            if apply_ms else None, "unit": "GB/s", "peak": peak,
                            "note": "k_apply alone (the residual pass when fused)"},
         "gpu_launches": int(launches),
-        "gpu_launches_per_step": launches / args.steps,
+        "gpu_launches_per_step": launches / steps,
         "clocks": clocks.summary(),
         "e2e": e2e,
         "setup_s": t_setup,
     }
-    if rank == 0 and not args.no_registry_rate:
+    if extras and rank == 0 and not args.no_registry_rate:
         res["registry_events_per_s"] = registry_rate(cg, tr, device)
-    if args.conc:
+    if extras and args.conc:
         res["next2"] = conc_rate(cg, descs, d_out, args, device, stream)
     chk.close()
     return res
+
+
+PER_CONFIG = ("c3_single", "c4_pitched", "c5_sharded")
+
+
+def per_config(args, device):
+    """The other BASELINE.json configurations, each through the same measured
+    step (its own setup, 3 warm-up steps, device-timed steps, CUDA-event stage
+    timing) so that every config is in the driver-observed line."""
+    import gc
+    import torch
+    out = {}
+    for cfg in PER_CONFIG:
+        steps = {"c3_single": 20, "c4_pitched": 6, "c5_sharded": 10}[cfg]
+        r = run_ours(args, 0, 1, device, config=cfg, steps=steps, warmup=3, e2e_on=False, extras=False)
+        out[cfg] = {"value": r["value"], "unit": UNIT, "ms_per_step": r["ms_per_step"], "steps": steps, "warmup": 3,
+                    "descriptors_per_s": r["descriptors_per_s"], "shadow_gbs": r["shadow_gbs"],
+                    "frac_of_hbm": r["frac_of_hbm"], "roofline": {k: r["roofline"][k] for k in
+                                                                  ("kernel", "achieved", "frac", "avg_launch_ms",
+                                                                   "share_of_step")},
+                    "stages_ms_per_step": r["stages_ms_per_step"], "epochs": r["config"]["epochs"],
+                    "gpu_launches_per_step": r["gpu_launches_per_step"], "clocks": r["clocks"],
+                    "config": {k: r["config"][k] for k in ("descriptors_per_step", "allocations", "host_window_bytes",
+                                                           "algorithmic_bytes_per_step", "entry")}}
+        gc.collect()
+        torch.cuda.empty_cache()
+    return out
 
 
 def conc_rate(cg, descs, d_out, args, device, stream):
@@ -524,55 +564,93 @@ def conc_rate(cg, descs, d_out, args, device, stream):
     return out
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 class OracleArm:
     """The CPU oracle, as it stands, on a bounded sample of the workload: the
     same generator and allocation table with fewer copies.  Setup events are
-    replayed once (untimed); every step replays the copy batch (timed).  A
-    repeated replay sees the same verdicts (DtoH checks read only A; HtoD
-    sources are never DtoH targets), so every step is the same work."""
+    replayed once (untimed); every step replays the copy batch (timed) with the
+    per-copy checks of each epoch on `threads` host threads
+    (or_replay_parallel; 1 = the sequential or_replay).  A repeated replay sees
+    the same verdicts (DtoH checks read only A; HtoD sources are never DtoH
+    targets), so every step is the same work.  Imports only oracle/ and
+    tracegen/ -- never the product package."""
 
-    def __init__(self, config: str):
+    def __init__(self, config: str, threads: int = 0, n_copies: int | None = None):
         import oracle
-        from paper_1310_0901_b200.replay import events_to_descs
         import tracegen as tg
+        self.threads = threads or os.cpu_count() or 1
         if config == "c2_small":
-            tr = tg.c2_small(n_copies=20000, n_allocs=100_000)
+            tr = tg.c2_small(n_copies=n_copies or (100_000 if self.threads > 1 else 20000), n_allocs=100_000)
         elif config == "c3_single":
-            tr = tg.c3_single(size=256 << 20)
+            tr = tg.c3_single(size=(2 << 30) if self.threads > 1 else 256 << 20)
+        elif config == "c5_sharded":
+            tr = tg.c5_sharded(scale=0.01)
         else:
-            tr = tg.c4_pitched(n_copies=400)
+            tr = tg.c4_pitched(n_copies=n_copies or (4000 if self.threads > 1 else 400))
         ev = tr.events
         self.o = oracle.Oracle(tr.host_base, tr.host_size)
         self.o.replay(ev[ev["op"] != 5], tr.blob)
         self.copies = ev[ev["op"] == 5]
         self.blob = tr.blob
-        self.descs = events_to_descs(self.copies)
+        self.descs = tg.events_to_descs(self.copies)
         self.nalloc = int(np.count_nonzero(ev["op"] == 3))
         self.config = config
+        self.verdicts = None
 
     def step(self):
         t0 = time.perf_counter()
-        v, _ = self.o.replay(self.copies, self.blob)
+        if self.threads > 1:
+            v, _ = self.o.replay_parallel(self.copies, self.blob, self.threads)
+        else:
+            v, _ = self.o.replay(self.copies, self.blob)
         dt = time.perf_counter() - t0
+        self.verdicts = v
         cb, ab = algorithmic_bytes(self.descs, v)
-        return (cb + ab), dt
+        return (cb + ab + len(self.descs) * (96 + 64)), dt
 
     def describe(self, value, dt_total, steps):
-        return {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                "descriptors_per_s": len(self.copies) * steps / dt_total,
+        return {"value": value, "unit": UNIT, "cores": self.threads, "kind": "oracle", "cpu_model": cpu_model(),
+                "nproc": os.cpu_count(), "descriptors_per_s": len(self.copies) * steps / dt_total,
                 "sample": f"{self.config} generator, {len(self.copies)} copies against {self.nalloc} "
-                          f"allocations per step x {steps} steps, single-threaded sequential replay "
-                          f"(plain C, linear allocation list)"}
+                          f"allocations per step x {steps} steps, "
+                          + (f"{self.threads} threads (or_replay_parallel: checks of each epoch in parallel)"
+                             if self.threads > 1 else "single-threaded sequential replay")
+                          + " -- plain C, linear allocation list"}
 
 
 def run_cpu_baseline(config: str, steps: int = 3):
+    """T-thread oracle (T = the host's cores) on a bounded sample, plus the
+    1-thread replay of a smaller sample; the T-thread verdicts of that smaller
+    sample must equal the 1-thread ones."""
+    if config not in ("c2_small", "c3_single", "c4_pitched", "c5_sharded"):
+        config = "c2_small"
     arm = OracleArm(config)
     tot_b = tot_t = 0.0
     for _ in range(steps):
         b, t = arm.step()
         tot_b += b
         tot_t += t
-    return arm.describe(tot_b / tot_t / 1e9, tot_t, steps)
+    out = arm.describe(tot_b / tot_t / 1e9, tot_t, steps)
+    one = OracleArm(config, threads=1)
+    b1, t1 = one.step()
+    par = OracleArm(config, threads=arm.threads, n_copies=len(one.copies))
+    par.step()
+    same = all(np.array_equal(one.verdicts[f], par.verdicts[f]) for f in one.verdicts.dtype.names)
+    assert same, "T-thread oracle differs from the 1-thread oracle"
+    out["single_thread"] = {"value": b1 / t1 / 1e9, "unit": UNIT, "cores": 1,
+                            "descriptors_per_s": len(one.copies) / t1, "copies": len(one.copies),
+                            "equal_to_T_thread": same}
+    return out
 
 
 def main():
@@ -586,6 +664,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-registry-rate", action="store_true")
+    ap.add_argument("--no-per-config", action="store_true", help="skip the C3/C4/C5 per_config runs")
     ap.add_argument("--unfused", action="store_true", help="check and apply as two calls")
     ap.add_argument("--track", action="store_true", help="NEXT-1 device V-bit tracking (apply = propagation)")
     ap.add_argument("--conc", type=int, default=0, help="NEXT-2: also time cg_conc_check with this many threads")
@@ -610,7 +689,10 @@ def main():
             tot_b += b
             tot_t += t
         val = tot_b / tot_t / 1e9
+        loaded = [l.split()[-1] for l in open("/proc/self/maps") if l.rstrip().endswith(".so")
+                  and ROOT in l]
         out = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+               "repo_libraries_loaded": sorted(set(loaded)),
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_t / args.steps * 1e3,
                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
                "data": "synthetic", "config": {"workload": workload_name(args.config)},
@@ -624,6 +706,9 @@ def main():
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
     res = run_ours(args, rank, world, local)
     if rank == 0:
+        if world == 1 and args.config == "c2_small" and not args.no_per_config and not args.track \
+                and args.shadow == "bytes":
+            res["per_config"] = per_config(args, local)
         if not args.no_cpu_baseline:
             res["cpu_baseline"] = run_cpu_baseline(args.config)
         print(json.dumps(res))

@@ -49,7 +49,7 @@ F_CONCURRENT = 1 << 9
 def build(force: bool = False) -> str:
     """Compile the oracle with plain gcc (building the checker is not using it)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", _LIB, _SRC])
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-pthread", "-shared", "-fPIC", "-o", _LIB, _SRC])
     return _LIB
 
 
@@ -83,6 +83,7 @@ def _load():
         lib.or_sync.argtypes = [P, U32, U64]
         lib.or_check_copy_mt.argtypes = [P, P, U32, P]
         lib.or_replay_mt.restype = U64; lib.or_replay_mt.argtypes = [P, P, U64, P, P, P, P]
+        lib.or_replay_parallel.restype = U64; lib.or_replay_parallel.argtypes = [P, P, U64, P, I, P, P]
         _lib = lib
     return _lib
 
@@ -197,6 +198,22 @@ class Oracle:
         assert t is None or len(t) == n
         self.lib.or_replay_mt(self.st, ev.ctypes.data, n, b.ctypes.data, t.ctypes.data if t is not None else None,
                               out_v.ctypes.data, out_s.ctypes.data)
+        return out_v[:ncopy], out_s[:n]
+
+
+    def replay_parallel(self, events: np.ndarray, blob: Optional[np.ndarray] = None, threads: int = 0):
+        """The same replay with the per-copy checks of each epoch on `threads`
+        host threads (0: os.cpu_count()); equal to replay() by construction
+        (cg_oracle.c or_replay_parallel; tests assert it)."""
+        ev = np.ascontiguousarray(events)
+        n = len(ev)
+        ncopy = int(np.count_nonzero(ev["op"] == 5))
+        out_v = np.zeros(max(ncopy, 1), VERDICT_DTYPE)
+        out_s = np.zeros(max(n, 1), np.uint32)
+        b = np.ascontiguousarray(blob if blob is not None and len(blob) else np.zeros(1, np.uint8))
+        T = threads or os.cpu_count() or 1
+        self.lib.or_replay_parallel(self.st, ev.ctypes.data, n, b.ctypes.data, T, out_v.ctypes.data,
+                                    out_s.ctypes.data)
         return out_v[:ncopy], out_s[:n]
 
 

@@ -475,8 +475,9 @@ static void apply_defined(or_state *st, const or_event *ev, uint64_t lo, uint64_
     const uint64_t hs = ev->dst + ev->dst_y * ev->dst_pitch + ev->dst_x;   /* fits: no Error */
     for (uint64_t r = 0; r < H && W; r++) {
         const uint64_t xr = hs + r * ev->dst_pitch;
-        for (uint64_t c = 0; c < W; c++)
-            if (xr + c >= lo && xr + c < hi) st->V[xr + c - st->h0] = 0x00;
+        const uint64_t c0 = lo > xr ? lo - xr : 0;                 /* the row's columns inside [lo, hi) */
+        const uint64_t c1 = hi > xr ? (hi - xr < W ? hi - xr : W) : 0;
+        for (uint64_t c = c0; c < c1; c++) st->V[xr + c - st->h0] = 0x00;
     }
 }
 
@@ -682,5 +683,131 @@ uint64_t or_replay_mt(or_state *st, const or_event *ev, uint64_t n, const uint8_
         }
         if (out_status) out_status[i] = s;
     }
+    return nc;
+}
+
+/* ------------------------------------------------ T-thread replay (timing) */
+/* The same replay on T host threads (SURVEY §8(d) "CPU oracle timing": the
+ * per-descriptor check loop parallelised inside epochs; its result must equal
+ * the 1-thread or_replay, which tests/ and bench.py assert).  An epoch is a
+ * maximal run of consecutive COPY events in which no HtoD / HtoA reads a host
+ * page (4 KiB) that an earlier DtoH / AtoH of the run writes (bounding ranges,
+ * conservative): inside it every check reads the state as it was at the
+ * epoch's start -- the registry does not change (registry events end an
+ * epoch), DtoH checks read only A, which no copy changes, and no HtoD reads a
+ * byte an earlier copy of the epoch defines -- so phase 1 runs the checks of
+ * the epoch in parallel (check_only: read-only), then phase 2 applies the
+ * error-free DtoH / AtoH copies, thread t writing only host bytes in its slice
+ * of the window (apply_defined, so no byte is written by two threads); the
+ * order of the applies does not matter (they all write 0x00).  Device V-bit
+ * tracking and the concurrency checks stay sequential (or_replay). */
+#include <pthread.h>
+
+typedef struct {
+    or_state *st;
+    const or_event *ev;
+    const uint64_t *idx;      /* event index of each copy of the epoch */
+    or_verdict *out;          /* verdict of each copy of the epoch */
+    uint64_t m;
+    int t, T, phase;
+} or_par_job;
+
+static void *par_worker(void *arg) {
+    or_par_job *j = (or_par_job *)arg;
+    if (j->phase == 1) {
+        for (uint64_t k = (uint64_t)j->t; k < j->m; k += (uint64_t)j->T)
+            check_only(j->st, &j->ev[j->idx[k]], &j->out[k]);
+    } else {
+        const uint64_t slice = (j->st->s + (uint64_t)j->T - 1) / (uint64_t)j->T;
+        const uint64_t lo = j->st->h0 + slice * (uint64_t)j->t;
+        const uint64_t hi = (uint64_t)j->t + 1 == (uint64_t)j->T ? j->st->h0 + j->st->s : lo + slice;
+        for (uint64_t k = 0; k < j->m; k++) {
+            const or_event *e = &j->ev[j->idx[k]];
+            if (j->out[k].status == 0 && (e->kind == OR_DTOH || e->kind == OR_ATOH)) apply_defined(j->st, e, lo, hi);
+        }
+    }
+    return NULL;
+}
+
+static void par_run(or_state *st, const or_event *ev, const uint64_t *idx, or_verdict *out, uint64_t m, int T,
+                    int phase) {
+    pthread_t th[256];
+    or_par_job jobs[256];
+    if (T > 256) T = 256;
+    for (int t = 0; t < T; t++) {
+        jobs[t] = (or_par_job){st, ev, idx, out, m, t, T, phase};
+        if (t) pthread_create(&th[t], NULL, par_worker, &jobs[t]);
+    }
+    par_worker(&jobs[0]);
+    for (int t = 1; t < T; t++) pthread_join(th[t], NULL);
+}
+
+/* host bounding range of a copy, clipped to the window, as window offsets [q0, q1) */
+static int host_bounds(const or_state *st, const or_event *e, int dst, uint64_t *q0, uint64_t *q1) {
+    uint64_t start, span;
+    const int ok = dst ? side_range(e->dst, e->dst_x, e->dst_y, e->dst_pitch, e->width, e->height, &start, &span)
+                       : side_range(e->src, e->src_x, e->src_y, e->src_pitch, e->width, e->height, &start, &span);
+    if (!ok || span == 0) return 0;
+    const uint64_t we = st->h0 + st->s, a = start < st->h0 ? st->h0 : start;
+    const uint64_t b = start + span > we ? we : start + span;
+    if (a >= b) return 0;
+    *q0 = a - st->h0;
+    *q1 = b - st->h0;
+    return 1;
+}
+
+/* one bit per host byte: set / test / clear [q0, q1) */
+static void bits_set(uint64_t *m, uint64_t q0, uint64_t q1, int on) {
+    for (uint64_t q = q0; q < q1;) {
+        if ((q & 63) == 0 && q + 64 <= q1) { m[q >> 6] = on ? ~0ull : 0; q += 64; continue; }
+        if (on) m[q >> 6] |= 1ull << (q & 63); else m[q >> 6] &= ~(1ull << (q & 63));
+        q++;
+    }
+}
+static int bits_any(const uint64_t *m, uint64_t q0, uint64_t q1) {
+    for (uint64_t q = q0; q < q1;) {
+        if ((q & 63) == 0 && q + 64 <= q1) { if (m[q >> 6]) return 1; q += 64; continue; }
+        if ((m[q >> 6] >> (q & 63)) & 1) return 1;
+        q++;
+    }
+    return 0;
+}
+
+uint64_t or_replay_parallel(or_state *st, const or_event *ev, uint64_t n, const uint8_t *blob, int nthreads,
+                            or_verdict *out_v, uint32_t *out_status) {
+    if (st->track || st->conc || nthreads <= 1) return or_replay(st, ev, n, blob, out_v, out_status);
+    uint64_t *written = (uint64_t *)calloc(st->s / 64 + 1, 8);   /* host bytes a DtoH of the epoch writes */
+    uint64_t *idx = (uint64_t *)malloc(sizeof(uint64_t) * (n ? n : 1));
+    uint64_t nc = 0, i = 0;
+    while (i < n) {
+        if (ev[i].op != OR_COPY) {           /* sequential, as or_replay */
+            or_replay(st, &ev[i], 1, blob, NULL, out_status ? &out_status[i] : NULL);
+            i++;
+            continue;
+        }
+        uint64_t j = i, m = 0;
+        for (; j < n && ev[j].op == OR_COPY; j++) {
+            const or_event *e = &ev[j];
+            uint64_t q0, q1;
+            if ((e->kind == OR_HTOD || e->kind == OR_HTOA) && host_bounds(st, e, 0, &q0, &q1) &&
+                bits_any(written, q0, q1))
+                break;                       /* reads a byte an earlier DtoH may define: next epoch */
+            if ((e->kind == OR_DTOH || e->kind == OR_ATOH) && host_bounds(st, e, 1, &q0, &q1))
+                bits_set(written, q0, q1, 1);
+            idx[m++] = j;
+        }
+        par_run(st, ev, idx, out_v + nc, m, nthreads, 1);
+        par_run(st, ev, idx, out_v + nc, m, nthreads, 2);
+        for (uint64_t k = 0; k < m; k++) {
+            const or_event *e = &ev[idx[k]];
+            uint64_t q0, q1;
+            if (out_status) out_status[idx[k]] = out_v[nc + k].status;
+            if ((e->kind == OR_DTOH || e->kind == OR_ATOH) && host_bounds(st, e, 1, &q0, &q1))
+                bits_set(written, q0, q1, 0);
+        }
+        nc += m;
+        i = j;
+    }
+    free(written); free(idx);
     return nc;
 }

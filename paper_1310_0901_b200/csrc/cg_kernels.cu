@@ -215,8 +215,9 @@ __device__ __forceinline__ HostClip host_clip(const Norm& nm, uint64_t H, const 
   c.pfu = kNone;
   const bool contig = H == 1 || nm.W == nm.hpitch;
   const uint64_t W = contig ? nm.nbytes : nm.W, Hr = contig ? 1 : H, pitch = contig ? 0 : nm.hpitch;
+  c.overlap = false;
+  if (nm.nbytes == 0) return c;   // W == 0 or H == 0: no host bytes
   c.overlap = !contig && pitch < W;
-  if (nm.nbytes == 0) return c;
   const uint64_t x0 = nm.hstart;
   if (x0 < sv.wb) {
     c.pfu = 0;

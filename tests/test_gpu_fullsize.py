@@ -170,3 +170,81 @@ def test_c2_full_tracking(cg):
         b, n = int(r["base"]), int(r["size"])
         assert np.array_equal(chk.device_vbits(b, n), o.device_vbits(b, n)), hex(b)
     chk.close()
+
+
+def _compare_shadow_chunks(chk, o, base, size, chunk=1 << 30):
+    """the whole final host shadow, GPU against oracle, chunk by chunk"""
+    Abits = o.A
+    for q in range(0, size, chunk):
+        n = min(chunk, size - q)
+        a, v = chk.shadow_read(base + q, n)
+        assert np.array_equal(v, o.V[q:q + n]), ("V", q)
+        oa = np.unpackbits(Abits[q // 8:(q + n) // 8], bitorder="little")
+        assert np.array_equal(a, oa), ("A", q)
+
+
+def _full_replay(cg, tr, fused=True, T=0):
+    """The GPU checks the trace the way bench.py does (setup events, then the
+    copies in the R-20 epochs cg_plan_batches cuts, fused where the epoch is
+    apply-disjoint; registry events are lifetime-stamped, so they all go first);
+    the oracle replays the whole trace in order on T host threads
+    (or_replay_parallel, equal to the 1-thread replay: tests/test_oracle_parallel.py)."""
+    import torch
+    ev = tr.events
+    is_copy = ev["op"] == tg.OP_COPY
+    copies = ev[is_copy]
+    nreg = int(np.count_nonzero(ev["op"] == tg.OP_REG))
+    chk = cg.Checker(tr.host_base, tr.host_size, max_descs=max(len(copies), 1024), max_allocs=max(nreg, 1024))
+    _, st = cg.replay_events(chk, ev[~is_copy], tr.blob)
+    descs = tg.events_to_descs(copies)
+    dd = cg.to_device_descs(descs)
+    dv = torch.empty(len(descs) * 64, dtype=torch.uint8, device=dd.device)
+    cuts = [0] + [int(c) for c in cg.plan_batches(descs)]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        if b <= a:
+            continue
+        x, y = dd[a * 96:b * 96], dv[a * 64:b * 64]
+        if fused and cg.batch_disjoint(descs[a:b]):
+            chk.check_apply(x, y)
+        else:
+            chk.check_copies(x, y)
+            chk.apply_dtoh(x, y)
+    torch.cuda.synchronize()
+    gv = cg.verdicts_to_numpy(dv)
+    o = oracle.Oracle(tr.host_base, tr.host_size)
+    ov, os_ = o.replay_parallel(ev, tr.blob, threads=T)
+    for f in ov.dtype.names:
+        bad = np.flatnonzero(gv[f] != ov[f])
+        assert len(bad) == 0, (tr.name, f, len(bad), bad[:5], gv[f][bad[:5]], ov[f][bad[:5]])
+    # registry statuses of the setup events
+    assert np.array_equal(st, os_[~is_copy])
+    gl, ol = chk.leak_report(), o.leaks()
+    assert np.array_equal(gl["base"], ol["base"]) and np.array_equal(gl["size"], ol["size"])
+    assert np.array_equal(gl["alloc_seq"], ol["seq"])
+    _compare_shadow_chunks(chk, o, tr.host_base, tr.host_size)
+    chk.close()
+    return gv, ov
+
+
+def test_c4_full(cg):
+    """C4 at full size: all 100k verdicts (273 GB of host bytes checked), the
+    final A and V shadow (8 GiB window) bit for bit against the T-thread oracle"""
+    tr = tg.c4_pitched()
+    gv, _ = _full_replay(cg, tr)
+    inj = tr.meta["inject"]
+    assert np.all(gv["flags"][inj == 0] == 0) and np.all(gv["flags"][inj != 0] != 0)
+
+
+def test_c5_full(cg):
+    """C5 at full size on one GPU: 10M descriptors in 11 R-20 epochs against a
+    ~150k-entry lifetime-stamped table with alloc / free bursts, the 64 GiB
+    window (V 64 GiB + A 8 GiB), leak report: every verdict, every registry
+    status, the leak list and the whole final shadow against the T-thread
+    oracle (~72 GiB of host memory)."""
+    import os
+    import psutil
+    if psutil.virtual_memory().available < (100 << 30):
+        pytest.skip("needs ~100 GiB of host memory for the oracle's 64 GiB window")
+    tr = tg.c5_sharded()
+    gv, _ = _full_replay(cg, tr)
+    assert int(np.count_nonzero(gv["flags"])) > 0

@@ -55,6 +55,26 @@ EVENT_DTYPE = np.dtype([
 ])
 assert EVENT_DTYPE.itemsize == 96
 
+# the copy-descriptor records the checker takes (include/cg.h cg_copy_desc, 96 B):
+# the COPY events' CUDA_MEMCPY2D fields, restated here so that the oracle arm
+# of bench.py never has to import the product package
+DESC_DTYPE = np.dtype([
+    ("kind", "<u4"), ("reserved", "<u4"), ("seq", "<u8"), ("width", "<u8"), ("height", "<u8"),
+    ("dst", "<u8"), ("dst_x", "<u8"), ("dst_y", "<u8"), ("dst_pitch", "<u8"),
+    ("src", "<u8"), ("src_x", "<u8"), ("src_y", "<u8"), ("src_pitch", "<u8"),
+])
+assert DESC_DTYPE.itemsize == 96
+
+
+def events_to_descs(ev: np.ndarray) -> np.ndarray:
+    """COPY events -> descriptor records (field copy)"""
+    d = np.zeros(len(ev), DESC_DTYPE)
+    for f in DESC_DTYPE.names:
+        if f != "reserved":
+            d[f] = ev[f]
+    return d
+
+
 DEVICE_HEAP_BASE = 0x0100_0000   # S:370
 DEVICE_ALIGN = 256               # invented (DESIGN.md R-17)
 KiB, MiB, GiB = 1 << 10, 1 << 20, 1 << 30
