@@ -237,7 +237,6 @@ def run_ours(args, rank, world, device, config=None, steps=None, warmup=None, e2
                                               shadow_format={"bytes": 0, "2bit": 1, "sparse": 2}[args.shadow])
     n = len(descs)
     stream = torch.cuda.current_stream()
-    d_descs = cg.to_device_descs(descs, device)
     d_out = torch.empty(n * 64, dtype=torch.uint8, device=device)
     nalloc = nreg
     d_leaks = torch.empty(max(nalloc, 1) * 24, dtype=torch.uint8, device=device)
@@ -250,8 +249,18 @@ def run_ours(args, rank, world, device, config=None, steps=None, warmup=None, e2
     # epoch whose HtoD and DtoH host ranges are disjoint runs fused
     cuts = [0] + [int(c) for c in cg.plan_batches(descs)]
     epochs = [(a, b) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
-    efused = [cg.batch_disjoint(descs[a:b]) and not args.unfused and not args.track for a, b in epochs]
+    # every epoch runs fused (cg_check_apply): the DtoH descriptors whose host
+    # range an HtoD of the same epoch reads carry CG_APPLY_AFTER (host planning,
+    # untimed, like the epoch cuts)
+    efused = [not args.unfused and not args.track for _ in epochs]
     fused = all(efused)
+    n_after = 0
+    if fused:
+        for a, b in epochs:
+            part = np.ascontiguousarray(descs[a:b])
+            n_after += cg.plan_apply_after(part)
+            descs[a:b] = part
+    d_descs = cg.to_device_descs(descs, device)
     waves = []   # NEXT-1: per epoch, the device index lists of its propagation waves (cg_plan_waves)
     t_waves = 0.0
     if args.track:
@@ -345,7 +354,7 @@ def run_ours(args, rank, world, device, config=None, steps=None, warmup=None, e2
                     and np.all(descs["dst_pitch"] == descs["width"]) and np.all(descs["src_pitch"] == descs["width"]))
         if is1d:
             d1 = np.zeros(n, cg.COPY1D_DTYPE)
-            for f in ("kind", "seq", "dst", "src"):
+            for f in ("kind", "reserved", "seq", "dst", "src"):
                 d1[f] = descs[f]
             d1["bytes"] = descs["width"]
             hbuf = torch.from_numpy(d1.view(np.uint8).copy()).pin_memory()
@@ -474,7 +483,7 @@ def run_ours(args, rank, world, device, config=None, steps=None, warmup=None, e2
                    "entry": ("cg_check_copies + cg_apply_copies (NEXT-1 V-bit propagation)" if args.track else
                              "cg_check_apply (fused)" if fused else "cg_check_copies + cg_apply_dtoh"
                              if not any(efused) else "cg_check_apply / cg_check_copies + cg_apply_dtoh per epoch"),
-                   "epochs": len(epochs),
+                   "epochs": len(epochs), "apply_after_descriptors": n_after,
                    "propagation_waves": sum(w.n_waves for w in waves) if args.track else None,
                    "wave_planning_s": t_waves if args.track else None},
         "descriptors_per_s": world * n / (ms_step * 1e-3),

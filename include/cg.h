@@ -108,7 +108,12 @@ enum {
  *    shard writes only its raw partial (first_unaddr, first_undef, undef_count,
  *    device fields, flags without HOST_*; status 0) for cg_straddler_pack /
  *    cg_straddler_finalize after the collective merge. */
-enum { CG_SHARD_NOT_OWNER = 1u << 0, CG_SHARD_RAW = 1u << 1 };
+enum { CG_SHARD_NOT_OWNER = 1u << 0, CG_SHARD_RAW = 1u << 1, CG_APPLY_AFTER = 1u << 2 };
+/* CG_APPLY_AFTER (cg_check_apply only): this DTOH / ATOH descriptor's host
+ * range overlaps the host range of an HTOD / HTOA descriptor of the same
+ * batch, so its apply waits until every check of the batch has read the
+ * shadow (the residual pass) instead of running inside the scan.  Set by
+ * cg_plan_apply_after. */
 
 typedef struct {
   uint32_t kind;       /* CG_HTOD / CG_DTOH / CG_DTOD / CG_HTOA / CG_ATOH */
@@ -456,9 +461,10 @@ cg_status cg_array_vbits(cg_ctx *ctx, uint64_t handle, uint64_t offset, uint64_t
 /* cg_check_copies followed by cg_apply_dtoh, fused: the shadow scan applies
  * every DtoH descriptor that fits one of its work groups as soon as its verdict
  * is final, and a residual apply pass handles the rest.  Same results as the
- * two calls PROVIDED that no HtoD host range of the batch overlaps any DtoH
- * host range of the batch (check with cg_batch_disjoint); otherwise call the
- * two functions.  Asynchronous on stream.  Errors: as cg_check_copies. */
+ * two calls PROVIDED that every DtoH descriptor whose host range overlaps an
+ * HtoD host range of the batch carries CG_APPLY_AFTER (cg_plan_apply_after
+ * sets exactly those; a batch where cg_batch_disjoint holds needs none).
+ * Asynchronous on stream.  Errors: as cg_check_copies. */
 cg_status cg_check_apply(cg_ctx *ctx, const cg_copy_desc *d_descs, uint64_t n, cg_verdict *d_out,
                          void *stream);
 
@@ -466,6 +472,13 @@ cg_status cg_check_apply(cg_ctx *ctx, const cg_copy_desc *d_descs, uint64_t n, c
  * overlaps any DtoH host range of them (the precondition of cg_check_apply).
  * Errors: CG_ERR_INVALID_VALUE on NULL. */
 cg_status cg_batch_disjoint(const cg_copy_desc *h_descs, uint64_t n, int *disjoint);
+
+/* Host helper for cg_check_apply: sets CG_APPLY_AFTER in h_descs[i].reserved
+ * for every DTOH / ATOH descriptor whose host range (bounding range for 2D)
+ * overlaps the host range of any HTOD / HTOA descriptor of the n (in either
+ * order) and clears it elsewhere; *n_after = how many carry it.  Errors:
+ * CG_ERR_INVALID_VALUE on NULL. */
+cg_status cg_plan_apply_after(cg_copy_desc *h_descs, uint64_t n, uint64_t *n_after);
 
 /* End-to-end entry point with HOST buffers: copies h_descs to the device,
  * runs cg_check_copies (apply = 0), cg_check_copies + cg_apply_dtoh

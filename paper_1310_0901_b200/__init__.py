@@ -110,6 +110,7 @@ def _load() -> ctypes.CDLL:
         "cg_format_leak": (U64, [P, P, U64]),
         "cg_shard_plan": (I, [P, U64, U64, U64, U32, P, P, P]),
         "cg_batch_disjoint": (I, [P, U64, P]),
+        "cg_plan_apply_after": (I, [P, U64, P]),
         "cg_leak_sweep": (I, [P, P, U64, P, P]),
         "cg_leak_report": (I, [P, P, U64, P]),
         "cg_plan_batches": (I, [P, U64, P, P]),
@@ -147,7 +148,7 @@ EXPORTED = ("cg_workspace_size", "cg_ctx_create", "cg_ctx_destroy", "cg_last_err
             "cg_host_mark_batch", "cg_host_set_vbits", "cg_register_alloc", "cg_free", "cg_registry_compact",
             "cg_check_copies", "cg_apply_dtoh", "cg_check_copies_host", "cg_leak_sweep", "cg_leak_report",
             "cg_plan_batches", "cg_kernel_launches", "cg_profile_begin", "cg_profile_end", "cg_check_apply",
-            "cg_batch_disjoint", "cg_straddler_pack", "cg_straddler_finalize", "cg_compact_dirty", "cg_shard_plan",
+            "cg_batch_disjoint", "cg_plan_apply_after", "cg_straddler_pack", "cg_straddler_finalize", "cg_compact_dirty", "cg_shard_plan",
             "cg_host_query_addressable", "cg_expand_copy1d", "cg_check_host", "cg_check_host_submit", "cg_check_host_wait", "cg_format_verdict",
             "cg_format_leak", "cg_apply_copies", "cg_device_vbits", "cg_array_vbits", "cg_plan_batches_propagate",
             "cg_host_shadow_read", "cg_apply_copies_subset", "cg_plan_waves", "cg_apply_flush", "cg_apply_copies_waves", "cg_summarize", "cg_format_summary", "cg_array_bytes", "cg_register_array", "cg_free_array", "cg_array_report", "cg_conc_create",
@@ -258,7 +259,7 @@ CG_FMT_2D, CG_FMT_1D = 0, 1
 COPY1D_DTYPE = np.dtype([("kind", "<u4"), ("reserved", "<u4"), ("seq", "<u8"), ("dst", "<u8"), ("src", "<u8"),
                          ("bytes", "<u8")])
 cg_shard_plan = _lib.cg_shard_plan
-CG_SHARD_NOT_OWNER, CG_SHARD_RAW = 1, 2
+CG_SHARD_NOT_OWNER, CG_SHARD_RAW, CG_APPLY_AFTER = 1, 2, 4
 cg_batch_disjoint = _lib.cg_batch_disjoint
 cg_leak_sweep = _lib.cg_leak_sweep
 cg_leak_report = _lib.cg_leak_report
@@ -315,6 +316,18 @@ def batch_disjoint(descs: np.ndarray) -> bool:
     if st:
         raise CgError(st, "cg_batch_disjoint")
     return bool(out.value)
+
+
+def plan_apply_after(descs: np.ndarray) -> int:
+    """cg_plan_apply_after: sets CG_APPLY_AFTER (in place) on the DtoH
+    descriptors whose host range overlaps an HtoD host range of the batch, so
+    that cg_check_apply is exact on any R-20 epoch; returns how many."""
+    assert descs.dtype == DESC_DTYPE and descs.flags["C_CONTIGUOUS"]
+    out = ctypes.c_uint64(0)
+    st = _lib.cg_plan_apply_after(descs.ctypes.data if len(descs) else None, len(descs), ctypes.byref(out))
+    if st:
+        raise CgError(st, "cg_plan_apply_after")
+    return int(out.value)
 
 
 def shard_plan(descs: np.ndarray, host_base: int, host_size: int, world: int):

@@ -256,9 +256,10 @@ struct __align__(16) ScanMeta {
   uint64_t hstart, hpitch, W, info;   // info: see kInfo*
 };
 // info: scanned bytes (the shard clip, < 2^40) | scan kind << 40 | host << 42 |
-// contiguous << 43 | raw << 44 | pfu << 45 | deferred << 46 | flags << 48
+// contiguous << 43 | raw << 44 | pfu << 45 | not the ring's (deferred pass or
+// small pass) << 46 | apply after the scan (CG_APPLY_AFTER) << 47 | flags << 48
 constexpr int kInfoKind = 40, kInfoHost = 42, kInfoContig = 43, kInfoRaw = 44, kInfoPfu = 45, kInfoDefer = 46,
-              kInfoFlags = 48;
+              kInfoAfter = 47, kInfoFlags = 48;
 constexpr uint64_t kInfoBytes = (1ull << 40) - 1;
 
 // ---------------------------------------------------------------------------
@@ -357,335 +358,6 @@ __device__ __forceinline__ uint64_t check_host_units(uint32_t skind, uint64_t ns
   return skind == CG_HTOD ? nscan : (nscan + 7) >> 3;
 }
 
-__device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs, uint64_t n, const Table& t,
-                                          cg_verdict* __restrict__ out, uint64_t* __restrict__ weight,
-                                          ScanMeta* __restrict__ meta, uint64_t* __restrict__ dvoff,
-                                          const ShadowView& sv, uint32_t* __restrict__ counter,
-                                          uint32_t* __restrict__ defer, uint64_t* s_split) {
-  // the scan's group counter, (apply count), residual count: reset here
-  // instead of by a memset node, which would break the PDL chain.  The
-  // deferred list (count, cursor: counter[4], [5]) is appended to right here,
-  // so the kernel after the scan resets it for the next check.
-  if (blockIdx.x == 0 && threadIdx.x < 3) counter[threadIdx.x] = 0;
-  load_splitters(t, s_split);
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const cg_copy_desc d = descs[i];
-    const Norm nm = normalize(d);
-    uint32_t flags = nm.flags;
-    uint64_t de = 0, df = 0, se = 0, sf = 0;
-    const bool owner = !(d.reserved & CG_SHARD_NOT_OWNER);   // only the owner shard looks up the device side
-    uint64_t dv_dst = 0, dv_src = 0;   // NEXT-1: device V-bit offsets in the pool
-    if (nm.kind >= CG_HTOA && owner) {  // NEXT-3: array side
-      const bool htoa = nm.kind == CG_HTOA;
-      uint64_t total, j;
-      if (nm.aok) {
-        if (!array_lookup(t, nm.ahandle, d.seq, total, j)) {
-          flags |= htoa ? CG_F_DST_NOT_ALLOCATED : CG_F_SRC_NOT_ALLOCATED;
-        } else {
-          if (nm.aoff + d.width * d.height > total) {
-            flags |= htoa ? CG_F_DST_TOO_SMALL : CG_F_SRC_TOO_SMALL;
-            const uint64_t ex = d.width * d.height, fd = nm.aoff < total ? total - nm.aoff : 0;
-            if (htoa) { de = ex; df = fd; } else { se = ex; sf = fd; }
-          }
-          // NEXT-1 x NEXT-3 (S:252 per-array shadow, R-30): the array side's V-bits in the pool
-          if (t.apool) (htoa ? dv_dst : dv_src) = __ldg(t.apool + j) + nm.aoff;
-        }
-      }
-    } else if (!(flags & CG_F_BAD_KIND) && owner) {
-      uint64_t end, j;
-      if ((nm.kind == CG_HTOD || nm.kind == CG_DTOD) && nm.dok) {      // dst side first (S:225)
-        if (!table_lookup(t, s_split, nm.ds, d.seq, end, j)) {
-          flags |= CG_F_DST_NOT_ALLOCATED;
-        } else {
-          if (end - nm.ds < nm.dspan) {
-            flags |= CG_F_DST_TOO_SMALL;
-            de = nm.dspan;
-            df = end - nm.ds;
-          }
-          if (t.pool) dv_dst = __ldg(t.pool + j) + (nm.ds - __ldg(t.base + j));
-        }
-      }
-      if ((nm.kind == CG_DTOH || nm.kind == CG_DTOD) && nm.sok) {
-        if (!table_lookup(t, s_split, nm.ss, d.seq, end, j)) {
-          flags |= CG_F_SRC_NOT_ALLOCATED;
-        } else {
-          if (end - nm.ss < nm.sspan) {
-            flags |= CG_F_SRC_TOO_SMALL;
-            se = nm.sspan;
-            sf = end - nm.ss;
-          }
-          if (t.pool) dv_src = __ldg(t.pool + j) + (nm.ss - __ldg(t.base + j));
-        }
-      }
-    }
-    if (t.pool) {
-      dvoff[2 * i] = dv_dst;
-      dvoff[2 * i + 1] = dv_src;
-    }
-    // R-10 / R-15: the shard part of the host side, and the analytic first
-    // offset outside the window (initial first_unaddr: partials min into it)
-    HostClip hc{0, 0, kNone, false};
-    if (nm.host) hc = host_clip(nm, d.height, sv);
-    const bool deferred = nm.host && (hc.overlap || (sv.sparse && hc.ohi - hc.olo > kDeferBytes));
-    const uint64_t nscan = nm.host && !deferred ? hc.ohi - hc.olo : 0;
-    if (deferred) defer[atomicAdd(counter + 4, 1u)] = (uint32_t)i;
-    cg_verdict v;
-    v.first_unaddr = hc.pfu;
-    v.first_undef = kNone;
-    v.undef_count = 0;
-    v.dst_expected = de;
-    v.dst_found = df;
-    v.src_expected = se;
-    v.src_found = sf;
-    v.flags = flags;
-    v.status = 0;
-    out[i] = v;
-    weight[i] = kItemCost + check_host_units(nm.skind, nscan, sv.two_bit != 0);
-    ScanMeta m;
-    m.hstart = nm.hstart;
-    m.hpitch = nm.hpitch;
-    m.W = nm.W;
-    const bool contig = d.height == 1 || d.width == nm.hpitch;
-    const bool raw = d.reserved & CG_SHARD_RAW;   // partial of a straddler: no finalisation here
-    m.info = nscan | ((uint64_t)(nm.skind & 3u) << kInfoKind) | ((uint64_t)(nscan != 0) << kInfoHost) |
-             ((uint64_t)contig << kInfoContig) | ((uint64_t)raw << kInfoRaw) | ((uint64_t)(hc.pfu != kNone) << kInfoPfu) |
-             ((uint64_t)deferred << kInfoDefer) | ((uint64_t)flags << kInfoFlags);
-    meta[i] = m;
-  }
-}
-
-__global__ void __launch_bounds__(kThreads) k_check_prep(const cg_copy_desc* __restrict__ descs,
-                                                         uint64_t n, Table t, cg_verdict* __restrict__ out,
-                                                         uint64_t* __restrict__ weight,
-                                                         ScanMeta* __restrict__ meta,
-                                                         uint64_t* __restrict__ dvoff, ShadowView sv,
-                                                         uint32_t* __restrict__ counter,
-                                                         uint32_t* __restrict__ defer) {
-  pdl_entry();
-  extern __shared__ uint64_t s_split[];
-  prep_body(descs, n, t, out, weight, meta, dvoff, sv, counter, defer, s_split);
-}
-
-// ---------------------------------------------------------------------------
-// a2: exclusive prefix sum (3 kernels) and the chunk plan
-// ---------------------------------------------------------------------------
-constexpr int kScanThreads = 256;
-constexpr int kScanItems = kScanTile / kScanThreads;   // 8
-
-__device__ __forceinline__ uint64_t block_exclusive_scan(uint64_t x, uint64_t* s_warp, uint64_t& total) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint64_t inc = x;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    uint64_t y = __shfl_up_sync(kFull, inc, o);
-    if (lane >= o) inc += y;
-  }
-  if (lane == 31) s_warp[wid] = inc;
-  __syncthreads();
-  if (wid == 0) {
-    uint64_t w = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
-    uint64_t wi = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint64_t y = __shfl_up_sync(kFull, wi, o);
-      if (lane >= o) wi += y;
-    }
-    if (lane < (int)(blockDim.x >> 5)) s_warp[lane] = wi - w;
-    if (lane == 31) s_warp[32] = wi;
-  }
-  __syncthreads();
-  total = s_warp[32];
-  uint64_t r = inc - x + s_warp[wid];
-  __syncthreads();
-  return r;
-}
-
-// n_dev != nullptr: the item count is min(n, *n_dev), known only on the device
-__device__ __forceinline__ uint64_t eff_n(uint64_t n, const uint32_t* n_dev) {
-  return n_dev ? umin64(n, *n_dev) : n;
-}
-
-__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint64_t* __restrict__ in, uint64_t n,
-                                                              uint64_t* __restrict__ bsum,
-                                                              const uint32_t* __restrict__ n_dev) {
-  pdl_entry();
-  __shared__ uint64_t s_warp[33];
-  n = eff_n(n, n_dev);
-  const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
-  if (base >= n && base > 0) return;
-  uint64_t acc = 0;
-#pragma unroll
-  for (int j = 0; j < kScanItems; ++j) {
-    uint64_t i = base + (uint64_t)j * kScanThreads + threadIdx.x;
-    if (i < n) acc += in[i];
-  }
-  uint64_t total;
-  block_exclusive_scan(acc, s_warp, total);
-  if (threadIdx.x == 0) bsum[blockIdx.x] = total;
-}
-
-// single block: exclusive scan of bsum[0..nb) in place; bsum[nb] = out[n] = total
-__global__ void __launch_bounds__(1024) k_scan_top(uint64_t* __restrict__ bsum, uint64_t n,
-                                                   uint64_t* __restrict__ out, const uint32_t* __restrict__ n_dev) {
-  pdl_entry();
-  __shared__ uint64_t s_warp[33];
-  n = eff_n(n, n_dev);
-  const uint64_t nb = (n + kScanTile - 1) / kScanTile;
-  uint64_t carry = 0;
-  for (uint64_t base = 0; base < nb; base += blockDim.x) {
-    uint64_t i = base + threadIdx.x;
-    uint64_t x = i < nb ? bsum[i] : 0;
-    uint64_t total;
-    uint64_t ex = block_exclusive_scan(x, s_warp, total);
-    if (i < nb) bsum[i] = carry + ex;
-    carry += total;
-  }
-  if (threadIdx.x == 0) {
-    bsum[nb] = carry;
-    out[n] = carry;
-  }
-}
-
-__global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint64_t* __restrict__ in, uint64_t n,
-                                                            const uint64_t* __restrict__ bsum,
-                                                            uint64_t* __restrict__ out,
-                                                            const uint32_t* __restrict__ n_dev) {
-  pdl_entry();
-  __shared__ uint64_t s_items[kScanTile];
-  __shared__ uint64_t s_warp[33];
-  n = eff_n(n, n_dev);
-  const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
-  if (base >= n) return;
-#pragma unroll
-  for (int j = 0; j < kScanItems; ++j) {
-    uint64_t i = base + (uint64_t)j * kScanThreads + threadIdx.x;
-    s_items[j * kScanThreads + threadIdx.x] = i < n ? in[i] : 0;
-  }
-  __syncthreads();
-  uint64_t loc[kScanItems];
-  uint64_t acc = 0;
-#pragma unroll
-  for (int j = 0; j < kScanItems; ++j) {
-    loc[j] = acc;
-    acc += s_items[threadIdx.x * kScanItems + j];
-  }
-  uint64_t total;
-  uint64_t ex = block_exclusive_scan(acc, s_warp, total) + bsum[blockIdx.x];
-#pragma unroll
-  for (int j = 0; j < kScanItems; ++j) s_items[threadIdx.x * kScanItems + j] = ex + loc[j];
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < kScanItems; ++j) {
-    uint64_t i = base + (uint64_t)j * kScanThreads + threadIdx.x;
-    if (i < n) out[i] = s_items[j * kScanThreads + threadIdx.x];
-  }
-}
-
-// T: the chunk map's granularity (weight units); Trule >= T: descriptors of
-// at most Trule weight are never split (owned by the group their weight
-// interval starts in), heavier ones always go through the split path
-constexpr uint64_t kSmallT = 128 * 1024;
-struct ChunkGeom {
-  uint64_t total, T, nchunks, Trule;
-};
-
-__device__ __forceinline__ ChunkGeom chunk_geom(const uint64_t* P, uint64_t n, uint64_t t_min,
-                                                uint64_t max_chunks) {
-  ChunkGeom g;
-  g.total = P[n];
-  uint64_t T = (g.total + max_chunks - 1) / max_chunks;
-  g.T = umax64(T, t_min);
-  g.nchunks = (g.total + g.T - 1) / g.T;
-  g.Trule = umax64(g.T, kSmallT);
-  return g;
-}
-
-// chunk_first[c] = the item whose weight interval [P[d], P[d+1]) contains c*T
-__global__ void __launch_bounds__(kThreads) k_plan(const uint64_t* __restrict__ P, uint64_t n, uint64_t t_min,
-                                                   uint64_t max_chunks, uint32_t* __restrict__ chunk_first,
-                                                   const uint32_t* __restrict__ n_dev) {
-  pdl_entry();
-  n = eff_n(n, n_dev);
-  const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
-  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < g.nchunks;
-       c += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t target = c * g.T;
-    uint64_t lo = 0, hi = n;   // P[lo] <= target < P[hi]
-    while (hi - lo > 1) {
-      uint64_t mid = (lo + hi) >> 1;
-      if (__ldg(P + mid) <= target) lo = mid; else hi = mid;
-    }
-    chunk_first[c] = (uint32_t)lo;
-  }
-}
-
-// a1-a3 + a2 in one cooperative launch: the prep (k_check_prep), then the
-// exclusive prefix sum of the weights and the chunk map with grid barriers
-// between the phases (k_scan_reduce / _top / _down, k_plan): one launch and
-// four barriers instead of five launches.
-__global__ void __launch_bounds__(kThreads) k_front(const cg_copy_desc* __restrict__ descs, uint64_t n, Table t,
-                                                    cg_verdict* __restrict__ out, uint64_t* __restrict__ weight,
-                                                    ScanMeta* __restrict__ meta, uint64_t* __restrict__ dvoff,
-                                                    ShadowView sv, uint32_t* __restrict__ counter,
-                                                    uint32_t* __restrict__ defer, uint64_t* P,
-                                                    uint64_t* __restrict__ bsum, uint64_t t_min, uint64_t max_chunks,
-                                                    uint32_t* __restrict__ chunk_first) {
-  pdl_entry();
-  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
-  extern __shared__ uint64_t s_split[];
-  __shared__ uint64_t s_warp[33];
-  prep_body(descs, n, t, out, weight, meta, dvoff, sv, counter, defer, s_split);
-  grid.sync();
-  // block b owns items [b*per, (b+1)*per)
-  const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
-  const uint64_t lo = umin64(n, (uint64_t)blockIdx.x * per), hi = umin64(n, lo + per);
-  {
-    uint64_t acc = 0;
-    for (uint64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) acc += __ldcg(weight + k);
-    uint64_t total;
-    block_exclusive_scan(acc, s_warp, total);
-    if (threadIdx.x == 0) bsum[blockIdx.x] = total;
-  }
-  grid.sync();
-  if (blockIdx.x == 0) {
-    uint64_t carry = 0;
-    for (uint64_t b0 = 0; b0 < gridDim.x; b0 += blockDim.x) {
-      const uint64_t b = b0 + threadIdx.x;
-      const uint64_t x = b < gridDim.x ? __ldcg(bsum + b) : 0;
-      uint64_t total;
-      const uint64_t ex = block_exclusive_scan(x, s_warp, total);
-      if (b < gridDim.x) bsum[b] = carry + ex;
-      carry += total;
-    }
-    if (threadIdx.x == 0) P[n] = carry;
-  }
-  grid.sync();
-  {
-    uint64_t carry = __ldcg(bsum + blockIdx.x);
-    for (uint64_t k0 = lo; k0 < hi; k0 += blockDim.x) {
-      const uint64_t k = k0 + threadIdx.x;
-      const uint64_t x = k < hi ? __ldcg(weight + k) : 0;
-      uint64_t total;
-      const uint64_t ex = block_exclusive_scan(x, s_warp, total);
-      if (k < hi) P[k] = carry + ex;
-      carry += total;
-    }
-  }
-  grid.sync();
-  const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
-  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < g.nchunks;
-       c += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t target = c * g.T;
-    uint64_t a = 0, b = n;   // P[a] <= target < P[b]
-    while (b - a > 1) {
-      const uint64_t mid = (a + b) >> 1;
-      if (__ldcg(P + mid) <= target) a = mid; else b = mid;
-    }
-    chunk_first[c] = (uint32_t)a;
-  }
-}
-
 // ---------------------------------------------------------------------------
 // a4: the host shadow scan -- one TMA bulk-copy ring per warp
 // ---------------------------------------------------------------------------
@@ -709,7 +381,8 @@ constexpr uint32_t kTileA = kTileV / 8;
 // (4 KiB of A), NEXT-4 2-bit states 16 KiB for both kinds (4 KiB of states)
 constexpr uint32_t kHtodShift = 12, kDtohShift = 15, k2bitShift = 14;
 constexpr uint32_t kGrab = 4;          // chunks per group while the plan is far from its end
-constexpr uint32_t kTileData = 1, kTileHtod = 2, kTileEnd = 4, kTileWhole = 8, kTileFuse = 16, kTileRaw = 32;
+constexpr uint32_t kTileData = 1, kTileHtod = 2, kTileEnd = 4, kTileWhole = 8, kTileFuse = 16, kTileRaw = 32,
+                   kTileAfter = 64;   // CG_APPLY_AFTER: a DtoH piece the residual pass applies
 
 struct __align__(16) TileInfo {
   uint64_t ob;        // logical offset of staged host byte 0
@@ -1062,6 +735,508 @@ __device__ __forceinline__ void warp_store_zero(uint8_t* V, uint64_t q0, uint64_
   for (uint64_t k = (a0 >> 4) + lane; k < (a1 >> 4); k += 32) stg_val16(V4 + k, 0u);
 }
 
+// ---------------------------------------------------------------------------
+// Small contiguous host sides are checked right in the prep (the "small
+// pass"), by teams of 8 lanes: each team streams through the small
+// descriptors of its warp's 32-descriptor window, 16 bytes of shadow per lane
+// per round, so every warp instruction serves up to 4 descriptors and the
+// teams stay converged (one loop, per-team data).  Bigger, 2D, split, raw and
+// deferred host sides go to the TMA-ring scan.  kSmallBytes bounds the host
+// bytes of a small side: HtoD 4 KiB = 32 rounds of V, DtoH 4 KiB = 4 rounds of A.
+// ---------------------------------------------------------------------------
+constexpr uint64_t kSmallBytes = 4096;
+constexpr int kTeam = 8;
+
+// host bytes covered by one lane per round: bytes format HtoD 16 (V bytes +
+// their A bits), DtoH 128 (16 bytes of A); 2-bit states 64 (16 state bytes)
+template <bool kTwoBit>
+__device__ __forceinline__ uint32_t lane_span(bool htod) {
+  return kTwoBit ? 64u : htod ? 16u : 128u;
+}
+
+// the lane's unit [gp, gp + span) of a small side [q0, q1) (shard bytes; logical
+// offset of shard byte q = ob + q): accumulate first unaddressable / first
+// undefined / undefined count
+template <bool kTwoBit>
+__device__ __forceinline__ void small_unit(const ShadowView& sv, uint64_t gp, uint64_t q0, uint64_t q1, uint64_t ob,
+                                           bool htod, Partial& p) {
+  if (kTwoBit) {
+    const uint4 s4 = __ldcs(reinterpret_cast<const uint4*>(sv.V + (gp >> 2)));
+    const uint32_t w[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t gb = gp + 16u * j;
+      if (gb + 16 <= q0 || gb >= q1) continue;
+      const uint32_t m = pair_mask(gb, q0, q1);
+      if (htod) word2<true>(w[j], m, ob + gb, p);
+      else word2<false>(w[j], m, ob + gb, p);
+    }
+    return;
+  }
+  if (htod) {
+    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(sv.V + gp));
+    const uint32_t a = __ldcs(reinterpret_cast<const unsigned short*>(sv.A + (gp >> 3)));
+    const uint32_t m = range_mask(gp, 16, q0, q1);
+    const uint32_t bad = ~a & m, und = nz16(v) & a & m;
+    if (bad) p.fu = umin64(p.fu, ob + gp + (__ffs(bad) - 1));
+    if (und) {
+      p.fd = umin64(p.fd, ob + gp + (__ffs(und) - 1));
+      p.cnt += __popc(und);
+    }
+    return;
+  }
+  const uint4 a4 = __ldcs(reinterpret_cast<const uint4*>(sv.A + (gp >> 3)));
+  const uint32_t w[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint64_t gb = gp + 32u * j;
+    if (gb + 32 <= q0 || gb >= q1) continue;
+    const uint32_t bad = ~w[j] & range_mask(gb, 32, q0, q1);
+    if (bad) {
+      p.fu = umin64(p.fu, ob + gb + (__ffs(bad) - 1));
+      break;
+    }
+  }
+}
+
+// every lane with `small` set owns one small side (q0, q1, ob, htod); on return
+// its `mine` holds that side's partial (first unaddressable, first undefined,
+// count).  Warp-uniform entry.
+template <bool kTwoBit>
+__device__ __noinline__ void small_pass(const ShadowView& sv, bool small, uint64_t q0, uint64_t q1, uint64_t ob,
+                                        bool htod, Partial& mine) {
+  const int lane = threadIdx.x & 31, tl = lane & (kTeam - 1);
+  uint32_t pend = __ballot_sync(kFull, small);
+  int own = -1;                 // team state, replicated in its 8 lanes
+  uint64_t t0 = 0, t1 = 0, tob = 0, g = 0;
+  bool th = false;
+  Partial acc{kNone, kNone, 0};
+  while (true) {
+    // idle teams take the next pending sides, lowest lane first
+    uint32_t idle = __ballot_sync(kFull, own < 0 && tl == 0);
+    while (idle && pend) {
+      const int team_lane = __ffs(idle) - 1;
+      idle &= idle - 1;
+      const int j = __ffs(pend) - 1;
+      pend &= pend - 1;
+      const uint64_t a = __shfl_sync(kFull, q0, j), b = __shfl_sync(kFull, q1, j), o = __shfl_sync(kFull, ob, j);
+      const bool h = __shfl_sync(kFull, htod, j);
+      if ((lane & ~(kTeam - 1)) == team_lane) {
+        own = j;
+        t0 = a;
+        t1 = b;
+        tob = o;
+        th = h;
+        const uint64_t u = kTwoBit ? 64 : h ? 16 : 128;
+        g = a / u * u;   // the first lane unit of the side
+      }
+    }
+    if (!__any_sync(kFull, own >= 0)) break;
+    // one round: lane tl takes unit g + tl of its team's side
+    if (own >= 0) {
+      const uint64_t u = lane_span<kTwoBit>(th);
+      const uint64_t gp = g + u * tl;
+      if (gp < t1) small_unit<kTwoBit>(sv, gp, t0, t1, tob, th, acc);
+      g += u * kTeam;
+    }
+    // teams whose side is done reduce within the team and hand the partial to its owner
+    const bool fin = own >= 0 && g >= t1;
+    if (__any_sync(kFull, fin)) {
+#pragma unroll
+      for (int o = kTeam / 2; o > 0; o >>= 1) {
+        acc.fu = umin64(acc.fu, __shfl_xor_sync(kFull, acc.fu, o));
+        acc.fd = umin64(acc.fd, __shfl_xor_sync(kFull, acc.fd, o));
+        acc.cnt += __shfl_xor_sync(kFull, acc.cnt, o);
+      }
+      uint32_t leaders = __ballot_sync(kFull, fin && tl == 0);
+      while (leaders) {
+        const int l = __ffs(leaders) - 1;
+        leaders &= leaders - 1;
+        const int who = __shfl_sync(kFull, own, l);
+        const uint64_t fu = __shfl_sync(kFull, acc.fu, l), fd = __shfl_sync(kFull, acc.fd, l);
+        const uint64_t cnt = __shfl_sync(kFull, acc.cnt, l);
+        if (lane == who) mine = Partial{fu, fd, cnt};
+      }
+      if (fin) {
+        own = -1;
+        acc = Partial{kNone, kNone, 0};
+      } else {   // the reduction summed the unfinished teams' lanes too: only finished teams reduced meaningfully
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs, uint64_t n, const Table& t,
+                                          cg_verdict* __restrict__ out, uint64_t* __restrict__ weight,
+                                          ScanMeta* __restrict__ meta, uint64_t* __restrict__ dvoff,
+                                          const ShadowView& sv, uint32_t* __restrict__ counter,
+                                          uint32_t* __restrict__ defer, uint64_t* s_split, uint32_t err_mask,
+                                          int fuse, uint32_t* __restrict__ resid) {
+  // the scan's group counter and the apply count: reset here instead of by a
+  // memset node, which would break the PDL chain.  The residual list (count:
+  // counter[2]) and the deferred list (count, cursor: counter[4], [5]) are
+  // appended to right here, so the kernels after the scan (k_finish,
+  // k_finalize_split) reset them for the next check.
+  if (blockIdx.x == 0 && threadIdx.x < 2) counter[threadIdx.x] = 0;
+  load_splitters(t, s_split);
+  const int lane = threadIdx.x & 31;
+  const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += nthr) {
+    const uint64_t i = base + lane;
+    const bool act = i < n;
+    cg_copy_desc d;
+    if (act) d = descs[i];
+    else d.kind = 0;
+    const Norm nm = normalize(d);
+    uint32_t flags = nm.flags;
+    uint64_t de = 0, df = 0, se = 0, sf = 0;
+    const bool owner = !(d.reserved & CG_SHARD_NOT_OWNER);   // only the owner shard looks up the device side
+    uint64_t dv_dst = 0, dv_src = 0;   // NEXT-1: device V-bit offsets in the pool
+    if (act && nm.kind >= CG_HTOA && owner) {  // NEXT-3: array side
+      const bool htoa = nm.kind == CG_HTOA;
+      uint64_t total, j;
+      if (nm.aok) {
+        if (!array_lookup(t, nm.ahandle, d.seq, total, j)) {
+          flags |= htoa ? CG_F_DST_NOT_ALLOCATED : CG_F_SRC_NOT_ALLOCATED;
+        } else {
+          if (nm.aoff + d.width * d.height > total) {
+            flags |= htoa ? CG_F_DST_TOO_SMALL : CG_F_SRC_TOO_SMALL;
+            const uint64_t ex = d.width * d.height, fd = nm.aoff < total ? total - nm.aoff : 0;
+            if (htoa) { de = ex; df = fd; } else { se = ex; sf = fd; }
+          }
+          // NEXT-1 x NEXT-3 (S:252 per-array shadow, R-30): the array side's V-bits in the pool
+          if (t.apool) (htoa ? dv_dst : dv_src) = __ldg(t.apool + j) + nm.aoff;
+        }
+      }
+    } else if (act && !(flags & CG_F_BAD_KIND) && owner) {
+      uint64_t end, j;
+      if ((nm.kind == CG_HTOD || nm.kind == CG_DTOD) && nm.dok) {      // dst side first (S:225)
+        if (!table_lookup(t, s_split, nm.ds, d.seq, end, j)) {
+          flags |= CG_F_DST_NOT_ALLOCATED;
+        } else {
+          if (end - nm.ds < nm.dspan) {
+            flags |= CG_F_DST_TOO_SMALL;
+            de = nm.dspan;
+            df = end - nm.ds;
+          }
+          if (t.pool) dv_dst = __ldg(t.pool + j) + (nm.ds - __ldg(t.base + j));
+        }
+      }
+      if ((nm.kind == CG_DTOH || nm.kind == CG_DTOD) && nm.sok) {
+        if (!table_lookup(t, s_split, nm.ss, d.seq, end, j)) {
+          flags |= CG_F_SRC_NOT_ALLOCATED;
+        } else {
+          if (end - nm.ss < nm.sspan) {
+            flags |= CG_F_SRC_TOO_SMALL;
+            se = nm.sspan;
+            sf = end - nm.ss;
+          }
+          if (t.pool) dv_src = __ldg(t.pool + j) + (nm.ss - __ldg(t.base + j));
+        }
+      }
+    }
+    if (act && t.pool) {
+      dvoff[2 * i] = dv_dst;
+      dvoff[2 * i + 1] = dv_src;
+    }
+    // R-10 / R-15: the shard part of the host side, and the analytic first
+    // offset outside the window (initial first_unaddr: partials min into it)
+    HostClip hc{0, 0, kNone, false};
+    if (act && nm.host) hc = host_clip(nm, d.height, sv);
+    const bool deferred = act && nm.host && (hc.overlap || (sv.sparse && hc.ohi - hc.olo > kDeferBytes));
+    const uint64_t nscan = act && nm.host && !deferred ? hc.ohi - hc.olo : 0;
+    if (deferred) defer[atomicAdd(counter + 4, 1u)] = (uint32_t)i;
+    const bool contig = d.height == 1 || d.width == nm.hpitch;
+    const bool raw = d.reserved & CG_SHARD_RAW;   // partial of a straddler: no finalisation here
+    // the small pass (bytes and dense 2-bit formats): contiguous, whole, not raw
+    const bool small = nscan != 0 && nscan <= kSmallBytes && contig && !raw && !sv.sparse;
+    uint64_t q0 = 0, q1 = 0, ob = 0;
+    if (small) {
+      const uint64_t x = nm.hstart + hc.olo;   // shard bytes [x, x + nscan), logical offset of shard byte q: q + sb - x0
+      q0 = x - sv.sb;
+      q1 = q0 + nscan;
+      ob = sv.sb - nm.hstart;
+    }
+    Partial mine{kNone, kNone, 0};
+    if (__any_sync(kFull, small)) {
+      if (sv.two_bit) small_pass<true>(sv, small, q0, q1, ob, nm.skind == CG_HTOD, mine);
+      else small_pass<false>(sv, small, q0, q1, ob, nm.skind == CG_HTOD, mine);
+    }
+    if (!act) continue;
+    cg_verdict v;
+    v.first_unaddr = umin64(hc.pfu, mine.fu);
+    v.first_undef = mine.fd;
+    v.undef_count = mine.cnt;
+    v.dst_expected = de;
+    v.dst_found = df;
+    v.src_expected = se;
+    v.src_found = sf;
+    v.flags = flags;
+    v.status = 0;
+    bool apply_me = false;
+    if (small) {   // final verdict (a5), and the fused DtoH apply (a6)
+      finalize_fields(v.flags, v.status, v.first_unaddr, v.undef_count, err_mask);
+      if (fuse && nm.skind == CG_DTOH && v.status == CG_OK) {
+        if (d.reserved & CG_APPLY_AFTER) resid[atomicAdd(counter + 2, 1u)] = (uint32_t)i;
+        else apply_me = true;
+      }
+    }
+    out[i] = v;
+    weight[i] = small ? 0 : kItemCost + check_host_units(nm.skind, nscan, sv.two_bit != 0);
+    ScanMeta m;
+    m.hstart = nm.hstart;
+    m.hpitch = nm.hpitch;
+    m.W = nm.W;
+    m.info = nscan | ((uint64_t)(nm.skind & 3u) << kInfoKind) | ((uint64_t)(nscan != 0) << kInfoHost) |
+             ((uint64_t)contig << kInfoContig) | ((uint64_t)raw << kInfoRaw) | ((uint64_t)(hc.pfu != kNone) << kInfoPfu) |
+             ((uint64_t)(deferred || small) << kInfoDefer) |
+             ((uint64_t)((d.reserved & CG_APPLY_AFTER) != 0) << kInfoAfter) | ((uint64_t)flags << kInfoFlags);
+    meta[i] = m;
+    // fused a6 of the small DtoH sides with status OK, by the whole warp
+    uint32_t todo = __ballot_sync(__activemask(), apply_me);
+    while (todo) {
+      const int j = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint64_t a = __shfl_sync(__activemask(), q0, j), b = __shfl_sync(__activemask(), q1, j);
+      if (sv.two_bit) warp_fill2(sv.V, a, b, 0xAAAAAAAAu);
+      else warp_store_zero(sv.V, a, b);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_check_prep(const cg_copy_desc* __restrict__ descs,
+                                                         uint64_t n, Table t, cg_verdict* __restrict__ out,
+                                                         uint64_t* __restrict__ weight,
+                                                         ScanMeta* __restrict__ meta,
+                                                         uint64_t* __restrict__ dvoff, ShadowView sv,
+                                                         uint32_t* __restrict__ counter,
+                                                         uint32_t* __restrict__ defer, uint32_t err_mask, int fuse,
+                                                         uint32_t* __restrict__ resid) {
+  pdl_entry();
+  extern __shared__ uint64_t s_split[];
+  prep_body(descs, n, t, out, weight, meta, dvoff, sv, counter, defer, s_split, err_mask, fuse, resid);
+}
+
+// ---------------------------------------------------------------------------
+// a2: exclusive prefix sum (3 kernels) and the chunk plan
+// ---------------------------------------------------------------------------
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = kScanTile / kScanThreads;   // 8
+
+__device__ __forceinline__ uint64_t block_exclusive_scan(uint64_t x, uint64_t* s_warp, uint64_t& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint64_t inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint64_t y = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_warp[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    uint64_t w = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
+    uint64_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint64_t y = __shfl_up_sync(kFull, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < (int)(blockDim.x >> 5)) s_warp[lane] = wi - w;
+    if (lane == 31) s_warp[32] = wi;
+  }
+  __syncthreads();
+  total = s_warp[32];
+  uint64_t r = inc - x + s_warp[wid];
+  __syncthreads();
+  return r;
+}
+
+// n_dev != nullptr: the item count is min(n, *n_dev), known only on the device
+__device__ __forceinline__ uint64_t eff_n(uint64_t n, const uint32_t* n_dev) {
+  return n_dev ? umin64(n, *n_dev) : n;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint64_t* __restrict__ in, uint64_t n,
+                                                              uint64_t* __restrict__ bsum,
+                                                              const uint32_t* __restrict__ n_dev) {
+  pdl_entry();
+  __shared__ uint64_t s_warp[33];
+  n = eff_n(n, n_dev);
+  const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+  if (base >= n && base > 0) return;
+  uint64_t acc = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    uint64_t i = base + (uint64_t)j * kScanThreads + threadIdx.x;
+    if (i < n) acc += in[i];
+  }
+  uint64_t total;
+  block_exclusive_scan(acc, s_warp, total);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = total;
+}
+
+// single block: exclusive scan of bsum[0..nb) in place; bsum[nb] = out[n] = total
+__global__ void __launch_bounds__(1024) k_scan_top(uint64_t* __restrict__ bsum, uint64_t n,
+                                                   uint64_t* __restrict__ out, const uint32_t* __restrict__ n_dev) {
+  pdl_entry();
+  __shared__ uint64_t s_warp[33];
+  n = eff_n(n, n_dev);
+  const uint64_t nb = (n + kScanTile - 1) / kScanTile;
+  uint64_t carry = 0;
+  for (uint64_t base = 0; base < nb; base += blockDim.x) {
+    uint64_t i = base + threadIdx.x;
+    uint64_t x = i < nb ? bsum[i] : 0;
+    uint64_t total;
+    uint64_t ex = block_exclusive_scan(x, s_warp, total);
+    if (i < nb) bsum[i] = carry + ex;
+    carry += total;
+  }
+  if (threadIdx.x == 0) {
+    bsum[nb] = carry;
+    out[n] = carry;
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint64_t* __restrict__ in, uint64_t n,
+                                                            const uint64_t* __restrict__ bsum,
+                                                            uint64_t* __restrict__ out,
+                                                            const uint32_t* __restrict__ n_dev) {
+  pdl_entry();
+  __shared__ uint64_t s_items[kScanTile];
+  __shared__ uint64_t s_warp[33];
+  n = eff_n(n, n_dev);
+  const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+  if (base >= n) return;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    uint64_t i = base + (uint64_t)j * kScanThreads + threadIdx.x;
+    s_items[j * kScanThreads + threadIdx.x] = i < n ? in[i] : 0;
+  }
+  __syncthreads();
+  uint64_t loc[kScanItems];
+  uint64_t acc = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    loc[j] = acc;
+    acc += s_items[threadIdx.x * kScanItems + j];
+  }
+  uint64_t total;
+  uint64_t ex = block_exclusive_scan(acc, s_warp, total) + bsum[blockIdx.x];
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) s_items[threadIdx.x * kScanItems + j] = ex + loc[j];
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    uint64_t i = base + (uint64_t)j * kScanThreads + threadIdx.x;
+    if (i < n) out[i] = s_items[j * kScanThreads + threadIdx.x];
+  }
+}
+
+// T: the chunk map's granularity (weight units); Trule >= T: descriptors of
+// at most Trule weight are never split (owned by the group their weight
+// interval starts in), heavier ones always go through the split path
+constexpr uint64_t kSmallT = 128 * 1024;
+struct ChunkGeom {
+  uint64_t total, T, nchunks, Trule;
+};
+
+__device__ __forceinline__ ChunkGeom chunk_geom(const uint64_t* P, uint64_t n, uint64_t t_min,
+                                                uint64_t max_chunks) {
+  ChunkGeom g;
+  g.total = P[n];
+  uint64_t T = (g.total + max_chunks - 1) / max_chunks;
+  g.T = umax64(T, t_min);
+  g.nchunks = (g.total + g.T - 1) / g.T;
+  g.Trule = umax64(g.T, kSmallT);
+  return g;
+}
+
+// chunk_first[c] = the item whose weight interval [P[d], P[d+1]) contains c*T
+__global__ void __launch_bounds__(kThreads) k_plan(const uint64_t* __restrict__ P, uint64_t n, uint64_t t_min,
+                                                   uint64_t max_chunks, uint32_t* __restrict__ chunk_first,
+                                                   const uint32_t* __restrict__ n_dev) {
+  pdl_entry();
+  n = eff_n(n, n_dev);
+  const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
+  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < g.nchunks;
+       c += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t target = c * g.T;
+    uint64_t lo = 0, hi = n;   // P[lo] <= target < P[hi]
+    while (hi - lo > 1) {
+      uint64_t mid = (lo + hi) >> 1;
+      if (__ldg(P + mid) <= target) lo = mid; else hi = mid;
+    }
+    chunk_first[c] = (uint32_t)lo;
+  }
+}
+
+// a1-a3 + a2 in one cooperative launch: the prep (k_check_prep), then the
+// exclusive prefix sum of the weights and the chunk map with grid barriers
+// between the phases (k_scan_reduce / _top / _down, k_plan): one launch and
+// four barriers instead of five launches.
+__global__ void __launch_bounds__(kThreads) k_front(const cg_copy_desc* __restrict__ descs, uint64_t n, Table t,
+                                                    cg_verdict* __restrict__ out, uint64_t* __restrict__ weight,
+                                                    ScanMeta* __restrict__ meta, uint64_t* __restrict__ dvoff,
+                                                    ShadowView sv, uint32_t* __restrict__ counter,
+                                                    uint32_t* __restrict__ defer, uint64_t* P,
+                                                    uint64_t* __restrict__ bsum, uint64_t t_min, uint64_t max_chunks,
+                                                    uint32_t* __restrict__ chunk_first, uint32_t err_mask, int fuse,
+                                                    uint32_t* __restrict__ resid) {
+  pdl_entry();
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  extern __shared__ uint64_t s_split[];
+  __shared__ uint64_t s_warp[33];
+  prep_body(descs, n, t, out, weight, meta, dvoff, sv, counter, defer, s_split, err_mask, fuse, resid);
+  grid.sync();
+  // block b owns items [b*per, (b+1)*per)
+  const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const uint64_t lo = umin64(n, (uint64_t)blockIdx.x * per), hi = umin64(n, lo + per);
+  {
+    uint64_t acc = 0;
+    for (uint64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) acc += __ldcg(weight + k);
+    uint64_t total;
+    block_exclusive_scan(acc, s_warp, total);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = total;
+  }
+  grid.sync();
+  if (blockIdx.x == 0) {
+    uint64_t carry = 0;
+    for (uint64_t b0 = 0; b0 < gridDim.x; b0 += blockDim.x) {
+      const uint64_t b = b0 + threadIdx.x;
+      const uint64_t x = b < gridDim.x ? __ldcg(bsum + b) : 0;
+      uint64_t total;
+      const uint64_t ex = block_exclusive_scan(x, s_warp, total);
+      if (b < gridDim.x) bsum[b] = carry + ex;
+      carry += total;
+    }
+    if (threadIdx.x == 0) P[n] = carry;
+  }
+  grid.sync();
+  {
+    uint64_t carry = __ldcg(bsum + blockIdx.x);
+    for (uint64_t k0 = lo; k0 < hi; k0 += blockDim.x) {
+      const uint64_t k = k0 + threadIdx.x;
+      const uint64_t x = k < hi ? __ldcg(weight + k) : 0;
+      uint64_t total;
+      const uint64_t ex = block_exclusive_scan(x, s_warp, total);
+      if (k < hi) P[k] = carry + ex;
+      carry += total;
+    }
+  }
+  grid.sync();
+  const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
+  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < g.nchunks;
+       c += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t target = c * g.T;
+    uint64_t a = 0, b = n;   // P[a] <= target < P[b]
+    while (b - a > 1) {
+      const uint64_t mid = (a + b) >> 1;
+      if (__ldcg(P + mid) <= target) a = mid; else b = mid;
+    }
+    chunk_first[c] = (uint32_t)a;
+  }
+}
+
 // Tile generator.  All bookkeeping is lane-parallel:
 //  * descriptor window: lane i owns descriptor wbase+i and, whenever the window
 //    or the group changes, computes its piece (its share of the group's weight
@@ -1218,7 +1393,8 @@ struct TileGen {
     const bool live = (p_fl & (kPieceIn | kPiece2D | kPieceEmpty)) == kPieceIn;
     set_segment(live, p_qs, p_qe, p_ob, p_fu, (uint32_t)(wbase + lane),
                 (p_fl & kPieceHtod ? kTileHtod : 0u) | (p_fl & kPieceWhole ? kTileWhole : 0u) | kSegEndLast |
-                    (((m_info >> kInfoRaw) & 1u) ? kTileRaw : 0u) | ((uint32_t)(m_info >> kInfoFlags) << 16));
+                    (((m_info >> kInfoRaw) & 1u) ? kTileRaw : 0u) | (((m_info >> kInfoAfter) & 1u) ? kTileAfter : 0u) |
+                    ((uint32_t)((m_info >> kInfoFlags) & 0x3FFu) << 16));
     phase = kPhaseContig;
   }
 
@@ -1352,7 +1528,7 @@ struct TileGen {
       uint32_t f = kTileData | (s_fl & ~(kSegEndLast | kTileWhole));
       if (j + 1 == s_k && (s_fl & kSegEndLast)) {
         f |= kTileEnd | (s_fl & kTileWhole);
-        if (fuse && !htod && !(s_fl & kTileRaw)) {   // a contiguous DtoH piece: the consumer may apply it
+        if (fuse && !htod && !(s_fl & (kTileRaw | kTileAfter))) {   // a contiguous DtoH piece: the consumer may apply it
           f |= kTileFuse;
           ti.qs = s_q0;
           ti.qe = s_q1;
@@ -1705,6 +1881,7 @@ __global__ void __launch_bounds__(kThreads) k_finalize_split(uint64_t n, const u
   // the deferred list of the next check starts empty (its prep appends to it,
   // so it cannot reset it itself); resid_n = counter + 2
   if (blockIdx.x == 0 && threadIdx.x == 0) resid_n[2] = resid_n[3] = 0;
+  if (!fuse && blockIdx.x == 0 && threadIdx.x == 0) resid_n[0] = 0;   // nothing appends to the residual list unfused
   const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
   for (uint64_t d = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; d < n;
        d += (uint64_t)gridDim.x * blockDim.x) {
@@ -2002,7 +2179,7 @@ __global__ void __launch_bounds__(kThreads) k_finish(
   }
   grid.sync();
   const uint64_t m = __ldcg(resid_n);
-  if (m == 0) return;   // uniform: nothing left to apply
+  if (m == 0) return;   // uniform: nothing left to apply (the count stays 0 for the next check)
   for (uint64_t k = tid; k < m; k += nthr) {   // residual records (k_apply_list_prep)
     const cg_copy_desc d = descs[resid[k]];
     const Norm nm = normalize(d);
@@ -2015,6 +2192,7 @@ __global__ void __launch_bounds__(kThreads) k_finish(
     weight[k] = kApplyItemCost + nm.nbytes;
   }
   grid.sync();
+  if (tid == 0) *resid_n = 0;   // every block has read m: the next check's residual list starts empty
   // prefix sum of weight[0..m) into P: block b owns items [b*per, (b+1)*per)
   const uint64_t per = (m + gridDim.x - 1) / gridDim.x;
   const uint64_t lo = umin64(m, (uint64_t)blockIdx.x * per), hi = umin64(m, lo + per);
@@ -3140,9 +3318,12 @@ static cudaError_t check_front(const Launch& L, const cg_copy_desc* d, uint64_t 
     uint64_t* bsum = p.fbsum;
     uint64_t t_min = p.t_min, max_chunks = p.max_chunks;
     uint32_t* chunk_first = p.chunk_first;
+    uint32_t em = err_mask;
+    int fu = fuse ? 1 : 0;
+    uint32_t* resid = p.resid;
     void* args[] = {(void*)&d, (void*)&n, (void*)&tc, (void*)&out, (void*)&weight, (void*)&meta, (void*)&dvoff,
                     (void*)&svc, (void*)&counter, (void*)&defer, (void*)&P, (void*)&bsum, (void*)&t_min,
-                    (void*)&max_chunks, (void*)&chunk_first};
+                    (void*)&max_chunks, (void*)&chunk_first, (void*)&em, (void*)&fu, (void*)&resid};
     const cudaError_t e =
         cudaLaunchCooperativeKernel((const void*)k_front, dim3((unsigned)L.front_blocks), dim3(kThreads), args, smem, s);
     *L.counter += 1;
@@ -3150,7 +3331,7 @@ static cudaError_t check_front(const Launch& L, const cg_copy_desc* d, uint64_t 
     if (e != cudaSuccess) return e;   // nothing after it may consume a stale plan
   } else {
     launch_pdl(k_check_prep, blocks_for(n, kThreads, L.num_sms * 4), kThreads, smem, s, d, n, t, out, p.weight, meta,
-               p.dvoff, sv, p.counter, p.defer);
+               p.dvoff, sv, p.counter, p.defer, err_mask, fuse ? 1 : 0, p.resid);
     *L.counter += 1;
     L.stage(CG_STAGE_CHECK_PREP, false, s);
     L.stage(CG_STAGE_CHECK_PLAN, true, s);

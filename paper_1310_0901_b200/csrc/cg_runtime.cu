@@ -1342,6 +1342,37 @@ static bool host_range(const cg_copy_desc& d, uint64_t& lo, uint64_t& hi) {
   return true;
 }
 
+cg_status cg_plan_apply_after(cg_copy_desc* h_descs, uint64_t n, uint64_t* n_after) {
+  if (!n_after || (n && !h_descs)) return CG_ERR_INVALID_VALUE;
+  std::vector<std::pair<uint64_t, uint64_t>> rd;   // HtoD / HtoA host ranges, merged
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t lo, hi;
+    if (reads_host(h_descs[i].kind) && host_range(h_descs[i], lo, hi)) rd.emplace_back(lo, hi);
+  }
+  std::sort(rd.begin(), rd.end());
+  std::vector<std::pair<uint64_t, uint64_t>> m;
+  for (const auto& r : rd) {
+    if (!m.empty() && r.first <= m.back().second) m.back().second = std::max(m.back().second, r.second);
+    else m.push_back(r);
+  }
+  uint64_t k = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    cg_copy_desc& d = h_descs[i];
+    d.reserved &= ~(uint32_t)CG_APPLY_AFTER;
+    uint64_t lo, hi;
+    if (!writes_host(d.kind) || !host_range(d, lo, hi)) continue;
+    auto it = std::upper_bound(m.begin(), m.end(), std::make_pair(lo, UINT64_MAX));   // first range starting after lo
+    bool hit = it != m.end() && it->first < hi;
+    if (!hit && it != m.begin()) hit = std::prev(it)->second > lo;
+    if (hit) {
+      d.reserved |= CG_APPLY_AFTER;
+      ++k;
+    }
+  }
+  *n_after = k;
+  return CG_OK;
+}
+
 cg_status cg_batch_disjoint(const cg_copy_desc* h_descs, uint64_t n, int* disjoint) {
   if (!disjoint || (n && !h_descs)) return CG_ERR_INVALID_VALUE;
   struct Iv {

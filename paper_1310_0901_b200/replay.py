@@ -113,6 +113,13 @@ def replay_events(chk, events: np.ndarray, blob=None, stream=None, fuse: bool = 
                                 chk.apply_copies(dd, dv, stream=stream)
                             else:
                                 chk.apply_waves(dd, dv, waves, stream=stream)
+                        elif fuse and fuse != "disjoint":
+                            # any R-20 epoch fuses: DtoH ranges that an HtoD of the
+                            # batch also reads are applied after the scan (CG_APPLY_AFTER)
+                            part = np.ascontiguousarray(descs[s0:s1])
+                            pkg.plan_apply_after(part)
+                            dd = to_device_descs(part, chk.device)
+                            dv = chk.check_apply(dd, stream=stream)
                         elif fuse and pkg.batch_disjoint(descs[s0:s1]):
                             dv = chk.check_apply(dd, stream=stream)
                         else:

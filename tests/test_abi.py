@@ -317,3 +317,28 @@ def test_plan_waves_brute_force(cg, seed, arrays):
         want.append(lv)
     assert list(lev) == want
     assert nl == (max(want) + 1 if want else 0)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_plan_apply_after(cg, seed):
+    """cg_plan_apply_after marks exactly the DtoH / AtoH descriptors whose host
+    bounding range overlaps the host range of some HtoD / HtoA of the batch"""
+    tr = tg.random_tiny(seed + 21000, arrays=seed % 2 == 0)
+    descs = np.ascontiguousarray(tg.events_to_descs(tr.events[tr.events["op"] == tg.OP_COPY]))
+    descs["reserved"] = np.where(np.arange(len(descs)) % 3 == 0, cg.CG_APPLY_AFTER, 0)   # stale bits get cleared
+
+    def hrange(d, p):
+        if d["width"] == 0 or d["height"] == 0:
+            return None
+        s = int(d[p]) + int(d[p + "_y"]) * int(d[p + "_pitch"]) + int(d[p + "_x"])
+        e = s + (int(d["height"]) - 1) * int(d[p + "_pitch"]) + int(d["width"])
+        return None if e > (1 << 64) - 1 else (s, e)
+    reads = [hrange(d, "src") for d in descs if int(d["kind"]) in (1, 4)]
+    reads = [r for r in reads if r]
+    expect = []
+    for d in descs:
+        w = hrange(d, "dst") if int(d["kind"]) in (2, 5) else None
+        expect.append(bool(w) and any(a < w[1] and w[0] < b for a, b in reads))
+    k = cg.plan_apply_after(descs)
+    got = (descs["reserved"] & cg.CG_APPLY_AFTER) != 0
+    assert list(got) == expect and k == sum(expect)
