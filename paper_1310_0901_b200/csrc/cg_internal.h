@@ -130,6 +130,7 @@ struct Launch {
   int finish_blocks;      // cooperative grid of k_finish
   int front_blocks;       // cooperative grid of k_front (0: prep + plan as separate launches)
   int leak_blocks = 0;    // cooperative grid of k_leak (0: the 5-launch sweep)
+  int small_blocks = 0;   // grid of k_check_small (the small pass)
   uint64_t* counter;      // host counter of kernel launches
   Profiler* prof;
   void stage(int st, bool begin, cudaStream_t s) const {
@@ -140,7 +141,7 @@ struct Launch {
 constexpr int kScanTile = 2048;   // items per block of the prefix scan
 
 uint64_t scan_blocks(uint64_t n);
-int persistent_blocks(int which);   // 0: k_check_scan, 1: k_apply, 2: k_prop_waves, 3: k_finish, 4: k_front, 5: k_leak (per SM)
+int persistent_blocks(int which);   // 0: k_check_scan, 1: k_apply, 2: k_prop_waves, 3: k_finish, 4: k_front, 5: k_leak, 6: k_check_small (per SM)
 constexpr uint64_t kFinishMaxBlocks = 4096;
 constexpr size_t kFrontSmem = (4096 + 2) * sizeof(uint64_t);   // k_front: the largest splitter array
 size_t prop_meta_bytes();

@@ -258,8 +258,9 @@ struct __align__(16) ScanMeta {
 // info: scanned bytes (the shard clip, < 2^40) | scan kind << 40 | host << 42 |
 // contiguous << 43 | raw << 44 | pfu << 45 | not the ring's (deferred pass or
 // small pass) << 46 | apply after the scan (CG_APPLY_AFTER) << 47 | flags << 48
+// | small pass << 58
 constexpr int kInfoKind = 40, kInfoHost = 42, kInfoContig = 43, kInfoRaw = 44, kInfoPfu = 45, kInfoDefer = 46,
-              kInfoAfter = 47, kInfoFlags = 48;
+              kInfoAfter = 47, kInfoFlags = 48, kInfoSmall = 58;   // flags: 10 bits (48..57)
 constexpr uint64_t kInfoBytes = (1ull << 40) - 1;
 
 // ---------------------------------------------------------------------------
@@ -842,25 +843,26 @@ __device__ __noinline__ void small_pass(const ShadowView& sv, bool small, uint64
     // teams whose side is done reduce within the team and hand the partial to its owner
     const bool fin = own >= 0 && g >= t1;
     if (__any_sync(kFull, fin)) {
+      // xor partners stay inside the team; unfinished teams reduce identities
+      Partial r = fin ? acc : Partial{kNone, kNone, 0};
 #pragma unroll
       for (int o = kTeam / 2; o > 0; o >>= 1) {
-        acc.fu = umin64(acc.fu, __shfl_xor_sync(kFull, acc.fu, o));
-        acc.fd = umin64(acc.fd, __shfl_xor_sync(kFull, acc.fd, o));
-        acc.cnt += __shfl_xor_sync(kFull, acc.cnt, o);
+        r.fu = umin64(r.fu, __shfl_xor_sync(kFull, r.fu, o));
+        r.fd = umin64(r.fd, __shfl_xor_sync(kFull, r.fd, o));
+        r.cnt += __shfl_xor_sync(kFull, r.cnt, o);
       }
       uint32_t leaders = __ballot_sync(kFull, fin && tl == 0);
       while (leaders) {
         const int l = __ffs(leaders) - 1;
         leaders &= leaders - 1;
         const int who = __shfl_sync(kFull, own, l);
-        const uint64_t fu = __shfl_sync(kFull, acc.fu, l), fd = __shfl_sync(kFull, acc.fd, l);
-        const uint64_t cnt = __shfl_sync(kFull, acc.cnt, l);
+        const uint64_t fu = __shfl_sync(kFull, r.fu, l), fd = __shfl_sync(kFull, r.fd, l);
+        const uint64_t cnt = __shfl_sync(kFull, r.cnt, l);
         if (lane == who) mine = Partial{fu, fd, cnt};
       }
       if (fin) {
         own = -1;
         acc = Partial{kNone, kNone, 0};
-      } else {   // the reduction summed the unfinished teams' lanes too: only finished teams reduced meaningfully
       }
     }
   }
@@ -870,8 +872,7 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
                                           cg_verdict* __restrict__ out, uint64_t* __restrict__ weight,
                                           ScanMeta* __restrict__ meta, uint64_t* __restrict__ dvoff,
                                           const ShadowView& sv, uint32_t* __restrict__ counter,
-                                          uint32_t* __restrict__ defer, uint64_t* s_split, uint32_t err_mask,
-                                          int fuse, uint32_t* __restrict__ resid) {
+                                          uint32_t* __restrict__ defer, uint64_t* s_split, uint32_t err_mask) {
   // the scan's group counter and the apply count: reset here instead of by a
   // memset node, which would break the PDL chain.  The residual list (count:
   // counter[2]) and the deferred list (count, cursor: counter[4], [5]) are
@@ -948,73 +949,112 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
     if (deferred) defer[atomicAdd(counter + 4, 1u)] = (uint32_t)i;
     const bool contig = d.height == 1 || d.width == nm.hpitch;
     const bool raw = d.reserved & CG_SHARD_RAW;   // partial of a straddler: no finalisation here
-    // the small pass (bytes and dense 2-bit formats): contiguous, whole, not raw
+    // the small pass (bytes and dense 2-bit formats): contiguous, whole, not
+    // raw -- checked by k_check_small, not by the ring; its verdict is written
+    // here already finalised as if the host side were clean (k_check_small
+    // rewrites only the dirty ones)
     const bool small = nscan != 0 && nscan <= kSmallBytes && contig && !raw && !sv.sparse;
+    if (act) {
+      cg_verdict v;
+      v.first_unaddr = hc.pfu;
+      v.first_undef = kNone;
+      v.undef_count = 0;
+      v.dst_expected = de;
+      v.dst_found = df;
+      v.src_expected = se;
+      v.src_found = sf;
+      v.flags = flags;
+      v.status = 0;
+      if (small) finalize_fields(v.flags, v.status, v.first_unaddr, 0, err_mask);
+      out[i] = v;
+      weight[i] = small ? 0 : kItemCost + check_host_units(nm.skind, nscan, sv.two_bit != 0);
+      ScanMeta m;
+      m.hstart = nm.hstart;
+      m.hpitch = nm.hpitch;
+      m.W = nm.W;
+      m.info = nscan | ((uint64_t)(nm.skind & 3u) << kInfoKind) | ((uint64_t)(nscan != 0) << kInfoHost) |
+               ((uint64_t)contig << kInfoContig) | ((uint64_t)raw << kInfoRaw) |
+               ((uint64_t)(hc.pfu != kNone) << kInfoPfu) | ((uint64_t)(deferred || small) << kInfoDefer) |
+               ((uint64_t)((d.reserved & CG_APPLY_AFTER) != 0) << kInfoAfter) | ((uint64_t)flags << kInfoFlags) |
+               ((uint64_t)small << kInfoSmall);
+      meta[i] = m;
+    }
+  }
+}
+
+// The small pass (a4-a6 for small contiguous host sides): a warp takes 32
+// consecutive descriptors (one coalesced meta load), its teams check the
+// small ones; a dirty verdict is rewritten, a clean one was final already;
+// small DtoH sides with status OK are applied here when fused (a6) unless
+// CG_APPLY_AFTER sends them to the residual pass.
+template <bool kTwoBit>
+__global__ void __launch_bounds__(kThreads) k_check_small(const ScanMeta* __restrict__ meta, uint64_t n,
+                                                          ShadowView sv, cg_verdict* __restrict__ out,
+                                                          uint32_t err_mask, int fuse, uint32_t* __restrict__ resid,
+                                                          uint32_t* __restrict__ resid_n) {
+  pdl_entry();
+  const int lane = threadIdx.x & 31;
+  const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += nthr) {
+    const uint64_t i = base + lane;
+    uint64_t info = 0, x0 = 0;
+    if (i < n) {
+      const ScanMeta m = meta[i];
+      info = m.info;
+      x0 = m.hstart;
+    }
+    const bool small = (info >> kInfoSmall) & 1u;
+    if (!__any_sync(kFull, small)) continue;
+    const bool htod = ((info >> kInfoKind) & 3u) == CG_HTOD;
     uint64_t q0 = 0, q1 = 0, ob = 0;
-    if (small) {
-      const uint64_t x = nm.hstart + hc.olo;   // shard bytes [x, x + nscan), logical offset of shard byte q: q + sb - x0
+    if (small) {   // shard bytes [x, x + nscan); logical offset of shard byte q = q + sb - x0 (R-10 clip)
+      const uint64_t x = x0 + (sv.sb > x0 ? sv.sb - x0 : 0);
       q0 = x - sv.sb;
-      q1 = q0 + nscan;
-      ob = sv.sb - nm.hstart;
+      q1 = q0 + (info & kInfoBytes);
+      ob = sv.sb - x0;
     }
     Partial mine{kNone, kNone, 0};
-    if (__any_sync(kFull, small)) {
-      if (sv.two_bit) small_pass<true>(sv, small, q0, q1, ob, nm.skind == CG_HTOD, mine);
-      else small_pass<false>(sv, small, q0, q1, ob, nm.skind == CG_HTOD, mine);
-    }
-    if (!act) continue;
-    cg_verdict v;
-    v.first_unaddr = umin64(hc.pfu, mine.fu);
-    v.first_undef = mine.fd;
-    v.undef_count = mine.cnt;
-    v.dst_expected = de;
-    v.dst_found = df;
-    v.src_expected = se;
-    v.src_found = sf;
-    v.flags = flags;
-    v.status = 0;
+    small_pass<kTwoBit>(sv, small, q0, q1, ob, htod, mine);
     bool apply_me = false;
-    if (small) {   // final verdict (a5), and the fused DtoH apply (a6)
-      finalize_fields(v.flags, v.status, v.first_unaddr, v.undef_count, err_mask);
-      if (fuse && nm.skind == CG_DTOH && v.status == CG_OK) {
-        if (d.reserved & CG_APPLY_AFTER) resid[atomicAdd(counter + 2, 1u)] = (uint32_t)i;
+    if (small) {
+      uint64_t fu = mine.fu;
+      if ((info >> kInfoPfu) & 1u) fu = umin64(fu, out[i].first_unaddr);
+      uint32_t flags = (uint32_t)((info >> kInfoFlags) & 0x3FFu), status;
+      finalize_fields(flags, status, fu, mine.cnt, err_mask);
+      if (fu != kNone || mine.fd != kNone || mine.cnt) {   // dirty: rewrite (clean verdicts are final already)
+        cg_verdict* v = out + i;
+        v->first_unaddr = fu;
+        v->first_undef = mine.fd;
+        v->undef_count = mine.cnt;
+        v->flags = flags;
+        v->status = status;
+      }
+      if (fuse && !htod && status == CG_OK) {
+        if ((info >> kInfoAfter) & 1u) resid[atomicAdd(resid_n, 1u)] = (uint32_t)i;
         else apply_me = true;
       }
     }
-    out[i] = v;
-    weight[i] = small ? 0 : kItemCost + check_host_units(nm.skind, nscan, sv.two_bit != 0);
-    ScanMeta m;
-    m.hstart = nm.hstart;
-    m.hpitch = nm.hpitch;
-    m.W = nm.W;
-    m.info = nscan | ((uint64_t)(nm.skind & 3u) << kInfoKind) | ((uint64_t)(nscan != 0) << kInfoHost) |
-             ((uint64_t)contig << kInfoContig) | ((uint64_t)raw << kInfoRaw) | ((uint64_t)(hc.pfu != kNone) << kInfoPfu) |
-             ((uint64_t)(deferred || small) << kInfoDefer) |
-             ((uint64_t)((d.reserved & CG_APPLY_AFTER) != 0) << kInfoAfter) | ((uint64_t)flags << kInfoFlags);
-    meta[i] = m;
-    // fused a6 of the small DtoH sides with status OK, by the whole warp
-    uint32_t todo = __ballot_sync(__activemask(), apply_me);
-    while (todo) {
+    uint32_t todo = __ballot_sync(kFull, apply_me);
+    while (todo) {   // fused a6, the whole warp per side
       const int j = __ffs(todo) - 1;
       todo &= todo - 1;
-      const uint64_t a = __shfl_sync(__activemask(), q0, j), b = __shfl_sync(__activemask(), q1, j);
-      if (sv.two_bit) warp_fill2(sv.V, a, b, 0xAAAAAAAAu);
+      const uint64_t a = __shfl_sync(kFull, q0, j), b = __shfl_sync(kFull, q1, j);
+      if (kTwoBit) warp_fill2(sv.V, a, b, 0xAAAAAAAAu);
       else warp_store_zero(sv.V, a, b);
     }
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_check_prep(const cg_copy_desc* __restrict__ descs,
+__global__ void __launch_bounds__(kThreads, 4) k_check_prep(const cg_copy_desc* __restrict__ descs,
                                                          uint64_t n, Table t, cg_verdict* __restrict__ out,
                                                          uint64_t* __restrict__ weight,
                                                          ScanMeta* __restrict__ meta,
                                                          uint64_t* __restrict__ dvoff, ShadowView sv,
                                                          uint32_t* __restrict__ counter,
-                                                         uint32_t* __restrict__ defer, uint32_t err_mask, int fuse,
-                                                         uint32_t* __restrict__ resid) {
+                                                         uint32_t* __restrict__ defer, uint32_t err_mask) {
   pdl_entry();
   extern __shared__ uint64_t s_split[];
-  prep_body(descs, n, t, out, weight, meta, dvoff, sv, counter, defer, s_split, err_mask, fuse, resid);
+  prep_body(descs, n, t, out, weight, meta, dvoff, sv, counter, defer, s_split, err_mask);
 }
 
 // ---------------------------------------------------------------------------
@@ -1174,19 +1214,18 @@ __global__ void __launch_bounds__(kThreads) k_plan(const uint64_t* __restrict__ 
 // exclusive prefix sum of the weights and the chunk map with grid barriers
 // between the phases (k_scan_reduce / _top / _down, k_plan): one launch and
 // four barriers instead of five launches.
-__global__ void __launch_bounds__(kThreads) k_front(const cg_copy_desc* __restrict__ descs, uint64_t n, Table t,
+__global__ void __launch_bounds__(kThreads, 4) k_front(const cg_copy_desc* __restrict__ descs, uint64_t n, Table t,
                                                     cg_verdict* __restrict__ out, uint64_t* __restrict__ weight,
                                                     ScanMeta* __restrict__ meta, uint64_t* __restrict__ dvoff,
                                                     ShadowView sv, uint32_t* __restrict__ counter,
                                                     uint32_t* __restrict__ defer, uint64_t* P,
                                                     uint64_t* __restrict__ bsum, uint64_t t_min, uint64_t max_chunks,
-                                                    uint32_t* __restrict__ chunk_first, uint32_t err_mask, int fuse,
-                                                    uint32_t* __restrict__ resid) {
+                                                    uint32_t* __restrict__ chunk_first, uint32_t err_mask) {
   pdl_entry();
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   extern __shared__ uint64_t s_split[];
   __shared__ uint64_t s_warp[33];
-  prep_body(descs, n, t, out, weight, meta, dvoff, sv, counter, defer, s_split, err_mask, fuse, resid);
+  prep_body(descs, n, t, out, weight, meta, dvoff, sv, counter, defer, s_split, err_mask);
   grid.sync();
   // block b owns items [b*per, (b+1)*per)
   const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
@@ -3319,11 +3358,9 @@ static cudaError_t check_front(const Launch& L, const cg_copy_desc* d, uint64_t 
     uint64_t t_min = p.t_min, max_chunks = p.max_chunks;
     uint32_t* chunk_first = p.chunk_first;
     uint32_t em = err_mask;
-    int fu = fuse ? 1 : 0;
-    uint32_t* resid = p.resid;
     void* args[] = {(void*)&d, (void*)&n, (void*)&tc, (void*)&out, (void*)&weight, (void*)&meta, (void*)&dvoff,
                     (void*)&svc, (void*)&counter, (void*)&defer, (void*)&P, (void*)&bsum, (void*)&t_min,
-                    (void*)&max_chunks, (void*)&chunk_first, (void*)&em, (void*)&fu, (void*)&resid};
+                    (void*)&max_chunks, (void*)&chunk_first, (void*)&em};
     const cudaError_t e =
         cudaLaunchCooperativeKernel((const void*)k_front, dim3((unsigned)L.front_blocks), dim3(kThreads), args, smem, s);
     *L.counter += 1;
@@ -3331,7 +3368,7 @@ static cudaError_t check_front(const Launch& L, const cg_copy_desc* d, uint64_t 
     if (e != cudaSuccess) return e;   // nothing after it may consume a stale plan
   } else {
     launch_pdl(k_check_prep, blocks_for(n, kThreads, L.num_sms * 4), kThreads, smem, s, d, n, t, out, p.weight, meta,
-               p.dvoff, sv, p.counter, p.defer, err_mask, fuse ? 1 : 0, p.resid);
+               p.dvoff, sv, p.counter, p.defer, err_mask);
     *L.counter += 1;
     L.stage(CG_STAGE_CHECK_PREP, false, s);
     L.stage(CG_STAGE_CHECK_PLAN, true, s);
@@ -3339,6 +3376,11 @@ static cudaError_t check_front(const Launch& L, const cg_copy_desc* d, uint64_t 
     L.stage(CG_STAGE_CHECK_PLAN, false, s);
   }
   L.stage(CG_STAGE_CHECK_SCAN, true, s);
+  if (!sv.sparse) {   // the small pass (k_check_small), then the ring scan
+    launch_pdl(sv.two_bit ? k_check_small<true> : k_check_small<false>, L.small_blocks, kThreads, 0, s, meta, n, sv,
+               out, err_mask, fuse ? 1 : 0, p.resid, p.counter + 2);
+    *L.counter += 1;
+  }
   auto scan = !sv.two_bit ? (fuse ? k_check_scan<false, true, false> : k_check_scan<false, false, false>)
               : sv.sparse ? (fuse ? k_check_scan<true, true, true> : k_check_scan<true, false, true>)
                           : (fuse ? k_check_scan<true, true, false> : k_check_scan<true, false, false>);
@@ -3634,6 +3676,11 @@ int persistent_blocks(int which) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_front, kThreads, kFrontSmem);
   } else if (which == 5) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_leak, kThreads, 0);
+  } else if (which == 6) {
+    int b2 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_check_small<false>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_check_small<true>, kThreads, 0);
+    b = std::min(b, b2);
   } else if (which == 3) {
     int b2 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_finish<false>, kThreads, 0);

@@ -434,6 +434,7 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
   c->launch.front_blocks = std::min(prop.multiProcessorCount * cgk::persistent_blocks(4), (int)cgk::kFinishMaxBlocks);
   if (const char* fr = getenv("CG_FRONT_COOP")) if (atoi(fr) == 0) c->launch.front_blocks = 0;
   c->launch.leak_blocks = std::min(prop.multiProcessorCount * cgk::persistent_blocks(5), (int)cgk::kFinishMaxBlocks);
+  c->launch.small_blocks = prop.multiProcessorCount * std::max(cgk::persistent_blocks(6), 1);
   if (const char* lk = getenv("CG_LEAK_COOP")) if (atoi(lk) == 0) c->launch.leak_blocks = 0;
   c->launch.finish_blocks = std::min(prop.multiProcessorCount * std::max(cgk::persistent_blocks(3), 1),
                                      (int)cgk::kFinishMaxBlocks);
