@@ -557,6 +557,90 @@ cg_status cg_compact_dirty(cg_ctx *ctx, const cg_verdict *d_verdicts, uint64_t n
 cg_status cg_shard_plan(const cg_copy_desc *h_descs, uint64_t n, uint64_t host_base, uint64_t host_size,
                         uint32_t world, uint32_t *h_owner, uint32_t *h_first, uint32_t *h_last);
 
+/* ---- host-address-range shards inside the library (
+ * BASELINE north_star: the shadow address space and the copy batch are
+ * partitioned across GPUs by host-address range, with an NCCL gather of the
+ * per-descriptor verdicts) ----
+ * A shard group is G <= 8 contexts whose shards split the same global window,
+ * every one holding the whole (replicated) allocation table.  cg_comm is the
+ * group's collective backend: NCCL (one rank = one context per process; the
+ * library loads libnccl.so.2 with dlopen -- in a torch process the copy torch
+ * loaded) or LOOPBACK (all G contexts in this process, on one device; the
+ * collectives read the G ranks' device buffers directly). */
+typedef struct cg_comm cg_comm;
+enum { CG_COMM_NCCL = 0, CG_COMM_LOOPBACK = 1 };
+#define CG_NCCL_ID_BYTES 128
+
+/* CUDA device ordinal of a context (or -1 for NULL). */
+int cg_ctx_device(const cg_ctx *ctx);
+
+/* A fresh NCCL unique id (128 bytes into h_id) -- on rank 0; the caller hands
+ * it to every rank (e.g. a torch.distributed broadcast).  CG_ERR_NCCL if
+ * libnccl cannot be loaded. */
+cg_status cg_comm_nccl_id(uint8_t *h_id);
+
+/* NCCL backend for this process's context `ctx`, rank `rank` of `world`
+ * (<= 8); every rank calls it with the same id (collective).
+ * max_straddlers: the most straddling descriptors one cg_check_sharded call
+ * may carry; cap: the most dirty verdicts one rank sends to the root per call
+ * (fixed-size gather buffers; more are counted and reported by
+ * cg_comm_overflow).  The comm allocates its own device scratch (cudaMalloc,
+ * freed by cg_comm_destroy).  Errors: CG_ERR_INVALID_VALUE, CG_ERR_NCCL,
+ * CG_ERR_OUT_OF_MEMORY. */
+cg_status cg_comm_create_nccl(cg_ctx *ctx, uint32_t world, uint32_t rank, const uint8_t *h_id,
+                              uint64_t max_straddlers, uint64_t cap, cg_comm **out);
+
+/* LOOPBACK backend over the world (<= 8) contexts ctxs[0..world) of this
+ * process, all on one device; rank r = ctxs[r], rank 0 is the root. */
+cg_status cg_comm_create_loopback(cg_ctx *const *ctxs, uint32_t world, uint64_t max_straddlers, uint64_t cap,
+                                  cg_comm **out);
+cg_status cg_comm_destroy(cg_comm *comm);
+const char *cg_comm_last_error(const cg_comm *comm);
+uint64_t cg_comm_kernel_launches(const cg_comm *comm);
+
+/* Synchronous: *overflow = 1 if, since the last query, some rank had more
+ * dirty verdicts than `cap` in a cg_check_sharded call (the root's list is
+ * then incomplete; the ranks' own verdict arrays are still exact); resets it. */
+cg_status cg_comm_overflow(cg_comm *comm, uint32_t *overflow);
+
+/* One local rank's part of a sharded batch (cg_shard_lists builds it). */
+typedef struct {
+  const cg_copy_desc *d_descs;   /* n_own owned descriptors, then the m straddlers (device) */
+  uint64_t n_own, m;             /* m: equal on every rank, same straddlers in the same order */
+  const uint64_t *d_gidx;        /* n_own + m global indices of the listed descriptors (device) */
+  cg_verdict *d_out;             /* n_own + m verdicts, final after the call (device) */
+} cg_shard_batch;
+
+/* The sharded check of one batch (a hazard-free R-20 epoch), for every local
+ * rank of comm (batches[r]; NCCL: one), asynchronous on stream with no host
+ * synchronisation: the fused check + DtoH apply of each rank's list, the
+ * straddler exchange (pack, three all-reduces: MIN of the first offsets, SUM
+ * of the count and of the owner-only device fields, MAX = OR of the flags;
+ * finalize on every rank; each rank applies its shard part of the straddling
+ * DtoH copies with status OK), then every rank's dirty verdicts with their
+ * global indices gathered to the root (rank 0) and merged there by a kernel
+ * into d_root_idx / d_root_dirty (capacity world * cap) with the count in
+ * *d_root_count (device u64), and, if d_dense is not NULL, scattered into the
+ * dense d_dense[n_total] (clean entries canonical).  Root outputs are only
+ * read on the root (may be NULL elsewhere).  Errors: CG_ERR_INVALID_VALUE
+ * (unequal m, m > max_straddlers, NULL), CG_ERR_NCCL, CG_ERR_CUDA, and those
+ * of cg_check_apply. */
+cg_status cg_check_sharded(cg_comm *comm, const cg_shard_batch *batches, uint64_t *d_root_idx,
+                           cg_verdict *d_root_dirty, uint64_t *d_root_count, cg_verdict *d_dense, uint64_t n_total,
+                           void *stream);
+
+/* Host planner of a sharded batch: rank `rank`'s list of the n descriptors
+ * h_descs (an R-20 epoch) over `world` equal shards of [host_base, host_base +
+ * host_size): the descriptors it owns (cg_shard_plan: host range in its shard
+ * only, or no host side and index mod world == rank) in order, then every
+ * straddler in order with CG_SHARD_RAW (and CG_SHARD_NOT_OWNER unless it owns
+ * it), CG_APPLY_AFTER set as cg_plan_apply_after sets it on the list.  h_out /
+ * h_gidx need room for n entries; *n_own, *m receive the counts.  Errors:
+ * CG_ERR_INVALID_VALUE (as cg_shard_plan). */
+cg_status cg_shard_lists(const cg_copy_desc *h_descs, uint64_t n, uint64_t host_base, uint64_t host_size,
+                         uint32_t world, uint32_t rank, cg_copy_desc *h_out, uint64_t *h_gidx, uint64_t *n_own,
+                         uint64_t *m);
+
 /* Leak sweep on the device: writes the live allocations
  * (ascending base) to d_out (at most cap records) and their total number to
  * *d_count (a device u64).  Asynchronous on stream. */

@@ -9,12 +9,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcgcheck.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("cg_kernels.cu", "cg_runtime.cu", "cg_conc.cu")]
+SOURCES = [os.path.join(CSRC, f) for f in ("cg_kernels.cu", "cg_runtime.cu", "cg_conc.cu", "cg_shard.cu")]
 HEADERS = [os.path.join(ROOT, "include", "cg.h"), os.path.join(CSRC, "cg_internal.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "-shared", "-Xptxas", "-v",
-         "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+         "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-ldl"]
 
 
 def stale() -> bool:

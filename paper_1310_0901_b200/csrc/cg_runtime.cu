@@ -1343,6 +1343,34 @@ static bool host_range(const cg_copy_desc& d, uint64_t& lo, uint64_t& hi) {
   return true;
 }
 
+int cg_ctx_device(const cg_ctx* c) { return c ? c->cfg.device : -1; }
+
+cg_status cg_shard_lists(const cg_copy_desc* h_descs, uint64_t n, uint64_t host_base, uint64_t host_size,
+                         uint32_t world, uint32_t rank, cg_copy_desc* h_out, uint64_t* h_gidx, uint64_t* n_own,
+                         uint64_t* m) {
+  if (!n_own || !m || rank >= world || (n && (!h_descs || !h_out || !h_gidx))) return CG_ERR_INVALID_VALUE;
+  std::vector<uint32_t> owner(n), first(n), last(n);
+  cg_status st = cg_shard_plan(h_descs, n, host_base, host_size, world, owner.data(), first.data(), last.data());
+  if (st != CG_OK) return st;
+  uint64_t k = 0;
+  for (uint64_t i = 0; i < n; ++i)
+    if (first[i] == last[i] && owner[i] == rank) {
+      h_out[k] = h_descs[i];
+      h_out[k].reserved = 0;
+      h_gidx[k++] = i;
+    }
+  *n_own = k;
+  for (uint64_t i = 0; i < n; ++i)
+    if (first[i] < last[i]) {
+      h_out[k] = h_descs[i];
+      h_out[k].reserved = CG_SHARD_RAW | (owner[i] == rank ? 0u : (uint32_t)CG_SHARD_NOT_OWNER);
+      h_gidx[k++] = i;
+    }
+  *m = k - *n_own;
+  uint64_t after = 0;
+  return cg_plan_apply_after(h_out, k, &after);
+}
+
 cg_status cg_plan_apply_after(cg_copy_desc* h_descs, uint64_t n, uint64_t* n_after) {
   if (!n_after || (n && !h_descs)) return CG_ERR_INVALID_VALUE;
   std::vector<std::pair<uint64_t, uint64_t>> rd;   // HtoD / HtoA host ranges, merged
@@ -1360,6 +1388,7 @@ cg_status cg_plan_apply_after(cg_copy_desc* h_descs, uint64_t n, uint64_t* n_aft
   for (uint64_t i = 0; i < n; ++i) {
     cg_copy_desc& d = h_descs[i];
     d.reserved &= ~(uint32_t)CG_APPLY_AFTER;
+    if (d.reserved & CG_SHARD_RAW) continue;   // a straddler is applied after the exchange anyway
     uint64_t lo, hi;
     if (!writes_host(d.kind) || !host_range(d, lo, hi)) continue;
     auto it = std::upper_bound(m.begin(), m.end(), std::make_pair(lo, UINT64_MAX));   // first range starting after lo
