@@ -2,23 +2,29 @@
 """Benchmark of the batched transfer checker on B200 (BASELINE.json metric:
 "shadow GB/s and copy-descriptors/s validated (1/2/4/8 B200, % of HBM peak)").
 
-One step = one pass of the whole hot path over one batch:
-cg_check_copies (a1-a5) + cg_apply_dtoh (a6) + cg_leak_sweep (a8) on the
-1M-copy / 100k-allocation configuration (BASELINE.json configs[1], C2).  The
+N=1 (default): one step = one pass of the whole hot path over
+the 1M-copy / 100k-allocation configuration (BASELINE.json configs[1], C2):
+cg_check_apply (a1-a6, fused) per R-20 epoch + cg_leak_sweep (a8).  The
 registry (a7) is built once before timing; its host throughput is reported
 separately.  Inputs are resident in HBM when the timed region starts; the
-shadow read per step (~8.5 GB) is far larger than the 126 MB L2, so no flush is
-needed.
+shadow read per step (~8.5 GB) is far larger than the 126 MB L2, so no flush
+is needed.  The same line carries `per_config`: C3, C4 and C5 (at one GPU)
+through the same measured step.
 
-`value` = algorithmic shadow bytes per step (HtoD 1.125 B, DtoH check 0.125 B
-+ apply 1 B per host byte) x steps / device time.  `e2e` = the
-same through cg_check_copies_host with pinned HOST descriptor / verdict
-buffers (the H2D and D2H copies inside the timed region).
+`value` = algorithmic bytes per step (shadow: HtoD 1.125 B, DtoH check 0.125 B
++ apply 1 B per host byte; descriptors: 96 B read + 64 B verdict written;
+SURVEY §8(d)) / device time.  `e2e` = the same through the public host-buffer
+entry point cg_check_host_submit / _wait (pinned host descriptors up, dirty
+verdicts down, inside the timed region).
 
---impl reference times the CPU oracle (the reference arm of this tier) on a
-bounded sample of the same workload on the host cores.
-Multi-GPU (torchrun, N>1): weak scaling -- every rank checks its own C2 batch
-over its own shard of the host window; time = max over ranks.
+N>1 (torchrun): strong scaling on C5 (configs[4], "64 GB host shadow space
+sharded across 8 B200"): the same trace on every rank, the window split N
+ways, one cg_check_sharded per epoch (NCCL straddler exchange + verdict
+gather inside the library); time = max over ranks.  --sharded runs that code
+path at N=1 (one NCCL rank), --loopback G with G shards on one GPU.
+
+--impl reference times the CPU oracle (the reference arm of this tier), on
+the host's cores, on a bounded sample of the same workload.
 """
 from __future__ import annotations
 
@@ -281,31 +287,9 @@ def run_ours(args, rank, world, device, config=None, steps=None, warmup=None, e2
                 chk.check_copies(dd, dv, stream=stream)
                 chk.apply_dtoh(dd, dv, stream=stream)
 
-    comm = None
-    if world > 1:
-        import torch.distributed as dist
-        comm = dist
-        g_idx = torch.empty(n, dtype=torch.int64, device=device)
-        g_dirty = torch.empty(n * 64, dtype=torch.uint8, device=device)
-        g_cnt = torch.zeros(1, dtype=torch.int32, device=device)
-        # one untimed probe fixes the padded gather size (the batch is the same every step)
-        check_epochs()
-        cg.cg_compact_dirty(chk.ctx, d_out.data_ptr(), n, g_idx.data_ptr(), g_dirty.data_ptr(),
-                            g_cnt.data_ptr(), stream.cuda_stream)
-        mx_t = g_cnt.to(torch.int64)
-        dist.all_reduce(mx_t, op=dist.ReduceOp.MAX)
-        from paper_1310_0901_b200.sharded import PackedDirtyGather
-        pg = PackedDirtyGather(dist, max(1, int(mx_t.item())), torch.device("cuda", device))
-
     def step():
         check_epochs()
         chk.leak_sweep(d_leaks, nalloc, d_cnt, stream=stream)
-        if comm is not None:
-            # the exchange: every rank's compacted dirty verdicts (count, index,
-            # 64-byte verdict) gathered over NCCL, device to device, no host sync
-            cg.cg_compact_dirty(chk.ctx, d_out.data_ptr(), n, pg.idx_ptr(), pg.dirty_ptr(), pg.count_ptr(),
-                                stream.cuda_stream)
-            pg.gather()   # one NCCL all_gather of the packed (count, index, verdict) buffers
 
     for _ in range(warmup):
         step()
@@ -328,14 +312,6 @@ def run_ours(args, rank, world, device, config=None, steps=None, warmup=None, e2
         ev1.record(stream)
         torch.cuda.synchronize()
     stages = chk.profile_end()
-    if world > 1:
-        torch.distributed.barrier()
-        got = pg.unpack()
-        mine = got[rank]
-        tot = torch.tensor([mine[0]], dtype=torch.int64, device=device)
-        torch.distributed.all_reduce(tot)
-        assert sum(c for c, _, _ in got) == int(tot.item()), "dirty-verdict gather lost records"
-        assert np.array_equal(mine[2]["flags"], verd["flags"][mine[1]]), "gathered verdicts differ"
     launches = chk.kernel_launches - launches0
     ms = ev0.elapsed_time(ev1)
     if world > 1:
@@ -509,6 +485,151 @@ def run_ours(args, rank, world, device, config=None, steps=None, warmup=None, e2
     return res
 
 
+def run_sharded_bench(args, rank, world, device, backend):
+    """Strong scaling on C5 (BASELINE.json configs[4]: "64 GB host shadow space
+    sharded across 8 B200, 10M mixed HtoD/DtoH/DtoD descriptors with
+    interleaved alloc/free and final leak report"): the SAME trace on every
+    rank, the 64 GiB window split `world` ways (shard r on rank r), the
+    allocation table replicated; per step and R-20 epoch one cg_check_sharded
+    (fused check + apply of the rank's list, the straddler exchange over NCCL,
+    the dirty-verdict gather to the root and its merge kernel, all on the
+    device), then the leak sweep.  backend "nccl": one rank per process
+    (torchrun); "loopback": all shards in this process on one GPU (the same
+    library path, for one-GPU measurement and testing)."""
+    import torch
+    import paper_1310_0901_b200 as cg
+    import tracegen as tg
+    from paper_1310_0901_b200.sharded import ShardGroup, replay_sharded
+    torch.cuda.set_device(device)
+    tr = make_workload("c5_sharded", 0, args.scale)   # one trace, the same on every rank
+    ev = tr.events
+    descs = tg.events_to_descs(ev[ev["op"] == 5])
+    n = len(descs)
+    nreg = int(np.count_nonzero(ev["op"] == 3))
+    cuts = [0] + [int(c) for c in cg.plan_batches(descs)]
+    epochs = [(a, b) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
+    max_epoch = max(b - a for a, b in epochs)
+    cap = max(4096, max_epoch // 8)
+    group = ShardGroup(tr.host_base, tr.host_size, world, backend=backend, rank=rank, device=device,
+                       max_descs=max_epoch, max_allocs=max(nreg, 1024), max_straddlers=max(4096, max_epoch // 64),
+                       cap=cap)
+    t0 = time.perf_counter()
+    replay_sharded(group, ev[ev["op"] != 5], tr.blob)
+    t_setup = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    batches = [group.batch(descs[a:b], dense=False) for a, b in epochs]
+    t_plan = time.perf_counter() - t0
+    stream = torch.cuda.current_stream()
+    leaks = [(torch.empty(max(nreg, 1) * 24, dtype=torch.uint8, device=device),
+              torch.zeros(1, dtype=torch.int64, device=device)) for _ in group.chks]
+    # e2e: every step uploads each rank's lists from pinned host memory and the
+    # root downloads its merged dirty lists
+    pinned = [[(torch.empty_like(t, device="cpu").pin_memory(), t) for t in (bt.keep[0][0], bt.keep[0][1])]
+              for bt in batches] if not args.no_e2e else None
+    if pinned:
+        for bp in pinned:
+            for h, d in bp:
+                h.copy_(d)
+
+    def step(upload=False):
+        for k, bt in enumerate(batches):
+            if upload:
+                for h, d in pinned[k]:
+                    d.copy_(h, non_blocking=True)
+            group.check(bt, stream=stream)
+        for c, (dl, dc) in zip(group.chks, leaks):
+            c.leak_sweep(dl, nreg, dc, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    assert not group.overflow(), "a rank had more dirty verdicts than the gather capacity"
+    # the root's merged dirty lists -> algorithmic bytes (an OK DtoH is a clean one)
+    dirty = np.zeros(n, bool)
+    if group.is_root:
+        for (a, b), bt in zip(epochs, batches):
+            c = int(bt.root_count.item())
+            dirty[a + bt.root_idx[:c].cpu().numpy()] = True
+    n_dirty = int(dirty.sum())
+    fake = np.zeros(n, [("status", "<u4")])
+    fake["status"] = dirty
+    check_b, apply_b = algorithmic_bytes(descs, fake)
+    desc_b = float(n) * (96 + 64)
+    bytes_per_step = check_b + apply_b + desc_b
+    dist = None
+    if backend == "nccl" and world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = group.kernel_launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(device) as clocks:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = group.kernel_launches - l0
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    e2e = None
+    if pinned:
+        k = max(3, args.steps // 4)
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        e0.record(stream)
+        for _ in range(k):
+            step(upload=True)
+            if group.is_root:   # the root reads its merged dirty lists (count, then the records)
+                for bt in batches:
+                    c = int(bt.root_count.item())
+                    bt.root_idx[:c].cpu()
+                    bt.root_dirty[:c * 64].cpu()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1) / k
+        if dist is not None:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        up = sum(h.numel() * h.element_size() for bp in pinned for h, _ in bp)
+        e2e = {"value": bytes_per_step / (e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e_ms,
+               "entry": "ShardGroup.check = cg_check_sharded per epoch, lists uploaded from pinned host memory, "
+                        "the root's merged dirty lists downloaded",
+               "h2d_bytes_per_step": int(up), "d2h_bytes_per_step": int(8 * len(batches) + 72 * n_dirty),
+               "wall_s": time.perf_counter() - w0}
+    peak, peak_kind = load_peaks()
+    value = bytes_per_step / (ms_step * 1e-3) / 1e9
+    res = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world if backend == "nccl" else 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": "c5_sharded (BASELINE.json configs[4]: 64 GiB host window, 10M mixed descriptors, "
+                               "alloc/free bursts, leak report)",
+                   "descriptors_per_step": n, "allocations": nreg, "host_window_bytes": tr.host_size,
+                   "algorithmic_bytes_per_step": bytes_per_step, "check_bytes": check_b, "apply_bytes": apply_b,
+                   "descriptor_bytes": desc_b, "epochs": len(epochs),
+                   "straddlers_per_step": int(sum(bt.m for bt in batches)),
+                   "parallelism": f"host-range shards x{world} ({backend})",
+                   "l2": "no flush: >= 1 GB of shadow streamed per rank per step vs 126 MB L2",
+                   "entry": "cg_check_sharded per epoch + cg_leak_sweep", "gather_cap_per_rank": cap},
+        "descriptors_per_s": n / (ms_step * 1e-3),
+        "shadow_gbs": (check_b + apply_b) / (ms_step * 1e-3) / 1e9,
+        "frac_of_hbm": value / ((world if backend == "nccl" else 1) * peak),
+        "gpu_launches": int(launches), "gpu_launches_per_step": launches / args.steps,
+        "clocks": clocks.summary(), "e2e": e2e, "setup_s": t_setup, "plan_s": t_plan,
+        "dirty_verdicts": n_dirty,
+    }
+    group.close()
+    return res
+
+
 PER_CONFIG = ("c3_single", "c4_pitched", "c5_sharded")
 
 
@@ -674,6 +795,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-registry-rate", action="store_true")
     ap.add_argument("--no-per-config", action="store_true", help="skip the C3/C4/C5 per_config runs")
+    ap.add_argument("--sharded", action="store_true",
+                    help="at N=1: the multi-GPU code path (C5 through cg_check_sharded, NCCL with one rank)")
+    ap.add_argument("--loopback", type=int, default=0,
+                    help="C5 split into this many shards on ONE GPU through the loopback cg_comm")
     ap.add_argument("--unfused", action="store_true", help="check and apply as two calls")
     ap.add_argument("--track", action="store_true", help="NEXT-1 device V-bit tracking (apply = propagation)")
     ap.add_argument("--conc", type=int, default=0, help="NEXT-2: also time cg_conc_check with this many threads")
@@ -711,8 +836,21 @@ def main():
         return
 
     import torch
-    if world > 1:
+    if world > 1 or args.sharded:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        res = run_sharded_bench(args, rank, world, local, "nccl")
+        if rank == 0:
+            print(json.dumps(res))
+        torch.distributed.destroy_process_group()
+        return
+    if args.loopback > 1:
+        print(json.dumps(run_sharded_bench(args, 0, args.loopback, local, "loopback")))
+        return
     res = run_ours(args, rank, world, local)
     if rank == 0:
         if world == 1 and args.config == "c2_small" and not args.no_per_config and not args.track \

@@ -135,6 +135,16 @@ def _load() -> ctypes.CDLL:
         "cg_conc_check": (I, [P, P, P, U64, P, P]),
         "cg_conc_stamps": (I, [P, P, P]),
         "cg_conc_kernel_launches": (U64, [P]),
+        "cg_ctx_device": (I, [P]),
+        "cg_comm_nccl_id": (I, [P]),
+        "cg_comm_create_nccl": (I, [P, U32, U32, P, U64, U64, P]),
+        "cg_comm_create_loopback": (I, [P, U32, U64, U64, P]),
+        "cg_comm_destroy": (I, [P]),
+        "cg_comm_last_error": (ctypes.c_char_p, [P]),
+        "cg_comm_kernel_launches": (U64, [P]),
+        "cg_comm_overflow": (I, [P, P]),
+        "cg_check_sharded": (I, [P, P, P, P, P, P, U64, P]),
+        "cg_shard_lists": (I, [P, U64, U64, U64, U32, U32, P, P, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -153,7 +163,9 @@ EXPORTED = ("cg_workspace_size", "cg_ctx_create", "cg_ctx_destroy", "cg_last_err
             "cg_format_leak", "cg_apply_copies", "cg_device_vbits", "cg_array_vbits", "cg_plan_batches_propagate",
             "cg_host_shadow_read", "cg_apply_copies_subset", "cg_plan_waves", "cg_apply_flush", "cg_apply_copies_waves", "cg_summarize", "cg_format_summary", "cg_array_bytes", "cg_register_array", "cg_free_array", "cg_array_report", "cg_conc_create",
             "cg_conc_destroy", "cg_conc_last_error", "cg_conc_sync", "cg_conc_check", "cg_conc_stamps",
-            "cg_conc_kernel_launches")
+            "cg_conc_kernel_launches", "cg_ctx_device", "cg_comm_nccl_id", "cg_comm_create_nccl",
+            "cg_comm_create_loopback", "cg_comm_destroy", "cg_comm_last_error", "cg_comm_kernel_launches",
+            "cg_comm_overflow", "cg_check_sharded", "cg_shard_lists")
 
 # ---- same-name thin wrappers (status codes returned unchanged) -------------
 cg_workspace_size = _lib.cg_workspace_size
@@ -260,6 +272,8 @@ COPY1D_DTYPE = np.dtype([("kind", "<u4"), ("reserved", "<u4"), ("seq", "<u8"), (
                          ("bytes", "<u8")])
 cg_shard_plan = _lib.cg_shard_plan
 CG_SHARD_NOT_OWNER, CG_SHARD_RAW, CG_APPLY_AFTER = 1, 2, 4
+CG_COMM_NCCL, CG_COMM_LOOPBACK = 0, 1
+CG_NCCL_ID_BYTES = 128
 cg_batch_disjoint = _lib.cg_batch_disjoint
 cg_leak_sweep = _lib.cg_leak_sweep
 cg_leak_report = _lib.cg_leak_report

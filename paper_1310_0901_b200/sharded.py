@@ -3,299 +3,181 @@
 by host-address range, with an NCCL gather over NVLink only for the
 per-descriptor verdicts").
 
+Argument marshalling only: the planning (cg_shard_lists), the check, the
+straddler exchange, the gather and the root merge all run in the library
+(cg_comm / cg_check_sharded, csrc/cg_shard.cu); torch provides the device
+buffers, the process group that hands the NCCL id to every rank, and the
+streams.
+
 Rank r stores the shadow of shard r = [H0 + r*S/G, H0 + (r+1)*S/G) of the
-global window (its context's shard) and replays every setup event (only its
-shard part is stored; the allocation table is replicated).  A batch is split
-with cg_shard_plan:
-
-* a descriptor whose host range lies in one shard goes to that shard's rank
-  only (the owner), which finalises it locally;
-* a straddler (host range over several shards) goes to every rank, flagged
-  CG_SHARD_RAW (and CG_SHARD_NOT_OWNER except on its owner): each rank writes
-  its raw partial, the partials are merged with three all-reduces (MIN of the
-  first offsets, SUM of the count and of the owner-only device fields, MAX of
-  the flags -- validation flags are identical everywhere, device flags come
-  from the owner only, so MAX = OR), and cg_straddler_finalize derives flags
-  and status on every rank; each rank then applies its shard part of the
-  straddling DtoH copies whose merged verdict is OK;
-* the root gathers every rank's dirty verdicts (cg_compact_dirty: clean
-  verdicts are canonical and are not sent) plus their counts and assembles the
-  dense verdict array.
-
-Two communicators implement the same three collectives: TorchComm
-(torch.distributed -- NCCL over NVLink on GPUs) and LoopbackGroup (G shards in
-one process on one GPU, reductions across the G tensors) for single-GPU
-testing.  The descriptors' reserved field carries the shard mode bits.
+global window and replays every setup event (only its shard part is stored;
+the allocation table is replicated).  Two backends: NCCL (one rank per
+process, torchrun) and loopback (all G shards in this process on one GPU --
+the single-GPU test and measurement of the same code path).
 """
 from __future__ import annotations
 
+import ctypes
 from typing import List, Optional
 
 import numpy as np
 
-from . import (CG_NONE, CG_SHARD_NOT_OWNER, CG_SHARD_RAW, DESC_DTYPE, VERDICT_DTYPE, Checker, CgError, _lib,
-               _stream_ptr, shard_plan, batch_disjoint, to_device_descs)
+from . import (CG_COMM_LOOPBACK, CG_COMM_NCCL, CG_NCCL_ID_BYTES, CG_NONE, DESC_DTYPE, MARK_DTYPE, VERDICT_DTYPE,
+               Checker, CgError, _lib, _stream_ptr, plan_batches)
 
 
-class BatchPlan:
-    """Per-rank descriptor lists of one batch (identical on every rank)."""
+def shard_lists(descs: np.ndarray, host_base: int, host_size: int, world: int, rank: int):
+    """cg_shard_lists: (rank's list with mode bits, global indices, n_own, m)"""
+    d = np.ascontiguousarray(descs, dtype=DESC_DTYPE)
+    n = len(d)
+    out = np.zeros(max(n, 1), DESC_DTYPE)
+    gidx = np.zeros(max(n, 1), np.uint64)
+    n_own, m = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    st = _lib.cg_shard_lists(d.ctypes.data if n else None, n, host_base, host_size, world, rank, out.ctypes.data,
+                             gidx.ctypes.data, ctypes.byref(n_own), ctypes.byref(m))
+    if st:
+        raise CgError(st, "cg_shard_lists")
+    k = n_own.value + m.value
+    return out[:k], gidx[:k], n_own.value, m.value
 
-    def __init__(self, descs: np.ndarray, host_base: int, host_size: int, world: int):
+
+class ShardBatch:
+    """One batch uploaded for every local rank (device lists, global indices,
+    verdict arrays) plus the root's outputs."""
+
+    def __init__(self, group: "ShardGroup", descs: np.ndarray, dense: bool = True):
+        torch = group.torch
         self.n = len(descs)
-        self.world = world
-        owner, first, last = shard_plan(descs, host_base, host_size, world)
-        self.owner = owner
-        self.straddler = first < last
-        self.strad_idx = np.flatnonzero(self.straddler)
-        self.mine_idx = [np.flatnonzero((owner == r) & ~self.straddler) for r in range(world)]
-        self.descs = descs
+        self.lists = []
+        self.keep = []
+        for r in group.local_ranks:
+            d, gidx, n_own, m = shard_lists(descs, group.host_base, group.host_size, group.world, r)
+            dev = torch.device("cuda", group.device)
+            dd = torch.from_numpy(d.view(np.uint8).copy()).to(dev) if len(d) else torch.empty(96, dtype=torch.uint8, device=dev)
+            dg = torch.from_numpy(gidx.view(np.int64).copy()).to(dev) if len(d) else torch.empty(1, dtype=torch.int64, device=dev)
+            dv = torch.empty(max(len(d), 1) * VERDICT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+            self.keep.append((dd, dg, dv))
+            self.lists.append((n_own, m))
+        self.m = self.lists[0][1]
+        B = _ShardBatchC * len(self.lists)
+        self.c = B()
+        for k, ((n_own, m), (dd, dg, dv)) in enumerate(zip(self.lists, self.keep)):
+            self.c[k] = _ShardBatchC(dd.data_ptr(), n_own, m, dg.data_ptr(), dv.data_ptr())
+        dev = torch.device("cuda", group.device)
+        cap_all = group.world * group.cap
+        self.root_idx = torch.empty(cap_all, dtype=torch.int64, device=dev)
+        self.root_dirty = torch.empty(cap_all * VERDICT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        self.root_count = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.dense = torch.empty(max(self.n, 1) * VERDICT_DTYPE.itemsize, dtype=torch.uint8, device=dev) \
+            if dense else None
 
-    def local(self, rank: int):
-        """(local descriptors with mode bits, global indices, n_mine, m)."""
-        mine, strad = self.mine_idx[rank], self.strad_idx
-        idx = np.concatenate([mine, strad])
-        d = np.ascontiguousarray(self.descs[idx]).copy()
-        d["reserved"] = 0
-        if len(strad):
-            bits = np.full(len(strad), CG_SHARD_RAW, np.uint32)
-            bits[self.owner[strad] != rank] |= CG_SHARD_NOT_OWNER
-            d["reserved"][len(mine):] = bits
-        return d, idx, len(mine), len(strad)
+
+class _ShardBatchC(ctypes.Structure):
+    _fields_ = [("d_descs", ctypes.c_void_p), ("n_own", ctypes.c_uint64), ("m", ctypes.c_uint64),
+                ("d_gidx", ctypes.c_void_p), ("d_out", ctypes.c_void_p)]
 
 
-class ShardedChecker:
-    """One rank: a Checker over its shard of the global window."""
+class ShardGroup:
+    """G shards of [host_base, host_base + host_size) with a cg_comm.  backend
+    "loopback": all G contexts here (one GPU); "nccl": this process's rank
+    (torch.distributed must be initialised; the NCCL id is broadcast over it)."""
 
-    def __init__(self, host_base: int, host_size: int, rank: int, world: int, device: int = 0, **kw):
+    def __init__(self, host_base: int, host_size: int, world: int, *, backend: str = "loopback", rank: int = 0,
+                 device: int = 0, max_straddlers: int = 1 << 16, cap: int = 1 << 16, **kw):
+        import torch
         if host_size % world or (host_size // world) % 4096:
             raise CgError(1, "shards must be multiples of 4096 bytes")
-        self.host_base, self.host_size, self.rank, self.world = host_base, host_size, rank, world
+        if world > 8:
+            raise CgError(1, "at most 8 shards")
+        self.torch = torch
+        self.host_base, self.host_size, self.world, self.device = host_base, host_size, world, device
+        self.cap = cap
+        self.backend = backend
         shard = host_size // world
-        self.chk = Checker(host_base, host_size, shard_base=host_base + rank * shard, shard_size=shard,
-                           device=device, **kw)
-        self.device = device
-        self.torch = self.chk.torch
+        self.local_ranks = list(range(world)) if backend == "loopback" else [rank]
+        self.rank = rank
+        self.chks = [Checker(host_base, host_size, shard_base=host_base + r * shard, shard_size=shard, device=device,
+                             **kw) for r in self.local_ranks]
+        comm = ctypes.c_void_p()
+        if backend == "loopback":
+            arr = (ctypes.c_void_p * world)(*[c.ctx.value for c in self.chks])
+            st = _lib.cg_comm_create_loopback(arr, world, max_straddlers, cap, ctypes.byref(comm))
+        else:
+            import torch.distributed as dist
+            nid = torch.zeros(CG_NCCL_ID_BYTES, dtype=torch.uint8)
+            if rank == 0:
+                buf = (ctypes.c_uint8 * CG_NCCL_ID_BYTES)()
+                st = _lib.cg_comm_nccl_id(buf)
+                if st:
+                    raise CgError(st, "cg_comm_nccl_id")
+                nid = torch.from_numpy(np.frombuffer(bytes(buf), np.uint8).copy())
+            if dist.get_backend() == "nccl":
+                nid = nid.to(torch.device("cuda", device))
+            dist.broadcast(nid, 0)
+            idb = (ctypes.c_uint8 * CG_NCCL_ID_BYTES)(*nid.cpu().numpy().tolist())
+            st = _lib.cg_comm_create_nccl(self.chks[0].ctx, world, rank, idb, max_straddlers, cap, ctypes.byref(comm))
+        if st:
+            raise CgError(st, "cg_comm_create")
+        self.comm = comm
+
+    @property
+    def is_root(self) -> bool:
+        return self.backend == "loopback" or self.rank == 0
 
     def close(self):
-        self.chk.close()
+        if getattr(self, "comm", None):
+            _lib.cg_comm_destroy(self.comm)
+            self.comm = None
+        for c in self.chks:
+            c.close()
 
-    # ---- per-rank steps (all in the library's kernels) ---------------------
-    def check(self, plan: BatchPlan, fuse: bool):
-        d, idx, n_mine, m = plan.local(self.rank)
-        dd = to_device_descs(d, self.device)
-        # fused only when the rank's whole batch is apply-disjoint
-        fused = fuse and batch_disjoint(d)
-        dv = self.chk.check_apply(dd) if fused else self.chk.check_copies(dd)
-        return dict(dd=dd, dv=dv, idx=idx, n_mine=n_mine, m=m, fused=fused)
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
-    def pack(self, st):
-        torch, m = self.torch, st["m"]
-        mins = torch.empty(2 * m, dtype=torch.int64, device=self.device)
-        sums = torch.empty(5 * m, dtype=torch.int64, device=self.device)
-        maxs = torch.empty(m, dtype=torch.int32, device=self.device)
-        if m:
-            raw = st["dv"].data_ptr() + st["n_mine"] * VERDICT_DTYPE.itemsize
-            self.chk._ok(_lib.cg_straddler_pack(self.chk.ctx, raw, m, mins.data_ptr(), sums.data_ptr(),
-                                                maxs.data_ptr(), _stream_ptr(None)), "cg_straddler_pack")
-        return mins, sums, maxs
+    @property
+    def kernel_launches(self) -> int:
+        return int(_lib.cg_comm_kernel_launches(self.comm)) + sum(c.kernel_launches for c in self.chks)
 
-    def finalize(self, st, mins, sums, maxs):
-        m = st["m"]
-        if m:
-            out = st["dv"].data_ptr() + st["n_mine"] * VERDICT_DTYPE.itemsize
-            self.chk._ok(_lib.cg_straddler_finalize(self.chk.ctx, mins.data_ptr(), sums.data_ptr(), maxs.data_ptr(),
-                                                    m, out, _stream_ptr(None)), "cg_straddler_finalize")
+    def batch(self, descs: np.ndarray, dense: bool = True) -> ShardBatch:
+        return ShardBatch(self, descs, dense)
 
-    def apply(self, st):
-        """DtoH apply after the merge: the straddlers (each rank its shard
-        part), plus everything if the check was not fused."""
-        W = VERDICT_DTYPE.itemsize
-        if not st["fused"]:
-            self.chk.apply_dtoh(st["dd"], st["dv"])
-        elif st["m"]:
-            n0 = st["n_mine"] * DESC_DTYPE.itemsize
-            self.chk.apply_dtoh(st["dd"][n0:], st["dv"][st["n_mine"] * W:])
+    def check(self, b: ShardBatch, stream=None):
+        """cg_check_sharded: every local rank's part, asynchronous"""
+        dense = b.dense.data_ptr() if b.dense is not None else None
+        st = _lib.cg_check_sharded(self.comm, b.c, b.root_idx.data_ptr(), b.root_dirty.data_ptr(),
+                                   b.root_count.data_ptr(), dense, b.n, _stream_ptr(stream))
+        if st:
+            raise CgError(st, "cg_check_sharded: " + _lib.cg_comm_last_error(self.comm).decode())
 
-    def compact(self, st):
-        torch, n = self.torch, st["n_mine"]
-        idx = torch.empty(max(n, 1), dtype=torch.int64, device=self.device)
-        dirty = torch.empty(max(n, 1) * VERDICT_DTYPE.itemsize, dtype=torch.uint8, device=self.device)
-        cnt = torch.zeros(1, dtype=torch.int32, device=self.device)
-        self.chk._ok(_lib.cg_compact_dirty(self.chk.ctx, st["dv"].data_ptr(), n, idx.data_ptr(), dirty.data_ptr(),
-                                           cnt.data_ptr(), _stream_ptr(None)), "cg_compact_dirty")
-        return cnt, idx, dirty
+    def overflow(self) -> bool:
+        o = ctypes.c_uint32(0)
+        st = _lib.cg_comm_overflow(self.comm, ctypes.byref(o))
+        if st:
+            raise CgError(st, "cg_comm_overflow")
+        return bool(o.value)
+
+    def dense(self, b: ShardBatch) -> np.ndarray:
+        """the root's dense verdicts of the last check of b (synchronises)"""
+        self.torch.cuda.synchronize(self.device)
+        assert not self.overflow(), "a rank had more dirty verdicts than cap"
+        return b.dense.cpu().numpy().view(VERDICT_DTYPE)[:b.n]
+
+    # ---- setup calls go to every local rank --------------------------------
+    def all(self, fn):
+        return [fn(c) for c in self.chks]
 
 
-def _clean(n: int) -> np.ndarray:
-    v = np.zeros(n, VERDICT_DTYPE)
-    v["first_unaddr"] = CG_NONE
-    v["first_undef"] = CG_NONE
-    return v
-
-
-def _assemble(plan: BatchPlan, per_rank, strad_dv) -> np.ndarray:
-    """Dense verdicts from every rank's (count, local idx, dirty) + the merged
-    straddlers (root side)."""
-    out = _clean(plan.n)
-    for r, (cnt, idx, dirty) in enumerate(per_rank):
-        c = int(cnt)
-        if c:
-            gidx = plan.mine_idx[r][idx[:c]]
-            out[gidx] = dirty[:c]
-    if len(plan.strad_idx):
-        out[plan.strad_idx] = strad_dv
-    return out
-
-
-class TorchComm:
-    """Collectives over torch.distributed (NCCL on GPUs)."""
-
-    def __init__(self):
-        import torch.distributed as dist
-        self.dist = dist
-
-    def allreduce3(self, mins, sums, maxs):
-        d = self.dist
-        if mins.numel():
-            d.all_reduce(mins, op=d.ReduceOp.MIN)   # u64 order mapped onto i64 by the caller
-            d.all_reduce(sums, op=d.ReduceOp.SUM)
-            d.all_reduce(maxs, op=d.ReduceOp.MAX)
-
-    def gather_dirty(self, cnt, idx, dirty, root: int = 0):
-        """all ranks' (count, idx, dirty) -> list on every rank (padded all_gather)."""
-        import torch
-        d = self.dist
-        world = d.get_world_size()
-        counts = [torch.zeros(1, dtype=torch.int32, device=cnt.device) for _ in range(world)]
-        d.all_gather(counts, cnt)
-        mx = max(1, max(int(c.item()) for c in counts))
-        W = VERDICT_DTYPE.itemsize
-        pi = torch.zeros(mx, dtype=torch.int64, device=cnt.device)
-        pd = torch.zeros(mx * W, dtype=torch.uint8, device=cnt.device)
-        c0 = int(cnt.item())
-        pi[:c0] = idx[:c0]
-        pd[:c0 * W] = dirty[:c0 * W]
-        gi = [torch.empty_like(pi) for _ in range(world)]
-        gd = [torch.empty_like(pd) for _ in range(world)]
-        d.all_gather(gi, pi)
-        d.all_gather(gd, pd)
-        return [(int(counts[r].item()), gi[r].cpu().numpy(), gd[r].cpu().numpy().view(VERDICT_DTYPE))
-                for r in range(world)]
-
-
-class PackedDirtyGather:
-    """The N>1 bench exchange in ONE collective: each rank packs (count,
-    index[mx], verdict[mx]) into a fixed buffer of 16 + 72 mx bytes that
-    cg_compact_dirty writes straight into (count at byte 0, indices at 16,
-    verdicts after them), and one all_gather_into_tensor moves every rank's
-    buffer to every rank, device to device, with no host synchronisation.
-    mx must bound every rank's dirty count (the bench fixes it from an
-    untimed probe of the same batch)."""
-
-    def __init__(self, dist, mx: int, device):
-        import torch
-        self.dist = dist
-        self.world = dist.get_world_size()
-        self.mx = mx + (mx & 1)   # keeps the verdicts 16-byte aligned
-        self.nbytes = 16 + 72 * self.mx
-        self.send = torch.zeros(self.nbytes, dtype=torch.uint8, device=device)
-        self.recv = torch.empty(self.world * self.nbytes, dtype=torch.uint8, device=device)
-
-    # device pointers for cg_compact_dirty
-    def count_ptr(self) -> int:
-        return self.send.data_ptr()
-
-    def idx_ptr(self) -> int:
-        return self.send.data_ptr() + 16
-
-    def dirty_ptr(self) -> int:
-        return self.send.data_ptr() + 16 + 8 * self.mx
-
-    def gather(self):
-        self.dist.all_gather_into_tensor(self.recv, self.send)
-
-    def unpack(self):
-        """host view of the last gather: [(count, idx, verdicts)] per rank"""
-        buf = self.recv.cpu().numpy()
-        out = []
-        for r in range(self.world):
-            b = buf[r * self.nbytes:(r + 1) * self.nbytes]
-            c = int(b[:4].view(np.int32)[0])
-            idx = b[16:16 + 8 * self.mx].view(np.int64)[:c]
-            dv = b[16 + 8 * self.mx:].view(VERDICT_DTYPE)[:c]
-            out.append((c, idx, dv))
-        return out
-
-
-def _u64_min_fix(t):
-    """MIN over u64 fields held in int64 tensors: map u64 order onto i64 order
-    (flip the sign bit) before and after the reduction."""
-    return t ^ (-(1 << 63))
-
-
-def run_distributed(sc: ShardedChecker, plan: BatchPlan, comm: Optional[TorchComm] = None, fuse: bool = True,
-                    root: int = 0) -> Optional[np.ndarray]:
-    """One rank's part of a sharded batch; returns the dense verdicts on root."""
-    comm = comm or TorchComm()
-    st = sc.check(plan, fuse)
-    mins, sums, maxs = sc.pack(st)
-    if st["m"]:
-        mins = _u64_min_fix(mins)
-        comm.allreduce3(mins, sums, maxs)
-        mins = _u64_min_fix(mins)
-    sc.finalize(st, mins, sums, maxs)
-    sc.apply(st)
-    cnt, idx, dirty = sc.compact(st)
-    gathered = comm.gather_dirty(cnt, idx, dirty, root)
-    if sc.rank != root:
-        return None
-    W = VERDICT_DTYPE.itemsize
-    strad = st["dv"][st["n_mine"] * W:].cpu().numpy().view(VERDICT_DTYPE)
-    return _assemble(plan, gathered, strad)
-
-
-class LoopbackGroup:
-    """G shards in one process on one GPU: the same per-rank kernels, with the
-    three all-reduces and the gather done across the G device tensors."""
-
-    def __init__(self, host_base: int, host_size: int, world: int, device: int = 0, **kw):
-        self.ranks = [ShardedChecker(host_base, host_size, r, world, device, **kw) for r in range(world)]
-        self.host_base, self.host_size, self.world = host_base, host_size, world
-
-    def close(self):
-        for r in self.ranks:
-            r.close()
-
-    def run(self, plan: BatchPlan, fuse: bool = True) -> np.ndarray:
-        import torch
-        sts = [sc.check(plan, fuse) for sc in self.ranks]
-        packed = [sc.pack(st) for sc, st in zip(self.ranks, sts)]
-        if plan.strad_idx.size:
-            mins = _u64_min_fix(torch.stack([_u64_min_fix(p[0]) for p in packed]).min(0).values)
-            sums = torch.stack([p[1] for p in packed]).sum(0)
-            maxs = torch.stack([p[2] for p in packed]).max(0).values
-        for sc, st, p in zip(self.ranks, sts, packed):
-            if st["m"]:
-                sc.finalize(st, mins.clone(), sums.clone(), maxs.clone())
-            sc.apply(st)
-        per_rank = []
-        for sc, st in zip(self.ranks, sts):
-            cnt, idx, dirty = sc.compact(st)
-            c = int(cnt.item())
-            per_rank.append((c, idx[:max(c, 1)].cpu().numpy(),
-                             dirty[:max(c, 1) * VERDICT_DTYPE.itemsize].cpu().numpy().view(VERDICT_DTYPE)))
-        W = VERDICT_DTYPE.itemsize
-        st0 = sts[0]
-        strad = st0["dv"][st0["n_mine"] * W:].cpu().numpy().view(VERDICT_DTYPE)
-        return _assemble(plan, per_rank, strad)
-
-
-def replay_sharded(group: LoopbackGroup, events: np.ndarray, blob=None, fuse: bool = True):
-    """Replay a call stream over the G shards of a LoopbackGroup: setup calls go
-    to every shard, copies are checked in hazard-free batches sharded by host
-    range.  Returns (verdicts of the copies, status per event)."""
+def replay_sharded(group: ShardGroup, events: np.ndarray, blob=None, fuse: bool = True):
+    """Replay a call stream over the shards of a group: setup calls go to every
+    local shard, copies are checked with cg_check_sharded in the hazard-free
+    batches cg_plan_batches cuts.  Returns (verdicts of the copies, status per
+    event) on the root (NCCL: every rank returns its statuses, the verdicts are
+    the root's).  fuse is accepted for symmetry: the sharded check is always
+    the fused one (CG_APPLY_AFTER planned per rank list)."""
     from .replay import OP_COPY, OP_FREE, OP_FREEA, OP_MARK, OP_REG, OP_REGA, OP_SETV, OP_SYNC, events_to_descs
-    from . import MARK_DTYPE, plan_batches
     ops = np.asarray(events["op"])
     n = len(events)
     status = np.zeros(n, np.uint32)
@@ -312,9 +194,9 @@ def replay_sharded(group: LoopbackGroup, events: np.ndarray, blob=None, fuse: bo
             m = np.zeros(j - i, MARK_DTYPE)
             m["addr"], m["len"], m["state"] = events["dst"][i:j], events["width"][i:j], events["kind"][i:j]
             sts = []
-            for sc in group.ranks:
+            for c in group.chks:
                 s_ = np.zeros(j - i, np.uint32)
-                sc.chk.host_mark_batch(m, status_out=s_)
+                c.host_mark_batch(m, status_out=s_)
                 sts.append(s_)
             status[i:j] = sts[0]
             i = j
@@ -322,11 +204,14 @@ def replay_sharded(group: LoopbackGroup, events: np.ndarray, blob=None, fuse: bo
             off, ln = int(events["src"][i]), int(events["width"][i])
             addr = int(events["dst"][i])
             # all-or-nothing across shards: every shard must hold only addressable bytes of it
-            if all(sc.chk.host_query_addressable(addr, ln) for sc in group.ranks):
-                rs = [sc.chk.host_set_vbits(addr, bytes(blob[off:off + ln])) for sc in group.ranks]
-                status[i] = max(rs)
-            else:
-                status[i] = 1
+            ok = all(c.host_query_addressable(addr, ln) for c in group.chks)
+            if group.backend == "nccl":
+                t = group.torch.tensor([0 if ok else 1], dtype=group.torch.int32,
+                                       device=group.torch.device("cuda", group.device))
+                import torch.distributed as dist
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ok = int(t.item()) == 0
+            status[i] = max(c.host_set_vbits(addr, bytes(blob[off:off + ln])) for c in group.chks) if ok else 1
             i += 1
         else:
             j = i
@@ -337,32 +222,30 @@ def replay_sharded(group: LoopbackGroup, events: np.ndarray, blob=None, fuse: bo
                 i += 1
                 continue
             for k in range(i, j):
+                e = events[k]
                 if ops[k] == OP_REG:
-                    rs = [sc.chk.register_alloc(int(events["dst"][k]), int(events["width"][k]),
-                                                int(events["seq"][k])) for sc in group.ranks]
-                    status[k] = rs[0]
+                    status[k] = group.all(lambda c: c.register_alloc(int(e["dst"]), int(e["width"]), int(e["seq"])))[0]
                 elif ops[k] == OP_FREE:
-                    rs = [sc.chk.free(int(events["dst"][k]), int(events["seq"][k])) for sc in group.ranks]
-                    status[k] = rs[0]
+                    status[k] = group.all(lambda c: c.free(int(e["dst"]), int(e["seq"])))[0]
                 elif ops[k] == OP_REGA:   # NEXT-3 arrays are replicated like allocations
-                    e = events[k]
-                    rs = [sc.chk.register_array(int(e["dst"]), int(e["width"]), int(e["height"]), int(e["dst_x"]),
-                                                int(e["dst_y"]), int(e["dst_pitch"]), int(e["seq"]))
-                          for sc in group.ranks]
-                    status[k] = rs[0]
+                    status[k] = group.all(lambda c: c.register_array(int(e["dst"]), int(e["width"]), int(e["height"]),
+                                                                     int(e["dst_x"]), int(e["dst_y"]),
+                                                                     int(e["dst_pitch"]), int(e["seq"])))[0]
                 elif ops[k] == OP_FREEA:
-                    rs = [sc.chk.free_array(int(events["dst"][k]), int(events["seq"][k])) for sc in group.ranks]
-                    status[k] = rs[0]
+                    status[k] = group.all(lambda c: c.free_array(int(e["dst"]), int(e["seq"])))[0]
             idx = np.flatnonzero(is_copy[i:j]) + i
             if len(idx):
                 descs = events_to_descs(events[idx])
                 cuts = [0] + [int(c) for c in plan_batches(descs)]
                 for a, b in zip(cuts[:-1], cuts[1:]):
-                    plan = BatchPlan(descs[a:b], group.host_base, group.host_size, group.world)
-                    v = group.run(plan, fuse=fuse)
-                    verdicts[copy_rank[idx[a:b]]] = v
-                    status[idx[a:b]] = v["status"]
+                    if b <= a:
+                        continue
+                    batch = group.batch(descs[a:b])
+                    group.check(batch)
+                    if group.is_root:
+                        v = group.dense(batch)
+                        verdicts[copy_rank[idx[a:b]]] = v
+                        status[idx[a:b]] = v["status"]
             i = j
-    import torch
-    torch.cuda.synchronize()
+    group.torch.cuda.synchronize(group.device)
     return verdicts, status

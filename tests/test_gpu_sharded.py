@@ -23,19 +23,24 @@ def cg():
 
 
 def run_sharded(cg, tr, world, fuse=True, **kw):
-    from paper_1310_0901_b200.sharded import LoopbackGroup, replay_sharded
+    """G shards of one window in this process (the library's loopback
+    cg_comm): per-rank lists from cg_shard_lists, cg_check_sharded (check,
+    straddler exchange, gather, root merge kernel into the dense array)"""
+    from paper_1310_0901_b200.sharded import ShardGroup, replay_sharded
     o, ov, os_, oleaks = oracle.replay_trace(tr)
     nreg = max(int(np.count_nonzero(tr.events["op"] == tg.OP_REG)), 1024)
-    grp = LoopbackGroup(tr.host_base, tr.host_size, world, max_descs=max(tr.n_copies, 1024), max_allocs=nreg, **kw)
+    n = max(tr.n_copies, 1024)
+    grp = ShardGroup(tr.host_base, tr.host_size, world, backend="loopback", max_descs=n, max_allocs=nreg,
+                     max_straddlers=n, cap=n, **kw)
     gv, gs = replay_sharded(grp, tr.events, tr.blob, fuse=fuse)
     for f in ov.dtype.names:
         bad = np.flatnonzero(gv[f] != ov[f])
         assert len(bad) == 0, (world, f, bad[:5], gv[f][bad[:5]], ov[f][bad[:5]])
     assert np.array_equal(gs, os_), np.flatnonzero(gs != os_)[:10]
-    for sc in grp.ranks:
-        l = sc.chk.leak_report()
+    for c in grp.chks:
+        l = c.leak_report()
         assert np.array_equal(l["base"], oleaks["base"]) and np.array_equal(l["size"], oleaks["size"])
-    shards = [sc.chk.shadow() for sc in grp.ranks]
+    shards = [c.shadow() for c in grp.chks]
     A = np.concatenate([s[0] for s in shards])
     V = np.concatenate([s[1] for s in shards])
     assert np.array_equal(A, o.A) and np.array_equal(V, o.V)
@@ -80,26 +85,47 @@ def test_c5_scaled_sharded(cg, world):
 
 
 def test_nccl_path_single_rank(cg):
-    """The torch.distributed (NCCL) driver end to end on a 1-rank process
-    group: check, (empty) straddler exchange, dirty-verdict gather, assembly."""
+    """The library's NCCL backend end to end on a 1-rank process group (the
+    NCCL id handed over with torch.distributed): check, (empty) straddler
+    exchange, gather, root merge -- equal to the oracle and to the loopback
+    backend with one shard."""
     import os
     import torch
     import torch.distributed as dist
-    from paper_1310_0901_b200.replay import events_to_descs
-    from paper_1310_0901_b200.sharded import BatchPlan, ShardedChecker, run_distributed
+    from paper_1310_0901_b200.sharded import ShardGroup, replay_sharded
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29531")
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
         tr = tg.c2_small(n_copies=20000, n_allocs=2000)
         o, ov, _, _ = oracle.replay_trace(tr)
-        sc = ShardedChecker(tr.host_base, tr.host_size, 0, 1, max_descs=20000, max_allocs=4096)
-        ev = tr.events
-        cg.replay_events(sc.chk, ev[ev["op"] != tg.OP_COPY], tr.blob)
-        descs = events_to_descs(ev[ev["op"] == tg.OP_COPY])
-        v = run_distributed(sc, BatchPlan(descs, tr.host_base, tr.host_size, 1))
+        grp = ShardGroup(tr.host_base, tr.host_size, 1, backend="nccl", rank=0, max_descs=20000, max_allocs=4096,
+                         max_straddlers=1024, cap=20000)
+        v, _ = replay_sharded(grp, tr.events, tr.blob)
         for f in ov.dtype.names:
             assert np.array_equal(v[f], ov[f]), f
-        sc.close()
+        grp.close()
+        v1 = run_sharded(cg, tr, 1)
+        assert np.array_equal(v1, v)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_cap_overflow_reported(cg, world):
+    """a cap smaller than a rank's dirty count: the root's list is marked
+    incomplete (cg_comm_overflow), the ranks' own verdicts stay exact"""
+    from paper_1310_0901_b200.sharded import ShardGroup
+    tr = tg.c2_small(n_copies=20000, n_allocs=2000, inject_frac=0.05)
+    grp = ShardGroup(tr.host_base, tr.host_size, world, backend="loopback", max_descs=20000, max_allocs=4096,
+                     max_straddlers=1024, cap=8)
+    ev = tr.events
+    for c in grp.chks:
+        cg.replay_events(c, ev[ev["op"] != tg.OP_COPY], tr.blob)
+    b = grp.batch(tg.events_to_descs(ev[ev["op"] == tg.OP_COPY]))
+    grp.check(b)
+    import torch
+    torch.cuda.synchronize()
+    assert grp.overflow()
+    assert not grp.overflow()          # the query resets it
+    grp.close()

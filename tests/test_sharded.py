@@ -1,7 +1,12 @@
-"""Multi-GPU host logic on CPU: the shard plan against brute force, and the
-N>1 communication path (three all-reduces with the u64->i64 order map, the
-padded all_gather of compacted verdicts, root assembly) on world_size-2 gloo
-process groups with 127.0.0.1 rendezvous."""
+"""Multi-GPU host logic on CPU: the shard plan against brute force, the
+per-rank lists of cg_shard_lists (a partition: every descriptor owned by one
+rank or a straddler everywhere, same straddler order on every rank, mode and
+apply-after bits), and the N>1 host path on world_size-2 gloo process groups
+with 127.0.0.1 rendezvous: every rank plans its own list independently, the
+NCCL unique id travels from rank 0 over torch.distributed as ShardGroup hands
+it over, and the lists the ranks built agree with each other.  The
+collectives themselves run inside the library (cg_check_sharded, NCCL) and
+are covered on the GPU (loopback backend, 1-rank NCCL)."""
 import os
 import socket
 
@@ -54,25 +59,36 @@ def test_shard_plan_brute_force(cg, world):
             assert (first[i], last[i]) == (min(shards), max(shards))
 
 
-def test_batch_plan_partition(cg):
-    from paper_1310_0901_b200.replay import events_to_descs
-    from paper_1310_0901_b200.sharded import BatchPlan
-    tr = tg.c4_pitched(n_copies=3000, n_bufs=4, rows=128)
-    descs = events_to_descs(tr.events[tr.events["op"] == tg.OP_COPY])
-    plan = BatchPlan(descs, tr.host_base, tr.host_size, 4)
-    # every descriptor is owned by exactly one rank or is a straddler on all
-    seen = np.zeros(len(descs), int)
-    for r in range(4):
-        d, idx, n_mine, m = plan.local(r)
-        assert m == len(plan.strad_idx)
-        seen[idx[:n_mine]] += 1
-        assert np.all(d["reserved"][:n_mine] == 0)
-        assert np.all(d["reserved"][n_mine:] & cg.CG_SHARD_RAW)
-        own = plan.owner[plan.strad_idx] == r
-        assert np.array_equal((d["reserved"][n_mine:] & cg.CG_SHARD_NOT_OWNER) == 0, own)
-    seen[plan.strad_idx] += 1
-    assert np.all(seen == 1)
-    assert len(plan.strad_idx) > 0
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_shard_lists_partition(cg, world):
+    from paper_1310_0901_b200.sharded import shard_lists
+    for tr in (tg.c4_pitched(n_copies=3000, n_bufs=4, rows=128), tg.random_tiny(77 + world),
+               tg.random_medium(3, n_copies=60)):
+        descs = tg.events_to_descs(tr.events[tr.events["op"] == tg.OP_COPY])
+        owner, first, last = cg.shard_plan(descs, tr.host_base, tr.host_size, world)
+        strad = np.flatnonzero(first < last)
+        seen = np.zeros(len(descs), int)
+        for r in range(world):
+            d, gidx, n_own, m = shard_lists(descs, tr.host_base, tr.host_size, world, r)
+            assert m == len(strad) and np.array_equal(gidx[n_own:], strad)
+            mine = gidx[:n_own].astype(np.int64)
+            assert np.all(owner[mine] == r) and np.all(first[mine] == last[mine])
+            seen[mine] += 1
+            raw = d["reserved"][n_own:]
+            assert np.all(raw & cg.CG_SHARD_RAW)
+            assert np.array_equal((raw & cg.CG_SHARD_NOT_OWNER) == 0, owner[strad] == r)
+            assert np.all((d["reserved"][:n_own] & (cg.CG_SHARD_RAW | cg.CG_SHARD_NOT_OWNER)) == 0)
+            # CG_APPLY_AFTER exactly as cg_plan_apply_after sets it on the owned part of the list
+            own = np.ascontiguousarray(d[:n_own]).copy()
+            own["reserved"] = 0
+            plain = np.ascontiguousarray(d).copy()
+            plain["reserved"] &= ~np.uint32(cg.CG_APPLY_AFTER)
+            cg.plan_apply_after(plain)
+            assert np.array_equal(plain["reserved"][:n_own], d["reserved"][:n_own])
+            for f in ("kind", "seq", "width", "height", "dst", "src", "dst_pitch", "src_pitch"):
+                assert np.array_equal(d[f], descs[f][gidx.astype(np.int64)])
+        seen[strad] += 1
+        assert np.all(seen == 1)
 
 
 def _free_port():
@@ -89,106 +105,44 @@ def _worker(rank, world, port, q):
     sys.path.insert(0, ROOT)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_1310_0901_b200 import VERDICT_DTYPE, CG_NONE
-        from paper_1310_0901_b200.sharded import TorchComm, _u64_min_fix
-        comm = TorchComm()
-        m = 5
-        rng = np.random.default_rng(rank)
-        # raw partials: first offsets (u64, NONE = 2^64-1), sums, flags
-        firsts = rng.integers(0, 1 << 62, 2 * m).astype(np.uint64)
-        firsts[rank::2] = np.uint64(CG_NONE)
-        firsts[0] = np.uint64((1 << 63) + rank)        # above 2^63: needs the order map
-        mins = torch.from_numpy(firsts.view(np.int64).copy())
-        sums = torch.from_numpy(rng.integers(0, 1000, 5 * m).astype(np.int64))
-        # validation flags are common to all shards; device flags come from the owner (rank 0)
-        common = np.array([64, 64, 0, 2, 4], np.int32)
-        dev = np.array([1, 0, 0, 1, 1], np.int32) if rank == 0 else 0
-        maxs = torch.from_numpy(common | dev)
-        all_f = [None] * world
-        mins = _u64_min_fix(mins)
-        comm.allreduce3(mins, sums, maxs)
-        mins = _u64_min_fix(mins)
-        # compacted verdict gather
-        n_dirty = rank + 1
-        dirty = np.zeros(n_dirty, VERDICT_DTYPE)
-        dirty["flags"] = rank + 1
-        dirty["first_unaddr"] = np.arange(n_dirty) + 10 * rank
-        idx = torch.arange(n_dirty, dtype=torch.int64) * 2 + rank
-        cnt = torch.tensor([n_dirty], dtype=torch.int32)
-        g = comm.gather_dirty(cnt, idx, torch.from_numpy(dirty.view(np.uint8).copy()))
-        q.put((rank, mins.numpy().view(np.uint64).tolist(), sums.tolist(), maxs.tolist(),
-               [(c, i[:c].tolist(), d[:c]["first_unaddr"].tolist(), d[:c]["flags"].tolist()) for c, i, d in g],
-               firsts.tolist(), rng.bit_generator.state is not None))
+        import tracegen as tgw
+        from paper_1310_0901_b200.sharded import shard_lists
+        tr = tgw.c5_sharded(scale=0.002, shards=world)
+        descs = tgw.events_to_descs(tr.events[tr.events["op"] == tgw.OP_COPY])
+        d, gidx, n_own, m = shard_lists(descs, tr.host_base, tr.host_size, world, rank)
+        # the id hand-over ShardGroup does for the NCCL backend (rank 0's bytes to all)
+        nid = torch.arange(128, dtype=torch.uint8) if rank == 0 else torch.zeros(128, dtype=torch.uint8)
+        dist.broadcast(nid, 0)
+        # every rank's view of the straddlers, gathered for comparison
+        sg = torch.from_numpy(gidx[n_own:].astype(np.int64))
+        lens = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(lens, torch.tensor([len(sg)]))
+        outs = [torch.zeros(int(l.item()), dtype=torch.int64) for l in lens]
+        dist.all_gather(outs, sg)
+        q.put((rank, nid.tolist(), n_own, m, [o.tolist() for o in outs], gidx[:n_own].tolist(), len(descs)))
     finally:
         dist.destroy_process_group()
 
 
-def test_gloo_world2_exchange():
+def test_gloo_world2_host_path():
     world, port = 2, _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in ps:
         p.start()
-    res = dict()
+    res = {}
     for _ in range(world):
-        r = q.get(timeout=180)
+        r = q.get(timeout=300)
         res[r[0]] = r
     for p in ps:
         p.join(timeout=60)
         assert p.exitcode == 0
-    # recompute the expected merge from the inputs each rank reported
-    f0, f1 = np.array(res[0][5], np.uint64), np.array(res[1][5], np.uint64)
-    exp_min = np.minimum(f0, f1)
     for r in range(world):
-        assert np.array_equal(np.array(res[r][1], np.uint64), exp_min)
-        assert res[r][3] == [65, 64, 0, 3, 5]          # MAX == OR for common | owner-only flags
-        gathered = res[r][4]
-        assert [g[0] for g in gathered] == [1, 2]
-        assert gathered[1][1] == [1, 3] and gathered[1][3] == [2, 2]
-    assert res[0][2] == res[1][2]
-
-
-def _packed_worker(rank, world, port, q):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    import sys
-    sys.path.insert(0, ROOT)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    try:
-        from paper_1310_0901_b200 import VERDICT_DTYPE
-        from paper_1310_0901_b200.sharded import PackedDirtyGather
-        g = PackedDirtyGather(dist, 5, torch.device("cpu"))
-        c = 2 + rank
-        # what cg_compact_dirty would write into the send buffer
-        g.send[:4] = torch.from_numpy(np.array([c], np.int32).view(np.uint8))
-        idx = np.arange(c, dtype=np.int64) * 3 + rank
-        g.send[16:16 + 8 * c] = torch.from_numpy(idx.view(np.uint8))
-        dv = np.zeros(c, VERDICT_DTYPE)
-        dv["flags"] = 100 + rank
-        dv["first_unaddr"] = idx * 7
-        off = 16 + 8 * g.mx
-        g.send[off:off + 64 * c] = torch.from_numpy(dv.view(np.uint8))
-        g.gather()
-        q.put((rank, [(cc, i.tolist(), d["flags"].tolist(), d["first_unaddr"].tolist()) for cc, i, d in g.unpack()]))
-    finally:
-        dist.destroy_process_group()
-
-
-def test_gloo_world2_packed_gather():
-    """the bench's one-collective exchange of compacted verdicts on world_size 2"""
-    world, port = 2, _free_port()
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    ps = [ctx.Process(target=_packed_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in ps:
-        p.start()
-    res = dict(q.get(timeout=180) for _ in range(world))
-    for p in ps:
-        p.join(timeout=60)
-        assert p.exitcode == 0
-    for r in range(world):
-        for src in range(world):
-            c, idx, flags, fu = res[r][src]
-            assert c == 2 + src
-            assert idx == [3 * k + src for k in range(c)]
-            assert flags == [100 + src] * c and fu == [7 * x for x in idx]
+        assert res[r][1] == list(range(128))                      # rank 0's NCCL id reached every rank
+        assert res[r][4][0] == res[r][4][1]                        # same straddlers, same order
+    n = res[0][6]
+    owned = sorted(res[0][5] + res[1][5])
+    strad = res[0][4][0]
+    assert sorted(owned + strad) == list(range(n))               # a partition of the batch
+    assert res[0][3] == res[1][3] == len(strad) and len(strad) > 0
