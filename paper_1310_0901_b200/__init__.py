@@ -167,41 +167,19 @@ EXPORTED = ("cg_workspace_size", "cg_ctx_create", "cg_ctx_destroy", "cg_last_err
             "cg_comm_create_loopback", "cg_comm_destroy", "cg_comm_last_error", "cg_comm_kernel_launches",
             "cg_comm_overflow", "cg_check_sharded", "cg_shard_lists")
 
-# ---- same-name thin wrappers (status codes returned unchanged) -------------
-cg_workspace_size = _lib.cg_workspace_size
-cg_ctx_create = _lib.cg_ctx_create
-cg_ctx_destroy = _lib.cg_ctx_destroy
-cg_last_error = _lib.cg_last_error
-cg_host_mark = _lib.cg_host_mark
-cg_host_mark_batch = _lib.cg_host_mark_batch
-cg_host_set_vbits = _lib.cg_host_set_vbits
-cg_register_alloc = _lib.cg_register_alloc
-cg_free = _lib.cg_free
-cg_registry_compact = _lib.cg_registry_compact
-cg_check_copies = _lib.cg_check_copies
-cg_apply_dtoh = _lib.cg_apply_dtoh
-cg_check_copies_host = _lib.cg_check_copies_host
-cg_check_apply = _lib.cg_check_apply
-cg_straddler_pack = _lib.cg_straddler_pack
-cg_straddler_finalize = _lib.cg_straddler_finalize
-cg_compact_dirty = _lib.cg_compact_dirty
-cg_host_query_addressable = _lib.cg_host_query_addressable
-cg_expand_copy1d = _lib.cg_expand_copy1d
-cg_check_host = _lib.cg_check_host
-cg_check_host_submit = _lib.cg_check_host_submit
-cg_check_host_wait = _lib.cg_check_host_wait
-cg_format_verdict = _lib.cg_format_verdict
-cg_format_leak = _lib.cg_format_leak
-cg_apply_copies = _lib.cg_apply_copies
-cg_device_vbits = _lib.cg_device_vbits
-cg_array_vbits = _lib.cg_array_vbits
-cg_plan_batches_propagate = _lib.cg_plan_batches_propagate
-cg_array_bytes = _lib.cg_array_bytes
-cg_host_shadow_read = _lib.cg_host_shadow_read
-cg_apply_copies_subset = _lib.cg_apply_copies_subset
-cg_plan_waves = _lib.cg_plan_waves
-cg_apply_flush = _lib.cg_apply_flush
-cg_apply_copies_waves = _lib.cg_apply_copies_waves
+# ---- same-name thin wrappers of every exported function (status codes returned unchanged) ----
+globals().update({_n: getattr(_lib, _n) for _n in EXPORTED})
+
+# ---- constants of include/cg.h and the numpy views of its records ----
+CG_SHADOW_BYTES, CG_SHADOW_2BIT, CG_SHADOW_SPARSE = 0, 1, 2
+CG_FMT_2D, CG_FMT_1D = 0, 1
+COPY1D_DTYPE = np.dtype([("kind", "<u4"), ("reserved", "<u4"), ("seq", "<u8"), ("dst", "<u8"), ("src", "<u8"),
+                         ("bytes", "<u8")])
+CG_SHARD_NOT_OWNER, CG_SHARD_RAW, CG_APPLY_AFTER = 1, 2, 4
+CG_COMM_NCCL, CG_COMM_LOOPBACK = 0, 1
+CG_NCCL_ID_BYTES = 128
+STAGES = ("check_prep", "check_plan", "check_scan", "check_finalize", "apply_prep", "apply_plan", "apply",
+          "leak_sweep")
 
 
 class Waves:
@@ -219,8 +197,6 @@ class Waves:
                                    if self.start[w + 1] > self.start[w] else 0 for w in range(nl)], np.uint64)
         self.index = torch.from_numpy(order.astype(np.int32)).to(torch.device("cuda", device))
         self.n_waves = nl
-cg_summarize = _lib.cg_summarize
-cg_format_summary = _lib.cg_format_summary
 
 
 def summarize(d_verdicts, undef_is_error: bool = False, stream=None):
@@ -240,17 +216,6 @@ def format_summary(errors: int, warnings: int, suppressed: int = 0) -> str:
     buf = ctypes.create_string_buffer(k + 1)
     _lib.cg_format_summary(errors, warnings, suppressed, buf, k + 1)
     return buf.value.decode()
-CG_SHADOW_BYTES, CG_SHADOW_2BIT, CG_SHADOW_SPARSE = 0, 1, 2
-cg_register_array = _lib.cg_register_array
-cg_free_array = _lib.cg_free_array
-cg_array_report = _lib.cg_array_report
-cg_conc_create = _lib.cg_conc_create
-cg_conc_destroy = _lib.cg_conc_destroy
-cg_conc_last_error = _lib.cg_conc_last_error
-cg_conc_sync = _lib.cg_conc_sync
-cg_conc_check = _lib.cg_conc_check
-cg_conc_stamps = _lib.cg_conc_stamps
-cg_conc_kernel_launches = _lib.cg_conc_kernel_launches
 
 
 def format_verdict(v, kind: int) -> str:
@@ -267,22 +232,6 @@ def format_leak(rec) -> str:
     buf = ctypes.create_string_buffer(128)
     _lib.cg_format_leak(a.ctypes.data, buf, 128)
     return buf.value.decode()
-CG_FMT_2D, CG_FMT_1D = 0, 1
-COPY1D_DTYPE = np.dtype([("kind", "<u4"), ("reserved", "<u4"), ("seq", "<u8"), ("dst", "<u8"), ("src", "<u8"),
-                         ("bytes", "<u8")])
-cg_shard_plan = _lib.cg_shard_plan
-CG_SHARD_NOT_OWNER, CG_SHARD_RAW, CG_APPLY_AFTER = 1, 2, 4
-CG_COMM_NCCL, CG_COMM_LOOPBACK = 0, 1
-CG_NCCL_ID_BYTES = 128
-cg_batch_disjoint = _lib.cg_batch_disjoint
-cg_leak_sweep = _lib.cg_leak_sweep
-cg_leak_report = _lib.cg_leak_report
-cg_plan_batches = _lib.cg_plan_batches
-cg_kernel_launches = _lib.cg_kernel_launches
-cg_profile_begin = _lib.cg_profile_begin
-cg_profile_end = _lib.cg_profile_end
-STAGES = ("check_prep", "check_plan", "check_scan", "check_finalize", "apply_prep", "apply_plan", "apply",
-          "leak_sweep")
 
 
 def plan_batches(descs: np.ndarray, propagate: bool = False) -> np.ndarray:
