@@ -405,9 +405,11 @@ cg_status cg_apply_dtoh(cg_ctx *ctx, const cg_copy_desc *d_descs, const cg_verdi
  * the same descriptor array (it uses the device V offsets that check found);
  * the batch must be hazard-free for propagation (cg_plan_batches with
  * CG_PLAN_PROPAGATE).  With tracking it synchronises on stream at the end.
+ * A self-overlapping 2D DtoD with unequal pitches is staged through an 8 MiB
+ * area; a larger one is staged, after the rest of the batch, through a device
+ * buffer of its own size the call allocates and frees (cudaMallocAsync).
  * Errors: as cg_apply_dtoh; CG_ERR_INVALID_VALUE if the preceding check was of
- * other descriptors, or a self-overlapping 2D DtoD with unequal pitches moves
- * more bytes than the 8 MiB staging area (its V-bits are then not moved). */
+ * other descriptors; CG_ERR_OUT_OF_MEMORY if that staging buffer cannot be had. */
 cg_status cg_apply_copies(cg_ctx *ctx, const cg_copy_desc *d_descs, const cg_verdict *d_verdicts, uint64_t n,
                           void *stream);
 
@@ -419,14 +421,17 @@ cg_status cg_apply_copies(cg_ctx *ctx, const cg_copy_desc *d_descs, const cg_ver
  * width*height among the m copies if the caller knows it (waves of copies up
  * to 1 MiB then run one warp per copy without a plan), else 0.
  * Asynchronous on stream: a
- * self-overlapping 2D DtoD that does not fit the staging area is reported by
- * the next cg_apply_flush.  Errors: CG_ERR_INVALID_VALUE (null, m > n, not
+ * self-overlapping 2D DtoD that does not fit the staging area is moved by the
+ * next cg_apply_flush.  Errors: CG_ERR_INVALID_VALUE (null, m > n, not
  * the checked descriptors), CG_ERR_NOT_INITIALIZED without tracking, CG_ERR_CUDA. */
 cg_status cg_apply_copies_subset(cg_ctx *ctx, const cg_copy_desc *d_descs, const cg_verdict *d_verdicts, uint64_t n,
                                  const uint32_t *d_index, uint64_t m, uint64_t max_bytes, void *stream);
 
-/* Synchronises stream and reports (then clears) a staging overflow of the
- * cg_apply_copies_subset calls since the last flush (CG_ERR_INVALID_VALUE). */
+/* Synchronises stream and moves the V-bits of the self-overlapping 2D DtoDs
+ * the cg_apply_copies_subset calls since the last flush could not stage (more
+ * than 8 MiB), each through a device buffer of its size; call it between a
+ * wave holding such a copy and a later wave that depends on it
+ * (cg_apply_copies_waves does).  Errors: CG_ERR_OUT_OF_MEMORY, CG_ERR_CUDA. */
 cg_status cg_apply_flush(cg_ctx *ctx, void *stream);
 
 /* All waves of a batch in one call: wave w is d_index[h_wave_start[w] ..

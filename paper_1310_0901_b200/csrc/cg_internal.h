@@ -156,6 +156,9 @@ cudaError_t propagate_waves(const Launch& L, const cg_copy_desc* d, const cg_ver
                             uint64_t m, const uint32_t* d_wstart, uint32_t n_waves, const ShadowView& sv,
                             uint8_t* pool, const Plan& p, uint8_t* scratch, uint32_t* overflow, cudaStream_t s);
 size_t scan_meta_bytes();
+cudaError_t memmove_list(const Launch& L, const cg_copy_desc* d, const uint64_t* dvoff, const uint32_t* list,
+                         const uint32_t* count, uint8_t* pool, uint8_t* scratch, uint64_t stage_cap,
+                         uint32_t* overflow, cudaStream_t s);
 
 cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out,
                          const Table& t, const ShadowView& sv, const Plan& p, uint32_t err_mask, bool fuse,

@@ -2604,10 +2604,13 @@ __global__ void __launch_bounds__(kThreads) k_prop_direct(const cg_copy_desc* __
 
 // one self-overlapping DtoD with the whole CTA: equal pitches shift every byte
 // by the same delta, so a directional block copy is exact memmove; unequal
-// pitches stage all logical bytes first (scratch of kStageBytes), else set
-// *overflow
-__device__ __forceinline__ void block_memmove(const cg_copy_desc& d, uint64_t so, uint64_t dso, uint8_t* pool,
-                                              uint8_t* scratch, uint32_t* overflow) {
+// pitches stage all logical bytes first (scratch of stage_cap bytes); one
+// that does not fit moves nothing here: it is flagged (*overflow) and listed
+// (overflow[1] entries after overflow[2..]: the descriptor index) for the
+// host's recovery pass, which stages it through a scratch of its size
+__device__ __forceinline__ void block_memmove(const cg_copy_desc& d, uint32_t i, uint64_t so, uint64_t dso,
+                                              uint8_t* pool, uint8_t* scratch, uint32_t* overflow,
+                                              uint64_t stage_cap = kStageBytes) {
   const uint64_t W = d.width, H = d.height;
   if (d.src_pitch == d.dst_pitch || H == 1) {
     // chunks of 16 bytes per thread, each read completely before it is
@@ -2645,7 +2648,7 @@ __device__ __forceinline__ void block_memmove(const cg_copy_desc& d, uint64_t so
         __syncthreads();
       }
     }
-  } else if (W * H <= kStageBytes) {
+  } else if (W * H <= stage_cap) {
     for (uint64_t o = threadIdx.x; o < W * H; o += blockDim.x)
       scratch[o] = __ldcg(pool + so + (o / W) * d.src_pitch + o % W);
     __syncthreads();
@@ -2654,6 +2657,7 @@ __device__ __forceinline__ void block_memmove(const cg_copy_desc& d, uint64_t so
     __syncthreads();
   } else if (threadIdx.x == 0) {
     atomicOr(overflow, 1u);
+    overflow[2 + atomicAdd(overflow + 1, 1u)] = i;
   }
 }
 
@@ -2663,7 +2667,7 @@ __global__ void __launch_bounds__(kThreads) k_memmove(const cg_copy_desc* __rest
                                                       const uint64_t* __restrict__ dvoff,
                                                       const uint32_t* __restrict__ mm,
                                                       const uint32_t* __restrict__ mm_count, uint8_t* pool,
-                                                      uint8_t* scratch, uint32_t* overflow) {
+                                                      uint8_t* scratch, uint32_t* overflow, uint64_t stage_cap) {
   pdl_entry();
   const uint32_t cnt = *mm_count;
   for (uint32_t k = 0; k < cnt; ++k) {
@@ -2671,7 +2675,7 @@ __global__ void __launch_bounds__(kThreads) k_memmove(const cg_copy_desc* __rest
     const cg_copy_desc d = descs[i];
     const bool shared = d.src_pitch != d.dst_pitch && d.height > 1;
     if (shared ? blockIdx.x != 0 : k % gridDim.x != blockIdx.x) continue;
-    block_memmove(d, dvoff[2 * i + 1], dvoff[2 * i], pool, scratch, overflow);
+    block_memmove(d, i, dvoff[2 * i + 1], dvoff[2 * i], pool, scratch, overflow, stage_cap);
   }
 }
 
@@ -3022,7 +3026,7 @@ __global__ void __launch_bounds__(kWRing * 32) k_prop_waves(const cg_copy_desc* 
         const cg_copy_desc d = descs[i];
         const bool shared = d.src_pitch != d.dst_pitch && d.height > 1;
         if (shared ? blockIdx.x != 0 : k % gridDim.x != blockIdx.x) continue;
-        block_memmove(d, __ldg(dvoff + 2 * i + 1), __ldg(dvoff + 2 * i), pool, scratch, overflow);
+        block_memmove(d, i, __ldg(dvoff + 2 * i + 1), __ldg(dvoff + 2 * i), pool, scratch, overflow);
       }
     }
     if (w + 1 < n_waves) {
@@ -3586,7 +3590,7 @@ cudaError_t propagate(const Launch& L, const cg_copy_desc* d, const cg_verdict* 
   cudaMemsetAsync(p.counter, 0, sizeof(uint32_t), s);
   launch_pdl(k_propagate, L.persist_blocks, kThreads, 0, s, pm, n, p.P, p.chunk_first, p.counter, p.t_min, p.max_chunks,
                                                     sv.V, pool, cnt);
-  launch_pdl(k_memmove, 64, kThreads, 0, s, d, p.dvoff, p.resid, mm_count, pool, scratch, overflow);
+  launch_pdl(k_memmove, 64, kThreads, 0, s, d, p.dvoff, p.resid, mm_count, pool, scratch, overflow, kStageBytes);
   L.stage(CG_STAGE_APPLY, false, s);
   *L.counter += 3;
   return cudaGetLastError();
@@ -3607,7 +3611,7 @@ cudaError_t propagate_direct(const Launch& L, const cg_copy_desc* d, const cg_ve
     launch_pdl(k_prop_direct, dim3((unsigned)m, (unsigned)slices), kThreads, 0, s, d, v, index, m, p.dvoff, sv.sb, sv.V, pool,
                                                                           p.resid, mm_count);
   }
-  launch_pdl(k_memmove, 64, kThreads, 0, s, d, p.dvoff, p.resid, mm_count, pool, scratch, overflow);
+  launch_pdl(k_memmove, 64, kThreads, 0, s, d, p.dvoff, p.resid, mm_count, pool, scratch, overflow, kStageBytes);
   L.stage(CG_STAGE_APPLY, false, s);
   *L.counter += 2;
   return cudaGetLastError();
@@ -3653,6 +3657,17 @@ cudaError_t propagate_waves(const Launch& L, const cg_copy_desc* d, const cg_ver
   L.stage(CG_STAGE_APPLY, false, s);
   *L.counter += 5;
   if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+// the recovery pass of the self-overlapping 2D DtoDs the staging area could
+// not hold (block_memmove's overflow list): staged through `scratch` of
+// stage_cap bytes, after the rest of their batch / wave
+cudaError_t memmove_list(const Launch& L, const cg_copy_desc* d, const uint64_t* dvoff, const uint32_t* list,
+                         const uint32_t* count, uint8_t* pool, uint8_t* scratch, uint64_t stage_cap,
+                         uint32_t* overflow, cudaStream_t s) {
+  launch_pdl(k_memmove, 64, kThreads, 0, s, d, dvoff, list, count, pool, scratch, overflow, stage_cap);
+  *L.counter += 1;
   return cudaGetLastError();
 }
 

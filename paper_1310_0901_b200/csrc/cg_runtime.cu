@@ -40,7 +40,8 @@ struct ArrayEntry {   // NEXT-3 device array (SPEC register_array S:166-168)
 };
 
 struct Layout {
-  uint64_t table, walk, arrays, weight, P, bsum, fbsum, chunk, meta, resid, defer, dvoff, scratch, waves, marks, flags, leaks,
+  uint64_t table, walk, arrays, weight, P, bsum, fbsum, chunk, meta, resid, defer, dvoff, scratch, waves, ovl, marks, flags,
+      leaks,
       desc_stage, chunk_list,
       verdict_stage, raw_stage,
       idx_stage, dirty_stage, dir, total;
@@ -96,6 +97,7 @@ Layout layout_of(const cg_config* c) {
   L.dvoff = c->dev_vbuf ? take(c->max_descs * 16) : 0;
   L.scratch = c->dev_vbuf ? take(cgk::stage_bytes()) : 0;
   L.waves = c->dev_vbuf ? take((c->max_descs + 1) * sizeof(uint32_t)) : 0;   // NEXT-1 wave offsets
+  L.ovl = c->dev_vbuf ? take((c->max_descs + 2) * sizeof(uint32_t)) : 0;     // NEXT-1 staging overflow: flag, count, list
   L.marks = take(std::min<uint64_t>(c->max_descs, kMarkRun) * sizeof(cg_mark));
   L.flags = take(256);
   L.leaks = take(c->max_allocs * sizeof(cg_alloc_record));
@@ -472,6 +474,7 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
   e = cudaMemset(c->ws + lay.flags, 0, 256);   // counters, overflow flag
   if (e == cudaSuccess) e = cgk::fresh_shadow(c->launch, c->sv, 0);
   if (e == cudaSuccess && cfg->dev_vbuf) e = cudaMemset(cfg->dev_vbuf, 0xFF, cfg->dev_vsize);
+  if (e == cudaSuccess && cfg->dev_vbuf) e = cudaMemset(c->ws + lay.ovl, 0, 8);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     cg_ctx_destroy(c);
@@ -979,7 +982,7 @@ cg_status cg_apply_copies_subset(cg_ctx* c, const cg_copy_desc* d_descs, const c
     return c->fail(CG_ERR_INVALID_VALUE, "cg_apply_copies must follow the check of the same descriptors");
   DeviceGuard g(c->cfg.device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  uint32_t* overflow = reinterpret_cast<uint32_t*>(c->ws + c->lay.flags + 224);
+  uint32_t* overflow = reinterpret_cast<uint32_t*>(c->ws + c->lay.ovl);
   // asynchronous: a staging overflow stays flagged until cg_apply_flush.  Waves
   // of copies up to kDirectMax bytes take the plan-free warp-per-copy kernel.
   constexpr uint64_t kDirectMax = 1ull << 20;
@@ -1000,7 +1003,9 @@ cg_status cg_apply_copies_waves(cg_ctx* c, const cg_copy_desc* d_descs, const cg
   for (uint32_t w = 0; w < n_waves; ++w)
     if (h_wave_start[w + 1] < h_wave_start[w] || h_wave_start[w + 1] > n)
       return c->fail(CG_ERR_INVALID_VALUE, "wave offsets not increasing or beyond n");
-  if (c->wave_kernel && n_waves && c->cfg.dev_vbuf) {   // every wave in one cooperative launch
+  bool big = false;   // a wave that may hold a self-overlapping copy beyond the staging area: recovered per wave
+  for (uint32_t w = 0; w < n_waves; ++w) big = big || h_max_bytes[w] > cgk::stage_bytes();
+  if (c->wave_kernel && n_waves && c->cfg.dev_vbuf && !big) {   // every wave in one cooperative launch
     if (!d_descs || !d_verdicts || !d_index) return c->fail(CG_ERR_INVALID_VALUE, "null descriptor, verdict or index array");
     if (d_descs != c->last_check || n != c->last_check_n)
       return c->fail(CG_ERR_INVALID_VALUE, "cg_apply_copies must follow the check of the same descriptors");
@@ -1016,32 +1021,63 @@ cg_status cg_apply_copies_waves(cg_ctx* c, const cg_copy_desc* d_descs, const cg
       if (e == cudaSuccess)
         e = cgk::propagate_waves(c->launch, d_descs, d_verdicts, d_index + a, m, dw, n_waves, c->sv,
                                  static_cast<uint8_t*>(c->cfg.dev_vbuf), c->plan(), c->ws + c->lay.scratch,
-                                 reinterpret_cast<uint32_t*>(c->ws + c->lay.flags + 224), s);
+                                 reinterpret_cast<uint32_t*>(c->ws + c->lay.ovl), s);
       if (e != cudaSuccess) return c->cuda(e, "propagate waves");
     }
     return cg_apply_flush(c, stream);
   }
   for (uint32_t w = 0; w < n_waves; ++w) {   // in level order, all launches from this loop
-    const cg_status st = cg_apply_copies_subset(c, d_descs, d_verdicts, n, d_index + h_wave_start[w],
-                                                h_wave_start[w + 1] - h_wave_start[w], h_max_bytes[w], stream);
+    cg_status st = cg_apply_copies_subset(c, d_descs, d_verdicts, n, d_index + h_wave_start[w],
+                                          h_wave_start[w + 1] - h_wave_start[w], h_max_bytes[w], stream);
+    if (st == CG_OK && h_max_bytes[w] > cgk::stage_bytes()) st = cg_apply_flush(c, stream);   // before the next wave
     if (st != CG_OK) return st;
   }
   return cg_apply_flush(c, stream);
+}
+
+// NEXT-1: the self-overlapping 2D DtoDs with unequal pitches that did not fit
+// the 8 MiB staging area were skipped and listed by the kernels; stage each
+// through a scratch of its own size now (their batch / wave is conflict-free,
+// so moving them after the rest of it is the sequential result)
+static cg_status recover_memmoves(cg_ctx* c, const cg_copy_desc* d_descs, cudaStream_t s) {
+  uint32_t* overflow = reinterpret_cast<uint32_t*>(c->ws + c->lay.ovl);
+  uint32_t h[2] = {0, 0};
+  cudaError_t e = cudaMemcpyAsync(h, overflow, sizeof h, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return c->cuda(e, "propagate");
+  if (!h[0]) return CG_OK;
+  std::vector<uint32_t> list(h[1]);
+  e = cudaMemcpy(list.data(), overflow + 2, h[1] * sizeof(uint32_t), cudaMemcpyDeviceToHost);
+  uint64_t need = 0;
+  for (uint32_t i : list) {
+    cg_copy_desc d;
+    if (e == cudaSuccess) e = cudaMemcpy(&d, d_descs + i, sizeof d, cudaMemcpyDeviceToHost);
+    need = std::max(need, d.width * d.height);
+  }
+  uint8_t* scratch = nullptr;
+  if (e == cudaSuccess) e = cudaMallocAsync(&scratch, need, s);
+  if (e != cudaSuccess) return c->fail(CG_ERR_OUT_OF_MEMORY, "staging of a %llu-byte self-overlapping copy: %s",
+                                       (unsigned long long)need, cudaGetErrorString(e));
+  e = cudaMemsetAsync(overflow, 0, 8, s);   // flag and count; the list itself is read by the kernel below
+  uint32_t* d_list = nullptr;
+  if (e == cudaSuccess) e = cudaMallocAsync(&d_list, (h[1] + 1) * sizeof(uint32_t), s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_list + 1, list.data(), h[1] * sizeof(uint32_t), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_list, &h[1], sizeof(uint32_t), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess)
+    e = cgk::memmove_list(c->launch, d_descs, c->plan().dvoff, d_list + 1, d_list, static_cast<uint8_t*>(c->cfg.dev_vbuf),
+                          scratch, need, overflow, s);
+  if (e == cudaSuccess) e = cudaFreeAsync(scratch, s);
+  if (e == cudaSuccess) e = cudaFreeAsync(d_list, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return c->cuda(e, "memmove recovery");
 }
 
 cg_status cg_apply_flush(cg_ctx* c, void* stream) {
   if (!c) return CG_ERR_INVALID_CONTEXT;
   if (!c->cfg.dev_vbuf) return CG_OK;
   DeviceGuard g(c->cfg.device);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  uint32_t* overflow = reinterpret_cast<uint32_t*>(c->ws + c->lay.flags + 224);
-  uint32_t h_over = 0;
-  cudaError_t e = cudaMemcpyAsync(&h_over, overflow, sizeof h_over, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(overflow, 0, sizeof(uint32_t), s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return c->cuda(e, "propagate");
-  if (h_over) return c->fail(CG_ERR_INVALID_VALUE, "self-overlapping 2D DtoD larger than the staging area");
-  return CG_OK;
+  if (!c->last_check) return CG_OK;
+  return recover_memmoves(c, static_cast<const cg_copy_desc*>(c->last_check), static_cast<cudaStream_t>(stream));
 }
 
 cg_status cg_apply_copies(cg_ctx* c, const cg_copy_desc* d_descs, const cg_verdict* d_verdicts, uint64_t n,
@@ -1054,16 +1090,12 @@ cg_status cg_apply_copies(cg_ctx* c, const cg_copy_desc* d_descs, const cg_verdi
     return c->fail(CG_ERR_INVALID_VALUE, "cg_apply_copies must follow the check of the same descriptors");
   DeviceGuard g(c->cfg.device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  uint32_t* overflow = reinterpret_cast<uint32_t*>(c->ws + c->lay.flags + 224);
+  uint32_t* overflow = reinterpret_cast<uint32_t*>(c->ws + c->lay.ovl);
   cudaError_t e = cgk::propagate(c->launch, d_descs, d_verdicts, nullptr, n, c->sv,
                                  static_cast<uint8_t*>(c->cfg.dev_vbuf), c->plan(), c->ws + c->lay.scratch, overflow, s,
-                                 true);
-  uint32_t h_over = 0;
-  if (e == cudaSuccess) e = cudaMemcpyAsync(&h_over, overflow, sizeof h_over, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+                                 false);
   if (e != cudaSuccess) return c->cuda(e, "propagate");
-  if (h_over) return c->fail(CG_ERR_INVALID_VALUE, "self-overlapping 2D DtoD larger than the staging area");
-  return CG_OK;
+  return recover_memmoves(c, d_descs, s);
 }
 
 cg_status cg_device_vbits(cg_ctx* c, uint64_t addr, uint64_t len, uint8_t* h_out) {

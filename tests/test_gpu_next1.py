@@ -158,3 +158,36 @@ def test_deep_chains_tracking(cg, seed):
             tb.copy1d(tg.DTOH, H0 + (1 << 17) + int(rng.integers(0, (1 << 16) - n)),
                       devs[rng.integers(4)] + int(rng.integers(0, (1 << 14) - n)), n)
     run_tracking(cg, tb.build())
+
+
+@pytest.mark.parametrize("shift", [-5000, 3333])
+@pytest.mark.parametrize("wave_kernel", ["0", "1"])
+def test_self_overlapping_2d_beyond_staging(cg, monkeypatch, shift, wave_kernel):
+    """S:84 / S:101 memmove semantics for a 32 MiB self-overlapping 2D DtoD with
+    unequal pitches -- four times the 8 MiB staging area: it is staged through
+    a buffer of its own size after the rest of its wave, and the next wave (a
+    DtoH of the moved bytes) sees the moved V-bits"""
+    monkeypatch.setenv("CG_WAVE_KERNEL", wave_kernel)
+    rng = np.random.default_rng(abs(shift))
+    H0 = 1 << 24
+    W, H = 8192, 4096                       # 32 MiB
+    sp, dp = 8192 + 512, 8192 + 128         # unequal pitches: the rows interleave
+    tb = tg.TraceBuilder("mm32", H0, 64 << 20)
+    d = tb.malloc((H + 2) * sp + (1 << 16))
+    n = (H - 1) * sp + W
+    pat = rng.integers(0, 256, n, dtype=np.uint8)
+    pat[rng.random(n) < 0.6] = 0
+    tb.mark(H0, n, tg.DEFINED)
+    tb.setv(H0, pat.tobytes())
+    s0 = 40000
+    tb.copy1d(tg.HTOD, d + s0, H0, n)
+    tb.copy2d(tg.DTOD, W, H, d + s0 + shift, 0, 0, dp, d + s0, 0, 0, sp)
+    tb.mark(H0 + (40 << 20), W * H, tg.UNDEFINED)
+    tb.copy2d(tg.DTOH, W, H, H0 + (40 << 20), 0, 0, W, d + s0 + shift, 0, 0, dp)
+    tr = tb.build()
+    run_tracking(cg, tr)
+    o = oracle.replay_trace(tr, track_device=True)[0]
+    # the DtoH brought the rows of the moved V-bits back: row r of the result = row r of the source pattern
+    got = o.V[40 << 20:(40 << 20) + W * H].reshape(H, W)
+    exp = np.stack([pat[r * sp:r * sp + W] for r in range(H)])
+    assert np.array_equal(got, exp)
