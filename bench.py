@@ -161,7 +161,18 @@ def workload_name(config: str) -> str:
     return config
 
 
+_TRACES = {}
+
+
 def make_workload(name: str, rank: int = 0, scale: float = 1.0):
+    key = (name, rank, scale)
+    if key not in _TRACES:
+        _TRACES.clear()   # one trace at a time (C5's is 1.1 GB)
+        _TRACES[key] = _make_workload(name, rank, scale)
+    return _TRACES[key]
+
+
+def _make_workload(name: str, rank: int = 0, scale: float = 1.0):
     """Rank r's workload.  Weak scaling: rank r's host buffers live in shard r
     of a global window [2^32, 2^32 + world * 8 GiB); its copies, allocations and
     verdicts are its own."""
@@ -208,20 +219,31 @@ def setup_checker(cg, tr, device: int, host_staging: bool, rank: int = 0, world:
 
 
 def registry_rate(cg, tr, device):
-    """a7 host throughput: registry events per second through the C ABI."""
+    """a7 host throughput: registry events per second through the C ABI, one
+    call per event (cg_register_alloc / cg_free from Python) and in one
+    cg_registry_batch call."""
     ev = tr.events
     regs = ev[(ev["op"] == 3) | (ev["op"] == 4)]
-    chk = cg.Checker(tr.host_base, 1 << 20 if tr.host_size > (1 << 20) else tr.host_size,
-                     max_descs=1024, max_allocs=max(len(regs), 1024), device=device)
-    t0 = time.perf_counter()
-    for e in regs:
-        if e["op"] == 3:
-            chk.register_alloc(int(e["dst"]), int(e["width"]), int(e["seq"]))
+    out = {}
+    for mode in ("per_call", "batch"):
+        chk = cg.Checker(tr.host_base, 1 << 20 if tr.host_size > (1 << 20) else tr.host_size,
+                         max_descs=1024, max_allocs=max(len(regs), 1024), device=device)
+        t0 = time.perf_counter()
+        if mode == "batch":
+            re = np.zeros(len(regs), cg.REG_EVENT_DTYPE)
+            re["op"] = np.where(regs["op"] == 3, cg.CG_REG_ALLOC, cg.CG_REG_FREE)
+            re["seq"], re["addr"], re["size"] = regs["seq"], regs["dst"], regs["width"]
+            chk.registry_batch(re)
         else:
-            chk.free(int(e["dst"]), int(e["seq"]))
-    dt = time.perf_counter() - t0
-    chk.close()
-    return len(regs) / dt if dt > 0 else None
+            for e in regs:
+                if e["op"] == 3:
+                    chk.register_alloc(int(e["dst"]), int(e["width"]), int(e["seq"]))
+                else:
+                    chk.free(int(e["dst"]), int(e["seq"]))
+        dt = time.perf_counter() - t0
+        chk.close()
+        out[mode] = len(regs) / dt if dt > 0 else None
+    return out
 
 
 def run_ours(args, rank, world, device, config=None, steps=None, warmup=None, e2e_on=None, extras=True):
@@ -630,6 +652,94 @@ def run_sharded_bench(args, rank, world, device, backend):
     return res
 
 
+def run_interleaved(args, device):
+    """C5 as a program issues it: the registry events (a7: 1000 bursts of 50
+    frees + 50 allocations, then the final frees) interleaved with the copy
+    checks inside the timed region -- per block: one cg_registry_batch, then
+    the R-20 epochs of the block's copies (cg_check_apply; the registry goes to
+    the device by difference inside the check call).  The host shadow setup
+    and the 100k initial allocations are replayed untimed; a pass mutates the
+    registry, so each pass runs on a fresh context (one warm-up pass, then the
+    timed one)."""
+    import torch
+    import paper_1310_0901_b200 as cg
+    import tracegen as tg
+    tr = make_workload("c5_sharded", 0, args.scale)
+    ev = tr.events
+    ops = ev["op"]
+    first_copy = int(np.flatnonzero(ops == 5)[0])
+    setup, rest = ev[:first_copy], ev[first_copy:]
+    rops = rest["op"]
+    # blocks: [registry run][copies ...] in trace order
+    blocks = []
+    i = 0
+    while i < len(rest):
+        j = i
+        while j < len(rest) and rops[j] in (3, 4):
+            j += 1
+        k = j
+        while k < len(rest) and rops[k] == 5:
+            k += 1
+        regs = rest[i:j]
+        re = np.zeros(len(regs), cg.REG_EVENT_DTYPE)
+        re["op"] = np.where(regs["op"] == 3, cg.CG_REG_ALLOC, cg.CG_REG_FREE)
+        re["seq"], re["addr"], re["size"] = regs["seq"], regs["dst"], regs["width"]
+        descs = tg.events_to_descs(rest[j:k])
+        cuts = [0] + [int(c) for c in cg.plan_batches(descs)] if len(descs) else [0]
+        eps = []
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            part = np.ascontiguousarray(descs[a:b])
+            cg.plan_apply_after(part)
+            descs[a:b] = part
+            eps.append((a, b))
+        blocks.append((re, descs, eps))
+        i = k
+    n = int(np.count_nonzero(rops == 5))
+    nreg_ev = int(np.count_nonzero((rops == 3) | (rops == 4)))
+    nreg = int(np.count_nonzero(ops == 3))
+    stream = torch.cuda.current_stream()
+
+    def one_pass(timed):
+        chk = cg.Checker(tr.host_base, tr.host_size, max_descs=max(max(len(d) for _, d, _ in blocks), 1024),
+                         max_allocs=max(nreg, 1024), device=device)
+        cg.replay_events(chk, setup, tr.blob)
+        dd = [cg.to_device_descs(d, device) if len(d) else None for _, d, _ in blocks]
+        dv = [torch.empty(max(len(d), 1) * 64, dtype=torch.uint8, device=device) for _, d, _ in blocks]
+        dl = torch.empty(max(nreg, 1) * 24, dtype=torch.uint8, device=device)
+        dc = torch.zeros(1, dtype=torch.int64, device=device)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t_reg = 0.0
+        w0 = time.perf_counter()
+        e0.record(stream)
+        for (re, descs, eps), x, y in zip(blocks, dd, dv):
+            if len(re):
+                t = time.perf_counter()
+                st = chk.registry_batch(re)
+                t_reg += time.perf_counter() - t
+                assert st == 0, cg.cg_last_error(chk.ctx)
+            for a, b in eps:
+                chk.check_apply(x[a * 96:b * 96], y[a * 64:b * 64], stream=stream)
+        chk.leak_sweep(dl, nreg, dc, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+        ms = e0.elapsed_time(e1)
+        launches = chk.kernel_launches
+        chk.close()
+        return ms, wall, t_reg, launches
+
+    one_pass(False)
+    ms, wall, t_reg, launches = one_pass(True)
+    return {"ms_per_pass": ms, "wall_s_per_pass": wall, "descriptors": n, "registry_events": nreg_ev,
+            "blocks": len(blocks), "epochs": sum(len(e) for _, _, e in blocks),
+            "registry_events_per_s": nreg_ev / t_reg if t_reg > 0 else None,
+            "registry_host_s": t_reg, "descriptors_per_s": n / (ms * 1e-3),
+            "gpu_launches_per_pass": launches,
+            "entry": "per block: cg_registry_batch, then cg_check_apply per R-20 epoch (table by diff upload); "
+                     "one timed pass on a fresh context after one warm-up pass"}
+
+
 PER_CONFIG = ("c3_single", "c4_pitched", "c5_sharded")
 
 
@@ -654,6 +764,10 @@ def per_config(args, device):
                                                            "algorithmic_bytes_per_step", "entry")}}
         gc.collect()
         torch.cuda.empty_cache()
+        if cfg == "c5_sharded" and not args.no_interleaved:
+            out["c5_interleaved"] = run_interleaved(args, device)
+            gc.collect()
+            torch.cuda.empty_cache()
     return out
 
 
@@ -795,6 +909,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-registry-rate", action="store_true")
     ap.add_argument("--no-per-config", action="store_true", help="skip the C3/C4/C5 per_config runs")
+    ap.add_argument("--no-interleaved", action="store_true", help="skip the interleaved C5 registry pass")
     ap.add_argument("--sharded", action="store_true",
                     help="at N=1: the multi-GPU code path (C5 through cg_check_sharded, NCCL with one rank)")
     ap.add_argument("--loopback", type=int, default=0,

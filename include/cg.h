@@ -297,6 +297,21 @@ cg_status cg_register_alloc(cg_ctx *ctx, uint64_t base, uint64_t size, uint64_t 
  * live base: offset pointer, double free, 0) or non-increasing seq. */
 cg_status cg_free(cg_ctx *ctx, uint64_t ptr, uint64_t seq);
 
+/* A registry event for cg_registry_batch: op CG_REG_ALLOC (cg_register_alloc
+ * of addr, size) or CG_REG_FREE (cg_free of addr).  32 bytes. */
+enum { CG_REG_ALLOC = 1, CG_REG_FREE = 2 };
+typedef struct {
+  uint32_t op, reserved;
+  uint64_t seq, addr, size;
+} cg_reg_event;
+
+/* n registry events applied in order, as n cg_register_alloc / cg_free calls
+ * (one call crossing the ABI instead of n); h_status[i] (if not NULL) gets
+ * event i's status.  The device table follows by difference at the next
+ * check (new entries and changed free stamps only).  Returns CG_OK if every
+ * event succeeded, else the first failing status (the others still apply). */
+cg_status cg_registry_batch(cg_ctx *ctx, const cg_reg_event *h_events, uint64_t n, uint32_t *h_status);
+
 /* Drops tombstones with free_seq <= before_seq (no later descriptor may have
  * seq < before_seq).  Synchronous host operation.  Tombstones count against
  * max_allocs until dropped: a long-running caller compacts at its epoch

@@ -145,6 +145,7 @@ def _load() -> ctypes.CDLL:
         "cg_comm_overflow": (I, [P, P]),
         "cg_check_sharded": (I, [P, P, P, P, P, P, U64, P]),
         "cg_shard_lists": (I, [P, U64, U64, U64, U32, U32, P, P, P, P]),
+        "cg_registry_batch": (I, [P, P, U64, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -165,7 +166,7 @@ EXPORTED = ("cg_workspace_size", "cg_ctx_create", "cg_ctx_destroy", "cg_last_err
             "cg_conc_destroy", "cg_conc_last_error", "cg_conc_sync", "cg_conc_check", "cg_conc_stamps",
             "cg_conc_kernel_launches", "cg_ctx_device", "cg_comm_nccl_id", "cg_comm_create_nccl",
             "cg_comm_create_loopback", "cg_comm_destroy", "cg_comm_last_error", "cg_comm_kernel_launches",
-            "cg_comm_overflow", "cg_check_sharded", "cg_shard_lists")
+            "cg_comm_overflow", "cg_check_sharded", "cg_shard_lists", "cg_registry_batch")
 
 # ---- same-name thin wrappers of every exported function (status codes returned unchanged) ----
 globals().update({_n: getattr(_lib, _n) for _n in EXPORTED})
@@ -178,6 +179,8 @@ COPY1D_DTYPE = np.dtype([("kind", "<u4"), ("reserved", "<u4"), ("seq", "<u8"), (
 CG_SHARD_NOT_OWNER, CG_SHARD_RAW, CG_APPLY_AFTER = 1, 2, 4
 CG_COMM_NCCL, CG_COMM_LOOPBACK = 0, 1
 CG_NCCL_ID_BYTES = 128
+CG_REG_ALLOC, CG_REG_FREE = 1, 2
+REG_EVENT_DTYPE = np.dtype([("op", "<u4"), ("reserved", "<u4"), ("seq", "<u8"), ("addr", "<u8"), ("size", "<u8")])
 STAGES = ("check_prep", "check_plan", "check_scan", "check_finalize", "apply_prep", "apply_plan", "apply",
           "leak_sweep")
 
@@ -422,6 +425,13 @@ class Checker:
     # ---- registry ------------------------------------------------------------
     def register_alloc(self, base: int, size: int, seq: int) -> int:
         return _lib.cg_register_alloc(self.ctx, base, size, seq)
+
+    def registry_batch(self, events: np.ndarray, status_out: Optional[np.ndarray] = None) -> int:
+        """cg_registry_batch over REG_EVENT_DTYPE records"""
+        e = np.ascontiguousarray(events, dtype=REG_EVENT_DTYPE)
+        st = status_out if status_out is not None else None
+        return _lib.cg_registry_batch(self.ctx, e.ctypes.data if len(e) else None, len(e),
+                                      st.ctypes.data if st is not None else None)
 
     def registry_compact(self, before_seq: int) -> int:
         """cg_registry_compact: drop tombstones no descriptor with seq >= before_seq can see"""

@@ -156,6 +156,8 @@ cudaError_t propagate_waves(const Launch& L, const cg_copy_desc* d, const cg_ver
                             uint64_t m, const uint32_t* d_wstart, uint32_t n_waves, const ShadowView& sv,
                             uint8_t* pool, const Plan& p, uint8_t* scratch, uint32_t* overflow, cudaStream_t s);
 size_t scan_meta_bytes();
+cudaError_t table_patch(const Launch& L, uint64_t* fseq, uint64_t* walk, const uint64_t* d_pairs, uint64_t k,
+                        cudaStream_t s);
 cudaError_t memmove_list(const Launch& L, const cg_copy_desc* d, const uint64_t* dvoff, const uint32_t* list,
                          const uint32_t* count, uint8_t* pool, uint8_t* scratch, uint64_t stage_cap,
                          uint32_t* overflow, cudaStream_t s);

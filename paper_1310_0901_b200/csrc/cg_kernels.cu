@@ -3671,6 +3671,25 @@ cudaError_t memmove_list(const Launch& L, const cg_copy_desc* d, const uint64_t*
   return cudaGetLastError();
 }
 
+// the free stamps of a registry diff upload: pairs (position, free seq) ->
+// fseq column and the walk record (prefix max, end, alloc seq, free seq)
+__global__ void k_table_patch(uint64_t* __restrict__ fseq, uint64_t* __restrict__ walk,
+                              const uint64_t* __restrict__ pairs, uint64_t k) {
+  pdl_entry();
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t pos = pairs[2 * i], f = pairs[2 * i + 1];
+    fseq[pos] = f;
+    walk[4 * pos + 3] = f;
+  }
+}
+
+cudaError_t table_patch(const Launch& L, uint64_t* fseq, uint64_t* walk, const uint64_t* d_pairs, uint64_t k,
+                        cudaStream_t s) {
+  launch_pdl(k_table_patch, blocks_for(k, kThreads, L.num_sms * 4), kThreads, 0, s, fseq, walk, d_pairs, k);
+  *L.counter += 1;
+  return cudaGetLastError();
+}
+
 size_t prop_meta_bytes() { return sizeof(PropMeta); }
 uint64_t stage_bytes() { return kStageBytes; }
 

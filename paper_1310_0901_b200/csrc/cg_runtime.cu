@@ -40,7 +40,7 @@ struct ArrayEntry {   // NEXT-3 device array (SPEC register_array S:166-168)
 };
 
 struct Layout {
-  uint64_t table, walk, arrays, weight, P, bsum, fbsum, chunk, meta, resid, defer, dvoff, scratch, waves, ovl, marks, flags,
+  uint64_t table, walk, patch, arrays, weight, P, bsum, fbsum, chunk, meta, resid, defer, dvoff, scratch, waves, ovl, marks, flags,
       leaks,
       desc_stage, chunk_list,
       verdict_stage, raw_stage,
@@ -85,6 +85,7 @@ Layout layout_of(const cg_config* c) {
   };
   L.table = take(6 * c->max_allocs * 8 + (4096 + 3) * 8 + (c->max_allocs / 4 + 16) * 8);   // SoA (+ pool offsets) + splitters + every 4th base
   L.walk = take(4 * c->max_allocs * 8);                      // (prefix max, end, alloc seq, free seq) per entry
+  L.patch = take(2 * c->max_allocs * 8);                     // (position, free seq) pairs of a diff upload
   L.arrays = take(5 * c->max_allocs * 8);                    // NEXT-3 array table (SoA + pool offsets)
   L.weight = take(L.max_items * 8);
   L.P = take((L.max_items + 1) * 8);
@@ -196,16 +197,23 @@ struct cg_ctx {
   }
   std::map<uint64_t, uint64_t> live_arrays; // handle -> total bytes
   uint64_t last_seq = 0;
-  bool dirty = true;
+  // registry diff upload state (sync_table)
+  uint64_t dev_n = 0, min_pos = 0, dev_stride = 0, uploads = 0;
+  std::vector<std::pair<uint64_t, uint64_t>> patches;   // (position, free seq) below min_pos
+  std::vector<uint64_t> pmax_host;                      // prefix max of ends by position
+  bool arrays_dirty = false;
+  int stage_slot = 0;
+  uint64_t* h_tab[2] = {nullptr, nullptr};              // pinned staging, double buffered
+  uint64_t* h_wlk[2] = {nullptr, nullptr};
+  uint64_t* h_arr[2] = {nullptr, nullptr};
+  uint64_t* h_patch[2] = {nullptr, nullptr};
+  cudaEvent_t staged_ev[2] = {nullptr, nullptr};
   uint64_t pool_cursor = 0;                 // NEXT-1 bump allocator in dev_vbuf
   const void* last_check = nullptr;         // descriptors of the last check (for cg_apply_copies)
   uint64_t last_check_n = 0;
   // pinned staging
-  uint64_t* h_table = nullptr;              // 10 * max_allocs + splitters
   cg_mark* h_marks = nullptr;               // kMarkRun
-  uint64_t* h_walk = nullptr;               // 4 * max_allocs: the lookup walk's records before upload
-  uint64_t* h_arrays = nullptr;             // 5 * max_allocs: the array table before upload
-  cudaEvent_t staged = nullptr;
+  cudaEvent_t staged = nullptr;             // the mark staging (h_marks) has been read
   cudaStream_t copy_stream = nullptr;        // host -> device uploads of cg_check_host
   cudaStream_t out_stream = nullptr;         // device -> host dirty-verdict downloads (cg_check_host_wait)
   cudaEvent_t chunk_ev[kHostSlots][kHostChunks] = {};
@@ -299,52 +307,82 @@ struct cg_ctx {
     return t;
   }
 
-  // upload the registry mirror (SoA + prefix max of ends) if it changed
+  // Registry upload by difference ("device table by diff
+  // upload"): the device table equals the mirror except positions [min_pos, n)
+  // (inserts shift the entries after them; a bump allocator only appends, so
+  // usually just the new tail) and the free stamps in `patches` (frees of
+  // entries below min_pos: 16 bytes each, scattered by k_table_patch).  The
+  // pinned staging is double buffered (an event per buffer), so an upload
+  // waits only for the one two uploads back, normally long finished.
   cg_status sync_table(cudaStream_t s) {
-    if (!dirty) return CG_OK;
     const uint64_t n = table.size(), cap = cfg.max_allocs;
-    if (n) {
-      cudaError_t e = cudaEventSynchronize(staged);   // previous upload finished reading h_table
-      if (e != cudaSuccess) return cuda(e, "cudaEventSynchronize");
-      uint64_t pm = 0;
-      for (uint64_t i = 0; i < n; ++i) {
+    if (min_pos >= n && n == dev_n && patches.empty() && !arrays_dirty) return CG_OK;
+    const int slot = stage_slot;
+    stage_slot ^= 1;
+    cudaError_t e = cudaEventSynchronize(staged_ev[slot]);   // this buffer's previous upload has been read
+    if (e != cudaSuccess) return cuda(e, "cudaEventSynchronize");
+    uint64_t* ht = h_tab[slot];
+    uint64_t* hw = h_wlk[slot];
+    uint64_t* dt = d(lay.table);
+    const uint64_t stride = split_stride(n), nsplit = (n + stride - 1) / stride;
+    const uint64_t so = (6 * cap + 1) & ~1ull;
+    const uint64_t a = std::min(min_pos, n);
+    if (a < n) {   // positions [a, n): SoA columns, prefix max of ends, walk records
+      uint64_t pm = a ? pmax_host[a - 1] : 0;
+      pmax_host.resize(n);
+      for (uint64_t i = a; i < n; ++i) {
         const Entry& x = table[i];
-        h_table[i] = x.base;
-        h_table[cap + i] = x.end;
-        h_table[2 * cap + i] = x.aseq;
-        h_table[3 * cap + i] = x.fseq;
+        ht[i] = x.base;
+        ht[cap + i] = x.end;
+        ht[2 * cap + i] = x.aseq;
+        ht[3 * cap + i] = x.fseq;
         pm = std::max(pm, x.end);
-        h_table[4 * cap + i] = pm;
-        h_table[5 * cap + i] = x.pool;
-        h_walk[4 * i] = pm;
-        h_walk[4 * i + 1] = x.end;
-        h_walk[4 * i + 2] = x.aseq;
-        h_walk[4 * i + 3] = x.fseq;
+        pmax_host[i] = pm;
+        ht[4 * cap + i] = pm;
+        ht[5 * cap + i] = x.pool;
+        hw[4 * i] = pm;
+        hw[4 * i + 1] = x.end;
+        hw[4 * i + 2] = x.aseq;
+        hw[4 * i + 3] = x.fseq;
       }
-      const uint64_t stride = split_stride(n), nsplit = (n + stride - 1) / stride;
-      const uint64_t so = (6 * cap + 1) & ~1ull;
-      for (uint64_t k = 0; k < nsplit; ++k) h_table[so + k] = table[k * stride].base;
-      h_table[so + nsplit] = UINT64_MAX;   // padding for the 16-byte loads
-      const uint64_t hl2 = so + 4099 + 4 * cap, nl2 = (n + 3) / 4;   // host staging of every 4th base
-      for (uint64_t k = 0; k < nl2; ++k) h_table[hl2 + k] = table[4 * k].base;
-      uint64_t* dt = d(lay.table);
       for (int k = 0; k < 6; ++k) {
-        e = cudaMemcpyAsync(dt + k * cap, h_table + k * cap, n * 8, cudaMemcpyHostToDevice, s);
+        e = cudaMemcpyAsync(dt + k * cap + a, ht + k * cap + a, (n - a) * 8, cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) return cuda(e, "table upload");
       }
-      e = cudaMemcpyAsync(d(lay.walk), h_walk, n * 32, cudaMemcpyHostToDevice, s);
+      e = cudaMemcpyAsync(d(lay.walk) + 4 * a, hw + 4 * a, (n - a) * 32, cudaMemcpyHostToDevice, s);
       if (e != cudaSuccess) return cuda(e, "walk upload");
-      e = cudaMemcpyAsync(dt + so, h_table + so, (nsplit + 1) * 8, cudaMemcpyHostToDevice, s);
-      if (e == cudaSuccess)
-        e = cudaMemcpyAsync(dt + l2_offset(cap), h_table + hl2, nl2 * 8, cudaMemcpyHostToDevice, s);
-      if (e != cudaSuccess) return cuda(e, "splitter upload");
     }
-    if (const uint64_t na = arrays.size()) {
-      uint64_t* ha = h_arrays;
-      if (!n) {
-        cudaError_t e = cudaEventSynchronize(staged);
-        if (e != cudaSuccess) return cuda(e, "cudaEventSynchronize");
+    if (a < n || n != dev_n) {   // splitters (every stride-th base) and every 4th base from a on
+      const uint64_t k0 = stride == dev_stride ? std::min(a / stride, nsplit) : 0;
+      for (uint64_t k = k0; k < nsplit; ++k) ht[so + k] = table[k * stride].base;
+      ht[so + nsplit] = UINT64_MAX;   // padding for the 16-byte loads
+      e = cudaMemcpyAsync(dt + so + k0, ht + so + k0, (nsplit + 1 - k0) * 8, cudaMemcpyHostToDevice, s);
+      const uint64_t hl2 = so + 4099 + 4 * cap, nl2 = (n + 3) / 4, j0 = std::min(a / 4, nl2);
+      for (uint64_t k = j0; k < nl2; ++k) ht[hl2 + k] = table[4 * k].base;
+      if (e == cudaSuccess && nl2 > j0)
+        e = cudaMemcpyAsync(dt + l2_offset(cap) + j0, ht + hl2 + j0, (nl2 - j0) * 8, cudaMemcpyHostToDevice, s);
+      if (e != cudaSuccess) return cuda(e, "splitter upload");
+      dev_stride = stride;
+    }
+    if (!patches.empty()) {   // free stamps below a: (position, free seq) pairs
+      uint64_t* hp = h_patch[slot];
+      uint64_t k = 0;
+      for (const auto& pr : patches) {
+        if (pr.first >= a) continue;
+        hp[2 * k] = pr.first;
+        hp[2 * k + 1] = pr.second;
+        ++k;
       }
+      if (k) {
+        uint64_t* dp = d(lay.patch);
+        e = cudaMemcpyAsync(dp, hp, k * 16, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cgk::table_patch(launch, dt + 3 * cap, d(lay.walk), dp, k, s);
+        if (e != cudaSuccess) return cuda(e, "free-stamp patch");
+      }
+    }
+    if (arrays_dirty && !arrays.empty()) {
+      uint64_t* ha = h_arr[slot];
+      const uint64_t na = arrays.size();
       for (uint64_t i = 0; i < na; ++i) {
         ha[i] = arrays[i].handle;
         ha[cap + i] = arrays[i].total;
@@ -354,13 +392,27 @@ struct cg_ctx {
       }
       uint64_t* da = d(lay.arrays);
       for (int k = 0; k < 5; ++k) {
-        cudaError_t e = cudaMemcpyAsync(da + k * cap, ha + k * cap, na * 8, cudaMemcpyHostToDevice, s);
+        e = cudaMemcpyAsync(da + k * cap, ha + k * cap, na * 8, cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) return cuda(e, "array table upload");
       }
     }
-    if (n || !arrays.empty()) cudaEventRecord(staged, s);
-    dirty = false;
+    cudaEventRecord(staged_ev[slot], s);
+    dev_n = n;
+    min_pos = n;
+    patches.clear();
+    arrays_dirty = false;
+    ++uploads;
     return CG_OK;
+  }
+  // the registry changed at position pos (insert: pos and everything after it move)
+  void touch_insert(uint64_t pos) {
+    min_pos = std::min(min_pos, pos);
+    patches.erase(std::remove_if(patches.begin(), patches.end(),
+                                 [&](const std::pair<uint64_t, uint64_t>& p) { return p.first >= pos; }),
+                  patches.end());
+  }
+  void touch_free(uint64_t pos, uint64_t fseq) {
+    if (pos < min_pos) patches.emplace_back(pos, fseq);
   }
 
   // word offset of the every-4th-base array in the device table (64-byte aligned)
@@ -444,11 +496,18 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
   c->prof.mark = &cg_ctx::mark_cb;
   c->prof.self = c;
   c->launch.prof = &c->prof;
-  if (cudaMallocHost(&c->h_table, 10 * cfg->max_allocs * 8 + (4096 + 5) * 8 + (cfg->max_allocs / 4 + 16) * 8) != cudaSuccess ||
-      cudaMallocHost(&c->h_marks, std::min<uint64_t>(cfg->max_descs, kMarkRun) * sizeof(cg_mark)) != cudaSuccess ||
-      cudaMallocHost(&c->h_walk, 4 * cfg->max_allocs * sizeof(uint64_t)) != cudaSuccess ||
-      cudaMallocHost(&c->h_arrays, 5 * cfg->max_allocs * sizeof(uint64_t)) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->staged, cudaEventDisableTiming) != cudaSuccess) {
+  bool pinned_ok = cudaMallocHost(&c->h_marks, std::min<uint64_t>(cfg->max_descs, kMarkRun) * sizeof(cg_mark)) ==
+                       cudaSuccess &&
+                   cudaEventCreateWithFlags(&c->staged, cudaEventDisableTiming) == cudaSuccess;
+  for (int k = 0; k < 2 && pinned_ok; ++k)
+    pinned_ok = cudaMallocHost(&c->h_tab[k], 10 * cfg->max_allocs * 8 + (4096 + 5) * 8 + (cfg->max_allocs / 4 + 16) * 8) ==
+                    cudaSuccess &&
+                cudaMallocHost(&c->h_wlk[k], 4 * cfg->max_allocs * sizeof(uint64_t)) == cudaSuccess &&
+                cudaMallocHost(&c->h_arr[k], 5 * cfg->max_allocs * sizeof(uint64_t)) == cudaSuccess &&
+                cudaMallocHost(&c->h_patch[k], 2 * cfg->max_allocs * sizeof(uint64_t)) == cudaSuccess &&
+                cudaEventCreateWithFlags(&c->staged_ev[k], cudaEventDisableTiming) == cudaSuccess &&
+                cudaEventRecord(c->staged_ev[k], 0) == cudaSuccess;
+  if (!pinned_ok) {
     cg_ctx_destroy(c);
     return CG_ERR_OUT_OF_MEMORY;
   }
@@ -505,10 +564,17 @@ cg_status cg_ctx_destroy(cg_ctx* c) {
   if (c->h_count) cudaFreeHost(c->h_count);
   for (auto& r : c->recs) { c->pool.push_back(r.a); c->pool.push_back(r.b); }
   for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
-  if (c->h_table) cudaFreeHost(c->h_table);
+  for (int k = 0; k < 2; ++k) {
+    if (c->staged_ev[k]) {
+      cudaEventSynchronize(c->staged_ev[k]);
+      cudaEventDestroy(c->staged_ev[k]);
+    }
+    if (c->h_tab[k]) cudaFreeHost(c->h_tab[k]);
+    if (c->h_wlk[k]) cudaFreeHost(c->h_wlk[k]);
+    if (c->h_arr[k]) cudaFreeHost(c->h_arr[k]);
+    if (c->h_patch[k]) cudaFreeHost(c->h_patch[k]);
+  }
   if (c->h_marks) cudaFreeHost(c->h_marks);
-  if (c->h_walk) cudaFreeHost(c->h_walk);
-  if (c->h_arrays) cudaFreeHost(c->h_arrays);
   delete c;
   return CG_OK;
 }
@@ -834,10 +900,10 @@ cg_status cg_register_alloc(cg_ctx* c, uint64_t base, uint64_t size, uint64_t se
   if (c->cfg.dev_vbuf) c->pool_cursor = pool + size;
   auto pos = std::upper_bound(c->table.begin(), c->table.end(), base,
                               [](uint64_t b, const Entry& e) { return b < e.base; });
+  c->touch_insert((uint64_t)(pos - c->table.begin()));
   c->table.insert(pos, x);
   c->live.emplace(base, end);
   c->last_seq = seq;
-  c->dirty = true;
   return CG_OK;
 }
 
@@ -851,13 +917,28 @@ cg_status cg_free(cg_ctx* c, uint64_t ptr, uint64_t seq) {
   for (; pos != c->table.end() && pos->base == ptr; ++pos) {
     if (pos->fseq == cgk::kInf) {
       pos->fseq = seq;
+      c->touch_free((uint64_t)(pos - c->table.begin()), seq);
       break;
     }
   }
   c->live.erase(it);
   c->last_seq = seq;
-  c->dirty = true;
   return CG_OK;
+}
+
+cg_status cg_registry_batch(cg_ctx* c, const cg_reg_event* h_events, uint64_t n, uint32_t* h_status) {
+  if (!c) return CG_ERR_INVALID_CONTEXT;
+  if (n && !h_events) return c->fail(CG_ERR_INVALID_VALUE, "null events");
+  cg_status first = CG_OK;
+  for (uint64_t i = 0; i < n; ++i) {
+    const cg_reg_event& e = h_events[i];
+    const cg_status st = e.op == CG_REG_ALLOC ? cg_register_alloc(c, e.addr, e.size, e.seq)
+                         : e.op == CG_REG_FREE ? cg_free(c, e.addr, e.seq)
+                                               : c->fail(CG_ERR_INVALID_VALUE, "unknown registry op");
+    if (h_status) h_status[i] = (uint32_t)st;
+    if (st != CG_OK && first == CG_OK) first = st;
+  }
+  return first;
 }
 
 cg_status cg_registry_compact(cg_ctx* c, uint64_t before_seq) {
@@ -865,14 +946,14 @@ cg_status cg_registry_compact(cg_ctx* c, uint64_t before_seq) {
   auto it = std::remove_if(c->table.begin(), c->table.end(),
                            [&](const Entry& e) { return e.fseq != cgk::kInf && e.fseq <= before_seq; });
   if (it != c->table.end()) {
+    c->touch_insert(0);   // entries move: re-upload all of them
     c->table.erase(it, c->table.end());
-    c->dirty = true;
   }
   auto ia = std::remove_if(c->arrays.begin(), c->arrays.end(),
                            [&](const ArrayEntry& e) { return e.fseq != cgk::kInf && e.fseq <= before_seq; });
   if (ia != c->arrays.end()) {
     c->arrays.erase(ia, c->arrays.end());
-    c->dirty = true;
+    c->arrays_dirty = true;
   }
   return CG_OK;
 }
@@ -905,7 +986,7 @@ cg_status cg_register_array(cg_ctx* c, uint64_t handle, uint64_t width, uint64_t
   c->arrays.insert(pos, ArrayEntry{handle, total, seq, cgk::kInf, pool});
   c->live_arrays.emplace(handle, total);
   c->last_seq = seq;
-  c->dirty = true;
+  c->arrays_dirty = true;
   return CG_OK;
 }
 
@@ -924,7 +1005,7 @@ cg_status cg_free_array(cg_ctx* c, uint64_t handle, uint64_t seq) {
   }
   c->live_arrays.erase(it);
   c->last_seq = seq;
-  c->dirty = true;
+  c->arrays_dirty = true;
   return CG_OK;
 }
 

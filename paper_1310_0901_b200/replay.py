@@ -36,7 +36,7 @@ def replay_events(chk, events: np.ndarray, blob=None, stream=None, fuse: bool = 
     checked batch to cg_conc_check with the copies' threads (threads[i] = the
     issuing thread of event i, default all 0)."""
     import torch
-    from . import MARK_DTYPE, VERDICT_DTYPE, to_device_descs, verdicts_to_numpy
+    from . import MARK_DTYPE, REG_EVENT_DTYPE, VERDICT_DTYPE, to_device_descs, verdicts_to_numpy
 
     ops = np.asarray(events["op"])
     n = len(events)
@@ -80,13 +80,21 @@ def replay_events(chk, events: np.ndarray, blob=None, stream=None, fuse: bool = 
             if regs_since > getattr(chk, "max_allocs", 1 << 62) // 2:
                 chk.registry_compact(int(events["seq"][i]))
                 regs_since = n_reg
-            for k in range(i, j):
-                if ops[k] == OP_REG:
-                    status[k] = chk.register_alloc(int(events["dst"][k]), int(events["width"][k]),
-                                                   int(events["seq"][k]))
-                elif ops[k] == OP_FREE:
-                    status[k] = chk.free(int(events["dst"][k]), int(events["seq"][k]))
-                elif ops[k] == OP_REGA:
+            k = i
+            while k < j:
+                if ops[k] in (OP_REG, OP_FREE):   # a run of registry events: one cg_registry_batch
+                    r = k
+                    while r < j and ops[r] in (OP_REG, OP_FREE):
+                        r += 1
+                    re = np.zeros(r - k, REG_EVENT_DTYPE)
+                    re["op"] = np.where(ops[k:r] == OP_REG, 1, 2)
+                    re["seq"], re["addr"], re["size"] = events["seq"][k:r], events["dst"][k:r], events["width"][k:r]
+                    st = np.zeros(r - k, np.uint32)
+                    chk.registry_batch(re, st)
+                    status[k:r] = st
+                    k = r
+                    continue
+                if ops[k] == OP_REGA:
                     e = events[k]
                     status[k] = chk.register_array(int(e["dst"]), int(e["width"]), int(e["height"]), int(e["dst_x"]),
                                                    int(e["dst_y"]), int(e["dst_pitch"]), int(e["seq"]))
@@ -94,6 +102,7 @@ def replay_events(chk, events: np.ndarray, blob=None, stream=None, fuse: bool = 
                     status[k] = chk.free_array(int(events["dst"][k]), int(events["seq"][k]))
                 elif ops[k] == OP_SYNC and conc is not None:
                     conc.sync(int(threads[k]) if threads is not None else 0, int(events["seq"][k]))
+                k += 1
             idx = np.flatnonzero(is_copy[i:j]) + i
             if len(idx):
                 descs = events_to_descs(events[idx])
