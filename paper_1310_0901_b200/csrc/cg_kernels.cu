@@ -451,19 +451,19 @@ __device__ __forceinline__ void finalize_fields(uint32_t& flags, uint32_t& statu
 }
 
 // HtoD tile: V bytes and their A bits, host bytes [q0, q1) of the staged tile.
-// Fast path: every lane folds its full 32-byte groups into one OR of the V
-// words and one AND of the A words (2 LDS.128 + 1 LDS.32 + 5 logic ops per 32
-// host bytes); only a lane that saw an undefined or unaddressable byte rescans
-// its groups with per-byte masks (__ffs for the first offset, __popc for the
-// count).  The partial 32-byte groups at the tile edges always take the
-// masked path.
-__device__ __forceinline__ void htod_group(const uint8_t* st, uint32_t i, uint32_t m, uint64_t ob, Partial& p) {
-  const uint4 v0 = reinterpret_cast<const uint4*>(st)[2 * i];
-  const uint4 v1 = reinterpret_cast<const uint4*>(st)[2 * i + 1];
-  const uint32_t a = reinterpret_cast<const uint32_t*>(st + kTileV)[i];
-  const uint32_t bad = ~a & m;
-  const uint32_t und = (nz16(v0) | (nz16(v1) << 16)) & a & m;
-  const uint64_t gb = ob + 32ull * i;
+// Fast path: lane j folds the 16-byte V units j, j+32, ... (contiguous 16-byte
+// lanes: one LDS.128 per lane reads 512 consecutive bytes, bank-conflict free)
+// into one OR, and their 16-bit A half-words into one AND (LDS.U16 of 64
+// consecutive bytes); only a lane that saw an undefined or unaddressable byte
+// rescans its units with per-byte masks (__ffs for the first offset, __popc
+// for the count).  The partial 32-byte groups at the tile edges always take
+// the masked path.
+__device__ __forceinline__ void htod_unit(const uint8_t* st, uint32_t u, uint64_t ob, Partial& p) {
+  const uint4 v = reinterpret_cast<const uint4*>(st)[u];
+  const uint32_t a = reinterpret_cast<const unsigned short*>(st + kTileV)[u];
+  const uint32_t bad = ~a & 0xFFFFu;
+  const uint32_t und = nz16(v) & a;
+  const uint64_t gb = ob + 16ull * u;
   if (bad) p.fu = umin64(p.fu, gb + (__ffs(bad) - 1));
   if (und) {
     p.fd = umin64(p.fd, gb + (__ffs(und) - 1));
@@ -493,18 +493,18 @@ __device__ __forceinline__ void htod_edge(const uint8_t* st, uint32_t g, uint32_
 __device__ __forceinline__ void consume_htod(const uint8_t* st, uint32_t q0, uint32_t q1, uint64_t ob,
                                              Partial& p) {
   const int lane = threadIdx.x & 31;
-  const uint32_t i0 = (q0 + 31) >> 5, i1 = q1 >> 5;   // full 32-byte groups [i0, i1)
+  const uint32_t i0 = (q0 + 31) >> 5, i1 = q1 >> 5;   // full 32-byte groups [i0, i1) = 16-byte units [2 i0, 2 i1)
   const uint4* V4 = reinterpret_cast<const uint4*>(st);
-  const uint32_t* A4 = reinterpret_cast<const uint32_t*>(st + kTileV);
-  uint32_t orv = 0, anda = 0xffffffffu;
+  const unsigned short* A2 = reinterpret_cast<const unsigned short*>(st + kTileV);
+  uint32_t orv = 0, anda = 0xFFFFu;
 #pragma unroll 4
-  for (uint32_t i = i0 + lane; i < i1; i += 32) {
-    const uint4 v0 = V4[2 * i], v1 = V4[2 * i + 1];
-    orv |= v0.x | v0.y | v0.z | v0.w | v1.x | v1.y | v1.z | v1.w;
-    anda &= A4[i];
+  for (uint32_t u = 2 * i0 + lane; u < 2 * i1; u += 32) {
+    const uint4 v = V4[u];
+    orv |= v.x | v.y | v.z | v.w;
+    anda &= A2[u];
   }
-  if (orv != 0 || anda != 0xffffffffu)
-    for (uint32_t i = i0 + lane; i < i1; i += 32) htod_group(st, i, 0xffffffffu, ob, p);
+  if (orv != 0 || anda != 0xFFFFu)
+    for (uint32_t u = 2 * i0 + lane; u < 2 * i1; u += 32) htod_unit(st, u, ob, p);
   // partial edge groups, warp-parallel
   if (i0 > i1) {                                   // [q0, q1) inside one 32-byte group
     htod_edge(st, i1, q0, q1, ob, p);
