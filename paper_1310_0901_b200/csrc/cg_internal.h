@@ -13,6 +13,7 @@ constexpr uint64_t kNone = UINT64_MAX;
 constexpr uint64_t kInf = UINT64_MAX;          // free_seq of a live allocation
 constexpr uint64_t kMaxShardBytes = 1ull << 38;  // host bytes one context stores (config limit; scan weights < 2^40 each)
 constexpr uint64_t kDeferBytes = 1ull << 36;     // sparse map: longer host sides go to the deferred pass
+constexpr uint64_t kSmallBytesDefault = 4096;    // the small pass's limit (at most 4096; env CG_SMALL_BYTES)
 constexpr uint64_t kMaxDescs = 1ull << 24;       // per call (keeps sum of weights < 2^63)
 
 // start = base + y*pitch + x; span = (w==0||h==0) ? 0 : (h-1)*pitch + w;
@@ -58,6 +59,9 @@ struct ShadowView {
   // pass walks them instead of the whole 64-bit range of a huge copy)
   const uint64_t* chunk_list;
   uint64_t n_chunks;
+  // the small pass (k_check_small) takes contiguous host sides of at most
+  // this many bytes (0: none; env CG_SMALL_BYTES)
+  uint64_t small_limit;
 };
 
 constexpr uint64_t kChunkShift = 16;               // 64 KiB host bytes per chunk

@@ -953,7 +953,7 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
     // raw -- checked by k_check_small, not by the ring; its verdict is written
     // here already finalised as if the host side were clean (k_check_small
     // rewrites only the dirty ones)
-    const bool small = nscan != 0 && nscan <= kSmallBytes && contig && !raw && !sv.sparse;
+    const bool small = nscan != 0 && nscan <= sv.small_limit && contig && !raw && !sv.sparse;
     if (act) {
       cg_verdict v;
       v.first_unaddr = hc.pfu;
@@ -3380,7 +3380,7 @@ static cudaError_t check_front(const Launch& L, const cg_copy_desc* d, uint64_t 
     L.stage(CG_STAGE_CHECK_PLAN, false, s);
   }
   L.stage(CG_STAGE_CHECK_SCAN, true, s);
-  if (!sv.sparse) {   // the small pass (k_check_small), then the ring scan
+  if (!sv.sparse && sv.small_limit) {   // the small pass (k_check_small), then the ring scan
     launch_pdl(sv.two_bit ? k_check_small<true> : k_check_small<false>, L.small_blocks, kThreads, 0, s, meta, n, sv,
                out, err_mask, fuse ? 1 : 0, p.resid, p.counter + 2);
     *L.counter += 1;

@@ -466,6 +466,8 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
   c->sv.v_bytes = sparse ? (cfg->host_size / 65536 + 1) * cgk::kSecondaryBytes : two_bit ? cfg->host_size / 4
                                                                                           : cfg->host_size;
   if (cfg->shard_size && !sparse) c->sv.v_bytes = two_bit ? cfg->shard_size / 4 : cfg->shard_size;
+  c->sv.small_limit = cgk::kSmallBytesDefault;
+  if (const char* sl = getenv("CG_SMALL_BYTES")) c->sv.small_limit = std::min<uint64_t>(strtoull(sl, nullptr, 10), 4096);
   if (sparse) {   // the whole 64-bit space; the directory lives in the workspace
     c->sv.wb = c->sv.sb = 0;
     c->sv.we = c->sv.se = UINT64_MAX;
