@@ -281,14 +281,16 @@ __device__ __forceinline__ bool table_lookup(const Table& t, const uint64_t* s_s
   }
   uint64_t a = (uint64_t)lo * t.stride;
   uint64_t b = umin64(a + t.stride, t.n);
-  if (t.stride == 32) {
-    // two independent-load rounds instead of five dependent ones: the bucket's
-    // 8 every-4th bases (64 B), then the 4 bases of the chosen quarter (32 B);
-    // each picks the last entry <= start (the first always is)
+  if (t.stride == 32 || t.stride == 64) {
+    // two independent-load rounds instead of five or six dependent ones: the
+    // bucket's 8 or 16 every-4th bases (64 or 128 B), then the 4 bases of the
+    // chosen quarter (32 B); each picks the last entry <= start (the first always is)
     const uint4* q = reinterpret_cast<const uint4*>(t.l2 + a / 4);
+    const int nq = (int)(t.stride >> 3);   // uint4 loads of 2 every-4th bases each
     uint32_t c2 = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < 8; ++k) {
+      if (k >= nq) break;
       const uint4 v = __ldg(q + k);
       c2 += (a + 8 * k < b && (((uint64_t)v.y << 32) | v.x) <= start) +
             (a + 8 * k + 4 < b && (((uint64_t)v.w << 32) | v.z) <= start);
