@@ -739,33 +739,59 @@ __device__ __forceinline__ void warp_store_zero(uint8_t* V, uint64_t q0, uint64_
 }
 
 // ---------------------------------------------------------------------------
-// Small contiguous host sides are checked right in the prep (the "small
-// pass"), by teams of 8 lanes: each team streams through the small
-// descriptors of its warp's 32-descriptor window, 16 bytes of shadow per lane
-// per round, so every warp instruction serves up to 4 descriptors and the
-// teams stay converged (one loop, per-team data).  Bigger, 2D, split, raw and
-// deferred host sides go to the TMA-ring scan.  kSmallBytes bounds the host
-// bytes of a small side: HtoD 4 KiB = 32 rounds of V, DtoH 4 KiB = 4 rounds of A.
+// The small pass: contiguous host sides of at most sv.small_limit (<= 4 KiB)
+// bytes are checked by k_check_small instead of the TMA ring: a warp takes 32
+// consecutive descriptors (one coalesced meta load), then checks its small
+// ones one after the other with the whole warp -- a round is one 16-byte
+// load per lane (HtoD: 16 V bytes + their 16 A bits = 512 host bytes per
+// round; DtoH: 16 A bytes = 4 KiB; 2-bit: 16 state bytes = 2 KiB) -- with a
+// two-deep software pipeline: the first round of the next small descriptor
+// is loaded before the current one is folded, so two rounds are in flight per
+// warp.  The fold is an OR / AND per lane; masks, __ffs and __popc and the
+// warp reduction only run for a side that has a finding.
 // ---------------------------------------------------------------------------
-constexpr uint64_t kSmallBytes = 4096;
-constexpr int kTeam = 8;
-
-// host bytes covered by one lane per round: bytes format HtoD 16 (V bytes +
-// their A bits), DtoH 128 (16 bytes of A); 2-bit states 64 (16 state bytes)
 template <bool kTwoBit>
 __device__ __forceinline__ uint32_t lane_span(bool htod) {
   return kTwoBit ? 64u : htod ? 16u : 128u;
 }
 
-// the lane's unit [gp, gp + span) of a small side [q0, q1) (shard bytes; logical
-// offset of shard byte q = ob + q): accumulate first unaddressable / first
-// undefined / undefined count
+struct SmallRound {
+  uint4 x;      // HtoD: V bytes; DtoH: A bytes; 2-bit: states
+  uint32_t a;   // HtoD: the A bits of the 16 V bytes
+};
+
+// round r of a small side: lane unit gp = g0 + (32 r + lane) span (shard bytes)
 template <bool kTwoBit>
-__device__ __forceinline__ void small_unit(const ShadowView& sv, uint64_t gp, uint64_t q0, uint64_t q1, uint64_t ob,
-                                           bool htod, Partial& p) {
+__device__ __forceinline__ SmallRound small_load(const ShadowView& sv, uint64_t gp, uint64_t q1, bool htod) {
+  SmallRound u{make_uint4(0, 0, 0, 0), 0xFFFFu};
+  if (gp >= q1) return u;
   if (kTwoBit) {
-    const uint4 s4 = __ldcs(reinterpret_cast<const uint4*>(sv.V + (gp >> 2)));
-    const uint32_t w[4] = {s4.x, s4.y, s4.z, s4.w};
+    u.x = __ldcs(reinterpret_cast<const uint4*>(sv.V + (gp >> 2)));
+  } else if (htod) {
+    u.x = __ldcs(reinterpret_cast<const uint4*>(sv.V + gp));
+    u.a = __ldcs(reinterpret_cast<const unsigned short*>(sv.A + (gp >> 3)));
+  } else {
+    u.x = __ldcs(reinterpret_cast<const uint4*>(sv.A + (gp >> 3)));
+  }
+  return u;
+}
+
+// fold one lane unit [gp, gp + span) of a side [q0, q1) into p (logical offset
+// of shard byte q = ob + q)
+template <bool kTwoBit>
+__device__ __forceinline__ void small_fold(const SmallRound& u, uint64_t gp, uint64_t q0, uint64_t q1, uint64_t ob,
+                                           bool htod, Partial& p) {
+  if (gp >= q1) return;
+  if (kTwoBit) {
+    const uint32_t w[4] = {u.x.x, u.x.y, u.x.z, u.x.w};
+    const bool inner = gp >= q0 && gp + 64 <= q1;
+    if (inner) {   // the common case: a clean unit costs the fold only
+      const uint32_t acc = htod ? ((w[0] ^ 0xAAAAAAAAu) | (w[1] ^ 0xAAAAAAAAu) | (w[2] ^ 0xAAAAAAAAu) |
+                                   (w[3] ^ 0xAAAAAAAAu))
+                                : (~((w[0] | (w[0] >> 1)) & (w[1] | (w[1] >> 1)) & (w[2] | (w[2] >> 1)) &
+                                     (w[3] | (w[3] >> 1))) & 0x55555555u);
+      if (!acc) return;
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const uint64_t gb = gp + 16u * j;
@@ -777,10 +803,9 @@ __device__ __forceinline__ void small_unit(const ShadowView& sv, uint64_t gp, ui
     return;
   }
   if (htod) {
-    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(sv.V + gp));
-    const uint32_t a = __ldcs(reinterpret_cast<const unsigned short*>(sv.A + (gp >> 3)));
-    const uint32_t m = range_mask(gp, 16, q0, q1);
-    const uint32_t bad = ~a & m, und = nz16(v) & a & m;
+    const uint32_t m = (gp >= q0 && gp + 16 <= q1) ? 0xFFFFu : range_mask(gp, 16, q0, q1);
+    if ((u.x.x | u.x.y | u.x.z | u.x.w) == 0 && (u.a & m) == m) return;   // clean
+    const uint32_t bad = ~u.a & m, und = nz16(u.x) & u.a & m;
     if (bad) p.fu = umin64(p.fu, ob + gp + (__ffs(bad) - 1));
     if (und) {
       p.fd = umin64(p.fd, ob + gp + (__ffs(und) - 1));
@@ -788,8 +813,8 @@ __device__ __forceinline__ void small_unit(const ShadowView& sv, uint64_t gp, ui
     }
     return;
   }
-  const uint4 a4 = __ldcs(reinterpret_cast<const uint4*>(sv.A + (gp >> 3)));
-  const uint32_t w[4] = {a4.x, a4.y, a4.z, a4.w};
+  if (gp >= q0 && gp + 128 <= q1 && (u.x.x & u.x.y & u.x.z & u.x.w) == 0xFFFFFFFFu) return;   // clean
+  const uint32_t w[4] = {u.x.x, u.x.y, u.x.z, u.x.w};
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const uint64_t gb = gp + 32u * j;
@@ -798,74 +823,6 @@ __device__ __forceinline__ void small_unit(const ShadowView& sv, uint64_t gp, ui
     if (bad) {
       p.fu = umin64(p.fu, ob + gb + (__ffs(bad) - 1));
       break;
-    }
-  }
-}
-
-// every lane with `small` set owns one small side (q0, q1, ob, htod); on return
-// its `mine` holds that side's partial (first unaddressable, first undefined,
-// count).  Warp-uniform entry.
-template <bool kTwoBit>
-__device__ __noinline__ void small_pass(const ShadowView& sv, bool small, uint64_t q0, uint64_t q1, uint64_t ob,
-                                        bool htod, Partial& mine) {
-  const int lane = threadIdx.x & 31, tl = lane & (kTeam - 1);
-  uint32_t pend = __ballot_sync(kFull, small);
-  int own = -1;                 // team state, replicated in its 8 lanes
-  uint64_t t0 = 0, t1 = 0, tob = 0, g = 0;
-  bool th = false;
-  Partial acc{kNone, kNone, 0};
-  while (true) {
-    // idle teams take the next pending sides, lowest lane first
-    uint32_t idle = __ballot_sync(kFull, own < 0 && tl == 0);
-    while (idle && pend) {
-      const int team_lane = __ffs(idle) - 1;
-      idle &= idle - 1;
-      const int j = __ffs(pend) - 1;
-      pend &= pend - 1;
-      const uint64_t a = __shfl_sync(kFull, q0, j), b = __shfl_sync(kFull, q1, j), o = __shfl_sync(kFull, ob, j);
-      const bool h = __shfl_sync(kFull, htod, j);
-      if ((lane & ~(kTeam - 1)) == team_lane) {
-        own = j;
-        t0 = a;
-        t1 = b;
-        tob = o;
-        th = h;
-        const uint64_t u = kTwoBit ? 64 : h ? 16 : 128;
-        g = a / u * u;   // the first lane unit of the side
-      }
-    }
-    if (!__any_sync(kFull, own >= 0)) break;
-    // one round: lane tl takes unit g + tl of its team's side
-    if (own >= 0) {
-      const uint64_t u = lane_span<kTwoBit>(th);
-      const uint64_t gp = g + u * tl;
-      if (gp < t1) small_unit<kTwoBit>(sv, gp, t0, t1, tob, th, acc);
-      g += u * kTeam;
-    }
-    // teams whose side is done reduce within the team and hand the partial to its owner
-    const bool fin = own >= 0 && g >= t1;
-    if (__any_sync(kFull, fin)) {
-      // xor partners stay inside the team; unfinished teams reduce identities
-      Partial r = fin ? acc : Partial{kNone, kNone, 0};
-#pragma unroll
-      for (int o = kTeam / 2; o > 0; o >>= 1) {
-        r.fu = umin64(r.fu, __shfl_xor_sync(kFull, r.fu, o));
-        r.fd = umin64(r.fd, __shfl_xor_sync(kFull, r.fd, o));
-        r.cnt += __shfl_xor_sync(kFull, r.cnt, o);
-      }
-      uint32_t leaders = __ballot_sync(kFull, fin && tl == 0);
-      while (leaders) {
-        const int l = __ffs(leaders) - 1;
-        leaders &= leaders - 1;
-        const int who = __shfl_sync(kFull, own, l);
-        const uint64_t fu = __shfl_sync(kFull, r.fu, l), fd = __shfl_sync(kFull, r.fd, l);
-        const uint64_t cnt = __shfl_sync(kFull, r.cnt, l);
-        if (lane == who) mine = Partial{fu, fd, cnt};
-      }
-      if (fin) {
-        own = -1;
-        acc = Partial{kNone, kNone, 0};
-      }
     }
   }
 }
@@ -984,11 +941,10 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
   }
 }
 
-// The small pass (a4-a6 for small contiguous host sides): a warp takes 32
-// consecutive descriptors (one coalesced meta load), its teams check the
-// small ones; a dirty verdict is rewritten, a clean one was final already;
-// small DtoH sides with status OK are applied here when fused (a6) unless
-// CG_APPLY_AFTER sends them to the residual pass.
+// The small pass (a4-a6 for small contiguous host sides; see small_load):
+// a dirty verdict is rewritten, a clean one was final already (the prep
+// wrote it); small DtoH sides with status OK are applied here when fused (a6)
+// unless CG_APPLY_AFTER sends them to the residual pass.
 template <bool kTwoBit>
 __global__ void __launch_bounds__(kThreads) k_check_small(const ScanMeta* __restrict__ meta, uint64_t n,
                                                           ShadowView sv, cg_verdict* __restrict__ out,
@@ -1006,7 +962,8 @@ __global__ void __launch_bounds__(kThreads) k_check_small(const ScanMeta* __rest
       x0 = m.hstart;
     }
     const bool small = (info >> kInfoSmall) & 1u;
-    if (!__any_sync(kFull, small)) continue;
+    uint32_t todo = __ballot_sync(kFull, small);
+    if (!todo) continue;
     const bool htod = ((info >> kInfoKind) & 3u) == CG_HTOD;
     uint64_t q0 = 0, q1 = 0, ob = 0;
     if (small) {   // shard bytes [x, x + nscan); logical offset of shard byte q = q + sb - x0 (R-10 clip)
@@ -1016,7 +973,50 @@ __global__ void __launch_bounds__(kThreads) k_check_small(const ScanMeta* __rest
       ob = sv.sb - x0;
     }
     Partial mine{kNone, kNone, 0};
-    small_pass<kTwoBit>(sv, small, q0, q1, ob, htod, mine);
+    // the two-deep pipeline: (j, its geometry, its round-0 data) current / next
+    int j = __ffs(todo) - 1;
+    todo &= todo - 1;
+    uint64_t cq0 = __shfl_sync(kFull, q0, j), cq1 = __shfl_sync(kFull, q1, j), cob = __shfl_sync(kFull, ob, j);
+    bool ch = __shfl_sync(kFull, htod, j);
+    uint64_t cspan = lane_span<kTwoBit>(ch), cg0 = cq0 / cspan * cspan;
+    SmallRound cu = small_load<kTwoBit>(sv, cg0 + cspan * lane, cq1, ch);
+    while (j >= 0) {
+      const int jn = todo ? __ffs(todo) - 1 : -1;
+      if (jn >= 0) todo &= todo - 1;
+      uint64_t nq0 = 0, nq1 = 0, nob = 0, nspan = 16, ng0 = 0;
+      bool nh = false;
+      SmallRound nu{make_uint4(0, 0, 0, 0), 0xFFFFu};
+      if (jn >= 0) {   // issue the next side's first round before folding this one
+        nq0 = __shfl_sync(kFull, q0, jn);
+        nq1 = __shfl_sync(kFull, q1, jn);
+        nob = __shfl_sync(kFull, ob, jn);
+        nh = __shfl_sync(kFull, htod, jn);
+        nspan = lane_span<kTwoBit>(nh);
+        ng0 = nq0 / nspan * nspan;
+        nu = small_load<kTwoBit>(sv, ng0 + nspan * lane, nq1, nh);
+      }
+      Partial p{kNone, kNone, 0};
+      small_fold<kTwoBit>(cu, cg0 + cspan * lane, cq0, cq1, cob, ch, p);
+      for (uint64_t g = cg0 + 32 * cspan; g < cq1; g += 32 * cspan) {   // rounds after the first (sides > one round)
+        const uint64_t gp = g + cspan * lane;
+        const SmallRound u = small_load<kTwoBit>(sv, gp, cq1, ch);
+        small_fold<kTwoBit>(u, gp, cq0, cq1, cob, ch, p);
+      }
+      if (__any_sync(kFull, p.fu != kNone || p.fd != kNone || p.cnt != 0)) {
+        p.fu = warp_min(p.fu);
+        p.fd = warp_min(p.fd);
+        p.cnt = warp_sum(p.cnt);
+        if (lane == j) mine = p;
+      }
+      j = jn;
+      cq0 = nq0;
+      cq1 = nq1;
+      cob = nob;
+      ch = nh;
+      cspan = nspan;
+      cg0 = ng0;
+      cu = nu;
+    }
     bool apply_me = false;
     if (small) {
       uint64_t fu = mine.fu;
@@ -1036,11 +1036,11 @@ __global__ void __launch_bounds__(kThreads) k_check_small(const ScanMeta* __rest
         else apply_me = true;
       }
     }
-    uint32_t todo = __ballot_sync(kFull, apply_me);
-    while (todo) {   // fused a6, the whole warp per side
-      const int j = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const uint64_t a = __shfl_sync(kFull, q0, j), b = __shfl_sync(kFull, q1, j);
+    uint32_t ap = __ballot_sync(kFull, apply_me);
+    while (ap) {   // fused a6, the whole warp per side
+      const int k = __ffs(ap) - 1;
+      ap &= ap - 1;
+      const uint64_t a = __shfl_sync(kFull, q0, k), b = __shfl_sync(kFull, q1, k);
       if (kTwoBit) warp_fill2(sv.V, a, b, 0xAAAAAAAAu);
       else warp_store_zero(sv.V, a, b);
     }
