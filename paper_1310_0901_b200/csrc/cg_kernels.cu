@@ -1358,6 +1358,12 @@ struct TileGen {
       m_info = 0;
       m_ps = m_pe = ~0ull;
     }
+    // the next window is usually needed next: bring its records into L2 now
+    // (no registers held), so that load does not stall the ring's owner warp
+    if (i + 32 < n) {
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(meta + i + 32));
+      if ((lane & 3) == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(P + i + 32));
+    }
   }
 
   __device__ __forceinline__ void compute_pieces() {
