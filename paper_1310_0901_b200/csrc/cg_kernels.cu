@@ -281,7 +281,7 @@ __device__ __forceinline__ bool table_lookup(const Table& t, const uint64_t* s_s
   }
   uint64_t a = (uint64_t)lo * t.stride;
   uint64_t b = umin64(a + t.stride, t.n);
-  if (t.stride == 32 || t.stride == 64) {
+  if (t.stride == 32 || (t.stride == 64 && t.two_round64)) {
     // two independent-load rounds instead of five or six dependent ones: the
     // bucket's 8 or 16 every-4th bases (64 or 128 B), then the 4 bases of the
     // chosen quarter (32 B); each picks the last entry <= start (the first always is)
@@ -973,6 +973,31 @@ __global__ void __launch_bounds__(kThreads) k_check_small(const ScanMeta* __rest
       ob = sv.sb - x0;
     }
     Partial mine{kNone, kNone, 0};
+    // tiny sides (at most 33 lane units: HtoD 512 B, DtoH 4 KiB, 2-bit 2 KiB)
+    // are checked by their own lane, four 16-byte loads in flight per lane
+    // per step, no warp reduction; the warp loops until its largest tiny side is done
+    {
+      const uint64_t span = lane_span<kTwoBit>(htod);
+      const bool tiny = small && q1 - q0 <= 32 * span;
+      const uint32_t tmask = __ballot_sync(kFull, tiny);
+      if (tmask) {
+        uint64_t g = q0 / span * span;
+        Partial tp{kNone, kNone, 0};
+        while (__any_sync(kFull, tiny && g < q1)) {
+          if (tiny && g < q1) {
+            SmallRound u[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) u[k] = small_load<kTwoBit>(sv, g + k * span, q1, htod);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) small_fold<kTwoBit>(u[k], g + k * span, q0, q1, ob, htod, tp);
+            g += 4 * span;
+          }
+        }
+        if (tiny) mine = tp;
+        todo &= ~tmask;
+      }
+    }
+    if (todo) {
     // the two-deep pipeline: (j, its geometry, its round-0 data) current / next
     int j = __ffs(todo) - 1;
     todo &= todo - 1;
@@ -1016,6 +1041,7 @@ __global__ void __launch_bounds__(kThreads) k_check_small(const ScanMeta* __rest
       cspan = nspan;
       cg0 = ng0;
       cu = nu;
+    }
     }
     bool apply_me = false;
     if (small) {

@@ -304,6 +304,11 @@ struct cg_ctx {
     const uint64_t stride = split_stride(t.n);
     t.stride = (uint32_t)stride;
     t.nsplit = (uint32_t)((t.n + stride - 1) / stride);
+    static const bool two = [] {
+      const char* e = getenv("CG_LOOKUP64");
+      return !(e && e[0] == '0');
+    }();
+    t.two_round64 = two ? 1u : 0u;
     return t;
   }
 
