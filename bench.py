@@ -275,19 +275,18 @@ def run_ours(args, rank, world, device, config=None, steps=None, warmup=None, e2
     # the batch contract (R-20): the copies are checked in the epochs
     # cg_plan_batches cuts (one epoch for C2-C4; C5's ping-pongs make ~11); an
     # epoch whose HtoD and DtoH host ranges are disjoint runs fused
-    cuts = [0] + [int(c) for c in cg.plan_batches(descs)]
+    # fused (cg_check_apply): the batches of cg_plan_batches_fused, which marks
+    # the DtoH copies an HtoD of their batch reads CG_APPLY_AFTER and the HtoD
+    # copies that read an earlier DtoH's bytes CG_CHECK_AFTER, so that a DtoH ->
+    # HtoD ping-pong no longer ends the batch; unfused / tracking: the R-20
+    # epochs of cg_plan_batches (host planning, untimed)
+    fused = not args.unfused and not args.track
+    descs = np.ascontiguousarray(descs)
+    cuts = [0] + [int(c) for c in (cg.plan_batches_fused(descs) if fused else cg.plan_batches(descs))]
     epochs = [(a, b) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
-    # every epoch runs fused (cg_check_apply): the DtoH descriptors whose host
-    # range an HtoD of the same epoch reads carry CG_APPLY_AFTER (host planning,
-    # untimed, like the epoch cuts)
-    efused = [not args.unfused and not args.track for _ in epochs]
-    fused = all(efused)
-    n_after = 0
-    if fused:
-        for a, b in epochs:
-            part = np.ascontiguousarray(descs[a:b])
-            n_after += cg.plan_apply_after(part)
-            descs[a:b] = part
+    efused = [fused for _ in epochs]
+    n_after = int(np.count_nonzero(descs["reserved"] & cg.CG_APPLY_AFTER))
+    n_late = int(np.count_nonzero(descs["reserved"] & cg.CG_CHECK_AFTER))
     d_descs = cg.to_device_descs(descs, device)
     waves = []   # NEXT-1: per epoch, the device index lists of its propagation waves (cg_plan_waves)
     t_waves = 0.0
@@ -481,7 +480,7 @@ def run_ours(args, rank, world, device, config=None, steps=None, warmup=None, e2
                    "entry": ("cg_check_copies + cg_apply_copies (NEXT-1 V-bit propagation)" if args.track else
                              "cg_check_apply (fused)" if fused else "cg_check_copies + cg_apply_dtoh"
                              if not any(efused) else "cg_check_apply / cg_check_copies + cg_apply_dtoh per epoch"),
-                   "epochs": len(epochs), "apply_after_descriptors": n_after,
+                   "epochs": len(epochs), "apply_after_descriptors": n_after, "check_after_descriptors": n_late,
                    "propagation_waves": sum(w.n_waves for w in waves) if args.track else None,
                    "wave_planning_s": t_waves if args.track else None},
         "descriptors_per_s": world * n / (ms_step * 1e-3),
@@ -684,14 +683,9 @@ def run_interleaved(args, device):
         re = np.zeros(len(regs), cg.REG_EVENT_DTYPE)
         re["op"] = np.where(regs["op"] == 3, cg.CG_REG_ALLOC, cg.CG_REG_FREE)
         re["seq"], re["addr"], re["size"] = regs["seq"], regs["dst"], regs["width"]
-        descs = tg.events_to_descs(rest[j:k])
-        cuts = [0] + [int(c) for c in cg.plan_batches(descs)] if len(descs) else [0]
-        eps = []
-        for a, b in zip(cuts[:-1], cuts[1:]):
-            part = np.ascontiguousarray(descs[a:b])
-            cg.plan_apply_after(part)
-            descs[a:b] = part
-            eps.append((a, b))
+        descs = np.ascontiguousarray(tg.events_to_descs(rest[j:k]))
+        cuts = [0] + [int(c) for c in cg.plan_batches_fused(descs)] if len(descs) else [0]
+        eps = [(a, b) for a, b in zip(cuts[:-1], cuts[1:])]
         blocks.append((re, descs, eps))
         i = k
     n = int(np.count_nonzero(rops == 5))

@@ -108,7 +108,12 @@ enum {
  *    shard writes only its raw partial (first_unaddr, first_undef, undef_count,
  *    device fields, flags without HOST_*; status 0) for cg_straddler_pack /
  *    cg_straddler_finalize after the collective merge. */
-enum { CG_SHARD_NOT_OWNER = 1u << 0, CG_SHARD_RAW = 1u << 1, CG_APPLY_AFTER = 1u << 2 };
+enum { CG_SHARD_NOT_OWNER = 1u << 0, CG_SHARD_RAW = 1u << 1, CG_APPLY_AFTER = 1u << 2, CG_CHECK_AFTER = 1u << 3 };
+/* CG_CHECK_AFTER (cg_check_apply only): this HTOD / HTOA descriptor reads host
+ * bytes that an earlier DTOH / ATOH of the same batch writes, so it is
+ * checked after every apply of the batch (no later DTOH / ATOH of the batch
+ * may write its range).  Set by cg_plan_batches_fused; ignored by
+ * cg_check_copies. */
 /* CG_APPLY_AFTER (cg_check_apply only): this DTOH / ATOH descriptor's host
  * range overlaps the host range of an HTOD / HTOA descriptor of the same
  * batch, so its apply waits until every check of the batch has read the
@@ -678,6 +683,17 @@ cg_status cg_leak_report(cg_ctx *ctx, cg_alloc_record *h_out, uint64_t cap, uint
  * batch to h_cuts (at most n entries; the last is n) and their number to
  * *n_cuts.  Errors: CG_ERR_INVALID_VALUE on NULL. */
 cg_status cg_plan_batches(const cg_copy_desc *h_descs, uint64_t n, uint64_t *h_cuts, uint64_t *n_cuts);
+
+/* Batches for cg_check_apply (fused), in place: like cg_plan_batches, but an
+ * HtoD that reads bytes an earlier DtoH of the batch writes does not end the
+ * batch: it gets CG_CHECK_AFTER (checked after the batch's applies) when its
+ * host range is at most 1 MiB; a DtoH that writes bytes of such an HtoD ends
+ * the batch (so every CG_CHECK_AFTER descriptor sees exactly the applies of
+ * the DtoH copies before it); every DtoH whose range an HtoD of its batch
+ * reads gets CG_APPLY_AFTER.  The result of cg_check_apply over each batch
+ * equals the sequential replay.  Writes the end of every batch to h_cuts (the
+ * last is n), their number to *n_cuts.  Errors: CG_ERR_INVALID_VALUE on NULL. */
+cg_status cg_plan_batches_fused(cg_copy_desc *h_descs, uint64_t n, uint64_t *h_cuts, uint64_t *n_cuts);
 
 /* As cg_plan_batches, for device V-bit tracking (NEXT-1): a batch is cut
  * before any copy whose reads (HtoD host source, DtoD/DtoH device source)

@@ -114,6 +114,7 @@ def _load() -> ctypes.CDLL:
         "cg_leak_sweep": (I, [P, P, U64, P, P]),
         "cg_leak_report": (I, [P, P, U64, P]),
         "cg_plan_batches": (I, [P, U64, P, P]),
+        "cg_plan_batches_fused": (I, [P, U64, P, P]),
         "cg_kernel_launches": (U64, [P]),
         "cg_profile_begin": (I, [P]),
         "cg_profile_end": (I, [P, P, P]),
@@ -166,7 +167,8 @@ EXPORTED = ("cg_workspace_size", "cg_ctx_create", "cg_ctx_destroy", "cg_last_err
             "cg_conc_destroy", "cg_conc_last_error", "cg_conc_sync", "cg_conc_check", "cg_conc_stamps",
             "cg_conc_kernel_launches", "cg_ctx_device", "cg_comm_nccl_id", "cg_comm_create_nccl",
             "cg_comm_create_loopback", "cg_comm_destroy", "cg_comm_last_error", "cg_comm_kernel_launches",
-            "cg_comm_overflow", "cg_check_sharded", "cg_shard_lists", "cg_registry_batch")
+            "cg_comm_overflow", "cg_check_sharded", "cg_shard_lists", "cg_registry_batch",
+            "cg_plan_batches_fused")
 
 # ---- same-name thin wrappers of every exported function (status codes returned unchanged) ----
 globals().update({_n: getattr(_lib, _n) for _n in EXPORTED})
@@ -176,7 +178,7 @@ CG_SHADOW_BYTES, CG_SHADOW_2BIT, CG_SHADOW_SPARSE = 0, 1, 2
 CG_FMT_2D, CG_FMT_1D = 0, 1
 COPY1D_DTYPE = np.dtype([("kind", "<u4"), ("reserved", "<u4"), ("seq", "<u8"), ("dst", "<u8"), ("src", "<u8"),
                          ("bytes", "<u8")])
-CG_SHARD_NOT_OWNER, CG_SHARD_RAW, CG_APPLY_AFTER = 1, 2, 4
+CG_SHARD_NOT_OWNER, CG_SHARD_RAW, CG_APPLY_AFTER, CG_CHECK_AFTER = 1, 2, 4, 8
 CG_COMM_NCCL, CG_COMM_LOOPBACK = 0, 1
 CG_NCCL_ID_BYTES = 128
 CG_REG_ALLOC, CG_REG_FREE = 1, 2
@@ -282,6 +284,19 @@ def batch_disjoint(descs: np.ndarray) -> bool:
     if st:
         raise CgError(st, "cg_batch_disjoint")
     return bool(out.value)
+
+
+def plan_batches_fused(descs: np.ndarray) -> np.ndarray:
+    """cg_plan_batches_fused: batch end indices for cg_check_apply, setting
+    CG_CHECK_AFTER / CG_APPLY_AFTER in place (descs: contiguous DESC_DTYPE)"""
+    assert descs.dtype == DESC_DTYPE and descs.flags["C_CONTIGUOUS"]
+    cuts = np.zeros(max(len(descs), 1), np.uint64)
+    nc = ctypes.c_uint64(0)
+    st = _lib.cg_plan_batches_fused(descs.ctypes.data if len(descs) else None, len(descs), cuts.ctypes.data,
+                                    ctypes.byref(nc))
+    if st:
+        raise CgError(st, "cg_plan_batches_fused")
+    return cuts[: nc.value]
 
 
 def plan_apply_after(descs: np.ndarray) -> int:

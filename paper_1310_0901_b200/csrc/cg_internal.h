@@ -115,6 +115,8 @@ struct Plan {
                           // [3] memmove-list count, [4] deferred-list count, [5] deferred-list cursor
   uint32_t* resid;        // [n] fused check: DtoH descriptors left to the residual apply
   uint32_t* defer;        // [n] descriptors whose host side the deferred pass checks (R-10, R-12)
+  uint32_t* late;         // [n] CG_CHECK_AFTER descriptors, checked by k_finish after the applies
+                          // (count, cursor: counter[6], [7])
   uint64_t* dvoff;        // [2n] NEXT-1: device V offsets (dst, src) found by the last check
   uint64_t max_chunks;
   uint64_t t_min;

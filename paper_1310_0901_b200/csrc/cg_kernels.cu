@@ -831,7 +831,8 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
                                           cg_verdict* __restrict__ out, uint64_t* __restrict__ weight,
                                           ScanMeta* __restrict__ meta, uint64_t* __restrict__ dvoff,
                                           const ShadowView& sv, uint32_t* __restrict__ counter,
-                                          uint32_t* __restrict__ defer, uint64_t* s_split, uint32_t err_mask) {
+                                          uint32_t* __restrict__ defer, uint64_t* s_split, uint32_t err_mask,
+                                          int fuse, uint32_t* __restrict__ late) {
   // the scan's group counter and the apply count: reset here instead of by a
   // memset node, which would break the PDL chain.  The residual list (count:
   // counter[2]) and the deferred list (count, cursor: counter[4], [5]) are
@@ -903,9 +904,12 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
     // offset outside the window (initial first_unaddr: partials min into it)
     HostClip hc{0, 0, kNone, false};
     if (act && nm.host) hc = host_clip(nm, d.height, sv);
-    const bool deferred = act && nm.host && (hc.overlap || (sv.sparse && hc.ohi - hc.olo > kDeferBytes));
-    const uint64_t nscan = act && nm.host && !deferred ? hc.ohi - hc.olo : 0;
+    // CG_CHECK_AFTER (fused only): checked by k_finish after the batch's applies
+    const bool is_late = act && fuse && nm.host && nm.skind == CG_HTOD && (d.reserved & CG_CHECK_AFTER);
+    const bool deferred = act && nm.host && !is_late && (hc.overlap || (sv.sparse && hc.ohi - hc.olo > kDeferBytes));
+    const uint64_t nscan = act && nm.host && !deferred && !is_late ? hc.ohi - hc.olo : 0;
     if (deferred) defer[atomicAdd(counter + 4, 1u)] = (uint32_t)i;
+    if (is_late) late[atomicAdd(counter + 6, 1u)] = (uint32_t)i;
     const bool contig = d.height == 1 || d.width == nm.hpitch;
     const bool raw = d.reserved & CG_SHARD_RAW;   // partial of a straddler: no finalisation here
     // the small pass (bytes and dense 2-bit formats): contiguous, whole, not
@@ -933,7 +937,7 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
       m.W = nm.W;
       m.info = nscan | ((uint64_t)(nm.skind & 3u) << kInfoKind) | ((uint64_t)(nscan != 0) << kInfoHost) |
                ((uint64_t)contig << kInfoContig) | ((uint64_t)raw << kInfoRaw) |
-               ((uint64_t)(hc.pfu != kNone) << kInfoPfu) | ((uint64_t)(deferred || small) << kInfoDefer) |
+               ((uint64_t)(hc.pfu != kNone) << kInfoPfu) | ((uint64_t)(deferred || small || is_late) << kInfoDefer) |
                ((uint64_t)((d.reserved & CG_APPLY_AFTER) != 0) << kInfoAfter) | ((uint64_t)flags << kInfoFlags) |
                ((uint64_t)small << kInfoSmall);
       meta[i] = m;
@@ -1079,10 +1083,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_check_prep(const cg_copy_desc* 
                                                          ScanMeta* __restrict__ meta,
                                                          uint64_t* __restrict__ dvoff, ShadowView sv,
                                                          uint32_t* __restrict__ counter,
-                                                         uint32_t* __restrict__ defer, uint32_t err_mask) {
+                                                         uint32_t* __restrict__ defer, uint32_t err_mask, int fuse,
+                                                         uint32_t* __restrict__ late) {
   pdl_entry();
   extern __shared__ uint64_t s_split[];
-  prep_body(descs, n, t, out, weight, meta, dvoff, sv, counter, defer, s_split, err_mask);
+  prep_body(descs, n, t, out, weight, meta, dvoff, sv, counter, defer, s_split, err_mask, fuse, late);
 }
 
 // ---------------------------------------------------------------------------
@@ -1248,12 +1253,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_front(const cg_copy_desc* __res
                                                     ShadowView sv, uint32_t* __restrict__ counter,
                                                     uint32_t* __restrict__ defer, uint64_t* P,
                                                     uint64_t* __restrict__ bsum, uint64_t t_min, uint64_t max_chunks,
-                                                    uint32_t* __restrict__ chunk_first, uint32_t err_mask) {
+                                                    uint32_t* __restrict__ chunk_first, uint32_t err_mask, int fuse,
+                                                    uint32_t* __restrict__ late) {
   pdl_entry();
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   extern __shared__ uint64_t s_split[];
   __shared__ uint64_t s_warp[33];
-  prep_body(descs, n, t, out, weight, meta, dvoff, sv, counter, defer, s_split, err_mask);
+  prep_body(descs, n, t, out, weight, meta, dvoff, sv, counter, defer, s_split, err_mask, fuse, late);
   grid.sync();
   // block b owns items [b*per, (b+1)*per)
   const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
@@ -1797,13 +1803,16 @@ __device__ __noinline__ void defer_one(const cg_copy_desc* __restrict__ descs, u
   p.fd = warp_min(p.fd);
   p.cnt = warp_sum(p.cnt);
   if (lane == 0) {
-    const uint64_t info = meta[d].info;
+    // the prep's device / validation flags: from the scan record, or (meta ==
+    // nullptr, the late pass) from the verdict the prep wrote
     cg_verdict* v = out + d;
+    const bool raw = meta ? ((meta[d].info >> kInfoRaw) & 1u) : (dd.reserved & CG_SHARD_RAW) != 0;
+    const uint32_t flags0 = meta ? (uint32_t)((meta[d].info >> kInfoFlags) & 0x3FFu) : v->flags;
     v->first_unaddr = p.fu;
     v->first_undef = p.fd;
     v->undef_count = p.cnt;
-    if (!((info >> kInfoRaw) & 1u)) {   // a raw straddler partial is finalised after the merge
-      uint32_t flags = (uint32_t)(info >> kInfoFlags), status;
+    if (!raw) {   // a raw straddler partial is finalised after the merge
+      uint32_t flags = flags0, status;
       finalize_fields(flags, status, p.fu, p.cnt, err_mask);
       v->flags = flags;
       v->status = status;
@@ -2223,7 +2232,7 @@ __global__ void __launch_bounds__(kThreads) k_finish(
     const cg_copy_desc* __restrict__ descs, uint64_t n, uint64_t* P, uint64_t t_min, uint64_t max_chunks,
     cg_verdict* __restrict__ out, uint32_t err_mask, ScanMeta* meta, uint32_t* __restrict__ resid,
     uint32_t* counter, uint64_t* __restrict__ weight, uint64_t* __restrict__ bsum, uint32_t* __restrict__ chunk_first,
-    ShadowView sv) {
+    ShadowView sv, const uint32_t* __restrict__ late_list) {
   pdl_entry();
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   __shared__ __align__(128) uint8_t zeros[kZeroPage];
@@ -2252,7 +2261,7 @@ __global__ void __launch_bounds__(kThreads) k_finish(
   }
   grid.sync();
   const uint64_t m = __ldcg(resid_n);
-  if (m == 0) return;   // uniform: nothing left to apply (the count stays 0 for the next check)
+  if (m > 0) {   // uniform
   for (uint64_t k = tid; k < m; k += nthr) {   // residual records (k_apply_list_prep)
     const cg_copy_desc d = descs[resid[k]];
     const Norm nm = normalize(d);
@@ -2317,6 +2326,20 @@ __global__ void __launch_bounds__(kThreads) k_finish(
   zero_page(zeros);
   grid.sync();
   apply_body<kTwoBit>(meta, m, P, chunk_first, counter, t_min, max_chunks, sv, zeros);
+  }
+  // CG_CHECK_AFTER: the HtoD sides that read bytes an earlier DtoH of the batch
+  // wrote, checked now that every apply of the batch is done (warp per side)
+  const uint32_t nl = __ldcg(counter + 6);
+  if (nl == 0) return;   // uniform
+  asm volatile("fence.proxy.async.global;" ::: "memory");   // the residual apply's bulk stores, before generic loads
+  __threadfence();
+  grid.sync();
+  const int lane = threadIdx.x & 31;
+  (void)lane;
+  for (uint64_t k = tid >> 5; k < nl; k += nthr >> 5)   // the records in meta[] were reused above: flags from the verdict
+    defer_one(descs, late_list[k], nullptr, sv, out, err_mask, 0, resid, resid_n);
+  grid.sync();
+  if (tid == 0) counter[6] = counter[7] = 0;   // the next check's late list starts empty
 }
 
 // fill shard-relative V bytes [q0, q1) with the byte value `val` (0x00/0xFF)
@@ -3396,9 +3419,11 @@ static cudaError_t check_front(const Launch& L, const cg_copy_desc* d, uint64_t 
     uint64_t t_min = p.t_min, max_chunks = p.max_chunks;
     uint32_t* chunk_first = p.chunk_first;
     uint32_t em = err_mask;
+    int fu = fuse ? 1 : 0;
+    uint32_t* late = p.late;
     void* args[] = {(void*)&d, (void*)&n, (void*)&tc, (void*)&out, (void*)&weight, (void*)&meta, (void*)&dvoff,
                     (void*)&svc, (void*)&counter, (void*)&defer, (void*)&P, (void*)&bsum, (void*)&t_min,
-                    (void*)&max_chunks, (void*)&chunk_first, (void*)&em};
+                    (void*)&max_chunks, (void*)&chunk_first, (void*)&em, (void*)&fu, (void*)&late};
     const cudaError_t e =
         cudaLaunchCooperativeKernel((const void*)k_front, dim3((unsigned)L.front_blocks), dim3(kThreads), args, smem, s);
     *L.counter += 1;
@@ -3406,7 +3431,7 @@ static cudaError_t check_front(const Launch& L, const cg_copy_desc* d, uint64_t 
     if (e != cudaSuccess) return e;   // nothing after it may consume a stale plan
   } else {
     launch_pdl(k_check_prep, blocks_for(n, kThreads, L.num_sms * 4), kThreads, smem, s, d, n, t, out, p.weight, meta,
-               p.dvoff, sv, p.counter, p.defer, err_mask);
+               p.dvoff, sv, p.counter, p.defer, err_mask, fuse ? 1 : 0, p.late);
     *L.counter += 1;
     L.stage(CG_STAGE_CHECK_PREP, false, s);
     L.stage(CG_STAGE_CHECK_PLAN, true, s);
@@ -3460,9 +3485,10 @@ cudaError_t check_apply(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_v
   uint64_t* bsum = p.fbsum;
   uint32_t* chunk_first = p.chunk_first;
   ShadowView svc = sv;
+  const uint32_t* late = p.late;
   void* args[] = {(void*)&d, (void*)&n, (void*)&P, (void*)&t_min, (void*)&max_chunks, (void*)&out, (void*)&err_mask,
                   (void*)&meta, (void*)&resid, (void*)&counter, (void*)&weight, (void*)&bsum, (void*)&chunk_first,
-                  (void*)&svc};
+                  (void*)&svc, (void*)&late};
   e = cudaLaunchCooperativeKernel(sv.two_bit ? (const void*)k_finish<true> : (const void*)k_finish<false>,
                                               dim3((unsigned)L.finish_blocks), dim3(kThreads), args, 0, s);
   L.stage(CG_STAGE_APPLY, false, s);

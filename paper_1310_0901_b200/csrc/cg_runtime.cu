@@ -40,7 +40,7 @@ struct ArrayEntry {   // NEXT-3 device array (SPEC register_array S:166-168)
 };
 
 struct Layout {
-  uint64_t table, walk, patch, arrays, weight, P, bsum, fbsum, chunk, meta, resid, defer, dvoff, scratch, waves, ovl, marks, flags,
+  uint64_t table, walk, patch, arrays, weight, P, bsum, fbsum, chunk, meta, resid, defer, late, dvoff, scratch, waves, ovl, marks, flags,
       leaks,
       desc_stage, chunk_list,
       verdict_stage, raw_stage,
@@ -95,6 +95,7 @@ Layout layout_of(const cg_config* c) {
   L.meta = take(c->max_descs * std::max(cgk::scan_meta_bytes(), cgk::prop_meta_bytes()));
   L.resid = take(c->max_descs * sizeof(uint32_t));
   L.defer = take(c->max_descs * sizeof(uint32_t));
+  L.late = take(c->max_descs * sizeof(uint32_t));
   L.dvoff = c->dev_vbuf ? take(c->max_descs * 16) : 0;
   L.scratch = c->dev_vbuf ? take(cgk::stage_bytes()) : 0;
   L.waves = c->dev_vbuf ? take((c->max_descs + 1) * sizeof(uint32_t)) : 0;   // NEXT-1 wave offsets
@@ -274,6 +275,7 @@ struct cg_ctx {
     p.counter = reinterpret_cast<uint32_t*>(ws + lay.flags + 128);
     p.resid = reinterpret_cast<uint32_t*>(ws + lay.resid);
     p.defer = reinterpret_cast<uint32_t*>(ws + lay.defer);
+    p.late = reinterpret_cast<uint32_t*>(ws + lay.late);
     p.dvoff = cfg.dev_vbuf ? reinterpret_cast<uint64_t*>(ws + lay.dvoff) : nullptr;
     p.max_chunks = lay.max_chunks;
     p.t_min = kChunkMin;
@@ -1752,6 +1754,55 @@ cg_status cg_plan_batches_propagate(const cg_copy_desc* h_descs, uint64_t n, uin
     if (w_ok) W.add(wlo, whi);
   }
   if (n) h_cuts[k++] = n;
+  *n_cuts = k;
+  return CG_OK;
+}
+
+cg_status cg_plan_batches_fused(cg_copy_desc* h_descs, uint64_t n, uint64_t* h_cuts, uint64_t* n_cuts) {
+  if (!n_cuts || (n && (!h_descs || !h_cuts))) return CG_ERR_INVALID_VALUE;
+  constexpr uint64_t kLateMax = 1ull << 20;   // larger dependent HtoDs end the batch instead
+  IvSet dtoh, late;                            // the batch's DtoH ranges, its CG_CHECK_AFTER HtoD ranges
+  uint64_t k = 0, start = 0;
+  auto close = [&](uint64_t end) {   // CG_APPLY_AFTER over [start, end)
+    std::vector<cg_copy_desc> tmp(h_descs + start, h_descs + end);
+    uint64_t after = 0;
+    cg_plan_apply_after(tmp.data(), tmp.size(), &after);
+    for (uint64_t i = start; i < end; ++i)
+      h_descs[i].reserved = (h_descs[i].reserved & ~(uint32_t)CG_APPLY_AFTER) | (tmp[i - start].reserved & CG_APPLY_AFTER);
+  };
+  for (uint64_t i = 0; i < n; ++i) {
+    cg_copy_desc& d = h_descs[i];
+    d.reserved &= ~(uint32_t)(CG_CHECK_AFTER | CG_APPLY_AFTER);
+    uint64_t lo, hi;
+    if (!host_range(d, lo, hi)) continue;
+    if (reads_host(d.kind)) {
+      if (dtoh.overlaps(lo, hi)) {
+        if (hi - lo <= kLateMax) {
+          d.reserved |= CG_CHECK_AFTER;
+          late.add(lo, hi);
+        } else {   // too large for the late pass: a new batch (the classic R-20 cut)
+          close(i);
+          h_cuts[k++] = i;
+          start = i;
+          dtoh.m.clear();
+          late.m.clear();
+        }
+      }
+    } else {
+      if (late.overlaps(lo, hi)) {   // it would write bytes a CG_CHECK_AFTER HtoD must not see
+        close(i);
+        h_cuts[k++] = i;
+        start = i;
+        dtoh.m.clear();
+        late.m.clear();
+      }
+      dtoh.add(lo, hi);
+    }
+  }
+  if (n) {
+    close(n);
+    h_cuts[k++] = n;
+  }
   *n_cuts = k;
   return CG_OK;
 }

@@ -109,11 +109,25 @@ def replay_events(chk, events: np.ndarray, blob=None, stream=None, fuse: bool = 
                 pkg = __import__(__package__)
                 tracking = getattr(chk, "tracking", False)
                 # R-20 epochs for the check; with tracking, each epoch's V-bit
-                # propagation runs in the waves of cg_plan_waves (R-28)
-                cuts = [0] + [int(c) for c in pkg.plan_batches(descs)]
+                # propagation runs in the waves of cg_plan_waves (R-28); fused
+                # (cg_check_apply): the batches of cg_plan_batches_fused, which
+                # also sets CG_CHECK_AFTER / CG_APPLY_AFTER
+                fused_plan = fuse and fuse != "disjoint" and not tracking
+                descs = np.ascontiguousarray(descs)
+                parts = []   # (s0, s1): batches of at most max_descs copies
+                cuts = [0] + [int(c) for c in (pkg.plan_batches_fused(descs) if fused_plan
+                                                else pkg.plan_batches(descs))]
                 for a, b in zip(cuts[:-1], cuts[1:]):
                     for s0 in range(a, b, chk.max_descs):
                         s1 = min(b, s0 + chk.max_descs)
+                        if fused_plan and s1 - s0 < b - a:   # a piece of a fused batch: its own plan
+                            part = np.ascontiguousarray(descs[s0:s1])
+                            sub = [0] + [int(c) for c in pkg.plan_batches_fused(part)]
+                            descs[s0:s1] = part
+                            parts += [(s0 + c0, s0 + c1) for c0, c1 in zip(sub[:-1], sub[1:])]
+                        else:
+                            parts.append((s0, s1))
+                for s0, s1 in parts:
                         dd = to_device_descs(descs[s0:s1], chk.device)
                         if tracking:    # NEXT-1: check, then move V-bits wave by wave
                             dv = chk.check_copies(dd, stream=stream)
@@ -122,12 +136,7 @@ def replay_events(chk, events: np.ndarray, blob=None, stream=None, fuse: bool = 
                                 chk.apply_copies(dd, dv, stream=stream)
                             else:
                                 chk.apply_waves(dd, dv, waves, stream=stream)
-                        elif fuse and fuse != "disjoint":
-                            # any R-20 epoch fuses: DtoH ranges that an HtoD of the
-                            # batch also reads are applied after the scan (CG_APPLY_AFTER)
-                            part = np.ascontiguousarray(descs[s0:s1])
-                            pkg.plan_apply_after(part)
-                            dd = to_device_descs(part, chk.device)
+                        elif fused_plan:
                             dv = chk.check_apply(dd, stream=stream)
                         elif fuse and pkg.batch_disjoint(descs[s0:s1]):
                             dv = chk.check_apply(dd, stream=stream)
