@@ -342,3 +342,43 @@ def test_plan_apply_after(cg, seed):
     k = cg.plan_apply_after(descs)
     got = (descs["reserved"] & cg.CG_APPLY_AFTER) != 0
     assert list(got) == expect and k == sum(expect)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_plan_batches_fused(cg, seed):
+    """cg_plan_batches_fused: inside every batch, an HtoD whose host range
+    overlaps an earlier DtoH of the batch carries CG_CHECK_AFTER, no DtoH
+    overlaps an earlier CG_CHECK_AFTER HtoD of its batch, and CG_APPLY_AFTER
+    is exactly cg_plan_apply_after of the batch"""
+    tr = tg.random_tiny(seed + 22000) if seed % 2 else tg.random_medium(seed, n_copies=80)
+    descs = np.ascontiguousarray(tg.events_to_descs(tr.events[tr.events["op"] == tg.OP_COPY]))
+    cuts = [0] + [int(c) for c in cg.plan_batches_fused(descs)]
+    assert cuts[-1] == len(descs)
+
+    def hrange(d):
+        k = int(d["kind"])
+        if k not in (1, 2, 4, 5) or d["width"] == 0 or d["height"] == 0:
+            return None
+        p = "src" if k in (1, 4) else "dst"
+        s = int(d[p]) + int(d[p + "_y"]) * int(d[p + "_pitch"]) + int(d[p + "_x"])
+        e = s + (int(d["height"]) - 1) * int(d[p + "_pitch"]) + int(d["width"])
+        return None if e > (1 << 64) - 1 else (s, e)
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        writes, late = [], []
+        for d in descs[a:b]:
+            r = hrange(d)
+            k = int(d["kind"])
+            if r is None:
+                continue
+            if k in (1, 4):
+                dep = any(x < r[1] and r[0] < y for x, y in writes)
+                assert bool(d["reserved"] & cg.CG_CHECK_AFTER) == dep
+                if dep:
+                    late.append(r)
+            else:
+                assert not any(x < r[1] and r[0] < y for x, y in late)
+                writes.append(r)
+        part = np.ascontiguousarray(descs[a:b]).copy()
+        part["reserved"] &= ~np.uint32(cg.CG_APPLY_AFTER)
+        cg.plan_apply_after(part)
+        assert np.array_equal(part["reserved"] & cg.CG_APPLY_AFTER, descs["reserved"][a:b] & cg.CG_APPLY_AFTER)
