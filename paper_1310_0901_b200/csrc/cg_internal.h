@@ -97,7 +97,7 @@ struct Table {
   uint64_t na;
   uint32_t stride;   // splitter stride (every stride-th base is staged in smem)
   uint32_t nsplit;
-  uint32_t two_round64;   // stride 64: two independent-load rounds (env CG_LOOKUP64=0: binary search)
+  uint32_t two_round64;   // stride 64: two independent-load rounds (env CG_LOOKUP64=1; default: binary search)
 };
 
 // A planned pass over n weighted items: P = exclusive prefix sum of weights

@@ -306,9 +306,9 @@ struct cg_ctx {
     const uint64_t stride = split_stride(t.n);
     t.stride = (uint32_t)stride;
     t.nsplit = (uint32_t)((t.n + stride - 1) / stride);
-    static const bool two = [] {
+    static const bool two = [] {   // measured slower than the binary search for C5 (1.58 vs 1.45 ms): opt-in
       const char* e = getenv("CG_LOOKUP64");
-      return !(e && e[0] == '0');
+      return e && e[0] == '1';
     }();
     t.two_round64 = two ? 1u : 0u;
     return t;
