@@ -1081,6 +1081,23 @@ __global__ void __launch_bounds__(kThreads) k_check_small(const ScanMeta* __rest
         else apply_me = true;
       }
     }
+    // fused a6: a side of at most 512 bytes by its own lane (16-byte stores,
+    // byte stores at the edges), bigger ones by the whole warp
+    if (apply_me && q1 - q0 <= 512) {
+      if (kTwoBit) {
+        lane_fill2(sv.V, q0, q1, 0xAAAAAAAAu);
+      } else {
+        const uint64_t a0 = (q0 + 15) & ~15ull, a1 = q1 & ~15ull;
+        if (a0 >= a1) {
+          for (uint64_t q = q0; q < q1; ++q) sv.V[q] = 0;
+        } else {
+          for (uint64_t q = q0; q < a0; ++q) sv.V[q] = 0;
+          for (uint64_t q = a0; q < a1; q += 16) stg_val16(reinterpret_cast<uint4*>(sv.V + q), 0u);
+          for (uint64_t q = a1; q < q1; ++q) sv.V[q] = 0;
+        }
+      }
+      apply_me = false;
+    }
     uint32_t ap = __ballot_sync(kFull, apply_me);
     while (ap) {   // fused a6, the whole warp per side
       const int k = __ffs(ap) - 1;
