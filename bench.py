@@ -702,6 +702,7 @@ def run_interleaved(args, device):
         dl = torch.empty(max(nreg, 1) * 24, dtype=torch.uint8, device=device)
         dc = torch.zeros(1, dtype=torch.int64, device=device)
         torch.cuda.synchronize()
+        l0 = chk.kernel_launches
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t_reg = 0.0
         w0 = time.perf_counter()
@@ -719,7 +720,7 @@ def run_interleaved(args, device):
         torch.cuda.synchronize()
         wall = time.perf_counter() - w0
         ms = e0.elapsed_time(e1)
-        launches = chk.kernel_launches
+        launches = chk.kernel_launches - l0
         chk.close()
         return ms, wall, t_reg, launches
 

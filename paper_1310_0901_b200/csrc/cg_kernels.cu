@@ -757,6 +757,18 @@ __device__ __forceinline__ uint32_t lane_span(bool htod) {
 
 constexpr uint64_t kSmallMeanBytes = 4096;   // the small pass runs when a batch's mean side is smaller
 
+// after a check: the small pass for the next check iff this batch's host
+// sides averaged fewer than kSmallMeanBytes (counter[9] = 1; 2 = the ring
+// only); the statistics (counter[10..13], two u64) restart.  A stream of
+// similar batches (a program's calls, the bench's steps) is thus served by the
+// path that suits it from its second batch on; the result is the same either way.
+__device__ __forceinline__ void next_small_choice(uint32_t* counter) {
+  unsigned long long* st = reinterpret_cast<unsigned long long*>(counter + 10);
+  const uint64_t bytes = st[0], sides = st[1];
+  counter[9] = (sides && bytes < kSmallMeanBytes * sides) ? 1u : 2u;
+  st[0] = st[1] = 0;
+}
+
 struct SmallRound {
   uint4 x;      // HtoD: V bytes; DtoH: A bytes; 2-bit: states
   uint32_t a;   // HtoD: the A bits of the 16 V bytes
@@ -841,6 +853,7 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
   // appended to right here, so the kernels after the scan (k_finish,
   // k_finalize_split) reset them for the next check.
   if (blockIdx.x == 0 && threadIdx.x < 2) counter[threadIdx.x] = 0;
+  const bool small_on = *reinterpret_cast<volatile const uint32_t*>(counter + 9) == 1u;
   load_splitters(t, s_split);
   const int lane = threadIdx.x & 31;
   const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
@@ -918,7 +931,11 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
     // raw -- checked by k_check_small, not by the ring; its verdict is written
     // here already finalised as if the host side were clean (k_check_small
     // rewrites only the dirty ones)
-    const bool small = nscan != 0 && nscan <= sv.small_limit && contig && !raw && !sv.sparse;
+    // the small pass runs when the previous check's sides were small on average
+    // (counter[9] == 1, decided after each check from the statistics below:
+    // many descriptors with few bytes each, C5); else (C2) the ring checks the
+    // small sides too, their latency hidden behind the big tiles' streams
+    const bool small = nscan != 0 && nscan <= sv.small_limit && contig && !raw && !sv.sparse && small_on;
     {   // the adaptive choice (k_front): host bytes scanned and descriptors with host bytes, per batch
       uint64_t sum = nscan, cnt = nscan != 0;
 #pragma unroll
@@ -969,7 +986,7 @@ __global__ void __launch_bounds__(kThreads) k_check_small(const ScanMeta* __rest
                                                           uint32_t err_mask, int fuse, uint32_t* __restrict__ resid,
                                                           uint32_t* __restrict__ resid_n) {
   pdl_entry();
-  if (*reinterpret_cast<volatile const uint32_t*>(resid_n + 7) == 2u) return;   // counter[9]: k_front chose the ring
+  if (*reinterpret_cast<volatile const uint32_t*>(resid_n + 7) != 1u) return;   // counter[9]: the ring takes them all
   const int lane = threadIdx.x & 31;
   const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += nthr) {
@@ -1293,28 +1310,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_front(const cg_copy_desc* __res
   __shared__ uint64_t s_warp[33];
   prep_body(descs, n, t, out, weight, meta, dvoff, sv, counter, defer, s_split, err_mask, fuse, late);
   grid.sync();
-  if (sv.small_limit) {
-    // the small pass pays off when the batch's sides are small on average
-    // (many descriptors, few bytes each: C5); otherwise (C2) the ring checks
-    // the small sides too, their latency hidden behind the big tiles' streams:
-    // give them back their weight and clear their small bit
-    const uint64_t bytes = __ldcg(reinterpret_cast<const unsigned long long*>(counter + 10));
-    const uint64_t sides = __ldcg(reinterpret_cast<const unsigned long long*>(counter + 12));
-    const bool on = sides && bytes < kSmallMeanBytes * sides;
-    if (blockIdx.x == 0 && threadIdx.x == 0) counter[9] = on ? 1u : 2u;   // read by k_check_small
-    if (!on) {
-      for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t info = meta[i].info;
-        if (!((info >> kInfoSmall) & 1u)) continue;
-        meta[i].info = info & ~((1ull << kInfoSmall) | (1ull << kInfoDefer));
-        weight[i] = kItemCost + check_host_units((uint32_t)(info >> kInfoKind) & 3u, info & kInfoBytes, sv.two_bit != 0);
-        cg_verdict* v = out + i;   // the ring finalises it: back to the prep's unfinalised form
-        v->flags = (uint32_t)((info >> kInfoFlags) & 0x3FFu);
-        v->status = 0;
-      }
-    }
-    grid.sync();
-  }
+
   // block b owns items [b*per, (b+1)*per)
   const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
   const uint64_t lo = umin64(n, (uint64_t)blockIdx.x * per), hi = umin64(n, lo + per);
@@ -2018,8 +2014,7 @@ __global__ void __launch_bounds__(kThreads) k_finalize_split(uint64_t n, const u
   // so it cannot reset it itself); resid_n = counter + 2
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     resid_n[2] = resid_n[3] = 0;   // counter[4], [5]: the deferred list
-    resid_n[7] = 0;                // counter[9]: the small-pass choice, counter[10..13] its statistics
-    resid_n[8] = resid_n[9] = resid_n[10] = resid_n[11] = 0;
+    next_small_choice(resid_n - 2);
   }
   if (!fuse && blockIdx.x == 0 && threadIdx.x == 0) resid_n[0] = 0;   // nothing appends to the residual list unfused
   const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
@@ -2315,8 +2310,7 @@ __global__ void __launch_bounds__(kThreads) k_finish(
     if (tid == 0) {
       counter[0] = 0;   // the apply walk's group counter
       counter[4] = counter[5] = 0;   // the deferred list of the next check (the prep appends to it)
-      counter[9] = 0;   // the small-pass choice and its statistics (counter[10..13])
-      counter[10] = counter[11] = counter[12] = counter[13] = 0;
+      next_small_choice(counter);
     }
   }
   grid.sync();

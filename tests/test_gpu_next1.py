@@ -172,7 +172,7 @@ def test_self_overlapping_2d_beyond_staging(cg, monkeypatch, shift, wave_kernel)
     H0 = 1 << 24
     W, H = 8192, 4096                       # 32 MiB
     sp, dp = 8192 + 512, 8192 + 128         # unequal pitches: the rows interleave
-    tb = tg.TraceBuilder("mm32", H0, 64 << 20)
+    tb = tg.TraceBuilder("mm32", H0, 96 << 20)
     d = tb.malloc((H + 2) * sp + (1 << 16))
     n = (H - 1) * sp + W
     pat = rng.integers(0, 256, n, dtype=np.uint8)
