@@ -263,6 +263,27 @@ constexpr int kInfoKind = 40, kInfoHost = 42, kInfoContig = 43, kInfoRaw = 44, k
               kInfoAfter = 47, kInfoFlags = 48, kInfoSmall = 58;   // flags: 10 bits (48..57)
 constexpr uint64_t kInfoBytes = (1ull << 40) - 1;
 
+// The table's lines are kept in L2 against the descriptor / verdict streams of
+// the prep (which evict them otherwise: a 150k-entry table is a few MB, the
+// streams hundreds of MB): its loads carry an L2 evict_last policy.
+__device__ __forceinline__ uint64_t evict_last_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t ld_keep(const uint64_t* a, uint64_t pol) {
+  uint64_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint4 ld_keep4(const uint4* a, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(a), "l"(pol));
+  return v;
+}
+
 // ---------------------------------------------------------------------------
 // a3: batched interval search (lifetime-stamped, base-sorted table)
 // ---------------------------------------------------------------------------
@@ -274,6 +295,7 @@ constexpr uint64_t kInfoBytes = (1ull << 40) - 1;
 __device__ __forceinline__ bool table_lookup(const Table& t, const uint64_t* s_split, uint64_t start,
                                              uint64_t seq, uint64_t& end_out, uint64_t& idx_out) {
   if (t.nsplit == 0 || s_split[0] > start) return false;
+  const uint64_t pol = evict_last_policy();
   uint32_t lo = 0, hi = t.nsplit;
   while (hi - lo > 1) {
     uint32_t mid = (lo + hi) >> 1;
@@ -291,7 +313,7 @@ __device__ __forceinline__ bool table_lookup(const Table& t, const uint64_t* s_s
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       if (k >= nq) break;
-      const uint4 v = __ldg(q + k);
+      const uint4 v = ld_keep4(q + k, pol);
       c2 += (a + 8 * k < b && (((uint64_t)v.y << 32) | v.x) <= start) +
             (a + 8 * k + 4 < b && (((uint64_t)v.w << 32) | v.z) <= start);
     }
@@ -300,7 +322,7 @@ __device__ __forceinline__ bool table_lookup(const Table& t, const uint64_t* s_s
     uint32_t c1 = 0;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      const uint4 v = __ldg(r + k);
+      const uint4 v = ld_keep4(r + k, pol);
       c1 += (a1 + 2 * k < b && (((uint64_t)v.y << 32) | v.x) <= start) +
             (a1 + 2 * k + 1 < b && (((uint64_t)v.w << 32) | v.z) <= start);
     }
@@ -308,11 +330,11 @@ __device__ __forceinline__ bool table_lookup(const Table& t, const uint64_t* s_s
   } else {
     while (b - a > 1) {
       const uint64_t mid = (a + b) >> 1;
-      if (__ldg(t.base + mid) <= start) a = mid; else b = mid;
+      if (ld_keep(t.base + mid, pol) <= start) a = mid; else b = mid;
     }
   }
   for (int64_t j = (int64_t)a; j >= 0; --j) {
-    const uint4 w0 = __ldg(t.walk + 2 * j), w1 = __ldg(t.walk + 2 * j + 1);   // one 32-byte sector
+    const uint4 w0 = ld_keep4(t.walk + 2 * j, pol), w1 = ld_keep4(t.walk + 2 * j + 1, pol);   // one 32-byte sector
     const uint64_t pm = ((uint64_t)w0.y << 32) | w0.x, e = ((uint64_t)w0.w << 32) | w0.z;
     const uint64_t as = ((uint64_t)w1.y << 32) | w1.x, fs = ((uint64_t)w1.w << 32) | w1.z;
     if (pm <= start) break;
@@ -757,16 +779,17 @@ __device__ __forceinline__ uint32_t lane_span(bool htod) {
 
 constexpr uint64_t kSmallMeanBytes = 4096;   // the small pass runs when a batch's mean side is smaller
 
-// after a check: the small pass for the next check iff this batch's host
-// sides averaged fewer than kSmallMeanBytes (counter[9] = 1; 2 = the ring
-// only); the statistics (counter[10..13], two u64) restart.  A stream of
+// after a check: the small pass for the next check iff at least 80 % of this
+// batch's host sides had at most kSmallMeanBytes bytes (C5: ~90 %, C2: ~60 %)
+// (counter[9] = 1; 2 = the ring only); the statistics (counter[10..11]:
+// smalls << 32 | sides) restart.  A stream of
 // similar batches (a program's calls, the bench's steps) is thus served by the
 // path that suits it from its second batch on; the result is the same either way.
 __device__ __forceinline__ void next_small_choice(uint32_t* counter) {
   unsigned long long* st = reinterpret_cast<unsigned long long*>(counter + 10);
-  const uint64_t bytes = st[0], sides = st[1];
-  counter[9] = (sides && bytes < kSmallMeanBytes * sides) ? 1u : 2u;
-  st[0] = st[1] = 0;
+  const uint64_t sides = st[0] & 0xFFFFFFFFull, smalls = st[0] >> 32;   // <= 2^24 each (kMaxDescs)
+  counter[9] = (sides && 10 * smalls >= 8 * sides) ? 1u : 2u;   // at least 80 % of the sides small
+  st[0] = 0;
 }
 
 struct SmallRound {
@@ -936,17 +959,12 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
     // many descriptors with few bytes each, C5); else (C2) the ring checks the
     // small sides too, their latency hidden behind the big tiles' streams
     const bool small = nscan != 0 && nscan <= sv.small_limit && contig && !raw && !sv.sparse && small_on;
-    {   // the adaptive choice (k_front): host bytes scanned and descriptors with host bytes, per batch
-      uint64_t sum = nscan, cnt = nscan != 0;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        sum += __shfl_xor_sync(kFull, sum, o);
-        cnt += __shfl_xor_sync(kFull, cnt, o);
-      }
-      if (lane == 0 && cnt) {
-        atomicAdd(reinterpret_cast<unsigned long long*>(counter + 10), (unsigned long long)sum);
-        atomicAdd(reinterpret_cast<unsigned long long*>(counter + 12), (unsigned long long)cnt);
-      }
+    {   // the statistics of the small-pass choice: host sides, and those of at most kSmallMeanBytes
+      const uint32_t sides = __popc(__ballot_sync(kFull, nscan != 0));
+      const uint32_t smalls = __popc(__ballot_sync(kFull, nscan != 0 && nscan <= kSmallMeanBytes));
+      if (lane == 0 && sides)
+        atomicAdd(reinterpret_cast<unsigned long long*>(counter + 10),
+                  ((unsigned long long)smalls << 32) | (unsigned long long)sides);
     }
     if (act) {
       cg_verdict v;
