@@ -26,7 +26,8 @@ def stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or stale():
-        cmd = [NVCC] + FLAGS + ["-o", LIB] + SOURCES
+        extra = os.environ.get("CG_NVCC_EXTRA", "").split()   # tuning experiments (-D...)
+        cmd = [NVCC] + FLAGS + extra + ["-o", LIB] + SOURCES
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

@@ -998,8 +998,14 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
 // a dirty verdict is rewritten, a clean one was final already (the prep
 // wrote it); small DtoH sides with status OK are applied here when fused (a6)
 // unless CG_APPLY_AFTER sends them to the residual pass.
+#ifndef CG_SMALL_MINB
+#define CG_SMALL_MINB 1
+#endif
+#ifndef CG_TINY_UNROLL
+#define CG_TINY_UNROLL 4
+#endif
 template <bool kTwoBit>
-__global__ void __launch_bounds__(kThreads) k_check_small(const ScanMeta* __restrict__ meta, uint64_t n,
+__global__ void __launch_bounds__(kThreads, CG_SMALL_MINB) k_check_small(const ScanMeta* __restrict__ meta, uint64_t n,
                                                           ShadowView sv, cg_verdict* __restrict__ out,
                                                           uint32_t err_mask, int fuse, uint32_t* __restrict__ resid,
                                                           uint32_t* __restrict__ resid_n) {
@@ -1039,12 +1045,12 @@ __global__ void __launch_bounds__(kThreads) k_check_small(const ScanMeta* __rest
         Partial tp{kNone, kNone, 0};
         while (__any_sync(kFull, tiny && g < q1)) {
           if (tiny && g < q1) {
-            SmallRound u[4];
+            SmallRound u[CG_TINY_UNROLL];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) u[k] = small_load<kTwoBit>(sv, g + k * span, q1, htod);
+            for (int k = 0; k < CG_TINY_UNROLL; ++k) u[k] = small_load<kTwoBit>(sv, g + k * span, q1, htod);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) small_fold<kTwoBit>(u[k], g + k * span, q0, q1, ob, htod, tp);
-            g += 4 * span;
+            for (int k = 0; k < CG_TINY_UNROLL; ++k) small_fold<kTwoBit>(u[k], g + k * span, q0, q1, ob, htod, tp);
+            g += CG_TINY_UNROLL * span;
           }
         }
         if (tiny) mine = tp;
