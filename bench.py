@@ -278,8 +278,9 @@ def run_ours(args, rank, world, device, config=None, steps=None, warmup=None, e2
     # fused (cg_check_apply): the batches of cg_plan_batches_fused, which marks
     # the DtoH copies an HtoD of their batch reads CG_APPLY_AFTER and the HtoD
     # copies that read an earlier DtoH's bytes CG_CHECK_AFTER, so that a DtoH ->
-    # HtoD ping-pong no longer ends the batch; unfused / tracking: the R-20
-    # epochs of cg_plan_batches (host planning, untimed)
+    # HtoD ping-pong no longer ends the batch (a DtoH that then writes such an
+    # HtoD's bytes is applied after the late checks, CG_APPLY_LAST); unfused /
+    # tracking: the R-20 epochs of cg_plan_batches (host planning, untimed)
     fused = not args.unfused and not args.track
     descs = np.ascontiguousarray(descs)
     cuts = [0] + [int(c) for c in (cg.plan_batches_fused(descs) if fused else cg.plan_batches(descs))]
@@ -287,6 +288,7 @@ def run_ours(args, rank, world, device, config=None, steps=None, warmup=None, e2
     efused = [fused for _ in epochs]
     n_after = int(np.count_nonzero(descs["reserved"] & cg.CG_APPLY_AFTER))
     n_late = int(np.count_nonzero(descs["reserved"] & cg.CG_CHECK_AFTER))
+    n_last = int(np.count_nonzero(descs["reserved"] & cg.CG_APPLY_LAST))
     d_descs = cg.to_device_descs(descs, device)
     waves = []   # NEXT-1: per epoch, the device index lists of its propagation waves (cg_plan_waves)
     t_waves = 0.0
@@ -481,6 +483,7 @@ def run_ours(args, rank, world, device, config=None, steps=None, warmup=None, e2
                              "cg_check_apply (fused)" if fused else "cg_check_copies + cg_apply_dtoh"
                              if not any(efused) else "cg_check_apply / cg_check_copies + cg_apply_dtoh per epoch"),
                    "epochs": len(epochs), "apply_after_descriptors": n_after, "check_after_descriptors": n_late,
+                   "apply_last_descriptors": n_last,
                    "propagation_waves": sum(w.n_waves for w in waves) if args.track else None,
                    "wave_planning_s": t_waves if args.track else None},
         "descriptors_per_s": world * n / (ms_step * 1e-3),

@@ -108,7 +108,13 @@ enum {
  *    shard writes only its raw partial (first_unaddr, first_undef, undef_count,
  *    device fields, flags without HOST_*; status 0) for cg_straddler_pack /
  *    cg_straddler_finalize after the collective merge. */
-enum { CG_SHARD_NOT_OWNER = 1u << 0, CG_SHARD_RAW = 1u << 1, CG_APPLY_AFTER = 1u << 2, CG_CHECK_AFTER = 1u << 3 };
+enum {
+  CG_SHARD_NOT_OWNER = 1u << 0,
+  CG_SHARD_RAW = 1u << 1,
+  CG_APPLY_AFTER = 1u << 2,
+  CG_CHECK_AFTER = 1u << 3,
+  CG_APPLY_LAST = 1u << 4
+};
 /* CG_CHECK_AFTER (cg_check_apply only): this HTOD / HTOA descriptor reads host
  * bytes that an earlier DTOH / ATOH of the same batch writes, so it is
  * checked after every apply of the batch (no later DTOH / ATOH of the batch
@@ -119,6 +125,11 @@ enum { CG_SHARD_NOT_OWNER = 1u << 0, CG_SHARD_RAW = 1u << 1, CG_APPLY_AFTER = 1u
  * batch, so its apply waits until every check of the batch has read the
  * shadow (the residual pass) instead of running inside the scan.  Set by
  * cg_plan_apply_after. */
+/* CG_APPLY_LAST (cg_check_apply only): this DTOH / ATOH descriptor writes host
+ * bytes that an earlier CG_CHECK_AFTER HTOD of the same batch reads, so its
+ * apply runs after the CG_CHECK_AFTER checks (no later HTOD of the batch may
+ * read its range).  Set by cg_plan_batches_fused; cg_check_copies (and the
+ * sharded path) treat it as CG_APPLY_AFTER. */
 
 typedef struct {
   uint32_t kind;       /* CG_HTOD / CG_DTOH / CG_DTOD / CG_HTOA / CG_ATOH */
@@ -687,10 +698,11 @@ cg_status cg_plan_batches(const cg_copy_desc *h_descs, uint64_t n, uint64_t *h_c
 /* Batches for cg_check_apply (fused), in place: like cg_plan_batches, but an
  * HtoD that reads bytes an earlier DtoH of the batch writes does not end the
  * batch: it gets CG_CHECK_AFTER (checked after the batch's applies) when its
- * host range is at most 1 MiB; a DtoH that writes bytes of such an HtoD ends
- * the batch (so every CG_CHECK_AFTER descriptor sees exactly the applies of
- * the DtoH copies before it); every DtoH whose range an HtoD of its batch
- * reads gets CG_APPLY_AFTER.  The result of cg_check_apply over each batch
+ * host range is at most 1 MiB; a DtoH that writes bytes of such an HtoD gets
+ * CG_APPLY_LAST (applied after the CG_CHECK_AFTER checks, so every one of them
+ * sees exactly the applies of the DtoH copies before it), and an HtoD that
+ * reads bytes of a CG_APPLY_LAST DtoH ends the batch; every other DtoH whose
+ * range an HtoD of its batch reads gets CG_APPLY_AFTER.  The result of cg_check_apply over each batch
  * equals the sequential replay.  Writes the end of every batch to h_cuts (the
  * last is n), their number to *n_cuts.  Errors: CG_ERR_INVALID_VALUE on NULL. */
 cg_status cg_plan_batches_fused(cg_copy_desc *h_descs, uint64_t n, uint64_t *h_cuts, uint64_t *n_cuts);

@@ -178,7 +178,7 @@ CG_SHADOW_BYTES, CG_SHADOW_2BIT, CG_SHADOW_SPARSE = 0, 1, 2
 CG_FMT_2D, CG_FMT_1D = 0, 1
 COPY1D_DTYPE = np.dtype([("kind", "<u4"), ("reserved", "<u4"), ("seq", "<u8"), ("dst", "<u8"), ("src", "<u8"),
                          ("bytes", "<u8")])
-CG_SHARD_NOT_OWNER, CG_SHARD_RAW, CG_APPLY_AFTER, CG_CHECK_AFTER = 1, 2, 4, 8
+CG_SHARD_NOT_OWNER, CG_SHARD_RAW, CG_APPLY_AFTER, CG_CHECK_AFTER, CG_APPLY_LAST = 1, 2, 4, 8, 16
 CG_COMM_NCCL, CG_COMM_LOOPBACK = 0, 1
 CG_NCCL_ID_BYTES = 128
 CG_REG_ALLOC, CG_REG_FREE = 1, 2
@@ -288,7 +288,7 @@ def batch_disjoint(descs: np.ndarray) -> bool:
 
 def plan_batches_fused(descs: np.ndarray) -> np.ndarray:
     """cg_plan_batches_fused: batch end indices for cg_check_apply, setting
-    CG_CHECK_AFTER / CG_APPLY_AFTER in place (descs: contiguous DESC_DTYPE)"""
+    CG_CHECK_AFTER / CG_APPLY_AFTER / CG_APPLY_LAST in place (descs: contiguous DESC_DTYPE)"""
     assert descs.dtype == DESC_DTYPE and descs.flags["C_CONTIGUOUS"]
     cuts = np.zeros(max(len(descs), 1), np.uint64)
     nc = ctypes.c_uint64(0)

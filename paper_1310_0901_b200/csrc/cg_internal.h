@@ -116,6 +116,7 @@ struct Plan {
   uint32_t* resid;        // [n] fused check: DtoH descriptors left to the residual apply
   uint32_t* defer;        // [n] descriptors whose host side the deferred pass checks (R-10, R-12)
   uint32_t* late;         // [n] CG_CHECK_AFTER descriptors, checked by k_finish after the applies
+  uint32_t* last;         // [n] CG_APPLY_LAST DtoH descriptors, applied by k_finish after the late checks
                           // (count, cursor: counter[6], [7])
   uint64_t* dvoff;        // [2n] NEXT-1: device V offsets (dst, src) found by the last check
   uint64_t max_chunks;

@@ -260,7 +260,8 @@ struct __align__(16) ScanMeta {
 // small pass) << 46 | apply after the scan (CG_APPLY_AFTER) << 47 | flags << 48
 // | small pass << 58
 constexpr int kInfoKind = 40, kInfoHost = 42, kInfoContig = 43, kInfoRaw = 44, kInfoPfu = 45, kInfoDefer = 46,
-              kInfoAfter = 47, kInfoFlags = 48, kInfoSmall = 58;   // flags: 10 bits (48..57)
+              kInfoAfter = 47, kInfoFlags = 48, kInfoSmall = 58,   // flags: 10 bits (48..57)
+              kInfoLast = 59;
 constexpr uint64_t kInfoBytes = (1ull << 40) - 1;
 
 // The table's lines are kept in L2 against the descriptor / verdict streams of
@@ -407,7 +408,8 @@ constexpr uint32_t kTileA = kTileV / 8;
 constexpr uint32_t kHtodShift = 12, kDtohShift = 15, k2bitShift = 14;
 constexpr uint32_t kGrab = 4;          // chunks per group while the plan is far from its end
 constexpr uint32_t kTileData = 1, kTileHtod = 2, kTileEnd = 4, kTileWhole = 8, kTileFuse = 16, kTileRaw = 32,
-                   kTileAfter = 64;   // CG_APPLY_AFTER: a DtoH piece the residual pass applies
+                   kTileAfter = 64,   // CG_APPLY_AFTER: a DtoH piece the residual pass applies
+                   kTileLast = 128;   // CG_APPLY_LAST: ... which k_finish applies after the late checks
 
 struct __align__(16) TileInfo {
   uint64_t ob;        // logical offset of staged host byte 0
@@ -943,7 +945,11 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
     HostClip hc{0, 0, kNone, false};
     if (act && nm.host) hc = host_clip(nm, d.height, sv);
     // CG_CHECK_AFTER (fused only): checked by k_finish after the batch's applies
-    const bool is_late = act && fuse && nm.host && nm.skind == CG_HTOD && (d.reserved & CG_CHECK_AFTER);
+    // (fuse == 2: cg_check_apply, whose k_finish runs the late pass and the
+    // CG_APPLY_LAST applies after it; fuse == 1 treats CG_APPLY_LAST as CG_APPLY_AFTER)
+    const bool is_late = act && fuse == 2 && nm.host && nm.skind == CG_HTOD && (d.reserved & CG_CHECK_AFTER);
+    const bool is_last = act && fuse == 2 && nm.host && nm.skind == CG_DTOH && (d.reserved & CG_APPLY_LAST);
+    const bool is_after = (d.reserved & (CG_APPLY_AFTER | CG_APPLY_LAST)) != 0;
     const bool deferred = act && nm.host && !is_late && (hc.overlap || (sv.sparse && hc.ohi - hc.olo > kDeferBytes));
     const uint64_t nscan = act && nm.host && !deferred && !is_late ? hc.ohi - hc.olo : 0;
     if (deferred) defer[atomicAdd(counter + 4, 1u)] = (uint32_t)i;
@@ -987,11 +993,20 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
       m.info = nscan | ((uint64_t)(nm.skind & 3u) << kInfoKind) | ((uint64_t)(nscan != 0) << kInfoHost) |
                ((uint64_t)contig << kInfoContig) | ((uint64_t)raw << kInfoRaw) |
                ((uint64_t)(hc.pfu != kNone) << kInfoPfu) | ((uint64_t)(deferred || small || is_late) << kInfoDefer) |
-               ((uint64_t)((d.reserved & CG_APPLY_AFTER) != 0) << kInfoAfter) | ((uint64_t)flags << kInfoFlags) |
-               ((uint64_t)small << kInfoSmall);
+               ((uint64_t)is_after << kInfoAfter) | ((uint64_t)flags << kInfoFlags) |
+               ((uint64_t)small << kInfoSmall) | ((uint64_t)is_last << kInfoLast);
       meta[i] = m;
     }
   }
+}
+
+// a DtoH side with status OK that a later pass applies: a CG_APPLY_LAST one to
+// the last list (count counter[8] = resid_n[6]; k_finish applies it after the
+// late checks), any other to the residual list (count counter[2] = resid_n[0])
+__device__ __forceinline__ void push_apply(bool is_last, uint32_t d, uint32_t* __restrict__ resid,
+                                           uint32_t* __restrict__ resid_n, uint32_t* __restrict__ last) {
+  if (is_last) last[atomicAdd(resid_n + 6, 1u)] = d;
+  else resid[atomicAdd(resid_n, 1u)] = d;
 }
 
 // The small pass (a4-a6 for small contiguous host sides; see small_load):
@@ -1008,7 +1023,7 @@ template <bool kTwoBit>
 __global__ void __launch_bounds__(kThreads, CG_SMALL_MINB) k_check_small(const ScanMeta* __restrict__ meta, uint64_t n,
                                                           ShadowView sv, cg_verdict* __restrict__ out,
                                                           uint32_t err_mask, int fuse, uint32_t* __restrict__ resid,
-                                                          uint32_t* __restrict__ resid_n) {
+                                                          uint32_t* __restrict__ resid_n, uint32_t* __restrict__ last) {
   pdl_entry();
   if (*reinterpret_cast<volatile const uint32_t*>(resid_n + 7) != 1u) return;   // counter[9]: the ring takes them all
   const int lane = threadIdx.x & 31;
@@ -1118,7 +1133,7 @@ __global__ void __launch_bounds__(kThreads, CG_SMALL_MINB) k_check_small(const S
         v->status = status;
       }
       if (fuse && !htod && status == CG_OK) {
-        if ((info >> kInfoAfter) & 1u) resid[atomicAdd(resid_n, 1u)] = (uint32_t)i;
+        if ((info >> kInfoAfter) & 1u) push_apply((info >> kInfoLast) & 1u, (uint32_t)i, resid, resid_n, last);
         else apply_me = true;
       }
     }
@@ -1532,7 +1547,7 @@ struct TileGen {
         if ((f & kPieceWhole) && ((m_info >> kInfoRaw) & 1u)) {
           v->first_unaddr = p_fu;   // raw partial (straddler): finalised after the merge
         } else if (f & kPieceWhole) {
-          uint32_t flags = (uint32_t)(m_info >> kInfoFlags), status;
+          uint32_t flags = (uint32_t)((m_info >> kInfoFlags) & 0x3FFu), status;
           finalize_fields(flags, status, p_fu, 0, err_mask);
           v->first_unaddr = p_fu;
           v->flags = flags;
@@ -1547,6 +1562,7 @@ struct TileGen {
     set_segment(live, p_qs, p_qe, p_ob, p_fu, (uint32_t)(wbase + lane),
                 (p_fl & kPieceHtod ? kTileHtod : 0u) | (p_fl & kPieceWhole ? kTileWhole : 0u) | kSegEndLast |
                     (((m_info >> kInfoRaw) & 1u) ? kTileRaw : 0u) | (((m_info >> kInfoAfter) & 1u) ? kTileAfter : 0u) |
+                    (((m_info >> kInfoLast) & 1u) ? kTileLast : 0u) |
                     ((uint32_t)((m_info >> kInfoFlags) & 0x3FFu) << 16));
     phase = kPhaseContig;
   }
@@ -1646,7 +1662,8 @@ struct TileGen {
           const uint64_t info = __shfl_sync(kFull, m_info, src);
           d2 = (uint32_t)(wbase + src);
           fl2 = (pf & kPieceHtod ? kTileHtod : 0u) | (pf & kPieceWhole ? kTileWhole : 0u) |
-                (((info >> kInfoRaw) & 1u) ? kTileRaw : 0u) | ((uint32_t)(info >> kInfoFlags) << 16);
+                (((info >> kInfoRaw) & 1u) ? kTileRaw : 0u) | (((info >> kInfoLast) & 1u) ? kTileLast : 0u) |
+                ((uint32_t)((info >> kInfoFlags) & 0x3FFu) << 16);
           r2 = lo2 / W;
           fu2 = __shfl_sync(kFull, p_fu, src);
           in2d = true;
@@ -1838,7 +1855,8 @@ __device__ __forceinline__ uint64_t gap_offset(const DeferSide& s, uint64_t y, u
 __device__ __noinline__ void defer_one(const cg_copy_desc* __restrict__ descs, uint32_t d,
                                        const ScanMeta* __restrict__ meta, const ShadowView& sv,
                                        cg_verdict* __restrict__ out, uint32_t err_mask, int fuse,
-                                       uint32_t* __restrict__ resid, uint32_t* __restrict__ resid_n) {
+                                       uint32_t* __restrict__ resid, uint32_t* __restrict__ resid_n,
+                                       uint32_t* __restrict__ last) {
   const int lane = threadIdx.x & 31;
   const cg_copy_desc dd = descs[d];
   const Norm nm = normalize(dd);
@@ -1890,7 +1908,8 @@ __device__ __noinline__ void defer_one(const cg_copy_desc* __restrict__ descs, u
       finalize_fields(flags, status, p.fu, p.cnt, err_mask);
       v->flags = flags;
       v->status = status;
-      if (fuse && status == CG_OK && !s.htod) resid[atomicAdd(resid_n, 1u)] = d;   // the residual pass applies it
+      if (fuse && status == CG_OK && !s.htod)   // the residual (or, CG_APPLY_LAST, the last) pass applies it
+        push_apply(meta && ((meta[d].info >> kInfoLast) & 1u), d, resid, resid_n, last);
     }
   }
   __syncwarp();
@@ -1900,7 +1919,8 @@ __device__ __noinline__ void defer_one(const cg_copy_desc* __restrict__ descs, u
 __device__ __noinline__ void defer_tail(const cg_copy_desc* __restrict__ descs, const uint32_t* __restrict__ defer,
                                         uint32_t* counter, const ScanMeta* __restrict__ meta, const ShadowView& sv,
                                         cg_verdict* __restrict__ out, uint32_t err_mask, int fuse,
-                                        uint32_t* __restrict__ resid, uint32_t* __restrict__ resid_n) {
+                                        uint32_t* __restrict__ resid, uint32_t* __restrict__ resid_n,
+                                        uint32_t* __restrict__ last) {
   const int lane = threadIdx.x & 31;
   const uint32_t n = *reinterpret_cast<volatile uint32_t*>(counter + 4);   // final: written by the prep
   while (true) {
@@ -1908,7 +1928,7 @@ __device__ __noinline__ void defer_tail(const cg_copy_desc* __restrict__ descs, 
     if (lane == 0) k = atomicAdd(counter + 5, 1u);
     k = __shfl_sync(kFull, k, 0);
     if (k >= n) break;
-    defer_one(descs, defer[k], meta, sv, out, err_mask, fuse, resid, resid_n);
+    defer_one(descs, defer[k], meta, sv, out, err_mask, fuse, resid, resid_n, last);
   }
 }
 
@@ -1920,7 +1940,8 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
     const ScanMeta* __restrict__ meta, uint64_t n, const uint64_t* __restrict__ P,
     const uint32_t* __restrict__ chunk_first, uint32_t* counter, uint64_t t_min, uint64_t max_chunks,
     ShadowView sv, cg_verdict* __restrict__ out, uint32_t err_mask, int fuse, uint32_t* __restrict__ resid,
-    uint32_t* __restrict__ resid_n, const cg_copy_desc* __restrict__ descs, const uint32_t* __restrict__ defer) {
+    uint32_t* __restrict__ resid_n, const cg_copy_desc* __restrict__ descs, const uint32_t* __restrict__ defer,
+    uint32_t* __restrict__ last) {
   pdl_entry();
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -2005,7 +2026,8 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
           v->status = status;
           apply = (t.flags & kTileFuse) && status == CG_OK;
           // a whole 2D DtoH piece with status OK: the residual pass applies it
-          if (kFuse && !(t.flags & (kTileFuse | kTileHtod)) && status == CG_OK) resid[atomicAdd(resid_n, 1u)] = t.d;
+          if (kFuse && !(t.flags & (kTileFuse | kTileHtod)) && status == CG_OK)
+            push_apply(t.flags & kTileLast, t.d, resid, resid_n, last);
         } else {
           if (p.fu != kNone) atomicMin(reinterpret_cast<unsigned long long*>(&v->first_unaddr), p.fu);
           if (p.fd != kNone) atomicMin(reinterpret_cast<unsigned long long*>(&v->first_undef), p.fd);
@@ -2022,7 +2044,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
     __syncwarp();
     if (!gen.next(ring, s, sv, policy)) --left;
   }
-  defer_tail(descs, defer, counter, meta, sv, out, err_mask, kFuse ? 1 : 0, resid, resid_n);
+  defer_tail(descs, defer, counter, meta, sv, out, err_mask, kFuse ? 1 : 0, resid, resid_n, last);
 }
 
 
@@ -2297,6 +2319,24 @@ __global__ void __launch_bounds__(kThreads) k_apply(const ScanMeta* __restrict__
   apply_body<kTwoBit>(meta, n, P, chunk_first, counter, t_min, max_chunks, sv, zeros);
 }
 
+// a6 for one whole DtoH descriptor with the whole warp, row by row (R-11),
+// clipped to the shard: its host bytes become defined (CG_APPLY_LAST; rare,
+// so plain generic stores and no plan)
+template <bool kTwoBit>
+__device__ __noinline__ void apply_whole(const cg_copy_desc d, const ShadowView& sv) {
+  const Norm nm = normalize(d);
+  const bool contig = d.height == 1 || d.width == nm.hpitch;
+  const uint64_t rows = contig ? 1 : d.height, len = contig ? nm.nbytes : nm.W;
+  for (uint64_t r = 0; r < rows && len; ++r) {
+    const uint64_t x = nm.hstart + r * nm.hpitch;
+    if (x >= sv.se) break;   // rows ascend (pitch >= 0)
+    const uint64_t y0 = umax64(x, sv.sb), y1 = umin64(x + len, sv.se);
+    if (y0 >= y1) continue;
+    if (kTwoBit) fill2_any<true>(sv, y0 - sv.sb, y1 - sv.sb, 0xAAAAAAAAu);
+    else warp_store_zero(sv.V, y0 - sv.sb, y1 - sv.sb);
+  }
+}
+
 // cg_check_apply's tail in one cooperative launch (after the fused scan):
 // finalise split descriptors (k_finalize_split), then -- only if the scan or
 // the finalisation left a residual DtoH list (split or 2D pieces) -- its
@@ -2309,7 +2349,7 @@ __global__ void __launch_bounds__(kThreads) k_finish(
     const cg_copy_desc* __restrict__ descs, uint64_t n, uint64_t* P, uint64_t t_min, uint64_t max_chunks,
     cg_verdict* __restrict__ out, uint32_t err_mask, ScanMeta* meta, uint32_t* __restrict__ resid,
     uint32_t* counter, uint64_t* __restrict__ weight, uint64_t* __restrict__ bsum, uint32_t* __restrict__ chunk_first,
-    ShadowView sv, const uint32_t* __restrict__ late_list) {
+    ShadowView sv, const uint32_t* __restrict__ late_list, uint32_t* __restrict__ last_list) {
   pdl_entry();
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   __shared__ __align__(128) uint8_t zeros[kZeroPage];
@@ -2329,7 +2369,7 @@ __global__ void __launch_bounds__(kThreads) k_finish(
       v->flags = flags;
       v->status = status;
       if (status == CG_OK && ((info >> kInfoKind) & 3u) == CG_DTOH && ((info >> kInfoHost) & 1u))
-        resid[atomicAdd(resid_n, 1u)] = (uint32_t)d;
+        push_apply((info >> kInfoLast) & 1u, (uint32_t)d, resid, resid_n, last_list);
     }
     if (tid == 0) {
       counter[0] = 0;   // the apply walk's group counter
@@ -2406,18 +2446,21 @@ __global__ void __launch_bounds__(kThreads) k_finish(
   apply_body<kTwoBit>(meta, m, P, chunk_first, counter, t_min, max_chunks, sv, zeros);
   }
   // CG_CHECK_AFTER: the HtoD sides that read bytes an earlier DtoH of the batch
-  // wrote, checked now that every apply of the batch is done (warp per side)
-  const uint32_t nl = __ldcg(counter + 6);
-  if (nl == 0) return;   // uniform
+  // wrote, checked now that every apply of the batch is done (warp per side);
+  // then the CG_APPLY_LAST DtoH sides, which write bytes such an HtoD reads
+  const uint32_t nl = __ldcg(counter + 6), nz = __ldcg(counter + 8);   // final since the first barrier
+  if (nl == 0 && nz == 0) return;   // uniform
   asm volatile("fence.proxy.async.global;" ::: "memory");   // the residual apply's bulk stores, before generic loads
   __threadfence();
   grid.sync();
-  const int lane = threadIdx.x & 31;
-  (void)lane;
   for (uint64_t k = tid >> 5; k < nl; k += nthr >> 5)   // the records in meta[] were reused above: flags from the verdict
-    defer_one(descs, late_list[k], nullptr, sv, out, err_mask, 0, resid, resid_n);
+    defer_one(descs, late_list[k], nullptr, sv, out, err_mask, 0, resid, resid_n, last_list);
+  if (nz) {   // uniform
+    grid.sync();   // every late check has read the shadow
+    for (uint64_t k = tid >> 5; k < nz; k += nthr >> 5) apply_whole<kTwoBit>(descs[last_list[k]], sv);
+  }
   grid.sync();
-  if (tid == 0) counter[6] = counter[7] = 0;   // the next check's late list starts empty
+  if (tid == 0) counter[6] = counter[7] = counter[8] = 0;   // the next check's late and last lists start empty
 }
 
 // fill shard-relative V bytes [q0, q1) with the byte value `val` (0x00/0xFF)
@@ -3481,7 +3524,9 @@ static cudaError_t plan(const Launch& L, uint64_t n, const Plan& p, cudaStream_t
 
 // a1-a4: prep, plan and the shadow scan
 static cudaError_t check_front(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out, const Table& t,
-                        const ShadowView& sv, const Plan& p, uint32_t err_mask, bool fuse, cudaStream_t s) {
+                        const ShadowView& sv, const Plan& p, uint32_t err_mask, int fuse, cudaStream_t s) {
+  // fuse: 0 check only, 1 fused scan (cg_check_copies' fused form), 2 cg_check_apply
+  // (k_finish runs the CG_CHECK_AFTER checks and the CG_APPLY_LAST applies)
   const size_t smem = ((size_t)t.nsplit + 1) * sizeof(uint64_t);
   ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
   L.stage(CG_STAGE_CHECK_PREP, true, s);
@@ -3497,7 +3542,7 @@ static cudaError_t check_front(const Launch& L, const cg_copy_desc* d, uint64_t 
     uint64_t t_min = p.t_min, max_chunks = p.max_chunks;
     uint32_t* chunk_first = p.chunk_first;
     uint32_t em = err_mask;
-    int fu = fuse ? 1 : 0;
+    int fu = fuse;
     uint32_t* late = p.late;
     void* args[] = {(void*)&d, (void*)&n, (void*)&tc, (void*)&out, (void*)&weight, (void*)&meta, (void*)&dvoff,
                     (void*)&svc, (void*)&counter, (void*)&defer, (void*)&P, (void*)&bsum, (void*)&t_min,
@@ -3509,7 +3554,7 @@ static cudaError_t check_front(const Launch& L, const cg_copy_desc* d, uint64_t 
     if (e != cudaSuccess) return e;   // nothing after it may consume a stale plan
   } else {
     launch_pdl(k_check_prep, blocks_for(n, kThreads, L.num_sms * 4), kThreads, smem, s, d, n, t, out, p.weight, meta,
-               p.dvoff, sv, p.counter, p.defer, err_mask, fuse ? 1 : 0, p.late);
+               p.dvoff, sv, p.counter, p.defer, err_mask, fuse, p.late);
     *L.counter += 1;
     L.stage(CG_STAGE_CHECK_PREP, false, s);
     L.stage(CG_STAGE_CHECK_PLAN, true, s);
@@ -3519,7 +3564,7 @@ static cudaError_t check_front(const Launch& L, const cg_copy_desc* d, uint64_t 
   L.stage(CG_STAGE_CHECK_SCAN, true, s);
   if (!sv.sparse && sv.small_limit) {   // the small pass (k_check_small), then the ring scan
     launch_pdl(sv.two_bit ? k_check_small<true> : k_check_small<false>, L.small_blocks, kThreads, 0, s, meta, n, sv,
-               out, err_mask, fuse ? 1 : 0, p.resid, p.counter + 2);
+               out, err_mask, fuse ? 1 : 0, p.resid, p.counter + 2, p.last);
     *L.counter += 1;
   }
   auto scan = !sv.two_bit ? (fuse ? k_check_scan<false, true, false> : k_check_scan<false, false, false>)
@@ -3527,7 +3572,7 @@ static cudaError_t check_front(const Launch& L, const cg_copy_desc* d, uint64_t 
                           : (fuse ? k_check_scan<true, true, false> : k_check_scan<true, false, false>);
   launch_pdl(scan, L.scan_blocks, kRingWarps * 32, kScanSmem, s, meta, n, p.P, p.chunk_first, p.counter,
                                                                  p.t_min, p.max_chunks, sv, out, err_mask,
-                                                                 fuse ? 1 : 0, p.resid, p.counter + 2, d, p.defer);
+                                                                 fuse ? 1 : 0, p.resid, p.counter + 2, d, p.defer, p.last);
   L.stage(CG_STAGE_CHECK_SCAN, false, s);
   *L.counter += 1;
   return cudaGetLastError();
@@ -3536,7 +3581,7 @@ static cudaError_t check_front(const Launch& L, const cg_copy_desc* d, uint64_t 
 cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out, const Table& t,
                          const ShadowView& sv, const Plan& p, uint32_t err_mask, bool fuse, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  cudaError_t e = check_front(L, d, n, out, t, sv, p, err_mask, fuse, s);
+  cudaError_t e = check_front(L, d, n, out, t, sv, p, err_mask, fuse ? 1 : 0, s);
   if (e != cudaSuccess) return e;
   ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
   L.stage(CG_STAGE_CHECK_FINAL, true, s);
@@ -3551,7 +3596,7 @@ cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_
 cudaError_t check_apply(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_verdict* out, const Table& t,
                         const ShadowView& sv, const Plan& p, uint32_t err_mask, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  cudaError_t e = check_front(L, d, n, out, t, sv, p, err_mask, true, s);
+  cudaError_t e = check_front(L, d, n, out, t, sv, p, err_mask, 2, s);
   if (e != cudaSuccess) return e;
   L.stage(CG_STAGE_APPLY, true, s);
   ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
@@ -3564,9 +3609,10 @@ cudaError_t check_apply(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_v
   uint32_t* chunk_first = p.chunk_first;
   ShadowView svc = sv;
   const uint32_t* late = p.late;
+  uint32_t* last = p.last;
   void* args[] = {(void*)&d, (void*)&n, (void*)&P, (void*)&t_min, (void*)&max_chunks, (void*)&out, (void*)&err_mask,
                   (void*)&meta, (void*)&resid, (void*)&counter, (void*)&weight, (void*)&bsum, (void*)&chunk_first,
-                  (void*)&svc, (void*)&late};
+                  (void*)&svc, (void*)&late, (void*)&last};
   e = cudaLaunchCooperativeKernel(sv.two_bit ? (const void*)k_finish<true> : (const void*)k_finish<false>,
                                               dim3((unsigned)L.finish_blocks), dim3(kThreads), args, 0, s);
   L.stage(CG_STAGE_APPLY, false, s);

@@ -40,7 +40,7 @@ struct ArrayEntry {   // NEXT-3 device array (SPEC register_array S:166-168)
 };
 
 struct Layout {
-  uint64_t table, walk, patch, arrays, weight, P, bsum, fbsum, chunk, meta, resid, defer, late, dvoff, scratch, waves, ovl, marks, flags,
+  uint64_t table, walk, patch, arrays, weight, P, bsum, fbsum, chunk, meta, resid, defer, late, last, dvoff, scratch, waves, ovl, marks, flags,
       leaks,
       desc_stage, chunk_list,
       verdict_stage, raw_stage,
@@ -96,6 +96,7 @@ Layout layout_of(const cg_config* c) {
   L.resid = take(c->max_descs * sizeof(uint32_t));
   L.defer = take(c->max_descs * sizeof(uint32_t));
   L.late = take(c->max_descs * sizeof(uint32_t));
+  L.last = take(c->max_descs * sizeof(uint32_t));
   L.dvoff = c->dev_vbuf ? take(c->max_descs * 16) : 0;
   L.scratch = c->dev_vbuf ? take(cgk::stage_bytes()) : 0;
   L.waves = c->dev_vbuf ? take((c->max_descs + 1) * sizeof(uint32_t)) : 0;   // NEXT-1 wave offsets
@@ -276,6 +277,7 @@ struct cg_ctx {
     p.resid = reinterpret_cast<uint32_t*>(ws + lay.resid);
     p.defer = reinterpret_cast<uint32_t*>(ws + lay.defer);
     p.late = reinterpret_cast<uint32_t*>(ws + lay.late);
+    p.last = reinterpret_cast<uint32_t*>(ws + lay.last);
     p.dvoff = cfg.dev_vbuf ? reinterpret_cast<uint64_t*>(ws + lay.dvoff) : nullptr;
     p.max_chunks = lay.max_chunks;
     p.t_min = kChunkMin;
@@ -1761,46 +1763,51 @@ cg_status cg_plan_batches_propagate(const cg_copy_desc* h_descs, uint64_t n, uin
 cg_status cg_plan_batches_fused(cg_copy_desc* h_descs, uint64_t n, uint64_t* h_cuts, uint64_t* n_cuts) {
   if (!n_cuts || (n && (!h_descs || !h_cuts))) return CG_ERR_INVALID_VALUE;
   constexpr uint64_t kLateMax = 1ull << 20;   // larger dependent HtoDs end the batch instead
-  IvSet dtoh, late;                            // the batch's DtoH ranges, its CG_CHECK_AFTER HtoD ranges
+  constexpr uint32_t kBits = CG_CHECK_AFTER | CG_APPLY_AFTER | CG_APPLY_LAST;
+  // the batch's DtoH ranges, its CG_CHECK_AFTER HtoD ranges, its CG_APPLY_LAST DtoH ranges
+  IvSet dtoh, late, last;
   uint64_t k = 0, start = 0;
-  auto close = [&](uint64_t end) {   // CG_APPLY_AFTER over [start, end)
-    std::vector<cg_copy_desc> tmp(h_descs + start, h_descs + end);
+  auto cut = [&](uint64_t i) {   // end the batch before i; CG_APPLY_AFTER over [start, i)
+    std::vector<cg_copy_desc> tmp(h_descs + start, h_descs + i);
     uint64_t after = 0;
     cg_plan_apply_after(tmp.data(), tmp.size(), &after);
-    for (uint64_t i = start; i < end; ++i)
-      h_descs[i].reserved = (h_descs[i].reserved & ~(uint32_t)CG_APPLY_AFTER) | (tmp[i - start].reserved & CG_APPLY_AFTER);
+    for (uint64_t j = start; j < i; ++j) {
+      cg_copy_desc& d = h_descs[j];
+      const uint32_t a = (d.reserved & CG_APPLY_LAST) ? 0u : (tmp[j - start].reserved & CG_APPLY_AFTER);
+      d.reserved = (d.reserved & ~(uint32_t)CG_APPLY_AFTER) | a;
+    }
+    if (i == n) return;
+    h_cuts[k++] = i;
+    start = i;
+    dtoh.m.clear();
+    late.m.clear();
+    last.m.clear();
   };
   for (uint64_t i = 0; i < n; ++i) {
     cg_copy_desc& d = h_descs[i];
-    d.reserved &= ~(uint32_t)(CG_CHECK_AFTER | CG_APPLY_AFTER);
+    d.reserved &= ~kBits;
     uint64_t lo, hi;
     if (!host_range(d, lo, hi)) continue;
     if (reads_host(d.kind)) {
+      if (last.overlaps(lo, hi)) cut(i);   // reads bytes applied only after the late checks
       if (dtoh.overlaps(lo, hi)) {
         if (hi - lo <= kLateMax) {
           d.reserved |= CG_CHECK_AFTER;
           late.add(lo, hi);
         } else {   // too large for the late pass: a new batch (the classic R-20 cut)
-          close(i);
-          h_cuts[k++] = i;
-          start = i;
-          dtoh.m.clear();
-          late.m.clear();
+          cut(i);
         }
       }
     } else {
-      if (late.overlaps(lo, hi)) {   // it would write bytes a CG_CHECK_AFTER HtoD must not see
-        close(i);
-        h_cuts[k++] = i;
-        start = i;
-        dtoh.m.clear();
-        late.m.clear();
+      if (late.overlaps(lo, hi)) {   // it writes bytes a CG_CHECK_AFTER HtoD must not see
+        d.reserved |= CG_APPLY_LAST;
+        last.add(lo, hi);
       }
       dtoh.add(lo, hi);
     }
   }
   if (n) {
-    close(n);
+    cut(n);
     h_cuts[k++] = n;
   }
   *n_cuts = k;

@@ -111,7 +111,7 @@ def replay_events(chk, events: np.ndarray, blob=None, stream=None, fuse: bool = 
                 # R-20 epochs for the check; with tracking, each epoch's V-bit
                 # propagation runs in the waves of cg_plan_waves (R-28); fused
                 # (cg_check_apply): the batches of cg_plan_batches_fused, which
-                # also sets CG_CHECK_AFTER / CG_APPLY_AFTER
+                # also sets CG_CHECK_AFTER / CG_APPLY_AFTER / CG_APPLY_LAST
                 fused_plan = fuse and fuse != "disjoint" and not tracking
                 descs = np.ascontiguousarray(descs)
                 parts = []   # (s0, s1): batches of at most max_descs copies

@@ -347,10 +347,15 @@ def test_plan_apply_after(cg, seed):
 @pytest.mark.parametrize("seed", range(20))
 def test_plan_batches_fused(cg, seed):
     """cg_plan_batches_fused: inside every batch, an HtoD whose host range
-    overlaps an earlier DtoH of the batch carries CG_CHECK_AFTER, no DtoH
-    overlaps an earlier CG_CHECK_AFTER HtoD of its batch, and CG_APPLY_AFTER
-    is exactly cg_plan_apply_after of the batch"""
-    tr = tg.random_tiny(seed + 22000) if seed % 2 else tg.random_medium(seed, n_copies=80)
+    overlaps an earlier DtoH of the batch carries CG_CHECK_AFTER, a DtoH
+    overlapping an earlier CG_CHECK_AFTER HtoD carries CG_APPLY_LAST, no HtoD
+    overlaps an earlier CG_APPLY_LAST DtoH of its batch, CG_APPLY_AFTER is
+    cg_plan_apply_after of the batch on the other DtoH copies, and every cut is
+    forced (an HtoD reading a CG_APPLY_LAST range, or a late HtoD > 1 MiB)"""
+    if seed % 4 == 3:
+        tr = tg.pingpong_trace(seed)
+    else:
+        tr = tg.random_tiny(seed + 22000) if seed % 2 else tg.random_medium(seed, n_copies=80)
     descs = np.ascontiguousarray(tg.events_to_descs(tr.events[tr.events["op"] == tg.OP_COPY]))
     cuts = [0] + [int(c) for c in cg.plan_batches_fused(descs)]
     assert cuts[-1] == len(descs)
@@ -363,22 +368,40 @@ def test_plan_batches_fused(cg, seed):
         s = int(d[p]) + int(d[p + "_y"]) * int(d[p + "_pitch"]) + int(d[p + "_x"])
         e = s + (int(d["height"]) - 1) * int(d[p + "_pitch"]) + int(d["width"])
         return None if e > (1 << 64) - 1 else (s, e)
+
+    def hits(r, rs):
+        return any(x < r[1] and r[0] < y for x, y in rs)
+    prev = None   # (writes, last) of the batch before
     for a, b in zip(cuts[:-1], cuts[1:]):
-        writes, late = [], []
+        if prev is not None:   # the cut is forced by descriptor a
+            r = hrange(descs[a])
+            assert r is not None and int(descs[a]["kind"]) in (1, 4)
+            assert hits(r, prev[1]) or (hits(r, prev[0]) and r[1] - r[0] > (1 << 20))
+        writes, late, last = [], [], []
         for d in descs[a:b]:
             r = hrange(d)
             k = int(d["kind"])
             if r is None:
+                assert not d["reserved"] & (cg.CG_CHECK_AFTER | cg.CG_APPLY_LAST)
                 continue
             if k in (1, 4):
-                dep = any(x < r[1] and r[0] < y for x, y in writes)
+                assert not hits(r, last)
+                dep = hits(r, writes)
                 assert bool(d["reserved"] & cg.CG_CHECK_AFTER) == dep
+                assert not d["reserved"] & cg.CG_APPLY_LAST
                 if dep:
                     late.append(r)
             else:
-                assert not any(x < r[1] and r[0] < y for x, y in late)
+                is_last = hits(r, late)
+                assert bool(d["reserved"] & cg.CG_APPLY_LAST) == is_last
+                assert not d["reserved"] & cg.CG_CHECK_AFTER
+                if is_last:
+                    last.append(r)
+                    assert not d["reserved"] & cg.CG_APPLY_AFTER
                 writes.append(r)
+        prev = (writes, last)
         part = np.ascontiguousarray(descs[a:b]).copy()
         part["reserved"] &= ~np.uint32(cg.CG_APPLY_AFTER)
         cg.plan_apply_after(part)
-        assert np.array_equal(part["reserved"] & cg.CG_APPLY_AFTER, descs["reserved"][a:b] & cg.CG_APPLY_AFTER)
+        expect = np.where(descs["reserved"][a:b] & cg.CG_APPLY_LAST, 0, part["reserved"] & cg.CG_APPLY_AFTER)
+        assert np.array_equal(expect, descs["reserved"][a:b] & cg.CG_APPLY_AFTER)

@@ -56,3 +56,19 @@ def test_medium_small_batches(cg, seed):
 @pytest.mark.parametrize("seed", range(4))
 def test_medium_sharded(cg, world, seed):
     run_sharded(cg, tg.random_medium(seed + 500, n_copies=60), world, fuse=bool(seed % 2))
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_pingpong_fused(cg, seed):
+    """DtoH -> HtoD ping-pongs: CG_CHECK_AFTER HtoDs, CG_APPLY_AFTER and
+    CG_APPLY_LAST DtoHs (some failing) in the same fused batch; bytes, 2-bit
+    and sparse formats"""
+    fmt = (0, 0, 1, 2)[seed % 4]
+    kw = dict(sparse_capacity=(8 << 20) + (1 << 20)) if fmt == 2 else {}
+    run_parity(cg, tg.pingpong_trace(seed), fuse=True, shadow_format=fmt, **kw)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_pingpong_small_batches(cg, seed):
+    """the same with max_descs 5: the replay splits fused batches into pieces"""
+    run_parity(cg, tg.pingpong_trace(seed + 100, n_copies=80), fuse=True, max_descs=5)

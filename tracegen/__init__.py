@@ -1073,3 +1073,56 @@ def random_medium(seed: int, n_copies: int = 120, window: int = 64 * MiB, host_b
         else:
             tb.copy2d(DTOH, w, h, start, x, 0, pitch, dptr, 0, 0, w)
     return tb.build()
+
+
+def pingpong_trace(seed: int, n_copies: int = 240, n_bufs: int = 12) -> Trace:
+    """DtoH -> HtoD ping-pongs on a few host buffers (the fused batch planner's
+    CG_CHECK_AFTER / CG_APPLY_AFTER / CG_APPLY_LAST cases): 1D and
+    2D copies over partly overlapping slices of buffers that start UNDEFINED
+    (or DEFINED with planted bytes), DtoH copies that fail (device source too
+    small or unallocated: nothing becomes defined) next to ones that succeed,
+    and now and then a 2 MiB HtoD (too large for the late pass: a cut)."""
+    rng = np.random.default_rng(seed + 0x9090)
+    H0, S = 1 << 30, 8 * MiB
+    tb = TraceBuilder(f"pingpong{seed}", H0, S)
+    tb.mark(H0, S, UNDEFINED)
+    slot = S // n_bufs // 4096 * 4096
+    bufs = []
+    for b in range(n_bufs):
+        start = H0 + b * slot + int(rng.integers(0, 64))
+        length = int(_log_uniform(rng, 64, min(slot - 128, 96 * KiB), 1)[0])
+        if rng.random() < 0.4:
+            tb.mark(start, length, DEFINED)
+            for _ in range(int(rng.integers(0, 3))):
+                tb.setv(start + int(rng.integers(0, length)), bytes([int(rng.integers(1, 256))]))
+        bufs.append((start, length))
+    dev = tb.malloc(4 * MiB)
+    small = tb.malloc(256)
+    for _ in range(n_copies):
+        start, length = bufs[int(rng.integers(len(bufs)))]
+        kind = int(rng.choice([HTOD, DTOH]))
+        if kind == HTOD and rng.random() < 0.03:                   # too large for the late pass
+            tb.copy1d(HTOD, dev, H0 + int(rng.integers(0, S - 2 * MiB)), 2 * MiB)
+            continue
+        a = int(rng.integers(0, length))
+        n = int(rng.integers(1, length - a + 1))
+        src_dev = dev
+        u = rng.random()
+        if kind == DTOH and u < 0.15:
+            src_dev = small if n > 256 else 1 << 52                # TooSmall / not allocated: the copy fails
+        if rng.random() < 0.25 and n >= 8:                          # 2D over the slice
+            w = int(rng.integers(1, min(n, 4096) + 1))
+            h = max(1, min(64, n // max(w, 1)))
+            pitch = w + int(rng.integers(0, 64))
+            while (h - 1) * pitch + w > length - a and h > 1:
+                h -= 1
+            if kind == HTOD:
+                tb.copy2d(HTOD, w, h, dev, 0, 0, w, start + a, 0, 0, pitch)
+            else:
+                tb.copy2d(DTOH, w, h, start + a, 0, 0, pitch, src_dev, 0, 0, w)
+        elif kind == HTOD:
+            tb.copy1d(HTOD, dev, start + a, n)
+        else:
+            tb.copy1d(DTOH, start + a, src_dev, n)
+    tb.meta.update(dict(bufs=bufs, dev=dev))
+    return tb.build()
