@@ -13,7 +13,8 @@ constexpr uint64_t kNone = UINT64_MAX;
 constexpr uint64_t kInf = UINT64_MAX;          // free_seq of a live allocation
 constexpr uint64_t kMaxShardBytes = 1ull << 38;  // host bytes one context stores (config limit; scan weights < 2^40 each)
 constexpr uint64_t kDeferBytes = 1ull << 36;     // sparse map: longer host sides go to the deferred pass
-constexpr uint64_t kSmallBytesDefault = 4096;    // the small pass's limit (at most 4096; env CG_SMALL_BYTES)
+constexpr uint64_t kSmallBytesDefault = 4096;    // the small pass's limit (env CG_SMALL_BYTES, at most 4 KiB: its stage)
+constexpr uint64_t kSmallStatDefault = 4096;     // its adaptive choice counts sides up to this (env CG_SMALL_STAT)
 constexpr uint64_t kMaxDescs = 1ull << 24;       // per call (keeps sum of weights < 2^63)
 
 // start = base + y*pitch + x; span = (w==0||h==0) ? 0 : (h-1)*pitch + w;
@@ -62,6 +63,10 @@ struct ShadowView {
   // the small pass (k_check_small) takes contiguous host sides of at most
   // this many bytes (0: none; env CG_SMALL_BYTES)
   uint64_t small_limit;
+  // its on/off choice: 0 adaptive (from the previous check's share of sides of
+  // at most small_stat bytes), 1 always, 2 never (env CG_SMALL_MODE, CG_SMALL_STAT)
+  uint32_t small_mode;
+  uint64_t small_stat;
 };
 
 constexpr uint64_t kChunkShift = 16;               // 64 KiB host bytes per chunk

@@ -258,7 +258,7 @@ struct __align__(16) ScanMeta {
 // info: scanned bytes (the shard clip, < 2^40) | scan kind << 40 | host << 42 |
 // contiguous << 43 | raw << 44 | pfu << 45 | not the ring's (deferred pass or
 // small pass) << 46 | apply after the scan (CG_APPLY_AFTER) << 47 | flags << 48
-// | small pass << 58
+// | small pass << 58 | CG_APPLY_LAST (cg_check_apply) << 59
 constexpr int kInfoKind = 40, kInfoHost = 42, kInfoContig = 43, kInfoRaw = 44, kInfoPfu = 45, kInfoDefer = 46,
               kInfoAfter = 47, kInfoFlags = 48, kInfoSmall = 58,   // flags: 10 bits (48..57)
               kInfoLast = 59;
@@ -409,7 +409,8 @@ constexpr uint32_t kHtodShift = 12, kDtohShift = 15, k2bitShift = 14;
 constexpr uint32_t kGrab = 4;          // chunks per group while the plan is far from its end
 constexpr uint32_t kTileData = 1, kTileHtod = 2, kTileEnd = 4, kTileWhole = 8, kTileFuse = 16, kTileRaw = 32,
                    kTileAfter = 64,   // CG_APPLY_AFTER: a DtoH piece the residual pass applies
-                   kTileLast = 128;   // CG_APPLY_LAST: ... which k_finish applies after the late checks
+                   kTileLast = 128,   // CG_APPLY_LAST: ... which k_finish applies after the late checks
+                   kTilePacked = 512;   // several whole rows of one 2D DtoH piece (see TileGen::packed_tile)
 
 struct __align__(16) TileInfo {
   uint64_t ob;        // logical offset of staged host byte 0
@@ -735,6 +736,7 @@ __device__ __forceinline__ void fill2_any(const ShadowView& sv, uint64_t q0, uin
     else lane_fill2(sv.V, q0, q1, pat);
     return;
   }
+  if constexpr (kMaySparse)
   for (uint64_t q = q0; q < q1;) {
     const uint64_t c = q >> kChunkShift;
     const uint64_t n = umin64(q1 - q, (1ull << kChunkShift) - (q & ((1ull << kChunkShift) - 1)));
@@ -765,24 +767,37 @@ __device__ __forceinline__ void warp_store_zero(uint8_t* V, uint64_t q0, uint64_
 // ---------------------------------------------------------------------------
 // The small pass: contiguous host sides of at most sv.small_limit (<= 4 KiB)
 // bytes are checked by k_check_small instead of the TMA ring: a warp takes 32
-// consecutive descriptors (one coalesced meta load), then checks its small
-// ones one after the other with the whole warp -- a round is one 16-byte
-// load per lane (HtoD: 16 V bytes + their 16 A bits = 512 host bytes per
-// round; DtoH: 16 A bytes = 4 KiB; 2-bit: 16 state bytes = 2 KiB) -- with a
-// two-deep software pipeline: the first round of the next small descriptor
-// is loaded before the current one is folded, so two rounds are in flight per
-// warp.  The fold is an OR / AND per lane; masks, __ffs and __popc and the
-// warp reduction only run for a side that has a finding.
+// consecutive descriptors (one coalesced meta load) and stages the shadow of
+// its small sides in shared memory with one cp.async.bulk per side (two for
+// an HtoD side in the bytes format: its V units and its A bytes), as many
+// sides per fill as fit kSmallStage bytes, all completing on one mbarrier --
+// so a whole window's loads are in flight at once without holding registers
+// (the earlier lane-load version kept 64 bytes in flight per lane and spent
+// ~2 us per side on dependent DRAM round trips).  Sides of at most 32 units
+// (HtoD 512 B, DtoH 4 KiB, 2-bit 2 KiB) are then folded by their own lane,
+// longer ones by the whole warp; a unit is 16 shadow bytes (HtoD: 16 V bytes
+// and their 16 A bits; DtoH: 16 A bytes = 128 host bytes; 2-bit: 16 state
+// bytes = 64 host bytes).  The fold is an OR / AND per unit; masks, __ffs and
+// __popc and the warp reduction only run for a side that has a finding.
 // ---------------------------------------------------------------------------
+#ifndef CG_SMALL_THREADS
+#define CG_SMALL_THREADS 128   // 4 warps per CTA: 10 KB stages within the 48 KB of static shared memory
+#endif
+#ifndef CG_SMALL_STAGE
+#define CG_SMALL_STAGE 10240
+#endif
+constexpr int kSmallThreads = CG_SMALL_THREADS;
+// staged bytes per warp and fill (a side of <= 4 KiB needs <= 4.7 KB; a C5
+// window's small sides ~14 KB: each fill is a DRAM round trip of its warp)
+constexpr uint32_t kSmallStage = CG_SMALL_STAGE;
 template <bool kTwoBit>
 __device__ __forceinline__ uint32_t lane_span(bool htod) {
   return kTwoBit ? 64u : htod ? 16u : 128u;
 }
 
-constexpr uint64_t kSmallMeanBytes = 4096;   // the small pass runs when a batch's mean side is smaller
 
 // after a check: the small pass for the next check iff at least 80 % of this
-// batch's host sides had at most kSmallMeanBytes bytes (C5: ~90 %, C2: ~60 %)
+// batch's host sides had at most sv.small_stat bytes (C5: ~90 %, C2: ~60 %)
 // (counter[9] = 1; 2 = the ring only); the statistics (counter[10..11]:
 // smalls << 32 | sides) restart.  A stream of
 // similar batches (a program's calls, the bench's steps) is thus served by the
@@ -798,22 +813,6 @@ struct SmallRound {
   uint4 x;      // HtoD: V bytes; DtoH: A bytes; 2-bit: states
   uint32_t a;   // HtoD: the A bits of the 16 V bytes
 };
-
-// round r of a small side: lane unit gp = g0 + (32 r + lane) span (shard bytes)
-template <bool kTwoBit>
-__device__ __forceinline__ SmallRound small_load(const ShadowView& sv, uint64_t gp, uint64_t q1, bool htod) {
-  SmallRound u{make_uint4(0, 0, 0, 0), 0xFFFFu};
-  if (gp >= q1) return u;
-  if (kTwoBit) {
-    u.x = __ldcs(reinterpret_cast<const uint4*>(sv.V + (gp >> 2)));
-  } else if (htod) {
-    u.x = __ldcs(reinterpret_cast<const uint4*>(sv.V + gp));
-    u.a = __ldcs(reinterpret_cast<const unsigned short*>(sv.A + (gp >> 3)));
-  } else {
-    u.x = __ldcs(reinterpret_cast<const uint4*>(sv.A + (gp >> 3)));
-  }
-  return u;
-}
 
 // fold one lane unit [gp, gp + span) of a side [q0, q1) into p (logical offset
 // of shard byte q = ob + q)
@@ -866,6 +865,45 @@ __device__ __forceinline__ void small_fold(const SmallRound& u, uint64_t gp, uin
   }
 }
 
+// The warp's descriptors [base, base + 32) (lane k gets base + k): 16-byte
+// coalesced loads through a per-warp staging area, half a window at a time
+// (16 descriptors, rows padded to 112 bytes so that the LDS.128 reads of eight
+// lanes hit distinct banks); a descriptor array that is not 16-byte aligned
+// (the header allows 8) falls back to per-lane loads.  Lane-per-descriptor
+// loads of the 96-byte records touch 24 cache lines per instruction, which
+// kept the L1 of k_front 70 % busy.
+constexpr int kDescRow = 7;   // uint4 per staged descriptor (6 + 1 pad)
+#ifndef CG_PREP_STAGED_STORES
+#define CG_PREP_STAGED_STORES 1   // verdicts and scan records leave the prep through the staging area too
+#endif
+__device__ __forceinline__ cg_copy_desc warp_load_desc(const cg_copy_desc* __restrict__ descs, uint64_t base,
+                                                       uint64_t n, uint4* stage) {
+  const int lane = threadIdx.x & 31;
+  union {
+    cg_copy_desc d;
+    uint4 u[6];
+  } r;
+  r.d.kind = 0;
+  if (reinterpret_cast<uintptr_t>(descs) & 15) {
+    if (base + lane < n) r.d = descs[base + lane];
+    return r.d;
+  }
+  const uint4* src = reinterpret_cast<const uint4*>(descs + base);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint64_t b = base + 16 * h;
+    const uint32_t cnt = b < n ? (uint32_t)umin64(16, n - b) : 0u;
+    for (uint32_t k = lane; k < cnt * 6; k += 32) stage[(k / 6) * kDescRow + k % 6] = __ldcs(src + 96 * h + k);
+    __syncwarp();
+    if ((lane >> 4) == h && (uint32_t)(lane & 15) < cnt) {
+#pragma unroll
+      for (int j = 0; j < 6; ++j) r.u[j] = stage[(lane & 15) * kDescRow + j];
+    }
+    __syncwarp();
+  }
+  return r.d;
+}
+
 __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs, uint64_t n, const Table& t,
                                           cg_verdict* __restrict__ out, uint64_t* __restrict__ weight,
                                           ScanMeta* __restrict__ meta, uint64_t* __restrict__ dvoff,
@@ -878,16 +916,17 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
   // appended to right here, so the kernels after the scan (k_finish,
   // k_finalize_split) reset them for the next check.
   if (blockIdx.x == 0 && threadIdx.x < 2) counter[threadIdx.x] = 0;
-  const bool small_on = *reinterpret_cast<volatile const uint32_t*>(counter + 9) == 1u;
+  __shared__ uint4 s_desc[kThreads / 32][16 * kDescRow];
+  const bool small_on = sv.small_mode == 1 ||
+                        (sv.small_mode == 0 && *reinterpret_cast<volatile const uint32_t*>(counter + 9) == 1u);
   load_splitters(t, s_split);
   const int lane = threadIdx.x & 31;
   const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += nthr) {
     const uint64_t i = base + lane;
     const bool act = i < n;
-    cg_copy_desc d;
-    if (act) d = descs[i];
-    else d.kind = 0;
+    cg_copy_desc d = warp_load_desc(descs, base, n, s_desc[threadIdx.x >> 5]);
+    if (!act) d.kind = 0;
     const Norm nm = normalize(d);
     uint32_t flags = nm.flags;
     uint64_t de = 0, df = 0, se = 0, sf = 0;
@@ -965,37 +1004,66 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
     // many descriptors with few bytes each, C5); else (C2) the ring checks the
     // small sides too, their latency hidden behind the big tiles' streams
     const bool small = nscan != 0 && nscan <= sv.small_limit && contig && !raw && !sv.sparse && small_on;
-    {   // the statistics of the small-pass choice: host sides, and those of at most kSmallMeanBytes
+    {   // the statistics of the small-pass choice: host sides, and those of at most sv.small_stat
       const uint32_t sides = __popc(__ballot_sync(kFull, nscan != 0));
-      const uint32_t smalls = __popc(__ballot_sync(kFull, nscan != 0 && nscan <= kSmallMeanBytes));
+      const uint32_t smalls = __popc(__ballot_sync(kFull, nscan != 0 && nscan <= sv.small_stat));
       if (lane == 0 && sides)
         atomicAdd(reinterpret_cast<unsigned long long*>(counter + 10),
                   ((unsigned long long)smalls << 32) | (unsigned long long)sides);
     }
-    if (act) {
+    union {
       cg_verdict v;
-      v.first_unaddr = hc.pfu;
-      v.first_undef = kNone;
-      v.undef_count = 0;
-      v.dst_expected = de;
-      v.dst_found = df;
-      v.src_expected = se;
-      v.src_found = sf;
-      v.flags = flags;
-      v.status = 0;
-      if (small) finalize_fields(v.flags, v.status, v.first_unaddr, 0, err_mask);
-      out[i] = v;
-      weight[i] = small ? 0 : kItemCost + check_host_units(nm.skind, nscan, sv.two_bit != 0);
+      uint4 u[4];
+    } V;
+    union {
       ScanMeta m;
-      m.hstart = nm.hstart;
-      m.hpitch = nm.hpitch;
-      m.W = nm.W;
-      m.info = nscan | ((uint64_t)(nm.skind & 3u) << kInfoKind) | ((uint64_t)(nscan != 0) << kInfoHost) |
+      uint4 u[2];
+    } M;
+    V.v.first_unaddr = hc.pfu;
+    V.v.first_undef = kNone;
+    V.v.undef_count = 0;
+    V.v.dst_expected = de;
+    V.v.dst_found = df;
+    V.v.src_expected = se;
+    V.v.src_found = sf;
+    V.v.flags = flags;
+    V.v.status = 0;
+    if (small) finalize_fields(V.v.flags, V.v.status, V.v.first_unaddr, 0, err_mask);
+    if (act) weight[i] = small ? 0 : kItemCost + check_host_units(nm.skind, nscan, sv.two_bit != 0);
+    M.m.hstart = nm.hstart;
+    M.m.hpitch = nm.hpitch;
+    M.m.W = nm.W;
+    M.m.info = nscan | ((uint64_t)(nm.skind & 3u) << kInfoKind) | ((uint64_t)(nscan != 0) << kInfoHost) |
                ((uint64_t)contig << kInfoContig) | ((uint64_t)raw << kInfoRaw) |
                ((uint64_t)(hc.pfu != kNone) << kInfoPfu) | ((uint64_t)(deferred || small || is_late) << kInfoDefer) |
                ((uint64_t)is_after << kInfoAfter) | ((uint64_t)flags << kInfoFlags) |
                ((uint64_t)small << kInfoSmall) | ((uint64_t)is_last << kInfoLast);
-      meta[i] = m;
+    // the 64-byte verdicts and 32-byte records of the warp's descriptors:
+    // coalesced 16-byte stores through the staging area (an 8-byte store per
+    // lane and field touched 32 sectors per instruction)
+    uint4* stg = s_desc[threadIdx.x >> 5];
+    if (CG_PREP_STAGED_STORES && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint64_t b = base + 16 * h;
+        const uint32_t cnt = b < n ? (uint32_t)umin64(16, n - b) : 0u;
+        if ((lane >> 4) == h && (uint32_t)(lane & 15) < cnt) {
+          uint4* row = stg + (lane & 15) * kDescRow;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) row[j] = V.u[j];
+          row[4] = M.u[0];
+          row[5] = M.u[1];
+        }
+        __syncwarp();
+        uint4* ov = reinterpret_cast<uint4*>(out + b);
+        uint4* om = reinterpret_cast<uint4*>(meta + b);
+        for (uint32_t k = lane; k < cnt * 4; k += 32) ov[k] = stg[(k >> 2) * kDescRow + (k & 3)];
+        if ((uint32_t)lane < cnt * 2) om[lane] = stg[(lane >> 1) * kDescRow + 4 + (lane & 1)];
+        __syncwarp();
+      }
+    } else if (act) {
+      out[i] = V.v;
+      meta[i] = M.m;
     }
   }
 }
@@ -1009,24 +1077,96 @@ __device__ __forceinline__ void push_apply(bool is_last, uint32_t d, uint32_t* _
   else resid[atomicAdd(resid_n, 1u)] = d;
 }
 
-// The small pass (a4-a6 for small contiguous host sides; see small_load):
+#ifndef CG_SMALL_VERIFY
+#define CG_SMALL_VERIFY 0   // debug builds: every staged side re-checked from global memory
+#endif
+#if CG_SMALL_VERIFY
+__device__ uint32_t g_small_verify;
+#endif
+
+// a staged small side (k_check_small's pass 1): its main units at stage + off
+// (16 bytes each), HtoD bytes format: its A half-words from stage + aoff, the
+// inclusive unit count of the fill's sides up to it, the bytes outside the
+// side at the start of unit 0 (skip) and the bytes inside it in the last unit
+// (keep)
+struct SmallSide {
+  uint32_t off, aoff, uincl, units;
+  uint32_t skip, keep;
+  bool htod;
+};
+
+template <bool kTwoBit>
+__device__ __forceinline__ uint32_t sh_of(bool htod) {
+  return kTwoBit ? 6u : htod ? 4u : 7u;
+}
+
+// bits [lo, hi) of a 32-bit group starting at bit b (lo, hi, b in bits of one unit)
+__device__ __forceinline__ uint32_t bits_in(uint32_t b, uint32_t lo, uint32_t hi) {
+  const uint32_t l = lo > b ? lo - b : 0u, h = hi > b ? min(hi - b, 32u) : 0u;
+  if (h <= l) return 0u;
+  return (h >= 32 ? 0xffffffffu : ((1u << h) - 1u)) & ~((1u << l) - 1u);
+}
+
+// unit k of a staged side clean (no unaddressable byte; HtoD: no undefined
+// byte) over its host bytes [lo, hi) relative to the unit's first byte
+template <bool kTwoBit>
+__device__ __forceinline__ bool small_unit_clean(const uint4& v, const uint8_t* stage, const SmallSide& r, uint32_t k,
+                                                 uint32_t lo, uint32_t hi) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  if (kTwoBit) {   // 16 host bytes per state word, 2 bits each
+    uint32_t bad = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t l = lo > 16u * i ? min(lo - 16u * i, 16u) : 0u;
+      const uint32_t h = hi > 16u * i ? min(hi - 16u * i, 16u) : 0u;
+      const uint32_t m = h <= l ? 0u : ((h >= 16 ? 0xffffffffu : ((1u << (2 * h)) - 1u)) & ~((1u << (2 * l)) - 1u));
+      bad |= (r.htod ? (w[i] ^ 0xAAAAAAAAu) : (~(w[i] | (w[i] >> 1)) & 0x55555555u)) & m;
+    }
+    return bad == 0;
+  }
+  if (r.htod) {   // 16 V bytes and their 16 A bits
+    const uint32_t m = bits_in(0, lo, hi) & 0xFFFFu;
+    const uint32_t a = *reinterpret_cast<const unsigned short*>(stage + r.aoff + 2 * k);
+    if ((a & m) != m) return false;
+    return (w[0] | w[1] | w[2] | w[3]) == 0 || (nz16(v) & m) == 0;
+  }
+  // DtoH: 16 A bytes = 128 host bytes
+  if (lo == 0 && hi == 128) return (w[0] & w[1] & w[2] & w[3]) == 0xffffffffu;
+  uint32_t bad = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) bad |= ~w[i] & bits_in(32u * i, lo, hi);
+  return bad == 0;
+}
+
+// The small pass (a4-a6 for small contiguous host sides; see kSmallStage):
 // a dirty verdict is rewritten, a clean one was final already (the prep
 // wrote it); small DtoH sides with status OK are applied here when fused (a6)
 // unless CG_APPLY_AFTER sends them to the residual pass.
 #ifndef CG_SMALL_MINB
-#define CG_SMALL_MINB 4   // 64 registers, 32 warps per SM: measured 6.16 ms for C5 vs 6.99 at 80 registers
-#endif
-#ifndef CG_TINY_UNROLL
-#define CG_TINY_UNROLL 4
+#define CG_SMALL_MINB 5   // 64 registers; 5 CTAs of 4 warps (shared memory)
 #endif
 template <bool kTwoBit>
-__global__ void __launch_bounds__(kThreads, CG_SMALL_MINB) k_check_small(const ScanMeta* __restrict__ meta, uint64_t n,
+__global__ void __launch_bounds__(kSmallThreads, CG_SMALL_MINB) k_check_small(const ScanMeta* __restrict__ meta, uint64_t n,
                                                           ShadowView sv, cg_verdict* __restrict__ out,
                                                           uint32_t err_mask, int fuse, uint32_t* __restrict__ resid,
                                                           uint32_t* __restrict__ resid_n, uint32_t* __restrict__ last) {
   pdl_entry();
-  if (*reinterpret_cast<volatile const uint32_t*>(resid_n + 7) != 1u) return;   // counter[9]: the ring takes them all
+  if (sv.small_mode == 2 || (sv.small_mode == 0 && *reinterpret_cast<volatile const uint32_t*>(resid_n + 7) != 1u))
+    return;   // counter[9]: the ring takes them all
+  __shared__ __align__(128) uint8_t s_stage[kSmallThreads / 32][kSmallStage];
+  __shared__ uint64_t s_bar[kSmallThreads / 32];
+  __shared__ SmallSide s_side[kSmallThreads / 32][32];
   const int lane = threadIdx.x & 31;
+  uint8_t* stage = s_stage[threadIdx.x >> 5];
+  uint64_t* bar = &s_bar[threadIdx.x >> 5];
+  SmallSide* side = s_side[threadIdx.x >> 5];
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  uint32_t parity = 0;
+  const uint64_t policy = evict_first_policy();
   const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += nthr) {
     const uint64_t i = base + lane;
@@ -1048,75 +1188,145 @@ __global__ void __launch_bounds__(kThreads, CG_SMALL_MINB) k_check_small(const S
       ob = sv.sb - x0;
     }
     Partial mine{kNone, kNone, 0};
-    // tiny sides (at most 33 lane units: HtoD 512 B, DtoH 4 KiB, 2-bit 2 KiB)
-    // are checked by their own lane, four 16-byte loads in flight per lane
-    // per step, no warp reduction; the warp loops until its largest tiny side is done
-    {
-      const uint64_t span = lane_span<kTwoBit>(htod);
-      const bool tiny = small && q1 - q0 <= 32 * span;
-      const uint32_t tmask = __ballot_sync(kFull, tiny);
-      if (tmask) {
-        uint64_t g = q0 / span * span;
-        Partial tp{kNone, kNone, 0};
-        while (__any_sync(kFull, tiny && g < q1)) {
-          if (tiny && g < q1) {
-            SmallRound u[CG_TINY_UNROLL];
-#pragma unroll
-            for (int k = 0; k < CG_TINY_UNROLL; ++k) u[k] = small_load<kTwoBit>(sv, g + k * span, q1, htod);
-#pragma unroll
-            for (int k = 0; k < CG_TINY_UNROLL; ++k) small_fold<kTwoBit>(u[k], g + k * span, q0, q1, ob, htod, tp);
-            g += CG_TINY_UNROLL * span;
-          }
-        }
-        if (tiny) mine = tp;
-        todo &= ~tmask;
-      }
+    // staging: the side's shadow units (16 bytes each: HtoD V, DtoH A, 2-bit
+    // states; lane unit gp = g0 + k span) and, HtoD bytes format, its A bytes
+    const uint32_t sh = kTwoBit ? 6u : htod ? 4u : 7u;   // log2 of the host bytes per unit
+    const uint64_t g0 = q0 & ~((1ull << sh) - 1);
+    const uint32_t mlen = small ? (uint32_t)(((q1 - g0 + (1ull << sh) - 1) >> sh) << 4) : 0u;
+    uint64_t ab = 0;
+    uint32_t alen = 0;
+    if (!kTwoBit && htod && small) {
+      ab = (g0 >> 3) & ~15ull;
+      alen = (uint32_t)((((q1 + 127) & ~127ull) >> 3) - ab);
     }
-    if (todo) {
-    // the two-deep pipeline: (j, its geometry, its round-0 data) current / next
-    int j = __ffs(todo) - 1;
-    todo &= todo - 1;
-    uint64_t cq0 = __shfl_sync(kFull, q0, j), cq1 = __shfl_sync(kFull, q1, j), cob = __shfl_sync(kFull, ob, j);
-    bool ch = __shfl_sync(kFull, htod, j);
-    uint64_t cspan = lane_span<kTwoBit>(ch), cg0 = cq0 / cspan * cspan;
-    SmallRound cu = small_load<kTwoBit>(sv, cg0 + cspan * lane, cq1, ch);
-    while (j >= 0) {
-      const int jn = todo ? __ffs(todo) - 1 : -1;
-      if (jn >= 0) todo &= todo - 1;
-      uint64_t nq0 = 0, nq1 = 0, nob = 0, nspan = 16, ng0 = 0;
-      bool nh = false;
-      SmallRound nu{make_uint4(0, 0, 0, 0), 0xFFFFu};
-      if (jn >= 0) {   // issue the next side's first round before folding this one
-        nq0 = __shfl_sync(kFull, q0, jn);
-        nq1 = __shfl_sync(kFull, q1, jn);
-        nob = __shfl_sync(kFull, ob, jn);
-        nh = __shfl_sync(kFull, htod, jn);
-        nspan = lane_span<kTwoBit>(nh);
-        ng0 = nq0 / nspan * nspan;
-        nu = small_load<kTwoBit>(sv, ng0 + nspan * lane, nq1, nh);
+    const uint32_t need = mlen + alen;   // <= 4.7 KB for a side of <= 4 KiB
+    uint32_t rem = todo;
+    while (rem) {   // fills: the longest prefix of the remaining sides that fits the stage
+      const bool cand = (rem >> lane) & 1u;
+      const uint32_t x = cand ? need : 0u;
+      uint32_t incl = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
       }
-      Partial p{kNone, kNone, 0};
-      small_fold<kTwoBit>(cu, cg0 + cspan * lane, cq0, cq1, cob, ch, p);
-      for (uint64_t g = cg0 + 32 * cspan; g < cq1; g += 32 * cspan) {   // rounds after the first (sides > one round)
-        const uint64_t gp = g + cspan * lane;
-        const SmallRound u = small_load<kTwoBit>(sv, gp, cq1, ch);
-        small_fold<kTwoBit>(u, gp, cq0, cq1, cob, ch, p);
+      const bool in = cand && incl <= kSmallStage;
+      const uint32_t fill = __ballot_sync(kFull, in);
+      const uint32_t total = __shfl_sync(kFull, incl, 31 - __clz(fill));
+      const uint32_t off = incl - x;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the last fill's generic reads first
+      if (lane == 0) mbar_arrive_tx(bar, total);
+      __syncwarp();
+      if (in) {
+        const uint8_t* src = kTwoBit ? sv.V + (g0 >> 2) : htod ? sv.V + g0 : sv.A + (g0 >> 3);
+        bulk_g2s(stage + off, src, mlen, bar, policy);
+        if (alen) bulk_g2s(stage + off + mlen, sv.A + ab, alen, bar, policy);
       }
-      if (__any_sync(kFull, p.fu != kNone || p.fd != kNone || p.cnt != 0)) {
+      mbar_wait(bar, parity);
+      parity ^= 1u;
+      // pass 1: every unit of the fill, spread evenly over the lanes (flat unit
+      // f -> side j = the lane whose inclusive unit count first exceeds f):
+      // only which sides have a finding
+      const uint32_t units = in ? (mlen >> 4) : 0u;
+      uint32_t uincl = units;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, uincl, o);
+        if (lane >= o) uincl += y;
+      }
+      const uint32_t U = __shfl_sync(kFull, uincl, 31);
+      {
+        SmallSide r;
+        r.off = off;
+        r.aoff = off + mlen + (uint32_t)((g0 >> 3) - ab);
+        r.uincl = uincl;
+        r.units = units;
+        r.skip = (uint32_t)(q0 - g0);
+        r.keep = units ? (uint32_t)(q1 - (g0 + ((uint64_t)(units - 1) << sh))) : 0u;
+        r.htod = htod;
+        side[lane] = r;
+      }
+      __syncwarp();
+      uint32_t dirty = 0;   // lane-local: bit j = side j has a finding
+      uint32_t j = 0;
+      for (uint32_t f = lane; f < U; f += 32) {
+        while (f >= side[j].uincl) ++j;
+        const SmallSide& r = side[j];
+        const uint32_t k = f - (r.uincl - r.units);
+        const uint4 v = *reinterpret_cast<const uint4*>(stage + r.off + 16 * k);
+        const uint32_t lo = k == 0 ? r.skip : 0u, hi = k + 1 == r.units ? r.keep : (1u << sh_of<kTwoBit>(r.htod));
+        if (!small_unit_clean<kTwoBit>(v, stage, r, k, lo, hi)) dirty |= 1u << j;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dirty |= __shfl_xor_sync(kFull, dirty, o);
+#if CG_SMALL_VERIFY
+      {   // debug: every side of the fill, exactly from the stage and from global memory
+        uint32_t all = fill;
+        while (all) {
+          const int jj = __ffs(all) - 1;
+          all &= all - 1;
+          const uint64_t cq0 = __shfl_sync(kFull, q0, jj), cq1 = __shfl_sync(kFull, q1, jj);
+          const uint64_t cob = __shfl_sync(kFull, ob, jj), cg0 = __shfl_sync(kFull, g0, jj);
+          const uint64_t cab = __shfl_sync(kFull, ab, jj);
+          const uint32_t coff = __shfl_sync(kFull, off, jj), cm = __shfl_sync(kFull, mlen, jj);
+          const bool ch = __shfl_sync(kFull, htod, jj);
+          const uint32_t csh = kTwoBit ? 6u : ch ? 4u : 7u;
+          const bool cd = __shfl_sync(kFull, dirty, 0) >> jj & 1u;
+          Partial ps{kNone, kNone, 0}, pg{kNone, kNone, 0};
+          uint32_t diffs = 0;
+          for (uint32_t k = lane; k < (cm >> 4); k += 32) {
+            const uint64_t gp = cg0 + ((uint64_t)k << csh);
+            SmallRound u, g;
+            u.x = *reinterpret_cast<const uint4*>(stage + coff + 16 * k);
+            u.a = (!kTwoBit && ch) ? *reinterpret_cast<const unsigned short*>(stage + coff + cm + ((gp >> 3) - cab))
+                                   : 0xFFFFu;
+            g.x = __ldcg(reinterpret_cast<const uint4*>(kTwoBit ? sv.V + (gp >> 2) : ch ? sv.V + gp : sv.A + (gp >> 3)));
+            g.a = (!kTwoBit && ch) ? __ldcg(reinterpret_cast<const unsigned short*>(sv.A + (gp >> 3))) : 0xFFFFu;
+            if (u.x.x != g.x.x || u.x.y != g.x.y || u.x.z != g.x.z || u.x.w != g.x.w || u.a != g.a) ++diffs;
+            small_fold<kTwoBit>(u, gp, cq0, cq1, cob, ch, ps);
+            small_fold<kTwoBit>(g, gp, cq0, cq1, cob, ch, pg);
+          }
+          ps.fu = warp_min(ps.fu); ps.fd = warp_min(ps.fd); ps.cnt = warp_sum(ps.cnt);
+          pg.fu = warp_min(pg.fu); pg.fd = warp_min(pg.fd); pg.cnt = warp_sum(pg.cnt);
+          diffs = (uint32_t)warp_sum(diffs);
+          const bool gd = pg.fu != kNone || pg.fd != kNone || pg.cnt != 0;
+          if (lane == 0 && (diffs || gd != cd || ps.fu != pg.fu || ps.fd != pg.fd || ps.cnt != pg.cnt) &&
+              atomicAdd(&g_small_verify, 1u) < 40)
+            printf("VERIFY i=%llu side=%d htod=%d q0=%llu q1=%llu off=%u mlen=%u total=%u fill=%08x diffs=%u dirty=%d/%d "
+                   "stage(%llx,%llx,%llu) global(%llx,%llx,%llu)\n",
+                   (unsigned long long)(base + jj), jj, (int)ch, (unsigned long long)cq0, (unsigned long long)cq1,
+                   coff, cm, total, fill, diffs, (int)cd, (int)gd, (unsigned long long)ps.fu,
+                   (unsigned long long)ps.fd, (unsigned long long)ps.cnt, (unsigned long long)pg.fu,
+                   (unsigned long long)pg.fd, (unsigned long long)pg.cnt);
+        }
+      }
+#endif
+      // pass 2: a side with a finding, exactly, by the whole warp
+      while (dirty) {
+        const int jj = __ffs(dirty) - 1;
+        dirty &= dirty - 1;
+        const uint64_t cq0 = __shfl_sync(kFull, q0, jj), cq1 = __shfl_sync(kFull, q1, jj);
+        const uint64_t cob = __shfl_sync(kFull, ob, jj), cg0 = __shfl_sync(kFull, g0, jj);
+        const uint64_t cab = __shfl_sync(kFull, ab, jj);
+        const uint32_t coff = __shfl_sync(kFull, off, jj), cm = __shfl_sync(kFull, mlen, jj);
+        const bool ch = __shfl_sync(kFull, htod, jj);
+        const uint32_t csh = kTwoBit ? 6u : ch ? 4u : 7u;
+        Partial p{kNone, kNone, 0};
+        for (uint32_t k = lane; k < (cm >> 4); k += 32) {
+          const uint64_t gp = cg0 + ((uint64_t)k << csh);
+          SmallRound u;
+          u.x = *reinterpret_cast<const uint4*>(stage + coff + 16 * k);
+          u.a = (!kTwoBit && ch) ? *reinterpret_cast<const unsigned short*>(stage + coff + cm + ((gp >> 3) - cab))
+                                 : 0xFFFFu;
+          small_fold<kTwoBit>(u, gp, cq0, cq1, cob, ch, p);
+        }
         p.fu = warp_min(p.fu);
         p.fd = warp_min(p.fd);
         p.cnt = warp_sum(p.cnt);
-        if (lane == j) mine = p;
+        if (lane == jj) mine = p;
       }
-      j = jn;
-      cq0 = nq0;
-      cq1 = nq1;
-      cob = nob;
-      ch = nh;
-      cspan = nspan;
-      cg0 = ng0;
-      cu = nu;
-    }
+      rem &= ~fill;
+      __syncwarp();
     }
     bool apply_me = false;
     if (small) {
@@ -1416,6 +1626,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_front(const cg_copy_desc* __res
 constexpr uint32_t kPieceIn = 1, kPieceWhole = 2, kPieceHtod = 4, kPiece2D = 8, kPieceEmpty = 16;
 constexpr uint32_t kSegEndLast = 1u << 8;   // the segment's last tile ends its piece
 constexpr int kPhaseGroup = 0, kPhaseContig = 1, kPhase2D = 2, kPhaseWindow = 3;
+constexpr uint32_t kSubNone = 0, kSubHead = 1, kSubBody = 2, kSubTail = 3;
 
 __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t x, uint32_t& total) {
   const int lane = threadIdx.x & 31;
@@ -1462,6 +1673,11 @@ struct TileGen {
   bool in2d;
   uint64_t x0, pitch, W, lo2, hi2, r2, fu2;
   uint32_t d2, fl2;
+  // packed rows of a 2D DtoH piece: sub-phase (kSubNone: rows one by one;
+  // kSubHead -> kSubBody -> kSubTail: the partial first row, the whole rows
+  // [r2, pk_end) several per tile, the partial last row) and the piece's end
+  uint32_t sub;
+  uint64_t pk_end, t_hi;
 
   __device__ __forceinline__ void load_window(uint64_t base) {
     const int lane = threadIdx.x & 31;
@@ -1625,6 +1841,68 @@ struct TileGen {
     r2 += 32;
   }
 
+  // Packed DtoH rows: a 2D DtoH piece's whole rows are staged several per tile
+  // (row j of the tile at byte j * pk_rs of the slot: its A bytes from the
+  // 16-byte boundary below it), instead of one tile per row segment, which
+  // made narrow-row copies (C4) issue-bound.  Only for pieces whose rows lie
+  // inside the stored shard, in the bytes format.  Row r starts at shard byte
+  // q_r = x0 + r pitch - sb, and the logical offset of its shard byte q is
+  // r W + q - q_r = ob_r + q, so ob_{r+j} = ob_r + j (W - pitch) (mod 2^64).
+  __device__ __forceinline__ static uint32_t packed_rs(uint64_t W) {   // A bytes of a row at any 128-byte phase, at most
+    return (uint32_t)(16 * ((W + 127) / 128 + 1));
+  }
+
+  __device__ __forceinline__ void enter_2d() {
+    sub = kSubNone;
+    if (two_bit || (fl2 & kTileHtod) || W == 0 || W > 16 * (kTileV + kTileA)) return;
+    if (2 * packed_rs(W) > kTileV + kTileA) return;
+    const uint64_t rA = (lo2 + W - 1) / W, rB = hi2 / W;   // whole rows [rA, rB)
+    if (rB <= rA) return;
+    const uint64_t a = x0 + rA * pitch, b = x0 + (rB - 1) * pitch + W;
+    if (a < sb || b > se) return;
+    pk_end = rB;
+    t_hi = hi2;
+    hi2 = umin64(hi2, rA * W);   // the head: [lo2, rA W)
+    sub = kSubHead;
+  }
+
+  // one tile of whole rows [r2, r2 + k): every lane stages its row's A bytes
+  __device__ __forceinline__ void packed_tile(WarpRing& ring, int s, const ShadowView& sv, uint64_t policy) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t rs = packed_rs(W);
+    const uint32_t k = (uint32_t)umin64(umin64(32, (kTileV + kTileA) / rs), pk_end - r2);
+    const uint64_t q_first = x0 + r2 * pitch - sb;
+    uint32_t len = 0;
+    uint64_t qa = 0;
+    if ((uint32_t)lane < k) {
+      const uint64_t q = q_first + (uint64_t)lane * pitch;
+      qa = q & ~127ull;
+      len = (uint32_t)((((q + W + 127) & ~127ull) - qa) >> 3);
+    }
+    uint32_t total = len;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(kFull, total, o);
+    if (lane == 0) {
+      TileInfo ti;
+      ti.ob = r2 * W - q_first;   // ob of row r2
+      ti.pend_fu = kNone;
+      ti.d = d2;
+      ti.flags = kTileData | kTilePacked | (fl2 & ~(kSegEndLast | kTileWhole));
+      ti.q0 = (uint32_t)W;
+      ti.q1 = k | (rs << 16);
+      ti.qs = q_first;
+      ti.qe = pitch;
+      ring.info[s] = ti;
+      mbar_arrive_tx(&ring.bar[s], total);
+    }
+    __syncwarp();
+    if (len) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bulk_g2s(ring.data[s] + lane * rs, sv.A + qa / 8, len, &ring.bar[s], policy);
+    }
+    r2 += k;
+  }
+
   // issues the next tile into ring slot s; false when the warp has no more work
   __device__ __forceinline__ bool next(WarpRing& ring, int s, const ShadowView& sv, uint64_t policy) {
     const int lane = threadIdx.x & 31;
@@ -1636,6 +1914,18 @@ struct TileGen {
         if (in2d) {
           if (r2 * W < hi2) {
             row_window();
+          } else if (sub == kSubHead) {   // head rows done: the whole rows, packed
+            sub = kSubBody;
+            r2 = (lo2 + W - 1) / W;
+          } else if (sub == kSubBody) {
+            if (r2 < pk_end) {
+              packed_tile(ring, s, sv, policy);
+              return true;
+            }
+            sub = kSubTail;   // then the partial last row, one by one
+            lo2 = pk_end * W;
+            hi2 = t_hi;
+            r2 = pk_end;
           } else {   // all rows done: a data-less END tile carrying the analytic offset
             in2d = false;
             if (lane == 0) {
@@ -1664,8 +1954,9 @@ struct TileGen {
           fl2 = (pf & kPieceHtod ? kTileHtod : 0u) | (pf & kPieceWhole ? kTileWhole : 0u) |
                 (((info >> kInfoRaw) & 1u) ? kTileRaw : 0u) | (((info >> kInfoLast) & 1u) ? kTileLast : 0u) |
                 ((uint32_t)((info >> kInfoFlags) & 0x3FFu) << 16);
-          r2 = lo2 / W;
           fu2 = __shfl_sync(kFull, p_fu, src);
+          enter_2d();
+          r2 = lo2 / W;
           in2d = true;
         } else {
           phase = kPhaseWindow;
@@ -1982,6 +2273,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
   gen.p_fl = 0;
   gen.twod = 0;
   gen.in2d = false;
+  gen.sub = kSubNone;
   gen.K = gen.t = 0;
 
   int filled = 0;
@@ -1998,6 +2290,13 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
         else consume_2bit<false>(ring.data[s], t.q0, t.q1, t.ob, p);
       } else if (t.flags & kTileHtod) {
         consume_htod(ring.data[s], t.q0, t.q1, t.ob, p);
+      } else if (t.flags & kTilePacked) {   // rows j = 0..k-1 (TileGen::packed_tile)
+        const uint32_t k = t.q1 & 0xFFFFu, rs = t.q1 >> 16, W = t.q0;
+        for (uint32_t j = 0; j < k; ++j) {
+          const uint64_t q = t.qs + (uint64_t)j * t.qe, qa = q & ~127ull;
+          const uint32_t c0 = (uint32_t)(q - qa);
+          consume_dtoh(ring.data[s] + j * rs, c0, c0 + W, t.ob + (uint64_t)j * (W - t.qe) + qa, p);
+        }
       } else {
         consume_dtoh(ring.data[s], t.q0, t.q1, t.ob, p);
       }
@@ -3563,7 +3862,7 @@ static cudaError_t check_front(const Launch& L, const cg_copy_desc* d, uint64_t 
   }
   L.stage(CG_STAGE_CHECK_SCAN, true, s);
   if (!sv.sparse && sv.small_limit) {   // the small pass (k_check_small), then the ring scan
-    launch_pdl(sv.two_bit ? k_check_small<true> : k_check_small<false>, L.small_blocks, kThreads, 0, s, meta, n, sv,
+    launch_pdl(sv.two_bit ? k_check_small<true> : k_check_small<false>, L.small_blocks, kSmallThreads, 0, s, meta, n, sv,
                out, err_mask, fuse ? 1 : 0, p.resid, p.counter + 2, p.last);
     *L.counter += 1;
   }
@@ -3896,8 +4195,8 @@ int persistent_blocks(int which) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_leak, kThreads, 0);
   } else if (which == 6) {
     int b2 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_check_small<false>, kThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_check_small<true>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_check_small<false>, kSmallThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_check_small<true>, kSmallThreads, 0);
     b = std::min(b, b2);
   } else if (which == 3) {
     int b2 = 0;

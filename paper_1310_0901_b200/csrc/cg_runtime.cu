@@ -476,7 +476,13 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
                                                                                           : cfg->host_size;
   if (cfg->shard_size && !sparse) c->sv.v_bytes = two_bit ? cfg->shard_size / 4 : cfg->shard_size;
   c->sv.small_limit = cgk::kSmallBytesDefault;
-  if (const char* sl = getenv("CG_SMALL_BYTES")) c->sv.small_limit = std::min<uint64_t>(strtoull(sl, nullptr, 10), 4096);
+  // the stage holds a side of at most 4 KiB (bytes format) / 16 KiB (2-bit states)
+  if (const char* sl = getenv("CG_SMALL_BYTES"))
+    c->sv.small_limit = std::min<uint64_t>(strtoull(sl, nullptr, 10), two_bit ? 16384 : 4096);
+  c->sv.small_mode = 0;
+  if (const char* sm = getenv("CG_SMALL_MODE")) c->sv.small_mode = (uint32_t)std::min<uint64_t>(strtoull(sm, nullptr, 10), 2);
+  c->sv.small_stat = cgk::kSmallStatDefault;
+  if (const char* ss = getenv("CG_SMALL_STAT")) c->sv.small_stat = strtoull(ss, nullptr, 10);
   if (sparse) {   // the whole 64-bit space; the directory lives in the workspace
     c->sv.wb = c->sv.sb = 0;
     c->sv.we = c->sv.se = UINT64_MAX;
@@ -1142,9 +1148,9 @@ static cg_status recover_memmoves(cg_ctx* c, const cg_copy_desc* d_descs, cudaSt
   e = cudaMemcpy(list.data(), overflow + 2, h[1] * sizeof(uint32_t), cudaMemcpyDeviceToHost);
   uint64_t need = 0;
   for (uint32_t i : list) {
-    cg_copy_desc d;
+    cg_copy_desc d{};
     if (e == cudaSuccess) e = cudaMemcpy(&d, d_descs + i, sizeof d, cudaMemcpyDeviceToHost);
-    need = std::max(need, d.width * d.height);
+    if (e == cudaSuccess) need = std::max(need, d.width * d.height);
   }
   uint8_t* scratch = nullptr;
   if (e == cudaSuccess) e = cudaMallocAsync(&scratch, need, s);

@@ -1,0 +1,24 @@
+#!/bin/bash
+# coalesced descriptor loads in the prep; small-pass mode / limit sweep (C5, C2 bytes, C2 2-bit); C5 scan capture
+mkdir -p gpurun_out
+T=r02n
+python paper_1310_0901_b200/build.py --force > gpurun_out/build_$T.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_medium.py -q -m gpu -x -k "tiny or toy or listing or fused or pingpong" > gpurun_out/pytest_$T.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/pytest_$T.log
+B="--no-cpu-baseline --no-registry-rate --no-e2e --no-per-config"
+run() { tag=$1; shift; echo "== $tag" >> gpurun_out/sweep_$T.txt; timeout 300 env "$@" >> gpurun_out/sweep_$T.txt 2>> gpurun_out/sweep_$T.err; }
+run c5_default python bench.py --config c5_sharded --steps 10 --warmup 3 $B
+run c5_ring CG_SMALL_MODE=2 python bench.py --config c5_sharded --steps 10 --warmup 3 $B
+run c2_default python bench.py --steps 20 --warmup 3 $B
+run c2_small4k CG_SMALL_MODE=1 python bench.py --steps 20 --warmup 3 $B
+run c2_small16k CG_SMALL_MODE=1 CG_SMALL_BYTES=16384 python bench.py --steps 20 --warmup 3 $B
+run c2x_default python bench.py --shadow 2bit --steps 20 --warmup 3 $B
+run c2x_small4k CG_SMALL_MODE=1 python bench.py --shadow 2bit --steps 20 --warmup 3 $B
+run c2x_small16k CG_SMALL_MODE=1 CG_SMALL_BYTES=16384 python bench.py --shadow 2bit --steps 20 --warmup 3 $B
+run c2x_small64k CG_SMALL_MODE=1 CG_SMALL_BYTES=65536 python bench.py --shadow 2bit --steps 20 --warmup 3 $B
+run c4_default python bench.py --config c4_pitched --steps 4 --warmup 3 $B
+K='regex:k_front|k_check|k_finish|k_leak|k_apply|k_prop|k_wave'
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name "$K" -c 100 --csv --log-file gpurun_out/launches_c5_$T.csv python bench.py --config c5_sharded --steps 1 --warmup 1 $B > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name "$K" -c 100 --csv --log-file gpurun_out/launches_c4_$T.csv python bench.py --config c4_pitched --steps 1 --warmup 1 $B > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name regex:k_check_scan --launch-skip 1 -c 1 -o gpurun_out/scan_c5_$T python bench.py --config c5_sharded --steps 1 --warmup 1 $B > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name regex:k_front --launch-skip 1 -c 1 -o gpurun_out/front_c5_$T python bench.py --config c5_sharded --steps 1 --warmup 1 $B > /dev/null 2>&1
