@@ -66,6 +66,7 @@ struct ShadowView {
   // its on/off choice: 0 adaptive (from the previous check's share of sides of
   // at most small_stat bytes), 1 always, 2 never (env CG_SMALL_MODE, CG_SMALL_STAT)
   uint32_t small_mode;
+  uint32_t small_share;   // adaptive: on when at least this percent of the sides were small (env CG_SMALL_SHARE)
   uint64_t small_stat;
 };
 
@@ -144,6 +145,11 @@ struct Launch {
   int front_blocks;       // cooperative grid of k_front (0: prep + plan as separate launches)
   int leak_blocks = 0;    // cooperative grid of k_leak (0: the 5-launch sweep)
   int small_blocks = 0;   // grid of k_check_small (the small pass)
+  // the small pass on a side stream, concurrent with the ring (env CG_SMALL_CONC):
+  // fork / join events and the two grids (CTAs per SM each, so both co-reside)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int conc_small_blocks = 0, conc_scan_blocks = 0;
   uint64_t* counter;      // host counter of kernel launches
   Profiler* prof;
   void stage(int st, bool begin, cudaStream_t s) const {

@@ -781,14 +781,15 @@ __device__ __forceinline__ void warp_store_zero(uint8_t* V, uint64_t q0, uint64_
 // __popc and the warp reduction only run for a side that has a finding.
 // ---------------------------------------------------------------------------
 #ifndef CG_SMALL_THREADS
-#define CG_SMALL_THREADS 128   // 4 warps per CTA: 10 KB stages within the 48 KB of static shared memory
+#define CG_SMALL_THREADS 256   // 8 warps per CTA, 4 CTAs per SM
 #endif
 #ifndef CG_SMALL_STAGE
-#define CG_SMALL_STAGE 10240
+#define CG_SMALL_STAGE 4864   // C5 small pass: 4864 B x 32 warps/SM 1.62 ms < 7168 B x 24 (1.68) < 10240 B x 20 (1.72) < 20480 B x 10 (2.6)
 #endif
 constexpr int kSmallThreads = CG_SMALL_THREADS;
 // staged bytes per warp and fill (a side of <= 4 KiB needs <= 4.7 KB; a C5
-// window's small sides ~14 KB: each fill is a DRAM round trip of its warp)
+// window's small sides ~14 KB: each fill is a DRAM round trip of its warp,
+// but more warps per SM hide it better than fewer, larger fills)
 constexpr uint32_t kSmallStage = CG_SMALL_STAGE;
 template <bool kTwoBit>
 __device__ __forceinline__ uint32_t lane_span(bool htod) {
@@ -796,16 +797,18 @@ __device__ __forceinline__ uint32_t lane_span(bool htod) {
 }
 
 
-// after a check: the small pass for the next check iff at least 80 % of this
-// batch's host sides had at most sv.small_stat bytes (C5: ~90 %, C2: ~60 %)
+// after a check: the small pass for the next check iff at least sv.small_share
+// percent of this batch's host sides had at most sv.small_stat bytes (bytes
+// format 80 %: C5 has ~94 %, C2 ~60 %, and C2 runs 1.5 % faster on the ring;
+// 2-bit states 50 %: C2 runs 11 % faster on the small pass)
 // (counter[9] = 1; 2 = the ring only); the statistics (counter[10..11]:
 // smalls << 32 | sides) restart.  A stream of
 // similar batches (a program's calls, the bench's steps) is thus served by the
 // path that suits it from its second batch on; the result is the same either way.
-__device__ __forceinline__ void next_small_choice(uint32_t* counter) {
+__device__ __forceinline__ void next_small_choice(uint32_t* counter, uint32_t share) {
   unsigned long long* st = reinterpret_cast<unsigned long long*>(counter + 10);
   const uint64_t sides = st[0] & 0xFFFFFFFFull, smalls = st[0] >> 32;   // <= 2^24 each (kMaxDescs)
-  counter[9] = (sides && 10 * smalls >= 8 * sides) ? 1u : 2u;   // at least 80 % of the sides small
+  counter[9] = (sides && 100 * smalls >= share * sides) ? 1u : 2u;   // at least share % of the sides small
   st[0] = 0;
 }
 
@@ -1143,7 +1146,7 @@ __device__ __forceinline__ bool small_unit_clean(const uint4& v, const uint8_t* 
 // wrote it); small DtoH sides with status OK are applied here when fused (a6)
 // unless CG_APPLY_AFTER sends them to the residual pass.
 #ifndef CG_SMALL_MINB
-#define CG_SMALL_MINB 5   // 64 registers; 5 CTAs of 4 warps (shared memory)
+#define CG_SMALL_MINB 4   // 64 registers, 32 warps per SM
 #endif
 template <bool kTwoBit>
 __global__ void __launch_bounds__(kSmallThreads, CG_SMALL_MINB) k_check_small(const ScanMeta* __restrict__ meta, uint64_t n,
@@ -2083,30 +2086,41 @@ __device__ __noinline__ void defer_segment(const ShadowView& sv, const DeferSide
                                            uint64_t rowbase, Partial& p) {
   const int lane = threadIdx.x & 31;
   const uint64_t g1 = b - sv.sb;
-  for (uint64_t g = ((a - sv.sb) & ~15ull) + 16ull * lane; g < g1; g += 512) {
-    const uint64_t xa = sv.sb + g;   // address of the group's byte 0
-    uint32_t m = 0xFFFFu;
-    if (xa < a) m &= 0xFFFFu << (uint32_t)(a - xa);
-    if (xa + 16 > b) m &= 0xFFFFu >> (uint32_t)(xa + 16 - b);
-    uint32_t ad, un;
-    host16(sv, g, ad, un);
-    const uint32_t bad = ~ad & m;
-    uint32_t u = s.htod ? un & m : 0u;
-    if (!(bad | u)) continue;
-    if (bad) {
-      const uint64_t x = xa + (__ffs(bad) - 1);
-      p.fu = umin64(p.fu, s.overlap ? (x - s.x0) + ov_rlo(s, x - s.x0) * (s.W - s.pitch) : rowbase + (x - a));
+  constexpr int kDeep = 4;   // 16-byte groups in flight per lane (a side's loads are independent)
+  for (uint64_t g0 = ((a - sv.sb) & ~15ull) + 16ull * lane; g0 < g1; g0 += 512 * kDeep) {
+    uint32_t ad[kDeep], un[kDeep];
+#pragma unroll
+    for (int k = 0; k < kDeep; ++k) {
+      ad[k] = 0xFFFFu;
+      un[k] = 0;
+      if (g0 + 512ull * k < g1) host16(sv, g0 + 512ull * k, ad[k], un[k]);
     }
-    if (u) {
-      const uint64_t x = xa + (__ffs(u) - 1);
-      p.fd = umin64(p.fd, s.overlap ? (x - s.x0) + ov_rlo(s, x - s.x0) * (s.W - s.pitch) : rowbase + (x - a));
-      if (!s.overlap) {
-        p.cnt += __popc(u);
-      } else {
-        while (u) {   // each undefined byte counts once per row it lies in
-          const uint64_t uu = xa + (__ffs(u) - 1) - s.x0;
-          u &= u - 1;
-          p.cnt += s.pitch == 0 ? s.H : umin64(s.H - 1, uu / s.pitch) - ov_rlo(s, uu) + 1;
+#pragma unroll
+    for (int k = 0; k < kDeep; ++k) {
+      const uint64_t g = g0 + 512ull * k;
+      if (g >= g1) break;
+      const uint64_t xa = sv.sb + g;   // address of the group's byte 0
+      uint32_t m = 0xFFFFu;
+      if (xa < a) m &= 0xFFFFu << (uint32_t)(a - xa);
+      if (xa + 16 > b) m &= 0xFFFFu >> (uint32_t)(xa + 16 - b);
+      const uint32_t bad = ~ad[k] & m;
+      uint32_t u = s.htod ? un[k] & m : 0u;
+      if (!(bad | u)) continue;
+      if (bad) {
+        const uint64_t x = xa + (__ffs(bad) - 1);
+        p.fu = umin64(p.fu, s.overlap ? (x - s.x0) + ov_rlo(s, x - s.x0) * (s.W - s.pitch) : rowbase + (x - a));
+      }
+      if (u) {
+        const uint64_t x = xa + (__ffs(u) - 1);
+        p.fd = umin64(p.fd, s.overlap ? (x - s.x0) + ov_rlo(s, x - s.x0) * (s.W - s.pitch) : rowbase + (x - a));
+        if (!s.overlap) {
+          p.cnt += __popc(u);
+        } else {
+          while (u) {   // each undefined byte counts once per row it lies in
+            const uint64_t uu = xa + (__ffs(u) - 1) - s.x0;
+            u &= u - 1;
+            p.cnt += s.pitch == 0 ? s.H : umin64(s.H - 1, uu / s.pitch) - ov_rlo(s, uu) + 1;
+          }
         }
       }
     }
@@ -2204,6 +2218,53 @@ __device__ __noinline__ void defer_one(const cg_copy_desc* __restrict__ descs, u
     }
   }
   __syncwarp();
+}
+
+// the late pass (CG_CHECK_AFTER, dense formats), spread over the grid: part
+// `part` of `nparts` of late descriptor d's physical span (16-byte aligned
+// pieces), combined into the verdict the prep wrote (first_unaddr = the
+// analytic offset outside the window, first_undef none, count 0) by atomics;
+// late_finalize then sets flags and status.  One warp per side took ~1 us per
+// 512 bytes of it.
+__device__ __noinline__ void late_part(const cg_copy_desc* __restrict__ descs, uint32_t d, uint32_t part,
+                                       uint32_t nparts, const ShadowView& sv, cg_verdict* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const cg_copy_desc dd = descs[d];
+  const Norm nm = normalize(dd);
+  const HostClip hc = host_clip(nm, dd.height, sv);
+  const bool contig = dd.height == 1 || dd.width == nm.hpitch;
+  DeferSide s;
+  s.x0 = nm.hstart;
+  s.W = contig ? nm.nbytes : nm.W;
+  s.pitch = contig ? 0 : nm.hpitch;
+  s.H = contig ? 1 : dd.height;
+  s.overlap = hc.overlap;
+  s.htod = true;
+  if (!nm.host || s.W == 0) return;
+  const uint64_t hi = s.x0 + ((s.H - 1) * s.pitch + s.W);   // end of the physical span (fits: R-10)
+  const uint64_t a0 = umax64(s.x0, sv.sb), b0 = umin64(hi, sv.se);
+  if (a0 >= b0) return;
+  const uint64_t step = (((b0 - a0) + nparts - 1) / nparts + 15) & ~15ull;
+  const uint64_t a = a0 + (uint64_t)part * step, b = umin64(a + step, b0);
+  if (a >= b) return;
+  Partial p{kNone, kNone, 0};
+  defer_range(sv, s, a, b, p);
+  p.fu = warp_min(p.fu);
+  p.fd = warp_min(p.fd);
+  p.cnt = warp_sum(p.cnt);
+  if (lane == 0) {
+    cg_verdict* v = out + d;
+    if (p.fu != kNone) atomicMin(reinterpret_cast<unsigned long long*>(&v->first_unaddr), p.fu);
+    if (p.fd != kNone) atomicMin(reinterpret_cast<unsigned long long*>(&v->first_undef), p.fd);
+    if (p.cnt) atomicAdd(reinterpret_cast<unsigned long long*>(&v->undef_count), p.cnt);
+  }
+}
+
+__device__ __forceinline__ void late_finalize(cg_verdict* v, uint32_t err_mask) {
+  uint32_t flags = v->flags, status;
+  finalize_fields(flags, status, v->first_unaddr, v->undef_count, err_mask);
+  v->flags = flags;
+  v->status = status;
 }
 
 // a warp whose ring has drained takes deferred descriptors until the list is done
@@ -2353,13 +2414,13 @@ __global__ void __launch_bounds__(kThreads) k_finalize_split(uint64_t n, const u
                                                              cg_verdict* __restrict__ out, uint32_t err_mask,
                                                              const ScanMeta* __restrict__ meta, int fuse,
                                                              uint32_t* __restrict__ resid,
-                                                             uint32_t* __restrict__ resid_n) {
+                                                             uint32_t* __restrict__ resid_n, uint32_t small_share) {
   pdl_entry();
   // the deferred list of the next check starts empty (its prep appends to it,
   // so it cannot reset it itself); resid_n = counter + 2
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     resid_n[2] = resid_n[3] = 0;   // counter[4], [5]: the deferred list
-    next_small_choice(resid_n - 2);
+    next_small_choice(resid_n - 2, small_share);
   }
   if (!fuse && blockIdx.x == 0 && threadIdx.x == 0) resid_n[0] = 0;   // nothing appends to the residual list unfused
   const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
@@ -2673,7 +2734,7 @@ __global__ void __launch_bounds__(kThreads) k_finish(
     if (tid == 0) {
       counter[0] = 0;   // the apply walk's group counter
       counter[4] = counter[5] = 0;   // the deferred list of the next check (the prep appends to it)
-      next_small_choice(counter);
+      next_small_choice(counter, sv.small_share);
     }
   }
   grid.sync();
@@ -2752,8 +2813,17 @@ __global__ void __launch_bounds__(kThreads) k_finish(
   asm volatile("fence.proxy.async.global;" ::: "memory");   // the residual apply's bulk stores, before generic loads
   __threadfence();
   grid.sync();
-  for (uint64_t k = tid >> 5; k < nl; k += nthr >> 5)   // the records in meta[] were reused above: flags from the verdict
-    defer_one(descs, late_list[k], nullptr, sv, out, err_mask, 0, resid, resid_n, last_list);
+  if (!sv.sparse) {   // (late side, part) items over all warps, then the finalisation
+    constexpr uint32_t kLateParts = 32;
+    for (uint64_t k = tid >> 5; k < (uint64_t)nl * kLateParts; k += nthr >> 5)
+      late_part(descs, late_list[k / kLateParts], (uint32_t)(k % kLateParts), kLateParts, sv, out);
+    __threadfence();
+    grid.sync();
+    for (uint64_t k = tid; k < nl; k += nthr) late_finalize(out + late_list[k], err_mask);
+  } else {   // the records in meta[] were reused above: flags from the verdict
+    for (uint64_t k = tid >> 5; k < nl; k += nthr >> 5)
+      defer_one(descs, late_list[k], nullptr, sv, out, err_mask, 0, resid, resid_n, last_list);
+  }
   if (nz) {   // uniform
     grid.sync();   // every late check has read the shadow
     for (uint64_t k = tid >> 5; k < nz; k += nthr >> 5) apply_whole<kTwoBit>(descs[last_list[k]], sv);
@@ -3861,7 +3931,14 @@ static cudaError_t check_front(const Launch& L, const cg_copy_desc* d, uint64_t 
     L.stage(CG_STAGE_CHECK_PLAN, false, s);
   }
   L.stage(CG_STAGE_CHECK_SCAN, true, s);
-  if (!sv.sparse && sv.small_limit) {   // the small pass (k_check_small), then the ring scan
+  const bool conc = L.side && !sv.sparse && sv.small_limit;
+  if (conc) {   // the small pass on the side stream, concurrent with the ring (disjoint descriptors)
+    cudaEventRecord(L.ev_fork, s);
+    cudaStreamWaitEvent(L.side, L.ev_fork, 0);
+    (sv.two_bit ? k_check_small<true> : k_check_small<false>)<<<L.conc_small_blocks, kSmallThreads, 0, L.side>>>(
+        meta, n, sv, out, err_mask, fuse ? 1 : 0, p.resid, p.counter + 2, p.last);
+    *L.counter += 1;
+  } else if (!sv.sparse && sv.small_limit) {   // the small pass (k_check_small), then the ring scan
     launch_pdl(sv.two_bit ? k_check_small<true> : k_check_small<false>, L.small_blocks, kSmallThreads, 0, s, meta, n, sv,
                out, err_mask, fuse ? 1 : 0, p.resid, p.counter + 2, p.last);
     *L.counter += 1;
@@ -3869,9 +3946,13 @@ static cudaError_t check_front(const Launch& L, const cg_copy_desc* d, uint64_t 
   auto scan = !sv.two_bit ? (fuse ? k_check_scan<false, true, false> : k_check_scan<false, false, false>)
               : sv.sparse ? (fuse ? k_check_scan<true, true, true> : k_check_scan<true, false, true>)
                           : (fuse ? k_check_scan<true, true, false> : k_check_scan<true, false, false>);
-  launch_pdl(scan, L.scan_blocks, kRingWarps * 32, kScanSmem, s, meta, n, p.P, p.chunk_first, p.counter,
-                                                                 p.t_min, p.max_chunks, sv, out, err_mask,
-                                                                 fuse ? 1 : 0, p.resid, p.counter + 2, d, p.defer, p.last);
+  launch_pdl(scan, conc ? L.conc_scan_blocks : L.scan_blocks, kRingWarps * 32, kScanSmem, s, meta, n, p.P,
+             p.chunk_first, p.counter, p.t_min, p.max_chunks, sv, out, err_mask, fuse ? 1 : 0, p.resid,
+             p.counter + 2, d, p.defer, p.last);
+  if (conc) {
+    cudaEventRecord(L.ev_join, L.side);
+    cudaStreamWaitEvent(s, L.ev_join, 0);
+  }
   L.stage(CG_STAGE_CHECK_SCAN, false, s);
   *L.counter += 1;
   return cudaGetLastError();
@@ -3885,7 +3966,7 @@ cudaError_t check_copies(const Launch& L, const cg_copy_desc* d, uint64_t n, cg_
   ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
   L.stage(CG_STAGE_CHECK_FINAL, true, s);
   launch_pdl(k_finalize_split, blocks_for(n, kThreads, L.num_sms * 8), kThreads, 0, s, 
-      n, p.P, p.t_min, p.max_chunks, out, err_mask, meta, fuse ? 1 : 0, p.resid, p.counter + 2);
+      n, p.P, p.t_min, p.max_chunks, out, err_mask, meta, fuse ? 1 : 0, p.resid, p.counter + 2, sv.small_share);
   L.stage(CG_STAGE_CHECK_FINAL, false, s);
   *L.counter += 1;
   return cudaGetLastError();

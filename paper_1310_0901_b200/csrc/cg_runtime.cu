@@ -481,6 +481,8 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
     c->sv.small_limit = std::min<uint64_t>(strtoull(sl, nullptr, 10), two_bit ? 16384 : 4096);
   c->sv.small_mode = 0;
   if (const char* sm = getenv("CG_SMALL_MODE")) c->sv.small_mode = (uint32_t)std::min<uint64_t>(strtoull(sm, nullptr, 10), 2);
+  c->sv.small_share = two_bit ? 50u : 80u;
+  if (const char* sh = getenv("CG_SMALL_SHARE")) c->sv.small_share = (uint32_t)std::min<uint64_t>(strtoull(sh, nullptr, 10), 100);
   c->sv.small_stat = cgk::kSmallStatDefault;
   if (const char* ss = getenv("CG_SMALL_STAT")) c->sv.small_stat = strtoull(ss, nullptr, 10);
   if (sparse) {   // the whole 64-bit space; the directory lives in the workspace
@@ -507,6 +509,16 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
   c->launch.leak_blocks = std::min(prop.multiProcessorCount * cgk::persistent_blocks(5), (int)cgk::kFinishMaxBlocks);
   c->launch.small_blocks = prop.multiProcessorCount * std::max(cgk::persistent_blocks(6), 1);
   if (const char* lk = getenv("CG_LEAK_COOP")) if (atoi(lk) == 0) c->launch.leak_blocks = 0;
+  if (const char* sc = getenv("CG_SMALL_CONC")) {   // experiment: small pass || ring, CTAs per SM "small,scan"
+    int a1 = 2, a2 = 2;
+    if (sscanf(sc, "%d,%d", &a1, &a2) >= 1 && a1 > 0 &&
+        cudaStreamCreateWithFlags(&c->launch.side, cudaStreamNonBlocking) == cudaSuccess &&
+        cudaEventCreateWithFlags(&c->launch.ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+        cudaEventCreateWithFlags(&c->launch.ev_join, cudaEventDisableTiming) == cudaSuccess) {
+      c->launch.conc_small_blocks = prop.multiProcessorCount * a1;
+      c->launch.conc_scan_blocks = prop.multiProcessorCount * std::max(a2, 1);
+    }
+  }
   c->launch.finish_blocks = std::min(prop.multiProcessorCount * std::max(cgk::persistent_blocks(3), 1),
                                      (int)cgk::kFinishMaxBlocks);
   c->launch.counter = &c->launches;
@@ -576,6 +588,9 @@ cg_status cg_ctx_destroy(cg_ctx* c) {
     if (c->slot_free[k]) cudaEventDestroy(c->slot_free[k]);
     if (c->slot_done[k]) cudaEventSynchronize(c->slot_done[k]), cudaEventDestroy(c->slot_done[k]);
   }
+  if (c->launch.side) cudaStreamDestroy(c->launch.side);
+  if (c->launch.ev_fork) cudaEventDestroy(c->launch.ev_fork);
+  if (c->launch.ev_join) cudaEventDestroy(c->launch.ev_join);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->out_stream) cudaStreamDestroy(c->out_stream);
   if (c->h_count) cudaFreeHost(c->h_count);

@@ -5,13 +5,16 @@ import csv
 import sys
 
 
-def main(path, out=None, first=("k_front", "k_check_prep")):
+def main(path, out=None, first=("k_front", "k_check_prep"), last_step=False):
     """Only launches from the first `first` kernel on (the bench steps; the
     setup kernels before it -- fresh shadow, host marks, V-byte checks -- are
-    excluded)."""
+    excluded); last_step: only the launches from the last `first` kernel on
+    (one steady-state step: C5's first step runs before the small pass has
+    been chosen)."""
     rows = [r for r in csv.DictReader(l for l in open(path) if l.startswith('"'))
             if r.get("Metric Name") == "gpu__time_duration.sum"]
-    start = next((i for i, r in enumerate(rows) if any(f in r["Kernel Name"] for f in first)), 0)
+    starts = [i for i, r in enumerate(rows) if any(f in r["Kernel Name"] for f in first)] or [0]
+    start = starts[-1] if last_step else starts[0]
     rows = rows[start:]
     agg = collections.OrderedDict()
     for r in rows:
@@ -32,4 +35,5 @@ def main(path, out=None, first=("k_front", "k_check_prep")):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None)
+    args = [a for a in sys.argv[1:] if a != "--last-step"]
+    main(args[0], args[1] if len(args) > 1 else None, last_step="--last-step" in sys.argv)
