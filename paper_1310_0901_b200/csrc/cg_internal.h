@@ -145,11 +145,6 @@ struct Launch {
   int front_blocks;       // cooperative grid of k_front (0: prep + plan as separate launches)
   int leak_blocks = 0;    // cooperative grid of k_leak (0: the 5-launch sweep)
   int small_blocks = 0;   // grid of k_check_small (the small pass)
-  // the small pass on a side stream, concurrent with the ring (env CG_SMALL_CONC):
-  // fork / join events and the two grids (CTAs per SM each, so both co-reside)
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  int conc_small_blocks = 0, conc_scan_blocks = 0;
   uint64_t* counter;      // host counter of kernel launches
   Profiler* prof;
   void stage(int st, bool begin, cudaStream_t s) const {

@@ -998,15 +998,18 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
     if (is_late) late[atomicAdd(counter + 6, 1u)] = (uint32_t)i;
     const bool contig = d.height == 1 || d.width == nm.hpitch;
     const bool raw = d.reserved & CG_SHARD_RAW;   // partial of a straddler: no finalisation here
-    // the small pass (bytes and dense 2-bit formats): contiguous, whole, not
-    // raw -- checked by k_check_small, not by the ring; its verdict is written
+    // the small pass (every format; in the sparse map a side inside one 64 KiB
+    // chunk): contiguous, whole, not raw -- checked by k_check_small, not by
+    // the ring; its verdict is written
     // here already finalised as if the host side were clean (k_check_small
     // rewrites only the dirty ones)
     // the small pass runs when the previous check's sides were small on average
     // (counter[9] == 1, decided after each check from the statistics below:
     // many descriptors with few bytes each, C5); else (C2) the ring checks the
     // small sides too, their latency hidden behind the big tiles' streams
-    const bool small = nscan != 0 && nscan <= sv.small_limit && contig && !raw && !sv.sparse && small_on;
+    const uint64_t xs = nm.hstart + (sv.sb > nm.hstart ? sv.sb - nm.hstart : 0);   // the side's first shard byte
+    const bool small = nscan != 0 && nscan <= sv.small_limit && contig && !raw && small_on &&
+                       (!sv.sparse || (xs >> kChunkShift) == ((xs + nscan - 1) >> kChunkShift));
     {   // the statistics of the small-pass choice: host sides, and those of at most sv.small_stat
       const uint32_t sides = __popc(__ballot_sync(kFull, nscan != 0));
       const uint32_t smalls = __popc(__ballot_sync(kFull, nscan != 0 && nscan <= sv.small_stat));
@@ -1159,10 +1162,12 @@ __global__ void __launch_bounds__(kSmallThreads, CG_SMALL_MINB) k_check_small(co
   __shared__ __align__(128) uint8_t s_stage[kSmallThreads / 32][kSmallStage];
   __shared__ uint64_t s_bar[kSmallThreads / 32];
   __shared__ SmallSide s_side[kSmallThreads / 32][32];
+  __shared__ __align__(16) uint8_t s_umap[kSmallThreads / 32][kSmallStage / 16 + 16];
   const int lane = threadIdx.x & 31;
   uint8_t* stage = s_stage[threadIdx.x >> 5];
   uint64_t* bar = &s_bar[threadIdx.x >> 5];
   SmallSide* side = s_side[threadIdx.x >> 5];
+  uint8_t* umap = s_umap[threadIdx.x >> 5];
   if (lane == 0) {
     mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1221,7 +1226,9 @@ __global__ void __launch_bounds__(kSmallThreads, CG_SMALL_MINB) k_check_small(co
       if (lane == 0) mbar_arrive_tx(bar, total);
       __syncwarp();
       if (in) {
-        const uint8_t* src = kTwoBit ? sv.V + (g0 >> 2) : htod ? sv.V + g0 : sv.A + (g0 >> 3);
+        const uint8_t* src = !kTwoBit ? (htod ? sv.V + g0 : sv.A + (g0 >> 3))
+                             : sv.sparse ? chunk_base(sv, g0 >> kChunkShift, sparse_secondary(sv, g0 >> kChunkShift)) + (g0 >> 2)
+                                         : sv.V + (g0 >> 2);
         bulk_g2s(stage + off, src, mlen, bar, policy);
         if (alen) bulk_g2s(stage + off + mlen, sv.A + ab, alen, bar, policy);
       }
@@ -1249,11 +1256,33 @@ __global__ void __launch_bounds__(kSmallThreads, CG_SMALL_MINB) k_check_small(co
         r.htod = htod;
         side[lane] = r;
       }
+      // the unit -> side map of the fill (one byte per unit, side + 1): side
+      // starts marked, then a prefix maximum (a block of ceil(U / 32) units
+      // per lane, the carries by a warp max-scan)
+      for (uint32_t w = lane; w < (U + 3) >> 2; w += 32) reinterpret_cast<uint32_t*>(umap)[w] = 0u;
+      __syncwarp();
+      if (units) umap[uincl - units] = (uint8_t)(lane + 1);
+      __syncwarp();
+      {
+        const uint32_t B = (U + 31) >> 5, b0 = min(U, lane * B), b1 = min(U, b0 + B);
+        uint32_t run = 0;
+        for (uint32_t f = b0; f < b1; ++f) run = max(run, (uint32_t)umap[f]);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, run, o);
+          if (lane >= o) run = max(run, y);
+        }
+        uint32_t cur = __shfl_up_sync(kFull, run, 1);
+        if (lane == 0) cur = 0;
+        for (uint32_t f = b0; f < b1; ++f) {
+          cur = max(cur, (uint32_t)umap[f]);
+          umap[f] = (uint8_t)cur;
+        }
+      }
       __syncwarp();
       uint32_t dirty = 0;   // lane-local: bit j = side j has a finding
-      uint32_t j = 0;
       for (uint32_t f = lane; f < U; f += 32) {
-        while (f >= side[j].uincl) ++j;
+        const uint32_t j = umap[f] - 1u;
         const SmallSide& r = side[j];
         const uint32_t k = f - (r.uincl - r.units);
         const uint4 v = *reinterpret_cast<const uint4*>(stage + r.off + 16 * k);
@@ -1354,7 +1383,7 @@ __global__ void __launch_bounds__(kSmallThreads, CG_SMALL_MINB) k_check_small(co
     // byte stores at the edges), bigger ones by the whole warp
     if (apply_me && q1 - q0 <= 512) {
       if (kTwoBit) {
-        lane_fill2(sv.V, q0, q1, 0xAAAAAAAAu);
+        fill2_any<false>(sv, q0, q1, 0xAAAAAAAAu);
       } else {
         const uint64_t a0 = (q0 + 15) & ~15ull, a1 = q1 & ~15ull;
         if (a0 >= a1) {
@@ -1372,7 +1401,7 @@ __global__ void __launch_bounds__(kSmallThreads, CG_SMALL_MINB) k_check_small(co
       const int k = __ffs(ap) - 1;
       ap &= ap - 1;
       const uint64_t a = __shfl_sync(kFull, q0, k), b = __shfl_sync(kFull, q1, k);
-      if (kTwoBit) warp_fill2(sv.V, a, b, 0xAAAAAAAAu);
+      if (kTwoBit) fill2_any<true>(sv, a, b, 0xAAAAAAAAu);
       else warp_store_zero(sv.V, a, b);
     }
   }
@@ -2408,6 +2437,26 @@ __global__ void __launch_bounds__(kRingWarps * 32, 4) k_check_scan(
 }
 
 
+// which of the descriptors d0 + u nthr (u < kSplitDeep) were split across
+// groups (weight above the never-split limit, see compute_pieces): their prefix
+// sums loaded together -- a plain grid-stride loop over 10M descriptors waited
+// one DRAM round trip per descriptor and thread (C5: 0.13 ms of k_finish)
+constexpr int kSplitDeep = 8;
+__device__ __forceinline__ uint32_t split_mask(const uint64_t* __restrict__ P, uint64_t n, uint64_t d0, uint64_t nthr,
+                                               uint64_t trule) {
+  uint64_t a[kSplitDeep], b[kSplitDeep];
+#pragma unroll
+  for (int u = 0; u < kSplitDeep; ++u) {
+    const uint64_t d = d0 + (uint64_t)u * nthr;
+    a[u] = d < n ? __ldcg(P + d) : 0;
+    b[u] = d < n ? __ldcg(P + d + 1) : 0;
+  }
+  uint32_t m = 0;
+#pragma unroll
+  for (int u = 0; u < kSplitDeep; ++u) m |= (uint32_t)(b[u] - a[u] > trule) << u;
+  return m;
+}
+
 // a5 for descriptors split across groups
 __global__ void __launch_bounds__(kThreads) k_finalize_split(uint64_t n, const uint64_t* __restrict__ P,
                                                              uint64_t t_min, uint64_t max_chunks,
@@ -2424,20 +2473,23 @@ __global__ void __launch_bounds__(kThreads) k_finalize_split(uint64_t n, const u
   }
   if (!fuse && blockIdx.x == 0 && threadIdx.x == 0) resid_n[0] = 0;   // nothing appends to the residual list unfused
   const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
-  for (uint64_t d = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; d < n;
-       d += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t pd = P[d], pd1 = P[d + 1];
-    if (pd1 - pd <= g.Trule) continue;   // never split (see compute_pieces)
-    const uint64_t info = meta[d].info;
-    if ((info >> kInfoRaw) & 1u) continue;   // raw partial of a straddler
-    cg_verdict* v = out + d;
-    uint32_t flags = v->flags, status;
-    finalize_fields(flags, status, v->first_unaddr, v->undef_count, err_mask);
-    v->flags = flags;
-    v->status = status;
-    // fused check: a split DtoH piece is applied by the residual pass
-    if (fuse && status == CG_OK && ((info >> kInfoKind) & 3u) == CG_DTOH && ((info >> kInfoHost) & 1u))
-      resid[atomicAdd(resid_n, 1u)] = (uint32_t)d;
+  const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t d0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; d0 < n; d0 += kSplitDeep * nthr) {
+    uint32_t split = split_mask(P, n, d0, nthr, g.Trule);
+    while (split) {
+      const uint64_t d = d0 + (uint64_t)(__ffs(split) - 1) * nthr;
+      split &= split - 1;
+      const uint64_t info = meta[d].info;
+      if ((info >> kInfoRaw) & 1u) continue;   // raw partial of a straddler
+      cg_verdict* v = out + d;
+      uint32_t flags = v->flags, status;
+      finalize_fields(flags, status, v->first_unaddr, v->undef_count, err_mask);
+      v->flags = flags;
+      v->status = status;
+      // fused check: a split DtoH piece is applied by the residual pass
+      if (fuse && status == CG_OK && ((info >> kInfoKind) & 3u) == CG_DTOH && ((info >> kInfoHost) & 1u))
+        resid[atomicAdd(resid_n, 1u)] = (uint32_t)d;
+    }
   }
 }
 
@@ -2718,18 +2770,21 @@ __global__ void __launch_bounds__(kThreads) k_finish(
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nthr = (uint64_t)gridDim.x * blockDim.x;
   {   // a5 for split descriptors
     const ChunkGeom g = chunk_geom(P, n, t_min, max_chunks);
-    for (uint64_t d = tid; d < n; d += nthr) {
-      const uint64_t pd = P[d], pd1 = P[d + 1];
-      if (pd1 - pd <= g.Trule) continue;   // never split (see compute_pieces)
-      const uint64_t info = meta[d].info;
-      if ((info >> kInfoRaw) & 1u) continue;     // raw partial of a straddler
-      cg_verdict* v = out + d;
-      uint32_t flags = v->flags, status;
-      finalize_fields(flags, status, v->first_unaddr, v->undef_count, err_mask);
-      v->flags = flags;
-      v->status = status;
-      if (status == CG_OK && ((info >> kInfoKind) & 3u) == CG_DTOH && ((info >> kInfoHost) & 1u))
-        push_apply((info >> kInfoLast) & 1u, (uint32_t)d, resid, resid_n, last_list);
+    for (uint64_t d0 = tid; d0 < n; d0 += kSplitDeep * nthr) {
+      uint32_t split = split_mask(P, n, d0, nthr, g.Trule);
+      while (split) {
+        const uint64_t d = d0 + (uint64_t)(__ffs(split) - 1) * nthr;
+        split &= split - 1;
+        const uint64_t info = meta[d].info;
+        if ((info >> kInfoRaw) & 1u) continue;     // raw partial of a straddler
+        cg_verdict* v = out + d;
+        uint32_t flags = v->flags, status;
+        finalize_fields(flags, status, v->first_unaddr, v->undef_count, err_mask);
+        v->flags = flags;
+        v->status = status;
+        if (status == CG_OK && ((info >> kInfoKind) & 3u) == CG_DTOH && ((info >> kInfoHost) & 1u))
+          push_apply((info >> kInfoLast) & 1u, (uint32_t)d, resid, resid_n, last_list);
+      }
     }
     if (tid == 0) {
       counter[0] = 0;   // the apply walk's group counter
@@ -3931,14 +3986,7 @@ static cudaError_t check_front(const Launch& L, const cg_copy_desc* d, uint64_t 
     L.stage(CG_STAGE_CHECK_PLAN, false, s);
   }
   L.stage(CG_STAGE_CHECK_SCAN, true, s);
-  const bool conc = L.side && !sv.sparse && sv.small_limit;
-  if (conc) {   // the small pass on the side stream, concurrent with the ring (disjoint descriptors)
-    cudaEventRecord(L.ev_fork, s);
-    cudaStreamWaitEvent(L.side, L.ev_fork, 0);
-    (sv.two_bit ? k_check_small<true> : k_check_small<false>)<<<L.conc_small_blocks, kSmallThreads, 0, L.side>>>(
-        meta, n, sv, out, err_mask, fuse ? 1 : 0, p.resid, p.counter + 2, p.last);
-    *L.counter += 1;
-  } else if (!sv.sparse && sv.small_limit) {   // the small pass (k_check_small), then the ring scan
+  if (sv.small_limit) {   // the small pass (k_check_small), then the ring scan
     launch_pdl(sv.two_bit ? k_check_small<true> : k_check_small<false>, L.small_blocks, kSmallThreads, 0, s, meta, n, sv,
                out, err_mask, fuse ? 1 : 0, p.resid, p.counter + 2, p.last);
     *L.counter += 1;
@@ -3946,13 +3994,8 @@ static cudaError_t check_front(const Launch& L, const cg_copy_desc* d, uint64_t 
   auto scan = !sv.two_bit ? (fuse ? k_check_scan<false, true, false> : k_check_scan<false, false, false>)
               : sv.sparse ? (fuse ? k_check_scan<true, true, true> : k_check_scan<true, false, true>)
                           : (fuse ? k_check_scan<true, true, false> : k_check_scan<true, false, false>);
-  launch_pdl(scan, conc ? L.conc_scan_blocks : L.scan_blocks, kRingWarps * 32, kScanSmem, s, meta, n, p.P,
-             p.chunk_first, p.counter, p.t_min, p.max_chunks, sv, out, err_mask, fuse ? 1 : 0, p.resid,
-             p.counter + 2, d, p.defer, p.last);
-  if (conc) {
-    cudaEventRecord(L.ev_join, L.side);
-    cudaStreamWaitEvent(s, L.ev_join, 0);
-  }
+  launch_pdl(scan, L.scan_blocks, kRingWarps * 32, kScanSmem, s, meta, n, p.P, p.chunk_first, p.counter, p.t_min,
+             p.max_chunks, sv, out, err_mask, fuse ? 1 : 0, p.resid, p.counter + 2, d, p.defer, p.last);
   L.stage(CG_STAGE_CHECK_SCAN, false, s);
   *L.counter += 1;
   return cudaGetLastError();

@@ -509,16 +509,7 @@ cg_status cg_ctx_create(const cg_config* cfg, cg_ctx** out) {
   c->launch.leak_blocks = std::min(prop.multiProcessorCount * cgk::persistent_blocks(5), (int)cgk::kFinishMaxBlocks);
   c->launch.small_blocks = prop.multiProcessorCount * std::max(cgk::persistent_blocks(6), 1);
   if (const char* lk = getenv("CG_LEAK_COOP")) if (atoi(lk) == 0) c->launch.leak_blocks = 0;
-  if (const char* sc = getenv("CG_SMALL_CONC")) {   // experiment: small pass || ring, CTAs per SM "small,scan"
-    int a1 = 2, a2 = 2;
-    if (sscanf(sc, "%d,%d", &a1, &a2) >= 1 && a1 > 0 &&
-        cudaStreamCreateWithFlags(&c->launch.side, cudaStreamNonBlocking) == cudaSuccess &&
-        cudaEventCreateWithFlags(&c->launch.ev_fork, cudaEventDisableTiming) == cudaSuccess &&
-        cudaEventCreateWithFlags(&c->launch.ev_join, cudaEventDisableTiming) == cudaSuccess) {
-      c->launch.conc_small_blocks = prop.multiProcessorCount * a1;
-      c->launch.conc_scan_blocks = prop.multiProcessorCount * std::max(a2, 1);
-    }
-  }
+
   c->launch.finish_blocks = std::min(prop.multiProcessorCount * std::max(cgk::persistent_blocks(3), 1),
                                      (int)cgk::kFinishMaxBlocks);
   c->launch.counter = &c->launches;
@@ -588,9 +579,6 @@ cg_status cg_ctx_destroy(cg_ctx* c) {
     if (c->slot_free[k]) cudaEventDestroy(c->slot_free[k]);
     if (c->slot_done[k]) cudaEventSynchronize(c->slot_done[k]), cudaEventDestroy(c->slot_done[k]);
   }
-  if (c->launch.side) cudaStreamDestroy(c->launch.side);
-  if (c->launch.ev_fork) cudaEventDestroy(c->launch.ev_fork);
-  if (c->launch.ev_join) cudaEventDestroy(c->launch.ev_join);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->out_stream) cudaStreamDestroy(c->out_stream);
   if (c->h_count) cudaFreeHost(c->h_count);
