@@ -293,7 +293,7 @@ __device__ __forceinline__ uint4 ld_keep4(const uint4* a, uint64_t pol) {
 // match (live allocations never overlap).  Probe i = last base <= start
 // (smem splitters, then a short global binary search), then walk left while
 // the prefix max of ends exceeds start (one step without address reuse).
-__device__ __forceinline__ bool table_lookup(const Table& t, const uint64_t* s_split, uint64_t start,
+[[maybe_unused]] __device__ __forceinline__ bool table_lookup(const Table& t, const uint64_t* s_split, uint64_t start,
                                              uint64_t seq, uint64_t& end_out, uint64_t& idx_out) {
   if (t.nsplit == 0 || s_split[0] > start) return false;
   const uint64_t pol = evict_last_policy();
@@ -346,6 +346,113 @@ __device__ __forceinline__ bool table_lookup(const Table& t, const uint64_t* s_s
     }
   }
   return false;
+}
+
+#ifndef CG_LOOKUP2
+#define CG_LOOKUP2 1   // the prep's two lookups (DtoD) in lockstep (table_lookup2)
+#endif
+#ifndef CG_FRONT_MINB
+#define CG_FRONT_MINB 3   // CTAs per SM of the prep kernels: 80 registers (the two lockstep lookups)
+#endif
+
+// table_lookup for two keys at once (a DtoD copy's destination and source):
+// every phase -- the splitter search, the bucket rounds, the walk -- runs for
+// both keys in lockstep, so their dependent load chains overlap.  A warp with
+// one DtoD lane (C5: 97 % of the warps at 10 % DtoD) waited for two chains
+// one after the other.
+__device__ __forceinline__ void table_lookup2(const Table& t, const uint64_t* s_split, const uint64_t key[2],
+                                              const bool want[2], uint64_t seq, uint64_t end_out[2],
+                                              uint64_t idx_out[2], bool found[2]) {
+  const uint64_t pol = evict_last_policy();
+  bool act[2];
+  uint64_t a[2], b[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    found[q] = false;
+    end_out[q] = idx_out[q] = 0;
+    act[q] = want[q] && t.nsplit != 0 && s_split[0] <= key[q];
+    uint32_t lo = 0, hi = t.nsplit;
+    if (act[q])
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_split[mid] <= key[q]) lo = mid; else hi = mid;
+      }
+    a[q] = (uint64_t)lo * t.stride;
+    b[q] = umin64(a[q] + t.stride, t.n);
+  }
+  if (t.stride == 32) {   // (the opt-in stride-64 rounds take the lockstep binary search here)
+    constexpr int nq = 4;   // uint4 loads of 2 every-4th bases each
+    uint4 v[2][nq];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int k = 0; k < nq; ++k)
+        v[q][k] = act[q] ? ld_keep4(reinterpret_cast<const uint4*>(t.l2 + a[q] / 4) + k, pol) : make_uint4(0, 0, 0, 0);
+    uint64_t a1[2];
+    uint4 r[2][2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      uint32_t c2 = 0;
+#pragma unroll
+      for (int k = 0; k < nq; ++k) {
+        c2 += (a[q] + 8 * k < b[q] && (((uint64_t)v[q][k].y << 32) | v[q][k].x) <= key[q]) +
+              (a[q] + 8 * k + 4 < b[q] && (((uint64_t)v[q][k].w << 32) | v[q][k].z) <= key[q]);
+      }
+      a1[q] = a[q] + 4 * (c2 > 0 ? c2 - 1 : 0);
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        r[q][k] = act[q] ? ld_keep4(reinterpret_cast<const uint4*>(t.base + a1[q]) + k, pol) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      uint32_t c1 = 0;
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        c1 += (a1[q] + 2 * k < b[q] && (((uint64_t)r[q][k].y << 32) | r[q][k].x) <= key[q]) +
+              (a1[q] + 2 * k + 1 < b[q] && (((uint64_t)r[q][k].w << 32) | r[q][k].z) <= key[q]);
+      a[q] = a1[q] + (c1 > 0 ? c1 - 1 : 0);
+    }
+  } else {
+    while ((act[0] && b[0] - a[0] > 1) || (act[1] && b[1] - a[1] > 1)) {
+      uint64_t m[2], x[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        m[q] = (a[q] + b[q]) >> 1;
+        x[q] = (act[q] && b[q] - a[q] > 1) ? ld_keep(t.base + m[q], pol) : 0;
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        if (act[q] && b[q] - a[q] > 1) {
+          if (x[q] <= key[q]) a[q] = m[q]; else b[q] = m[q];
+        }
+    }
+  }
+  int64_t j[2] = {(int64_t)a[0], (int64_t)a[1]};
+  while ((act[0] && j[0] >= 0) || (act[1] && j[1] >= 0)) {   // the prefix-max walks, in lockstep
+    uint4 w0[2], w1[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      if (act[q] && j[q] >= 0) {
+        w0[q] = ld_keep4(t.walk + 2 * j[q], pol);
+        w1[q] = ld_keep4(t.walk + 2 * j[q] + 1, pol);   // one 32-byte sector
+      }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (!(act[q] && j[q] >= 0)) continue;
+      const uint64_t pm = ((uint64_t)w0[q].y << 32) | w0[q].x, e = ((uint64_t)w0[q].w << 32) | w0[q].z;
+      const uint64_t as = ((uint64_t)w1[q].y << 32) | w1[q].x, fs = ((uint64_t)w1[q].w << 32) | w1[q].z;
+      if (pm <= key[q]) {
+        act[q] = false;
+      } else if (e > key[q] && as < seq && seq < fs) {
+        end_out[q] = e;
+        idx_out[q] = (uint64_t)j[q];
+        found[q] = true;
+        act[q] = false;
+      } else {
+        --j[q];
+      }
+    }
+  }
 }
 
 // NEXT-3: the array with this handle alive at seq -> its total bytes
@@ -951,6 +1058,41 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
           if (t.apool) (htoa ? dv_dst : dv_src) = __ldg(t.apool + j) + nm.aoff;
         }
       }
+#if CG_LOOKUP2
+    } else if (act && !(flags & CG_F_BAD_KIND) && owner) {
+      // dst side first in the flag order; both lookups in lockstep
+      const uint64_t key[2] = {nm.ds, nm.ss};
+      const bool want[2] = {(nm.kind == CG_HTOD || nm.kind == CG_DTOD) && nm.dok,
+                            (nm.kind == CG_DTOH || nm.kind == CG_DTOD) && nm.sok};
+      uint64_t end[2], j[2];
+      bool found[2];
+      table_lookup2(t, s_split, key, want, d.seq, end, j, found);
+      if (want[0]) {
+        if (!found[0]) {
+          flags |= CG_F_DST_NOT_ALLOCATED;
+        } else {
+          if (end[0] - nm.ds < nm.dspan) {
+            flags |= CG_F_DST_TOO_SMALL;
+            de = nm.dspan;
+            df = end[0] - nm.ds;
+          }
+          if (t.pool) dv_dst = __ldg(t.pool + j[0]) + (nm.ds - __ldg(t.base + j[0]));
+        }
+      }
+      if (want[1]) {
+        if (!found[1]) {
+          flags |= CG_F_SRC_NOT_ALLOCATED;
+        } else {
+          if (end[1] - nm.ss < nm.sspan) {
+            flags |= CG_F_SRC_TOO_SMALL;
+            se = nm.sspan;
+            sf = end[1] - nm.ss;
+          }
+          if (t.pool) dv_src = __ldg(t.pool + j[1]) + (nm.ss - __ldg(t.base + j[1]));
+        }
+      }
+    }
+#else
     } else if (act && !(flags & CG_F_BAD_KIND) && owner) {
       uint64_t end, j;
       if ((nm.kind == CG_HTOD || nm.kind == CG_DTOD) && nm.dok) {      // dst side first
@@ -978,6 +1120,7 @@ __device__ __forceinline__ void prep_body(const cg_copy_desc* __restrict__ descs
         }
       }
     }
+#endif
     if (act && t.pool) {
       dvoff[2 * i] = dv_dst;
       dvoff[2 * i + 1] = dv_src;
@@ -1407,7 +1550,7 @@ __global__ void __launch_bounds__(kSmallThreads, CG_SMALL_MINB) k_check_small(co
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 4) k_check_prep(const cg_copy_desc* __restrict__ descs,
+__global__ void __launch_bounds__(kThreads, CG_FRONT_MINB) k_check_prep(const cg_copy_desc* __restrict__ descs,
                                                          uint64_t n, Table t, cg_verdict* __restrict__ out,
                                                          uint64_t* __restrict__ weight,
                                                          ScanMeta* __restrict__ meta,
@@ -1577,7 +1720,7 @@ __global__ void __launch_bounds__(kThreads) k_plan(const uint64_t* __restrict__ 
 // exclusive prefix sum of the weights and the chunk map with grid barriers
 // between the phases (k_scan_reduce / _top / _down, k_plan): one launch and
 // four barriers instead of five launches.
-__global__ void __launch_bounds__(kThreads, 4) k_front(const cg_copy_desc* __restrict__ descs, uint64_t n, Table t,
+__global__ void __launch_bounds__(kThreads, CG_FRONT_MINB) k_front(const cg_copy_desc* __restrict__ descs, uint64_t n, Table t,
                                                     cg_verdict* __restrict__ out, uint64_t* __restrict__ weight,
                                                     ScanMeta* __restrict__ meta, uint64_t* __restrict__ dvoff,
                                                     ShadowView sv, uint32_t* __restrict__ counter,
