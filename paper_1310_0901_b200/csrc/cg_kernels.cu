@@ -348,11 +348,13 @@ __device__ __forceinline__ uint4 ld_keep4(const uint4* a, uint64_t pol) {
   return false;
 }
 
+// CG_LOOKUP2=1: the prep's two lookups (a DtoD copy) in lockstep (table_lookup2);
+// measured slower on C5 (prep 1.05 -> 1.21 ms at 64 registers, 1.23 at 80) and C2
 #ifndef CG_LOOKUP2
-#define CG_LOOKUP2 1   // the prep's two lookups (DtoD) in lockstep (table_lookup2)
+#define CG_LOOKUP2 0
 #endif
 #ifndef CG_FRONT_MINB
-#define CG_FRONT_MINB 3   // CTAs per SM of the prep kernels: 80 registers (the two lockstep lookups)
+#define CG_FRONT_MINB 4   // CTAs per SM of the prep kernels (64 registers)
 #endif
 
 // table_lookup for two keys at once (a DtoD copy's destination and source):
