@@ -362,7 +362,7 @@ __device__ __forceinline__ uint4 ld_keep4(const uint4* a, uint64_t pol) {
 // both keys in lockstep, so their dependent load chains overlap.  A warp with
 // one DtoD lane (C5: 97 % of the warps at 10 % DtoD) waited for two chains
 // one after the other.
-__device__ __forceinline__ void table_lookup2(const Table& t, const uint64_t* s_split, const uint64_t key[2],
+[[maybe_unused]] __device__ __forceinline__ void table_lookup2(const Table& t, const uint64_t* s_split, const uint64_t key[2],
                                               const bool want[2], uint64_t seq, uint64_t end_out[2],
                                               uint64_t idx_out[2], bool found[2]) {
   const uint64_t pol = evict_last_policy();
