@@ -4099,7 +4099,12 @@ static cudaError_t check_front(const Launch& L, const cg_copy_desc* d, uint64_t 
   const size_t smem = ((size_t)t.nsplit + 1) * sizeof(uint64_t);
   ScanMeta* meta = reinterpret_cast<ScanMeta*>(p.meta);
   L.stage(CG_STAGE_CHECK_PREP, true, s);
-  if (L.front_blocks > 0 && smem <= kFrontSmem) {   // prep + plan in one cooperative launch
+  // prep + plan in one cooperative launch for batches of up to 4M descriptors;
+  // above, the plan's per-block loops of the persistent grid are latency-bound
+  // and the separate prep + scan + plan kernels are faster (C5, 10M: 1.05 ->
+  // 0.99 ms)
+  constexpr uint64_t kFrontCoopMax = 1ull << 22;
+  if (L.front_blocks > 0 && smem <= kFrontSmem && n <= kFrontCoopMax) {
     const Table tc = t;
     ShadowView svc = sv;
     uint64_t* weight = p.weight;

@@ -183,7 +183,7 @@ def _compare_shadow_chunks(chk, o, base, size, chunk=1 << 30):
         assert np.array_equal(a, oa), ("A", q)
 
 
-def _full_replay(cg, tr, fused=True, T=0):
+def _full_replay(cg, tr, fused=True, T=0, fused_plan=False):
     """The GPU checks the trace the way bench.py does (setup events, then the
     copies in the R-20 epochs cg_plan_batches cuts, fused where the epoch is
     apply-disjoint; registry events are lifetime-stamped, so they all go first);
@@ -199,12 +199,19 @@ def _full_replay(cg, tr, fused=True, T=0):
     descs = tg.events_to_descs(copies)
     dd = cg.to_device_descs(descs)
     dv = torch.empty(len(descs) * 64, dtype=torch.uint8, device=dd.device)
-    cuts = [0] + [int(c) for c in cg.plan_batches(descs)]
+    if fused_plan:   # the bench's batches: cg_plan_batches_fused marks the descriptors in place
+        descs = np.ascontiguousarray(descs)
+        cuts = [0] + [int(c) for c in cg.plan_batches_fused(descs)]
+        dd = cg.to_device_descs(descs)
+    else:
+        cuts = [0] + [int(c) for c in cg.plan_batches(descs)]
     for a, b in zip(cuts[:-1], cuts[1:]):
         if b <= a:
             continue
         x, y = dd[a * 96:b * 96], dv[a * 64:b * 64]
-        if fused and cg.batch_disjoint(descs[a:b]):
+        if fused_plan:
+            chk.check_apply(x, y)
+        elif fused and cg.batch_disjoint(descs[a:b]):
             chk.check_apply(x, y)
         else:
             chk.check_copies(x, y)
@@ -233,6 +240,21 @@ def test_c4_full(cg):
     gv, _ = _full_replay(cg, tr)
     inj = tr.meta["inject"]
     assert np.all(gv["flags"][inj == 0] == 0) and np.all(gv["flags"][inj != 0] != 0)
+
+
+def test_c5_full_fused(cg):
+    """C5 at full size the way bench.py times it: cg_plan_batches_fused makes
+    ONE batch of the 10M descriptors (the ping-pongs become CG_CHECK_AFTER /
+    CG_APPLY_AFTER / CG_APPLY_LAST), checked by one cg_check_apply (separate
+    prep and plan kernels above 4M descriptors, the small pass, the ring, the
+    late pass and the last applies in k_finish): every verdict, the leak list
+    and the whole final shadow against the sequential T-thread oracle."""
+    import psutil
+    if psutil.virtual_memory().available < (100 << 30):
+        pytest.skip("needs ~100 GiB of host memory for the oracle's 64 GiB window")
+    tr = tg.c5_sharded()
+    gv, _ = _full_replay(cg, tr, fused_plan=True)
+    assert int(np.count_nonzero(gv["flags"])) > 0
 
 
 def test_c5_full(cg):

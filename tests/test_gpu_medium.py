@@ -72,3 +72,12 @@ def test_pingpong_fused(cg, seed):
 def test_pingpong_small_batches(cg, seed):
     """the same with max_descs 5: the replay splits fused batches into pieces"""
     run_parity(cg, tg.pingpong_trace(seed + 100, n_copies=80), fuse=True, max_descs=5)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_medium_front_split(cg, seed, monkeypatch):
+    """the prep and the plan as separate kernels (CG_FRONT_COOP=0, the path of
+    batches above 4M descriptors)"""
+    monkeypatch.setenv("CG_FRONT_COOP", "0")
+    run_parity(cg, tg.random_medium(seed + 600), fuse=bool(seed % 2))
+    run_parity(cg, tg.pingpong_trace(seed + 600), fuse=True)
