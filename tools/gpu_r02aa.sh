@@ -1,0 +1,13 @@
+#!/bin/bash
+# small pass: inner units without masks
+mkdir -p gpurun_out
+T=r02aa
+python paper_1310_0901_b200/build.py --force > gpurun_out/build_$T.log 2>&1
+B="--no-cpu-baseline --no-registry-rate --no-e2e --no-per-config"
+run() { tag=$1; shift; echo "== $tag" >> gpurun_out/sweep_$T.txt; timeout 300 env "$@" >> gpurun_out/sweep_$T.txt 2>> gpurun_out/sweep_$T.err; }
+run c5 python bench.py --config c5_sharded --steps 10 --warmup 3 $B
+run c2x python bench.py --shadow 2bit --steps 20 --warmup 3 $B
+run c2s python bench.py --shadow sparse --steps 20 --warmup 3 $B
+run c5x python bench.py --config c5_sharded --shadow 2bit --steps 10 --warmup 3 $B
+timeout 900 env CG_SMALL_MODE=1 python -m pytest tests/test_gpu_medium.py tests/test_gpu_parity.py tests/test_gpu_next4.py -q -m gpu -x > gpurun_out/pytest_small_$T.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/pytest_small_$T.log
