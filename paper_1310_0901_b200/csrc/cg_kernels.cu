@@ -590,15 +590,15 @@ __device__ __forceinline__ void finalize_fields(uint32_t& flags, uint32_t& statu
 // Fast path: lane j folds the 16-byte V units j, j+32, ... (contiguous 16-byte
 // lanes: one LDS.128 per lane reads 512 consecutive bytes, bank-conflict free)
 // into one OR, and their 16-bit A half-words into one AND (LDS.U16 of 64
-// consecutive bytes); the (at most two) units at the edges of [q0, q1) are
-// tested with their byte mask by their own lane.  Only a lane that saw an
-// undefined or unaddressable byte rescans its units with per-byte masks
-// (__ffs for the first offset, __popc for the count).
-__device__ __forceinline__ void htod_unit(const uint8_t* st, uint32_t u, uint32_t m, uint64_t ob, Partial& p) {
+// consecutive bytes); only a lane that saw an undefined or unaddressable byte
+// rescans its units with per-byte masks (__ffs for the first offset, __popc
+// for the count).  The partial 32-byte groups at the tile edges always take
+// the masked path.
+__device__ __forceinline__ void htod_unit(const uint8_t* st, uint32_t u, uint64_t ob, Partial& p) {
   const uint4 v = reinterpret_cast<const uint4*>(st)[u];
   const uint32_t a = reinterpret_cast<const unsigned short*>(st + kTileV)[u];
-  const uint32_t bad = ~a & m;
-  const uint32_t und = nz16(v) & a & m;
+  const uint32_t bad = ~a & 0xFFFFu;
+  const uint32_t und = nz16(v) & a;
   const uint64_t gb = ob + 16ull * u;
   if (bad) p.fu = umin64(p.fu, gb + (__ffs(bad) - 1));
   if (und) {
@@ -607,35 +607,47 @@ __device__ __forceinline__ void htod_unit(const uint8_t* st, uint32_t u, uint32_
   }
 }
 
-// the byte mask of 16-byte unit u inside [q0, q1) (staged coordinates)
-__device__ __forceinline__ uint32_t unit_mask16(uint32_t u, uint32_t q0, uint32_t q1) {
-  const uint32_t b = u << 4;
-  const uint32_t l = q0 > b ? q0 - b : 0u, h = q1 - b < 16u ? q1 - b : 16u;
-  return (0xFFFFu >> (16u - h)) & ~((1u << l) - 1u);
+// a partial 32-byte HtoD group g with the whole warp: lane j looks at host byte 32 g + j
+__device__ __forceinline__ void htod_edge(const uint8_t* st, uint32_t g, uint32_t q0, uint32_t q1, uint64_t ob,
+                                          Partial& p) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t x = (g << 5) + lane;
+  const bool in = x >= q0 && x < q1;
+  const uint32_t a = (st[kTileV + (x >> 3)] >> (x & 7)) & 1u;
+  const uint32_t bad = __ballot_sync(kFull, in && !a);
+  const uint32_t und = __ballot_sync(kFull, in && a && st[x] != 0);
+  if (lane == 0) {
+    const uint64_t gb = ob + ((uint64_t)g << 5);
+    if (bad) p.fu = umin64(p.fu, gb + (__ffs(bad) - 1));
+    if (und) {
+      p.fd = umin64(p.fd, gb + (__ffs(und) - 1));
+      p.cnt += __popc(und);
+    }
+  }
 }
 
 __device__ __forceinline__ void consume_htod(const uint8_t* st, uint32_t q0, uint32_t q1, uint64_t ob,
                                              Partial& p) {
   const int lane = threadIdx.x & 31;
-  const uint32_t u0 = q0 >> 4, u1 = (q1 + 15) >> 4;   // the 16-byte units touching [q0, q1)
+  const uint32_t i0 = (q0 + 31) >> 5, i1 = q1 >> 5;   // full 32-byte groups [i0, i1) = 16-byte units [2 i0, 2 i1)
   const uint4* V4 = reinterpret_cast<const uint4*>(st);
   const unsigned short* A2 = reinterpret_cast<const unsigned short*>(st + kTileV);
-  uint32_t orv = 0, anda = 0xFFFFu, edge = 0;
+  uint32_t orv = 0, anda = 0xFFFFu;
 #pragma unroll 4
-  for (uint32_t u = u0 + lane; u < u1; u += 32) {
+  for (uint32_t u = 2 * i0 + lane; u < 2 * i1; u += 32) {
     const uint4 v = V4[u];
-    const uint32_t a = A2[u];
-    if (u == u0 || u + 1 == u1) {   // an edge unit: its bytes outside [q0, q1) do not count
-      const uint32_t m = unit_mask16(u, q0, q1);
-      edge |= (~a & m) | (nz16(v) & a & m);
-    } else {
-      orv |= v.x | v.y | v.z | v.w;
-      anda &= a;
-    }
+    orv |= v.x | v.y | v.z | v.w;
+    anda &= A2[u];
   }
-  if (orv != 0 || anda != 0xFFFFu || edge != 0)
-    for (uint32_t u = u0 + lane; u < u1; u += 32)
-      htod_unit(st, u, (u == u0 || u + 1 == u1) ? unit_mask16(u, q0, q1) : 0xFFFFu, ob, p);
+  if (orv != 0 || anda != 0xFFFFu)
+    for (uint32_t u = 2 * i0 + lane; u < 2 * i1; u += 32) htod_unit(st, u, ob, p);
+  // partial edge groups, warp-parallel
+  if (i0 > i1) {                                   // [q0, q1) inside one 32-byte group
+    htod_edge(st, i1, q0, q1, ob, p);
+  } else {
+    if (q0 & 31) htod_edge(st, i0 - 1, q0, q1, ob, p);
+    if (q1 & 31) htod_edge(st, i1, q0, q1, ob, p);
+  }
 }
 
 // DtoH tile: A bits only; one 16-byte A vector covers 128 host bytes
@@ -655,28 +667,47 @@ __device__ __forceinline__ void dtoh_group(const uint8_t* st, uint32_t i, uint32
   }
 }
 
+// a partial 128-byte DtoH group g: lanes 0-3 take its four A words
+__device__ __forceinline__ void dtoh_edge(const uint8_t* st, uint32_t g, uint32_t q0, uint32_t q1, uint64_t ob,
+                                          Partial& p) {
+  const int lane = threadIdx.x & 31;
+  uint32_t bad = 0;
+  if (lane < 4) {
+    const uint32_t k = g * 4 + lane;
+    const int base = (int)(k << 5);
+    const int lo = max((int)q0 - base, 0), hi = min((int)q1 - base, 32);
+    if (hi > lo) {
+      const uint32_t m = (hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
+      bad = ~reinterpret_cast<const uint32_t*>(st)[k] & m;
+    }
+  }
+  const uint32_t any = __ballot_sync(kFull, bad != 0);
+  if (any) {
+    const int fl = __ffs(any) - 1;
+    const uint32_t b = __shfl_sync(kFull, bad, fl);
+    if (lane == 0) p.fu = umin64(p.fu, ob + ((uint64_t)(g * 4 + fl) << 5) + (__ffs(b) - 1));
+  }
+}
+
 __device__ __forceinline__ void consume_dtoh(const uint8_t* st, uint32_t q0, uint32_t q1, uint64_t ob,
                                              Partial& p) {
   const int lane = threadIdx.x & 31;
-  const uint32_t i0 = q0 >> 7, i1 = (q1 + 127) >> 7;   // the 128-byte groups touching [q0, q1)
+  const uint32_t i0 = (q0 + 127) >> 7, i1 = q1 >> 7;   // full 128-byte groups [i0, i1)
   const uint4* A16 = reinterpret_cast<const uint4*>(st);
-  uint32_t anda = 0xffffffffu, edge = 0;
+  uint32_t anda = 0xffffffffu;
 #pragma unroll 4
   for (uint32_t i = i0 + lane; i < i1; i += 32) {
     const uint4 a = A16[i];
-    if (i == i0 || i + 1 == i1) {   // an edge group: its bytes outside [q0, q1) do not count
-      const uint32_t w[4] = {a.x, a.y, a.z, a.w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t gb = i * 128 + 32 * j;
-        if (gb + 32 > q0 && gb < q1) edge |= ~w[j] & range_mask(gb, 32, q0, q1);
-      }
-    } else {
-      anda &= a.x & a.y & a.z & a.w;
-    }
+    anda &= a.x & a.y & a.z & a.w;
   }
-  if (anda != 0xffffffffu || edge != 0)
+  if (anda != 0xffffffffu)
     for (uint32_t i = i0 + lane; i < i1; i += 32) dtoh_group(st, i, q0, q1, ob, p);
+  if (i0 > i1) {
+    dtoh_edge(st, i1, q0, q1, ob, p);
+  } else {
+    if (q0 & 127) dtoh_edge(st, i0 - 1, q0, q1, ob, p);
+    if (q1 & 127) dtoh_edge(st, i1, q0, q1, ob, p);
+  }
 }
 
 
