@@ -1,12 +1,14 @@
-"""Diagnostic: C5 full size, GPU (per R-20 epoch, as tests/test_gpu_fullsize.py
-_full_replay) against the T-thread oracle; prints the mismatching verdict rows
-and their descriptors for each small-pass mode in argv (CG_SMALL_MODE values)."""
+"""Test infrastructure, run by hand on a GPU box (not collected by pytest):
+C5 at full size on the GPU (per R-20 epoch, as tests/test_gpu_fullsize.py
+_full_replay) against the T-thread oracle; prints the mismatching verdict
+rows and their descriptors for each small-pass mode in argv (CG_SMALL_MODE
+values)."""
 import os
 import sys
 
 import numpy as np
 
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))   # repo root
 import oracle  # noqa: E402
 import tracegen as tg  # noqa: E402
 

@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 T=r02q
 CG_NVCC_EXTRA="-DCG_SMALL_VERIFY=1" python paper_1310_0901_b200/build.py --force > gpurun_out/build_v_$T.log 2>&1
-timeout 1500 python tools/diag_c5.py 1 > gpurun_out/diag_v_$T.txt 2>&1
+timeout 1500 python tests/diag_c5.py 1 > gpurun_out/diag_v_$T.txt 2>&1
 python paper_1310_0901_b200/build.py --force > gpurun_out/build_$T.log 2>&1
 timeout 900 env CG_SMALL_MODE=1 python -m pytest tests/test_gpu_parity.py tests/test_gpu_medium.py tests/test_gpu_next4.py -q -m gpu -x > gpurun_out/pytest_small_$T.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pytest_small_$T.log

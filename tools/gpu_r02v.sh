@@ -10,6 +10,6 @@ run() { tag=$1; shift; echo "== $tag" >> gpurun_out/sweep_$T.txt; timeout 300 en
 run c5 python bench.py --config c5_sharded --steps 10 --warmup 3 $B
 run c2x python bench.py --shadow 2bit --steps 20 --warmup 3 $B
 run c2s python bench.py --shadow sparse --steps 20 --warmup 3 $B
-timeout 1500 python tools/diag_c5.py 1 > gpurun_out/diag_$T.txt 2>&1
+timeout 1500 python tests/diag_c5.py 1 > gpurun_out/diag_$T.txt 2>&1
 K='regex:k_front|k_check|k_finish|k_leak|k_apply|k_prop|k_wave'
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name "$K" -c 100 --csv --log-file gpurun_out/launches_c5_$T.csv python bench.py --config c5_sharded --steps 2 --warmup 1 $B > /dev/null 2>&1
