@@ -2776,6 +2776,9 @@ __device__ __forceinline__ void warp_zero(uint8_t* V, uint64_t q0, uint64_t q1, 
     bulk_s2g(V + p, zeros, (uint32_t)umin64(kZeroPage, a1 - p));
 }
 
+#ifndef CG_APPLY_BULK
+#define CG_APPLY_BULK 1   // the apply's warp pieces: bulk stores from a zero page (0: 16-byte stores of all lanes)
+#endif
 // the apply walk over planned groups (shared by k_apply and k_finish)
 template <bool kTwoBit>
 __device__ __forceinline__ void apply_body(const ScanMeta* __restrict__ meta, uint64_t n,
@@ -2833,7 +2836,8 @@ __device__ __forceinline__ void apply_body(const ScanMeta* __restrict__ meta, ui
         if ((s_info >> kApplyContig) & 1u) {
           const uint64_t a = __shfl_sync(kFull, qs, src), b = __shfl_sync(kFull, qe, src);
           if (kTwoBit) fill2_any<true>(sv, a, b, 0xAAAAAAAAu);
-          else warp_zero(sv.V, a, b, zeros);
+          else if (CG_APPLY_BULK) warp_zero(sv.V, a, b, zeros);
+          else warp_store_zero(sv.V, a, b);
         } else {
           const uint64_t x0 = __shfl_sync(kFull, m.hstart, src), pitch = __shfl_sync(kFull, m.hpitch, src);
           const uint64_t W = __shfl_sync(kFull, m.W, src);
@@ -2845,7 +2849,8 @@ __device__ __forceinline__ void apply_body(const ScanMeta* __restrict__ meta, ui
             const uint64_t y0 = umax64(x, sv.sb), y1 = umin64(x + len, sv.se);
             if (y0 < y1) {
               if (kTwoBit) fill2_any<true>(sv, y0 - sv.sb, y1 - sv.sb, 0xAAAAAAAAu);
-              else warp_zero(sv.V, y0 - sv.sb, y1 - sv.sb, zeros);
+              else if (CG_APPLY_BULK) warp_zero(sv.V, y0 - sv.sb, y1 - sv.sb, zeros);
+              else warp_store_zero(sv.V, y0 - sv.sb, y1 - sv.sb);
             }
             oo += len;
             ++r;
