@@ -900,6 +900,8 @@ constexpr int kSmallThreads = CG_SMALL_THREADS;
 // window's small sides ~14 KB: each fill is a DRAM round trip of its warp,
 // but more warps per SM hide it better than fewer, larger fills)
 constexpr uint32_t kSmallStage = CG_SMALL_STAGE;
+// a side of 4 KiB (the limit) stages at most 257 V units + 34 A units = 4656 bytes
+static_assert(kSmallStage >= 4656 && kSmallStage % 16 == 0, "the stage must hold the largest small side");
 template <bool kTwoBit>
 __device__ __forceinline__ uint32_t lane_span(bool htod) {
   return kTwoBit ? 64u : htod ? 16u : 128u;
