@@ -270,12 +270,8 @@ def run_ours(args, rank, world, device, config=None, steps=None, warmup=None, e2
     d_leaks = torch.empty(max(nalloc, 1) * 24, dtype=torch.uint8, device=device)
     d_cnt = torch.zeros(1, dtype=torch.int64, device=device)
 
-    # the batch is one epoch; if no HtoD range overlaps a DtoH range the check
-    # and the apply run fused (cg_check_apply), else as two calls
-    # the batch contract (R-20): the copies are checked in the epochs
-    # cg_plan_batches cuts (one epoch for C2-C4; C5's ping-pongs make ~11); an
-    # epoch whose HtoD and DtoH host ranges are disjoint runs fused
-    # fused (cg_check_apply): the batches of cg_plan_batches_fused, which marks
+    # fused (cg_check_apply): the batches of cg_plan_batches_fused (one for
+    # every config, C5's ping-pongs included), which marks
     # the DtoH copies an HtoD of their batch reads CG_APPLY_AFTER and the HtoD
     # copies that read an earlier DtoH's bytes CG_CHECK_AFTER, so that a DtoH ->
     # HtoD ping-pong no longer ends the batch (a DtoH that then writes such an
